@@ -1,0 +1,127 @@
+/*
+ * tucomp_b200.h — C ABI of the B200 (sm_100a) compress path.
+ *
+ * Drop-in boundary for the reference operator API
+ *   tucomp::pipeline::compress(const container::SourceBuffer&, const Params&)
+ *   (/root/reference/proj/include/tucomp/pipeline.hpp:57, implemented at
+ *    /root/reference/proj/src/pipeline.cpp:240-252)
+ * flattened to plain pointers and sizes so any FFI (ctypes, cgo, JNI, N-API)
+ * can bind it; include/tucomp/pipeline.hpp re-exposes it with the reference's
+ * C++ types.  Every function returns 0 on success; on failure it returns
+ * non-zero and tcb_last_error() holds the reference's error text
+ * (e.g. "sthosvd: input contains non-finite values").
+ *
+ * There is no CPU fallback: every entry point runs CUDA kernels on the
+ * current device and fails loudly when no sm_100a device is present.
+ */
+#ifndef TUCOMP_B200_H
+#define TUCOMP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* tucomp::pipeline::Params (pipeline.hpp:14-28), fixed-size arrays for d <= 8 */
+typedef struct tcb_params {
+    int has_target_re;           /* exactly one of the two targets must be set */
+    double target_re;
+    int has_target_sse;
+    double target_sse;
+    double rtmss;                /* errormodel::kDefaultRtmss = 0.5 */
+    int threads;                 /* host helper threads (results never depend on it) */
+    int method;                  /* vectorize::Method; 0 = lexicographic */
+    int has_storage_order;
+    uint64_t storage_order[8];
+    int has_mode_order;
+    uint64_t mode_order[8];
+    int coder;                   /* entropy::Coder; 0 = arithmetic, 1 = rANS */
+    int split_planes;
+    int simple_factor_weights;
+    uint64_t block_size;         /* 0 = codec default */
+    int internal_float32;
+    int svd_backend;             /* sthosvd::SvdBackend; 0 automatic, 1 gram, 2 direct */
+} tcb_params;
+
+/* tucomp::pipeline::PhaseTimes (pipeline.hpp:30-37), milliseconds */
+typedef struct tcb_times {
+    double sthosvd_ms, quantize_ms, core_encode_ms, factor_encode_ms, serialize_ms, total_ms;
+} tcb_times;
+
+/* tucomp::pipeline::CompressResult (pipeline.hpp:39-55) */
+typedef struct tcb_result {
+    uint8_t* container;          /* owned by the library: release with tcb_free */
+    uint64_t container_size;
+    double truncation_sse, core_quantization_sse, factor_terms[8]; /* ErrorEstimate */
+    double estimate_sse;
+    double norm_sq, target_sse;
+    uint64_t ranks[8];
+    int order;
+    tcb_times times;
+    uint64_t peak_alloc_estimate;
+    uint64_t original_bytes;
+    int ingest_precision_loss;
+    /* device-path diagnostics (no reference counterpart) */
+    int core_last_plane, core_scale_exponent;
+    int uncertified_decisions;   /* plans decided by the serial-replay fallback */
+    uint64_t kernel_launches;
+} tcb_result;
+
+void tcb_default_params(tcb_params* p);
+
+/* pipeline::compress with a HOST SourceBuffer {bytes, dtype, shape, skip_bytes}
+ * (container.hpp:34-39); host->device copy included. dtype = container::Dtype. */
+int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d,
+                 uint64_t skip_bytes, const tcb_params* params, tcb_result* out);
+
+/* Same, with the element bytes (after skip) already resident in device memory. */
+int tcb_compress_device(const void* device_bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d,
+                        const tcb_params* params, tcb_result* out);
+
+void tcb_free(void* p);
+const char* tcb_last_error(void);
+uint64_t tcb_kernel_launches(void);
+
+/* ---- lower-level entry points on host buffers (each wraps device kernels);
+ * the reference symbols they replace are named per function. ---- */
+
+/* sthosvd::compress<double> (sthosvd.hpp:66-68). core: processing order;
+ * factors[i]: n_i x r_i row-major; out arrays sized by the caller
+ * (core: prod(shape), factors[i]: n_i*n_i). */
+int tcb_sthosvd_f64(const double* a, const uint64_t* shape, int d, double sse_target, const uint64_t* order,
+                    int backend, double* core, uint64_t* core_shape, double** factors, uint64_t* ranks,
+                    double* trunc, uint64_t* order_out);
+
+/* G = B B^T (sthosvd.cpp:78-79), B row-major rows x cols, G full row-major. */
+int tcb_gram_f64(const double* b, uint64_t rows, uint64_t cols, double* g);
+/* next = B^T U (sthosvd.cpp:158-166), U rows x r row-major, next cols x r. */
+int tcb_ttm_f64(const double* b, uint64_t rows, uint64_t cols, const double* u, uint64_t r, double* next);
+/* SelfAdjointEigenSolver (sthosvd.cpp:80-90): descending eigenvalues and the
+ * top-r eigenvectors (n x r row-major, sign-fixed as sthosvd.cpp:103-110). */
+int tcb_eig_f64(const double* g, uint64_t n, uint64_t r, double* evals_desc, double* u);
+
+/* corecodec::quantize (core_codec.cpp:55-93), lexicographic order. */
+int tcb_quantize_f64(const double* core, const uint64_t* shape, int d, uint64_t* mag, uint8_t* neg, int* k,
+                     int* zero, double* slice_norms);
+
+/* corecodec::Encoder plan+finalize (core_codec.cpp:173-413); *stream receives
+ * the serialized stream section (container.cpp:231-247). fixed_plane < 0: none. */
+int tcb_encode(const uint64_t* mag, const uint8_t* neg, uint64_t n, double target_sse_int, int coder,
+               uint64_t block_size, int split, int fixed_plane, uint8_t** stream, uint64_t* stream_len,
+               int* last_plane, double* achieved_sse_int, uint64_t* decoded, int* uncertified);
+
+/* entropy::encode_symbols (entropy.cpp:429-445) for one symbol sequence. */
+int tcb_encode_symbols(int coder, const uint64_t* syms, uint64_t n, uint8_t** out, uint64_t* len);
+
+/* factorcodec::encode_factor<double> (factor_codec.cpp:153-244). */
+int tcb_encode_factor_f64(const double* u, uint64_t n, uint64_t r, const uint8_t* dead, const double* slice_norms,
+                          int coder, int simple, int core_step_log2, double term_cap, uint8_t** stream,
+                          uint64_t* len, int* k, uint64_t* count, int8_t* flips, double* term, int* plane);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TUCOMP_B200_H */

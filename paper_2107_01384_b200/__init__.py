@@ -1,0 +1,368 @@
+"""B200-native ATC compress path behind the reference's pipeline API.
+
+Python mirror of ``tucomp::pipeline`` (/root/reference/proj/include/tucomp/
+pipeline.hpp:14-71) over the C ABI in ``include/tucomp_b200.h``
+(``libtucomp_b200.so``, hand-written sm_100a CUDA).  Names, argument meaning
+and error text follow the reference: ``compress(SourceBuffer, Params)``
+returns a ``CompressResult`` whose ``container`` bytes are the reference's
+TKC1 format.  There is no CPU fallback: importing works anywhere (so the
+library can be inspected), every compute call runs CUDA kernels and raises
+``TucompError`` when the extension or a GPU is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtucomp_b200.so")
+_LIB = None
+
+
+class TucompError(RuntimeError):
+    """tucomp::Error (tensor.hpp:14-17)."""
+
+
+class Dtype(enum.IntEnum):  # container::Dtype (container.hpp:16-27)
+    int8 = 0
+    uint8 = 1
+    int16 = 2
+    uint16 = 3
+    int32 = 4
+    uint32 = 5
+    int64 = 6
+    uint64 = 7
+    float32 = 8
+    float64 = 9
+
+
+_NP2DT = {np.dtype(getattr(np, d.name)): d for d in Dtype}
+
+
+class Coder(enum.IntEnum):  # entropy::Coder (entropy.hpp:11-14)
+    arithmetic = 0
+    rans = 1
+
+
+class SvdBackend(enum.IntEnum):  # sthosvd::SvdBackend (sthosvd.hpp:48-52)
+    automatic = 0
+    gram = 1
+    direct = 2
+
+
+class _CParams(C.Structure):
+    _fields_ = [
+        ("has_target_re", C.c_int), ("target_re", C.c_double), ("has_target_sse", C.c_int),
+        ("target_sse", C.c_double), ("rtmss", C.c_double), ("threads", C.c_int), ("method", C.c_int),
+        ("has_storage_order", C.c_int), ("storage_order", C.c_uint64 * 8),
+        ("has_mode_order", C.c_int), ("mode_order", C.c_uint64 * 8),
+        ("coder", C.c_int), ("split_planes", C.c_int), ("simple_factor_weights", C.c_int),
+        ("block_size", C.c_uint64), ("internal_float32", C.c_int), ("svd_backend", C.c_int),
+    ]
+
+
+class _CTimes(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("sthosvd_ms", "quantize_ms", "core_encode_ms", "factor_encode_ms",
+                                          "serialize_ms", "total_ms")]
+
+
+class _CResult(C.Structure):
+    _fields_ = [
+        ("container", C.POINTER(C.c_uint8)), ("container_size", C.c_uint64),
+        ("truncation_sse", C.c_double), ("core_quantization_sse", C.c_double),
+        ("factor_terms", C.c_double * 8), ("estimate_sse", C.c_double), ("norm_sq", C.c_double),
+        ("target_sse", C.c_double), ("ranks", C.c_uint64 * 8), ("order", C.c_int), ("times", _CTimes),
+        ("peak_alloc_estimate", C.c_uint64), ("original_bytes", C.c_uint64),
+        ("ingest_precision_loss", C.c_int), ("core_last_plane", C.c_int), ("core_scale_exponent", C.c_int),
+        ("uncertified_decisions", C.c_int), ("kernel_launches", C.c_uint64),
+    ]
+
+
+def lib():
+    """Load libtucomp_b200.so; raises TucompError if it was not built."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise TucompError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.tcb_last_error.restype = C.c_char_p
+        L.tcb_kernel_launches.restype = C.c_uint64
+        _LIB = L
+    return _LIB
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise TucompError(lib().tcb_last_error().decode())
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _take_bytes(ptr, n) -> bytes:
+    out = C.string_at(ptr, n) if n else b""
+    lib().tcb_free(C.cast(ptr, C.c_void_p))
+    return out
+
+
+def kernel_launches() -> int:
+    return int(lib().tcb_kernel_launches())
+
+
+# ---------------------------------------------------------------- pipeline API
+@dataclass
+class Params:
+    """tucomp::pipeline::Params (pipeline.hpp:14-28)."""
+    target_re: Optional[float] = None
+    target_sse: Optional[float] = None
+    rtmss: float = 0.5  # errormodel::kDefaultRtmss
+    threads: int = 1
+    method: int = 0  # vectorize::Method::lexicographic
+    storage_order: Optional[Sequence[int]] = None
+    mode_order: Optional[Sequence[int]] = None
+    coder: int = Coder.arithmetic
+    split_planes: bool = True
+    simple_factor_weights: bool = False
+    block_size: int = 0
+    internal_float32: bool = False
+    svd_backend: int = SvdBackend.automatic
+
+    def to_c(self, d: int) -> _CParams:
+        p = _CParams()
+        p.has_target_re = int(self.target_re is not None)
+        p.target_re = float(self.target_re or 0.0)
+        p.has_target_sse = int(self.target_sse is not None)
+        p.target_sse = float(self.target_sse or 0.0)
+        p.rtmss = self.rtmss
+        p.threads = self.threads
+        p.method = int(self.method)
+        if self.storage_order is not None:
+            p.has_storage_order = 1
+            for i, v in enumerate(self.storage_order):
+                p.storage_order[i] = v
+        if self.mode_order is not None:
+            p.has_mode_order = 1
+            for i, v in enumerate(self.mode_order):
+                p.mode_order[i] = v
+        p.coder = int(self.coder)
+        p.split_planes = int(self.split_planes)
+        p.simple_factor_weights = int(self.simple_factor_weights)
+        p.block_size = self.block_size
+        p.internal_float32 = int(self.internal_float32)
+        p.svd_backend = int(self.svd_backend)
+        return p
+
+
+@dataclass
+class SourceBuffer:
+    """container::SourceBuffer (container.hpp:34-39)."""
+    bytes: bytes
+    dtype: Dtype
+    shape: Sequence[int]
+    skip_bytes: int = 0
+
+    @staticmethod
+    def from_array(a: np.ndarray) -> "SourceBuffer":
+        a = np.ascontiguousarray(a)
+        return SourceBuffer(a.tobytes(), _NP2DT[a.dtype], list(a.shape))
+
+
+@dataclass
+class PhaseTimes:
+    sthosvd_ms: float = 0.0
+    quantize_ms: float = 0.0
+    core_encode_ms: float = 0.0
+    factor_encode_ms: float = 0.0
+    serialize_ms: float = 0.0
+    total_ms: float = 0.0
+
+
+@dataclass
+class ErrorEstimate:
+    truncation_sse: float = 0.0
+    core_quantization_sse: float = 0.0
+    factor_terms: list = field(default_factory=list)
+
+    def total(self) -> float:
+        t = self.truncation_sse + self.core_quantization_sse
+        for f in self.factor_terms:
+            t += f
+        return t
+
+
+@dataclass
+class CompressResult:
+    """tucomp::pipeline::CompressResult (pipeline.hpp:39-55)."""
+    container: bytes
+    estimate: ErrorEstimate
+    norm_sq: float
+    target_sse: float
+    ranks: list
+    times: PhaseTimes
+    peak_alloc_estimate: int
+    original_bytes: int
+    ingest_precision_loss: bool
+    core_last_plane: int = 63
+    core_scale_exponent: int = 0
+    uncertified_decisions: int = 0
+    kernel_launches: int = 0
+
+    def compression_factor(self) -> float:
+        return 0.0 if not self.container else self.original_bytes / len(self.container)
+
+
+def _result(r: _CResult) -> CompressResult:
+    d = r.order
+    t = r.times
+    return CompressResult(
+        container=_take_bytes(r.container, r.container_size),
+        estimate=ErrorEstimate(r.truncation_sse, r.core_quantization_sse, [r.factor_terms[i] for i in range(d)]),
+        norm_sq=r.norm_sq, target_sse=r.target_sse, ranks=[int(r.ranks[i]) for i in range(d)],
+        times=PhaseTimes(t.sthosvd_ms, t.quantize_ms, t.core_encode_ms, t.factor_encode_ms, t.serialize_ms,
+                         t.total_ms),
+        peak_alloc_estimate=r.peak_alloc_estimate, original_bytes=r.original_bytes,
+        ingest_precision_loss=bool(r.ingest_precision_loss), core_last_plane=r.core_last_plane,
+        core_scale_exponent=r.core_scale_exponent, uncertified_decisions=r.uncertified_decisions,
+        kernel_launches=int(r.kernel_launches))
+
+
+def compress(src: SourceBuffer, params: Params) -> CompressResult:
+    """tucomp::pipeline::compress (pipeline.cpp:240-252) on the B200."""
+    shape = np.asarray(list(src.shape), np.uint64)
+    buf = np.frombuffer(src.bytes, np.uint8) if len(src.bytes) else np.zeros(1, np.uint8)
+    res = _CResult()
+    _check(lib().tcb_compress(_p(buf), C.c_uint64(len(src.bytes)), int(src.dtype), _p(shape), len(shape),
+                              C.c_uint64(src.skip_bytes), C.byref(params.to_c(len(shape))), C.byref(res)))
+    return _result(res)
+
+
+def compress_device(ptr: int, nbytes: int, dtype: Dtype, shape: Sequence[int], params: Params) -> CompressResult:
+    """Same as compress() with the element bytes already resident in device memory (e.g. a torch tensor)."""
+    sh = np.asarray(list(shape), np.uint64)
+    res = _CResult()
+    _check(lib().tcb_compress_device(C.c_void_p(ptr), C.c_uint64(nbytes), int(dtype), _p(sh), len(sh),
+                                     C.byref(params.to_c(len(sh))), C.byref(res)))
+    return _result(res)
+
+
+# ---------------------------------------------------------------- lower-level ops
+def sthosvd(a: np.ndarray, sse_target: float, order=None, backend=0) -> dict:
+    """sthosvd::compress<double> (sthosvd.hpp:66-68) on the device."""
+    a = np.ascontiguousarray(a, np.float64)
+    d = a.ndim
+    shape = np.asarray(a.shape, np.uint64)
+    core = np.zeros(a.size)
+    cs = (C.c_uint64 * d)()
+    facs = [np.zeros(n * n) for n in a.shape]
+    fptr = (C.c_void_p * d)(*[f.ctypes.data for f in facs])
+    ranks = (C.c_uint64 * d)()
+    trunc = (C.c_double * d)()
+    ordo = (C.c_uint64 * d)()
+    oarr = np.asarray(order, np.uint64) if order is not None else None
+    _check(lib().tcb_sthosvd_f64(_p(a), _p(shape), d, C.c_double(sse_target),
+                                 _p(oarr) if oarr is not None else None, backend, _p(core), cs, fptr, ranks, trunc,
+                                 ordo))
+    core_shape = [int(cs[i]) for i in range(d)]
+    rk = [int(ranks[i]) for i in range(d)]
+    return dict(core=core[:int(np.prod(core_shape))].reshape(core_shape), ranks=rk,
+                trunc=[trunc[i] for i in range(d)], order=[int(ordo[i]) for i in range(d)],
+                factors=[facs[i][:a.shape[i] * rk[i]].reshape(a.shape[i], rk[i]) for i in range(d)])
+
+
+def gram(b: np.ndarray) -> np.ndarray:
+    b = np.ascontiguousarray(b, np.float64)
+    g = np.zeros((b.shape[0], b.shape[0]))
+    _check(lib().tcb_gram_f64(_p(b), C.c_uint64(b.shape[0]), C.c_uint64(b.shape[1]), _p(g)))
+    return g
+
+
+def ttm(b: np.ndarray, u: np.ndarray) -> np.ndarray:
+    b = np.ascontiguousarray(b, np.float64)
+    u = np.ascontiguousarray(u, np.float64)
+    out = np.zeros((b.shape[1], u.shape[1]))
+    _check(lib().tcb_ttm_f64(_p(b), C.c_uint64(b.shape[0]), C.c_uint64(b.shape[1]), _p(u), C.c_uint64(u.shape[1]),
+                             _p(out)))
+    return out
+
+
+def eig(g: np.ndarray, r: int):
+    """Descending eigenvalues and the top-r sign-fixed eigenvectors of a symmetric matrix."""
+    g = np.ascontiguousarray(g, np.float64)
+    n = g.shape[0]
+    ev = np.zeros(n)
+    u = np.zeros((n, max(r, 1)))
+    _check(lib().tcb_eig_f64(_p(g), C.c_uint64(n), C.c_uint64(r), _p(ev), _p(u)))
+    return ev, u[:, :r]
+
+
+def quantize(core: np.ndarray):
+    core = np.ascontiguousarray(core, np.float64)
+    shape = np.asarray(core.shape, np.uint64)
+    mag = np.zeros(core.size, np.uint64)
+    neg = np.zeros(core.size, np.uint8)
+    k = C.c_int()
+    zero = C.c_int()
+    sn = np.zeros(int(sum(core.shape)))
+    _check(lib().tcb_quantize_f64(_p(core), _p(shape), core.ndim, _p(mag), _p(neg), C.byref(k), C.byref(zero),
+                                  _p(sn)))
+    parts, o = [], 0
+    for e in core.shape:
+        parts.append(sn[o:o + e].copy())
+        o += e
+    return mag, neg, k.value, bool(zero.value), parts
+
+
+def encode(mag, neg, target_int, coder=0, block_size=0, split=True, fixed_plane=-1):
+    """corecodec::Encoder plan+finalize; returns (stream section, last_plane, achieved_sse_int, decoded, uncertified)."""
+    mag = np.ascontiguousarray(mag, np.uint64)
+    neg = np.ascontiguousarray(neg, np.uint8)
+    n = mag.size
+    out = C.POINTER(C.c_uint8)()
+    ln = C.c_uint64()
+    lp = C.c_int()
+    ach = C.c_double()
+    unc = C.c_int()
+    dec = np.zeros(max(n, 1), np.uint64)
+    _check(lib().tcb_encode(_p(mag) if n else None, _p(neg) if n else None, C.c_uint64(n), C.c_double(target_int),
+                            coder, C.c_uint64(block_size), int(split), fixed_plane, C.byref(out), C.byref(ln),
+                            C.byref(lp), C.byref(ach), _p(dec), C.byref(unc)))
+    return _take_bytes(out, ln.value), lp.value, ach.value, dec[:n], unc.value
+
+
+def encode_symbols(coder, syms) -> bytes:
+    s = np.ascontiguousarray(syms, np.uint64)
+    out = C.POINTER(C.c_uint8)()
+    ln = C.c_uint64()
+    _check(lib().tcb_encode_symbols(coder, _p(s) if s.size else None, C.c_uint64(s.size), C.byref(out),
+                                    C.byref(ln)))
+    return _take_bytes(out, ln.value)
+
+
+def encode_factor(u, dead, slice_norms, coder=0, simple=False, core_step_log2=0, term_cap=0.0) -> dict:
+    u = np.ascontiguousarray(u, np.float64)
+    n, r = u.shape
+    dead = np.ascontiguousarray(dead, np.uint8)
+    sn = np.ascontiguousarray(slice_norms, np.float64)
+    out = C.POINTER(C.c_uint8)()
+    ln = C.c_uint64()
+    k = C.c_int()
+    cnt = C.c_uint64()
+    flips = np.zeros(max(r, 1), np.int8)
+    term = C.c_double()
+    plane = C.c_int()
+    _check(lib().tcb_encode_factor_f64(_p(u), C.c_uint64(n), C.c_uint64(r), _p(dead), _p(sn), coder, int(simple),
+                                       core_step_log2, C.c_double(term_cap), C.byref(out), C.byref(ln), C.byref(k),
+                                       C.byref(cnt), _p(flips), C.byref(term), C.byref(plane)))
+    return dict(stream=_take_bytes(out, ln.value), k=k.value, count=cnt.value, flips=flips[:r], term=term.value,
+                plane=plane.value)
+
+
+EXPORTED = ("tcb_compress", "tcb_compress_device", "tcb_default_params", "tcb_free", "tcb_last_error",
+            "tcb_kernel_launches", "tcb_sthosvd_f64", "tcb_gram_f64", "tcb_ttm_f64", "tcb_eig_f64",
+            "tcb_quantize_f64", "tcb_encode", "tcb_encode_symbols", "tcb_encode_factor_f64")

@@ -1,0 +1,311 @@
+// extern "C" boundary (include/tucomp_b200.h).  Each entry point owns one CUDA
+// stream for the call, converts exceptions into status + message, and never
+// falls back to host computation.
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/tucomp_b200.h"
+#include "codec.cuh"
+#include "kernels.cuh"
+#include "pipeline.hpp"
+#include "quant.cuh"
+
+namespace tcb {
+u64& launch_counter() {
+    static u64 c = 0;
+    return c;
+}
+}  // namespace tcb
+
+using namespace tcb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Stream {
+    cudaStream_t s = nullptr;
+    Stream() {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+            throw Error("tucomp_b200: no CUDA device (the B200 path has no CPU fallback)");
+        TCB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    }
+    ~Stream() {
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
+};
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        cudaGetLastError();
+        return 1;
+    }
+}
+
+template <class T>
+T* dup(const std::vector<T>& v) {
+    T* p = static_cast<T*>(std::malloc(v.size() * sizeof(T) + 1));
+    if (!v.empty()) std::memcpy(p, v.data(), v.size() * sizeof(T));
+    return p;
+}
+
+Params to_params(const tcb_params* p, int d) {
+    Params o;
+    if (p->has_target_re) o.target_re = p->target_re;
+    if (p->has_target_sse) o.target_sse = p->target_sse;
+    o.rtmss = p->rtmss;
+    o.threads = p->threads;
+    o.method = p->method;
+    if (p->has_storage_order) o.storage_order = std::vector<u64>(p->storage_order, p->storage_order + d);
+    if (p->has_mode_order) o.mode_order = std::vector<u64>(p->mode_order, p->mode_order + d);
+    o.coder = p->coder;
+    o.split = p->split_planes != 0;
+    o.simple = p->simple_factor_weights != 0;
+    o.block = p->block_size;
+    o.f32 = p->internal_float32 != 0;
+    o.backend = p->svd_backend;
+    return o;
+}
+
+void fill(const Result& r, int d, tcb_result* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->container = dup(r.container);
+    out->container_size = r.container.size();
+    out->truncation_sse = r.trunc;
+    out->core_quantization_sse = r.core_quant;
+    for (int i = 0; i < d && i < 8; ++i) {
+        out->factor_terms[i] = i < static_cast<int>(r.factor_terms.size()) ? r.factor_terms[i] : 0.0;
+        out->ranks[i] = r.ranks[i];
+    }
+    out->estimate_sse = r.estimate;
+    out->norm_sq = r.norm_sq;
+    out->target_sse = r.target_sse;
+    out->order = d;
+    out->times = tcb_times{r.times.sthosvd, r.times.quantize, r.times.core, r.times.factor, r.times.serialize,
+                           r.times.total};
+    out->peak_alloc_estimate = r.peak_alloc;
+    out->original_bytes = r.original_bytes;
+    out->ingest_precision_loss = r.precision_loss;
+    out->core_last_plane = r.core_last_plane;
+    out->core_scale_exponent = r.core_k;
+    out->uncertified_decisions = r.uncertified;
+    out->kernel_launches = launch_counter();
+}
+
+std::size_t dtype_bytes(int t) {
+    static const std::size_t sz[10] = {1, 1, 2, 2, 4, 4, 8, 8, 4, 8};
+    if (t < 0 || t > 9) throw Error("container: unknown dtype");
+    return sz[t];
+}
+
+}  // namespace
+
+extern "C" {
+
+void tcb_default_params(tcb_params* p) {
+    std::memset(p, 0, sizeof(*p));
+    p->rtmss = 0.5;
+    p->threads = 1;
+    p->split_planes = 1;
+}
+
+const char* tcb_last_error(void) { return g_err.c_str(); }
+void tcb_free(void* p) { std::free(p); }
+uint64_t tcb_kernel_launches(void) { return launch_counter(); }
+
+int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d, uint64_t skip,
+                 const tcb_params* params, tcb_result* out) {
+    return guard([&] {
+        std::vector<u64> sh(shape, shape + d);
+        u64 n = 1;
+        for (auto v : sh) n *= v;
+        const u64 expect = skip + n * dtype_bytes(dtype);
+        if (nbytes != expect)
+            throw Error("ingest: buffer holds " + std::to_string(nbytes) + " bytes, expected " + std::to_string(expect));
+        Stream st;
+        DevBuf<u8> dev(nbytes - skip + 16, st.s);
+        dev.upload(bytes + skip, nbytes - skip);
+        const Result r = compress_device(dev.p, nbytes - skip, dtype, sh, to_params(params, d), st.s);
+        fill(r, d, out);
+    });
+}
+
+int tcb_compress_device(const void* device_bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d,
+                        const tcb_params* params, tcb_result* out) {
+    return guard([&] {
+        std::vector<u64> sh(shape, shape + d);
+        Stream st;
+        const Result r = compress_device(device_bytes, nbytes, dtype, sh, to_params(params, d), st.s);
+        fill(r, d, out);
+    });
+}
+
+int tcb_sthosvd_f64(const double* a, const uint64_t* shape, int d, double sse_target, const uint64_t* order,
+                    int backend, double* core, uint64_t* core_shape, double** factors, uint64_t* ranks, double* trunc,
+                    uint64_t* order_out) {
+    return guard([&] {
+        std::vector<u64> sh(shape, shape + d);
+        u64 n = 1;
+        for (auto v : sh) n *= v;
+        Stream st;
+        DevBuf<double> x(n, st.s);
+        x.upload(a, n);
+        std::optional<std::vector<u64>> ord;
+        if (order) ord = std::vector<u64>(order, order + d);
+        Tucker f = sthosvd_device(std::move(x), sh, sse_target, ord, backend, st.s);
+        u64 nc = 1;
+        for (int i = 0; i < d; ++i) {
+            core_shape[i] = f.core_shape[i];
+            nc *= f.core_shape[i];
+            ranks[i] = f.r[i];
+            trunc[i] = f.trunc[i];
+            order_out[i] = f.order[i];
+            f.factors[i].download(factors[i], f.n[i] * f.r[i]);
+        }
+        f.core.download(core, nc);
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int tcb_gram_f64(const double* b, uint64_t rows, uint64_t cols, double* g) {
+    return guard([&] {
+        Stream st;
+        DevBuf<double> B(rows * cols, st.s), G(rows * rows, st.s);
+        B.upload(b, rows * cols);
+        gram_f64(B.p, rows, cols, G.p, st.s);
+        G.download(g, rows * rows);
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int tcb_ttm_f64(const double* b, uint64_t rows, uint64_t cols, const double* u, uint64_t r, double* next) {
+    return guard([&] {
+        Stream st;
+        DevBuf<double> B(rows * cols, st.s), U(rows * r, st.s), O(cols * r, st.s);
+        B.upload(b, rows * cols);
+        U.upload(u, rows * r);
+        ttm_f64(B.p, rows, cols, U.p, r, O.p, st.s);
+        O.download(next, cols * r);
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int tcb_eig_f64(const double* g, uint64_t n, uint64_t r, double* evals_desc, double* u) {
+    return guard([&] {
+        Stream st;
+        DevBuf<double> G(n * n, st.s);
+        G.upload(g, n * n);
+        EigWork w;
+        const auto ev = eig_values(G.p, n, w, st.s);
+        std::memcpy(evals_desc, ev.data(), n * sizeof(double));
+        if (r > 0) {
+            DevBuf<double> U(n * r, st.s);
+            eig_vectors(w, r, U.p, st.s);
+            fix_column_signs(U.p, n, r, st.s);
+            U.download(u, n * r);
+        }
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int tcb_quantize_f64(const double* core, const uint64_t* shape, int d, uint64_t* mag, uint8_t* neg, int* k, int* zero,
+                     double* slice_norms_out) {
+    return guard([&] {
+        std::vector<u64> sh(shape, shape + d);
+        u64 n = 1, se = 0;
+        for (auto v : sh) {
+            n *= v;
+            se += v;
+        }
+        Stream st;
+        DevBuf<double> x(n, st.s);
+        x.upload(core, n);
+        bool fin = true;
+        sum_squares(x.p, n, &fin, st.s);
+        if (!fin) throw Error("quantize: non-finite core values");
+        const double mx = max_abs(x.p, n, st.s);
+        *zero = mx == 0.0;
+        *k = *zero ? 0 : 63 - std::ilogb(mx);
+        if (*zero) {
+            std::memset(slice_norms_out, 0, se * sizeof(double));
+            return;
+        }
+        DevBuf<u64> dm(n, st.s);
+        DevBuf<u8> dn(n, st.s);
+        quantize_f64(x.p, n, *k, dm.p, dn.p, st.s);
+        DevBuf<double> sn(se, st.s);
+        slice_norms(dm.p, sh, std::ldexp(1.0, -2 * *k), sn.p, st.s);
+        dm.download(mag, n);
+        dn.download(neg, n);
+        sn.download(slice_norms_out, se);
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int tcb_encode(const uint64_t* mag, const uint8_t* neg, uint64_t n, double target, int coder, uint64_t block,
+               int split, int fixed_plane, uint8_t** stream, uint64_t* stream_len, int* last_plane,
+               double* achieved, uint64_t* decoded, int* uncertified) {
+    return guard([&] {
+        Stream st;
+        DevBuf<u64> m(n + 1, st.s), dec(n + 1, st.s);
+        DevBuf<u8> ng(n + 1, st.s);
+        m.upload(mag, n);
+        ng.upload(neg, n);
+        EncodeOpts o;
+        o.coder = coder;
+        o.block = block;
+        o.split = split != 0;
+        if (fixed_plane >= 0) o.fixed_plane = fixed_plane;
+        const PlanResult pl = plan_stream(m.p, n, target, o, dec.p, st.s);
+        const auto body = finalize_stream(m.p, ng.p, n, pl, coder, n, st.s);
+        const SumRec a = n ? device_sum(SumKind::diff_backward, m.p, dec.p, n, 0, st.s) : SumRec{0, 0, 0, 0};
+        if (decoded) dec.download(decoded, n);
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+        *stream = dup(body);
+        *stream_len = body.size();
+        *last_plane = pl.last_plane;
+        *achieved = a.hi + a.lo;
+        if (uncertified) *uncertified = pl.fallbacks;
+    });
+}
+
+int tcb_encode_symbols(int coder, const uint64_t* syms, uint64_t n, uint8_t** out, uint64_t* len) {
+    return guard([&] {
+        Stream st;
+        const auto b = encode_symbols_device(coder, syms, n, st.s);
+        *out = dup(b);
+        *len = b.size();
+    });
+}
+
+int tcb_encode_factor_f64(const double* u, uint64_t n, uint64_t r, const uint8_t* dead, const double* sn, int coder,
+                          int simple, int core_step_log2, double cap, uint8_t** stream, uint64_t* len, int* k,
+                          uint64_t* count, int8_t* flips, double* term, int* plane) {
+    return guard([&] {
+        Stream st;
+        DevBuf<double> U(n * r + 1, st.s);
+        U.upload(u, n * r);
+        const auto fe = encode_factor_device(U.p, n, r, std::vector<u8>(dead, dead + r),
+                                             std::vector<double>(sn, sn + r), coder, simple != 0, core_step_log2, cap,
+                                             false, st.s);
+        *stream = dup(fe.stream);
+        *len = fe.stream.size();
+        *k = fe.k;
+        *count = fe.count;
+        for (u64 j = 0; j < r; ++j) flips[j] = fe.flips[j];
+        *term = fe.term;
+        *plane = fe.plane;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,872 @@
+// Bit-plane codec kernels: the bit-exact half of the compress path.
+//
+// Statistics (core_codec.cpp:120-171, error_model.cpp:34-72): every term is
+// computed with separately rounded __dmul_rn/__dsub_rn exactly as the
+// reference's x86-64 build (no FMA contraction), summed in double-double
+// (error ~2^-104) together with a rigorous bound on the reference's serial
+// rounding error, so the host can certify each breakpoint/stop decision and
+// fall back to the serial replay kernels below only when it cannot.
+//
+// Emission (core_codec.cpp:120-171, entropy.cpp:22-239): one CTA per
+// (plane, block) stream classifies positions with CTA-wide scans, writes the
+// zero-run symbols and the MSB-first raw bits; the adaptive range coder then
+// runs one thread per stream; payloads are compacted in stream order.
+#include <algorithm>
+#include <cfloat>
+
+#include "codec.cuh"
+
+namespace tcb {
+
+namespace {
+
+__device__ __forceinline__ int top_bit(u64 m) { return m ? 63 - __clzll(static_cast<long long>(m)) : -1; }
+
+// residual^2 of a significant coefficient with planes >= p known (core_codec.cpp:20-30)
+__device__ __forceinline__ double sig2(u64 m, int p) {
+    if (p == 0) return 0.0;
+    const u64 low = m & ((u64{1} << p) - 1);
+    const double r = __dsub_rn(__ull2double_rn(low), __ull2double_rn(u64{1} << (p - 1)));
+    return __dmul_rn(r, r);
+}
+__device__ __forceinline__ double insig2(u64 m) {
+    const double v = __ull2double_rn(m);
+    return __dmul_rn(v, v);
+}
+__device__ __forceinline__ double trail_gain(u64 m, int p) { return __dsub_rn(sig2(m, p + 1), sig2(m, p)); }
+__device__ __forceinline__ double lead_gain(u64 m, int p) { return __dsub_rn(insig2(m), sig2(m, p)); }
+
+struct DD {
+    double hi, lo;
+};
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+    s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+__device__ __forceinline__ DD dd_add(DD x, double t) {
+    double s, e;
+    two_sum(x.hi, t, s, e);
+    e = __dadd_rn(e, x.lo);
+    DD r;
+    two_sum(s, e, r.hi, r.lo);
+    return r;
+}
+__device__ __forceinline__ DD dd_add(DD x, DD y) {
+    double s, e;
+    two_sum(x.hi, y.hi, s, e);
+    e = __dadd_rn(e, __dadd_rn(x.lo, y.lo));
+    DD r;
+    two_sum(s, e, r.hi, r.lo);
+    return r;
+}
+
+__device__ __forceinline__ double recal_term(u64 m, int plane) {
+    double r;
+    if (plane >= 64 || (m >> plane) == 0) r = __ull2double_rn(m);
+    else if (plane == 0) r = 0.0;
+    else r = __dsub_rn(__ull2double_rn(m & ((u64{1} << plane) - 1)), __ull2double_rn(u64{1} << (plane - 1)));
+    return __dmul_rn(r, r);
+}
+
+__device__ __forceinline__ double sum_term(SumKind k, const u64* m, const u64* dec, u64 i, int plane) {
+    switch (k) {
+        case SumKind::sq_backward: return insig2(m[i]);
+        case SumKind::recal_backward: return recal_term(m[i], plane);
+        default: {
+            const double r = __dsub_rn(__ull2double_rn(m[i]), __ull2double_rn(dec[i]));
+            return __dmul_rn(r, r);
+        }
+    }
+}
+
+constexpr int kSumThreads = 256;
+
+__global__ void sum_kernel(SumKind kind, const u64* __restrict__ m, const u64* __restrict__ dec, u64 n, int plane,
+                           SumRec* __restrict__ part) {
+    __shared__ double sh[3][kSumThreads / 32];
+    DD acc{0.0, 0.0};
+    double w = 0.0;
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double t = sum_term(kind, m, dec, i, plane);
+        acc = dd_add(acc, t);
+        w = fma(fabs(t), static_cast<double>(i + 1), w);  // backward: x_i sits in i+1 partial sums
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        DD other{__shfl_down_sync(0xffffffffu, acc.hi, o), __shfl_down_sync(0xffffffffu, acc.lo, o)};
+        acc = dd_add(acc, other);
+        w += __shfl_down_sync(0xffffffffu, w, o);
+    }
+    const int wid = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        sh[0][wid] = acc.hi;
+        sh[1][wid] = acc.lo;
+        sh[2][wid] = w;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        DD t{0.0, 0.0};
+        double ww = 0.0;
+        for (int i = 0; i < kSumThreads / 32; ++i) {
+            t = dd_add(t, DD{sh[0][i], sh[1][i]});
+            ww += sh[2][i];
+        }
+        part[blockIdx.x] = SumRec{t.hi, t.lo, ww, 0};
+    }
+}
+
+__global__ void sum_serial_kernel(SumKind kind, const u64* __restrict__ m, const u64* __restrict__ dec, u64 n,
+                                  int plane, double* out) {
+    double s = 0.0;
+    for (u64 i = n; i-- > 0;) s = __dadd_rn(s, sum_term(kind, m, dec, i, plane));
+    *out = s;
+}
+
+// ---------------------------------------------------------------- per-plane stats
+constexpr int kStatThreads = 256;
+constexpr int kStatPer = 8;
+constexpr u64 kChunk = static_cast<u64>(kStatThreads) * kStatPer;
+
+struct Partial {
+    double lhi, llo, lw, thi, tlo, tw;
+    u64 nlead, nones, ntrail;
+};
+
+__global__ void stats_kernel(const u64* __restrict__ m, u64 n, u64 block, u64 cpb, int p_hi,
+                             Partial* __restrict__ part) {
+    const int p = p_hi - static_cast<int>(blockIdx.y);
+    const u64 b = blockIdx.x / cpb, j = blockIdx.x % cpb;
+    const u64 blo = b * block, bhi = min(n, blo + block);
+    const u64 lo = blo + j * kChunk, hi = min(bhi, lo + kChunk);
+    DD L{0.0, 0.0}, T{0.0, 0.0};
+    double lw = 0.0, tw = 0.0;
+    u64 nl = 0, no = 0, nt = 0;
+    for (u64 i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const u64 v = m[i];
+        const int tb = top_bit(v);
+        const double rest = static_cast<double>(bhi - i);  // >= #terms from here to the block end
+        if (tb > p) {
+            const double t = trail_gain(v, p);
+            T = dd_add(T, t);
+            tw = fma(fabs(t), rest, tw);
+            ++nt;
+        } else {
+            ++nl;
+            if (tb == p) {
+                const double t = lead_gain(v, p);
+                L = dd_add(L, t);
+                lw = fma(fabs(t), rest, lw);
+                ++no;
+            }
+        }
+    }
+    __shared__ Partial sh[kStatThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) {
+        L = dd_add(L, DD{__shfl_down_sync(0xffffffffu, L.hi, o), __shfl_down_sync(0xffffffffu, L.lo, o)});
+        T = dd_add(T, DD{__shfl_down_sync(0xffffffffu, T.hi, o), __shfl_down_sync(0xffffffffu, T.lo, o)});
+        lw += __shfl_down_sync(0xffffffffu, lw, o);
+        tw += __shfl_down_sync(0xffffffffu, tw, o);
+        nl += __shfl_down_sync(0xffffffffu, nl, o);
+        no += __shfl_down_sync(0xffffffffu, no, o);
+        nt += __shfl_down_sync(0xffffffffu, nt, o);
+    }
+    const int wid = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) sh[wid] = Partial{L.hi, L.lo, lw, T.hi, T.lo, tw, nl, no, nt};
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        DD l{0.0, 0.0}, t{0.0, 0.0};
+        Partial r{};
+        for (int i = 0; i < kStatThreads / 32; ++i) {
+            l = dd_add(l, DD{sh[i].lhi, sh[i].llo});
+            t = dd_add(t, DD{sh[i].thi, sh[i].tlo});
+            r.lw += sh[i].lw;
+            r.tw += sh[i].tw;
+            r.nlead += sh[i].nlead;
+            r.nones += sh[i].nones;
+            r.ntrail += sh[i].ntrail;
+        }
+        r.lhi = l.hi;
+        r.llo = l.lo;
+        r.thi = t.hi;
+        r.tlo = t.lo;
+        part[(static_cast<u64>(blockIdx.y) * gridDim.x) + blockIdx.x] = r;
+    }
+}
+
+__global__ void stats_combine(const Partial* __restrict__ part, u64 nb, u64 cpb, int nplanes,
+                              PlaneBlockRec* __restrict__ out, u64 n, u64 block) {
+    const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= nb * static_cast<u64>(nplanes)) return;
+    const u64 pl = idx / nb, b = idx % nb;
+    DD l{0.0, 0.0}, t{0.0, 0.0};
+    PlaneBlockRec r{};
+    for (u64 j = 0; j < cpb; ++j) {
+        const Partial& q = part[pl * nb * cpb + b * cpb + j];
+        l = dd_add(l, DD{q.lhi, q.llo});
+        t = dd_add(t, DD{q.thi, q.tlo});
+        r.lead.wabs += q.lw;
+        r.trail.wabs += q.tw;
+        r.nlead += q.nlead;
+        r.nones += q.nones;
+        r.ntrail += q.ntrail;
+    }
+    r.lead.hi = l.hi;
+    r.lead.lo = l.lo;
+    r.lead.nterms = r.nones;
+    r.trail.hi = t.hi;
+    r.trail.lo = t.lo;
+    r.trail.nterms = r.ntrail;
+    (void)n;
+    (void)block;
+    out[idx] = r;
+}
+
+// serial replay of build_block's sums for every block of one plane (one thread per block)
+__global__ void stats_serial_kernel(const u64* __restrict__ m, u64 n, u64 block, u64 nb, int p,
+                                    PlaneBlockRec* __restrict__ out) {
+    const u64 b = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const u64 lo = b * block, hi = min(n, lo + block);
+    double l = 0.0, t = 0.0;
+    u64 nl = 0, no = 0, nt = 0;
+    for (u64 i = lo; i < hi; ++i) {
+        const u64 v = m[i];
+        const int tb = top_bit(v);
+        if (tb > p) {
+            t = __dadd_rn(t, trail_gain(v, p));
+            ++nt;
+        } else {
+            ++nl;
+            if (tb == p) {
+                l = __dadd_rn(l, lead_gain(v, p));
+                ++no;
+            }
+        }
+    }
+    PlaneBlockRec r{};
+    r.lead = SumRec{l, 0.0, 0.0, no};
+    r.trail = SumRec{t, 0.0, 0.0, nt};
+    r.nlead = nl;
+    r.nones = no;
+    r.ntrail = nt;
+    out[b] = r;
+}
+
+__global__ void crossing_kernel(const u64* __restrict__ m, u64 lo, u64 hi, int p, int category,
+                                const double* __restrict__ cum0, const double* __restrict__ need, int npairs,
+                                u64* __restrict__ out) {
+    const int k = threadIdx.x;
+    if (k >= npairs) return;
+    double cum = cum0[k];
+    const double nd = need[k];
+    u64 c = 0, nl = 0, nt = 0;
+    for (u64 i = lo; i < hi && cum < nd; ++i) {
+        const u64 v = m[i];
+        const int tb = top_bit(v);
+        if (category == 0) {
+            if (tb > p) continue;
+            if (tb == p) cum = __dadd_rn(cum, lead_gain(v, p));
+            ++c;
+        } else if (category == 1) {
+            if (tb <= p) continue;
+            cum = __dadd_rn(cum, trail_gain(v, p));
+            ++c;
+        } else {
+            if (tb > p) {
+                cum = __dadd_rn(cum, trail_gain(v, p));
+                ++nt;
+            } else {
+                if (tb == p) cum = __dadd_rn(cum, lead_gain(v, p));
+                ++nl;
+            }
+        }
+    }
+    if (category == 2) {
+        out[2 * k] = nl;
+        out[2 * k + 1] = nt;
+    } else {
+        out[2 * k] = c;
+        out[2 * k + 1] = 0;
+    }
+}
+
+// ---------------------------------------------------------------- CTA scans
+template <int NT>
+__device__ __forceinline__ u64 cta_excl_scan(u64 v, u64* sh, u64& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    u64 x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh[w] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 run = 0;
+        for (int i = 0; i < NT / 32; ++i) {
+            const u64 t = sh[i];
+            sh[i] = run;
+            run += t;
+        }
+        sh[NT / 32] = run;
+    }
+    __syncthreads();
+    const u64 res = sh[w] + x - v;
+    total = sh[NT / 32];
+    __syncthreads();
+    return res;
+}
+
+template <int NT>
+__device__ __forceinline__ long long cta_excl_max(long long v, long long* sh, long long init) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = max(x, y);
+    }
+    long long ex = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) ex = LLONG_MIN;
+    if (lane == 31) sh[w] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long run = init;
+        for (int i = 0; i < NT / 32; ++i) {
+            const long long t = sh[i];
+            sh[i] = run;
+            run = max(run, t);
+        }
+        sh[NT / 32] = run;
+    }
+    __syncthreads();
+    const long long res = max(sh[w], ex);
+    __syncthreads();
+    return res;
+}
+
+// ---------------------------------------------------------------- decoded model
+constexpr int kDecThreads = 256;
+constexpr int kDecPer = 4;
+
+__global__ void decode_model_kernel(const u64* __restrict__ m, u64 n, u64 block, int lp,
+                                    const u64* __restrict__ stops, u64* __restrict__ dec) {
+    __shared__ u64 sh[kDecThreads / 32 + 1];
+    const u64 b = blockIdx.x;
+    const u64 lo = b * block, hi = min(n, lo + block);
+    const u64 lstop = stops[2 * b], tstop = stops[2 * b + 1];
+    u64 lbase = 0, tbase = 0;
+    for (u64 c0 = lo; c0 < hi; c0 += static_cast<u64>(kDecThreads) * kDecPer) {
+        const u64 i0 = c0 + static_cast<u64>(threadIdx.x) * kDecPer;
+        u64 v[kDecPer];
+        int tb[kDecPer];
+        u32 nl = 0, nt = 0;
+#pragma unroll
+        for (int q = 0; q < kDecPer; ++q) {
+            const u64 i = i0 + q;
+            v[q] = i < hi ? m[i] : 0;
+            tb[q] = i < hi ? top_bit(v[q]) : -2;
+            nt += tb[q] > lp;
+            nl += (tb[q] <= lp && tb[q] > -2);
+        }
+        u64 tot;
+        const u64 pre = cta_excl_scan<kDecThreads>((static_cast<u64>(nt) << 32) | nl, sh, tot);
+        u64 li = lbase + (pre & 0xffffffffu), ti = tbase + (pre >> 32);
+#pragma unroll
+        for (int q = 0; q < kDecPer; ++q) {
+            const u64 i = i0 + q;
+            if (tb[q] == -2) continue;
+            int pe = -1;
+            if (tb[q] > lp) {
+                pe = (ti++ < tstop) ? lp : lp + 1;
+            } else {
+                const bool within = li++ < lstop;
+                if (tb[q] == lp && within) pe = lp;
+            }
+            u64 out = 0;
+            if (pe >= 0) {
+                out = pe >= 64 ? 0 : (v[q] >> pe) << pe;
+                if (pe >= 1 && pe < 64) out += u64{1} << (pe - 1);
+            }
+            dec[i] = out;
+        }
+        lbase += tot & 0xffffffffu;
+        tbase += tot >> 32;
+    }
+}
+
+// ---------------------------------------------------------------- emission
+constexpr int kEmT = 256;
+constexpr int kEmPer = 4;
+
+struct StreamDesc {
+    u64 lo, hi;          // block range
+    u64 lstop, tstop;
+    u64 sym_off;         // into syms
+    u64 raw_off;         // bit offset into raw words (multiple of 32)
+    int plane;
+    int pad;
+};
+
+struct StreamOut {
+    u64 nsyms;    // 0 when the leading column is empty
+    u64 nraw;     // raw bits
+};
+
+__global__ void __launch_bounds__(kEmT) emit_kernel(const u64* __restrict__ m, const u8* __restrict__ neg,
+                                                    const StreamDesc* __restrict__ desc, u64* __restrict__ syms,
+                                                    u32* __restrict__ raw, StreamOut* __restrict__ sout) {
+    __shared__ u64 sh[kEmT / 32 + 1];
+    __shared__ long long shm[kEmT / 32 + 1];
+    const StreamDesc d = desc[blockIdx.x];
+    const int p = d.plane;
+    u64 lcnt = 0, tcnt = 0, rawcnt = 0, onecnt = 0;
+    long long last = -1;  // lead index of the previous one
+    for (u64 c0 = d.lo; c0 < d.hi; c0 += static_cast<u64>(kEmT) * kEmPer) {
+        const u64 i0 = c0 + static_cast<u64>(threadIdx.x) * kEmPer;
+        u64 v[kEmPer];
+        int tb[kEmPer];
+        u32 nl = 0, nt = 0;
+#pragma unroll
+        for (int q = 0; q < kEmPer; ++q) {
+            const u64 i = i0 + q;
+            const bool in = i < d.hi;
+            v[q] = in ? m[i] : 0;
+            tb[q] = in ? top_bit(v[q]) : -2;
+            nt += tb[q] > p;
+            nl += (tb[q] <= p && tb[q] > -2);
+        }
+        u64 tot;
+        const u64 pre = cta_excl_scan<kEmT>((static_cast<u64>(nt) << 32) | nl, sh, tot);
+        u64 li = lcnt + (pre & 0xffffffffu), ti = tcnt + (pre >> 32);
+        // classify within the stops
+        u32 rflag = 0, oflag = 0, nr = 0, no = 0;
+        long long lastL = -1;
+        u64 lidx[kEmPer];
+#pragma unroll
+        for (int q = 0; q < kEmPer; ++q) {
+            lidx[q] = 0;
+            if (tb[q] == -2) continue;
+            if (tb[q] > p) {
+                if (ti++ < d.tstop) {
+                    rflag |= 1u << q;
+                    ++nr;
+                }
+            } else {
+                const u64 myl = li++;
+                if (myl < d.lstop && tb[q] == p) {
+                    oflag |= 1u << q;
+                    rflag |= 1u << q;
+                    ++nr;
+                    ++no;
+                    lidx[q] = myl;
+                    lastL = static_cast<long long>(myl);
+                }
+            }
+        }
+        u64 tot2;
+        const u64 pre2 = cta_excl_scan<kEmT>((static_cast<u64>(nr) << 32) | no, sh, tot2);
+        const long long prevL = cta_excl_max<kEmT>(lastL, shm, last);
+        u64 ri = rawcnt + (pre2 >> 32), oi = onecnt + (pre2 & 0xffffffffu);
+        long long pl = prevL;
+#pragma unroll
+        for (int q = 0; q < kEmPer; ++q) {
+            if (!(rflag >> q & 1u)) continue;
+            bool bit;
+            if (oflag >> q & 1u) {
+                bit = neg ? neg[i0 + q] != 0 : false;
+                syms[d.sym_off + oi] = static_cast<u64>(static_cast<long long>(lidx[q]) - pl - 1);
+                pl = static_cast<long long>(lidx[q]);
+                ++oi;
+            } else {
+                bit = (v[q] >> p) & 1u;
+            }
+            if (bit) {
+                const u64 R = d.raw_off + ri;
+                atomicOr(raw + (R >> 5), 1u << (8 * ((R >> 3) & 3) + (7 - (R & 7))));
+            }
+            ++ri;
+        }
+        lcnt += tot & 0xffffffffu;
+        tcnt += tot >> 32;
+        rawcnt += tot2 >> 32;
+        onecnt += tot2 & 0xffffffffu;
+        // last one index so far
+        __shared__ long long shl;
+        if (threadIdx.x == kEmT - 1) shl = max(prevL, lastL);
+        __syncthreads();
+        last = shl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const u64 ncol = min(lcnt, d.lstop);
+        StreamOut o;
+        o.nraw = rawcnt;
+        if (ncol > 0) {
+            syms[d.sym_off + onecnt] = static_cast<u64>(static_cast<long long>(ncol) - 1 - last);
+            o.nsyms = onecnt + 1;
+        } else {
+            o.nsyms = 0;
+        }
+        sout[blockIdx.x] = o;
+    }
+}
+
+// ---------------------------------------------------------------- adaptive range coder
+struct AcDesc {
+    u64 sym_off;     // symbols
+    u64 out_off;     // output byte offset (capacity 5 + 7*nsyms + 16)
+    u64 model_off;   // u32 words of scratch
+    u32 cap;         // model capacity (>= distinct symbols + 1)
+    u32 fen;         // fenwick array size (power of two >= cap + 1)
+    u32 hbits;       // hash table has 1 << hbits u32 slots
+    u32 pad;
+};
+
+struct AcState {
+    u64 low;
+    u32 range;
+    u8 cache;
+    u64 pending;
+    u8* out;
+    u64 pos;
+};
+
+__device__ __forceinline__ void ac_shift(AcState& s) {
+    if (static_cast<u32>(s.low) < 0xFF000000u || (s.low >> 32) != 0) {
+        const u8 carry = static_cast<u8>(s.low >> 32);
+        u8 first = s.cache;
+        while (s.pending) {
+            s.out[s.pos++] = static_cast<u8>(first + carry);
+            first = 0xFF;
+            --s.pending;
+        }
+        s.cache = static_cast<u8>(s.low >> 24);
+    }
+    ++s.pending;
+    s.low = (s.low << 8) & 0xFFFFFFFFull;
+}
+
+__device__ __forceinline__ void ac_code(AcState& s, u32 cum, u32 freq, u32 total) {
+    s.range /= total;
+    s.low += static_cast<u64>(cum) * s.range;
+    s.range *= freq;
+    while (s.range < (1u << 24)) {
+        ac_shift(s);
+        s.range <<= 8;
+    }
+}
+
+__device__ __forceinline__ u32 hslot(u64 sym, u32 hbits) {
+    return static_cast<u32>((sym * 0x9E3779B97F4A7C15ull) >> (64 - hbits));
+}
+
+__global__ void ac_kernel(const u64* __restrict__ syms, const StreamOut* __restrict__ sout,
+                          const AcDesc* __restrict__ desc, int nstreams, u8* __restrict__ outbuf,
+                          u32* __restrict__ scratch, u64* __restrict__ elen) {
+    const int sidx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sidx >= nstreams) return;
+    const u64 ns = sout[sidx].nsyms;
+    if (ns == 0) {
+        elen[sidx] = 0;
+        return;
+    }
+    const AcDesc d = desc[sidx];
+    u32* cnt = scratch + d.model_off;                 // cap
+    u32* fen = cnt + d.cap;                           // fen
+    u32* hidx = fen + d.fen;                          // 1 << hbits (index + 1)
+    u64* val = reinterpret_cast<u64*>(hidx + (1u << d.hbits));  // cap (8-byte aligned by construction)
+    for (u32 i = 0; i < d.fen; ++i) fen[i] = 0;
+    for (u32 i = 0; i < (1u << d.hbits); ++i) hidx[i] = 0;
+    u8* out = outbuf + d.out_off;
+    out[0] = 0;  // coder id: arithmetic
+    const u32 cnt32 = static_cast<u32>(ns);
+    for (int i = 0; i < 4; ++i) out[1 + i] = static_cast<u8>(cnt32 >> (8 * i));
+    AcState st{0, 0xFFFFFFFFu, 0, 1, out, 5};
+    u32 nsym = 1, total = 1;
+    cnt[0] = 1;
+    val[0] = 0;
+    auto fadd = [&](u32 i, u32 dlt) {
+        for (u32 j = i + 1; j < d.fen; j += j & (~j + 1)) fen[j] += dlt;
+    };
+    auto below = [&](u32 i) {
+        u32 s = 0;
+        for (u32 j = i; j > 0; j -= j & (~j + 1)) s += fen[j];
+        return s;
+    };
+    auto rebuild = [&]() {
+        for (u32 i = 0; i < d.fen; ++i) fen[i] = 0;
+        for (u32 i = 0; i < nsym; ++i) fen[i + 1] = cnt[i];
+        for (u32 i = 1; i < d.fen; ++i) {
+            const u32 j = i + (i & (~i + 1));
+            if (j < d.fen) fen[j] += fen[i];
+        }
+    };
+    auto halve = [&]() {
+        total = 0;
+        for (u32 i = 0; i < nsym; ++i) {
+            cnt[i] = max(1u, cnt[i] >> 1);
+            total += cnt[i];
+        }
+        rebuild();
+    };
+    fadd(0, 1);
+    const u64* sy = syms + d.sym_off;
+    for (u64 t = 0; t < ns; ++t) {
+        const u64 s = sy[t];
+        u32 h = hslot(s, d.hbits), found = 0;
+        while (hidx[h]) {
+            if (val[hidx[h] - 1] == s) {
+                found = hidx[h];
+                break;
+            }
+            h = (h + 1) & ((1u << d.hbits) - 1);
+        }
+        if (found) {
+            const u32 i = found - 1;
+            ac_code(st, below(i), cnt[i], total);
+            if (total + 32 >= (1u << 16)) halve();
+            cnt[i] += 32;
+            total += 32;
+            fadd(i, 32);
+        } else {
+            ac_code(st, 0, cnt[0], total);
+            for (int b = 31; b >= 0; --b) ac_code(st, static_cast<u32>((s >> b) & 1u), 1, 2);
+            if (total + 32 >= (1u << 16)) halve();
+            const u32 i = nsym++;
+            val[i] = s;
+            cnt[i] = 32;
+            fadd(i, 32);
+            total += 32;
+            hidx[h] = i + 1;
+        }
+    }
+    for (int i = 0; i < 5; ++i) ac_shift(st);
+    elen[sidx] = st.pos;
+}
+
+// ---------------------------------------------------------------- assembly
+__global__ void assemble_kernel(const u8* __restrict__ ent, const AcDesc* __restrict__ acd,
+                                const u64* __restrict__ elen, const u32* __restrict__ raw,
+                                const StreamDesc* __restrict__ sd, const StreamOut* __restrict__ so,
+                                const u64* __restrict__ dst_off, u8* __restrict__ body) {
+    const int s = blockIdx.x;
+    const u64 el = elen[s];
+    const u64 rb = (so[s].nraw + 7) / 8;
+    const u64 payload = 4 + el + rb;
+    u8* o = body + dst_off[s];
+    if (threadIdx.x < 4) {
+        o[threadIdx.x] = static_cast<u8>(static_cast<u32>(payload) >> (8 * threadIdx.x));
+        o[4 + threadIdx.x] = static_cast<u8>(static_cast<u32>(el) >> (8 * threadIdx.x));
+    }
+    const u8* e = ent + acd[s].out_off;
+    for (u64 i = threadIdx.x; i < el; i += blockDim.x) o[8 + i] = e[i];
+    const u64 rbyte0 = sd[s].raw_off >> 3;
+    const u8* rbytes = reinterpret_cast<const u8*>(raw);
+    for (u64 i = threadIdx.x; i < rb; i += blockDim.x) o[8 + el + i] = rbytes[rbyte0 + i];
+}
+
+}  // namespace
+
+// ================================================================ host launchers
+SumRec device_sum(SumKind kind, const u64* m, const u64* dec, u64 n, int plane, cudaStream_t s) {
+    const int grid = sm_count() * 4;
+    DevBuf<SumRec> part(grid, s);
+    sum_kernel<<<grid, kSumThreads, 0, s>>>(kind, m, dec, n, plane, part.p);
+    count_launch();
+    TCB_LAUNCH();
+    auto h = part.to_host();
+    // fixed-order double-double combine on the host
+    double hi = 0.0, lo = 0.0, w = 0.0;
+    for (const auto& r : h) {
+        const double s1 = hi + r.hi;
+        const double bb = s1 - hi;
+        const double e1 = (hi - (s1 - bb)) + (r.hi - bb);
+        const double e = e1 + lo + r.lo;
+        hi = s1 + e;
+        lo = e - (hi - s1);
+        w += r.wabs;
+    }
+    return SumRec{hi, lo, w, n};
+}
+
+double device_sum_serial(SumKind kind, const u64* m, const u64* dec, u64 n, int plane, cudaStream_t s) {
+    DevBuf<double> out(1, s);
+    sum_serial_kernel<<<1, 1, 0, s>>>(kind, m, dec, n, plane, out.p);
+    count_launch();
+    TCB_LAUNCH();
+    return out.to_host()[0];
+}
+
+void plane_stats(const u64* m, u64 n, u64 block, int p_hi, int p_lo, PlaneBlockRec* out_host, cudaStream_t s) {
+    const u64 nb = (n + block - 1) / block;
+    const u64 cpb = (block + kChunk - 1) / kChunk;
+    const int np = p_hi - p_lo + 1;
+    DevBuf<Partial> part(nb * cpb * np, s);
+    DevBuf<PlaneBlockRec> out(nb * np, s);
+    dim3 grid(static_cast<unsigned>(nb * cpb), static_cast<unsigned>(np));
+    stats_kernel<<<grid, kStatThreads, 0, s>>>(m, n, block, cpb, p_hi, part.p);
+    stats_combine<<<cdiv(nb * np, 128), 128, 0, s>>>(part.p, nb, cpb, np, out.p, n, block);
+    count_launch(2);
+    TCB_LAUNCH();
+    out.download(out_host, nb * np);
+    TCB_CUDA(cudaStreamSynchronize(s));
+}
+
+void plane_stats_serial(const u64* m, u64 n, u64 block, int p, PlaneBlockRec* out_host, cudaStream_t s) {
+    const u64 nb = (n + block - 1) / block;
+    DevBuf<PlaneBlockRec> out(nb, s);
+    stats_serial_kernel<<<cdiv(nb, 64), 64, 0, s>>>(m, n, block, nb, p, out.p);
+    count_launch();
+    TCB_LAUNCH();
+    out.download(out_host, nb);
+    TCB_CUDA(cudaStreamSynchronize(s));
+}
+
+void crossing_scan(const u64* m, u64 n, u64 block, u64 b, int plane, int category, const double* cum,
+                   const double* need, int npairs, u64* counts_host, cudaStream_t s) {
+    DevBuf<double> c(npairs, s), nd(npairs, s);
+    DevBuf<u64> out(2 * npairs, s);
+    c.upload(cum, npairs);
+    nd.upload(need, npairs);
+    const u64 lo = b * block, hi = std::min<u64>(n, lo + block);
+    crossing_kernel<<<1, 32, 0, s>>>(m, lo, hi, plane, category, c.p, nd.p, npairs, out.p);
+    count_launch();
+    TCB_LAUNCH();
+    out.download(counts_host, 2 * npairs);
+    TCB_CUDA(cudaStreamSynchronize(s));
+}
+
+void decode_model(const u64* m, u64 n, u64 block, int last_plane, const u64* stops_dev, u64* dec, cudaStream_t s) {
+    const u64 nb = (n + block - 1) / block;
+    if (nb == 0) return;
+    decode_model_kernel<<<static_cast<unsigned>(nb), kDecThreads, 0, s>>>(m, n, block, last_plane, stops_dev, dec);
+    count_launch();
+    TCB_LAUNCH();
+}
+
+std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cudaStream_t s) {
+    if (coder != 0) throw Error("core codec: the rANS backend is not available on the device path yet");
+    std::vector<u8> out{static_cast<u8>(coder)};
+    for (int i = 0; i < 4; ++i) out.push_back(static_cast<u8>(static_cast<u32>(n) >> (8 * i)));
+    if (n == 0) return out;
+    DevBuf<u64> syms(n, s);
+    syms.upload(syms_host, n);
+    StreamOut so{n, 0};
+    DevBuf<StreamOut> dso(1, s);
+    dso.upload(&so, 1);
+    AcDesc a{};
+    a.cap = static_cast<u32>((n + 2) & ~u64{1});
+    a.fen = 2;
+    while (a.fen < a.cap + 1) a.fen *= 2;
+    a.hbits = 4;
+    while ((1u << a.hbits) < 2 * a.cap) ++a.hbits;
+    DevBuf<AcDesc> dad(1, s);
+    dad.upload(&a, 1);
+    DevBuf<u8> ent(5 + 7 * n + 16, s);
+    DevBuf<u32> scratch(a.cap + a.fen + (u64{1} << a.hbits) + 2ull * a.cap + 2, s);
+    DevBuf<u64> elen(1, s);
+    ac_kernel<<<1, 32, 0, s>>>(syms.p, dso.p, dad.p, 1, ent.p, scratch.p, elen.p);
+    count_launch();
+    TCB_LAUNCH();
+    const u64 el = elen.to_host()[0];
+    out.resize(el);
+    ent.download(out.data(), el);
+    TCB_CUDA(cudaStreamSynchronize(s));
+    return out;
+}
+
+EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
+                       const u64* stops_host, int coder, bool want_body, cudaStream_t s) {
+    EmitResult res;
+    if (coder != 0) throw Error("core codec: the rANS backend is not available on the device path yet");
+    const u64 nb = n == 0 ? 0 : (n + block - 1) / block;
+    const int np = top_plane - last_plane + 1;
+    const u64 ns = nb * static_cast<u64>(np);
+    if (ns == 0 || np <= 0) return res;
+    // upper bounds per stream: symbols <= positions + 1, raw bits <= positions
+    std::vector<StreamDesc> sd(ns);
+    u64 sym_total = 0, raw_words = 0;
+    for (int pi = 0; pi < np; ++pi) {
+        const int p = top_plane - pi;
+        for (u64 b = 0; b < nb; ++b) {
+            StreamDesc& d = sd[pi * nb + b];
+            d.lo = b * block;
+            d.hi = std::min<u64>(n, d.lo + block);
+            d.plane = p;
+            const bool bp = p == last_plane && stops_host != nullptr;
+            d.lstop = bp ? stops_host[2 * b] : kFull;
+            d.tstop = bp ? stops_host[2 * b + 1] : kFull;
+            d.sym_off = sym_total;
+            sym_total += d.hi - d.lo + 1;
+            d.raw_off = raw_words * 32;
+            raw_words += (d.hi - d.lo + 31) / 32;
+        }
+    }
+    DevBuf<StreamDesc> dsd(ns, s);
+    dsd.upload(sd.data(), ns);
+    DevBuf<u64> syms(sym_total, s);
+    DevBuf<u32> raw(raw_words + 1, s);
+    raw.zero();
+    DevBuf<StreamOut> so(ns, s);
+    emit_kernel<<<static_cast<unsigned>(ns), kEmT, 0, s>>>(m, neg, dsd.p, syms.p, raw.p, so.p);
+    count_launch();
+    TCB_LAUNCH();
+    std::vector<StreamOut> soh(ns);
+    so.download(soh.data(), ns);
+    TCB_CUDA(cudaStreamSynchronize(s));
+    // model scratch and output capacity per stream
+    std::vector<AcDesc> ad(ns);
+    u64 out_total = 0, scratch_total = 0;
+    for (u64 i = 0; i < ns; ++i) {
+        AcDesc& a = ad[i];
+        a.sym_off = sd[i].sym_off;
+        const u64 k = soh[i].nsyms;
+        a.out_off = out_total;
+        out_total += k ? 5 + 7 * k + 16 : 0;
+        u32 cap = static_cast<u32>((k + 2) & ~u64{1});  // even: keeps the u64 value array aligned
+        u32 fen = 2;
+        while (fen < cap + 1) fen *= 2;
+        u32 hb = 4;
+        while ((1u << hb) < 2 * cap) ++hb;
+        a.cap = cap;
+        a.fen = fen;
+        a.hbits = hb;
+        a.model_off = scratch_total;
+        if (k) {
+            scratch_total += cap + fen + (u64{1} << hb) + 2ull * cap;
+        }
+    }
+    DevBuf<AcDesc> dad(ns, s);
+    dad.upload(ad.data(), ns);
+    DevBuf<u8> ent(out_total + 1, s);
+    DevBuf<u32> scratch(scratch_total + 2, s);
+    DevBuf<u64> elen(ns, s);
+    ac_kernel<<<cdiv(ns, 32), 32, 0, s>>>(syms.p, so.p, dad.p, static_cast<int>(ns), ent.p, scratch.p, elen.p);
+    count_launch();
+    TCB_LAUNCH();
+    std::vector<u64> el(ns);
+    elen.download(el.data(), ns);
+    TCB_CUDA(cudaStreamSynchronize(s));
+    res.entropy_bytes = el;
+    if (!want_body) return res;
+    std::vector<u64> off(ns);
+    u64 tot = 0;
+    for (u64 i = 0; i < ns; ++i) {
+        off[i] = tot;
+        tot += 4 + 4 + el[i] + (soh[i].nraw + 7) / 8;
+    }
+    DevBuf<u64> doff(ns, s);
+    doff.upload(off.data(), ns);
+    DevBuf<u8> body(tot, s);
+    assemble_kernel<<<static_cast<unsigned>(ns), 128, 0, s>>>(ent.p, dad.p, elen.p, raw.p, dsd.p, so.p, doff.p,
+                                                               body.p);
+    count_launch();
+    TCB_LAUNCH();
+    res.body.resize(tot);
+    body.download(res.body.data(), tot);
+    TCB_CUDA(cudaStreamSynchronize(s));
+    return res;
+}
+
+}  // namespace tcb

@@ -1,0 +1,94 @@
+// Shared device/host plumbing for the B200 compress path (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace tcb {
+
+using u8 = std::uint8_t;
+using u32 = std::uint32_t;
+using u64 = std::uint64_t;
+using i64 = std::int64_t;
+
+// Same exception type/messages as the reference's tucomp::Error (tensor.hpp:14-17).
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define TCB_CUDA(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t _e = (expr);                                                                \
+        if (_e != cudaSuccess)                                                                  \
+            throw ::tcb::Error(std::string("cuda: ") + cudaGetErrorString(_e) + " at " + #expr); \
+    } while (0)
+
+#define TCB_LAUNCH() TCB_CUDA(cudaGetLastError())
+
+constexpr u64 kFull = ~u64{0};
+
+// Stream-ordered device buffer (cudaMallocAsync pool; freed on the same stream).
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    std::size_t n = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(std::size_t count, cudaStream_t st) : n(count), s(st) {
+        if (n) TCB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), s));
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p; n = o.n; s = o.s;
+            o.p = nullptr; o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    void zero() {
+        if (n) TCB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+    void upload(const T* h, std::size_t cnt) {
+        if (cnt) TCB_CUDA(cudaMemcpyAsync(p, h, cnt * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void download(T* h, std::size_t cnt) const {
+        if (cnt) TCB_CUDA(cudaMemcpyAsync(h, p, cnt * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+    std::vector<T> to_host() const {
+        std::vector<T> v(n);
+        download(v.data(), n);
+        TCB_CUDA(cudaStreamSynchronize(s));
+        return v;
+    }
+};
+
+inline int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
+    return n;
+}
+
+inline unsigned cdiv(u64 a, u64 b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+// Launch counter for the bench's "gpu_launches" claim.
+u64& launch_counter();
+inline void count_launch(u64 k = 1) { launch_counter() += k; }
+
+}  // namespace tcb

@@ -1,0 +1,38 @@
+// Host driver of the device bit-plane encoder (corecodec::Encoder,
+// core_codec.cpp:105-413): certified plan decisions + device emission.
+#pragma once
+
+#include <optional>
+
+#include "codec.cuh"
+
+namespace tcb {
+
+struct EncodeOpts {
+    int coder = 0;       // entropy::Coder (0 = arithmetic)
+    u64 block = 0;       // 0 = max(4096, ceil(n/64))
+    bool split = true;
+    std::optional<int> fixed_plane;
+};
+
+struct PlanResult {
+    int last_plane = 63;
+    int nplanes = 0;
+    std::vector<u64> stops;  // 2 per block: leading, trailing
+    u64 block = 0;
+    bool certified = true;   // false when the serial-replay fallback decided
+    int fallbacks = 0;
+};
+
+u64 default_block(u64 n);
+
+// plan(): decides last_plane and stops exactly as the reference's serial double
+// arithmetic would; `dec` receives the decoder-side magnitudes.
+PlanResult plan_stream(const u64* m, u64 n, double target_int, const EncodeOpts& o, u64* dec, cudaStream_t s);
+
+// finalize(): emits planes [last_plane, 63] with the given signs and returns
+// the serialized stream section (container.cpp:231-247) for `count` elements.
+std::vector<u8> finalize_stream(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,
+                                cudaStream_t s);
+
+}  // namespace tcb

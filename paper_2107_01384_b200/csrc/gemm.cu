@@ -1,0 +1,312 @@
+// fp64 tensor-core contractions of the ST-HOSVD mode loop (sthosvd.cpp:72-99,158-166).
+//
+//  * gram_f64 : G = B B^T  (SYRK, lower-triangle 64x64 tiles, deterministic split-K)
+//  * ttm_f64  : out = B^T U (the projection fused with the circular mode shift)
+//
+// Both use DMMA (mma.sync.m8n8k4.f64 — tcgen05 has no f64 kind on sm_100a) fed
+// by cp.async double-buffered shared-memory tiles with bank-conflict-free
+// padding.  Split-K partials are reduced in a fixed order, so results are
+// bitwise reproducible run to run.
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace tcb {
+
+namespace {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int sz = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int sz = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ------------------------------------------------------------------ SYRK
+constexpr int GT = 64;        // output tile
+constexpr int GBK = 32;       // k slab
+constexpr int GPAD = GBK + 4; // row stride in smem (doubles): conflict-free fragment reads
+
+// Load rows [r0, r0+64) x k [k0, k0+32) of row-major B into s[64][GPAD]
+template <bool V16>
+__device__ __forceinline__ void load_slab(double (*s)[GPAD], const double* __restrict__ B, u64 rows, u64 cols,
+                                          u64 r0, u64 k0, u64 k1) {
+    if constexpr (V16) {
+        // 64 rows x 16 chunks of 16 B
+        for (int c = threadIdx.x; c < GT * (GBK / 2); c += blockDim.x) {
+            const int rr = c / (GBK / 2), kk = (c % (GBK / 2)) * 2;
+            const u64 gr = r0 + rr, gk = k0 + kk;
+            const bool ok = gr < rows && gk < k1;  // k1 even here: pairs never straddle
+            cp_async16(&s[rr][kk], ok ? B + gr * cols + gk : B, ok);
+        }
+    } else {
+        for (int c = threadIdx.x; c < GT * GBK; c += blockDim.x) {
+            const int rr = c / GBK, kk = c % GBK;
+            const u64 gr = r0 + rr, gk = k0 + kk;
+            const bool ok = gr < rows && gk < k1;
+            cp_async8(&s[rr][kk], ok ? B + gr * cols + gk : B, ok);
+        }
+    }
+}
+
+template <bool V16>
+__global__ void __launch_bounds__(256) syrk_kernel(const double* __restrict__ B, u64 rows, u64 cols, u64 kchunk,
+                                                   int ntiles_lower, double* __restrict__ ws) {
+    extern __shared__ __align__(16) double smem_syrk[];
+    auto As = reinterpret_cast<double (*)[GT][GPAD]>(smem_syrk);
+    auto Bs = reinterpret_cast<double (*)[GT][GPAD]>(smem_syrk + 2 * GT * GPAD);
+    const int tile = blockIdx.x % ntiles_lower;
+    const int split = blockIdx.x / ntiles_lower;
+    // lower tile index -> (ti, tj), ti >= tj
+    int ti = 0;
+    while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
+    const int tj = tile - ti * (ti + 1) / 2;
+    const bool diag = ti == tj;
+    const u64 k0 = static_cast<u64>(split) * kchunk;
+    const u64 k1 = min(cols, k0 + kchunk);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const u64 ra = static_cast<u64>(ti) * GT, rb = static_cast<u64>(tj) * GT;
+    const int nslab = k1 > k0 ? static_cast<int>((k1 - k0 + GBK - 1) / GBK) : 0;
+    if (nslab > 0) {
+        load_slab<V16>(As[0], B, rows, cols, ra, k0, k1);
+        if (!diag) load_slab<V16>(Bs[0], B, rows, cols, rb, k0, k1);
+        cp_commit();
+    }
+    for (int sl = 0; sl < nslab; ++sl) {
+        const int cur = sl & 1;
+        if (sl + 1 < nslab) {
+            const u64 kn = k0 + static_cast<u64>(sl + 1) * GBK;
+            load_slab<V16>(As[cur ^ 1], B, rows, cols, ra, kn, k1);
+            if (!diag) load_slab<V16>(Bs[cur ^ 1], B, rows, cols, rb, kn, k1);
+            cp_commit();
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        double (*As_)[GPAD] = As[cur];
+        double (*Bs_)[GPAD] = diag ? As[cur] : Bs[cur];
+#pragma unroll
+        for (int kk = 0; kk < GBK; kk += 4) {
+            double a[4], b[2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = As_[wm + mi * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) b[ni] = Bs_[wn + ni * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        __syncthreads();
+    }
+    double* out = ws + (static_cast<u64>(split) * ntiles_lower + tile) * GT * GT;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+            const int m = wm + mi * 8 + (lane >> 2);
+            const int n = wn + ni * 8 + 2 * (lane & 3);
+            *reinterpret_cast<double2*>(out + m * GT + n) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+        }
+}
+
+// fixed-order split reduction; writes the full symmetric G (row-major)
+__global__ void syrk_reduce(const double* __restrict__ ws, int splits, int ntiles_lower, u64 rows,
+                            double* __restrict__ G) {
+    const int tile = blockIdx.x;
+    int ti = 0;
+    while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
+    const int tj = tile - ti * (ti + 1) / 2;
+    for (int e = threadIdx.x; e < GT * GT; e += blockDim.x) {
+        const int m = e / GT, n = e % GT;
+        const u64 gi = static_cast<u64>(ti) * GT + m, gj = static_cast<u64>(tj) * GT + n;
+        if (gi >= rows || gj >= rows || gj > gi) continue;
+        double s = 0.0;
+        for (int sp = 0; sp < splits; ++sp) s += ws[(static_cast<u64>(sp) * ntiles_lower + tile) * GT * GT + e];
+        G[gi * rows + gj] = s;
+        G[gj * rows + gi] = s;
+    }
+}
+
+// ------------------------------------------------------------------ TTM
+constexpr int TM = 128, TN = 64, TBK = 16;
+constexpr int APAD = TM + 4, UPAD = TN + 4;
+
+template <bool AV16>
+__global__ void __launch_bounds__(256) ttm_kernel(const double* __restrict__ B, u64 rows, u64 cols,
+                                                  const double* __restrict__ U, u64 r, double* __restrict__ out) {
+    extern __shared__ __align__(16) double smem_ttm[];
+    auto As = reinterpret_cast<double (*)[TBK][APAD]>(smem_ttm);
+    auto Us = reinterpret_cast<double (*)[TBK][UPAD]>(smem_ttm + 2 * TBK * APAD);
+    const u64 m0 = static_cast<u64>(blockIdx.x) * TM;
+    const u64 n0 = static_cast<u64>(blockIdx.y) * TN;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    auto load = [&](int buf, u64 k0) {
+        if constexpr (AV16) {
+            for (int c = threadIdx.x; c < TBK * (TM / 2); c += blockDim.x) {
+                const int kk = c / (TM / 2), mm = (c % (TM / 2)) * 2;
+                const u64 gk = k0 + kk, gm = m0 + mm;
+                const bool ok = gk < rows && gm < cols;  // cols even: pairs never straddle
+                cp_async16(&As[buf][kk][mm], ok ? B + gk * cols + gm : B, ok);
+            }
+        } else {
+            for (int c = threadIdx.x; c < TBK * TM; c += blockDim.x) {
+                const int kk = c / TM, mm = c % TM;
+                const u64 gk = k0 + kk, gm = m0 + mm;
+                const bool ok = gk < rows && gm < cols;
+                cp_async8(&As[buf][kk][mm], ok ? B + gk * cols + gm : B, ok);
+            }
+        }
+        for (int c = threadIdx.x; c < TBK * TN; c += blockDim.x) {
+            const int kk = c / TN, nn = c % TN;
+            const u64 gk = k0 + kk, gn = n0 + nn;
+            const bool ok = gk < rows && gn < r;
+            cp_async8(&Us[buf][kk][nn], ok ? U + gk * r + gn : U, ok);
+        }
+    };
+    const int nslab = static_cast<int>((rows + TBK - 1) / TBK);
+    load(0, 0);
+    cp_commit();
+    for (int sl = 0; sl < nslab; ++sl) {
+        const int cur = sl & 1;
+        if (sl + 1 < nslab) {
+            load(cur ^ 1, static_cast<u64>(sl + 1) * TBK);
+            cp_commit();
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < TBK; kk += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = As[cur][kk + (lane & 3)][wm + mi * 8 + (lane >> 2)];
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) b[ni] = Us[cur][kk + (lane & 3)][wn + ni * 8 + (lane >> 2)];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const u64 m = m0 + wm + mi * 8 + (lane >> 2);
+            const u64 n = n0 + wn + ni * 8 + 2 * (lane & 3);
+            if (m >= cols) continue;
+            if (n < r) out[m * r + n] = acc[mi][ni][0];
+            if (n + 1 < r) out[m * r + n + 1] = acc[mi][ni][1];
+        }
+}
+
+// ------------------------------------------------------------------ small helpers
+__global__ void gram_cols_kernel(const double* __restrict__ B, u64 rows, u64 cols, double* __restrict__ G) {
+    const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= cols * cols) return;
+    const u64 i = idx / cols, j = idx % cols;
+    if (j > i) return;
+    double s = 0.0;
+    for (u64 k = 0; k < rows; ++k) s = fma(B[k * cols + i], B[k * cols + j], s);
+    G[i * cols + j] = s;
+    G[j * cols + i] = s;
+}
+
+__global__ void gemm_nn_kernel(const double* __restrict__ B, u64 rows, u64 cols, const double* __restrict__ V, u64 r,
+                               double* __restrict__ out) {
+    const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= rows * r) return;
+    const u64 i = idx / r, j = idx % r;
+    double s = 0.0;
+    for (u64 k = 0; k < cols; ++k) s = fma(B[i * cols + k], V[k * r + j], s);
+    out[idx] = s;
+}
+
+}  // namespace
+
+void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
+    const int nt = static_cast<int>((rows + GT - 1) / GT);
+    const int lower = nt * (nt + 1) / 2;
+    const u64 want = static_cast<u64>(2 * sm_count());
+    u64 splits = std::max<u64>(1, (want + lower - 1) / lower);
+    splits = std::min<u64>(splits, std::max<u64>(1, cols / 256));
+    u64 kchunk = (cols + splits - 1) / splits;
+    kchunk = (kchunk + GBK - 1) / GBK * GBK;
+    splits = (cols + kchunk - 1) / kchunk;
+    DevBuf<double> ws(splits * lower * GT * GT, s);
+    const unsigned grid = static_cast<unsigned>(splits * lower);
+    const bool v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+    const int smem = 4 * GT * GPAD * sizeof(double);
+    static bool attr = [&] {
+        cudaFuncSetAttribute(syrk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(syrk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        return true;
+    }();
+    (void)attr;
+    if (v16) syrk_kernel<true><<<grid, 256, smem, s>>>(B, rows, cols, kchunk, lower, ws.p);
+    else syrk_kernel<false><<<grid, 256, smem, s>>>(B, rows, cols, kchunk, lower, ws.p);
+    syrk_reduce<<<lower, 256, 0, s>>>(ws.p, static_cast<int>(splits), lower, rows, G);
+    count_launch(2);
+    TCB_LAUNCH();
+}
+
+void gram_cols_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
+    gram_cols_kernel<<<cdiv(cols * cols, 256), 256, 0, s>>>(B, rows, cols, G);
+    count_launch();
+    TCB_LAUNCH();
+}
+
+void ttm_f64(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s) {
+    dim3 grid(cdiv(cols, TM), cdiv(r, TN));
+    const bool v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+    const int smem = 2 * TBK * (APAD + UPAD) * sizeof(double);
+    static bool attr = [&] {
+        cudaFuncSetAttribute(ttm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(ttm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        return true;
+    }();
+    (void)attr;
+    if (v16) ttm_kernel<true><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out);
+    else ttm_kernel<false><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out);
+    count_launch();
+    TCB_LAUNCH();
+}
+
+void gemm_nn_f64(const double* B, u64 rows, u64 cols, const double* V, u64 r, double* out, cudaStream_t s) {
+    gemm_nn_kernel<<<cdiv(rows * r, 256), 256, 0, s>>>(B, rows, cols, V, r, out);
+    count_launch();
+    TCB_LAUNCH();
+}
+
+}  // namespace tcb

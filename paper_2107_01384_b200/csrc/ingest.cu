@@ -1,0 +1,315 @@
+// Ingest: source dtype -> T cast (container.cpp:51-94), finite check
+// (kernels_avx2.cpp:68-95), ||A||^2 (tensor.cpp:152-155), exact max |x|, and
+// the single row-major axis permutation (tensor.cpp:105-144).
+// All HBM-bound: 16-byte vector loads, grid = k x 148 SMs, fixed reduction tree.
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace tcb {
+
+namespace {
+
+template <class S>
+__device__ __forceinline__ double as_d(S v) { return static_cast<double>(v); }
+
+template <class S, class T>
+__global__ void cast_kernel(const S* __restrict__ src, T* __restrict__ dst, u64 n) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        dst[i] = static_cast<T>(src[i]);
+}
+
+// double -> double fast path: 16-byte copies
+__global__ void copy16_kernel(const double2* __restrict__ src, double2* __restrict__ dst, u64 n2) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n2; i += stride) dst[i] = src[i];
+}
+
+template <class T>
+void cast_any(const void* src, int dtype, u64 n, T* dst, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(sm_count() * 8), blk = 256;
+    switch (dtype) {
+        case 0: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const int8_t*>(src), dst, n); break;
+        case 1: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const uint8_t*>(src), dst, n); break;
+        case 2: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const int16_t*>(src), dst, n); break;
+        case 3: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const uint16_t*>(src), dst, n); break;
+        case 4: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const int32_t*>(src), dst, n); break;
+        case 5: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const uint32_t*>(src), dst, n); break;
+        case 6: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const int64_t*>(src), dst, n); break;
+        case 7: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const uint64_t*>(src), dst, n); break;
+        case 8: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const float*>(src), dst, n); break;
+        case 9:
+            if constexpr (std::is_same_v<T, double>) {
+                if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 &&
+                    n % 2 == 0) {
+                    copy16_kernel<<<grid, blk, 0, s>>>(static_cast<const double2*>(src),
+                                                       reinterpret_cast<double2*>(dst), n / 2);
+                    break;
+                }
+            }
+            cast_kernel<<<grid, blk, 0, s>>>(static_cast<const double*>(src), dst, n);
+            break;
+        default: throw Error("container: unknown dtype");
+    }
+    count_launch();
+    TCB_LAUNCH();
+}
+
+constexpr int kRedThreads = 256;
+
+// stage 1: per-CTA partial sums of squares + non-finite flag (fixed tree)
+template <class T>
+__global__ void sumsq_stage1(const T* __restrict__ x, u64 n, double* __restrict__ part, int* __restrict__ bad) {
+    __shared__ double sh[kRedThreads / 32];
+    double acc = 0.0;
+    int nonfinite = 0;
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double v = static_cast<double>(x[i]);
+        nonfinite |= !isfinite(v);
+        acc = fma(v, v, acc);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    if (__syncthreads_or(nonfinite) && threadIdx.x == 0) *bad = 1;
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) t += sh[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void sum_stage2(const double* __restrict__ part, int n, double* __restrict__ out) {
+    __shared__ double sh[kRedThreads];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) t += part[i];
+    sh[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+template <class T>
+double sumsq_impl(const T* x, u64 n, bool* finite, cudaStream_t s) {
+    const int grid = sm_count() * 4;
+    DevBuf<double> part(grid + 1, s);
+    DevBuf<int> bad(1, s);
+    bad.zero();
+    sumsq_stage1<T><<<grid, kRedThreads, 0, s>>>(x, n, part.p, bad.p);
+    sum_stage2<<<1, kRedThreads, 0, s>>>(part.p, grid, part.p + grid);
+    count_launch(2);
+    TCB_LAUNCH();
+    double r = 0;
+    int b = 0;
+    TCB_CUDA(cudaMemcpyAsync(&r, part.p + grid, sizeof(double), cudaMemcpyDeviceToHost, s));
+    TCB_CUDA(cudaMemcpyAsync(&b, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    TCB_CUDA(cudaStreamSynchronize(s));
+    if (finite) *finite = b == 0;
+    return r;
+}
+
+__global__ void maxabs_stage1(const double* __restrict__ x, u64 n, double* __restrict__ part) {
+    __shared__ double sh[kRedThreads / 32];
+    double m = 0.0;
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        m = fmax(m, fabs(x[i]));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) t = fmax(t, sh[w]);
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void max_stage2(const double* __restrict__ part, int n, double* __restrict__ out) {
+    double m = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, part[i]);
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) t = fmax(t, sh[w]);
+        *out = t;
+    }
+}
+
+// gather permutation: output written contiguously (coalesced), input gathered
+template <class T, int D>
+__global__ void permute_kernel(const T* __restrict__ src, T* __restrict__ dst, u64 n,
+                               const u64* __restrict__ meta /* out_shape[D], gather_stride[D] */) {
+    u64 oshape[D], g[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        oshape[i] = meta[i];
+        g[i] = meta[D + i];
+    }
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 o = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; o < n; o += stride) {
+        u64 rem = o, off = 0;
+#pragma unroll
+        for (int i = D - 1; i >= 0; --i) {
+            const u64 idx = rem % oshape[i];
+            rem /= oshape[i];
+            off += idx * g[i];
+        }
+        dst[o] = src[off];
+    }
+}
+
+// 3-D permutations that move the last axis: 32x32 smem tiles over the pair
+// (input-last axis, output-last axis) so both sides stay coalesced.
+template <class T>
+__global__ void permute3_tiled(const T* __restrict__ src, T* __restrict__ dst, u64 s0, u64 s1, u64 s2,
+                               int p0, int p1, int p2) {
+    // output shape (S[p0], S[p1], S[p2]); input row-major (s0, s1, s2)
+    __shared__ T tile[32][33];
+    const u64 S[3] = {s0, s1, s2};
+    const u64 in_st[3] = {s1 * s2, s2, 1};
+    const int P[3] = {p0, p1, p2};
+    // axis roles: a = input-last (2), b = output-last (P[2]); c = the remaining axis
+    const int ax_b = P[2];
+    const int ax_c = 3 - 2 - ax_b;  // since ax_b != 2 here
+    const u64 nb = S[ax_b], na = S[2], nc = S[ax_c];
+    const u64 tiles_a = (na + 31) / 32, tiles_b = (nb + 31) / 32;
+    u64 t = blockIdx.x;
+    const u64 ta = t % tiles_a;
+    t /= tiles_a;
+    const u64 tb = t % tiles_b;
+    const u64 ic = t / tiles_b;
+    if (ic >= nc) return;
+    // output strides
+    u64 out_st[3];
+    out_st[2] = 1;
+    out_st[1] = S[P[2]];
+    out_st[0] = S[P[2]] * S[P[1]];
+    u64 ost_of_axis[3];
+    for (int i = 0; i < 3; ++i) ost_of_axis[P[i]] = out_st[i];
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const u64 ib = tb * 32 + j, ia = ta * 32 + threadIdx.x;
+        if (ib < nb && ia < na) {
+            const u64 off = ib * in_st[ax_b] + ia * in_st[2] + ic * in_st[ax_c];
+            tile[j][threadIdx.x] = src[off];
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const u64 ia = ta * 32 + j, ib = tb * 32 + threadIdx.x;
+        if (ib < nb && ia < na) {
+            const u64 off = ib * ost_of_axis[ax_b] + ia * ost_of_axis[2] + ic * ost_of_axis[ax_c];
+            dst[off] = tile[threadIdx.x][j];
+        }
+    }
+}
+
+__global__ void precision_kernel(const void* __restrict__ src, int is_signed, u64 n, int* __restrict__ flag) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    int bad = 0;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        u64 mag;
+        if (is_signed) {
+            const long long v = static_cast<const long long*>(src)[i];
+            mag = static_cast<u64>(v < 0 ? -(v + 1) : v);
+        } else {
+            mag = static_cast<const u64*>(src)[i];
+        }
+        bad |= mag > (u64{1} << 53);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+}  // namespace
+
+bool ingest_precision_loss(const void* src, int dtype, u64 n, cudaStream_t s) {
+    DevBuf<int> f(1, s);
+    f.zero();
+    precision_kernel<<<sm_count() * 4, 256, 0, s>>>(src, dtype == 6 ? 1 : 0, n, f.p);
+    count_launch();
+    TCB_LAUNCH();
+    return f.to_host()[0] != 0;
+}
+
+void ingest_cast(const void* src, int dtype, u64 n, double* dst, cudaStream_t s) { cast_any(src, dtype, n, dst, s); }
+void ingest_cast_f32(const void* src, int dtype, u64 n, float* dst, cudaStream_t s) { cast_any(src, dtype, n, dst, s); }
+
+double sum_squares(const double* x, u64 n, bool* finite, cudaStream_t s) { return sumsq_impl(x, n, finite, s); }
+double sum_squares(const float* x, u64 n, bool* finite, cudaStream_t s) { return sumsq_impl(x, n, finite, s); }
+
+double max_abs(const double* x, u64 n, cudaStream_t s) {
+    const int grid = sm_count() * 4;
+    DevBuf<double> part(grid + 1, s);
+    maxabs_stage1<<<grid, kRedThreads, 0, s>>>(x, n, part.p);
+    max_stage2<<<1, 1024, 0, s>>>(part.p, grid, part.p + grid);
+    count_launch(2);
+    TCB_LAUNCH();
+    double r = 0;
+    TCB_CUDA(cudaMemcpyAsync(&r, part.p + grid, sizeof(double), cudaMemcpyDeviceToHost, s));
+    TCB_CUDA(cudaStreamSynchronize(s));
+    return r;
+}
+
+template <class T>
+void permute_axes(const T* src, T* dst, const std::vector<u64>& shape, const std::vector<u64>& perm,
+                  cudaStream_t s) {
+    const int d = static_cast<int>(shape.size());
+    u64 n = 1;
+    for (auto v : shape) n *= v;
+    bool identity = true;
+    for (int i = 0; i < d; ++i) identity &= perm[i] == static_cast<u64>(i);
+    if (identity) {
+        TCB_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    if (d == 3 && perm[2] != 2) {
+        const u64 nb = shape[perm[2]], na = shape[2];
+        const u64 nc = shape[3 - 2 - perm[2]];
+        const u64 blocks = ((na + 31) / 32) * ((nb + 31) / 32) * nc;
+        permute3_tiled<T><<<static_cast<unsigned>(blocks), dim3(32, 8), 0, s>>>(
+            src, dst, shape[0], shape[1], shape[2], static_cast<int>(perm[0]), static_cast<int>(perm[1]),
+            static_cast<int>(perm[2]));
+        count_launch();
+        TCB_LAUNCH();
+        return;
+    }
+    std::vector<u64> st(d);
+    u64 acc = 1;
+    for (int i = d - 1; i >= 0; --i) {
+        st[i] = acc;
+        acc *= shape[i];
+    }
+    std::vector<u64> meta(2 * d);
+    for (int i = 0; i < d; ++i) {
+        meta[i] = shape[perm[i]];
+        meta[d + i] = st[perm[i]];
+    }
+    DevBuf<u64> m(2 * d, s);
+    m.upload(meta.data(), meta.size());
+    const unsigned grid = static_cast<unsigned>(sm_count() * 8);
+    switch (d) {
+        case 1: permute_kernel<T, 1><<<grid, 256, 0, s>>>(src, dst, n, m.p); break;
+        case 2: permute_kernel<T, 2><<<grid, 256, 0, s>>>(src, dst, n, m.p); break;
+        case 3: permute_kernel<T, 3><<<grid, 256, 0, s>>>(src, dst, n, m.p); break;
+        case 4: permute_kernel<T, 4><<<grid, 256, 0, s>>>(src, dst, n, m.p); break;
+        case 5: permute_kernel<T, 5><<<grid, 256, 0, s>>>(src, dst, n, m.p); break;
+        case 6: permute_kernel<T, 6><<<grid, 256, 0, s>>>(src, dst, n, m.p); break;
+        case 7: permute_kernel<T, 7><<<grid, 256, 0, s>>>(src, dst, n, m.p); break;
+        case 8: permute_kernel<T, 8><<<grid, 256, 0, s>>>(src, dst, n, m.p); break;
+        default: throw Error("transpose: order above 8 unsupported");
+    }
+    count_launch();
+    TCB_LAUNCH();
+}
+template void permute_axes(const double*, double*, const std::vector<u64>&, const std::vector<u64>&, cudaStream_t);
+template void permute_axes(const float*, float*, const std::vector<u64>&, const std::vector<u64>&, cudaStream_t);
+template void permute_axes(const u64*, u64*, const std::vector<u64>&, const std::vector<u64>&, cudaStream_t);
+template void permute_axes(const u8*, u8*, const std::vector<u64>&, const std::vector<u64>&, cudaStream_t);
+
+}  // namespace tcb

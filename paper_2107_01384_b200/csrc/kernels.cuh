@@ -1,0 +1,56 @@
+// Host-callable launchers for every sm_100a kernel of the compress path.
+#pragma once
+
+#include "common.cuh"
+
+namespace tcb {
+
+// ---- ingest.cu: cast + finite check + ||A||^2 (container.cpp:51-94, kernels_avx2.cpp:68-160)
+// dtype codes follow container::Dtype (container.hpp:16-27).
+void ingest_cast(const void* src, int dtype, u64 n, double* dst, cudaStream_t s);
+void ingest_cast_f32(const void* src, int dtype, u64 n, float* dst, cudaStream_t s);
+// Deterministic fixed-tree sum of squares in double; *finite = all elements finite.
+double sum_squares(const double* x, u64 n, bool* finite, cudaStream_t s);
+double sum_squares(const float* x, u64 n, bool* finite, cudaStream_t s);
+// Row-major axis permutation (tensor.cpp:105-144): out axis i = in axis perm[i].
+template <class T>
+void permute_axes(const T* src, T* dst, const std::vector<u64>& shape, const std::vector<u64>& perm,
+                  cudaStream_t s);
+// int64/uint64 sources whose magnitude exceeds 2^53 (container.cpp:60-63)
+bool ingest_precision_loss(const void* src, int dtype, u64 n, cudaStream_t s);
+// Exact max |x| (kernels_avx2.cpp:40-66 is order-independent, so exact on any tree).
+double max_abs(const double* x, u64 n, cudaStream_t s);
+
+// ---- gram.cu: G = B B^T (B row-major rows x cols), fp64 DMMA, deterministic split-K.
+// G is written full symmetric, row-major rows x rows.
+void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s);
+// G = B^T B (cols x cols) for the rows > cols branch (sthosvd.cpp:91-99 stand-in).
+void gram_cols_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s);
+
+// ---- ttm.cu: out (cols x r, row-major) = B^T U (sthosvd.cpp:158-166), fp64 DMMA.
+void ttm_f64(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s);
+// out (rows x r) = B V  (B rows x cols row-major, V cols x r row-major); small.
+void gemm_nn_f64(const double* B, u64 rows, u64 cols, const double* V, u64 r, double* out, cudaStream_t s);
+
+// ---- eig.cu: symmetric eigensolver for n <= 1024 (SelfAdjointEigenSolver stand-in).
+struct EigWork {
+    DevBuf<double> a;    // n x n working copy (row-major), reflectors below the subdiagonal
+    DevBuf<double> d, e, tau, evals, z;
+    u64 n = 0;
+};
+// Householder tridiagonalisation of the symmetric row-major A (n x n) and
+// all eigenvalues by bisection, returned in DESCENDING order (host copy).
+std::vector<double> eig_values(const double* A, u64 n, EigWork& w, cudaStream_t s);
+// Top-r orthonormal eigenvectors (n x r, row-major) after eig_values.
+void eig_vectors(EigWork& w, u64 r, double* U, cudaStream_t s);
+// Column sign convention (sthosvd.cpp:103-110): largest |u| (first on ties) >= 0.
+void fix_column_signs(double* U, u64 n, u64 r, cudaStream_t s);
+// Normalise columns of U (n x r row-major) by 1/sigma_j and re-orthonormalise (MGS).
+void scale_orthonormalize(double* U, u64 n, u64 r, const double* sigma, cudaStream_t s);
+
+// ---- quant.cu (core_codec.cpp:55-93)
+void quantize_f64(const double* x, u64 n, int k, u64* mag, u8* neg, cudaStream_t s);
+// Per-axis slice sums of (double)m^2 replayed in lexicographic order, then sqrt(s*down).
+void slice_norms(const u64* mag, const std::vector<u64>& shape, double down, double* out, cudaStream_t s);
+
+}  // namespace tcb

@@ -1,0 +1,475 @@
+// Host orchestration of the B200 compress path, mirroring compress_impl
+// (pipeline.cpp:24-195), sthosvd::compress (sthosvd.cpp:114-171) and
+// factorcodec::encode_factor (factor_codec.cpp:153-244).  All tensor work runs
+// in the device kernels; the host keeps the reference's scalar decisions
+// (rank rule, budget roll-forward, plane deepening) in the same double
+// arithmetic (no FMA contraction in this TU).
+#include "pipeline.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "kernels.cuh"
+#include "quant.cuh"
+
+namespace tcb {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t0) { return std::chrono::duration<double, std::milli>(Clock::now() - t0).count(); }
+
+bool valid_perm(const std::vector<u64>& p, std::size_t d) {
+    if (p.size() != d) return false;
+    std::vector<char> seen(d, 0);
+    for (auto v : p) {
+        if (v >= d || seen[v]) return false;
+        seen[v] = 1;
+    }
+    return true;
+}
+
+std::size_t dtype_size(int t) {
+    switch (t) {
+        case 0: case 1: return 1;
+        case 2: case 3: return 2;
+        case 4: case 5: case 8: return 4;
+        case 6: case 7: case 9: return 8;
+    }
+    throw Error("container: unknown dtype");
+}
+
+// sthosvd.cpp:13-26
+std::pair<u64, double> pick_rank(const std::vector<double>& s2, double budget) {
+    if (s2.empty()) throw Error("rank choice: empty singular values");
+    if (budget < 0) throw Error("rank choice: negative budget");
+    u64 r = s2.size();
+    double gone = 0.0;
+    while (r > 0) {
+        const double next = gone + s2[r - 1];
+        if (next > budget) break;
+        gone = next;
+        --r;
+    }
+    return {r, gone};
+}
+
+struct W {
+    std::vector<u8> b;
+    void u8v(u8 v) { b.push_back(v); }
+    void u32v(u32 v) {
+        for (int i = 0; i < 4; ++i) b.push_back(static_cast<u8>(v >> (8 * i)));
+    }
+    void u64v(u64 v) {
+        for (int i = 0; i < 8; ++i) b.push_back(static_cast<u8>(v >> (8 * i)));
+    }
+    void f64v(double v) {
+        u64 x;
+        std::memcpy(&x, &v, 8);
+        u64v(x);
+    }
+    void raw(const std::vector<u8>& x) { b.insert(b.end(), x.begin(), x.end()); }
+};
+
+std::vector<u8> empty_stream_section(u64 count, u64 block) {
+    W w;
+    w.u64v(count);
+    w.u64v(block);
+    w.u8v(63);
+    w.u32v(0);
+    w.u32v(0);
+    return w.b;
+}
+
+__attribute__((unused)) void sync(cudaStream_t s) { TCB_CUDA(cudaStreamSynchronize(s)); }
+
+}  // namespace
+
+std::vector<u64> stable_ascending(const std::vector<u64>& s) {
+    std::vector<u64> p(s.size());
+    std::iota(p.begin(), p.end(), u64{0});
+    std::stable_sort(p.begin(), p.end(), [&](u64 a, u64 b) { return s[a] < s[b]; });
+    return p;
+}
+
+std::vector<double> alpha_weights(const std::vector<double>& sn, u64 n) {
+    const std::size_t r = sn.size();
+    if (n < r) throw Error("weights: factor has more columns than rows");
+    std::vector<double> al(r);
+    double tail = 0.0;
+    for (std::size_t k = 0; k < r; ++k) tail += sn[k] * sn[k];
+    for (std::size_t j = 0; j < r; ++j) {
+        const double sj = sn[j];
+        tail -= sj * sj;
+        const double nj = static_cast<double>(n - j);
+        const double q = std::sqrt(nj);
+        const double own = 1.0 + (nj + 5.0 * q + 2.0) / ((q + 1.0) * (q + 1.0) * q);
+        al[j] = own * sj * sj;
+        if (tail > 0.0) {
+            const double tc = 2.0 / (nj - 1.0) + (nj + 2.0 * q + 2.0) / ((q + 1.0) * (q + 1.0) * (q + 1.0) * q);
+            al[j] += tc * tail;
+        }
+    }
+    return al;
+}
+
+Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double target,
+                      const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s) {
+    if (target < 0) throw Error("sthosvd: negative SSE target");
+    const std::size_t d = shape.size();
+    u64 n_el = 1;
+    for (auto v : shape) n_el *= v;
+    bool finite = true;
+    sum_squares(a.p, n_el, &finite, s);
+    if (!finite) throw Error("sthosvd: input contains non-finite values");
+    std::vector<u64> p = order ? *order : stable_ascending(shape);
+    if (!valid_perm(p, d)) throw Error("sthosvd: invalid processing order");
+    Tucker f;
+    f.order = p;
+    f.n = shape;
+    f.r.assign(d, 0);
+    f.trunc.assign(d, 0.0);
+    f.factors.resize(d);
+    DevBuf<double> x(n_el, s);
+    permute_axes(a.p, x.p, shape, p, s);
+    a.release();
+    std::vector<u64> cur(d);
+    for (std::size_t i = 0; i < d; ++i) cur[i] = shape[p[i]];
+    double remaining = target;
+    for (std::size_t step = 0; step < d; ++step) {
+        u64 tot = 1;
+        for (auto v : cur) tot *= v;
+        const u64 rows = cur[0], cols = tot / rows;
+        const bool via_gram = backend == 1 || (backend == 0 && rows <= cols);
+        EigWork w;
+        std::vector<double> s2;
+        const u64 m = via_gram ? rows : cols;
+        {
+            DevBuf<double> G(m * m, s);
+            if (via_gram) gram_f64(x.p, rows, cols, G.p, s);
+            else gram_cols_f64(x.p, rows, cols, G.p, s);
+            const auto ev = eig_values(G.p, m, w, s);
+            s2.resize(m);
+            for (u64 j = 0; j < m; ++j) s2[j] = std::max(0.0, ev[j]);
+        }
+        const double budget = remaining / static_cast<double>(d - step);
+        auto [r, gone] = pick_rank(s2, budget);
+        if (r == 0) {  // a budget above the whole mode energy still keeps one vector
+            r = 1;
+            gone -= s2[0];
+        }
+        remaining = std::max(0.0, remaining - gone);
+        f.trunc[p[step]] = gone;
+        DevBuf<double> U(rows * r, s);
+        if (via_gram) {
+            eig_vectors(w, r, U.p, s);
+        } else {
+            DevBuf<double> V(cols * r, s);
+            eig_vectors(w, r, V.p, s);
+            gemm_nn_f64(x.p, rows, cols, V.p, r, U.p, s);
+            std::vector<double> sig(r);
+            for (u64 j = 0; j < r; ++j) sig[j] = std::sqrt(s2[j]);
+            DevBuf<double> ds(r, s);
+            ds.upload(sig.data(), r);
+            scale_orthonormalize(U.p, rows, r, ds.p, s);
+            TCB_CUDA(cudaStreamSynchronize(s));
+        }
+        fix_column_signs(U.p, rows, r, s);
+        DevBuf<double> nx(cols * r, s);
+        ttm_f64(x.p, rows, cols, U.p, r, nx.p, s);
+        x = std::move(nx);
+        f.factors[p[step]] = std::move(U);
+        f.r[p[step]] = r;
+        cur.erase(cur.begin());
+        cur.push_back(r);
+    }
+    f.core = std::move(x);
+    f.core_shape = cur;
+    TCB_CUDA(cudaStreamSynchronize(s));
+    return f;
+}
+
+FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<u8>& dead,
+                               const std::vector<double>& sn, int coder, bool simple, int core_step_log2,
+                               double cap, bool f32, cudaStream_t s) {
+    if (dead.size() != r || sn.size() != r) throw Error("factor encode: column metadata mismatch");
+    FactorEnc out;
+    out.dead = dead;
+    out.slice_norms = sn;
+    out.flips.assign(r, 1);
+    std::vector<u64> live;
+    std::vector<double> ln;
+    for (u64 j = 0; j < r; ++j)
+        if (!dead[j]) {
+            live.push_back(j);
+            ln.push_back(sn[j]);
+        }
+    const u64 rl = live.size();
+    if (rl == 0) {
+        out.stream = empty_stream_section(0, 0);
+        return out;
+    }
+    if (rl > n) throw Error("factorize: more columns than rows");
+    if (orth_deviation(U, n, r, live, f32, s) > 1e-8) throw Error("factorize: input columns are not orthonormal");
+    DevBuf<double> V(n * rl, s);
+    std::vector<signed char> fl(rl);
+    householder(U, n, r, live, V.p, fl.data(), s);
+    for (u64 j = 0; j < rl; ++j) out.flips[live[j]] = fl[j];
+    std::vector<double> sc(rl);
+    if (simple) {
+        sc = ln;
+    } else {
+        const auto al = alpha_weights(ln, n);
+        for (u64 j = 0; j < rl; ++j) sc[j] = std::sqrt(2.0 * al[j]);
+    }
+    DevBuf<double> dsc(rl, s);
+    dsc.upload(sc.data(), rl);
+    DevBuf<signed char> dfl(rl, s);
+    dfl.upload(fl.data(), rl);
+    out.count = n * rl - rl * (rl + 1) / 2;
+    const u64 cnt = out.count;
+    DevBuf<double> st(cnt, s);
+    reflector_stream(V.p, n, rl, dsc.p, st.p, s);
+    const double mx = cnt ? max_abs(st.p, cnt, s) : 0.0;
+    out.k = mx > 0.0 ? 63 - std::ilogb(mx) : 0;
+    DevBuf<u64> mag(cnt, s), dec(cnt, s);
+    DevBuf<u8> neg(cnt, s);
+    quantize_f64(st.p, cnt, out.k, mag.p, neg.p, s);
+    int plane = std::clamp(core_step_log2 + out.k, 0, 63);
+    while (true) {
+        EncodeOpts eo;
+        eo.coder = coder;
+        eo.split = false;
+        eo.fixed_plane = plane;
+        const PlanResult pl = plan_stream(mag.p, cnt, 0.0, eo, dec.p, s);
+        const auto res = factor_residuals(dec.p, neg.p, out.k, n, r, live, dsc.p, U, dfl.p, s);
+        out.term = 0.0;
+        for (u64 j = 0; j < rl; ++j) out.term += ln[j] * ln[j] * res[j];
+        if (out.term <= cap || plane == 0) {
+            out.stream = finalize_stream(mag.p, neg.p, cnt, pl, coder, cnt, s);
+            out.plane = plane;
+            return out;
+        }
+        const double excess = out.term / std::max(cap, 1e-300);
+        const int stp = std::max(1, static_cast<int>(std::ceil(0.25 * std::log2(excess))));
+        plane = std::max(0, plane - stp);
+    }
+}
+
+Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,
+                       const Params& prm, cudaStream_t s) {
+    const auto t_all = Clock::now();
+    Result res;
+    const std::size_t d = shape.size();
+    if (d == 0 || d > 8) throw Error("compress: tensor order must be between 1 and 8");
+    u64 n_el = 1;
+    for (auto v : shape) {
+        if (v == 0) throw Error("tensor: zero-sized mode");
+        n_el *= v;
+    }
+    if (nbytes != n_el * dtype_size(dtype))
+        throw Error("ingest: buffer holds " + std::to_string(nbytes) + " bytes, expected " +
+                    std::to_string(n_el * dtype_size(dtype)));
+    res.original_bytes = n_el * dtype_size(dtype);
+    if (prm.target_re && prm.target_sse)
+        throw Error("compress: relative-error and SSE targets are mutually exclusive");
+    if (!prm.target_re && !prm.target_sse) throw Error("compress: no error target given");
+    if (prm.method != 0) throw Error("compress: only lexicographic vectorization is implemented on the device path");
+
+    // ingest (container.cpp:69-94): the internal tensor in double; with
+    // internal_float32 the values are first rounded to float as the reference does
+    DevBuf<double> a(n_el, s);
+    if (prm.f32) {
+        DevBuf<float> af(n_el, s);
+        ingest_cast_f32(device_bytes, dtype, n_el, af.p, s);
+        ingest_cast(af.p, 8, n_el, a.p, s);
+        res.norm_sq = sum_squares(af.p, n_el, nullptr, s);
+    } else {
+        ingest_cast(device_bytes, dtype, n_el, a.p, s);
+        res.norm_sq = sum_squares(a.p, n_el, nullptr, s);
+    }
+    if (dtype == 6 || dtype == 7) res.precision_loss = ingest_precision_loss(device_bytes, dtype, n_el, s);
+    double target;
+    if (prm.target_re) {
+        if (*prm.target_re < 0) throw Error("budget: negative relative-error target");
+        target = *prm.target_re * *prm.target_re * res.norm_sq;
+    } else {
+        target = *prm.target_sse;
+    }
+    if (target < 0) throw Error("budget: negative SSE target");
+    if (prm.rtmss < 0 || prm.rtmss > 1) throw Error("budget: rtmss outside [0, 1]");
+    res.target_sse = target;
+
+    auto t0 = Clock::now();
+    Tucker f = sthosvd_device(std::move(a), shape, prm.rtmss * target, prm.mode_order, prm.backend, s);
+    double trunc = 0;
+    for (double v : f.trunc) trunc += v;
+    double core_target = target - trunc;
+    if (core_target < 0) core_target = 0;
+    res.times.sthosvd = ms_since(t0);
+    res.trunc = trunc;
+    res.ranks = f.r;
+
+    // phase 2: storage order + quantisation
+    t0 = Clock::now();
+    std::vector<u64> storage = prm.storage_order ? *prm.storage_order : stable_ascending(f.core_shape);
+    if (!valid_perm(storage, d)) throw Error("compress: invalid storage order");
+    std::vector<u64> cs(d);
+    for (std::size_t i = 0; i < d; ++i) cs[i] = f.core_shape[storage[i]];
+    u64 nc = 1;
+    for (auto v : cs) nc *= v;
+    DevBuf<double> core_s(nc, s);
+    permute_axes(f.core.p, core_s.p, f.core_shape, storage, s);
+    f.core.release();
+    if (prm.f32) {  // the float core of the reference
+        DevBuf<float> cf(nc, s);
+        ingest_cast_f32(core_s.p, 9, nc, cf.p, s);
+        ingest_cast(cf.p, 8, nc, core_s.p, s);
+    }
+    bool core_finite = true;
+    sum_squares(core_s.p, nc, &core_finite, s);
+    if (!core_finite) throw Error("quantize: non-finite core values");
+    const double mx = max_abs(core_s.p, nc, s);
+    const bool zero = mx == 0.0;
+    const int k = zero ? 0 : 63 - std::ilogb(mx);
+    res.core_k = k;
+    DevBuf<u64> mag(nc, s);
+    DevBuf<u8> neg(nc, s);
+    std::vector<double> sn_flat;
+    u64 sum_ext = 0;
+    for (auto v : cs) sum_ext += v;
+    if (!zero) {
+        quantize_f64(core_s.p, nc, k, mag.p, neg.p, s);
+        DevBuf<double> dsn(sum_ext, s);
+        slice_norms(mag.p, cs, std::ldexp(1.0, -2 * k), dsn.p, s);
+        sn_flat = dsn.to_host();
+    }
+    core_s.release();
+    res.times.quantize = ms_since(t0);
+    const u64 block = prm.block ? prm.block : default_block(zero ? 0 : nc);
+
+    // header (container.hpp:59-82)
+    W w;
+    for (char c : {'T', 'K', 'C', '1'}) w.u8v(static_cast<u8>(c));
+    w.u8v(1);
+    w.u8v(static_cast<u8>(dtype));
+    w.u8v(prm.f32 ? 1 : 0);
+    w.u8v(static_cast<u8>(d));
+    w.u8v(static_cast<u8>(prm.coder));
+    w.u8v(static_cast<u8>(prm.method));
+    w.u8v(static_cast<u8>((zero ? 1 : 0) | (prm.split ? 2 : 0) | (prm.simple ? 4 : 0)));
+    w.u8v(0);
+    for (auto v : shape) w.u64v(v);
+    for (auto v : f.r) w.u64v(v);
+    for (auto v : f.order) w.u8v(static_cast<u8>(v));
+    for (auto v : storage) w.u8v(static_cast<u8>(v));
+    w.u32v(static_cast<u32>(k));
+    w.u64v(block);
+    w.f64v(prm.rtmss);
+    w.f64v(target);
+    w.f64v(res.norm_sq);
+    w.f64v(trunc);
+
+    if (zero) {
+        res.estimate = trunc;
+        w.f64v(0.0);
+        w.f64v(trunc);
+        res.container = std::move(w.b);
+        res.times.total = ms_since(t_all);
+        return res;
+    }
+
+    std::vector<u64> mode_of(d);
+    for (std::size_t ax = 0; ax < d; ++ax) mode_of[ax] = f.order[storage[ax]];
+    std::vector<std::vector<double>> sn_mode(d);
+    {
+        u64 o = 0;
+        for (std::size_t ax = 0; ax < d; ++ax) {
+            sn_mode[mode_of[ax]].assign(sn_flat.begin() + o, sn_flat.begin() + o + cs[ax]);
+            o += cs[ax];
+        }
+    }
+
+    // phase 3: plan the core bit placement
+    t0 = Clock::now();
+    EncodeOpts eo;
+    eo.coder = prm.coder;
+    eo.block = block;
+    eo.split = prm.split;
+    DevBuf<u64> dec(nc, s);
+    const PlanResult plan = plan_stream(mag.p, nc, std::ldexp(core_target, 2 * k), eo, dec.p, s);
+    res.core_last_plane = plan.last_plane;
+    res.uncertified += plan.fallbacks;
+    res.times.core = ms_since(t0);
+    const auto dead_flat = dead_slices(dec.p, cs, s);
+    std::vector<std::vector<u8>> dead_mode(d);
+    {
+        u64 o = 0;
+        for (std::size_t ax = 0; ax < d; ++ax) {
+            dead_mode[mode_of[ax]].assign(dead_flat.begin() + o, dead_flat.begin() + o + cs[ax]);
+            o += cs[ax];
+        }
+    }
+
+    // phase 4: factors
+    t0 = Clock::now();
+    const int core_step = plan.last_plane - k;
+    const double cap = 0.02 * target / static_cast<double>(d);
+    std::vector<FactorEnc> fe(d);
+    res.factor_terms.assign(d, 0.0);
+    for (std::size_t i = 0; i < d; ++i) {
+        fe[i] = encode_factor_device(f.factors[i].p, f.n[i], f.r[i], dead_mode[i], sn_mode[i], prm.coder, prm.simple,
+                                     core_step, cap, prm.f32, s);
+        res.factor_terms[i] = fe[i].term;
+    }
+    res.times.factor = ms_since(t0);
+
+    // sign fold + finalize (pipeline.cpp:161-176)
+    t0 = Clock::now();
+    std::vector<signed char> flips_axis;
+    for (std::size_t ax = 0; ax < d; ++ax)
+        flips_axis.insert(flips_axis.end(), fe[mode_of[ax]].flips.begin(), fe[mode_of[ax]].flips.end());
+    sign_fold(neg.p, cs, flips_axis, s);
+    u64 count = 1;
+    for (auto v : f.r) count *= v;
+    const auto core_stream = finalize_stream(mag.p, neg.p, nc, plan, prm.coder, count, s);
+    const SumRec ach = device_sum(SumKind::diff_backward, mag.p, dec.p, nc, 0, s);
+    res.times.core += ms_since(t0);
+    res.core_quant = std::ldexp(ach.hi + ach.lo, -2 * k);
+    double est = trunc + res.core_quant;
+    for (double v : res.factor_terms) est += v;
+    res.estimate = est;
+    w.f64v(res.core_quant);
+    w.f64v(est);
+
+    t0 = Clock::now();
+    for (std::size_t i = 0; i < d; ++i) {
+        W fw;
+        const auto& fi = fe[i];
+        const std::size_t r = fi.slice_norms.size();
+        for (std::size_t j = 0; j < r; j += 8) {
+            u8 bits = 0;
+            for (std::size_t q = 0; q < 8 && j + q < r; ++q)
+                if (fi.dead[j + q]) bits |= static_cast<u8>(1u << q);
+            fw.u8v(bits);
+        }
+        for (double v : fi.slice_norms) fw.f64v(v);
+        fw.u32v(static_cast<u32>(fi.k));
+        fw.u64v(fi.count);
+        fw.raw(fi.stream);
+        w.u64v(fw.b.size());
+        w.raw(fw.b);
+    }
+    w.u64v(core_stream.size());
+    w.raw(core_stream);
+    res.container = std::move(w.b);
+    res.times.serialize = ms_since(t0);
+    res.times.total = ms_since(t_all);
+    res.peak_alloc = 2 * n_el * 8 + nc * 9 + res.container.size() * 2;
+    return res;
+}
+
+}  // namespace tcb

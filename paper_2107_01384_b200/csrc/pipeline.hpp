@@ -1,0 +1,73 @@
+// Host orchestration of the device compress path (pipeline.cpp:24-195).
+#pragma once
+
+#include <array>
+#include <optional>
+
+#include "common.cuh"
+#include "encoder.hpp"
+
+namespace tcb {
+
+struct Params {
+    std::optional<double> target_re, target_sse;
+    double rtmss = 0.5;
+    int threads = 1;
+    int method = 0;
+    std::optional<std::vector<u64>> storage_order, mode_order;
+    int coder = 0;
+    bool split = true;
+    bool simple = false;
+    u64 block = 0;
+    bool f32 = false;
+    int backend = 0;
+};
+
+struct Times {
+    double sthosvd = 0, quantize = 0, core = 0, factor = 0, serialize = 0, total = 0;
+};
+
+struct Result {
+    std::vector<u8> container;
+    double trunc = 0, core_quant = 0, estimate = 0, norm_sq = 0, target_sse = 0;
+    std::vector<double> factor_terms;
+    std::vector<u64> ranks;
+    Times times;
+    u64 peak_alloc = 0, original_bytes = 0;
+    bool precision_loss = false;
+    int core_last_plane = 63, core_k = 0, uncertified = 0;
+};
+
+// device_bytes: element bytes (skip already applied) resident on the device
+Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,
+                       const Params& p, cudaStream_t s);
+
+struct Tucker {
+    DevBuf<double> core;
+    std::vector<u64> core_shape;
+    std::vector<DevBuf<double>> factors;  // n_i x r_i row-major, by original mode
+    std::vector<u64> n, r, order;
+    std::vector<double> trunc;
+};
+// sthosvd::compress (sthosvd.cpp:114-171) on a device tensor (consumed)
+Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double target,
+                      const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s);
+
+struct FactorEnc {
+    std::vector<u8> dead;
+    std::vector<double> slice_norms;
+    int k = 0;
+    u64 count = 0;
+    std::vector<u8> stream;  // serialized section
+    std::vector<signed char> flips;
+    double term = 0;
+    int plane = 0;
+};
+FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<u8>& dead,
+                               const std::vector<double>& sn, int coder, bool simple, int core_step_log2,
+                               double cap, bool f32, cudaStream_t s);
+
+std::vector<double> alpha_weights(const std::vector<double>& sn, u64 n);
+std::vector<u64> stable_ascending(const std::vector<u64>& s);
+
+}  // namespace tcb

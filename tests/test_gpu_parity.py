@@ -1,0 +1,264 @@
+"""GPU parity tests: every device kernel of the compress path against the CPU
+oracle (bit-exact for integer/bitstream work, stated tolerances for FP)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def principal_sine(u, v):
+    """largest principal-angle sine between span(u) and span(v) (orthonormal columns)."""
+    s = np.linalg.svd(u.T @ v, compute_uv=False)
+    return float(np.sqrt(max(0.0, 1.0 - min(1.0, s.min()) ** 2)))
+
+
+# ---------------------------------------------------------------- dense kernels
+@pytest.mark.parametrize("rows,cols", [(64, 4096), (100, 2500), (256, 65536), (37, 1001), (5, 7)])
+def test_gram_matches_fp64_reference(gpu_pkg, rows, cols):
+    b = np.random.default_rng(rows + cols).standard_normal((rows, cols))
+    g = gpu_pkg.gram(b)
+    ref = b @ b.T
+    # tolerance: fp64 accumulation over `cols` terms
+    assert np.abs(g - ref).max() <= 1e-13 * cols * np.abs(ref).max() ** 0 * np.abs(b).max() ** 2 * 10
+    assert np.array_equal(g, g.T)
+
+
+@pytest.mark.parametrize("rows,cols,r", [(64, 4096, 20), (256, 65536, 64), (100, 2500, 100), (7, 33, 3),
+                                         (256, 1001, 255)])
+def test_ttm_matches_fp64_reference(gpu_pkg, rows, cols, r):
+    rng = np.random.default_rng(rows * 7 + r)
+    b = rng.standard_normal((rows, cols))
+    u = rng.standard_normal((rows, r))
+    out = gpu_pkg.ttm(b, u)
+    ref = b.T @ u
+    assert np.abs(out - ref).max() <= 1e-12 * rows * np.abs(ref).max()
+
+
+def test_gram_is_deterministic(gpu_pkg):
+    b = np.random.default_rng(0).standard_normal((256, 8192))
+    assert np.array_equal(gpu_pkg.gram(b), gpu_pkg.gram(b))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 64, 100, 256, 500])
+def test_eigensolver_matches_lapack(gpu_pkg, n):
+    rng = np.random.default_rng(n)
+    b = rng.standard_normal((n, 3 * n + 5))
+    # graded spectrum like a Tucker unfolding Gram
+    b *= (np.arange(1, n + 1) ** -1.5)[:, None]
+    g = b @ b.T
+    w_ref, v_ref = np.linalg.eigh(g)
+    w_ref, v_ref = w_ref[::-1], v_ref[:, ::-1]
+    r = max(1, n // 3)
+    ev, u = gpu_pkg.eig(g, r)
+    assert np.abs(ev - w_ref).max() <= 1e-12 * abs(w_ref).max() * max(1, n) ** 0.5
+    assert np.abs(u.T @ u - np.eye(r)).max() <= 1e-12
+    assert principal_sine(u, v_ref[:, :r]) <= 1e-6
+    # sign convention: the largest-magnitude entry of every column is non-negative
+    for j in range(r):
+        assert u[np.argmax(np.abs(u[:, j])), j] >= 0
+
+
+def test_eigensolver_clusters_stay_orthonormal(gpu_pkg):
+    n = 128
+    q, _ = np.linalg.qr(np.random.default_rng(1).standard_normal((n, n)))
+    w = np.concatenate([np.linspace(10, 5, 8), 1e-6 * (1 + 1e-9 * np.arange(n - 8))])
+    g = (q * w) @ q.T
+    g = 0.5 * (g + g.T)
+    ev, u = gpu_pkg.eig(g, n)
+    assert np.abs(u.T @ u - np.eye(n)).max() <= 1e-10
+    assert principal_sine(u[:, :8], q[:, :8]) <= 1e-8
+
+
+# ---------------------------------------------------------------- quantisation
+@pytest.mark.parametrize("shape", [(8, 9, 10), (59, 58, 57), (3, 1, 4), (1, 1, 1)])
+def test_quantize_bit_exact(gpu_pkg, shape):
+    core = synth.small("random", shape, seed=sum(shape)) * np.logspace(0, -8, int(np.prod(shape))).reshape(shape)
+    a = gpu_pkg.quantize(core)
+    b = oracle.quantize(core)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2] and a[3] == b[3]
+    for x, y in zip(a[4], b[4]):
+        assert np.array_equal(x, y)  # serial-order slice norms: bitwise
+
+
+def test_quantize_zero_core(gpu_pkg):
+    mag, neg, k, zero, sn = gpu_pkg.quantize(np.zeros((4, 3, 2)))
+    assert zero and k == 0
+
+
+def test_quantize_spec_example(gpu_pkg):
+    mag, neg, k, zero, _ = gpu_pkg.quantize(np.array([[[0.5, -0.25]]]))
+    assert k == 64 and mag.tolist() == [2 ** 63, 2 ** 62] and neg.tolist() == [0, 1]
+
+
+# ---------------------------------------------------------------- encoder
+def _core_mags(shape=(40, 41, 42), seed=0, decay=6.0):
+    rng = np.random.default_rng(seed)
+    idx = np.indices(shape).sum(0).astype(np.float64)
+    core = rng.standard_normal(shape) * np.exp(-decay * idx / idx.max())
+    mag, neg, k, zero, sn = oracle.quantize(core)
+    return mag, neg
+
+
+@pytest.mark.parametrize("frac", [1e-1, 1e-3, 1e-6, 1e-9, 1e-12, 0.0, 2.0])
+@pytest.mark.parametrize("split", [True, False])
+def test_encoder_bitstream_bit_exact(gpu_pkg, frac, split):
+    mag, neg = _core_mags()
+    tot = float((mag.astype(np.float64) ** 2).sum())
+    tgt = tot * frac
+    s_gpu, lp_gpu, ach_gpu, dec_gpu, _ = gpu_pkg.encode(mag, neg, tgt, split=split)
+    s_ref, lp_ref, ach_ref, dec_ref = oracle.encode(mag, neg, tgt, split=split)
+    assert lp_gpu == lp_ref
+    assert np.array_equal(dec_gpu, dec_ref)
+    assert s_gpu == s_ref
+    assert ach_gpu == pytest.approx(ach_ref, rel=1e-12, abs=0)
+
+
+@pytest.mark.parametrize("fixed", [63, 50, 40, 10, 0])
+def test_encoder_fixed_plane_bit_exact(gpu_pkg, fixed):
+    mag, neg = _core_mags((17, 19, 23), seed=5)
+    a = gpu_pkg.encode(mag, neg, 0.0, split=False, fixed_plane=fixed)
+    b = oracle.encode(mag, neg, 0.0, split=False, fixed_plane=fixed)
+    assert a[0] == b[0] and a[1] == b[1] and np.array_equal(a[3], b[3])
+
+
+@pytest.mark.parametrize("block", [4096, 5000, 100000])
+def test_encoder_block_sizes(gpu_pkg, block):
+    mag, neg = _core_mags((50, 60, 70), seed=9)
+    tot = float((mag.astype(np.float64) ** 2).sum())
+    a = gpu_pkg.encode(mag, neg, tot * 1e-7, block_size=block)
+    b = oracle.encode(mag, neg, tot * 1e-7, block_size=block)
+    assert a[0] == b[0] and a[1] == b[1]
+
+
+def test_encoder_edge_cases(gpu_pkg):
+    for mag in [np.zeros(0, np.uint64), np.zeros(10, np.uint64), np.array([1], np.uint64),
+                np.array([2 ** 63, 0, 1, 2 ** 64 - 1], np.uint64)]:
+        neg = (np.arange(mag.size) % 2).astype(np.uint8)
+        for tgt in [0.0, 1.0, 1e300]:
+            a = gpu_pkg.encode(mag, neg, tgt)
+            b = oracle.encode(mag, neg, tgt)
+            assert a[0] == b[0] and a[1] == b[1], (mag, tgt)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_encode_symbols_bit_exact(gpu_pkg, seed):
+    rng = np.random.default_rng(seed)
+    syms = np.concatenate([rng.geometric(0.05, 3000) - 1, rng.integers(0, 2 ** 32 - 1, 50)]).astype(np.uint64)
+    rng.shuffle(syms)
+    assert gpu_pkg.encode_symbols(0, syms) == oracle.encode_symbols(0, syms)
+    assert gpu_pkg.encode_symbols(0, []) == oracle.encode_symbols(0, [])
+
+
+# ---------------------------------------------------------------- factor codec
+@pytest.mark.parametrize("n,r", [(40, 10), (64, 59), (30, 30), (1, 1), (100, 3)])
+def test_factor_stream_matches_oracle(gpu_pkg, n, r):
+    rng = np.random.default_rng(n * 100 + r)
+    q, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    sn = np.sort(rng.uniform(0.1, 10, r))[::-1]
+    dead = np.zeros(r, np.uint8)
+    if r > 3:
+        dead[-1] = 1
+    a = gpu_pkg.encode_factor(q, dead, sn, core_step_log2=-30, term_cap=1e-9)
+    b = oracle.encode_factor(q, dead, sn, core_step_log2=-30, term_cap=1e-9)
+    assert a["k"] == b["k"] and a["count"] == b["count"] and np.array_equal(a["flips"], b["flips"])
+    assert a["plane"] == b["plane"]
+    assert a["term"] == pytest.approx(b["term"], rel=1e-6, abs=1e-300)
+    assert a["stream"] == b["stream"]
+
+
+def test_factor_rejects_non_orthonormal(gpu_pkg):
+    u = np.ones((5, 2))
+    with pytest.raises(gpu_pkg.TucompError, match="not orthonormal"):
+        gpu_pkg.encode_factor(u, np.zeros(2, np.uint8), np.ones(2))
+
+
+# ---------------------------------------------------------------- ST-HOSVD
+@pytest.mark.parametrize("kind,shape,frac", [("sin", (32, 32, 32), 1e-6), ("sin_decay", (48, 40, 36), 1e-8),
+                                             ("blobs", (20, 50, 50), 1e-4), ("sin", (64, 24, 8), 1e-3),
+                                             ("random", (6, 7, 200), 1e-2)])
+def test_sthosvd_ranks_and_subspaces(gpu_pkg, kind, shape, frac):
+    x = synth.small(kind, shape, seed=1)
+    tgt = frac * float((x.astype(np.float64) ** 2).sum())
+    a = gpu_pkg.sthosvd(x, tgt)
+    b = oracle.sthosvd(x, tgt)
+    assert a["ranks"] == b["ranks"] and a["order"] == b["order"]
+    for fa, fb in zip(a["factors"], b["factors"]):
+        assert principal_sine(fa, fb) <= 1e-6
+        assert np.abs(fa.T @ fa - np.eye(fa.shape[1])).max() <= 1e-10
+    assert np.allclose(a["trunc"], b["trunc"], rtol=1e-6, atol=1e-9 * tgt)
+
+
+# ---------------------------------------------------------------- end to end
+@pytest.mark.parametrize("kind,shape,dtype,re", [
+    ("sin", (64, 64, 64), np.float32, 1e-3),       # c1 (BASELINE configs[0])
+    ("sin_decay", (64, 64, 64), np.float64, 1e-4),  # c2 family, reduced
+    ("blobs", (25, 60, 60), np.float32, 1e-3),      # c3 family, reduced
+    ("sin", (40, 30, 20), np.float64, 1e-2),
+])
+def test_compress_end_to_end(gpu_pkg, kind, shape, dtype, re):
+    x = synth.small(kind, shape, seed=7, dtype=dtype)
+    res = gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(target_re=re))
+    ref = oracle.compress(x, target_re=re)
+    assert res.ranks == ref.ranks
+    assert abs(len(res.container) - len(ref.container)) <= 0.01 * len(ref.container)
+    xd = x.astype(np.float64)
+    y = oracle.decompress(res.container, x.shape)
+    yr = oracle.decompress(ref.container, x.shape)
+    e = np.sqrt(((y - xd) ** 2).sum() / (xd ** 2).sum())
+    er = np.sqrt(((yr - xd) ** 2).sum() / (xd ** 2).sum())
+    assert abs(e - er) <= 0.01 * er
+    assert res.norm_sq == pytest.approx(ref.norm_sq, rel=1e-12)
+    assert res.estimate.truncation_sse == pytest.approx(ref.truncation_sse, rel=1e-6)
+
+
+def test_container_parses_with_verbatim_reference_reader(gpu_pkg):
+    """The GPU container round-trips byte-for-byte through the reference's own
+    read_container/write_container (oracle/_ref, compiled verbatim)."""
+    import oracle.ref as R
+
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    x = synth.small("sin", (48, 40, 36), seed=2)
+    res = gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(target_re=1e-3))
+    assert R.container_rewrite(res.container) == res.container
+    mag, neg = R.container_core(res.container)
+    assert mag.size == int(np.prod(res.ranks))
+
+
+def test_compress_uint16_permuted_modes(gpu_pkg):
+    x = synth.spectral_cube((48, 40, 24), n_materials=4, seed=1)  # c4 family: p != identity
+    res = gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(target_re=1e-3))
+    ref = oracle.compress(x, target_re=1e-3)
+    assert res.ranks == ref.ranks
+    assert abs(len(res.container) - len(ref.container)) <= 0.01 * len(ref.container)
+
+
+def test_compress_errors_match_reference(gpu_pkg):
+    x = np.ones((4, 4, 4))
+    x[1, 1, 1] = np.nan
+    with pytest.raises(gpu_pkg.TucompError, match="sthosvd: input contains non-finite values"):
+        gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(target_re=1e-2))
+    y = np.ones((4, 4, 4))
+    with pytest.raises(gpu_pkg.TucompError, match="mutually exclusive"):
+        gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(y), gpu_pkg.Params(target_re=1e-2, target_sse=1.0))
+    with pytest.raises(gpu_pkg.TucompError, match="no error target"):
+        gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(y), gpu_pkg.Params())
+    with pytest.raises(gpu_pkg.TucompError, match="rtmss"):
+        gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(y), gpu_pkg.Params(target_re=1e-2, rtmss=2))
+    src = gpu_pkg.SourceBuffer(b"\0" * 10, gpu_pkg.Dtype.float64, [4, 4, 4])
+    with pytest.raises(gpu_pkg.TucompError, match="ingest: buffer holds 10 bytes, expected 512"):
+        gpu_pkg.compress(src, gpu_pkg.Params(target_re=1e-2))
+
+
+def test_compress_zero_tensor(gpu_pkg):
+    x = np.zeros((8, 8, 8))
+    res = gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(target_re=1e-2))
+    ref = oracle.compress(x, target_re=1e-2)
+    assert res.container == ref.container
