@@ -1,0 +1,301 @@
+#!/usr/bin/env python
+"""Compress-throughput benchmark (BASELINE.json metric) for the B200 path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (configs[1] of BASELINE.json): c2 = 256^3 fp64 tensor, 64 separable
+sinusoid terms with k^-1.5 amplitudes + N(0,1e-5) noise (seeded synthetic —
+the paper's datasets are not available), requested relative error 1e-4.
+A step = one pipeline::compress of that tensor (device-resident input ->
+container bytes on the host).  Inputs are 128 MiB (> L2 is 126 MB) and L2 is
+additionally flushed (256 MiB write) before every timed step, outside the
+per-step CUDA-event window.  N > 1: one independent replica per rank (weak
+scaling; the sharded Gram all-reduce path is not built yet), max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = "c2: 256^3 fp64, 64 separable k^-1.5 sinusoid terms + N(0,1e-5), RE 1e-4"
+METRIC = "compress throughput GB/s (input bytes)"
+STAGES = ["ingest", "permute", "gram", "eig", "ttm", "quant", "stats", "emit", "ac", "factor", "sum"]
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([v.strip() for v in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def algorithmic_work(shape, ranks, order):
+    """Gram flops (SYRK lower-triangle count), TTM flops, per SURVEY.md 8(d)."""
+    cur = [shape[p] for p in order]
+    gram = ttm = 0.0
+    for step, mode in enumerate(order):
+        rows = cur[0]
+        cols = int(np.prod(cur)) // rows
+        r = ranks[mode]
+        if rows <= cols:
+            gram += rows * (rows + 1) * cols
+        else:
+            gram += cols * (cols + 1) * rows + 2.0 * rows * cols * r
+        ttm += 2.0 * rows * cols * r
+        cur = cur[1:] + [r]
+    return gram, ttm
+
+
+def cpu_reference_step(x, re):
+    import oracle
+
+    t0 = time.perf_counter()
+    info = oracle.compress(x, target_re=re)
+    return time.perf_counter() - t0, info
+
+
+def run_reference(args):
+    rank, _, world = _env_rank()
+    if rank != 0:
+        return
+    import synth
+
+    x = synth.make("c2", seed=0)
+    nbytes = x.nbytes
+    for _ in range(args.warmup_ref):
+        cpu_reference_step(x, args.re)
+    times = []
+    for _ in range(args.steps):
+        dt, info = cpu_reference_step(x, args.re)
+        times.append(dt)
+    tot = sum(times)
+    value = nbytes * len(times) / tot / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup_ref, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "input_bytes": nbytes, "ranks": info.ranks},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "port",
+                         "sample": "full c2 compress per step on one host core (oracle/ restatement; the "
+                                   "reference's Eigen GEMMs are single-threaded too)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--re", type=float, default=1e-4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup_ref = min(args.warmup, 1)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+
+    import paper_2107_01384_b200 as tcb
+    import synth
+
+    rank, local, world = _env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    x = synth.make("c2", seed=rank)
+    nbytes = x.nbytes
+    host = torch.from_numpy(x.view(np.uint8).reshape(-1)).pin_memory()
+    d_in = host.to(dev, non_blocking=False)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    params = tcb.Params(target_re=args.re)
+    L = tcb.lib()
+
+    def step_device():
+        return tcb.compress_device(d_in.data_ptr(), nbytes, tcb.Dtype.float64, x.shape, params)
+
+    for _ in range(args.warmup):
+        res = step_device()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = tcb.kernel_launches()
+    barrier()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        res = step_device()
+        b.record()
+        b.synchronize()
+        step_ms.append(a.elapsed_time(b))
+    barrier()
+    launches = (tcb.kernel_launches() - launches0) // max(1, args.steps)
+    # ---- end to end: pinned host bytes in, container bytes out
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        r2 = tcb.compress(tcb.SourceBuffer(memoryview(host.numpy()), tcb.Dtype.float64, x.shape), params)
+        b.record()
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    barrier()
+    clk = clocks.stop()
+
+    tot = float(sum(step_ms))
+    tot_e2e = float(sum(e2e_ms))
+    if world > 1:
+        t = torch.tensor([tot, tot_e2e], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot, tot_e2e = float(t[0]), float(t[1])
+    value = world * nbytes * args.steps / (tot * 1e-3) / 1e9
+    e2e = world * nbytes * args.steps / (tot_e2e * 1e-3) / 1e9
+
+    # ---- per-stage breakdown (one extra profiled step) and roofline of the dominant kernel
+    L.tcb_prof_enable(1)
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    res_p = step_device()
+    L.tcb_prof_enable(0)
+    import ctypes as C
+
+    ms = (C.c_double * len(STAGES))()
+    cnt = (C.c_uint64 * len(STAGES))()
+    L.tcb_prof_read(ms, cnt, len(STAGES))
+    stage_ms = {s: round(ms[i], 4) for i, s in enumerate(STAGES)}
+    L.tcb_peak_dmma_tflops.restype = C.c_double
+    dmma_peak = float(L.tcb_peak_dmma_tflops())
+    peaks, peak_src = _peaks()
+    order = sorted(range(3), key=lambda i: (x.shape[i], i))
+    gram_flop, ttm_flop = algorithmic_work(list(x.shape), res.ranks, order)
+    dom = max(stage_ms, key=stage_ms.get)
+    if dom in ("gram", "ttm"):
+        work = gram_flop if dom == "gram" else ttm_flop
+        achieved = work / (stage_ms[dom] * 1e-3) / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
+                "frac": achieved / dmma_peak, "traffic": None,
+                "peak_source": "measured fp64 DMMA probe (tcb_peak_dmma_tflops); MEASURED_PEAKS.json has no fp64"}
+    else:
+        nc = int(np.prod(res.ranks))
+        alg_bytes = {"ingest": 2.0 * nbytes, "permute": 2.0 * nbytes, "quant": 8.0 * 3 * nc, "stats": 8.0 * nc,
+                     "emit": 8.0 * nc + len(res.container), "ac": 2.0 * len(res.container),
+                     "sum": 8.0 * nc, "eig": 8.0 * 256 * 256, "factor": 8.0 * 256 * 64}.get(dom, 8.0 * nc)
+        achieved = alg_bytes / (stage_ms[dom] * 1e-3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src}
+    roof["gram"] = {"flop": gram_flop, "ms": stage_ms["gram"],
+                    "tflops": gram_flop / max(stage_ms["gram"], 1e-9) / 1e9, "peak_tflops": dmma_peak}
+    roof["ttm"] = {"flop": ttm_flop, "ms": stage_ms["ttm"],
+                   "tflops": ttm_flop / max(stage_ms["ttm"], 1e-9) / 1e9, "peak_tflops": dmma_peak}
+
+    # ---- CPU baseline (rank 0, N=1 only): the oracle on a bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ts = []
+        t_start = time.perf_counter()
+        while time.perf_counter() - t_start < 10.0 or not ts:
+            dt, _ = cpu_reference_step(x, args.re)
+            ts.append(dt)
+        cpu = {"value": nbytes * len(ts) / sum(ts) / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
+               "sample": f"{len(ts)} full c2 compress(es) on one host core via oracle/ (restated reference; "
+                         f"the reference's Eigen GEMMs are single-threaded)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "input_bytes": nbytes, "ranks": res.ranks,
+                       "container_bytes": len(res.container), "compression_factor": res.compression_factor(),
+                       "core_last_plane": res.core_last_plane, "l2": "256 MiB flush before every timed step; "
+                       "input 128 MiB > L2", "parallelism": f"{world} independent replica(s)"},
+            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": nbytes,
+                    "d2h_bytes_per_step": len(r2.container)},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "stage_ms": stage_ms,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "uncertified_decisions": res.uncertified_decisions,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

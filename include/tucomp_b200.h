@@ -84,6 +84,16 @@ void tcb_free(void* p);
 const char* tcb_last_error(void);
 uint64_t tcb_kernel_launches(void);
 
+/* Per-stage device timing with CUDA events on the launching stream (no
+ * reference counterpart; replaces PhaseTimes' wall clocks for roofline work).
+ * Stage order: ingest, permute, gram, eig, ttm, quant, stats, emit, ac,
+ * factor, sum.  tcb_prof_read synchronizes, returns and clears the totals. */
+void tcb_prof_enable(int on);
+int tcb_prof_read(double* ms, uint64_t* counts, int nstages);
+/* Measured fp64 DMMA throughput of this device (TFLOP/s), the roofline
+ * denominator for the Gram/TTM kernels (MEASURED_PEAKS.json has no fp64). */
+double tcb_peak_dmma_tflops(void);
+
 /* ---- lower-level entry points on host buffers (each wraps device kernels);
  * the reference symbols they replace are named per function. ---- */
 

@@ -16,6 +16,29 @@ u64& launch_counter() {
     static u64 c = 0;
     return c;
 }
+
+namespace {
+bool g_prof = false;
+struct Rec {
+    int cat;
+    cudaEvent_t a, b;
+};
+std::vector<Rec> g_recs;
+}  // namespace
+
+ProfScope::ProfScope(Cat c, cudaStream_t s) : cat(c), st(s) {
+    if (!g_prof) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+}
+ProfScope::~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    g_recs.push_back({cat, a, b});
+}
+
+double peak_dmma_tflops();
 }  // namespace tcb
 
 using namespace tcb;
@@ -120,6 +143,38 @@ void tcb_default_params(tcb_params* p) {
 }
 
 const char* tcb_last_error(void) { return g_err.c_str(); }
+
+void tcb_prof_enable(int on) { g_prof = on != 0; }
+
+int tcb_prof_read(double* ms, uint64_t* counts, int ncat) {
+    return guard([&] {
+        TCB_CUDA(cudaDeviceSynchronize());
+        for (int i = 0; i < ncat; ++i) {
+            ms[i] = 0.0;
+            counts[i] = 0;
+        }
+        for (auto& r : g_recs) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, r.a, r.b);
+            if (r.cat < ncat) {
+                ms[r.cat] += t;
+                counts[r.cat] += 1;
+            }
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        g_recs.clear();
+    });
+}
+
+double tcb_peak_dmma_tflops(void) {
+    try {
+        return peak_dmma_tflops();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1.0;
+    }
+}
 void tcb_free(void* p) { std::free(p); }
 uint64_t tcb_kernel_launches(void) { return launch_counter(); }
 

@@ -670,6 +670,7 @@ __global__ void assemble_kernel(const u8* __restrict__ ent, const AcDesc* __rest
 
 // ================================================================ host launchers
 SumRec device_sum(SumKind kind, const u64* m, const u64* dec, u64 n, int plane, cudaStream_t s) {
+    ProfScope prof_scope(kSum, s);
     const int grid = sm_count() * 4;
     DevBuf<SumRec> part(grid, s);
     sum_kernel<<<grid, kSumThreads, 0, s>>>(kind, m, dec, n, plane, part.p);
@@ -691,6 +692,7 @@ SumRec device_sum(SumKind kind, const u64* m, const u64* dec, u64 n, int plane, 
 }
 
 double device_sum_serial(SumKind kind, const u64* m, const u64* dec, u64 n, int plane, cudaStream_t s) {
+    ProfScope prof_scope(kSum, s);
     DevBuf<double> out(1, s);
     sum_serial_kernel<<<1, 1, 0, s>>>(kind, m, dec, n, plane, out.p);
     count_launch();
@@ -699,6 +701,7 @@ double device_sum_serial(SumKind kind, const u64* m, const u64* dec, u64 n, int 
 }
 
 void plane_stats(const u64* m, u64 n, u64 block, int p_hi, int p_lo, PlaneBlockRec* out_host, cudaStream_t s) {
+    ProfScope prof_scope(kStats, s);
     const u64 nb = (n + block - 1) / block;
     const u64 cpb = (block + kChunk - 1) / kChunk;
     const int np = p_hi - p_lo + 1;
@@ -714,6 +717,7 @@ void plane_stats(const u64* m, u64 n, u64 block, int p_hi, int p_lo, PlaneBlockR
 }
 
 void plane_stats_serial(const u64* m, u64 n, u64 block, int p, PlaneBlockRec* out_host, cudaStream_t s) {
+    ProfScope prof_scope(kStats, s);
     const u64 nb = (n + block - 1) / block;
     DevBuf<PlaneBlockRec> out(nb, s);
     stats_serial_kernel<<<cdiv(nb, 64), 64, 0, s>>>(m, n, block, nb, p, out.p);
@@ -725,6 +729,7 @@ void plane_stats_serial(const u64* m, u64 n, u64 block, int p, PlaneBlockRec* ou
 
 void crossing_scan(const u64* m, u64 n, u64 block, u64 b, int plane, int category, const double* cum,
                    const double* need, int npairs, u64* counts_host, cudaStream_t s) {
+    ProfScope prof_scope(kStats, s);
     DevBuf<double> c(npairs, s), nd(npairs, s);
     DevBuf<u64> out(2 * npairs, s);
     c.upload(cum, npairs);
@@ -738,6 +743,7 @@ void crossing_scan(const u64* m, u64 n, u64 block, u64 b, int plane, int categor
 }
 
 void decode_model(const u64* m, u64 n, u64 block, int last_plane, const u64* stops_dev, u64* dec, cudaStream_t s) {
+    ProfScope prof_scope(kStats, s);
     const u64 nb = (n + block - 1) / block;
     if (nb == 0) return;
     decode_model_kernel<<<static_cast<unsigned>(nb), kDecThreads, 0, s>>>(m, n, block, last_plane, stops_dev, dec);
@@ -809,7 +815,10 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
     DevBuf<u32> raw(raw_words + 1, s);
     raw.zero();
     DevBuf<StreamOut> so(ns, s);
+    {
+    ProfScope pe(kEmit, s);
     emit_kernel<<<static_cast<unsigned>(ns), kEmT, 0, s>>>(m, neg, dsd.p, syms.p, raw.p, so.p);
+    }
     count_launch();
     TCB_LAUNCH();
     std::vector<StreamOut> soh(ns);
@@ -842,7 +851,10 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
     DevBuf<u8> ent(out_total + 1, s);
     DevBuf<u32> scratch(scratch_total + 2, s);
     DevBuf<u64> elen(ns, s);
+    {
+    ProfScope pa(kAc, s);
     ac_kernel<<<cdiv(ns, 32), 32, 0, s>>>(syms.p, so.p, dad.p, static_cast<int>(ns), ent.p, scratch.p, elen.p);
+    }
     count_launch();
     TCB_LAUNCH();
     std::vector<u64> el(ns);
@@ -859,6 +871,7 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
     DevBuf<u64> doff(ns, s);
     doff.upload(off.data(), ns);
     DevBuf<u8> body(tot, s);
+    ProfScope pz(kEmit, s);
     assemble_kernel<<<static_cast<unsigned>(ns), 128, 0, s>>>(ent.p, dad.p, elen.p, raw.p, dsd.p, so.p, doff.p,
                                                                body.p);
     count_launch();

@@ -91,4 +91,15 @@ inline unsigned cdiv(u64 a, u64 b) { return static_cast<unsigned>((a + b - 1) / 
 u64& launch_counter();
 inline void count_launch(u64 k = 1) { launch_counter() += k; }
 
+// Optional per-stage device timing (CUDA events on the launching stream),
+// enabled by tcb_prof_enable(); read back with tcb_prof_read().
+enum Cat : int { kIngest = 0, kPermute, kGram, kEig, kTtm, kQuant, kStats, kEmit, kAc, kFactor, kSum, kNumCat };
+struct ProfScope {
+    ProfScope(Cat c, cudaStream_t s);
+    ~ProfScope();
+    Cat cat;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+};
+
 }  // namespace tcb

@@ -386,6 +386,7 @@ __global__ void scale_mgs_kernel(double* __restrict__ U, int n, int r, const dou
 }  // namespace
 
 std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_t s) {
+    ProfScope prof_scope(kEig, s);
     const int n = static_cast<int>(n64);
     if (n64 > 1024) throw Error("sthosvd: device eigensolver supports mode sizes up to 1024");
     w.n = n64;
@@ -427,6 +428,7 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
 }
 
 void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
+    ProfScope prof_scope(kEig, s);
     const int n = static_cast<int>(w.n), r = static_cast<int>(r64);
     std::vector<double> ev(w.n), d(w.n), e(w.n + 1);
     w.evals.download(ev.data(), w.n);
@@ -438,6 +440,7 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
         const double rr = std::fabs(d[i]) + (i > 0 ? std::fabs(e[i - 1]) : 0.0) + (i + 1 < n ? std::fabs(e[i]) : 0.0);
         tnorm = std::max(tnorm, rr);
     }
+    if (!(tnorm > 0.0)) tnorm = 1.0;  // zero matrix: any orthonormal basis is an eigenbasis
     const double ortol = 1e-3 * tnorm;
     std::vector<int> cl{0};
     for (int j = 1; j < r; ++j)
@@ -455,12 +458,14 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
 }
 
 void fix_column_signs(double* U, u64 n, u64 r, cudaStream_t s) {
+    ProfScope prof_scope(kEig, s);
     sign_kernel<<<cdiv(r, 4), 128, 0, s>>>(U, static_cast<int>(n), static_cast<int>(r));
     count_launch();
     TCB_LAUNCH();
 }
 
 void scale_orthonormalize(double* U, u64 n, u64 r, const double* sigma, cudaStream_t s) {
+    ProfScope prof_scope(kEig, s);
     scale_mgs_kernel<<<1, 256, 32 * sizeof(double), s>>>(U, static_cast<int>(n), static_cast<int>(r), sigma);
     count_launch();
     TCB_LAUNCH();

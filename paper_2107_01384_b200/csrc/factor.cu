@@ -179,6 +179,7 @@ __global__ void expand_residual(const double* __restrict__ Vd, u64 n, u64 rl, co
 }  // namespace
 
 double orth_deviation(const double* U, u64 n, u64 r, const std::vector<u64>& live, bool as_float, cudaStream_t s) {
+    ProfScope prof_scope(kFactor, s);
     const u64 rl = live.size();
     if (rl == 0) return 0.0;
     DevBuf<u64> dl(rl, s);
@@ -193,6 +194,7 @@ double orth_deviation(const double* U, u64 n, u64 r, const std::vector<u64>& liv
 
 void householder(const double* U, u64 n, u64 r, const std::vector<u64>& live, double* V, signed char* flips_host,
                  cudaStream_t s) {
+    ProfScope prof_scope(kFactor, s);
     const u64 rl = live.size();
     if (rl == 0) return;
     DevBuf<u64> dl(rl, s);
@@ -226,6 +228,7 @@ void householder(const double* U, u64 n, u64 r, const std::vector<u64>& live, do
 }
 
 void reflector_stream(const double* V, u64 n, u64 rl, const double* scales_dev, double* st, cudaStream_t s) {
+    ProfScope prof_scope(kFactor, s);
     if (rl == 0) return;
     stream_kernel<<<static_cast<unsigned>(rl), 128, 0, s>>>(V, n, rl, scales_dev, st);
     count_launch();
@@ -235,6 +238,7 @@ void reflector_stream(const double* V, u64 n, u64 rl, const double* scales_dev, 
 std::vector<double> factor_residuals(const u64* dec, const u8* neg, int k, u64 n, u64 r,
                                      const std::vector<u64>& live, const double* scales_dev, const double* U,
                                      const signed char* flips_dev, cudaStream_t s) {
+    ProfScope prof_scope(kFactor, s);
     const u64 rl = live.size();
     if (n > 1024) throw Error("factor codec: mode sizes above 1024 unsupported on the device path");
     DevBuf<u64> dl(rl, s);

@@ -253,9 +253,46 @@ __global__ void gemm_nn_kernel(const double* __restrict__ B, u64 rows, u64 cols,
     out[idx] = s;
 }
 
+// Peak probe: independent DMMA chains per warp, no memory traffic.
+__global__ void dmma_peak_kernel(int iters, double* out) {
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+    const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma(c[i][0], c[i][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+    if (s == 12345.678) out[0] = s;
+}
+
 }  // namespace
 
+double peak_dmma_tflops() {
+    cudaStream_t s = nullptr;
+    DevBuf<double> o(1, s);
+    const int iters = 4096, blocks = sm_count() * 4, threads = 256;
+    dmma_peak_kernel<<<blocks, threads, 0, s>>>(64, o.p);  // warm-up
+    cudaEvent_t a, b;
+    TCB_CUDA(cudaEventCreate(&a));
+    TCB_CUDA(cudaEventCreate(&b));
+    TCB_CUDA(cudaEventRecord(a, s));
+    dmma_peak_kernel<<<blocks, threads, 0, s>>>(iters, o.p);
+    TCB_CUDA(cudaEventRecord(b, s));
+    TCB_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    TCB_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 8 * 8 * 4 * 8.0 * iters * (static_cast<double>(blocks) * threads / 32);
+    return flops / (ms * 1e-3) / 1e12;
+}
+
 void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
+    ProfScope prof_scope(kGram, s);
     const int nt = static_cast<int>((rows + GT - 1) / GT);
     const int lower = nt * (nt + 1) / 2;
     const u64 want = static_cast<u64>(2 * sm_count());
@@ -282,12 +319,14 @@ void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
 }
 
 void gram_cols_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
+    ProfScope prof_scope(kGram, s);
     gram_cols_kernel<<<cdiv(cols * cols, 256), 256, 0, s>>>(B, rows, cols, G);
     count_launch();
     TCB_LAUNCH();
 }
 
 void ttm_f64(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s) {
+    ProfScope prof_scope(kTtm, s);
     dim3 grid(cdiv(cols, TM), cdiv(r, TN));
     const bool v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
     const int smem = 2 * TBK * (APAD + UPAD) * sizeof(double);
@@ -304,6 +343,7 @@ void ttm_f64(const double* B, u64 rows, u64 cols, const double* U, u64 r, double
 }
 
 void gemm_nn_f64(const double* B, u64 rows, u64 cols, const double* V, u64 r, double* out, cudaStream_t s) {
+    ProfScope prof_scope(kTtm, s);
     gemm_nn_kernel<<<cdiv(rows * r, 256), 256, 0, s>>>(B, rows, cols, V, r, out);
     count_launch();
     TCB_LAUNCH();

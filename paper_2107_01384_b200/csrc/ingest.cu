@@ -28,6 +28,7 @@ __global__ void copy16_kernel(const double2* __restrict__ src, double2* __restri
 
 template <class T>
 void cast_any(const void* src, int dtype, u64 n, T* dst, cudaStream_t s) {
+    ProfScope prof_scope(kIngest, s);
     const unsigned grid = static_cast<unsigned>(sm_count() * 8), blk = 256;
     switch (dtype) {
         case 0: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const int8_t*>(src), dst, n); break;
@@ -95,6 +96,7 @@ __global__ void sum_stage2(const double* __restrict__ part, int n, double* __res
 
 template <class T>
 double sumsq_impl(const T* x, u64 n, bool* finite, cudaStream_t s) {
+    ProfScope prof_scope(kIngest, s);
     const int grid = sm_count() * 4;
     DevBuf<double> part(grid + 1, s);
     DevBuf<int> bad(1, s);
@@ -229,6 +231,7 @@ __global__ void precision_kernel(const void* __restrict__ src, int is_signed, u6
 }  // namespace
 
 bool ingest_precision_loss(const void* src, int dtype, u64 n, cudaStream_t s) {
+    ProfScope prof_scope(kIngest, s);
     DevBuf<int> f(1, s);
     f.zero();
     precision_kernel<<<sm_count() * 4, 256, 0, s>>>(src, dtype == 6 ? 1 : 0, n, f.p);
@@ -244,6 +247,7 @@ double sum_squares(const double* x, u64 n, bool* finite, cudaStream_t s) { retur
 double sum_squares(const float* x, u64 n, bool* finite, cudaStream_t s) { return sumsq_impl(x, n, finite, s); }
 
 double max_abs(const double* x, u64 n, cudaStream_t s) {
+    ProfScope prof_scope(kSum, s);
     const int grid = sm_count() * 4;
     DevBuf<double> part(grid + 1, s);
     maxabs_stage1<<<grid, kRedThreads, 0, s>>>(x, n, part.p);
@@ -259,6 +263,7 @@ double max_abs(const double* x, u64 n, cudaStream_t s) {
 template <class T>
 void permute_axes(const T* src, T* dst, const std::vector<u64>& shape, const std::vector<u64>& perm,
                   cudaStream_t s) {
+    ProfScope prof_scope(kPermute, s);
     const int d = static_cast<int>(shape.size());
     u64 n = 1;
     for (auto v : shape) n *= v;

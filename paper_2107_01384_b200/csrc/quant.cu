@@ -92,6 +92,7 @@ std::vector<u64> axis_meta(const std::vector<u64>& shape) {
 }  // namespace
 
 void quantize_f64(const double* x, u64 n, int k, u64* mag, u8* neg, cudaStream_t s) {
+    ProfScope prof_scope(kQuant, s);
     if (n == 0) return;
     quantize_kernel<<<sm_count() * 8, 256, 0, s>>>(x, n, k, mag, neg);
     count_launch();
@@ -99,6 +100,7 @@ void quantize_f64(const double* x, u64 n, int k, u64* mag, u8* neg, cudaStream_t
 }
 
 void slice_norms(const u64* mag, const std::vector<u64>& shape, double down, double* out, cudaStream_t s) {
+    ProfScope prof_scope(kQuant, s);
     u64 total = 0;
     for (auto v : shape) total += v;
     DevBuf<u64> sh(shape.size(), s);
@@ -109,6 +111,7 @@ void slice_norms(const u64* mag, const std::vector<u64>& shape, double down, dou
 }
 
 std::vector<u8> dead_slices(const u64* dec, const std::vector<u64>& shape, cudaStream_t s) {
+    ProfScope prof_scope(kQuant, s);
     const auto meta = axis_meta(shape);
     u64 n = 1, total = 0;
     for (auto v : shape) {
@@ -127,6 +130,7 @@ std::vector<u8> dead_slices(const u64* dec, const std::vector<u64>& shape, cudaS
 
 void sign_fold(u8* neg, const std::vector<u64>& shape, const std::vector<signed char>& flips_by_axis,
                cudaStream_t s) {
+    ProfScope prof_scope(kQuant, s);
     const auto meta = axis_meta(shape);
     u64 n = 1;
     for (auto v : shape) n *= v;

@@ -24,16 +24,19 @@ CONFIGS = {
 
 
 def _separable(shape, amps, rng, out_dtype):
-    acc = np.zeros(shape, dtype=np.float64)
-    for a in amps:
-        vecs = []
-        for n in shape:
+    """sum_k a_k v1_k (x) v2_k (x) v3_k as one GEMM: (V1 diag a) @ KhatriRao(V2, V3)^T."""
+    K = len(amps)
+    mats = [np.empty((n, K)) for n in shape]
+    for k in range(K):
+        for m, n in enumerate(shape):
             f = rng.uniform(0.5, 4.0)
             ph = rng.uniform(0.0, 2 * np.pi)
             x = np.arange(n, dtype=np.float64) / n
-            vecs.append(np.sin(2 * np.pi * f * x + ph))
-        acc += a * np.einsum("i,j,k->ijk", *vecs)
-    return acc
+            mats[m][:, k] = np.sin(2 * np.pi * f * x + ph)
+    rest = mats[1]
+    for m in mats[2:]:
+        rest = (rest[:, None, :] * m[None, :, :]).reshape(-1, K)
+    return ((mats[0] * np.asarray(amps)[None, :]) @ rest.T).reshape(shape)
 
 
 def sinusoids(shape, n_terms, decay=None, noise=1e-3, seed=0, dtype=np.float64):

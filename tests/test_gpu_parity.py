@@ -14,9 +14,9 @@ def rel(a, b):
 
 
 def principal_sine(u, v):
-    """largest principal-angle sine between span(u) and span(v) (orthonormal columns)."""
-    s = np.linalg.svd(u.T @ v, compute_uv=False)
-    return float(np.sqrt(max(0.0, 1.0 - min(1.0, s.min()) ** 2)))
+    """largest principal-angle sine between span(u) and span(v) (orthonormal
+    columns): ||(I - V V^T) U||_2, accurate for small angles (unlike sqrt(1-cos^2))."""
+    return float(np.linalg.norm(u - v @ (v.T @ u), 2))
 
 
 # ---------------------------------------------------------------- dense kernels
