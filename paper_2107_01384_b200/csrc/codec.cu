@@ -516,8 +516,8 @@ __global__ void __launch_bounds__(kEmT) emit_kernel(const u64* __restrict__ m, c
 struct AcDesc {
     u64 sym_off;     // symbols
     u64 out_off;     // output byte offset (capacity 5 + 7*nsyms + 16)
-    u64 model_off;   // u32 words of scratch
-    u32 cap;         // model capacity (>= distinct symbols + 1)
+    u64 model_off;   // u32 words of global scratch (global mode)
+    u32 cap;         // model capacity (>= distinct symbols + 1), even
     u32 fen;         // fenwick array size (power of two >= cap + 1)
     u32 hbits;       // hash table has 1 << hbits u32 slots
     u32 pad;
@@ -547,13 +547,26 @@ __device__ __forceinline__ void ac_shift(AcState& s) {
     s.low = (s.low << 8) & 0xFFFFFFFFull;
 }
 
+__device__ __forceinline__ void ac_norm(AcState& s) {
+    while (s.range < (1u << 24)) {
+        ac_shift(s);
+        s.range <<= 8;
+    }
+}
+
 __device__ __forceinline__ void ac_code(AcState& s, u32 cum, u32 freq, u32 total) {
     s.range /= total;
     s.low += static_cast<u64>(cum) * s.range;
     s.range *= freq;
-    while (s.range < (1u << 24)) {
-        ac_shift(s);
-        s.range <<= 8;
+    ac_norm(s);
+}
+
+// 32 raw bits as encode(bit, 1, 2) each: range/2 is a shift (entropy.cpp:95-100)
+__device__ __forceinline__ void ac_raw32(AcState& s, u64 v) {
+    for (int b = 31; b >= 0; --b) {
+        s.range >>= 1;
+        if ((v >> b) & 1u) s.low += s.range;
+        ac_norm(s);
     }
 }
 
@@ -561,10 +574,33 @@ __device__ __forceinline__ u32 hslot(u64 sym, u32 hbits) {
     return static_cast<u32>((sym * 0x9E3779B97F4A7C15ull) >> (64 - hbits));
 }
 
-__global__ void ac_kernel(const u64* __restrict__ syms, const StreamOut* __restrict__ sout,
-                          const AcDesc* __restrict__ desc, int nstreams, u8* __restrict__ outbuf,
-                          u32* __restrict__ scratch, u64* __restrict__ elen) {
-    const int sidx = blockIdx.x * blockDim.x + threadIdx.x;
+constexpr u32 kAcSmemCap = 2048;  // model entries kept in shared memory
+
+__host__ __device__ inline u32 pow2_at_least(u32 v) {
+    u32 p = 2;
+    while (p < v) p *= 2;
+    return p;
+}
+__host__ __device__ inline u32 log2_at_least(u32 v) {
+    u32 b = 4;
+    while ((1u << b) < v) ++b;
+    return b;
+}
+__host__ __device__ inline u64 ac_smem_bytes(u32 cap) {
+    return 4ull * cap + 4ull * pow2_at_least(cap + 1) + 4ull * (1u << log2_at_least(2 * cap)) + 8ull * cap + 16;
+}
+
+// One warp per stream (lane 0 codes).  The adaptive model lives in shared
+// memory when its capacity fits (smem_cap entries), else in the stream's
+// global scratch; a shared-memory model that overflows flags the stream for a
+// global-memory rerun.
+__global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, const StreamOut* __restrict__ sout,
+                                                const AcDesc* __restrict__ desc, const int* __restrict__ ids,
+                                                int nstreams, u8* __restrict__ outbuf, u32* __restrict__ scratch,
+                                                u64* __restrict__ elen, u32 smem_cap, int* __restrict__ redo) {
+    extern __shared__ __align__(16) u8 ac_smem[];
+    if (threadIdx.x != 0) return;
+    const int sidx = ids ? ids[blockIdx.x] : static_cast<int>(blockIdx.x);
     if (sidx >= nstreams) return;
     const u64 ns = sout[sidx].nsyms;
     if (ns == 0) {
@@ -572,12 +608,28 @@ __global__ void ac_kernel(const u64* __restrict__ syms, const StreamOut* __restr
         return;
     }
     const AcDesc d = desc[sidx];
-    u32* cnt = scratch + d.model_off;                 // cap
-    u32* fen = cnt + d.cap;                           // fen
-    u32* hidx = fen + d.fen;                          // 1 << hbits (index + 1)
-    u64* val = reinterpret_cast<u64*>(hidx + (1u << d.hbits));  // cap (8-byte aligned by construction)
-    for (u32 i = 0; i < d.fen; ++i) fen[i] = 0;
-    for (u32 i = 0; i < (1u << d.hbits); ++i) hidx[i] = 0;
+    u32 cap, fenn, hb;
+    u32 *cnt, *fen, *hidx;
+    u64* val;
+    if (smem_cap > 0) {
+        cap = min(d.cap, smem_cap);
+        fenn = pow2_at_least(cap + 1);
+        hb = log2_at_least(2 * cap);
+        val = reinterpret_cast<u64*>(ac_smem);
+        cnt = reinterpret_cast<u32*>(val + cap);
+        fen = cnt + cap;
+        hidx = fen + fenn;
+    } else {
+        cap = d.cap;
+        fenn = d.fen;
+        hb = d.hbits;
+        cnt = scratch + d.model_off;
+        fen = cnt + cap;
+        hidx = fen + fenn;
+        val = reinterpret_cast<u64*>(hidx + (1u << hb));
+    }
+    for (u32 i = 0; i < fenn; ++i) fen[i] = 0;
+    for (u32 i = 0; i < (1u << hb); ++i) hidx[i] = 0;
     u8* out = outbuf + d.out_off;
     out[0] = 0;  // coder id: arithmetic
     const u32 cnt32 = static_cast<u32>(ns);
@@ -587,40 +639,38 @@ __global__ void ac_kernel(const u64* __restrict__ syms, const StreamOut* __restr
     cnt[0] = 1;
     val[0] = 0;
     auto fadd = [&](u32 i, u32 dlt) {
-        for (u32 j = i + 1; j < d.fen; j += j & (~j + 1)) fen[j] += dlt;
+        for (u32 j = i + 1; j < fenn; j += j & (~j + 1)) fen[j] += dlt;
     };
     auto below = [&](u32 i) {
         u32 s = 0;
         for (u32 j = i; j > 0; j -= j & (~j + 1)) s += fen[j];
         return s;
     };
-    auto rebuild = [&]() {
-        for (u32 i = 0; i < d.fen; ++i) fen[i] = 0;
-        for (u32 i = 0; i < nsym; ++i) fen[i + 1] = cnt[i];
-        for (u32 i = 1; i < d.fen; ++i) {
-            const u32 j = i + (i & (~i + 1));
-            if (j < d.fen) fen[j] += fen[i];
-        }
-    };
     auto halve = [&]() {
         total = 0;
+        for (u32 i = 0; i < fenn; ++i) fen[i] = 0;
         for (u32 i = 0; i < nsym; ++i) {
             cnt[i] = max(1u, cnt[i] >> 1);
             total += cnt[i];
+            fen[i + 1] = cnt[i];
         }
-        rebuild();
+        for (u32 i = 1; i < fenn; ++i) {
+            const u32 j = i + (i & (~i + 1));
+            if (j < fenn) fen[j] += fen[i];
+        }
     };
     fadd(0, 1);
     const u64* sy = syms + d.sym_off;
+    const u32 hmask = (1u << hb) - 1;
     for (u64 t = 0; t < ns; ++t) {
         const u64 s = sy[t];
-        u32 h = hslot(s, d.hbits), found = 0;
+        u32 h = hslot(s, hb), found = 0;
         while (hidx[h]) {
             if (val[hidx[h] - 1] == s) {
                 found = hidx[h];
                 break;
             }
-            h = (h + 1) & ((1u << d.hbits) - 1);
+            h = (h + 1) & hmask;
         }
         if (found) {
             const u32 i = found - 1;
@@ -630,8 +680,13 @@ __global__ void ac_kernel(const u64* __restrict__ syms, const StreamOut* __restr
             total += 32;
             fadd(i, 32);
         } else {
+            if (nsym >= cap) {  // shared-memory model full: rerun from global scratch
+                *redo = 1;
+                elen[sidx] = ~u64{0};
+                return;
+            }
             ac_code(st, 0, cnt[0], total);
-            for (int b = 31; b >= 0; --b) ac_code(st, static_cast<u32>((s >> b) & 1u), 1, 2);
+            ac_raw32(st, s);
             if (total + 32 >= (1u << 16)) halve();
             const u32 i = nsym++;
             val[i] = s;
@@ -643,6 +698,51 @@ __global__ void ac_kernel(const u64* __restrict__ syms, const StreamOut* __restr
     }
     for (int i = 0; i < 5; ++i) ac_shift(st);
     elen[sidx] = st.pos;
+}
+
+// Host side: shared-memory pass for every stream, global-scratch rerun for
+// the ones whose model overflowed.
+void run_ac(const u64* syms, const StreamOut* so, const AcDesc* dad, const std::vector<AcDesc>& ad,
+            const std::vector<StreamOut>& soh, int ns, u8* ent, u32* scratch, u64* elen, cudaStream_t s) {
+    u32 need = 0;
+    for (int i = 0; i < ns; ++i)
+        if (soh[i].nsyms) need = std::max<u32>(need, std::min<u32>(ad[i].cap, kAcSmemCap));
+    if (need == 0) {
+        TCB_CUDA(cudaMemsetAsync(elen, 0, ns * sizeof(u64), s));
+        return;
+    }
+    const u64 smem = ac_smem_bytes(need);
+    static bool attr = [] {
+        cudaFuncSetAttribute(ac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(ac_smem_bytes(kAcSmemCap)));
+        return true;
+    }();
+    (void)attr;
+    DevBuf<int> redo(1, s);
+    redo.zero();
+    {
+        ProfScope pa(kAc, s);
+        ac_kernel<<<static_cast<unsigned>(ns), 32, smem, s>>>(syms, so, dad, nullptr, ns, ent, scratch, elen, need,
+                                                             redo.p);
+    }
+    count_launch();
+    TCB_LAUNCH();
+    if (redo.to_host()[0] == 0) return;
+    std::vector<u64> el(ns);
+    TCB_CUDA(cudaMemcpyAsync(el.data(), elen, ns * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    TCB_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> ids;
+    for (int i = 0; i < ns; ++i)
+        if (el[i] == ~u64{0}) ids.push_back(i);
+    DevBuf<int> dids(ids.size(), s);
+    dids.upload(ids.data(), ids.size());
+    {
+        ProfScope pa(kAc, s);
+        ac_kernel<<<static_cast<unsigned>(ids.size()), 32, 0, s>>>(syms, so, dad, dids.p, ns, ent, scratch, elen, 0,
+                                                                  redo.p);
+    }
+    count_launch();
+    TCB_LAUNCH();
 }
 
 // ---------------------------------------------------------------- assembly
@@ -772,9 +872,7 @@ std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cu
     DevBuf<u8> ent(5 + 7 * n + 16, s);
     DevBuf<u32> scratch(a.cap + a.fen + (u64{1} << a.hbits) + 2ull * a.cap + 2, s);
     DevBuf<u64> elen(1, s);
-    ac_kernel<<<1, 32, 0, s>>>(syms.p, dso.p, dad.p, 1, ent.p, scratch.p, elen.p);
-    count_launch();
-    TCB_LAUNCH();
+    run_ac(syms.p, dso.p, dad.p, std::vector<AcDesc>{a}, std::vector<StreamOut>{so}, 1, ent.p, scratch.p, elen.p, s);
     const u64 el = elen.to_host()[0];
     out.resize(el);
     ent.download(out.data(), el);
@@ -851,12 +949,7 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
     DevBuf<u8> ent(out_total + 1, s);
     DevBuf<u32> scratch(scratch_total + 2, s);
     DevBuf<u64> elen(ns, s);
-    {
-    ProfScope pa(kAc, s);
-    ac_kernel<<<cdiv(ns, 32), 32, 0, s>>>(syms.p, so.p, dad.p, static_cast<int>(ns), ent.p, scratch.p, elen.p);
-    }
-    count_launch();
-    TCB_LAUNCH();
+    run_ac(syms.p, so.p, dad.p, ad, soh, static_cast<int>(ns), ent.p, scratch.p, elen.p, s);
     std::vector<u64> el(ns);
     elen.download(el.data(), ns);
     TCB_CUDA(cudaStreamSynchronize(s));

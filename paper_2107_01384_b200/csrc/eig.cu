@@ -1,14 +1,18 @@
 // Device symmetric eigensolver for the per-mode Gram (n <= 1024, fp64):
 // the SelfAdjointEigenSolver call of sthosvd.cpp:80-90, re-designed for B200.
 //
-//  1. Householder tridiagonalisation: one 8-CTA thread-block cluster, matrix in
-//     L2, rows interleaved over the CTAs, two hardware cluster barriers/step.
-//  2. All eigenvalues by Sturm-count bisection, one thread per eigenvalue.
-//  3. Top-r eigenvectors of the tridiagonal by inverse iteration with
-//     modified Gram-Schmidt inside eigenvalue clusters (LAPACK dstein scheme);
-//     independent clusters run in parallel CTAs.
-//  4. Back-transform U = Q Z (warp per column) and the column sign convention
-//     of sthosvd.cpp:103-110.
+//  1. Householder tridiagonalisation on one 8-CTA thread-block cluster.
+//     n <= 448: the matrix lives in distributed shared memory (rows
+//     interleaved over the CTAs); p-slices and the next column are pushed to
+//     every CTA with DSMEM stores, two hardware cluster barriers per step.
+//     Larger n: same schedule with the matrix in L2.
+//  2. All eigenvalues by Sturm-count multisection: one warp per eigenvalue,
+//     32 probes per round (5 bits/round), reciprocal via rcp.approx + Newton.
+//  3. Top-r eigenvectors of the tridiagonal by inverse iteration, one CTA
+//     per vector (all in parallel), then modified Gram-Schmidt inside tight
+//     eigenvalue clusters (gap <= 1e-6 ||T||), independent clusters in parallel.
+//  4. Back-transform U = Q Z with reflector chunks staged in shared memory,
+//     and the column sign convention of sthosvd.cpp:103-110.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -25,6 +29,7 @@ namespace {
 
 constexpr int kCluster = 8;
 constexpr int kTriThreads = 512;
+constexpr int kDsmemMaxN = 448;
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -37,21 +42,122 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return t;
 }
 
-// A: row-major n x n symmetric (overwritten).  Outputs d[n], e[n-1],
-// V[k*n + i] (Householder vector of step k, entries i >= k+1), tau[k].
-__global__ void __launch_bounds__(kTriThreads) tridiag_kernel(double* __restrict__ A, int n, double* __restrict__ d,
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ---------------------------------------------------------------- tridiagonalisation (DSMEM)
+// Row i lives in CTA (i % 8), local slot i / 8.  Outputs d, e, V (reflector k
+// at V[k*n + i], i >= k+1), tau.
+__global__ void __launch_bounds__(kTriThreads) tridiag_dsmem(const double* __restrict__ Ag, int n,
+                                                            double* __restrict__ d, double* __restrict__ e,
+                                                            double* __restrict__ V, double* __restrict__ tau) {
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = static_cast<int>(cl.block_rank());
+    extern __shared__ double sm[];
+    const int nloc = (n + kCluster - 1) / kCluster;
+    double* A = sm;                   // nloc x n
+    double* v = A + nloc * n;         // n
+    double* w = v + n;                // n
+    double* p = w + n;                // n (replicated, filled by DSMEM pushes)
+    double* rowk = p + n;             // n (replicated next column)
+    double* red = rowk + n;           // 32
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int li = 0; li < nloc; ++li) {
+        const int gi = li * kCluster + rank;
+        if (gi >= n) break;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) A[li * n + j] = Ag[static_cast<size_t>(gi) * n + j];
+    }
+    for (int j = threadIdx.x; j < n; j += blockDim.x) rowk[j] = Ag[j];
+    cl.sync();
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m = n - k - 1;
+        double ss = 0.0;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const double x = rowk[k + 1 + i];
+            v[i] = x;
+            ss += x * x;
+        }
+        const double alpha = sqrt(block_sum(ss, red));
+        const double x0 = v[0];
+        const double beta = x0 >= 0.0 ? -alpha : alpha;
+        __syncthreads();
+        if (threadIdx.x == 0) v[0] = x0 - beta;
+        __syncthreads();
+        double vv = 0.0;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) vv += v[i] * v[i];
+        vv = block_sum(vv, red);
+        const double t = (alpha == 0.0 || vv == 0.0) ? 0.0 : 2.0 / vv;
+        if (rank == 0) {
+            if (threadIdx.x == 0) {
+                e[k] = t == 0.0 ? x0 : beta;
+                tau[k] = t;
+                d[k] = rowk[k];
+            }
+            for (int i = threadIdx.x; i < m; i += blockDim.x) V[static_cast<size_t>(k) * n + k + 1 + i] = v[i];
+        }
+        if (t != 0.0) {
+            // p_i = t * A[i][k+1:] . v for owned rows, pushed to every CTA
+            for (int gi = k + 1 + ((rank - (k + 1)) % kCluster + kCluster) % kCluster + kCluster * warp; gi < n;
+                 gi += kCluster * nwarp) {
+                const double* row = A + (gi / kCluster) * n + k + 1;
+                double s = 0.0;
+                for (int j = lane; j < m; j += 32) s += row[j] * v[j];
+                s = warp_sum(s) * t;
+                if (lane < kCluster) *cl.map_shared_rank(p + gi, lane) = s;
+            }
+            cl.sync();
+            double pv = 0.0;
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                const double q = p[k + 1 + i];
+                w[i] = q;
+                pv += q * v[i];
+            }
+            const double K = 0.5 * t * block_sum(pv, red);
+            for (int i = threadIdx.x; i < m; i += blockDim.x) w[i] -= K * v[i];
+            __syncthreads();
+            for (int gi = k + 1 + ((rank - (k + 1)) % kCluster + kCluster) % kCluster + kCluster * warp; gi < n;
+                 gi += kCluster * nwarp) {
+                double* row = A + (gi / kCluster) * n + k + 1;
+                const double vi = v[gi - k - 1], wi = w[gi - k - 1];
+                for (int j = lane; j < m; j += 32) row[j] -= vi * w[j] + wi * v[j];
+            }
+        }
+        __syncthreads();
+        // owner of row k+1 pushes it (the next column) to every CTA
+        if ((k + 1) % kCluster == rank) {
+            const double* row = A + ((k + 1) / kCluster) * n;
+            for (int idx = threadIdx.x; idx < kCluster * (n - k - 1); idx += blockDim.x) {
+                const int dst = idx / (n - k - 1), j = k + 1 + idx % (n - k - 1);
+                *cl.map_shared_rank(rowk + j, dst) = row[j];
+            }
+        }
+        cl.sync();
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+        if (n >= 2) {
+            d[n - 2] = rowk[n - 2];
+            e[n - 2] = rowk[n - 1];
+        }
+    }
+    if (n >= 2 && (n - 1) % kCluster == rank && threadIdx.x == 0) d[n - 1] = A[((n - 1) / kCluster) * n + n - 1];
+    if (n == 1 && rank == 0 && threadIdx.x == 0) d[0] = rowk[0];
+}
+
+// Same schedule with the matrix in L2 (n > kDsmemMaxN).
+__global__ void __launch_bounds__(kTriThreads) tridiag_global(double* __restrict__ A, int n, double* __restrict__ d,
                                                              double* __restrict__ e, double* __restrict__ V,
                                                              double* __restrict__ tau, double* __restrict__ P) {
     cg::cluster_group cl = cg::this_cluster();
     const int rank = static_cast<int>(cl.block_rank());
     extern __shared__ double sh_tri[];
-    double* v = sh_tri;          // n
-    double* w = sh_tri + n;      // n
-    double* red = sh_tri + 2 * n;  // 32
+    double* v = sh_tri;
+    double* w = sh_tri + n;
+    double* red = sh_tri + 2 * n;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1;
-        // x = A[k][k+1..n-1] (row k == column k by symmetry), redundantly in every CTA
         double ss = 0.0;
         for (int i = threadIdx.x; i < m; i += blockDim.x) {
             const double x = __ldcg(A + static_cast<size_t>(k) * n + k + 1 + i);
@@ -77,20 +183,19 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(double* __restrict
             for (int i = threadIdx.x; i < m; i += blockDim.x) V[static_cast<size_t>(k) * n + k + 1 + i] = v[i];
         }
         if (t != 0.0) {
-            // p_i = t * sum_j A[i][j] v_j for owned rows i (warp per row)
             for (int r = k + 1 + rank + kCluster * warp; r < n; r += kCluster * nwarp) {
                 const double* row = A + static_cast<size_t>(r) * n + k + 1;
                 double s = 0.0;
                 for (int j = lane; j < m; j += 32) s += __ldcg(row + j) * v[j];
-                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                s = warp_sum(s);
                 if (lane == 0) P[r] = t * s;
             }
             cl.sync();
             double pv = 0.0;
             for (int i = threadIdx.x; i < m; i += blockDim.x) {
-                const double p = __ldcg(P + k + 1 + i);
-                w[i] = p;
-                pv += p * v[i];
+                const double q = __ldcg(P + k + 1 + i);
+                w[i] = q;
+                pv += q * v[i];
             }
             const double K = 0.5 * t * block_sum(pv, red);
             for (int i = threadIdx.x; i < m; i += blockDim.x) w[i] -= K * v[i];
@@ -112,53 +217,78 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(double* __restrict
     }
 }
 
-// Sturm count: number of eigenvalues of T strictly below x.
+// ---------------------------------------------------------------- eigenvalues
+__device__ __forceinline__ double frcp(double q) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+    y = fma(y, fma(-q, y, 1.0), y);
+    y = fma(y, fma(-q, y, 1.0), y);
+    return y;
+}
+
 __device__ __forceinline__ int sturm(const double* d, const double* e2, int n, double x, double pivmin) {
     double q = d[0] - x;
     int c = q < 0.0;
     for (int i = 1; i < n; ++i) {
         if (fabs(q) < pivmin) q = -pivmin;
-        q = (d[i] - x) - e2[i - 1] / q;
+        q = (d[i] - x) - e2[i - 1] * frcp(q);
         c += q < 0.0;
     }
     return c;
 }
 
-// one thread per eigenvalue; ascending index j -> descending slot n-1-j
-__global__ void bisect_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n,
-                              double* __restrict__ evals_desc) {
+// one warp per eigenvalue (ascending index j), 32 probes per round
+__global__ void multisect_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n,
+                                 double* __restrict__ evals_desc) {
     extern __shared__ double sh_bis[];
     double* d = sh_bis;
     double* e2 = sh_bis + n;
-    double gl = DBL_MAX, gu = -DBL_MAX, emax2 = 0.0;
+    __shared__ double bounds[3];
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         d[i] = dg[i];
         if (i + 1 < n) e2[i] = eg[i] * eg[i];
     }
     __syncthreads();
-    // Gershgorin bounds (every thread computes the same, cheap for n <= 1024)
-    for (int i = 0; i < n; ++i) {
-        const double r = (i > 0 ? fabs(eg[i - 1]) : 0.0) + (i + 1 < n ? fabs(eg[i]) : 0.0);
-        gl = fmin(gl, d[i] - r);
-        gu = fmax(gu, d[i] + r);
-        if (i + 1 < n) emax2 = fmax(emax2, e2[i]);
+    if (threadIdx.x == 0) {
+        double gl = DBL_MAX, gu = -DBL_MAX, emax2 = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double r = (i > 0 ? fabs(eg[i - 1]) : 0.0) + (i + 1 < n ? fabs(eg[i]) : 0.0);
+            gl = fmin(gl, d[i] - r);
+            gu = fmax(gu, d[i] + r);
+            if (i + 1 < n) emax2 = fmax(emax2, e2[i]);
+        }
+        const double tnorm = fmax(fabs(gl), fabs(gu));
+        const double pivmin = DBL_MIN * fmax(1.0, emax2);
+        bounds[0] = gl - 2.0 * DBL_EPSILON * tnorm * n - 2.0 * pivmin;
+        bounds[1] = gu + 2.0 * DBL_EPSILON * tnorm * n + 2.0 * pivmin;
+        bounds[2] = pivmin;
     }
-    const double tnorm = fmax(fabs(gl), fabs(gu));
-    const double pivmin = DBL_MIN * fmax(1.0, emax2);
-    gl -= 2.0 * DBL_EPSILON * tnorm * n + 2.0 * pivmin;
-    gu += 2.0 * DBL_EPSILON * tnorm * n + 2.0 * pivmin;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (j >= n) return;
-    double lo = gl, hi = gu;  // invariant: count(lo) <= j < count(hi)
-    for (int it = 0; it < 80; ++it) {
-        const double mid = 0.5 * (lo + hi);
-        if (mid <= lo || mid >= hi) break;
-        if (sturm(d, e2, n, mid, pivmin) > j) hi = mid;
-        else lo = mid;
+    double lo = bounds[0], hi = bounds[1];
+    const double pivmin = bounds[2];
+    for (int it = 0; it < 24; ++it) {
+        const double width = hi - lo;
+        if (!(width > 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin)) break;
+        double x = lo + width * (static_cast<double>(lane + 1) / 33.0);
+        x = fmin(fmax(x, lo), hi);
+        const bool above = sturm(d, e2, n, x, pivmin) > j;  // x is above eigenvalue j
+        const unsigned ball = __ballot_sync(0xffffffffu, above);
+        const int first = ball ? __ffs(ball) - 1 : 32;
+        const double xh = __shfl_sync(0xffffffffu, x, first < 32 ? first : 31);
+        const double xl = __shfl_sync(0xffffffffu, x, first > 0 ? first - 1 : 0);
+        const double nlo = first > 0 ? xl : lo;
+        const double nhi = first < 32 ? xh : hi;
+        if (nlo == lo && nhi == hi) break;
+        lo = nlo;
+        hi = nhi;
     }
-    evals_desc[n - 1 - j] = 0.5 * (lo + hi);
+    if (lane == 0) evals_desc[n - 1 - j] = 0.5 * (lo + hi);
 }
 
+// ---------------------------------------------------------------- eigenvectors
 __device__ __forceinline__ double hash_unit(unsigned a, unsigned b) {
     unsigned h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u;
     h ^= h >> 15;
@@ -169,146 +299,162 @@ __device__ __forceinline__ double hash_unit(unsigned a, unsigned b) {
     return (static_cast<double>(h) / 4294967295.0) * 2.0 - 1.0;
 }
 
-// Inverse iteration for one eigenvalue cluster per CTA.
-// clusters[c] = first descending index of cluster c (clusters[nc] = r).
-// Z: column-major n x r.
-__global__ void invit_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n,
-                             const double* __restrict__ evals_desc, const int* __restrict__ clusters, double tnorm,
-                             double* __restrict__ Z) {
+// Inverse iteration for eigenvalue j (one CTA of 32 threads per vector).
+// shift[j] is the (cluster-perturbed) eigenvalue; Z column-major n x r.
+__global__ void __launch_bounds__(32) invit_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n,
+                                                   const double* __restrict__ shift, double tol,
+                                                   double* __restrict__ Z) {
     extern __shared__ double sh_inv[];
-    double* a = sh_inv;          // U diagonal
-    double* b = a + n;           // first superdiagonal
-    double* c = b + n;           // multipliers
-    double* dd = c + n;          // second superdiagonal
-    double* x = dd + n;          // iterate
-    double* red = x + n;         // 32
-    int* piv = reinterpret_cast<int*>(red + 32);
-    const int j0 = clusters[blockIdx.x], j1 = clusters[blockIdx.x + 1];
-    const double eps = DBL_EPSILON;
-    const double tol = eps * tnorm + DBL_MIN;
-    double prev = 0.0;
-    for (int j = j0; j < j1; ++j) {
-        double lam = evals_desc[j];
-        if (j > j0) {
-            const double pertol = 10.0 * eps * fabs(lam) + 2.0 * DBL_MIN;
-            if (prev - lam < pertol) lam = prev - pertol;
+    double* a = sh_inv;      // U diagonal reciprocal
+    double* b = a + n;       // first superdiagonal
+    double* c = b + n;       // multipliers
+    double* dd = c + n;      // second superdiagonal
+    double* x = dd + n;      // iterate
+    int* piv = reinterpret_cast<int*>(x + n);
+    const int j = blockIdx.x;
+    const double lam = shift[j];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < n; ++i) {
+            a[i] = dg[i] - lam;
+            b[i] = i + 1 < n ? eg[i] : 0.0;
+            c[i] = i + 1 < n ? eg[i] : 0.0;
+            dd[i] = 0.0;
         }
-        prev = lam;
+        for (int k = 0; k + 1 < n; ++k) {  // LU with partial pivoting (LAPACK dlagtf scheme)
+            double ak = a[k];
+            if (fabs(ak) >= fabs(c[k])) {
+                if (fabs(ak) < tol) ak = ak < 0.0 ? -tol : tol;
+                const double mult = c[k] / ak;
+                c[k] = mult;
+                a[k + 1] -= mult * b[k];
+                piv[k] = 0;
+                a[k] = ak;
+            } else {
+                const double mult = ak / c[k];
+                a[k] = c[k];
+                const double tmp = a[k + 1];
+                a[k + 1] = b[k] - mult * tmp;
+                if (k + 2 < n) {
+                    dd[k] = b[k + 1];
+                    b[k + 1] = -mult * dd[k];
+                }
+                b[k] = tmp;
+                c[k] = mult;
+                piv[k] = 1;
+            }
+        }
+        for (int i = 0; i < n; ++i) {
+            double ai = a[i];
+            if (fabs(ai) < tol) ai = ai < 0.0 ? -tol : tol;
+            a[i] = 1.0 / ai;
+        }
+    }
+    for (int i = threadIdx.x; i < n; i += 32) x[i] = hash_unit(static_cast<unsigned>(j) + 1u, i);
+    __syncwarp();
+    for (int it = 0; it < 3; ++it) {
         if (threadIdx.x == 0) {
-            // LU with partial pivoting of T - lam I (LAPACK dlagtf scheme)
-            for (int i = 0; i < n; ++i) {
-                a[i] = dg[i] - lam;
-                b[i] = i + 1 < n ? eg[i] : 0.0;
-                c[i] = i + 1 < n ? eg[i] : 0.0;
-                dd[i] = 0.0;
-            }
             for (int k = 0; k + 1 < n; ++k) {
-                if (fabs(a[k]) >= fabs(c[k])) {
-                    const double mult = a[k] == 0.0 ? 0.0 : c[k] / a[k];
-                    c[k] = mult;
-                    a[k + 1] -= mult * b[k];
-                    piv[k] = 0;
+                if (piv[k]) {
+                    const double t = x[k];
+                    x[k] = x[k + 1];
+                    x[k + 1] = t - c[k] * x[k];
                 } else {
-                    const double mult = a[k] / c[k];
-                    a[k] = c[k];
-                    const double tmp = a[k + 1];
-                    a[k + 1] = b[k] - mult * tmp;
-                    if (k + 2 < n) {
-                        dd[k] = b[k + 1];
-                        b[k + 1] = -mult * dd[k];
-                    }
-                    b[k] = tmp;
-                    c[k] = mult;
-                    piv[k] = 1;
+                    x[k + 1] -= c[k] * x[k];
                 }
             }
-            for (int i = 0; i < n; ++i)
-                if (fabs(a[i]) < tol) a[i] = a[i] < 0.0 ? -tol : tol;
+            double x1 = 0.0, x2 = 0.0;
+            for (int k = n - 1; k >= 0; --k) {
+                double t = x[k] - b[k] * x1 - dd[k] * x2;
+                t *= a[k];
+                if (fabs(t) > 1e150) {  // rescale the partial solution
+                    for (int q = k + 1; q < n; ++q) x[q] *= 1e-150;
+                    t *= 1e-150;
+                    x1 *= 1e-150;
+                }
+                x[k] = t;
+                x2 = x1;
+                x1 = t;
+            }
         }
-        for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = hash_unit(static_cast<unsigned>(j), i);
-        __syncthreads();
-        for (int it = 0; it < 4; ++it) {
-            if (threadIdx.x == 0) {
-                // apply L^{-1} (with the recorded interchanges), then U^{-1}
-                for (int k = 0; k + 1 < n; ++k) {
-                    if (piv[k]) {
-                        const double t = x[k];
-                        x[k] = x[k + 1];
-                        x[k + 1] = t - c[k] * x[k];
-                    } else {
-                        x[k + 1] -= c[k] * x[k];
-                    }
-                }
-                double scale = 1.0;
-                for (int k = n - 1; k >= 0; --k) {
-                    double t = x[k];
-                    if (k + 1 < n) t -= b[k] * x[k + 1];
-                    if (k + 2 < n) t -= dd[k] * x[k + 2];
-                    t /= a[k];
-                    x[k] = t;
-                    if (fabs(t) > 1e150) {  // rescale the partial solution
-                        for (int q = k; q < n; ++q) x[q] *= 1e-150;
-                        scale *= 1e-150;
-                    }
-                }
-                (void)scale;
-            }
-            __syncthreads();
-            // normalise, then orthogonalise against earlier members of the cluster
-            double s = 0.0;
-            for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i] * x[i];
-            double inv = 1.0 / sqrt(block_sum(s, red));
-            for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] *= inv;
-            __syncthreads();
+        __syncwarp();
+        double s = 0.0;
+        for (int i = threadIdx.x; i < n; i += 32) s += x[i] * x[i];
+        const double inv = 1.0 / sqrt(warp_sum(s));
+        for (int i = threadIdx.x; i < n; i += 32) x[i] *= inv;
+        __syncwarp();
+    }
+    for (int i = threadIdx.x; i < n; i += 32) Z[static_cast<size_t>(j) * n + i] = x[i];
+}
+
+// modified Gram-Schmidt inside each tight cluster (one CTA per cluster)
+__global__ void cluster_mgs_kernel(const int* __restrict__ clusters, int n, double* __restrict__ Z) {
+    __shared__ double red[32];
+    const int j0 = clusters[2 * blockIdx.x], j1 = clusters[2 * blockIdx.x + 1];
+    for (int j = j0; j < j1; ++j) {
+        double* zj = Z + static_cast<size_t>(j) * n;
+        for (int pass = 0; pass < 2; ++pass)
             for (int q = j0; q < j; ++q) {
                 const double* zq = Z + static_cast<size_t>(q) * n;
                 double dt = 0.0;
-                for (int i = threadIdx.x; i < n; i += blockDim.x) dt += zq[i] * x[i];
+                for (int i = threadIdx.x; i < n; i += blockDim.x) dt += zq[i] * zj[i];
                 dt = block_sum(dt, red);
-                for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] -= dt * zq[i];
+                for (int i = threadIdx.x; i < n; i += blockDim.x) zj[i] -= dt * zq[i];
                 __syncthreads();
             }
-            s = 0.0;
-            for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i] * x[i];
-            inv = 1.0 / sqrt(block_sum(s, red));
-            for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] *= inv;
-            __syncthreads();
-        }
-        for (int i = threadIdx.x; i < n; i += blockDim.x) Z[static_cast<size_t>(j) * n + i] = x[i];
+        double s = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) s += zj[i] * zj[i];
+        const double inv = 1.0 / sqrt(block_sum(s, red));
+        for (int i = threadIdx.x; i < n; i += blockDim.x) zj[i] *= inv;
         __syncthreads();
     }
 }
 
-// U (row-major n x r) = H_0 ... H_{n-3} Z; warp per column
-__global__ void backtransform_kernel(const double* __restrict__ V, const double* __restrict__ tau, int n, int r,
-                                     const double* __restrict__ Z, double* __restrict__ U) {
+// U (row-major n x r) = H_0 ... H_{n-3} Z.  Each CTA owns up to 8 columns
+// (one per warp, 32 entries per lane in registers); reflectors are staged in
+// shared memory 16 at a time, applied from the last to the first.
+constexpr int kBtChunk = 16;
+__global__ void __launch_bounds__(256) backtransform_kernel(const double* __restrict__ V,
+                                                            const double* __restrict__ tau, int n, int r,
+                                                            const double* __restrict__ Z, double* __restrict__ U) {
+    extern __shared__ double sv[];  // kBtChunk x n
     const int lane = threadIdx.x & 31;
     const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (col >= r) return;
-    double z[32];  // n <= 1024: 32 entries per lane (entry i = lane + 32 q)
+    const bool active = col < r;
+    double z[32];
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
         const int i = lane + 32 * q;
-        z[q] = i < n ? Z[static_cast<size_t>(col) * n + i] : 0.0;
+        z[q] = (active && i < n) ? Z[static_cast<size_t>(col) * n + i] : 0.0;
     }
-    for (int k = n - 3; k >= 0; --k) {
-        const double t = tau[k];
-        if (t == 0.0) continue;
-        const double* vk = V + static_cast<size_t>(k) * n;
-        double s = 0.0;
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const int i = lane + 32 * q;
-            if (i > k && i < n) s += vk[i] * z[q];
+    const int last = n - 3;
+    for (int hi = last; hi >= 0; hi -= kBtChunk) {
+        const int lo = max(0, hi - kBtChunk + 1);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < (hi - lo + 1) * n; idx += blockDim.x) {
+            const int kk = lo + idx / n, i = idx % n;
+            sv[(kk - lo) * n + i] = i > kk ? V[static_cast<size_t>(kk) * n + i] : 0.0;
         }
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        s *= t;
+        __syncthreads();
+        if (!active) continue;
+        for (int k = hi; k >= lo; --k) {
+            const double t = tau[k];
+            if (t == 0.0) continue;
+            const double* vk = sv + (k - lo) * n;
+            double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const int i = lane + 32 * q;
-            if (i > k && i < n) z[q] -= s * vk[i];
+            for (int q = 0; q < 32; ++q) {
+                const int i = lane + 32 * q;
+                if (i < n) s += vk[i] * z[q];
+            }
+            s = warp_sum(s) * t;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+                const int i = lane + 32 * q;
+                if (i < n) z[q] -= s * vk[i];
+            }
         }
     }
+    if (!active) return;
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
         const int i = lane + 32 * q;
@@ -390,22 +536,19 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
     const int n = static_cast<int>(n64);
     if (n64 > 1024) throw Error("sthosvd: device eigensolver supports mode sizes up to 1024");
     w.n = n64;
-    w.a = DevBuf<double>(n64 * n64, s);
     w.d = DevBuf<double>(n64, s);
     w.e = DevBuf<double>(n64 + 1, s);
     w.tau = DevBuf<double>(n64 + 1, s);
     w.evals = DevBuf<double>(n64, s);
-    DevBuf<double> V(n64 * n64, s), P(n64, s);
-    w.z = std::move(V);
-    TCB_CUDA(cudaMemcpyAsync(w.a.p, A, n64 * n64 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    w.z = DevBuf<double>(n64 * n64, s);  // Householder vectors
     w.tau.zero();
+    w.e.zero();
     if (n == 1) {
         TCB_CUDA(cudaMemcpyAsync(w.d.p, A, sizeof(double), cudaMemcpyDeviceToDevice, s));
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(kCluster);
         cfg.blockDim = dim3(kTriThreads);
-        cfg.dynamicSmemBytes = (2 * n + 32) * sizeof(double);
         cfg.stream = s;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -414,11 +557,27 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        TCB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_kernel, w.a.p, n, w.d.p, w.e.p, w.z.p, w.tau.p, P.p));
+        if (n <= kDsmemMaxN) {
+            const int nloc = (n + kCluster - 1) / kCluster;
+            const size_t smem = (static_cast<size_t>(nloc) * n + 4 * n + 32) * sizeof(double);
+            static bool attr = [] {
+                cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                return true;
+            }();
+            (void)attr;
+            cfg.dynamicSmemBytes = smem;
+            TCB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_dsmem, A, n, w.d.p, w.e.p, w.z.p, w.tau.p));
+        } else {
+            w.a = DevBuf<double>(n64 * n64, s);
+            DevBuf<double> P(n64, s);
+            TCB_CUDA(cudaMemcpyAsync(w.a.p, A, n64 * n64 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            cfg.dynamicSmemBytes = (2 * n + 32) * sizeof(double);
+            TCB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_global, w.a.p, n, w.d.p, w.e.p, w.z.p, w.tau.p, P.p));
+        }
         count_launch();
     }
-    const int bthreads = 128;
-    bisect_kernel<<<cdiv(n64, bthreads), bthreads, 2 * n * sizeof(double), s>>>(w.d.p, w.e.p, n, w.evals.p);
+    const int wpb = 8;
+    multisect_kernel<<<cdiv(n64, wpb), 32 * wpb, 2 * n * sizeof(double), s>>>(w.d.p, w.e.p, n, w.evals.p);
     count_launch();
     TCB_LAUNCH();
     std::vector<double> ev(n64);
@@ -433,7 +592,7 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
     std::vector<double> ev(w.n), d(w.n), e(w.n + 1);
     w.evals.download(ev.data(), w.n);
     w.d.download(d.data(), w.n);
-    w.e.download(e.data(), w.n > 1 ? w.n - 1 : 0);
+    w.e.download(e.data(), w.n + 1);
     TCB_CUDA(cudaStreamSynchronize(s));
     double tnorm = 0.0;
     for (int i = 0; i < n; ++i) {
@@ -441,20 +600,53 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
         tnorm = std::max(tnorm, rr);
     }
     if (!(tnorm > 0.0)) tnorm = 1.0;  // zero matrix: any orthonormal basis is an eigenbasis
-    const double ortol = 1e-3 * tnorm;
-    std::vector<int> cl{0};
-    for (int j = 1; j < r; ++j)
-        if (ev[j - 1] - ev[j] > ortol) cl.push_back(j);
-    cl.push_back(r);
-    DevBuf<int> clb(cl.size(), s);
-    clb.upload(cl.data(), cl.size());
+    // tight clusters: consecutive eigenvalues closer than 1e-6 ||T||; their
+    // vectors are orthogonalised against each other after inverse iteration
+    const double ctol = 1e-6 * tnorm;
+    std::vector<double> shift(r);
+    std::vector<int> clusters;
+    int start = 0;
+    for (int j = 0; j < r; ++j) {
+        shift[j] = ev[j];
+        if (j > 0 && ev[j - 1] - ev[j] <= ctol) {
+            const double pertol = 10.0 * DBL_EPSILON * std::fabs(ev[j]);
+            if (shift[j - 1] - shift[j] < pertol) shift[j] = shift[j - 1] - pertol;
+        } else {
+            if (j - start >= 2) {
+                clusters.push_back(start);
+                clusters.push_back(j);
+            }
+            start = j;
+        }
+    }
+    if (r - start >= 2) {
+        clusters.push_back(start);
+        clusters.push_back(r);
+    }
+    DevBuf<double> dsh(r, s);
+    dsh.upload(shift.data(), r);
     DevBuf<double> Z(static_cast<u64>(n) * r, s);
-    const size_t smem = (5 * n + 32) * sizeof(double) + n * sizeof(int);
-    invit_kernel<<<static_cast<unsigned>(cl.size() - 1), 256, smem, s>>>(w.d.p, w.e.p, n, w.evals.p, clb.p, tnorm,
-                                                                         Z.p);
-    backtransform_kernel<<<cdiv(r64, 4), 128, 0, s>>>(w.z.p, w.tau.p, n, r, Z.p, U);
-    count_launch(2);
+    const size_t smem = 5 * n * sizeof(double) + n * sizeof(int);
+    invit_kernel<<<static_cast<unsigned>(r), 32, smem, s>>>(w.d.p, w.e.p, n, dsh.p, DBL_EPSILON * tnorm, Z.p);
+    count_launch();
+    if (!clusters.empty()) {
+        DevBuf<int> dcl(clusters.size(), s);
+        dcl.upload(clusters.data(), clusters.size());
+        cluster_mgs_kernel<<<static_cast<unsigned>(clusters.size() / 2), 256, 0, s>>>(dcl.p, n, Z.p);
+        count_launch();
+        TCB_CUDA(cudaStreamSynchronize(s));
+    }
+    const size_t btsmem = static_cast<size_t>(kBtChunk) * n * sizeof(double);
+    static bool attr = [] {
+        cudaFuncSetAttribute(backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kBtChunk * 1024 * sizeof(double));
+        return true;
+    }();
+    (void)attr;
+    backtransform_kernel<<<cdiv(r64, 8), 256, btsmem, s>>>(w.z.p, w.tau.p, n, r, Z.p, U);
+    count_launch();
     TCB_LAUNCH();
+    TCB_CUDA(cudaStreamSynchronize(s));
 }
 
 void fix_column_signs(double* U, u64 n, u64 r, cudaStream_t s) {
