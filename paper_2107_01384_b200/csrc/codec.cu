@@ -253,41 +253,66 @@ __global__ void stats_serial_kernel(const u64* __restrict__ m, u64 n, u64 block,
     out[b] = r;
 }
 
+// One warp per (cum, need) pair: lanes classify 32 positions at a time and
+// the warp replays the serial accumulation over them in position order.
 __global__ void crossing_kernel(const u64* __restrict__ m, u64 lo, u64 hi, int p, int category,
                                 const double* __restrict__ cum0, const double* __restrict__ need, int npairs,
                                 u64* __restrict__ out) {
-    const int k = threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int k = threadIdx.x >> 5;
     if (k >= npairs) return;
     double cum = cum0[k];
     const double nd = need[k];
     u64 c = 0, nl = 0, nt = 0;
-    for (u64 i = lo; i < hi && cum < nd; ++i) {
-        const u64 v = m[i];
-        const int tb = top_bit(v);
-        if (category == 0) {
-            if (tb > p) continue;
-            if (tb == p) cum = __dadd_rn(cum, lead_gain(v, p));
-            ++c;
-        } else if (category == 1) {
-            if (tb <= p) continue;
-            cum = __dadd_rn(cum, trail_gain(v, p));
-            ++c;
-        } else {
-            if (tb > p) {
-                cum = __dadd_rn(cum, trail_gain(v, p));
-                ++nt;
+    for (u64 base = lo; base < hi && cum < nd; base += 32) {
+        const u64 i = base + lane;
+        int kind = 0;  // 0 skip, 1 counted without term, 2 counted with term; category 2: 3 trailing
+        double t = 0.0;
+        if (i < hi) {
+            const u64 v = m[i];
+            const int tb = top_bit(v);
+            if (category == 0) {
+                if (tb <= p) {
+                    kind = tb == p ? 2 : 1;
+                    if (tb == p) t = lead_gain(v, p);
+                }
+            } else if (category == 1) {
+                if (tb > p) {
+                    kind = 2;
+                    t = trail_gain(v, p);
+                }
             } else {
-                if (tb == p) cum = __dadd_rn(cum, lead_gain(v, p));
-                ++nl;
+                if (tb > p) {
+                    kind = 3;
+                    t = trail_gain(v, p);
+                } else {
+                    kind = tb == p ? 2 : 1;
+                    if (tb == p) t = lead_gain(v, p);
+                }
+            }
+        }
+        const int cnt = static_cast<int>(hi - base < 32 ? hi - base : 32);
+        for (int q = 0; q < cnt && cum < nd; ++q) {
+            const int kq = __shfl_sync(0xffffffffu, kind, q);
+            const double tq = __shfl_sync(0xffffffffu, t, q);
+            if (kq == 0) continue;
+            if (kq >= 2) cum = __dadd_rn(cum, tq);
+            if (category == 2) {
+                if (kq == 3) ++nt;
+                else ++nl;
+            } else {
+                ++c;
             }
         }
     }
-    if (category == 2) {
-        out[2 * k] = nl;
-        out[2 * k + 1] = nt;
-    } else {
-        out[2 * k] = c;
-        out[2 * k + 1] = 0;
+    if (lane == 0) {
+        if (category == 2) {
+            out[2 * k] = nl;
+            out[2 * k + 1] = nt;
+        } else {
+            out[2 * k] = c;
+            out[2 * k + 1] = 0;
+        }
     }
 }
 
@@ -835,7 +860,7 @@ void crossing_scan(const u64* m, u64 n, u64 block, u64 b, int plane, int categor
     c.upload(cum, npairs);
     nd.upload(need, npairs);
     const u64 lo = b * block, hi = std::min<u64>(n, lo + block);
-    crossing_kernel<<<1, 32, 0, s>>>(m, lo, hi, plane, category, c.p, nd.p, npairs, out.p);
+    crossing_kernel<<<1, 32 * npairs, 0, s>>>(m, lo, hi, plane, category, c.p, nd.p, npairs, out.p);
     count_launch();
     TCB_LAUNCH();
     out.download(counts_host, 2 * npairs);

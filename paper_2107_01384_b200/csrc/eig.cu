@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kCluster = 8;
 constexpr int kTriThreads = 512;
-constexpr int kDsmemMaxN = 448;
+constexpr int kDsmemMaxN = 440;
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -48,31 +48,45 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ---------------------------------------------------------------- tridiagonalisation (DSMEM)
-// Row i lives in CTA (i % 8), local slot i / 8.  Outputs d, e, V (reflector k
-// at V[k*n + i], i >= k+1), tau.
-__global__ void __launch_bounds__(kTriThreads) tridiag_dsmem(const double* __restrict__ Ag, int n,
-                                                            double* __restrict__ d, double* __restrict__ e,
-                                                            double* __restrict__ V, double* __restrict__ tau) {
+// Row i lives in CTA (i % 8), local slot i / 8.  Per step ONE cluster barrier:
+// every CTA pushes its p-slice (p = tau A v) and partial p.v into all CTAs'
+// double-buffered receive arrays, the owner of row k+1 pushes that row's
+// pre-update values, and after the barrier each CTA updates its own rows and
+// recomputes the updated row k+1 (the next column) locally with the same
+// floating-point expression the owner uses.  Outputs d, e, V (reflector k at
+// V[k*n + i], i >= k+1), tau.
+constexpr int kTdThreads = 256;
+constexpr int kTdWarps = kTdThreads / 32;
+__global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __restrict__ Ag, int n,
+                                                           double* __restrict__ d, double* __restrict__ e,
+                                                           double* __restrict__ V, double* __restrict__ tau) {
     cg::cluster_group cl = cg::this_cluster();
     const int rank = static_cast<int>(cl.block_rank());
     extern __shared__ double sm[];
     const int nloc = (n + kCluster - 1) / kCluster;
-    double* A = sm;                   // nloc x n
-    double* v = A + nloc * n;         // n
-    double* w = v + n;                // n
-    double* p = w + n;                // n (replicated, filled by DSMEM pushes)
-    double* rowk = p + n;             // n (replicated next column)
-    double* red = rowk + n;           // 32
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    double* A = sm;                         // nloc x n
+    double* v = A + nloc * n;               // n
+    double* w = v + n;                      // n
+    double* pbuf = w + n;                   // 2 x n   (remote-written)
+    double* obuf = pbuf + 2 * n;            // 2 x n   (remote-written old row k+1)
+    double* rowk = obuf + 2 * n;            // n
+    double* pvbuf = rowk + n;               // 2 x (kCluster * kTdWarps) (remote-written)
+    double* red = pvbuf + 2 * kCluster * kTdWarps;  // 32
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int li = 0; li < nloc; ++li) {
         const int gi = li * kCluster + rank;
         if (gi >= n) break;
         for (int j = threadIdx.x; j < n; j += blockDim.x) A[li * n + j] = Ag[static_cast<size_t>(gi) * n + j];
     }
     for (int j = threadIdx.x; j < n; j += blockDim.x) rowk[j] = Ag[j];
+    __syncthreads();
     cl.sync();
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1;
+        const int buf = k & 1;
+        double* p = pbuf + buf * n;
+        double* orow = obuf + buf * n;
+        double* pv = pvbuf + buf * kCluster * kTdWarps;
         double ss = 0.0;
         for (int i = threadIdx.x; i < m; i += blockDim.x) {
             const double x = rowk[k + 1 + i];
@@ -80,15 +94,12 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_dsmem(const double* __res
             ss += x * x;
         }
         const double alpha = sqrt(block_sum(ss, red));
-        const double x0 = v[0];
+        const double x0 = rowk[k + 1];
         const double beta = x0 >= 0.0 ? -alpha : alpha;
-        __syncthreads();
+        const double vv = 2.0 * alpha * (alpha + fabs(x0));  // |x - beta e1|^2
+        const double t = (alpha == 0.0 || vv == 0.0) ? 0.0 : 2.0 / vv;
         if (threadIdx.x == 0) v[0] = x0 - beta;
         __syncthreads();
-        double vv = 0.0;
-        for (int i = threadIdx.x; i < m; i += blockDim.x) vv += v[i] * v[i];
-        vv = block_sum(vv, red);
-        const double t = (alpha == 0.0 || vv == 0.0) ? 0.0 : 2.0 / vv;
         if (rank == 0) {
             if (threadIdx.x == 0) {
                 e[k] = t == 0.0 ? x0 : beta;
@@ -97,52 +108,50 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_dsmem(const double* __res
             }
             for (int i = threadIdx.x; i < m; i += blockDim.x) V[static_cast<size_t>(k) * n + k + 1 + i] = v[i];
         }
+        const int first = k + 1 + ((rank - (k + 1)) % kCluster + kCluster) % kCluster;
         if (t != 0.0) {
-            // p_i = t * A[i][k+1:] . v for owned rows, pushed to every CTA
-            for (int gi = k + 1 + ((rank - (k + 1)) % kCluster + kCluster) % kCluster + kCluster * warp; gi < n;
-                 gi += kCluster * nwarp) {
+            double pvw = 0.0;
+            for (int gi = first + kCluster * warp; gi < n; gi += kCluster * kTdWarps) {
                 const double* row = A + (gi / kCluster) * n + k + 1;
                 double s = 0.0;
                 for (int j = lane; j < m; j += 32) s += row[j] * v[j];
                 s = warp_sum(s) * t;
+                pvw += s * v[gi - k - 1];
                 if (lane < kCluster) *cl.map_shared_rank(p + gi, lane) = s;
             }
-            cl.sync();
-            double pv = 0.0;
-            for (int i = threadIdx.x; i < m; i += blockDim.x) {
-                const double q = p[k + 1 + i];
-                w[i] = q;
-                pv += q * v[i];
-            }
-            const double K = 0.5 * t * block_sum(pv, red);
-            for (int i = threadIdx.x; i < m; i += blockDim.x) w[i] -= K * v[i];
-            __syncthreads();
-            for (int gi = k + 1 + ((rank - (k + 1)) % kCluster + kCluster) % kCluster + kCluster * warp; gi < n;
-                 gi += kCluster * nwarp) {
-                double* row = A + (gi / kCluster) * n + k + 1;
-                const double vi = v[gi - k - 1], wi = w[gi - k - 1];
-                for (int j = lane; j < m; j += 32) row[j] -= vi * w[j] + wi * v[j];
-            }
+            if (lane < kCluster) *cl.map_shared_rank(pv + rank * kTdWarps + warp, lane) = pvw;
         }
-        __syncthreads();
-        // owner of row k+1 pushes it (the next column) to every CTA
-        if ((k + 1) % kCluster == rank) {
+        if ((k + 1) % kCluster == rank) {  // pre-update row k+1 to every CTA
             const double* row = A + ((k + 1) / kCluster) * n;
-            for (int idx = threadIdx.x; idx < kCluster * (n - k - 1); idx += blockDim.x) {
-                const int dst = idx / (n - k - 1), j = k + 1 + idx % (n - k - 1);
-                *cl.map_shared_rank(rowk + j, dst) = row[j];
+            for (int idx = threadIdx.x; idx < kCluster * m; idx += blockDim.x) {
+                const int dst = idx / m, j = k + 1 + idx % m;
+                *cl.map_shared_rank(orow + j, dst) = row[j];
             }
         }
         cl.sync();
-    }
-    if (rank == 0 && threadIdx.x == 0) {
-        if (n >= 2) {
-            d[n - 2] = rowk[n - 2];
-            e[n - 2] = rowk[n - 1];
+        if (t != 0.0) {
+            double sum = 0.0;
+            for (int q = 0; q < kCluster * kTdWarps; ++q) sum += pv[q];
+            const double K = 0.5 * t * sum;
+            for (int i = threadIdx.x; i < m; i += blockDim.x) w[i] = p[k + 1 + i] - K * v[i];
+            __syncthreads();
+            for (int gi = first + kCluster * warp; gi < n; gi += kCluster * kTdWarps) {
+                double* row = A + (gi / kCluster) * n + k + 1;
+                const double vi = v[gi - k - 1], wi = w[gi - k - 1];
+                for (int j = lane; j < m; j += 32) row[j] = row[j] - (vi * w[j] + wi * v[j]);
+            }
+            const double v0 = v[0], w0 = w[0];
+            for (int i = threadIdx.x; i < m; i += blockDim.x) rowk[k + 1 + i] = orow[k + 1 + i] - (v0 * w[i] + w0 * v[i]);
+        } else {
+            for (int i = threadIdx.x; i < m; i += blockDim.x) rowk[k + 1 + i] = orow[k + 1 + i];
         }
+        __syncthreads();
+    }
+    if (rank == 0 && threadIdx.x == 0 && n >= 2) {
+        d[n - 2] = rowk[n - 2];
+        e[n - 2] = rowk[n - 1];
     }
     if (n >= 2 && (n - 1) % kCluster == rank && threadIdx.x == 0) d[n - 1] = A[((n - 1) / kCluster) * n + n - 1];
-    if (n == 1 && rank == 0 && threadIdx.x == 0) d[0] = rowk[0];
 }
 
 // Same schedule with the matrix in L2 (n > kDsmemMaxN).
@@ -226,18 +235,28 @@ __device__ __forceinline__ double frcp(double q) {
     return y;
 }
 
-__device__ __forceinline__ int sturm(const double* d, const double* e2, int n, double x, double pivmin) {
-    double q = d[0] - x;
-    int c = q < 0.0;
-    for (int i = 1; i < n; ++i) {
-        if (fabs(q) < pivmin) q = -pivmin;
-        q = (d[i] - x) - e2[i - 1] * frcp(q);
-        c += q < 0.0;
+// Sturm counts (eigenvalues of T below x) for 4 probes at once: 4
+// independent division chains per thread hide the fp64 latency.
+__device__ __forceinline__ void sturm4(const double* d, const double* e2, int n, const double (&x)[4],
+                                       double pivmin, int (&c)[4]) {
+    double q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        q[u] = d[0] - x[u];
+        c[u] = q[u] < 0.0;
     }
-    return c;
+    for (int i = 1; i < n; ++i) {
+        const double di = d[i], ei = e2[i - 1];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+            q[u] = (di - x[u]) - ei * frcp(q[u]);
+            c[u] += q[u] < 0.0;
+        }
+    }
 }
 
-// one warp per eigenvalue (ascending index j), 32 probes per round
+// one warp per eigenvalue (ascending index j), 128 probes per round (7 bits)
 __global__ void multisect_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n,
                                  double* __restrict__ evals_desc) {
     extern __shared__ double sh_bis[];
@@ -269,18 +288,26 @@ __global__ void multisect_kernel(const double* __restrict__ dg, const double* __
     if (j >= n) return;
     double lo = bounds[0], hi = bounds[1];
     const double pivmin = bounds[2];
-    for (int it = 0; it < 24; ++it) {
-        const double width = hi - lo;
-        if (!(width > 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin)) break;
-        double x = lo + width * (static_cast<double>(lane + 1) / 33.0);
-        x = fmin(fmax(x, lo), hi);
-        const bool above = sturm(d, e2, n, x, pivmin) > j;  // x is above eigenvalue j
-        const unsigned ball = __ballot_sync(0xffffffffu, above);
-        const int first = ball ? __ffs(ball) - 1 : 32;
-        const double xh = __shfl_sync(0xffffffffu, x, first < 32 ? first : 31);
-        const double xl = __shfl_sync(0xffffffffu, x, first > 0 ? first - 1 : 0);
-        const double nlo = first > 0 ? xl : lo;
-        const double nhi = first < 32 ? xh : hi;
+    auto probe = [&](int idx) { return fmin(fmax(lo + (hi - lo) * (static_cast<double>(idx + 1) / 129.0), lo), hi); };
+    for (int it = 0; it < 16; ++it) {
+        if (!(hi - lo > 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin)) break;
+        double x[4];
+        int c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = probe(4 * lane + u);
+        sturm4(d, e2, n, x, pivmin, c);
+        unsigned m4 = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) m4 |= (c[u] > j ? 1u : 0u) << u;
+        const unsigned ball = __ballot_sync(0xffffffffu, m4 != 0);
+        int first = 128;
+        if (ball) {
+            const int fl = __ffs(ball) - 1;
+            const unsigned fm = __shfl_sync(0xffffffffu, m4, fl);
+            first = 4 * fl + __ffs(fm) - 1;
+        }
+        const double nhi = first < 128 ? probe(first) : hi;
+        const double nlo = first > 0 ? probe(first - 1) : lo;
         if (nlo == lo && nhi == hi) break;
         lo = nlo;
         hi = nhi;
@@ -324,13 +351,13 @@ __global__ void __launch_bounds__(32) invit_kernel(const double* __restrict__ dg
             double ak = a[k];
             if (fabs(ak) >= fabs(c[k])) {
                 if (fabs(ak) < tol) ak = ak < 0.0 ? -tol : tol;
-                const double mult = c[k] / ak;
+                const double mult = c[k] * frcp(ak);
                 c[k] = mult;
                 a[k + 1] -= mult * b[k];
                 piv[k] = 0;
                 a[k] = ak;
             } else {
-                const double mult = ak / c[k];
+                const double mult = ak * frcp(c[k]);
                 a[k] = c[k];
                 const double tmp = a[k + 1];
                 a[k + 1] = b[k] - mult * tmp;
@@ -346,7 +373,7 @@ __global__ void __launch_bounds__(32) invit_kernel(const double* __restrict__ dg
         for (int i = 0; i < n; ++i) {
             double ai = a[i];
             if (fabs(ai) < tol) ai = ai < 0.0 ? -tol : tol;
-            a[i] = 1.0 / ai;
+            a[i] = frcp(ai);
         }
     }
     for (int i = threadIdx.x; i < n; i += 32) x[i] = hash_unit(static_cast<unsigned>(j) + 1u, i);
@@ -410,45 +437,46 @@ __global__ void cluster_mgs_kernel(const int* __restrict__ clusters, int n, doub
 }
 
 // U (row-major n x r) = H_0 ... H_{n-3} Z.  Each CTA owns up to 8 columns
-// (one per warp, 32 entries per lane in registers); reflectors are staged in
-// shared memory 16 at a time, applied from the last to the first.
+// (one per warp, NQ entries per lane in registers); reflectors and their taus
+// are staged in shared memory 16 at a time, applied from the last to the first.
 constexpr int kBtChunk = 16;
+template <int NQ>
 __global__ void __launch_bounds__(256) backtransform_kernel(const double* __restrict__ V,
                                                             const double* __restrict__ tau, int n, int r,
                                                             const double* __restrict__ Z, double* __restrict__ U) {
-    extern __shared__ double sv[];  // kBtChunk x n
+    extern __shared__ double sv[];  // kBtChunk x n reflectors, then kBtChunk taus
+    double* stau = sv + kBtChunk * n;
     const int lane = threadIdx.x & 31;
     const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const bool active = col < r;
-    double z[32];
+    double z[NQ];
 #pragma unroll
-    for (int q = 0; q < 32; ++q) {
+    for (int q = 0; q < NQ; ++q) {
         const int i = lane + 32 * q;
         z[q] = (active && i < n) ? Z[static_cast<size_t>(col) * n + i] : 0.0;
     }
-    const int last = n - 3;
-    for (int hi = last; hi >= 0; hi -= kBtChunk) {
+    for (int hi = n - 3; hi >= 0; hi -= kBtChunk) {
         const int lo = max(0, hi - kBtChunk + 1);
         __syncthreads();
-        for (int idx = threadIdx.x; idx < (hi - lo + 1) * n; idx += blockDim.x) {
-            const int kk = lo + idx / n, i = idx % n;
-            sv[(kk - lo) * n + i] = i > kk ? V[static_cast<size_t>(kk) * n + i] : 0.0;
-        }
+        for (int kk = lo; kk <= hi; ++kk)
+            for (int i = threadIdx.x; i < n; i += blockDim.x)
+                sv[(kk - lo) * n + i] = i > kk ? V[static_cast<size_t>(kk) * n + i] : 0.0;
+        if (threadIdx.x <= hi - lo) stau[threadIdx.x] = tau[lo + threadIdx.x];
         __syncthreads();
         if (!active) continue;
         for (int k = hi; k >= lo; --k) {
-            const double t = tau[k];
+            const double t = stau[k - lo];
             if (t == 0.0) continue;
             const double* vk = sv + (k - lo) * n;
             double s = 0.0;
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
+            for (int q = 0; q < NQ; ++q) {
                 const int i = lane + 32 * q;
                 if (i < n) s += vk[i] * z[q];
             }
             s = warp_sum(s) * t;
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
+            for (int q = 0; q < NQ; ++q) {
                 const int i = lane + 32 * q;
                 if (i < n) z[q] -= s * vk[i];
             }
@@ -456,7 +484,7 @@ __global__ void __launch_bounds__(256) backtransform_kernel(const double* __rest
     }
     if (!active) return;
 #pragma unroll
-    for (int q = 0; q < 32; ++q) {
+    for (int q = 0; q < NQ; ++q) {
         const int i = lane + 32 * q;
         if (i < n) U[static_cast<size_t>(i) * r + col] = z[q];
     }
@@ -559,7 +587,8 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
         cfg.numAttrs = 1;
         if (n <= kDsmemMaxN) {
             const int nloc = (n + kCluster - 1) / kCluster;
-            const size_t smem = (static_cast<size_t>(nloc) * n + 4 * n + 32) * sizeof(double);
+            const size_t smem = (static_cast<size_t>(nloc) * n + 7 * n + 2 * kCluster * kTdWarps + 32) * sizeof(double);
+            cfg.blockDim = dim3(kTdThreads);
             static bool attr = [] {
                 cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
                 return true;
@@ -636,14 +665,18 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
         count_launch();
         TCB_CUDA(cudaStreamSynchronize(s));
     }
-    const size_t btsmem = static_cast<size_t>(kBtChunk) * n * sizeof(double);
+    const size_t btsmem = static_cast<size_t>(kBtChunk) * (n + 1) * sizeof(double);
     static bool attr = [] {
-        cudaFuncSetAttribute(backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kBtChunk * 1024 * sizeof(double));
+        const int mx = kBtChunk * 1025 * sizeof(double);
+        cudaFuncSetAttribute(backtransform_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(backtransform_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(backtransform_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         return true;
     }();
     (void)attr;
-    backtransform_kernel<<<cdiv(r64, 8), 256, btsmem, s>>>(w.z.p, w.tau.p, n, r, Z.p, U);
+    if (n <= 256) backtransform_kernel<8><<<cdiv(r64, 8), 256, btsmem, s>>>(w.z.p, w.tau.p, n, r, Z.p, U);
+    else if (n <= 512) backtransform_kernel<16><<<cdiv(r64, 8), 256, btsmem, s>>>(w.z.p, w.tau.p, n, r, Z.p, U);
+    else backtransform_kernel<32><<<cdiv(r64, 8), 256, btsmem, s>>>(w.z.p, w.tau.p, n, r, Z.p, U);
     count_launch();
     TCB_LAUNCH();
     TCB_CUDA(cudaStreamSynchronize(s));

@@ -19,23 +19,26 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// dev[a*rl+b] = |sum_i U_a U_b - delta|, computed in double or float
+// dev[a*rl+b] = |sum_i U_a U_b - delta|, computed in double or float; warp per pair
 __global__ void orth_kernel(const double* __restrict__ U, u64 n, u64 r, const u64* __restrict__ live, u64 rl,
                             int as_float, double* __restrict__ dev) {
-    const u64 t = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const u64 t = static_cast<u64>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (t >= rl * rl) return;
     const u64 a = live[t / rl], b = live[t % rl];
     double out;
     if (as_float) {
         float s = 0.f;
-        for (u64 i = 0; i < n; ++i) s += static_cast<float>(U[i * r + a]) * static_cast<float>(U[i * r + b]);
+        for (u64 i = lane; i < n; i += 32) s += static_cast<float>(U[i * r + a]) * static_cast<float>(U[i * r + b]);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         out = fabsf(s - (a == b ? 1.f : 0.f));
     } else {
         double s = 0.0;
-        for (u64 i = 0; i < n; ++i) s += U[i * r + a] * U[i * r + b];
+        for (u64 i = lane; i < n; i += 32) s += U[i * r + a] * U[i * r + b];
+        s = warp_sum(s);
         out = fabs(s - (a == b ? 1.0 : 0.0));
     }
-    dev[t] = out;
+    if (lane == 0) dev[t] = out;
 }
 
 __global__ void gather_cols(const double* __restrict__ U, u64 n, u64 r, const u64* __restrict__ live, u64 rl,
@@ -111,61 +114,89 @@ __global__ void stream_kernel(const double* __restrict__ V, u64 n, u64 rl, const
     for (u64 i = j + 1 + threadIdx.x; i < n; i += blockDim.x) st[off + (i - j - 1)] = V[j * n + i] * scales[j];
 }
 
-// decoded stream -> reflector columns (column-major), diagonal from unit norm
-__global__ void refl_from_stream(const u64* __restrict__ dec, const u8* __restrict__ neg, int k, u64 n, u64 rl,
-                                 const double* __restrict__ scales, double* __restrict__ Vd, int* __restrict__ err) {
+// decoded stream at candidate plane P[blockIdx.y] -> reflector columns
+// (column-major n x rl per plane), diagonal rebuilt from the unit norm
+// (factor_codec.cpp:59-77, 119-149).  Fixed-plane decoding: coefficients with
+// msb >= P keep planes >= P plus the midpoint (core_codec.cpp:344-367).
+__global__ void refl_from_stream(const u64* __restrict__ mag, const u8* __restrict__ neg, int k, u64 n, u64 rl,
+                                 const int* __restrict__ planes, const double* __restrict__ scales,
+                                 double* __restrict__ Vd, int* __restrict__ err) {
     const int lane = threadIdx.x & 31;
     const u64 j = static_cast<u64>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (j >= rl) return;
+    const int P = planes[blockIdx.y];
+    double* V = Vd + static_cast<u64>(blockIdx.y) * n * rl;
     const u64 off = j * n - j * (j + 1) / 2;
     double below = 0.0;
     for (u64 i = lane; i < n; i += 32) {
         double v = 0.0;
         if (i > j) {
             const u64 s = off + (i - j - 1);
-            double val = scalbn(__ull2double_rn(dec[s]), -k);
+            const u64 m = mag[s];
+            u64 dec = 0;
+            if (m != 0 && 63 - __clzll(static_cast<long long>(m)) >= P) {
+                dec = (m >> P) << P;
+                if (P >= 1) dec += u64{1} << (P - 1);
+            }
+            double val = scalbn(__ull2double_rn(dec), -k);
             if (neg[s]) val = -val;
             v = val / scales[j];
             below += v * v;
         }
-        Vd[j * n + i] = v;
+        V[j * n + i] = v;
     }
     below = warp_sum(below);
     if (lane == 0) {
         if (below >= 1.0) *err = 1;
-        Vd[j * n + j] = sqrt(fmax(0.0, 1.0 - below));
+        V[j * n + j] = sqrt(fmax(0.0, 1.0 - below));
     }
 }
 
-// X(:, c) = H_0 ... H_{rl-1} e_c ; residual_c = |X(:,c) - flip_c U(:, live_c)|^2
-__global__ void expand_residual(const double* __restrict__ Vd, u64 n, u64 rl, const double* __restrict__ U, u64 r,
-                                const u64* __restrict__ live, const signed char* __restrict__ flips,
-                                double* __restrict__ res) {
+// X(:, c) = H_0 ... H_{rl-1} e_c ; res[c] = |X(:,c) - flip_c U(:, live_c)|^2.
+// Warp per column, NQ entries per lane; reflectors staged 16 at a time in smem.
+constexpr int kExChunk = 16;
+template <int NQ>
+__global__ void __launch_bounds__(256) expand_residual(const double* __restrict__ Vd, u64 n, u64 rl,
+                                                       const double* __restrict__ U, u64 r,
+                                                       const u64* __restrict__ live,
+                                                       const signed char* __restrict__ flips,
+                                                       double* __restrict__ res) {
+    extern __shared__ double sv[];
     const int lane = threadIdx.x & 31;
     const u64 c = static_cast<u64>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (c >= rl) return;
-    double x[32];
+    const double* V = Vd + static_cast<u64>(blockIdx.y) * n * rl;
+    const bool active = c < rl;
+    double x[NQ];
 #pragma unroll
-    for (int q = 0; q < 32; ++q) x[q] = (static_cast<u64>(lane + 32 * q) == c) ? 1.0 : 0.0;
-    for (u64 jj = rl; jj-- > 0;) {
-        const double* v = Vd + jj * n;
-        double t = 0.0;
+    for (int q = 0; q < NQ; ++q) x[q] = (static_cast<u64>(lane + 32 * q) == c) ? 1.0 : 0.0;
+    for (long long hi = static_cast<long long>(rl) - 1; hi >= 0; hi -= kExChunk) {
+        const long long lo = hi - kExChunk + 1 < 0 ? 0 : hi - kExChunk + 1;
+        __syncthreads();
+        for (long long jj = lo; jj <= hi; ++jj)
+            for (u64 i = threadIdx.x; i < n; i += blockDim.x) sv[(jj - lo) * n + i] = V[jj * n + i];
+        __syncthreads();
+        if (!active) continue;
+        for (long long jj = hi; jj >= lo; --jj) {
+            const double* v = sv + (jj - lo) * n;
+            double t = 0.0;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const u64 i = lane + 32 * q;
-            if (i >= jj && i < n) t += v[i] * x[q];
-        }
-        t = warp_sum(t);
+            for (int q = 0; q < NQ; ++q) {
+                const u64 i = lane + 32 * q;
+                if (i >= static_cast<u64>(jj) && i < n) t += v[i] * x[q];
+            }
+            t = warp_sum(t);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const u64 i = lane + 32 * q;
-            if (i >= jj && i < n) x[q] -= 2.0 * t * v[i];
+            for (int q = 0; q < NQ; ++q) {
+                const u64 i = lane + 32 * q;
+                if (i >= static_cast<u64>(jj) && i < n) x[q] -= 2.0 * t * v[i];
+            }
         }
     }
+    if (!active) return;
     const double f = flips[c] < 0 ? -1.0 : 1.0;
     double s = 0.0;
 #pragma unroll
-    for (int q = 0; q < 32; ++q) {
+    for (int q = 0; q < NQ; ++q) {
         const u64 i = lane + 32 * q;
         if (i < n) {
             const double dlt = x[q] - f * U[i * r + live[c]];
@@ -173,7 +204,7 @@ __global__ void expand_residual(const double* __restrict__ Vd, u64 n, u64 rl, co
         }
     }
     s = warp_sum(s);
-    if (lane == 0) res[c] = s;
+    if (lane == 0) res[static_cast<u64>(blockIdx.y) * rl + c] = s;
 }
 
 }  // namespace
@@ -185,7 +216,7 @@ double orth_deviation(const double* U, u64 n, u64 r, const std::vector<u64>& liv
     DevBuf<u64> dl(rl, s);
     dl.upload(live.data(), rl);
     DevBuf<double> dev(rl * rl, s);
-    orth_kernel<<<cdiv(rl * rl, 128), 128, 0, s>>>(U, n, r, dl.p, rl, as_float ? 1 : 0, dev.p);
+    orth_kernel<<<cdiv(rl * rl, 8), 256, 0, s>>>(U, n, r, dl.p, rl, as_float ? 1 : 0, dev.p);
     count_launch();
     TCB_LAUNCH();
     const double mx = max_abs(dev.p, rl * rl, s);
@@ -235,19 +266,34 @@ void reflector_stream(const double* V, u64 n, u64 rl, const double* scales_dev, 
     TCB_LAUNCH();
 }
 
-std::vector<double> factor_residuals(const u64* dec, const u8* neg, int k, u64 n, u64 r,
+std::vector<double> factor_residuals(const u64* mag, const u8* neg, int k, u64 n, u64 r,
                                      const std::vector<u64>& live, const double* scales_dev, const double* U,
-                                     const signed char* flips_dev, cudaStream_t s) {
+                                     const signed char* flips_dev, const std::vector<int>& planes, cudaStream_t s) {
     ProfScope prof_scope(kFactor, s);
     const u64 rl = live.size();
+    const unsigned np = static_cast<unsigned>(planes.size());
     if (n > 1024) throw Error("factor codec: mode sizes above 1024 unsupported on the device path");
     DevBuf<u64> dl(rl, s);
     dl.upload(live.data(), rl);
-    DevBuf<double> Vd(n * rl, s), res(rl, s);
+    DevBuf<int> dp(np, s);
+    dp.upload(planes.data(), np);
+    DevBuf<double> Vd(n * rl * np, s), res(rl * np, s);
     DevBuf<int> err(1, s);
     err.zero();
-    refl_from_stream<<<cdiv(rl, 4), 128, 0, s>>>(dec, neg, k, n, rl, scales_dev, Vd.p, err.p);
-    expand_residual<<<cdiv(rl, 4), 128, 0, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
+    refl_from_stream<<<dim3(cdiv(rl, 4), np), 128, 0, s>>>(mag, neg, k, n, rl, dp.p, scales_dev, Vd.p, err.p);
+    const size_t smem = static_cast<size_t>(kExChunk) * n * sizeof(double);
+    static bool attr = [] {
+        const int mx = kExChunk * 1024 * sizeof(double);
+        cudaFuncSetAttribute(expand_residual<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(expand_residual<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(expand_residual<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        return true;
+    }();
+    (void)attr;
+    const dim3 grid(cdiv(rl, 8), np);
+    if (n <= 256) expand_residual<8><<<grid, 256, smem, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
+    else if (n <= 512) expand_residual<16><<<grid, 256, smem, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
+    else expand_residual<32><<<grid, 256, smem, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
     count_launch(2);
     TCB_LAUNCH();
     int e = 0;

@@ -135,10 +135,11 @@ __global__ void __launch_bounds__(256) syrk_kernel(const double* __restrict__ B,
 __global__ void syrk_reduce(const double* __restrict__ ws, int splits, int ntiles_lower, u64 rows,
                             double* __restrict__ G) {
     const int tile = blockIdx.x;
+    const int e0 = blockIdx.y * (GT * GT / 16), e1 = e0 + GT * GT / 16;
     int ti = 0;
     while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
     const int tj = tile - ti * (ti + 1) / 2;
-    for (int e = threadIdx.x; e < GT * GT; e += blockDim.x) {
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
         const int m = e / GT, n = e % GT;
         const u64 gi = static_cast<u64>(ti) * GT + m, gj = static_cast<u64>(tj) * GT + n;
         if (gi >= rows || gj >= rows || gj > gi) continue;
@@ -313,7 +314,7 @@ void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
     (void)attr;
     if (v16) syrk_kernel<true><<<grid, 256, smem, s>>>(B, rows, cols, kchunk, lower, ws.p);
     else syrk_kernel<false><<<grid, 256, smem, s>>>(B, rows, cols, kchunk, lower, ws.p);
-    syrk_reduce<<<lower, 256, 0, s>>>(ws.p, static_cast<int>(splits), lower, rows, G);
+    syrk_reduce<<<dim3(lower, 16), 256, 0, s>>>(ws.p, static_cast<int>(splits), lower, rows, G);
     count_launch(2);
     TCB_LAUNCH();
 }

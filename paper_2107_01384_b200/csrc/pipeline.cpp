@@ -235,28 +235,43 @@ FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<
     reflector_stream(V.p, n, rl, dsc.p, st.p, s);
     const double mx = cnt ? max_abs(st.p, cnt, s) : 0.0;
     out.k = mx > 0.0 ? 63 - std::ilogb(mx) : 0;
-    DevBuf<u64> mag(cnt, s), dec(cnt, s);
+    DevBuf<u64> mag(cnt, s);
     DevBuf<u8> neg(cnt, s);
     quantize_f64(st.p, cnt, out.k, mag.p, neg.p, s);
     int plane = std::clamp(core_step_log2 + out.k, 0, 63);
+    // The reference deepens the plane while the factor term exceeds the cap
+    // (factor_codec.cpp:218-243).  Terms for a window of candidate planes are
+    // evaluated in one batched launch; the host then replays the reference's
+    // deepening decisions over them.
+    std::vector<double> term_of(64, -1.0);
     while (true) {
-        EncodeOpts eo;
-        eo.coder = coder;
-        eo.split = false;
-        eo.fixed_plane = plane;
-        const PlanResult pl = plan_stream(mag.p, cnt, 0.0, eo, dec.p, s);
-        const auto res = factor_residuals(dec.p, neg.p, out.k, n, r, live, dsc.p, U, dfl.p, s);
-        out.term = 0.0;
-        for (u64 j = 0; j < rl; ++j) out.term += ln[j] * ln[j] * res[j];
-        if (out.term <= cap || plane == 0) {
-            out.stream = finalize_stream(mag.p, neg.p, cnt, pl, coder, cnt, s);
-            out.plane = plane;
-            return out;
+        if (term_of[plane] < 0.0) {
+            std::vector<int> cand;
+            for (int p = plane; p >= 0 && static_cast<int>(cand.size()) < 16; --p)
+                if (term_of[p] < 0.0) cand.push_back(p);
+            const auto res = factor_residuals(mag.p, neg.p, out.k, n, r, live, dsc.p, U, dfl.p, cand, s);
+            for (std::size_t c = 0; c < cand.size(); ++c) {
+                double t = 0.0;
+                for (u64 j = 0; j < rl; ++j) t += ln[j] * ln[j] * res[c * rl + j];
+                term_of[cand[c]] = t;
+            }
         }
+        out.term = term_of[plane];
+        if (out.term <= cap || plane == 0) break;
         const double excess = out.term / std::max(cap, 1e-300);
         const int stp = std::max(1, static_cast<int>(std::ceil(0.25 * std::log2(excess))));
         plane = std::max(0, plane - stp);
     }
+    PlanResult pl;  // fixed last plane: planes 63..plane in full (core_codec.cpp:328-391)
+    pl.block = default_block(cnt);
+    if (cnt > 0) {
+        pl.last_plane = plane;
+        pl.nplanes = 64 - plane;
+        pl.stops.assign(2 * ((cnt + pl.block - 1) / pl.block), kFull);
+    }
+    out.stream = finalize_stream(mag.p, neg.p, cnt, pl, coder, cnt, s);
+    out.plane = plane;
+    return out;
 }
 
 Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,

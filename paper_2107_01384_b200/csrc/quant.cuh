@@ -19,10 +19,11 @@ void householder(const double* U, u64 n, u64 r, const std::vector<u64>& live, do
                  cudaStream_t s);
 // weighted reflector stream: st[s] = V(i,j) * scale_j for j < rl, i > j (column-major)
 void reflector_stream(const double* V, u64 n, u64 rl, const double* scales_dev, double* st, cudaStream_t s);
-// decoded stream -> reflectors -> Householder expansion; returns per-live-column
-// sum_i (X(i,j) - flip_j U(i,live_j))^2 (host combines with the slice norms)
-std::vector<double> factor_residuals(const u64* dec, const u8* neg, int k, u64 n, u64 r,
+// For each candidate plane P: fixed-plane decoded stream -> reflectors ->
+// Householder expansion; returns res[plane_idx * rl + j] =
+// sum_i (X(i,j) - flip_j U(i,live_j))^2 (the host combines with the slice norms)
+std::vector<double> factor_residuals(const u64* mag, const u8* neg, int k, u64 n, u64 r,
                                      const std::vector<u64>& live, const double* scales_dev, const double* U,
-                                     const signed char* flips_dev, cudaStream_t s);
+                                     const signed char* flips_dev, const std::vector<int>& planes, cudaStream_t s);
 
 }  // namespace tcb
