@@ -48,13 +48,18 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ---------------------------------------------------------------- tridiagonalisation (DSMEM)
-// Row i lives in CTA (i % 8), local slot i / 8.  Per step ONE cluster barrier:
-// every CTA pushes its p-slice (p = tau A v) and partial p.v into all CTAs'
-// double-buffered receive arrays, the owner of row k+1 pushes that row's
-// pre-update values, and after the barrier each CTA updates its own rows and
-// recomputes the updated row k+1 (the next column) locally with the same
-// floating-point expression the owner uses.  Outputs d, e, V (reflector k at
-// V[k*n + i], i >= k+1), tau.
+// Row i lives in CTA (i % 8), local slot i / 8; the stored matrix stays
+// bitwise symmetric (every update is symmetric in (i, j)).  Per step k:
+//   A. every CTA derives alpha/beta/tau from the replicated column k (rowk),
+//      whose |x|^2 partials were accumulated while it was built;
+//   B. each CTA forms p_i = tau * A_i . v for its rows and pushes (p_i,
+//      A_i,k+1 = pre-update row k+1 by symmetry, partial p.v) into every CTA's
+//      double-buffered receive arrays over DSMEM;
+//   -- one cluster barrier --
+//   C. each CTA updates its rows with w = p - K v recomputed inline and
+//      rebuilds the updated row k+1 (next column) with the owner's exact
+//      expression; one CTA barrier.
+// Outputs d, e, V (reflector k at V[k*n + i], i >= k+1), tau.
 constexpr int kTdThreads = 256;
 constexpr int kTdWarps = kTdThreads / 32;
 __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __restrict__ Ag, int n,
@@ -64,92 +69,109 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
     const int rank = static_cast<int>(cl.block_rank());
     extern __shared__ double sm[];
     const int nloc = (n + kCluster - 1) / kCluster;
-    double* A = sm;                         // nloc x n
-    double* v = A + nloc * n;               // n
-    double* w = v + n;                      // n
-    double* pbuf = w + n;                   // 2 x n   (remote-written)
-    double* obuf = pbuf + 2 * n;            // 2 x n   (remote-written old row k+1)
-    double* rowk = obuf + 2 * n;            // n
-    double* pvbuf = rowk + n;               // 2 x (kCluster * kTdWarps) (remote-written)
-    double* red = pvbuf + 2 * kCluster * kTdWarps;  // 32
+    double* A = sm;                                  // nloc x n
+    double* pbuf = A + nloc * n;                     // 2 x n (remote-written p)
+    double* obuf = pbuf + 2 * n;                     // 2 x n (remote-written pre-update column k+1)
+    double* rbuf = obuf + 2 * n;                     // 2 x n (local replicated column k)
+    double* pvbuf = rbuf + 2 * n;                    // 2 x (kCluster * kTdWarps) (remote-written)
+    double* ssbuf = pvbuf + 2 * kCluster * kTdWarps; // 2 x kTdWarps (local)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int li = 0; li < nloc; ++li) {
         const int gi = li * kCluster + rank;
         if (gi >= n) break;
         for (int j = threadIdx.x; j < n; j += blockDim.x) A[li * n + j] = Ag[static_cast<size_t>(gi) * n + j];
     }
-    for (int j = threadIdx.x; j < n; j += blockDim.x) rowk[j] = Ag[j];
+    {
+        double ss = 0.0;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            const double x = Ag[j];
+            rbuf[j] = x;
+            if (j >= 1) ss += x * x;
+        }
+        ss = warp_sum(ss);
+        if (lane == 0) ssbuf[warp] = ss;
+    }
     __syncthreads();
     cl.sync();
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1;
         const int buf = k & 1;
+        const double* rowk = rbuf + buf * n;
+        double* rnext = rbuf + (buf ^ 1) * n;
         double* p = pbuf + buf * n;
         double* orow = obuf + buf * n;
         double* pv = pvbuf + buf * kCluster * kTdWarps;
         double ss = 0.0;
-        for (int i = threadIdx.x; i < m; i += blockDim.x) {
-            const double x = rowk[k + 1 + i];
-            v[i] = x;
-            ss += x * x;
-        }
-        const double alpha = sqrt(block_sum(ss, red));
+        for (int q = 0; q < kTdWarps; ++q) ss += ssbuf[buf * kTdWarps + q];
+        const double alpha = sqrt(ss);
         const double x0 = rowk[k + 1];
         const double beta = x0 >= 0.0 ? -alpha : alpha;
+        const double v0 = x0 - beta;
         const double vv = 2.0 * alpha * (alpha + fabs(x0));  // |x - beta e1|^2
         const double t = (alpha == 0.0 || vv == 0.0) ? 0.0 : 2.0 / vv;
-        if (threadIdx.x == 0) v[0] = x0 - beta;
-        __syncthreads();
         if (rank == 0) {
             if (threadIdx.x == 0) {
                 e[k] = t == 0.0 ? x0 : beta;
                 tau[k] = t;
                 d[k] = rowk[k];
             }
-            for (int i = threadIdx.x; i < m; i += blockDim.x) V[static_cast<size_t>(k) * n + k + 1 + i] = v[i];
+            for (int i = threadIdx.x; i < m; i += blockDim.x)
+                V[static_cast<size_t>(k) * n + k + 1 + i] = i == 0 ? v0 : rowk[k + 1 + i];
         }
         const int first = k + 1 + ((rank - (k + 1)) % kCluster + kCluster) % kCluster;
-        if (t != 0.0) {
-            double pvw = 0.0;
-            for (int gi = first + kCluster * warp; gi < n; gi += kCluster * kTdWarps) {
-                const double* row = A + (gi / kCluster) * n + k + 1;
-                double s = 0.0;
-                for (int j = lane; j < m; j += 32) s += row[j] * v[j];
+        double pvw = 0.0;
+        for (int gi = first + kCluster * warp; gi < n; gi += kCluster * kTdWarps) {
+            const double* row = A + (gi / kCluster) * n;
+            double s = 0.0;
+            if (t != 0.0) {
+                for (int j = k + 1 + lane; j < n; j += 32) s += row[j] * (j == k + 1 ? v0 : rowk[j]);
                 s = warp_sum(s) * t;
-                pvw += s * v[gi - k - 1];
-                if (lane < kCluster) *cl.map_shared_rank(p + gi, lane) = s;
+                pvw += s * (gi == k + 1 ? v0 : rowk[gi]);
             }
-            if (lane < kCluster) *cl.map_shared_rank(pv + rank * kTdWarps + warp, lane) = pvw;
-        }
-        if ((k + 1) % kCluster == rank) {  // pre-update row k+1 to every CTA
-            const double* row = A + ((k + 1) / kCluster) * n;
-            for (int idx = threadIdx.x; idx < kCluster * m; idx += blockDim.x) {
-                const int dst = idx / m, j = k + 1 + idx % m;
-                *cl.map_shared_rank(orow + j, dst) = row[j];
+            const double col = row[k + 1];
+            if (lane < kCluster) {
+                *cl.map_shared_rank(p + gi, lane) = s;
+                *cl.map_shared_rank(orow + gi, lane) = col;
             }
         }
+        if (lane < kCluster) *cl.map_shared_rank(pv + rank * kTdWarps + warp, lane) = pvw;
         cl.sync();
+        double K = 0.0;
         if (t != 0.0) {
-            double sum = 0.0;
-            for (int q = 0; q < kCluster * kTdWarps; ++q) sum += pv[q];
-            const double K = 0.5 * t * sum;
-            for (int i = threadIdx.x; i < m; i += blockDim.x) w[i] = p[k + 1 + i] - K * v[i];
-            __syncthreads();
-            for (int gi = first + kCluster * warp; gi < n; gi += kCluster * kTdWarps) {
-                double* row = A + (gi / kCluster) * n + k + 1;
-                const double vi = v[gi - k - 1], wi = w[gi - k - 1];
-                for (int j = lane; j < m; j += 32) row[j] = row[j] - (vi * w[j] + wi * v[j]);
-            }
-            const double v0 = v[0], w0 = w[0];
-            for (int i = threadIdx.x; i < m; i += blockDim.x) rowk[k + 1 + i] = orow[k + 1 + i] - (v0 * w[i] + w0 * v[i]);
-        } else {
-            for (int i = threadIdx.x; i < m; i += blockDim.x) rowk[k + 1 + i] = orow[k + 1 + i];
+            K = pv[lane] + pv[lane + 32];
+            K = 0.5 * t * warp_sum(K);
         }
+        auto vj = [&](int j) { return j == k + 1 ? v0 : rowk[j]; };
+        if (t != 0.0) {
+            for (int gi = first + kCluster * warp; gi < n; gi += kCluster * kTdWarps) {
+                double* row = A + (gi / kCluster) * n;
+                const double vi = vj(gi), wi = p[gi] - K * vi;
+                for (int j = k + 1 + lane; j < n; j += 32) {
+                    const double vjj = vj(j), wj = p[j] - K * vjj;
+                    row[j] = row[j] - (vi * wj + wi * vjj);
+                }
+            }
+        }
+        // updated row k+1 (= next column), rebuilt locally with the owner's expression
+        double ssn = 0.0;
+        const double vk1 = v0, wk1 = p[k + 1] - K * v0;
+        for (int j = k + 1 + threadIdx.x; j < n; j += blockDim.x) {
+            double val = orow[j];
+            if (t != 0.0) {
+                const double vjj = vj(j), wj = p[j] - K * vjj;
+                val = val - (vk1 * wj + wk1 * vjj);
+            }
+            rnext[j] = val;
+            if (j >= k + 2) ssn += val * val;
+        }
+        ssn = warp_sum(ssn);
+        if (lane == 0) ssbuf[(buf ^ 1) * kTdWarps + warp] = ssn;
         __syncthreads();
     }
+    const double* rowl = rbuf + ((n - 2) & 1) * n;  // row n-2 after the last step
     if (rank == 0 && threadIdx.x == 0 && n >= 2) {
-        d[n - 2] = rowk[n - 2];
-        e[n - 2] = rowk[n - 1];
+        d[n - 2] = rowl[n - 2];
+        e[n - 2] = rowl[n - 1];
     }
     if (n >= 2 && (n - 1) % kCluster == rank && threadIdx.x == 0) d[n - 1] = A[((n - 1) / kCluster) * n + n - 1];
 }
@@ -235,20 +257,21 @@ __device__ __forceinline__ double frcp(double q) {
     return y;
 }
 
-// Sturm counts (eigenvalues of T below x) for 4 probes at once: 4
-// independent division chains per thread hide the fp64 latency.
-__device__ __forceinline__ void sturm4(const double* d, const double* e2, int n, const double (&x)[4],
-                                       double pivmin, int (&c)[4]) {
-    double q[4];
+// Sturm counts (eigenvalues of T below x) for PR probes at once: independent
+// division chains per thread hide the fp64 latency.
+template <int PR>
+__device__ __forceinline__ void sturm_n(const double* d, const double* e2, int n, const double (&x)[PR],
+                                        double pivmin, int (&c)[PR]) {
+    double q[PR];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < PR; ++u) {
         q[u] = d[0] - x[u];
         c[u] = q[u] < 0.0;
     }
     for (int i = 1; i < n; ++i) {
         const double di = d[i], ei = e2[i - 1];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < PR; ++u) {
             if (fabs(q[u]) < pivmin) q[u] = -pivmin;
             q[u] = (di - x[u]) - ei * frcp(q[u]);
             c[u] += q[u] < 0.0;
@@ -256,7 +279,8 @@ __device__ __forceinline__ void sturm4(const double* d, const double* e2, int n,
     }
 }
 
-// one warp per eigenvalue (ascending index j), 128 probes per round (7 bits)
+// one warp per eigenvalue (ascending index j), 64 probes per round (6 bits)
+constexpr int kProbes = 2;
 __global__ void multisect_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n,
                                  double* __restrict__ evals_desc) {
     extern __shared__ double sh_bis[];
@@ -286,27 +310,30 @@ __global__ void multisect_kernel(const double* __restrict__ dg, const double* __
     const int lane = threadIdx.x & 31;
     const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (j >= n) return;
+    constexpr int NP = 32 * kProbes;
     double lo = bounds[0], hi = bounds[1];
     const double pivmin = bounds[2];
-    auto probe = [&](int idx) { return fmin(fmax(lo + (hi - lo) * (static_cast<double>(idx + 1) / 129.0), lo), hi); };
-    for (int it = 0; it < 16; ++it) {
+    auto probe = [&](int idx) {
+        return fmin(fmax(lo + (hi - lo) * (static_cast<double>(idx + 1) / (NP + 1)), lo), hi);
+    };
+    for (int it = 0; it < 20; ++it) {
         if (!(hi - lo > 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin)) break;
-        double x[4];
-        int c[4];
+        double x[kProbes];
+        int c[kProbes];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] = probe(4 * lane + u);
-        sturm4(d, e2, n, x, pivmin, c);
-        unsigned m4 = 0;
+        for (int u = 0; u < kProbes; ++u) x[u] = probe(kProbes * lane + u);
+        sturm_n<kProbes>(d, e2, n, x, pivmin, c);
+        unsigned mk = 0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) m4 |= (c[u] > j ? 1u : 0u) << u;
-        const unsigned ball = __ballot_sync(0xffffffffu, m4 != 0);
-        int first = 128;
+        for (int u = 0; u < kProbes; ++u) mk |= (c[u] > j ? 1u : 0u) << u;
+        const unsigned ball = __ballot_sync(0xffffffffu, mk != 0);
+        int first = NP;
         if (ball) {
             const int fl = __ffs(ball) - 1;
-            const unsigned fm = __shfl_sync(0xffffffffu, m4, fl);
-            first = 4 * fl + __ffs(fm) - 1;
+            const unsigned fm = __shfl_sync(0xffffffffu, mk, fl);
+            first = kProbes * fl + __ffs(fm) - 1;
         }
-        const double nhi = first < 128 ? probe(first) : hi;
+        const double nhi = first < NP ? probe(first) : hi;
         const double nlo = first > 0 ? probe(first - 1) : lo;
         if (nlo == lo && nhi == hi) break;
         lo = nlo;
@@ -436,57 +463,100 @@ __global__ void cluster_mgs_kernel(const int* __restrict__ clusters, int n, doub
     }
 }
 
-// U (row-major n x r) = H_0 ... H_{n-3} Z.  Each CTA owns up to 8 columns
-// (one per warp, NQ entries per lane in registers); reflectors and their taus
-// are staged in shared memory 16 at a time, applied from the last to the first.
-constexpr int kBtChunk = 16;
-template <int NQ>
-__global__ void __launch_bounds__(256) backtransform_kernel(const double* __restrict__ V,
-                                                            const double* __restrict__ tau, int n, int r,
-                                                            const double* __restrict__ Z, double* __restrict__ U) {
-    extern __shared__ double sv[];  // kBtChunk x n reflectors, then kBtChunk taus
-    double* stau = sv + kBtChunk * n;
-    const int lane = threadIdx.x & 31;
-    const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const bool active = col < r;
-    double z[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int i = lane + 32 * q;
-        z[q] = (active && i < n) ? Z[static_cast<size_t>(col) * n + i] : 0.0;
+// U (row-major n x r) = H_0 ... H_{n-3} Z with the compact WY form: chunks of
+// 16 consecutive reflectors H_lo..H_hi = I - Y T Y^T (T upper triangular,
+// LAPACK dlarft forward) are applied as Z <- Z - Y (T (Y^T Z)), last chunk
+// first.  Each CTA owns 8 columns of Z in shared memory; 4 barriers per chunk.
+constexpr int kWyChunk = 16;
+constexpr int kWyCols = 8;
+__global__ void __launch_bounds__(256) backtransform_wy(const double* __restrict__ V, const double* __restrict__ tau,
+                                                       int n, int r, const double* __restrict__ Z,
+                                                       double* __restrict__ U) {
+    extern __shared__ double swy[];
+    double* Y = swy;                          // kWyChunk x n
+    double* Zb = Y + kWyChunk * n;            // n x kWyCols
+    double* S = Zb + n * kWyCols;             // kWyChunk x kWyChunk
+    double* T = S + kWyChunk * kWyChunk;      // kWyChunk x kWyChunk
+    double* W = T + kWyChunk * kWyChunk;      // kWyChunk x kWyCols
+    double* W2 = W + kWyChunk * kWyCols;      // kWyChunk x kWyCols
+    double* tk = W2 + kWyChunk * kWyCols;     // kWyChunk
+    const int c0 = blockIdx.x * kWyCols;
+    const int nc = min(kWyCols, r - c0);
+    for (int idx = threadIdx.x; idx < n * kWyCols; idx += blockDim.x) {
+        const int i = idx / kWyCols, c = idx % kWyCols;
+        Zb[idx] = c < nc ? Z[static_cast<size_t>(c0 + c) * n + i] : 0.0;
     }
-    for (int hi = n - 3; hi >= 0; hi -= kBtChunk) {
-        const int lo = max(0, hi - kBtChunk + 1);
+    for (int hi = n - 3; hi >= 0; hi -= kWyChunk) {
+        const int lo = max(0, hi - kWyChunk + 1);
+        const int kc = hi - lo + 1;
         __syncthreads();
-        for (int kk = lo; kk <= hi; ++kk)
+        for (int q = 0; q < kc; ++q)
             for (int i = threadIdx.x; i < n; i += blockDim.x)
-                sv[(kk - lo) * n + i] = i > kk ? V[static_cast<size_t>(kk) * n + i] : 0.0;
-        if (threadIdx.x <= hi - lo) stau[threadIdx.x] = tau[lo + threadIdx.x];
+                Y[q * n + i] = i > lo + q ? V[static_cast<size_t>(lo + q) * n + i] : 0.0;
+        if (threadIdx.x < kc) tk[threadIdx.x] = tau[lo + threadIdx.x];
         __syncthreads();
-        if (!active) continue;
-        for (int k = hi; k >= lo; --k) {
-            const double t = stau[k - lo];
-            if (t == 0.0) continue;
-            const double* vk = sv + (k - lo) * n;
-            double s = 0.0;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const int i = lane + 32 * q;
-                if (i < n) s += vk[i] * z[q];
-            }
-            s = warp_sum(s) * t;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const int i = lane + 32 * q;
-                if (i < n) z[q] -= s * vk[i];
+        // S = Y^T Y (upper part) and W = Y^T Zb
+        for (int e = threadIdx.x; e < kc * kc + kc * kWyCols; e += blockDim.x) {
+            double s0 = 0.0, s1 = 0.0;
+            if (e < kc * kc) {
+                const int a2 = e / kc, b2 = e % kc;
+                if (a2 > b2) continue;
+                const double* ya = Y + a2 * n;
+                const double* yb = Y + b2 * n;
+                int i = lo + b2 + 1;  // y_b is zero above lo+b+1
+                for (; i + 1 < n; i += 2) {
+                    s0 += ya[i] * yb[i];
+                    s1 += ya[i + 1] * yb[i + 1];
+                }
+                if (i < n) s0 += ya[i] * yb[i];
+                S[a2 * kWyChunk + b2] = s0 + s1;
+            } else {
+                const int f = e - kc * kc, q = f / kWyCols, c = f % kWyCols;
+                const double* yq = Y + q * n;
+                int i = lo + q + 1;
+                for (; i + 1 < n; i += 2) {
+                    s0 += yq[i] * Zb[i * kWyCols + c];
+                    s1 += yq[i + 1] * Zb[(i + 1) * kWyCols + c];
+                }
+                if (i < n) s0 += yq[i] * Zb[i * kWyCols + c];
+                W[q * kWyCols + c] = s0 + s1;
             }
         }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // T (dlarft forward, columnwise); lane a owns row a
+            const int a2 = threadIdx.x;
+            for (int i = 0; i < kc; ++i) {
+                double v = 0.0;
+                if (a2 < i) {
+                    for (int b2 = a2; b2 < i; ++b2) v += T[a2 * kWyChunk + b2] * S[b2 * kWyChunk + i];
+                    v *= -tk[i];
+                } else if (a2 == i) {
+                    v = tk[i];
+                }
+                __syncwarp();
+                if (a2 < kWyChunk) T[a2 * kWyChunk + i] = a2 <= i ? v : 0.0;
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < kc * kWyCols; e += blockDim.x) {  // W2 = T W
+            const int q = e / kWyCols, c = e % kWyCols;
+            double v = 0.0;
+            for (int b2 = q; b2 < kc; ++b2) v += T[q * kWyChunk + b2] * W[b2 * kWyCols + c];
+            W2[e] = v;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < n * kWyCols; e += blockDim.x) {  // Zb -= Y W2
+            const int i = e / kWyCols, c = e % kWyCols;
+            double v = 0.0;
+            for (int q = 0; q < kc; ++q) v += Y[q * n + i] * W2[q * kWyCols + c];
+            Zb[e] -= v;
+        }
     }
-    if (!active) return;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int i = lane + 32 * q;
-        if (i < n) U[static_cast<size_t>(i) * r + col] = z[q];
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < n * nc; idx += blockDim.x) {
+        const int i = idx / nc, c = idx % nc;
+        U[static_cast<size_t>(i) * r + c0 + c] = Zb[i * kWyCols + c];
     }
 }
 
@@ -587,7 +657,8 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
         cfg.numAttrs = 1;
         if (n <= kDsmemMaxN) {
             const int nloc = (n + kCluster - 1) / kCluster;
-            const size_t smem = (static_cast<size_t>(nloc) * n + 7 * n + 2 * kCluster * kTdWarps + 32) * sizeof(double);
+            const size_t smem =
+                (static_cast<size_t>(nloc) * n + 6 * n + 2 * kCluster * kTdWarps + 2 * kTdWarps) * sizeof(double);
             cfg.blockDim = dim3(kTdThreads);
             static bool attr = [] {
                 cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -605,7 +676,7 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
         }
         count_launch();
     }
-    const int wpb = 8;
+    const int wpb = 2;
     multisect_kernel<<<cdiv(n64, wpb), 32 * wpb, 2 * n * sizeof(double), s>>>(w.d.p, w.e.p, n, w.evals.p);
     count_launch();
     TCB_LAUNCH();
@@ -665,18 +736,14 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
         count_launch();
         TCB_CUDA(cudaStreamSynchronize(s));
     }
-    const size_t btsmem = static_cast<size_t>(kBtChunk) * (n + 1) * sizeof(double);
+    const size_t wysmem = (static_cast<size_t>(kWyChunk) * n + static_cast<size_t>(n) * kWyCols +
+                           2 * kWyChunk * kWyChunk + 2 * kWyChunk * kWyCols + kWyChunk) * sizeof(double);
     static bool attr = [] {
-        const int mx = kBtChunk * 1025 * sizeof(double);
-        cudaFuncSetAttribute(backtransform_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(backtransform_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(backtransform_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(backtransform_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         return true;
     }();
     (void)attr;
-    if (n <= 256) backtransform_kernel<8><<<cdiv(r64, 8), 256, btsmem, s>>>(w.z.p, w.tau.p, n, r, Z.p, U);
-    else if (n <= 512) backtransform_kernel<16><<<cdiv(r64, 8), 256, btsmem, s>>>(w.z.p, w.tau.p, n, r, Z.p, U);
-    else backtransform_kernel<32><<<cdiv(r64, 8), 256, btsmem, s>>>(w.z.p, w.tau.p, n, r, Z.p, U);
+    backtransform_wy<<<cdiv(r64, kWyCols), 256, wysmem, s>>>(w.z.p, w.tau.p, n, r, Z.p, U);  // n < 3: plain copy
     count_launch();
     TCB_LAUNCH();
     TCB_CUDA(cudaStreamSynchronize(s));
