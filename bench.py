@@ -291,6 +291,8 @@ def main():
             "cpu_baseline": cpu,
             "clocks": clk,
             "uncertified_decisions": res.uncertified_decisions,
+            "step_ms_all": [round(v, 3) for v in step_ms],
+            "e2e_ms_all": [round(v, 3) for v in e2e_ms],
         }
         print(json.dumps(line), flush=True)
     if world > 1:

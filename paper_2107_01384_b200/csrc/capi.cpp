@@ -54,6 +54,17 @@ struct Stream {
         if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
             throw Error("tucomp_b200: no CUDA device (the B200 path has no CPU fallback)");
         TCB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        static bool pool = [] {  // keep freed pool memory mapped between calls
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaMemPool_t mp;
+            if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+                u64 thr = ~u64{0};
+                cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            return true;
+        }();
+        (void)pool;
     }
     ~Stream() {
         if (s) {
