@@ -262,3 +262,40 @@ def test_compress_zero_tensor(gpu_pkg):
     res = gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(target_re=1e-2))
     ref = oracle.compress(x, target_re=1e-2)
     assert res.container == ref.container
+
+
+# ---------------------------------------------------------------- golden vectors (reference's own code)
+import hashlib as _hl  # noqa: E402
+import json as _json  # noqa: E402
+import os as _os  # noqa: E402
+
+_GOLDEN = _json.load(open(_os.path.join(_os.path.dirname(__file__), "golden", "golden.json")))
+
+
+def _golden_core(g):
+    rng = np.random.default_rng(g["seed"])
+    shape = tuple(g["shape"])
+    idx = np.indices(shape).sum(0).astype(np.float64)
+    return rng.standard_normal(shape) * np.exp(-g["decay"] * idx / idx.max())
+
+
+@pytest.mark.parametrize("g", [g for g in _GOLDEN["encode"] if g["coder"] == 0],
+                         ids=lambda g: f"s{g['seed']}-f{g['frac']}-sp{int(g['split'])}-fx{g['fixed']}")
+def test_gpu_encoder_matches_reference_golden(gpu_pkg, g):
+    mag, neg, k, zero, sn = gpu_pkg.quantize(_golden_core(g))
+    tot = float((mag.astype(np.float64) ** 2).sum())
+    s, lp, ach, dec, _ = gpu_pkg.encode(mag, neg, tot * g["frac"], split=g["split"], fixed_plane=g["fixed"])
+    assert lp == g["last_plane"] and len(s) == g["len"] and _hl.sha256(s).hexdigest() == g["sha"]
+    assert _hl.sha256(dec.tobytes()).hexdigest() == g["dec_sha"]
+
+
+@pytest.mark.parametrize("g", _GOLDEN["quantize"], ids=lambda g: f"seed{g['seed']}")
+def test_gpu_quantize_matches_reference_golden(gpu_pkg, g):
+    mag, neg, k, zero, sn = gpu_pkg.quantize(_golden_core(g))
+    assert k == g["k"] and _hl.sha256(mag.tobytes()).hexdigest() == g["mag_sha"]
+    assert [[float(v).hex() for v in ax] for ax in sn] == g["slice_norms_hex"]
+
+
+@pytest.mark.parametrize("g", [g for g in _GOLDEN["symbols"] if g["coder"] == 0], ids=lambda g: f"case{g['case']}")
+def test_gpu_entropy_matches_reference_golden(gpu_pkg, g):
+    assert gpu_pkg.encode_symbols(0, g["symbols"]).hex() == g["bytes"]
