@@ -599,7 +599,7 @@ __device__ __forceinline__ u32 hslot(u64 sym, u32 hbits) {
     return static_cast<u32>((sym * 0x9E3779B97F4A7C15ull) >> (64 - hbits));
 }
 
-constexpr u32 kAcSmemCap = 2048;  // model entries kept in shared memory
+constexpr u32 kAcSmemCap = 2048;  // model entries kept in shared memory (global scratch beyond)
 
 __host__ __device__ inline u32 pow2_at_least(u32 v) {
     u32 p = 2;
@@ -607,122 +607,192 @@ __host__ __device__ inline u32 pow2_at_least(u32 v) {
     return p;
 }
 __host__ __device__ inline u32 log2_at_least(u32 v) {
-    u32 b = 4;
+    u32 b = 5;
     while ((1u << b) < v) ++b;
     return b;
 }
-__host__ __device__ inline u64 ac_smem_bytes(u32 cap) {
-    return 4ull * cap + 4ull * pow2_at_least(cap + 1) + 4ull * (1u << log2_at_least(2 * cap)) + 8ull * cap + 16;
+// model layout (u32 words): cnt[cap] | l1[cap/32+1] | l2[cap/1024+1] | hidx[1<<hb] | val[cap] (u64)
+__host__ __device__ inline u64 ac_model_words(u32 cap) {
+    const u64 w = cap + (cap / 32 + 1) + (cap / 1024 + 1) + (u64{1} << log2_at_least(2 * cap));
+    return ((w + 1) & ~u64{1}) + 2ull * cap;
 }
 
-// One warp per stream (lane 0 codes).  The adaptive model lives in shared
-// memory when its capacity fits (smem_cap entries), else in the stream's
-// global scratch; a shared-memory model that overflows flags the stream for a
-// global-memory rerun.
+// One warp per stream.  All lanes run the range coder redundantly (identical
+// state); the adaptive model (entropy.cpp:155-239) is probed and updated
+// cooperatively: hash lookups test 32 slots per ballot, prefix(i) is a
+// 3-level (1 / 32 / 1024) count sum reduced in one warp shuffle tree, and
+// halving rescales the counts with all lanes.  Lane 0 writes the bytes.
 __global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, const StreamOut* __restrict__ sout,
                                                 const AcDesc* __restrict__ desc, const int* __restrict__ ids,
                                                 int nstreams, u8* __restrict__ outbuf, u32* __restrict__ scratch,
                                                 u64* __restrict__ elen, u32 smem_cap, int* __restrict__ redo) {
     extern __shared__ __align__(16) u8 ac_smem[];
-    if (threadIdx.x != 0) return;
+    const int lane = threadIdx.x;
     const int sidx = ids ? ids[blockIdx.x] : static_cast<int>(blockIdx.x);
     if (sidx >= nstreams) return;
     const u64 ns = sout[sidx].nsyms;
     if (ns == 0) {
-        elen[sidx] = 0;
+        if (lane == 0) elen[sidx] = 0;
         return;
     }
     const AcDesc d = desc[sidx];
-    u32 cap, fenn, hb;
-    u32 *cnt, *fen, *hidx;
-    u64* val;
-    if (smem_cap > 0) {
-        cap = min(d.cap, smem_cap);
-        fenn = pow2_at_least(cap + 1);
-        hb = log2_at_least(2 * cap);
-        val = reinterpret_cast<u64*>(ac_smem);
-        cnt = reinterpret_cast<u32*>(val + cap);
-        fen = cnt + cap;
-        hidx = fen + fenn;
-    } else {
-        cap = d.cap;
-        fenn = d.fen;
-        hb = d.hbits;
-        cnt = scratch + d.model_off;
-        fen = cnt + cap;
-        hidx = fen + fenn;
-        val = reinterpret_cast<u64*>(hidx + (1u << hb));
-    }
-    for (u32 i = 0; i < fenn; ++i) fen[i] = 0;
-    for (u32 i = 0; i < (1u << hb); ++i) hidx[i] = 0;
+    const u32 cap = smem_cap > 0 ? min(d.cap, smem_cap) : d.cap;
+    u32* base = smem_cap > 0 ? reinterpret_cast<u32*>(ac_smem) : scratch + d.model_off;
+    u32* cnt = base;
+    u32* l1 = cnt + cap;
+    u32* l2 = l1 + (cap / 32 + 1);
+    u32* hidx = l2 + (cap / 1024 + 1);
+    const u32 hb = log2_at_least(2 * cap);
+    const u32 hmask = (1u << hb) - 1;
+    u64* val = reinterpret_cast<u64*>(base + ((cap + (cap / 32 + 1) + (cap / 1024 + 1) + (1u << hb) + 1) & ~1u));
+    for (u32 i = lane; i <= cap / 32; i += 32) l1[i] = 0;
+    for (u32 i = lane; i <= cap / 1024; i += 32) l2[i] = 0;
+    for (u32 i = lane; i < (1u << hb); i += 32) hidx[i] = 0;
     u8* out = outbuf + d.out_off;
-    out[0] = 0;  // coder id: arithmetic
-    const u32 cnt32 = static_cast<u32>(ns);
-    for (int i = 0; i < 4; ++i) out[1 + i] = static_cast<u8>(cnt32 >> (8 * i));
-    AcState st{0, 0xFFFFFFFFu, 0, 1, out, 5};
-    u32 nsym = 1, total = 1;
-    cnt[0] = 1;
-    val[0] = 0;
-    auto fadd = [&](u32 i, u32 dlt) {
-        for (u32 j = i + 1; j < fenn; j += j & (~j + 1)) fen[j] += dlt;
+    if (lane == 0) {
+        out[0] = 0;  // coder id: arithmetic
+        const u32 cnt32 = static_cast<u32>(ns);
+        for (int i = 0; i < 4; ++i) out[1 + i] = static_cast<u8>(cnt32 >> (8 * i));
+        cnt[0] = 1;
+        val[0] = 0;
+        l1[0] = 1;
+        l2[0] = 1;
+    }
+    __syncwarp();
+    // range coder state (identical in every lane)
+    u64 low = 0, pending = 1, pos = 5;
+    u32 range = 0xFFFFFFFFu;
+    u8 cache = 0;
+    auto shift = [&]() {
+        if (static_cast<u32>(low) < 0xFF000000u || (low >> 32) != 0) {
+            const u8 carry = static_cast<u8>(low >> 32);
+            u8 first = cache;
+            if (lane == 0) {
+                for (u64 q = 0; q < pending; ++q) {
+                    out[pos + q] = static_cast<u8>(first + carry);
+                    first = 0xFF;
+                }
+            }
+            pos += pending;
+            pending = 0;
+            cache = static_cast<u8>(low >> 24);
+        }
+        ++pending;
+        low = (low << 8) & 0xFFFFFFFFull;
     };
-    auto below = [&](u32 i) {
+    auto norm = [&]() {
+        while (range < (1u << 24)) {
+            shift();
+            range <<= 8;
+        }
+    };
+    u32 nsym = 1, total = 1;
+    auto below = [&](u32 i) {  // sum of cnt[0..i)
+        const u32 b1 = i >> 5, b2 = i >> 10;
         u32 s = 0;
-        for (u32 j = i; j > 0; j -= j & (~j + 1)) s += fen[j];
+        if ((b1 << 5) + lane < i) s += cnt[(b1 << 5) + lane];
+        if ((b2 << 5) + lane < b1) s += l1[(b2 << 5) + lane];
+        for (u32 b = lane; b < b2; b += 32) s += l2[b];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         return s;
     };
     auto halve = [&]() {
-        total = 0;
-        for (u32 i = 0; i < fenn; ++i) fen[i] = 0;
-        for (u32 i = 0; i < nsym; ++i) {
-            cnt[i] = max(1u, cnt[i] >> 1);
-            total += cnt[i];
-            fen[i + 1] = cnt[i];
+        __syncwarp();
+        for (u32 i = lane; i <= cap / 32; i += 32) l1[i] = 0;
+        for (u32 i = lane; i <= cap / 1024; i += 32) l2[i] = 0;
+        __syncwarp();
+        u32 t = 0;
+        for (u32 i0 = 0; i0 < nsym; i0 += 32) {
+            const u32 i = i0 + lane;
+            u32 c = 0;
+            if (i < nsym) {
+                c = max(1u, cnt[i] >> 1);
+                cnt[i] = c;
+            }
+            u32 bs = c;  // block i0/32 sum
+            for (int o = 16; o > 0; o >>= 1) bs += __shfl_xor_sync(0xffffffffu, bs, o);
+            if (lane == 0) {
+                l1[i0 >> 5] = bs;
+                l2[i0 >> 10] += bs;
+            }
+            t += bs;
+            __syncwarp();
         }
-        for (u32 i = 1; i < fenn; ++i) {
-            const u32 j = i + (i & (~i + 1));
-            if (j < fenn) fen[j] += fen[i];
-        }
+        total = t;
+        __syncwarp();
     };
-    fadd(0, 1);
     const u64* sy = syms + d.sym_off;
-    const u32 hmask = (1u << hb) - 1;
-    for (u64 t = 0; t < ns; ++t) {
-        const u64 s = sy[t];
-        u32 h = hslot(s, hb), found = 0;
-        while (hidx[h]) {
-            if (val[hidx[h] - 1] == s) {
-                found = hidx[h];
+    for (u64 tt = 0; tt < ns; ++tt) {
+        const u64 s = sy[tt];
+        // probe 32 hash slots per round: stop at the first match or the first empty slot
+        u32 h = static_cast<u32>((s * 0x9E3779B97F4A7C15ull) >> (64 - hb));
+        int found = -1;
+        u32 empty_slot = 0;
+        while (true) {
+            const u32 slot = (h + lane) & hmask;
+            const u32 e = hidx[slot];
+            const bool match = e != 0 && val[e - 1] == s;
+            const unsigned mm = __ballot_sync(0xffffffffu, match);
+            const unsigned me = __ballot_sync(0xffffffffu, e == 0);
+            const int fm = mm ? __ffs(mm) - 1 : 32, fe = me ? __ffs(me) - 1 : 32;
+            if (fm < fe) {
+                found = static_cast<int>(__shfl_sync(0xffffffffu, e, fm)) - 1;
                 break;
             }
-            h = (h + 1) & hmask;
+            if (fe < 32) {
+                empty_slot = (h + fe) & hmask;
+                break;
+            }
+            h = (h + 32) & hmask;
         }
-        if (found) {
-            const u32 i = found - 1;
-            ac_code(st, below(i), cnt[i], total);
+        if (found >= 0) {
+            const u32 i = static_cast<u32>(found);
+            const u32 cum = below(i);
+            const u32 f = cnt[i];
+            range /= total;
+            low += static_cast<u64>(cum) * range;
+            range *= f;
+            norm();
             if (total + 32 >= (1u << 16)) halve();
-            cnt[i] += 32;
+            __syncwarp();
+            if (lane == 0) {
+                cnt[i] += 32;
+                l1[i >> 5] += 32;
+                l2[i >> 10] += 32;
+            }
             total += 32;
-            fadd(i, 32);
         } else {
             if (nsym >= cap) {  // shared-memory model full: rerun from global scratch
-                *redo = 1;
-                elen[sidx] = ~u64{0};
+                if (lane == 0) {
+                    *redo = 1;
+                    elen[sidx] = ~u64{0};
+                }
                 return;
             }
-            ac_code(st, 0, cnt[0], total);
-            ac_raw32(st, s);
+            range /= total;  // escape occupies [0, cnt[0])
+            range *= cnt[0];
+            norm();
+            for (int b = 31; b >= 0; --b) {  // 32 raw bits as encode(bit, 1, 2)
+                range >>= 1;
+                if ((s >> b) & 1u) low += range;
+                norm();
+            }
             if (total + 32 >= (1u << 16)) halve();
+            __syncwarp();
             const u32 i = nsym++;
-            val[i] = s;
-            cnt[i] = 32;
-            fadd(i, 32);
+            if (lane == 0) {
+                val[i] = s;
+                cnt[i] = 32;
+                l1[i >> 5] += 32;
+                l2[i >> 10] += 32;
+                hidx[empty_slot] = i + 1;
+            }
             total += 32;
-            hidx[h] = i + 1;
         }
+        __syncwarp();
     }
-    for (int i = 0; i < 5; ++i) ac_shift(st);
-    elen[sidx] = st.pos;
+    for (int i = 0; i < 5; ++i) shift();
+    if (lane == 0) elen[sidx] = pos;
 }
 
 // Host side: shared-memory pass for every stream, global-scratch rerun for
@@ -736,10 +806,10 @@ void run_ac(const u64* syms, const StreamOut* so, const AcDesc* dad, const std::
         TCB_CUDA(cudaMemsetAsync(elen, 0, ns * sizeof(u64), s));
         return;
     }
-    const u64 smem = ac_smem_bytes(need);
+    const u64 smem = ac_model_words(need) * 4 + 16;
     static bool attr = [] {
         cudaFuncSetAttribute(ac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(ac_smem_bytes(kAcSmemCap)));
+                             static_cast<int>(ac_model_words(kAcSmemCap) * 4 + 16));
         return true;
     }();
     (void)attr;
@@ -887,15 +957,12 @@ std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cu
     DevBuf<StreamOut> dso(1, s);
     dso.upload(&so, 1);
     AcDesc a{};
-    a.cap = static_cast<u32>((n + 2) & ~u64{1});
-    a.fen = 2;
-    while (a.fen < a.cap + 1) a.fen *= 2;
-    a.hbits = 4;
-    while ((1u << a.hbits) < 2 * a.cap) ++a.hbits;
+    a.cap = static_cast<u32>(n + 1);
+    a.hbits = log2_at_least(2 * a.cap);
     DevBuf<AcDesc> dad(1, s);
     dad.upload(&a, 1);
     DevBuf<u8> ent(5 + 7 * n + 16, s);
-    DevBuf<u32> scratch(a.cap + a.fen + (u64{1} << a.hbits) + 2ull * a.cap + 2, s);
+    DevBuf<u32> scratch(ac_model_words(a.cap) + 2, s);
     DevBuf<u64> elen(1, s);
     run_ac(syms.p, dso.p, dad.p, std::vector<AcDesc>{a}, std::vector<StreamOut>{so}, 1, ent.p, scratch.p, elen.p, s);
     const u64 el = elen.to_host()[0];
@@ -956,18 +1023,12 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
         const u64 k = soh[i].nsyms;
         a.out_off = out_total;
         out_total += k ? 5 + 7 * k + 16 : 0;
-        u32 cap = static_cast<u32>((k + 2) & ~u64{1});  // even: keeps the u64 value array aligned
-        u32 fen = 2;
-        while (fen < cap + 1) fen *= 2;
-        u32 hb = 4;
-        while ((1u << hb) < 2 * cap) ++hb;
+        const u32 cap = static_cast<u32>(k + 1);
         a.cap = cap;
-        a.fen = fen;
-        a.hbits = hb;
+        a.fen = 0;
+        a.hbits = log2_at_least(2 * cap);
         a.model_off = scratch_total;
-        if (k) {
-            scratch_total += cap + fen + (u64{1} << hb) + 2ull * cap;
-        }
+        if (k) scratch_total += ac_model_words(cap);
     }
     DevBuf<AcDesc> dad(ns, s);
     dad.upload(ad.data(), ns);

@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kCluster = 8;
 constexpr int kTriThreads = 512;
-constexpr int kDsmemMaxN = 440;
+constexpr int kDsmemMaxN = 600;
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -48,36 +48,80 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ---------------------------------------------------------------- tridiagonalisation (DSMEM)
-// Row i lives in CTA (i % 8), local slot i / 8; the stored matrix stays
-// bitwise symmetric (every update is symmetric in (i, j)).  Per step k:
+// Row i lives in CTA (i % C), local slot i / C (C = 16-CTA cluster, the
+// non-portable maximum); the stored matrix stays bitwise symmetric (every
+// update is symmetric in (i, j)).  Per step k:
 //   A. every CTA derives alpha/beta/tau from the replicated column k (rowk),
 //      whose |x|^2 partials were accumulated while it was built;
-//   B. each CTA forms p_i = tau * A_i . v for its rows and pushes (p_i,
-//      A_i,k+1 = pre-update row k+1 by symmetry, partial p.v) into every CTA's
-//      double-buffered receive arrays over DSMEM;
-//   -- one cluster barrier --
+//   B. each warp forms p_i = tau * A_i . v for up to 4 of its rows at once and
+//      pushes (p_i, A_i,k+1 = pre-update row k+1 by symmetry, partial p.v)
+//      into every CTA's double-buffered receive arrays with st.async, each
+//      store completing transaction bytes on the receiver's mbarrier;
+//   -- wait on the local mbarrier for 16 m + 1024 bytes (no cluster barrier,
+//      no GPU-scope fence) --
 //   C. each CTA updates its rows with w = p - K v recomputed inline and
 //      rebuilds the updated row k+1 (next column) with the owner's exact
 //      expression; one CTA barrier.
+// Completion of step k+1's receive at any CTA implies every CTA finished
+// step k, so double buffering is enough for the write-after-read hazard.
 // Outputs d, e, V (reflector k at V[k*n + i], i >= k+1), tau.
 constexpr int kTdThreads = 256;
 constexpr int kTdWarps = kTdThreads / 32;
+constexpr int kTdCluster = 16;
+constexpr int kTdPv = kTdCluster * kTdWarps;  // 128 partial p.v slots
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned cluster_map(unsigned addr, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_f64(unsigned raddr, double v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(unsigned bar, unsigned tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
 __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __restrict__ Ag, int n,
                                                            double* __restrict__ d, double* __restrict__ e,
                                                            double* __restrict__ V, double* __restrict__ tau) {
+    constexpr int C = kTdCluster;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = static_cast<int>(cl.block_rank());
-    extern __shared__ double sm[];
-    const int nloc = (n + kCluster - 1) / kCluster;
-    double* A = sm;                                  // nloc x n
-    double* pbuf = A + nloc * n;                     // 2 x n (remote-written p)
-    double* obuf = pbuf + 2 * n;                     // 2 x n (remote-written pre-update column k+1)
-    double* rbuf = obuf + 2 * n;                     // 2 x n (local replicated column k)
-    double* pvbuf = rbuf + 2 * n;                    // 2 x (kCluster * kTdWarps) (remote-written)
-    double* ssbuf = pvbuf + 2 * kCluster * kTdWarps; // 2 x kTdWarps (local)
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(8) unsigned long long mbar[2];
+    const int nloc = (n + C - 1) / C;
+    double* A = sm;                         // nloc x n
+    double* pbuf = A + nloc * n;            // 2 x n (remote-written p)
+    double* obuf = pbuf + 2 * n;            // 2 x n (remote-written pre-update column k+1)
+    double* rbuf = obuf + 2 * n;            // 2 x n (local replicated column k)
+    double* pvbuf = rbuf + 2 * n;           // 2 x kTdPv (remote-written)
+    double* ssbuf = pvbuf + 2 * kTdPv;      // 2 x kTdWarps (local)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        mbar_init(smem_addr(&mbar[0]), 1);
+        mbar_init(smem_addr(&mbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     for (int li = 0; li < nloc; ++li) {
-        const int gi = li * kCluster + rank;
+        const int gi = li * C + rank;
         if (gi >= n) break;
         for (int j = threadIdx.x; j < n; j += blockDim.x) A[li * n + j] = Ag[static_cast<size_t>(gi) * n + j];
     }
@@ -93,15 +137,23 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
     }
     __syncthreads();
     cl.sync();
+    // remote addresses of the receive buffers / mbarriers of CTA `lane` (lanes < C)
+    const unsigned my_p = smem_addr(pbuf), my_o = smem_addr(obuf), my_pv = smem_addr(pvbuf);
+    const unsigned dst = lane < C ? lane : 0;
+    const unsigned r_p = cluster_map(my_p, dst), r_o = cluster_map(my_o, dst), r_pv = cluster_map(my_pv, dst);
+    const unsigned r_bar0 = cluster_map(smem_addr(&mbar[0]), dst), r_bar1 = cluster_map(smem_addr(&mbar[1]), dst);
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1;
         const int buf = k & 1;
         const double* rowk = rbuf + buf * n;
         double* rnext = rbuf + (buf ^ 1) * n;
-        double* p = pbuf + buf * n;
-        double* orow = obuf + buf * n;
-        double* pv = pvbuf + buf * kCluster * kTdWarps;
+        const double* p = pbuf + buf * n;
+        const double* orow = obuf + buf * n;
+        const double* pv = pvbuf + buf * kTdPv;
+        const unsigned rbar = buf ? r_bar1 : r_bar0;
+        if (threadIdx.x == 0) mbar_arrive_expect(smem_addr(&mbar[buf]), static_cast<unsigned>(16 * m + 8 * kTdPv));
         double ss = 0.0;
+#pragma unroll
         for (int q = 0; q < kTdWarps; ++q) ss += ssbuf[buf * kTdWarps + q];
         const double alpha = sqrt(ss);
         const double x0 = rowk[k + 1];
@@ -109,7 +161,52 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
         const double v0 = x0 - beta;
         const double vv = 2.0 * alpha * (alpha + fabs(x0));  // |x - beta e1|^2
         const double t = (alpha == 0.0 || vv == 0.0) ? 0.0 : 2.0 / vv;
-        if (rank == 0) {
+        const int first = k + 1 + ((rank - (k + 1)) % C + C) % C;  // first owned row >= k+1
+        const int stride = C * kTdWarps;
+        double pvw = 0.0;
+        for (int g0 = first + C * warp; g0 < n; g0 += 4 * stride) {
+            int gi[4];
+            const double* row[4];
+            double s[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                gi[u] = g0 + u * stride;
+                row[u] = A + (min(gi[u], n - 1) / C) * n;
+                s[u] = 0.0;
+            }
+            if (t != 0.0) {
+                if (lane == 0) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) s[u] = row[u][k + 1] * v0;
+                }
+                for (int j = k + 2 + lane; j < n; j += 32) {
+                    const double vj = rowk[j];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) s[u] += row[u][j] * vj;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (gi[u] >= n) break;
+                const double su = s[u] * t;
+                pvw += su * (gi[u] == k + 1 ? v0 : rowk[gi[u]]);
+                const double col = row[u][k + 1];
+                if (lane < C) {
+                    const unsigned off = static_cast<unsigned>((buf * n + gi[u]) * sizeof(double));
+                    st_async_f64(r_p + off, su, rbar);
+                    st_async_f64(r_o + off, col, rbar);
+                }
+            }
+        }
+        if (lane < C)
+            st_async_f64(r_pv + static_cast<unsigned>((buf * kTdPv + rank * kTdWarps + warp) * sizeof(double)), pvw,
+                         rbar);
+        mbar_wait(smem_addr(&mbar[buf]), static_cast<unsigned>((k >> 1) & 1));
+        if (rank == k % C) {  // global outputs, off the exchange's critical path
             if (threadIdx.x == 0) {
                 e[k] = t == 0.0 ? x0 : beta;
                 tau[k] = t;
@@ -118,48 +215,45 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
             for (int i = threadIdx.x; i < m; i += blockDim.x)
                 V[static_cast<size_t>(k) * n + k + 1 + i] = i == 0 ? v0 : rowk[k + 1 + i];
         }
-        const int first = k + 1 + ((rank - (k + 1)) % kCluster + kCluster) % kCluster;
-        double pvw = 0.0;
-        for (int gi = first + kCluster * warp; gi < n; gi += kCluster * kTdWarps) {
-            const double* row = A + (gi / kCluster) * n;
-            double s = 0.0;
-            if (t != 0.0) {
-                for (int j = k + 1 + lane; j < n; j += 32) s += row[j] * (j == k + 1 ? v0 : rowk[j]);
-                s = warp_sum(s) * t;
-                pvw += s * (gi == k + 1 ? v0 : rowk[gi]);
-            }
-            const double col = row[k + 1];
-            if (lane < kCluster) {
-                *cl.map_shared_rank(p + gi, lane) = s;
-                *cl.map_shared_rank(orow + gi, lane) = col;
-            }
-        }
-        if (lane < kCluster) *cl.map_shared_rank(pv + rank * kTdWarps + warp, lane) = pvw;
-        cl.sync();
         double K = 0.0;
         if (t != 0.0) {
-            K = pv[lane] + pv[lane + 32];
+            K = pv[lane] + pv[lane + 32] + pv[lane + 64] + pv[lane + 96];
             K = 0.5 * t * warp_sum(K);
         }
-        auto vj = [&](int j) { return j == k + 1 ? v0 : rowk[j]; };
+        const double wk1 = p[k + 1] - K * v0;
         if (t != 0.0) {
-            for (int gi = first + kCluster * warp; gi < n; gi += kCluster * kTdWarps) {
-                double* row = A + (gi / kCluster) * n;
-                const double vi = vj(gi), wi = p[gi] - K * vi;
-                for (int j = k + 1 + lane; j < n; j += 32) {
-                    const double vjj = vj(j), wj = p[j] - K * vjj;
-                    row[j] = row[j] - (vi * wj + wi * vjj);
+            for (int g0 = first + C * warp; g0 < n; g0 += 4 * stride) {
+                int gi[4];
+                double* row[4];
+                double vi[4], wi[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    gi[u] = g0 + u * stride;
+                    const int gc = min(gi[u], n - 1);
+                    row[u] = A + (gc / C) * n;
+                    vi[u] = gc == k + 1 ? v0 : rowk[gc];
+                    wi[u] = p[gc] - K * vi[u];
+                }
+                if (lane == 0) {  // column k+1: v_{k+1} = v0
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (gi[u] < n) row[u][k + 1] = row[u][k + 1] - (vi[u] * wk1 + wi[u] * v0);
+                }
+                for (int j = k + 2 + lane; j < n; j += 32) {
+                    const double vjj = rowk[j], wj = p[j] - K * vjj;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (gi[u] < n) row[u][j] = row[u][j] - (vi[u] * wj + wi[u] * vjj);
                 }
             }
         }
         // updated row k+1 (= next column), rebuilt locally with the owner's expression
         double ssn = 0.0;
-        const double vk1 = v0, wk1 = p[k + 1] - K * v0;
         for (int j = k + 1 + threadIdx.x; j < n; j += blockDim.x) {
             double val = orow[j];
             if (t != 0.0) {
-                const double vjj = vj(j), wj = p[j] - K * vjj;
-                val = val - (vk1 * wj + wk1 * vjj);
+                const double vjj = j == k + 1 ? v0 : rowk[j], wj = p[j] - K * vjj;
+                val = val - (v0 * wj + wk1 * vjj);
             }
             rnext[j] = val;
             if (j >= k + 2) ssn += val * val;
@@ -173,7 +267,8 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
         d[n - 2] = rowl[n - 2];
         e[n - 2] = rowl[n - 1];
     }
-    if (n >= 2 && (n - 1) % kCluster == rank && threadIdx.x == 0) d[n - 1] = A[((n - 1) / kCluster) * n + n - 1];
+    if (n >= 2 && (n - 1) % C == rank && threadIdx.x == 0) d[n - 1] = A[((n - 1) / C) * n + n - 1];
+    cl.sync();  // no CTA leaves while cluster peers may still address its shared memory
 }
 
 // Same schedule with the matrix in L2 (n > kDsmemMaxN).
@@ -464,38 +559,60 @@ __global__ void cluster_mgs_kernel(const int* __restrict__ clusters, int n, doub
 }
 
 // U (row-major n x r) = H_0 ... H_{n-3} Z with the compact WY form: chunks of
-// 16 consecutive reflectors H_lo..H_hi = I - Y T Y^T (T upper triangular,
-// LAPACK dlarft forward) are applied as Z <- Z - Y (T (Y^T Z)), last chunk
-// first.  Each CTA owns 8 columns of Z in shared memory; 4 barriers per chunk.
+// KC consecutive reflectors H_lo..H_hi = I - Y T Y^T (T upper triangular,
+// T = (diag(1/tau) + striu(Y^T Y))^{-1}) are applied as Z <- Z - Y (T (Y^T Z)),
+// last chunk first.  Each CTA owns 8 columns of Z in shared memory; the next
+// chunk's reflectors stream in with cp.async while the current one is applied.
 constexpr int kWyChunk = 16;
 constexpr int kWyCols = 8;
+__device__ __forceinline__ void cp_async8_eig(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
 __global__ void __launch_bounds__(256) backtransform_wy(const double* __restrict__ V, const double* __restrict__ tau,
-                                                       int n, int r, const double* __restrict__ Z,
+                                                       int n, int r, int KC, const double* __restrict__ Z,
                                                        double* __restrict__ U) {
     extern __shared__ double swy[];
-    double* Y = swy;                          // kWyChunk x n
-    double* Zb = Y + kWyChunk * n;            // n x kWyCols
-    double* S = Zb + n * kWyCols;             // kWyChunk x kWyChunk
-    double* T = S + kWyChunk * kWyChunk;      // kWyChunk x kWyChunk
-    double* W = T + kWyChunk * kWyChunk;      // kWyChunk x kWyCols
-    double* W2 = W + kWyChunk * kWyCols;      // kWyChunk x kWyCols
-    double* tk = W2 + kWyChunk * kWyCols;     // kWyChunk
+    double* Ybuf = swy;                          // 2 x KC x n
+    double* Zb = Ybuf + 2 * KC * n;              // n x kWyCols
+    double* S = Zb + n * kWyCols;                // kWyChunk x kWyChunk
+    double* T = S + kWyChunk * kWyChunk;         // kWyChunk x kWyChunk
+    double* W = T + kWyChunk * kWyChunk;         // kWyChunk x kWyCols
+    double* W2 = W + kWyChunk * kWyCols;         // kWyChunk x kWyCols
+    double* tk = W2 + kWyChunk * kWyCols;        // 2 x kWyChunk
     const int c0 = blockIdx.x * kWyCols;
     const int nc = min(kWyCols, r - c0);
     for (int idx = threadIdx.x; idx < n * kWyCols; idx += blockDim.x) {
         const int i = idx / kWyCols, c = idx % kWyCols;
         Zb[idx] = c < nc ? Z[static_cast<size_t>(c0 + c) * n + i] : 0.0;
     }
-    for (int hi = n - 3; hi >= 0; hi -= kWyChunk) {
-        const int lo = max(0, hi - kWyChunk + 1);
+    // chunk list from the last reflector down: chunk ci covers [lo, hi]
+    auto load = [&](int hi, int b) {
+        const int lo = max(0, hi - KC + 1);
+        double* Y = Ybuf + b * KC * n;
+        for (int q = 0; q <= hi - lo; ++q) {
+            const int kk = lo + q;
+            for (int i = kk + 1 + threadIdx.x; i < n; i += blockDim.x)
+                cp_async8_eig(Y + q * n + i, V + static_cast<size_t>(kk) * n + i);
+        }
+        if (threadIdx.x <= hi - lo) tk[b * kWyChunk + threadIdx.x] = tau[lo + threadIdx.x];
+        asm volatile("cp.async.commit_group;\n");
+    };
+    int buf = 0;
+    if (n >= 3) load(n - 3, 0);
+    for (int hi = n - 3; hi >= 0; hi -= KC) {
+        const int lo = max(0, hi - KC + 1);
         const int kc = hi - lo + 1;
+        if (hi - KC >= 0) {
+            load(hi - KC, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n");
+        }
         __syncthreads();
-        for (int q = 0; q < kc; ++q)
-            for (int i = threadIdx.x; i < n; i += blockDim.x)
-                Y[q * n + i] = i > lo + q ? V[static_cast<size_t>(lo + q) * n + i] : 0.0;
-        if (threadIdx.x < kc) tk[threadIdx.x] = tau[lo + threadIdx.x];
-        __syncthreads();
-        // S = Y^T Y (upper part) and W = Y^T Zb
+        const double* Y = Ybuf + buf * KC * n;
+        const double* tb = tk + buf * kWyChunk;
+        // S = Y^T Y (upper part) and W = Y^T Zb; y_q is zero above row lo+q
         for (int e = threadIdx.x; e < kc * kc + kc * kWyCols; e += blockDim.x) {
             double s0 = 0.0, s1 = 0.0;
             if (e < kc * kc) {
@@ -503,7 +620,7 @@ __global__ void __launch_bounds__(256) backtransform_wy(const double* __restrict
                 if (a2 > b2) continue;
                 const double* ya = Y + a2 * n;
                 const double* yb = Y + b2 * n;
-                int i = lo + b2 + 1;  // y_b is zero above lo+b+1
+                int i = lo + b2 + 1;
                 for (; i + 1 < n; i += 2) {
                     s0 += ya[i] * yb[i];
                     s1 += ya[i + 1] * yb[i + 1];
@@ -523,19 +640,18 @@ __global__ void __launch_bounds__(256) backtransform_wy(const double* __restrict
             }
         }
         __syncthreads();
-        if (threadIdx.x < 32) {  // T (dlarft forward, columnwise); lane a owns row a
-            const int a2 = threadIdx.x;
-            for (int i = 0; i < kc; ++i) {
-                double v = 0.0;
-                if (a2 < i) {
-                    for (int b2 = a2; b2 < i; ++b2) v += T[a2 * kWyChunk + b2] * S[b2 * kWyChunk + i];
-                    v *= -tk[i];
-                } else if (a2 == i) {
-                    v = tk[i];
+        if (threadIdx.x < kWyChunk) {
+            // column j of T by back-substitution, all columns in parallel; tau = 0 rows stay 0
+            const int j = threadIdx.x;
+            for (int i = 0; i < kWyChunk; ++i) T[i * kWyChunk + j] = 0.0;
+            if (j < kc && tb[j] != 0.0) {
+                T[j * kWyChunk + j] = tb[j];
+                for (int i = j - 1; i >= 0; --i) {
+                    if (tb[i] == 0.0) continue;
+                    double acc = 0.0;
+                    for (int l = i + 1; l <= j; ++l) acc += S[i * kWyChunk + l] * T[l * kWyChunk + j];
+                    T[i * kWyChunk + j] = -tb[i] * acc;
                 }
-                __syncwarp();
-                if (a2 < kWyChunk) T[a2 * kWyChunk + i] = a2 <= i ? v : 0.0;
-                __syncwarp();
             }
         }
         __syncthreads();
@@ -546,14 +662,16 @@ __global__ void __launch_bounds__(256) backtransform_wy(const double* __restrict
             W2[e] = v;
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < n * kWyCols; e += blockDim.x) {  // Zb -= Y W2
+        for (int e = (lo + 1) * kWyCols + threadIdx.x; e < n * kWyCols; e += blockDim.x) {  // Zb -= Y W2
             const int i = e / kWyCols, c = e % kWyCols;
+            const int qmax = min(kc, i - lo);  // y_q(i) != 0 only for i > lo + q
             double v = 0.0;
-            for (int q = 0; q < kc; ++q) v += Y[q * n + i] * W2[q * kWyCols + c];
+            for (int q = 0; q < qmax; ++q) v += Y[q * n + i] * W2[q * kWyCols + c];
             Zb[e] -= v;
         }
+        __syncthreads();
+        buf ^= 1;
     }
-    __syncthreads();
     for (int idx = threadIdx.x; idx < n * nc; idx += blockDim.x) {
         const int i = idx / nc, c = idx % nc;
         U[static_cast<size_t>(i) * r + c0 + c] = Zb[i * kWyCols + c];
@@ -655,19 +773,29 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
+        bool dsmem = false;
         if (n <= kDsmemMaxN) {
-            const int nloc = (n + kCluster - 1) / kCluster;
-            const size_t smem =
-                (static_cast<size_t>(nloc) * n + 6 * n + 2 * kCluster * kTdWarps + 2 * kTdWarps) * sizeof(double);
-            cfg.blockDim = dim3(kTdThreads);
+            const int nloc = (n + kTdCluster - 1) / kTdCluster;
+            const size_t smem = (static_cast<size_t>(nloc) * n + 6 * n + 2 * kTdPv + 2 * kTdWarps) * sizeof(double);
             static bool attr = [] {
                 cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
                 return true;
             }();
             (void)attr;
+            cfg.gridDim = dim3(kTdCluster);
+            cfg.blockDim = dim3(kTdThreads);
+            at[0].val.clusterDim.x = kTdCluster;
             cfg.dynamicSmemBytes = smem;
-            TCB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_dsmem, A, n, w.d.p, w.e.p, w.z.p, w.tau.p));
-        } else {
+            int ncl = 0;  // a 16-CTA cluster with this much shared memory must fit one GPC
+            dsmem = cudaOccupancyMaxActiveClusters(&ncl, tridiag_dsmem, &cfg) == cudaSuccess && ncl > 0;
+            cudaGetLastError();
+            if (dsmem) TCB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_dsmem, A, n, w.d.p, w.e.p, w.z.p, w.tau.p));
+        }
+        if (!dsmem) {
+            cfg.gridDim = dim3(kCluster);
+            cfg.blockDim = dim3(kTriThreads);
+            at[0].val.clusterDim.x = kCluster;
             w.a = DevBuf<double>(n64 * n64, s);
             DevBuf<double> P(n64, s);
             TCB_CUDA(cudaMemcpyAsync(w.a.p, A, n64 * n64 * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -736,14 +864,15 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
         count_launch();
         TCB_CUDA(cudaStreamSynchronize(s));
     }
-    const size_t wysmem = (static_cast<size_t>(kWyChunk) * n + static_cast<size_t>(n) * kWyCols +
-                           2 * kWyChunk * kWyChunk + 2 * kWyChunk * kWyCols + kWyChunk) * sizeof(double);
+    const int KC = n <= 512 ? kWyChunk : kWyChunk / 2;
+    const size_t wysmem = (2 * static_cast<size_t>(KC) * n + static_cast<size_t>(n) * kWyCols +
+                           2 * kWyChunk * kWyChunk + 2 * kWyChunk * kWyCols + 2 * kWyChunk) * sizeof(double);
     static bool attr = [] {
         cudaFuncSetAttribute(backtransform_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         return true;
     }();
     (void)attr;
-    backtransform_wy<<<cdiv(r64, kWyCols), 256, wysmem, s>>>(w.z.p, w.tau.p, n, r, Z.p, U);  // n < 3: plain copy
+    backtransform_wy<<<cdiv(r64, kWyCols), 256, wysmem, s>>>(w.z.p, w.tau.p, n, r, KC, Z.p, U);  // n < 3: plain copy
     count_launch();
     TCB_LAUNCH();
     TCB_CUDA(cudaStreamSynchronize(s));
