@@ -130,6 +130,30 @@ int tcb_encode_factor_f64(const double* u, uint64_t n, uint64_t r, const uint8_t
                           int coder, int simple, int core_step_log2, double term_cap, uint8_t** stream,
                           uint64_t* len, int* k, uint64_t* count, int8_t* flips, double* term, int* plane);
 
+/* ---- device-pointer building blocks of the sharded multi-GPU mode loop
+ * (paper_2107_01384_b200/shard.py).  All pointers are device
+ * pointers on the current device; capacities as noted. ---- */
+
+/* ||x||^2 and the all-finite flag (tensor.cpp:152-155, sthosvd.cpp:118). */
+int tcb_dev_sumsq(const double* x, uint64_t n, double* out, int* finite);
+/* row-major axis permutation (tensor.cpp:105-144). */
+int tcb_dev_permute(const double* src, double* dst, const uint64_t* shape, const uint64_t* perm, int d);
+/* partial Gram of a column shard: g (rows x rows) = b b^T (sthosvd.cpp:79). */
+int tcb_dev_gram(const double* b, uint64_t rows, uint64_t cols, double* g);
+/* eigensolve + rank rule + sign fix of an all-reduced Gram (sthosvd.cpp:80-90,144-156);
+ * u capacity n*n, receives n x r row-major. */
+int tcb_dev_factor_from_gram(const double* g, uint64_t n, double budget, double* u, uint64_t* r, double* discarded);
+/* one replicated mode step (sthosvd.cpp:136-166); u cap rows*rows, next cap cols*rows. */
+int tcb_dev_mode_step(const double* b, uint64_t rows, uint64_t cols, double budget, int backend, double* u,
+                      double* next, uint64_t* r, double* discarded);
+/* shard-local projection next (cols x r) = b^T u (sthosvd.cpp:158-166). */
+int tcb_dev_ttm(const double* b, uint64_t rows, uint64_t cols, const double* u, uint64_t r, double* next);
+/* phases 2-5 of compress_impl (pipeline.cpp:77-189) on a device factorization
+ * (core in processing order, factors[i] n_i x r_i row-major). */
+int tcb_dev_encode_tucker(const double* core, const double* const* factors, const uint64_t* n, const uint64_t* r,
+                          const uint64_t* order, const double* trunc, int d, int dtype, double norm_sq,
+                          double target_sse, const tcb_params* params, tcb_result* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -375,3 +375,101 @@ int tcb_encode_factor_f64(const double* u, uint64_t n, uint64_t r, const uint8_t
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- device-pointer building blocks
+// Used by the sharded multi-GPU mode loop (paper_2107_01384_b200/shard.py):
+// inputs/outputs are device pointers on the current device; each call runs on
+// a private stream and returns after it completes.
+extern "C" {
+
+int tcb_dev_sumsq(const double* x, uint64_t n, double* out, int* finite) {
+    return guard([&] {
+        Stream st;
+        bool f = true;
+        *out = sum_squares(x, n, &f, st.s);
+        *finite = f ? 1 : 0;
+    });
+}
+
+int tcb_dev_permute(const double* src, double* dst, const uint64_t* shape, const uint64_t* perm, int d) {
+    return guard([&] {
+        Stream st;
+        permute_axes(src, dst, std::vector<u64>(shape, shape + d), std::vector<u64>(perm, perm + d), st.s);
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int tcb_dev_gram(const double* b, uint64_t rows, uint64_t cols, double* g) {
+    return guard([&] {
+        Stream st;
+        if (cols == 0) {
+            TCB_CUDA(cudaMemsetAsync(g, 0, rows * rows * sizeof(double), st.s));
+        } else {
+            gram_f64(b, rows, cols, g, st.s);
+        }
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int tcb_dev_factor_from_gram(const double* g, uint64_t n, double budget, double* u, uint64_t* r, double* discarded) {
+    return guard([&] {
+        Stream st;
+        StepOut o = factor_from_gram(g, n, budget, st.s);
+        TCB_CUDA(cudaMemcpyAsync(u, o.U.p, n * o.r * sizeof(double), cudaMemcpyDeviceToDevice, st.s));
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+        *r = o.r;
+        *discarded = o.discarded;
+    });
+}
+
+int tcb_dev_mode_step(const double* b, uint64_t rows, uint64_t cols, double budget, int backend, double* u,
+                      double* next, uint64_t* r, double* discarded) {
+    return guard([&] {
+        Stream st;
+        StepOut o = mode_step(b, rows, cols, budget, backend, st.s);
+        TCB_CUDA(cudaMemcpyAsync(u, o.U.p, rows * o.r * sizeof(double), cudaMemcpyDeviceToDevice, st.s));
+        TCB_CUDA(cudaMemcpyAsync(next, o.next.p, cols * o.r * sizeof(double), cudaMemcpyDeviceToDevice, st.s));
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+        *r = o.r;
+        *discarded = o.discarded;
+    });
+}
+
+int tcb_dev_ttm(const double* b, uint64_t rows, uint64_t cols, const double* u, uint64_t r, double* next) {
+    return guard([&] {
+        Stream st;
+        if (cols > 0) ttm_f64(b, rows, cols, u, r, next, st.s);
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int tcb_dev_encode_tucker(const double* core, const double* const* factors, const uint64_t* n, const uint64_t* r,
+                          const uint64_t* order, const double* trunc, int d, int dtype, double norm_sq,
+                          double target_sse, const tcb_params* params, tcb_result* out) {
+    return guard([&] {
+        Stream st;
+        Tucker f;
+        f.n.assign(n, n + d);
+        f.r.assign(r, r + d);
+        f.order.assign(order, order + d);
+        f.trunc.assign(trunc, trunc + d);
+        f.core_shape.resize(d);
+        u64 nc = 1;
+        for (int i = 0; i < d; ++i) {
+            f.core_shape[i] = r[order[i]];
+            nc *= f.core_shape[i];
+        }
+        f.core = DevBuf<double>(nc, st.s);
+        TCB_CUDA(cudaMemcpyAsync(f.core.p, core, nc * sizeof(double), cudaMemcpyDeviceToDevice, st.s));
+        f.factors.resize(d);
+        for (int i = 0; i < d; ++i) {
+            f.factors[i] = DevBuf<double>(n[i] * r[i], st.s);
+            TCB_CUDA(cudaMemcpyAsync(f.factors[i].p, factors[i], n[i] * r[i] * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, st.s));
+        }
+        const Result res = encode_tucker_device(f, dtype, norm_sq, target_sse, to_params(params, d), st.s);
+        fill(res, d, out);
+    });
+}
+
+}  // extern "C"

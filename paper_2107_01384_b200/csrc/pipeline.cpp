@@ -116,6 +116,63 @@ std::vector<double> alpha_weights(const std::vector<double>& sn, u64 n) {
     return al;
 }
 
+StepOut factor_from_gram(const double* G, u64 n, double budget, cudaStream_t s) {
+    EigWork w;
+    const auto ev = eig_values(G, n, w, s);
+    std::vector<double> s2(n);
+    for (u64 j = 0; j < n; ++j) s2[j] = std::max(0.0, ev[j]);
+    auto [r, gone] = pick_rank(s2, budget);
+    if (r == 0) {  // a budget above the whole mode energy still keeps one vector (sthosvd.cpp:146-150)
+        r = 1;
+        gone -= s2[0];
+    }
+    StepOut o;
+    o.r = r;
+    o.discarded = gone;
+    o.U = DevBuf<double>(n * r, s);
+    eig_vectors(w, r, o.U.p, s);
+    fix_column_signs(o.U.p, n, r, s);
+    return o;
+}
+
+StepOut mode_step(const double* x, u64 rows, u64 cols, double budget, int backend, cudaStream_t s) {
+    const bool via_gram = backend == 1 || (backend == 0 && rows <= cols);
+    StepOut o;
+    if (via_gram) {
+        DevBuf<double> G(rows * rows, s);
+        gram_f64(x, rows, cols, G.p, s);
+        o = factor_from_gram(G.p, rows, budget, s);
+    } else {  // thin left singular vectors from the Gram of B^T (sthosvd.cpp:91-99)
+        EigWork w;
+        DevBuf<double> G(cols * cols, s);
+        gram_cols_f64(x, rows, cols, G.p, s);
+        const auto ev = eig_values(G.p, cols, w, s);
+        std::vector<double> s2(cols);
+        for (u64 j = 0; j < cols; ++j) s2[j] = std::max(0.0, ev[j]);
+        auto [r, gone] = pick_rank(s2, budget);
+        if (r == 0) {
+            r = 1;
+            gone -= s2[0];
+        }
+        o.r = r;
+        o.discarded = gone;
+        o.U = DevBuf<double>(rows * r, s);
+        DevBuf<double> V(cols * r, s);
+        eig_vectors(w, r, V.p, s);
+        gemm_nn_f64(x, rows, cols, V.p, r, o.U.p, s);
+        std::vector<double> sig(r);
+        for (u64 j = 0; j < r; ++j) sig[j] = std::sqrt(s2[j]);
+        DevBuf<double> ds(r, s);
+        ds.upload(sig.data(), r);
+        scale_orthonormalize(o.U.p, rows, r, ds.p, s);
+        TCB_CUDA(cudaStreamSynchronize(s));
+        fix_column_signs(o.U.p, rows, r, s);
+    }
+    o.next = DevBuf<double>(cols * o.r, s);
+    ttm_f64(x, rows, cols, o.U.p, o.r, o.next.p, s);
+    return o;
+}
+
 Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double target,
                       const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s) {
     if (target < 0) throw Error("sthosvd: negative SSE target");
@@ -143,48 +200,15 @@ Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double 
         u64 tot = 1;
         for (auto v : cur) tot *= v;
         const u64 rows = cur[0], cols = tot / rows;
-        const bool via_gram = backend == 1 || (backend == 0 && rows <= cols);
-        EigWork w;
-        std::vector<double> s2;
-        const u64 m = via_gram ? rows : cols;
-        {
-            DevBuf<double> G(m * m, s);
-            if (via_gram) gram_f64(x.p, rows, cols, G.p, s);
-            else gram_cols_f64(x.p, rows, cols, G.p, s);
-            const auto ev = eig_values(G.p, m, w, s);
-            s2.resize(m);
-            for (u64 j = 0; j < m; ++j) s2[j] = std::max(0.0, ev[j]);
-        }
         const double budget = remaining / static_cast<double>(d - step);
-        auto [r, gone] = pick_rank(s2, budget);
-        if (r == 0) {  // a budget above the whole mode energy still keeps one vector
-            r = 1;
-            gone -= s2[0];
-        }
-        remaining = std::max(0.0, remaining - gone);
-        f.trunc[p[step]] = gone;
-        DevBuf<double> U(rows * r, s);
-        if (via_gram) {
-            eig_vectors(w, r, U.p, s);
-        } else {
-            DevBuf<double> V(cols * r, s);
-            eig_vectors(w, r, V.p, s);
-            gemm_nn_f64(x.p, rows, cols, V.p, r, U.p, s);
-            std::vector<double> sig(r);
-            for (u64 j = 0; j < r; ++j) sig[j] = std::sqrt(s2[j]);
-            DevBuf<double> ds(r, s);
-            ds.upload(sig.data(), r);
-            scale_orthonormalize(U.p, rows, r, ds.p, s);
-            TCB_CUDA(cudaStreamSynchronize(s));
-        }
-        fix_column_signs(U.p, rows, r, s);
-        DevBuf<double> nx(cols * r, s);
-        ttm_f64(x.p, rows, cols, U.p, r, nx.p, s);
-        x = std::move(nx);
-        f.factors[p[step]] = std::move(U);
-        f.r[p[step]] = r;
+        StepOut so = mode_step(x.p, rows, cols, budget, backend, s);
+        remaining = std::max(0.0, remaining - so.discarded);
+        f.trunc[p[step]] = so.discarded;
+        x = std::move(so.next);
+        f.factors[p[step]] = std::move(so.U);
+        f.r[p[step]] = so.r;
         cur.erase(cur.begin());
-        cur.push_back(r);
+        cur.push_back(so.r);
     }
     f.core = std::move(x);
     f.core_shape = cur;
@@ -274,62 +298,14 @@ FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<
     return out;
 }
 
-Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,
-                       const Params& prm, cudaStream_t s) {
-    const auto t_all = Clock::now();
-    Result res;
+// Phases 2-5 of compress_impl (pipeline.cpp:77-189): storage order,
+// quantisation, core plan, factors, sign fold, finalize, container.
+void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtype, double target,
+                 double core_target, double trunc, const Params& prm, cudaStream_t s, Clock::time_point t_all,
+                 u64 n_el) {
     const std::size_t d = shape.size();
-    if (d == 0 || d > 8) throw Error("compress: tensor order must be between 1 and 8");
-    u64 n_el = 1;
-    for (auto v : shape) {
-        if (v == 0) throw Error("tensor: zero-sized mode");
-        n_el *= v;
-    }
-    if (nbytes != n_el * dtype_size(dtype))
-        throw Error("ingest: buffer holds " + std::to_string(nbytes) + " bytes, expected " +
-                    std::to_string(n_el * dtype_size(dtype)));
-    res.original_bytes = n_el * dtype_size(dtype);
-    if (prm.target_re && prm.target_sse)
-        throw Error("compress: relative-error and SSE targets are mutually exclusive");
-    if (!prm.target_re && !prm.target_sse) throw Error("compress: no error target given");
-    if (prm.method != 0) throw Error("compress: only lexicographic vectorization is implemented on the device path");
-
-    // ingest (container.cpp:69-94): the internal tensor in double; with
-    // internal_float32 the values are first rounded to float as the reference does
-    DevBuf<double> a(n_el, s);
-    if (prm.f32) {
-        DevBuf<float> af(n_el, s);
-        ingest_cast_f32(device_bytes, dtype, n_el, af.p, s);
-        ingest_cast(af.p, 8, n_el, a.p, s);
-        res.norm_sq = sum_squares(af.p, n_el, nullptr, s);
-    } else {
-        ingest_cast(device_bytes, dtype, n_el, a.p, s);
-        res.norm_sq = sum_squares(a.p, n_el, nullptr, s);
-    }
-    if (dtype == 6 || dtype == 7) res.precision_loss = ingest_precision_loss(device_bytes, dtype, n_el, s);
-    double target;
-    if (prm.target_re) {
-        if (*prm.target_re < 0) throw Error("budget: negative relative-error target");
-        target = *prm.target_re * *prm.target_re * res.norm_sq;
-    } else {
-        target = *prm.target_sse;
-    }
-    if (target < 0) throw Error("budget: negative SSE target");
-    if (prm.rtmss < 0 || prm.rtmss > 1) throw Error("budget: rtmss outside [0, 1]");
-    res.target_sse = target;
-
     auto t0 = Clock::now();
-    Tucker f = sthosvd_device(std::move(a), shape, prm.rtmss * target, prm.mode_order, prm.backend, s);
-    double trunc = 0;
-    for (double v : f.trunc) trunc += v;
-    double core_target = target - trunc;
-    if (core_target < 0) core_target = 0;
-    res.times.sthosvd = ms_since(t0);
-    res.trunc = trunc;
-    res.ranks = f.r;
-
     // phase 2: storage order + quantisation
-    t0 = Clock::now();
     std::vector<u64> storage = prm.storage_order ? *prm.storage_order : stable_ascending(f.core_shape);
     if (!valid_perm(storage, d)) throw Error("compress: invalid storage order");
     std::vector<u64> cs(d);
@@ -394,7 +370,7 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
         w.f64v(trunc);
         res.container = std::move(w.b);
         res.times.total = ms_since(t_all);
-        return res;
+        return;
     }
 
     std::vector<u64> mode_of(d);
@@ -484,7 +460,83 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     res.times.serialize = ms_since(t0);
     res.times.total = ms_since(t_all);
     res.peak_alloc = 2 * n_el * 8 + nc * 9 + res.container.size() * 2;
+}
+Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,
+                       const Params& prm, cudaStream_t s) {
+    const auto t_all = Clock::now();
+    Result res;
+    const std::size_t d = shape.size();
+    if (d == 0 || d > 8) throw Error("compress: tensor order must be between 1 and 8");
+    u64 n_el = 1;
+    for (auto v : shape) {
+        if (v == 0) throw Error("tensor: zero-sized mode");
+        n_el *= v;
+    }
+    if (nbytes != n_el * dtype_size(dtype))
+        throw Error("ingest: buffer holds " + std::to_string(nbytes) + " bytes, expected " +
+                    std::to_string(n_el * dtype_size(dtype)));
+    res.original_bytes = n_el * dtype_size(dtype);
+    if (prm.target_re && prm.target_sse)
+        throw Error("compress: relative-error and SSE targets are mutually exclusive");
+    if (!prm.target_re && !prm.target_sse) throw Error("compress: no error target given");
+    if (prm.method != 0) throw Error("compress: only lexicographic vectorization is implemented on the device path");
+
+    // ingest (container.cpp:69-94): the internal tensor in double; with
+    // internal_float32 the values are first rounded to float as the reference does
+    DevBuf<double> a(n_el, s);
+    if (prm.f32) {
+        DevBuf<float> af(n_el, s);
+        ingest_cast_f32(device_bytes, dtype, n_el, af.p, s);
+        ingest_cast(af.p, 8, n_el, a.p, s);
+        res.norm_sq = sum_squares(af.p, n_el, nullptr, s);
+    } else {
+        ingest_cast(device_bytes, dtype, n_el, a.p, s);
+        res.norm_sq = sum_squares(a.p, n_el, nullptr, s);
+    }
+    if (dtype == 6 || dtype == 7) res.precision_loss = ingest_precision_loss(device_bytes, dtype, n_el, s);
+    double target;
+    if (prm.target_re) {
+        if (*prm.target_re < 0) throw Error("budget: negative relative-error target");
+        target = *prm.target_re * *prm.target_re * res.norm_sq;
+    } else {
+        target = *prm.target_sse;
+    }
+    if (target < 0) throw Error("budget: negative SSE target");
+    if (prm.rtmss < 0 || prm.rtmss > 1) throw Error("budget: rtmss outside [0, 1]");
+    res.target_sse = target;
+
+    auto t0 = Clock::now();
+    Tucker f = sthosvd_device(std::move(a), shape, prm.rtmss * target, prm.mode_order, prm.backend, s);
+    double trunc = 0;
+    for (double v : f.trunc) trunc += v;
+    double core_target = target - trunc;
+    if (core_target < 0) core_target = 0;
+    res.times.sthosvd = ms_since(t0);
+    res.trunc = trunc;
+    res.ranks = f.r;
+
+    encode_into(res, f, shape, dtype, target, core_target, trunc, prm, s, t_all, n_el);
     return res;
 }
+
+Result encode_tucker_device(Tucker& f, int dtype, double norm_sq, double target, const Params& prm, cudaStream_t s) {
+    const auto t_all = Clock::now();
+    Result res;
+    const std::vector<u64> shape = f.n;
+    u64 n_el = 1;
+    for (auto v : shape) n_el *= v;
+    res.original_bytes = n_el * dtype_size(dtype);
+    res.norm_sq = norm_sq;
+    res.target_sse = target;
+    double trunc = 0;
+    for (double v : f.trunc) trunc += v;
+    double core_target = target - trunc;
+    if (core_target < 0) core_target = 0;
+    res.trunc = trunc;
+    res.ranks = f.r;
+    encode_into(res, f, shape, dtype, target, core_target, trunc, prm, s, t_all, n_el);
+    return res;
+}
+
 
 }  // namespace tcb

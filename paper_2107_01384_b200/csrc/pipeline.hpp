@@ -49,6 +49,16 @@ struct Tucker {
     std::vector<u64> n, r, order;
     std::vector<double> trunc;
 };
+// One mode step (sthosvd.cpp:136-166): factor U (rows x r, sign-fixed), the
+// discarded energy, and the projected/shifted tensor next = B^T U (cols x r).
+struct StepOut {
+    u64 r = 0;
+    double discarded = 0.0;
+    DevBuf<double> U, next;
+};
+StepOut mode_step(const double* x, u64 rows, u64 cols, double budget, int backend, cudaStream_t s);
+// eigensolve + rank rule + sign fix on an (all-reduced) Gram; U is n x r
+StepOut factor_from_gram(const double* G, u64 n, double budget, cudaStream_t s);
 // sthosvd::compress (sthosvd.cpp:114-171) on a device tensor (consumed)
 Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double target,
                       const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s);
@@ -63,6 +73,10 @@ struct FactorEnc {
     double term = 0;
     int plane = 0;
 };
+// Phases 2-5 of compress_impl on an existing device factorization (used by
+// the sharded multi-GPU mode loop, whose rank 0 encodes the gathered core).
+Result encode_tucker_device(Tucker& f, int dtype, double norm_sq, double target, const Params& p, cudaStream_t s);
+
 FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<u8>& dead,
                                const std::vector<double>& sn, int coder, bool simple, int core_step_log2,
                                double cap, bool f32, cudaStream_t s);

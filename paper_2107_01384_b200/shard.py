@@ -1,0 +1,229 @@
+"""Sharded multi-GPU ST-HOSVD mode loop (reference
+sthosvd.cpp:114-171 run across ranks).
+
+The tensor is partitioned along the LAST processed mode p[d-1]: rank k holds a
+contiguous slab of that mode.  Thanks to the circular shift (the TTM output of
+step s is the next step's tensor, sthosvd.cpp:158-166) the sharded mode moves
+one axis to the left per step and is never the contracted (row) axis before
+the last step, so for steps 0..d-2:
+
+    local Gram of the column shard -> all_reduce(SUM) -> replicated eigensolve
+    + rank rule (bitwise identical on every rank, deterministic kernels on an
+    identical Gram) -> shard-local TTM, no data exchange.
+
+Before the last step the (small) tensor is all-gathered along its leading axis
+and the last step runs replicated; rank 0 encodes the core.  If a middle step
+hits the rows > cols branch (sthosvd.cpp:75-76) its tensor is gathered along
+the sharded axis, the step runs replicated and every rank keeps its slab.
+
+`ops` supplies the per-rank compute: DeviceOps (B200 kernels through the C
+ABI, NCCL collectives) or, in the CPU tests, a numpy implementation.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import Params, TucompError, _check, _result, _CResult, lib
+
+
+def shard_bounds(extent: int, world: int, rank: int):
+    """Contiguous split of one mode: first `extent % world` ranks get one more."""
+    base, extra = divmod(extent, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def stable_ascending(shape):
+    return sorted(range(len(shape)), key=lambda i: (shape[i], i))
+
+
+class DeviceOps:
+    """B200 kernels on torch CUDA float64 tensors (device pointers into the C ABI)."""
+
+    @staticmethod
+    def _p(t):
+        return C.c_void_p(t.data_ptr())
+
+    def sumsq(self, x):
+        torch.cuda.synchronize()
+        out, fin = C.c_double(), C.c_int()
+        _check(lib().tcb_dev_sumsq(self._p(x), C.c_uint64(x.numel()), C.byref(out), C.byref(fin)))
+        return out.value, bool(fin.value)
+
+    def permute(self, x, perm):
+        shape = np.asarray(x.shape, np.uint64)
+        pm = np.asarray(perm, np.uint64)
+        out = torch.empty([x.shape[i] for i in perm], dtype=x.dtype, device=x.device)
+        torch.cuda.synchronize()
+        _check(lib().tcb_dev_permute(self._p(x), self._p(out), shape.ctypes.data_as(C.c_void_p),
+                                     pm.ctypes.data_as(C.c_void_p), x.dim()))
+        return out
+
+    def gram(self, b2):
+        rows, cols = b2.shape
+        g = torch.empty((rows, rows), dtype=torch.float64, device=b2.device)
+        torch.cuda.synchronize()
+        _check(lib().tcb_dev_gram(self._p(b2), C.c_uint64(rows), C.c_uint64(cols), self._p(g)))
+        return g
+
+    def factor_from_gram(self, g, budget):
+        n = g.shape[0]
+        u = torch.empty(n * n, dtype=torch.float64, device=g.device)
+        r, disc = C.c_uint64(), C.c_double()
+        torch.cuda.synchronize()
+        _check(lib().tcb_dev_factor_from_gram(self._p(g), C.c_uint64(n), C.c_double(budget), self._p(u),
+                                              C.byref(r), C.byref(disc)))
+        return u[: n * r.value].view(n, r.value), r.value, disc.value
+
+    def ttm(self, b2, u):
+        rows, cols = b2.shape
+        r = u.shape[1]
+        out = torch.empty((cols, r), dtype=torch.float64, device=b2.device)
+        torch.cuda.synchronize()
+        _check(lib().tcb_dev_ttm(self._p(b2), C.c_uint64(rows), C.c_uint64(cols), self._p(u.contiguous()),
+                                 C.c_uint64(r), self._p(out)))
+        return out
+
+    def mode_step(self, b2, budget, backend):
+        rows, cols = b2.shape
+        u = torch.empty(rows * rows, dtype=torch.float64, device=b2.device)
+        nx = torch.empty(cols * rows, dtype=torch.float64, device=b2.device)
+        r, disc = C.c_uint64(), C.c_double()
+        torch.cuda.synchronize()
+        _check(lib().tcb_dev_mode_step(self._p(b2), C.c_uint64(rows), C.c_uint64(cols), C.c_double(budget),
+                                       int(backend), self._p(u), self._p(nx), C.byref(r), C.byref(disc)))
+        return u[: rows * r.value].view(rows, r.value), nx[: cols * r.value].view(cols, r.value), r.value, disc.value
+
+    def encode(self, core, factors, n, r, order, trunc, dtype, norm_sq, target, params: Params):
+        d = len(n)
+        arr = lambda v, t: np.asarray(v, t)  # noqa: E731
+        na, ra, oa, ta = arr(n, np.uint64), arr(r, np.uint64), arr(order, np.uint64), arr(trunc, np.float64)
+        fptr = (C.c_void_p * d)(*[f.data_ptr() for f in factors])
+        res = _CResult()
+        torch.cuda.synchronize()
+        _check(lib().tcb_dev_encode_tucker(self._p(core), fptr, na.ctypes.data_as(C.c_void_p),
+                                           ra.ctypes.data_as(C.c_void_p), oa.ctypes.data_as(C.c_void_p),
+                                           ta.ctypes.data_as(C.c_void_p), d, int(dtype), C.c_double(norm_sq),
+                                           C.c_double(target), C.byref(params.to_c(d)), C.byref(res)))
+        return _result(res)
+
+
+@dataclass
+class ShardedTucker:
+    core: object            # processing-order core (replicated)
+    factors: list           # by original mode, n_i x r_i
+    ranks: list
+    order: list
+    trunc: list
+    norm_sq: float
+
+
+def _all_gather_cat(t, axis, group, world):
+    """Concatenate every rank's tensor along `axis` (extents may differ per rank)."""
+    if world == 1:
+        return t
+    sizes = [torch.zeros(1, dtype=torch.int64, device=t.device) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([t.shape[axis]], dtype=torch.int64, device=t.device), group=group)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(sizes)
+    pad_shape = list(t.shape)
+    pad_shape[axis] = mx
+    padded = torch.zeros(pad_shape, dtype=t.dtype, device=t.device)
+    padded.narrow(axis, 0, t.shape[axis]).copy_(t)
+    bufs = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(bufs, padded.contiguous(), group=group)
+    return torch.cat([b.narrow(axis, 0, s) for b, s in zip(bufs, sizes)], dim=axis).contiguous()
+
+
+def sthosvd_sharded(x_local, shape, target, ops, order=None, backend=0, group=None):
+    """ST-HOSVD over ranks; `x_local` is this rank's slab of mode order[-1]
+    (original axis order).  Returns the replicated factorization."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    d = len(shape)
+    p = list(order) if order is not None else stable_ascending(shape)
+    ssq, finite = ops.sumsq(x_local)
+    stats = torch.tensor([ssq, 0.0 if finite else 1.0], dtype=torch.float64, device=x_local.device)
+    if world > 1:
+        dist.all_reduce(stats, group=group)
+    if target < 0:
+        raise TucompError("sthosvd: negative SSE target")
+    if stats[1].item() != 0.0:
+        raise TucompError("sthosvd: input contains non-finite values")
+    xl = ops.permute(x_local, p)  # (n_p0, ..., n_p(d-1) local slab)
+    cur = list(xl.shape)
+    sh_axis = d - 1  # position of the sharded mode in `cur`
+    remaining = float(target)
+    factors, ranks, trunc = [None] * d, [0] * d, [0.0] * d
+    for step in range(d):
+        budget = remaining / float(d - step)
+        rows = cur[0]
+        if sh_axis == 0 or step == d - 1:
+            full = _all_gather_cat(xl.view(cur), 0, group, world) if sh_axis == 0 else xl.view(cur)
+            fc = list(full.shape)
+            u, nx, r, disc = ops.mode_step(full.view(fc[0], -1), budget, backend)
+            xl = nx
+            cur = fc[1:] + [r]
+            sh_axis = -1  # replicated from here on
+        else:
+            cols_local = int(np.prod(cur[1:]))
+            cols_t = torch.tensor([float(cols_local)], dtype=torch.float64, device=xl.device)
+            if world > 1:
+                dist.all_reduce(cols_t, group=group)
+            cols_global = int(cols_t.item())
+            via_gram = backend == 1 or (backend == 0 and rows <= cols_global)
+            if via_gram:
+                g = ops.gram(xl.view(rows, cols_local))
+                if world > 1:
+                    dist.all_reduce(g, group=group)
+                u, r, disc = ops.factor_from_gram(g, budget)
+                xl = ops.ttm(xl.view(rows, cols_local), u)
+                cur = cur[1:] + [r]
+                sh_axis -= 1
+            else:  # thin-SVD branch: gather along the sharded axis, step replicated, keep my slab
+                full = _all_gather_cat(xl.view(cur), sh_axis, group, world)
+                fc = list(full.shape)
+                u, nx, r, disc = ops.mode_step(full.view(fc[0], -1), budget, backend)
+                nfull = nx.view(fc[1:] + [r])
+                sh_axis -= 1
+                lo, hi = shard_bounds(fc[sh_axis + 1], world, rank)
+                xl = nfull.narrow(sh_axis, lo, hi - lo).contiguous()
+                cur = list(xl.shape)
+        remaining = max(0.0, remaining - disc)
+        trunc[p[step]] = disc
+        factors[p[step]] = u
+        ranks[p[step]] = r
+    return ShardedTucker(core=xl.view(cur), factors=factors, ranks=ranks, order=p, trunc=trunc,
+                         norm_sq=float(stats[0].item()))
+
+
+def compress_sharded(x_local, shape, dtype, params: Params, ops=None, group=None):
+    """pipeline::compress across the ranks of `group`; rank 0 returns the
+    CompressResult (container bytes), the other ranks return None."""
+    ops = ops or DeviceOps()
+    if params.target_re is not None and params.target_sse is not None:
+        raise TucompError("compress: relative-error and SSE targets are mutually exclusive")
+    if params.target_re is None and params.target_sse is None:
+        raise TucompError("compress: no error target given")
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    ssq, _ = ops.sumsq(x_local)
+    t = torch.tensor([ssq], dtype=torch.float64, device=x_local.device)
+    if world > 1:
+        dist.all_reduce(t, group=group)
+    norm_sq = float(t.item())
+    target = params.target_re ** 2 * norm_sq if params.target_re is not None else params.target_sse
+    if target < 0:
+        raise TucompError("budget: negative SSE target")
+    if not 0.0 <= params.rtmss <= 1.0:
+        raise TucompError("budget: rtmss outside [0, 1]")
+    f = sthosvd_sharded(x_local, shape, params.rtmss * target, ops, params.mode_order, params.svd_backend, group)
+    if rank != 0:
+        return None
+    return ops.encode(f.core.contiguous(), [u.contiguous() for u in f.factors], list(shape), f.ranks, f.order,
+                      f.trunc, dtype, norm_sq, target, params)
