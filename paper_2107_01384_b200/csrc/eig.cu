@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -68,7 +70,6 @@ __device__ __forceinline__ double warp_sum(double v) {
 constexpr int kTdThreads = 256;
 constexpr int kTdWarps = kTdThreads / 32;
 constexpr int kTdCluster = 16;
-constexpr int kTdPv = kTdCluster * kTdWarps;  // 128 partial p.v slots
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -81,6 +82,11 @@ __device__ __forceinline__ unsigned cluster_map(unsigned addr, unsigned rank) {
 __device__ __forceinline__ void st_async_f64(unsigned raddr, double v, unsigned rbar) {
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
                  "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_v2f64(unsigned raddr, double a, double b, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(rbar)
                  : "memory");
 }
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
@@ -99,21 +105,38 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
         : "memory");
 }
 
+#ifdef TCB_TRIDIAG_TIMING
+__device__ unsigned long long g_tri_phase[16 * 10];
+#define TRI_T(i)                                           \
+    do {                                                   \
+        const long long now_ = clock64();                  \
+        if (threadIdx.x == 0) tacc[i] += now_ - tprev;     \
+        tprev = now_;                                      \
+    } while (0)
+#else
+#define TRI_T(i) \
+    do {         \
+    } while (0)
+#endif
 __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __restrict__ Ag, int n,
                                                            double* __restrict__ d, double* __restrict__ e,
                                                            double* __restrict__ V, double* __restrict__ tau) {
     constexpr int C = kTdCluster;
+    constexpr int G = 8;  // rows per register group
+#ifdef TCB_TRIDIAG_TIMING
+    long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long tprev = clock64();
+#endif
     cg::cluster_group cl = cg::this_cluster();
     const int rank = static_cast<int>(cl.block_rank());
     extern __shared__ __align__(16) double sm[];
     __shared__ __align__(8) unsigned long long mbar[2];
     const int nloc = (n + C - 1) / C;
-    double* A = sm;                         // nloc x n
-    double* pbuf = A + nloc * n;            // 2 x n (remote-written p)
-    double* obuf = pbuf + 2 * n;            // 2 x n (remote-written pre-update column k+1)
-    double* rbuf = obuf + 2 * n;            // 2 x n (local replicated column k)
-    double* pvbuf = rbuf + 2 * n;           // 2 x kTdPv (remote-written)
-    double* ssbuf = pvbuf + 2 * kTdPv;      // 2 x kTdWarps (local)
+    double* A = sm;                                        // nloc x n (row slot li = global row li*C + rank)
+    double2* pobuf = reinterpret_cast<double2*>(A + ((nloc * n + 1) & ~1));  // 2 x n {p_i, pre-update A_i,k+1}
+    double* rbuf = reinterpret_cast<double*>(pobuf + 2 * n);  // 2 x n (local replicated column k)
+    double* part = rbuf + 2 * n;                           // kTdWarps x nloc (matvec partials)
+    double* ssbuf = part + kTdWarps * nloc; // 2 x kTdWarps
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         mbar_init(smem_addr(&mbar[0]), 1);
@@ -122,8 +145,8 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
     }
     for (int li = 0; li < nloc; ++li) {
         const int gi = li * C + rank;
-        if (gi >= n) break;
-        for (int j = threadIdx.x; j < n; j += blockDim.x) A[li * n + j] = Ag[static_cast<size_t>(gi) * n + j];
+        for (int j = threadIdx.x; j < n; j += blockDim.x)
+            A[li * n + j] = gi < n ? Ag[static_cast<size_t>(gi) * n + j] : 0.0;
     }
     {
         double ss = 0.0;
@@ -137,21 +160,19 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
     }
     __syncthreads();
     cl.sync();
-    // remote addresses of the receive buffers / mbarriers of CTA `lane` (lanes < C)
-    const unsigned my_p = smem_addr(pbuf), my_o = smem_addr(obuf), my_pv = smem_addr(pvbuf);
-    const unsigned dst = lane < C ? lane : 0;
-    const unsigned r_p = cluster_map(my_p, dst), r_o = cluster_map(my_o, dst), r_pv = cluster_map(my_pv, dst);
-    const unsigned r_bar0 = cluster_map(smem_addr(&mbar[0]), dst), r_bar1 = cluster_map(smem_addr(&mbar[1]), dst);
+    // push target of this thread: CTA dst = threadIdx.x % C (loop invariant)
+    const unsigned rpo = cluster_map(smem_addr(pobuf), threadIdx.x % C);
+    const unsigned rbar2[2] = {cluster_map(smem_addr(&mbar[0]), threadIdx.x % C),
+                               cluster_map(smem_addr(&mbar[1]), threadIdx.x % C)};
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1;
         const int buf = k & 1;
         const double* rowk = rbuf + buf * n;
         double* rnext = rbuf + (buf ^ 1) * n;
-        const double* p = pbuf + buf * n;
-        const double* orow = obuf + buf * n;
-        const double* pv = pvbuf + buf * kTdPv;
-        const unsigned rbar = buf ? r_bar1 : r_bar0;
-        if (threadIdx.x == 0) mbar_arrive_expect(smem_addr(&mbar[buf]), static_cast<unsigned>(16 * m + 8 * kTdPv));
+        const double2* po = pobuf + buf * n;
+        TRI_T(0);
+        if (threadIdx.x == 0)
+            mbar_arrive_expect(smem_addr(&mbar[buf]), static_cast<unsigned>(16 * m));
         double ss = 0.0;
 #pragma unroll
         for (int q = 0; q < kTdWarps; ++q) ss += ssbuf[buf * kTdWarps + q];
@@ -161,51 +182,57 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
         const double v0 = x0 - beta;
         const double vv = 2.0 * alpha * (alpha + fabs(x0));  // |x - beta e1|^2
         const double t = (alpha == 0.0 || vv == 0.0) ? 0.0 : 2.0 / vv;
-        const int first = k + 1 + ((rank - (k + 1)) % C + C) % C;  // first owned row >= k+1
-        const int stride = C * kTdWarps;
-        double pvw = 0.0;
-        for (int g0 = first + C * warp; g0 < n; g0 += 4 * stride) {
-            int gi[4];
-            const double* row[4];
-            double s[4];
+        const int li0 = (k + 1 - rank + C - 1) / C;  // first local slot with global row >= k+1
+        TRI_T(1);
+        // matvec partials: this warp's column slice j = k+2 + lane + 32*(warp + 8*q)
+        // for 16 rows at a time (column k+1, which needs v0, is added below so the
+        // sqrt/divide above overlap the loads); 16 values per lane are reduced
+        // across the warp by recursive halving (16+8+4+2+1 shuffles): afterwards
+        // lane l holds the sum for row (l >> 1) of the group.
+        for (int g0 = li0; g0 < nloc; g0 += 16) {
+            double s[16];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                gi[u] = g0 + u * stride;
-                row[u] = A + (min(gi[u], n - 1) / C) * n;
-                s[u] = 0.0;
+            for (int u = 0; u < 16; ++u) s[u] = 0.0;
+            for (int j = k + 2 + lane + 32 * warp; j < n; j += 32 * kTdWarps) {
+                const double vj = rowk[j];
+#pragma unroll
+                for (int u = 0; u < 16; ++u)
+                    if (g0 + u < nloc) s[u] += A[(g0 + u) * n + j] * vj;
             }
-            if (t != 0.0) {
-                if (lane == 0) {
+            if (warp == 0 && lane == 0) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) s[u] = row[u][k + 1] * v0;
-                }
-                for (int j = k + 2 + lane; j < n; j += 32) {
-                    const double vj = rowk[j];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) s[u] += row[u][j] * vj;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+                for (int u = 0; u < 16; ++u)
+                    if (g0 + u < nloc) s[u] += A[(g0 + u) * n + k + 1] * v0;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (gi[u] >= n) break;
-                const double su = s[u] * t;
-                pvw += su * (gi[u] == k + 1 ? v0 : rowk[gi[u]]);
-                const double col = row[u][k + 1];
-                if (lane < C) {
-                    const unsigned off = static_cast<unsigned>((buf * n + gi[u]) * sizeof(double));
-                    st_async_f64(r_p + off, su, rbar);
-                    st_async_f64(r_o + off, col, rbar);
+            for (int h = 8; h >= 1; h >>= 1) {  // keep the half selected by lane bit (h*2)
+                const bool up = (lane & (2 * h)) != 0;
+#pragma unroll
+                for (int u = 0; u < h; ++u) {
+                    const double send = up ? s[u] : s[u + h];
+                    const double recv = __shfl_xor_sync(0xffffffffu, send, 2 * h);
+                    s[u] = (up ? s[u + h] : s[u]) + recv;
                 }
             }
+            s[0] += __shfl_xor_sync(0xffffffffu, s[0], 1);
+            // lane bits 4..1 select the row: row = bit4*8 + bit3*4 + bit2*2 + bit1
+            const int row = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+            if ((lane & 1) == 0 && g0 + row < nloc) part[warp * nloc + g0 + row] = s[0];
         }
-        if (lane < C)
-            st_async_f64(r_pv + static_cast<unsigned>((buf * kTdPv + rank * kTdWarps + warp) * sizeof(double)), pvw,
-                         rbar);
+        __syncthreads();
+        // thread (li, dst = tid % C): finish p_li and push {p, pre-update A[gi][k+1]} to CTA dst
+        for (int li = li0 + static_cast<int>(threadIdx.x) / C; li < nloc; li += kTdThreads / C) {
+            const int gi = li * C + rank;
+            if (gi >= n) break;
+            double su = 0.0;
+#pragma unroll
+            for (int q = 0; q < kTdWarps; ++q) su += part[q * nloc + li];
+            st_async_v2f64(rpo + static_cast<unsigned>((buf * n + gi) * sizeof(double2)), su * t, A[li * n + k + 1],
+                           rbar2[buf]);
+        }
+        TRI_T(2);
         mbar_wait(smem_addr(&mbar[buf]), static_cast<unsigned>((k >> 1) & 1));
+        TRI_T(3);
         if (rank == k % C) {  // global outputs, off the exchange's critical path
             if (threadIdx.x == 0) {
                 e[k] = t == 0.0 ? x0 : beta;
@@ -215,53 +242,51 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
             for (int i = threadIdx.x; i < m; i += blockDim.x)
                 V[static_cast<size_t>(k) * n + k + 1 + i] = i == 0 ? v0 : rowk[k + 1 + i];
         }
+        // K = tau/2 p.v over the replicated p and v: same data, same order on every CTA
         double K = 0.0;
-        if (t != 0.0) {
-            K = pv[lane] + pv[lane + 32] + pv[lane + 64] + pv[lane + 96];
-            K = 0.5 * t * warp_sum(K);
-        }
-        const double wk1 = p[k + 1] - K * v0;
-        if (t != 0.0) {
-            for (int g0 = first + C * warp; g0 < n; g0 += 4 * stride) {
-                int gi[4];
-                double* row[4];
-                double vi[4], wi[4];
+        for (int q = k + 1 + lane; q < n; q += 32) K += po[q].x * (q == k + 1 ? v0 : rowk[q]);
+        K = 0.5 * t * warp_sum(K);
+        const double wk1 = po[k + 1].x - K * v0;
+        TRI_T(4);
+        // rank-2 update of this warp's column slice for every active row
+        for (int g0 = li0; g0 < nloc; g0 += G) {
+            double vi[G], wi[G];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    gi[u] = g0 + u * stride;
-                    const int gc = min(gi[u], n - 1);
-                    row[u] = A + (gc / C) * n;
-                    vi[u] = gc == k + 1 ? v0 : rowk[gc];
-                    wi[u] = p[gc] - K * vi[u];
-                }
-                if (lane == 0) {  // column k+1: v_{k+1} = v0
+            for (int u = 0; u < G; ++u) {
+                const int gi = min((g0 + u) * C + rank, n - 1);
+                vi[u] = gi == k + 1 ? v0 : rowk[gi];
+                wi[u] = po[gi].x - K * vi[u];
+            }
+            for (int j = k + 1 + lane + 32 * warp; j < n; j += 32 * kTdWarps) {
+                const double vjj = j == k + 1 ? v0 : rowk[j], wj = po[j].x - K * vjj;
+                double a[G];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (gi[u] < n) row[u][k + 1] = row[u][k + 1] - (vi[u] * wk1 + wi[u] * v0);
-                }
-                for (int j = k + 2 + lane; j < n; j += 32) {
-                    const double vjj = rowk[j], wj = p[j] - K * vjj;
+                for (int u = 0; u < G; ++u) a[u] = g0 + u < nloc ? A[(g0 + u) * n + j] : 0.0;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (gi[u] < n) row[u][j] = row[u][j] - (vi[u] * wj + wi[u] * vjj);
-                }
+                for (int u = 0; u < G; ++u)
+                    if (g0 + u < nloc && (g0 + u) * C + rank < n) A[(g0 + u) * n + j] = a[u] - (vi[u] * wj + wi[u] * vjj);
             }
         }
+        TRI_T(5);
         // updated row k+1 (= next column), rebuilt locally with the owner's expression
         double ssn = 0.0;
         for (int j = k + 1 + threadIdx.x; j < n; j += blockDim.x) {
-            double val = orow[j];
-            if (t != 0.0) {
-                const double vjj = j == k + 1 ? v0 : rowk[j], wj = p[j] - K * vjj;
-                val = val - (v0 * wj + wk1 * vjj);
-            }
+            const double2 pj = po[j];
+            const double vjj = j == k + 1 ? v0 : rowk[j], wj = pj.x - K * vjj;
+            const double val = pj.y - (v0 * wj + wk1 * vjj);
             rnext[j] = val;
             if (j >= k + 2) ssn += val * val;
         }
         ssn = warp_sum(ssn);
         if (lane == 0) ssbuf[(buf ^ 1) * kTdWarps + warp] = ssn;
+        TRI_T(6);
         __syncthreads();
+        TRI_T(7);
     }
+#ifdef TCB_TRIDIAG_TIMING
+    if (threadIdx.x == 0)
+        for (int i = 0; i < 8; ++i) g_tri_phase[rank * 10 + i] = tacc[i];
+#endif
     const double* rowl = rbuf + ((n - 2) & 1) * n;  // row n-2 after the last step
     if (rank == 0 && threadIdx.x == 0 && n >= 2) {
         d[n - 2] = rowl[n - 2];
@@ -776,9 +801,10 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
         bool dsmem = false;
         if (n <= kDsmemMaxN) {
             const int nloc = (n + kTdCluster - 1) / kTdCluster;
-            const size_t smem = (static_cast<size_t>(nloc) * n + 6 * n + 2 * kTdPv + 2 * kTdWarps) * sizeof(double);
+            const size_t smem = ((static_cast<size_t>(nloc) * n + 1) / 2 * 2 + 6 * n +
+                                 static_cast<size_t>(kTdWarps) * nloc + 2 * kTdWarps) * sizeof(double);
             static bool attr = [] {
-                cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
                 cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
                 return true;
             }();
@@ -788,7 +814,11 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
             at[0].val.clusterDim.x = kTdCluster;
             cfg.dynamicSmemBytes = smem;
             int ncl = 0;  // a 16-CTA cluster with this much shared memory must fit one GPC
-            dsmem = cudaOccupancyMaxActiveClusters(&ncl, tridiag_dsmem, &cfg) == cudaSuccess && ncl > 0;
+            const cudaError_t qe = cudaOccupancyMaxActiveClusters(&ncl, tridiag_dsmem, &cfg);
+            dsmem = qe == cudaSuccess && ncl > 0;
+            if (std::getenv("TCB_DEBUG"))
+                std::fprintf(stderr, "tridiag_dsmem n=%d smem=%zu clusters=%d err=%s\n", n, smem, ncl,
+                             cudaGetErrorString(qe));
             cudaGetLastError();
             if (dsmem) TCB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_dsmem, A, n, w.d.p, w.e.p, w.z.p, w.tau.p));
         }
@@ -893,3 +923,9 @@ void scale_orthonormalize(double* U, u64 n, u64 r, const double* sigma, cudaStre
 }
 
 }  // namespace tcb
+
+#ifdef TCB_TRIDIAG_TIMING
+namespace tcb {
+void tri_phase_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_tri_phase, sizeof(unsigned long long) * 160); }
+}  // namespace tcb
+#endif
