@@ -31,7 +31,7 @@ namespace {
 
 constexpr int kCluster = 8;
 constexpr int kTriThreads = 512;
-constexpr int kDsmemMaxN = 600;
+constexpr int kDsmemMaxN = 600;  // nloc <= 38: at most 2 row slots per warp
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -51,25 +51,29 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // ---------------------------------------------------------------- tridiagonalisation (DSMEM)
 // Row i lives in CTA (i % C), local slot i / C (C = 16-CTA cluster, the
-// non-portable maximum); the stored matrix stays bitwise symmetric (every
-// update is symmetric in (i, j)).  Per step k:
+// non-portable maximum).  One warp per row slot (slot li -> warp li % nw,
+// nw = min(nloc, 32) warps, so up to 1024 threads hide shared-memory
+// latency); lanes stride the columns.  Per step k:
 //   A. every CTA derives alpha/beta/tau from the replicated column k (rowk),
 //      whose |x|^2 partials were accumulated while it was built;
-//   B. each warp forms p_i = tau * A_i . v for up to 4 of its rows at once and
-//      pushes (p_i, A_i,k+1 = pre-update row k+1 by symmetry, partial p.v)
-//      into every CTA's double-buffered receive arrays with st.async, each
-//      store completing transaction bytes on the receiver's mbarrier;
-//   -- wait on the local mbarrier for 16 m + 1024 bytes (no cluster barrier,
+//   B. each warp forms p_i = tau A_i . v for its active rows (xor butterfly:
+//      every lane ends with the same bits) and lanes 0..C-1 push
+//      {p_i, pre-update A_i,k+1} to CTA `lane` with one 16-byte st.async that
+//      completes transaction bytes on the receiver's mbarrier; the CTA's sum
+//      of p_i v_i (fixed order) is pushed to every CTA the same way;
+//   -- wait on the local mbarrier for 16 m + 8 C bytes (no cluster barrier,
 //      no GPU-scope fence) --
-//   C. each CTA updates its rows with w = p - K v recomputed inline and
-//      rebuilds the updated row k+1 (next column) with the owner's exact
-//      expression; one CTA barrier.
-// Completion of step k+1's receive at any CTA implies every CTA finished
-// step k, so double buffering is enough for the write-after-read hazard.
+//   C. K = tau/2 (sum of the C partials, same order on every CTA); each warp
+//      updates its rows, A_ij -= v_i w_j + w_i v_j with w = p - K v, and every
+//      CTA rebuilds the updated row k+1 (the next column) from the pushed
+//      pre-update column with one shared expression; one CTA barrier.
+// Step k+1's pushes into a CTA's buffer (k+1)&1 are issued only after the
+// sender passed step k's wait, i.e. after every CTA finished step k-1, the
+// last reader of that buffer, so double buffering is enough.
 // Outputs d, e, V (reflector k at V[k*n + i], i >= k+1), tau.
-constexpr int kTdThreads = 256;
-constexpr int kTdWarps = kTdThreads / 32;
 constexpr int kTdCluster = 16;
+constexpr int kTdMaxWarps = 32;
+constexpr int kTdMaxRowsPerWarp = 2;  // nloc <= 64, i.e. n <= 1024
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -118,11 +122,10 @@ __device__ unsigned long long g_tri_phase[16 * 10];
     do {         \
     } while (0)
 #endif
-__global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __restrict__ Ag, int n,
-                                                           double* __restrict__ d, double* __restrict__ e,
-                                                           double* __restrict__ V, double* __restrict__ tau) {
+__global__ void __launch_bounds__(1024) tridiag_dsmem(const double* __restrict__ Ag, int n, double* __restrict__ d,
+                                                      double* __restrict__ e, double* __restrict__ V,
+                                                      double* __restrict__ tau) {
     constexpr int C = kTdCluster;
-    constexpr int G = 8;  // rows per register group
 #ifdef TCB_TRIDIAG_TIMING
     long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tprev = clock64();
@@ -131,12 +134,14 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
     const int rank = static_cast<int>(cl.block_rank());
     extern __shared__ __align__(16) double sm[];
     __shared__ __align__(8) unsigned long long mbar[2];
+    __shared__ double red[kTdMaxWarps];        // per-warp sums of p_i v_i
+    __shared__ double ssbuf[2 * kTdMaxWarps];  // per-warp |next column|^2 partials
+    __shared__ double kbuf[2 * C];             // remote-written CTA sums of p_i v_i
     const int nloc = (n + C - 1) / C;
-    double* A = sm;                                        // nloc x n (row slot li = global row li*C + rank)
+    const int nw = static_cast<int>(blockDim.x >> 5);
+    double* A = sm;                                                           // nloc x n
     double2* pobuf = reinterpret_cast<double2*>(A + ((nloc * n + 1) & ~1));  // 2 x n {p_i, pre-update A_i,k+1}
-    double* rbuf = reinterpret_cast<double*>(pobuf + 2 * n);  // 2 x n (local replicated column k)
-    double* part = rbuf + 2 * n;                           // kTdWarps x nloc (matvec partials)
-    double* ssbuf = part + kTdWarps * nloc; // 2 x kTdWarps
+    double* rbuf = reinterpret_cast<double*>(pobuf + 2 * n);                  // 2 x n replicated column k
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         mbar_init(smem_addr(&mbar[0]), 1);
@@ -160,79 +165,88 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
     }
     __syncthreads();
     cl.sync();
-    // push target of this thread: CTA dst = threadIdx.x % C (loop invariant)
-    const unsigned rpo = cluster_map(smem_addr(pobuf), threadIdx.x % C);
-    const unsigned rbar2[2] = {cluster_map(smem_addr(&mbar[0]), threadIdx.x % C),
-                               cluster_map(smem_addr(&mbar[1]), threadIdx.x % C)};
+    // push target of this lane: CTA lane % C (loop invariant)
+    const unsigned dst = static_cast<unsigned>(lane & (C - 1));
+    const unsigned rpo = cluster_map(smem_addr(pobuf), dst), rkb = cluster_map(smem_addr(kbuf), dst);
+    const unsigned rbar[2] = {cluster_map(smem_addr(&mbar[0]), dst), cluster_map(smem_addr(&mbar[1]), dst)};
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1;
         const int buf = k & 1;
         const double* rowk = rbuf + buf * n;
         double* rnext = rbuf + (buf ^ 1) * n;
         const double2* po = pobuf + buf * n;
+        const double* kb = kbuf + buf * C;
         TRI_T(0);
-        if (threadIdx.x == 0)
-            mbar_arrive_expect(smem_addr(&mbar[buf]), static_cast<unsigned>(16 * m));
-        double ss = 0.0;
+        if (threadIdx.x == 0) mbar_arrive_expect(smem_addr(&mbar[buf]), static_cast<unsigned>(16 * m + 8 * C));
+        // this warp's active row slots (warp-uniform)
+        int li[kTdMaxRowsPerWarp];
+        bool act[kTdMaxRowsPerWarp];
 #pragma unroll
-        for (int q = 0; q < kTdWarps; ++q) ss += ssbuf[buf * kTdWarps + q];
+        for (int r = 0; r < kTdMaxRowsPerWarp; ++r) {
+            li[r] = warp + r * nw;
+            const int gi = li[r] * C + rank;
+            act[r] = li[r] < nloc && gi >= k + 1 && gi < n;
+        }
+        // B1. matvec over columns j >= k+2 (independent of alpha, so it overlaps the sqrt/divide)
+        double acc[kTdMaxRowsPerWarp];
+#pragma unroll
+        for (int r = 0; r < kTdMaxRowsPerWarp; ++r) {
+            acc[r] = 0.0;
+            if (act[r]) {
+                const double* Ar = A + li[r] * n;
+                double a2 = 0.0;
+                int j = k + 2 + lane;
+                for (; j + 32 < n; j += 64) {
+                    acc[r] = fma(Ar[j], rowk[j], acc[r]);
+                    a2 = fma(Ar[j + 32], rowk[j + 32], a2);
+                }
+                if (j < n) acc[r] = fma(Ar[j], rowk[j], acc[r]);
+                acc[r] += a2;
+            }
+        }
+        // A. reflector of column k
+        double ss = 0.0;
+        for (int q = 0; q < nw; ++q) ss += ssbuf[buf * kTdMaxWarps + q];
         const double alpha = sqrt(ss);
         const double x0 = rowk[k + 1];
         const double beta = x0 >= 0.0 ? -alpha : alpha;
         const double v0 = x0 - beta;
         const double vv = 2.0 * alpha * (alpha + fabs(x0));  // |x - beta e1|^2
         const double t = (alpha == 0.0 || vv == 0.0) ? 0.0 : 2.0 / vv;
-        const int li0 = (k + 1 - rank + C - 1) / C;  // first local slot with global row >= k+1
         TRI_T(1);
-        // matvec partials: this warp's column slice j = k+2 + lane + 32*(warp + 8*q)
-        // for 16 rows at a time (column k+1, which needs v0, is added below so the
-        // sqrt/divide above overlap the loads); 16 values per lane are reduced
-        // across the warp by recursive halving (16+8+4+2+1 shuffles): afterwards
-        // lane l holds the sum for row (l >> 1) of the group.
-        for (int g0 = li0; g0 < nloc; g0 += 16) {
-            double s[16];
+        // B2. finish p_i, push {p_i, A_i,k+1} and the CTA's p.v partial
+        double p[kTdMaxRowsPerWarp], vi[kTdMaxRowsPerWarp];
+        double kp = 0.0;
 #pragma unroll
-            for (int u = 0; u < 16; ++u) s[u] = 0.0;
-            for (int j = k + 2 + lane + 32 * warp; j < n; j += 32 * kTdWarps) {
-                const double vj = rowk[j];
+        for (int r = 0; r < kTdMaxRowsPerWarp; ++r) {
+            p[r] = 0.0;
+            vi[r] = 0.0;
+            if (act[r]) {
+                const int gi = li[r] * C + rank;
+                const double ak1 = A[li[r] * n + k + 1];
+                double s = acc[r] + (lane == 0 ? ak1 * v0 : 0.0);
 #pragma unroll
-                for (int u = 0; u < 16; ++u)
-                    if (g0 + u < nloc) s[u] += A[(g0 + u) * n + j] * vj;
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                p[r] = t * s;
+                vi[r] = gi == k + 1 ? v0 : rowk[gi];
+                kp += p[r] * vi[r];
+                if (lane < C)
+                    st_async_v2f64(rpo + static_cast<unsigned>((buf * n + gi) * sizeof(double2)), p[r], ak1,
+                                   rbar[buf]);
             }
-            if (warp == 0 && lane == 0) {
-#pragma unroll
-                for (int u = 0; u < 16; ++u)
-                    if (g0 + u < nloc) s[u] += A[(g0 + u) * n + k + 1] * v0;
-            }
-#pragma unroll
-            for (int h = 8; h >= 1; h >>= 1) {  // keep the half selected by lane bit (h*2)
-                const bool up = (lane & (2 * h)) != 0;
-#pragma unroll
-                for (int u = 0; u < h; ++u) {
-                    const double send = up ? s[u] : s[u + h];
-                    const double recv = __shfl_xor_sync(0xffffffffu, send, 2 * h);
-                    s[u] = (up ? s[u + h] : s[u]) + recv;
-                }
-            }
-            s[0] += __shfl_xor_sync(0xffffffffu, s[0], 1);
-            // lane bits 4..1 select the row: row = bit4*8 + bit3*4 + bit2*2 + bit1
-            const int row = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-            if ((lane & 1) == 0 && g0 + row < nloc) part[warp * nloc + g0 + row] = s[0];
         }
+        if (lane == 0) red[warp] = kp;
+        TRI_T(9);
         __syncthreads();
-        // thread (li, dst = tid % C): finish p_li and push {p, pre-update A[gi][k+1]} to CTA dst
-        for (int li = li0 + static_cast<int>(threadIdx.x) / C; li < nloc; li += kTdThreads / C) {
-            const int gi = li * C + rank;
-            if (gi >= n) break;
-            double su = 0.0;
-#pragma unroll
-            for (int q = 0; q < kTdWarps; ++q) su += part[q * nloc + li];
-            st_async_v2f64(rpo + static_cast<unsigned>((buf * n + gi) * sizeof(double2)), su * t, A[li * n + k + 1],
-                           rbar2[buf]);
-        }
         TRI_T(2);
-        mbar_wait(smem_addr(&mbar[buf]), static_cast<unsigned>((k >> 1) & 1));
+        if (warp == 0 && lane < C) {
+            double s = 0.0;
+            for (int q = 0; q < nw; ++q) s += red[q];
+            st_async_f64(rkb + static_cast<unsigned>((buf * C + rank) * sizeof(double)), s, rbar[buf]);
+        }
         TRI_T(3);
+        mbar_wait(smem_addr(&mbar[buf]), static_cast<unsigned>((k >> 1) & 1));
+        TRI_T(4);
         if (rank == k % C) {  // global outputs, off the exchange's critical path
             if (threadIdx.x == 0) {
                 e[k] = t == 0.0 ? x0 : beta;
@@ -242,33 +256,27 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
             for (int i = threadIdx.x; i < m; i += blockDim.x)
                 V[static_cast<size_t>(k) * n + k + 1 + i] = i == 0 ? v0 : rowk[k + 1 + i];
         }
-        // K = tau/2 p.v over the replicated p and v: same data, same order on every CTA
-        double K = 0.0;
-        for (int q = k + 1 + lane; q < n; q += 32) K += po[q].x * (q == k + 1 ? v0 : rowk[q]);
-        K = 0.5 * t * warp_sum(K);
+        // K = tau/2 p.v: butterfly over the C partials, identical bits on every lane and CTA
+        double K = kb[lane & (C - 1)];
+#pragma unroll
+        for (int o = C / 2; o > 0; o >>= 1) K += __shfl_xor_sync(0xffffffffu, K, o);
+        K *= 0.5 * t;
         const double wk1 = po[k + 1].x - K * v0;
-        TRI_T(4);
-        // rank-2 update of this warp's column slice for every active row
-        for (int g0 = li0; g0 < nloc; g0 += G) {
-            double vi[G], wi[G];
+        TRI_T(5);
+        // C. rank-2 update of this warp's rows
 #pragma unroll
-            for (int u = 0; u < G; ++u) {
-                const int gi = min((g0 + u) * C + rank, n - 1);
-                vi[u] = gi == k + 1 ? v0 : rowk[gi];
-                wi[u] = po[gi].x - K * vi[u];
-            }
-            for (int j = k + 1 + lane + 32 * warp; j < n; j += 32 * kTdWarps) {
-                const double vjj = j == k + 1 ? v0 : rowk[j], wj = po[j].x - K * vjj;
-                double a[G];
-#pragma unroll
-                for (int u = 0; u < G; ++u) a[u] = g0 + u < nloc ? A[(g0 + u) * n + j] : 0.0;
-#pragma unroll
-                for (int u = 0; u < G; ++u)
-                    if (g0 + u < nloc && (g0 + u) * C + rank < n) A[(g0 + u) * n + j] = a[u] - (vi[u] * wj + wi[u] * vjj);
+        for (int r = 0; r < kTdMaxRowsPerWarp; ++r) {
+            if (act[r]) {
+                double* Ar = A + li[r] * n;
+                const double wi = p[r] - K * vi[r];
+                for (int j = k + 1 + lane; j < n; j += 32) {
+                    const double vjj = j == k + 1 ? v0 : rowk[j], wj = po[j].x - K * vjj;
+                    Ar[j] = Ar[j] - (vi[r] * wj + wi * vjj);
+                }
             }
         }
-        TRI_T(5);
-        // updated row k+1 (= next column), rebuilt locally with the owner's expression
+        TRI_T(6);
+        // updated row k+1 (= next column), rebuilt on every CTA from the pushed pre-update column
         double ssn = 0.0;
         for (int j = k + 1 + threadIdx.x; j < n; j += blockDim.x) {
             const double2 pj = po[j];
@@ -278,14 +286,14 @@ __global__ void __launch_bounds__(kTdThreads) tridiag_dsmem(const double* __rest
             if (j >= k + 2) ssn += val * val;
         }
         ssn = warp_sum(ssn);
-        if (lane == 0) ssbuf[(buf ^ 1) * kTdWarps + warp] = ssn;
-        TRI_T(6);
-        __syncthreads();
+        if (lane == 0) ssbuf[(buf ^ 1) * kTdMaxWarps + warp] = ssn;
         TRI_T(7);
+        __syncthreads();
+        TRI_T(8);
     }
 #ifdef TCB_TRIDIAG_TIMING
     if (threadIdx.x == 0)
-        for (int i = 0; i < 8; ++i) g_tri_phase[rank * 10 + i] = tacc[i];
+        for (int i = 0; i < 10; ++i) g_tri_phase[rank * 10 + i] = tacc[i];
 #endif
     const double* rowl = rbuf + ((n - 2) & 1) * n;  // row n-2 after the last step
     if (rank == 0 && threadIdx.x == 0 && n >= 2) {
@@ -801,16 +809,15 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
         bool dsmem = false;
         if (n <= kDsmemMaxN) {
             const int nloc = (n + kTdCluster - 1) / kTdCluster;
-            const size_t smem = ((static_cast<size_t>(nloc) * n + 1) / 2 * 2 + 6 * n +
-                                 static_cast<size_t>(kTdWarps) * nloc + 2 * kTdWarps) * sizeof(double);
+            const size_t smem = ((static_cast<size_t>(nloc) * n + 1) / 2 * 2 + 6 * n) * sizeof(double);
             static bool attr = [] {
-                cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+                cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
                 cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
                 return true;
             }();
             (void)attr;
             cfg.gridDim = dim3(kTdCluster);
-            cfg.blockDim = dim3(kTdThreads);
+            cfg.blockDim = dim3(32 * std::min(nloc, kTdMaxWarps));
             at[0].val.clusterDim.x = kTdCluster;
             cfg.dynamicSmemBytes = smem;
             int ncl = 0;  // a 16-CTA cluster with this much shared memory must fit one GPC
