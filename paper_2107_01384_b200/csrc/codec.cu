@@ -617,11 +617,12 @@ __host__ __device__ inline u64 ac_model_words(u32 cap) {
     return ((w + 1) & ~u64{1}) + 2ull * cap;
 }
 
-// One warp per stream.  All lanes run the range coder redundantly (identical
-// state); the adaptive model (entropy.cpp:155-239) is probed and updated
-// cooperatively: hash lookups test 32 slots per ballot, prefix(i) is a
-// 3-level (1 / 32 / 1024) count sum reduced in one warp shuffle tree, and
-// halving rescales the counts with all lanes.  Lane 0 writes the bytes.
+// One warp per stream.  The adaptive model (entropy.cpp:155-239) is resolved
+// 32 symbols at a time (see the chunk comment below); all lanes then run the
+// range coder redundantly (identical state) and lane 0 writes the bytes.
+// Counts keep a 3-level (1 / 32 / 1024) prefix structure; halving rescales
+// them with all lanes.
+template <bool kShared>
 __global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, const StreamOut* __restrict__ sout,
                                                 const AcDesc* __restrict__ desc, const int* __restrict__ ids,
                                                 int nstreams, u8* __restrict__ outbuf, u32* __restrict__ scratch,
@@ -636,8 +637,9 @@ __global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, co
         return;
     }
     const AcDesc d = desc[sidx];
-    const u32 cap = smem_cap > 0 ? min(d.cap, smem_cap) : d.cap;
-    u32* base = smem_cap > 0 ? reinterpret_cast<u32*>(ac_smem) : scratch + d.model_off;
+    // kShared: the model lives in shared memory (LDS/STS, no generic accesses)
+    const u32 cap = kShared ? min(d.cap, smem_cap) : d.cap;
+    u32* base = kShared ? reinterpret_cast<u32*>(ac_smem) : scratch + d.model_off;
     u32* cnt = base;
     u32* l1 = cnt + cap;
     u32* l2 = l1 + (cap / 32 + 1);
@@ -645,9 +647,11 @@ __global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, co
     const u32 hb = log2_at_least(2 * cap);
     const u32 hmask = (1u << hb) - 1;
     u64* val = reinterpret_cast<u64*>(base + ((cap + (cap / 32 + 1) + (cap / 1024 + 1) + (1u << hb) + 1) & ~1u));
+    for (u32 i = lane; i < cap; i += 32) cnt[i] = 0;
     for (u32 i = lane; i <= cap / 32; i += 32) l1[i] = 0;
     for (u32 i = lane; i <= cap / 1024; i += 32) l2[i] = 0;
     for (u32 i = lane; i < (1u << hb); i += 32) hidx[i] = 0;
+    __syncwarp();
     u8* out = outbuf + d.out_off;
     if (lane == 0) {
         out[0] = 0;  // coder id: arithmetic
@@ -687,15 +691,6 @@ __global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, co
         }
     };
     u32 nsym = 1, total = 1;
-    auto below = [&](u32 i) {  // sum of cnt[0..i)
-        const u32 b1 = i >> 5, b2 = i >> 10;
-        u32 s = 0;
-        if ((b1 << 5) + lane < i) s += cnt[(b1 << 5) + lane];
-        if ((b2 << 5) + lane < b1) s += l1[(b2 << 5) + lane];
-        for (u32 b = lane; b < b2; b += 32) s += l2[b];
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        return s;
-    };
     auto halve = [&]() {
         __syncwarp();
         for (u32 i = lane; i <= cap / 32; i += 32) l1[i] = 0;
@@ -721,75 +716,126 @@ __global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, co
         total = t;
         __syncwarp();
     };
+    // Chunked model: between halvings the adaptive model (entropy.cpp:155-239)
+    // has a closed form, so 32 symbols (lane l <-> symbol t0 + l) resolve in
+    // parallel against the model as of t0:
+    //   index I: hash lookup, else a new symbol; repeats inside the chunk share
+    //            the first occurrence's index (match_any), new indices follow
+    //            first-occurrence order (ballot prefix);
+    //   cum     = count below I at t0 + 32 * #{earlier chunk symbols with index < I};
+    //   freq    = count of I at t0 + 32 * #{earlier chunk occurrences of I};
+    //   total   = total(t0) + 32 l; escapes code (0, cnt[0] = 1, total).
+    // A chunk ends at the first halving point (after coding the symbol whose
+    // pre-update total + 32 reaches 2^16), applied between that symbol's
+    // coding and its increment.  Only the range-coder arithmetic is sequential.
     const u64* sy = syms + d.sym_off;
-    for (u64 tt = 0; tt < ns; ++tt) {
-        const u64 s = sy[tt];
-        // probe 32 hash slots per round: stop at the first match or the first empty slot
-        u32 h = static_cast<u32>((s * 0x9E3779B97F4A7C15ull) >> (64 - hb));
-        int found = -1;
-        u32 empty_slot = 0;
-        while (true) {
-            const u32 slot = (h + lane) & hmask;
-            const u32 e = hidx[slot];
-            const bool match = e != 0 && val[e - 1] == s;
-            const unsigned mm = __ballot_sync(0xffffffffu, match);
-            const unsigned me = __ballot_sync(0xffffffffu, e == 0);
-            const int fm = mm ? __ffs(mm) - 1 : 32, fe = me ? __ffs(me) - 1 : 32;
-            if (fm < fe) {
-                found = static_cast<int>(__shfl_sync(0xffffffffu, e, fm)) - 1;
-                break;
+    const unsigned below_me = (1u << lane) - 1u;
+    u64 cur = lane < ns ? sy[lane] : 0;
+    for (u64 t0 = 0; t0 < ns;) {
+        u32 L = static_cast<u32>(ns - t0 < 32 ? ns - t0 : 32);
+        // first l with total + 32 l + 32 >= 2^16 (total < 2^16 between symbols)
+        const u32 lh = total >= 65504u ? 0u : (65504u - total + 31u) / 32u;
+        const bool halv = lh < L;
+        if (halv) L = lh + 1;
+        const u64 nxt = t0 + L + lane < ns ? sy[t0 + L + lane] : 0;  // next chunk, in flight
+        const bool act = static_cast<u32>(lane) < L;
+        const u64 sv = cur;
+        int I = -1;
+        if (act) {
+            u32 h = hslot(sv, hb);
+            while (true) {
+                const u32 e = hidx[h];
+                if (e == 0) break;
+                if (val[e - 1] == sv) {
+                    I = static_cast<int>(e) - 1;
+                    break;
+                }
+                h = (h + 1) & hmask;
             }
-            if (fe < 32) {
-                empty_slot = (h + fe) & hmask;
-                break;
-            }
-            h = (h + 32) & hmask;
         }
-        if (found >= 0) {
-            const u32 i = static_cast<u32>(found);
-            const u32 cum = below(i);
-            const u32 f = cnt[i];
-            range /= total;
-            low += static_cast<u64>(cum) * range;
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        const unsigned same = __match_any_sync(0xffffffffu, sv) & am;
+        const int leader = act ? __ffs(same) - 1 : lane;
+        const bool isnew = act && I < 0 && leader == lane;
+        const unsigned newm = __ballot_sync(0xffffffffu, isnew);
+        if (nsym + __popc(newm) > cap) {  // model full: rerun from global scratch
+            if (lane == 0) {
+                *redo = 1;
+                elen[sidx] = ~u64{0};
+            }
+            return;
+        }
+        if (isnew) I = static_cast<int>(nsym + __popc(newm & below_me));
+        const int IL = __shfl_sync(0xffffffffu, I, leader);
+        if (act && I < 0) I = IL;
+        u32 base = 0, f0 = 0;
+        if (act) {
+            const u32 ui = static_cast<u32>(I);
+            if (ui < nsym) {
+                const u32 b1 = ui >> 5, b2 = ui >> 10;
+                for (u32 j = b1 << 5; j < ui; ++j) base += cnt[j];
+                for (u32 j = b2 << 5; j < b1; ++j) base += l1[j];
+                for (u32 j = 0; j < b2; ++j) base += l2[j];
+                f0 = cnt[ui];
+            } else {
+                base = total;  // every index present at t0 is below a new one
+            }
+        }
+        u32 within = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int Ij = __shfl_sync(0xffffffffu, I, j);
+            within += (j < lane && Ij < I) ? 1u : 0u;
+        }
+        const u32 cum = isnew ? 0u : base + 32u * within;
+        const u32 freq = isnew ? 1u : f0 + 32u * __popc(same & below_me);
+        const u32 tot = total + 32u * static_cast<u32>(lane);
+        // range coder over the chunk (identical state in every lane)
+        for (u32 l = 0; l < L; ++l) {
+            const u32 c = __shfl_sync(0xffffffffu, cum, l), f = __shfl_sync(0xffffffffu, freq, l);
+            const u32 T = __shfl_sync(0xffffffffu, tot, l);
+            const u64 v = __shfl_sync(0xffffffffu, sv, l);
+            range /= T;
+            low += static_cast<u64>(c) * range;
             range *= f;
             norm();
-            if (total + 32 >= (1u << 16)) halve();
-            __syncwarp();
-            if (lane == 0) {
-                cnt[i] += 32;
-                l1[i >> 5] += 32;
-                l2[i >> 10] += 32;
-            }
-            total += 32;
-        } else {
-            if (nsym >= cap) {  // shared-memory model full: rerun from global scratch
-                if (lane == 0) {
-                    *redo = 1;
-                    elen[sidx] = ~u64{0};
+            if ((newm >> l) & 1u) {
+                for (int b = 31; b >= 0; --b) {  // 32 raw bits as encode(bit, 1, 2)
+                    range >>= 1;
+                    if ((v >> b) & 1u) low += range;
+                    norm();
                 }
-                return;
             }
-            range /= total;  // escape occupies [0, cnt[0])
-            range *= cnt[0];
-            norm();
-            for (int b = 31; b >= 0; --b) {  // 32 raw bits as encode(bit, 1, 2)
-                range >>= 1;
-                if ((s >> b) & 1u) low += range;
-                norm();
+        }
+        // model update: increments in symbol order, a halving before the last one
+        auto inc = [&](bool doit) {
+            if (!doit) return;
+            const u32 ui = static_cast<u32>(I);
+            if (isnew) {
+                val[ui] = sv;
+                u32 h = hslot(sv, hb);
+                while (atomicCAS(&hidx[h], 0u, ui + 1u) != 0u) h = (h + 1) & hmask;
             }
-            if (total + 32 >= (1u << 16)) halve();
-            __syncwarp();
-            const u32 i = nsym++;
-            if (lane == 0) {
-                val[i] = s;
-                cnt[i] = 32;
-                l1[i >> 5] += 32;
-                l2[i >> 10] += 32;
-                hidx[empty_slot] = i + 1;
-            }
-            total += 32;
+            atomicAdd(&cnt[ui], 32u);
+            atomicAdd(&l1[ui >> 5], 32u);
+            atomicAdd(&l2[ui >> 10], 32u);
+        };
+        if (halv) {
+            const unsigned lastbit = 1u << (L - 1);
+            inc(act && static_cast<u32>(lane) != L - 1);
+            nsym += __popc(newm & ~lastbit);
+            halve();
+            inc(static_cast<u32>(lane) == L - 1);
+            nsym += (newm & lastbit) ? 1u : 0u;
+            total += 32u;
+        } else {
+            inc(act);
+            nsym += __popc(newm);
+            total += 32u * L;
         }
         __syncwarp();
+        t0 += L;
+        cur = nxt;
     }
     for (int i = 0; i < 5; ++i) shift();
     if (lane == 0) elen[sidx] = pos;
@@ -808,7 +854,7 @@ void run_ac(const u64* syms, const StreamOut* so, const AcDesc* dad, const std::
     }
     const u64 smem = ac_model_words(need) * 4 + 16;
     static bool attr = [] {
-        cudaFuncSetAttribute(ac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(ac_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(ac_model_words(kAcSmemCap) * 4 + 16));
         return true;
     }();
@@ -817,7 +863,7 @@ void run_ac(const u64* syms, const StreamOut* so, const AcDesc* dad, const std::
     redo.zero();
     {
         ProfScope pa(kAc, s);
-        ac_kernel<<<static_cast<unsigned>(ns), 32, smem, s>>>(syms, so, dad, nullptr, ns, ent, scratch, elen, need,
+        ac_kernel<true><<<static_cast<unsigned>(ns), 32, smem, s>>>(syms, so, dad, nullptr, ns, ent, scratch, elen, need,
                                                              redo.p);
     }
     count_launch();
@@ -833,7 +879,7 @@ void run_ac(const u64* syms, const StreamOut* so, const AcDesc* dad, const std::
     dids.upload(ids.data(), ids.size());
     {
         ProfScope pa(kAc, s);
-        ac_kernel<<<static_cast<unsigned>(ids.size()), 32, 0, s>>>(syms, so, dad, dids.p, ns, ent, scratch, elen, 0,
+        ac_kernel<false><<<static_cast<unsigned>(ids.size()), 32, 0, s>>>(syms, so, dad, dids.p, ns, ent, scratch, elen, 0,
                                                                   redo.p);
     }
     count_launch();

@@ -156,6 +156,22 @@ def test_encode_symbols_bit_exact(gpu_pkg, seed):
     assert gpu_pkg.encode_symbols(0, []) == oracle.encode_symbols(0, [])
 
 
+@pytest.mark.parametrize("kind", ["constant", "distinct", "long", "runs"])
+def test_encode_symbols_model_edges(gpu_pkg, kind):
+    """Chunked adaptive model: repeats inside a chunk, > 2048 distinct symbols
+    (shared-memory model overflow -> global-scratch rerun), many halvings."""
+    rng = np.random.default_rng(7)
+    if kind == "constant":
+        syms = np.zeros(5000, np.uint64)
+    elif kind == "distinct":
+        syms = rng.permutation(np.arange(6000, dtype=np.uint64) * 2654435761 % (2 ** 32))
+    elif kind == "long":
+        syms = (rng.geometric(0.2, 40000) - 1).astype(np.uint64)
+    else:
+        syms = np.repeat(rng.integers(0, 40, 700), rng.integers(1, 60, 700)).astype(np.uint64)
+    assert gpu_pkg.encode_symbols(0, syms) == oracle.encode_symbols(0, syms)
+
+
 # ---------------------------------------------------------------- factor codec
 @pytest.mark.parametrize("n,r", [(40, 10), (64, 59), (30, 30), (1, 1), (100, 3)])
 def test_factor_stream_matches_oracle(gpu_pkg, n, r):
