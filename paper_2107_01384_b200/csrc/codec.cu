@@ -548,64 +548,12 @@ struct AcDesc {
     u32 pad;
 };
 
-struct AcState {
-    u64 low;
-    u32 range;
-    u8 cache;
-    u64 pending;
-    u8* out;
-    u64 pos;
-};
-
-__device__ __forceinline__ void ac_shift(AcState& s) {
-    if (static_cast<u32>(s.low) < 0xFF000000u || (s.low >> 32) != 0) {
-        const u8 carry = static_cast<u8>(s.low >> 32);
-        u8 first = s.cache;
-        while (s.pending) {
-            s.out[s.pos++] = static_cast<u8>(first + carry);
-            first = 0xFF;
-            --s.pending;
-        }
-        s.cache = static_cast<u8>(s.low >> 24);
-    }
-    ++s.pending;
-    s.low = (s.low << 8) & 0xFFFFFFFFull;
-}
-
-__device__ __forceinline__ void ac_norm(AcState& s) {
-    while (s.range < (1u << 24)) {
-        ac_shift(s);
-        s.range <<= 8;
-    }
-}
-
-__device__ __forceinline__ void ac_code(AcState& s, u32 cum, u32 freq, u32 total) {
-    s.range /= total;
-    s.low += static_cast<u64>(cum) * s.range;
-    s.range *= freq;
-    ac_norm(s);
-}
-
-// 32 raw bits as encode(bit, 1, 2) each: range/2 is a shift (entropy.cpp:95-100)
-__device__ __forceinline__ void ac_raw32(AcState& s, u64 v) {
-    for (int b = 31; b >= 0; --b) {
-        s.range >>= 1;
-        if ((v >> b) & 1u) s.low += s.range;
-        ac_norm(s);
-    }
-}
-
 __device__ __forceinline__ u32 hslot(u64 sym, u32 hbits) {
     return static_cast<u32>((sym * 0x9E3779B97F4A7C15ull) >> (64 - hbits));
 }
 
 constexpr u32 kAcSmemCap = 2048;  // model entries kept in shared memory (global scratch beyond)
 
-__host__ __device__ inline u32 pow2_at_least(u32 v) {
-    u32 p = 2;
-    while (p < v) p *= 2;
-    return p;
-}
 __host__ __device__ inline u32 log2_at_least(u32 v) {
     u32 b = 5;
     while ((1u << b) < v) ++b;

@@ -591,123 +591,195 @@ __global__ void cluster_mgs_kernel(const int* __restrict__ clusters, int n, doub
     }
 }
 
-// U (row-major n x r) = H_0 ... H_{n-3} Z with the compact WY form: chunks of
-// KC consecutive reflectors H_lo..H_hi = I - Y T Y^T (T upper triangular,
-// T = (diag(1/tau) + striu(Y^T Y))^{-1}) are applied as Z <- Z - Y (T (Y^T Z)),
-// last chunk first.  Each CTA owns 8 columns of Z in shared memory; the next
-// chunk's reflectors stream in with cp.async while the current one is applied.
-constexpr int kWyChunk = 16;
-constexpr int kWyCols = 8;
-__device__ __forceinline__ void cp_async8_eig(void* smem, const void* gmem) {
+// ---------------------------------------------------------------- back-transform
+// U = Q Z with Q = H_0 ... H_{n-3} (the Gram's eigenvectors from those of the
+// tridiagonal, sthosvd.cpp:80-90).  Reflector chunks of KC (32 / 16 / 8 for
+// n <= 256 / 512 / 1024) are listed from the last reflector down: chunk c is
+// [lo, hi], hi = n-3-c*KC, lo = max(0, hi-KC+1).  H_lo ... H_hi = I - Y T Y^T
+// with Y's column q = reflector lo+q (zero above row lo+q+1) and T upper
+// triangular: T_jj = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] (Y^T Y)[0:j, j].
+//   wy_tmat : one CTA per chunk (chunks are independent) -> T to global;
+//   wy_apply: Z <- Z - Y (T (Y^T Z)) for the chunks in order, one CTA per ZC
+//             columns of Z, the next chunk's Y streaming in by cp.async while
+//             the current one is applied.  Y^T Z and Y W are 4x4
+//             register-blocked; Y^T Z splits the rows over interleaved slices.
+constexpr int kBtThreads = 256;
+
+__device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bool valid) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0));
 }
-__global__ void __launch_bounds__(256) backtransform_wy(const double* __restrict__ V, const double* __restrict__ tau,
-                                                       int n, int r, int KC, const double* __restrict__ Z,
-                                                       double* __restrict__ U) {
-    extern __shared__ double swy[];
-    double* Ybuf = swy;                          // 2 x KC x n
-    double* Zb = Ybuf + 2 * KC * n;              // n x kWyCols
-    double* S = Zb + n * kWyCols;                // kWyChunk x kWyChunk
-    double* T = S + kWyChunk * kWyChunk;         // kWyChunk x kWyChunk
-    double* W = T + kWyChunk * kWyChunk;         // kWyChunk x kWyCols
-    double* W2 = W + kWyChunk * kWyCols;         // kWyChunk x kWyCols
-    double* tk = W2 + kWyChunk * kWyCols;        // 2 x kWyChunk
-    const int c0 = blockIdx.x * kWyCols;
-    const int nc = min(kWyCols, r - c0);
-    for (int idx = threadIdx.x; idx < n * kWyCols; idx += blockDim.x) {
-        const int i = idx / kWyCols, c = idx % kWyCols;
-        Zb[idx] = c < nc ? Z[static_cast<size_t>(c0 + c) * n + i] : 0.0;
+
+// Yt[q][i] (row stride n + 1) = V[(lo+q) n + i] for i >= lo+q+1 and q < kc, else 0
+__device__ __forceinline__ void bt_load_chunk(double* Yt, const double* __restrict__ V, int n, int lo, int kc,
+                                              int KC) {
+    const int ld = n + 1;
+    for (int idx = threadIdx.x; idx < KC * n; idx += blockDim.x) {
+        const int q = idx / n, i = idx - q * n;
+        const bool valid = q < kc && i >= lo + q + 1;
+        cp_async8_zfill(Yt + q * ld + i, V + (valid ? static_cast<size_t>(lo + q) * n + i : 0), valid);
     }
-    // chunk list from the last reflector down: chunk ci covers [lo, hi]
-    auto load = [&](int hi, int b) {
-        const int lo = max(0, hi - KC + 1);
-        double* Y = Ybuf + b * KC * n;
-        for (int q = 0; q <= hi - lo; ++q) {
-            const int kk = lo + q;
-            for (int i = kk + 1 + threadIdx.x; i < n; i += blockDim.x)
-                cp_async8_eig(Y + q * n + i, V + static_cast<size_t>(kk) * n + i);
+    asm volatile("cp.async.commit_group;\n");
+}
+
+__global__ void __launch_bounds__(kBtThreads) wy_tmat(const double* __restrict__ V, const double* __restrict__ tau,
+                                                     int n, int KC, double* __restrict__ Tg) {
+    extern __shared__ double sbt[];
+    const int ld = n + 1, ts = KC + 1;
+    const int c = blockIdx.x;
+    const int hi = n - 3 - c * KC, lo = max(0, hi - KC + 1), kc = hi - lo + 1;
+    double* Yt = sbt;            // KC x ld
+    double* S = Yt + KC * ld;    // KC x ts
+    double* T = S + KC * ts;     // KC x ts
+    bt_load_chunk(Yt, V, n, lo, kc, KC);
+    asm volatile("cp.async.wait_group 0;\n");
+    __syncthreads();
+    for (int e = threadIdx.x; e < KC * KC; e += blockDim.x) {  // S = Y^T Y, upper part
+        const int a = e / KC, b = e % KC;
+        double s0 = 0.0, s1 = 0.0;
+        if (a <= b && b < kc) {
+            const double* ya = Yt + a * ld;
+            const double* yb = Yt + b * ld;
+            int i = lo + b + 1;
+            for (; i + 1 < n; i += 2) {
+                s0 = fma(ya[i], yb[i], s0);
+                s1 = fma(ya[i + 1], yb[i + 1], s1);
+            }
+            if (i < n) s0 = fma(ya[i], yb[i], s0);
         }
-        if (threadIdx.x <= hi - lo) tk[b * kWyChunk + threadIdx.x] = tau[lo + threadIdx.x];
+        S[a * ts + b] = s0 + s1;
+        T[a * ts + b] = 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < kc; ++j) {
+        const double tj = tau[lo + j];
+        if (static_cast<int>(threadIdx.x) < j) {
+            const int i = threadIdx.x;
+            double acc = 0.0;
+            for (int l = i; l < j; ++l) acc = fma(T[i * ts + l], S[l * ts + j], acc);
+            T[i * ts + j] = -tj * acc;
+        }
+        if (threadIdx.x == 0) T[j * ts + j] = tj;
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < KC * KC; e += blockDim.x)
+        Tg[static_cast<size_t>(c) * KC * KC + e] = T[(e / KC) * ts + e % KC];
+}
+
+// One CTA per 4 columns of Z.  W = Y^T Z: thread (slice, 4-row q block) sums
+// rows i = slice (mod nslice) into a 4x4 register block, pairs of adjacent
+// slices combine by shuffles; Z -= Y (T W): one row per thread.
+__global__ void __launch_bounds__(kBtThreads) wy_apply(const double* __restrict__ V, const double* __restrict__ Tg,
+                                                      int n, int r, int KC, int nchunks,
+                                                      const double* __restrict__ Z, double* __restrict__ U) {
+    constexpr int ZC = 4;
+    extern __shared__ __align__(16) double sbt[];
+    const int ld = n + 1;
+    const int nblk = KC / 4, nslice = kBtThreads / nblk;
+    double* Ybuf = sbt;                          // 2 x KC x ld
+    double* Tb = Ybuf + 2 * KC * ld;             // 2 x KC x KC
+    double* Zs = Tb + 2 * KC * KC;               // n x 4
+    double* part = Zs + n * ZC;                  // (nslice / 4) x KC x 4
+    double* Wm = part + (nslice / 4) * KC * ZC;  // KC x 4
+    double* W2 = Wm + KC * ZC;                   // KC x 4
+    const int c0 = blockIdx.x * ZC;
+    const int nc = min(ZC, r - c0);
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll
+        for (int c = 0; c < ZC; ++c) Zs[i * ZC + c] = c < nc ? Z[static_cast<size_t>(c0 + c) * n + i] : 0.0;
+    auto bounds = [&](int c, int& lo, int& kc) {
+        const int hi = n - 3 - c * KC;
+        lo = max(0, hi - KC + 1);
+        kc = hi - lo + 1;
+    };
+    auto load = [&](int c) {  // chunk c's reflectors (zero-filled) and T, one cp.async group
+        int lo, kc;
+        bounds(c, lo, kc);
+        double* Yt = Ybuf + (c & 1) * KC * ld;
+        for (int q = 0; q < KC; ++q) {
+            const double* src = V + static_cast<size_t>(lo + q) * n;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const bool valid = q < kc && i >= lo + q + 1;
+                cp_async8_zfill(Yt + q * ld + i, valid ? src + i : V, valid);
+            }
+        }
+        double* Tc = Tb + (c & 1) * KC * KC;
+        for (int e = threadIdx.x; e < KC * KC; e += blockDim.x)
+            cp_async8_zfill(Tc + e, Tg + static_cast<size_t>(c) * KC * KC + e, true);
         asm volatile("cp.async.commit_group;\n");
     };
-    int buf = 0;
-    if (n >= 3) load(n - 3, 0);
-    for (int hi = n - 3; hi >= 0; hi -= KC) {
-        const int lo = max(0, hi - KC + 1);
-        const int kc = hi - lo + 1;
-        if (hi - KC >= 0) {
-            load(hi - KC, buf ^ 1);
+    if (nchunks > 0) load(0);
+    const int t = threadIdx.x;
+    const int slice = t % nslice, qb = (t / nslice) * 4;
+    for (int c = 0; c < nchunks; ++c) {
+        int lo, kc;
+        bounds(c, lo, kc);
+        if (c + 1 < nchunks) {
+            load(c + 1);
             asm volatile("cp.async.wait_group 1;\n");
         } else {
             asm volatile("cp.async.wait_group 0;\n");
         }
         __syncthreads();
-        const double* Y = Ybuf + buf * KC * n;
-        const double* tb = tk + buf * kWyChunk;
-        // S = Y^T Y (upper part) and W = Y^T Zb; y_q is zero above row lo+q
-        for (int e = threadIdx.x; e < kc * kc + kc * kWyCols; e += blockDim.x) {
-            double s0 = 0.0, s1 = 0.0;
-            if (e < kc * kc) {
-                const int a2 = e / kc, b2 = e % kc;
-                if (a2 > b2) continue;
-                const double* ya = Y + a2 * n;
-                const double* yb = Y + b2 * n;
-                int i = lo + b2 + 1;
-                for (; i + 1 < n; i += 2) {
-                    s0 += ya[i] * yb[i];
-                    s1 += ya[i + 1] * yb[i + 1];
-                }
-                if (i < n) s0 += ya[i] * yb[i];
-                S[a2 * kWyChunk + b2] = s0 + s1;
-            } else {
-                const int f = e - kc * kc, q = f / kWyCols, c = f % kWyCols;
-                const double* yq = Y + q * n;
-                int i = lo + q + 1;
-                for (; i + 1 < n; i += 2) {
-                    s0 += yq[i] * Zb[i * kWyCols + c];
-                    s1 += yq[i + 1] * Zb[(i + 1) * kWyCols + c];
-                }
-                if (i < n) s0 += yq[i] * Zb[i * kWyCols + c];
-                W[q * kWyCols + c] = s0 + s1;
+        const double* Yt = Ybuf + (c & 1) * KC * ld;
+        const double* Tc = Tb + (c & 1) * KC * KC;
+        const int i0 = lo + 1;  // Y is zero above row lo + 1
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (int i = i0 + slice; i < n; i += nslice) {
+            const double2 z01 = *reinterpret_cast<const double2*>(Zs + i * ZC);
+            const double2 z23 = *reinterpret_cast<const double2*>(Zs + i * ZC + 2);
+            const double z[4] = {z01.x, z01.y, z23.x, z23.y};
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const double y = Yt[(qb + a) * ld + i];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fma(y, z[b], acc[a][b]);
             }
         }
-        __syncthreads();
-        if (threadIdx.x < kWyChunk) {
-            // column j of T by back-substitution, all columns in parallel; tau = 0 rows stay 0
-            const int j = threadIdx.x;
-            for (int i = 0; i < kWyChunk; ++i) T[i * kWyChunk + j] = 0.0;
-            if (j < kc && tb[j] != 0.0) {
-                T[j * kWyChunk + j] = tb[j];
-                for (int i = j - 1; i >= 0; --i) {
-                    if (tb[i] == 0.0) continue;
-                    double acc = 0.0;
-                    for (int l = i + 1; l <= j; ++l) acc += S[i * kWyChunk + l] * T[l * kWyChunk + j];
-                    T[i * kWyChunk + j] = -tb[i] * acc;
-                }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                double v = acc[a][b];
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                if ((slice & 3) == 0) part[((slice >> 2) * KC + qb + a) * ZC + b] = v;
             }
-        }
         __syncthreads();
-        for (int e = threadIdx.x; e < kc * kWyCols; e += blockDim.x) {  // W2 = T W
-            const int q = e / kWyCols, c = e % kWyCols;
+        for (int e = t; e < KC * ZC; e += blockDim.x) {
             double v = 0.0;
-            for (int b2 = q; b2 < kc; ++b2) v += T[q * kWyChunk + b2] * W[b2 * kWyCols + c];
+            for (int s4 = 0; s4 < nslice / 4; ++s4) v += part[s4 * KC * ZC + e];
+            Wm[e] = v;
+        }
+        __syncthreads();
+        for (int e = t; e < KC * ZC; e += blockDim.x) {  // W2 = T W (T upper)
+            const int q = e / ZC, cc = e % ZC;
+            double v = 0.0;
+            for (int l = q; l < kc; ++l) v = fma(Tc[q * KC + l], Wm[l * ZC + cc], v);
             W2[e] = v;
         }
         __syncthreads();
-        for (int e = (lo + 1) * kWyCols + threadIdx.x; e < n * kWyCols; e += blockDim.x) {  // Zb -= Y W2
-            const int i = e / kWyCols, c = e % kWyCols;
-            const int qmax = min(kc, i - lo);  // y_q(i) != 0 only for i > lo + q
-            double v = 0.0;
-            for (int q = 0; q < qmax; ++q) v += Y[q * n + i] * W2[q * kWyCols + c];
-            Zb[e] -= v;
+        for (int i = i0 + t; i < n; i += blockDim.x) {  // Z -= Y W2, one row per thread
+            double u[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int q = 0; q < kc; ++q) {
+                const double y = Yt[q * ld + i];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) u[b] = fma(y, W2[q * ZC + b], u[b]);
+            }
+            double2* zr = reinterpret_cast<double2*>(Zs + i * ZC);
+            const double2 z01 = zr[0], z23 = zr[1];
+            zr[0] = make_double2(z01.x - u[0], z01.y - u[1]);
+            zr[1] = make_double2(z23.x - u[2], z23.y - u[3]);
         }
         __syncthreads();
-        buf ^= 1;
     }
     for (int idx = threadIdx.x; idx < n * nc; idx += blockDim.x) {
         const int i = idx / nc, c = idx % nc;
-        U[static_cast<size_t>(i) * r + c0 + c] = Zb[i * kWyCols + c];
+        U[static_cast<size_t>(i) * r + c0 + c] = Zs[i * ZC + c];
     }
 }
 
@@ -780,6 +852,26 @@ __global__ void scale_mgs_kernel(double* __restrict__ U, int n, int r, const dou
 
 }  // namespace
 
+namespace {
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    SideStream() {
+        TCB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        TCB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        TCB_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    }
+};
+SideStream& side_stream() {  // one per host thread and device
+    static thread_local std::vector<SideStream*> per_dev;
+    int dev = 0;
+    TCB_CUDA(cudaGetDevice(&dev));
+    if (per_dev.size() <= static_cast<size_t>(dev)) per_dev.resize(dev + 1, nullptr);
+    if (!per_dev[dev]) per_dev[dev] = new SideStream();
+    return *per_dev[dev];
+}
+}  // namespace
+
 std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_t s) {
     ProfScope prof_scope(kEig, s);
     const int n = static_cast<int>(n64);
@@ -841,9 +933,28 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
         }
         count_launch();
     }
+    // compact-WY T matrices of the reflector chunks on a side stream, overlapping the multisection
+    w.kc = n <= 256 ? 32 : n <= 512 ? 16 : 8;
+    w.nchunks = n >= 3 ? (n - 2 + w.kc - 1) / w.kc : 0;
+    w.tg = DevBuf<double>(static_cast<u64>(std::max(w.nchunks, 1)) * w.kc * w.kc, s);
+    SideStream& side = side_stream();
+    if (w.nchunks > 0) {
+        static bool tattr = [] {
+            cudaFuncSetAttribute(wy_tmat, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            return true;
+        }();
+        (void)tattr;
+        TCB_CUDA(cudaEventRecord(side.fork, s));
+        TCB_CUDA(cudaStreamWaitEvent(side.s, side.fork, 0));
+        const size_t tsm = (static_cast<size_t>(w.kc) * (n + 1) + 2 * w.kc * (w.kc + 1)) * sizeof(double);
+        wy_tmat<<<static_cast<unsigned>(w.nchunks), kBtThreads, tsm, side.s>>>(w.z.p, w.tau.p, n, w.kc, w.tg.p);
+        count_launch();
+        TCB_CUDA(cudaEventRecord(side.join, side.s));
+    }
     const int wpb = 2;
     multisect_kernel<<<cdiv(n64, wpb), 32 * wpb, 2 * n * sizeof(double), s>>>(w.d.p, w.e.p, n, w.evals.p);
     count_launch();
+    if (w.nchunks > 0) TCB_CUDA(cudaStreamWaitEvent(s, side.join, 0));
     TCB_LAUNCH();
     std::vector<double> ev(n64);
     w.evals.download(ev.data(), n64);
@@ -901,15 +1012,16 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
         count_launch();
         TCB_CUDA(cudaStreamSynchronize(s));
     }
-    const int KC = n <= 512 ? kWyChunk : kWyChunk / 2;
-    const size_t wysmem = (2 * static_cast<size_t>(KC) * n + static_cast<size_t>(n) * kWyCols +
-                           2 * kWyChunk * kWyChunk + 2 * kWyChunk * kWyCols + 2 * kWyChunk) * sizeof(double);
+    // T matrices come from wy_tmat on the side stream (launched by eig_values)
     static bool attr = [] {
-        cudaFuncSetAttribute(backtransform_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(wy_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         return true;
     }();
     (void)attr;
-    backtransform_wy<<<cdiv(r64, kWyCols), 256, wysmem, s>>>(w.z.p, w.tau.p, n, r, KC, Z.p, U);  // n < 3: plain copy
+    const int KC = w.kc, nslice = kBtThreads / (KC / 4);
+    const size_t asm_ = (2 * static_cast<size_t>(KC) * (n + 1) + 2 * KC * KC + static_cast<size_t>(n) * 4 +
+                         static_cast<size_t>(nslice / 4 + 2) * KC * 4) * sizeof(double);
+    wy_apply<<<cdiv(r64, 4), kBtThreads, asm_, s>>>(w.z.p, w.tg.p, n, r, KC, w.nchunks, Z.p, U);
     count_launch();
     TCB_LAUNCH();
     TCB_CUDA(cudaStreamSynchronize(s));

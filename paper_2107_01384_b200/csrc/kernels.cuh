@@ -36,6 +36,8 @@ void gemm_nn_f64(const double* B, u64 rows, u64 cols, const double* V, u64 r, do
 struct EigWork {
     DevBuf<double> a;    // n x n working copy (row-major), reflectors below the subdiagonal
     DevBuf<double> d, e, tau, evals, z;
+    DevBuf<double> tg;       // compact-WY T matrices, nchunks x kc x kc
+    int kc = 0, nchunks = 0;
     u64 n = 0;
 };
 // Householder tridiagonalisation of the symmetric row-major A (n x n) and
