@@ -387,24 +387,72 @@ __device__ __forceinline__ double frcp(double q) {
 
 // Sturm counts (eigenvalues of T below x) for PR probes at once: independent
 // division chains per thread hide the fp64 latency.
+// Sturm count (eigenvalues < x) by the three-term recurrence
+// p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2} = det(T_i - x I) on a T scaled by a
+// power of two to ||T|| < 1.  The critical chain is one FMA per step (the
+// e^2 p_{i-2} product is ready a step early); a count is a sign change of
+// consecutive terms (XOR of sign bits, off the chain).  e^2 == 0 needs no
+// restart: the sequence continues as a product and the changes add up per
+// block.  Every 8 steps both terms are rescaled by an exact power of two.
+// Each step's rounding is a relative perturbation of d_i - x and e^2, so the
+// count is exact for a matrix within a few ulps of ||T||, as for the ratio
+// form.  An exact zero term (measure zero) sets `hit` and the caller recounts
+// with the ratio form's q -> -pivmin rule.
+__device__ __forceinline__ int dexp(double v) {
+    return static_cast<int>((__double_as_longlong(v) >> 52) & 0x7FF) - 1023;
+}
+__device__ __forceinline__ unsigned sgn(double v) {
+    return static_cast<unsigned>(__double_as_longlong(v) >> 63) & 1u;
+}
 template <int PR>
-__device__ __forceinline__ void sturm_n(const double* d, const double* e2, int n, const double (&x)[PR],
-                                        double pivmin, int (&c)[PR]) {
-    double q[PR];
+__device__ __forceinline__ void sturm_poly(const double* ds, const double* e2s, int n, const double (&x)[PR],
+                                           int (&c)[PR], bool& hit) {
+    double p0[PR], p1[PR];
+    unsigned zero = 0;
 #pragma unroll
     for (int u = 0; u < PR; ++u) {
-        q[u] = d[0] - x[u];
-        c[u] = q[u] < 0.0;
+        p0[u] = 1.0;
+        p1[u] = ds[0] - x[u];
+        c[u] = static_cast<int>(sgn(p1[u]));
+        zero |= p1[u] == 0.0;
     }
-    for (int i = 1; i < n; ++i) {
-        const double di = d[i], ei = e2[i - 1];
+    auto step = [&](int i) {
+        const double di = ds[i], ei = e2s[i - 1];
 #pragma unroll
         for (int u = 0; u < PR; ++u) {
-            if (fabs(q[u]) < pivmin) q[u] = -pivmin;
-            q[u] = (di - x[u]) - ei * frcp(q[u]);
-            c[u] += q[u] < 0.0;
+            const double t = ei * p0[u];
+            const double p = fma(di - x[u], p1[u], -t);
+            c[u] += static_cast<int>(sgn(p) ^ sgn(p1[u]));
+            zero |= p == 0.0;
+            p0[u] = p1[u];
+            p1[u] = p;
+        }
+    };
+    int i = 1;
+    for (; i + 8 <= n; i += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) step(i + k);
+#pragma unroll
+        for (int u = 0; u < PR; ++u) {
+            const int ex = max(dexp(p0[u]), dexp(p1[u]));
+            const double sc = __longlong_as_double(static_cast<long long>(1023 - ex) << 52);
+            p0[u] *= sc;
+            p1[u] *= sc;
         }
     }
+    for (; i < n; ++i) step(i);
+    hit = zero != 0;
+}
+// reference count for the rare exact-zero probes: LAPACK's ratio recurrence
+__device__ __noinline__ int sturm_ratio(const double* ds, const double* e2s, int n, double x, double pivmin) {
+    double q = ds[0] - x;
+    int c = q < 0.0;
+    for (int i = 1; i < n; ++i) {
+        if (fabs(q) < pivmin) q = -pivmin;
+        q = (ds[i] - x) - e2s[i - 1] / q;
+        c += q < 0.0;
+    }
+    return c;
 }
 
 // one warp per eigenvalue (ascending index j), 64 probes per round (6 bits)
@@ -414,25 +462,49 @@ __global__ void multisect_kernel(const double* __restrict__ dg, const double* __
     extern __shared__ double sh_bis[];
     double* d = sh_bis;
     double* e2 = sh_bis + n;
-    __shared__ double bounds[3];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        d[i] = dg[i];
-        if (i + 1 < n) e2[i] = eg[i] * eg[i];
+    __shared__ double bounds[4];
+    __shared__ double red3[3][32];
+    {  // Gershgorin interval and max e^2: block-wide min/max (exact, order-free)
+        double gl = DBL_MAX, gu = -DBL_MAX, emax2 = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const double r = (i > 0 ? fabs(eg[i - 1]) : 0.0) + (i + 1 < n ? fabs(eg[i]) : 0.0);
+            const double di = dg[i];
+            gl = fmin(gl, di - r);
+            gu = fmax(gu, di + r);
+            if (i + 1 < n) emax2 = fmax(emax2, eg[i] * eg[i]);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+            gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+            emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            red3[0][threadIdx.x >> 5] = gl;
+            red3[1][threadIdx.x >> 5] = gu;
+            red3[2][threadIdx.x >> 5] = emax2;
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double gl = DBL_MAX, gu = -DBL_MAX, emax2 = 0.0;
-        for (int i = 0; i < n; ++i) {
-            const double r = (i > 0 ? fabs(eg[i - 1]) : 0.0) + (i + 1 < n ? fabs(eg[i]) : 0.0);
-            gl = fmin(gl, d[i] - r);
-            gu = fmax(gu, d[i] + r);
-            if (i + 1 < n) emax2 = fmax(emax2, e2[i]);
+        for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) {
+            gl = fmin(gl, red3[0][w2]);
+            gu = fmax(gu, red3[1][w2]);
+            emax2 = fmax(emax2, red3[2][w2]);
         }
         const double tnorm = fmax(fabs(gl), fabs(gu));
         const double pivmin = DBL_MIN * fmax(1.0, emax2);
         bounds[0] = gl - 2.0 * DBL_EPSILON * tnorm * n - 2.0 * pivmin;
         bounds[1] = gu + 2.0 * DBL_EPSILON * tnorm * n + 2.0 * pivmin;
         bounds[2] = pivmin;
+        // power of two >= ||T|| (exact scaling of d, e^2 and the probes)
+        bounds[3] = tnorm > 0.0 ? __longlong_as_double(static_cast<long long>(1023 - dexp(tnorm) - 1) << 52) : 1.0;
+    }
+    __syncthreads();
+    const double inv_sc = bounds[3];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        d[i] = dg[i] * inv_sc;
+        if (i + 1 < n) e2[i] = (eg[i] * inv_sc) * (eg[i] * inv_sc);
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -449,8 +521,13 @@ __global__ void multisect_kernel(const double* __restrict__ dg, const double* __
         double x[kProbes];
         int c[kProbes];
 #pragma unroll
-        for (int u = 0; u < kProbes; ++u) x[u] = probe(kProbes * lane + u);
-        sturm_n<kProbes>(d, e2, n, x, pivmin, c);
+        for (int u = 0; u < kProbes; ++u) x[u] = probe(kProbes * lane + u) * inv_sc;
+        bool hit;
+        sturm_poly<kProbes>(d, e2, n, x, c, hit);
+        if (hit) {
+#pragma unroll
+            for (int u = 0; u < kProbes; ++u) c[u] = sturm_ratio(d, e2, n, x[u], pivmin * inv_sc * inv_sc);
+        }
         unsigned mk = 0;
 #pragma unroll
         for (int u = 0; u < kProbes; ++u) mk |= (c[u] > j ? 1u : 0u) << u;
