@@ -572,59 +572,66 @@ __global__ void __launch_bounds__(32) invit_kernel(const double* __restrict__ dg
     int* piv = reinterpret_cast<int*>(x + n);
     const int j = blockIdx.x;
     const double lam = shift[j];
+    // stage T - lam I (a: diagonal, b: superdiagonal, c: subdiagonal) with all lanes
+    for (int i = threadIdx.x; i < n; i += 32) {
+        a[i] = dg[i] - lam;
+        b[i] = i + 1 < n ? eg[i] : 0.0;
+        c[i] = b[i];
+        dd[i] = 0.0;
+        x[i] = hash_unit(static_cast<unsigned>(j) + 1u, i);
+    }
+    __syncwarp();
+    auto tolfix = [&](double v) { return fabs(v) < tol ? (v < 0.0 ? -tol : tol) : v; };
     if (threadIdx.x == 0) {
-        for (int i = 0; i < n; ++i) {
-            a[i] = dg[i] - lam;
-            b[i] = i + 1 < n ? eg[i] : 0.0;
-            c[i] = i + 1 < n ? eg[i] : 0.0;
-            dd[i] = 0.0;
-        }
-        for (int k = 0; k + 1 < n; ++k) {  // LU with partial pivoting (LAPACK dlagtf scheme)
-            double ak = a[k];
-            if (fabs(ak) >= fabs(c[k])) {
-                if (fabs(ak) < tol) ak = ak < 0.0 ? -tol : tol;
-                const double mult = c[k] * frcp(ak);
+        // LU with partial pivoting (LAPACK dlagtf scheme); the updated a[k+1]
+        // and b[k+1] ride in registers, a[] receives the pivots' reciprocals
+        double ak = a[0], bk = b[0];
+        for (int k = 0; k + 1 < n; ++k) {
+            const double ck = c[k], an = a[k + 1], bn = b[k + 1];
+            if (fabs(ak) >= fabs(ck)) {
+                ak = tolfix(ak);
+                const double mult = ck * frcp(ak);
                 c[k] = mult;
-                a[k + 1] -= mult * b[k];
                 piv[k] = 0;
-                a[k] = ak;
+                a[k] = frcp(ak);
+                b[k] = bk;
+                ak = an - mult * bk;
+                bk = bn;
             } else {
-                const double mult = ak * frcp(c[k]);
-                a[k] = c[k];
-                const double tmp = a[k + 1];
-                a[k + 1] = b[k] - mult * tmp;
-                if (k + 2 < n) {
-                    dd[k] = b[k + 1];
-                    b[k + 1] = -mult * dd[k];
-                }
-                b[k] = tmp;
+                const double mult = ak * frcp(ck);
+                a[k] = frcp(tolfix(ck));
+                b[k] = an;
                 c[k] = mult;
                 piv[k] = 1;
+                const double d2 = k + 2 < n ? bn : 0.0;
+                dd[k] = d2;
+                ak = bk - mult * an;
+                bk = k + 2 < n ? -mult * d2 : bn;
             }
         }
-        for (int i = 0; i < n; ++i) {
-            double ai = a[i];
-            if (fabs(ai) < tol) ai = ai < 0.0 ? -tol : tol;
-            a[i] = frcp(ai);
-        }
+        a[n - 1] = frcp(tolfix(ak));
+        b[n - 1] = bk;
     }
-    for (int i = threadIdx.x; i < n; i += 32) x[i] = hash_unit(static_cast<unsigned>(j) + 1u, i);
     __syncwarp();
     for (int it = 0; it < 3; ++it) {
         if (threadIdx.x == 0) {
+            // forward: the carried x[k] stays in a register
+            double xk = x[0];
             for (int k = 0; k + 1 < n; ++k) {
+                const double xn = x[k + 1], ck = c[k];
                 if (piv[k]) {
-                    const double t = x[k];
-                    x[k] = x[k + 1];
-                    x[k + 1] = t - c[k] * x[k];
+                    x[k] = xn;
+                    xk = xk - ck * xn;
                 } else {
-                    x[k + 1] -= c[k] * x[k];
+                    x[k] = xk;
+                    xk = xn - ck * xk;
                 }
             }
+            x[n - 1] = xk;
+            // back substitution with x1 = x[k+1], x2 = x[k+2] in registers
             double x1 = 0.0, x2 = 0.0;
             for (int k = n - 1; k >= 0; --k) {
-                double t = x[k] - b[k] * x1 - dd[k] * x2;
-                t *= a[k];
+                double t = (x[k] - b[k] * x1 - dd[k] * x2) * a[k];
                 if (fabs(t) > 1e150) {  // rescale the partial solution
                     for (int q = k + 1; q < n; ++q) x[q] *= 1e-150;
                     t *= 1e-150;
