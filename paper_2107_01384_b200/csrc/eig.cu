@@ -993,7 +993,8 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
             }();
             (void)attr;
             cfg.gridDim = dim3(kTdCluster);
-            cfg.blockDim = dim3(32 * std::min(nloc, kTdMaxWarps));
+            // one row slot per warp up to n = 256, two beyond (fewer redundant per-warp steps)
+            cfg.blockDim = dim3(32 * (nloc <= 16 ? nloc : (nloc + 1) / 2));
             at[0].val.clusterDim.x = kTdCluster;
             cfg.dynamicSmemBytes = smem;
             int ncl = 0;  // a 16-CTA cluster with this much shared memory must fit one GPC
