@@ -484,8 +484,20 @@ __global__ void multisect_kernel(const double* __restrict__ dg, const double* __
             red3[2][threadIdx.x >> 5] = emax2;
         }
     }
+    if (blockIdx.x == 0) {  // ||T||_inf = max_i |d_i| + |e_i-1| + |e_i| for eig_vectors' tolerances
+        double rn = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            rn = fmax(rn, fabs(dg[i]) + (i > 0 ? fabs(eg[i - 1]) : 0.0) + (i + 1 < n ? fabs(eg[i]) : 0.0));
+        for (int o = 16; o > 0; o >>= 1) rn = fmax(rn, __shfl_xor_sync(0xffffffffu, rn, o));
+        if ((threadIdx.x & 31) == 0) red3[0][16 + (threadIdx.x >> 5)] = rn;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) {
+            double rn = 0.0;
+            for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) rn = fmax(rn, red3[0][16 + w2]);
+            evals_desc[n] = rn;
+        }
         double gl = DBL_MAX, gu = -DBL_MAX, emax2 = 0.0;
         for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) {
             gl = fmin(gl, red3[0][w2]);
@@ -964,7 +976,7 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
     w.d = DevBuf<double>(n64, s);
     w.e = DevBuf<double>(n64 + 1, s);
     w.tau = DevBuf<double>(n64 + 1, s);
-    w.evals = DevBuf<double>(n64, s);
+    w.evals = DevBuf<double>(n64 + 1, s);  // + ||T||_inf (multisect block 0)
     w.z = DevBuf<double>(n64 * n64, s);  // Householder vectors
     w.tau.zero();
     w.e.zero();
@@ -1041,25 +1053,20 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
     count_launch();
     if (w.nchunks > 0) TCB_CUDA(cudaStreamWaitEvent(s, side.join, 0));
     TCB_LAUNCH();
-    std::vector<double> ev(n64);
-    w.evals.download(ev.data(), n64);
+    std::vector<double> ev(n64 + 1);
+    w.evals.download(ev.data(), n64 + 1);  // one synchronising copy: eigenvalues and ||T||_inf
     TCB_CUDA(cudaStreamSynchronize(s));
+    w.tnorm = ev[n64];
+    ev.resize(n64);
+    w.ev = ev;
     return ev;
 }
 
 void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
     ProfScope prof_scope(kEig, s);
     const int n = static_cast<int>(w.n), r = static_cast<int>(r64);
-    std::vector<double> ev(w.n), d(w.n), e(w.n + 1);
-    w.evals.download(ev.data(), w.n);
-    w.d.download(d.data(), w.n);
-    w.e.download(e.data(), w.n + 1);
-    TCB_CUDA(cudaStreamSynchronize(s));
-    double tnorm = 0.0;
-    for (int i = 0; i < n; ++i) {
-        const double rr = std::fabs(d[i]) + (i > 0 ? std::fabs(e[i - 1]) : 0.0) + (i + 1 < n ? std::fabs(e[i]) : 0.0);
-        tnorm = std::max(tnorm, rr);
-    }
+    const std::vector<double>& ev = w.ev;  // host copies made by eig_values: no round trip here
+    double tnorm = w.tnorm;
     if (!(tnorm > 0.0)) tnorm = 1.0;  // zero matrix: any orthonormal basis is an eigenbasis
     // tight clusters: consecutive eigenvalues closer than 1e-6 ||T||; their
     // vectors are orthogonalised against each other after inverse iteration
@@ -1095,7 +1102,6 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
         dcl.upload(clusters.data(), clusters.size());
         cluster_mgs_kernel<<<static_cast<unsigned>(clusters.size() / 2), 256, 0, s>>>(dcl.p, n, Z.p);
         count_launch();
-        TCB_CUDA(cudaStreamSynchronize(s));
     }
     // T matrices come from wy_tmat on the side stream (launched by eig_values)
     static bool attr = [] {
@@ -1109,7 +1115,6 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
     wy_apply<<<cdiv(r64, 4), kBtThreads, asm_, s>>>(w.z.p, w.tg.p, n, r, KC, w.nchunks, Z.p, U);
     count_launch();
     TCB_LAUNCH();
-    TCB_CUDA(cudaStreamSynchronize(s));
 }
 
 void fix_column_signs(double* U, u64 n, u64 r, cudaStream_t s) {

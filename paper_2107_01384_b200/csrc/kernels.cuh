@@ -38,6 +38,8 @@ struct EigWork {
     DevBuf<double> d, e, tau, evals, z;
     DevBuf<double> tg;       // compact-WY T matrices, nchunks x kc x kc
     int kc = 0, nchunks = 0;
+    std::vector<double> ev;  // host copy of the descending eigenvalues (eig_values)
+    double tnorm = 0.0;      // host: ||T||_inf
     u64 n = 0;
 };
 // Householder tridiagonalisation of the symmetric row-major A (n x n) and
