@@ -12,8 +12,8 @@
 #include "quant.cuh"
 
 namespace tcb {
-u64& launch_counter() {
-    static u64 c = 0;
+std::atomic<u64>& launch_counter() {
+    static std::atomic<u64> c{0};
     return c;
 }
 
@@ -25,6 +25,8 @@ struct Rec {
 };
 std::vector<Rec> g_recs;
 }  // namespace
+
+bool prof_enabled() { return g_prof; }
 
 ProfScope::ProfScope(Cat c, cudaStream_t s) : cat(c), st(s) {
     if (!g_prof) return;
@@ -133,7 +135,7 @@ void fill(const Result& r, int d, tcb_result* out) {
     out->core_last_plane = r.core_last_plane;
     out->core_scale_exponent = r.core_k;
     out->uncertified_decisions = r.uncertified;
-    out->kernel_launches = launch_counter();
+    out->kernel_launches = launch_counter().load();
 }
 
 std::size_t dtype_bytes(int t) {
@@ -187,7 +189,7 @@ double tcb_peak_dmma_tflops(void) {
     }
 }
 void tcb_free(void* p) { std::free(p); }
-uint64_t tcb_kernel_launches(void) { return launch_counter(); }
+uint64_t tcb_kernel_launches(void) { return launch_counter().load(); }
 
 int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d, uint64_t skip,
                  const tcb_params* params, tcb_result* out) {

@@ -1,6 +1,8 @@
 // Shared device/host plumbing for the B200 compress path (sm_100a only).
 #pragma once
 
+#include <atomic>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -88,8 +90,10 @@ inline int sm_count() {
 inline unsigned cdiv(u64 a, u64 b) { return static_cast<unsigned>((a + b - 1) / b); }
 
 // Launch counter for the bench's "gpu_launches" claim.
-u64& launch_counter();
-inline void count_launch(u64 k = 1) { launch_counter() += k; }
+std::atomic<u64>& launch_counter();
+inline void count_launch(u64 k = 1) { launch_counter().fetch_add(k, std::memory_order_relaxed); }
+// true while tcb_prof_enable(1): the pipeline then runs its stages sequentially
+bool prof_enabled();
 
 // Optional per-stage device timing (CUDA events on the launching stream),
 // enabled by tcb_prof_enable(); read back with tcb_prof_read().

@@ -9,13 +9,99 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <future>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <numeric>
+#include <thread>
 
 #include "kernels.cuh"
 #include "quant.cuh"
 
 namespace tcb {
+
+namespace {
+// Host worker pool for the concurrent factor encodes: persistent threads (a
+// thread per call would cost more than the overlap saves) and one
+// non-blocking CUDA stream per (device, slot).
+class Workers {
+public:
+    static Workers& get() {
+        static Workers w;
+        return w;
+    }
+    std::future<void> submit(std::function<void()> f) {
+        auto task = std::make_shared<std::packaged_task<void()>>(std::move(f));
+        auto fut = task->get_future();
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            q_.push_back([task] { (*task)(); });
+        }
+        cv_.notify_one();
+        return fut;
+    }
+    cudaStream_t stream(int dev, int slot) {
+        std::lock_guard<std::mutex> lk(m_);
+        auto& v = streams_[dev];
+        while (static_cast<int>(v.size()) <= slot) {
+            cudaStream_t st;
+            TCB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            v.push_back(st);
+        }
+        return v[slot];
+    }
+
+private:
+    Workers() {
+        for (int i = 0; i < 8; ++i) th_.emplace_back([this] { run(); });
+    }
+    ~Workers() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void run() {
+        for (;;) {
+            std::function<void()> f;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+                if (stop_ && q_.empty()) return;
+                f = std::move(q_.front());
+                q_.pop_front();
+            }
+            f();
+        }
+    }
+    std::mutex m_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    std::vector<std::thread> th_;
+    std::map<int, std::vector<cudaStream_t>> streams_;
+    bool stop_ = false;
+};
+// waits for every submitted task before the stack data they reference unwinds
+struct JoinAll {
+    std::vector<std::future<void>>& f;
+    ~JoinAll() {
+        for (auto& x : f)
+            if (x.valid()) x.wait();
+    }
+};
+struct EventHandle {
+    cudaEvent_t e = nullptr;
+    EventHandle() { TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+    ~EventHandle() { cudaEventDestroy(e); }
+};
+}  // namespace
+
 
 namespace {
 
@@ -218,7 +304,8 @@ Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double 
 
 FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<u8>& dead,
                                const std::vector<double>& sn, int coder, bool simple, int core_step_log2,
-                               double cap, bool f32, cudaStream_t s) {
+                               double cap, bool f32, cudaStream_t s,
+                               const std::function<void(const std::vector<signed char>&)>& on_flips) {
     if (dead.size() != r || sn.size() != r) throw Error("factor encode: column metadata mismatch");
     FactorEnc out;
     out.dead = dead;
@@ -233,6 +320,7 @@ FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<
         }
     const u64 rl = live.size();
     if (rl == 0) {
+        if (on_flips) on_flips(out.flips);
         out.stream = empty_stream_section(0, 0);
         return out;
     }
@@ -242,6 +330,7 @@ FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<
     std::vector<signed char> fl(rl);
     householder(U, n, r, live, V.p, fl.data(), s);
     for (u64 j = 0; j < rl; ++j) out.flips[live[j]] = fl[j];
+    if (on_flips) on_flips(out.flips);
     std::vector<double> sc(rl);
     if (simple) {
         sc = ln;
@@ -405,30 +494,71 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
         }
     }
 
-    // phase 4: factors
+    // phase 4: factors, concurrently on worker streams (each factor's plane
+    // search and stream finalisation is a chain of small launches and host
+    // decisions); the core's sign fold and finalisation run on `s` as soon as
+    // every factor has published its column sign flips.  Sequential while
+    // per-stage profiling is on.
     t0 = Clock::now();
     const int core_step = plan.last_plane - k;
     const double cap = 0.02 * target / static_cast<double>(d);
     std::vector<FactorEnc> fe(d);
     res.factor_terms.assign(d, 0.0);
-    for (std::size_t i = 0; i < d; ++i) {
+    std::vector<std::vector<signed char>> flips_of(d);
+    auto run_factor = [&](std::size_t i, cudaStream_t si,
+                          const std::function<void(const std::vector<signed char>&)>& cb) {
         fe[i] = encode_factor_device(f.factors[i].p, f.n[i], f.r[i], dead_mode[i], sn_mode[i], prm.coder, prm.simple,
-                                     core_step, cap, prm.f32, s);
-        res.factor_terms[i] = fe[i].term;
+                                     core_step, cap, prm.f32, si, cb);
+    };
+    const bool par = d > 1 && !prof_enabled();
+    std::vector<std::promise<void>> flips_ready(d);
+    std::vector<std::future<void>> flips_fut, done;
+    JoinAll join{done};
+    if (par) {
+        int dev = 0;
+        TCB_CUDA(cudaGetDevice(&dev));
+        EventHandle ready;
+        TCB_CUDA(cudaEventRecord(ready.e, s));
+        Workers& pool = Workers::get();
+        for (std::size_t i = 0; i < d; ++i) {
+            flips_fut.push_back(flips_ready[i].get_future());
+            cudaStream_t si = pool.stream(dev, static_cast<int>(i));
+            TCB_CUDA(cudaStreamWaitEvent(si, ready.e, 0));
+            done.push_back(pool.submit([&, i, si, dev] {
+                bool sent = false;
+                try {
+                    TCB_CUDA(cudaSetDevice(dev));
+                    run_factor(i, si, [&](const std::vector<signed char>& fl) {
+                        flips_of[i] = fl;
+                        sent = true;
+                        flips_ready[i].set_value();
+                    });
+                } catch (...) {
+                    if (!sent) flips_ready[i].set_exception(std::current_exception());
+                    throw;
+                }
+            }));
+        }
+        for (auto& fu : flips_fut) fu.get();  // rethrows a factor's early error (join waits for the rest)
+    } else {
+        for (std::size_t i = 0; i < d; ++i)
+            run_factor(i, s, [&](const std::vector<signed char>& fl) { flips_of[i] = fl; });
     }
-    res.times.factor = ms_since(t0);
 
     // sign fold + finalize (pipeline.cpp:161-176)
-    t0 = Clock::now();
+    const auto t1 = Clock::now();
     std::vector<signed char> flips_axis;
     for (std::size_t ax = 0; ax < d; ++ax)
-        flips_axis.insert(flips_axis.end(), fe[mode_of[ax]].flips.begin(), fe[mode_of[ax]].flips.end());
+        flips_axis.insert(flips_axis.end(), flips_of[mode_of[ax]].begin(), flips_of[mode_of[ax]].end());
     sign_fold(neg.p, cs, flips_axis, s);
     u64 count = 1;
     for (auto v : f.r) count *= v;
     const auto core_stream = finalize_stream(mag.p, neg.p, nc, plan, prm.coder, count, s);
     const SumRec ach = device_sum(SumKind::diff_backward, mag.p, dec.p, nc, 0, s);
-    res.times.core += ms_since(t0);
+    res.times.core += ms_since(t1);
+    for (auto& fu : done) fu.get();
+    for (std::size_t i = 0; i < d; ++i) res.factor_terms[i] = fe[i].term;
+    res.times.factor = ms_since(t0);
     res.core_quant = std::ldexp(ach.hi + ach.lo, -2 * k);
     double est = trunc + res.core_quant;
     for (double v : res.factor_terms) est += v;

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <array>
+#include <functional>
 #include <optional>
 
 #include "common.cuh"
@@ -77,9 +78,12 @@ struct FactorEnc {
 // the sharded multi-GPU mode loop, whose rank 0 encodes the gathered core).
 Result encode_tucker_device(Tucker& f, int dtype, double norm_sq, double target, const Params& p, cudaStream_t s);
 
+// on_flips (optional) receives the column sign flips as soon as they are known,
+// before the plane search and stream finalisation.
 FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<u8>& dead,
                                const std::vector<double>& sn, int coder, bool simple, int core_step_log2,
-                               double cap, bool f32, cudaStream_t s);
+                               double cap, bool f32, cudaStream_t s,
+                               const std::function<void(const std::vector<signed char>&)>& on_flips = {});
 
 std::vector<double> alpha_weights(const std::vector<double>& sn, u64 n);
 std::vector<u64> stable_ascending(const std::vector<u64>& s);
