@@ -3,6 +3,7 @@
 // the single row-major axis permutation (tensor.cpp:105-144).
 // All HBM-bound: 16-byte vector loads, grid = k x 148 SMs, fixed reduction tree.
 #include <cmath>
+#include <cstdint>
 
 #include "kernels.cuh"
 
@@ -61,18 +62,70 @@ constexpr int kRedThreads = 256;
 
 // stage 1: per-CTA partial sums of squares + non-finite flag (fixed tree)
 template <class T>
+struct Vec16;  // 16-byte vector of T
+template <>
+struct Vec16<double> {
+    using type = double2;
+    static constexpr int W = 2;
+    __device__ static void get(const double2& v, double (&o)[4]) { o[0] = v.x, o[1] = v.y, o[2] = o[3] = 0.0; }
+};
+template <>
+struct Vec16<float> {
+    using type = float4;
+    static constexpr int W = 4;
+    __device__ static void get(const float4& v, double (&o)[4]) { o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w; }
+};
+
+// sum of squares + non-finite flag; kVec: x is 16-byte aligned, so the body
+// streams 16-byte vectors, four in flight per thread into four accumulators
+template <class T, bool kVec>
 __global__ void sumsq_stage1(const T* __restrict__ x, u64 n, double* __restrict__ part, int* __restrict__ bad) {
     __shared__ double sh[kRedThreads / 32];
-    double acc = 0.0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     int nonfinite = 0;
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u64 tid = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    u64 done = 0;
+    if (kVec) {
+        using V = typename Vec16<T>::type;
+        constexpr int W = Vec16<T>::W;
+        const V* xv = reinterpret_cast<const V*>(x);
+        const u64 nv = n / W;
+        u64 i = tid;
+        for (; i + 3 * stride < nv; i += 4 * stride) {
+            V v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldcs(xv + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                double e[4];
+                Vec16<T>::get(v[u], e);
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    nonfinite |= !isfinite(e[w]);
+                    acc[u] = fma(e[w], e[w], acc[u]);
+                }
+            }
+        }
+        for (; i < nv; i += stride) {
+            double e[4];
+            Vec16<T>::get(__ldcs(xv + i), e);
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                nonfinite |= !isfinite(e[w]);
+                acc[0] = fma(e[w], e[w], acc[0]);
+            }
+        }
+        done = nv * W;
+    }
+    for (u64 i = done + tid; i < n; i += stride) {
         const double v = static_cast<double>(x[i]);
         nonfinite |= !isfinite(v);
-        acc = fma(v, v, acc);
+        acc[1] = fma(v, v, acc[1]);
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    double t0 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    for (int o = 16; o > 0; o >>= 1) t0 += __shfl_down_sync(0xffffffffu, t0, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t0;
     if (__syncthreads_or(nonfinite) && threadIdx.x == 0) *bad = 1;
     if (threadIdx.x == 0) {
         double t = 0.0;
@@ -101,7 +154,10 @@ double sumsq_impl(const T* x, u64 n, bool* finite, cudaStream_t s) {
     DevBuf<double> part(grid + 1, s);
     DevBuf<int> bad(1, s);
     bad.zero();
-    sumsq_stage1<T><<<grid, kRedThreads, 0, s>>>(x, n, part.p, bad.p);
+    if (reinterpret_cast<uintptr_t>(x) % 16 == 0)
+        sumsq_stage1<T, true><<<grid, kRedThreads, 0, s>>>(x, n, part.p, bad.p);
+    else
+        sumsq_stage1<T, false><<<grid, kRedThreads, 0, s>>>(x, n, part.p, bad.p);
     sum_stage2<<<1, kRedThreads, 0, s>>>(part.p, grid, part.p + grid);
     count_launch(2);
     TCB_LAUNCH();

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdint>
 #include <cstring>
 #include <deque>
 #include <future>
@@ -259,14 +260,18 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, double budget, int backen
     return o;
 }
 
-Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double target,
-                      const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s) {
+Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vector<u64>& shape, double target,
+                      const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite) {
     if (target < 0) throw Error("sthosvd: negative SSE target");
     const std::size_t d = shape.size();
     u64 n_el = 1;
     for (auto v : shape) n_el *= v;
-    bool finite = true;
-    sum_squares(a.p, n_el, &finite, s);
+    const double* a = ext ? ext : owned.p;
+    if (finite < 0) {
+        bool fin = true;
+        sum_squares(a, n_el, &fin, s);
+        finite = fin ? 1 : 0;
+    }
     if (!finite) throw Error("sthosvd: input contains non-finite values");
     std::vector<u64> p = order ? *order : stable_ascending(shape);
     if (!valid_perm(p, d)) throw Error("sthosvd: invalid processing order");
@@ -276,9 +281,23 @@ Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double 
     f.r.assign(d, 0);
     f.trunc.assign(d, 0.0);
     f.factors.resize(d);
-    DevBuf<double> x(n_el, s);
-    permute_axes(a.p, x.p, shape, p, s);
-    a.release();
+    bool ident = true;
+    for (std::size_t i = 0; i < d; ++i) ident = ident && p[i] == i;
+    DevBuf<double> x;
+    const double* xp = nullptr;
+    if (ident) {  // mode 0 reads the input in place
+        if (ext) {
+            xp = ext;
+        } else {
+            x = std::move(owned);
+            xp = x.p;
+        }
+    } else {
+        x = DevBuf<double>(n_el, s);
+        permute_axes(a, x.p, shape, p, s);
+        owned.release();
+        xp = x.p;
+    }
     std::vector<u64> cur(d);
     for (std::size_t i = 0; i < d; ++i) cur[i] = shape[p[i]];
     double remaining = target;
@@ -287,10 +306,11 @@ Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double 
         for (auto v : cur) tot *= v;
         const u64 rows = cur[0], cols = tot / rows;
         const double budget = remaining / static_cast<double>(d - step);
-        StepOut so = mode_step(x.p, rows, cols, budget, backend, s);
+        StepOut so = mode_step(xp, rows, cols, budget, backend, s);
         remaining = std::max(0.0, remaining - so.discarded);
         f.trunc[p[step]] = so.discarded;
         x = std::move(so.next);
+        xp = x.p;
         f.factors[p[step]] = std::move(so.U);
         f.r[p[step]] = so.r;
         cur.erase(cur.begin());
@@ -613,15 +633,22 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
 
     // ingest (container.cpp:69-94): the internal tensor in double; with
     // internal_float32 the values are first rounded to float as the reference does
-    DevBuf<double> a(n_el, s);
-    if (prm.f32) {
+    // fp64 input (container::Dtype 9) is used in place: no ingest copy
+    const bool direct = !prm.f32 && dtype == 9 && reinterpret_cast<uintptr_t>(device_bytes) % 16 == 0;
+    DevBuf<double> a;
+    bool finite = true;
+    if (direct) {
+        res.norm_sq = sum_squares(static_cast<const double*>(device_bytes), n_el, &finite, s);
+    } else if (prm.f32) {
+        a = DevBuf<double>(n_el, s);
         DevBuf<float> af(n_el, s);
         ingest_cast_f32(device_bytes, dtype, n_el, af.p, s);
         ingest_cast(af.p, 8, n_el, a.p, s);
-        res.norm_sq = sum_squares(af.p, n_el, nullptr, s);
+        res.norm_sq = sum_squares(af.p, n_el, &finite, s);
     } else {
+        a = DevBuf<double>(n_el, s);
         ingest_cast(device_bytes, dtype, n_el, a.p, s);
-        res.norm_sq = sum_squares(a.p, n_el, nullptr, s);
+        res.norm_sq = sum_squares(a.p, n_el, &finite, s);
     }
     if (dtype == 6 || dtype == 7) res.precision_loss = ingest_precision_loss(device_bytes, dtype, n_el, s);
     double target;
@@ -636,7 +663,8 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     res.target_sse = target;
 
     auto t0 = Clock::now();
-    Tucker f = sthosvd_device(std::move(a), shape, prm.rtmss * target, prm.mode_order, prm.backend, s);
+    Tucker f = sthosvd_device(std::move(a), direct ? static_cast<const double*>(device_bytes) : nullptr, shape,
+                              prm.rtmss * target, prm.mode_order, prm.backend, s, finite ? 1 : 0);
     double trunc = 0;
     for (double v : f.trunc) trunc += v;
     double core_target = target - trunc;

@@ -60,9 +60,17 @@ struct StepOut {
 StepOut mode_step(const double* x, u64 rows, u64 cols, double budget, int backend, cudaStream_t s);
 // eigensolve + rank rule + sign fix on an (all-reduced) Gram; U is n x r
 StepOut factor_from_gram(const double* G, u64 n, double budget, cudaStream_t s);
-// sthosvd::compress (sthosvd.cpp:114-171) on a device tensor (consumed)
-Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double target,
-                      const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s);
+// sthosvd::compress (sthosvd.cpp:114-171) on a device tensor.  The input is
+// `ext` when non-null (read-only, e.g. the caller's fp64 buffer: with an
+// identity processing order mode 0 reads it in place), else `owned`, which is
+// released as soon as it is no longer needed.  finite: 1 / 0 when the caller
+// already scanned the values (the norm pass), -1 to scan here.
+Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vector<u64>& shape, double target,
+                      const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite = -1);
+inline Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double target,
+                             const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s) {
+    return sthosvd_device(std::move(a), nullptr, shape, target, order, backend, s);
+}
 
 struct FactorEnc {
     std::vector<u8> dead;
