@@ -308,3 +308,8 @@ def transpose(x: np.ndarray, perm):
     out = np.zeros(x.size)
     _check(lib().orc_transpose_f64(_p(x), _p(shape), x.ndim, _p(p), _p(out)))
     return out.reshape([x.shape[i] for i in perm])
+
+
+def threads() -> int:
+    """Host threads the oracle's OpenMP loops use (results do not depend on it)."""
+    return int(lib().orc_threads())

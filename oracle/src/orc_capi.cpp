@@ -1,6 +1,9 @@
 // CPU ORACLE — TEST INFRASTRUCTURE ONLY (see orc.hpp).
 // extern "C" surface loaded by tests/ (ctypes) and bench.py's CPU baseline.
 #include <cstdlib>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <cstring>
 #include <string>
 
@@ -59,6 +62,16 @@ Bytes serial(u64 count, const Stream& s) {
 }  // namespace
 
 extern "C" {
+
+// host threads the oracle's Gram / projection loops use (OpenMP; results do
+// not depend on it)
+int orc_threads() {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
 
 struct orc_params {
     int has_re;

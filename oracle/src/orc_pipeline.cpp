@@ -42,6 +42,8 @@ namespace {
 template <class T>
 void gram_lower(const T* b, std::size_t rows, std::size_t cols, std::vector<T>& g) {
     g.assign(rows * rows, T(0));
+    // one output per (i, j), each summed in the same order whatever the thread count
+#pragma omp parallel for schedule(dynamic, 1)
     for (std::size_t j = 0; j < rows; ++j)
         for (std::size_t i = j; i < rows; ++i) {
             const T* x = b + i * cols;
@@ -134,13 +136,19 @@ Tucker<T> sthosvd(const std::vector<T>& a, const Shape& shape, double target,
         f.r[p[step]] = r;
         // projection fused with the circular shift: next (cols x r) = B^T U_r
         std::vector<T> nx(cols * r, T(0));
-        for (std::size_t i = 0; i < rows; ++i) {
-            const T* brow = x.data() + i * cols;
-            const T* urow = fac.data() + i * r;
-            for (std::size_t c = 0; c < cols; ++c) {
-                const T bv = brow[c];
-                T* o = nx.data() + c * r;
-                for (std::size_t j = 0; j < r; ++j) o[j] += bv * urow[j];
+        // column ranges in parallel; every output still accumulates i = 0, 1, ... in order
+        const std::size_t cb = 4096;
+#pragma omp parallel for schedule(static)
+        for (std::size_t c0 = 0; c0 < cols; c0 += cb) {
+            const std::size_t c1 = std::min(cols, c0 + cb);
+            for (std::size_t i = 0; i < rows; ++i) {
+                const T* brow = x.data() + i * cols;
+                const T* urow = fac.data() + i * r;
+                for (std::size_t c = c0; c < c1; ++c) {
+                    const T bv = brow[c];
+                    T* o = nx.data() + c * r;
+                    for (std::size_t j = 0; j < r; ++j) o[j] += bv * urow[j];
+                }
             }
         }
         x = std::move(nx);
