@@ -62,113 +62,152 @@ __device__ __forceinline__ void load_slab(double (*s)[GPAD], const double* __res
     }
 }
 
+// Stream-K SYRK: the lower-triangle tiles' k-slabs form one unit range
+// [0, lower * nslab) split evenly over exactly (SMs x resident CTAs) CTAs, so
+// every SM gets the same DMMA work (a fixed split-K leaves SMs with 2 or 3
+// CTAs).  A CTA writes one partial per tile it touches (slot = tiles since its
+// first); syrk_sk_reduce sums each tile's partials in CTA order.
 template <bool V16>
-__global__ void __launch_bounds__(256) syrk_kernel(const double* __restrict__ B, u64 rows, u64 cols, u64 kchunk,
-                                                   int ntiles_lower, double* __restrict__ ws) {
+__global__ void __launch_bounds__(256) syrk_sk_kernel(const double* __restrict__ B, u64 rows, u64 cols,
+                                                     int ntiles_lower, u64 nslab, int maxslots,
+                                                     double* __restrict__ ws) {
     extern __shared__ __align__(16) double smem_syrk[];
     auto As = reinterpret_cast<double (*)[GT][GPAD]>(smem_syrk);
     auto Bs = reinterpret_cast<double (*)[GT][GPAD]>(smem_syrk + 2 * GT * GPAD);
-    const int tile = blockIdx.x % ntiles_lower;
-    const int split = blockIdx.x / ntiles_lower;
-    // lower tile index -> (ti, tj), ti >= tj
-    int ti = 0;
-    while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
-    const int tj = tile - ti * (ti + 1) / 2;
-    const bool diag = ti == tj;
-    const u64 k0 = static_cast<u64>(split) * kchunk;
-    const u64 k1 = min(cols, k0 + kchunk);
+    const u64 U = static_cast<u64>(ntiles_lower) * nslab;
+    const u64 u0 = static_cast<u64>(blockIdx.x) * U / gridDim.x, u1 = static_cast<u64>(blockIdx.x + 1) * U / gridDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
-    double acc[4][2][2];
+    int slot = 0;
+    for (u64 u = u0; u < u1; ++slot) {
+        const int tile = static_cast<int>(u / nslab);
+        const u64 s0 = u % nslab, s1 = min(nslab, s0 + (u1 - u));
+        u += s1 - s0;
+        int ti = 0;
+        while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
+        const int tj = tile - ti * (ti + 1) / 2;
+        const bool diag = ti == tj;
+        const u64 k0 = s0 * GBK, k1 = min(cols, s1 * GBK);
+        const u64 ra = static_cast<u64>(ti) * GT, rb = static_cast<u64>(tj) * GT;
+        double acc[4][2][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    const u64 ra = static_cast<u64>(ti) * GT, rb = static_cast<u64>(tj) * GT;
-    const int nslab = k1 > k0 ? static_cast<int>((k1 - k0 + GBK - 1) / GBK) : 0;
-    if (nslab > 0) {
+            for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        const int ns = static_cast<int>(s1 - s0);
+        __syncthreads();  // previous tile's last slab fully consumed before refilling stage 0
         load_slab<V16>(As[0], B, rows, cols, ra, k0, k1);
         if (!diag) load_slab<V16>(Bs[0], B, rows, cols, rb, k0, k1);
         cp_commit();
+        for (int sl = 0; sl < ns; ++sl) {
+            const int cur = sl & 1;
+            if (sl + 1 < ns) {
+                const u64 kn = k0 + static_cast<u64>(sl + 1) * GBK;
+                load_slab<V16>(As[cur ^ 1], B, rows, cols, ra, kn, k1);
+                if (!diag) load_slab<V16>(Bs[cur ^ 1], B, rows, cols, rb, kn, k1);
+                cp_commit();
+                cp_wait<1>();
+            } else {
+                cp_wait<0>();
+            }
+            __syncthreads();
+            double (*As_)[GPAD] = As[cur];
+            double (*Bs_)[GPAD] = diag ? As[cur] : Bs[cur];
+#pragma unroll
+            for (int kk = 0; kk < GBK; kk += 4) {
+                double a[4], b[2];
+#pragma unroll
+                for (int mi = 0; mi < 4; ++mi) a[mi] = As_[wm + mi * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+                for (int ni = 0; ni < 2; ++ni) b[ni] = Bs_[wn + ni * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+                for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+            }
+            __syncthreads();
+        }
+        double* out = ws + (static_cast<u64>(blockIdx.x) * maxslots + slot) * GT * GT;
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) {
+                const int m = wm + mi * 8 + (lane >> 2);
+                const int n = wn + ni * 8 + 2 * (lane & 3);
+                *reinterpret_cast<double2*>(out + m * GT + n) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+            }
     }
-    for (int sl = 0; sl < nslab; ++sl) {
-        const int cur = sl & 1;
-        if (sl + 1 < nslab) {
-            const u64 kn = k0 + static_cast<u64>(sl + 1) * GBK;
-            load_slab<V16>(As[cur ^ 1], B, rows, cols, ra, kn, k1);
-            if (!diag) load_slab<V16>(Bs[cur ^ 1], B, rows, cols, rb, kn, k1);
-            cp_commit();
-            cp_wait<1>();
-        } else {
-            cp_wait<0>();
-        }
-        __syncthreads();
-        double (*As_)[GPAD] = As[cur];
-        double (*Bs_)[GPAD] = diag ? As[cur] : Bs[cur];
-#pragma unroll
-        for (int kk = 0; kk < GBK; kk += 4) {
-            double a[4], b[2];
-#pragma unroll
-            for (int mi = 0; mi < 4; ++mi) a[mi] = As_[wm + mi * 8 + (lane >> 2)][kk + (lane & 3)];
-#pragma unroll
-            for (int ni = 0; ni < 2; ++ni) b[ni] = Bs_[wn + ni * 8 + (lane >> 2)][kk + (lane & 3)];
-#pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-                for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-        }
-        __syncthreads();
-    }
-    double* out = ws + (static_cast<u64>(split) * ntiles_lower + tile) * GT * GT;
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-            const int m = wm + mi * 8 + (lane >> 2);
-            const int n = wn + ni * 8 + 2 * (lane & 3);
-            *reinterpret_cast<double2*>(out + m * GT + n) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
-        }
 }
 
-// fixed-order split reduction; writes the full symmetric G (row-major)
-__global__ void syrk_reduce(const double* __restrict__ ws, int splits, int ntiles_lower, u64 rows,
-                            double* __restrict__ G) {
+// tile t's partials come from the contiguous CTA range covering units
+// [t nslab, (t+1) nslab); CTA c's slot for t = t - (first tile of c)
+__global__ void syrk_sk_reduce(const double* __restrict__ ws, int nctas, int maxslots, int ntiles_lower, u64 nslab,
+                               u64 rows, double* __restrict__ G) {
     const int tile = blockIdx.x;
     const int e0 = blockIdx.y * (GT * GT / 16), e1 = e0 + GT * GT / 16;
     int ti = 0;
     while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
     const int tj = tile - ti * (ti + 1) / 2;
+    const u64 U = static_cast<u64>(ntiles_lower) * nslab;
+    const u64 lo = static_cast<u64>(tile) * nslab, hi = lo + nslab;
+    // contributing CTAs (a contiguous range, in order) and their slots, once per block
+    __shared__ long long off[512];
+    __shared__ int noff;
+    const int cf = max(static_cast<int>((lo * nctas) / U) - 1, 0);
+    const int cl = min(static_cast<int>(((hi - 1) * nctas) / U) + 1, nctas - 1);
+    const int nc = cl - cf + 1;
+    for (int q = threadIdx.x; q < nc && q < 512; q += blockDim.x) {
+        const int c = cf + q;
+        const u64 cu0 = static_cast<u64>(c) * U / nctas, cu1 = static_cast<u64>(c + 1) * U / nctas;
+        const bool hit = !(cu1 <= lo || cu0 >= hi || cu1 == cu0);
+        off[q] = hit ? static_cast<long long>((static_cast<u64>(c) * maxslots + (tile - cu0 / nslab)) * GT * GT) : -1;
+    }
+    if (threadIdx.x == 0) noff = min(nc, 512);
+    __syncthreads();
     for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
         const int m = e / GT, n = e % GT;
         const u64 gi = static_cast<u64>(ti) * GT + m, gj = static_cast<u64>(tj) * GT + n;
         if (gi >= rows || gj >= rows || gj > gi) continue;
         double s = 0.0;
-        for (int sp = 0; sp < splits; ++sp) s += ws[(static_cast<u64>(sp) * ntiles_lower + tile) * GT * GT + e];
+        for (int q = 0; q < noff; ++q)
+            if (off[q] >= 0) s += ws[off[q] + e];
         G[gi * rows + gj] = s;
         G[gj * rows + gi] = s;
     }
 }
 
 // ------------------------------------------------------------------ TTM
-constexpr int TM = 128, TN = 64, TBK = 16;
-constexpr int APAD = TM + 4, UPAD = TN + 4;
+// out (cols x r) = B^T U: HBM-bound for small r (one pass over B), so the
+// output tile width follows r (TN = 16 / 32 / 64) instead of padding every
+// projection to 64 columns of DMMA work, and B streams through a 3-stage
+// cp.async pipeline (TM = 128 columns of B x TBK = 16 rows per stage).
+constexpr int TM = 128, TBK = 16, kTtmStages = 3;
+constexpr int APAD = TM + 4;
 
-template <bool AV16>
+template <int TN>
+struct TtmShape {  // 8 warps: TN 64 -> 4x2 warps of 32x32; else 8x1 warps of 16 x TN
+    static constexpr int WM = TN == 64 ? 32 : 16, WN = TN == 64 ? 32 : TN;
+    static constexpr int MI = WM / 8, NI = WN / 8, UPAD = TN + 4;
+    static constexpr int smem_doubles = kTtmStages * TBK * (APAD + UPAD);
+};
+
+template <bool AV16, int TN>
 __global__ void __launch_bounds__(256) ttm_kernel(const double* __restrict__ B, u64 rows, u64 cols,
                                                   const double* __restrict__ U, u64 r, double* __restrict__ out) {
+    using S = TtmShape<TN>;
+    constexpr int MI = S::MI, NI = S::NI, UPAD = S::UPAD;
     extern __shared__ __align__(16) double smem_ttm[];
     auto As = reinterpret_cast<double (*)[TBK][APAD]>(smem_ttm);
-    auto Us = reinterpret_cast<double (*)[TBK][UPAD]>(smem_ttm + 2 * TBK * APAD);
+    auto Us = reinterpret_cast<double (*)[TBK][UPAD]>(smem_ttm + kTtmStages * TBK * APAD);
     const u64 m0 = static_cast<u64>(blockIdx.x) * TM;
     const u64 n0 = static_cast<u64>(blockIdx.y) * TN;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-    double acc[4][4][2];
+    const int wm = TN == 64 ? (warp >> 1) * 32 : warp * 16, wn = TN == 64 ? (warp & 1) * 32 : 0;
+    double acc[MI][NI][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     auto load = [&](int buf, u64 k0) {
         if constexpr (AV16) {
@@ -194,36 +233,35 @@ __global__ void __launch_bounds__(256) ttm_kernel(const double* __restrict__ B, 
         }
     };
     const int nslab = static_cast<int>((rows + TBK - 1) / TBK);
-    load(0, 0);
-    cp_commit();
+#pragma unroll
+    for (int st = 0; st < kTtmStages - 1; ++st) {
+        if (st < nslab) load(st, static_cast<u64>(st) * TBK);
+        cp_commit();
+    }
     for (int sl = 0; sl < nslab; ++sl) {
-        const int cur = sl & 1;
-        if (sl + 1 < nslab) {
-            load(cur ^ 1, static_cast<u64>(sl + 1) * TBK);
-            cp_commit();
-            cp_wait<1>();
-        } else {
-            cp_wait<0>();
-        }
+        const int cur = sl % kTtmStages;
+        cp_wait<kTtmStages - 2>();
         __syncthreads();
+        // refill the stage consumed last iteration (all warps are past it)
+        if (sl + kTtmStages - 1 < nslab) load((sl + kTtmStages - 1) % kTtmStages, static_cast<u64>(sl + kTtmStages - 1) * TBK);
+        cp_commit();
 #pragma unroll
         for (int kk = 0; kk < TBK; kk += 4) {
-            double a[4], b[4];
+            double a[MI], b[NI];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) a[mi] = As[cur][kk + (lane & 3)][wm + mi * 8 + (lane >> 2)];
+            for (int mi = 0; mi < MI; ++mi) a[mi] = As[cur][kk + (lane & 3)][wm + mi * 8 + (lane >> 2)];
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) b[ni] = Us[cur][kk + (lane & 3)][wn + ni * 8 + (lane >> 2)];
+            for (int ni = 0; ni < NI; ++ni) b[ni] = Us[cur][kk + (lane & 3)][wn + ni * 8 + (lane >> 2)];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
+            for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+                for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
         }
-        __syncthreads();
     }
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
+        for (int ni = 0; ni < NI; ++ni) {
             const u64 m = m0 + wm + mi * 8 + (lane >> 2);
             const u64 n = n0 + wn + ni * 8 + 2 * (lane & 3);
             if (m >= cols) continue;
@@ -296,25 +334,26 @@ void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
     ProfScope prof_scope(kGram, s);
     const int nt = static_cast<int>((rows + GT - 1) / GT);
     const int lower = nt * (nt + 1) / 2;
-    const u64 want = static_cast<u64>(2 * sm_count());
-    u64 splits = std::max<u64>(1, (want + lower - 1) / lower);
-    splits = std::min<u64>(splits, std::max<u64>(1, cols / 256));
-    u64 kchunk = (cols + splits - 1) / splits;
-    kchunk = (kchunk + GBK - 1) / GBK * GBK;
-    splits = (cols + kchunk - 1) / kchunk;
-    DevBuf<double> ws(splits * lower * GT * GT, s);
-    const unsigned grid = static_cast<unsigned>(splits * lower);
+    const u64 nslab = (cols + GBK - 1) / GBK;
     const bool v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
     const int smem = 4 * GT * GPAD * sizeof(double);
-    static bool attr = [&] {
-        cudaFuncSetAttribute(syrk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(syrk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        return true;
+    static int per_sm = [&] {
+        cudaFuncSetAttribute(syrk_sk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(syrk_sk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, syrk_sk_kernel<true>, 256, smem);
+        return std::max(1, b);
     }();
-    (void)attr;
-    if (v16) syrk_kernel<true><<<grid, 256, smem, s>>>(B, rows, cols, kchunk, lower, ws.p);
-    else syrk_kernel<false><<<grid, 256, smem, s>>>(B, rows, cols, kchunk, lower, ws.p);
-    syrk_reduce<<<dim3(lower, 16), 256, 0, s>>>(ws.p, static_cast<int>(splits), lower, rows, G);
+    const u64 units = static_cast<u64>(lower) * nslab;
+    const int nctas = static_cast<int>(std::min<u64>(units, static_cast<u64>(per_sm) * sm_count()));
+    // a CTA spans at most ceil(units / nctas / nslab) + 1 tiles
+    const int maxslots = static_cast<int>((units / nctas + nslab - 1) / nslab) + 1;
+    DevBuf<double> ws(static_cast<u64>(nctas) * maxslots * GT * GT, s);
+    if (v16)
+        syrk_sk_kernel<true><<<nctas, 256, smem, s>>>(B, rows, cols, lower, nslab, maxslots, ws.p);
+    else
+        syrk_sk_kernel<false><<<nctas, 256, smem, s>>>(B, rows, cols, lower, nslab, maxslots, ws.p);
+    syrk_sk_reduce<<<dim3(lower, 16), 256, 0, s>>>(ws.p, nctas, maxslots, lower, nslab, rows, G);
     count_launch(2);
     TCB_LAUNCH();
 }
@@ -326,19 +365,26 @@ void gram_cols_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t 
     TCB_LAUNCH();
 }
 
-void ttm_f64(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s) {
-    ProfScope prof_scope(kTtm, s);
+template <int TN>
+void launch_ttm(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s) {
     dim3 grid(cdiv(cols, TM), cdiv(r, TN));
     const bool v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
-    const int smem = 2 * TBK * (APAD + UPAD) * sizeof(double);
-    static bool attr = [&] {
-        cudaFuncSetAttribute(ttm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(ttm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    constexpr int smem = TtmShape<TN>::smem_doubles * sizeof(double);
+    static bool attr = [] {
+        cudaFuncSetAttribute(ttm_kernel<true, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(ttm_kernel<false, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         return true;
     }();
     (void)attr;
-    if (v16) ttm_kernel<true><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out);
-    else ttm_kernel<false><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out);
+    if (v16) ttm_kernel<true, TN><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out);
+    else ttm_kernel<false, TN><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out);
+}
+
+void ttm_f64(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s) {
+    ProfScope prof_scope(kTtm, s);
+    if (r <= 16) launch_ttm<16>(B, rows, cols, U, r, out, s);
+    else if (r <= 32) launch_ttm<32>(B, rows, cols, U, r, out, s);
+    else launch_ttm<64>(B, rows, cols, U, r, out, s);
     count_launch();
     TCB_LAUNCH();
 }
