@@ -52,6 +52,13 @@ void fix_column_signs(double* U, u64 n, u64 r, cudaStream_t s);
 // Normalise columns of U (n x r row-major) by 1/sigma_j and re-orthonormalise (MGS).
 void scale_orthonormalize(double* U, u64 n, u64 r, const double* sigma, cudaStream_t s);
 
+// ---- topk.cu: certified top-p eigenpairs by block subspace iteration + Rayleigh-Ritz.
+bool topk_supported(u64 n, int p);
+// X (n x p row-major): Ritz vectors for theta (descending); resid[j] = |G x_j - theta_j x_j|;
+// trace = trace(G).  Synchronises the stream (host copies of theta / resid / trace).
+void topk_eig(const double* G, u64 n, int p, int extra_iters, double* X, std::vector<double>& theta,
+              std::vector<double>& resid, double& trace, cudaStream_t s);
+
 // ---- quant.cu (core_codec.cpp:55-93)
 void quantize_f64(const double* x, u64 n, int k, u64* mag, u8* neg, cudaStream_t s);
 // Per-axis slice sums of (double)m^2 replayed in lexicographic order, then sqrt(s*down).

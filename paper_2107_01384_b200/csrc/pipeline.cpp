@@ -7,10 +7,12 @@
 #include "pipeline.hpp"
 
 #include <algorithm>
+#include <cfloat>
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <future>
@@ -19,6 +21,7 @@
 #include <mutex>
 #include <numeric>
 #include <thread>
+#include <tuple>
 
 #include "kernels.cuh"
 #include "quant.cuh"
@@ -203,7 +206,72 @@ std::vector<double> alpha_weights(const std::vector<double>& sn, u64 n) {
     return al;
 }
 
+// Fast path of the eigensolve + rank rule (topk.cu): top-32 Ritz pairs by
+// block subspace iteration, accepted only with a certificate --
+//   * the rank rule's cutoff r leaves >= 8 vectors of the block unused, with
+//     the discarded energy taken as trace(G) - sum_{j<r} theta_j;
+//   * every kept residual |G x_j - theta_j x_j| is at the roundoff floor
+//     (16 eps sqrt(n) theta_0), so |theta_j - lambda_j| is negligible;
+//   * the Davis-Kahan bound |R_kept|_F / (theta_{r-1} - theta_r - |r_r|) on
+//     the kept subspace's sine is <= 5e-7 (the parity tolerance is 1e-6).
+// V receives the n x r Ritz vectors (unsigned).  false: use the full solver.
+bool topk_factor(const double* G, u64 n, double budget, cudaStream_t s, u64& r_out, double& gone_out,
+                 std::vector<double>& s2_out, DevBuf<double>& V) {
+    constexpr int p = 32, spare = 8;
+    if (!topk_supported(n, p)) return false;
+    if (const char* e = std::getenv("TCB_NO_TOPK"); e && *e && *e != '0') return false;
+    DevBuf<double> X(n * p, s);
+    for (int extra : {2, 5}) {
+        std::vector<double> th, res;
+        double tr = 0.0;
+        topk_eig(G, n, p, extra, X.p, th, res, tr, s);
+        std::vector<double> s2(p);
+        for (int j = 0; j < p; ++j) s2[j] = std::max(0.0, th[j]);
+        int r = -1;
+        double gone = 0.0, pref = 0.0;
+        for (int k = 0; k <= p - spare; ++k) {
+            const double tail = std::max(0.0, tr - pref);
+            if (tail <= budget) {
+                r = k;
+                gone = tail;
+                break;
+            }
+            pref += s2[k];
+        }
+        if (r < 0) return false;  // cutoff beyond the block
+        if (r == 0) {             // sthosvd.cpp:146-150
+            r = 1;
+            gone -= s2[0];
+        }
+        const double floor_res = 16.0 * DBL_EPSILON * std::sqrt(static_cast<double>(n)) * std::max(th[0], 0.0);
+        double rk2 = 0.0, rmax = 0.0;
+        for (int j = 0; j < r; ++j) {
+            rk2 += res[j] * res[j];
+            rmax = std::max(rmax, res[j]);
+        }
+        const double gap = th[r - 1] - th[r] - res[r];
+        const bool ok = rmax <= floor_res && gap > 0.0 && std::sqrt(rk2) <= 5e-7 * gap;
+        if (!ok) continue;
+        r_out = static_cast<u64>(r);
+        gone_out = gone;
+        s2_out = s2;
+        V = DevBuf<double>(n * r, s);
+        TCB_CUDA(cudaMemcpy2DAsync(V.p, r * sizeof(double), X.p, p * sizeof(double), r * sizeof(double), n,
+                                   cudaMemcpyDeviceToDevice, s));
+        return true;
+    }
+    return false;
+}
+
 StepOut factor_from_gram(const double* G, u64 n, double budget, cudaStream_t s) {
+    {
+        StepOut o;
+        std::vector<double> s2;
+        if (topk_factor(G, n, budget, s, o.r, o.discarded, s2, o.U)) {
+            fix_column_signs(o.U.p, n, o.r, s);
+            return o;
+        }
+    }
     EigWork w;
     const auto ev = eig_values(G, n, w, s);
     std::vector<double> s2(n);
@@ -233,19 +301,25 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, double budget, int backen
         EigWork w;
         DevBuf<double> G(cols * cols, s);
         gram_cols_f64(x, rows, cols, G.p, s);
-        const auto ev = eig_values(G.p, cols, w, s);
-        std::vector<double> s2(cols);
-        for (u64 j = 0; j < cols; ++j) s2[j] = std::max(0.0, ev[j]);
-        auto [r, gone] = pick_rank(s2, budget);
-        if (r == 0) {
-            r = 1;
-            gone -= s2[0];
+        u64 r = 0;
+        double gone = 0.0;
+        std::vector<double> s2;
+        DevBuf<double> V;
+        if (!topk_factor(G.p, cols, budget, s, r, gone, s2, V)) {
+            const auto ev = eig_values(G.p, cols, w, s);
+            s2.assign(cols, 0.0);
+            for (u64 j = 0; j < cols; ++j) s2[j] = std::max(0.0, ev[j]);
+            std::tie(r, gone) = pick_rank(s2, budget);
+            if (r == 0) {
+                r = 1;
+                gone -= s2[0];
+            }
+            V = DevBuf<double>(cols * r, s);
+            eig_vectors(w, r, V.p, s);
         }
         o.r = r;
         o.discarded = gone;
         o.U = DevBuf<double>(rows * r, s);
-        DevBuf<double> V(cols * r, s);
-        eig_vectors(w, r, V.p, s);
         gemm_nn_f64(x, rows, cols, V.p, r, o.U.p, s);
         std::vector<double> sig(r);
         for (u64 j = 0; j < r; ++j) sig[j] = std::sqrt(s2[j]);

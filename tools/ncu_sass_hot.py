@@ -8,7 +8,12 @@ h = next(r for r in rows if r and r[0] == "Address")
 hi = rows.index(h)
 si = h.index("Warp Stall Sampling (All Samples)")
 stall = [(i, c) for i, c in enumerate(h) if c.startswith("stall_")]
-body = [r for r in rows[hi + 1:] if len(r) == len(h)]
+body = []
+for r in rows[hi + 1:]:  # first kernel's section only
+    if r and r[0] in ("Address", "Kernel Name"):
+        break
+    if len(r) == len(h):
+        body.append(r)
 tot = sum(int(r[si]) for r in body)
 print(f"total samples {tot}")
 for n, r in enumerate(body):
