@@ -62,115 +62,93 @@ __device__ __forceinline__ void load_slab(double (*s)[GPAD], const double* __res
     }
 }
 
-// Stream-K SYRK: the lower-triangle tiles' k-slabs form one unit range
-// [0, lower * nslab) split evenly over exactly (SMs x resident CTAs) CTAs, so
-// every SM gets the same DMMA work (a fixed split-K leaves SMs with 2 or 3
-// CTAs).  A CTA writes one partial per tile it touches (slot = tiles since its
-// first); syrk_sk_reduce sums each tile's partials in CTA order.
+// Split-K SYRK sized to the machine: grid = tiles x splits with splits =
+// floor(SMs x resident CTAs / tiles), so every SM gets the same DMMA work
+// (a fixed split count leaves SMs with 2 or 3 CTAs), and blockIdx runs tile-
+// fastest so the CTAs resident together cover all lower-triangle tiles of the
+// same k-chunk and share B's row blocks through L2 (one DRAM pass over B).
 template <bool V16>
-__global__ void __launch_bounds__(256) syrk_sk_kernel(const double* __restrict__ B, u64 rows, u64 cols,
-                                                     int ntiles_lower, u64 nslab, int maxslots,
-                                                     double* __restrict__ ws) {
+__global__ void __launch_bounds__(256) syrk_kernel(const double* __restrict__ B, u64 rows, u64 cols,
+                                                  int ntiles_lower, u64 slabs_per_split, u64 nslab,
+                                                  double* __restrict__ ws) {
     extern __shared__ __align__(16) double smem_syrk[];
     auto As = reinterpret_cast<double (*)[GT][GPAD]>(smem_syrk);
     auto Bs = reinterpret_cast<double (*)[GT][GPAD]>(smem_syrk + 2 * GT * GPAD);
-    const u64 U = static_cast<u64>(ntiles_lower) * nslab;
-    const u64 u0 = static_cast<u64>(blockIdx.x) * U / gridDim.x, u1 = static_cast<u64>(blockIdx.x + 1) * U / gridDim.x;
+    const int tile = blockIdx.x % ntiles_lower;
+    const u64 split = blockIdx.x / ntiles_lower;
+    const u64 s0 = split * slabs_per_split, s1 = min(nslab, s0 + slabs_per_split);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
-    int slot = 0;
-    for (u64 u = u0; u < u1; ++slot) {
-        const int tile = static_cast<int>(u / nslab);
-        const u64 s0 = u % nslab, s1 = min(nslab, s0 + (u1 - u));
-        u += s1 - s0;
-        int ti = 0;
-        while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
-        const int tj = tile - ti * (ti + 1) / 2;
-        const bool diag = ti == tj;
-        const u64 k0 = s0 * GBK, k1 = min(cols, s1 * GBK);
-        const u64 ra = static_cast<u64>(ti) * GT, rb = static_cast<u64>(tj) * GT;
-        double acc[4][2][2];
+    int ti = 0;
+    while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
+    const int tj = tile - ti * (ti + 1) / 2;
+    const bool diag = ti == tj;
+    const u64 k0 = s0 * GBK, k1 = min(cols, s1 * GBK);
+    const u64 ra = static_cast<u64>(ti) * GT, rb = static_cast<u64>(tj) * GT;
+    double acc[4][2][2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        const int ns = static_cast<int>(s1 - s0);
-        __syncthreads();  // previous tile's last slab fully consumed before refilling stage 0
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int ns = s1 > s0 ? static_cast<int>(s1 - s0) : 0;
+    if (ns > 0) {
         load_slab<V16>(As[0], B, rows, cols, ra, k0, k1);
         if (!diag) load_slab<V16>(Bs[0], B, rows, cols, rb, k0, k1);
         cp_commit();
-        for (int sl = 0; sl < ns; ++sl) {
-            const int cur = sl & 1;
-            if (sl + 1 < ns) {
-                const u64 kn = k0 + static_cast<u64>(sl + 1) * GBK;
-                load_slab<V16>(As[cur ^ 1], B, rows, cols, ra, kn, k1);
-                if (!diag) load_slab<V16>(Bs[cur ^ 1], B, rows, cols, rb, kn, k1);
-                cp_commit();
-                cp_wait<1>();
-            } else {
-                cp_wait<0>();
-            }
-            __syncthreads();
-            double (*As_)[GPAD] = As[cur];
-            double (*Bs_)[GPAD] = diag ? As[cur] : Bs[cur];
-#pragma unroll
-            for (int kk = 0; kk < GBK; kk += 4) {
-                double a[4], b[2];
-#pragma unroll
-                for (int mi = 0; mi < 4; ++mi) a[mi] = As_[wm + mi * 8 + (lane >> 2)][kk + (lane & 3)];
-#pragma unroll
-                for (int ni = 0; ni < 2; ++ni) b[ni] = Bs_[wn + ni * 8 + (lane >> 2)][kk + (lane & 3)];
-#pragma unroll
-                for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-                    for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-            }
-            __syncthreads();
-        }
-        double* out = ws + (static_cast<u64>(blockIdx.x) * maxslots + slot) * GT * GT;
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < 2; ++ni) {
-                const int m = wm + mi * 8 + (lane >> 2);
-                const int n = wn + ni * 8 + 2 * (lane & 3);
-                *reinterpret_cast<double2*>(out + m * GT + n) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
-            }
     }
+    for (int sl = 0; sl < ns; ++sl) {
+        const int cur = sl & 1;
+        if (sl + 1 < ns) {
+            const u64 kn = k0 + static_cast<u64>(sl + 1) * GBK;
+            load_slab<V16>(As[cur ^ 1], B, rows, cols, ra, kn, k1);
+            if (!diag) load_slab<V16>(Bs[cur ^ 1], B, rows, cols, rb, kn, k1);
+            cp_commit();
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        double (*As_)[GPAD] = As[cur];
+        double (*Bs_)[GPAD] = diag ? As[cur] : Bs[cur];
+#pragma unroll
+        for (int kk = 0; kk < GBK; kk += 4) {
+            double a[4], b[2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = As_[wm + mi * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) b[ni] = Bs_[wn + ni * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        __syncthreads();
+    }
+    double* out = ws + static_cast<u64>(blockIdx.x) * GT * GT;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+            const int m = wm + mi * 8 + (lane >> 2);
+            const int n = wn + ni * 8 + 2 * (lane & 3);
+            *reinterpret_cast<double2*>(out + m * GT + n) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+        }
 }
 
-// tile t's partials come from the contiguous CTA range covering units
-// [t nslab, (t+1) nslab); CTA c's slot for t = t - (first tile of c)
-__global__ void syrk_sk_reduce(const double* __restrict__ ws, int nctas, int maxslots, int ntiles_lower, u64 nslab,
-                               u64 rows, double* __restrict__ G) {
+// fixed-order split reduction (split 0, 1, ...); writes the full symmetric G (row-major)
+__global__ void syrk_reduce(const double* __restrict__ ws, int splits, int ntiles_lower, u64 rows,
+                            double* __restrict__ G) {
     const int tile = blockIdx.x;
     const int e0 = blockIdx.y * (GT * GT / 16), e1 = e0 + GT * GT / 16;
     int ti = 0;
     while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
     const int tj = tile - ti * (ti + 1) / 2;
-    const u64 U = static_cast<u64>(ntiles_lower) * nslab;
-    const u64 lo = static_cast<u64>(tile) * nslab, hi = lo + nslab;
-    // contributing CTAs (a contiguous range, in order) and their slots, once per block
-    __shared__ long long off[512];
-    __shared__ int noff;
-    const int cf = max(static_cast<int>((lo * nctas) / U) - 1, 0);
-    const int cl = min(static_cast<int>(((hi - 1) * nctas) / U) + 1, nctas - 1);
-    const int nc = cl - cf + 1;
-    for (int q = threadIdx.x; q < nc && q < 512; q += blockDim.x) {
-        const int c = cf + q;
-        const u64 cu0 = static_cast<u64>(c) * U / nctas, cu1 = static_cast<u64>(c + 1) * U / nctas;
-        const bool hit = !(cu1 <= lo || cu0 >= hi || cu1 == cu0);
-        off[q] = hit ? static_cast<long long>((static_cast<u64>(c) * maxslots + (tile - cu0 / nslab)) * GT * GT) : -1;
-    }
-    if (threadIdx.x == 0) noff = min(nc, 512);
-    __syncthreads();
     for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
         const int m = e / GT, n = e % GT;
         const u64 gi = static_cast<u64>(ti) * GT + m, gj = static_cast<u64>(tj) * GT + n;
         if (gi >= rows || gj >= rows || gj > gi) continue;
         double s = 0.0;
-        for (int q = 0; q < noff; ++q)
-            if (off[q] >= 0) s += ws[off[q] + e];
+        for (int sp = 0; sp < splits; ++sp) s += ws[(static_cast<u64>(sp) * ntiles_lower + tile) * GT * GT + e];
         G[gi * rows + gj] = s;
         G[gj * rows + gi] = s;
     }
@@ -338,22 +316,23 @@ void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
     const bool v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
     const int smem = 4 * GT * GPAD * sizeof(double);
     static int per_sm = [&] {
-        cudaFuncSetAttribute(syrk_sk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(syrk_sk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(syrk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(syrk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, syrk_sk_kernel<true>, 256, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, syrk_kernel<true>, 256, smem);
         return std::max(1, b);
     }();
-    const u64 units = static_cast<u64>(lower) * nslab;
-    const int nctas = static_cast<int>(std::min<u64>(units, static_cast<u64>(per_sm) * sm_count()));
-    // a CTA spans at most ceil(units / nctas / nslab) + 1 tiles
-    const int maxslots = static_cast<int>((units / nctas + nslab - 1) / nslab) + 1;
-    DevBuf<double> ws(static_cast<u64>(nctas) * maxslots * GT * GT, s);
+    const u64 slots = static_cast<u64>(per_sm) * sm_count();
+    u64 splits = std::max<u64>(1, std::min<u64>(nslab, slots / lower));
+    const u64 per = (nslab + splits - 1) / splits;
+    splits = (nslab + per - 1) / per;
+    DevBuf<double> ws(splits * lower * GT * GT, s);
+    const unsigned grid = static_cast<unsigned>(splits * lower);
     if (v16)
-        syrk_sk_kernel<true><<<nctas, 256, smem, s>>>(B, rows, cols, lower, nslab, maxslots, ws.p);
+        syrk_kernel<true><<<grid, 256, smem, s>>>(B, rows, cols, lower, per, nslab, ws.p);
     else
-        syrk_sk_kernel<false><<<nctas, 256, smem, s>>>(B, rows, cols, lower, nslab, maxslots, ws.p);
-    syrk_sk_reduce<<<dim3(lower, 16), 256, 0, s>>>(ws.p, nctas, maxslots, lower, nslab, rows, G);
+        syrk_kernel<false><<<grid, 256, smem, s>>>(B, rows, cols, lower, per, nslab, ws.p);
+    syrk_reduce<<<dim3(lower, 16), 256, 0, s>>>(ws.p, static_cast<int>(splits), lower, rows, G);
     count_launch(2);
     TCB_LAUNCH();
 }
