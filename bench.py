@@ -9,8 +9,9 @@ the paper's datasets are not available), requested relative error 1e-4.
 A step = one pipeline::compress of that tensor (device-resident input ->
 container bytes on the host).  Inputs are 128 MiB (> L2 is 126 MB) and L2 is
 additionally flushed (256 MiB write) before every timed step, outside the
-per-step CUDA-event window.  N > 1: one independent replica per rank (weak
-scaling; the sharded Gram all-reduce path is not built yet), max over ranks.
+per-step CUDA-event window.  N > 1 (or --sharded): the ranks compress ONE
+256 x 256 x (256 N) tensor sharded along its last processed mode (NCCL
+all-reduce of partial Grams; weak scaling, 128 MiB per rank), max over ranks.
 """
 from __future__ import annotations
 
@@ -142,6 +143,132 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def c2_slab(world, rank, seed=0):
+    """Rank `rank`'s 256^3 slab (along mode 2) of the weak-scaled c2-family
+    tensor 256 x 256 x (256 world): the c2 generator (64 separable k^-1.5
+    sinusoid terms, x = i/n per mode) on the global extents, plus independent
+    N(0, 1e-5) noise per slab."""
+    rng = np.random.default_rng(seed)
+    shape = (256, 256, 256 * world)
+    K = 64
+    amps = np.arange(1, K + 1, dtype=np.float64) ** -1.5
+    mats = [np.empty((n, K)) for n in shape]
+    for k in range(K):
+        for m, n in enumerate(shape):
+            f = rng.uniform(0.5, 4.0)
+            ph = rng.uniform(0.0, 2 * np.pi)
+            mats[m][:, k] = np.sin(2 * np.pi * f * (np.arange(n, dtype=np.float64) / n) + ph)
+    v3 = mats[2][rank * 256:(rank + 1) * 256]
+    rest = (mats[1][:, None, :] * v3[None, :, :]).reshape(-1, K)
+    slab = ((mats[0] * amps[None, :]) @ rest.T).reshape(256, 256, 256)
+    slab += 1e-5 * np.random.default_rng(seed * 7919 + 1 + rank).standard_normal(slab.shape)
+    return np.ascontiguousarray(slab)
+
+
+def main_sharded(args, rank, local, world):
+    """N ranks compress ONE tensor 256 x 256 x (256 N) sharded along its last
+    processed mode (shard.py: partial Grams all-reduced over NCCL, replicated
+    eigensolve, shard-local TTM, gather before the last step, rank 0 encodes).
+    Weak scaling: 128 MiB per rank; value = N x 128 MiB / max-over-ranks time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2107_01384_b200 as tcb
+    from paper_2107_01384_b200 import shard
+
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    xs = c2_slab(world, rank)
+    shape = [256, 256, 256 * world]
+    nbytes = xs.nbytes
+    host = torch.from_numpy(xs).pin_memory()
+    d_in = host.to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    params = tcb.Params(target_re=args.re)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(x):
+        return shard.compress_sharded(x, shape, tcb.Dtype.float64, params)
+
+    for _ in range(args.warmup):
+        res = step(d_in)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = tcb.kernel_launches()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        res = step(d_in)
+        b.record()
+        b.synchronize()
+        step_ms.append(a.elapsed_time(b))
+    barrier()
+    launches = (tcb.kernel_launches() - launches0) // max(1, args.steps)
+    e2e_ms = []
+    for _ in range(args.steps):  # e2e: this rank's slab from pinned host memory, container to rank 0's host
+        flush.fill_(1)
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        r2 = step(host.to(dev, non_blocking=True))
+        b.record()
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    barrier()
+    clk = clocks.stop()
+    t = torch.tensor([sum(step_ms), sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot, tot_e2e = float(t[0]), float(t[1])
+    value = world * nbytes * args.steps / (tot * 1e-3) / 1e9
+    e2e = world * nbytes * args.steps / (tot_e2e * 1e-3) / 1e9
+    if rank == 0:
+        order = [0, 1, 2]
+        gram_flop, ttm_flop = algorithmic_work(shape, res.ranks, order)
+        per_rank = (gram_flop + ttm_flop) / world
+        ach = per_rank / (tot / args.steps * 1e-3) / 1e12
+        L = tcb.lib()
+        import ctypes as C
+
+        L.tcb_peak_dmma_tflops.restype = C.c_double
+        peak = float(L.tcb_peak_dmma_tflops())
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"c2 family weak-scaled: 256 x 256 x {256 * world} fp64 (128 MiB per rank), "
+                                   f"RE {args.re}", "input_bytes": world * nbytes, "ranks": res.ranks,
+                       "container_bytes": len(res.container), "l2": "256 MiB flush before every timed step; "
+                       "128 MiB per rank > L2",
+                       "parallelism": f"shard mode 2 over {world} ranks (NCCL all-reduce of partial Grams, "
+                                      f"replicated eigensolve, shard-local TTM)"},
+            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": nbytes,
+                    "d2h_bytes_per_step": len(r2.container)},
+            "gpu_launches": int(launches),
+            "roofline": {"kernel": "per-rank Gram + TTM (whole step as the time base)", "bound": "tensor",
+                         "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+                         "note": "lower bound: the step also holds the eigensolves and the encode"},
+            "cpu_baseline": None,
+            "clocks": clk,
+            "step_ms_all": [round(v, 3) for v in step_ms],
+            "e2e_ms_all": [round(v, 3) for v in e2e_ms],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -150,10 +277,18 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--re", type=float, default=1e-4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="sharded one-tensor path also at N=1")
     args = ap.parse_args()
     args.warmup_ref = min(args.warmup, 1)
     if args.impl == "reference":
         run_reference(args)
+        return
+    rank, local, world = _env_rank()
+    if world > 1 or args.sharded:
+        import torch
+
+        torch.cuda.set_device(local)
+        main_sharded(args, rank, local, world)
         return
 
     import torch
@@ -309,7 +444,7 @@ def main():
             "config": {"workload": WORKLOAD, "input_bytes": nbytes, "ranks": res.ranks,
                        "container_bytes": len(res.container), "compression_factor": res.compression_factor(),
                        "core_last_plane": res.core_last_plane, "l2": "256 MiB flush before every timed step; "
-                       "input 128 MiB > L2", "parallelism": f"{world} independent replica(s)"},
+                       "input 128 MiB > L2", "parallelism": "single GPU"},
             "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": nbytes,
                     "d2h_bytes_per_step": len(r2.container)},
             "gpu_launches": int(launches),

@@ -140,22 +140,30 @@ def _all_gather_cat(t, axis, group, world):
     return torch.cat([b.narrow(axis, 0, s) for b, s in zip(bufs, sizes)], dim=axis).contiguous()
 
 
-def sthosvd_sharded(x_local, shape, target, ops, order=None, backend=0, group=None):
-    """ST-HOSVD over ranks; `x_local` is this rank's slab of mode order[-1]
-    (original axis order).  Returns the replicated factorization."""
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    d = len(shape)
-    p = list(order) if order is not None else stable_ascending(shape)
+def _global_stats(x_local, ops, group, world):
+    """(||x||^2 over all ranks, every value finite on every rank) in one pass per rank."""
     ssq, finite = ops.sumsq(x_local)
     stats = torch.tensor([ssq, 0.0 if finite else 1.0], dtype=torch.float64, device=x_local.device)
     if world > 1:
         dist.all_reduce(stats, group=group)
+    return float(stats[0].item()), stats[1].item() == 0.0
+
+
+def sthosvd_sharded(x_local, shape, target, ops, order=None, backend=0, group=None, stats=None):
+    """ST-HOSVD over ranks; `x_local` is this rank's slab of mode order[-1]
+    (original axis order).  `stats` = (norm^2, all finite) when the caller
+    already scanned the input.  Returns the replicated factorization."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    d = len(shape)
+    p = list(order) if order is not None else stable_ascending(shape)
+    norm_sq, finite = stats if stats is not None else _global_stats(x_local, ops, group, world)
     if target < 0:
         raise TucompError("sthosvd: negative SSE target")
-    if stats[1].item() != 0.0:
+    if not finite:
         raise TucompError("sthosvd: input contains non-finite values")
-    xl = ops.permute(x_local, p)  # (n_p0, ..., n_p(d-1) local slab)
+    # identity processing order: mode 0 reads the slab in place (tensor.cpp:105-144 is a no-op then)
+    xl = x_local.contiguous() if p == list(range(d)) else ops.permute(x_local, p)
     cur = list(xl.shape)
     sh_axis = d - 1  # position of the sharded mode in `cur`
     remaining = float(target)
@@ -199,7 +207,7 @@ def sthosvd_sharded(x_local, shape, target, ops, order=None, backend=0, group=No
         factors[p[step]] = u
         ranks[p[step]] = r
     return ShardedTucker(core=xl.view(cur), factors=factors, ranks=ranks, order=p, trunc=trunc,
-                         norm_sq=float(stats[0].item()))
+                         norm_sq=norm_sq)
 
 
 def compress_sharded(x_local, shape, dtype, params: Params, ops=None, group=None):
@@ -212,17 +220,14 @@ def compress_sharded(x_local, shape, dtype, params: Params, ops=None, group=None
         raise TucompError("compress: no error target given")
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    ssq, _ = ops.sumsq(x_local)
-    t = torch.tensor([ssq], dtype=torch.float64, device=x_local.device)
-    if world > 1:
-        dist.all_reduce(t, group=group)
-    norm_sq = float(t.item())
+    norm_sq, finite = _global_stats(x_local, ops, group, world)
     target = params.target_re ** 2 * norm_sq if params.target_re is not None else params.target_sse
     if target < 0:
         raise TucompError("budget: negative SSE target")
     if not 0.0 <= params.rtmss <= 1.0:
         raise TucompError("budget: rtmss outside [0, 1]")
-    f = sthosvd_sharded(x_local, shape, params.rtmss * target, ops, params.mode_order, params.svd_backend, group)
+    f = sthosvd_sharded(x_local, shape, params.rtmss * target, ops, params.mode_order, params.svd_backend, group,
+                        stats=(norm_sq, finite))
     if rank != 0:
         return None
     return ops.encode(f.core.contiguous(), [u.contiguous() for u in f.factors], list(shape), f.ranks, f.order,
