@@ -1,8 +1,12 @@
 // extern "C" boundary (include/tucomp_b200.h).  Each entry point owns one CUDA
 // stream for the call, converts exceptions into status + message, and never
 // falls back to host computation.
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "../../include/tucomp_b200.h"
@@ -27,6 +31,42 @@ std::vector<Rec> g_recs;
 }  // namespace
 
 bool prof_enabled() { return g_prof; }
+
+namespace {
+std::mutex g_trace_mu;
+std::map<std::string, std::pair<double, u64>> g_trace;
+bool trace_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_TRACE");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+long long now_ns() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+}  // namespace
+
+HostTrace::HostTrace(const char* l) : label(l) {
+    if (trace_on()) t0 = now_ns();
+}
+HostTrace::~HostTrace() {
+    if (!trace_on()) return;
+    const double ms = (now_ns() - t0) * 1e-6;
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    auto& e = g_trace[label];
+    e.first += ms;
+    e.second += 1;
+}
+void host_trace_dump() {
+    if (!trace_on()) return;
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    for (auto& [k, v] : g_trace) std::fprintf(stderr, "[tcb trace] %-28s %8.3f ms  x%llu\n", k.c_str(), v.first,
+                                               static_cast<unsigned long long>(v.second));
+    g_trace.clear();
+}
 
 ProfScope::ProfScope(Cat c, cudaStream_t s) : cat(c), st(s) {
     if (!g_prof) return;
@@ -204,6 +244,7 @@ int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_
         DevBuf<u8> dev(nbytes - skip + 16, st.s);
         dev.upload(bytes + skip, nbytes - skip);
         const Result r = compress_device(dev.p, nbytes - skip, dtype, sh, to_params(params, d), st.s);
+        host_trace_dump();
         fill(r, d, out);
     });
 }
@@ -214,6 +255,7 @@ int tcb_compress_device(const void* device_bytes, uint64_t nbytes, int dtype, co
         std::vector<u64> sh(shape, shape + d);
         Stream st;
         const Result r = compress_device(device_bytes, nbytes, dtype, sh, to_params(params, d), st.s);
+        host_trace_dump();
         fill(r, d, out);
     });
 }

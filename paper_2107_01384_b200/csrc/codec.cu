@@ -255,22 +255,36 @@ __global__ void stats_serial_kernel(const u64* __restrict__ m, u64 n, u64 block,
 
 // One warp per (cum, need) pair: lanes classify 32 positions at a time and
 // the warp replays the serial accumulation over them in position order.
-__global__ void crossing_kernel(const u64* __restrict__ m, u64 lo, u64 hi, int p, int category,
-                                const double* __restrict__ cum0, const double* __restrict__ need, int npairs,
-                                u64* __restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const int k = threadIdx.x >> 5;
-    if (k >= npairs) return;
-    double cum = cum0[k];
-    const double nd = need[k];
+// Serial replay of the reference's running sum over one block (the stop
+// placement of core_codec.cpp:270-320): the CTA classifies a chunk of
+// elements and computes their gains in parallel into shared memory, then one
+// thread per pair (interval endpoint) runs the dependent __dadd_rn chain out
+// of shared memory -- the loads do not depend on the chain, so each element
+// costs about one add latency.  Elements are counted up to and including the
+// one whose gain makes the sum reach `need`.
+constexpr int kCrossThreads = 256, kCrossChunk = 4096;
+__global__ void __launch_bounds__(kCrossThreads) crossing_kernel(const u64* __restrict__ m, u64 lo, u64 hi, int p,
+                                                                int category, const double* __restrict__ cum0,
+                                                                const double* __restrict__ need, int npairs,
+                                                                u64* __restrict__ out) {
+    __shared__ double tg[kCrossChunk];
+    __shared__ unsigned char kd[kCrossChunk];  // 0 skip, 1 counted without term, 2 with term; 3 trailing (cat 2)
+    __shared__ int live_s;
+    const int k = threadIdx.x;  // serial-chain owner for pair k (threads < npairs)
+    double cum = k < npairs ? cum0[k] : 0.0;
+    const double nd = k < npairs ? need[k] : 0.0;
     u64 c = 0, nl = 0, nt = 0;
-    for (u64 base = lo; base < hi && cum < nd; base += 32) {
-        const u64 i = base + lane;
-        int kind = 0;  // 0 skip, 1 counted without term, 2 counted with term; category 2: 3 trailing
-        double t = 0.0;
-        if (i < hi) {
-            const u64 v = m[i];
+    bool going = k < npairs && cum < nd;
+    for (u64 base = lo; base < hi; base += kCrossChunk) {
+        if (threadIdx.x == 0) live_s = 0;
+        __syncthreads();
+        if (going) atomicOr(&live_s, 1);
+        const int cnt = static_cast<int>(hi - base < kCrossChunk ? hi - base : kCrossChunk);
+        for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+            const u64 v = m[base + q];
             const int tb = top_bit(v);
+            int kind = 0;
+            double t = 0.0;
             if (category == 0) {
                 if (tb <= p) {
                     kind = tb == p ? 2 : 1;
@@ -281,31 +295,47 @@ __global__ void crossing_kernel(const u64* __restrict__ m, u64 lo, u64 hi, int p
                     kind = 2;
                     t = trail_gain(v, p);
                 }
+            } else if (tb > p) {
+                kind = 3;
+                t = trail_gain(v, p);
             } else {
-                if (tb > p) {
-                    kind = 3;
-                    t = trail_gain(v, p);
-                } else {
-                    kind = tb == p ? 2 : 1;
-                    if (tb == p) t = lead_gain(v, p);
+                kind = tb == p ? 2 : 1;
+                if (tb == p) t = lead_gain(v, p);
+            }
+            kd[q] = static_cast<unsigned char>(kind);
+            tg[q] = t;
+        }
+        __syncthreads();
+        if (!live_s) break;
+        if (going) {
+            // 8 elements per step: their kinds and gains are loaded into registers
+            // first, so the serial chain runs on registers, not on load latency
+            for (int q0 = 0; q0 < cnt && going; q0 += 8) {
+                int kk[8];
+                double tt[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    kk[u] = q0 + u < cnt ? kd[q0 + u] : 0;
+                    tt[u] = q0 + u < cnt ? tg[q0 + u] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int kq = kk[u];
+                    if (!going || kq == 0) continue;
+                    if (kq >= 2) cum = __dadd_rn(cum, tt[u]);
+                    if (category == 2) {
+                        if (kq == 3) ++nt;
+                        else ++nl;
+                    } else {
+                        ++c;
+                    }
+                    if (!(cum < nd)) going = false;
                 }
             }
         }
-        const int cnt = static_cast<int>(hi - base < 32 ? hi - base : 32);
-        for (int q = 0; q < cnt && cum < nd; ++q) {
-            const int kq = __shfl_sync(0xffffffffu, kind, q);
-            const double tq = __shfl_sync(0xffffffffu, t, q);
-            if (kq == 0) continue;
-            if (kq >= 2) cum = __dadd_rn(cum, tq);
-            if (category == 2) {
-                if (kq == 3) ++nt;
-                else ++nl;
-            } else {
-                ++c;
-            }
-        }
+        __syncthreads();  // the chunk buffer is refilled next iteration
     }
-    if (lane == 0) {
+    if (k < npairs) {
         if (category == 2) {
             out[2 * k] = nl;
             out[2 * k + 1] = nt;
@@ -924,7 +954,8 @@ void crossing_scan(const u64* m, u64 n, u64 block, u64 b, int plane, int categor
     c.upload(cum, npairs);
     nd.upload(need, npairs);
     const u64 lo = b * block, hi = std::min<u64>(n, lo + block);
-    crossing_kernel<<<1, 32 * npairs, 0, s>>>(m, lo, hi, plane, category, c.p, nd.p, npairs, out.p);
+    if (npairs > kCrossThreads) throw Error("crossing scan: too many pairs");
+    crossing_kernel<<<1, kCrossThreads, 0, s>>>(m, lo, hi, plane, category, c.p, nd.p, npairs, out.p);
     count_launch();
     TCB_LAUNCH();
     out.download(counts_host, 2 * npairs);

@@ -98,6 +98,16 @@ bool prof_enabled();
 // Optional per-stage device timing (CUDA events on the launching stream),
 // enabled by tcb_prof_enable(); read back with tcb_prof_read().
 enum Cat : int { kIngest = 0, kPermute, kGram, kEig, kTtm, kQuant, kStats, kEmit, kAc, kFactor, kSum, kNumCat };
+
+// Opt-in host wall-clock trace (TCB_TRACE=1): per-label totals printed to
+// stderr by tcb_compress / tcb_compress_device; a debugging aid only.
+struct HostTrace {
+    explicit HostTrace(const char* label);
+    ~HostTrace();
+    const char* label;
+    long long t0 = 0;
+};
+void host_trace_dump();
 struct ProfScope {
     ProfScope(Cat c, cudaStream_t s);
     ~ProfScope();

@@ -81,6 +81,7 @@ struct Planner {
         if (p > batch_hi || p < batch_lo) {
             const int lo = std::max(floor_p, p - 7);
             batch.resize(nb * (p - lo + 1));
+            HostTrace ht("plan: plane_stats batch");
             plane_stats(m, n, block, p, lo, batch.data(), s);
             batch_hi = p;
             batch_lo = lo;
@@ -95,6 +96,7 @@ struct Planner {
         const double c[2] = {cum.lo, cum.hi};
         const double nd[2] = {need.hi, need.lo};
         u64 out[4];
+        HostTrace ht("plan: crossing_scan");
         crossing_scan(m, n, block, b, p, cat, c, nd, 2, out, s);
         if (out[0] != out[2] || out[1] != out[3]) throw Ambiguous{};
         if (second) *second = out[1];
@@ -159,6 +161,7 @@ struct Planner {
         auto finish = [&](int lp) {
             pr.last_plane = lp;
             if (n > 0) {
+                HostTrace ht("plan: decode_model");
                 DevBuf<u64> ds(2 * nb, s);
                 ds.upload(pr.stops.data(), 2 * nb);
                 decode_model(m, n, block, lp, ds.p, dec, s);
@@ -173,6 +176,7 @@ struct Planner {
             for (auto& v : pr.stops) v = kFull;
             return finish(fp);
         }
+        HostTrace ht0("plan: initial sum");
         Iv tracked = exact ? pt(device_sum_serial(SumKind::sq_backward, m, nullptr, n, 0, s))
                            : from_sum(device_sum(SumKind::sq_backward, m, nullptr, n, 0, s), false);
         Iv ref = tracked;
@@ -196,6 +200,7 @@ struct Planner {
             if (le(sub(tracked, red), tgt)) {
                 u64 ebits = 0;
                 if (o.split && have_prev) {
+                    HostTrace ht("plan: split probe emit");
                     const auto er = emit_planes(m, nullptr, n, block, p + 1, p + 1, nullptr, o.coder, false, s);
                     for (u64 e : er.entropy_bytes) ebits += e * 8;
                 }
@@ -212,6 +217,7 @@ struct Planner {
             else if (c * ref.hi <= 0.1 * tracked.lo) due = false;
             else throw Ambiguous{};
             if (due) {
+                HostTrace ht("plan: recalibration sum");
                 tracked = exact ? pt(device_sum_serial(SumKind::recal_backward, m, nullptr, n, p, s))
                                 : from_sum(device_sum(SumKind::recal_backward, m, nullptr, n, p, s), false);
                 ref = tracked;
@@ -262,6 +268,7 @@ std::vector<u8> finalize_stream(const u64* m, const u8* neg, u64 n, const PlanRe
     }
     put_le(o, static_cast<u64>(pl.nplanes), 4);
     if (pl.nplanes > 0 && nb > 0) {
+        HostTrace ht("finalize: emit_planes");
         const auto er = emit_planes(m, neg, n, pl.block, pl.last_plane, 63, pl.stops.data(), coder, true, s);
         o.insert(o.end(), er.body.begin(), er.body.end());
     }

@@ -380,6 +380,7 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
         for (auto v : cur) tot *= v;
         const u64 rows = cur[0], cols = tot / rows;
         const double budget = remaining / static_cast<double>(d - step);
+        HostTrace ht("sthosvd: mode step");
         StepOut so = mode_step(xp, rows, cols, budget, backend, s);
         remaining = std::max(0.0, remaining - so.discarded);
         f.trunc[p[step]] = so.discarded;
@@ -396,10 +397,30 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
     return f;
 }
 
+FactorPrep factor_prepare(const double* U, u64 n, u64 r, const std::vector<u8>& dead, bool f32, cudaStream_t s) {
+    FactorPrep pp;
+    for (u64 j = 0; j < r; ++j)
+        if (!dead[j]) pp.live.push_back(j);
+    const u64 rl = pp.live.size();
+    try {
+        if (rl == 0) return pp;
+        if (rl > n) throw Error("factorize: more columns than rows");
+        if (orth_deviation(U, n, r, pp.live, f32, s) > 1e-8)
+            throw Error("factorize: input columns are not orthonormal");
+        pp.V = DevBuf<double>(n * rl, s);
+        pp.fl.resize(rl);
+        householder(U, n, r, pp.live, pp.V.p, pp.fl.data(), s);
+    } catch (...) {
+        pp.err = std::current_exception();
+    }
+    return pp;
+}
+
 FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<u8>& dead,
                                const std::vector<double>& sn, int coder, bool simple, int core_step_log2,
                                double cap, bool f32, cudaStream_t s,
-                               const std::function<void(const std::vector<signed char>&)>& on_flips) {
+                               const std::function<void(const std::vector<signed char>&)>& on_flips,
+                               FactorPrep* prep) {
     if (dead.size() != r || sn.size() != r) throw Error("factor encode: column metadata mismatch");
     FactorEnc out;
     out.dead = dead;
@@ -418,11 +439,16 @@ FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<
         out.stream = empty_stream_section(0, 0);
         return out;
     }
-    if (rl > n) throw Error("factorize: more columns than rows");
-    if (orth_deviation(U, n, r, live, f32, s) > 1e-8) throw Error("factorize: input columns are not orthonormal");
-    DevBuf<double> V(n * rl, s);
-    std::vector<signed char> fl(rl);
-    householder(U, n, r, live, V.p, fl.data(), s);
+    // the orthonormality check + reflectors (factor_codec.cpp:29-31, 153-200), reused
+    // from a speculative preparation when it was made for the same live columns
+    FactorPrep own;
+    if (!prep || prep->live != live) {
+        own = factor_prepare(U, n, r, dead, f32, s);
+        prep = &own;
+    }
+    if (prep->err) std::rethrow_exception(prep->err);
+    DevBuf<double>& V = prep->V;
+    const std::vector<signed char>& fl = prep->fl;
     for (u64 j = 0; j < rl; ++j) out.flips[live[j]] = fl[j];
     if (on_flips) on_flips(out.flips);
     std::vector<double> sc(rl);
@@ -567,47 +593,37 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
         }
     }
 
-    // phase 3: plan the core bit placement
+    // phases 3-4: the core plan on `s`; meanwhile every factor's orthonormality
+    // check + reflectors run speculatively on a worker stream (assuming no dead
+    // columns, redone for the real live set if the plan kills some); then each
+    // factor's plane search and stream finalisation, its column sign flips
+    // published as soon as they are final so that the core's sign fold and
+    // finalisation overlap the factors.  Sequential while per-stage profiling is on.
     t0 = Clock::now();
     EncodeOpts eo;
     eo.coder = prm.coder;
     eo.block = block;
     eo.split = prm.split;
     DevBuf<u64> dec(nc, s);
-    const PlanResult plan = plan_stream(mag.p, nc, std::ldexp(core_target, 2 * k), eo, dec.p, s);
-    res.core_last_plane = plan.last_plane;
-    res.uncertified += plan.fallbacks;
-    res.times.core = ms_since(t0);
-    const auto dead_flat = dead_slices(dec.p, cs, s);
-    std::vector<std::vector<u8>> dead_mode(d);
-    {
-        u64 o = 0;
-        for (std::size_t ax = 0; ax < d; ++ax) {
-            dead_mode[mode_of[ax]].assign(dead_flat.begin() + o, dead_flat.begin() + o + cs[ax]);
-            o += cs[ax];
-        }
-    }
-
-    // phase 4: factors, concurrently on worker streams (each factor's plane
-    // search and stream finalisation is a chain of small launches and host
-    // decisions); the core's sign fold and finalisation run on `s` as soon as
-    // every factor has published its column sign flips.  Sequential while
-    // per-stage profiling is on.
-    t0 = Clock::now();
-    const int core_step = plan.last_plane - k;
     const double cap = 0.02 * target / static_cast<double>(d);
     std::vector<FactorEnc> fe(d);
     res.factor_terms.assign(d, 0.0);
     std::vector<std::vector<signed char>> flips_of(d);
-    auto run_factor = [&](std::size_t i, cudaStream_t si,
-                          const std::function<void(const std::vector<signed char>&)>& cb) {
-        fe[i] = encode_factor_device(f.factors[i].p, f.n[i], f.r[i], dead_mode[i], sn_mode[i], prm.coder, prm.simple,
-                                     core_step, cap, prm.f32, si, cb);
-    };
+    std::vector<std::vector<u8>> dead_mode(d);
+    int core_step = 0;
     const bool par = d > 1 && !prof_enabled();
+    std::promise<void> plan_ready;
+    std::shared_future<void> plan_fut = plan_ready.get_future().share();
     std::vector<std::promise<void>> flips_ready(d);
     std::vector<std::future<void>> flips_fut, done;
     JoinAll join{done};
+    struct PlanGuard {  // a throwing plan must still release the workers
+        std::promise<void>& p;
+        bool set = false;
+        ~PlanGuard() {
+            if (!set) p.set_exception(std::make_exception_ptr(Error("compress: core plan failed")));
+        }
+    } plan_guard{plan_ready};
     if (par) {
         int dev = 0;
         TCB_CUDA(cudaGetDevice(&dev));
@@ -622,21 +638,57 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
                 bool sent = false;
                 try {
                     TCB_CUDA(cudaSetDevice(dev));
-                    run_factor(i, si, [&](const std::vector<signed char>& fl) {
-                        flips_of[i] = fl;
-                        sent = true;
-                        flips_ready[i].set_value();
-                    });
+                    FactorPrep prep = factor_prepare(f.factors[i].p, f.n[i], f.r[i], std::vector<u8>(f.r[i], 0),
+                                                     prm.f32, si);
+                    plan_fut.get();
+                    fe[i] = encode_factor_device(
+                        f.factors[i].p, f.n[i], f.r[i], dead_mode[i], sn_mode[i], prm.coder, prm.simple, core_step,
+                        cap, prm.f32, si,
+                        [&](const std::vector<signed char>& fl) {
+                            flips_of[i] = fl;
+                            sent = true;
+                            flips_ready[i].set_value();
+                        },
+                        &prep);
                 } catch (...) {
                     if (!sent) flips_ready[i].set_exception(std::current_exception());
                     throw;
                 }
             }));
         }
+    }
+    PlanResult plan;
+    {
+        HostTrace ht("encode: core plan");
+        plan = plan_stream(mag.p, nc, std::ldexp(core_target, 2 * k), eo, dec.p, s);
+    }
+    res.core_last_plane = plan.last_plane;
+    res.uncertified += plan.fallbacks;
+    res.times.core = ms_since(t0);
+    std::vector<u8> dead_flat;
+    {
+        HostTrace ht("encode: dead slices");
+        dead_flat = dead_slices(dec.p, cs, s);
+    }
+    {
+        u64 o = 0;
+        for (std::size_t ax = 0; ax < d; ++ax) {
+            dead_mode[mode_of[ax]].assign(dead_flat.begin() + o, dead_flat.begin() + o + cs[ax]);
+            o += cs[ax];
+        }
+    }
+    core_step = plan.last_plane - k;
+    plan_guard.set = true;
+    plan_ready.set_value();
+    t0 = Clock::now();
+    if (par) {
+        HostTrace ht("encode: wait factor flips");
         for (auto& fu : flips_fut) fu.get();  // rethrows a factor's early error (join waits for the rest)
     } else {
         for (std::size_t i = 0; i < d; ++i)
-            run_factor(i, s, [&](const std::vector<signed char>& fl) { flips_of[i] = fl; });
+            fe[i] = encode_factor_device(f.factors[i].p, f.n[i], f.r[i], dead_mode[i], sn_mode[i], prm.coder,
+                                         prm.simple, core_step, cap, prm.f32, s,
+                                         [&](const std::vector<signed char>& fl) { flips_of[i] = fl; });
     }
 
     // sign fold + finalize (pipeline.cpp:161-176)
@@ -647,10 +699,18 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     sign_fold(neg.p, cs, flips_axis, s);
     u64 count = 1;
     for (auto v : f.r) count *= v;
-    const auto core_stream = finalize_stream(mag.p, neg.p, nc, plan, prm.coder, count, s);
-    const SumRec ach = device_sum(SumKind::diff_backward, mag.p, dec.p, nc, 0, s);
+    std::vector<u8> core_stream;
+    SumRec ach;
+    {
+        HostTrace ht("encode: core finalize+sum");
+        core_stream = finalize_stream(mag.p, neg.p, nc, plan, prm.coder, count, s);
+        ach = device_sum(SumKind::diff_backward, mag.p, dec.p, nc, 0, s);
+    }
     res.times.core += ms_since(t1);
-    for (auto& fu : done) fu.get();
+    {
+        HostTrace ht("encode: wait factors");
+        for (auto& fu : done) fu.get();
+    }
     for (std::size_t i = 0; i < d; ++i) res.factor_terms[i] = fe[i].term;
     res.times.factor = ms_since(t0);
     res.core_quant = std::ldexp(ach.hi + ach.lo, -2 * k);

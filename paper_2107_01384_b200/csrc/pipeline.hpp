@@ -2,6 +2,7 @@
 #pragma once
 
 #include <array>
+#include <exception>
 #include <functional>
 #include <optional>
 
@@ -86,12 +87,24 @@ struct FactorEnc {
 // the sharded multi-GPU mode loop, whose rank 0 encodes the gathered core).
 Result encode_tucker_device(Tucker& f, int dtype, double norm_sq, double target, const Params& p, cudaStream_t s);
 
+// The orthonormality check and Householder reflectors of a factor's live
+// columns (factor_codec.cpp:29-31,153-200); an error is captured in `err` and
+// rethrown when the factor is actually encoded.
+struct FactorPrep {
+    std::vector<u64> live;
+    DevBuf<double> V;               // n x live reflectors
+    std::vector<signed char> fl;    // per live column
+    std::exception_ptr err;
+};
+FactorPrep factor_prepare(const double* U, u64 n, u64 r, const std::vector<u8>& dead, bool f32, cudaStream_t s);
 // on_flips (optional) receives the column sign flips as soon as they are known,
-// before the plane search and stream finalisation.
+// before the plane search and stream finalisation; `prep` (optional) is reused
+// when it was made for the same live columns.
 FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<u8>& dead,
                                const std::vector<double>& sn, int coder, bool simple, int core_step_log2,
                                double cap, bool f32, cudaStream_t s,
-                               const std::function<void(const std::vector<signed char>&)>& on_flips = {});
+                               const std::function<void(const std::vector<signed char>&)>& on_flips = {},
+                               FactorPrep* prep = nullptr);
 
 std::vector<double> alpha_weights(const std::vector<double>& sn, u64 n);
 std::vector<u64> stable_ascending(const std::vector<u64>& s);
