@@ -160,5 +160,26 @@ inline CompressResult compress(const container::SourceBuffer& src, const Params&
     return detail::from_c(r);
 }
 
+struct DecompressResult {  // reference pipeline.hpp:59-64
+    std::vector<std::uint8_t> bytes;
+    container::Dtype dtype = container::Dtype::float64;
+    Shape shape;
+    double total_ms = 0;
+};
+
+// pipeline::decompress (reference pipeline.cpp:266-283) on the B200.
+inline DecompressResult decompress(std::span<const std::uint8_t> container_bytes, int threads) {
+    tcb_decompress_result r;
+    if (tcb_decompress(container_bytes.data(), container_bytes.size(), threads, &r) != 0)
+        throw Error(tcb_last_error());
+    DecompressResult o;
+    o.bytes.assign(r.bytes, r.bytes + r.nbytes);
+    tcb_free(r.bytes);
+    o.dtype = static_cast<container::Dtype>(r.dtype);
+    o.shape.assign(r.shape, r.shape + r.d);
+    o.total_ms = r.total_ms;
+    return o;
+}
+
 }  // namespace pipeline
 }  // namespace tucomp

@@ -80,6 +80,24 @@ int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_
 int tcb_compress_device(const void* device_bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d,
                         const tcb_params* params, tcb_result* out);
 
+/* pipeline::DecompressResult (pipeline.hpp:59-64) */
+typedef struct tcb_decompress_result {
+    uint8_t* bytes;              /* source-dtype bytes, owned by the library: release with tcb_free */
+    uint64_t nbytes;
+    int dtype;                   /* container::Dtype of the source */
+    int d;
+    uint64_t shape[8];
+    double total_ms;
+} tcb_decompress_result;
+
+/* pipeline::decompress(container_bytes, threads) (pipeline.hpp:66, pipeline.cpp:266-283):
+ * decode, reconstruct and emit in the source dtype (container.cpp:98-140). */
+int tcb_decompress(const uint8_t* container, uint64_t len, int threads, tcb_decompress_result* out);
+/* pipeline::decompress_tensor<double> (pipeline.hpp:70-71): the reconstructed tensor in
+ * fp64, row-major, original axis order; *out is released with tcb_free; shape has room for 8. */
+int tcb_decompress_tensor_f64(const uint8_t* container, uint64_t len, double** out, uint64_t* count,
+                              uint64_t* shape, int* d);
+
 void tcb_free(void* p);
 const char* tcb_last_error(void);
 uint64_t tcb_kernel_launches(void);

@@ -251,6 +251,49 @@ def compress_device(ptr: int, nbytes: int, dtype: Dtype, shape: Sequence[int], p
     return _result(res)
 
 
+class _CDecompress(C.Structure):  # tcb_decompress_result
+    _fields_ = [("bytes", C.POINTER(C.c_uint8)), ("nbytes", C.c_uint64), ("dtype", C.c_int), ("d", C.c_int),
+                ("shape", C.c_uint64 * 8), ("total_ms", C.c_double)]
+
+
+@dataclass
+class DecompressResult:  # pipeline::DecompressResult (pipeline.hpp:59-64)
+    bytes: bytes
+    dtype: Dtype
+    shape: tuple
+    total_ms: float
+
+    def to_array(self) -> np.ndarray:
+        dt = {Dtype.int8: np.int8, Dtype.uint8: np.uint8, Dtype.int16: np.int16, Dtype.uint16: np.uint16,
+              Dtype.int32: np.int32, Dtype.uint32: np.uint32, Dtype.int64: np.int64, Dtype.uint64: np.uint64,
+              Dtype.float32: np.float32, Dtype.float64: np.float64}[self.dtype]
+        return np.frombuffer(self.bytes, dt).reshape(self.shape)
+
+
+def decompress(container: bytes, threads: int = 1) -> DecompressResult:
+    """tucomp::pipeline::decompress (pipeline.cpp:266-283) on the B200: decode,
+    reconstruct and emit the source dtype's bytes (container.cpp:98-140)."""
+    buf = np.frombuffer(container, np.uint8) if len(container) else np.zeros(1, np.uint8)
+    r = _CDecompress()
+    _check(lib().tcb_decompress(_p(buf), C.c_uint64(len(container)), int(threads), C.byref(r)))
+    data = _take_bytes(r.bytes, r.nbytes)
+    return DecompressResult(data, Dtype(r.dtype), tuple(int(r.shape[i]) for i in range(r.d)), float(r.total_ms))
+
+
+def decompress_tensor(container: bytes) -> np.ndarray:
+    """tucomp::pipeline::decompress_tensor<double> (pipeline.hpp:70-71) on the B200."""
+    buf = np.frombuffer(container, np.uint8) if len(container) else np.zeros(1, np.uint8)
+    ptr = C.POINTER(C.c_double)()
+    cnt, d = C.c_uint64(), C.c_int()
+    shape = (C.c_uint64 * 8)()
+    _check(lib().tcb_decompress_tensor_f64(_p(buf), C.c_uint64(len(container)), C.byref(ptr), C.byref(cnt), shape,
+                                           C.byref(d)))
+    n = int(cnt.value)
+    out = np.ctypeslib.as_array(ptr, shape=(n,)).copy() if n else np.zeros(0)
+    lib().tcb_free(C.cast(ptr, C.c_void_p))
+    return out.reshape(tuple(int(shape[i]) for i in range(d.value)))
+
+
 # ---------------------------------------------------------------- lower-level ops
 def sthosvd(a: np.ndarray, sse_target: float, order=None, backend=0) -> dict:
     """sthosvd::compress<double> (sthosvd.hpp:66-68) on the device."""
@@ -363,6 +406,7 @@ def encode_factor(u, dead, slice_norms, coder=0, simple=False, core_step_log2=0,
                 plane=plane.value)
 
 
-EXPORTED = ("tcb_compress", "tcb_compress_device", "tcb_default_params", "tcb_free", "tcb_last_error",
+EXPORTED = ("tcb_compress", "tcb_compress_device", "tcb_decompress", "tcb_decompress_tensor_f64",
+            "tcb_default_params", "tcb_free", "tcb_last_error",
             "tcb_kernel_launches", "tcb_sthosvd_f64", "tcb_gram_f64", "tcb_ttm_f64", "tcb_eig_f64",
             "tcb_quantize_f64", "tcb_encode", "tcb_encode_symbols", "tcb_encode_factor_f64")

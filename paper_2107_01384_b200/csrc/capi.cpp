@@ -12,6 +12,7 @@
 #include "../../include/tucomp_b200.h"
 #include "codec.cuh"
 #include "kernels.cuh"
+#include "decompress.hpp"
 #include "pipeline.hpp"
 #include "quant.cuh"
 
@@ -257,6 +258,39 @@ int tcb_compress_device(const void* device_bytes, uint64_t nbytes, int dtype, co
         const Result r = compress_device(device_bytes, nbytes, dtype, sh, to_params(params, d), st.s);
         host_trace_dump();
         fill(r, d, out);
+    });
+}
+
+int tcb_decompress(const uint8_t* container, uint64_t len, int threads, tcb_decompress_result* out) {
+    (void)threads;  // the device path has no host worker count
+    return guard([&] {
+        Stream st;
+        const auto t = decompress_device(container, len, st.s);
+        const auto bytes = emit_bytes(t, st.s);
+        host_trace_dump();
+        out->bytes = dup(bytes);
+        out->nbytes = bytes.size();
+        out->dtype = t.dtype;
+        out->d = static_cast<int>(t.shape.size());
+        for (std::size_t i = 0; i < t.shape.size() && i < 8; ++i) out->shape[i] = t.shape[i];
+        out->total_ms = t.ms;
+    });
+}
+
+int tcb_decompress_tensor_f64(const uint8_t* container, uint64_t len, double** out, uint64_t* count,
+                              uint64_t* shape, int* d) {
+    return guard([&] {
+        Stream st;
+        const auto t = decompress_device(container, len, st.s);
+        u64 total = 1;
+        for (auto v : t.shape) total *= v;
+        std::vector<double> h(total);
+        if (total) t.x.download(h.data(), total);
+        TCB_CUDA(cudaStreamSynchronize(st.s));
+        *out = dup(h);
+        *count = total;
+        *d = static_cast<int>(t.shape.size());
+        for (std::size_t i = 0; i < t.shape.size() && i < 8; ++i) shape[i] = t.shape[i];
     });
 }
 

@@ -207,6 +207,49 @@ __global__ void __launch_bounds__(256) expand_residual(const double* __restrict_
     if (lane == 0) res[static_cast<u64>(blockIdx.y) * rl + c] = s;
 }
 
+// Decoder side (factor_codec.cpp:246-264): X(:, c) = H_0 ... H_{rl-1} e_c written
+// to U(:, live_c) (row-major n x r).  Same warp-per-column expansion as above.
+template <int NQ>
+__global__ void __launch_bounds__(256) expand_columns(const double* __restrict__ V, u64 n, u64 rl,
+                                                      const u64* __restrict__ live, double* __restrict__ U, u64 r) {
+    extern __shared__ double sv[];
+    const int lane = threadIdx.x & 31;
+    const u64 c = static_cast<u64>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const bool active = c < rl;
+    double x[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) x[q] = (static_cast<u64>(lane + 32 * q) == c) ? 1.0 : 0.0;
+    for (long long hi = static_cast<long long>(rl) - 1; hi >= 0; hi -= kExChunk) {
+        const long long lo = hi - kExChunk + 1 < 0 ? 0 : hi - kExChunk + 1;
+        __syncthreads();
+        for (long long jj = lo; jj <= hi; ++jj)
+            for (u64 i = threadIdx.x; i < n; i += blockDim.x) sv[(jj - lo) * n + i] = V[jj * n + i];
+        __syncthreads();
+        if (!active) continue;
+        for (long long jj = hi; jj >= lo; --jj) {
+            const double* v = sv + (jj - lo) * n;
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const u64 i = lane + 32 * q;
+                if (i >= static_cast<u64>(jj) && i < n) t += v[i] * x[q];
+            }
+            t = warp_sum(t);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const u64 i = lane + 32 * q;
+                if (i >= static_cast<u64>(jj) && i < n) x[q] -= 2.0 * t * v[i];
+            }
+        }
+    }
+    if (!active) return;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const u64 i = lane + 32 * q;
+        if (i < n) U[i * r + live[c]] = x[q];
+    }
+}
+
 }  // namespace
 
 double orth_deviation(const double* U, u64 n, u64 r, const std::vector<u64>& live, bool as_float, cudaStream_t s) {
@@ -301,6 +344,47 @@ std::vector<double> factor_residuals(const u64* mag, const u8* neg, int k, u64 n
     auto h = res.to_host();
     if (e) throw Error("reconstruct: reflector sub-diagonal norm reaches 1");
     return h;
+}
+
+}  // namespace tcb
+
+namespace tcb {
+
+void factor_expand(const u64* mag, const u8* neg, int k, u64 n, u64 r, const std::vector<u64>& live,
+                   const double* scales_dev, double* U, cudaStream_t s) {
+    ProfScope prof_scope(kFactor, s);
+    TCB_CUDA(cudaMemsetAsync(U, 0, n * r * sizeof(double), s));
+    const u64 rl = live.size();
+    if (rl == 0) return;
+    if (n > 1024) throw Error("factor codec: mode sizes above 1024 unsupported on the device path");
+    DevBuf<u64> dl(rl, s);
+    dl.upload(live.data(), rl);
+    const int zero = 0;
+    DevBuf<int> dp(1, s);
+    dp.upload(&zero, 1);
+    DevBuf<double> Vd(n * rl, s);
+    DevBuf<int> err(1, s);
+    err.zero();
+    refl_from_stream<<<dim3(cdiv(rl, 4), 1), 128, 0, s>>>(mag, neg, k, n, rl, dp.p, scales_dev, Vd.p, err.p);
+    const size_t smem = static_cast<size_t>(kExChunk) * n * sizeof(double);
+    static bool attr = [] {
+        const int mx = kExChunk * 1024 * sizeof(double);
+        cudaFuncSetAttribute(expand_columns<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(expand_columns<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(expand_columns<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        return true;
+    }();
+    (void)attr;
+    const unsigned grid = cdiv(rl, 8);
+    if (n <= 256) expand_columns<8><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);
+    else if (n <= 512) expand_columns<16><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);
+    else expand_columns<32><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);
+    count_launch(2);
+    TCB_LAUNCH();
+    int e = 0;
+    err.download(&e, 1);
+    TCB_CUDA(cudaStreamSynchronize(s));
+    if (e) throw Error("reconstruct: reflector sub-diagonal norm reaches 1");
 }
 
 }  // namespace tcb

@@ -25,5 +25,9 @@ void reflector_stream(const double* V, u64 n, u64 rl, const double* scales_dev, 
 std::vector<double> factor_residuals(const u64* mag, const u8* neg, int k, u64 n, u64 r,
                                      const std::vector<u64>& live, const double* scales_dev, const double* U,
                                      const signed char* flips_dev, const std::vector<int>& planes, cudaStream_t s);
+// Decoder: decoded reflector stream (mag, neg, k; column scales) -> U (row-major
+// n x r; dead columns zero) by the Householder expansion (factor_codec.cpp:246-264)
+void factor_expand(const u64* mag, const u8* neg, int k, u64 n, u64 r, const std::vector<u64>& live,
+                   const double* scales_dev, double* U, cudaStream_t s);
 
 }  // namespace tcb
