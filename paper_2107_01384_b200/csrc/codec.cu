@@ -864,6 +864,167 @@ void run_ac(const u64* syms, const StreamOut* so, const AcDesc* dad, const std::
     TCB_LAUNCH();
 }
 
+// ---------------------------------------------------------------- semi-static rANS (entropy.cpp:290-421)
+// One warp per stream, lane 0: histogram through an open-addressing hash
+// (first-occurrence indices), the distinct symbols heap-sorted by value, the
+// reference's table normalisation (floor-scaled counts, then +-1 on the first
+// largest count until the total is 2^bits, bits = max(12, ceil log2 distinct)),
+// then the backwards encode; output framing as the range coder's (coder id 1,
+// u32 count, varint table, 8-byte state, 32-bit words in reverse).
+__host__ __device__ inline u64 rans_scratch_words(u64 nsyms) {
+    const u64 cap = nsyms + 1;
+    const u64 hs = u64{1} << log2_at_least(static_cast<u32>(2 * cap));
+    return 2 * cap /*val*/ + 2 * cap /*cnt*/ + hs /*hash*/ + 4 * cap /*order,f,pos,c*/ + 4 + (nsyms + 4) /*words*/ + 2;
+}
+__host__ __device__ inline u64 rans_out_cap(u64 nsyms) { return 24 * nsyms + 64; }
+
+__global__ void __launch_bounds__(32) rans_kernel(const u64* __restrict__ syms, const StreamOut* __restrict__ sout,
+                                                  const AcDesc* __restrict__ desc, int nstreams, u8* __restrict__ outbuf,
+                                                  u32* __restrict__ scratch, u64* __restrict__ elen) {
+    const int sidx = static_cast<int>(blockIdx.x);
+    if (sidx >= nstreams || threadIdx.x != 0) return;
+    const u64 N = sout[sidx].nsyms;
+    if (N == 0) {
+        elen[sidx] = 0;
+        return;
+    }
+    const AcDesc d = desc[sidx];
+    const u64* sy = syms + d.sym_off;
+    u8* out = outbuf + d.out_off;
+    const u64 cap = N + 1;
+    const u32 hb = log2_at_least(static_cast<u32>(2 * cap));
+    const u32 hmask = (1u << hb) - 1;
+    u32* base = scratch + d.model_off;  // 8-byte aligned by the host
+    u64* val = reinterpret_cast<u64*>(base);
+    u64* cnt = val + cap;
+    u32* hidx = reinterpret_cast<u32*>(cnt + cap);
+    u32* order = hidx + (1u << hb);
+    u32* f = order + cap;
+    u32* pos = f + cap;
+    u32* c = pos + cap;
+    u32* words = c + cap + 1;
+    for (u32 i = 0; i <= hmask; ++i) hidx[i] = 0;
+    u32 nd = 0;
+    for (u64 t = 0; t < N; ++t) {  // histogram, first-occurrence indices
+        const u64 s = sy[t];
+        u32 h = hslot(s, hb);
+        while (true) {
+            const u32 e = hidx[h];
+            if (e == 0) {
+                val[nd] = s;
+                cnt[nd] = 1;
+                hidx[h] = ++nd;
+                break;
+            }
+            if (val[e - 1] == s) {
+                ++cnt[e - 1];
+                break;
+            }
+            h = (h + 1) & hmask;
+        }
+    }
+    // heap sort of the distinct indices by value
+    for (u32 i = 0; i < nd; ++i) order[i] = i;
+    auto sift = [&](u32 root, u32 end) {
+        while (2 * root + 1 < end) {
+            u32 ch = 2 * root + 1;
+            if (ch + 1 < end && val[order[ch + 1]] > val[order[ch]]) ++ch;
+            if (val[order[root]] >= val[order[ch]]) return;
+            const u32 tmp = order[root];
+            order[root] = order[ch];
+            order[ch] = tmp;
+            root = ch;
+        }
+    };
+    for (u32 i = nd / 2; i-- > 0;) sift(i, nd);
+    for (u32 end = nd; end-- > 1;) {
+        const u32 tmp = order[0];
+        order[0] = order[end];
+        order[end] = tmp;
+        sift(0, end);
+    }
+    u32 bits = 12;
+    while ((u64{1} << bits) < nd) ++bits;
+    const u64 scale = u64{1} << bits;
+    u64 sum = 0;
+    for (u32 j = 0; j < nd; ++j) {
+        u64 q = cnt[order[j]] * scale / N;
+        if (q == 0) q = 1;
+        f[j] = static_cast<u32>(q);
+        pos[order[j]] = j;
+        sum += q;
+    }
+    while (sum != scale) {
+        const bool grow = sum < scale;
+        u32 pick = 0;
+        for (u32 i = 1; i < nd; ++i) {
+            const bool better = grow ? f[i] > f[pick] : (f[i] > f[pick] && f[i] > 1);
+            if (better) pick = i;
+        }
+        if (grow) {
+            ++f[pick];
+            ++sum;
+        } else {
+            if (f[pick] <= 1) {  // the reference throws "entropy: cannot normalize rans table"
+                elen[sidx] = ~u64{1};
+                return;
+            }
+            --f[pick];
+            --sum;
+        }
+    }
+    c[0] = 0;
+    for (u32 j = 0; j < nd; ++j) c[j + 1] = c[j] + f[j];
+    // header: coder id, u32 count, varint table
+    u64 o = 0;
+    out[o++] = 1;
+    for (int i = 0; i < 4; ++i) out[o++] = static_cast<u8>(static_cast<u32>(N) >> (8 * i));
+    auto varint = [&](u64 v) {
+        for (; v >= 0x80; v >>= 7) out[o++] = static_cast<u8>(v) | 0x80u;
+        out[o++] = static_cast<u8>(v);
+    };
+    varint(nd);
+    varint(bits);
+    u64 prev = 0;
+    for (u32 j = 0; j < nd; ++j) {
+        varint(val[order[j]] - prev);
+        varint(f[j]);
+        prev = val[order[j]];
+    }
+    // backwards encode
+    constexpr u64 L = u64{1} << 31;
+    u64 x = L;
+    u64 nw = 0;
+    for (u64 t = N; t-- > 0;) {
+        const u64 s = sy[t];
+        u32 h = hslot(s, hb);
+        while (val[hidx[h] - 1] != s) h = (h + 1) & hmask;
+        const u32 j = pos[hidx[h] - 1];
+        const u64 fj = f[j];
+        const u64 lim = ((L >> bits) << 32) * fj;
+        while (x >= lim) {
+            words[nw++] = static_cast<u32>(x);
+            x >>= 32;
+        }
+        x = ((x / fj) << bits) + (x % fj) + c[j];
+    }
+    for (int i = 0; i < 8; ++i) out[o++] = static_cast<u8>(x >> (8 * i));
+    for (u64 w = nw; w-- > 0;)
+        for (int b = 0; b < 4; ++b) out[o++] = static_cast<u8>(words[w] >> (8 * b));
+    elen[sidx] = o;
+}
+
+void run_rans(const u64* syms, const StreamOut* so, const AcDesc* dad, int ns, u8* ent, u32* scratch, u64* elen,
+              cudaStream_t s) {
+    if (ns == 0) return;
+    {
+        ProfScope pa(kAc, s);
+        rans_kernel<<<static_cast<unsigned>(ns), 32, 0, s>>>(syms, so, dad, ns, ent, scratch, elen);
+    }
+    count_launch();
+    TCB_LAUNCH();
+}
+
 // ---------------------------------------------------------------- assembly
 __global__ void assemble_kernel(const u8* __restrict__ ent, const AcDesc* __restrict__ acd,
                                 const u64* __restrict__ elen, const u32* __restrict__ raw,
@@ -972,7 +1133,27 @@ void decode_model(const u64* m, u64 n, u64 block, int last_plane, const u64* sto
 }
 
 std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cudaStream_t s) {
-    if (coder != 0) throw Error("core codec: the rANS backend is not available on the device path yet");
+    if (coder != 0 && coder != 1) throw Error("entropy: unknown coder");
+    if (coder == 1 && n > 0) {
+        DevBuf<u64> syms(n, s);
+        syms.upload(syms_host, n);
+        StreamOut so{n, 0};
+        DevBuf<StreamOut> dso(1, s);
+        dso.upload(&so, 1);
+        AcDesc a{};
+        DevBuf<AcDesc> dad(1, s);
+        dad.upload(&a, 1);
+        DevBuf<u8> ent(rans_out_cap(n), s);
+        DevBuf<u32> scratch(rans_scratch_words(n) + 2, s);
+        DevBuf<u64> elen(1, s);
+        run_rans(syms.p, dso.p, dad.p, 1, ent.p, scratch.p, elen.p, s);
+        const u64 el = elen.to_host()[0];
+        if (el == ~u64{1}) throw Error("entropy: cannot normalize rans table");
+        std::vector<u8> out(el);
+        ent.download(out.data(), el);
+        TCB_CUDA(cudaStreamSynchronize(s));
+        return out;
+    }
     std::vector<u8> out{static_cast<u8>(coder)};
     for (int i = 0; i < 4; ++i) out.push_back(static_cast<u8>(static_cast<u32>(n) >> (8 * i)));
     if (n == 0) return out;
@@ -1000,7 +1181,7 @@ std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cu
 EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
                        const u64* stops_host, int coder, bool want_body, cudaStream_t s) {
     EmitResult res;
-    if (coder != 0) throw Error("core codec: the rANS backend is not available on the device path yet");
+    if (coder != 0 && coder != 1) throw Error("entropy: unknown coder");
     const u64 nb = n == 0 ? 0 : (n + block - 1) / block;
     const int np = top_plane - last_plane + 1;
     const u64 ns = nb * static_cast<u64>(np);
@@ -1047,23 +1228,34 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
         a.sym_off = sd[i].sym_off;
         const u64 k = soh[i].nsyms;
         a.out_off = out_total;
-        out_total += k ? 5 + 7 * k + 16 : 0;
         const u32 cap = static_cast<u32>(k + 1);
         a.cap = cap;
         a.fen = 0;
         a.hbits = log2_at_least(2 * cap);
-        a.model_off = scratch_total;
-        if (k) scratch_total += ac_model_words(cap);
+        if (coder == 1) {
+            out_total += k ? rans_out_cap(k) : 0;
+            a.model_off = (scratch_total + 1) & ~u64{1};
+            if (k) scratch_total = a.model_off + rans_scratch_words(k);
+        } else {
+            out_total += k ? 5 + 7 * k + 16 : 0;
+            a.model_off = scratch_total;
+            if (k) scratch_total += ac_model_words(cap);
+        }
     }
     DevBuf<AcDesc> dad(ns, s);
     dad.upload(ad.data(), ns);
     DevBuf<u8> ent(out_total + 1, s);
     DevBuf<u32> scratch(scratch_total + 2, s);
     DevBuf<u64> elen(ns, s);
-    run_ac(syms.p, so.p, dad.p, ad, soh, static_cast<int>(ns), ent.p, scratch.p, elen.p, s);
+    if (coder == 1)
+        run_rans(syms.p, so.p, dad.p, static_cast<int>(ns), ent.p, scratch.p, elen.p, s);
+    else
+        run_ac(syms.p, so.p, dad.p, ad, soh, static_cast<int>(ns), ent.p, scratch.p, elen.p, s);
     std::vector<u64> el(ns);
     elen.download(el.data(), ns);
     TCB_CUDA(cudaStreamSynchronize(s));
+    for (u64 v : el)
+        if (v == ~u64{1}) throw Error("entropy: cannot normalize rans table");
     res.entropy_bytes = el;
     if (!want_body) return res;
     std::vector<u64> off(ns);

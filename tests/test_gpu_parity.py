@@ -108,12 +108,13 @@ def _core_mags(shape=(40, 41, 42), seed=0, decay=6.0):
 
 @pytest.mark.parametrize("frac", [1e-1, 1e-3, 1e-6, 1e-9, 1e-12, 0.0, 2.0])
 @pytest.mark.parametrize("split", [True, False])
-def test_encoder_bitstream_bit_exact(gpu_pkg, frac, split):
+@pytest.mark.parametrize("coder", [0, 1])
+def test_encoder_bitstream_bit_exact(gpu_pkg, frac, split, coder):
     mag, neg = _core_mags()
     tot = float((mag.astype(np.float64) ** 2).sum())
     tgt = tot * frac
-    s_gpu, lp_gpu, ach_gpu, dec_gpu, _ = gpu_pkg.encode(mag, neg, tgt, split=split)
-    s_ref, lp_ref, ach_ref, dec_ref = oracle.encode(mag, neg, tgt, split=split)
+    s_gpu, lp_gpu, ach_gpu, dec_gpu, _ = gpu_pkg.encode(mag, neg, tgt, coder=coder, split=split)
+    s_ref, lp_ref, ach_ref, dec_ref = oracle.encode(mag, neg, tgt, coder=coder, split=split)
     assert lp_gpu == lp_ref
     assert np.array_equal(dec_gpu, dec_ref)
     assert s_gpu == s_ref
@@ -152,8 +153,9 @@ def test_encode_symbols_bit_exact(gpu_pkg, seed):
     rng = np.random.default_rng(seed)
     syms = np.concatenate([rng.geometric(0.05, 3000) - 1, rng.integers(0, 2 ** 32 - 1, 50)]).astype(np.uint64)
     rng.shuffle(syms)
-    assert gpu_pkg.encode_symbols(0, syms) == oracle.encode_symbols(0, syms)
-    assert gpu_pkg.encode_symbols(0, []) == oracle.encode_symbols(0, [])
+    for coder in (0, 1):
+        assert gpu_pkg.encode_symbols(coder, syms) == oracle.encode_symbols(coder, syms)
+        assert gpu_pkg.encode_symbols(coder, []) == oracle.encode_symbols(coder, [])
 
 
 @pytest.mark.parametrize("kind", ["constant", "distinct", "long", "runs"])
@@ -234,6 +236,27 @@ def test_compress_end_to_end(gpu_pkg, kind, shape, dtype, re):
     assert res.estimate.truncation_sse == pytest.approx(ref.truncation_sse, rel=1e-6)
 
 
+@pytest.mark.parametrize("gopts,oopts", [
+    (dict(coder=1), dict(coder=1)),
+    (dict(split_planes=False), dict(split=False)),
+    (dict(simple_factor_weights=True), dict(simple=True)),
+    (dict(coder=1, split_planes=False, block_size=1024), dict(coder=1, split=False, block_size=1024)),
+])
+def test_compress_coding_options_end_to_end(gpu_pkg, gopts, oopts):
+    """Non-default coding options: rANS, non-split planes,
+    simple factor weights, small blocks -- against the oracle."""
+    x = synth.small("sin_decay", (48, 44, 40), seed=8)
+    res = gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(target_re=1e-4, **gopts))
+    ref = oracle.compress(x, target_re=1e-4, **oopts)
+    assert res.ranks == ref.ranks
+    assert abs(len(res.container) - len(ref.container)) <= 0.01 * len(ref.container)
+    y, yr = oracle.decompress(res.container, x.shape), oracle.decompress(ref.container, x.shape)
+    e = np.linalg.norm(y - x) / np.linalg.norm(x)
+    er = np.linalg.norm(yr - x) / np.linalg.norm(x)
+    assert abs(e - er) <= 0.01 * er
+    assert np.max(np.abs(gpu_pkg.decompress_tensor(res.container) - y)) <= 1e-12 * np.max(np.abs(y))
+
+
 def test_container_parses_with_verbatim_reference_reader(gpu_pkg):
     """The GPU container round-trips byte-for-byte through the reference's own
     read_container/write_container (oracle/_ref, compiled verbatim)."""
@@ -295,12 +318,13 @@ def _golden_core(g):
     return rng.standard_normal(shape) * np.exp(-g["decay"] * idx / idx.max())
 
 
-@pytest.mark.parametrize("g", [g for g in _GOLDEN["encode"] if g["coder"] == 0],
-                         ids=lambda g: f"s{g['seed']}-f{g['frac']}-sp{int(g['split'])}-fx{g['fixed']}")
+@pytest.mark.parametrize("g", _GOLDEN["encode"],
+                         ids=lambda g: f"c{g['coder']}-s{g['seed']}-f{g['frac']}-sp{int(g['split'])}-fx{g['fixed']}")
 def test_gpu_encoder_matches_reference_golden(gpu_pkg, g):
     mag, neg, k, zero, sn = gpu_pkg.quantize(_golden_core(g))
     tot = float((mag.astype(np.float64) ** 2).sum())
-    s, lp, ach, dec, _ = gpu_pkg.encode(mag, neg, tot * g["frac"], split=g["split"], fixed_plane=g["fixed"])
+    s, lp, ach, dec, _ = gpu_pkg.encode(mag, neg, tot * g["frac"], coder=g["coder"], split=g["split"],
+                                        fixed_plane=g["fixed"])
     assert lp == g["last_plane"] and len(s) == g["len"] and _hl.sha256(s).hexdigest() == g["sha"]
     assert _hl.sha256(dec.tobytes()).hexdigest() == g["dec_sha"]
 
@@ -312,6 +336,6 @@ def test_gpu_quantize_matches_reference_golden(gpu_pkg, g):
     assert [[float(v).hex() for v in ax] for ax in sn] == g["slice_norms_hex"]
 
 
-@pytest.mark.parametrize("g", [g for g in _GOLDEN["symbols"] if g["coder"] == 0], ids=lambda g: f"case{g['case']}")
+@pytest.mark.parametrize("g", _GOLDEN["symbols"], ids=lambda g: f"c{g['coder']}-case{g['case']}")
 def test_gpu_entropy_matches_reference_golden(gpu_pkg, g):
-    assert gpu_pkg.encode_symbols(0, g["symbols"]).hex() == g["bytes"]
+    assert gpu_pkg.encode_symbols(g["coder"], g["symbols"]).hex() == g["bytes"]
