@@ -40,7 +40,7 @@ class Params(C.Structure):
         ("rtmss", C.c_double), ("coder", C.c_int), ("split", C.c_int), ("simple", C.c_int),
         ("f32", C.c_int), ("backend", C.c_int), ("block", C.c_uint64),
         ("has_storage", C.c_int), ("storage", C.c_uint64 * 8),
-        ("has_mode", C.c_int), ("mode", C.c_uint64 * 8),
+        ("has_mode", C.c_int), ("mode", C.c_uint64 * 8), ("method", C.c_int),
     ]
 
 
@@ -90,8 +90,9 @@ def _take(ptr, n, ctype, dtype):
 
 
 def make_params(target_re=None, target_sse=None, rtmss=0.5, coder=0, split=True, simple=False,
-                internal_float32=False, backend=0, block_size=0, storage_order=None, mode_order=None):
+                internal_float32=False, backend=0, block_size=0, storage_order=None, mode_order=None, method=0):
     p = Params()
+    p.method = int(method)
     p.has_re = int(target_re is not None)
     p.re = float(target_re or 0.0)
     p.has_sse = int(target_sse is not None)
@@ -201,7 +202,8 @@ def eig(a: np.ndarray):
     return ev, flat.reshape((n, n), order="F")
 
 
-def quantize(core: np.ndarray):
+def quantize(core: np.ndarray, method: int = 0):
+    """corecodec::quantize (core_codec.cpp:55-93) under vectorize::Method `method`."""
     core = np.ascontiguousarray(core, dtype=np.float64)
     n = core.size
     shape = np.asarray(core.shape, np.uint64)
@@ -210,8 +212,8 @@ def quantize(core: np.ndarray):
     k = C.c_int()
     zero = C.c_int()
     sn = np.zeros(int(sum(core.shape)), np.float64)
-    _check(lib().orc_quantize_f64(_p(core), _p(shape), core.ndim, _p(mag), _p(neg), C.byref(k), C.byref(zero),
-                                  _p(sn)))
+    _check(lib().orc_quantize_method_f64(_p(core), _p(shape), core.ndim, int(method), _p(mag), _p(neg), C.byref(k),
+                                         C.byref(zero), _p(sn)))
     parts, o = [], 0
     for e in core.shape:
         parts.append(sn[o:o + e].copy())
@@ -313,3 +315,11 @@ def transpose(x: np.ndarray, perm):
 def threads() -> int:
     """Host threads the oracle's OpenMP loops use (results do not depend on it)."""
     return int(lib().orc_threads())
+
+
+def order_map(method: int, shape) -> np.ndarray:
+    """vectorize::OrderMap::build (vectorize.cpp:163-170): flat position of each coefficient."""
+    sh = np.asarray(shape, np.uint64)
+    out = np.empty(int(np.prod(sh)), np.uint64)
+    _check(lib().orc_order_map(int(method), _p(sh), len(sh), _p(out)))
+    return out

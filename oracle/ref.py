@@ -133,3 +133,26 @@ def backward_sum(m) -> float:
 
 def backend() -> str:
     return lib().ref_backend().decode()
+
+
+def order_map(method: int, shape) -> np.ndarray:
+    """The reference's own vectorize::OrderMap::build (vectorize.cpp:163-170)."""
+    sh = np.asarray(shape, np.uint64)
+    out = np.empty(int(np.prod(sh)), np.uint64)
+    _check(lib().ref_order_map(int(method), sh.ctypes.data_as(C.c_void_p), len(sh), out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def quantize_method(core: np.ndarray, method: int):
+    """The reference's corecodec::quantize under a vectorization method: (mag, neg, k, zero, slice norms)."""
+    core = np.ascontiguousarray(core, np.float64)
+    sh = np.asarray(core.shape, np.uint64)
+    n = core.size
+    mag = np.zeros(n, np.uint64)
+    neg = np.zeros(n, np.uint8)
+    k, zero = C.c_int(), C.c_int()
+    sn = np.zeros(int(sh.sum()), np.float64)
+    _check(lib().ref_quantize_method_f64(core.ctypes.data_as(C.c_void_p), sh.ctypes.data_as(C.c_void_p), core.ndim,
+                                         int(method), mag.ctypes.data_as(C.c_void_p), neg.ctypes.data_as(C.c_void_p),
+                                         C.byref(k), C.byref(zero), sn.ctypes.data_as(C.c_void_p)))
+    return mag, neg, k.value, bool(zero.value), sn

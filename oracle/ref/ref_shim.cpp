@@ -117,6 +117,34 @@ int ref_quantize_f64(const double* core, const uint64_t* shape, int d, uint64_t*
     });
 }
 
+int ref_order_map(int method, const uint64_t* shape, int d, uint64_t* out) {
+    return guard([&] {
+        Shape sh(shape, shape + d);
+        const auto om = vectorize::OrderMap::build(static_cast<vectorize::Method>(method), sh);
+        for (std::uint64_t v = 0; v < om.size(); ++v) out[v] = om[v];
+    });
+}
+
+// corecodec::quantize with a non-default vectorization (slice norms summed in that order)
+int ref_quantize_method_f64(const double* core, const uint64_t* shape, int d, int method, uint64_t* mag,
+                            uint8_t* neg, int* k, int* zero, double* slice_norms) {
+    return guard([&] {
+        Shape sh(shape, shape + d);
+        DenseTensor<double> t(sh, std::vector<double>(core, core + shape_numel(sh)));
+        auto om = vectorize::OrderMap::build(static_cast<vectorize::Method>(method), sh);
+        auto q = corecodec::quantize(t, om);
+        *k = q.scale_exponent;
+        *zero = q.zero_flag;
+        if (!q.zero_flag) {
+            std::memcpy(mag, q.magnitudes.data(), q.magnitudes.size() * 8);
+            std::memcpy(neg, q.signs.data(), q.signs.size());
+        }
+        std::size_t o = 0;
+        for (auto& ax : q.slice_norms)
+            for (double s : ax) slice_norms[o++] = s;
+    });
+}
+
 int ref_encode_symbols(int coder, const uint64_t* s, uint64_t n, uint8_t** out, uint64_t* len) {
     return guard([&] {
         auto b = entropy::encode_symbols(static_cast<entropy::Coder>(coder), {s, n});

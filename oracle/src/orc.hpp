@@ -81,7 +81,10 @@ struct Quantized {
     std::vector<std::vector<double>> slice_norms;
 };
 template <class T>
-Quantized quantize(const std::vector<T>& core, const Shape& shape);  // lex order only
+Quantized quantize(const std::vector<T>& core, const Shape& shape, std::span<const u64> order = {});
+// vectorize::OrderMap (vectorize.cpp:40-170): flat position of the v-th coefficient;
+// empty = lexicographic (identity).  method: 0 lexicographic, 1 zigzag, 2 zorder
+std::vector<u64> order_map(int method, const Shape& shape);
 
 struct Stops {
     u64 lead = 0, trail = 0;
@@ -151,7 +154,8 @@ struct Decoded {
     std::vector<u8> neg;
 };
 Decoded decode_stream(const StreamMeta& meta, const std::vector<std::vector<std::span<const u8>>>& pl);
-std::vector<std::vector<u8>> dead_slices(const Shape& shape, std::span<const u64> decoded);
+std::vector<std::vector<u8>> dead_slices(const Shape& shape, std::span<const u64> decoded,
+                                         std::span<const u64> order = {});
 
 // ---------------------------------------------------------------- error model (error_model.cpp)
 double backward_sq(std::span<const u64> v);
@@ -235,6 +239,7 @@ struct Params {
     u64 block = 0;
     bool f32 = false;
     SvdBackend backend = SvdBackend::automatic;
+    int method = 0;  // vectorize::Method
 };
 
 struct Result {

@@ -65,6 +65,15 @@ extern "C" {
 
 // host threads the oracle's Gram / projection loops use (OpenMP; results do
 // not depend on it)
+int orc_order_map(int method, const uint64_t* shape, int d, uint64_t* out) {
+    return guard([&] {
+        const Shape sh(shape, shape + d);
+        const auto o = order_map(method, sh);
+        const u64 n = numel(sh);
+        for (u64 v = 0; v < n; ++v) out[v] = o.empty() ? v : o[v];
+    });
+}
+
 int orc_threads() {
 #ifdef _OPENMP
     return omp_get_max_threads();
@@ -89,6 +98,7 @@ struct orc_params {
     uint64_t storage[8];
     int has_mode;
     uint64_t mode[8];
+    int method;  // vectorize::Method
 };
 
 struct orc_result {
@@ -120,6 +130,7 @@ int orc_compress(const uint8_t* bytes, uint64_t n, int dtype, const uint64_t* sh
         p.simple = pp->simple != 0;
         p.f32 = pp->f32 != 0;
         p.backend = static_cast<SvdBackend>(pp->backend);
+        p.method = pp->method;
         p.block = pp->block;
         if (pp->has_storage) p.storage_order = Perm(pp->storage, pp->storage + d);
         if (pp->has_mode) p.mode_order = Perm(pp->mode, pp->mode + d);
@@ -199,12 +210,13 @@ int orc_eig_f64(double* a, uint64_t n, double* evals) {
     });
 }
 
-int orc_quantize_f64(const double* core, const uint64_t* shape, int d, uint64_t* mag, uint8_t* neg, int* k,
-                     int* zero, double* slice_norms) {
+int orc_quantize_method_f64(const double* core, const uint64_t* shape, int d, int method, uint64_t* mag,
+                            uint8_t* neg, int* k, int* zero, double* slice_norms) {
     return guard([&] {
         const Shape sh = to_shape(shape, d);
         std::vector<double> x(core, core + numel(sh));
-        auto q = quantize(x, sh);
+        const auto om = order_map(method, sh);
+        auto q = quantize(x, sh, om);
         *k = q.k;
         *zero = q.zero;
         if (!q.zero) {
@@ -215,6 +227,11 @@ int orc_quantize_f64(const double* core, const uint64_t* shape, int d, uint64_t*
         for (int a = 0; a < d; ++a)
             for (double s : q.slice_norms[a]) slice_norms[o++] = s;
     });
+}
+
+int orc_quantize_f64(const double* core, const uint64_t* shape, int d, uint64_t* mag, uint8_t* neg, int* k,
+                     int* zero, double* slice_norms) {
+    return orc_quantize_method_f64(core, shape, d, 0, mag, neg, k, zero, slice_norms);
 }
 
 int orc_encode(const uint64_t* m, const uint8_t* neg, uint64_t n, double target_int, int coder, uint64_t block,

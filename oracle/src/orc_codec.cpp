@@ -73,8 +73,9 @@ double recal_sse(std::span<const u64> m, int plane) {
 
 // ---------------------------------------------------------------- quantize
 template <class T>
-Quantized quantize(const std::vector<T>& core, const Shape& shape) {
+Quantized quantize(const std::vector<T>& core, const Shape& shape, std::span<const u64> order) {
     const std::size_t n = core.size();
+    if (!order.empty() && order.size() != n) throw Error("quantize: order map does not match core");
     if (numel(shape) != n) throw Error("quantize: order map does not match core");
     if (!finite_all(core.data(), n)) throw Error("quantize: non-finite core values");
     Quantized q;
@@ -93,20 +94,102 @@ Quantized quantize(const std::vector<T>& core, const Shape& shape) {
     q.mag.resize(n);
     q.neg.resize(n);
     for (std::size_t v = 0; v < n; ++v) {
-        const double x = static_cast<double>(core[v]);
+        const u64 pos = order.empty() ? v : order[v];
+        const double x = static_cast<double>(core[pos]);
         const u64 m = static_cast<u64>(std::nearbyint(std::ldexp(std::fabs(x), q.k)));
         q.mag[v] = m;
         q.neg[v] = x < 0 ? 1 : 0;
         const double sq = dbl(m) * dbl(m);
-        for (std::size_t a = 0; a < shape.size(); ++a) q.slice_norms[a][(v / st[a]) % shape[a]] += sq;
+        for (std::size_t a = 0; a < shape.size(); ++a) q.slice_norms[a][(pos / st[a]) % shape[a]] += sq;
     }
     const double down = std::ldexp(1.0, -2 * q.k);
     for (auto& ax : q.slice_norms)
         for (double& s : ax) s = std::sqrt(s * down);
     return q;
 }
-template Quantized quantize(const std::vector<float>&, const Shape&);
-template Quantized quantize(const std::vector<double>&, const Shape&);
+template Quantized quantize(const std::vector<float>&, const Shape&, std::span<const u64>);
+template Quantized quantize(const std::vector<double>&, const Shape&, std::span<const u64>);
+
+// ---------------------------------------------------------------- vectorization order
+// Restates vectorize::PositionIterator (vectorize.cpp:40-135): zigzag walks the
+// anti-diagonal layers (coordinate sum 0, 1, ...) and inside a layer moves to the
+// next composition in lexicographic order; zorder visits Morton keys (axis 0
+// most significant inside each bit level) in increasing order, skipping the
+// subcubes that leave the shape.
+std::vector<u64> order_map(int method, const Shape& shape) {
+    if (method == 0) return {};
+    if (method != 1 && method != 2) throw Error("vectorize: unknown method");
+    const std::size_t d = shape.size();
+    if (d == 0) throw Error("vectorize: empty shape");
+    const auto st = strides_of(shape);
+    const u64 n = numel(shape);
+    std::vector<u64> out;
+    out.reserve(n);
+    std::vector<std::size_t> pos(d, 0);
+    auto flat = [&] {
+        u64 f = 0;
+        for (std::size_t i = 0; i < d; ++i) f += pos[i] * st[i];
+        return f;
+    };
+    if (method == 1) {
+        std::size_t layer_max = 0, layer = 0;
+        for (auto v : shape) layer_max += v - 1;
+        while (true) {
+            out.push_back(flat());
+            bool moved = false;
+            std::size_t tail = 0;
+            for (std::size_t i = d - 1; i-- > 0;) {
+                tail += pos[i + 1];
+                if (tail >= 1 && pos[i] + 1 <= shape[i] - 1) {
+                    ++pos[i];
+                    std::size_t rem = tail - 1;
+                    for (std::size_t j = d; j-- > i + 1;) {
+                        pos[j] = std::min(rem, shape[j] - 1);
+                        rem -= pos[j];
+                    }
+                    moved = true;
+                    break;
+                }
+            }
+            if (moved) continue;
+            if (++layer > layer_max) break;
+            std::size_t rem = layer;
+            for (std::size_t j = d; j-- > 0;) {
+                pos[j] = std::min(rem, shape[j] - 1);
+                rem -= pos[j];
+            }
+        }
+        return out;
+    }
+    unsigned levels = 0;
+    for (auto v : shape) {
+        unsigned b = 0;
+        while ((u64{1} << b) < v) ++b;
+        levels = std::max(levels, b);
+    }
+    if (static_cast<u64>(levels) * d > 63) throw Error("vectorize: shape too large for 64-bit Morton keys");
+    const u64 key_end = u64{1} << (levels * d);
+    for (u64 key = 0; key < key_end;) {
+        bool ok = true;
+        for (std::size_t a = 0; a < d && ok; ++a) {
+            u64 c = 0;
+            for (unsigned t = levels; t-- > 0;) c = (c << 1) | ((key >> (t * d + (d - 1 - a))) & 1u);
+            if (c >= shape[a]) {
+                const u64 bad = c ^ (shape[a] - 1);
+                const unsigned t = 63u - static_cast<unsigned>(__builtin_clzll(bad));
+                const unsigned g = t * static_cast<unsigned>(d) + static_cast<unsigned>(d - 1 - a);
+                key = (key | ((u64{1} << g) - 1)) + 1;
+                ok = false;
+            } else {
+                pos[a] = static_cast<std::size_t>(c);
+            }
+        }
+        if (!ok) continue;
+        out.push_back(flat());
+        ++key;
+    }
+    return out;
+}
 
 // ---------------------------------------------------------------- encoder
 u64 default_block(u64 n) { return std::max<u64>(4096, (n + 63) / 64); }
@@ -430,13 +513,14 @@ Decoded decode_stream(const StreamMeta& meta, const std::vector<std::vector<std:
     return d;
 }
 
-std::vector<std::vector<u8>> dead_slices(const Shape& shape, std::span<const u64> dec) {
+std::vector<std::vector<u8>> dead_slices(const Shape& shape, std::span<const u64> dec, std::span<const u64> order) {
     std::vector<std::vector<u8>> dead(shape.size());
     for (std::size_t a = 0; a < shape.size(); ++a) dead[a].assign(shape[a], 1);
     const auto st = strides_of(shape);
     for (std::size_t v = 0; v < dec.size(); ++v) {
         if (!dec[v]) continue;
-        for (std::size_t a = 0; a < shape.size(); ++a) dead[a][(v / st[a]) % shape[a]] = 0;
+        const u64 pos = order.empty() ? v : order[v];
+        for (std::size_t a = 0; a < shape.size(); ++a) dead[a][(pos / st[a]) % shape[a]] = 0;
     }
     return dead;
 }

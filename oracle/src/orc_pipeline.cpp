@@ -740,7 +740,9 @@ Result compress_as(std::vector<T> a, const Shape& shape, Dtype dt, const Params&
     Shape cs(d);
     for (std::size_t i = 0; i < d; ++i) cs[i] = f.core_shape[storage[i]];
     std::vector<T> core_s = permute_axes(f.core, f.core_shape, storage);
-    Quantized q = quantize(core_s, cs);
+    const std::vector<u64> vorder = order_map(prm.method, cs);  // vectorize::OrderMap::build (pipeline.cpp:87)
+    h.method = static_cast<u8>(prm.method);
+    Quantized q = quantize(core_s, cs, vorder);
     core_s.clear();
     res.t_quant = ms_since(t0);
     h.zero = q.zero;
@@ -769,7 +771,7 @@ Result compress_as(std::vector<T> a, const Shape& shape, Dtype dt, const Params&
     enc.plan(std::ldexp(core_target, 2 * q.k));
     res.t_core = ms_since(t0);
     res.core_last_plane = enc.planned().last_plane;
-    const auto dead_ax = dead_slices(cs, enc.planned().decoded);
+    const auto dead_ax = dead_slices(cs, enc.planned().decoded, vorder);
     std::vector<std::vector<u8>> dead_mode(d);
     for (std::size_t ax = 0; ax < d; ++ax) dead_mode[mode_of[ax]] = dead_ax[ax];
 
@@ -798,9 +800,10 @@ Result compress_as(std::vector<T> a, const Shape& shape, Dtype dt, const Params&
     const auto st = strides_of(cs);
     std::vector<u8> neg = q.neg;
     for (std::size_t v = 0; v < neg.size(); ++v) {
+        const u64 pos = vorder.empty() ? v : vorder[v];
         u8 par = 0;
         for (std::size_t ax = 0; ax < d; ++ax)
-            if (flips[mode_of[ax]][(v / st[ax]) % cs[ax]] < 0) par ^= 1;
+            if (flips[mode_of[ax]][(pos / st[ax]) % cs[ax]] < 0) par ^= 1;
         neg[v] ^= par;
     }
     Stream cst = enc.finalize(neg);
@@ -847,7 +850,7 @@ std::vector<T> decompress_tensor(std::span<const u8> cont, Shape& shape_out) {
     if (d == 0) throw Error("container: zero tensor order");
     h.coder = static_cast<Coder>(r.u8v());
     h.method = r.u8v();
-    if (h.method != 0) throw Error("oracle: only lexicographic vectorization is restated");
+    if (h.method > 2) throw Error("container: unknown vectorization method");
     const u8 fl = r.u8v();
     h.zero = fl & 1;
     h.simple = fl & 4;
@@ -897,11 +900,12 @@ std::vector<T> decompress_tensor(std::span<const u8> cont, Shape& shape_out) {
     for (std::size_t a = 0; a < d; ++a) cs[a] = cp[h.storage[a]];
     if (cv.meta.count != numel(cs)) throw Error("container: core length does not match ranks");
     const auto dec = decode_stream(cv.meta, cv.pl);
+    const std::vector<u64> vorder = order_map(h.method, cs);
     std::vector<T> core_s(numel(cs));
     for (std::size_t v = 0; v < core_s.size(); ++v) {
         double val = std::ldexp(static_cast<double>(dec.mag[v]), -h.k);
         if (dec.neg[v]) val = -val;
-        core_s[v] = static_cast<T>(val);
+        core_s[vorder.empty() ? v : vorder[v]] = static_cast<T>(val);
     }
     f.core = permute_axes(core_s, cs, inverse_perm(h.storage));
     f.core_shape = cp;

@@ -408,11 +408,11 @@ __global__ void __launch_bounds__(kDsT) dec_stream_kernel(const u8* __restrict__
 
 // core value = +-ldexp(mag, -k)
 __global__ void dequant_kernel(const u64* __restrict__ mag, const u8* __restrict__ neg, u64 n, int k,
-                               double* __restrict__ out) {
+                               double* __restrict__ out, const u64* __restrict__ order) {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         const double v = scalbn(__ull2double_rn(mag[i]), -k);
-        out[i] = neg[i] ? -v : v;
+        out[order ? order[i] : i] = neg[i] ? -v : v;
     }
 }
 
@@ -482,9 +482,9 @@ void decode_streams(const u8* cont, const DecStream* streams, const DecBlock* bl
     TCB_LAUNCH();
 }
 
-void dequantize(const u64* mag, const u8* neg, u64 n, int k, double* out, cudaStream_t s) {
+void dequantize(const u64* mag, const u8* neg, u64 n, int k, double* out, cudaStream_t s, const u64* order) {
     if (n == 0) return;
-    dequant_kernel<<<std::min<unsigned>(cdiv(n, 256), 4 * sm_count()), 256, 0, s>>>(mag, neg, n, k, out);
+    dequant_kernel<<<std::min<unsigned>(cdiv(n, 256), 4 * sm_count()), 256, 0, s>>>(mag, neg, n, k, out, order);
     count_launch();
     TCB_LAUNCH();
 }

@@ -53,7 +53,9 @@ void decode_entropy(const u8* cont, const DecSection* sec_dev, const std::vector
 void decode_streams(const u8* cont, const DecStream* streams, const DecBlock* blocks, u64 nblocks,
                     const DecSection* sec, const u64* syms, u64* mag, u8* neg, u8* pe, u8* colbits, int* err,
                     cudaStream_t s);
-void dequantize(const u64* mag, const u8* neg, u64 n, int k, double* out, cudaStream_t s);
+// core value = +-ldexp(mag, -k), scattered to order[v] when a vectorisation map is given
+void dequantize(const u64* mag, const u8* neg, u64 n, int k, double* out, cudaStream_t s,
+                const u64* order = nullptr);
 void emit_dtype(const double* x, u64 n, int dtype, void* out, cudaStream_t s);
 
 }  // namespace tcb

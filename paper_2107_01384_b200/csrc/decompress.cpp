@@ -194,7 +194,6 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
         out.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         return out;
     }
-    if (method != 0) throw Error("decompress: only lexicographic vectorization is implemented on the device path");
     // ---- parse factor and core sections
     std::vector<FactorMeta> fm(d);
     std::vector<StreamParse> sp;
@@ -347,7 +346,8 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
     // ---- core: dequantise, storage -> processing order (pipeline.cpp:206-219)
     const u64 nc = prod(cs);
     DevBuf<double> core_s(nc, s), core_p(nc, s);
-    dequantize(mag.p + ds[d].out_off, neg.p + ds[d].out_off, nc, k, core_s.p, s);
+    const DevBuf<u64> vorder = order_map_device(method, cs, s);  // OrderMap::build (pipeline.cpp:210)
+    dequantize(mag.p + ds[d].out_off, neg.p + ds[d].out_off, nc, k, core_s.p, s, vorder.p);
     permute_axes(core_s.p, core_p.p, cs, inverse(storage), s);
     core_s.release();
     // ---- reconstruct (sthosvd.cpp:173-218): decompression order, TTM expansions, final transpose

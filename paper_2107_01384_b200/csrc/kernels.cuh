@@ -60,8 +60,10 @@ void topk_eig(const double* G, u64 n, int p, int extra_iters, double* X, std::ve
               std::vector<double>& resid, double& trace, cudaStream_t s);
 
 // ---- quant.cu (core_codec.cpp:55-93)
-void quantize_f64(const double* x, u64 n, int k, u64* mag, u8* neg, cudaStream_t s);
-// Per-axis slice sums of (double)m^2 replayed in lexicographic order, then sqrt(s*down).
-void slice_norms(const u64* mag, const std::vector<u64>& shape, double down, double* out, cudaStream_t s);
+// order (optional): the vectorisation map, coefficient v = x[order[v]]
+void quantize_f64(const double* x, u64 n, int k, u64* mag, u8* neg, cudaStream_t s, const u64* order = nullptr);
+// Per-axis slice sums of (double)m^2 replayed in vectorisation order, then sqrt(s*down).
+void slice_norms(const u64* mag, const std::vector<u64>& shape, double down, double* out, cudaStream_t s,
+                 const u64* order = nullptr);
 
 }  // namespace tcb

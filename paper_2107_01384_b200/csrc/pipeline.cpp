@@ -524,6 +524,8 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     DevBuf<double> core_s(nc, s);
     permute_axes(f.core.p, core_s.p, f.core_shape, storage, s);
     f.core.release();
+    // vectorize::OrderMap::build (pipeline.cpp:87): null for the lexicographic default
+    const DevBuf<u64> vorder = order_map_device(prm.method, cs, s);
     if (prm.f32) {  // the float core of the reference
         DevBuf<float> cf(nc, s);
         ingest_cast_f32(core_s.p, 9, nc, cf.p, s);
@@ -542,9 +544,9 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     u64 sum_ext = 0;
     for (auto v : cs) sum_ext += v;
     if (!zero) {
-        quantize_f64(core_s.p, nc, k, mag.p, neg.p, s);
+        quantize_f64(core_s.p, nc, k, mag.p, neg.p, s, vorder.p);
         DevBuf<double> dsn(sum_ext, s);
-        slice_norms(mag.p, cs, std::ldexp(1.0, -2 * k), dsn.p, s);
+        slice_norms(mag.p, cs, std::ldexp(1.0, -2 * k), dsn.p, s, vorder.p);
         sn_flat = dsn.to_host();
     }
     core_s.release();
@@ -668,7 +670,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     std::vector<u8> dead_flat;
     {
         HostTrace ht("encode: dead slices");
-        dead_flat = dead_slices(dec.p, cs, s);
+        dead_flat = dead_slices(dec.p, cs, s, vorder.p);
     }
     {
         u64 o = 0;
@@ -696,7 +698,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     std::vector<signed char> flips_axis;
     for (std::size_t ax = 0; ax < d; ++ax)
         flips_axis.insert(flips_axis.end(), flips_of[mode_of[ax]].begin(), flips_of[mode_of[ax]].end());
-    sign_fold(neg.p, cs, flips_axis, s);
+    sign_fold(neg.p, cs, flips_axis, s, vorder.p);
     u64 count = 1;
     for (auto v : f.r) count *= v;
     std::vector<u8> core_stream;
@@ -763,7 +765,6 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     if (prm.target_re && prm.target_sse)
         throw Error("compress: relative-error and SSE targets are mutually exclusive");
     if (!prm.target_re && !prm.target_sse) throw Error("compress: no error target given");
-    if (prm.method != 0) throw Error("compress: only lexicographic vectorization is implemented on the device path");
 
     // ingest (container.cpp:69-94): the internal tensor in double; with
     // internal_float32 the values are first rounded to float as the reference does

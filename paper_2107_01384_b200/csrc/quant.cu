@@ -1,5 +1,7 @@
 // Core quantisation (core_codec.cpp:55-93), dead slices (:510-523) and the
 // Householder sign fold (pipeline.cpp:161-175).  Integer-exact kernels.
+#include <cub/device/device_radix_sort.cuh>
+
 #include "kernels.cuh"
 #include "quant.cuh"
 
@@ -9,10 +11,10 @@ namespace {
 
 // m = nearbyint(ldexp(|x|, k)) (round-half-even), sign = x < 0
 __global__ void quantize_kernel(const double* __restrict__ x, u64 n, int k, u64* __restrict__ mag,
-                                u8* __restrict__ neg) {
+                                u8* __restrict__ neg, const u64* __restrict__ order) {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const double v = x[i];
+        const double v = x[order ? order[i] : i];
         mag[i] = __double2ull_rn(scalbn(fabs(v), k));
         neg[i] = v < 0.0 ? 1 : 0;
     }
@@ -48,28 +50,88 @@ __global__ void slice_norm_kernel(const u64* __restrict__ mag, const u64* __rest
 }
 
 __global__ void dead_kernel(const u64* __restrict__ dec, u64 n, const u64* __restrict__ meta /* shape, stride, off */,
-                            int d, u8* __restrict__ dead) {
+                            int d, u8* __restrict__ dead, const u64* __restrict__ order) {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 v = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
         if (dec[v] == 0) continue;
+        const u64 pos = order ? order[v] : v;
         for (int a = 0; a < d; ++a) {
-            const u64 idx = (v / meta[d + a]) % meta[a];
+            const u64 idx = (pos / meta[d + a]) % meta[a];
             dead[meta[2 * d + a] + idx] = 0;
         }
     }
 }
 
 __global__ void signfold_kernel(u8* __restrict__ neg, u64 n, const u64* __restrict__ meta, int d,
-                                const signed char* __restrict__ flips /* concatenated per storage axis */) {
+                                const signed char* __restrict__ flips /* concatenated per storage axis */,
+                                const u64* __restrict__ order) {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 v = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+        const u64 pos = order ? order[v] : v;
         u8 par = 0;
         for (int a = 0; a < d; ++a) {
-            const u64 idx = (v / meta[d + a]) % meta[a];
+            const u64 idx = (pos / meta[d + a]) % meta[a];
             par ^= flips[meta[2 * d + a] + idx] < 0 ? 1 : 0;
         }
         neg[v] ^= par;
     }
+}
+
+// vectorize::OrderMap keys (vectorize.cpp:40-135): zigzag = (coordinate sum,
+// row-major index), i.e. each anti-diagonal layer in lexicographic order;
+// zorder = the Morton key (axis 0 most significant in each bit level).  A
+// stable sort of the positions by key gives the iteration order.
+__global__ void order_keys_kernel(const u64* __restrict__ meta, int d, u64 n, int method, unsigned levels,
+                                  u64* __restrict__ keys, u64* __restrict__ pos) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 f = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; f < n; f += stride) {
+        u64 key = 0;
+        if (method == 1) {
+            u64 sum = 0;
+            for (int a = 0; a < d; ++a) sum += (f / meta[d + a]) % meta[a];
+            key = sum * n + f;
+        } else {
+            for (int a = 0; a < d; ++a) {
+                const u64 c = (f / meta[d + a]) % meta[a];
+                for (unsigned t = 0; t < levels; ++t)
+                    key |= ((c >> t) & 1u) << (t * static_cast<unsigned>(d) + static_cast<unsigned>(d - 1 - a));
+            }
+        }
+        keys[f] = key;
+        pos[f] = f;
+    }
+}
+
+// coordinate along `axis` of each vectorised coefficient (sort key of its slice list)
+__global__ void slice_keys_kernel(const u64* __restrict__ order, u64 n, u64 stride_a, u64 ext_a,
+                                  u32* __restrict__ keys, u64* __restrict__ vals) {
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 v = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+        keys[v] = static_cast<u32>((order[v] / stride_a) % ext_a);
+        vals[v] = v;
+    }
+}
+
+// serial replay per slice over its coefficients in vectorised order (list
+// segment [idx * per, (idx + 1) * per)), one thread per slice
+__global__ void slice_norm_list_kernel(const u64* __restrict__ mag, const u64* __restrict__ list, u64 ext, u64 per,
+                                       double down, double* __restrict__ out) {
+    const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= ext) return;
+    double s = 0.0;
+    for (u64 j = idx * per; j < (idx + 1) * per; ++j) {
+        const double v = __ull2double_rn(mag[list[j]]);
+        s = __dadd_rn(s, __dmul_rn(v, v));
+    }
+    out[idx] = __dsqrt_rn(__dmul_rn(s, down));
+}
+
+template <class K>
+void radix_sort_pairs(const K* kin, K* kout, const u64* vin, u64* vout, u64 n, int bits, cudaStream_t s) {
+    size_t tmp = 0;
+    TCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, static_cast<int>(n), 0, bits, s));
+    DevBuf<u8> t(std::max<size_t>(tmp, 1), s);
+    TCB_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, kin, kout, vin, vout, static_cast<int>(n), 0, bits, s));
 }
 
 std::vector<u64> axis_meta(const std::vector<u64>& shape) {
@@ -91,26 +153,80 @@ std::vector<u64> axis_meta(const std::vector<u64>& shape) {
 
 }  // namespace
 
-void quantize_f64(const double* x, u64 n, int k, u64* mag, u8* neg, cudaStream_t s) {
+DevBuf<u64> order_map_device(int method, const std::vector<u64>& shape, cudaStream_t s) {
+    if (method == 0) return DevBuf<u64>();
+    if (method != 1 && method != 2) throw Error("vectorize: unknown method");
+    const int d = static_cast<int>(shape.size());
+    if (d == 0) throw Error("vectorize: empty shape");
+    u64 n = 1;
+    for (auto v : shape) n *= v;
+    unsigned levels = 0;
+    for (auto v : shape) {
+        unsigned b = 0;
+        while ((u64{1} << b) < v) ++b;
+        levels = std::max(levels, b);
+    }
+    if (method == 2 && static_cast<u64>(levels) * d > 63)
+        throw Error("vectorize: shape too large for 64-bit Morton keys");
+    if (n > 0x7FFFFFFFull) throw Error("vectorize: core too large for the device order map");
+    const auto meta = axis_meta(shape);
+    DevBuf<u64> dm(meta.size(), s);
+    dm.upload(meta.data(), meta.size());
+    DevBuf<u64> keys(n, s), keys2(n, s), pos(n, s), order(n, s);
+    order_keys_kernel<<<std::min<unsigned>(cdiv(n, 256), 4 * sm_count()), 256, 0, s>>>(dm.p, d, n, method, levels,
+                                                                                       keys.p, pos.p);
+    count_launch();
+    TCB_LAUNCH();
+    radix_sort_pairs<u64>(keys.p, keys2.p, pos.p, order.p, n, 64, s);
+    return order;
+}
+
+void quantize_f64(const double* x, u64 n, int k, u64* mag, u8* neg, cudaStream_t s, const u64* order) {
     ProfScope prof_scope(kQuant, s);
     if (n == 0) return;
-    quantize_kernel<<<sm_count() * 8, 256, 0, s>>>(x, n, k, mag, neg);
+    quantize_kernel<<<sm_count() * 8, 256, 0, s>>>(x, n, k, mag, neg, order);
     count_launch();
     TCB_LAUNCH();
 }
 
-void slice_norms(const u64* mag, const std::vector<u64>& shape, double down, double* out, cudaStream_t s) {
+void slice_norms(const u64* mag, const std::vector<u64>& shape, double down, double* out, cudaStream_t s,
+                 const u64* order) {
     ProfScope prof_scope(kQuant, s);
-    u64 total = 0;
-    for (auto v : shape) total += v;
-    DevBuf<u64> sh(shape.size(), s);
-    sh.upload(shape.data(), shape.size());
-    slice_norm_kernel<<<cdiv(total, 64), 64, 0, s>>>(mag, sh.p, static_cast<int>(shape.size()), total, down, out);
-    count_launch();
-    TCB_LAUNCH();
+    u64 total = 0, n = 1;
+    for (auto v : shape) {
+        total += v;
+        n *= v;
+    }
+    if (!order) {
+        DevBuf<u64> sh(shape.size(), s);
+        sh.upload(shape.data(), shape.size());
+        slice_norm_kernel<<<cdiv(total, 64), 64, 0, s>>>(mag, sh.p, static_cast<int>(shape.size()), total, down,
+                                                         out);
+        count_launch();
+        TCB_LAUNCH();
+        return;
+    }
+    // non-lexicographic: each slice's coefficients in vectorised order (stable sort by coordinate)
+    const auto meta = axis_meta(shape);
+    const int d = static_cast<int>(shape.size());
+    DevBuf<u32> k1(n, s), k2(n, s);
+    DevBuf<u64> v1(n, s), list(n, s);
+    u64 off = 0;
+    for (int a = 0; a < d; ++a) {
+        slice_keys_kernel<<<std::min<unsigned>(cdiv(n, 256), 4 * sm_count()), 256, 0, s>>>(order, n, meta[d + a],
+                                                                                           shape[a], k1.p, v1.p);
+        int bits = 1;
+        while ((u64{1} << bits) < shape[a]) ++bits;
+        radix_sort_pairs<u32>(k1.p, k2.p, v1.p, list.p, n, bits, s);
+        slice_norm_list_kernel<<<cdiv(shape[a], 64), 64, 0, s>>>(mag, list.p, shape[a], n / shape[a], down,
+                                                                 out + off);
+        count_launch(2);
+        TCB_LAUNCH();
+        off += shape[a];
+    }
 }
 
-std::vector<u8> dead_slices(const u64* dec, const std::vector<u64>& shape, cudaStream_t s) {
+std::vector<u8> dead_slices(const u64* dec, const std::vector<u64>& shape, cudaStream_t s, const u64* order) {
     ProfScope prof_scope(kQuant, s);
     const auto meta = axis_meta(shape);
     u64 n = 1, total = 0;
@@ -122,14 +238,14 @@ std::vector<u8> dead_slices(const u64* dec, const std::vector<u64>& shape, cudaS
     dm.upload(meta.data(), meta.size());
     DevBuf<u8> dead(total, s);
     TCB_CUDA(cudaMemsetAsync(dead.p, 1, total, s));
-    dead_kernel<<<sm_count() * 4, 256, 0, s>>>(dec, n, dm.p, static_cast<int>(shape.size()), dead.p);
+    dead_kernel<<<sm_count() * 4, 256, 0, s>>>(dec, n, dm.p, static_cast<int>(shape.size()), dead.p, order);
     count_launch();
     TCB_LAUNCH();
     return dead.to_host();
 }
 
 void sign_fold(u8* neg, const std::vector<u64>& shape, const std::vector<signed char>& flips_by_axis,
-               cudaStream_t s) {
+               cudaStream_t s, const u64* order) {
     ProfScope prof_scope(kQuant, s);
     const auto meta = axis_meta(shape);
     u64 n = 1;
@@ -138,7 +254,7 @@ void sign_fold(u8* neg, const std::vector<u64>& shape, const std::vector<signed 
     dm.upload(meta.data(), meta.size());
     DevBuf<signed char> fl(flips_by_axis.size(), s);
     fl.upload(flips_by_axis.data(), flips_by_axis.size());
-    signfold_kernel<<<sm_count() * 4, 256, 0, s>>>(neg, n, dm.p, static_cast<int>(shape.size()), fl.p);
+    signfold_kernel<<<sm_count() * 4, 256, 0, s>>>(neg, n, dm.p, static_cast<int>(shape.size()), fl.p, order);
     count_launch();
     TCB_LAUNCH();
 }

@@ -5,11 +5,15 @@
 
 namespace tcb {
 
+// vectorize::OrderMap::build on the device (flat position of each coefficient);
+// empty for the lexicographic method (identity)
+DevBuf<u64> order_map_device(int method, const std::vector<u64>& shape, cudaStream_t s);
 // per-axis "all insignificant" bitmaps, concatenated over axes (core_codec.cpp:510-523)
-std::vector<u8> dead_slices(const u64* dec, const std::vector<u64>& shape, cudaStream_t s);
+std::vector<u8> dead_slices(const u64* dec, const std::vector<u64>& shape, cudaStream_t s,
+                            const u64* order = nullptr);
 // neg ^= parity of factor column flips along each storage axis (pipeline.cpp:161-175)
 void sign_fold(u8* neg, const std::vector<u64>& shape, const std::vector<signed char>& flips_by_axis,
-               cudaStream_t s);
+               cudaStream_t s, const u64* order = nullptr);
 
 // ---- factor.cu (factor_codec.cpp:23-244)
 // max |U_live^T U_live - I| (the orthonormality guard of factorize), computed in T

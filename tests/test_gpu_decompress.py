@@ -32,7 +32,8 @@ def test_decompress_gpu_containers(gpu_pkg, kind, shape, re):
 
 
 @pytest.mark.parametrize("opts", [dict(coder=1), dict(split=False), dict(simple=True), dict(block_size=256),
-                                  dict(coder=1, split=False, block_size=512), dict(storage_order=(2, 0, 1))])
+                                  dict(coder=1, split=False, block_size=512), dict(storage_order=(2, 0, 1)),
+                                  dict(method=1), dict(method=2, block_size=512)])
 def test_decompress_oracle_containers(gpu_pkg, opts):
     """Containers written by the oracle (rANS, non-split, simple weights, multi-block
     streams, a non-default storage order): every decode path on the device."""

@@ -241,6 +241,9 @@ def test_compress_end_to_end(gpu_pkg, kind, shape, dtype, re):
     (dict(split_planes=False), dict(split=False)),
     (dict(simple_factor_weights=True), dict(simple=True)),
     (dict(coder=1, split_planes=False, block_size=1024), dict(coder=1, split=False, block_size=1024)),
+    (dict(method=1), dict(method=1)),  # zigzag vectorization
+    (dict(method=2), dict(method=2)),  # Z-order vectorization
+    (dict(method=2, block_size=1024, coder=1), dict(method=2, block_size=1024, coder=1)),
 ])
 def test_compress_coding_options_end_to_end(gpu_pkg, gopts, oopts):
     """Non-default coding options: rANS, non-split planes,

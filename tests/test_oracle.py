@@ -208,3 +208,37 @@ def test_uint16_source_precision_flag():
     big = np.full((4, 4, 4), 2 ** 60, np.int64)
     big[0, 0, 0] = 1
     assert oracle.compress(big, target_re=1e-2).precision_loss
+
+
+# ---------------------------------------------------------------- vectorization methods
+@pytest.mark.parametrize("shape", [(3, 4, 5), (13, 11, 7), (9, 6, 4, 3), (1, 8, 1), (17,)])
+@pytest.mark.parametrize("method", [1, 2])
+def test_order_map_matches_reference(shape, method):
+    import oracle.ref as R
+
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    assert np.array_equal(oracle.order_map(method, shape), R.order_map(method, shape))
+
+
+@pytest.mark.parametrize("method", [1, 2])
+def test_quantize_method_matches_reference(method):
+    import oracle.ref as R
+
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(method)
+    core = rng.standard_normal((11, 9, 7)) * np.exp(-np.indices((11, 9, 7)).sum(0) / 4.0)
+    mag, neg, k, zero, sn = oracle.quantize(core, method)
+    rm, rn, rk, rz, rsn = R.quantize_method(core, method)
+    assert k == rk and zero == rz and np.array_equal(mag, rm) and np.array_equal(neg, rn)
+    assert np.concatenate(sn).tobytes() == rsn.tobytes()  # slice norms summed in vectorised order
+
+
+@pytest.mark.parametrize("method", [1, 2])
+def test_compress_method_round_trip(method):
+    x = synth.small("sin_decay", (24, 20, 16), seed=3)
+    info = oracle.compress(x, target_re=1e-3, method=method)
+    assert info.container[9] == method  # header byte 9: vectorize::Method
+    y = oracle.decompress(info.container, x.shape)
+    assert np.linalg.norm(y - x) / np.linalg.norm(x) <= 1.05e-3
