@@ -342,3 +342,31 @@ def test_gpu_quantize_matches_reference_golden(gpu_pkg, g):
 @pytest.mark.parametrize("g", _GOLDEN["symbols"], ids=lambda g: f"c{g['coder']}-case{g['case']}")
 def test_gpu_entropy_matches_reference_golden(gpu_pkg, g):
     assert gpu_pkg.encode_symbols(g["coder"], g["symbols"]).hex() == g["bytes"]
+
+
+# ---------------------------------------------------------------- ingest completeness
+@pytest.mark.parametrize("dtype", [np.int8, np.uint8, np.int16, np.uint16, np.int32, np.uint32, np.int64, np.uint64,
+                                   np.float32, np.float64])
+def test_compress_every_source_dtype_with_skip_bytes(gpu_pkg, dtype):
+    """container.cpp:51-94: all 10 source dtypes, a skipped prefix, the int64
+    precision-loss flag -- ranks, sizes and errors against the oracle."""
+    base = synth.small("blobs", (24, 20, 16), seed=11)
+    if np.issubdtype(dtype, np.integer):
+        info = np.iinfo(dtype)
+        hi = min(info.max, 2 ** 62) if dtype in (np.int64, np.uint64) else info.max
+        lo = 0 if info.min == 0 else max(info.min, -hi)
+        x = np.round((base - base.min()) / np.ptp(base) * (hi - lo) * 0.9 + lo).astype(dtype)
+    else:
+        x = base.astype(dtype)
+    skip = bytes(range(7))
+    src = gpu_pkg.SourceBuffer(skip + x.tobytes(), gpu_pkg.Dtype(oracle.DTYPES[np.dtype(dtype)]), x.shape,
+                               skip_bytes=len(skip))
+    res = gpu_pkg.compress(src, gpu_pkg.Params(target_re=1e-3))
+    ref = oracle.compress(x, skip_bytes=skip, target_re=1e-3)
+    assert res.ranks == ref.ranks
+    assert res.ingest_precision_loss == ref.precision_loss
+    assert res.original_bytes == ref.original_bytes == x.nbytes
+    assert abs(len(res.container) - len(ref.container)) <= 0.01 * len(ref.container) + 8
+    y = oracle.decompress(res.container, x.shape)
+    xd = x.astype(np.float64)
+    assert np.linalg.norm(y - xd) <= 1.05e-3 * np.linalg.norm(xd)
