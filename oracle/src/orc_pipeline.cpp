@@ -842,15 +842,19 @@ std::vector<T> decompress_tensor(std::span<const u8> cont, Shape& shape_out) {
     R r{cont, 0, "header"};
     const auto mg = r.raw(4);
     if (std::memcmp(mg.data(), "TKC1", 4) != 0) throw Error("container: bad magic");
-    if (r.u8v() != 1) throw Error("container: unsupported format version");
+    const int version = r.u8v();
+    if (version != 1) throw Error("container: unsupported format version " + std::to_string(version));
     Header h;
     h.dt = static_cast<Dtype>(r.u8v());
+    if (static_cast<int>(h.dt) > 9) throw Error("container: unknown source dtype");
     h.f32 = r.u8v() != 0;
     const std::size_t d = r.u8v();
     if (d == 0) throw Error("container: zero tensor order");
-    h.coder = static_cast<Coder>(r.u8v());
+    const int coder = r.u8v();
+    if (coder > 1) throw Error("container: unknown entropy coder id");
+    h.coder = static_cast<Coder>(coder);
     h.method = r.u8v();
-    if (h.method > 2) throw Error("container: unknown vectorization method");
+    if (h.method > 2) throw Error("container: unknown vectorization method id");
     const u8 fl = r.u8v();
     h.zero = fl & 1;
     h.simple = fl & 4;
@@ -863,6 +867,18 @@ std::vector<T> decompress_tensor(std::span<const u8> cont, Shape& shape_out) {
     h.storage.resize(d);
     for (auto& v : h.order) v = r.u8v();
     for (auto& v : h.storage) v = r.u8v();
+    // read_container's checks (container.cpp:338-420)
+    auto is_perm = [d](const Perm& p) {
+        std::vector<char> seen(d, 0);
+        for (auto v : p) {
+            if (v >= d || seen[v]) return false;
+            seen[v] = 1;
+        }
+        return true;
+    };
+    if (!is_perm(h.order) || !is_perm(h.storage)) throw Error("container: corrupt mode permutations");
+    for (std::size_t i = 0; i < d; ++i)
+        if (h.n[i] == 0 || h.r[i] == 0 || h.r[i] > h.n[i]) throw Error("container: corrupt mode sizes or ranks");
     h.k = static_cast<std::int32_t>(r.u32v());
     h.block = r.u64v();
     for (int i = 0; i < 6; ++i) r.f64v();

@@ -166,15 +166,17 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
     Rd r{c, len, 0, "header"};
     if (len < 4 || std::memcmp(c, "TKC1", 4) != 0) throw Error("container: bad magic");
     r.pos = 4;
-    if (r.u8v() != 1) throw Error("container: unsupported format version");
+    const int version = r.u8v();
+    if (version != 1) throw Error("container: unsupported format version " + std::to_string(version));
     DecompressOut out;
     out.dtype = r.u8v();
-    if (out.dtype > 9) throw Error("container: unknown dtype");
+    if (out.dtype > 9) throw Error("container: unknown source dtype");
     out.f32 = r.u8v() != 0;
     const std::size_t d = r.u8v();
     if (d == 0) throw Error("container: zero tensor order");
-    r.u8v();  // coder (each entropy section carries its own coder id)
+    if (r.u8v() > 1) throw Error("container: unknown entropy coder id");  // each section carries its own id too
     const int method = r.u8v();
+    if (method > 2) throw Error("container: unknown vectorization method id");
     const u8 flags = r.u8v();
     const bool zero = flags & 1, simple = flags & 4;
     r.u8v();
@@ -183,6 +185,17 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
     for (auto& v : rk) v = r.u64v();
     for (auto& v : order) v = r.u8v();
     for (auto& v : storage) v = r.u8v();
+    auto is_perm = [&](const std::vector<u64>& p) {
+        std::vector<u8> seen(d, 0);
+        for (auto v : p) {
+            if (v >= d || seen[v]) return false;
+            seen[v] = 1;
+        }
+        return true;
+    };
+    if (!is_perm(order) || !is_perm(storage)) throw Error("container: corrupt mode permutations");
+    for (std::size_t i = 0; i < d; ++i)
+        if (n[i] == 0 || rk[i] == 0 || rk[i] > n[i]) throw Error("container: corrupt mode sizes or ranks");
     const int k = static_cast<std::int32_t>(r.u32v());
     r.u64v();  // block size (each stream carries its own)
     for (int i = 0; i < 6; ++i) r.f64v();

@@ -83,3 +83,32 @@ def test_decompress_errors(gpu_pkg):
         gpu_pkg.decompress(b"XXXX" + c[4:])
     with pytest.raises(gpu_pkg.TucompError, match="container: truncated"):
         gpu_pkg.decompress(c[: len(c) // 2])
+
+
+def _patch(c, off, val):
+    b = bytearray(c)
+    b[off:off + len(val)] = val
+    return bytes(b)
+
+
+@pytest.mark.parametrize("off,val,msg", [
+    (4, b"\x02", "container: unsupported format version 2"),
+    (5, b"\x0c", "container: unknown source dtype"),
+    (8, b"\x02", "container: unknown entropy coder id"),
+    (9, b"\x03", "container: unknown vectorization method id"),
+    (60, b"\x00\x00", "container: corrupt mode permutations"),   # processing order (0,0,..)
+    (63, b"\x03", "container: corrupt mode permutations"),       # storage order entry out of range
+    (36, (0).to_bytes(8, "little"), "container: corrupt mode sizes or ranks"),   # rank 0
+    (36, (17).to_bytes(8, "little"), "container: corrupt mode sizes or ranks"),  # rank > size
+    (12, (0).to_bytes(8, "little"), "container: corrupt mode sizes or ranks"),   # size 0
+])
+def test_decompress_header_validation(gpu_pkg, off, val, msg):
+    """Header checks of read_container (reference container.cpp:338-420), byte
+    offsets per the layout in container.cpp write_container: magic[0:4] version[4]
+    dtype[5] f32[6] d[7] coder[8] method[9] flags[10] pad[11] sizes[12:36]
+    ranks[36:60] processing order[60:63] storage order[63:66] for d=3."""
+    x = synth.small("sin", (16, 16, 16), seed=1)
+    c = gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(target_re=1e-3)).container
+    assert c[7] == 3
+    with pytest.raises(gpu_pkg.TucompError, match=msg):
+        gpu_pkg.decompress(_patch(c, off, val))

@@ -242,3 +242,26 @@ def test_compress_method_round_trip(method):
     assert info.container[9] == method  # header byte 9: vectorize::Method
     y = oracle.decompress(info.container, x.shape)
     assert np.linalg.norm(y - x) / np.linalg.norm(x) <= 1.05e-3
+
+
+@pytest.mark.parametrize("off,val,msg", [
+    (4, b"\x02", "container: unsupported format version 2"),
+    (5, b"\x0c", "container: unknown source dtype"),
+    (8, b"\x02", "container: unknown entropy coder id"),
+    (9, b"\x03", "container: unknown vectorization method id"),
+    (60, b"\x00\x00", "container: corrupt mode permutations"),
+    (63, b"\x03", "container: corrupt mode permutations"),
+    (36, (0).to_bytes(8, "little"), "container: corrupt mode sizes or ranks"),
+    (36, (17).to_bytes(8, "little"), "container: corrupt mode sizes or ranks"),
+])
+def test_oracle_header_validation(off, val, msg):
+    """The oracle's decoder rejects the headers read_container rejects
+    (reference container.cpp:338-420), with the same messages."""
+    x = synth.small("sin", (16, 16, 16), seed=1)
+    c = bytearray(oracle.compress(x, target_re=1e-3).container)
+    c[off:off + len(val)] = val
+    with pytest.raises(oracle.OracleError, match=msg):
+        oracle.decompress(bytes(c), (16, 16, 16))
+    if R.available():  # pin: the reference's read_container gives the same message
+        with pytest.raises(R.RefError, match=msg):
+            R.container_rewrite(bytes(c))
