@@ -41,10 +41,102 @@ struct SourceBuffer {
 
 namespace entropy {
 enum class Coder : std::uint8_t { arithmetic = 0, rans = 1 };
+// entropy.cpp:10-19
+inline const char* coder_name(Coder c) { return c == Coder::arithmetic ? "ac" : "rans"; }
+inline std::optional<Coder> coder_from_name(const std::string& s) {
+    if (s == "ac" || s == "arithmetic") return Coder::arithmetic;
+    if (s == "rans") return Coder::rans;
+    return std::nullopt;
 }
+}  // namespace entropy
 namespace vectorize {
 enum class Method : std::uint8_t { lexicographic = 0, zigzag = 1, zorder = 2 };
+// vectorize.cpp:9-22
+inline const char* method_name(Method m) {
+    static const char* const names[] = {"lex", "zigzag", "zorder"};
+    return static_cast<unsigned>(m) < 3 ? names[static_cast<unsigned>(m)] : "?";
 }
+inline std::optional<Method> method_from_name(const std::string& s) {
+    if (s == "lex" || s == "lexicographic") return Method::lexicographic;
+    if (s == "zigzag") return Method::zigzag;
+    if (s == "zorder") return Method::zorder;
+    return std::nullopt;
+}
+}  // namespace vectorize
+
+namespace container {
+inline constexpr std::uint8_t kFormatVersion = 1;
+// container.cpp:9-47
+inline const char* dtype_name(Dtype t) {
+    static const char* const names[] = {"int8",  "uint8",  "int16",  "uint16",  "int32",
+                                        "uint32", "int64", "uint64", "float32", "float64"};
+    return static_cast<unsigned>(t) < 10 ? names[static_cast<unsigned>(t)] : "?";
+}
+inline std::size_t dtype_size(Dtype t) {
+    static const std::size_t sizes[] = {1, 1, 2, 2, 4, 4, 8, 8, 4, 8};
+    return static_cast<unsigned>(t) < 10 ? sizes[static_cast<unsigned>(t)] : 0;
+}
+inline std::optional<Dtype> dtype_from_name(const std::string& s) {
+    for (unsigned i = 0; i < 10; ++i)
+        if (s == dtype_name(static_cast<Dtype>(i))) return static_cast<Dtype>(i);
+    return std::nullopt;
+}
+
+// container.hpp:59-82 (orders 0-based)
+struct Header {
+    Dtype source_dtype = Dtype::float64;
+    bool internal_float32 = false;
+    std::vector<std::uint64_t> mode_sizes, ranks;
+    ModePermutation processing_order, storage_order;
+    vectorize::Method method = vectorize::Method::lexicographic;
+    entropy::Coder coder = entropy::Coder::arithmetic;
+    bool zero_flag = false, split_planes = true, simple_weights = false;
+    std::int32_t core_scale_exponent = 0;
+    std::uint64_t block_size = 0;
+    double rtmss = 0.5, target_sse = 0, norm_sq = 0, truncation_sse = 0, core_quant_sse = 0, estimate_sse = 0;
+
+    std::size_t order() const { return mode_sizes.size(); }
+    std::uint64_t element_count() const {
+        std::uint64_t n = 1;
+        for (auto v : mode_sizes) n *= v;
+        return n;
+    }
+};
+struct ParsedContainer {  // the header part of container.hpp's ParsedContainer
+    Header header;
+};
+
+// container::read_container (container.cpp:338-420): header plus the structural
+// checks of every section; host only.
+inline ParsedContainer read_container(std::span<const std::uint8_t> bytes) {
+    tcb_container_header c;
+    if (tcb_read_container_header(bytes.data(), bytes.size(), &c) != 0) throw Error(tcb_last_error());
+    ParsedContainer p;
+    Header& h = p.header;
+    h.source_dtype = static_cast<Dtype>(c.source_dtype);
+    h.internal_float32 = c.internal_float32 != 0;
+    for (int i = 0; i < c.d; ++i) {
+        h.mode_sizes.push_back(c.mode_sizes[i]);
+        h.ranks.push_back(c.ranks[i]);
+        h.processing_order.push_back(c.processing_order[i]);
+        h.storage_order.push_back(c.storage_order[i]);
+    }
+    h.method = static_cast<vectorize::Method>(c.method);
+    h.coder = static_cast<entropy::Coder>(c.coder);
+    h.zero_flag = c.zero_flag != 0;
+    h.split_planes = c.split_planes != 0;
+    h.simple_weights = c.simple_weights != 0;
+    h.core_scale_exponent = c.core_scale_exponent;
+    h.block_size = c.block_size;
+    h.rtmss = c.rtmss;
+    h.target_sse = c.target_sse;
+    h.norm_sq = c.norm_sq;
+    h.truncation_sse = c.truncation_sse;
+    h.core_quant_sse = c.core_quant_sse;
+    h.estimate_sse = c.estimate_sse;
+    return p;
+}
+}  // namespace container
 namespace sthosvd {
 enum class SvdBackend { automatic, gram, direct };
 }
@@ -179,6 +271,34 @@ inline DecompressResult decompress(std::span<const std::uint8_t> container_bytes
     o.shape.assign(r.shape, r.shape + r.d);
     o.total_ms = r.total_ms;
     return o;
+}
+
+// pipeline::decompress_tensor<T> (pipeline.hpp:70-71): the reconstruction in the
+// original axis order, row-major.  The device computes in fp64; T = float rounds.
+template <class T>
+inline std::vector<T> decompress_tensor(std::span<const std::uint8_t> container_bytes, int threads = 1) {
+    (void)threads;
+    double* p = nullptr;
+    std::uint64_t n = 0, shape[8];
+    int d = 0;
+    if (tcb_decompress_tensor_f64(container_bytes.data(), container_bytes.size(), &p, &n, shape, &d) != 0)
+        throw Error(tcb_last_error());
+    std::vector<T> out(p, p + n);
+    tcb_free(p);
+    return out;
+}
+
+// B200 extension: the CLI's measure_error (tucomp_main.cpp:121-135) with the
+// ingest, decompress and SSE on the device; returns the SSE.
+inline double measure_sse(const container::SourceBuffer& src, std::span<const std::uint8_t> container_bytes,
+                          bool internal_float32) {
+    std::vector<std::uint64_t> shape(src.shape.begin(), src.shape.end());
+    double sse = 0;
+    if (tcb_measure_error(src.bytes.data(), src.bytes.size(), static_cast<int>(src.dtype), shape.data(),
+                          static_cast<int>(shape.size()), src.skip_bytes, internal_float32 ? 1 : 0,
+                          container_bytes.data(), container_bytes.size(), &sse) != 0)
+        throw Error(tcb_last_error());
+    return sse;
 }
 
 }  // namespace pipeline

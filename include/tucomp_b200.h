@@ -98,6 +98,26 @@ int tcb_decompress(const uint8_t* container, uint64_t len, int threads, tcb_deco
 int tcb_decompress_tensor_f64(const uint8_t* container, uint64_t len, double** out, uint64_t* count,
                               uint64_t* shape, int* d);
 
+/* The CLI's measure_error (tools/tucomp_main.cpp:121-135): decompress `container`
+ * on the device, ingest the source bytes (same meaning as tcb_compress) on the
+ * device and return sse_between (tensor.cpp:147-164) of the two; internal_float32
+ * compares float-rounded values as the reference's float tensors do. */
+int tcb_measure_error(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d, uint64_t skip,
+                      int internal_float32, const uint8_t* container, uint64_t len, double* sse);
+
+/* container::Header (container.hpp:59-82) as read by container::read_container
+ * (container.cpp:338-420): every header and section-structure check, host only
+ * (no device work; the CLI's `info`, tucomp_main.cpp:196-228). Orders are 0-based. */
+typedef struct tcb_container_header {
+    int version, source_dtype, internal_float32, d, coder, method;
+    int zero_flag, split_planes, simple_weights;
+    uint64_t mode_sizes[8], ranks[8], processing_order[8], storage_order[8];
+    int core_scale_exponent;
+    uint64_t block_size;
+    double rtmss, target_sse, norm_sq, truncation_sse, core_quant_sse, estimate_sse;
+} tcb_container_header;
+int tcb_read_container_header(const uint8_t* container, uint64_t len, tcb_container_header* out);
+
 void tcb_free(void* p);
 const char* tcb_last_error(void);
 uint64_t tcb_kernel_launches(void);

@@ -251,6 +251,19 @@ def compress_device(ptr: int, nbytes: int, dtype: Dtype, shape: Sequence[int], p
     return _result(res)
 
 
+def measure_error(src: SourceBuffer, container: bytes, internal_float32: bool = False) -> float:
+    """The CLI's measure_error (tools/tucomp_main.cpp:121-135) on the device:
+    sse_between(ingest(src), decompress_tensor(container)) (tensor.cpp:147-164)."""
+    shape = np.asarray(list(src.shape), np.uint64)
+    buf = np.frombuffer(src.bytes, np.uint8) if len(src.bytes) else np.zeros(1, np.uint8)
+    cb = np.frombuffer(container, np.uint8) if len(container) else np.zeros(1, np.uint8)
+    sse = C.c_double()
+    _check(lib().tcb_measure_error(_p(buf), C.c_uint64(len(src.bytes)), int(src.dtype), _p(shape), len(shape),
+                                   C.c_uint64(src.skip_bytes), int(bool(internal_float32)), _p(cb),
+                                   C.c_uint64(len(container)), C.byref(sse)))
+    return float(sse.value)
+
+
 class _CDecompress(C.Structure):  # tcb_decompress_result
     _fields_ = [("bytes", C.POINTER(C.c_uint8)), ("nbytes", C.c_uint64), ("dtype", C.c_int), ("d", C.c_int),
                 ("shape", C.c_uint64 * 8), ("total_ms", C.c_double)]
@@ -292,6 +305,59 @@ def decompress_tensor(container: bytes) -> np.ndarray:
     out = np.ctypeslib.as_array(ptr, shape=(n,)).copy() if n else np.zeros(0)
     lib().tcb_free(C.cast(ptr, C.c_void_p))
     return out.reshape(tuple(int(shape[i]) for i in range(d.value)))
+
+
+class _CHeader(C.Structure):  # tcb_container_header
+    _fields_ = [(n, C.c_int) for n in ("version", "source_dtype", "internal_float32", "d", "coder", "method",
+                                       "zero_flag", "split_planes", "simple_weights")] + \
+               [(n, C.c_uint64 * 8) for n in ("mode_sizes", "ranks", "processing_order", "storage_order")] + \
+               [("core_scale_exponent", C.c_int), ("block_size", C.c_uint64)] + \
+               [(n, C.c_double) for n in ("rtmss", "target_sse", "norm_sq", "truncation_sse", "core_quant_sse",
+                                          "estimate_sse")]
+
+
+@dataclass
+class Header:  # container::Header (container.hpp:59-82); orders 0-based
+    version: int
+    source_dtype: Dtype
+    internal_float32: bool
+    mode_sizes: tuple
+    ranks: tuple
+    processing_order: tuple
+    storage_order: tuple
+    method: int
+    coder: int
+    zero_flag: bool
+    split_planes: bool
+    simple_weights: bool
+    core_scale_exponent: int
+    block_size: int
+    rtmss: float
+    target_sse: float
+    norm_sq: float
+    truncation_sse: float
+    core_quant_sse: float
+    estimate_sse: float
+
+    def order(self) -> int:
+        return len(self.mode_sizes)
+
+    def element_count(self) -> int:
+        return int(np.prod(self.mode_sizes, dtype=object))
+
+
+def read_container(container: bytes) -> Header:
+    """container::read_container (container.cpp:338-420): the header, after every
+    header and section-structure check.  Host only (no device work)."""
+    buf = np.frombuffer(container, np.uint8) if len(container) else np.zeros(1, np.uint8)
+    h = _CHeader()
+    _check(lib().tcb_read_container_header(_p(buf), C.c_uint64(len(container)), C.byref(h)))
+    d = h.d
+    t = lambda a: tuple(int(a[i]) for i in range(d))  # noqa: E731
+    return Header(h.version, Dtype(h.source_dtype), bool(h.internal_float32), t(h.mode_sizes), t(h.ranks),
+                  t(h.processing_order), t(h.storage_order), h.method, h.coder, bool(h.zero_flag),
+                  bool(h.split_planes), bool(h.simple_weights), h.core_scale_exponent, int(h.block_size), h.rtmss,
+                  h.target_sse, h.norm_sq, h.truncation_sse, h.core_quant_sse, h.estimate_sse)
 
 
 # ---------------------------------------------------------------- lower-level ops
@@ -406,7 +472,7 @@ def encode_factor(u, dead, slice_norms, coder=0, simple=False, core_step_log2=0,
                 plane=plane.value)
 
 
-EXPORTED = ("tcb_compress", "tcb_compress_device", "tcb_decompress", "tcb_decompress_tensor_f64",
+EXPORTED = ("tcb_compress", "tcb_compress_device", "tcb_decompress", "tcb_decompress_tensor_f64", "tcb_read_container_header", "tcb_measure_error",
             "tcb_default_params", "tcb_free", "tcb_last_error",
             "tcb_kernel_launches", "tcb_sthosvd_f64", "tcb_gram_f64", "tcb_ttm_f64", "tcb_eig_f64",
             "tcb_quantize_f64", "tcb_encode", "tcb_encode_symbols", "tcb_encode_factor_f64")

@@ -261,6 +261,26 @@ int tcb_compress_device(const void* device_bytes, uint64_t nbytes, int dtype, co
     });
 }
 
+int tcb_measure_error(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d, uint64_t skip,
+                      int internal_float32, const uint8_t* container, uint64_t len, double* sse) {
+    return guard([&] {
+        std::vector<u64> sh(shape, shape + d);
+        u64 n = 1;
+        for (auto v : sh) n *= v;
+        const u64 expect = skip + n * dtype_bytes(dtype);
+        if (nbytes != expect)
+            throw Error("ingest: buffer holds " + std::to_string(nbytes) + " bytes, expected " + std::to_string(expect));
+        Stream st;
+        const auto t = decompress_device(container, len, st.s);
+        if (t.shape != sh) throw Error("sse_between: shape mismatch");
+        DevBuf<u8> dev(nbytes - skip + 16, st.s);
+        dev.upload(bytes + skip, nbytes - skip);
+        DevBuf<double> x(std::max<u64>(n, 1), st.s);
+        ingest_cast(dev.p, dtype, n, x.p, st.s);
+        *sse = n ? sse_between(x.p, t.x.p, n, internal_float32 != 0, st.s) : 0.0;
+    });
+}
+
 int tcb_decompress(const uint8_t* container, uint64_t len, int threads, tcb_decompress_result* out) {
     (void)threads;  // the device path has no host worker count
     return guard([&] {
@@ -291,6 +311,37 @@ int tcb_decompress_tensor_f64(const uint8_t* container, uint64_t len, double** o
         *count = total;
         *d = static_cast<int>(t.shape.size());
         for (std::size_t i = 0; i < t.shape.size() && i < 8; ++i) shape[i] = t.shape[i];
+    });
+}
+
+int tcb_read_container_header(const uint8_t* container, uint64_t len, tcb_container_header* out) {
+    return guard([&] {
+        const auto h = read_container_header(container, len);
+        if (h.n.size() > 8) throw Error("container: order above 8 is not supported by this interface");
+        *out = tcb_container_header{};
+        out->version = h.version;
+        out->source_dtype = h.dtype;
+        out->internal_float32 = h.f32;
+        out->d = static_cast<int>(h.n.size());
+        out->coder = h.coder;
+        out->method = h.method;
+        out->zero_flag = h.zero;
+        out->split_planes = h.split;
+        out->simple_weights = h.simple;
+        for (std::size_t i = 0; i < h.n.size(); ++i) {
+            out->mode_sizes[i] = h.n[i];
+            out->ranks[i] = h.rk[i];
+            out->processing_order[i] = h.order[i];
+            out->storage_order[i] = h.storage[i];
+        }
+        out->core_scale_exponent = h.k;
+        out->block_size = h.block;
+        out->rtmss = h.rtmss;
+        out->target_sse = h.target_sse;
+        out->norm_sq = h.norm_sq;
+        out->truncation_sse = h.trunc_sse;
+        out->core_quant_sse = h.cq_sse;
+        out->estimate_sse = h.est_sse;
     });
 }
 

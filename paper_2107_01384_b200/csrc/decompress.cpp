@@ -160,31 +160,35 @@ struct FactorMeta {
 
 }  // namespace
 
-DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
-    const auto t0 = std::chrono::steady_clock::now();
-    HostTrace ht("decompress");
+ContainerHeader parse_header(const u8* c, u64 len, u64* end) {
     Rd r{c, len, 0, "header"};
     if (len < 4 || std::memcmp(c, "TKC1", 4) != 0) throw Error("container: bad magic");
     r.pos = 4;
-    const int version = r.u8v();
-    if (version != 1) throw Error("container: unsupported format version " + std::to_string(version));
-    DecompressOut out;
-    out.dtype = r.u8v();
-    if (out.dtype > 9) throw Error("container: unknown source dtype");
-    out.f32 = r.u8v() != 0;
+    ContainerHeader h;
+    h.version = r.u8v();
+    if (h.version != 1) throw Error("container: unsupported format version " + std::to_string(h.version));
+    h.dtype = r.u8v();
+    if (h.dtype > 9) throw Error("container: unknown source dtype");
+    h.f32 = r.u8v() != 0;
     const std::size_t d = r.u8v();
     if (d == 0) throw Error("container: zero tensor order");
-    if (r.u8v() > 1) throw Error("container: unknown entropy coder id");  // each section carries its own id too
-    const int method = r.u8v();
-    if (method > 2) throw Error("container: unknown vectorization method id");
+    h.coder = r.u8v();  // each entropy section carries its own id too
+    if (h.coder > 1) throw Error("container: unknown entropy coder id");
+    h.method = r.u8v();
+    if (h.method > 2) throw Error("container: unknown vectorization method id");
     const u8 flags = r.u8v();
-    const bool zero = flags & 1, simple = flags & 4;
+    h.zero = flags & 1;
+    h.split = flags & 2;
+    h.simple = flags & 4;
     r.u8v();
-    std::vector<u64> n(d), rk(d), order(d), storage(d);
-    for (auto& v : n) v = r.u64v();
-    for (auto& v : rk) v = r.u64v();
-    for (auto& v : order) v = r.u8v();
-    for (auto& v : storage) v = r.u8v();
+    h.n.resize(d);
+    h.rk.resize(d);
+    h.order.resize(d);
+    h.storage.resize(d);
+    for (auto& v : h.n) v = r.u64v();
+    for (auto& v : h.rk) v = r.u64v();
+    for (auto& v : h.order) v = r.u8v();
+    for (auto& v : h.storage) v = r.u8v();
     auto is_perm = [&](const std::vector<u64>& p) {
         std::vector<u8> seen(d, 0);
         for (auto v : p) {
@@ -193,12 +197,89 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
         }
         return true;
     };
-    if (!is_perm(order) || !is_perm(storage)) throw Error("container: corrupt mode permutations");
+    if (!is_perm(h.order) || !is_perm(h.storage)) throw Error("container: corrupt mode permutations");
     for (std::size_t i = 0; i < d; ++i)
-        if (n[i] == 0 || rk[i] == 0 || rk[i] > n[i]) throw Error("container: corrupt mode sizes or ranks");
-    const int k = static_cast<std::int32_t>(r.u32v());
-    r.u64v();  // block size (each stream carries its own)
-    for (int i = 0; i < 6; ++i) r.f64v();
+        if (h.n[i] == 0 || h.rk[i] == 0 || h.rk[i] > h.n[i]) throw Error("container: corrupt mode sizes or ranks");
+    h.k = static_cast<std::int32_t>(r.u32v());
+    h.block = r.u64v();
+    h.rtmss = r.f64v();
+    h.target_sse = r.f64v();
+    h.norm_sq = r.f64v();
+    h.trunc_sse = r.f64v();
+    h.cq_sse = r.f64v();
+    h.est_sse = r.f64v();
+    *end = r.pos;
+    return h;
+}
+
+namespace {
+
+struct Sections {
+    std::vector<FactorMeta> fm;
+    std::vector<StreamParse> sp;  // factor streams, then the core stream
+};
+
+// factor and core sections (container.cpp read_container's section loop)
+Sections parse_sections(const u8* c, u64 len, u64 pos, const ContainerHeader& h) {
+    Rd r{c, len, pos, "header"};
+    const std::size_t d = h.n.size();
+    Sections o;
+    o.fm.resize(d);
+    for (std::size_t i = 0; i < d; ++i) {
+        const u64 flen = r.u64v();
+        const u64 at = r.skip(flen);
+        Rd fr{c + at, flen, 0, "factor " + std::to_string(i + 1)};
+        auto& f = o.fm[i];
+        f.dead.assign(h.rk[i], 0);
+        for (u64 j = 0; j < h.rk[i]; j += 8) {
+            const u8 b = fr.u8v();
+            for (u64 q = 0; q < 8 && j + q < h.rk[i]; ++q) f.dead[j + q] = (b >> q) & 1;
+        }
+        f.sn.resize(h.rk[i]);
+        for (auto& v : f.sn) v = fr.f64v();
+        f.k = static_cast<std::int32_t>(fr.u32v());
+        f.count = fr.u64v();
+        o.sp.push_back(get_stream(fr, at));
+        if (o.sp.back().count != f.count) throw Error("container: factor stream length mismatch");
+    }
+    {
+        const u64 clen = r.u64v();
+        const u64 at = r.skip(clen);
+        Rd cr{c + at, clen, 0, "core"};
+        o.sp.push_back(get_stream(cr, at));
+    }
+    std::vector<u64> cp(d), cs(d);
+    for (std::size_t j = 0; j < d; ++j) cp[j] = h.rk[h.order[j]];
+    for (std::size_t a = 0; a < d; ++a) cs[a] = cp[h.storage[a]];
+    if (o.sp.back().count != prod(cs)) throw Error("container: core length does not match ranks");
+    return o;
+}
+
+}  // namespace
+
+ContainerHeader read_container_header(const u8* c, u64 len) {
+    u64 pos = 0;
+    ContainerHeader h = parse_header(c, len, &pos);
+    if (!h.zero) parse_sections(c, len, pos, h);
+    return h;
+}
+
+DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
+    const auto t0 = std::chrono::steady_clock::now();
+    HostTrace ht("decompress");
+    u64 hpos = 0;
+    const ContainerHeader h = parse_header(c, len, &hpos);
+    DecompressOut out;
+    out.dtype = h.dtype;
+    out.f32 = h.f32;
+    const std::size_t d = h.n.size();
+    const bool zero = h.zero, simple = h.simple;
+    const int method = h.method;
+    const int k = h.k;
+    const auto& n = h.n;
+    const auto& rk = h.rk;
+    const auto& order = h.order;
+    const auto& storage = h.storage;
     out.shape = n;
     const u64 total = prod(n);
     out.x = DevBuf<double>(total, s);
@@ -207,36 +288,12 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
         out.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         return out;
     }
-    // ---- parse factor and core sections
-    std::vector<FactorMeta> fm(d);
-    std::vector<StreamParse> sp;
-    for (std::size_t i = 0; i < d; ++i) {
-        const u64 flen = r.u64v();
-        const u64 at = r.skip(flen);
-        Rd fr{c + at, flen, 0, "factor " + std::to_string(i + 1)};
-        auto& f = fm[i];
-        f.dead.assign(rk[i], 0);
-        for (u64 j = 0; j < rk[i]; j += 8) {
-            const u8 b = fr.u8v();
-            for (u64 q = 0; q < 8 && j + q < rk[i]; ++q) f.dead[j + q] = (b >> q) & 1;
-        }
-        f.sn.resize(rk[i]);
-        for (auto& v : f.sn) v = fr.f64v();
-        f.k = static_cast<std::int32_t>(fr.u32v());
-        f.count = fr.u64v();
-        sp.push_back(get_stream(fr, at));
-        if (sp.back().count != f.count) throw Error("container: factor stream length mismatch");
-    }
-    {
-        const u64 clen = r.u64v();
-        const u64 at = r.skip(clen);
-        Rd cr{c + at, clen, 0, "core"};
-        sp.push_back(get_stream(cr, at));
-    }
+    Sections secs = parse_sections(c, len, hpos, h);
+    auto& fm = secs.fm;
+    auto& sp = secs.sp;
     std::vector<u64> cp(d), cs(d);
     for (std::size_t j = 0; j < d; ++j) cp[j] = rk[order[j]];
     for (std::size_t a = 0; a < d; ++a) cs[a] = cp[storage[a]];
-    if (sp.back().count != prod(cs)) throw Error("container: core length does not match ranks");
     // ---- descriptors (decode_stream's checks, core_codec.cpp:421-440)
     std::vector<DecSection> sec;
     std::vector<DecStream> ds(sp.size());

@@ -15,6 +15,20 @@ struct DecompressOut {
     double ms = 0.0;
 };
 
+// read_container's header (container.hpp Header; container.cpp:338-420), host side
+struct ContainerHeader {
+    int version = 1, dtype = 9, coder = 0, method = 0;
+    bool f32 = false, zero = false, split = true, simple = false;
+    std::vector<u64> n, rk, order, storage;  // order/storage 0-based
+    int k = 0;                               // core scale exponent
+    u64 block = 0;
+    double rtmss = 0, target_sse = 0, norm_sq = 0, trunc_sse = 0, cq_sse = 0, est_sse = 0;
+};
+// header fields only; *end = offset of the first section
+ContainerHeader parse_header(const u8* container, u64 len, u64* end);
+// header plus a structural walk of every section (read_container's validation)
+ContainerHeader read_container_header(const u8* container, u64 len);
+
 // container bytes on the host; the result stays on the device
 DecompressOut decompress_device(const u8* container, u64 len, cudaStream_t s);
 // emit (container.cpp:98-140): the source dtype's bytes, on the host

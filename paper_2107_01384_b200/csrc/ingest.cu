@@ -302,6 +302,49 @@ void ingest_cast_f32(const void* src, int dtype, u64 n, float* dst, cudaStream_t
 double sum_squares(const double* x, u64 n, bool* finite, cudaStream_t s) { return sumsq_impl(x, n, finite, s); }
 double sum_squares(const float* x, u64 n, bool* finite, cudaStream_t s) { return sumsq_impl(x, n, finite, s); }
 
+// sse_between (tensor.cpp:147-164) of the ingested source and a reconstruction;
+// with f32 both sides are rounded to float first (the reference's float tensors).
+template <bool kF32>
+__global__ void sse_stage1(const double* __restrict__ a, const double* __restrict__ b, u64 n,
+                           double* __restrict__ part) {
+    __shared__ double sh[kRedThreads / 32];
+    double acc = 0.0;
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        double x = __ldcs(a + i), y = __ldcs(b + i);
+        if (kF32) {
+            x = static_cast<double>(static_cast<float>(x));
+            y = static_cast<double>(static_cast<float>(y));
+        }
+        const double e = x - y;
+        acc = fma(e, e, acc);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) t += sh[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+double sse_between(const double* a, const double* b, u64 n, bool f32, cudaStream_t s) {
+    const int grid = sm_count() * 4;
+    DevBuf<double> part(grid + 1, s);
+    if (f32)
+        sse_stage1<true><<<grid, kRedThreads, 0, s>>>(a, b, n, part.p);
+    else
+        sse_stage1<false><<<grid, kRedThreads, 0, s>>>(a, b, n, part.p);
+    sum_stage2<<<1, kRedThreads, 0, s>>>(part.p, grid, part.p + grid);
+    count_launch(2);
+    TCB_LAUNCH();
+    double r = 0;
+    TCB_CUDA(cudaMemcpyAsync(&r, part.p + grid, sizeof(double), cudaMemcpyDeviceToHost, s));
+    TCB_CUDA(cudaStreamSynchronize(s));
+    return r;
+}
+
 double max_abs(const double* x, u64 n, cudaStream_t s) {
     ProfScope prof_scope(kSum, s);
     const int grid = sm_count() * 4;

@@ -18,6 +18,8 @@ void permute_axes(const T* src, T* dst, const std::vector<u64>& shape, const std
                   cudaStream_t s);
 // int64/uint64 sources whose magnitude exceeds 2^53 (container.cpp:60-63)
 bool ingest_precision_loss(const void* src, int dtype, u64 n, cudaStream_t s);
+// sum of (a_i - b_i)^2 (tensor.cpp:147-164); f32 rounds both sides to float first
+double sse_between(const double* a, const double* b, u64 n, bool f32, cudaStream_t s);
 // Exact max |x| (kernels_avx2.cpp:40-66 is order-independent, so exact on any tree).
 double max_abs(const double* x, u64 n, cudaStream_t s);
 
