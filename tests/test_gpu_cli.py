@@ -71,10 +71,11 @@ def test_cli_compress_matches_api(tmp_path, gpu_pkg, dtype, flags, params):
     if params.get("internal_float32"):
         xd, y = xd.astype(np.float32).astype(np.float64), y.astype(np.float32).astype(np.float64)
     sse = float(((y - xd) ** 2).sum())
-    tol = 1e-3 if params.get("internal_float32") else 1e-6  # float32 decoder vs fp64 device decode
+    # report lines print 6 significant digits; float32 decoder vs fp64 device decode
+    tol = 1e-3 if params.get("internal_float32") else 1e-5
     assert abs(m["achieved_sse"] - sse) <= tol * sse + 1e-300
     assert m["achieved_re"] <= params["target_re"] * 1.05
-    assert abs(m["estimate_sse"] - api.estimate.total()) <= 1e-6 * api.estimate.total()
+    assert abs(m["estimate_sse"] - api.estimate.total()) <= 1e-5 * api.estimate.total()
     # decompress through the CLI == pipeline::decompress
     rec = tmp_path / "out.raw"
     text = run("decompress", "-i", out, "-o", rec)
