@@ -41,8 +41,7 @@ def test_compress_is_deterministic(gpu_pkg):
      dict(target_re=1e-3, storage_order=(2, 0, 1), block_size=1024, split_planes=False)),
     (np.int16, ["--simple-factor-weights", "--vectorization", "zigzag", "--rtmss", "0.3"],
      dict(target_re=1e-3, simple_factor_weights=True, method=1, rtmss=0.3)),
-    (np.float32, ["--internal-float32", "--mode-order", "2,3,1"], dict(target_re=1e-3, internal_float32=True,
-                                                                         mode_order=(1, 2, 0))),
+    (np.float32, ["--mode-order", "2,3,1"], dict(target_re=1e-3, mode_order=(1, 2, 0))),
 ])
 def test_cli_compress_matches_api(tmp_path, gpu_pkg, dtype, flags, params):
     shape = (36, 28, 20)
@@ -66,13 +65,11 @@ def test_cli_compress_matches_api(tmp_path, gpu_pkg, dtype, flags, params):
     m = _machine(text)
     assert m["bytes"] == len(cont)
     # measured error: device ingest + decompress + SSE vs the oracle's decoder in numpy
-    y = oracle.decompress(cont, shape, internal_float32=params.get("internal_float32", False))
+    y = oracle.decompress(cont, shape)
     xd = x.astype(np.float64)
-    if params.get("internal_float32"):
-        xd, y = xd.astype(np.float32).astype(np.float64), y.astype(np.float32).astype(np.float64)
     sse = float(((y - xd) ** 2).sum())
-    # report lines print 6 significant digits; float32 decoder vs fp64 device decode
-    tol = 1e-3 if params.get("internal_float32") else 1e-5
+    # report lines print 6 significant digits
+    tol = 1e-5
     assert abs(m["achieved_sse"] - sse) <= tol * sse + 1e-300
     assert m["achieved_re"] <= params["target_re"] * 1.05
     assert abs(m["estimate_sse"] - api.estimate.total()) <= 1e-5 * api.estimate.total()
@@ -81,6 +78,20 @@ def test_cli_compress_matches_api(tmp_path, gpu_pkg, dtype, flags, params):
     text = run("decompress", "-i", out, "-o", rec)
     assert text.startswith(f"wrote {x.nbytes} bytes ({np.dtype(dtype).name}, shape {' '.join(map(str, shape))})")
     assert rec.read_bytes() == gpu_pkg.decompress(cont).bytes
+
+
+def test_cli_internal_float32_fails_like_api(tmp_path, gpu_pkg):
+    """internal_float32 throws in factorize exactly where the reference throws
+    (DESIGN.md §0); the CLI reports the same text with exit code 1."""
+    x = synth.small("sin", (20, 16, 12), seed=2).astype(np.float32)
+    raw = tmp_path / "in.raw"
+    raw.write_bytes(x.tobytes())
+    with pytest.raises(gpu_pkg.TucompError) as ei:
+        gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(target_re=1e-3, internal_float32=True))
+    r = subprocess.run([EXE, "compress", "-i", raw, "--shape", "20,16,12", "--dtype", "float32", "-o",
+                        tmp_path / "c.tkc", "--target-re", "1e-3", "--internal-float32"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 1 and r.stderr.strip() == f"error: {ei.value}"
 
 
 def test_cli_no_verify_and_target_sse(tmp_path, gpu_pkg):
