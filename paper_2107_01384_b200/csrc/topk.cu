@@ -76,140 +76,273 @@ __global__ void tk_random(double* __restrict__ W, int n, int p) {
     if (idx < n * p) W[idx] = tk_hash_unit(static_cast<unsigned>(idx / p) + 7u, static_cast<unsigned>(idx % p) + 1u);
 }
 
-// Z (n x p, row-major) = G (n x n, row-major) Q (n x p, row-major).  A CTA owns
-// 8 rows of Z: it stages those 8 rows of G and all of Q in shared memory
-// (coalesced), then thread (row, col) runs its dot product from shared memory.
-__global__ void __launch_bounds__(256) tk_gq(const double* __restrict__ G, const double* __restrict__ Q, int n, int p,
-                                            double* __restrict__ Z) {
-    extern __shared__ double sm_gq[];
-    double* Gs = sm_gq;       // 8 x n
-    double* Qs = Gs + 8 * n;  // n x p
-    const int r0 = blockIdx.x * 8;
-    const int nr = min(8, n - r0);
-    for (int idx = threadIdx.x; idx < nr * n; idx += blockDim.x) Gs[idx] = G[static_cast<size_t>(r0) * n + idx];
-    for (int idx = threadIdx.x; idx < n * p; idx += blockDim.x) Qs[idx] = Q[idx];
-    __syncthreads();
-    for (int o = threadIdx.x; o < nr * p; o += blockDim.x) {
-        const int r = o / p, c = o % p;
-        const double* g = Gs + r * n;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int k = 0;
-        for (; k + 4 <= n; k += 4) {
-            a0 = fma(g[k], Qs[k * p + c], a0);
-            a1 = fma(g[k + 1], Qs[(k + 1) * p + c], a1);
-            a2 = fma(g[k + 2], Qs[(k + 2) * p + c], a2);
-            a3 = fma(g[k + 3], Qs[(k + 3) * p + c], a3);
+// Shared-memory row stride (doubles) of every n x 32 panel and 32 x 32 matrix:
+// 36 = 4 (mod 16), so the DMMA fragment reads below (lane (r, q) = (lane / 4,
+// lane % 4) reading element [q][r] or [r][q] of an 8 x 4 / 4 x 8 block) hit 16
+// distinct 8-byte banks in each half-warp.
+constexpr int kP = 32, kS = 36;
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_wait_all() {
+    asm volatile("cp.async.commit_group;\n");
+    asm volatile("cp.async.wait_group 0;\n");
+}
+
+// C (32 x 32, stride kS) = A^T B over rows [0, nr) (nr % 8 == 0) of two staged
+// panels, on DMMA: warp w owns the tiles (w / 2, 2 (w % 2) + {0, 1}); two k
+// chains per tile for ILP.  diag_add is added to C's diagonal.  8 warps.
+__device__ __forceinline__ void tk_atb(const double* A, const double* B, int nr, double* C, double diag_add) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & 3, r = lane >> 2;
+    const int mb = (warp >> 1) * 8, nb = (warp & 1) * 16;
+    double c[2][2][2] = {};
+    for (int k = 0; k < nr; k += 8) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int kr = (k + 4 * h + q) * kS;
+            const double a = A[kr + mb + r];
+            const double b0 = B[kr + nb + r], b1 = B[kr + nb + 8 + r];
+            dmma(c[h][0][0], c[h][0][1], a, b0);
+            dmma(c[h][1][0], c[h][1][1], a, b1);
         }
-        for (; k < n; ++k) a0 = fma(g[k], Qs[k * p + c], a0);
-        Z[static_cast<size_t>(r0 + r) * p + c] = (a0 + a1) + (a2 + a3);
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int row = mb + r, col = nb + 8 * t + 2 * q;
+        C[row * kS + col] = (c[0][t][0] + c[1][t][0]) + (row == col ? diag_add : 0.0);
+        C[row * kS + col + 1] = (c[0][t][1] + c[1][t][1]) + (row == col + 1 ? diag_add : 0.0);
     }
 }
 
-// Block-parallel Cholesky of C (32 x 33 shared; p <= 32 real columns, the rest
-// made identity): C = R^T R, R (upper) written to a separate 32 x 33 array so
-// one barrier per column suffices (the trailing update reads the unscaled row
-// k of C while row k of R is written).  Returns true if a pivot is not positive.
-__device__ bool tk_block_chol(double* C, double* R, int p, int* bad_s) {
-    constexpr int P = 32, PP = 33;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int e = tid; e < P * P; e += nt) {
-        const int i = e >> 5, j = e & 31;
-        if (j >= p) C[i * PP + j] = i == j ? 1.0 : 0.0;
-        R[i * PP + j] = 0.0;
+// Z (n x p, row-major) = G (n x n, row-major) W (n x p, row-major) on DMMA.  A
+// CTA owns 8 rows of Z; its 8 warps split the k range, each accumulating the
+// 8 x 32 block over its k slice from the staged G rows and W, and the 8
+// partials are summed in a fixed order.
+constexpr int kGqThreads = 256;
+__global__ void __launch_bounds__(kGqThreads) tk_gq(const double* __restrict__ G, const double* __restrict__ W, int n,
+                                                   int p, double* __restrict__ Z) {
+    extern __shared__ __align__(16) double sm_gq[];
+    const int nk = (n + 31) & ~31;   // k padded to 8 warps x 4
+    const int gs = ((nk + 15) & ~15) + 4;  // G-row stride, = 4 (mod 16)
+    double* Gs = sm_gq;                // 8 x gs
+    double* Ws = Gs + 8 * gs;          // nk x kS
+    double* part = Ws + nk * kS;       // 8 warps x 8 x kS
+    const int r0 = blockIdx.x * 8;
+    const int nr = min(8, n - r0);
+    for (int e = threadIdx.x; e < 8 * nk; e += blockDim.x) {
+        const int i = e / nk, k = e % nk;
+        if (i < nr && k < n)
+            cp_async8(Gs + i * gs + k, G + static_cast<size_t>(r0 + i) * n + k);
+        else
+            Gs[i * gs + k] = 0.0;
     }
-    if (tid == 0) *bad_s = 0;
+    for (int e = threadIdx.x; e < nk * kP; e += blockDim.x) {
+        const int i = e >> 5, j = e & 31;
+        if (i < n && j < p)
+            cp_async8(Ws + i * kS + j, W + static_cast<size_t>(i) * p + j);
+        else
+            Ws[i * kS + j] = 0.0;
+    }
+    cp_wait_all();
     __syncthreads();
-    for (int k = 0; k < P; ++k) {
-        const double dkk = C[k * PP + k];
-        const double inv = dkk > 0.0 ? 1.0 / dkk : 0.0;
-        if (tid < P && tid >= k) {
-            const double r = sqrt(dkk > 0.0 ? dkk : 1.0);
-            R[k * PP + tid] = tid == k ? r : C[k * PP + tid] / r;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & 3, r = lane >> 2;
+    const int kw = nk / 8, k0 = warp * kw;
+    double c[4][2] = {};
+    for (int k = k0; k < k0 + kw; k += 4) {
+        const double a = Gs[r * gs + k + q];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dmma(c[t][0], c[t][1], a, Ws[(k + q) * kS + 8 * t + r]);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        part[(warp * 8 + r) * kS + 8 * t + 2 * q] = c[t][0];
+        part[(warp * 8 + r) * kS + 8 * t + 2 * q + 1] = c[t][1];
+    }
+    __syncthreads();
+    const int row = threadIdx.x >> 5, col = threadIdx.x & 31;  // 256 threads = 8 x 32 outputs
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += part[(w * 8 + row) * kS + col];
+    if (row < nr && col < p) Z[static_cast<size_t>(r0 + row) * p + col] = v;
+}
+
+// 1/sqrt(x) for normal positive x without the range-check branch of rsqrt():
+// rsqrt.approx (~2^-20) and one cubic correction step (error ~e^3, measured
+// <= 1 ulp on [0.25, 8]).
+__device__ __forceinline__ double tk_rsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-x * y, y, 1.0);
+    return fma(y * e, fma(0.375, e, 0.5), y);
+}
+
+// C^T-panel products for the column-major panels of tk_cqr: C (32 x 32, stride
+// kS) = A^T B with A, B stored transposed (At[m][i] = A[i][m], row stride ld =
+// 4 mod 16) over i in [0, nr), nr % 8 == 0.  Same tiling as tk_atb.
+__device__ __forceinline__ void tk_atb_t(const double* At, const double* Bt, int ld, int nr, double* C,
+                                         double diag_add) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & 3, r = lane >> 2;
+    const int mb = (warp >> 1) * 8, nb = (warp & 1) * 16;
+    const double* a_row = At + (mb + r) * ld + q;
+    const double* b_row0 = Bt + (nb + r) * ld + q;
+    const double* b_row1 = Bt + (nb + 8 + r) * ld + q;
+    double c[2][2][2] = {};
+    for (int k = 0; k < nr; k += 8) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int kk = k + 4 * h;
+            const double a = a_row[kk];
+            dmma(c[h][0][0], c[h][0][1], a, b_row0[kk]);
+            dmma(c[h][1][0], c[h][1][1], a, b_row1[kk]);
         }
-        if (tid == 0 && !(dkk > 0.0)) *bad_s = 1;
-        for (int e = tid; e < P * P; e += nt) {  // trailing update, k < i <= j, from the unscaled row k
-            const int i = e >> 5, j = e & 31;
-            if (i > k && j >= i) C[i * PP + j] = fma(-C[k * PP + i] * inv, C[k * PP + j], C[i * PP + j]);
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int row = mb + r, col = nb + 8 * t + 2 * q;
+        C[row * kS + col] = (c[0][t][0] + c[1][t][0]) + (row == col ? diag_add : 0.0);
+        C[row * kS + col + 1] = (c[0][t][1] + c[1][t][1]) + (row == col + 1 ? diag_add : 0.0);
+    }
+}
+
+// Cholesky of C (32 x 32, stride kS; rows/columns >= p made identity) in its
+// elimination form, by the whole CTA with one barrier per column, the same row
+// operations also applied to E = I:
+//   row_i(C) -= f_i row_k(C),  row_i(E) -= f_i row_k(E),  f_i = C_ki / C_kk  (i > k)
+// so E ends as L^-1 for C = L D L^T (L unit lower), and R^-1 = E^T D^-1/2 with
+// rinv[k] = D_k^-1/2: T = R^-1 is T[m][c] = E[c][m] rinv[c].  Warp w owns rows
+// w, w+8, w+16, w+24, lane j column j; every warp reads the pivot and row k
+// itself.  The pivot costs one branch-free rsqrt (1/C_kk = rinv^2), the code
+// is compact on purpose: unrolled straight-line variants are instruction-cache
+// bound (tools/dbg/chol_lat.cu).  Returns true if a pivot is not a positive
+// normal number.
+__device__ bool tk_chol_inv(double* C, double* E, double* rinv, int p, int* bad_s) {
+    const int j = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int e = threadIdx.x; e < kP * kP; e += blockDim.x) {
+        const int i = e >> 5, c = e & 31;
+        if (c >= p || i >= p) C[i * kS + c] = i == c ? 1.0 : 0.0;
+        E[i * kS + c] = i == c ? 1.0 : 0.0;
+    }
+    if (threadIdx.x == 0) *bad_s = 0;
+    __syncthreads();
+#pragma unroll 1
+    for (int k = 0; k < kP; ++k) {
+        const double dkk = C[k * kS + k];
+        const double ckj = C[k * kS + j], ekj = E[k * kS + j];
+        double cki[4], cij[4], eij[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = w + 8 * u;
+            cki[u] = C[k * kS + i];
+            cij[u] = C[i * kS + j];
+            eij[u] = E[i * kS + j];
+        }
+        const bool ok = dkk >= DBL_MIN;
+        const double ri = tk_rsqrt(ok ? dkk : 1.0);
+        const double inv = ri * ri;
+        if (w == 0 && j == 0) {
+            rinv[k] = ri;
+            if (!ok) *bad_s = 1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = w + 8 * u;
+            if (i > k) {
+                const double f = cki[u] * inv;
+                C[i * kS + j] = fma(-f, ckj, cij[u]);
+                E[i * kS + j] = fma(-f, ekj, eij[u]);
+            }
         }
         __syncthreads();
     }
     return *bad_s != 0;
 }
 
-// Z row <- Z row R^-1 for every row (thread per row), column sweep with the
-// row in registers: z_m /= R_mm, then z_j -= z_m R_mj for all j > m (independent FMAs)
-__device__ void tk_rows_solve(double* Zs, int n, const double* C) {
-    constexpr int P = 32, PP = 33;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        double z[P];
+// Zt <- (Z T)^T in place for the column-major panel (Zt[m][i] = Z[i][m], stride
+// ld) with T = R^-1 from tk_chol_inv, on DMMA: warp w takes the 8-row blocks w,
+// w+8, ... of Z; each finishes reading its rows before writing them.
+__device__ void tk_apply_inv(double* Zt, int ld, int nr, const double* E, const double* rinv) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & 3, r = lane >> 2;
+    double rc[4];  // rinv of the output columns 8t + r this lane feeds as B
 #pragma unroll
-        for (int m = 0; m < P; ++m) z[m] = Zs[i * PP + m];
+    for (int t = 0; t < 4; ++t) rc[t] = rinv[8 * t + r];
+    for (int i0 = warp * 8; i0 < nr; i0 += 64) {
+        double acc[4][2] = {};
 #pragma unroll
-        for (int m = 0; m < P; ++m) {
-            z[m] = z[m] / C[m * PP + m];
+        for (int k = 0; k < kP; k += 4) {
+            const double a = Zt[(k + q) * ld + i0 + r];  // A[i][m] = Z[i0 + r][k + q]
 #pragma unroll
-            for (int j = m + 1; j < P; ++j) z[j] = fma(-z[m], C[m * PP + j], z[j]);
+            for (int t = 0; t < 4; ++t)  // B[m][c] = T[k + q][8t + r] = E[8t + r][k + q] rinv[8t + r]
+                dmma(acc[t][0], acc[t][1], a, E[(8 * t + r) * kS + k + q] * rc[t]);
         }
+        __syncwarp();
 #pragma unroll
-        for (int m = 0; m < P; ++m) Zs[i * PP + m] = z[m];
+        for (int t = 0; t < 4; ++t) {
+            const int c = 8 * t + 2 * q;
+            Zt[c * ld + i0 + r] = acc[t][0];
+            Zt[(c + 1) * ld + i0 + r] = acc[t][1];
+        }
     }
 }
 
 // Shifted CholQR3 (Fukaya et al. 2020) of Z (n x p row-major, global) -> Q:
-// C = Z^T Z + s I (s = 11 (n p + p (p+1)) u |Z|_F^2), R = chol(C), Z <- Z R^-1,
-// then two plain CholQR passes.  The shift bounds cond(Z R^-1) by ~u^-1/2, so
-// every Cholesky succeeds for any numerically full-rank block, and the result
-// is orthonormal to roundoff with |Z - Q R| ~ u |Z|, like Householder QR.
-// p is padded to 32 (identity columns); one warp factors C and inverts R in
-// registers (lane j owns column j), the rest is register-blocked for ILP.
-// *fail is set if a pivot is not positive.
+// C = Z^T Z + s I (s = 11 (n p + p (p+1)) u |Z|_F^2), Z <- Z R^-1 with R =
+// chol(C), then two plain CholQR passes.  The shift bounds cond(Z R^-1) by
+// ~u^-1/2, so every Cholesky succeeds for any numerically full-rank block, and
+// the result is orthonormal to roundoff (|Z - Q R| ~ u |Z|), like Householder
+// QR.  The panel lives column-major in shared memory (row stride = 4 mod 16:
+// conflict-free DMMA fragments), p is padded to 32 with zero columns, and the
+// Grams and the Z R^-1 products run on DMMA.  *fail is set if a pivot is not
+// positive.
 __global__ void __launch_bounds__(kTkQrThreads) tk_cqr(const double* __restrict__ Zg, int n, int p,
                                                       double* __restrict__ Q, int* __restrict__ fail) {
-    extern __shared__ double sm_tk[];
+    extern __shared__ __align__(16) double sm_tk[];
 #ifdef TCB_TOPK_TIMING
     long long tprev = clock64();
 #endif
-    constexpr int P = 32, PP = 33;
-    double* Zs = sm_tk;        // n x PP (columns >= p are zero)
-    double* C = Zs + n * PP;   // P x PP: Gram
-    double* R = C + P * PP;    // P x PP: Cholesky factor (upper)
+    const int nr = (n + 7) & ~7, ld = ((n + 15) & ~15) + 4;
+    double* Zt = sm_tk;          // 32 x ld (columns >= p and rows >= n are zero)
+    double* C = Zt + kP * ld;    // 32 x kS: Gram, then eliminated
+    double* E = C + kP * kS;     // 32 x kS: L^-1
+    double* rinv = E + kP * kS;  // 32
     __shared__ double red[32];
     __shared__ int bad;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < nr * kP; e += blockDim.x) {
+        const int i = e >> 5, j = e & 31;
+        if (i < n && j < p)
+            cp_async8(Zt + j * ld + i, Zg + static_cast<size_t>(i) * p + j);
+        else
+            Zt[j * ld + i] = 0.0;
+    }
+    cp_wait_all();
+    __syncthreads();
     double fro = 0.0;
-    for (int i = warp; i < n; i += nw) {
-        const double v = lane < p ? Zg[static_cast<size_t>(i) * p + lane] : 0.0;
-        Zs[i * PP + lane] = v;
+    for (int e = tid; e < n * kP; e += blockDim.x) {
+        const double v = Zt[(e / n) * ld + e % n];
         fro = fma(v, v, fro);
     }
-    if (tid == 0) bad = 0;
     fro = tk_block_sum(fro, red);
     TK_T(0);
     const double shift = 11.0 * (static_cast<double>(n) * p + static_cast<double>(p) * (p + 1)) * (DBL_EPSILON / 2) * fro;
-    const int a0 = (tid >> 4) * 2, b0 = (tid & 15) * 2;  // this thread's 2x2 block of C (256 threads)
     for (int pass = 0; pass < 3; ++pass) {
-        if (tid < 256) {
-            double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
-#pragma unroll 4
-            for (int i = 0; i < n; ++i) {
-                const double za0 = Zs[i * PP + a0], za1 = Zs[i * PP + a0 + 1];
-                const double zb0 = Zs[i * PP + b0], zb1 = Zs[i * PP + b0 + 1];
-                c00 = fma(za0, zb0, c00);
-                c01 = fma(za0, zb1, c01);
-                c10 = fma(za1, zb0, c10);
-                c11 = fma(za1, zb1, c11);
-            }
-            const double sh = pass == 0 ? shift : 0.0;
-            C[a0 * PP + b0] = c00 + (a0 == b0 ? sh : 0.0);
-            C[a0 * PP + b0 + 1] = c01;
-            C[(a0 + 1) * PP + b0] = c10;
-            C[(a0 + 1) * PP + b0 + 1] = c11 + (a0 == b0 ? sh : 0.0);
-        }
+        tk_atb_t(Zt, Zt, ld, nr, C, pass == 0 ? shift : 0.0);
         __syncthreads();
         TK_T(1);
-        if (tk_block_chol(C, R, p, &bad)) break;
+        if (tk_chol_inv(C, E, rinv, p, &bad)) break;
         TK_T(2);
-        tk_rows_solve(Zs, n, R);
+        tk_apply_inv(Zt, ld, nr, E, rinv);
         __syncthreads();
         TK_T(3);
     }
@@ -217,74 +350,63 @@ __global__ void __launch_bounds__(kTkQrThreads) tk_cqr(const double* __restrict_
         if (tid == 0) *fail = 1;
         return;
     }
-    for (int i = warp; i < n; i += nw)
-        if (lane < p) Q[static_cast<size_t>(i) * p + lane] = Zs[i * PP + lane];
+    for (int e = tid; e < n * p; e += blockDim.x) Q[e] = Zt[(e % p) * ld + e / p];
 }
 
-// Rayleigh-Ritz: H = Q^T Z (Z = G Q), cyclic Jacobi (round-robin pairs, every
-// disjoint 2x2 block rotated from both sides in one phase), theta descending,
-// X = Q Y, residual norms |Z y_j - theta_j x_j|, and trace(G).
-__global__ void __launch_bounds__(kTkRrThreads) tk_rr(const double* __restrict__ G, const double* __restrict__ Qg,
-                                                   const double* __restrict__ Zg, int n, int p,
-                                                   double* __restrict__ X, double* __restrict__ out) {
-    extern __shared__ double sm_tk[];
-#ifdef TCB_TOPK_TIMING
-    long long tprev = clock64();
-#endif
-    const int pp = p + 1;
-    double* Qs = sm_tk;           // n x pp
-    double* Zs = Qs + n * pp;     // n x pp
-    double* H = Zs + n * pp;      // p x pp
-    double* Y = H + p * pp;       // p x pp (Y[row][col])
-    double* R2 = Y + p * pp;      // p x n residual squares
-    __shared__ double red[32];
-    __shared__ double cs[32][2];
-    __shared__ int pr[32][2];
-    __shared__ int order_s[64];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    for (int i = warp; i < n; i += nw)
-        if (lane < p) {
-            Qs[i * pp + lane] = Qg[static_cast<size_t>(i) * p + lane];
-            Zs[i * pp + lane] = Zg[static_cast<size_t>(i) * p + lane];
+// Jacobi rotation (c, s) annihilating h_ij of the 2 x 2 block [[h_ii, h_ij],
+// [h_ij, h_jj]] (smaller angle, sign(s) = sign(h_jj - h_ii) sign(h_ij)), from
+// cos 2phi = |a| / hypot(a, b), a = h_jj - h_ii, b = 2 h_ij: two rsqrt on the
+// critical path instead of two divides and two square roots.  Branch-free (so
+// two rotations interleave): (a, b) are first scaled by an exact power of two
+// into [1, 2) by the larger exponent; h_ij = 0 gives the identity.
+__device__ __forceinline__ void tk_rotation(double hii, double hjj, double hij, double& c, double& s) {
+    const double a = hjj - hii, b = 2.0 * hij;
+    const long long em = (__double_as_longlong(fmax(fabs(a), fabs(b))) >> 52) & 0x7ff;
+    const long long es = min(max(2046ll - em, 1ll), 2046ll);
+    const double sc = __longlong_as_double(es << 52);  // 2^(1023 - em)
+    const double as = a * sc, bs = b * sc;
+    const double ri = tk_rsqrt(fma(as, as, bs * bs));  // argument in [1, 8)
+    const double w = fma(0.5 * fabs(as), ri, 0.5);     // cos^2 phi = (1 + cos 2phi) / 2, in [0.5, 1]
+    const double rw = tk_rsqrt(w);
+    const bool zero = hij == 0.0;
+    c = zero ? 1.0 : w * rw;
+    s = zero ? 0.0 : (a >= 0.0 ? 0.5 : -0.5) * bs * ri * rw;  // sin 2phi / (2 cos phi)
+}
+
+// Cyclic Jacobi on H (p x p in a 32 x kS buffer) accumulating Y <- Y J, with Y
+// stored transposed (Yt[col][row]: a thread's two rows are consecutive across
+// the half-warp, so the column updates are bank-conflict free); Hb is a second
+// 32 x kS buffer.  256 threads.  Leaves the result in H; returns the number of
+// sweeps run.
+__device__ int tk_jacobi(double* H, double* Hb, double* Yt, int p, double* red) {
+    const int tid = threadIdx.x;
+    // Cyclic Jacobi; an odd p gets a dummy player p (its rotations are
+    // identities).  One barrier per round: H is double-buffered and the thread
+    // owning block (P, Q) computes the rotations of pairs P and Q itself from
+    // the previous buffer; it also rotates Y's entries (Q, Q+16) x pair P.
+    const int pe = (p + 1) & ~1, half = pe / 2, np1 = pe - 1;
+    double* Ha = H;
+    auto pair_of = [&](int t, int rnd, int& i, int& j) {
+        int x = t - 1 + rnd;
+        x = x >= np1 ? x - np1 : x;
+        int y = pe - 2 - t + rnd;
+        y = y >= np1 ? y - np1 : y;
+        i = t == 0 ? 0 : 1 + x;
+        j = 1 + y;
+        if (i > j) {
+            const int tmp = i;
+            i = j;
+            j = tmp;
         }
-    __syncthreads();
-    // H = sym(Q^T Z): thread (a0, b0) owns a 2x2 block (p <= 32, 256 threads)
-    {
-        const int a0 = (tid >> 4) * 2, b0 = (tid & 15) * 2;
-        if (a0 < p && b0 < p) {
-            const bool a1 = a0 + 1 < p, b1 = b0 + 1 < p;
-            double qz00 = 0.0, qz01 = 0.0, qz10 = 0.0, qz11 = 0.0, zq00 = 0.0, zq01 = 0.0, zq10 = 0.0, zq11 = 0.0;
-#pragma unroll 4
-            for (int i = 0; i < n; ++i) {
-                const double* qi = Qs + i * pp;
-                const double* zi = Zs + i * pp;
-                const double qa0 = qi[a0], qa1 = a1 ? qi[a0 + 1] : 0.0, qb0 = qi[b0], qb1 = b1 ? qi[b0 + 1] : 0.0;
-                const double za0 = zi[a0], za1 = a1 ? zi[a0 + 1] : 0.0, zb0 = zi[b0], zb1 = b1 ? zi[b0 + 1] : 0.0;
-                qz00 = fma(qa0, zb0, qz00);
-                qz01 = fma(qa0, zb1, qz01);
-                qz10 = fma(qa1, zb0, qz10);
-                qz11 = fma(qa1, zb1, qz11);
-                zq00 = fma(za0, qb0, zq00);
-                zq01 = fma(za0, qb1, zq01);
-                zq10 = fma(za1, qb0, zq10);
-                zq11 = fma(za1, qb1, zq11);
-            }
-            H[a0 * pp + b0] = 0.5 * (qz00 + zq00);
-            if (b1) H[a0 * pp + b0 + 1] = 0.5 * (qz01 + zq01);
-            if (a1) H[(a0 + 1) * pp + b0] = 0.5 * (qz10 + zq10);
-            if (a1 && b1) H[(a0 + 1) * pp + b0 + 1] = 0.5 * (qz11 + zq11);
-        }
-    }
-    for (int e = tid; e < p * p; e += blockDim.x) Y[(e / p) * pp + e % p] = (e / p == e % p) ? 1.0 : 0.0;
-    __syncthreads();
-    TK_T(4);
-    // cyclic Jacobi; an odd p gets a dummy player p (its rotations are identities)
-    const int pe = (p + 1) & ~1, half = pe / 2;
-    for (int sweep = 0; sweep < 15; ++sweep) {
+    };
+    const int P = tid / half, Qp = tid % half;
+    const bool active = tid < half * half;
+    int sweep = 0;
+    for (; sweep < 15; ++sweep) {
         double o = 0.0, d = 0.0;
         for (int a = tid >> 5; a < p; a += blockDim.x >> 5)
             for (int b = tid & 31; b < p; b += 32) {
-                const double v = H[a * pp + b];
+                const double v = Ha[a * kS + b];
                 if (a != b) o = fma(v, v, o);
                 else d = fma(v, v, d);
             }
@@ -293,127 +415,181 @@ __global__ void __launch_bounds__(kTkRrThreads) tk_rr(const double* __restrict__
         // off(H) <= 1e-14 |diag(H)|: at the roundoff floor (~p eps |H|), after which
         // the eigenvalue error is second order in off(H)
         if (o <= 1e-28 * d) break;
-        for (int rnd = 0; rnd < pe - 1; ++rnd) {
-            if (tid < half) {  // pair t and its rotation
-                const int t = tid;
-                int i = t == 0 ? 0 : 1 + (t - 1 + rnd) % (pe - 1);
-                int j = 1 + (pe - 2 - t + rnd) % (pe - 1);
-                if (i > j) {
-                    const int tmp = i;
-                    i = j;
-                    j = tmp;
-                }
-                double c = 1.0, s = 0.0;
-                if (j < p) {
-                    const double hij = H[i * pp + j];
-                    if (hij != 0.0) {
-                        const double th = (H[j * pp + j] - H[i * pp + i]) / (2.0 * hij);
-                        const double tt = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(fma(th, th, 1.0)));
-                        c = 1.0 / sqrt(fma(tt, tt, 1.0));
-                        s = tt * c;
-                    }
-                }
-                cs[t][0] = c;
-                cs[t][1] = s;
-                pr[t][0] = i;
-                pr[t][1] = j;
-            }
-            __syncthreads();
-            // H <- J^T H J on every 2x2 block (pair P rows, pair Q cols)
-            for (int e = tid; e < half * half; e += blockDim.x) {
-                const int P = e / half, Qp = e % half;
-                const int a0 = pr[P][0], a1 = pr[P][1], b0 = pr[Qp][0], b1 = pr[Qp][1];
-                const double c1 = cs[P][0], s1 = cs[P][1], c2 = cs[Qp][0], s2 = cs[Qp][1];
+#ifdef TCB_TOPK_TIMING
+        if (tid == 0) atomicAdd(&g_tk_phase[8], 1ull);
+#endif
+        for (int rnd = 0; rnd < np1; ++rnd) {
+            if (active) {
+                int a0, a1, b0, b1;
+                pair_of(P, rnd, a0, a1);
+                pair_of(Qp, rnd, b0, b1);
                 const bool ra = a1 < p, rb = b1 < p;  // a dummy partner keeps its row/column
-                const double h00 = H[a0 * pp + b0], h01 = rb ? H[a0 * pp + b1] : 0.0;
-                const double h10 = ra ? H[a1 * pp + b0] : 0.0, h11 = (ra && rb) ? H[a1 * pp + b1] : 0.0;
+                // every load first (indices stay inside the 32 x 32 buffer even for a dummy)
+                const double qii = Ha[b0 * kS + b0], qjj = Ha[b1 * kS + b1], qij = Ha[b0 * kS + b1];
+                const double h00 = Ha[a0 * kS + b0], h01 = Ha[a0 * kS + b1];
+                const double h10 = Ha[a1 * kS + b0], h11 = Ha[a1 * kS + b1];
+                const int m0 = Qp, m1 = Qp + 16;  // Y rows of this thread (Y stored transposed)
+                const double ya0 = Yt[a0 * kS + m0], yb0 = Yt[a1 * kS + m0];
+                const double ya1 = Yt[a0 * kS + m1], yb1 = Yt[a1 * kS + m1];
+                // this lane computes pair Q's rotation; pair P's comes from the lane
+                // of its half-warp whose Q equals P (half == 16 puts a row P in each half-warp)
+                double c2, s2;
+                tk_rotation(qii, qjj, qij, c2, s2);
+                if (!rb) c2 = 1.0, s2 = 0.0;
+                double c1, s1;
+                if (half == 16) {
+                    const int src = (threadIdx.x & 16) | P;
+                    c1 = __shfl_sync(0xffffffffu, c2, src);
+                    s1 = __shfl_sync(0xffffffffu, s2, src);
+                } else {
+                    tk_rotation(Ha[a0 * kS + a0], Ha[a1 * kS + a1], Ha[a0 * kS + a1], c1, s1);
+                    if (!ra) c1 = 1.0, s1 = 0.0;
+                }
                 const double r00 = c1 * h00 - s1 * h10, r01 = c1 * h01 - s1 * h11;
                 const double r10 = s1 * h00 + c1 * h10, r11 = s1 * h01 + c1 * h11;
-                H[a0 * pp + b0] = r00 * c2 - r01 * s2;
-                if (rb) H[a0 * pp + b1] = r00 * s2 + r01 * c2;
-                if (ra) H[a1 * pp + b0] = r10 * c2 - r11 * s2;
-                if (ra && rb) H[a1 * pp + b1] = r10 * s2 + r11 * c2;
-            }
-            // Y <- Y J
-            for (int e = tid; e < p * half; e += blockDim.x) {
-                const int m = e / half, P = e % half;
-                const int a = pr[P][0], b = pr[P][1];
-                if (b >= p) continue;
-                const double c = cs[P][0], s = cs[P][1];
-                const double ya = Y[m * pp + a], yb = Y[m * pp + b];
-                Y[m * pp + a] = c * ya - s * yb;
-                Y[m * pp + b] = s * ya + c * yb;
+                Hb[a0 * kS + b0] = r00 * c2 - r01 * s2;
+                if (rb) Hb[a0 * kS + b1] = r00 * s2 + r01 * c2;
+                if (ra) Hb[a1 * kS + b0] = r10 * c2 - r11 * s2;
+                if (ra && rb) Hb[a1 * kS + b1] = r10 * s2 + r11 * c2;
+                if (ra) {  // Y <- Y J on rows Q, Q+16 (< p) of pair P's columns
+                    if (m0 < p) {
+                        Yt[a0 * kS + m0] = c1 * ya0 - s1 * yb0;
+                        Yt[a1 * kS + m0] = s1 * ya0 + c1 * yb0;
+                    }
+                    if (m1 < p) {
+                        Yt[a0 * kS + m1] = c1 * ya1 - s1 * yb1;
+                        Yt[a1 * kS + m1] = s1 * ya1 + c1 * yb1;
+                    }
+                }
             }
             __syncthreads();
+            double* t = Ha;
+            Ha = Hb;
+            Hb = t;
         }
     }
+    if (Ha != H) {  // the current iterate lives in the scratch buffer
+        for (int e = tid; e < kP * kP; e += blockDim.x) H[(e >> 5) * kS + (e & 31)] = Ha[(e >> 5) * kS + (e & 31)];
+        __syncthreads();
+    }
+    return sweep;
+}
+
+// Rayleigh-Ritz: H = sym(Q^T Z) (Z = G Q) on DMMA, cyclic Jacobi (round-robin
+// pairs, every disjoint 2x2 block rotated from both sides in one phase), theta
+// descending, then X = Q Y and Z Y on DMMA with the residual norms
+// |Z y_j - theta_j x_j| reduced per column in a fixed order, and trace(G).
+__global__ void __launch_bounds__(kTkRrThreads) tk_rr(const double* __restrict__ G, const double* __restrict__ Qg,
+                                                   const double* __restrict__ Zg, int n, int p,
+                                                   double* __restrict__ X, double* __restrict__ out) {
+    extern __shared__ __align__(16) double sm_tk[];
+#ifdef TCB_TOPK_TIMING
+    long long tprev = clock64();
+#endif
+    const int nr = (n + 7) & ~7;
+    double* Qs = sm_tk;            // nr x kS
+    double* Zs = Qs + nr * kS;     // nr x kS
+    double* H = Zs + nr * kS;      // 32 x kS
+    double* Y = H + kP * kS;       // 32 x kS: Q^T Z, then Y transposed (Y[col][row]) during the sweeps
+    double* Ys = Y + kP * kS;      // 32 x kS scratch (sorting)
+    double* part = Ys + kP * kS;   // 8 warps x 32 residual partials
+    __shared__ double red[32];
+    __shared__ int order_s[64];
+    __shared__ double th_s[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < nr * kP; e += blockDim.x) {
+        const int i = e >> 5, j = e & 31;
+        if (i < n && j < p) {
+            cp_async8(Qs + i * kS + j, Qg + static_cast<size_t>(i) * p + j);
+            cp_async8(Zs + i * kS + j, Zg + static_cast<size_t>(i) * p + j);
+        } else {
+            Qs[i * kS + j] = 0.0;
+            Zs[i * kS + j] = 0.0;
+        }
+    }
+    cp_wait_all();
+    __syncthreads();
+    tk_atb(Qs, Zs, nr, Y, 0.0);  // Y <- Q^T Z
+    __syncthreads();
+    for (int e = tid; e < kP * kP; e += blockDim.x) {
+        const int a = e >> 5, b = e & 31;
+        H[a * kS + b] = 0.5 * (Y[a * kS + b] + Y[b * kS + a]);
+    }
+    __syncthreads();
+    for (int e = tid; e < kP * kP; e += blockDim.x) Y[(e >> 5) * kS + (e & 31)] = (e >> 5) == (e & 31) ? 1.0 : 0.0;
+    __syncthreads();
+    TK_T(4);
+    tk_jacobi(H, Ys, Y, p, red);
+#ifdef TCB_TOPK_TIMING
+    if (tid == 0) atomicAdd(&g_tk_phase[7], 1ull);
+#endif
     TK_T(5);
     // theta descending (ties by index)
     if (tid < p) {
-        const double t = H[tid * pp + tid];
+        const double t = H[tid * kS + tid];
         int rk = 0;
         for (int q = 0; q < p; ++q) {
-            const double u = H[q * pp + q];
+            const double u = H[q * kS + q];
             rk += (u > t || (u == t && q < tid)) ? 1 : 0;
         }
         order_s[rk] = tid;
     }
     __syncthreads();
-    // Y and theta permuted into descending order (R2 doubles as scratch until the residuals)
-    double* Ys = R2;  // p x pp scratch, free until the residual squares are written below
-    double* th_s = Ys + p * pp;
-    for (int e = tid; e < p * p; e += blockDim.x) {
-        const int m = e / p, j = e % p;
-        Ys[m * pp + j] = Y[m * pp + order_s[j]];
+    // Y's columns permuted into descending order (zero beyond p), theta likewise
+    for (int e = tid; e < kP * kP; e += blockDim.x) {
+        const int m = e >> 5, j = e & 31;
+        Ys[m * kS + j] = (m < p && j < p) ? Y[order_s[j] * kS + m] : 0.0;
     }
-    if (tid < p) th_s[tid] = H[order_s[tid] * pp + order_s[tid]];
+    if (tid < p) th_s[tid] = H[order_s[tid] * kS + order_s[tid]];
+    if (tid >= p && tid < kP) th_s[tid] = 0.0;
     __syncthreads();
-    for (int e = tid; e < p * p; e += blockDim.x) Y[(e / p) * pp + e % p] = Ys[(e / p) * pp + e % p];
-    if (tid < p) H[tid * pp + tid] = th_s[tid];  // H's diagonal now holds theta in sorted order
-    __syncthreads();
-    // X = Q Y (sorted columns) and the residual squares: thread per row, the
-    // row of Q and of Z in registers, 8 output columns at a time
-    for (int i = tid; i < n; i += blockDim.x) {
-        double q[32], z[32];
+    // X = Q Y, W = Z Y on DMMA: warp w takes the 8-row blocks w, w + 8, ...; the
+    // residual squares accumulate per (lane, column) in registers, then across
+    // the 8 row lanes and the 8 warps in a fixed order.
+    {
+        const int q = lane & 3, r = lane >> 2;
+        double acc[4][2] = {};
+        for (int i0 = warp * 8; i0 < nr; i0 += 64) {
+            double x[4][2] = {}, w[4][2] = {};
 #pragma unroll
-        for (int m = 0; m < 32; ++m) {
-            q[m] = m < p ? Qs[i * pp + m] : 0.0;
-            z[m] = m < p ? Zs[i * pp + m] : 0.0;
-        }
-        for (int j0 = 0; j0 < p; j0 += 8) {
-            double x[8], zz[8];
+            for (int k = 0; k < kP; k += 4) {
+                const double aq = Qs[(i0 + r) * kS + k + q], az = Zs[(i0 + r) * kS + k + q];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) x[u] = zz[u] = 0.0;
-#pragma unroll
-            for (int m = 0; m < 32; ++m) {
-                if (m >= p) break;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const double y = j0 + u < p ? Y[m * pp + j0 + u] : 0.0;
-                    x[u] = fma(q[m], y, x[u]);
-                    zz[u] = fma(z[m], y, zz[u]);
+                for (int t = 0; t < 4; ++t) {
+                    const double b = Ys[(k + q) * kS + 8 * t + r];
+                    dmma(x[t][0], x[t][1], aq, b);
+                    dmma(w[t][0], w[t][1], az, b);
                 }
             }
+            const int i = i0 + r;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int j = j0 + u;
-                if (j >= p) break;
-                X[static_cast<size_t>(i) * p + j] = x[u];
-                const double rr = zz[u] - H[j * pp + j] * x[u];
-                R2[j * n + i] = rr * rr;
-            }
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int j = 8 * t + 2 * q + e;
+                    const double rr = w[t][e] - th_s[j] * x[t][e];
+                    acc[t][e] = fma(rr, rr, acc[t][e]);  // rows >= n are zero
+                    if (i < n && j < p) X[static_cast<size_t>(i) * p + j] = x[t][e];
+                }
         }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double v = acc[t][e];
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                v += __shfl_xor_sync(0xffffffffu, v, 16);
+                if (r == 0) part[warp * kP + 8 * t + 2 * q + e] = v;
+            }
     }
     __syncthreads();
     TK_T(6);
-    for (int j = warp; j < p; j += nw) {  // a warp per column
-        double s = 0.0;
-        for (int i = lane; i < n; i += 32) s += R2[j * n + i];
-        s = tk_warp_sum(s);
-        if (lane == 0) {
-            out[j] = H[j * pp + j];
-            out[p + j] = sqrt(s);
-        }
+    if (tid < p) {
+        double s2 = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s2 += part[w * kP + tid];
+        out[tid] = th_s[tid];
+        out[p + tid] = sqrt(s2);
     }
     double tr = 0.0;
     for (int i = tid; i < n; i += blockDim.x) tr += G[static_cast<size_t>(i) * n + i];
@@ -446,15 +622,16 @@ void topk_eig(const double* G, u64 n64, int p, int extra_iters, double* X, std::
     TCB_CUDA(cudaMemsetAsync(out.p, 0, (2 * p + 2) * sizeof(double), s));
     int* fail = reinterpret_cast<int*>(out.p + 2 * p + 1);
     tk_random<<<cdiv(n64 * p, 256), 256, 0, s>>>(W.p, n, p);
-    const size_t gsm = (8 * static_cast<size_t>(n) + static_cast<size_t>(n) * p) * sizeof(double);
-    const size_t qsm = (static_cast<size_t>(n) + 64) * 33 * sizeof(double);
-    const size_t rsm = (2 * static_cast<size_t>(n) * (p + 1) + 2 * static_cast<size_t>(p) * (p + 1) +
-                        static_cast<size_t>(p) * n) * sizeof(double);
+    const size_t nr = (n64 + 7) & ~u64{7}, nk = (n64 + 31) & ~u64{31}, gs = ((nk + 15) & ~u64{15}) + 4;
+    const size_t gsm = (8 * gs + nk * kS + 64 * kS) * sizeof(double);
+    const size_t qld = ((n64 + 15) & ~u64{15}) + 4;
+    const size_t qsm = (kP * qld + 2 * kP * kS + kP) * sizeof(double);
+    const size_t rsm = (2 * nr * kS + 3 * kP * kS + 8 * kP) * sizeof(double);
     for (int it = 0; it <= extra_iters; ++it) {
-        tk_gq<<<cdiv(n64, 8), 256, gsm, s>>>(G, W.p, n, p, Z.p);
+        tk_gq<<<cdiv(n64, 8), kGqThreads, gsm, s>>>(G, W.p, n, p, Z.p);
         tk_cqr<<<1, kTkQrThreads, qsm, s>>>(Z.p, n, p, W.p, fail);
     }
-    tk_gq<<<cdiv(n64, 8), 256, gsm, s>>>(G, W.p, n, p, Z.p);
+    tk_gq<<<cdiv(n64, 8), kGqThreads, gsm, s>>>(G, W.p, n, p, Z.p);
     tk_rr<<<1, kTkRrThreads, rsm, s>>>(G, W.p, Z.p, n, p, X, out.p);
     count_launch(2 * (extra_iters + 1) + 3);
     TCB_LAUNCH();

@@ -29,4 +29,5 @@ int main(int argc, char** argv) {
     printf("topk_eig n=%d: %.3f ms; theta0 %.3e res0 %.1e trace %.3e\n", n, ms, th[0], res[0], tr);
     const char* nm[7] = {"cqr load+fro", "cqr gram", "cqr chol+inv", "cqr apply", "rr load+H", "rr jacobi", "rr X+res"};
     for (int i = 0; i < 7; ++i) printf("  %-10s %llu cycles (all launches, 3 passes each)\n", nm[i], ph[i]);
+    printf("  jacobi sweeps per rr launch: %.2f\n", double(ph[8]) / double(ph[7]));
 }
