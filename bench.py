@@ -386,22 +386,29 @@ def main():
     gram_flop, ttm_flop = algorithmic_work(list(x.shape), res.ranks, order)
     dom = max(stage_ms, key=stage_ms.get)
     if dom == "eig":
-        # Householder tridiagonalisation 4/3 n^3 + back-transform 2 n^2 r per mode step (fp64);
-        # the eigensolver is latency-bound: the fraction is reported, not a target
+        # Certified top-p path (csrc/topk.cu, p = 32, 2 extra iterations) per mode with n <= 256:
+        # 4 products G W (2 n^2 p each), 3 x shifted CholQR3 (3 passes of Gram 2 n p^2 + apply
+        # 2 n p^2), Rayleigh-Ritz (H 2 n p^2, X and G X 4 n p^2).  Larger modes take the full
+        # solver: tridiagonalisation 4/3 n^3 + back-transform 2 n^2 r.  The eigensolve is a
+        # chain of dependent small steps on one SM per launch (latency-bound).
         cur = [x.shape[i] for i in order]
-        eig_flop = 0.0
+        eig_flop, p_blk = 0.0, 32
         for mode in order:
             rows, cols = cur[0], int(np.prod(cur)) // cur[0]
             n_eig = rows if rows <= cols else cols
-            eig_flop += 4.0 / 3.0 * n_eig ** 3 + 2.0 * n_eig * n_eig * res.ranks[mode]
+            if 2 * p_blk <= n_eig <= 256 and not os.environ.get("TCB_NO_TOPK"):
+                eig_flop += 4 * 2.0 * n_eig ** 2 * p_blk + 9 * 4.0 * n_eig * p_blk ** 2 + 6.0 * n_eig * p_blk ** 2
+            else:
+                eig_flop += 4.0 / 3.0 * n_eig ** 3 + 2.0 * n_eig * n_eig * res.ranks[mode]
             cur = cur[1:] + [res.ranks[mode]]
         achieved = eig_flop / (stage_ms["eig"] * 1e-3) / 1e12
-        roof = {"kernel": "eig (tridiag_dsmem + multisect + invit + wy_apply)", "bound": "tensor",
+        roof = {"kernel": "eig (certified top-32: tk_gq + tk_cqr + tk_rr per mode)", "bound": "tensor",
                 "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s", "frac": achieved / dmma_peak,
                 "traffic": None, "flop": eig_flop,
                 "peak_source": "measured fp64 DMMA probe (tcb_peak_dmma_tflops); MEASURED_PEAKS.json has no fp64",
-                "note": "latency-bound: n-2 dependent Householder steps on one 16-CTA cluster, each an "
-                        "all-to-all DSMEM exchange (~400 cycles + ~2 per 16-byte store, tools/dbg/dsmem_ping.cu)"}
+                "note": "latency-bound: per mode 3 block subspace iterations, each a 32-step Cholesky with one "
+                        "CTA barrier per step, then ~2-3 Jacobi sweeps of 31 dependent rounds, on one SM "
+                        "(DESIGN.md 3a); the stage time includes the host certificate's sync per mode"}
     elif dom in ("gram", "ttm"):
         work = gram_flop if dom == "gram" else ttm_flop
         achieved = work / (stage_ms[dom] * 1e-3) / 1e12

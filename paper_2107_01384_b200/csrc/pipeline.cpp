@@ -221,7 +221,20 @@ bool topk_factor(const double* G, u64 n, double budget, cudaStream_t s, u64& r_o
     if (!topk_supported(n, p)) return false;
     if (const char* e = std::getenv("TCB_NO_TOPK"); e && *e && *e != '0') return false;
     DevBuf<double> X(n * p, s);
-    for (int extra : {2, 5}) {
+    static const std::vector<int> attempts = [] {  // TCB_TOPK_ITERS="2,5": extra iterations per attempt
+        std::vector<int> v;
+        if (const char* e = std::getenv("TCB_TOPK_ITERS"); e && *e) {
+            for (const char* c = e; *c;) {
+                v.push_back(std::atoi(c));
+                while (*c && *c != ',') ++c;
+                if (*c) ++c;
+            }
+        }
+        if (v.empty()) v = {2, 5};
+        return v;
+    }();
+    for (int extra : attempts) {
+        HostTrace ht(extra <= 1 ? "topk: attempt (extra<=1)" : extra <= 3 ? "topk: attempt (extra 2-3)" : "topk: attempt (extra>3)");
         std::vector<double> th, res;
         double tr = 0.0;
         topk_eig(G, n, p, extra, X.p, th, res, tr, s);

@@ -17,9 +17,13 @@
 // solve passes instead of p dependent Householder steps; stable like
 // Householder QR (|Z - QR| ~ u |Z|, so a direction's span error is
 // u |Z| / sigma_j), which keeps eigenvalues 1e-9 below the largest usable.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+
+#include <cooperative_groups.h>
 
 #include "kernels.cuh"
 
@@ -597,6 +601,265 @@ __global__ void __launch_bounds__(kTkRrThreads) tk_rr(const double* __restrict__
     if (tid == 0) out[2 * p] = tr;
 }
 
+// ---------------------------------------------------------------------------
+// The whole top-p solve in ONE launch on an 8-CTA thread-block cluster.  CTA c
+// owns rows [c nb, c nb + nb) of G (resident in its shared memory for all
+// iterations), of Z = G W and of the basis Q; every CTA holds the full current
+// basis W (n x 32) for the products.  Per iteration:
+//   Z_c = G_c W                       (DMMA, local rows, the flop-heavy part)
+//   3 x { P_c = Z_c^T Z_c (DMMA); cluster barrier; C = sum_c P_c read over
+//         DSMEM in a fixed order (bitwise identical in every CTA; pass 0 adds
+//         the CholQR3 shift from trace C = |Z|_F^2); Cholesky with inverse
+//         (redundant per CTA, identical); Z_c <- Z_c R^-1 (DMMA) }
+//   all-gather: every CTA stores its rows of Q into every CTA's W (DSMEM);
+//   cluster barrier.
+// Then Z_c = G_c Q, H = sum_c Q_c^T Z_c, Jacobi (redundant, identical), X_c =
+// Q_c Y and the residual/trace partials reduced on CTA 0.  The partial Grams
+// are double-buffered, so one cluster barrier per pass suffices.
+constexpr int kTkNC = 8;
+
+// C (32 x kS) = A^T B over nr rows (nr % 8 == 0) of row-major panels, for
+// remote-free local use (same tiling as tk_atb).
+__device__ __forceinline__ void tk_cl_gq(const double* Gl, int gs, const double* W, int nk, int nb, double* Zl) {
+    // Zl (nb x 32, stride kS) = Gl (nb x nk, stride gs) W (nk x 32, stride kS);
+    // warp w: row block w & 3, column tiles 2 (w >> 2) + {0, 1}; two k chains
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & 3, r = lane >> 2;
+    const int rb = (warp & 3) * 8, t0 = (warp >> 2) * 2;
+    if (rb >= nb) return;
+    double c[2][2][2] = {};
+    const double* a_row = Gl + (rb + r) * gs + q;
+    for (int k = 0; k < nk; k += 8) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int kk = k + 4 * h;
+            const double a = a_row[kk];
+            const double* b = W + (kk + q) * kS + r;
+            dmma(c[h][0][0], c[h][0][1], a, b[8 * t0]);
+            dmma(c[h][1][0], c[h][1][1], a, b[8 * (t0 + 1)]);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int col = 8 * (t0 + t) + 2 * q;
+        Zl[(rb + r) * kS + col] = c[0][t][0] + c[1][t][0];
+        Zl[(rb + r) * kS + col + 1] = c[0][t][1] + c[1][t][1];
+    }
+}
+
+// Zl (nb x 32 row-major) <- Zl T, T = R^-1 (E, rinv): results held in
+// registers across a CTA barrier (warps w and w + 4 share row block w & 3)
+__device__ __forceinline__ void tk_cl_apply(double* Zl, int nb, const double* E, const double* rinv) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & 3, r = lane >> 2;
+    const int rb = (warp & 3) * 8, t0 = (warp >> 2) * 2;
+    double acc[2][2] = {};
+    if (rb < nb) {
+        const double rc0 = rinv[8 * t0 + r], rc1 = rinv[8 * (t0 + 1) + r];
+#pragma unroll
+        for (int k = 0; k < kP; k += 4) {
+            const double a = Zl[(rb + r) * kS + k + q];
+            dmma(acc[0][0], acc[0][1], a, E[(8 * t0 + r) * kS + k + q] * rc0);
+            dmma(acc[1][0], acc[1][1], a, E[(8 * (t0 + 1) + r) * kS + k + q] * rc1);
+        }
+    }
+    __syncthreads();
+    if (rb < nb) {
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int col = 8 * (t0 + t) + 2 * q;
+            Zl[(rb + r) * kS + col] = acc[t][0];
+            Zl[(rb + r) * kS + col + 1] = acc[t][1];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) tk_cluster(const double* __restrict__ G, int n, int p, int iters,
+                                                  double* __restrict__ X, double* __restrict__ out) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) double sm_cl[];
+    const int crank = static_cast<int>(cl.block_rank());
+    const int nk = (n + 31) & ~31, gs = ((nk + 15) & ~15) + 4;
+    const int nb = (((n + kTkNC - 1) / kTkNC) + 7) & ~7;
+    const int nw = max(nk, kTkNC * nb);
+    const int r0 = crank * nb, nl = max(0, min(n, r0 + nb) - r0);
+    double* Gl = sm_cl;               // nb x gs: rows [r0, r0 + nl) of G, zero padded
+    double* W = Gl + nb * gs;         // nw x kS: the full basis (rows >= n zero)
+    double* Zl = W + nw * kS;         // nb x kS
+    double* Pg = Zl + nb * kS;        // 2 x 32 x kS: partial Grams (double-buffered, read remotely)
+    double* C = Pg + 2 * kP * kS;     // 32 x kS
+    double* E = C + kP * kS;          // 32 x kS
+    double* Ys = E + kP * kS;         // 32 x kS (Rayleigh-Ritz)
+    double* rinv = Ys + kP * kS;      // 32
+    double* part = rinv + kP;         // kTkNC x (2 kP + 1): residual / trace partials (CTA 0's is used)
+    __shared__ double red[32];
+    __shared__ int bad;
+    __shared__ int order_s[64];
+    __shared__ double th_s[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // ---- load the owned rows of G, generate W (the same seeded hash as tk_random)
+    for (int e = tid; e < nb * nk; e += blockDim.x) {
+        const int i = e / nk, k = e % nk;
+        if (i < nl && k < n)
+            cp_async8(Gl + i * gs + k, G + static_cast<size_t>(r0 + i) * n + k);
+        else
+            Gl[i * gs + k] = 0.0;
+    }
+    for (int e = tid; e < nw * kP; e += blockDim.x) {
+        const int i = e >> 5, j = e & 31;
+        W[i * kS + j] = (i < n && j < p) ? tk_hash_unit(static_cast<unsigned>(i) + 7u, static_cast<unsigned>(j) + 1u)
+                                         : 0.0;
+    }
+    if (tid == 0) bad = 0;
+    cp_wait_all();
+    __syncthreads();
+    int pb = 0;  // partial-Gram buffer toggle
+    auto reduce_pg = [&](double* dst) {  // dst = sum over the cluster of Pg[pb], fixed order
+        for (int e = tid; e < kP * kP; e += blockDim.x) {
+            const int off = pb * kP * kS + (e >> 5) * kS + (e & 31);
+            double v = 0.0;
+#pragma unroll
+            for (int c = 0; c < kTkNC; ++c) v += cl.map_shared_rank(Pg, c)[off];
+            dst[(e >> 5) * kS + (e & 31)] = v;
+        }
+    };
+    for (int it = 0; it < iters; ++it) {
+        tk_cl_gq(Gl, gs, W, nk, nb, Zl);
+        __syncthreads();
+        for (int pass = 0; pass < 3; ++pass) {
+            tk_atb(Zl, Zl, nb, Pg + pb * kP * kS, 0.0);
+            cl.sync();
+            reduce_pg(C);
+            __syncthreads();
+            if (pass == 0) {  // CholQR3 shift from |Z|_F^2 = trace C (identical in every CTA)
+                double tr = 0.0;
+                for (int j = 0; j < p; ++j) tr += C[j * kS + j];
+                const double shift =
+                    11.0 * (static_cast<double>(n) * p + static_cast<double>(p) * (p + 1)) * (DBL_EPSILON / 2) * tr;
+                __syncthreads();
+                if (tid < p) C[tid * kS + tid] += shift;
+            }
+            pb ^= 1;
+            if (tk_chol_inv(C, E, rinv, p, &bad)) break;
+            tk_cl_apply(Zl, nb, E, rinv);
+            __syncthreads();
+        }
+        if (bad) break;  // identical in every CTA
+        // all-gather the new basis rows into every CTA's W
+        for (int e = tid; e < nl * kP; e += blockDim.x) {
+            const int i = e >> 5, j = e & 31;
+            const double v = j < p ? Zl[i * kS + j] : 0.0;
+#pragma unroll
+            for (int c = 0; c < kTkNC; ++c) cl.map_shared_rank(W, c)[(r0 + i) * kS + j] = v;
+        }
+        cl.sync();
+    }
+    if (bad) {
+        if (crank == 0 && tid == 0) reinterpret_cast<int*>(out + 2 * p + 1)[0] = 1;
+        cl.sync();
+        return;
+    }
+    // ---- Rayleigh-Ritz: Z = G Q, H = sym(Q^T Z) over the cluster
+    tk_cl_gq(Gl, gs, W, nk, nb, Zl);
+    __syncthreads();
+    tk_atb(W + r0 * kS, Zl, nb, Pg + pb * kP * kS, 0.0);  // local Q rows (zero beyond n)
+    cl.sync();
+    reduce_pg(E);  // E <- Q^T Z
+    __syncthreads();
+    double* H = C;
+    for (int e = tid; e < kP * kP; e += blockDim.x) {
+        const int a = e >> 5, b = e & 31;
+        H[a * kS + b] = 0.5 * (E[a * kS + b] + E[b * kS + a]);
+    }
+    __syncthreads();
+    double* Yt = E;
+    for (int e = tid; e < kP * kP; e += blockDim.x) Yt[(e >> 5) * kS + (e & 31)] = (e >> 5) == (e & 31) ? 1.0 : 0.0;
+    __syncthreads();
+    tk_jacobi(H, Ys, Yt, p, red);
+    if (tid < p) {
+        const double t = H[tid * kS + tid];
+        int rk = 0;
+        for (int q = 0; q < p; ++q) {
+            const double u = H[q * kS + q];
+            rk += (u > t || (u == t && q < tid)) ? 1 : 0;
+        }
+        order_s[rk] = tid;
+    }
+    __syncthreads();
+    for (int e = tid; e < kP * kP; e += blockDim.x) {
+        const int m = e >> 5, j = e & 31;
+        Ys[m * kS + j] = (m < p && j < p) ? Yt[order_s[j] * kS + m] : 0.0;
+    }
+    if (tid < p) th_s[tid] = H[order_s[tid] * kS + order_s[tid]];
+    if (tid >= p && tid < kP) th_s[tid] = 0.0;
+    __syncthreads();
+    // X_c = Q_c Y, R_c = Z_c Y - X_c diag(theta): warp w row block w & 3, column tiles 2 (w >> 2) + {0, 1}
+    double* wpart = Pg + (pb ^ 1) * kP * kS;  // 8 warps x 32 columns (that buffer is no longer read remotely)
+    {
+        const int q = lane & 3, r = lane >> 2;
+        const int rb = (warp & 3) * 8, t0 = (warp >> 2) * 2;
+        double x[2][2] = {}, w2[2][2] = {};
+        if (rb < nb) {
+#pragma unroll
+            for (int k = 0; k < kP; k += 4) {
+                const double aq = W[(r0 + rb + r) * kS + k + q], az = Zl[(rb + r) * kS + k + q];
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const double b = Ys[(k + q) * kS + 8 * (t0 + t) + r];
+                    dmma(x[t][0], x[t][1], aq, b);
+                    dmma(w2[t][0], w2[t][1], az, b);
+                }
+            }
+        }
+        const int i = rb + r;
+        double acc[2][2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int j = 8 * (t0 + t) + 2 * q + e;
+                const double rr = w2[t][e] - th_s[j] * x[t][e];
+                acc[t][e] = (rb < nb && i < nl) ? rr * rr : 0.0;
+                if (rb < nb && i < nl && j < p) X[static_cast<size_t>(r0 + i) * p + j] = x[t][e];
+            }
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double v = acc[t][e];
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                v += __shfl_xor_sync(0xffffffffu, v, 16);
+                if (r == 0) wpart[warp * kP + 8 * (t0 + t) + 2 * q + e] = v;
+            }
+    }
+    __syncthreads();
+    // CTA partials (fixed warp order: warps w and w + 4 cover the same columns of different tiles)
+    double* dst0 = cl.map_shared_rank(part, 0) + crank * (2 * kP + 1);
+    if (tid < kP) {
+        double s2 = 0.0;
+        for (int w = 0; w < 8; ++w) s2 += ((w >> 2) * 16 <= tid && tid < (w >> 2) * 16 + 16) ? wpart[w * kP + tid] : 0.0;
+        dst0[tid] = s2;
+    }
+    double tr = 0.0;
+    for (int i = tid; i < nl; i += blockDim.x) tr += Gl[i * gs + r0 + i];
+    tr = tk_block_sum(tr, red);
+    if (tid == 0) dst0[2 * kP] = tr;
+    cl.sync();
+    if (crank == 0 && tid < p) {
+        double s2 = 0.0;
+        for (int c = 0; c < kTkNC; ++c) s2 += part[c * (2 * kP + 1) + tid];
+        out[tid] = th_s[tid];
+        out[p + tid] = sqrt(s2);
+    }
+    if (crank == 0 && tid == 0) {
+        double t = 0.0;
+        for (int c = 0; c < kTkNC; ++c) t += part[c * (2 * kP + 1) + 2 * kP];
+        out[2 * p] = t;
+    }
+}
+
 }  // namespace
 
 #ifdef TCB_TOPK_TIMING
@@ -618,8 +881,58 @@ void topk_eig(const double* G, u64 n64, int p, int extra_iters, double* X, std::
         return true;
     }();
     (void)attr;
-    DevBuf<double> W(n64 * p, s), Z(n64 * p, s), out(2 * p + 2, s);
+    DevBuf<double> out(2 * p + 2, s);
     TCB_CUDA(cudaMemsetAsync(out.p, 0, (2 * p + 2) * sizeof(double), s));
+    // one launch on an 8-CTA cluster when it fits (the multi-launch path below otherwise)
+    {
+        const int nk = (n + 31) & ~31, gs = ((nk + 15) & ~15) + 4;
+        const int nb = (((n + kTkNC - 1) / kTkNC) + 7) & ~7, nw = std::max(nk, kTkNC * nb);
+        const size_t smem = (static_cast<size_t>(nb) * gs + static_cast<size_t>(nw) * kS + nb * kS + 5 * kP * kS +
+                             kP + kTkNC * (2 * kP + 1)) * sizeof(double);
+        static const bool cl_attr = [] {
+            return cudaFuncSetAttribute(tk_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024) ==
+                   cudaSuccess;
+        }();
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(kTkNC);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = kTkNC;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        static int ncl = -1;
+        if (ncl < 0) {
+            if (!cl_attr || cudaOccupancyMaxActiveClusters(&ncl, tk_cluster, &cfg) != cudaSuccess) ncl = 0;
+            cudaGetLastError();
+        }
+        const char* e = std::getenv("TCB_TOPK_NO_CLUSTER");
+        if (ncl > 0 && smem <= 224 * 1024 && !(e && *e && *e != '0')) {
+            TCB_CUDA(cudaLaunchKernelEx(&cfg, tk_cluster, G, n, p, extra_iters + 1, X, out.p));
+            count_launch(1);
+            TCB_LAUNCH();
+            std::vector<double> h(2 * p + 2);
+            out.download(h.data(), 2 * p + 2);
+            TCB_CUDA(cudaStreamSynchronize(s));
+            int failed = 0;
+            std::memcpy(&failed, &h[2 * p + 1], sizeof(int));
+            if (failed) {
+                theta.assign(p, 0.0);
+                resid.assign(p, HUGE_VAL);
+                trace = 0.0;
+                return;
+            }
+            theta.assign(h.begin(), h.begin() + p);
+            resid.assign(h.begin() + p, h.begin() + 2 * p);
+            trace = h[2 * p];
+            return;
+        }
+    }
+    DevBuf<double> W(n64 * p, s), Z(n64 * p, s);
     int* fail = reinterpret_cast<int*>(out.p + 2 * p + 1);
     tk_random<<<cdiv(n64 * p, 256), 256, 0, s>>>(W.p, n, p);
     const size_t nr = (n64 + 7) & ~u64{7}, nk = (n64 + 31) & ~u64{31}, gs = ((nk + 15) & ~u64{15}) + 4;
