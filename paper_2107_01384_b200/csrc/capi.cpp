@@ -1,6 +1,7 @@
 // extern "C" boundary (include/tucomp_b200.h).  Each entry point owns one CUDA
 // stream for the call, converts exceptions into status + message, and never
 // falls back to host computation.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -36,6 +37,22 @@ bool prof_enabled() { return g_prof; }
 namespace {
 std::mutex g_trace_mu;
 std::map<std::string, std::pair<double, u64>> g_trace;
+// TCB_TIMELINE=1: every ProfScope records a (stream, start, end) event pair without
+// serialising anything; dumped relative to the call's first event (debugging aid)
+bool timeline_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_TIMELINE");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+struct TlRec {
+    int cat;
+    cudaStream_t st;
+    cudaEvent_t a, b;
+};
+std::vector<TlRec> g_tl;
+std::mutex g_tl_mu;
 bool trace_on() {
     static const bool on = [] {
         const char* e = std::getenv("TCB_TRACE");
@@ -53,15 +70,18 @@ long long now_ns() {
 HostTrace::HostTrace(const char* l) : label(l) {
     if (trace_on()) t0 = now_ns();
 }
-HostTrace::~HostTrace() {
-    if (!trace_on()) return;
+void HostTrace::stop() {
+    if (done || !trace_on()) return;
+    done = true;
     const double ms = (now_ns() - t0) * 1e-6;
     std::lock_guard<std::mutex> lk(g_trace_mu);
     auto& e = g_trace[label];
     e.first += ms;
     e.second += 1;
 }
+void timeline_dump();
 void host_trace_dump() {
+    timeline_dump();
     if (!trace_on()) return;
     std::lock_guard<std::mutex> lk(g_trace_mu);
     for (auto& [k, v] : g_trace) std::fprintf(stderr, "[tcb trace] %-28s %8.3f ms  x%llu\n", k.c_str(), v.first,
@@ -70,7 +90,7 @@ void host_trace_dump() {
 }
 
 ProfScope::ProfScope(Cat c, cudaStream_t s) : cat(c), st(s) {
-    if (!g_prof) return;
+    if (!g_prof && !timeline_on()) return;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a, s);
@@ -78,7 +98,51 @@ ProfScope::ProfScope(Cat c, cudaStream_t s) : cat(c), st(s) {
 ProfScope::~ProfScope() {
     if (!a) return;
     cudaEventRecord(b, st);
-    g_recs.push_back({cat, a, b});
+    if (g_prof) {
+        g_recs.push_back({cat, a, b});
+    } else {
+        std::lock_guard<std::mutex> lk(g_tl_mu);
+        g_tl.push_back({cat, st, a, b});
+    }
+}
+
+void timeline_dump() {
+    if (!timeline_on()) return;
+    const cudaError_t se = cudaDeviceSynchronize();
+    std::lock_guard<std::mutex> lk(g_tl_mu);
+    if (se != cudaSuccess || g_tl.empty()) {
+        std::fprintf(stderr, "[tcb tl] sync: %s, %zu records, first query %s\n", cudaGetErrorString(se), g_tl.size(),
+                     g_tl.empty() ? "-" : cudaGetErrorString(cudaEventQuery(g_tl[0].a)));
+    }
+    if (g_tl.empty()) return;
+    static const char* names[] = {"ingest", "permute", "gram", "eig", "ttm", "quant", "stats", "emit", "ac", "factor", "sum"};
+    cudaEvent_t ref = g_tl[0].a;
+    std::vector<std::pair<float, std::string>> lines;
+    std::map<cudaStream_t, int> sid;
+    for (auto& r : g_tl) {
+        float t0 = 0, t1 = 0;
+        const cudaError_t e0 = cudaEventElapsedTime(&t0, ref, r.a);
+        const cudaError_t e1 = cudaEventElapsedTime(&t1, ref, r.b);
+        if (e0 != cudaSuccess || e1 != cudaSuccess) {
+            std::fprintf(stderr, "[tcb tl] event error %s / %s\n", cudaGetErrorString(e0), cudaGetErrorString(e1));
+            cudaGetLastError();
+        }
+        if (!sid.count(r.st)) {
+            const int k = static_cast<int>(sid.size());
+            sid[r.st] = k;
+        }
+        char buf[160];
+        std::snprintf(buf, sizeof(buf), "[tcb tl] s%-2d %-8s %8.3f -> %8.3f ms (%6.3f)", sid[r.st], names[r.cat], t0, t1,
+                      t1 - t0);
+        lines.push_back({t0, buf});
+    }
+    for (auto& r : g_tl) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    std::sort(lines.begin(), lines.end(), [](auto& x, auto& y) { return x.first < y.first; });
+    for (auto& l : lines) std::fprintf(stderr, "%s\n", l.second.c_str());
+    g_tl.clear();
 }
 
 double peak_dmma_tflops();

@@ -318,18 +318,21 @@ __global__ void __launch_bounds__(kCrossThreads) crossing_kernel(const u64* __re
                     kk[u] = q0 + u < cnt ? kd[q0 + u] : 0;
                     tt[u] = q0 + u < cnt ? tg[q0 + u] : 0.0;
                 }
+                // branch-free: kinds 0 and 1 carry a zero gain (x + 0 = x exactly), and
+                // `going` is re-evaluated after every element (unchanged sums repeat the
+                // previous verdict), so the chain is one add per element
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int kq = kk[u];
-                    if (!going || kq == 0) continue;
-                    if (kq >= 2) cum = __dadd_rn(cum, tt[u]);
+                    const bool counted = going && kq != 0;
+                    cum = __dadd_rn(cum, tt[u]);
                     if (category == 2) {
-                        if (kq == 3) ++nt;
-                        else ++nl;
+                        nt += (counted && kq == 3) ? 1u : 0u;
+                        nl += (counted && kq != 3) ? 1u : 0u;
                     } else {
-                        ++c;
+                        c += counted ? 1u : 0u;
                     }
-                    if (!(cum < nd)) going = false;
+                    going = going && cum < nd;
                 }
             }
         }
@@ -615,8 +618,10 @@ __global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, co
         return;
     }
     const AcDesc d = desc[sidx];
-    // kShared: the model lives in shared memory (LDS/STS, no generic accesses)
-    const u32 cap = kShared ? min(d.cap, smem_cap) : d.cap;
+    // kShared: the model lives in shared memory (LDS/STS, no generic accesses).
+    // Capacity from the actual symbol count (the host sizes buffers from bounds).
+    const u32 cap_need = static_cast<u32>(ns + 1);
+    const u32 cap = kShared ? min(cap_need, smem_cap) : cap_need;
     u32* base = kShared ? reinterpret_cast<u32*>(ac_smem) : scratch + d.model_off;
     u32* cnt = base;
     u32* l1 = cnt + cap;
@@ -768,19 +773,39 @@ __global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, co
         const u32 cum = isnew ? 0u : base + 32u * within;
         const u32 freq = isnew ? 1u : f0 + 32u * __popc(same & below_me);
         const u32 tot = total + 32u * static_cast<u32>(lane);
+        // floor(range / T) by multiply-high: with m = ceil(2^64 / T) the product's high
+        // word is exact for range < 2^32 and 1 < T < 2^32 (the error term is below
+        // 2^-32 while a non-integer quotient is at least 1/T below the next integer);
+        // each lane prepares its own T's multiplier off the sequential path.
+        const u64 magic = tot > 1u ? (~u64{0} / tot) + 1u : 0u;
         // range coder over the chunk (identical state in every lane)
         for (u32 l = 0; l < L; ++l) {
             const u32 c = __shfl_sync(0xffffffffu, cum, l), f = __shfl_sync(0xffffffffu, freq, l);
             const u32 T = __shfl_sync(0xffffffffu, tot, l);
             const u64 v = __shfl_sync(0xffffffffu, sv, l);
-            range /= T;
+            const u64 M = __shfl_sync(0xffffffffu, magic, l);
+            range = T > 1u ? static_cast<u32>(__umul64hi(static_cast<u64>(range), M)) : range;
             low += static_cast<u64>(c) * range;
             range *= f;
             norm();
             if ((newm >> l) & 1u) {
-                for (int b = 31; b >= 0; --b) {  // 32 raw bits as encode(bit, 1, 2)
-                    range >>= 1;
-                    if ((v >> b) & 1u) low += range;
+                // 32 raw bits, MSB first, each encode(bit, 1, 2): range >>= 1; low += bit ?
+                // range : 0; norm().  With range in [2^24, 2^32) exactly k = floor(log2
+                // range) - 23 halvings happen before the next normalisation, so up to k
+                // bits go at once: low += sum_j bit_j (range >> j), range >>= k, norm().
+                // Identical arithmetic, about five groups instead of 32 steps.
+                const u32 raw = static_cast<u32>(v);
+                int left = 32;
+                while (left > 0) {
+                    const int k = min(left, (31 - __clz(static_cast<int>(range))) - 23);
+                    const u32 c = (raw >> (left - k)) & ((1u << k) - 1u);
+                    u64 add = 0;
+#pragma unroll
+                    for (int j = 1; j <= 8; ++j)
+                        if (j <= k && ((c >> (k - j)) & 1u)) add += range >> j;
+                    low += add;
+                    range >>= k;
+                    left -= k;
                     norm();
                 }
             }
@@ -860,6 +885,26 @@ void run_ac(const u64* syms, const StreamOut* so, const AcDesc* dad, const std::
         ac_kernel<false><<<static_cast<unsigned>(ids.size()), 32, 0, s>>>(syms, so, dad, dids.p, ns, ent, scratch, elen, 0,
                                                                   redo.p);
     }
+    count_launch();
+    TCB_LAUNCH();
+}
+
+// Launch-only variant for emit_planes: every stream's shared-memory pass with
+// the largest model that fits; streams whose model overflows report ~0 in
+// elen and are rerun by the caller from global scratch once the lengths are
+// back on the host (no extra round trip in the common case).
+void launch_ac_shared(const u64* syms, const StreamOut* so, const AcDesc* dad, int ns, u8* ent, u64* elen,
+                      int* redo, cudaStream_t s) {
+    const u64 smem = ac_model_words(kAcSmemCap) * 4 + 16;
+    static bool attr = [] {
+        cudaFuncSetAttribute(ac_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(ac_model_words(kAcSmemCap) * 4 + 16));
+        return true;
+    }();
+    (void)attr;
+    ProfScope pa(kAc, s);
+    ac_kernel<true><<<static_cast<unsigned>(ns), 32, smem, s>>>(syms, so, dad, nullptr, ns, ent, nullptr, elen,
+                                                         kAcSmemCap, redo);
     count_launch();
     TCB_LAUNCH();
 }
@@ -1051,7 +1096,7 @@ __global__ void assemble_kernel(const u8* __restrict__ ent, const AcDesc* __rest
 // ================================================================ host launchers
 SumRec device_sum(SumKind kind, const u64* m, const u64* dec, u64 n, int plane, cudaStream_t s) {
     ProfScope prof_scope(kSum, s);
-    const int grid = sm_count() * 4;
+    const int grid = grid_for(n, kSumThreads, 4, 4);
     DevBuf<SumRec> part(grid, s);
     sum_kernel<<<grid, kSumThreads, 0, s>>>(kind, m, dec, n, plane, part.p);
     count_launch();
@@ -1205,6 +1250,10 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
             raw_words += (d.hi - d.lo + 31) / 32;
         }
     }
+    // No round trip between the symbol pass and the coder: entropy buffers are
+    // sized from per-stream bounds (symbols <= positions + 1); the coder reads
+    // the actual counts on the device.
+    HostTrace ht_a("emit: symbols+entropy+sync");
     DevBuf<StreamDesc> dsd(ns, s);
     dsd.upload(sd.data(), ns);
     DevBuf<u64> syms(sym_total, s);
@@ -1217,47 +1266,73 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
     }
     count_launch();
     TCB_LAUNCH();
-    std::vector<StreamOut> soh(ns);
-    so.download(soh.data(), ns);
-    TCB_CUDA(cudaStreamSynchronize(s));
-    // model scratch and output capacity per stream
     std::vector<AcDesc> ad(ns);
     u64 out_total = 0, scratch_total = 0;
     for (u64 i = 0; i < ns; ++i) {
         AcDesc& a = ad[i];
         a.sym_off = sd[i].sym_off;
-        const u64 k = soh[i].nsyms;
+        const u64 kmax = sd[i].hi - sd[i].lo + 1;
         a.out_off = out_total;
-        const u32 cap = static_cast<u32>(k + 1);
-        a.cap = cap;
+        a.cap = static_cast<u32>(kmax + 1);
         a.fen = 0;
-        a.hbits = log2_at_least(2 * cap);
+        a.hbits = log2_at_least(2 * a.cap);
         if (coder == 1) {
-            out_total += k ? rans_out_cap(k) : 0;
+            out_total += rans_out_cap(kmax);
             a.model_off = (scratch_total + 1) & ~u64{1};
-            if (k) scratch_total = a.model_off + rans_scratch_words(k);
+            scratch_total = a.model_off + rans_scratch_words(kmax);
         } else {
-            out_total += k ? 5 + 7 * k + 16 : 0;
-            a.model_off = scratch_total;
-            if (k) scratch_total += ac_model_words(cap);
+            out_total += 5 + 7 * kmax + 16;
+            a.model_off = 0;  // global scratch only for an overflow rerun (set below)
         }
     }
     DevBuf<AcDesc> dad(ns, s);
     dad.upload(ad.data(), ns);
     DevBuf<u8> ent(out_total + 1, s);
-    DevBuf<u32> scratch(scratch_total + 2, s);
     DevBuf<u64> elen(ns, s);
-    if (coder == 1)
+    DevBuf<u32> scratch(coder == 1 ? scratch_total + 2 : 2, s);
+    DevBuf<int> redo(1, s);
+    if (coder == 1) {
         run_rans(syms.p, so.p, dad.p, static_cast<int>(ns), ent.p, scratch.p, elen.p, s);
-    else
-        run_ac(syms.p, so.p, dad.p, ad, soh, static_cast<int>(ns), ent.p, scratch.p, elen.p, s);
+    } else {
+        redo.zero();
+        launch_ac_shared(syms.p, so.p, dad.p, static_cast<int>(ns), ent.p, elen.p, redo.p, s);
+    }
     std::vector<u64> el(ns);
+    std::vector<StreamOut> soh(ns);
     elen.download(el.data(), ns);
+    so.download(soh.data(), ns);
     TCB_CUDA(cudaStreamSynchronize(s));
+    if (coder == 0) {  // rerun the streams whose model outgrew shared memory from global scratch
+        std::vector<int> ids;
+        u64 words = 0;
+        for (u64 i = 0; i < ns; ++i)
+            if (el[i] == ~u64{0}) {
+                ids.push_back(static_cast<int>(i));
+                ad[i].model_off = words;
+                words += ac_model_words(static_cast<u32>(soh[i].nsyms + 1));
+            }
+        if (!ids.empty()) {
+            DevBuf<u32> gscr(words + 2, s);
+            dad.upload(ad.data(), ns);
+            DevBuf<int> dids(ids.size(), s);
+            dids.upload(ids.data(), ids.size());
+            {
+                ProfScope pa(kAc, s);
+                ac_kernel<false><<<static_cast<unsigned>(ids.size()), 32, 0, s>>>(
+                    syms.p, so.p, dad.p, dids.p, static_cast<int>(ns), ent.p, gscr.p, elen.p, 0, redo.p);
+            }
+            count_launch();
+            TCB_LAUNCH();
+            elen.download(el.data(), ns);
+            TCB_CUDA(cudaStreamSynchronize(s));
+        }
+    }
     for (u64 v : el)
         if (v == ~u64{1}) throw Error("entropy: cannot normalize rans table");
     res.entropy_bytes = el;
+    ht_a.stop();
     if (!want_body) return res;
+    HostTrace ht_b("emit: assemble+sync");
     std::vector<u64> off(ns);
     u64 tot = 0;
     for (u64 i = 0; i < ns; ++i) {

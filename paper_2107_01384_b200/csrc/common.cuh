@@ -89,6 +89,15 @@ inline int sm_count() {
 
 inline unsigned cdiv(u64 a, u64 b) { return static_cast<unsigned>((a + b - 1) / b); }
 
+// Grid for a grid-stride pass over n elements: per_sm CTAs per SM for large n,
+// but no more CTAs than there are `per_thread`-element slices (a 3k-element
+// core gets a handful of CTAs, not 600, and a 600-entry partial array).
+inline int grid_for(u64 n, int threads, int per_thread, int per_sm) {
+    const u64 want = (n + static_cast<u64>(threads) * per_thread - 1) / (static_cast<u64>(threads) * per_thread);
+    const u64 cap = static_cast<u64>(sm_count()) * per_sm;
+    return static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
 // Launch counter for the bench's "gpu_launches" claim.
 std::atomic<u64>& launch_counter();
 inline void count_launch(u64 k = 1) { launch_counter().fetch_add(k, std::memory_order_relaxed); }
@@ -103,9 +112,11 @@ enum Cat : int { kIngest = 0, kPermute, kGram, kEig, kTtm, kQuant, kStats, kEmit
 // stderr by tcb_compress / tcb_compress_device; a debugging aid only.
 struct HostTrace {
     explicit HostTrace(const char* label);
-    ~HostTrace();
+    ~HostTrace() { stop(); }
+    void stop();  // record now (idempotent)
     const char* label;
     long long t0 = 0;
+    bool done = false;
 };
 void host_trace_dump();
 struct ProfScope {

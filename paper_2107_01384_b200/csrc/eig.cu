@@ -907,14 +907,23 @@ __global__ void sign_kernel(double* __restrict__ U, int n, int r) {
 // U (row-major n x r): column j /= sigma_j, then modified Gram-Schmidt; a
 // column that collapses is replaced by the first unit vector orthogonal to
 // the others (orthonormal completion for zero singular values).
-__global__ void scale_mgs_kernel(double* __restrict__ U, int n, int r, const double* __restrict__ sigma) {
+__global__ void scale_cols_kernel(double* __restrict__ U, int n, int r, const double* __restrict__ sigma) {
+    const u64 total = static_cast<u64>(n) * r;
+    for (u64 e = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const double sg = sigma[e % r];
+        if (sg > 0.0) U[e] /= sg;
+    }
+}
+
+// Modified Gram-Schmidt with reorthogonalisation (a vanishing column is
+// replaced by the first unit vector that survives).  With `skip`, it runs only
+// if the CholQR pass before it reported a failure (*skip != 0).
+__global__ void mgs_kernel(double* __restrict__ U, int n, int r, const int* __restrict__ skip) {
+    if (skip && *skip == 0) return;
     extern __shared__ double sh_mgs[];
     double* red = sh_mgs;
     for (int j = 0; j < r; ++j) {
-        const double sg = sigma[j];
-        if (sg > 0.0)
-            for (int i = threadIdx.x; i < n; i += blockDim.x) U[static_cast<size_t>(i) * r + j] /= sg;
-        __syncthreads();
         for (int attempt = 0; attempt <= n; ++attempt) {
             if (attempt > 0)
                 for (int i = threadIdx.x; i < n; i += blockDim.x)
@@ -1124,10 +1133,17 @@ void fix_column_signs(double* U, u64 n, u64 r, cudaStream_t s) {
     TCB_LAUNCH();
 }
 
+// U <- orth(U diag(1/sigma)) (the thin branch, sthosvd.cpp:91-99 stand-in): the
+// columns are already nearly orthonormal, so shifted CholQR3 on one CTA
+// (topk.cu) does it in a few DMMA passes; MGS runs only if that reports a
+// Cholesky breakdown (or the panel is too large for it).
 void scale_orthonormalize(double* U, u64 n, u64 r, const double* sigma, cudaStream_t s) {
     ProfScope prof_scope(kEig, s);
-    scale_mgs_kernel<<<1, 256, 32 * sizeof(double), s>>>(U, static_cast<int>(n), static_cast<int>(r), sigma);
-    count_launch();
+    scale_cols_kernel<<<grid_for(n * r, 256, 4, 4), 256, 0, s>>>(U, static_cast<int>(n), static_cast<int>(r), sigma);
+    DevBuf<int> fail(1, s);
+    const bool fast = cholqr_inplace(U, n, static_cast<int>(r), fail.p, s);
+    mgs_kernel<<<1, 256, 32 * sizeof(double), s>>>(U, static_cast<int>(n), static_cast<int>(r), fast ? fail.p : nullptr);
+    count_launch(2);
     TCB_LAUNCH();
 }
 

@@ -79,7 +79,10 @@ struct Planner {
             return batch.data();
         }
         if (p > batch_hi || p < batch_lo) {
-            const int lo = std::max(floor_p, p - 7);
+            // planes per batch: every remaining plane when the core is small (each plane
+            // is a pass over the magnitudes; one round trip instead of one per 8 planes)
+            const int span = n <= (u64{1} << 18) ? 63 : n <= (u64{1} << 21) ? 15 : 7;
+            const int lo = std::max(floor_p, p - span);
             batch.resize(nb * (p - lo + 1));
             HostTrace ht("plan: plane_stats batch");
             plane_stats(m, n, block, p, lo, batch.data(), s);

@@ -5,6 +5,8 @@
 #include <cmath>
 #include <cstdint>
 
+#include <cstring>
+
 #include "kernels.cuh"
 
 namespace tcb {
@@ -30,7 +32,7 @@ __global__ void copy16_kernel(const double2* __restrict__ src, double2* __restri
 template <class T>
 void cast_any(const void* src, int dtype, u64 n, T* dst, cudaStream_t s) {
     ProfScope prof_scope(kIngest, s);
-    const unsigned grid = static_cast<unsigned>(sm_count() * 8), blk = 256;
+    const unsigned grid = static_cast<unsigned>(grid_for(n, 256, 4, 8)), blk = 256;
     switch (dtype) {
         case 0: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const int8_t*>(src), dst, n); break;
         case 1: cast_kernel<<<grid, blk, 0, s>>>(static_cast<const uint8_t*>(src), dst, n); break;
@@ -150,7 +152,7 @@ __global__ void sum_stage2(const double* __restrict__ part, int n, double* __res
 template <class T>
 double sumsq_impl(const T* x, u64 n, bool* finite, cudaStream_t s) {
     ProfScope prof_scope(kIngest, s);
-    const int grid = sm_count() * 4;
+    const int grid = grid_for(n, kRedThreads, 8, 4);
     DevBuf<double> part(grid + 1, s);
     DevBuf<int> bad(1, s);
     bad.zero();
@@ -290,7 +292,7 @@ bool ingest_precision_loss(const void* src, int dtype, u64 n, cudaStream_t s) {
     ProfScope prof_scope(kIngest, s);
     DevBuf<int> f(1, s);
     f.zero();
-    precision_kernel<<<sm_count() * 4, 256, 0, s>>>(src, dtype == 6 ? 1 : 0, n, f.p);
+    precision_kernel<<<grid_for(n, 256, 4, 4), 256, 0, s>>>(src, dtype == 6 ? 1 : 0, n, f.p);
     count_launch();
     TCB_LAUNCH();
     return f.to_host()[0] != 0;
@@ -330,7 +332,7 @@ __global__ void sse_stage1(const double* __restrict__ a, const double* __restric
 }
 
 double sse_between(const double* a, const double* b, u64 n, bool f32, cudaStream_t s) {
-    const int grid = sm_count() * 4;
+    const int grid = grid_for(n, kRedThreads, 4, 4);
     DevBuf<double> part(grid + 1, s);
     if (f32)
         sse_stage1<true><<<grid, kRedThreads, 0, s>>>(a, b, n, part.p);
@@ -345,9 +347,50 @@ double sse_between(const double* a, const double* b, u64 n, bool f32, cudaStream
     return r;
 }
 
+// max |x| and the finiteness flag of a (small) tensor in one pass and one round
+// trip (the quantiser's scale and its non-finite check, core_codec.cpp:55-70)
+__global__ void maxfin_stage1(const double* __restrict__ x, u64 n, double* __restrict__ part, int* __restrict__ bad) {
+    __shared__ double sh[kRedThreads / 32];
+    double m = 0.0;
+    bool nonfinite = false;
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double v = x[i];
+        nonfinite |= !isfinite(v);
+        m = fmax(m, fabs(v));
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+    if (__syncthreads_or(nonfinite) && threadIdx.x == 0) *bad = 1;
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) t = fmax(t, sh[w]);
+        part[blockIdx.x] = t;
+    }
+}
+
+double max_abs_finite(const double* x, u64 n, bool* finite, cudaStream_t s) {
+    ProfScope prof_scope(kSum, s);
+    const int grid = grid_for(n, kRedThreads, 4, 4);
+    DevBuf<double> part(grid + 2, s);
+    int* bad = reinterpret_cast<int*>(part.p + grid + 1);
+    TCB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    maxfin_stage1<<<grid, kRedThreads, 0, s>>>(x, n, part.p, bad);
+    max_stage2<<<1, 1024, 0, s>>>(part.p, grid, part.p + grid);
+    count_launch(2);
+    TCB_LAUNCH();
+    double r[2] = {0, 0};
+    TCB_CUDA(cudaMemcpyAsync(r, part.p + grid, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    TCB_CUDA(cudaStreamSynchronize(s));
+    int b = 0;
+    std::memcpy(&b, &r[1], sizeof(int));
+    *finite = b == 0;
+    return r[0];
+}
+
 double max_abs(const double* x, u64 n, cudaStream_t s) {
     ProfScope prof_scope(kSum, s);
-    const int grid = sm_count() * 4;
+    const int grid = grid_for(n, kRedThreads, 4, 4);
     DevBuf<double> part(grid + 1, s);
     maxabs_stage1<<<grid, kRedThreads, 0, s>>>(x, n, part.p);
     max_stage2<<<1, 1024, 0, s>>>(part.p, grid, part.p + grid);

@@ -20,6 +20,8 @@ void permute_axes(const T* src, T* dst, const std::vector<u64>& shape, const std
 bool ingest_precision_loss(const void* src, int dtype, u64 n, cudaStream_t s);
 // sum of (a_i - b_i)^2 (tensor.cpp:147-164); f32 rounds both sides to float first
 double sse_between(const double* a, const double* b, u64 n, bool f32, cudaStream_t s);
+// max |x| with the all-finite flag, one pass and one round trip
+double max_abs_finite(const double* x, u64 n, bool* finite, cudaStream_t s);
 // Exact max |x| (kernels_avx2.cpp:40-66 is order-independent, so exact on any tree).
 double max_abs(const double* x, u64 n, cudaStream_t s);
 
@@ -53,6 +55,10 @@ void eig_vectors(EigWork& w, u64 r, double* U, cudaStream_t s);
 void fix_column_signs(double* U, u64 n, u64 r, cudaStream_t s);
 // Normalise columns of U (n x r row-major) by 1/sigma_j and re-orthonormalise (MGS).
 void scale_orthonormalize(double* U, u64 n, u64 r, const double* sigma, cudaStream_t s);
+// In-place shifted CholQR3 of a row-major n x r panel (n <= 256, r <= 32) on one
+// CTA; *fail_dev is zeroed and set on a Cholesky breakdown (U then unchanged).
+// Returns false (nothing launched) when the panel does not fit.
+bool cholqr_inplace(double* U, u64 n, int r, int* fail_dev, cudaStream_t s);
 
 // ---- topk.cu: certified top-p eigenpairs by block subspace iteration + Rayleigh-Ritz.
 bool topk_supported(u64 n, int p);

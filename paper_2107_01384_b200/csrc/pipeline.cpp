@@ -545,9 +545,8 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
         ingest_cast(cf.p, 8, nc, core_s.p, s);
     }
     bool core_finite = true;
-    sum_squares(core_s.p, nc, &core_finite, s);
+    const double mx = max_abs_finite(core_s.p, nc, &core_finite, s);
     if (!core_finite) throw Error("quantize: non-finite core values");
-    const double mx = max_abs(core_s.p, nc, s);
     const bool zero = mx == 0.0;
     const int k = zero ? 0 : 63 - std::ilogb(mx);
     res.core_k = k;

@@ -184,7 +184,7 @@ DevBuf<u64> order_map_device(int method, const std::vector<u64>& shape, cudaStre
 void quantize_f64(const double* x, u64 n, int k, u64* mag, u8* neg, cudaStream_t s, const u64* order) {
     ProfScope prof_scope(kQuant, s);
     if (n == 0) return;
-    quantize_kernel<<<sm_count() * 8, 256, 0, s>>>(x, n, k, mag, neg, order);
+    quantize_kernel<<<grid_for(n, 256, 4, 8), 256, 0, s>>>(x, n, k, mag, neg, order);
     count_launch();
     TCB_LAUNCH();
 }
@@ -238,7 +238,7 @@ std::vector<u8> dead_slices(const u64* dec, const std::vector<u64>& shape, cudaS
     dm.upload(meta.data(), meta.size());
     DevBuf<u8> dead(total, s);
     TCB_CUDA(cudaMemsetAsync(dead.p, 1, total, s));
-    dead_kernel<<<sm_count() * 4, 256, 0, s>>>(dec, n, dm.p, static_cast<int>(shape.size()), dead.p, order);
+    dead_kernel<<<grid_for(n, 256, 4, 4), 256, 0, s>>>(dec, n, dm.p, static_cast<int>(shape.size()), dead.p, order);
     count_launch();
     TCB_LAUNCH();
     return dead.to_host();
@@ -254,7 +254,7 @@ void sign_fold(u8* neg, const std::vector<u64>& shape, const std::vector<signed 
     dm.upload(meta.data(), meta.size());
     DevBuf<signed char> fl(flips_by_axis.size(), s);
     fl.upload(flips_by_axis.data(), flips_by_axis.size());
-    signfold_kernel<<<sm_count() * 4, 256, 0, s>>>(neg, n, dm.p, static_cast<int>(shape.size()), fl.p, order);
+    signfold_kernel<<<grid_for(n, 256, 4, 4), 256, 0, s>>>(neg, n, dm.p, static_cast<int>(shape.size()), fl.p, order);
     count_launch();
     TCB_LAUNCH();
 }

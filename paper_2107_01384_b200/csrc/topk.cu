@@ -34,14 +34,23 @@ namespace {
 constexpr int kTkQrThreads = 256;
 
 #ifdef TCB_TOPK_TIMING
-__device__ unsigned long long g_tk_phase[16];
+__device__ unsigned long long g_tk_phase[32];
 #define TK_T(i)                                                     \
     do {                                                            \
         const long long now_ = clock64();                           \
         if (threadIdx.x == 0) atomicAdd(&g_tk_phase[i], now_ - tprev); \
         tprev = now_;                                               \
     } while (0)
+#define TK_TC(i)                                                                \
+    do {                                                                        \
+        const long long now_ = clock64();                                       \
+        if (threadIdx.x == 0 && crank == 0) atomicAdd(&g_tk_phase[i], now_ - tprev); \
+        tprev = now_;                                                           \
+    } while (0)
 #else
+#define TK_TC(i) \
+    do {         \
+    } while (0)
 #define TK_T(i) \
     do {        \
     } while (0)
@@ -698,6 +707,9 @@ __global__ void __launch_bounds__(256) tk_cluster(const double* __restrict__ G, 
     __shared__ int order_s[64];
     __shared__ double th_s[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef TCB_TOPK_TIMING
+    long long tprev = clock64();
+#endif
     // ---- load the owned rows of G, generate W (the same seeded hash as tk_random)
     for (int e = tid; e < nb * nk; e += blockDim.x) {
         const int i = e / nk, k = e % nk;
@@ -714,6 +726,7 @@ __global__ void __launch_bounds__(256) tk_cluster(const double* __restrict__ G, 
     if (tid == 0) bad = 0;
     cp_wait_all();
     __syncthreads();
+    TK_TC(16);
     int pb = 0;  // partial-Gram buffer toggle
     auto reduce_pg = [&](double* dst) {  // dst = sum over the cluster of Pg[pb], fixed order
         for (int e = tid; e < kP * kP; e += blockDim.x) {
@@ -727,11 +740,15 @@ __global__ void __launch_bounds__(256) tk_cluster(const double* __restrict__ G, 
     for (int it = 0; it < iters; ++it) {
         tk_cl_gq(Gl, gs, W, nk, nb, Zl);
         __syncthreads();
+        TK_TC(17);
         for (int pass = 0; pass < 3; ++pass) {
             tk_atb(Zl, Zl, nb, Pg + pb * kP * kS, 0.0);
+            TK_TC(18);
             cl.sync();
+            TK_TC(19);
             reduce_pg(C);
             __syncthreads();
+            TK_TC(20);
             if (pass == 0) {  // CholQR3 shift from |Z|_F^2 = trace C (identical in every CTA)
                 double tr = 0.0;
                 for (int j = 0; j < p; ++j) tr += C[j * kS + j];
@@ -742,8 +759,10 @@ __global__ void __launch_bounds__(256) tk_cluster(const double* __restrict__ G, 
             }
             pb ^= 1;
             if (tk_chol_inv(C, E, rinv, p, &bad)) break;
+            TK_TC(21);
             tk_cl_apply(Zl, nb, E, rinv);
             __syncthreads();
+            TK_TC(22);
         }
         if (bad) break;  // identical in every CTA
         // all-gather the new basis rows into every CTA's W
@@ -753,7 +772,9 @@ __global__ void __launch_bounds__(256) tk_cluster(const double* __restrict__ G, 
 #pragma unroll
             for (int c = 0; c < kTkNC; ++c) cl.map_shared_rank(W, c)[(r0 + i) * kS + j] = v;
         }
+        TK_TC(23);
         cl.sync();
+        TK_TC(24);
     }
     if (bad) {
         if (crank == 0 && tid == 0) reinterpret_cast<int*>(out + 2 * p + 1)[0] = 1;
@@ -776,7 +797,9 @@ __global__ void __launch_bounds__(256) tk_cluster(const double* __restrict__ G, 
     double* Yt = E;
     for (int e = tid; e < kP * kP; e += blockDim.x) Yt[(e >> 5) * kS + (e & 31)] = (e >> 5) == (e & 31) ? 1.0 : 0.0;
     __syncthreads();
+    TK_TC(25);
     tk_jacobi(H, Ys, Yt, p, red);
+    TK_TC(26);
     if (tid < p) {
         const double t = H[tid * kS + tid];
         int rk = 0;
@@ -858,13 +881,30 @@ __global__ void __launch_bounds__(256) tk_cluster(const double* __restrict__ G, 
         for (int c = 0; c < kTkNC; ++c) t += part[c * (2 * kP + 1) + 2 * kP];
         out[2 * p] = t;
     }
+    TK_TC(27);
 }
 
 }  // namespace
 
 #ifdef TCB_TOPK_TIMING
-void topk_phase_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_tk_phase, sizeof(unsigned long long) * 16); }
+void topk_phase_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_tk_phase, sizeof(unsigned long long) * 32); }
 #endif
+
+bool cholqr_inplace(double* U, u64 n64, int r, int* fail_dev, cudaStream_t s) {
+    if (n64 > 256 || r < 1 || r > kP || n64 < static_cast<u64>(r)) return false;
+    static const bool attr = [] {
+        cudaFuncSetAttribute(tk_cqr, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        return true;
+    }();
+    (void)attr;
+    TCB_CUDA(cudaMemsetAsync(fail_dev, 0, sizeof(int), s));
+    const size_t qld = ((n64 + 15) & ~u64{15}) + 4;
+    const size_t qsm = (kP * qld + 2 * kP * kS + kP) * sizeof(double);
+    tk_cqr<<<1, kTkQrThreads, qsm, s>>>(U, static_cast<int>(n64), r, U, fail_dev);
+    count_launch();
+    TCB_LAUNCH();
+    return true;
+}
 
 bool topk_supported(u64 n, int p) {  // shared-memory footprints: tk_rr (3 n p + 2 p^2) and tk_gq (n (p + 8))
     return p >= 8 && p <= 32 && n >= static_cast<u64>(2 * p) && n <= 256;

@@ -25,9 +25,11 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, s); tcb::topk_eig(G.p, n, 32, 2, X.p, th, res, tr, s); cudaEventRecord(e1, s); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
-    unsigned long long ph[16]; tcb::topk_phase_read(ph);
+    unsigned long long ph[32]; tcb::topk_phase_read(ph);
     printf("topk_eig n=%d: %.3f ms; theta0 %.3e res0 %.1e trace %.3e\n", n, ms, th[0], res[0], tr);
     const char* nm[7] = {"cqr load+fro", "cqr gram", "cqr chol+inv", "cqr apply", "rr load+H", "rr jacobi", "rr X+res"};
     for (int i = 0; i < 7; ++i) printf("  %-10s %llu cycles (all launches, 3 passes each)\n", nm[i], ph[i]);
-    printf("  jacobi sweeps per rr launch: %.2f\n", double(ph[8]) / double(ph[7]));
+    if (ph[7]) printf("  jacobi sweeps per rr launch: %.2f\n", double(ph[8]) / double(ph[7]));
+    const char* cn[12] = {"cl load", "cl gq", "cl gram", "cl sync", "cl reduce", "cl chol", "cl apply", "cl gather", "cl gsync", "cl rr pre", "cl jacobi", "cl tail"};
+    for (int i = 0; i < 12; ++i) if (ph[16 + i]) printf("  %-10s %llu cycles (3 calls)\n", cn[i], ph[16 + i]);
 }
