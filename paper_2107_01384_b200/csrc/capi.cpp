@@ -2,6 +2,7 @@
 // stream for the call, converts exceptions into status + message, and never
 // falls back to host computation.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -79,11 +80,27 @@ void HostTrace::stop() {
     e.first += ms;
     e.second += 1;
 }
+namespace {
+std::atomic<u64> g_syncs{0}, g_sync_ns{0};
+}
+void stream_sync(cudaStream_t s) {
+    if (!trace_on()) {
+        TCB_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    const long long t0 = now_ns();
+    TCB_CUDA(cudaStreamSynchronize(s));
+    g_syncs += 1;
+    g_sync_ns += static_cast<u64>(now_ns() - t0);
+}
+
 void timeline_dump();
 void host_trace_dump() {
     timeline_dump();
     if (!trace_on()) return;
     std::lock_guard<std::mutex> lk(g_trace_mu);
+    std::fprintf(stderr, "[tcb trace] host syncs: %llu, waiting %.3f ms (all threads)\n",
+                 static_cast<unsigned long long>(g_syncs.exchange(0)), g_sync_ns.exchange(0) * 1e-6);
     for (auto& [k, v] : g_trace) std::fprintf(stderr, "[tcb trace] %-28s %8.3f ms  x%llu\n", k.c_str(), v.first,
                                                static_cast<unsigned long long>(v.second));
     g_trace.clear();
@@ -160,7 +177,11 @@ struct Stream {
         int n = 0;
         if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
             throw Error("tucomp_b200: no CUDA device (the B200 path has no CPU fallback)");
-        TCB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        // the call's own stream carries the critical path (sthosvd, core plan and
+        // finalisation): highest priority over the factor workers' streams
+        int lo = 0, hi = 0;
+        TCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        TCB_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
         static bool pool = [] {  // keep freed pool memory mapped between calls
             int dev = 0;
             cudaGetDevice(&dev);
@@ -370,7 +391,7 @@ int tcb_decompress_tensor_f64(const uint8_t* container, uint64_t len, double** o
         for (auto v : t.shape) total *= v;
         std::vector<double> h(total);
         if (total) t.x.download(h.data(), total);
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
         *out = dup(h);
         *count = total;
         *d = static_cast<int>(t.shape.size());
@@ -432,7 +453,7 @@ int tcb_sthosvd_f64(const double* a, const uint64_t* shape, int d, double sse_ta
             f.factors[i].download(factors[i], f.n[i] * f.r[i]);
         }
         f.core.download(core, nc);
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
     });
 }
 
@@ -443,7 +464,7 @@ int tcb_gram_f64(const double* b, uint64_t rows, uint64_t cols, double* g) {
         B.upload(b, rows * cols);
         gram_f64(B.p, rows, cols, G.p, st.s);
         G.download(g, rows * rows);
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
     });
 }
 
@@ -455,7 +476,7 @@ int tcb_ttm_f64(const double* b, uint64_t rows, uint64_t cols, const double* u, 
         U.upload(u, rows * r);
         ttm_f64(B.p, rows, cols, U.p, r, O.p, st.s);
         O.download(next, cols * r);
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
     });
 }
 
@@ -473,7 +494,7 @@ int tcb_eig_f64(const double* g, uint64_t n, uint64_t r, double* evals_desc, dou
             fix_column_signs(U.p, n, r, st.s);
             U.download(u, n * r);
         }
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
     });
 }
 
@@ -507,7 +528,7 @@ int tcb_quantize_f64(const double* core, const uint64_t* shape, int d, uint64_t*
         dm.download(mag, n);
         dn.download(neg, n);
         sn.download(slice_norms_out, se);
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
     });
 }
 
@@ -529,7 +550,7 @@ int tcb_encode(const uint64_t* mag, const uint8_t* neg, uint64_t n, double targe
         const auto body = finalize_stream(m.p, ng.p, n, pl, coder, n, st.s);
         const SumRec a = n ? device_sum(SumKind::diff_backward, m.p, dec.p, n, 0, st.s) : SumRec{0, 0, 0, 0};
         if (decoded) dec.download(decoded, n);
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
         *stream = dup(body);
         *stream_len = body.size();
         *last_plane = pl.last_plane;
@@ -588,7 +609,7 @@ int tcb_dev_permute(const double* src, double* dst, const uint64_t* shape, const
     return guard([&] {
         Stream st;
         permute_axes(src, dst, std::vector<u64>(shape, shape + d), std::vector<u64>(perm, perm + d), st.s);
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
     });
 }
 
@@ -600,7 +621,7 @@ int tcb_dev_gram(const double* b, uint64_t rows, uint64_t cols, double* g) {
         } else {
             gram_f64(b, rows, cols, g, st.s);
         }
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
     });
 }
 
@@ -609,7 +630,7 @@ int tcb_dev_factor_from_gram(const double* g, uint64_t n, double budget, double*
         Stream st;
         StepOut o = factor_from_gram(g, n, budget, st.s);
         TCB_CUDA(cudaMemcpyAsync(u, o.U.p, n * o.r * sizeof(double), cudaMemcpyDeviceToDevice, st.s));
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
         *r = o.r;
         *discarded = o.discarded;
     });
@@ -622,7 +643,7 @@ int tcb_dev_mode_step(const double* b, uint64_t rows, uint64_t cols, double budg
         StepOut o = mode_step(b, rows, cols, budget, backend, st.s);
         TCB_CUDA(cudaMemcpyAsync(u, o.U.p, rows * o.r * sizeof(double), cudaMemcpyDeviceToDevice, st.s));
         TCB_CUDA(cudaMemcpyAsync(next, o.next.p, cols * o.r * sizeof(double), cudaMemcpyDeviceToDevice, st.s));
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
         *r = o.r;
         *discarded = o.discarded;
     });
@@ -632,7 +653,7 @@ int tcb_dev_ttm(const double* b, uint64_t rows, uint64_t cols, const double* u, 
     return guard([&] {
         Stream st;
         if (cols > 0) ttm_f64(b, rows, cols, u, r, next, st.s);
-        TCB_CUDA(cudaStreamSynchronize(st.s));
+        stream_sync(st.s);
     });
 }
 

@@ -874,7 +874,7 @@ void run_ac(const u64* syms, const StreamOut* so, const AcDesc* dad, const std::
     if (redo.to_host()[0] == 0) return;
     std::vector<u64> el(ns);
     TCB_CUDA(cudaMemcpyAsync(el.data(), elen, ns * sizeof(u64), cudaMemcpyDeviceToHost, s));
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     std::vector<int> ids;
     for (int i = 0; i < ns; ++i)
         if (el[i] == ~u64{0}) ids.push_back(i);
@@ -1138,7 +1138,7 @@ void plane_stats(const u64* m, u64 n, u64 block, int p_hi, int p_lo, PlaneBlockR
     count_launch(2);
     TCB_LAUNCH();
     out.download(out_host, nb * np);
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
 }
 
 void plane_stats_serial(const u64* m, u64 n, u64 block, int p, PlaneBlockRec* out_host, cudaStream_t s) {
@@ -1149,7 +1149,7 @@ void plane_stats_serial(const u64* m, u64 n, u64 block, int p, PlaneBlockRec* ou
     count_launch();
     TCB_LAUNCH();
     out.download(out_host, nb);
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
 }
 
 void crossing_scan(const u64* m, u64 n, u64 block, u64 b, int plane, int category, const double* cum,
@@ -1165,7 +1165,7 @@ void crossing_scan(const u64* m, u64 n, u64 block, u64 b, int plane, int categor
     count_launch();
     TCB_LAUNCH();
     out.download(counts_host, 2 * npairs);
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
 }
 
 void decode_model(const u64* m, u64 n, u64 block, int last_plane, const u64* stops_dev, u64* dec, cudaStream_t s) {
@@ -1196,7 +1196,7 @@ std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cu
         if (el == ~u64{1}) throw Error("entropy: cannot normalize rans table");
         std::vector<u8> out(el);
         ent.download(out.data(), el);
-        TCB_CUDA(cudaStreamSynchronize(s));
+        stream_sync(s);
         return out;
     }
     std::vector<u8> out{static_cast<u8>(coder)};
@@ -1219,7 +1219,7 @@ std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cu
     const u64 el = elen.to_host()[0];
     out.resize(el);
     ent.download(out.data(), el);
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     return out;
 }
 
@@ -1301,7 +1301,7 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
     std::vector<StreamOut> soh(ns);
     elen.download(el.data(), ns);
     so.download(soh.data(), ns);
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     if (coder == 0) {  // rerun the streams whose model outgrew shared memory from global scratch
         std::vector<int> ids;
         u64 words = 0;
@@ -1324,7 +1324,7 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
             count_launch();
             TCB_LAUNCH();
             elen.download(el.data(), ns);
-            TCB_CUDA(cudaStreamSynchronize(s));
+            stream_sync(s);
         }
     }
     for (u64 v : el)
@@ -1349,7 +1349,7 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
     TCB_LAUNCH();
     res.body.resize(tot);
     body.download(res.body.data(), tot);
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     return res;
 }
 

@@ -33,6 +33,9 @@ struct Error : std::runtime_error {
 
 constexpr u64 kFull = ~u64{0};
 
+// Host wait on a stream; counted (and timed under TCB_TRACE) per call site class.
+void stream_sync(cudaStream_t s);
+
 // Stream-ordered device buffer (cudaMallocAsync pool; freed on the same stream).
 template <class T>
 struct DevBuf {
@@ -72,7 +75,7 @@ struct DevBuf {
     std::vector<T> to_host() const {
         std::vector<T> v(n);
         download(v.data(), n);
-        TCB_CUDA(cudaStreamSynchronize(s));
+        stream_sync(s);
         return v;
     }
 };

@@ -383,7 +383,7 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
     decode_streams(dc.p, dstr.p, dblk.p, blk.size(), dsec.p, syms.p, mag.p, neg.p, pe.p, colb.p, err.p, s);
     int e = 0;
     err.download(&e, 1);
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     if (e) throw Error(dec_message(e));
     // ---- factors (decode_factor, factor_codec.cpp:246-264)
     std::vector<DevBuf<double>> U(d);
@@ -442,7 +442,7 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
         cur.push_back(nn);
     }
     permute_axes(x.p, out.x.p, cur, inverse(q), s);
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     out.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return out;
 }
@@ -455,7 +455,7 @@ std::vector<u8> emit_bytes(const DecompressOut& t, cudaStream_t s) {
     DevBuf<u8> db(bytes.size(), s);
     emit_dtype(t.x.p, total, t.dtype, db.p, s);
     db.download(bytes.data(), bytes.size());
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     return bytes;
 }
 

@@ -1064,7 +1064,7 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
     TCB_LAUNCH();
     std::vector<double> ev(n64 + 1);
     w.evals.download(ev.data(), n64 + 1);  // one synchronising copy: eigenvalues and ||T||_inf
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     w.tnorm = ev[n64];
     ev.resize(n64);
     w.ev = ev;

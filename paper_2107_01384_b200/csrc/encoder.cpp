@@ -163,12 +163,13 @@ struct Planner {
         pr.stops.assign(2 * nb, 0);
         auto finish = [&](int lp) {
             pr.last_plane = lp;
+            if (o.on_last_plane && !o.fixed_plane) o.on_last_plane(lp);
             if (n > 0) {
                 HostTrace ht("plan: decode_model");
                 DevBuf<u64> ds(2 * nb, s);
                 ds.upload(pr.stops.data(), 2 * nb);
                 decode_model(m, n, block, lp, ds.p, dec, s);
-                TCB_CUDA(cudaStreamSynchronize(s));
+                stream_sync(s);
             }
             return pr;
         };
@@ -201,6 +202,7 @@ struct Planner {
             const Iv red = add(tot.lead, tot.trail);
             ++pr.nplanes;
             if (le(sub(tracked, red), tgt)) {
+                if (o.on_last_plane) o.on_last_plane(p);
                 u64 ebits = 0;
                 if (o.split && have_prev) {
                     HostTrace ht("plan: split probe emit");

@@ -2,6 +2,7 @@
 // core_codec.cpp:105-413): certified plan decisions + device emission.
 #pragma once
 
+#include <functional>
 #include <optional>
 
 #include "codec.cuh"
@@ -13,6 +14,10 @@ struct EncodeOpts {
     u64 block = 0;       // 0 = max(4096, ceil(n/64))
     bool split = true;
     std::optional<int> fixed_plane;
+    // called once the last plane is certified (before the stop placement), so
+    // work that depends only on it can start early; may be called again with
+    // the same value by the exact-mode rerun
+    std::function<void(int)> on_last_plane;
 };
 
 struct PlanResult {

@@ -297,7 +297,7 @@ void householder(const double* U, u64 n, u64 r, const std::vector<u64>& live, do
     fl.download(flips_host, rl);
     int e = 0;
     err.download(&e, 1);
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     if (e) throw Error("factorize: degenerate reflector");
 }
 
@@ -383,7 +383,7 @@ void factor_expand(const u64* mag, const u8* neg, int k, u64 n, u64 r, const std
     TCB_LAUNCH();
     int e = 0;
     err.download(&e, 1);
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     if (e) throw Error("reconstruct: reflector sub-diagonal norm reaches 1");
 }
 

@@ -167,7 +167,7 @@ double sumsq_impl(const T* x, u64 n, bool* finite, cudaStream_t s) {
     int b = 0;
     TCB_CUDA(cudaMemcpyAsync(&r, part.p + grid, sizeof(double), cudaMemcpyDeviceToHost, s));
     TCB_CUDA(cudaMemcpyAsync(&b, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     if (finite) *finite = b == 0;
     return r;
 }
@@ -343,7 +343,7 @@ double sse_between(const double* a, const double* b, u64 n, bool f32, cudaStream
     TCB_LAUNCH();
     double r = 0;
     TCB_CUDA(cudaMemcpyAsync(&r, part.p + grid, sizeof(double), cudaMemcpyDeviceToHost, s));
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     return r;
 }
 
@@ -381,7 +381,7 @@ double max_abs_finite(const double* x, u64 n, bool* finite, cudaStream_t s) {
     TCB_LAUNCH();
     double r[2] = {0, 0};
     TCB_CUDA(cudaMemcpyAsync(r, part.p + grid, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     int b = 0;
     std::memcpy(&b, &r[1], sizeof(int));
     *finite = b == 0;
@@ -398,7 +398,7 @@ double max_abs(const double* x, u64 n, cudaStream_t s) {
     TCB_LAUNCH();
     double r = 0;
     TCB_CUDA(cudaMemcpyAsync(&r, part.p + grid, sizeof(double), cudaMemcpyDeviceToHost, s));
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     return r;
 }
 

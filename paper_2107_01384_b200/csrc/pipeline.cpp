@@ -7,6 +7,7 @@
 #include "pipeline.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cfloat>
 #include <chrono>
 #include <cmath>
@@ -174,7 +175,7 @@ std::vector<u8> empty_stream_section(u64 count, u64 block) {
     return w.b;
 }
 
-__attribute__((unused)) void sync(cudaStream_t s) { TCB_CUDA(cudaStreamSynchronize(s)); }
+__attribute__((unused)) void sync(cudaStream_t s) { stream_sync(s); }
 
 }  // namespace
 
@@ -339,7 +340,7 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, double budget, int backen
         DevBuf<double> ds(r, s);
         ds.upload(sig.data(), r);
         scale_orthonormalize(o.U.p, rows, r, ds.p, s);
-        TCB_CUDA(cudaStreamSynchronize(s));
+        stream_sync(s);
         fix_column_signs(o.U.p, rows, r, s);
     }
     o.next = DevBuf<double>(cols * o.r, s);
@@ -406,7 +407,7 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
     }
     f.core = std::move(x);
     f.core_shape = cur;
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     return f;
 }
 
@@ -429,11 +430,70 @@ FactorPrep factor_prepare(const double* U, u64 n, u64 r, const std::vector<u8>& 
     return pp;
 }
 
+void factor_quantize(FactorQuant& q, const FactorPrep& prep, u64 n, const std::vector<double>& sn_live, bool simple,
+                     cudaStream_t s) {
+    const u64 rl = prep.live.size();
+    q.live = prep.live;
+    q.ln = sn_live;
+    q.sc.assign(rl, 0.0);
+    if (simple) {
+        q.sc = q.ln;
+    } else {
+        const auto al = alpha_weights(q.ln, n);
+        for (u64 j = 0; j < rl; ++j) q.sc[j] = std::sqrt(2.0 * al[j]);
+    }
+    q.dsc = DevBuf<double>(rl, s);
+    q.dsc.upload(q.sc.data(), rl);
+    q.dfl = DevBuf<signed char>(rl, s);
+    q.dfl.upload(prep.fl.data(), rl);
+    q.cnt = n * rl - rl * (rl + 1) / 2;
+    DevBuf<double> st(q.cnt, s);
+    reflector_stream(prep.V.p, n, rl, q.dsc.p, st.p, s);
+    const double mx = q.cnt ? max_abs(st.p, q.cnt, s) : 0.0;
+    q.k = mx > 0.0 ? 63 - std::ilogb(mx) : 0;
+    q.mag = DevBuf<u64>(q.cnt, s);
+    q.neg = DevBuf<u8>(q.cnt, s);
+    quantize_f64(st.p, q.cnt, q.k, q.mag.p, q.neg.p, s);
+}
+
+void factor_plane_search(FactorQuant& q, const double* U, u64 n, u64 r, int core_step_log2, double cap,
+                         cudaStream_t s) {
+    const u64 rl = q.live.size();
+    int plane = std::clamp(core_step_log2 + q.k, 0, 63);
+    // The reference deepens the plane while the factor term exceeds the cap
+    // (factor_codec.cpp:218-243).  Terms for a window of candidate planes are
+    // evaluated in one batched launch; the host then replays the reference's
+    // deepening decisions over them.
+    std::vector<double> term_of(64, -1.0);
+    double term = 0.0;
+    while (true) {
+        if (term_of[plane] < 0.0) {
+            std::vector<int> cand;
+            for (int p = plane; p >= 0 && static_cast<int>(cand.size()) < 16; --p)
+                if (term_of[p] < 0.0) cand.push_back(p);
+            const auto res = factor_residuals(q.mag.p, q.neg.p, q.k, n, r, q.live, q.dsc.p, U, q.dfl.p, cand, s);
+            for (std::size_t c = 0; c < cand.size(); ++c) {
+                double t = 0.0;
+                for (u64 j = 0; j < rl; ++j) t += q.ln[j] * q.ln[j] * res[c * rl + j];
+                term_of[cand[c]] = t;
+            }
+        }
+        term = term_of[plane];
+        if (term <= cap || plane == 0) break;
+        const double excess = term / std::max(cap, 1e-300);
+        const int stp = std::max(1, static_cast<int>(std::ceil(0.25 * std::log2(excess))));
+        plane = std::max(0, plane - stp);
+    }
+    q.core_step = core_step_log2;
+    q.plane = plane;
+    q.term = term;
+}
+
 FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<u8>& dead,
                                const std::vector<double>& sn, int coder, bool simple, int core_step_log2,
                                double cap, bool f32, cudaStream_t s,
                                const std::function<void(const std::vector<signed char>&)>& on_flips,
-                               FactorPrep* prep) {
+                               FactorPrep* prep, FactorQuant* spec) {
     if (dead.size() != r || sn.size() != r) throw Error("factor encode: column metadata mismatch");
     FactorEnc out;
     out.dead = dead;
@@ -458,66 +518,41 @@ FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<
     if (!prep || prep->live != live) {
         own = factor_prepare(U, n, r, dead, f32, s);
         prep = &own;
+        spec = nullptr;
     }
     if (prep->err) std::rethrow_exception(prep->err);
-    DevBuf<double>& V = prep->V;
-    const std::vector<signed char>& fl = prep->fl;
-    for (u64 j = 0; j < rl; ++j) out.flips[live[j]] = fl[j];
+    for (u64 j = 0; j < rl; ++j) out.flips[live[j]] = prep->fl[j];
     if (on_flips) on_flips(out.flips);
-    std::vector<double> sc(rl);
-    if (simple) {
-        sc = ln;
-    } else {
-        const auto al = alpha_weights(ln, n);
-        for (u64 j = 0; j < rl; ++j) sc[j] = std::sqrt(2.0 * al[j]);
+    FactorQuant ownq;
+    FactorQuant* q = spec && spec->live == live && spec->ln == ln ? spec : nullptr;
+    if (!q) {
+        factor_quantize(ownq, *prep, n, ln, simple, s);
+        q = &ownq;
     }
-    DevBuf<double> dsc(rl, s);
-    dsc.upload(sc.data(), rl);
-    DevBuf<signed char> dfl(rl, s);
-    dfl.upload(fl.data(), rl);
-    out.count = n * rl - rl * (rl + 1) / 2;
-    const u64 cnt = out.count;
-    DevBuf<double> st(cnt, s);
-    reflector_stream(V.p, n, rl, dsc.p, st.p, s);
-    const double mx = cnt ? max_abs(st.p, cnt, s) : 0.0;
-    out.k = mx > 0.0 ? 63 - std::ilogb(mx) : 0;
-    DevBuf<u64> mag(cnt, s);
-    DevBuf<u8> neg(cnt, s);
-    quantize_f64(st.p, cnt, out.k, mag.p, neg.p, s);
-    int plane = std::clamp(core_step_log2 + out.k, 0, 63);
-    // The reference deepens the plane while the factor term exceeds the cap
-    // (factor_codec.cpp:218-243).  Terms for a window of candidate planes are
-    // evaluated in one batched launch; the host then replays the reference's
-    // deepening decisions over them.
-    std::vector<double> term_of(64, -1.0);
-    while (true) {
-        if (term_of[plane] < 0.0) {
-            std::vector<int> cand;
-            for (int p = plane; p >= 0 && static_cast<int>(cand.size()) < 16; --p)
-                if (term_of[p] < 0.0) cand.push_back(p);
-            const auto res = factor_residuals(mag.p, neg.p, out.k, n, r, live, dsc.p, U, dfl.p, cand, s);
-            for (std::size_t c = 0; c < cand.size(); ++c) {
-                double t = 0.0;
-                for (u64 j = 0; j < rl; ++j) t += ln[j] * ln[j] * res[c * rl + j];
-                term_of[cand[c]] = t;
-            }
-        }
-        out.term = term_of[plane];
-        if (out.term <= cap || plane == 0) break;
-        const double excess = out.term / std::max(cap, 1e-300);
-        const int stp = std::max(1, static_cast<int>(std::ceil(0.25 * std::log2(excess))));
-        plane = std::max(0, plane - stp);
+    if (q->core_step != core_step_log2 || q->plane < 0) {
+        factor_plane_search(*q, U, n, r, core_step_log2, cap, s);
+        q->finalized = false;
     }
+    if (!q->finalized) factor_finalize(*q, coder, s);
+    out.count = q->cnt;
+    out.k = q->k;
+    out.term = q->term;
+    out.stream = std::move(q->stream);
+    out.plane = q->plane;
+    return out;
+}
+
+void factor_finalize(FactorQuant& q, int coder, cudaStream_t s) {
+    const u64 cnt = q.cnt;
     PlanResult pl;  // fixed last plane: planes 63..plane in full (core_codec.cpp:328-391)
     pl.block = default_block(cnt);
     if (cnt > 0) {
-        pl.last_plane = plane;
-        pl.nplanes = 64 - plane;
+        pl.last_plane = q.plane;
+        pl.nplanes = 64 - q.plane;
         pl.stops.assign(2 * ((cnt + pl.block - 1) / pl.block), kFull);
     }
-    out.stream = finalize_stream(mag.p, neg.p, cnt, pl, coder, cnt, s);
-    out.plane = plane;
-    return out;
+    q.stream = finalize_stream(q.mag.p, q.neg.p, cnt, pl, coder, cnt, s);
+    q.finalized = true;
 }
 
 // Phases 2-5 of compress_impl (pipeline.cpp:77-189): storage order,
@@ -622,22 +657,35 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     const double cap = 0.02 * target / static_cast<double>(d);
     std::vector<FactorEnc> fe(d);
     res.factor_terms.assign(d, 0.0);
-    std::vector<std::vector<signed char>> flips_of(d);
+    std::vector<std::vector<signed char>> flips_of(d), flips_of_core(d);
     std::vector<std::vector<u8>> dead_mode(d);
     int core_step = 0;
     const bool par = d > 1 && !prof_enabled();
     std::promise<void> plan_ready;
     std::shared_future<void> plan_fut = plan_ready.get_future().share();
+    // the core's last plane, published by the planner as soon as it is certified:
+    // each factor's plane search depends only on it (and on the live columns)
+    std::promise<int> lp_ready;
+    std::shared_future<int> lp_fut = lp_ready.get_future().share();
+    std::atomic<bool> lp_set{false};
     std::vector<std::promise<void>> flips_ready(d);
     std::vector<std::future<void>> flips_fut, done;
+    // the speculative preparation's flips (every column live): final whenever the
+    // plan kills no column of that mode, so the core need not wait for the worker
+    std::vector<std::vector<signed char>> spec_flips(d);
+    std::vector<std::promise<bool>> spec_ready(d);
+    std::vector<std::future<bool>> spec_fut;
     JoinAll join{done};
     struct PlanGuard {  // a throwing plan must still release the workers
         std::promise<void>& p;
+        std::promise<int>& lp;
+        std::atomic<bool>& lp_set;
         bool set = false;
         ~PlanGuard() {
             if (!set) p.set_exception(std::make_exception_ptr(Error("compress: core plan failed")));
+            if (!lp_set.exchange(true)) lp.set_exception(std::make_exception_ptr(Error("compress: core plan failed")));
         }
-    } plan_guard{plan_ready};
+    } plan_guard{plan_ready, lp_ready, lp_set};
     if (par) {
         int dev = 0;
         TCB_CUDA(cudaGetDevice(&dev));
@@ -646,6 +694,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
         Workers& pool = Workers::get();
         for (std::size_t i = 0; i < d; ++i) {
             flips_fut.push_back(flips_ready[i].get_future());
+            spec_fut.push_back(spec_ready[i].get_future());
             cudaStream_t si = pool.stream(dev, static_cast<int>(i));
             TCB_CUDA(cudaStreamWaitEvent(si, ready.e, 0));
             done.push_back(pool.submit([&, i, si, dev] {
@@ -654,6 +703,23 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
                     TCB_CUDA(cudaSetDevice(dev));
                     FactorPrep prep = factor_prepare(f.factors[i].p, f.n[i], f.r[i], std::vector<u8>(f.r[i], 0),
                                                      prm.f32, si);
+                    if (!prep.err && prep.live.size() == f.r[i]) {
+                        spec_flips[i] = prep.fl;
+                        spec_ready[i].set_value(true);
+                    } else {
+                        spec_ready[i].set_value(false);
+                    }
+                    // speculation "no dead columns": quantised stream now, plane search as
+                    // soon as the core's last plane is certified
+                    FactorQuant spec;
+                    bool have_spec = false;
+                    if (!prep.err && !prep.live.empty()) {
+                        factor_quantize(spec, prep, f.n[i], sn_mode[i], prm.simple, si);
+                        have_spec = true;
+                        const int lp = lp_fut.get();
+                        factor_plane_search(spec, f.factors[i].p, f.n[i], f.r[i], lp - k, cap, si);
+                        factor_finalize(spec, prm.coder, si);
+                    }
                     plan_fut.get();
                     fe[i] = encode_factor_device(
                         f.factors[i].p, f.n[i], f.r[i], dead_mode[i], sn_mode[i], prm.coder, prm.simple, core_step,
@@ -663,7 +729,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
                             sent = true;
                             flips_ready[i].set_value();
                         },
-                        &prep);
+                        &prep, have_spec ? &spec : nullptr);
                 } catch (...) {
                     if (!sent) flips_ready[i].set_exception(std::current_exception());
                     throw;
@@ -674,6 +740,10 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     PlanResult plan;
     {
         HostTrace ht("encode: core plan");
+        if (par)
+            eo.on_last_plane = [&](int lp) {
+                if (!lp_set.exchange(true)) lp_ready.set_value(lp);
+            };
         plan = plan_stream(mag.p, nc, std::ldexp(core_target, 2 * k), eo, dec.p, s);
     }
     res.core_last_plane = plan.last_plane;
@@ -697,19 +767,29 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     t0 = Clock::now();
     if (par) {
         HostTrace ht("encode: wait factor flips");
-        for (auto& fu : flips_fut) fu.get();  // rethrows a factor's early error (join waits for the rest)
+        for (std::size_t i = 0; i < d; ++i) {
+            bool all_live = true;
+            for (u8 v : dead_mode[i]) all_live = all_live && v == 0;
+            if (all_live && spec_fut[i].get()) {
+                flips_of_core[i] = spec_flips[i];  // identical to what the worker will publish
+            } else {
+                flips_fut[i].get();  // rethrows a factor's early error (join waits for the rest)
+                flips_of_core[i] = flips_of[i];
+            }
+        }
     } else {
         for (std::size_t i = 0; i < d; ++i)
             fe[i] = encode_factor_device(f.factors[i].p, f.n[i], f.r[i], dead_mode[i], sn_mode[i], prm.coder,
                                          prm.simple, core_step, cap, prm.f32, s,
                                          [&](const std::vector<signed char>& fl) { flips_of[i] = fl; });
+        flips_of_core = flips_of;
     }
 
     // sign fold + finalize (pipeline.cpp:161-176)
     const auto t1 = Clock::now();
     std::vector<signed char> flips_axis;
     for (std::size_t ax = 0; ax < d; ++ax)
-        flips_axis.insert(flips_axis.end(), flips_of[mode_of[ax]].begin(), flips_of[mode_of[ax]].end());
+        flips_axis.insert(flips_axis.end(), flips_of_core[mode_of[ax]].begin(), flips_of_core[mode_of[ax]].end());
     sign_fold(neg.p, cs, flips_axis, s, vorder.p);
     u64 count = 1;
     for (auto v : f.r) count *= v;

@@ -97,6 +97,31 @@ struct FactorPrep {
     std::exception_ptr err;
 };
 FactorPrep factor_prepare(const double* U, u64 n, u64 r, const std::vector<u8>& dead, bool f32, cudaStream_t s);
+// The quantised reflector stream of a factor for a given live set
+// (factor_codec.cpp:200-217) and, once the core's last plane is known, the
+// plane search over it (factor_codec.cpp:218-243): computed speculatively for
+// "no dead columns" while the core plan runs, reused when the plan agrees.
+struct FactorQuant {
+    std::vector<u64> live;
+    std::vector<double> ln, sc;
+    DevBuf<double> dsc;
+    DevBuf<signed char> dfl;
+    u64 cnt = 0;
+    int k = 0;
+    DevBuf<u64> mag;
+    DevBuf<u8> neg;
+    int core_step = 1 << 30;  // the core step the plane search below was made for
+    int plane = -1;
+    double term = 0.0;
+    std::vector<u8> stream;   // the finalised stream section for `plane` (when `finalized`)
+    bool finalized = false;
+};
+// finalise q's stream section for its plane (factor_codec.cpp:244, core_codec.cpp:328-391)
+void factor_finalize(FactorQuant& q, int coder, cudaStream_t s);
+void factor_quantize(FactorQuant& q, const FactorPrep& prep, u64 n, const std::vector<double>& sn_live, bool simple,
+                     cudaStream_t s);
+void factor_plane_search(FactorQuant& q, const double* U, u64 n, u64 r, int core_step_log2, double cap,
+                         cudaStream_t s);
 // on_flips (optional) receives the column sign flips as soon as they are known,
 // before the plane search and stream finalisation; `prep` (optional) is reused
 // when it was made for the same live columns.
@@ -104,7 +129,7 @@ FactorEnc encode_factor_device(const double* U, u64 n, u64 r, const std::vector<
                                const std::vector<double>& sn, int coder, bool simple, int core_step_log2,
                                double cap, bool f32, cudaStream_t s,
                                const std::function<void(const std::vector<signed char>&)>& on_flips = {},
-                               FactorPrep* prep = nullptr);
+                               FactorPrep* prep = nullptr, FactorQuant* spec = nullptr);
 
 std::vector<double> alpha_weights(const std::vector<double>& sn, u64 n);
 std::vector<u64> stable_ascending(const std::vector<u64>& s);

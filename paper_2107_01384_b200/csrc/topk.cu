@@ -957,7 +957,7 @@ void topk_eig(const double* G, u64 n64, int p, int extra_iters, double* X, std::
             TCB_LAUNCH();
             std::vector<double> h(2 * p + 2);
             out.download(h.data(), 2 * p + 2);
-            TCB_CUDA(cudaStreamSynchronize(s));
+            stream_sync(s);
             int failed = 0;
             std::memcpy(&failed, &h[2 * p + 1], sizeof(int));
             if (failed) {
@@ -990,7 +990,7 @@ void topk_eig(const double* G, u64 n64, int p, int extra_iters, double* X, std::
     TCB_LAUNCH();
     std::vector<double> h(2 * p + 2);
     out.download(h.data(), 2 * p + 2);
-    TCB_CUDA(cudaStreamSynchronize(s));
+    stream_sync(s);
     int failed = 0;
     std::memcpy(&failed, &h[2 * p + 1], sizeof(int));
     if (failed) {  // a Cholesky pivot broke down: report "not converged"
