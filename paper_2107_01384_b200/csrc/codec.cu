@@ -12,6 +12,7 @@
 // zero-run symbols and the MSB-first raw bits; the adaptive range coder then
 // runs one thread per stream; payloads are compacted in stream order.
 #include <algorithm>
+#include <mutex>
 #include <cfloat>
 
 #include "codec.cuh"
@@ -1220,6 +1221,142 @@ std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cu
     out.resize(el);
     ent.download(out.data(), el);
     stream_sync(s);
+    return out;
+}
+
+struct ProbeCache {
+    u64 n = 0, nb = 0;
+    int coder = 0;
+    cudaStream_t s = nullptr;
+    std::vector<StreamDesc> sd;
+    std::vector<AcDesc> ad;
+    DevBuf<StreamDesc> dsd;
+    DevBuf<u64> syms;
+    DevBuf<u32> raw;
+    DevBuf<StreamOut> so;
+    DevBuf<AcDesc> dad;
+    DevBuf<u8> ent;
+    DevBuf<u64> elen;
+    DevBuf<u32> scratch;
+    DevBuf<int> redo;
+    cudaEvent_t done = nullptr;
+    bool ready = false;
+    std::vector<u64> el;
+    std::mutex mu;
+    ~ProbeCache() {
+        if (done) {
+            cudaEventSynchronize(done);
+            cudaEventDestroy(done);
+        }
+    }
+};
+
+std::shared_ptr<ProbeCache> probe_planes_async(const u64* m, u64 n, u64 block, int coder, cudaStream_t side) {
+    auto c = std::make_shared<ProbeCache>();
+    c->n = n;
+    c->coder = coder;
+    c->s = side;
+    const u64 nb = n == 0 ? 0 : (n + block - 1) / block;
+    c->nb = nb;
+    const u64 ns = nb * 64;
+    if (ns == 0) return c;
+    c->sd.resize(ns);
+    u64 sym_total = 0, raw_words = 0;
+    for (int pi = 0; pi < 64; ++pi)
+        for (u64 b = 0; b < nb; ++b) {
+            StreamDesc& d = c->sd[pi * nb + b];
+            d.lo = b * block;
+            d.hi = std::min<u64>(n, d.lo + block);
+            d.plane = 63 - pi;
+            d.lstop = d.tstop = kFull;
+            d.sym_off = sym_total;
+            sym_total += d.hi - d.lo + 1;
+            d.raw_off = raw_words * 32;
+            raw_words += (d.hi - d.lo + 31) / 32;
+        }
+    c->ad.resize(ns);
+    u64 out_total = 0, scratch_total = 0;
+    for (u64 i = 0; i < ns; ++i) {
+        AcDesc& a = c->ad[i];
+        const u64 kmax = c->sd[i].hi - c->sd[i].lo + 1;
+        a.sym_off = c->sd[i].sym_off;
+        a.out_off = out_total;
+        a.cap = static_cast<u32>(kmax + 1);
+        a.fen = 0;
+        a.hbits = log2_at_least(2 * a.cap);
+        if (coder == 1) {
+            out_total += rans_out_cap(kmax);
+            a.model_off = (scratch_total + 1) & ~u64{1};
+            scratch_total = a.model_off + rans_scratch_words(kmax);
+        } else {
+            out_total += 5 + 7 * kmax + 16;
+            a.model_off = 0;
+        }
+    }
+    c->dsd = DevBuf<StreamDesc>(ns, side);
+    c->dsd.upload(c->sd.data(), ns);
+    c->syms = DevBuf<u64>(sym_total, side);
+    c->raw = DevBuf<u32>(raw_words + 1, side);
+    c->raw.zero();
+    c->so = DevBuf<StreamOut>(ns, side);
+    emit_kernel<<<static_cast<unsigned>(ns), kEmT, 0, side>>>(m, nullptr, c->dsd.p, c->syms.p, c->raw.p, c->so.p);
+    count_launch();
+    TCB_LAUNCH();
+    c->dad = DevBuf<AcDesc>(ns, side);
+    c->dad.upload(c->ad.data(), ns);
+    c->ent = DevBuf<u8>(out_total + 1, side);
+    c->elen = DevBuf<u64>(ns, side);
+    c->scratch = DevBuf<u32>(coder == 1 ? scratch_total + 2 : 2, side);
+    c->redo = DevBuf<int>(1, side);
+    if (coder == 1) {
+        run_rans(c->syms.p, c->so.p, c->dad.p, static_cast<int>(ns), c->ent.p, c->scratch.p, c->elen.p, side);
+    } else {
+        c->redo.zero();
+        launch_ac_shared(c->syms.p, c->so.p, c->dad.p, static_cast<int>(ns), c->ent.p, c->elen.p, c->redo.p, side);
+    }
+    TCB_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
+    TCB_CUDA(cudaEventRecord(c->done, side));
+    return c;
+}
+
+std::vector<u64> probe_entropy_bytes(ProbeCache& c, int p) {
+    std::lock_guard<std::mutex> lk(c.mu);
+    const u64 ns = c.nb * 64;
+    if (!c.ready && ns > 0) {
+        TCB_CUDA(cudaEventSynchronize(c.done));
+        c.el.resize(ns);
+        std::vector<StreamOut> soh(ns);
+        c.elen.download(c.el.data(), ns);
+        c.so.download(soh.data(), ns);
+        stream_sync(c.s);
+        if (c.coder == 0) {  // model overflow: rerun those streams from global scratch
+            std::vector<int> ids;
+            u64 words = 0;
+            for (u64 i = 0; i < ns; ++i)
+                if (c.el[i] == ~u64{0}) {
+                    ids.push_back(static_cast<int>(i));
+                    c.ad[i].model_off = words;
+                    words += ac_model_words(static_cast<u32>(soh[i].nsyms + 1));
+                }
+            if (!ids.empty()) {
+                DevBuf<u32> gscr(words + 2, c.s);
+                c.dad.upload(c.ad.data(), ns);
+                DevBuf<int> dids(ids.size(), c.s);
+                dids.upload(ids.data(), ids.size());
+                ac_kernel<false><<<static_cast<unsigned>(ids.size()), 32, 0, c.s>>>(
+                    c.syms.p, c.so.p, c.dad.p, dids.p, static_cast<int>(ns), c.ent.p, gscr.p, c.elen.p, 0, c.redo.p);
+                count_launch();
+                TCB_LAUNCH();
+                c.elen.download(c.el.data(), ns);
+                stream_sync(c.s);
+            }
+        }
+        for (u64 v : c.el)
+            if (v == ~u64{1}) throw Error("entropy: cannot normalize rans table");
+        c.ready = true;
+    }
+    std::vector<u64> out(c.nb);
+    for (u64 b = 0; b < c.nb; ++b) out[b] = c.el[static_cast<u64>(63 - p) * c.nb + b];
     return out;
 }
 

@@ -1,6 +1,8 @@
 // Bit-plane codec kernels (core_codec.cpp / entropy.cpp / error_model.cpp).
 #pragma once
 
+#include <memory>
+
 #include "common.cuh"
 
 namespace tcb {
@@ -51,6 +53,16 @@ struct EmitResult {
 EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
                        const u64* stops_host /*2*nb, for last_plane*/, int coder, bool want_body,
                        cudaStream_t s);
+
+// Speculative split-plane probe: the entropy-coded size of every full plane
+// stream (planes 63..0, no stops, signs not needed) launched on a side stream
+// as soon as the magnitudes exist, so the planner's probe of plane p+1
+// (core_codec.cpp:244-290) is a lookup instead of a round trip on the
+// critical path.
+struct ProbeCache;
+std::shared_ptr<ProbeCache> probe_planes_async(const u64* m, u64 n, u64 block, int coder, cudaStream_t side);
+// entropy bytes of plane p's streams (one per block); waits for the side stream
+std::vector<u64> probe_entropy_bytes(ProbeCache& c, int p);
 
 // entropy::encode_symbols for one host symbol sequence (arithmetic coder)
 std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cudaStream_t s);

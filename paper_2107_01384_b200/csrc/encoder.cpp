@@ -206,8 +206,12 @@ struct Planner {
                 u64 ebits = 0;
                 if (o.split && have_prev) {
                     HostTrace ht("plan: split probe emit");
-                    const auto er = emit_planes(m, nullptr, n, block, p + 1, p + 1, nullptr, o.coder, false, s);
-                    for (u64 e : er.entropy_bytes) ebits += e * 8;
+                    if (o.probe) {
+                        for (u64 e : probe_entropy_bytes(*o.probe, p + 1)) ebits += e * 8;
+                    } else {
+                        const auto er = emit_planes(m, nullptr, n, block, p + 1, p + 1, nullptr, o.coder, false, s);
+                        for (u64 e : er.entropy_bytes) ebits += e * 8;
+                    }
                 }
                 // the stats batch may have been replaced by the probe: refetch
                 per = stats(p, 0);

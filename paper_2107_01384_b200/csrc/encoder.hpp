@@ -18,6 +18,8 @@ struct EncodeOpts {
     // work that depends only on it can start early; may be called again with
     // the same value by the exact-mode rerun
     std::function<void(int)> on_last_plane;
+    // speculative full-plane entropy sizes for the split probe (optional)
+    ProbeCache* probe = nullptr;
 };
 
 struct PlanResult {

@@ -349,7 +349,8 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, double budget, int backen
 }
 
 Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vector<u64>& shape, double target,
-                      const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite) {
+                      const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite,
+                      const std::function<void(std::size_t, const double*, u64, u64)>& on_factor) {
     if (target < 0) throw Error("sthosvd: negative SSE target");
     const std::size_t d = shape.size();
     u64 n_el = 1;
@@ -402,6 +403,7 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
         xp = x.p;
         f.factors[p[step]] = std::move(so.U);
         f.r[p[step]] = so.r;
+        if (on_factor) on_factor(p[step], f.factors[p[step]].p, rows, so.r);
         cur.erase(cur.begin());
         cur.push_back(so.r);
     }
@@ -559,7 +561,7 @@ void factor_finalize(FactorQuant& q, int coder, cudaStream_t s) {
 // quantisation, core plan, factors, sign fold, finalize, container.
 void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtype, double target,
                  double core_target, double trunc, const Params& prm, cudaStream_t s, Clock::time_point t_all,
-                 u64 n_el) {
+                 u64 n_el, std::vector<std::future<FactorPrep>>* preps = nullptr) {
     const std::size_t d = shape.size();
     auto t0 = Clock::now();
     // phase 2: storage order + quantisation
@@ -686,6 +688,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
             if (!lp_set.exchange(true)) lp.set_exception(std::make_exception_ptr(Error("compress: core plan failed")));
         }
     } plan_guard{plan_ready, lp_ready, lp_set};
+    HostTrace ht_launch("encode: launch workers");
     if (par) {
         int dev = 0;
         TCB_CUDA(cudaGetDevice(&dev));
@@ -701,8 +704,10 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
                 bool sent = false;
                 try {
                     TCB_CUDA(cudaSetDevice(dev));
-                    FactorPrep prep = factor_prepare(f.factors[i].p, f.n[i], f.r[i], std::vector<u8>(f.r[i], 0),
-                                                     prm.f32, si);
+                    FactorPrep prep = preps && i < preps->size() && (*preps)[i].valid()
+                                          ? (*preps)[i].get()  // made during the mode loop
+                                          : factor_prepare(f.factors[i].p, f.n[i], f.r[i],
+                                                           std::vector<u8>(f.r[i], 0), prm.f32, si);
                     if (!prep.err && prep.live.size() == f.r[i]) {
                         spec_flips[i] = prep.fl;
                         spec_ready[i].set_value(true);
@@ -737,6 +742,22 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
             }));
         }
     }
+    ht_launch.stop();
+    HostTrace ht_probe("encode: probe launch");
+    // speculative split probe: every full plane's entropy size on a side stream
+    // (small cores only: 64 streams per block)
+    std::shared_ptr<ProbeCache> probe;
+    if (par && prm.split && nc <= (u64{1} << 20) && 64 * ((nc + block - 1) / block) <= 4096) {
+        int dev = 0;
+        TCB_CUDA(cudaGetDevice(&dev));
+        cudaStream_t side = Workers::get().stream(dev, static_cast<int>(d));
+        EventHandle q;
+        TCB_CUDA(cudaEventRecord(q.e, s));
+        TCB_CUDA(cudaStreamWaitEvent(side, q.e, 0));
+        probe = probe_planes_async(mag.p, nc, block, prm.coder, side);
+        eo.probe = probe.get();
+    }
+    ht_probe.stop();
     PlanResult plan;
     {
         HostTrace ht("encode: core plan");
@@ -890,8 +911,41 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     res.target_sse = target;
 
     auto t0 = Clock::now();
+    // each factor's orthonormality check + reflectors start on its worker stream
+    // as soon as its mode step is done, overlapping the rest of the mode loop
+    const std::size_t dd = shape.size();
+    std::vector<std::future<FactorPrep>> preps(dd);
+    struct PrepJoin {  // no prep task may outlive this frame
+        std::vector<std::future<FactorPrep>>& v;
+        ~PrepJoin() {
+            for (auto& x : v)
+                if (x.valid()) x.wait();
+        }
+    } prep_join{preps};
+    std::function<void(std::size_t, const double*, u64, u64)> on_factor;
+    if (dd > 1 && !prof_enabled()) {
+        int dev = 0;
+        TCB_CUDA(cudaGetDevice(&dev));
+        on_factor = [&, dev](std::size_t mode, const double* U, u64 n, u64 r) {
+            cudaStream_t si = Workers::get().stream(dev, static_cast<int>(mode));
+            auto ready = std::make_shared<EventHandle>();
+            TCB_CUDA(cudaEventRecord(ready->e, s));
+            TCB_CUDA(cudaStreamWaitEvent(si, ready->e, 0));
+            // the task works on its own copy of U (the Tucker may unwind first on an error)
+            auto Uc = std::make_shared<DevBuf<double>>(n * r, si);
+            if (n * r)
+                TCB_CUDA(cudaMemcpyAsync(Uc->p, U, n * r * sizeof(double), cudaMemcpyDeviceToDevice, si));
+            auto task = std::make_shared<std::packaged_task<FactorPrep()>>([Uc, n, r, f32 = prm.f32, si, dev, ready] {
+                TCB_CUDA(cudaSetDevice(dev));
+                FactorPrep pp = factor_prepare(Uc->p, n, r, std::vector<u8>(r, 0), f32, si);
+                return pp;
+            });
+            preps[mode] = task->get_future();
+            Workers::get().submit([task] { (*task)(); });
+        };
+    }
     Tucker f = sthosvd_device(std::move(a), direct ? static_cast<const double*>(device_bytes) : nullptr, shape,
-                              prm.rtmss * target, prm.mode_order, prm.backend, s, finite ? 1 : 0);
+                              prm.rtmss * target, prm.mode_order, prm.backend, s, finite ? 1 : 0, on_factor);
     double trunc = 0;
     for (double v : f.trunc) trunc += v;
     double core_target = target - trunc;
@@ -900,7 +954,7 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     res.trunc = trunc;
     res.ranks = f.r;
 
-    encode_into(res, f, shape, dtype, target, core_target, trunc, prm, s, t_all, n_el);
+    encode_into(res, f, shape, dtype, target, core_target, trunc, prm, s, t_all, n_el, &preps);
     return res;
 }
 

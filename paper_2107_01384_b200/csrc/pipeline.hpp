@@ -66,8 +66,11 @@ StepOut factor_from_gram(const double* G, u64 n, double budget, cudaStream_t s);
 // identity processing order mode 0 reads it in place), else `owned`, which is
 // released as soon as it is no longer needed.  finite: 1 / 0 when the caller
 // already scanned the values (the norm pass), -1 to scan here.
+// on_factor (optional) is called after each mode step with (mode, U, n, r), U
+// complete on `s`.
 Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vector<u64>& shape, double target,
-                      const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite = -1);
+                      const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite = -1,
+                      const std::function<void(std::size_t, const double*, u64, u64)>& on_factor = {});
 inline Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double target,
                              const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s) {
     return sthosvd_device(std::move(a), nullptr, shape, target, order, backend, s);

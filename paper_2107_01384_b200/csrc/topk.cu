@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(kTkRrThreads) tk_rr(const double* __restrict__
 // iterations), of Z = G W and of the basis Q; every CTA holds the full current
 // basis W (n x 32) for the products.  Per iteration:
 //   Z_c = G_c W                       (DMMA, local rows, the flop-heavy part)
-//   3 x { P_c = Z_c^T Z_c (DMMA); cluster barrier; C = sum_c P_c read over
+//   2 (3 on the last iteration) x { P_c = Z_c^T Z_c (DMMA); cluster barrier; C = sum_c P_c over
 //         DSMEM in a fixed order (bitwise identical in every CTA; pass 0 adds
 //         the CholQR3 shift from trace C = |Z|_F^2); Cholesky with inverse
 //         (redundant per CTA, identical); Z_c <- Z_c R^-1 (DMMA) }
@@ -741,7 +741,11 @@ __global__ void __launch_bounds__(256) tk_cluster(const double* __restrict__ G, 
         tk_cl_gq(Gl, gs, W, nk, nb, Zl);
         __syncthreads();
         TK_TC(17);
-        for (int pass = 0; pass < 3; ++pass) {
+        // intermediate iterations only need the span (the next product is
+        // re-orthonormalised): shifted CholQR2 there, the full CholQR3 on the
+        // basis the Rayleigh-Ritz step uses
+        const int passes = it == iters - 1 ? 3 : 2;
+        for (int pass = 0; pass < passes; ++pass) {
             tk_atb(Zl, Zl, nb, Pg + pb * kP * kS, 0.0);
             TK_TC(18);
             cl.sync();
