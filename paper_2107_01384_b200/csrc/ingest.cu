@@ -388,6 +388,28 @@ double max_abs_finite(const double* x, u64 n, bool* finite, cudaStream_t s) {
     return r[0];
 }
 
+__global__ void diag_sum_kernel(const double* __restrict__ G, u64 n, double* __restrict__ out) {
+    __shared__ double sh[kRedThreads / 32];
+    double t = 0.0;
+    for (u64 i = threadIdx.x; i < n; i += blockDim.x) t += G[i * n + i];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) a += sh[w];
+        *out = a;
+    }
+}
+
+double gram_trace(const double* G, u64 n, cudaStream_t s) {
+    DevBuf<double> o(1, s);
+    diag_sum_kernel<<<1, kRedThreads, 0, s>>>(G, n, o.p);
+    count_launch();
+    TCB_LAUNCH();
+    return o.to_host()[0];
+}
+
 double max_abs(const double* x, u64 n, cudaStream_t s) {
     ProfScope prof_scope(kSum, s);
     const int grid = grid_for(n, kRedThreads, 4, 4);

@@ -20,6 +20,8 @@ void permute_axes(const T* src, T* dst, const std::vector<u64>& shape, const std
 bool ingest_precision_loss(const void* src, int dtype, u64 n, cudaStream_t s);
 // sum of (a_i - b_i)^2 (tensor.cpp:147-164); f32 rounds both sides to float first
 double sse_between(const double* a, const double* b, u64 n, bool f32, cudaStream_t s);
+// trace of an n x n row-major matrix (one round trip)
+double gram_trace(const double* G, u64 n, cudaStream_t s);
 // max |x| with the all-finite flag, one pass and one round trip
 double max_abs_finite(const double* x, u64 n, bool* finite, cudaStream_t s);
 // Exact max |x| (kernels_avx2.cpp:40-66 is order-independent, so exact on any tree).

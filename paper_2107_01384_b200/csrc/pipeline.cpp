@@ -216,7 +216,7 @@ std::vector<double> alpha_weights(const std::vector<double>& sn, u64 n) {
 //   * the Davis-Kahan bound |R_kept|_F / (theta_{r-1} - theta_r - |r_r|) on
 //     the kept subspace's sine is <= 5e-7 (the parity tolerance is 1e-6).
 // V receives the n x r Ritz vectors (unsigned).  false: use the full solver.
-bool topk_factor(const double* G, u64 n, double budget, cudaStream_t s, u64& r_out, double& gone_out,
+bool topk_factor(const double* G, u64 n, const Budget& bud, cudaStream_t s, u64& r_out, double& gone_out,
                  std::vector<double>& s2_out, DevBuf<double>& V) {
     constexpr int p = 32, spare = 8;
     if (!topk_supported(n, p)) return false;
@@ -239,6 +239,7 @@ bool topk_factor(const double* G, u64 n, double budget, cudaStream_t s, u64& r_o
         std::vector<double> th, res;
         double tr = 0.0;
         topk_eig(G, n, p, extra, X.p, th, res, tr, s);
+        const double budget = bud.eval(tr);
         std::vector<double> s2(p);
         for (int j = 0; j < p; ++j) s2[j] = std::max(0.0, th[j]);
         int r = -1;
@@ -277,15 +278,16 @@ bool topk_factor(const double* G, u64 n, double budget, cudaStream_t s, u64& r_o
     return false;
 }
 
-StepOut factor_from_gram(const double* G, u64 n, double budget, cudaStream_t s) {
+StepOut factor_from_gram(const double* G, u64 n, const Budget& bud, cudaStream_t s) {
     {
         StepOut o;
         std::vector<double> s2;
-        if (topk_factor(G, n, budget, s, o.r, o.discarded, s2, o.U)) {
+        if (topk_factor(G, n, bud, s, o.r, o.discarded, s2, o.U)) {
             fix_column_signs(o.U.p, n, o.r, s);
             return o;
         }
     }
+    const double budget = bud.eval(bud.trace_out ? gram_trace(G, n, s) : 0.0);  // (checks the trace first)
     EigWork w;
     const auto ev = eig_values(G, n, w, s);
     std::vector<double> s2(n);
@@ -304,7 +306,7 @@ StepOut factor_from_gram(const double* G, u64 n, double budget, cudaStream_t s) 
     return o;
 }
 
-StepOut mode_step(const double* x, u64 rows, u64 cols, double budget, int backend, cudaStream_t s) {
+StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int backend, cudaStream_t s) {
     const bool via_gram = backend == 1 || (backend == 0 && rows <= cols);
     StepOut o;
     if (via_gram) {
@@ -320,10 +322,11 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, double budget, int backen
         std::vector<double> s2;
         DevBuf<double> V;
         if (!topk_factor(G.p, cols, budget, s, r, gone, s2, V)) {
+            const double bv = budget.eval(budget.trace_out ? gram_trace(G.p, cols, s) : 0.0);
             const auto ev = eig_values(G.p, cols, w, s);
             s2.assign(cols, 0.0);
             for (u64 j = 0; j < cols; ++j) s2[j] = std::max(0.0, ev[j]);
-            std::tie(r, gone) = pick_rank(s2, budget);
+            std::tie(r, gone) = pick_rank(s2, bv);
             if (r == 0) {
                 r = 1;
                 gone -= s2[0];
@@ -350,7 +353,8 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, double budget, int backen
 
 Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vector<u64>& shape, double target,
                       const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite,
-                      const std::function<void(std::size_t, const double*, u64, u64)>& on_factor) {
+                      const std::function<void(std::size_t, const double*, u64, u64)>& on_factor,
+                      double norm_scale, double* norm_out) {
     if (target < 0) throw Error("sthosvd: negative SSE target");
     const std::size_t d = shape.size();
     u64 n_el = 1;
@@ -394,9 +398,18 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
         u64 tot = 1;
         for (auto v : cur) tot *= v;
         const u64 rows = cur[0], cols = tot / rows;
-        const double budget = remaining / static_cast<double>(d - step);
+        Budget budget(remaining / static_cast<double>(d - step));
+        double trace0 = 0.0;
+        if (step == 0 && norm_out) {  // the norm from this Gram; target = norm_scale |A|^2 if >= 0
+            if (norm_scale >= 0) budget.scale = norm_scale / static_cast<double>(d);
+            budget.trace_out = &trace0;
+        }
         HostTrace ht("sthosvd: mode step");
         StepOut so = mode_step(xp, rows, cols, budget, backend, s);
+        if (step == 0 && norm_out) {
+            if (norm_scale >= 0) remaining = norm_scale * trace0;
+            *norm_out = trace0;
+        }
         remaining = std::max(0.0, remaining - so.discarded);
         f.trunc[p[step]] = so.discarded;
         x = std::move(so.next);
@@ -860,6 +873,19 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     res.times.total = ms_since(t_all);
     res.peak_alloc = 2 * n_el * 8 + nc * 9 + res.container.size() * 2;
 }
+namespace {
+thread_local int g_force_norm_pass = 0;
+struct ForceNormPass {
+    ForceNormPass() { ++g_force_norm_pass; }
+    ~ForceNormPass() { --g_force_norm_pass; }
+};
+bool norm_pass_forced() {
+    if (g_force_norm_pass > 0) return true;
+    const char* e = std::getenv("TCB_NORM_PASS");  // debugging: the separate norm pass
+    return e && *e && *e != '0';
+}
+}  // namespace
+
 Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,
                        const Params& prm, cudaStream_t s) {
     const auto t_all = Clock::now();
@@ -883,9 +909,15 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     // internal_float32 the values are first rounded to float as the reference does
     // fp64 input (container::Dtype 9) is used in place: no ingest copy
     const bool direct = !prm.f32 && dtype == 9 && reinterpret_cast<uintptr_t>(device_bytes) % 16 == 0;
+    // fp64 in place: |A|^2 is read off the first mode's Gram (its trace), so no
+    // separate norm pass precedes the mode loop; a non-finite trace falls back to
+    // the element scan (the reference's non-finite error, or a huge finite input)
+    const bool norm_from_gram = direct && !norm_pass_forced();
     DevBuf<double> a;
     bool finite = true;
-    if (direct) {
+    if (direct && norm_from_gram) {
+        res.norm_sq = 0.0;  // set after the first mode step
+    } else if (direct) {
         res.norm_sq = sum_squares(static_cast<const double*>(device_bytes), n_el, &finite, s);
     } else if (prm.f32) {
         a = DevBuf<double>(n_el, s);
@@ -909,6 +941,10 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     if (target < 0) throw Error("budget: negative SSE target");
     if (prm.rtmss < 0 || prm.rtmss > 1) throw Error("budget: rtmss outside [0, 1]");
     res.target_sse = target;
+    // with the norm from the first Gram: target = norm_scale |A|^2 (relative
+    // target), else fixed; either way the norm is reported from the trace
+    double norm_scale = -1.0, norm_trace = 0.0;
+    if (norm_from_gram) norm_scale = prm.target_re ? prm.rtmss * *prm.target_re * *prm.target_re : -1.0;
 
     auto t0 = Clock::now();
     // each factor's orthonormality check + reflectors start on its worker stream
@@ -944,8 +980,25 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
             Workers::get().submit([task] { (*task)(); });
         };
     }
-    Tucker f = sthosvd_device(std::move(a), direct ? static_cast<const double*>(device_bytes) : nullptr, shape,
-                              prm.rtmss * target, prm.mode_order, prm.backend, s, finite ? 1 : 0, on_factor);
+    Tucker f;
+    try {
+        f = sthosvd_device(std::move(a), direct ? static_cast<const double*>(device_bytes) : nullptr, shape,
+                           prm.rtmss * target, prm.mode_order, prm.backend, s, finite ? 1 : 0, on_factor,
+                           norm_scale, norm_from_gram ? &norm_trace : nullptr);
+    } catch (const TraceNonFinite&) {  // scan the elements: the reference error, or a norm pass rerun
+        bool fin = true;
+        sum_squares(static_cast<const double*>(device_bytes), n_el, &fin, s);
+        if (!fin) throw Error("sthosvd: input contains non-finite values");
+        ForceNormPass force;
+        return compress_device(device_bytes, nbytes, dtype, shape, prm, s);
+    }
+    if (norm_from_gram) {
+        res.norm_sq = norm_trace;
+        if (prm.target_re) {
+            target = *prm.target_re * *prm.target_re * res.norm_sq;
+            res.target_sse = target;
+        }
+    }
     double trunc = 0;
     for (double v : f.trunc) trunc += v;
     double core_target = target - trunc;

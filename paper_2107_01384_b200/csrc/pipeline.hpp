@@ -3,6 +3,7 @@
 
 #include <array>
 #include <exception>
+#include <cmath>
 #include <functional>
 #include <optional>
 
@@ -58,9 +59,26 @@ struct StepOut {
     double discarded = 0.0;
     DevBuf<double> U, next;
 };
-StepOut mode_step(const double* x, u64 rows, u64 cols, double budget, int backend, cudaStream_t s);
+// A mode step's SSE budget: a fixed value, or `scale` x trace(G) of the step's
+// Gram -- on the first step trace(B B^T) = |A|_F^2, so the input norm comes with
+// the Gram instead of a separate pass.  The trace used is reported.
+struct TraceNonFinite {};  // the Gram's trace is not finite (scan the input)
+struct Budget {
+    double value = 0.0;
+    double scale = -1.0;
+    double* trace_out = nullptr;
+    Budget(double v = 0.0) : value(v) {}  // NOLINT: implicit from a fixed budget
+    double eval(double trace) const {
+        if (trace_out) {
+            *trace_out = trace;
+            if (!std::isfinite(trace)) throw TraceNonFinite{};
+        }
+        return scale < 0 ? value : scale * trace;
+    }
+};
+StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int backend, cudaStream_t s);
 // eigensolve + rank rule + sign fix on an (all-reduced) Gram; U is n x r
-StepOut factor_from_gram(const double* G, u64 n, double budget, cudaStream_t s);
+StepOut factor_from_gram(const double* G, u64 n, const Budget& budget, cudaStream_t s);
 // sthosvd::compress (sthosvd.cpp:114-171) on a device tensor.  The input is
 // `ext` when non-null (read-only, e.g. the caller's fp64 buffer: with an
 // identity processing order mode 0 reads it in place), else `owned`, which is
@@ -68,9 +86,12 @@ StepOut factor_from_gram(const double* G, u64 n, double budget, cudaStream_t s);
 // already scanned the values (the norm pass), -1 to scan here.
 // on_factor (optional) is called after each mode step with (mode, U, n, r), U
 // complete on `s`.
+// norm_scale >= 0: the target is norm_scale x |A|_F^2 with the norm read off the
+// first Gram's trace (written to *norm_out; TraceNonFinite when it is not finite).
 Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vector<u64>& shape, double target,
                       const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite = -1,
-                      const std::function<void(std::size_t, const double*, u64, u64)>& on_factor = {});
+                      const std::function<void(std::size_t, const double*, u64, u64)>& on_factor = {},
+                      double norm_scale = -1.0, double* norm_out = nullptr);
 inline Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double target,
                              const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s) {
     return sthosvd_device(std::move(a), nullptr, shape, target, order, backend, s);

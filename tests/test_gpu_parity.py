@@ -370,3 +370,25 @@ def test_compress_every_source_dtype_with_skip_bytes(gpu_pkg, dtype):
     y = oracle.decompress(res.container, x.shape)
     xd = x.astype(np.float64)
     assert np.linalg.norm(y - xd) <= 1.05e-3 * np.linalg.norm(xd)
+
+
+def test_norm_from_first_gram(gpu_pkg):
+    """fp64 inputs take |A|^2 from the first mode's Gram trace (no separate norm
+    pass): the reported norm matches numpy, a NaN is still the reference's
+    error under either target kind, and a finite input whose squares overflow
+    falls back to the norm pass (same outcome as before)."""
+    x = synth.small("sin_decay", (40, 36, 28), seed=3)
+    res = gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(target_re=1e-4))
+    assert abs(res.norm_sq - float((x * x).sum())) <= 1e-12 * float((x * x).sum())
+    ref = oracle.compress(x, target_re=1e-4)
+    assert res.ranks == ref.ranks
+    y = x.copy()
+    y[3, 4, 5] = np.inf
+    for prm in (gpu_pkg.Params(target_re=1e-3), gpu_pkg.Params(target_sse=1.0)):
+        with pytest.raises(gpu_pkg.TucompError, match="sthosvd: input contains non-finite values"):
+            gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(y), prm)
+    big = x * 1e160  # finite, but the squares overflow: the element scan decides, then
+    try:              # the separate-norm path runs (an error there is the old behaviour)
+        gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(big), gpu_pkg.Params(target_sse=1e300))
+    except gpu_pkg.TucompError as e:
+        assert "non-finite values" not in str(e)
