@@ -317,6 +317,59 @@ double tcb_peak_dmma_tflops(void) {
 void tcb_free(void* p) { std::free(p); }
 uint64_t tcb_kernel_launches(void) { return launch_counter().load(); }
 
+namespace {
+// fp64 from pinned host memory with the identity processing order: the upload
+// goes in column chunks of the first mode's unfolding (rows x cols, row-major)
+// on a copy stream, and the first Gram's split-K blocks for each chunk start as
+// soon as it lands, so the Gram hides under the PCIe transfer.  Bitwise the same
+// Gram as gram_f64 (same split plan, same reduction).  false: plain upload.
+bool upload_overlapping_gram(const u8* host, u64 nbytes, int dtype, const std::vector<u64>& sh, const Params& prm,
+                             u8* dev, DevBuf<double>& g0, DevBuf<double>& ws, cudaStream_t s) {
+    if (dtype != 9 || prm.f32 || sh.size() < 2 || nbytes < (u64{32} << 20)) return false;
+    if (const char* e = std::getenv("TCB_PLAIN_UPLOAD"); e && *e && *e != '0') return false;
+    const std::vector<u64> p = prm.mode_order ? *prm.mode_order : stable_ascending(sh);
+    for (std::size_t i = 0; i < p.size(); ++i)
+        if (p[i] != i) return false;
+    const u64 rows = sh[0], cols = nbytes / 8 / rows;
+    if (!(prm.backend == 1 || (prm.backend == 0 && rows <= cols))) return false;
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, host) != cudaSuccess || pa.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        return false;  // pageable memory: the copies would not overlap anyway
+    }
+    const double* B = reinterpret_cast<const double*>(dev);
+    const GramPlan gp = gram_plan(B, rows, cols);
+    g0 = DevBuf<double>(rows * rows, s);
+    ws = DevBuf<double>(gram_ws_doubles(gp), s);
+    static cudaStream_t copy = [] {
+        cudaStream_t c;
+        TCB_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+        return c;
+    }();
+    cudaEvent_t start;
+    TCB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    TCB_CUDA(cudaEventRecord(start, s));  // the buffers exist on `s`
+    TCB_CUDA(cudaStreamWaitEvent(copy, start, 0));
+    const u64 chunks = std::min<u64>(8, gp.splits);
+    std::vector<cudaEvent_t> ev(chunks);
+    for (u64 c = 0; c < chunks; ++c) {
+        const u64 sp0 = gp.splits * c / chunks, sp1 = gp.splits * (c + 1) / chunks;
+        const u64 k0 = gram_split_col(gp, sp0, cols), k1 = gram_split_col(gp, sp1, cols);
+        if (k1 > k0)
+            TCB_CUDA(cudaMemcpy2DAsync(dev + k0 * 8, cols * 8, host + k0 * 8, cols * 8, (k1 - k0) * 8, rows,
+                                       cudaMemcpyHostToDevice, copy));
+        TCB_CUDA(cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming));
+        TCB_CUDA(cudaEventRecord(ev[c], copy));
+        TCB_CUDA(cudaStreamWaitEvent(s, ev[c], 0));
+        gram_splits(B, rows, cols, gp, sp0, sp1, ws.p, s);
+    }
+    gram_reduce(gp, ws.p, rows, g0.p, s);
+    for (auto e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(start);
+    return true;
+}
+}  // namespace
+
 int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d, uint64_t skip,
                  const tcb_params* params, tcb_result* out) {
     return guard([&] {
@@ -327,9 +380,12 @@ int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_
         if (nbytes != expect)
             throw Error("ingest: buffer holds " + std::to_string(nbytes) + " bytes, expected " + std::to_string(expect));
         Stream st;
+        const Params prm = to_params(params, d);
         DevBuf<u8> dev(nbytes - skip + 16, st.s);
-        dev.upload(bytes + skip, nbytes - skip);
-        const Result r = compress_device(dev.p, nbytes - skip, dtype, sh, to_params(params, d), st.s);
+        DevBuf<double> g0, ws;
+        if (!upload_overlapping_gram(bytes + skip, nbytes - skip, dtype, sh, prm, dev.p, g0, ws, st.s))
+            dev.upload(bytes + skip, nbytes - skip);
+        const Result r = compress_device(dev.p, nbytes - skip, dtype, sh, prm, st.s, g0.p);
         host_trace_dump();
         fill(r, d, out);
     });

@@ -69,13 +69,13 @@ __device__ __forceinline__ void load_slab(double (*s)[GPAD], const double* __res
 // same k-chunk and share B's row blocks through L2 (one DRAM pass over B).
 template <bool V16>
 __global__ void __launch_bounds__(256) syrk_kernel(const double* __restrict__ B, u64 rows, u64 cols,
-                                                  int ntiles_lower, u64 slabs_per_split, u64 nslab,
+                                                  int ntiles_lower, u64 slabs_per_split, u64 nslab, u64 split0,
                                                   double* __restrict__ ws) {
     extern __shared__ __align__(16) double smem_syrk[];
     auto As = reinterpret_cast<double (*)[GT][GPAD]>(smem_syrk);
     auto Bs = reinterpret_cast<double (*)[GT][GPAD]>(smem_syrk + 2 * GT * GPAD);
     const int tile = blockIdx.x % ntiles_lower;
-    const u64 split = blockIdx.x / ntiles_lower;
+    const u64 split = split0 + blockIdx.x / ntiles_lower;
     const u64 s0 = split * slabs_per_split, s1 = min(nslab, s0 + slabs_per_split);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(256) syrk_kernel(const double* __restrict__ B,
         }
         __syncthreads();
     }
-    double* out = ws + static_cast<u64>(blockIdx.x) * GT * GT;
+    double* out = ws + (split * ntiles_lower + tile) * GT * GT;
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -308,12 +308,12 @@ double peak_dmma_tflops() {
     return flops / (ms * 1e-3) / 1e12;
 }
 
-void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
-    ProfScope prof_scope(kGram, s);
+GramPlan gram_plan(const double* B, u64 rows, u64 cols) {
+    GramPlan gp;
     const int nt = static_cast<int>((rows + GT - 1) / GT);
-    const int lower = nt * (nt + 1) / 2;
-    const u64 nslab = (cols + GBK - 1) / GBK;
-    const bool v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+    gp.lower = nt * (nt + 1) / 2;
+    gp.nslab = (cols + GBK - 1) / GBK;
+    gp.v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
     const int smem = 4 * GT * GPAD * sizeof(double);
     static int per_sm = [&] {
         cudaFuncSetAttribute(syrk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -323,18 +323,42 @@ void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
         return std::max(1, b);
     }();
     const u64 slots = static_cast<u64>(per_sm) * sm_count();
-    u64 splits = std::max<u64>(1, std::min<u64>(nslab, slots / lower));
-    const u64 per = (nslab + splits - 1) / splits;
-    splits = (nslab + per - 1) / per;
-    DevBuf<double> ws(splits * lower * GT * GT, s);
-    const unsigned grid = static_cast<unsigned>(splits * lower);
-    if (v16)
-        syrk_kernel<true><<<grid, 256, smem, s>>>(B, rows, cols, lower, per, nslab, ws.p);
+    u64 splits = std::max<u64>(1, std::min<u64>(gp.nslab, slots / gp.lower));
+    gp.per = (gp.nslab + splits - 1) / splits;
+    gp.splits = (gp.nslab + gp.per - 1) / gp.per;
+    return gp;
+}
+
+u64 gram_ws_doubles(const GramPlan& gp) { return gp.splits * gp.lower * GT * GT; }
+
+u64 gram_split_col(const GramPlan& gp, u64 split, u64 cols) { return std::min<u64>(cols, split * gp.per * GBK); }
+
+void gram_splits(const double* B, u64 rows, u64 cols, const GramPlan& gp, u64 sp0, u64 sp1, double* ws,
+                 cudaStream_t s) {
+    if (sp1 <= sp0) return;
+    ProfScope prof_scope(kGram, s);
+    const int smem = 4 * GT * GPAD * sizeof(double);
+    const unsigned grid = static_cast<unsigned>((sp1 - sp0) * gp.lower);
+    if (gp.v16)
+        syrk_kernel<true><<<grid, 256, smem, s>>>(B, rows, cols, gp.lower, gp.per, gp.nslab, sp0, ws);
     else
-        syrk_kernel<false><<<grid, 256, smem, s>>>(B, rows, cols, lower, per, nslab, ws.p);
-    syrk_reduce<<<dim3(lower, 16), 256, 0, s>>>(ws.p, static_cast<int>(splits), lower, rows, G);
-    count_launch(2);
+        syrk_kernel<false><<<grid, 256, smem, s>>>(B, rows, cols, gp.lower, gp.per, gp.nslab, sp0, ws);
+    count_launch();
     TCB_LAUNCH();
+}
+
+void gram_reduce(const GramPlan& gp, const double* ws, u64 rows, double* G, cudaStream_t s) {
+    ProfScope prof_scope(kGram, s);
+    syrk_reduce<<<dim3(gp.lower, 16), 256, 0, s>>>(ws, static_cast<int>(gp.splits), gp.lower, rows, G);
+    count_launch();
+    TCB_LAUNCH();
+}
+
+void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
+    const GramPlan gp = gram_plan(B, rows, cols);
+    DevBuf<double> ws(gram_ws_doubles(gp), s);
+    gram_splits(B, rows, cols, gp, 0, gp.splits, ws.p, s);
+    gram_reduce(gp, ws.p, rows, G, s);
 }
 
 void gram_cols_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {

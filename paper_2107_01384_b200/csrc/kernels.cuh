@@ -30,6 +30,21 @@ double max_abs(const double* x, u64 n, cudaStream_t s);
 // ---- gram.cu: G = B B^T (B row-major rows x cols), fp64 DMMA, deterministic split-K.
 // G is written full symmetric, row-major rows x rows.
 void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s);
+// The same computation in pieces (bitwise identical): the split-K plan, the
+// splits [sp0, sp1) (they read only columns [split_col(sp0), split_col(sp1)) of
+// B, so they can run as soon as those columns are resident), the fixed-order
+// reduction.  gram_f64 = plan + all splits + reduce.
+struct GramPlan {
+    int lower = 0;
+    u64 nslab = 0, per = 0, splits = 0;
+    bool v16 = false;
+};
+GramPlan gram_plan(const double* B, u64 rows, u64 cols);
+u64 gram_ws_doubles(const GramPlan& gp);
+u64 gram_split_col(const GramPlan& gp, u64 split, u64 cols);
+void gram_splits(const double* B, u64 rows, u64 cols, const GramPlan& gp, u64 sp0, u64 sp1, double* ws,
+                 cudaStream_t s);
+void gram_reduce(const GramPlan& gp, const double* ws, u64 rows, double* G, cudaStream_t s);
 // G = B^T B (cols x cols) for the rows > cols branch (sthosvd.cpp:91-99 stand-in).
 void gram_cols_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s);
 

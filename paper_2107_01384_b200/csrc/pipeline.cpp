@@ -306,13 +306,17 @@ StepOut factor_from_gram(const double* G, u64 n, const Budget& bud, cudaStream_t
     return o;
 }
 
-StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int backend, cudaStream_t s) {
+StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int backend, cudaStream_t s,
+                  const double* gram) {
     const bool via_gram = backend == 1 || (backend == 0 && rows <= cols);
     StepOut o;
     if (via_gram) {
-        DevBuf<double> G(rows * rows, s);
-        gram_f64(x, rows, cols, G.p, s);
-        o = factor_from_gram(G.p, rows, budget, s);
+        DevBuf<double> G;
+        if (!gram) {
+            G = DevBuf<double>(rows * rows, s);
+            gram_f64(x, rows, cols, G.p, s);
+        }
+        o = factor_from_gram(gram ? gram : G.p, rows, budget, s);
     } else {  // thin left singular vectors from the Gram of B^T (sthosvd.cpp:91-99)
         EigWork w;
         DevBuf<double> G(cols * cols, s);
@@ -354,7 +358,7 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
 Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vector<u64>& shape, double target,
                       const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite,
                       const std::function<void(std::size_t, const double*, u64, u64)>& on_factor,
-                      double norm_scale, double* norm_out) {
+                      double norm_scale, double* norm_out, const double* gram0) {
     if (target < 0) throw Error("sthosvd: negative SSE target");
     const std::size_t d = shape.size();
     u64 n_el = 1;
@@ -405,7 +409,7 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
             budget.trace_out = &trace0;
         }
         HostTrace ht("sthosvd: mode step");
-        StepOut so = mode_step(xp, rows, cols, budget, backend, s);
+        StepOut so = mode_step(xp, rows, cols, budget, backend, s, step == 0 && ident ? gram0 : nullptr);
         if (step == 0 && norm_out) {
             if (norm_scale >= 0) remaining = norm_scale * trace0;
             *norm_out = trace0;
@@ -887,7 +891,7 @@ bool norm_pass_forced() {
 }  // namespace
 
 Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,
-                       const Params& prm, cudaStream_t s) {
+                       const Params& prm, cudaStream_t s, const double* gram0) {
     const auto t_all = Clock::now();
     Result res;
     const std::size_t d = shape.size();
@@ -984,13 +988,13 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     try {
         f = sthosvd_device(std::move(a), direct ? static_cast<const double*>(device_bytes) : nullptr, shape,
                            prm.rtmss * target, prm.mode_order, prm.backend, s, finite ? 1 : 0, on_factor,
-                           norm_scale, norm_from_gram ? &norm_trace : nullptr);
+                           norm_scale, norm_from_gram ? &norm_trace : nullptr, direct ? gram0 : nullptr);
     } catch (const TraceNonFinite&) {  // scan the elements: the reference error, or a norm pass rerun
         bool fin = true;
         sum_squares(static_cast<const double*>(device_bytes), n_el, &fin, s);
         if (!fin) throw Error("sthosvd: input contains non-finite values");
         ForceNormPass force;
-        return compress_device(device_bytes, nbytes, dtype, shape, prm, s);
+        return compress_device(device_bytes, nbytes, dtype, shape, prm, s, gram0);
     }
     if (norm_from_gram) {
         res.norm_sq = norm_trace;

@@ -42,8 +42,11 @@ struct Result {
 };
 
 // device_bytes: element bytes (skip already applied) resident on the device
+// gram0 (optional): the first mode's Gram of the fp64 input, already computed
+// (bitwise as gram_f64 would; the host entry point overlaps it with the upload)
 Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,
-                       const Params& p, cudaStream_t s);
+                       const Params& p, cudaStream_t s,
+                       const double* gram0 = nullptr);
 
 struct Tucker {
     DevBuf<double> core;
@@ -76,7 +79,9 @@ struct Budget {
         return scale < 0 ? value : scale * trace;
     }
 };
-StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int backend, cudaStream_t s);
+// gram (optional): this step's Gram B B^T already computed (rows <= cols branch)
+StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int backend, cudaStream_t s,
+                  const double* gram = nullptr);
 // eigensolve + rank rule + sign fix on an (all-reduced) Gram; U is n x r
 StepOut factor_from_gram(const double* G, u64 n, const Budget& budget, cudaStream_t s);
 // sthosvd::compress (sthosvd.cpp:114-171) on a device tensor.  The input is
@@ -91,7 +96,7 @@ StepOut factor_from_gram(const double* G, u64 n, const Budget& budget, cudaStrea
 Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vector<u64>& shape, double target,
                       const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite = -1,
                       const std::function<void(std::size_t, const double*, u64, u64)>& on_factor = {},
-                      double norm_scale = -1.0, double* norm_out = nullptr);
+                      double norm_scale = -1.0, double* norm_out = nullptr, const double* gram0 = nullptr);
 inline Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double target,
                              const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s) {
     return sthosvd_device(std::move(a), nullptr, shape, target, order, backend, s);
