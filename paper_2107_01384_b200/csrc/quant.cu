@@ -38,13 +38,24 @@ __global__ void slice_norm_kernel(const u64* __restrict__ mag, const u64* __rest
     for (int i = a + 1; i < d; ++i) inner *= shape[i];
     for (int i = 0; i < a; ++i) outer *= shape[i];
     const u64 ext = shape[a];
+    // the reference's serial order (outer, then inner), 8 elements per step: their
+    // loads are issued together so the dependent adds do not wait on memory
     double s = 0.0;
-    for (u64 o = 0; o < outer; ++o) {
-        const u64* p = mag + (o * ext + idx) * inner;
-        for (u64 q = 0; q < inner; ++q) {
-            const double v = __ull2double_rn(p[q]);
-            s = __dadd_rn(s, __dmul_rn(v, v));
+    const u64 cnt = outer * inner;
+    u64 o = 0, q = 0;  // position of element j in (outer, inner)
+    for (u64 j0 = 0; j0 < cnt; j0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            v[u] = j0 + u < cnt ? __ull2double_rn(mag[(o * ext + idx) * inner + q]) : 0.0;
+            if (++q == inner) {
+                q = 0;
+                ++o;
+            }
         }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (j0 + u < cnt) s = __dadd_rn(s, __dmul_rn(v[u], v[u]));
     }
     out[t] = __dsqrt_rn(__dmul_rn(s, down));
 }
@@ -119,9 +130,14 @@ __global__ void slice_norm_list_kernel(const u64* __restrict__ mag, const u64* _
     const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= ext) return;
     double s = 0.0;
-    for (u64 j = idx * per; j < (idx + 1) * per; ++j) {
-        const double v = __ull2double_rn(mag[list[j]]);
-        s = __dadd_rn(s, __dmul_rn(v, v));
+    const u64 j1 = (idx + 1) * per;
+    for (u64 j0 = idx * per; j0 < j1; j0 += 8) {  // 8 gathers in flight per step
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = j0 + u < j1 ? __ull2double_rn(mag[list[j0 + u]]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (j0 + u < j1) s = __dadd_rn(s, __dmul_rn(v[u], v[u]));
     }
     out[idx] = __dsqrt_rn(__dmul_rn(s, down));
 }
