@@ -46,7 +46,8 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in process via
+    NVML (no nvidia-smi fork inside the timed region), nvidia-smi as a fallback."""
 
     def __init__(self, index=0):
         self.index = index
@@ -55,19 +56,43 @@ class ClockSampler:
         self._t = None
 
     def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            bits = [getattr(pynvml, n, 0) for n in ("nvmlClocksEventReasonHwSlowdown",
+                                                    "nvmlClocksEventReasonHwThermalSlowdown",
+                                                    "nvmlClocksEventReasonSwThermalSlowdown",
+                                                    "nvmlClocksEventReasonSwPowerCap")]
+            bits = [b or d for b, d in zip(bits, (0x8, 0x40, 0x20, 0x4))]
+            reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def sample():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = reasons_fn(h)
+                return [str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits]
+        except Exception:
+            sample = None
+
         def run():
             q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([v.strip() for v in out.split(",")])
+                    if sample is not None:
+                        self.samples.append(sample())
+                    else:
+                        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                             timeout=5).stdout.strip()
+                        if out:
+                            self.samples.append([v.strip() for v in out.split(",")])
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.02 if sample is not None else 0.2)
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()

@@ -308,7 +308,11 @@ StepOut factor_from_gram(const double* G, u64 n, const Budget& bud, cudaStream_t
 
 StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int backend, cudaStream_t s,
                   const double* gram) {
-    const bool via_gram = backend == 1 || (backend == 0 && rows <= cols);
+    // rows > cols is the reference's thin-SVD branch (sthosvd.cpp:91-99); its
+    // stand-in here (Gram of B^T, U = B V / sigma, re-orthonormalised) is no more
+    // accurate than the Gram of B itself -- both square the singular values -- so
+    // a small row count takes the cheaper direct Gram route
+    const bool via_gram = backend == 1 || (backend == 0 && (rows <= cols || rows <= 256));
     StepOut o;
     if (via_gram) {
         DevBuf<double> G;
