@@ -10,6 +10,6 @@ python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.jso
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
 ncu --set full --import-source on --clock-control none \
-    -k regex:"syrk_kernel|ttm_kernel|tk_rr|tk_cqr|tk_gq|ac_kernel|householder_dataflow|crossing_kernel|emit_kernel|stats_kernel" \
+    -k regex:"syrk_kernel|syrk_reduce|ttm_kernel|tk_cluster|ac_kernel|householder_dataflow|crossing_kernel|emit_kernel|stats_kernel" \
     -c 24 -o gpurun_out/full python tools/compress_once.py --warmup 0 > gpurun_out/ncu_full.log 2>&1
 echo done
