@@ -653,13 +653,12 @@ __global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, co
     u8 cache = 0;
     auto shift = [&]() {
         if (static_cast<u32>(low) < 0xFF000000u || (low >> 32) != 0) {
+            // the cached byte and the pending 0xFF run (plus the carry), one byte per
+            // lane: no serial loop, no divergent branch
             const u8 carry = static_cast<u8>(low >> 32);
-            u8 first = cache;
-            if (lane == 0) {
-                for (u64 q = 0; q < pending; ++q) {
-                    out[pos + q] = static_cast<u8>(first + carry);
-                    first = 0xFF;
-                }
+            for (u64 q0 = 0; q0 < pending; q0 += 32) {
+                const u64 q = q0 + static_cast<u64>(lane);
+                if (q < pending) out[pos + q] = static_cast<u8>((q == 0 ? cache : u8{0xFF}) + carry);
             }
             pos += pending;
             pending = 0;
@@ -779,12 +778,17 @@ __global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, co
         // 2^-32 while a non-integer quotient is at least 1/T below the next integer);
         // each lane prepares its own T's multiplier off the sequential path.
         const u64 magic = tot > 1u ? (~u64{0} / tot) + 1u : 0u;
-        // range coder over the chunk (identical state in every lane)
+        // range coder over the chunk (identical state in every lane); symbol l + 1's
+        // operands are fetched while symbol l is coded (the shuffles are off the
+        // coder's dependency chain)
+        u32 c = __shfl_sync(0xffffffffu, cum, 0), f = __shfl_sync(0xffffffffu, freq, 0);
+        u32 T = __shfl_sync(0xffffffffu, tot, 0);
+        u64 v = __shfl_sync(0xffffffffu, sv, 0), M = __shfl_sync(0xffffffffu, magic, 0);
         for (u32 l = 0; l < L; ++l) {
-            const u32 c = __shfl_sync(0xffffffffu, cum, l), f = __shfl_sync(0xffffffffu, freq, l);
-            const u32 T = __shfl_sync(0xffffffffu, tot, l);
-            const u64 v = __shfl_sync(0xffffffffu, sv, l);
-            const u64 M = __shfl_sync(0xffffffffu, magic, l);
+            const u32 ln = l + 1 < L ? l + 1 : l;
+            const u32 c_n = __shfl_sync(0xffffffffu, cum, ln), f_n = __shfl_sync(0xffffffffu, freq, ln);
+            const u32 T_n = __shfl_sync(0xffffffffu, tot, ln);
+            const u64 v_n = __shfl_sync(0xffffffffu, sv, ln), M_n = __shfl_sync(0xffffffffu, magic, ln);
             range = T > 1u ? static_cast<u32>(__umul64hi(static_cast<u64>(range), M)) : range;
             low += static_cast<u64>(c) * range;
             range *= f;
@@ -799,17 +803,22 @@ __global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, co
                 int left = 32;
                 while (left > 0) {
                     const int k = min(left, (31 - __clz(static_cast<int>(range))) - 23);
-                    const u32 c = (raw >> (left - k)) & ((1u << k) - 1u);
+                    const u32 cb = (raw >> (left - k)) & ((1u << k) - 1u);
                     u64 add = 0;
 #pragma unroll
                     for (int j = 1; j <= 8; ++j)
-                        if (j <= k && ((c >> (k - j)) & 1u)) add += range >> j;
+                        if (j <= k && ((cb >> (k - j)) & 1u)) add += range >> j;
                     low += add;
                     range >>= k;
                     left -= k;
                     norm();
                 }
             }
+            c = c_n;
+            f = f_n;
+            T = T_n;
+            v = v_n;
+            M = M_n;
         }
         // model update: increments in symbol order, a halving before the last one
         auto inc = [&](bool doit) {
