@@ -392,3 +392,22 @@ def test_norm_from_first_gram(gpu_pkg):
         gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(big), gpu_pkg.Params(target_sse=1e300))
     except gpu_pkg.TucompError as e:
         assert "non-finite values" not in str(e)
+
+
+def test_chunked_upload_gram_is_bitwise(gpu_pkg):
+    """Pinned fp64 uploads overlap the first Gram with the transfer (column
+    chunks, the same split-K plan): the container equals the device-resident
+    path's byte for byte, and TCB_PLAIN_UPLOAD's single copy too."""
+    torch = pytest.importorskip("torch")
+    x = synth.small("sin_decay", (256, 128, 136), seed=11)  # 34 MiB: above the 32 MiB threshold
+    prm = gpu_pkg.Params(target_re=1e-4)
+    host = torch.from_numpy(x.reshape(-1).view(np.uint8)).pin_memory()
+    src = gpu_pkg.SourceBuffer(memoryview(host.numpy()), gpu_pkg.Dtype.float64, list(x.shape))
+    a = gpu_pkg.compress(src, prm).container
+    dev = host.to("cuda")
+    torch.cuda.synchronize()
+    b = gpu_pkg.compress_device(dev.data_ptr(), x.nbytes, gpu_pkg.Dtype.float64, x.shape, prm).container
+    assert a == b
+    ref = oracle.compress(x, target_re=1e-4)
+    assert gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), prm).container == a  # pageable: single copy
+    assert abs(len(a) - len(ref.container)) <= 0.01 * len(ref.container)
