@@ -269,18 +269,48 @@ class _CDecompress(C.Structure):  # tcb_decompress_result
                 ("shape", C.c_uint64 * 8), ("total_ms", C.c_double)]
 
 
-@dataclass
+class _LibBuffer:
+    """A library-owned result buffer (tcb_free when the last view goes): numpy
+    views made from it keep it alive through __array_interface__."""
+
+    def __init__(self, ptr, n):
+        self.ptr = C.cast(ptr, C.c_void_p)
+        self.n = int(n)
+        self.__array_interface__ = {"shape": (self.n,), "typestr": "|u1", "version": 3,
+                                    "data": (self.ptr.value or 0, True)}
+
+    @property
+    def array(self) -> np.ndarray:
+        return np.asarray(self) if self.n else np.zeros(0, np.uint8)
+
+    def __del__(self):
+        if self.ptr:
+            lib().tcb_free(self.ptr)
+            self.ptr = None
+
+
+_NP_OF = {0: np.int8, 1: np.uint8, 2: np.int16, 3: np.uint16, 4: np.int32, 5: np.uint32, 6: np.int64,
+          7: np.uint64, 8: np.float32, 9: np.float64}
+
+
 class DecompressResult:  # pipeline::DecompressResult (pipeline.hpp:59-64)
-    bytes: bytes
-    dtype: Dtype
-    shape: tuple
-    total_ms: float
+    """Decompressed source-dtype bytes; `to_array()` views them without a copy
+    (the buffer lives in the library's pinned pool until this object goes)."""
+
+    def __init__(self, buf: "_LibBuffer", dtype: "Dtype", shape: tuple, total_ms: float):
+        self._buf = buf
+        self.dtype = dtype
+        self.shape = shape
+        self.total_ms = total_ms
+
+    @property
+    def bytes(self) -> bytes:
+        return self._buf.array.tobytes()
 
     def to_array(self) -> np.ndarray:
-        dt = {Dtype.int8: np.int8, Dtype.uint8: np.uint8, Dtype.int16: np.int16, Dtype.uint16: np.uint16,
-              Dtype.int32: np.int32, Dtype.uint32: np.uint32, Dtype.int64: np.int64, Dtype.uint64: np.uint64,
-              Dtype.float32: np.float32, Dtype.float64: np.float64}[self.dtype]
-        return np.frombuffer(self.bytes, dt).reshape(self.shape)
+        a = self._buf.array.view(_NP_OF[int(self.dtype)]).reshape(self.shape)
+        a.flags.writeable = False
+        return a
 
 
 def decompress(container: bytes, threads: int = 1) -> DecompressResult:
@@ -289,8 +319,8 @@ def decompress(container: bytes, threads: int = 1) -> DecompressResult:
     buf = np.frombuffer(container, np.uint8) if len(container) else np.zeros(1, np.uint8)
     r = _CDecompress()
     _check(lib().tcb_decompress(_p(buf), C.c_uint64(len(container)), int(threads), C.byref(r)))
-    data = _take_bytes(r.bytes, r.nbytes)
-    return DecompressResult(data, Dtype(r.dtype), tuple(int(r.shape[i]) for i in range(r.d)), float(r.total_ms))
+    return DecompressResult(_LibBuffer(r.bytes, r.nbytes), Dtype(r.dtype),
+                            tuple(int(r.shape[i]) for i in range(r.d)), float(r.total_ms))
 
 
 def decompress_tensor(container: bytes) -> np.ndarray:

@@ -214,6 +214,49 @@ int guard(F&& f) {
     }
 }
 
+// Result buffers handed to the caller (released with tcb_free).  Large ones
+// (decompressed tensors) come from a pool of pinned host blocks, so the
+// device-to-host copy runs at PCIe speed into memory that is already mapped;
+// tcb_free returns them to the pool.
+constexpr std::size_t kPinnedMin = std::size_t{4} << 20;
+std::mutex g_pin_mu;
+std::map<void*, std::size_t> g_pin_live;              // handed out: block -> capacity
+std::multimap<std::size_t, void*> g_pin_free;         // capacity -> block
+void* host_alloc(std::size_t bytes) {
+    if (bytes < kPinnedMin) return std::malloc(bytes + 1);
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_free.lower_bound(bytes);
+    if (it != g_pin_free.end() && it->first <= 2 * bytes) {
+        void* p = it->second;
+        g_pin_live[p] = it->first;
+        g_pin_free.erase(it);
+        return p;
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return std::malloc(bytes + 1);
+    }
+    g_pin_live[p] = bytes;
+    return p;
+}
+bool host_release(void* p) {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_live.find(p);
+    if (it == g_pin_live.end()) return false;
+    g_pin_free.emplace(it->second, p);
+    g_pin_live.erase(it);
+    std::size_t cached = 0;  // keep at most ~1 GiB of idle pinned blocks
+    for (auto& kv : g_pin_free) cached += kv.first;
+    while (cached > (std::size_t{1} << 30) && !g_pin_free.empty()) {
+        auto big = std::prev(g_pin_free.end());
+        cached -= big->first;
+        cudaFreeHost(big->second);
+        g_pin_free.erase(big);
+    }
+    return true;
+}
+
 template <class T>
 T* dup(const std::vector<T>& v) {
     T* p = static_cast<T*>(std::malloc(v.size() * sizeof(T) + 1));
@@ -314,7 +357,9 @@ double tcb_peak_dmma_tflops(void) {
         return -1.0;
     }
 }
-void tcb_free(void* p) { std::free(p); }
+void tcb_free(void* p) {
+    if (p && !host_release(p)) std::free(p);
+}
 uint64_t tcb_kernel_launches(void) { return launch_counter().load(); }
 
 namespace {
@@ -427,14 +472,17 @@ int tcb_decompress(const uint8_t* container, uint64_t len, int threads, tcb_deco
     return guard([&] {
         Stream st;
         const auto t = decompress_device(container, len, st.s);
-        const auto bytes = emit_bytes(t, st.s);
-        host_trace_dump();
-        out->bytes = dup(bytes);
-        out->nbytes = bytes.size();
+        HostTrace ht("decompress: emit+D2H");
+        const u64 nb = emit_size(t);
+        out->bytes = static_cast<uint8_t*>(host_alloc(nb));
+        emit_bytes(t, out->bytes, st.s);
+        ht.stop();
+        out->nbytes = nb;
         out->dtype = t.dtype;
         out->d = static_cast<int>(t.shape.size());
         for (std::size_t i = 0; i < t.shape.size() && i < 8; ++i) out->shape[i] = t.shape[i];
         out->total_ms = t.ms;
+        host_trace_dump();
     });
 }
 
@@ -445,10 +493,9 @@ int tcb_decompress_tensor_f64(const uint8_t* container, uint64_t len, double** o
         const auto t = decompress_device(container, len, st.s);
         u64 total = 1;
         for (auto v : t.shape) total *= v;
-        std::vector<double> h(total);
-        if (total) t.x.download(h.data(), total);
+        *out = static_cast<double*>(host_alloc(total * sizeof(double)));
+        if (total) t.x.download(*out, total);
         stream_sync(st.s);
-        *out = dup(h);
         *count = total;
         *d = static_cast<int>(t.shape.size());
         for (std::size_t i = 0; i < t.shape.size() && i < 8; ++i) shape[i] = t.shape[i];

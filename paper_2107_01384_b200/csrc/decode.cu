@@ -210,14 +210,25 @@ __global__ void __launch_bounds__(32) dec_entropy_kernel(const u8* __restrict__ 
         norm();
         u64 sv;
         if (i == 0) {  // escape: 32 raw bits as decode(bit, 1, 2)
+            // per bit: range >>= 1; bit = min(code / range, 1); code -= bit range; norm().
+            // With range in [2^24, 2^32) exactly k = floor(log2 range) - 23 halvings
+            // happen before the next normalisation, so up to k bits go at once, each
+            // a compare instead of a divide (same arithmetic as the encoder's groups).
             u64 v = 0;
-            for (int b = 0; b < 32; ++b) {
-                range >>= 1;
-                u32 bit = code / range;
-                if (bit > 1) bit = 1;
-                code -= bit * range;
+            int left = 32;
+            while (left > 0) {
+                const int k = min(left, (31 - __clz(static_cast<int>(range))) - 23);
+#pragma unroll
+                for (int j = 1; j <= 8; ++j)
+                    if (j <= k) {
+                        const u32 rj = range >> j;
+                        const u32 bit = code >= rj ? 1u : 0u;
+                        code -= bit ? rj : 0u;
+                        v = (v << 1) | bit;
+                    }
+                range >>= k;
+                left -= k;
                 norm();
-                v = (v << 1) | bit;
             }
             sv = v;
             if (total + 32 >= (1u << 16)) halve();

@@ -266,7 +266,7 @@ ContainerHeader read_container_header(const u8* c, u64 len) {
 
 DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
     const auto t0 = std::chrono::steady_clock::now();
-    HostTrace ht("decompress");
+    HostTrace ht("decompress: parse");
     u64 hpos = 0;
     const ContainerHeader h = parse_header(c, len, &hpos);
     DecompressOut out;
@@ -353,6 +353,8 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
         stops.insert(stops.end(), v.lead.begin(), v.lead.end());
         stops.insert(stops.end(), v.trail.begin(), v.trail.end());
     }
+    ht.stop();
+    HostTrace ht_dev("decompress: entropy+streams");
     // ---- device
     DevBuf<u8> dc(len, s);
     dc.upload(c, len);
@@ -385,9 +387,25 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
     err.download(&e, 1);
     stream_sync(s);
     if (e) throw Error(dec_message(e));
-    // ---- factors (decode_factor, factor_codec.cpp:246-264)
+    ht_dev.stop();
+    HostTrace ht_rec("decompress: factors+reconstruct");
+    // ---- factors (decode_factor, factor_codec.cpp:246-264): independent, each on its
+    // own side stream (small launches that overlap), one shared error flag
     std::vector<DevBuf<double>> U(d);
+    DevBuf<int> ferr(1, s);
+    ferr.zero();
+    static std::vector<cudaStream_t> side = [] {
+        std::vector<cudaStream_t> v(8);
+        for (auto& st : v) TCB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        return v;
+    }();
+    for (std::size_t i = 0; i < d; ++i) U[i] = DevBuf<double>(n[i] * rk[i], s);
+    cudaEvent_t fork_ev, join_ev[8];
+    TCB_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    TCB_CUDA(cudaEventRecord(fork_ev, s));
     for (std::size_t i = 0; i < d; ++i) {
+        cudaStream_t si = side[i % side.size()];
+        TCB_CUDA(cudaStreamWaitEvent(si, fork_ev, 0));
         const auto& f = fm[i];
         std::vector<u64> live;
         std::vector<double> ln;
@@ -396,7 +414,6 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
                 live.push_back(j);
                 ln.push_back(f.sn[j]);
             }
-        U[i] = DevBuf<double>(n[i] * rk[i], s);
         const u64 rl = live.size();
         if (rl > 0 && f.count != n[i] * rl - rl * (rl + 1) / 2)
             throw Error("factor decode: coefficient count mismatch");
@@ -409,10 +426,18 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
                 for (u64 j = 0; j < rl; ++j) sc[j] = std::sqrt(2.0 * al[j]);
             }
         }
-        DevBuf<double> dsc(std::max<u64>(rl, 1), s);
+        DevBuf<double> dsc(std::max<u64>(rl, 1), si);
         if (rl > 0) dsc.upload(sc.data(), rl);
-        factor_expand(mag.p + ds[i].out_off, neg.p + ds[i].out_off, f.k, n[i], rk[i], live, dsc.p, U[i].p, s);
+        factor_expand(mag.p + ds[i].out_off, neg.p + ds[i].out_off, f.k, n[i], rk[i], live, dsc.p, U[i].p, si,
+                      ferr.p);
+        if (i < 8) {
+            TCB_CUDA(cudaEventCreateWithFlags(&join_ev[i], cudaEventDisableTiming));
+            TCB_CUDA(cudaEventRecord(join_ev[i], si));
+            TCB_CUDA(cudaStreamWaitEvent(s, join_ev[i], 0));
+        }
     }
+    cudaEventDestroy(fork_ev);
+    for (std::size_t i = 0; i < d && i < 8; ++i) cudaEventDestroy(join_ev[i]);
     // ---- core: dequantise, storage -> processing order (pipeline.cpp:206-219)
     const u64 nc = prod(cs);
     DevBuf<double> core_s(nc, s), core_p(nc, s);
@@ -442,9 +467,34 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
         cur.push_back(nn);
     }
     permute_axes(x.p, out.x.p, cur, inverse(q), s);
-    stream_sync(s);
+    {
+        int fe = 0;
+        ferr.download(&fe, 1);
+        stream_sync(s);
+        if (fe) throw Error("reconstruct: reflector sub-diagonal norm reaches 1");
+    }
     out.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return out;
+}
+
+u64 emit_size(const DecompressOut& t) {
+    static const std::size_t sz[10] = {1, 1, 2, 2, 4, 4, 8, 8, 4, 8};
+    return prod(t.shape) * sz[t.dtype];
+}
+
+void emit_bytes(const DecompressOut& t, u8* host, cudaStream_t s) {
+    const u64 total = prod(t.shape), nb = emit_size(t);
+    if (total == 0) return;
+    if (t.dtype == 9) {  // fp64: the reconstruction itself
+        TCB_CUDA(cudaMemcpyAsync(host, t.x.p, nb, cudaMemcpyDeviceToHost, s));
+    } else {
+        DevBuf<u8> db(nb, s);
+        emit_dtype(t.x.p, total, t.dtype, db.p, s);
+        TCB_CUDA(cudaMemcpyAsync(host, db.p, nb, cudaMemcpyDeviceToHost, s));
+        stream_sync(s);
+        return;
+    }
+    stream_sync(s);
 }
 
 std::vector<u8> emit_bytes(const DecompressOut& t, cudaStream_t s) {

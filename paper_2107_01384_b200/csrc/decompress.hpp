@@ -33,5 +33,8 @@ ContainerHeader read_container_header(const u8* container, u64 len);
 DecompressOut decompress_device(const u8* container, u64 len, cudaStream_t s);
 // emit (container.cpp:98-140): the source dtype's bytes, on the host
 std::vector<u8> emit_bytes(const DecompressOut& t, cudaStream_t s);
+// the same into caller memory of emit_size(t) bytes
+u64 emit_size(const DecompressOut& t);
+void emit_bytes(const DecompressOut& t, u8* host, cudaStream_t s);
 
 }  // namespace tcb

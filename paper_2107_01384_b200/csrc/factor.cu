@@ -351,7 +351,7 @@ std::vector<double> factor_residuals(const u64* mag, const u8* neg, int k, u64 n
 namespace tcb {
 
 void factor_expand(const u64* mag, const u8* neg, int k, u64 n, u64 r, const std::vector<u64>& live,
-                   const double* scales_dev, double* U, cudaStream_t s) {
+                   const double* scales_dev, double* U, cudaStream_t s, int* err_dev) {
     ProfScope prof_scope(kFactor, s);
     TCB_CUDA(cudaMemsetAsync(U, 0, n * r * sizeof(double), s));
     const u64 rl = live.size();
@@ -363,9 +363,13 @@ void factor_expand(const u64* mag, const u8* neg, int k, u64 n, u64 r, const std
     DevBuf<int> dp(1, s);
     dp.upload(&zero, 1);
     DevBuf<double> Vd(n * rl, s);
-    DevBuf<int> err(1, s);
-    err.zero();
-    refl_from_stream<<<dim3(cdiv(rl, 4), 1), 128, 0, s>>>(mag, neg, k, n, rl, dp.p, scales_dev, Vd.p, err.p);
+    DevBuf<int> err;
+    if (!err_dev) {
+        err = DevBuf<int>(1, s);
+        err.zero();
+    }
+    int* ep = err_dev ? err_dev : err.p;
+    refl_from_stream<<<dim3(cdiv(rl, 4), 1), 128, 0, s>>>(mag, neg, k, n, rl, dp.p, scales_dev, Vd.p, ep);
     const size_t smem = static_cast<size_t>(kExChunk) * n * sizeof(double);
     static bool attr = [] {
         const int mx = kExChunk * 1024 * sizeof(double);
@@ -381,6 +385,7 @@ void factor_expand(const u64* mag, const u8* neg, int k, u64 n, u64 r, const std
     else expand_columns<32><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);
     count_launch(2);
     TCB_LAUNCH();
+    if (err_dev) return;  // the caller checks the shared flag once
     int e = 0;
     err.download(&e, 1);
     stream_sync(s);

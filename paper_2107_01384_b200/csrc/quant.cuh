@@ -32,6 +32,7 @@ std::vector<double> factor_residuals(const u64* mag, const u8* neg, int k, u64 n
 // Decoder: decoded reflector stream (mag, neg, k; column scales) -> U (row-major
 // n x r; dead columns zero) by the Householder expansion (factor_codec.cpp:246-264)
 void factor_expand(const u64* mag, const u8* neg, int k, u64 n, u64 r, const std::vector<u64>& live,
-                   const double* scales_dev, double* U, cudaStream_t s);
+                   const double* scales_dev, double* U, cudaStream_t s,
+                   int* err_dev = nullptr);
 
 }  // namespace tcb
