@@ -398,6 +398,35 @@ def main():
         b.synchronize()
         e2e_ms.append(a.elapsed_time(b))
     barrier()
+    # ---- decompress of the same container: device-resident output, and
+    # end to end (container bytes in from the host, source-dtype bytes out to the host)
+    d_out = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    cont = res.container
+    for _ in range(args.warmup):
+        tcb.decompress_device(cont, d_out.data_ptr(), nbytes)
+        del_h = tcb.decompress(cont)  # warms the pinned result pool too
+        del del_h
+    torch.cuda.synchronize()
+    dec_ms, dec_e2e_ms = [], []
+    for _ in range(args.steps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        tcb.decompress_device(cont, d_out.data_ptr(), nbytes)
+        b.record()
+        b.synchronize()
+        dec_ms.append(a.elapsed_time(b))
+    for _ in range(args.steps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        out_h = tcb.decompress(cont)
+        b.record()
+        b.synchronize()
+        dec_e2e_ms.append(a.elapsed_time(b))
+        del out_h
+    dec_ok = bool(torch.equal(d_out.view(torch.float64).view(x.shape).cpu(),
+                              torch.from_numpy(tcb.decompress(cont).to_array().copy())))
     clk = clocks.stop()
 
     tot = float(sum(step_ms))
@@ -491,6 +520,16 @@ def main():
                     "d2h_bytes_per_step": len(r2.container)},
             "gpu_launches": int(launches),
             "roofline": roof,
+            "decompress": {"metric": "decompress throughput GB/s (output bytes)",
+                           "value": nbytes * len(dec_ms) / (sum(dec_ms) * 1e-3) / 1e9, "unit": "GB/s",
+                           "ms_per_step": sum(dec_ms) / len(dec_ms),
+                           "e2e": {"value": nbytes * len(dec_e2e_ms) / (sum(dec_e2e_ms) * 1e-3) / 1e9,
+                                   "unit": "GB/s", "h2d_bytes_per_step": len(cont), "d2h_bytes_per_step": nbytes,
+                                   "ms_per_step": sum(dec_e2e_ms) / len(dec_e2e_ms)},
+                           "matches_host_path": dec_ok,
+                           "note": "tcb_decompress_device into a device buffer (timed with CUDA events around "
+                                   "the call: container parse, upload, decode, reconstruction, emit); e2e "
+                                   "through tcb_decompress into pinned host memory"},
             "stage_ms": stage_ms,
             "cpu_baseline": cpu,
             "clocks": clk,

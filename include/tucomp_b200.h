@@ -93,6 +93,11 @@ typedef struct tcb_decompress_result {
 /* pipeline::decompress(container_bytes, threads) (pipeline.hpp:66, pipeline.cpp:266-283):
  * decode, reconstruct and emit in the source dtype (container.cpp:98-140). */
 int tcb_decompress(const uint8_t* container, uint64_t len, int threads, tcb_decompress_result* out);
+/* pipeline::decompress with the emitted source-dtype bytes written to device
+ * memory (`device_out`, at least `capacity` bytes; out->bytes is NULL): no
+ * host copy of the tensor.  B200 extension of pipeline.hpp:66. */
+int tcb_decompress_device(const uint8_t* container, uint64_t len, void* device_out, uint64_t capacity,
+                          tcb_decompress_result* out);
 /* pipeline::decompress_tensor<double> (pipeline.hpp:70-71): the reconstructed tensor in
  * fp64, row-major, original axis order; *out is released with tcb_free; shape has room for 8. */
 int tcb_decompress_tensor_f64(const uint8_t* container, uint64_t len, double** out, uint64_t* count,

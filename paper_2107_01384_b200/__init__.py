@@ -323,6 +323,16 @@ def decompress(container: bytes, threads: int = 1) -> DecompressResult:
                             tuple(int(r.shape[i]) for i in range(r.d)), float(r.total_ms))
 
 
+def decompress_device(container: bytes, device_ptr: int, capacity: int):
+    """pipeline::decompress into device memory (B200 extension): the emitted
+    source-dtype bytes land at `device_ptr`; returns (dtype, shape, total_ms)."""
+    buf = np.frombuffer(container, np.uint8) if len(container) else np.zeros(1, np.uint8)
+    r = _CDecompress()
+    _check(lib().tcb_decompress_device(_p(buf), C.c_uint64(len(container)), C.c_void_p(device_ptr),
+                                       C.c_uint64(capacity), C.byref(r)))
+    return Dtype(r.dtype), tuple(int(r.shape[i]) for i in range(r.d)), float(r.total_ms)
+
+
 def decompress_tensor(container: bytes) -> np.ndarray:
     """tucomp::pipeline::decompress_tensor<double> (pipeline.hpp:70-71) on the B200."""
     buf = np.frombuffer(container, np.uint8) if len(container) else np.zeros(1, np.uint8)
@@ -502,7 +512,7 @@ def encode_factor(u, dead, slice_norms, coder=0, simple=False, core_step_log2=0,
                 plane=plane.value)
 
 
-EXPORTED = ("tcb_compress", "tcb_compress_device", "tcb_decompress", "tcb_decompress_tensor_f64", "tcb_read_container_header", "tcb_measure_error",
+EXPORTED = ("tcb_compress", "tcb_compress_device", "tcb_decompress", "tcb_decompress_tensor_f64", "tcb_decompress_device", "tcb_read_container_header", "tcb_measure_error",
             "tcb_default_params", "tcb_free", "tcb_last_error",
             "tcb_kernel_launches", "tcb_sthosvd_f64", "tcb_gram_f64", "tcb_ttm_f64", "tcb_eig_f64",
             "tcb_quantize_f64", "tcb_encode", "tcb_encode_symbols", "tcb_encode_factor_f64")

@@ -14,6 +14,7 @@
 #include "../../include/tucomp_b200.h"
 #include "codec.cuh"
 #include "kernels.cuh"
+#include "decode.cuh"
 #include "decompress.hpp"
 #include "pipeline.hpp"
 #include "quant.cuh"
@@ -477,6 +478,37 @@ int tcb_decompress(const uint8_t* container, uint64_t len, int threads, tcb_deco
         out->bytes = static_cast<uint8_t*>(host_alloc(nb));
         emit_bytes(t, out->bytes, st.s);
         ht.stop();
+        out->nbytes = nb;
+        out->dtype = t.dtype;
+        out->d = static_cast<int>(t.shape.size());
+        for (std::size_t i = 0; i < t.shape.size() && i < 8; ++i) out->shape[i] = t.shape[i];
+        out->total_ms = t.ms;
+        host_trace_dump();
+    });
+}
+
+int tcb_decompress_device(const uint8_t* container, uint64_t len, void* device_out, uint64_t capacity,
+                          tcb_decompress_result* out) {
+    return guard([&] {
+        Stream st;
+        const auto t = decompress_device(container, len, st.s);
+        const u64 nb = emit_size(t);
+        if (nb > capacity)
+            throw Error("decompress: output buffer holds " + std::to_string(capacity) + " bytes, needs " +
+                        std::to_string(nb));
+        const u64 total = [&] {
+            u64 v = 1;
+            for (auto x : t.shape) v *= x;
+            return v;
+        }();
+        if (total) {
+            if (t.dtype == 9)
+                TCB_CUDA(cudaMemcpyAsync(device_out, t.x.p, nb, cudaMemcpyDeviceToDevice, st.s));
+            else
+                emit_dtype(t.x.p, total, t.dtype, device_out, st.s);
+        }
+        stream_sync(st.s);
+        out->bytes = nullptr;
         out->nbytes = nb;
         out->dtype = t.dtype;
         out->d = static_cast<int>(t.shape.size());

@@ -112,3 +112,21 @@ def test_decompress_header_validation(gpu_pkg, off, val, msg):
     assert c[7] == 3
     with pytest.raises(gpu_pkg.TucompError, match=msg):
         gpu_pkg.decompress(_patch(c, off, val))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.uint16])
+def test_decompress_into_device_memory(gpu_pkg, dtype):
+    """tcb_decompress_device writes the same source-dtype bytes as
+    tcb_decompress, into a caller device buffer; a short buffer is an error."""
+    torch = pytest.importorskip("torch")
+    shape = (40, 32, 24)
+    base = synth.small("blobs", shape, seed=9)
+    x = (np.round((base - base.min()) / np.ptp(base) * 4000).astype(dtype) if dtype != np.float64 else base)
+    c = gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(target_re=1e-3)).container
+    host = gpu_pkg.decompress(c)
+    out = torch.empty(x.nbytes, dtype=torch.uint8, device="cuda")
+    dt, sh, _ = gpu_pkg.decompress_device(c, out.data_ptr(), x.nbytes)
+    assert dt == host.dtype and sh == shape
+    assert out.cpu().numpy().tobytes() == host.bytes
+    with pytest.raises(gpu_pkg.TucompError, match="output buffer holds"):
+        gpu_pkg.decompress_device(c, out.data_ptr(), x.nbytes - 1)
