@@ -117,11 +117,43 @@ __global__ void sum_kernel(SumKind kind, const u64* __restrict__ m, const u64* _
     }
 }
 
-__global__ void sum_serial_kernel(SumKind kind, const u64* __restrict__ m, const u64* __restrict__ dec, u64 n,
-                                  int plane, double* out) {
+// Serial replay of a backward sum (the exact-mode fallback): the CTA computes
+// the terms of the next chunk into shared memory (coalesced loads) while
+// thread 0 runs the dependent __dadd_rn chain over the current one from
+// registers, 8 at a time -- about one add latency per element instead of one
+// memory latency.
+constexpr int kSerThreads = 256, kSerChunk = 2048;
+__global__ void __launch_bounds__(kSerThreads) sum_serial_kernel(SumKind kind, const u64* __restrict__ m,
+                                                                const u64* __restrict__ dec, u64 n, int plane,
+                                                                double* out) {
+    __shared__ double buf[2][kSerChunk];
+    const u64 nchunk = (n + kSerChunk - 1) / kSerChunk;
+    auto fill = [&](u64 c, int b) {  // chunk c = indices [n - (c+1) C, n - c C), stored in descending order
+        const u64 hi = n - c * kSerChunk;
+        for (int q = threadIdx.x; q < kSerChunk; q += blockDim.x)
+            buf[b][q] = static_cast<u64>(q) < hi ? sum_term(kind, m, dec, hi - 1 - q, plane) : 0.0;
+    };
     double s = 0.0;
-    for (u64 i = n; i-- > 0;) s = __dadd_rn(s, sum_term(kind, m, dec, i, plane));
-    *out = s;
+    if (nchunk) fill(0, 0);
+    __syncthreads();
+    for (u64 c = 0; c < nchunk; ++c) {
+        const int b = static_cast<int>(c & 1);
+        if (c + 1 < nchunk) fill(c + 1, b ^ 1);
+        if (threadIdx.x == 0) {
+            const u64 hi = n - c * kSerChunk;
+            const int cnt = static_cast<int>(hi < kSerChunk ? hi : kSerChunk);
+            for (int q0 = 0; q0 < cnt; q0 += 8) {
+                double t[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) t[u] = buf[b][q0 + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (q0 + u < cnt) s = __dadd_rn(s, t[u]);
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = s;
 }
 
 // ---------------------------------------------------------------- per-plane stats
@@ -224,27 +256,75 @@ __global__ void stats_combine(const Partial* __restrict__ part, u64 nb, u64 cpb,
 }
 
 // serial replay of build_block's sums for every block of one plane (one thread per block)
-__global__ void stats_serial_kernel(const u64* __restrict__ m, u64 n, u64 block, u64 nb, int p,
-                                    PlaneBlockRec* __restrict__ out) {
-    const u64 b = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+constexpr int kStatChunk = 1024;
+// Exact per-block plane statistics (serial sums in position order): one CTA per
+// block; the CTA classifies a chunk and stages the lead / trail gains in shared
+// memory (zero where a position does not contribute: x + 0 = x exactly) while
+// thread 0 replays both chains over the previous chunk; counts are parallel.
+__global__ void __launch_bounds__(kSerThreads) stats_serial_kernel(const u64* __restrict__ m, u64 n, u64 block,
+                                                                  u64 nb, int p, PlaneBlockRec* __restrict__ out) {
+    __shared__ double lg[2][kStatChunk], tg[2][kStatChunk];
+    __shared__ unsigned long long cnt_s[3];
+    const u64 b = blockIdx.x;
     if (b >= nb) return;
     const u64 lo = b * block, hi = min(n, lo + block);
+    const u64 len = hi - lo, nchunk = (len + kStatChunk - 1) / kStatChunk;
+    if (threadIdx.x < 3) cnt_s[threadIdx.x] = 0;
+    u64 my_nl = 0, my_no = 0, my_nt = 0;
+    auto fill = [&](u64 c, int bb) {
+        for (int q = threadIdx.x; q < kStatChunk; q += blockDim.x) {
+            const u64 i = lo + c * kStatChunk + q;
+            double l = 0.0, t = 0.0;
+            if (i < hi) {
+                const u64 v = m[i];
+                const int tb = top_bit(v);
+                if (tb > p) {
+                    t = trail_gain(v, p);
+                    ++my_nt;
+                } else {
+                    ++my_nl;
+                    if (tb == p) {
+                        l = lead_gain(v, p);
+                        ++my_no;
+                    }
+                }
+            }
+            lg[bb][q] = l;
+            tg[bb][q] = t;
+        }
+    };
     double l = 0.0, t = 0.0;
-    u64 nl = 0, no = 0, nt = 0;
-    for (u64 i = lo; i < hi; ++i) {
-        const u64 v = m[i];
-        const int tb = top_bit(v);
-        if (tb > p) {
-            t = __dadd_rn(t, trail_gain(v, p));
-            ++nt;
-        } else {
-            ++nl;
-            if (tb == p) {
-                l = __dadd_rn(l, lead_gain(v, p));
-                ++no;
+    if (nchunk) fill(0, 0);
+    __syncthreads();
+    for (u64 c = 0; c < nchunk; ++c) {
+        const int bb = static_cast<int>(c & 1);
+        if (c + 1 < nchunk) fill(c + 1, bb ^ 1);
+        if (threadIdx.x == 0) {
+            const u64 rem = len - c * kStatChunk;
+            const int cnt = static_cast<int>(rem < kStatChunk ? rem : kStatChunk);
+            for (int q0 = 0; q0 < cnt; q0 += 8) {
+                double a[8], e[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    a[u] = lg[bb][q0 + u];
+                    e[u] = tg[bb][q0 + u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (q0 + u < cnt) {
+                        l = __dadd_rn(l, a[u]);
+                        t = __dadd_rn(t, e[u]);
+                    }
             }
         }
+        __syncthreads();
     }
+    atomicAdd(&cnt_s[0], static_cast<unsigned long long>(my_nl));
+    atomicAdd(&cnt_s[1], static_cast<unsigned long long>(my_no));
+    atomicAdd(&cnt_s[2], static_cast<unsigned long long>(my_nt));
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const u64 nl = cnt_s[0], no = cnt_s[1], nt = cnt_s[2];
     PlaneBlockRec r{};
     r.lead = SumRec{l, 0.0, 0.0, no};
     r.trail = SumRec{t, 0.0, 0.0, nt};
@@ -1129,7 +1209,7 @@ SumRec device_sum(SumKind kind, const u64* m, const u64* dec, u64 n, int plane, 
 double device_sum_serial(SumKind kind, const u64* m, const u64* dec, u64 n, int plane, cudaStream_t s) {
     ProfScope prof_scope(kSum, s);
     DevBuf<double> out(1, s);
-    sum_serial_kernel<<<1, 1, 0, s>>>(kind, m, dec, n, plane, out.p);
+    sum_serial_kernel<<<1, kSerThreads, 0, s>>>(kind, m, dec, n, plane, out.p);
     count_launch();
     TCB_LAUNCH();
     return out.to_host()[0];
@@ -1155,7 +1235,7 @@ void plane_stats_serial(const u64* m, u64 n, u64 block, int p, PlaneBlockRec* ou
     ProfScope prof_scope(kStats, s);
     const u64 nb = (n + block - 1) / block;
     DevBuf<PlaneBlockRec> out(nb, s);
-    stats_serial_kernel<<<cdiv(nb, 64), 64, 0, s>>>(m, n, block, nb, p, out.p);
+    stats_serial_kernel<<<static_cast<unsigned>(nb), kSerThreads, 0, s>>>(m, n, block, nb, p, out.p);
     count_launch();
     TCB_LAUNCH();
     out.download(out_host, nb);
