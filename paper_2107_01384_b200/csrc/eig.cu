@@ -687,6 +687,83 @@ __global__ void cluster_mgs_kernel(const int* __restrict__ clusters, int n, doub
     }
 }
 
+// ---------------------------------------------------------------- large clusters
+// A cluster of k > 32 inverse-iteration vectors (rows j0..j1 of Z) is
+// orthonormalised by CholQR2 instead of MGS (MGS costs 2k^2 dependent dot
+// products, ~150 ms for the 468-vector noise-floor cluster of a 500-row mode):
+// C = Z_c Z_c^T (the SYRK kernel), an elimination-form Cholesky of C with the
+// inverse accumulated (E = L^-1, C = L D L^T; one launch per pivot, the
+// trailing update spread over the GPU), Z_c <- D^-1/2 E Z_c (the TTM kernel);
+// twice.  Like MGS it keeps the nested spans of the vectors in order; a
+// non-positive pivot falls back to MGS for that cluster.
+__global__ void bigchol_init_kernel(double* __restrict__ E, int k) {
+    const u64 kk = static_cast<u64>(k) * k;
+    for (u64 e = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; e < kk; e += static_cast<u64>(gridDim.x) * blockDim.x)
+        E[e] = (e / k) == (e % k) ? 1.0 : 0.0;
+}
+
+__global__ void bigchol_step_kernel(double* __restrict__ C, double* __restrict__ E, double* __restrict__ rinv, int k,
+                                    int j, int* __restrict__ bad) {
+    const double djj = C[static_cast<u64>(j) * k + j];
+    if (!(djj >= DBL_MIN)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) *bad = 1;
+        return;
+    }
+    const double ri = rsqrt(djj), inv = ri * ri;
+    if (blockIdx.x == 0 && threadIdx.x == 0) rinv[j] = ri;
+    const u64 m = static_cast<u64>(k - j - 1);                 // trailing rows
+    const u64 nc = m, ne = static_cast<u64>(j + 1);             // C columns > j, E columns <= j
+    const u64 total = m * (nc + ne);
+    const double* rowj = C + static_cast<u64>(j) * k;
+    const double* erow = E + static_cast<u64>(j) * k;
+    for (u64 e = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u64 i = j + 1 + e / (nc + ne), c = e % (nc + ne);
+        const double f = rowj[i] * inv;
+        if (c < nc) {
+            const u64 col = j + 1 + c;
+            C[i * k + col] = fma(-f, rowj[col], C[i * k + col]);
+        } else {
+            const u64 col = c - nc;
+            E[i * k + col] = fma(-f, erow[col], E[i * k + col]);
+        }
+    }
+}
+
+// W[m][c] = E[c][m] rinv[c]  (so that Z_c^T W = (D^-1/2 E Z_c)^T)
+__global__ void bigchol_w_kernel(const double* __restrict__ E, const double* __restrict__ rinv, int k,
+                                 double* __restrict__ W) {
+    const u64 kk = static_cast<u64>(k) * k;
+    for (u64 e = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; e < kk; e += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u64 m = e / k, c = e % k;
+        W[e] = c >= m ? E[c * k + m] * rinv[c] : 0.0;
+    }
+}
+
+// true on success; Zc (k rows of length n) orthonormalised in place
+bool cluster_cholqr2(double* Zc, int n, int k, cudaStream_t s) {
+    DevBuf<double> C(static_cast<u64>(k) * k, s), E(static_cast<u64>(k) * k, s), W(static_cast<u64>(k) * k, s);
+    DevBuf<double> rinv(k, s), out(static_cast<u64>(n) * k, s);
+    DevBuf<int> bad(1, s);
+    bad.zero();
+    for (int pass = 0; pass < 2; ++pass) {
+        gram_f64(Zc, static_cast<u64>(k), static_cast<u64>(n), C.p, s);
+        bigchol_init_kernel<<<grid_for(static_cast<u64>(k) * k, 256, 4, 4), 256, 0, s>>>(E.p, k);
+        for (int j = 0; j < k; ++j) {
+            const u64 work = static_cast<u64>(k - j - 1) * static_cast<u64>(k);
+            bigchol_step_kernel<<<grid_for(std::max<u64>(work, 1), 256, 2, 2), 256, 0, s>>>(C.p, E.p, rinv.p, k, j,
+                                                                                        bad.p);
+        }
+        bigchol_w_kernel<<<grid_for(static_cast<u64>(k) * k, 256, 4, 4), 256, 0, s>>>(E.p, rinv.p, k, W.p);
+        ttm_f64(Zc, static_cast<u64>(k), static_cast<u64>(n), W.p, static_cast<u64>(k), out.p, s);  // n x k
+        permute_axes(out.p, Zc, std::vector<u64>{static_cast<u64>(n), static_cast<u64>(k)},
+                     std::vector<u64>{1, 0}, s);
+        count_launch(static_cast<u64>(k) + 2);
+    }
+    TCB_LAUNCH();
+    return bad.to_host()[0] == 0;
+}
+
 // ---------------------------------------------------------------- back-transform
 // U = Q Z with Q = H_0 ... H_{n-3} (the Gram's eigenvectors from those of the
 // tridiagonal, sthosvd.cpp:80-90).  Reflector chunks of KC (32 / 16 / 8 for
@@ -1107,10 +1184,31 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
     invit_kernel<<<static_cast<unsigned>(r), 32, smem, s>>>(w.d.p, w.e.p, n, dsh.p, DBL_EPSILON * tnorm, Z.p);
     count_launch();
     if (!clusters.empty()) {
-        DevBuf<int> dcl(clusters.size(), s);
-        dcl.upload(clusters.data(), clusters.size());
-        cluster_mgs_kernel<<<static_cast<unsigned>(clusters.size() / 2), 256, 0, s>>>(dcl.p, n, Z.p);
-        count_launch();
+        // big clusters by CholQR2 (MGS where it breaks down), the rest by MGS
+        std::vector<int> small;
+        for (std::size_t c = 0; c < clusters.size(); c += 2) {
+            const int j0 = clusters[c], j1 = clusters[c + 1], k = j1 - j0;
+            bool done = false;
+            if (k > 32) {
+                DevBuf<double> keep(static_cast<u64>(k) * n, s);
+                TCB_CUDA(cudaMemcpyAsync(keep.p, Z.p + static_cast<u64>(j0) * n, keep.n * sizeof(double),
+                                         cudaMemcpyDeviceToDevice, s));
+                done = cluster_cholqr2(Z.p + static_cast<u64>(j0) * n, n, k, s);
+                if (!done)
+                    TCB_CUDA(cudaMemcpyAsync(Z.p + static_cast<u64>(j0) * n, keep.p, keep.n * sizeof(double),
+                                             cudaMemcpyDeviceToDevice, s));
+            }
+            if (!done) {
+                small.push_back(j0);
+                small.push_back(j1);
+            }
+        }
+        if (!small.empty()) {
+            DevBuf<int> dcl(small.size(), s);
+            dcl.upload(small.data(), small.size());
+            cluster_mgs_kernel<<<static_cast<unsigned>(small.size() / 2), 256, 0, s>>>(dcl.p, n, Z.p);
+            count_launch();
+        }
     }
     // T matrices come from wy_tmat on the side stream (launched by eig_values)
     static bool attr = [] {

@@ -411,3 +411,24 @@ def test_chunked_upload_gram_is_bitwise(gpu_pkg):
     ref = oracle.compress(x, target_re=1e-4)
     assert gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), prm).container == a  # pageable: single copy
     assert abs(len(a) - len(ref.container)) <= 0.01 * len(ref.container)
+
+
+def test_eig_large_cluster_cholqr(gpu_pkg):
+    """A mode whose kept eigenvalues include a big noise-floor cluster (c3's
+    500-row modes): the cluster is orthonormalised by CholQR2 (MGS only on a
+    breakdown); the vectors stay orthonormal to roundoff, the strong directions
+    match LAPACK's subspace, and every kept pair has a small residual."""
+    rng = np.random.default_rng(5)
+    n, k, r = 300, 1200, 280
+    b = rng.standard_normal((n, k)) * np.where(np.arange(k) < 24, 1.0, 1e-4)
+    g = b @ b.T
+    ev, u = gpu_pkg.eig(g, r)
+    lam, vec = np.linalg.eigh(g)
+    lam, vec = lam[::-1], vec[:, ::-1]
+    assert np.max(np.abs(ev - lam)) <= 1e-12 * lam[0] * np.sqrt(n)
+    assert np.max(np.abs(u.T @ u - np.eye(r))) < 1e-12
+    # strong directions: principal-angle sine against LAPACK
+    s = np.linalg.svd(vec[:, :24].T @ u[:, :24], compute_uv=False)
+    assert np.sqrt(max(0.0, 1 - s.min() ** 2)) < 1e-6
+    res = np.linalg.norm(g @ u - u * ev[:r], axis=0)
+    assert res.max() <= 1e-9 * lam[0]
