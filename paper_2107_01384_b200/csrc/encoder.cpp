@@ -35,11 +35,13 @@ inline Iv sub(Iv a, Iv b) { return {a.lo - b.hi, a.hi - b.lo}; }
 inline bool le(Iv a, Iv b) {  // a <= b
     if (a.hi <= b.lo) return true;
     if (a.lo > b.hi) return false;
+    HostTrace ht("plan: ambiguous le");
     throw Ambiguous{};
 }
 inline bool ge(Iv a, Iv b) {  // a >= b
     if (a.lo >= b.hi) return true;
     if (a.hi < b.lo) return false;
+    HostTrace ht("plan: ambiguous ge");
     throw Ambiguous{};
 }
 
@@ -101,7 +103,10 @@ struct Planner {
         u64 out[4];
         HostTrace ht("plan: crossing_scan");
         crossing_scan(m, n, block, b, p, cat, c, nd, 2, out, s);
-        if (out[0] != out[2] || out[1] != out[3]) throw Ambiguous{};
+        if (out[0] != out[2] || out[1] != out[3]) {
+            HostTrace ht("plan: ambiguous crossing");
+            throw Ambiguous{};
+        }
         if (second) *second = out[1];
         return out[0];
     }
@@ -224,7 +229,10 @@ struct Planner {
             bool due;
             if (c * ref.lo > 0.1 * tracked.hi) due = true;
             else if (c * ref.hi <= 0.1 * tracked.lo) due = false;
-            else throw Ambiguous{};
+            else {
+                HostTrace ht("plan: ambiguous recalibration");
+                throw Ambiguous{};
+            }
             if (due) {
                 HostTrace ht("plan: recalibration sum");
                 tracked = exact ? pt(device_sum_serial(SumKind::recal_backward, m, nullptr, n, p, s))

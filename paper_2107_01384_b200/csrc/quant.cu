@@ -2,6 +2,8 @@
 // Householder sign fold (pipeline.cpp:161-175).  Integer-exact kernels.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "quant.cuh"
 
@@ -58,6 +60,62 @@ __global__ void slice_norm_kernel(const u64* __restrict__ mag, const u64* __rest
             if (j0 + u < cnt) s = __dadd_rn(s, __dmul_rn(v[u], v[u]));
     }
     out[t] = __dsqrt_rn(__dmul_rn(s, down));
+}
+
+// The same serial slice sums, one CTA per slice, for large slices: the CTA
+// stages the next chunk of squares in shared memory (the divisions and the
+// strided loads spread over the CTA) while thread 0 runs the dependent add
+// chain over the current chunk.
+constexpr int kSnThreads = 256, kSnChunk = 2048;
+__global__ void __launch_bounds__(kSnThreads) slice_norm_cta_kernel(const u64* __restrict__ mag,
+                                                                    const u64* __restrict__ shape, int d,
+                                                                    double down, double* __restrict__ out) {
+    __shared__ double buf[2][kSnChunk];
+    const u64 t = blockIdx.x;
+    int a = 0;
+    u64 base = 0;
+    while (t >= base + shape[a]) {
+        base += shape[a];
+        ++a;
+    }
+    const u64 idx = t - base;
+    u64 inner = 1, outer = 1;
+    for (int i = a + 1; i < d; ++i) inner *= shape[i];
+    for (int i = 0; i < a; ++i) outer *= shape[i];
+    const u64 ext = shape[a], cnt = outer * inner, nchunk = (cnt + kSnChunk - 1) / kSnChunk;
+    auto fill = [&](u64 c, int b) {
+        for (int q = threadIdx.x; q < kSnChunk; q += blockDim.x) {
+            const u64 j = c * kSnChunk + q;
+            double sq = 0.0;
+            if (j < cnt) {
+                const u64 o = j / inner, r = j - o * inner;
+                const double v = __ull2double_rn(mag[(o * ext + idx) * inner + r]);
+                sq = __dmul_rn(v, v);
+            }
+            buf[b][q] = sq;
+        }
+    };
+    double s = 0.0;
+    if (nchunk) fill(0, 0);
+    __syncthreads();
+    for (u64 c = 0; c < nchunk; ++c) {
+        const int b = static_cast<int>(c & 1);
+        if (c + 1 < nchunk) fill(c + 1, b ^ 1);
+        if (threadIdx.x == 0) {
+            const u64 rem = cnt - c * kSnChunk;
+            const int m = static_cast<int>(rem < kSnChunk ? rem : kSnChunk);
+            for (int q0 = 0; q0 < m; q0 += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = buf[b][q0 + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (q0 + u < m) s = __dadd_rn(s, v[u]);
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[t] = __dsqrt_rn(__dmul_rn(s, down));
 }
 
 __global__ void dead_kernel(const u64* __restrict__ dec, u64 n, const u64* __restrict__ meta /* shape, stride, off */,
@@ -216,6 +274,13 @@ void slice_norms(const u64* mag, const std::vector<u64>& shape, double down, dou
     if (!order) {
         DevBuf<u64> sh(shape.size(), s);
         sh.upload(shape.data(), shape.size());
+        if (n / std::max<u64>(1, *std::min_element(shape.begin(), shape.end())) >= 16384) {  // large slices
+            slice_norm_cta_kernel<<<static_cast<unsigned>(total), kSnThreads, 0, s>>>(
+                mag, sh.p, static_cast<int>(shape.size()), down, out);
+            count_launch();
+            TCB_LAUNCH();
+            return;
+        }
         slice_norm_kernel<<<cdiv(total, 64), 64, 0, s>>>(mag, sh.p, static_cast<int>(shape.size()), total, down,
                                                          out);
         count_launch();
