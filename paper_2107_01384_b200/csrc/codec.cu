@@ -123,10 +123,8 @@ __global__ void sum_kernel(SumKind kind, const u64* __restrict__ m, const u64* _
 // registers, 8 at a time -- about one add latency per element instead of one
 // memory latency.
 constexpr int kSerThreads = 256, kSerChunk = 2048;
-__global__ void __launch_bounds__(kSerThreads) sum_serial_kernel(SumKind kind, const u64* __restrict__ m,
-                                                                const u64* __restrict__ dec, u64 n, int plane,
-                                                                double* out) {
-    __shared__ double buf[2][kSerChunk];
+__device__ double serial_sum_cta(SumKind kind, const u64* __restrict__ m, const u64* __restrict__ dec, u64 n,
+                                 int plane, double (*buf)[kSerChunk]) {
     const u64 nchunk = (n + kSerChunk - 1) / kSerChunk;
     auto fill = [&](u64 c, int b) {  // chunk c = indices [n - (c+1) C, n - c C), stored in descending order
         const u64 hi = n - c * kSerChunk;
@@ -153,7 +151,26 @@ __global__ void __launch_bounds__(kSerThreads) sum_serial_kernel(SumKind kind, c
         }
         __syncthreads();
     }
+    return s;
+}
+
+__global__ void __launch_bounds__(kSerThreads) sum_serial_kernel(SumKind kind, const u64* __restrict__ m,
+                                                                const u64* __restrict__ dec, u64 n, int plane,
+                                                                double* out) {
+    __shared__ double buf[2][kSerChunk];
+    const double s = serial_sum_cta(kind, m, dec, n, plane, buf);
     if (threadIdx.x == 0) *out = s;
+}
+
+// several independent serial sums at once (one CTA each): the exact planner's
+// initial sum and every plane's recalibration sum, in the time of one
+__global__ void __launch_bounds__(kSerThreads) sum_serial_multi_kernel(const int* __restrict__ kinds,
+                                                                      const int* __restrict__ planes,
+                                                                      const u64* __restrict__ m, u64 n,
+                                                                      double* __restrict__ out) {
+    __shared__ double buf[2][kSerChunk];
+    const double s = serial_sum_cta(static_cast<SumKind>(kinds[blockIdx.x]), m, nullptr, n, planes[blockIdx.x], buf);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
 // ---------------------------------------------------------------- per-plane stats
@@ -262,7 +279,8 @@ constexpr int kStatChunk = 1024;
 // memory (zero where a position does not contribute: x + 0 = x exactly) while
 // thread 0 replays both chains over the previous chunk; counts are parallel.
 __global__ void __launch_bounds__(kSerThreads) stats_serial_kernel(const u64* __restrict__ m, u64 n, u64 block,
-                                                                  u64 nb, int p, PlaneBlockRec* __restrict__ out) {
+                                                                  u64 nb, int p_hi, PlaneBlockRec* __restrict__ out) {
+    const int p = p_hi - static_cast<int>(blockIdx.y);
     __shared__ double lg[2][kStatChunk], tg[2][kStatChunk];
     __shared__ unsigned long long cnt_s[3];
     const u64 b = blockIdx.x;
@@ -331,7 +349,7 @@ __global__ void __launch_bounds__(kSerThreads) stats_serial_kernel(const u64* __
     r.nlead = nl;
     r.nones = no;
     r.ntrail = nt;
-    out[b] = r;
+    out[static_cast<u64>(blockIdx.y) * nb + b] = r;
 }
 
 // One warp per (cum, need) pair: lanes classify 32 positions at a time and
@@ -1235,10 +1253,44 @@ void plane_stats_serial(const u64* m, u64 n, u64 block, int p, PlaneBlockRec* ou
     ProfScope prof_scope(kStats, s);
     const u64 nb = (n + block - 1) / block;
     DevBuf<PlaneBlockRec> out(nb, s);
-    stats_serial_kernel<<<static_cast<unsigned>(nb), kSerThreads, 0, s>>>(m, n, block, nb, p, out.p);
+    stats_serial_kernel<<<dim3(static_cast<unsigned>(nb), 1), kSerThreads, 0, s>>>(m, n, block, nb, p, out.p);
     count_launch();
     TCB_LAUNCH();
     out.download(out_host, nb);
+    stream_sync(s);
+}
+
+std::vector<double> device_sums_serial(const std::vector<std::pair<SumKind, int>>& list, const u64* m, u64 n,
+                                       cudaStream_t s) {
+    ProfScope prof_scope(kSum, s);
+    const int k = static_cast<int>(list.size());
+    if (k == 0) return {};
+    std::vector<int> kinds(k), planes(k);
+    for (int i = 0; i < k; ++i) {
+        kinds[i] = static_cast<int>(list[i].first);
+        planes[i] = list[i].second;
+    }
+    DevBuf<int> dk(k, s), dp(k, s);
+    dk.upload(kinds.data(), k);
+    dp.upload(planes.data(), k);
+    DevBuf<double> out(k, s);
+    sum_serial_multi_kernel<<<static_cast<unsigned>(k), kSerThreads, 0, s>>>(dk.p, dp.p, m, n, out.p);
+    count_launch();
+    TCB_LAUNCH();
+    return out.to_host();
+}
+
+void plane_stats_serial_range(const u64* m, u64 n, u64 block, int p_hi, int p_lo, PlaneBlockRec* out_host,
+                              cudaStream_t s) {
+    ProfScope prof_scope(kStats, s);
+    const u64 nb = (n + block - 1) / block;
+    const int np = p_hi - p_lo + 1;
+    DevBuf<PlaneBlockRec> out(nb * np, s);
+    stats_serial_kernel<<<dim3(static_cast<unsigned>(nb), static_cast<unsigned>(np)), kSerThreads, 0, s>>>(
+        m, n, block, nb, p_hi, out.p);
+    count_launch();
+    TCB_LAUNCH();
+    out.download(out_host, nb * np);
     stream_sync(s);
 }
 

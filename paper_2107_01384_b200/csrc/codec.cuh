@@ -2,6 +2,8 @@
 #pragma once
 
 #include <memory>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -32,6 +34,12 @@ double device_sum_serial(SumKind kind, const u64* m, const u64* dec, u64 n, int 
 void plane_stats(const u64* m, u64 n, u64 block, int p_hi, int p_lo, PlaneBlockRec* out_host, cudaStream_t s);
 // exact serial replay of the per-block sums for one plane
 void plane_stats_serial(const u64* m, u64 n, u64 block, int p, PlaneBlockRec* out_host, cudaStream_t s);
+// the exact statistics of planes p_hi..p_lo at once (plane-major: (p_hi - p) * nb + block)
+void plane_stats_serial_range(const u64* m, u64 n, u64 block, int p_hi, int p_lo, PlaneBlockRec* out_host,
+                              cudaStream_t s);
+// several serial sums (kind, plane) over m at once, each in its own CTA
+std::vector<double> device_sums_serial(const std::vector<std::pair<SumKind, int>>& list, const u64* m, u64 n,
+                                       cudaStream_t s);
 
 // Crossing scan of place_stops (core_codec.cpp:268-341): count positions of the
 // given category in block b until cum >= need; returns counts for (cum, need).

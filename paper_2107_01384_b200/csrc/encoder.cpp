@@ -73,12 +73,19 @@ struct Planner {
     std::vector<PlaneBlockRec> batch;
     int batch_hi = -1, batch_lo = 64;
 
+    // exact mode: every plane's serial statistics in one launch, and the initial
+    // and every plane's recalibration sum in another (independent serial chains
+    // side by side), computed on first use
+    std::vector<PlaneBlockRec> ex_stats;
+    std::vector<double> ex_sums;  // [0] initial, [1 + p] recalibration at plane p
     const PlaneBlockRec* stats(int p, int floor_p) {
         if (exact) {
-            batch.resize(nb);
-            plane_stats_serial(m, n, block, p, batch.data(), s);
-            batch_hi = batch_lo = p;
-            return batch.data();
+            if (ex_stats.empty()) {
+                HostTrace ht("plan: exact stats (all planes)");
+                ex_stats.resize(nb * 64);
+                plane_stats_serial_range(m, n, block, 63, 0, ex_stats.data(), s);
+            }
+            return ex_stats.data() + static_cast<u64>(63 - p) * nb;
         }
         if (p > batch_hi || p < batch_lo) {
             // planes per batch: every remaining plane when the core is small (each plane
@@ -186,7 +193,16 @@ struct Planner {
             return finish(fp);
         }
         HostTrace ht0("plan: initial sum");
-        Iv tracked = exact ? pt(device_sum_serial(SumKind::sq_backward, m, nullptr, n, 0, s))
+        auto exact_sum = [&](int which) {  // which: -1 initial, else the recalibration at that plane
+            if (ex_sums.empty()) {
+                HostTrace ht("plan: exact sums (initial + recalibrations)");
+                std::vector<std::pair<SumKind, int>> list{{SumKind::sq_backward, 0}};
+                for (int q = 0; q < 64; ++q) list.push_back({SumKind::recal_backward, q});
+                ex_sums = device_sums_serial(list, m, n, s);
+            }
+            return ex_sums[which < 0 ? 0 : 1 + which];
+        };
+        Iv tracked = exact ? pt(exact_sum(-1))
                            : from_sum(device_sum(SumKind::sq_backward, m, nullptr, n, 0, s), false);
         Iv ref = tracked;
         u64 terms = 0;
@@ -235,7 +251,7 @@ struct Planner {
             }
             if (due) {
                 HostTrace ht("plan: recalibration sum");
-                tracked = exact ? pt(device_sum_serial(SumKind::recal_backward, m, nullptr, n, p, s))
+                tracked = exact ? pt(exact_sum(p))
                                 : from_sum(device_sum(SumKind::recal_backward, m, nullptr, n, p, s), false);
                 ref = tracked;
                 terms = 0;
