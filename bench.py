@@ -481,6 +481,10 @@ def main():
         else:
             eig_flop += 4.0 / 3.0 * n_eig ** 3 + 2.0 * n_eig * n_eig * res.ranks[mode]
         cur = cur[1:] + [res.ranks[mode]]
+    roof["note"] = ("ncu launch-list shares for this command (profiles/launches_*_summary.txt): the encoder's "
+                    "ac_kernel, syrk_kernel and tk_cluster are each ~13-14 %; of the 5 ac_kernel launches per "
+                    "compress only the core finalisation's is on the critical path (the probe and the factor "
+                    "streams run on side streams), so the Gram is the dominant critical-path kernel")
     roof["eig"] = {"kernel": "tk_cluster (one 8-CTA cluster launch per mode)", "flop": eig_flop,
                    "ms": stage_ms["eig"], "tflops": eig_flop / max(stage_ms["eig"], 1e-9) / 1e9,
                    "note": "latency-bound: per mode 3 block subspace iterations, each 2-3 CholQR passes "
