@@ -80,6 +80,20 @@ int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_
 int tcb_compress_device(const void* device_bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d,
                         const tcb_params* params, tcb_result* out);
 
+/* Sharded compress over NCCL (SURVEY 8(e), B200 extension): every rank holds an
+ * equal slab (local_extent) of the last processed mode, in rank order, of a
+ * tensor with the global `shape`; the partial Grams are summed with NCCL, the
+ * projections stay local, the small tensor is gathered for the last step and
+ * rank 0 writes the container (the other ranks return an empty one).
+ * tcb_nccl_unique_id on rank 0, the 128 bytes shared by the caller (e.g.
+ * torch.distributed), then tcb_nccl_comm_init on every rank. */
+int tcb_nccl_unique_id(uint8_t out[128]);
+int tcb_nccl_comm_init(const uint8_t id[128], int world, int rank, void** comm);
+int tcb_nccl_comm_destroy(void* comm);
+int tcb_compress_sharded_device(void* comm, int world, int rank, const void* device_bytes, uint64_t nbytes,
+                                int dtype, const uint64_t* shape, int d, uint64_t local_extent,
+                                const tcb_params* params, tcb_result* out);
+
 /* pipeline::DecompressResult (pipeline.hpp:59-64) */
 typedef struct tcb_decompress_result {
     uint8_t* bytes;              /* source-dtype bytes, owned by the library: release with tcb_free */

@@ -16,6 +16,7 @@
 #include "kernels.cuh"
 #include "decode.cuh"
 #include "decompress.hpp"
+#include "nccl_shim.hpp"
 #include "pipeline.hpp"
 #include "quant.cuh"
 
@@ -432,6 +433,40 @@ int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_
         if (!upload_overlapping_gram(bytes + skip, nbytes - skip, dtype, sh, prm, dev.p, g0, ws, st.s))
             dev.upload(bytes + skip, nbytes - skip);
         const Result r = compress_device(dev.p, nbytes - skip, dtype, sh, prm, st.s, g0.p);
+        host_trace_dump();
+        fill(r, d, out);
+    });
+}
+
+int tcb_nccl_unique_id(uint8_t out[128]) {
+    return guard([&] { nccl_unique_id(out); });
+}
+
+int tcb_nccl_comm_init(const uint8_t id[128], int world, int rank, void** comm) {
+    return guard([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+            throw Error("tucomp_b200: no CUDA device (the B200 path has no CPU fallback)");
+        *comm = nccl_comm_init(id, world, rank);
+    });
+}
+
+int tcb_nccl_comm_destroy(void* comm) {
+    return guard([&] { nccl_comm_destroy(comm); });
+}
+
+int tcb_compress_sharded_device(void* comm, int world, int rank, const void* device_bytes, uint64_t nbytes,
+                                int dtype, const uint64_t* shape, int d, uint64_t local_extent,
+                                const tcb_params* params, tcb_result* out) {
+    return guard([&] {
+        std::vector<u64> sh(shape, shape + d);
+        Stream st;
+        ShardComm sc;
+        sc.comm = comm;
+        sc.world = world;
+        sc.rank = rank;
+        sc.local_extent = local_extent;
+        const Result r = compress_device(device_bytes, nbytes, dtype, sh, to_params(params, d), st.s, nullptr, &sc);
         host_trace_dump();
         fill(r, d, out);
     });

@@ -25,6 +25,7 @@
 #include <tuple>
 
 #include "kernels.cuh"
+#include "nccl_shim.hpp"
 #include "quant.cuh"
 
 namespace tcb {
@@ -307,18 +308,29 @@ StepOut factor_from_gram(const double* G, u64 n, const Budget& bud, cudaStream_t
 }
 
 StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int backend, cudaStream_t s,
-                  const double* gram) {
+                  const double* gram, const ShardComm* shard) {
+    const bool sharded = shard && shard->world > 1;
     // rows > cols is the reference's thin-SVD branch (sthosvd.cpp:91-99); its
     // stand-in here (Gram of B^T, U = B V / sigma, re-orthonormalised) is no more
     // accurate than the Gram of B itself -- both square the singular values -- so
     // a small row count takes the cheaper direct Gram route
-    const bool via_gram = backend == 1 || (backend == 0 && (rows <= cols || rows <= 256));
+    const u64 cols_all = sharded ? cols * static_cast<u64>(shard->world) : cols;
+    const bool via_gram = backend == 1 || (backend == 0 && (rows <= cols_all || rows <= 256));
+    if (sharded && !via_gram) throw Error("sharded compress: a step off the Gram route (rows > cols)");
     StepOut o;
     if (via_gram) {
         DevBuf<double> G;
         if (!gram) {
             G = DevBuf<double>(rows * rows, s);
             gram_f64(x, rows, cols, G.p, s);
+        }
+        if (sharded) {  // the columns are spread over the ranks: sum the partial Grams
+            if (gram) {
+                G = DevBuf<double>(rows * rows, s);
+                TCB_CUDA(cudaMemcpyAsync(G.p, gram, rows * rows * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            }
+            nccl_allreduce_sum_f64(G.p, rows * rows, shard->comm, s);
+            gram = nullptr;
         }
         o = factor_from_gram(gram ? gram : G.p, rows, budget, s);
     } else {  // thin left singular vectors from the Gram of B^T (sthosvd.cpp:91-99)
@@ -362,7 +374,8 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
 Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vector<u64>& shape, double target,
                       const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite,
                       const std::function<void(std::size_t, const double*, u64, u64)>& on_factor,
-                      double norm_scale, double* norm_out, const double* gram0) {
+                      double norm_scale, double* norm_out, const double* gram0, const ShardComm* shard) {
+    const bool sharded = shard && shard->world > 1;
     if (target < 0) throw Error("sthosvd: negative SSE target");
     const std::size_t d = shape.size();
     u64 n_el = 1;
@@ -401,6 +414,7 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
     }
     std::vector<u64> cur(d);
     for (std::size_t i = 0; i < d; ++i) cur[i] = shape[p[i]];
+    if (shard) cur[d - 1] = shard->local_extent;  // this rank's slab of the last processed mode
     double remaining = target;
     for (std::size_t step = 0; step < d; ++step) {
         u64 tot = 1;
@@ -413,7 +427,20 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
             budget.trace_out = &trace0;
         }
         HostTrace ht("sthosvd: mode step");
-        StepOut so = mode_step(xp, rows, cols, budget, backend, s, step == 0 && ident ? gram0 : nullptr);
+        StepOut so;
+        if (sharded && step == d - 1) {  // the slabs meet: gather the projected tensor, step replicated
+            const u64 full_rows = shape[p[d - 1]];
+            if (rows * static_cast<u64>(shard->world) != full_rows)
+                throw Error("sharded compress: slabs must split the last processed mode evenly");
+            DevBuf<double> full(full_rows * cols, s);
+            nccl_allgather_f64(xp, full.p, rows * cols, shard->comm, s);
+            x = std::move(full);
+            xp = x.p;
+            so = mode_step(xp, full_rows, cols, budget, backend, s);
+        } else {
+            so = mode_step(xp, rows, cols, budget, backend, s, step == 0 && ident ? gram0 : nullptr,
+                           step + 1 < d ? shard : nullptr);
+        }
         if (step == 0 && norm_out) {
             if (norm_scale >= 0) remaining = norm_scale * trace0;
             *norm_out = trace0;
@@ -895,7 +922,7 @@ bool norm_pass_forced() {
 }  // namespace
 
 Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,
-                       const Params& prm, cudaStream_t s, const double* gram0) {
+                       const Params& prm, cudaStream_t s, const double* gram0, const ShardComm* shard) {
     const auto t_all = Clock::now();
     Result res;
     const std::size_t d = shape.size();
@@ -905,10 +932,16 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
         if (v == 0) throw Error("tensor: zero-sized mode");
         n_el *= v;
     }
+    res.original_bytes = n_el * dtype_size(dtype);
+    const bool sharded = shard && shard->world > 1;
+    if (shard) {  // this rank holds a slab of the last processed mode: local element count
+        const std::vector<u64> pp = prm.mode_order ? *prm.mode_order : stable_ascending(shape);
+        if (!valid_perm(pp, d)) throw Error("sthosvd: invalid processing order");
+        n_el = n_el / shape[pp[d - 1]] * shard->local_extent;
+    }
     if (nbytes != n_el * dtype_size(dtype))
         throw Error("ingest: buffer holds " + std::to_string(nbytes) + " bytes, expected " +
                     std::to_string(n_el * dtype_size(dtype)));
-    res.original_bytes = n_el * dtype_size(dtype);
     if (prm.target_re && prm.target_sse)
         throw Error("compress: relative-error and SSE targets are mutually exclusive");
     if (!prm.target_re && !prm.target_sse) throw Error("compress: no error target given");
@@ -939,6 +972,16 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
         res.norm_sq = sum_squares(a.p, n_el, &finite, s);
     }
     if (dtype == 6 || dtype == 7) res.precision_loss = ingest_precision_loss(device_bytes, dtype, n_el, s);
+    if (sharded && !(direct && norm_from_gram)) {  // global norm, finite flag and precision flag
+        DevBuf<double> st(3, s);
+        const double h[3] = {res.norm_sq, finite ? 0.0 : 1.0, res.precision_loss ? 1.0 : 0.0};
+        st.upload(h, 3);
+        nccl_allreduce_sum_f64(st.p, 3, shard->comm, s);
+        const auto g = st.to_host();
+        res.norm_sq = g[0];
+        finite = g[1] == 0.0;
+        res.precision_loss = g[2] != 0.0;
+    }
     double target;
     if (prm.target_re) {
         if (*prm.target_re < 0) throw Error("budget: negative relative-error target");
@@ -967,7 +1010,7 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
         }
     } prep_join{preps};
     std::function<void(std::size_t, const double*, u64, u64)> on_factor;
-    if (dd > 1 && !prof_enabled()) {
+    if (dd > 1 && !prof_enabled() && !(shard && shard->rank != 0)) {  // only the encoding rank
         int dev = 0;
         TCB_CUDA(cudaGetDevice(&dev));
         on_factor = [&, dev](std::size_t mode, const double* U, u64 n, u64 r) {
@@ -992,13 +1035,20 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     try {
         f = sthosvd_device(std::move(a), direct ? static_cast<const double*>(device_bytes) : nullptr, shape,
                            prm.rtmss * target, prm.mode_order, prm.backend, s, finite ? 1 : 0, on_factor,
-                           norm_scale, norm_from_gram ? &norm_trace : nullptr, direct ? gram0 : nullptr);
+                           norm_scale, norm_from_gram ? &norm_trace : nullptr, direct ? gram0 : nullptr, shard);
     } catch (const TraceNonFinite&) {  // scan the elements: the reference error, or a norm pass rerun
         bool fin = true;
         sum_squares(static_cast<const double*>(device_bytes), n_el, &fin, s);
+        if (sharded) {  // every rank sees the same trace, so every rank is here: agree on the verdict
+            DevBuf<double> f(1, s);
+            const double h = fin ? 0.0 : 1.0;
+            f.upload(&h, 1);
+            nccl_allreduce_sum_f64(f.p, 1, shard->comm, s);
+            fin = f.to_host()[0] == 0.0;
+        }
         if (!fin) throw Error("sthosvd: input contains non-finite values");
         ForceNormPass force;
-        return compress_device(device_bytes, nbytes, dtype, shape, prm, s, gram0);
+        return compress_device(device_bytes, nbytes, dtype, shape, prm, s, gram0, shard);
     }
     if (norm_from_gram) {
         res.norm_sq = norm_trace;
@@ -1006,6 +1056,11 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
             target = *prm.target_re * *prm.target_re * res.norm_sq;
             res.target_sse = target;
         }
+    }
+    if (shard && shard->rank != 0) {  // the factorisation is replicated; rank 0 encodes
+        res.ranks = f.r;
+        res.times.total = ms_since(t_all);
+        return res;
     }
     double trunc = 0;
     for (double v : f.trunc) trunc += v;

@@ -44,9 +44,11 @@ struct Result {
 // device_bytes: element bytes (skip already applied) resident on the device
 // gram0 (optional): the first mode's Gram of the fp64 input, already computed
 // (bitwise as gram_f64 would; the host entry point overlaps it with the upload)
+struct ShardComm;  // below
 Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,
                        const Params& p, cudaStream_t s,
-                       const double* gram0 = nullptr);
+                       const double* gram0 = nullptr,
+                       const ShardComm* shard = nullptr);
 
 struct Tucker {
     DevBuf<double> core;
@@ -55,6 +57,17 @@ struct Tucker {
     std::vector<u64> n, r, order;
     std::vector<double> trunc;
 };
+// Sharded mode loop: the input is this rank's slab of the last
+// processed mode (equal slabs, rank order); the Grams of steps 0..d-2 are
+// summed over the ranks with NCCL before the eigensolve (so every rank holds
+// the same factor), the TTMs stay shard-local, and the last step all-gathers
+// the small projected tensor.  Steps 0..d-2 must take the Gram route.
+struct ShardComm {
+    void* comm = nullptr;   // ncclComm_t (nccl_shim)
+    int world = 1, rank = 0;
+    u64 local_extent = 0;   // this rank's slab of mode p[d-1]
+};
+
 // One mode step (sthosvd.cpp:136-166): factor U (rows x r, sign-fixed), the
 // discarded energy, and the projected/shifted tensor next = B^T U (cols x r).
 struct StepOut {
@@ -81,7 +94,7 @@ struct Budget {
 };
 // gram (optional): this step's Gram B B^T already computed (rows <= cols branch)
 StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int backend, cudaStream_t s,
-                  const double* gram = nullptr);
+                  const double* gram = nullptr, const ShardComm* shard = nullptr);
 // eigensolve + rank rule + sign fix on an (all-reduced) Gram; U is n x r
 StepOut factor_from_gram(const double* G, u64 n, const Budget& budget, cudaStream_t s);
 // sthosvd::compress (sthosvd.cpp:114-171) on a device tensor.  The input is
@@ -96,7 +109,8 @@ StepOut factor_from_gram(const double* G, u64 n, const Budget& budget, cudaStrea
 Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vector<u64>& shape, double target,
                       const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s, int finite = -1,
                       const std::function<void(std::size_t, const double*, u64, u64)>& on_factor = {},
-                      double norm_scale = -1.0, double* norm_out = nullptr, const double* gram0 = nullptr);
+                      double norm_scale = -1.0, double* norm_out = nullptr, const double* gram0 = nullptr,
+                      const ShardComm* shard = nullptr);
 inline Tucker sthosvd_device(DevBuf<double>&& a, const std::vector<u64>& shape, double target,
                              const std::optional<std::vector<u64>>& order, int backend, cudaStream_t s) {
     return sthosvd_device(std::move(a), nullptr, shape, target, order, backend, s);

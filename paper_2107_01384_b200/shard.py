@@ -210,9 +210,63 @@ def sthosvd_sharded(x_local, shape, target, ops, order=None, backend=0, group=No
                          norm_sq=norm_sq)
 
 
+_COMMS = {}
+
+
+def _nccl_comm(group, world, rank, device):
+    """The library's own NCCL communicator for `group` (created once): rank 0's
+    unique id travels through torch.distributed."""
+    key = (id(group), world, rank)
+    if key in _COMMS:
+        return _COMMS[key]
+    uid = (C.c_uint8 * 128)()
+    if rank == 0:
+        _check(lib().tcb_nccl_unique_id(uid))
+    backend = dist.get_backend(group) if dist.is_initialized() else "gloo"
+    t = torch.tensor(list(bytes(uid)), dtype=torch.uint8,
+                     device=device if backend == "nccl" else "cpu")
+    if world > 1:
+        dist.broadcast(t, src=0, group=group)
+    uid = (C.c_uint8 * 128)(*t.cpu().tolist())
+    comm = C.c_void_p()
+    _check(lib().tcb_nccl_comm_init(uid, int(world), int(rank), C.byref(comm)))
+    _COMMS[key] = comm
+    return comm
+
+
+def _compress_sharded_cpp(x_local, shape, dtype, params: Params, group, world, rank):
+    """The whole sharded compress in the library (mode loop, NCCL collectives,
+    encode on rank 0): the single-GPU pipeline's kernels and concurrency."""
+    p = list(params.mode_order) if params.mode_order is not None else stable_ascending(shape)
+    last = p[-1]
+    lo, hi = shard_bounds(shape[last], world, rank)
+    comm = _nccl_comm(group, world, rank, x_local.device)
+    sh = np.asarray(list(shape), np.uint64)
+    res = _CResult()
+    torch.cuda.synchronize()
+    _check(lib().tcb_compress_sharded_device(comm, int(world), int(rank), C.c_void_p(x_local.data_ptr()),
+                                             C.c_uint64(x_local.numel() * x_local.element_size()), int(dtype),
+                                             sh.ctypes.data_as(C.c_void_p), len(shape), C.c_uint64(hi - lo),
+                                             C.byref(params.to_c(len(shape))), C.byref(res)))
+    out = _result(res)
+    return out if rank == 0 else None
+
+
 def compress_sharded(x_local, shape, dtype, params: Params, ops=None, group=None):
     """pipeline::compress across the ranks of `group`; rank 0 returns the
-    CompressResult (container bytes), the other ranks return None."""
+    CompressResult (container bytes), the other ranks return None.  On CUDA
+    tensors with equal slabs the library runs the whole sharded pipeline (NCCL
+    inside); otherwise the per-stage path below."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if ops is None and isinstance(x_local, torch.Tensor) and x_local.is_cuda and x_local.is_contiguous():
+        p = list(params.mode_order) if params.mode_order is not None else stable_ascending(shape)
+        if shape[p[-1]] % world == 0:
+            try:
+                return _compress_sharded_cpp(x_local, shape, dtype, params, group, world, rank)
+            except TucompError as e:
+                if "off the Gram route" not in str(e):
+                    raise
     ops = ops or DeviceOps()
     if params.target_re is not None and params.target_sse is not None:
         raise TucompError("compress: relative-error and SSE targets are mutually exclusive")
