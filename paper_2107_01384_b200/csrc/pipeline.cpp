@@ -378,8 +378,12 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
     const bool sharded = shard && shard->world > 1;
     if (target < 0) throw Error("sthosvd: negative SSE target");
     const std::size_t d = shape.size();
+    std::vector<u64> p = order ? *order : stable_ascending(shape);
+    const bool perm_ok = valid_perm(p, d);  // checked after the finiteness test, as the reference does
+    std::vector<u64> lshape = shape;  // this rank's slab: the last processed mode is local
+    if (shard && perm_ok) lshape[p[d - 1]] = shard->local_extent;
     u64 n_el = 1;
-    for (auto v : shape) n_el *= v;
+    for (auto v : lshape) n_el *= v;
     const double* a = ext ? ext : owned.p;
     if (finite < 0) {
         bool fin = true;
@@ -387,8 +391,7 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
         finite = fin ? 1 : 0;
     }
     if (!finite) throw Error("sthosvd: input contains non-finite values");
-    std::vector<u64> p = order ? *order : stable_ascending(shape);
-    if (!valid_perm(p, d)) throw Error("sthosvd: invalid processing order");
+    if (!perm_ok) throw Error("sthosvd: invalid processing order");
     Tucker f;
     f.order = p;
     f.n = shape;
@@ -408,13 +411,12 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
         }
     } else {
         x = DevBuf<double>(n_el, s);
-        permute_axes(a, x.p, shape, p, s);
+        permute_axes(a, x.p, lshape, p, s);
         owned.release();
         xp = x.p;
     }
     std::vector<u64> cur(d);
-    for (std::size_t i = 0; i < d; ++i) cur[i] = shape[p[i]];
-    if (shard) cur[d - 1] = shard->local_extent;  // this rank's slab of the last processed mode
+    for (std::size_t i = 0; i < d; ++i) cur[i] = lshape[p[i]];
     double remaining = target;
     for (std::size_t step = 0; step < d; ++step) {
         u64 tot = 1;

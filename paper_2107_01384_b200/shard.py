@@ -240,13 +240,18 @@ def _compress_sharded_cpp(x_local, shape, dtype, params: Params, group, world, r
     p = list(params.mode_order) if params.mode_order is not None else stable_ascending(shape)
     last = p[-1]
     lo, hi = shard_bounds(shape[last], world, rank)
+    with torch.cuda.device(x_local.device):  # the library works on the calling thread's device
+        return _compress_sharded_cpp_on(x_local, shape, dtype, params, group, world, rank, hi - lo)
+
+
+def _compress_sharded_cpp_on(x_local, shape, dtype, params, group, world, rank, local_extent):
     comm = _nccl_comm(group, world, rank, x_local.device)
     sh = np.asarray(list(shape), np.uint64)
     res = _CResult()
     torch.cuda.synchronize()
     _check(lib().tcb_compress_sharded_device(comm, int(world), int(rank), C.c_void_p(x_local.data_ptr()),
                                              C.c_uint64(x_local.numel() * x_local.element_size()), int(dtype),
-                                             sh.ctypes.data_as(C.c_void_p), len(shape), C.c_uint64(hi - lo),
+                                             sh.ctypes.data_as(C.c_void_p), len(shape), C.c_uint64(local_extent),
                                              C.byref(params.to_c(len(shape))), C.byref(res)))
     out = _result(res)
     return out if rank == 0 else None
