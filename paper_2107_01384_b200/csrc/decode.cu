@@ -196,10 +196,11 @@ __global__ void __launch_bounds__(32) dec_entropy_kernel(const u8* __restrict__ 
         if (t >= total) t = total - 1;
         // locate: 1024-blocks, then 32-blocks, then entries
         u32 b2b = 0, b1b = 0, cb = 0;
+        // a level with a single block holds the whole remaining range: no search
         const u32 n2 = (nsym + 1023) / 1024;
-        const u32 b2 = find(l2, n2, t, &b2b);
+        const u32 b2 = n2 == 1 ? 0u : find(l2, n2, t, &b2b);
         const u32 lo1 = b2 * 32, n1 = min((nsym + 31) / 32 - lo1, 32u);
-        const u32 b1 = b2 < n2 ? find(l1 + lo1, n1, t - b2b, &b1b) : n1;
+        const u32 b1 = b2 < n2 ? (n1 == 1 ? 0u : find(l1 + lo1, n1, t - b2b, &b1b)) : n1;
         const u32 lo0 = (lo1 + b1) * 32, n0 = min(nsym - lo0, 32u);
         const u32 c0 = b1 < n1 ? find(cnt + lo0, n0, t - b2b - b1b, &cb) : n0;
         if (b2 >= n2 || b1 >= n1 || c0 >= n0) return dec_fail(err, kDecErrEntropy);
@@ -259,6 +260,7 @@ __global__ void __launch_bounds__(32) dec_entropy_kernel(const u8* __restrict__ 
 
 // ---------------------------------------------------------------- plane / block reconstruction
 constexpr int kDsT = 256;
+constexpr int kDsI = 8;  // coefficients per thread in a plane pass
 
 __device__ __forceinline__ u32 dec_cta_excl_scan(u32 v, u32* sh, u32& total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -372,41 +374,62 @@ __global__ void __launch_bounds__(kDsT) dec_stream_kernel(const u8* __restrict__
             }
             __syncthreads();
         }
-        // coefficient pass: ranks among insignificant / significant / bit consumers
+        // coefficient pass: ranks among insignificant / significant / bit consumers.
+        // Each thread owns kDsI consecutive coefficients of a kDsT*kDsI chunk, so a
+        // chunk costs two CTA scans: (insignificant, significant) packed in one
+        // u32, then the bit consumers
         const u8* raw = cont + d.raw_off;
         const u64 rawbits = static_cast<u64>(d.raw_len) * 8;
         u64 ins_base = 0, sig_base = 0, raw_base = 0;
-        for (u64 c0 = lo; c0 < hi; c0 += kDsT) {
-            const u64 i = c0 + threadIdx.x;
-            const bool in = i < hi;
-            const u64 mv = in ? m[i] : 0;
-            const bool sig = in && mv != 0, isn = in && mv == 0;
-            u32 tot_ins = 0, tot_sig = 0, tot_raw = 0;
-            const u32 rin = dec_cta_excl_scan(isn ? 1u : 0u, shs, tot_ins);
-            const u32 rsg = dec_cta_excl_scan(sig ? 1u : 0u, shs, tot_sig);
-            const u64 lu = ins_base + rin, tu = sig_base + rsg;
-            const bool refine = sig && tu < ts;
-            const bool lead = isn && lu < ls && lu < clen;
-            const bool one = lead && col[lo + lu] != 0;
-            const u32 rr = dec_cta_excl_scan((refine || one) ? 1u : 0u, shs, tot_raw);
-            if (refine || one) {
-                const u64 bpos = raw_base + rr;
+        for (u64 c0 = lo; c0 < hi; c0 += static_cast<u64>(kDsT) * kDsI) {
+            const u64 i0 = c0 + static_cast<u64>(threadIdx.x) * kDsI;
+            u64 mv[kDsI];
+            u32 nin = 0, nsg = 0;
+#pragma unroll
+            for (int j = 0; j < kDsI; ++j) {
+                const bool in = i0 + j < hi;
+                mv[j] = in ? m[i0 + j] : 0;
+                nin += (in && mv[j] == 0) ? 1u : 0u;
+                nsg += mv[j] != 0 ? 1u : 0u;
+            }
+            u32 tot_is = 0, tot_raw = 0;
+            const u32 ex = dec_cta_excl_scan(nin | (nsg << 16), shs, tot_is);
+            u64 lu = ins_base + (ex & 0xFFFFu), tu = sig_base + (ex >> 16);
+            u32 cons = 0, refm = 0;  // per-item bit masks: consumes a raw bit / is a refinement
+#pragma unroll
+            for (int j = 0; j < kDsI; ++j) {
+                if (i0 + j >= hi) continue;
+                if (mv[j] != 0) {
+                    if (tu < ts) {
+                        cons |= 1u << j;
+                        refm |= 1u << j;
+                    }
+                    ++tu;
+                } else {
+                    if (lu < ls && lu < clen && col[lo + lu] != 0) cons |= 1u << j;
+                    ++lu;
+                }
+            }
+            u64 bpos = raw_base + dec_cta_excl_scan(static_cast<u32>(__popc(cons)), shs, tot_raw);
+#pragma unroll
+            for (int j = 0; j < kDsI; ++j) {
+                if (!(cons >> j & 1u)) continue;
                 if (bpos >= rawbits) {
                     dec_fail(err, kDecErrBits);
                 } else {
                     const bool bit = (raw[bpos >> 3] >> (7 - (bpos & 7))) & 1u;
-                    if (refine) {
-                        if (bit) m[i] = mv | (u64{1} << p);
-                        pl[i] = static_cast<u8>(p);
+                    if (refm >> j & 1u) {
+                        if (bit) m[i0 + j] = mv[j] | (u64{1} << p);
                     } else {
-                        m[i] = u64{1} << p;
-                        ng[i] = bit ? 1 : 0;
-                        pl[i] = static_cast<u8>(p);
+                        m[i0 + j] = u64{1} << p;
+                        ng[i0 + j] = bit ? 1 : 0;
                     }
+                    pl[i0 + j] = static_cast<u8>(p);
                 }
+                ++bpos;
             }
-            ins_base += tot_ins;
-            sig_base += tot_sig;
+            ins_base += tot_is & 0xFFFFu;
+            sig_base += tot_is >> 16;
             raw_base += tot_raw;
             __syncthreads();
         }
