@@ -12,4 +12,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --set full --import-source on --clock-control none \
     -k regex:"syrk_kernel|syrk_reduce|ttm_kernel|tk_cluster|ac_kernel|householder_dataflow|crossing_kernel|emit_kernel|stats_kernel" \
     -c 24 -o gpurun_out/full python tools/compress_once.py --warmup 0 > gpurun_out/ncu_full.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/dec_launches.csv \
+    python tools/decompress_once.py --steps 1 --warmup 0 > gpurun_out/dec_ncu.log 2>&1
 echo done

@@ -25,6 +25,23 @@ with open(os.path.join(PROF, f"launches_{tag}_c2_1e-4_summary.txt"), "w") as f:
     f.write("# (cold-cache, serialised launches; 6 compress calls: 3 warm-up, 2 timed, 1 profiled + e2e)\n")
     f.write(summ)
 
+# decompress launch list (one c2 compress, then one decompress: the dec_* kernels onward)
+dec = os.path.join(OUT, "dec_launches.csv")
+if os.path.exists(dec):
+    rows = list(csv.DictReader(l for l in open(dec) if l.startswith('"')))
+    first = next((i for i, r in enumerate(rows) if "dec_entropy" in r["Kernel Name"]), None)
+    if first is not None:
+        with open(os.path.join(PROF, f"launches_{tag}_decompress_c2.txt"), "w") as f:
+            f.write("# ncu --metrics gpu__time_duration.sum --clock-control none, tools/decompress_once.py "
+                    "--steps 1 --warmup 0\n# (cold-cache, serialised): the decompress call's kernels\n")
+            tot = 0.0
+            for r in rows[first:]:
+                ns = float(r["Metric Value"].replace(",", ""))
+                tot += ns
+                f.write(f"{ns / 1e3:9.1f} us  grid {r['Grid Size']:>14} block {r['Block Size']:>12}  "
+                        f"{r['Kernel Name'][:90]}\n")
+            f.write(f"{tot / 1e3:9.1f} us  total\n")
+
 # full capture: per-kernel key metrics
 raw = subprocess.run(["ncu", "-i", os.path.join(OUT, "full.ncu-rep"), "--page", "raw", "--csv"],
                      capture_output=True, text=True).stdout
