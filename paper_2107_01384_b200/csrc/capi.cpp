@@ -96,6 +96,27 @@ void stream_sync(cudaStream_t s) {
     g_sync_ns += static_cast<u64>(now_ns() - t0);
 }
 
+// Device-to-host reads of small results go through a per-thread pinned bounce
+// buffer: a copy into pageable memory is synchronous inside the driver and
+// stalls the other host threads' CUDA calls for its duration (measured: a
+// factor-prep worker's pageable reads held the mode loop's launches back by
+// ~0.15 ms per mode); a pinned copy + stream sync blocks only this thread.
+void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t s) {
+    if (!bytes) return;
+    constexpr std::size_t kBounce = std::size_t{1} << 20;
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, h) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    if (pinned || bytes > kBounce) {  // already asynchronous: the caller syncs
+        TCB_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
+        return;
+    }
+    thread_local void* buf = nullptr;  // lives for the thread (never freed: exit order vs. the context)
+    if (!buf) TCB_CUDA(cudaMallocHost(&buf, kBounce));
+    TCB_CUDA(cudaMemcpyAsync(buf, d, bytes, cudaMemcpyDeviceToHost, s));
+    stream_sync(s);
+    std::memcpy(h, buf, bytes);
+}
+
 void timeline_dump();
 void host_trace_dump() {
     timeline_dump();

@@ -981,7 +981,7 @@ void run_ac(const u64* syms, const StreamOut* so, const AcDesc* dad, const std::
     TCB_LAUNCH();
     if (redo.to_host()[0] == 0) return;
     std::vector<u64> el(ns);
-    TCB_CUDA(cudaMemcpyAsync(el.data(), elen, ns * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    d2h(el.data(), elen, ns * sizeof(u64), s);
     stream_sync(s);
     std::vector<int> ids;
     for (int i = 0; i < ns; ++i)

@@ -35,6 +35,9 @@ constexpr u64 kFull = ~u64{0};
 
 // Host wait on a stream; counted (and timed under TCB_TRACE) per call site class.
 void stream_sync(cudaStream_t s);
+// device-to-host read; the caller syncs `s` before using `h` (pageable `h` up
+// to 1 MiB: through a pinned bounce buffer, complete on return)
+void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t s);
 
 // Stream-ordered device buffer (cudaMallocAsync pool; freed on the same stream).
 template <class T>
@@ -70,7 +73,7 @@ struct DevBuf {
         if (cnt) TCB_CUDA(cudaMemcpyAsync(p, h, cnt * sizeof(T), cudaMemcpyHostToDevice, s));
     }
     void download(T* h, std::size_t cnt) const {
-        if (cnt) TCB_CUDA(cudaMemcpyAsync(h, p, cnt * sizeof(T), cudaMemcpyDeviceToHost, s));
+        d2h(h, p, cnt * sizeof(T), s);
     }
     std::vector<T> to_host() const {
         std::vector<T> v(n);

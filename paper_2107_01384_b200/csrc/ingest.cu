@@ -165,8 +165,8 @@ double sumsq_impl(const T* x, u64 n, bool* finite, cudaStream_t s) {
     TCB_LAUNCH();
     double r = 0;
     int b = 0;
-    TCB_CUDA(cudaMemcpyAsync(&r, part.p + grid, sizeof(double), cudaMemcpyDeviceToHost, s));
-    TCB_CUDA(cudaMemcpyAsync(&b, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    d2h(&r, part.p + grid, sizeof(double), s);
+    d2h(&b, bad.p, sizeof(int), s);
     stream_sync(s);
     if (finite) *finite = b == 0;
     return r;
@@ -342,7 +342,7 @@ double sse_between(const double* a, const double* b, u64 n, bool f32, cudaStream
     count_launch(2);
     TCB_LAUNCH();
     double r = 0;
-    TCB_CUDA(cudaMemcpyAsync(&r, part.p + grid, sizeof(double), cudaMemcpyDeviceToHost, s));
+    d2h(&r, part.p + grid, sizeof(double), s);
     stream_sync(s);
     return r;
 }
@@ -380,7 +380,7 @@ double max_abs_finite(const double* x, u64 n, bool* finite, cudaStream_t s) {
     count_launch(2);
     TCB_LAUNCH();
     double r[2] = {0, 0};
-    TCB_CUDA(cudaMemcpyAsync(r, part.p + grid, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    d2h(r, part.p + grid, 2 * sizeof(double), s);
     stream_sync(s);
     int b = 0;
     std::memcpy(&b, &r[1], sizeof(int));
@@ -419,7 +419,7 @@ double max_abs(const double* x, u64 n, cudaStream_t s) {
     count_launch(2);
     TCB_LAUNCH();
     double r = 0;
-    TCB_CUDA(cudaMemcpyAsync(&r, part.p + grid, sizeof(double), cudaMemcpyDeviceToHost, s));
+    d2h(&r, part.p + grid, sizeof(double), s);
     stream_sync(s);
     return r;
 }

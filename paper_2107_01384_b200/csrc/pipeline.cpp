@@ -1012,7 +1012,11 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
         }
     } prep_join{preps};
     std::function<void(std::size_t, const double*, u64, u64)> on_factor;
-    if (dd > 1 && !prof_enabled() && !(shard && shard->rank != 0)) {  // only the encoding rank
+    static const bool no_early_prep = [] {  // debugging: factor prep after the mode loop
+        const char* e = std::getenv("TCB_NO_EARLY_PREP");
+        return e && *e && *e != '0';
+    }();
+    if (dd > 1 && !prof_enabled() && !no_early_prep && !(shard && shard->rank != 0)) {  // only the encoding rank
         int dev = 0;
         TCB_CUDA(cudaGetDevice(&dev));
         on_factor = [&, dev](std::size_t mode, const double* U, u64 n, u64 r) {
