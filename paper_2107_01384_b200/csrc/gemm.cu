@@ -8,6 +8,7 @@
 // padding.  Split-K partials are reduced in a fixed order, so results are
 // bitwise reproducible run to run.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -36,25 +37,24 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // ------------------------------------------------------------------ SYRK
-constexpr int GT = 64;        // output tile
-constexpr int GBK = 32;       // k slab
-constexpr int GPAD = GBK + 4; // row stride in smem (doubles): conflict-free fragment reads
+constexpr int GT = 64;  // output tile
 
-// Load rows [r0, r0+64) x k [k0, k0+32) of row-major B into s[64][GPAD]
-template <bool V16>
-__device__ __forceinline__ void load_slab(double (*s)[GPAD], const double* __restrict__ B, u64 rows, u64 cols,
+// Load rows [r0, r0+64) x k [k0, k0+BK) of row-major B into s[64][BK+4]
+// (row stride BK+4 doubles: the fragment reads below are bank-conflict free).
+template <bool V16, int BK>
+__device__ __forceinline__ void load_slab(double (*s)[BK + 4], const double* __restrict__ B, u64 rows, u64 cols,
                                           u64 r0, u64 k0, u64 k1) {
     if constexpr (V16) {
-        // 64 rows x 16 chunks of 16 B
-        for (int c = threadIdx.x; c < GT * (GBK / 2); c += blockDim.x) {
-            const int rr = c / (GBK / 2), kk = (c % (GBK / 2)) * 2;
+        // 64 rows x BK/2 chunks of 16 B
+        for (int c = threadIdx.x; c < GT * (BK / 2); c += blockDim.x) {
+            const int rr = c / (BK / 2), kk = (c % (BK / 2)) * 2;
             const u64 gr = r0 + rr, gk = k0 + kk;
             const bool ok = gr < rows && gk < k1;  // k1 even here: pairs never straddle
             cp_async16(&s[rr][kk], ok ? B + gr * cols + gk : B, ok);
         }
     } else {
-        for (int c = threadIdx.x; c < GT * GBK; c += blockDim.x) {
-            const int rr = c / GBK, kk = c % GBK;
+        for (int c = threadIdx.x; c < GT * BK; c += blockDim.x) {
+            const int rr = c / BK, kk = c % BK;
             const u64 gr = r0 + rr, gk = k0 + kk;
             const bool ok = gr < rows && gk < k1;
             cp_async8(&s[rr][kk], ok ? B + gr * cols + gk : B, ok);
@@ -67,13 +67,22 @@ __device__ __forceinline__ void load_slab(double (*s)[GPAD], const double* __res
 // (a fixed split count leaves SMs with 2 or 3 CTAs), and blockIdx runs tile-
 // fastest so the CTAs resident together cover all lower-triangle tiles of the
 // same k-chunk and share B's row blocks through L2 (one DRAM pass over B).
-template <bool V16>
-__global__ void __launch_bounds__(256) syrk_kernel(const double* __restrict__ B, u64 rows, u64 cols,
+// ST-stage cp.async ring with one barrier per k slab.  On a diagonal tile the
+// two warps whose 32x16 block lies wholly above the diagonal issue no DMMA
+// (the reduction never reads the upper half): 10 % less tensor work on a
+// 256-row Gram, which co-resident CTAs' warps pick up.
+template <int BK, int ST>
+constexpr int syrk_min_blocks() {  // CTAs per SM the shared memory allows; registers are capped to match
+    return (228 * 1024) / (2 * ST * 64 * (BK + 4) * 8 + 1024) >= 3 ? 3 : 2;
+}
+template <bool V16, int BK, int ST>
+__global__ void __launch_bounds__(256, syrk_min_blocks<BK, ST>()) syrk_kernel(const double* __restrict__ B, u64 rows, u64 cols,
                                                   int ntiles_lower, u64 slabs_per_split, u64 nslab, u64 split0,
                                                   double* __restrict__ ws) {
+    constexpr int PAD = BK + 4;
     extern __shared__ __align__(16) double smem_syrk[];
-    auto As = reinterpret_cast<double (*)[GT][GPAD]>(smem_syrk);
-    auto Bs = reinterpret_cast<double (*)[GT][GPAD]>(smem_syrk + 2 * GT * GPAD);
+    auto As = reinterpret_cast<double (*)[GT][PAD]>(smem_syrk);
+    auto Bs = reinterpret_cast<double (*)[GT][PAD]>(smem_syrk + ST * GT * PAD);
     const int tile = blockIdx.x % ntiles_lower;
     const u64 split = split0 + blockIdx.x / ntiles_lower;
     const u64 s0 = split * slabs_per_split, s1 = min(nslab, s0 + slabs_per_split);
@@ -83,7 +92,8 @@ __global__ void __launch_bounds__(256) syrk_kernel(const double* __restrict__ B,
     while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
     const int tj = tile - ti * (ti + 1) / 2;
     const bool diag = ti == tj;
-    const u64 k0 = s0 * GBK, k1 = min(cols, s1 * GBK);
+    const bool idle = diag && wn >= wm + 32;
+    const u64 k0 = s0 * BK, k1 = min(cols, s1 * BK);
     const u64 ra = static_cast<u64>(ti) * GT, rb = static_cast<u64>(tj) * GT;
     double acc[4][2][2];
 #pragma unroll
@@ -91,27 +101,28 @@ __global__ void __launch_bounds__(256) syrk_kernel(const double* __restrict__ B,
 #pragma unroll
         for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int ns = s1 > s0 ? static_cast<int>(s1 - s0) : 0;
-    if (ns > 0) {
-        load_slab<V16>(As[0], B, rows, cols, ra, k0, k1);
-        if (!diag) load_slab<V16>(Bs[0], B, rows, cols, rb, k0, k1);
+    auto load = [&](int buf, int sl) {
+        const u64 kn = k0 + static_cast<u64>(sl) * BK;
+        load_slab<V16, BK>(As[buf], B, rows, cols, ra, kn, k1);
+        if (!diag) load_slab<V16, BK>(Bs[buf], B, rows, cols, rb, kn, k1);
+    };
+#pragma unroll
+    for (int st = 0; st < ST - 1; ++st) {
+        if (st < ns) load(st, st);
         cp_commit();
     }
     for (int sl = 0; sl < ns; ++sl) {
-        const int cur = sl & 1;
-        if (sl + 1 < ns) {
-            const u64 kn = k0 + static_cast<u64>(sl + 1) * GBK;
-            load_slab<V16>(As[cur ^ 1], B, rows, cols, ra, kn, k1);
-            if (!diag) load_slab<V16>(Bs[cur ^ 1], B, rows, cols, rb, kn, k1);
-            cp_commit();
-            cp_wait<1>();
-        } else {
-            cp_wait<0>();
-        }
+        const int cur = sl % ST;
+        cp_wait<ST - 2>();
         __syncthreads();
-        double (*As_)[GPAD] = As[cur];
-        double (*Bs_)[GPAD] = diag ? As[cur] : Bs[cur];
+        // refill the stage consumed last iteration (every warp is past it)
+        if (sl + ST - 1 < ns) load((sl + ST - 1) % ST, sl + ST - 1);
+        cp_commit();
+        if (idle) continue;
+        double (*As_)[PAD] = As[cur];
+        double (*Bs_)[PAD] = diag ? As[cur] : Bs[cur];
 #pragma unroll
-        for (int kk = 0; kk < GBK; kk += 4) {
+        for (int kk = 0; kk < BK; kk += 4) {
             double a[4], b[2];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi) a[mi] = As_[wm + mi * 8 + (lane >> 2)][kk + (lane & 3)];
@@ -122,7 +133,6 @@ __global__ void __launch_bounds__(256) syrk_kernel(const double* __restrict__ B,
 #pragma unroll
                 for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
         }
-        __syncthreads();
     }
     double* out = ws + (split * ntiles_lower + tile) * GT * GT;
 #pragma unroll
@@ -134,6 +144,24 @@ __global__ void __launch_bounds__(256) syrk_kernel(const double* __restrict__ B,
             *reinterpret_cast<double2*>(out + m * GT + n) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
         }
 }
+
+// Kernel shapes (k slab BK, pipeline stages ST); TCB_GRAM_VARIANT picks one
+// for measurement, the default is the fastest on the c2 Gram.
+struct SyrkVariant {
+    int bk, st;
+    void (*k16)(const double*, u64, u64, int, u64, u64, u64, double*);
+    void (*k8)(const double*, u64, u64, int, u64, u64, u64, double*);
+    int smem() const { return 2 * st * GT * (bk + 4) * static_cast<int>(sizeof(double)); }
+};
+const SyrkVariant kSyrk[] = {
+    {32, 2, syrk_kernel<true, 32, 2>, syrk_kernel<false, 32, 2>},
+    {32, 3, syrk_kernel<true, 32, 3>, syrk_kernel<false, 32, 3>},
+    {16, 3, syrk_kernel<true, 16, 3>, syrk_kernel<false, 16, 3>},
+    {16, 4, syrk_kernel<true, 16, 4>, syrk_kernel<false, 16, 4>},
+    {32, 4, syrk_kernel<true, 32, 4>, syrk_kernel<false, 32, 4>},
+};
+constexpr int kSyrkVariants = sizeof(kSyrk) / sizeof(kSyrk[0]);
+constexpr int kSyrkDefault = 1;
 
 // fixed-order split reduction (split 0, 1, ...); writes the full symmetric G (row-major)
 __global__ void syrk_reduce(const double* __restrict__ ws, int splits, int ntiles_lower, u64 rows,
@@ -309,19 +337,26 @@ double peak_dmma_tflops() {
 }
 
 GramPlan gram_plan(const double* B, u64 rows, u64 cols) {
-    GramPlan gp;
-    const int nt = static_cast<int>((rows + GT - 1) / GT);
-    gp.lower = nt * (nt + 1) / 2;
-    gp.nslab = (cols + GBK - 1) / GBK;
-    gp.v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
-    const int smem = 4 * GT * GPAD * sizeof(double);
-    static int per_sm = [&] {
-        cudaFuncSetAttribute(syrk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(syrk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    static const int variant = [] {
+        const char* e = std::getenv("TCB_GRAM_VARIANT");
+        const int v = e && *e ? std::atoi(e) : kSyrkDefault;
+        return v >= 0 && v < kSyrkVariants ? v : kSyrkDefault;
+    }();
+    static const int per_sm = [] {
+        const SyrkVariant& k = kSyrk[variant];
+        cudaFuncSetAttribute(k.k16, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem());
+        cudaFuncSetAttribute(k.k8, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem());
         int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, syrk_kernel<true>, 256, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k.k16, 256, k.smem());
         return std::max(1, b);
     }();
+    GramPlan gp;
+    gp.variant = variant;
+    gp.bk = kSyrk[variant].bk;
+    const int nt = static_cast<int>((rows + GT - 1) / GT);
+    gp.lower = nt * (nt + 1) / 2;
+    gp.nslab = (cols + gp.bk - 1) / gp.bk;
+    gp.v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
     const u64 slots = static_cast<u64>(per_sm) * sm_count();
     u64 splits = std::max<u64>(1, std::min<u64>(gp.nslab, slots / gp.lower));
     gp.per = (gp.nslab + splits - 1) / splits;
@@ -331,18 +366,17 @@ GramPlan gram_plan(const double* B, u64 rows, u64 cols) {
 
 u64 gram_ws_doubles(const GramPlan& gp) { return gp.splits * gp.lower * GT * GT; }
 
-u64 gram_split_col(const GramPlan& gp, u64 split, u64 cols) { return std::min<u64>(cols, split * gp.per * GBK); }
+u64 gram_split_col(const GramPlan& gp, u64 split, u64 cols) {
+    return std::min<u64>(cols, split * gp.per * static_cast<u64>(gp.bk));
+}
 
 void gram_splits(const double* B, u64 rows, u64 cols, const GramPlan& gp, u64 sp0, u64 sp1, double* ws,
                  cudaStream_t s) {
     if (sp1 <= sp0) return;
     ProfScope prof_scope(kGram, s);
-    const int smem = 4 * GT * GPAD * sizeof(double);
+    const SyrkVariant& k = kSyrk[gp.variant];
     const unsigned grid = static_cast<unsigned>((sp1 - sp0) * gp.lower);
-    if (gp.v16)
-        syrk_kernel<true><<<grid, 256, smem, s>>>(B, rows, cols, gp.lower, gp.per, gp.nslab, sp0, ws);
-    else
-        syrk_kernel<false><<<grid, 256, smem, s>>>(B, rows, cols, gp.lower, gp.per, gp.nslab, sp0, ws);
+    (gp.v16 ? k.k16 : k.k8)<<<grid, 256, k.smem(), s>>>(B, rows, cols, gp.lower, gp.per, gp.nslab, sp0, ws);
     count_launch();
     TCB_LAUNCH();
 }

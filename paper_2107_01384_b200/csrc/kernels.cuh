@@ -38,6 +38,7 @@ struct GramPlan {
     int lower = 0;
     u64 nslab = 0, per = 0, splits = 0;
     bool v16 = false;
+    int variant = 0, bk = 32;  // SYRK kernel shape (gemm.cu kSyrk)
 };
 GramPlan gram_plan(const double* B, u64 rows, u64 cols);
 u64 gram_ws_doubles(const GramPlan& gp);
