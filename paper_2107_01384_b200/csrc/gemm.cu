@@ -71,14 +71,19 @@ __device__ __forceinline__ void load_slab(double (*s)[BK + 4], const double* __r
 // two warps whose 32x16 block lies wholly above the diagonal issue no DMMA
 // (the reduction never reads the upper half): 10 % less tensor work on a
 // 256-row Gram, which co-resident CTAs' warps pick up.
-template <int BK, int ST>
+template <int BK, int ST, int WN>
 constexpr int syrk_min_blocks() {  // CTAs per SM the shared memory allows; registers are capped to match
-    return (228 * 1024) / (2 * ST * 64 * (BK + 4) * 8 + 1024) >= 3 ? 3 : 2;
+    constexpr int by_smem = (228 * 1024) / (2 * ST * 64 * (BK + 4) * 8 + 1024);
+    constexpr int cap = WN == 16 ? 3 : 4;
+    return by_smem < 1 ? 1 : (by_smem > cap ? cap : by_smem);
 }
-template <bool V16, int BK, int ST>
-__global__ void __launch_bounds__(256, syrk_min_blocks<BK, ST>()) syrk_kernel(const double* __restrict__ B, u64 rows, u64 cols,
-                                                  int ntiles_lower, u64 slabs_per_split, u64 nslab, u64 split0,
-                                                  double* __restrict__ ws) {
+// WN: warp tile 32 x WN (16: 8 warps, 8 DMMA per 6 fragment loads; 32: 4 warps,
+// 16 independent DMMA per 8 fragment loads).
+template <bool V16, int BK, int ST, int WN>
+__global__ void __launch_bounds__(WN == 16 ? 256 : 128, syrk_min_blocks<BK, ST, WN>()) syrk_kernel(
+    const double* __restrict__ B, u64 rows, u64 cols, int ntiles_lower, u64 slabs_per_split, u64 nslab, u64 split0,
+    double* __restrict__ ws) {
+    constexpr int NI = WN / 8, WCOLS = GT / WN;
     constexpr int PAD = BK + 4;
     extern __shared__ __align__(16) double smem_syrk[];
     auto As = reinterpret_cast<double (*)[GT][PAD]>(smem_syrk);
@@ -87,7 +92,7 @@ __global__ void __launch_bounds__(256, syrk_min_blocks<BK, ST>()) syrk_kernel(co
     const u64 split = split0 + blockIdx.x / ntiles_lower;
     const u64 s0 = split * slabs_per_split, s1 = min(nslab, s0 + slabs_per_split);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+    const int wm = (warp / WCOLS) * 32, wn = (warp % WCOLS) * WN;
     int ti = 0;
     while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
     const int tj = tile - ti * (ti + 1) / 2;
@@ -95,11 +100,11 @@ __global__ void __launch_bounds__(256, syrk_min_blocks<BK, ST>()) syrk_kernel(co
     const bool idle = diag && wn >= wm + 32;
     const u64 k0 = s0 * BK, k1 = min(cols, s1 * BK);
     const u64 ra = static_cast<u64>(ti) * GT, rb = static_cast<u64>(tj) * GT;
-    double acc[4][2][2];
+    double acc[4][NI][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int ns = s1 > s0 ? static_cast<int>(s1 - s0) : 0;
     auto load = [&](int buf, int sl) {
         const u64 kn = k0 + static_cast<u64>(sl) * BK;
@@ -123,22 +128,22 @@ __global__ void __launch_bounds__(256, syrk_min_blocks<BK, ST>()) syrk_kernel(co
         double (*Bs_)[PAD] = diag ? As[cur] : Bs[cur];
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
-            double a[4], b[2];
+            double a[4], b[NI];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi) a[mi] = As_[wm + mi * 8 + (lane >> 2)][kk + (lane & 3)];
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) b[ni] = Bs_[wn + ni * 8 + (lane >> 2)][kk + (lane & 3)];
+            for (int ni = 0; ni < NI; ++ni) b[ni] = Bs_[wn + ni * 8 + (lane >> 2)][kk + (lane & 3)];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+                for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
         }
     }
     double* out = ws + (split * ntiles_lower + tile) * GT * GT;
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
+        for (int ni = 0; ni < NI; ++ni) {
             const int m = wm + mi * 8 + (lane >> 2);
             const int n = wn + ni * 8 + 2 * (lane & 3);
             *reinterpret_cast<double2*>(out + m * GT + n) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
@@ -148,20 +153,19 @@ __global__ void __launch_bounds__(256, syrk_min_blocks<BK, ST>()) syrk_kernel(co
 // Kernel shapes (k slab BK, pipeline stages ST); TCB_GRAM_VARIANT picks one
 // for measurement, the default is the fastest on the c2 Gram.
 struct SyrkVariant {
-    int bk, st;
+    int bk, st, threads;
     void (*k16)(const double*, u64, u64, int, u64, u64, u64, double*);
     void (*k8)(const double*, u64, u64, int, u64, u64, u64, double*);
     int smem() const { return 2 * st * GT * (bk + 4) * static_cast<int>(sizeof(double)); }
 };
+#define TCB_SYRK(BK, ST, WN) {BK, ST, WN == 16 ? 256 : 128, syrk_kernel<true, BK, ST, WN>, syrk_kernel<false, BK, ST, WN>}
 const SyrkVariant kSyrk[] = {
-    {32, 2, syrk_kernel<true, 32, 2>, syrk_kernel<false, 32, 2>},
-    {32, 3, syrk_kernel<true, 32, 3>, syrk_kernel<false, 32, 3>},
-    {16, 3, syrk_kernel<true, 16, 3>, syrk_kernel<false, 16, 3>},
-    {16, 4, syrk_kernel<true, 16, 4>, syrk_kernel<false, 16, 4>},
-    {32, 4, syrk_kernel<true, 32, 4>, syrk_kernel<false, 32, 4>},
+    TCB_SYRK(32, 2, 16), TCB_SYRK(32, 3, 16), TCB_SYRK(16, 3, 16), TCB_SYRK(16, 4, 16), TCB_SYRK(32, 4, 16),
+    TCB_SYRK(32, 2, 32), TCB_SYRK(16, 3, 32), TCB_SYRK(16, 4, 32), TCB_SYRK(32, 3, 32), TCB_SYRK(16, 2, 32),
 };
+#undef TCB_SYRK
 constexpr int kSyrkVariants = sizeof(kSyrk) / sizeof(kSyrk[0]);
-constexpr int kSyrkDefault = 1;
+constexpr int kSyrkDefault = 7;
 
 // fixed-order split reduction (split 0, 1, ...); writes the full symmetric G (row-major)
 __global__ void syrk_reduce(const double* __restrict__ ws, int splits, int ntiles_lower, u64 rows,
@@ -347,7 +351,7 @@ GramPlan gram_plan(const double* B, u64 rows, u64 cols) {
         cudaFuncSetAttribute(k.k16, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem());
         cudaFuncSetAttribute(k.k8, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem());
         int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k.k16, 256, k.smem());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k.k16, k.threads, k.smem());
         return std::max(1, b);
     }();
     GramPlan gp;
@@ -376,7 +380,7 @@ void gram_splits(const double* B, u64 rows, u64 cols, const GramPlan& gp, u64 sp
     ProfScope prof_scope(kGram, s);
     const SyrkVariant& k = kSyrk[gp.variant];
     const unsigned grid = static_cast<unsigned>((sp1 - sp0) * gp.lower);
-    (gp.v16 ? k.k16 : k.k8)<<<grid, 256, k.smem(), s>>>(B, rows, cols, gp.lower, gp.per, gp.nslab, sp0, ws);
+    (gp.v16 ? k.k16 : k.k8)<<<grid, k.threads, k.smem(), s>>>(B, rows, cols, gp.lower, gp.per, gp.nslab, sp0, ws);
     count_launch();
     TCB_LAUNCH();
 }
