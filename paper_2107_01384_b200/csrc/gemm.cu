@@ -71,6 +71,16 @@ __device__ __forceinline__ void load_slab(double (*s)[BK + 4], const double* __r
 // two warps whose 32x16 block lies wholly above the diagonal issue no DMMA
 // (the reduction never reads the upper half): 10 % less tensor work on a
 // 256-row Gram, which co-resident CTAs' warps pick up.
+// One SYRK launch: off-diagonal splits [so0, so0 + off_ctas / n_off) and
+// diagonal splits [sd0, sd0 + (grid - off_ctas) / n_diag).  Diagonal tiles
+// leave their upper warp blocks idle, so they take per_d = per_o x (active
+// warps off / on the diagonal) slabs per CTA: every CTA issues the same DMMA
+// count, and the SMs are balanced whatever tiles the scheduler co-locates.
+struct SyrkLaunch {
+    int n_off, n_diag;
+    u64 per_o, per_d, nslab, so0, sd0, splits_o, off_ctas;
+};
+
 template <int BK, int ST, int WN>
 constexpr int syrk_min_blocks() {  // CTAs per SM the shared memory allows; registers are capped to match
     constexpr int by_smem = (228 * 1024) / (2 * ST * 64 * (BK + 4) * 8 + 1024);
@@ -79,32 +89,23 @@ constexpr int syrk_min_blocks() {  // CTAs per SM the shared memory allows; regi
 }
 // WN: warp tile 32 x WN (16: 8 warps, 8 DMMA per 6 fragment loads; 32: 4 warps,
 // 16 independent DMMA per 8 fragment loads).
-template <bool V16, int BK, int ST, int WN>
-__global__ void __launch_bounds__(WN == 16 ? 256 : 128, syrk_min_blocks<BK, ST, WN>()) syrk_kernel(
-    const double* __restrict__ B, u64 rows, u64 cols, int ntiles_lower, u64 slabs_per_split, u64 nslab, u64 split0,
-    double* __restrict__ ws) {
-    constexpr int NI = WN / 8, WCOLS = GT / WN;
+// One CTA's split-K SYRK over k slabs [s0, s1): ST-stage cp.async ring with
+// one barrier per slab; the warp accumulates NS output strips of 32 rows x 8
+// columns at (sr[j], sc[j]) of the 64x64 tile (A fragments reloaded only when
+// a strip's rows change).  `idle` warps only help load.
+template <bool V16, int BK, int ST, int NS>
+__device__ __forceinline__ void syrk_run(double (*As)[GT][BK + 4], double (*Bs)[GT][BK + 4],
+                                         const double* __restrict__ B, u64 rows, u64 cols, u64 ra, u64 rb, bool diag,
+                                         u64 s0, u64 s1, u64 nslab, const int (&sr)[NS], const int (&sc)[NS],
+                                         bool idle, double* __restrict__ out) {
     constexpr int PAD = BK + 4;
-    extern __shared__ __align__(16) double smem_syrk[];
-    auto As = reinterpret_cast<double (*)[GT][PAD]>(smem_syrk);
-    auto Bs = reinterpret_cast<double (*)[GT][PAD]>(smem_syrk + ST * GT * PAD);
-    const int tile = blockIdx.x % ntiles_lower;
-    const u64 split = split0 + blockIdx.x / ntiles_lower;
-    const u64 s0 = split * slabs_per_split, s1 = min(nslab, s0 + slabs_per_split);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp / WCOLS) * 32, wn = (warp % WCOLS) * WN;
-    int ti = 0;
-    while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
-    const int tj = tile - ti * (ti + 1) / 2;
-    const bool diag = ti == tj;
-    const bool idle = diag && wn >= wm + 32;
+    const int lane = threadIdx.x & 31;
     const u64 k0 = s0 * BK, k1 = min(cols, s1 * BK);
-    const u64 ra = static_cast<u64>(ti) * GT, rb = static_cast<u64>(tj) * GT;
-    double acc[4][NI][2];
+    double acc[4][NS][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NS; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int ns = s1 > s0 ? static_cast<int>(s1 - s0) : 0;
     auto load = [&](int buf, int sl) {
         const u64 kn = k0 + static_cast<u64>(sl) * BK;
@@ -128,34 +129,93 @@ __global__ void __launch_bounds__(WN == 16 ? 256 : 128, syrk_min_blocks<BK, ST, 
         double (*Bs_)[PAD] = diag ? As[cur] : Bs[cur];
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
-            double a[4], b[NI];
+            double a[4], b[NS];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) a[mi] = As_[wm + mi * 8 + (lane >> 2)][kk + (lane & 3)];
+            for (int j = 0; j < NS; ++j) b[j] = Bs_[sc[j] + (lane >> 2)][kk + (lane & 3)];
 #pragma unroll
-            for (int ni = 0; ni < NI; ++ni) b[ni] = Bs_[wn + ni * 8 + (lane >> 2)][kk + (lane & 3)];
+            for (int j = 0; j < NS; ++j) {
+                if (j == 0 || (NS == 3 && sr[j] != sr[j - 1])) {  // NS 3: diagonal strips change rows
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
+                    for (int mi = 0; mi < 4; ++mi) a[mi] = As_[sr[j] + mi * 8 + (lane >> 2)][kk + (lane & 3)];
+                }
 #pragma unroll
-                for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+                for (int mi = 0; mi < 4; ++mi) dmma(acc[mi][j][0], acc[mi][j][1], a[mi], b[j]);
+            }
         }
     }
-    double* out = ws + (split * ntiles_lower + tile) * GT * GT;
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-            const int m = wm + mi * 8 + (lane >> 2);
-            const int n = wn + ni * 8 + 2 * (lane & 3);
-            *reinterpret_cast<double2*>(out + m * GT + n) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+        for (int j = 0; j < NS; ++j) {
+            const int m = sr[j] + mi * 8 + (lane >> 2);
+            const int n = sc[j] + 2 * (lane & 3);
+            *reinterpret_cast<double2*>(out + m * GT + n) = make_double2(acc[mi][j][0], acc[mi][j][1]);
         }
+}
+
+template <bool V16, int BK, int ST, int WN>
+__global__ void __launch_bounds__(WN == 16 ? 256 : 128, syrk_min_blocks<BK, ST, WN>()) syrk_kernel(
+    const double* __restrict__ B, u64 rows, u64 cols, SyrkLaunch L, double* __restrict__ ws) {
+    constexpr int NI = WN / 8, WCOLS = GT / WN;
+    constexpr int PAD = BK + 4;
+    extern __shared__ __align__(16) double smem_syrk[];
+    auto As = reinterpret_cast<double (*)[GT][PAD]>(smem_syrk);
+    auto Bs = reinterpret_cast<double (*)[GT][PAD]>(smem_syrk + ST * GT * PAD);
+    (void)PAD;
+    // CTAs [0, off_ctas): off-diagonal tiles, tile-fastest; then diagonal tiles
+    int ti, tj;
+    u64 s0, s1;
+    double* out;
+    if (blockIdx.x < L.off_ctas) {
+        const int o = static_cast<int>(blockIdx.x % L.n_off);
+        const u64 split = L.so0 + blockIdx.x / L.n_off;
+        ti = 1;
+        while ((ti + 1) * ti / 2 <= o) ++ti;
+        tj = o - ti * (ti - 1) / 2;
+        s0 = split * L.per_o;
+        s1 = min(L.nslab, s0 + L.per_o);
+        out = ws + (split * L.n_off + o) * GT * GT;
+    } else {
+        const u64 b = blockIdx.x - L.off_ctas;
+        const int d = static_cast<int>(b % L.n_diag);
+        const u64 split = L.sd0 + b / L.n_diag;
+        ti = tj = d;
+        s0 = split * L.per_d;
+        s1 = min(L.nslab, s0 + L.per_d);
+        out = ws + (L.splits_o * L.n_off + split * L.n_diag + d) * GT * GT;
+    }
+    const int warp = threadIdx.x >> 5;
+    const bool diag = ti == tj;
+    const u64 ra = static_cast<u64>(ti) * GT, rb = static_cast<u64>(tj) * GT;
+    if constexpr (WN == 32) {
+        if (diag) {
+            // the diagonal tile's 3 lower 32x32 blocks as 12 strips of 32x8,
+            // 3 per warp: every warp (so every SM sub-partition) stays busy
+            int sr[3], sc[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const int idx = 3 * warp + j;
+                sr[j] = idx < 4 ? 0 : 32;
+                sc[j] = idx < 4 ? 8 * idx : 8 * (idx - 4);
+            }
+            syrk_run<V16, BK, ST, 3>(As, Bs, B, rows, cols, ra, rb, true, s0, s1, L.nslab, sr, sc, false, out);
+            return;
+        }
+    }
+    int sr[NI], sc[NI];
+    const int wm = (warp / WCOLS) * 32, wn = (warp % WCOLS) * WN;
+#pragma unroll
+    for (int j = 0; j < NI; ++j) sr[j] = wm, sc[j] = wn + 8 * j;
+    syrk_run<V16, BK, ST, NI>(As, Bs, B, rows, cols, ra, rb, diag, s0, s1, L.nslab, sr, sc,
+                              diag && wn >= wm + 32, out);
 }
 
 // Kernel shapes (k slab BK, pipeline stages ST); TCB_GRAM_VARIANT picks one
 // for measurement, the default is the fastest on the c2 Gram.
 struct SyrkVariant {
     int bk, st, threads;
-    void (*k16)(const double*, u64, u64, int, u64, u64, u64, double*);
-    void (*k8)(const double*, u64, u64, int, u64, u64, u64, double*);
+    void (*k16)(const double*, u64, u64, SyrkLaunch, double*);
+    void (*k8)(const double*, u64, u64, SyrkLaunch, double*);
     int smem() const { return 2 * st * GT * (bk + 4) * static_cast<int>(sizeof(double)); }
 };
 #define TCB_SYRK(BK, ST, WN) {BK, ST, WN == 16 ? 256 : 128, syrk_kernel<true, BK, ST, WN>, syrk_kernel<false, BK, ST, WN>}
@@ -165,22 +225,26 @@ const SyrkVariant kSyrk[] = {
 };
 #undef TCB_SYRK
 constexpr int kSyrkVariants = sizeof(kSyrk) / sizeof(kSyrk[0]);
-constexpr int kSyrkDefault = 7;
+constexpr int kSyrkDefault = 6;
 
 // fixed-order split reduction (split 0, 1, ...); writes the full symmetric G (row-major)
-__global__ void syrk_reduce(const double* __restrict__ ws, int splits, int ntiles_lower, u64 rows,
-                            double* __restrict__ G) {
+__global__ void syrk_reduce(const double* __restrict__ ws, int splits_o, int splits_d, int n_off, int n_diag,
+                            u64 rows, double* __restrict__ G) {
     const int tile = blockIdx.x;
     const int e0 = blockIdx.y * (GT * GT / 16), e1 = e0 + GT * GT / 16;
     int ti = 0;
     while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
     const int tj = tile - ti * (ti + 1) / 2;
+    const bool diag = ti == tj;
+    const int splits = diag ? splits_d : splits_o;
+    const u64 base = diag ? static_cast<u64>(splits_o) * n_off + ti : static_cast<u64>(ti * (ti - 1) / 2 + tj);
+    const u64 stride = diag ? n_diag : n_off;
     for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
         const int m = e / GT, n = e % GT;
         const u64 gi = static_cast<u64>(ti) * GT + m, gj = static_cast<u64>(tj) * GT + n;
         if (gi >= rows || gj >= rows || gj > gi) continue;
         double s = 0.0;
-        for (int sp = 0; sp < splits; ++sp) s += ws[(static_cast<u64>(sp) * ntiles_lower + tile) * GT * GT + e];
+        for (int sp = 0; sp < splits; ++sp) s += ws[(base + sp * stride) * GT * GT + e];
         G[gi * rows + gj] = s;
         G[gj * rows + gi] = s;
     }
@@ -359,35 +423,71 @@ GramPlan gram_plan(const double* B, u64 rows, u64 cols) {
     gp.bk = kSyrk[variant].bk;
     const int nt = static_cast<int>((rows + GT - 1) / GT);
     gp.lower = nt * (nt + 1) / 2;
+    gp.n_diag = nt;
+    gp.n_off = gp.lower - nt;
     gp.nslab = (cols + gp.bk - 1) / gp.bk;
     gp.v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+    // DMMA per warp and k step, off / on the diagonal: 32x32-warp kernels spread
+    // a diagonal tile's 3 lower blocks over all 4 warps (16 vs 12).  With
+    // TCB_GRAM_DIAG_BALANCE=1 diagonal CTAs take 4/3 the slabs (equal DMMA per
+    // CTA); by default every CTA takes the same slabs and the diagonal CTAs'
+    // lighter warps leave DMMA issue slots to co-resident CTAs (measured
+    // equal or faster on the c2 Gram: profiles/gram_variants_r01.txt).
+    static const bool balance = [] {
+        const char* e = std::getenv("TCB_GRAM_DIAG_BALANCE");
+        return e && *e && *e != '0';
+    }();
+    const u64 w_o = 4, w_d = (kSyrk[variant].threads == 128 && balance) ? 3 : 4;
     const u64 slots = static_cast<u64>(per_sm) * sm_count();
-    u64 splits = std::max<u64>(1, std::min<u64>(gp.nslab, slots / gp.lower));
-    gp.per = (gp.nslab + splits - 1) / splits;
+    auto ctas = [&](u64 po) {
+        const u64 pd = (po * w_o + w_d - 1) / w_d;
+        return gp.n_off * ((gp.nslab + po - 1) / po) + gp.n_diag * ((gp.nslab + pd - 1) / pd);
+    };
+    u64 po = std::max<u64>(1, (gp.nslab * (gp.n_off * w_o + gp.n_diag * w_d)) / (w_o * slots));
+    while (po < gp.nslab && ctas(po) > slots) ++po;
+    gp.per = po;
+    gp.per_d = std::min<u64>(gp.nslab, (po * w_o + w_d - 1) / w_d);
     gp.splits = (gp.nslab + gp.per - 1) / gp.per;
+    gp.splits_d = (gp.nslab + gp.per_d - 1) / gp.per_d;
     return gp;
 }
 
-u64 gram_ws_doubles(const GramPlan& gp) { return gp.splits * gp.lower * GT * GT; }
+u64 gram_ws_doubles(const GramPlan& gp) {
+    return (gp.splits * gp.n_off + gp.splits_d * gp.n_diag) * GT * GT;
+}
 
 u64 gram_split_col(const GramPlan& gp, u64 split, u64 cols) {
     return std::min<u64>(cols, split * gp.per * static_cast<u64>(gp.bk));
 }
 
+// Off-diagonal splits [sp0, sp1) plus the diagonal splits whose columns end
+// inside (col(sp0), col(sp1)] — every one of them reads only columns below
+// col(sp1), and consecutive ranges launch each diagonal split exactly once.
 void gram_splits(const double* B, u64 rows, u64 cols, const GramPlan& gp, u64 sp0, u64 sp1, double* ws,
                  cudaStream_t s) {
     if (sp1 <= sp0) return;
+    const u64 c0 = gram_split_col(gp, sp0, cols), c1 = sp1 >= gp.splits ? cols : gram_split_col(gp, sp1, cols);
+    const u64 dcols = gp.per_d * static_cast<u64>(gp.bk);
+    auto dend = [&](u64 d) { return std::min<u64>(cols, (d + 1) * dcols); };
+    u64 sd0 = 0;
+    if (sp0 > 0)
+        while (sd0 < gp.splits_d && dend(sd0) <= c0) ++sd0;
+    u64 sd1 = sd0;
+    while (sd1 < gp.splits_d && dend(sd1) <= c1) ++sd1;
     ProfScope prof_scope(kGram, s);
     const SyrkVariant& k = kSyrk[gp.variant];
-    const unsigned grid = static_cast<unsigned>((sp1 - sp0) * gp.lower);
-    (gp.v16 ? k.k16 : k.k8)<<<grid, k.threads, k.smem(), s>>>(B, rows, cols, gp.lower, gp.per, gp.nslab, sp0, ws);
+    SyrkLaunch L{gp.n_off, gp.n_diag, gp.per, gp.per_d, gp.nslab, sp0, sd0, gp.splits, (sp1 - sp0) * gp.n_off};
+    const unsigned grid = static_cast<unsigned>(L.off_ctas + (sd1 - sd0) * gp.n_diag);
+    if (grid == 0) return;
+    (gp.v16 ? k.k16 : k.k8)<<<grid, k.threads, k.smem(), s>>>(B, rows, cols, L, ws);
     count_launch();
     TCB_LAUNCH();
 }
 
 void gram_reduce(const GramPlan& gp, const double* ws, u64 rows, double* G, cudaStream_t s) {
     ProfScope prof_scope(kGram, s);
-    syrk_reduce<<<dim3(gp.lower, 16), 256, 0, s>>>(ws, static_cast<int>(gp.splits), gp.lower, rows, G);
+    syrk_reduce<<<dim3(gp.lower, 16), 256, 0, s>>>(ws, static_cast<int>(gp.splits), static_cast<int>(gp.splits_d),
+                                                   gp.n_off, gp.n_diag, rows, G);
     count_launch();
     TCB_LAUNCH();
 }

@@ -39,6 +39,8 @@ struct GramPlan {
     u64 nslab = 0, per = 0, splits = 0;
     bool v16 = false;
     int variant = 0, bk = 32;  // SYRK kernel shape (gemm.cu kSyrk)
+    int n_off = 0, n_diag = 0;  // lower-triangle tiles off / on the diagonal
+    u64 per_d = 0, splits_d = 0;  // diagonal tiles' slabs per CTA and split count (per, splits: off-diagonal)
 };
 GramPlan gram_plan(const double* B, u64 rows, u64 cols);
 u64 gram_ws_doubles(const GramPlan& gp);
