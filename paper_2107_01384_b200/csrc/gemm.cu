@@ -243,8 +243,19 @@ __global__ void syrk_reduce(const double* __restrict__ ws, int splits_o, int spl
         const int m = e / GT, n = e % GT;
         const u64 gi = static_cast<u64>(ti) * GT + m, gj = static_cast<u64>(tj) * GT + n;
         if (gi >= rows || gj >= rows || gj > gi) continue;
+        // partials fetched 8 at a time (independent loads in flight), summed in split order
+        const double* p = ws + base * GT * GT + e;
+        const u64 step = stride * GT * GT;
         double s = 0.0;
-        for (int sp = 0; sp < splits; ++sp) s += ws[(base + sp * stride) * GT * GT + e];
+        int sp = 0;
+        for (; sp + 8 <= splits; sp += 8) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = __ldcs(p + (sp + q) * step);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s += v[q];
+        }
+        for (; sp < splits; ++sp) s += __ldcs(p + sp * step);
         G[gi * rows + gj] = s;
         G[gj * rows + gi] = s;
     }
