@@ -505,7 +505,7 @@ def main():
             eig_flop += 4.0 / 3.0 * n_eig ** 3 + 2.0 * n_eig * n_eig * res.ranks[mode]
         cur = cur[1:] + [res.ranks[mode]]
     roof["note"] = ("ncu launch-list shares for this command (profiles/launches_*_summary.txt): the encoder's "
-                    "ac_kernel, syrk_kernel and tk_cluster are each ~13-14 %; of the 5 ac_kernel launches per "
+                    "syrk_kernel (incl. the 5 live-timed mode-0 launches), ac_kernel and tk_cluster are each ~14-18 %; of the 5 ac_kernel launches per "
                     "compress only the core finalisation's is on the critical path (the probe and the factor "
                     "streams run on side streams), so the Gram is the dominant critical-path kernel")
     roof["eig"] = {"kernel": "tk_cluster (one 8-CTA cluster launch per mode)", "flop": eig_flop,
