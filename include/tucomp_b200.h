@@ -179,6 +179,22 @@ int tcb_encode(const uint64_t* mag, const uint8_t* neg, uint64_t n, double targe
                uint64_t block_size, int split, int fixed_plane, uint8_t** stream, uint64_t* stream_len,
                int* last_plane, double* achieved_sse_int, uint64_t* decoded, int* uncertified);
 
+/* The encoder's serial double sums, bit-exact (exact.cu): for every kind k and
+ * segment g, s = seg_s0[g]; for each element of [seg_lo, seg_hi) (descending
+ * when seg_backward) s = fl(s + term_k(element)); with a finite seg_need the
+ * scan stops after the first element that brings s to >= need (place_stops).
+ * Terms (kind_term): 0 lead gain, 1 trail gain, 2 both (non-split scan) at
+ * kind_plane -- build_block's statistics, core_codec.cpp:131-155, 268-341;
+ * 3 (double)m^2 -- backward_sum_sse, error_model.cpp:34-41; 4 recalibrate_sse's
+ * term, error_model.cpp:54-72; 5 (m - dec)^2 -- core_codec.cpp:405-411.
+ * Outputs indexed k * nseg + g; c0 / c1 count lead / trail positions (lead
+ * kind: c1 = new ones) up to the crossing.  reference != 0: the plain
+ * one-thread serial chain (verification). */
+int tcb_exact_sums(const uint64_t* mag, const uint64_t* dec, uint64_t n, const uint64_t* seg_lo,
+                   const uint64_t* seg_hi, const int* seg_backward, const double* seg_s0, const double* seg_need,
+                   int nseg, const int* kind_term, const int* kind_plane, int nk, int reference, double* sums,
+                   uint64_t* c0, uint64_t* c1, int* crossed);
+
 /* entropy::encode_symbols (entropy.cpp:429-445) for one symbol sequence. */
 int tcb_encode_symbols(int coder, const uint64_t* syms, uint64_t n, uint8_t** out, uint64_t* len);
 

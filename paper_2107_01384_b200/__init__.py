@@ -484,6 +484,37 @@ def encode(mag, neg, target_int, coder=0, block_size=0, split=True, fixed_plane=
     return _take_bytes(out, ln.value), lp.value, ach.value, dec[:n], unc.value
 
 
+EX_LEAD, EX_TRAIL, EX_BOTH, EX_SQ, EX_RECAL, EX_DIFF = range(6)
+
+
+def exact_sums(mag, segs, kinds, dec=None, reference=False):
+    """The encoder's serial double sums, bit-exact (tcb_exact_sums).  segs: list of
+    (lo, hi, backward, s0, need) with need=inf for a plain sum; kinds: list of
+    (term, plane).  Returns (sums, c0, c1, crossed), each of shape (len(kinds), len(segs))."""
+    mag = np.ascontiguousarray(mag, np.uint64)
+    n = mag.size
+    d = None if dec is None else np.ascontiguousarray(dec, np.uint64)
+    g = len(segs)
+    lo = np.array([x[0] for x in segs], np.uint64)
+    hi = np.array([x[1] for x in segs], np.uint64)
+    bw = np.array([int(x[2]) for x in segs], np.int32)
+    s0 = np.array([float(x[3]) for x in segs], np.float64)
+    nd = np.array([float(x[4]) for x in segs], np.float64)
+    kt = np.array([k[0] for k in kinds], np.int32)
+    kp = np.array([k[1] for k in kinds], np.int32)
+    nj = max(1, g * len(kinds))
+    sums = np.zeros(nj, np.float64)
+    c0 = np.zeros(nj, np.uint64)
+    c1 = np.zeros(nj, np.uint64)
+    cr = np.zeros(nj, np.int32)
+    _check(lib().tcb_exact_sums(_p(mag) if n else None, _p(d) if d is not None else None, C.c_uint64(n), _p(lo), _p(hi),
+                                _p(bw), _p(s0), _p(nd), g, _p(kt), _p(kp), len(kinds), int(reference), _p(sums),
+                                _p(c0), _p(c1), _p(cr)))
+    shp = (len(kinds), g)
+    nj = g * len(kinds)
+    return sums[:nj].reshape(shp), c0[:nj].reshape(shp), c1[:nj].reshape(shp), cr[:nj].reshape(shp)
+
+
 def encode_symbols(coder, syms) -> bytes:
     s = np.ascontiguousarray(syms, np.uint64)
     out = C.POINTER(C.c_uint8)()
@@ -516,4 +547,4 @@ EXPORTED = ("tcb_compress", "tcb_compress_device", "tcb_decompress", "tcb_decomp
             "tcb_nccl_unique_id", "tcb_nccl_comm_init", "tcb_nccl_comm_destroy", "tcb_compress_sharded_device", "tcb_measure_error",
             "tcb_default_params", "tcb_free", "tcb_last_error",
             "tcb_kernel_launches", "tcb_sthosvd_f64", "tcb_gram_f64", "tcb_ttm_f64", "tcb_eig_f64",
-            "tcb_quantize_f64", "tcb_encode", "tcb_encode_symbols", "tcb_encode_factor_f64")
+            "tcb_quantize_f64", "tcb_encode", "tcb_exact_sums", "tcb_encode_symbols", "tcb_encode_factor_f64")

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "../../include/tucomp_b200.h"
+#include "exact.cuh"
 #include "codec.cuh"
 #include "kernels.cuh"
 #include "decode.cuh"
@@ -739,14 +740,45 @@ int tcb_encode(const uint64_t* mag, const uint8_t* neg, uint64_t n, double targe
         if (fixed_plane >= 0) o.fixed_plane = fixed_plane;
         const PlanResult pl = plan_stream(m.p, n, target, o, dec.p, st.s);
         const auto body = finalize_stream(m.p, ng.p, n, pl, coder, n, st.s);
-        const SumRec a = n ? device_sum(SumKind::diff_backward, m.p, dec.p, n, 0, st.s) : SumRec{0, 0, 0, 0};
+        const double a = exact_backward_sum(kExDiff, 0, m.p, dec.p, n, st.s);
         if (decoded) dec.download(decoded, n);
         stream_sync(st.s);
         *stream = dup(body);
         *stream_len = body.size();
         *last_plane = pl.last_plane;
-        *achieved = a.hi + a.lo;
+        *achieved = a;
         if (uncertified) *uncertified = pl.fallbacks;
+    });
+}
+
+int tcb_exact_sums(const uint64_t* mag, const uint64_t* dec, uint64_t n, const uint64_t* seg_lo,
+                   const uint64_t* seg_hi, const int* seg_backward, const double* seg_s0, const double* seg_need,
+                   int nseg, const int* kind_term, const int* kind_plane, int nk, int reference, double* sums,
+                   uint64_t* c0, uint64_t* c1, int* crossed) {
+    return guard([&] {
+        Stream st;
+        DevBuf<u64> m(n + 1, st.s), d(n + 1, st.s);
+        m.upload(mag, n);
+        if (dec) d.upload(dec, n);
+        std::vector<ExSeg> segs(nseg);
+        for (int g = 0; g < nseg; ++g) {
+            if (seg_hi[g] < seg_lo[g] || seg_hi[g] > n) throw Error("exact sums: segment out of range");
+            segs[g] = ExSeg{seg_lo[g], seg_hi[g], seg_backward[g], seg_s0[g], seg_need[g]};
+        }
+        std::vector<ExKind> kinds(nk);
+        for (int k = 0; k < nk; ++k) {
+            if (kind_term[k] < 0 || kind_term[k] > kExDiff || kind_plane[k] < 0 || kind_plane[k] > 64)
+                throw Error("exact sums: bad kind");
+            kinds[k] = ExKind{kind_term[k], kind_plane[k]};
+        }
+        const auto out = reference ? exact_serial_reference(m.p, dec ? d.p : nullptr, segs, kinds, st.s)
+                                   : exact_serial(m.p, dec ? d.p : nullptr, segs, kinds, st.s);
+        for (std::size_t j = 0; j < out.size(); ++j) {
+            sums[j] = out[j].sum;
+            c0[j] = out[j].c0;
+            c1[j] = out[j].c1;
+            crossed[j] = out[j].crossed;
+        }
     });
 }
 

@@ -1,0 +1,654 @@
+// Exact parallel evaluation of the reference encoder's serial double sums
+// (see exact.cuh for the method).  Reference loops reproduced:
+//   backward_sum_sse      error_model.cpp:34-41   (kExSq, backward)
+//   recalibrate_sse       error_model.cpp:54-72   (kExRecal, backward)
+//   build_block stats     core_codec.cpp:131-155  (kExLead / kExTrail, per block, forward)
+//   place_stops scans     core_codec.cpp:268-341  (crossing: first s >= need)
+//   finalize achieved SSE core_codec.cpp:405-411  (kExDiff, backward)
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+
+#include "exact.cuh"
+#include "terms.cuh"
+
+namespace tcb {
+
+namespace {
+
+constexpr long long kBig = 1LL << 62;        // "no partial sum" sentinel for min/max
+constexpr long long kLim = 1LL << 56;        // |increment| beyond any region's width: reject
+constexpr long long kAMax = (1LL << 53) - 1;  // strict interior of a region, in units
+constexpr long long kAMin = (1LL << 52) + 1;
+constexpr int kExThreads = 256;
+
+struct DevSeg {
+    u64 lo, hi;
+    double s0, need;
+    int backward;
+    int pad;
+};
+
+// Summary of a run of terms for one region: per start parity pi, the total
+// increment K (in units), the min / max partial increment after each nonzero
+// term (kBig / -kBig when none), and the end parity (bit pi of q).
+struct Fn {
+    long long K0, K1, mn0, mn1, mx0, mx1;
+    int q;
+    int bad;
+};
+
+struct ExRec {  // pass-2 table entry for one (kind, chunk): 64 bytes
+    long long K0, K1, mn0, mn1, mx0, mx1;
+    int rid;
+    int qbad;  // q | bad << 2
+    u32 c0, c1;
+};
+
+__device__ __forceinline__ Fn fn_id() { return Fn{0, 0, kBig, kBig, -kBig, -kBig, 2, 0}; }
+
+__device__ __forceinline__ Fn fn_then(const Fn& f, const Fn& g) {  // f first, then g
+    const int m0 = f.q & 1, m1 = (f.q >> 1) & 1;
+    Fn h;
+    const long long gK0 = m0 ? g.K1 : g.K0, gn0 = m0 ? g.mn1 : g.mn0, gx0 = m0 ? g.mx1 : g.mx0;
+    const long long gK1 = m1 ? g.K1 : g.K0, gn1 = m1 ? g.mn1 : g.mn0, gx1 = m1 ? g.mx1 : g.mx0;
+    h.K0 = f.K0 + gK0;
+    h.K1 = f.K1 + gK1;
+    h.mn0 = min(f.mn0, f.K0 + gn0);
+    h.mn1 = min(f.mn1, f.K1 + gn1);
+    h.mx0 = max(f.mx0, f.K0 + gx0);
+    h.mx1 = max(f.mx1, f.K1 + gx1);
+    h.q = ((g.q >> m0) & 1) | (((g.q >> m1) & 1) << 1);
+    h.bad = f.bad | g.bad | (llabs(h.K0) > kLim) | (llabs(h.K1) > kLim);
+    if (h.bad) h.K0 = h.K1 = 0;  // keep the (discarded) arithmetic in range
+    return h;
+}
+
+// Region of a running sum: e = exponent of |s| for |s| >= 2^53 (signed: the
+// sign is part of the region), 52 for |s| < 2^53 (integers: exact).
+__device__ __forceinline__ int region_of(double s) {
+    const u64 b = static_cast<u64>(__double_as_longlong(s));
+    const int e = static_cast<int>((b >> 52) & 0x7ff) - 1023;
+    if (e <= 52) return 52;
+    return (b >> 63) ? -e : e;
+}
+__device__ __forceinline__ int rexp(int rid) { return rid < 0 ? -rid : rid; }
+__device__ __forceinline__ long long units_of(double s, int rid) {
+    return __double2ll_rz(scalbn(s, 52 - rexp(rid)));
+}
+__device__ __forceinline__ double value_of(long long a, int rid) {
+    return scalbn(static_cast<double>(a), rexp(rid) - 52);
+}
+__device__ __forceinline__ long long lo_bound(int rid) { return rid > 52 ? kAMin : -kAMax; }
+__device__ __forceinline__ long long hi_bound(int rid) { return rid < 0 ? -kAMin : kAMax; }
+
+// t / u for an integer-valued double t and u = 2^(e-52): the round-half-even
+// quotient j, or at an exact tie its floor k (tie = true).  false: |t/u| is
+// too large for any sum to stay in the region.
+__device__ __forceinline__ bool unitize(double t, int e, long long& j, bool& tie) {
+    tie = false;
+    const u64 b = static_cast<u64>(__double_as_longlong(t));
+    const bool neg = b >> 63;
+    const int E = static_cast<int>((b >> 52) & 0x7ff) - 1075;
+    const u64 M = (b & ((u64{1} << 52) - 1)) | (u64{1} << 52);
+    const int sh = (e - 52) - E;
+    if (sh <= 0) {
+        if (sh < -8) return false;
+        const long long q = static_cast<long long>(M << (-sh));
+        j = neg ? -q : q;
+        return true;
+    }
+    if (sh >= 54) {  // |t| < u/2
+        j = 0;
+        return true;
+    }
+    const u64 qq = M >> sh, rem = M & ((u64{1} << sh) - 1), half = u64{1} << (sh - 1);
+    if (rem == half) {
+        tie = true;
+        j = neg ? -static_cast<long long>(qq) - 1 : static_cast<long long>(qq);
+        return true;
+    }
+    const long long r = static_cast<long long>(qq) + (rem > half ? 1 : 0);
+    j = neg ? -r : r;
+    return true;
+}
+
+__device__ __forceinline__ void fn_push(Fn& f, long long j, bool tie) {
+    const int p0 = f.q & 1, p1 = (f.q >> 1) & 1;
+    const int jb = static_cast<int>(j & 1);
+    long long i0 = j, i1 = j;
+    int n0, n1;
+    if (tie) {  // a + k + 1/2 -> the even neighbour
+        i0 += (p0 ^ jb);
+        i1 += (p1 ^ jb);
+        n0 = n1 = 0;
+    } else {
+        n0 = p0 ^ jb;
+        n1 = p1 ^ jb;
+    }
+    f.K0 += i0;
+    f.K1 += i1;
+    f.mn0 = min(f.mn0, f.K0);
+    f.mn1 = min(f.mn1, f.K1);
+    f.mx0 = max(f.mx0, f.K0);
+    f.mx1 = max(f.mx1, f.K1);
+    f.q = n0 | (n1 << 1);
+    if (llabs(f.K0) > kLim || llabs(f.K1) > kLim) {
+        f.bad = 1;
+        f.K0 = f.K1 = 0;
+    }
+}
+
+__device__ __forceinline__ void fn_term(Fn& f, double t, int e) {
+    if (t == 0.0 || f.bad) return;  // s + 0 = s exactly
+    long long j;
+    bool tie;
+    if (!unitize(t, e, j, tie)) {
+        f.bad = 1;
+        f.K0 = f.K1 = 0;
+        return;
+    }
+    fn_push(f, j, tie);
+}
+
+// term of element value v (and decoded value d) for a kind; cat0/cat1: the
+// element's category counts (see ExOut)
+__device__ __forceinline__ double ex_term(int term, int p, u64 v, u64 d, u32& cat0, u32& cat1) {
+    switch (term) {
+        case kExLead: {
+            const int tb = top_bit64(v);
+            cat0 = tb <= p;
+            cat1 = tb == p;
+            return tb == p ? t_lead_gain(v, p) : 0.0;
+        }
+        case kExTrail: {
+            const int tb = top_bit64(v);
+            cat0 = 0;
+            cat1 = tb > p;
+            return tb > p ? t_trail_gain(v, p) : 0.0;
+        }
+        case kExBoth: {
+            const int tb = top_bit64(v);
+            cat0 = tb <= p;
+            cat1 = tb > p;
+            return tb > p ? t_trail_gain(v, p) : (tb == p ? t_lead_gain(v, p) : 0.0);
+        }
+        case kExSq: cat0 = cat1 = 0; return t_insig2(v);
+        case kExRecal: cat0 = cat1 = 0; return t_recal(v, p);
+        default: cat0 = cat1 = 0; return t_diff2(v, d);
+    }
+}
+
+__device__ __forceinline__ u64 elem_index(const DevSeg& g, u64 q) { return g.backward ? g.hi - 1 - q : g.lo + q; }
+
+__device__ __forceinline__ int seg_of(const u64* choff, int nseg, u64 c) {
+    int lo = 0, hi = nseg - 1;  // last g with choff[g] <= c
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(choff + mid) <= c) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ Fn shfl_fn(const Fn& f, int src, bool up_by) {
+    (void)up_by;
+    Fn g;
+    g.K0 = __shfl_sync(0xffffffffu, f.K0, src);
+    g.K1 = __shfl_sync(0xffffffffu, f.K1, src);
+    g.mn0 = __shfl_sync(0xffffffffu, f.mn0, src);
+    g.mn1 = __shfl_sync(0xffffffffu, f.mn1, src);
+    g.mx0 = __shfl_sync(0xffffffffu, f.mx0, src);
+    g.mx1 = __shfl_sync(0xffffffffu, f.mx1, src);
+    g.q = __shfl_sync(0xffffffffu, f.q, src);
+    g.bad = __shfl_sync(0xffffffffu, f.bad, src);
+    return g;
+}
+
+// inclusive warp scan of the composition (lane order = sequence order)
+__device__ __forceinline__ Fn warp_scan_fn(Fn f) {
+    const int lane = threadIdx.x & 31;
+    for (int o = 1; o < 32; o <<= 1) {
+        const Fn g = shfl_fn(f, lane >= o ? lane - o : lane, true);
+        if (lane >= o) f = fn_then(g, f);
+    }
+    return f;
+}
+
+// ---------------------------------------------------------------- pass 1: approximate chunk sums
+template <int PER>
+__global__ void __launch_bounds__(kExThreads) ex_approx_kernel(const u64* __restrict__ m, const u64* __restrict__ dec,
+                                                               const DevSeg* __restrict__ segs, int nseg,
+                                                               const u64* __restrict__ choff,
+                                                               const ExKind* __restrict__ kinds, int nk, u64 nch,
+                                                               double* __restrict__ A) {
+    constexpr u64 C = static_cast<u64>(kExThreads) * PER;
+    __shared__ double red[kExThreads / 32];
+    const u64 c = blockIdx.x;
+    const int g = seg_of(choff, nseg, c);
+    const DevSeg sg = segs[g];
+    const u64 len = sg.hi - sg.lo;
+    const u64 q0 = (c - choff[g]) * C + static_cast<u64>(threadIdx.x) * PER;
+    u64 v[PER], dv[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+        const u64 q = q0 + e;
+        v[e] = q < len ? m[elem_index(sg, q)] : 0;
+        dv[e] = (dec && q < len) ? dec[elem_index(sg, q)] : 0;
+    }
+    for (int k = 0; k < nk; ++k) {
+        const ExKind kd = kinds[k];
+        double acc = 0.0;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            u32 a0, a1;
+            if (q0 + e < len) acc += ex_term(kd.term, kd.plane, v[e], dv[e], a0, a1);
+        }
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < kExThreads / 32; ++w) t += red[w];
+            A[static_cast<u64>(k) * nch + c] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// exclusive prefix (plus s0) of the approximate chunk sums of each (kind, segment)
+__global__ void __launch_bounds__(1024) ex_scan_kernel(const DevSeg* __restrict__ segs, int nseg,
+                                                       const u64* __restrict__ choff, u64 nch,
+                                                       const double* __restrict__ A, double* __restrict__ P) {
+    __shared__ double sh[32];
+    __shared__ double carry_s;
+    const int k = blockIdx.x / nseg, g = blockIdx.x % nseg;
+    const u64 b0 = choff[g], b1 = choff[g + 1];
+    const double* a = A + static_cast<u64>(k) * nch;
+    double* p = P + static_cast<u64>(k) * nch;
+    if (threadIdx.x == 0) carry_s = segs[g].s0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (u64 t0 = b0; t0 < b1; t0 += blockDim.x) {
+        const u64 i = t0 + threadIdx.x;
+        const double x = i < b1 ? a[i] : 0.0;
+        double y = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double z = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += z;
+        }
+        if (lane == 31) sh[w] = y;
+        __syncthreads();
+        if (w == 0) {
+            double z = lane < static_cast<int>(blockDim.x >> 5) ? sh[lane] : 0.0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const double zz = __shfl_up_sync(0xffffffffu, z, o);
+                if (lane >= o) z += zz;
+            }
+            sh[lane] = z;  // inclusive warp totals
+        }
+        __syncthreads();
+        const double carry = carry_s;
+        const double excl = carry + (w > 0 ? sh[w - 1] : 0.0) + (y - x);
+        if (i < b1) p[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == 0) carry_s = carry + sh[(blockDim.x >> 5) - 1];
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- pass 2: chunk functions
+template <int PER>
+__global__ void __launch_bounds__(kExThreads) ex_fn_kernel(const u64* __restrict__ m, const u64* __restrict__ dec,
+                                                           const DevSeg* __restrict__ segs, int nseg,
+                                                           const u64* __restrict__ choff,
+                                                           const ExKind* __restrict__ kinds, int nk, u64 nch,
+                                                           const double* __restrict__ P, ExRec* __restrict__ out) {
+    constexpr u64 C = static_cast<u64>(kExThreads) * PER;
+    __shared__ Fn wf[kExThreads / 32];
+    __shared__ u32 wc[2][kExThreads / 32];
+    const u64 c = blockIdx.x;
+    const int g = seg_of(choff, nseg, c);
+    const DevSeg sg = segs[g];
+    const u64 len = sg.hi - sg.lo;
+    const u64 q0 = (c - choff[g]) * C + static_cast<u64>(threadIdx.x) * PER;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    u64 v[PER], dv[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+        const u64 q = q0 + e;
+        v[e] = q < len ? m[elem_index(sg, q)] : 0;
+        dv[e] = (dec && q < len) ? dec[elem_index(sg, q)] : 0;
+    }
+    for (int k = 0; k < nk; ++k) {
+        const ExKind kd = kinds[k];
+        const int rid = region_of(P[static_cast<u64>(k) * nch + c]);
+        const int e = rexp(rid);
+        Fn f = fn_id();
+        u32 x0 = 0, x1 = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            if (q0 + i >= len) break;
+            u32 a0, a1;
+            const double t = ex_term(kd.term, kd.plane, v[i], dv[i], a0, a1);
+            x0 += a0;
+            x1 += a1;
+            fn_term(f, t, e);
+        }
+        // ordered reduction: lane l (aligned) absorbs [l + o, l + 2o)
+        for (int o = 1; o < 32; o <<= 1) {
+            const Fn h = shfl_fn(f, (lane + o) & 31, false);
+            if ((lane & (2 * o - 1)) == 0) f = fn_then(f, h);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            x0 += __shfl_down_sync(0xffffffffu, x0, o);
+            x1 += __shfl_down_sync(0xffffffffu, x1, o);
+        }
+        if (lane == 0) {
+            wf[w] = f;
+            wc[0][w] = x0;
+            wc[1][w] = x1;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            Fn t = wf[0];
+            u32 y0 = wc[0][0], y1 = wc[1][0];
+            for (int ww = 1; ww < kExThreads / 32; ++ww) {
+                t = fn_then(t, wf[ww]);
+                y0 += wc[0][ww];
+                y1 += wc[1][ww];
+            }
+            ExRec r;
+            r.K0 = t.K0;
+            r.K1 = t.K1;
+            r.mn0 = t.mn0;
+            r.mn1 = t.mn1;
+            r.mx0 = t.mx0;
+            r.mx1 = t.mx1;
+            r.rid = rid;
+            r.qbad = t.q | (t.bad << 2);
+            r.c0 = y0;
+            r.c1 = y1;
+            out[static_cast<u64>(k) * nch + c] = r;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- the walk
+struct WalkState {
+    double s;
+    u64 c0, c1;
+    int crossed;
+};
+
+// Warp-cooperative exact resolution of processing positions [q, q1) of one
+// segment: 8-term functions per lane for the current region, composed by a
+// warp scan; the lanes before the first rejected one are applied at once, the
+// rejected lane's terms are added serially.
+__device__ void ex_fine(const u64* __restrict__ m, const u64* __restrict__ dec, const ExKind kd, const DevSeg& sg,
+                        u64 q, u64 q1, WalkState& st) {
+    const int lane = threadIdx.x & 31;
+    const bool xing = sg.need < HUGE_VAL;
+    while (q < q1 && !st.crossed) {
+        const int rid = region_of(st.s);
+        const long long a = units_of(st.s, rid);
+        const int pi0 = static_cast<int>(a & 1);
+        const u64 lb = q + 8ull * lane, le = min(lb + 8, q1);
+        Fn f = fn_id();
+        u32 x0 = 0, x1 = 0;
+        for (u64 qq = lb; qq < le; ++qq) {
+            const u64 idx = elem_index(sg, qq);
+            u32 a0, a1;
+            const double t = ex_term(kd.term, kd.plane, m[idx], dec ? dec[idx] : 0, a0, a1);
+            x0 += a0;
+            x1 += a1;
+            fn_term(f, t, rexp(rid));
+        }
+        const Fn incl = warp_scan_fn(f);
+        Fn ex = shfl_fn(incl, lane > 0 ? lane - 1 : 0, true);
+        if (lane == 0) ex = fn_id();
+        const long long al = a + (pi0 ? ex.K1 : ex.K0);
+        const int pil = (ex.q >> pi0) & 1;
+        const long long rn = pil ? f.mn1 : f.mn0, rx = pil ? f.mx1 : f.mx0;
+        bool ok = !f.bad && !ex.bad && al + rn >= lo_bound(rid) && al + rx <= hi_bound(rid);
+        if (ok && xing && rx > -kBig && value_of(al + rx, rid) >= sg.need) ok = false;
+        const unsigned bm = __ballot_sync(0xffffffffu, !ok);
+        const int b = bm ? __ffs(bm) - 1 : 32;
+        if (b > 0) {
+            const long long inc = __shfl_sync(0xffffffffu, pi0 ? incl.K1 : incl.K0, b - 1);
+            st.s = value_of(a + inc, rid);
+            u32 y0 = lane < b ? x0 : 0, y1 = lane < b ? x1 : 0;
+            for (int o = 16; o > 0; o >>= 1) {
+                y0 += __shfl_xor_sync(0xffffffffu, y0, o);
+                y1 += __shfl_xor_sync(0xffffffffu, y1, o);
+            }
+            st.c0 += y0;
+            st.c1 += y1;
+        }
+        if (b == 32) {
+            q += 256;
+            continue;
+        }
+        // lane b's terms one at a time (every lane redundantly: identical state)
+        const u64 sb = q + 8ull * b, se = min(sb + 8, q1);
+        for (u64 qq = sb; qq < se; ++qq) {
+            const u64 idx = elem_index(sg, qq);
+            u32 a0, a1;
+            const double t = ex_term(kd.term, kd.plane, m[idx], dec ? dec[idx] : 0, a0, a1);
+            st.c0 += a0;
+            st.c1 += a1;
+            st.s = __dadd_rn(st.s, t);
+            if (xing && st.s >= sg.need) {
+                st.crossed = 1;
+                break;
+            }
+        }
+        q = se;
+    }
+}
+
+template <int PER>
+__global__ void __launch_bounds__(128) ex_walk_kernel(const u64* __restrict__ m, const u64* __restrict__ dec,
+                                                      const DevSeg* __restrict__ segs, int nseg,
+                                                      const u64* __restrict__ choff, const ExKind* __restrict__ kinds,
+                                                      int njobs, u64 nch, const ExRec* __restrict__ recs,
+                                                      ExOut* __restrict__ out) {
+    constexpr u64 C = static_cast<u64>(kExThreads) * PER;
+    const int job = static_cast<int>((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    if (job >= njobs) return;
+    const int lane = threadIdx.x & 31;
+    const int k = job / nseg, g = job % nseg;
+    const ExKind kd = kinds[k];
+    const DevSeg sg = segs[g];
+    const bool xing = sg.need < HUGE_VAL;
+    WalkState st{sg.s0, 0, 0, 0};
+    const u64 len = sg.hi - sg.lo;
+    if (xing && st.s >= sg.need) {
+        st.crossed = 1;
+    } else if (recs && len > 0) {
+        const u64 nc = (len + C - 1) / C;
+        const ExRec* rk = recs + static_cast<u64>(k) * nch + choff[g];
+        for (u64 c = 0; c < nc && !st.crossed;) {
+            const int rid = region_of(st.s);
+            const long long a = units_of(st.s, rid);
+            const int pi0 = static_cast<int>(a & 1);
+            const u64 cc = c + lane;
+            const bool have = cc < nc;
+            ExRec r;
+            if (have) r = rk[cc];
+            Fn f = fn_id();
+            bool pre = false;
+            if (have) {
+                f = Fn{r.K0, r.K1, r.mn0, r.mn1, r.mx0, r.mx1, r.qbad & 3, (r.qbad >> 2) & 1};
+                pre = r.rid == rid && !f.bad;
+                if (!pre) f = fn_id();
+            } else {
+                r.c0 = r.c1 = 0;
+            }
+            const Fn incl = warp_scan_fn(f);
+            Fn ex = shfl_fn(incl, lane > 0 ? lane - 1 : 0, true);
+            if (lane == 0) ex = fn_id();
+            const long long al = a + (pi0 ? ex.K1 : ex.K0);
+            const int pil = (ex.q >> pi0) & 1;
+            const long long rn = pil ? f.mn1 : f.mn0, rx = pil ? f.mx1 : f.mx0;
+            bool ok = pre && !ex.bad && al + rn >= lo_bound(rid) && al + rx <= hi_bound(rid);
+            if (ok && xing && rx > -kBig && value_of(al + rx, rid) >= sg.need) ok = false;
+            const unsigned bm = __ballot_sync(0xffffffffu, !ok);
+            const int b = bm ? __ffs(bm) - 1 : 32;
+            if (b > 0) {
+                const long long inc = __shfl_sync(0xffffffffu, pi0 ? incl.K1 : incl.K0, b - 1);
+                st.s = value_of(a + inc, rid);
+                u32 y0 = lane < b ? r.c0 : 0, y1 = lane < b ? r.c1 : 0;
+                for (int o = 16; o > 0; o >>= 1) {
+                    y0 += __shfl_xor_sync(0xffffffffu, y0, o);
+                    y1 += __shfl_xor_sync(0xffffffffu, y1, o);
+                }
+                st.c0 += y0;
+                st.c1 += y1;
+            }
+            c += b;
+            if (b < 32 && c < nc) {
+                ex_fine(m, dec, kd, sg, c * C, min((c + 1) * C, len), st);
+                c += 1;
+            }
+        }
+    } else if (len > 0) {
+        ex_fine(m, dec, kd, sg, 0, len, st);
+    }
+    if (lane == 0) out[job] = ExOut{st.s, st.c0, st.c1, st.crossed};
+}
+
+// one thread per job: the plain serial loop (verification only)
+__global__ void ex_serial_kernel(const u64* __restrict__ m, const u64* __restrict__ dec,
+                                 const DevSeg* __restrict__ segs, int nseg, const ExKind* __restrict__ kinds,
+                                 int njobs, ExOut* __restrict__ out) {
+    const int job = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
+    if (job >= njobs) return;
+    const int k = job / nseg, g = job % nseg;
+    const ExKind kd = kinds[k];
+    const DevSeg sg = segs[g];
+    const bool xing = sg.need < HUGE_VAL;
+    ExOut o{sg.s0, 0, 0, 0};
+    if (xing && o.sum >= sg.need) {
+        o.crossed = 1;
+    } else {
+        for (u64 q = 0; q < sg.hi - sg.lo; ++q) {
+            const u64 idx = elem_index(sg, q);
+            u32 a0, a1;
+            const double t = ex_term(kd.term, kd.plane, m[idx], dec ? dec[idx] : 0, a0, a1);
+            o.c0 += a0;
+            o.c1 += a1;
+            o.sum = __dadd_rn(o.sum, t);
+            if (xing && o.sum >= sg.need) {
+                o.crossed = 1;
+                break;
+            }
+        }
+    }
+    out[job] = o;
+}
+
+struct Prepared {
+    std::vector<DevSeg> hs;
+    std::vector<u64> choff;
+    DevBuf<DevSeg> segs;
+    DevBuf<u64> dch;
+    DevBuf<ExKind> dk;
+    u64 nch = 0, maxlen = 0;
+};
+
+Prepared prepare(const std::vector<ExSeg>& segs, const std::vector<ExKind>& kinds, u64 C, cudaStream_t s) {
+    Prepared p;
+    p.hs.resize(segs.size());
+    p.choff.assign(segs.size() + 1, 0);
+    for (std::size_t g = 0; g < segs.size(); ++g) {
+        const ExSeg& e = segs[g];
+        if (e.hi < e.lo) throw Error("exact sum: bad segment");
+        p.hs[g] = DevSeg{e.lo, e.hi, e.s0, e.need, e.backward, 0};
+        const u64 len = e.hi - e.lo;
+        p.maxlen = std::max(p.maxlen, len);
+        p.choff[g + 1] = p.choff[g] + (len + C - 1) / C;
+    }
+    p.nch = p.choff.back();
+    p.segs = DevBuf<DevSeg>(segs.size(), s);
+    p.segs.upload(p.hs.data(), segs.size());
+    p.dch = DevBuf<u64>(segs.size() + 1, s);
+    p.dch.upload(p.choff.data(), segs.size() + 1);
+    p.dk = DevBuf<ExKind>(kinds.size(), s);
+    p.dk.upload(kinds.data(), kinds.size());
+    return p;
+}
+
+template <int PER>
+void run_exact(const u64* m, const u64* dec, const std::vector<ExSeg>& segs, const std::vector<ExKind>& kinds,
+               ExOut* dout, cudaStream_t s) {
+    constexpr u64 C = static_cast<u64>(kExThreads) * PER;
+    Prepared p = prepare(segs, kinds, C, s);
+    const int nseg = static_cast<int>(segs.size()), nk = static_cast<int>(kinds.size());
+    const int njobs = nseg * nk;
+    // short segments: the warp resolves them directly (no tables)
+    const bool tables = p.maxlen >= 8 * C;
+    DevBuf<double> A, P;
+    DevBuf<ExRec> recs;
+    if (tables) {
+        A = DevBuf<double>(p.nch * nk, s);
+        P = DevBuf<double>(p.nch * nk, s);
+        recs = DevBuf<ExRec>(p.nch * nk, s);
+        ex_approx_kernel<PER><<<static_cast<unsigned>(p.nch), kExThreads, 0, s>>>(m, dec, p.segs.p, nseg, p.dch.p,
+                                                                                  p.dk.p, nk, p.nch, A.p);
+        ex_scan_kernel<<<static_cast<unsigned>(njobs), 1024, 0, s>>>(p.segs.p, nseg, p.dch.p, p.nch, A.p, P.p);
+        ex_fn_kernel<PER><<<static_cast<unsigned>(p.nch), kExThreads, 0, s>>>(m, dec, p.segs.p, nseg, p.dch.p,
+                                                                              p.dk.p, nk, p.nch, P.p, recs.p);
+        count_launch(3);
+        TCB_LAUNCH();
+    }
+    ex_walk_kernel<PER><<<cdiv(static_cast<u64>(njobs) * 32, 128), 128, 0, s>>>(
+        m, dec, p.segs.p, nseg, p.dch.p, p.dk.p, njobs, p.nch, tables ? recs.p : nullptr, dout);
+    count_launch();
+    TCB_LAUNCH();
+}
+
+}  // namespace
+
+std::vector<ExOut> exact_serial(const u64* m, const u64* dec, const std::vector<ExSeg>& segs,
+                                const std::vector<ExKind>& kinds, cudaStream_t s) {
+    static const bool ref_chain = [] {
+        const char* e = std::getenv("TCB_EXACT_REFERENCE");
+        return e && *e && *e != '0';
+    }();
+    if (ref_chain) return exact_serial_reference(m, dec, segs, kinds, s);
+    ProfScope prof(kSum, s);
+    const std::size_t njobs = segs.size() * kinds.size();
+    std::vector<ExOut> out(njobs);
+    if (njobs == 0) return out;
+    DevBuf<ExOut> d(njobs, s);
+    u64 maxlen = 0;
+    for (const auto& g : segs) maxlen = std::max(maxlen, g.hi - g.lo);
+    // few huge sums (the whole-core backward sums): longer chunks, a shorter walk
+    if (njobs <= 4 && maxlen >= (u64{1} << 24))
+        run_exact<32>(m, dec, segs, kinds, d.p, s);
+    else
+        run_exact<8>(m, dec, segs, kinds, d.p, s);
+    d.download(out.data(), njobs);
+    stream_sync(s);
+    return out;
+}
+
+std::vector<ExOut> exact_serial_reference(const u64* m, const u64* dec, const std::vector<ExSeg>& segs,
+                                          const std::vector<ExKind>& kinds, cudaStream_t s) {
+    const std::size_t njobs = segs.size() * kinds.size();
+    std::vector<ExOut> out(njobs);
+    if (njobs == 0) return out;
+    Prepared p = prepare(segs, kinds, 2048, s);
+    DevBuf<ExOut> d(njobs, s);
+    ex_serial_kernel<<<cdiv(njobs, 64), 64, 0, s>>>(m, dec, p.segs.p, static_cast<int>(segs.size()), p.dk.p,
+                                                    static_cast<int>(njobs), d.p);
+    count_launch();
+    TCB_LAUNCH();
+    d.download(out.data(), njobs);
+    stream_sync(s);
+    return out;
+}
+
+}  // namespace tcb

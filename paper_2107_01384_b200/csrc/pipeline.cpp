@@ -24,6 +24,7 @@
 #include <thread>
 #include <tuple>
 
+#include "exact.cuh"
 #include "kernels.cuh"
 #include "nccl_shim.hpp"
 #include "quant.cuh"
@@ -865,11 +866,12 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     u64 count = 1;
     for (auto v : f.r) count *= v;
     std::vector<u8> core_stream;
-    SumRec ach;
+    double ach;
     {
         HostTrace ht("encode: core finalize+sum");
         core_stream = finalize_stream(mag.p, neg.p, nc, plan, prm.coder, count, s);
-        ach = device_sum(SumKind::diff_backward, mag.p, dec.p, nc, 0, s);
+        // achieved_sse_int, accumulated backward (core_codec.cpp:405-411)
+        ach = exact_backward_sum(kExDiff, 0, mag.p, dec.p, nc, s);
     }
     res.times.core += ms_since(t1);
     {
@@ -878,7 +880,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     }
     for (std::size_t i = 0; i < d; ++i) res.factor_terms[i] = fe[i].term;
     res.times.factor = ms_since(t0);
-    res.core_quant = std::ldexp(ach.hi + ach.lo, -2 * k);
+    res.core_quant = std::ldexp(ach, -2 * k);
     double est = trunc + res.core_quant;
     for (double v : res.factor_terms) est += v;
     res.estimate = est;
