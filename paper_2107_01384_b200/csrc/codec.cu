@@ -12,9 +12,12 @@
 // zero-run symbols and the MSB-first raw bits; the adaptive range coder then
 // runs one thread per stream; payloads are compacted in stream order.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <cfloat>
 
+#include "ac.cuh"
 #include "codec.cuh"
 
 namespace tcb {
@@ -684,346 +687,11 @@ __device__ __forceinline__ u32 hslot(u64 sym, u32 hbits) {
     return static_cast<u32>((sym * 0x9E3779B97F4A7C15ull) >> (64 - hbits));
 }
 
-constexpr u32 kAcSmemCap = 2048;  // model entries kept in shared memory (global scratch beyond)
-
 __host__ __device__ inline u32 log2_at_least(u32 v) {
     u32 b = 5;
     while ((1u << b) < v) ++b;
     return b;
 }
-// model layout (u32 words): cnt[cap] | l1[cap/32+1] | l2[cap/1024+1] | hidx[1<<hb] | val[cap] (u64)
-__host__ __device__ inline u64 ac_model_words(u32 cap) {
-    const u64 w = cap + (cap / 32 + 1) + (cap / 1024 + 1) + (u64{1} << log2_at_least(2 * cap));
-    return ((w + 1) & ~u64{1}) + 2ull * cap;
-}
-
-// One warp per stream.  The adaptive model (entropy.cpp:155-239) is resolved
-// 32 symbols at a time (see the chunk comment below); all lanes then run the
-// range coder redundantly (identical state) and lane 0 writes the bytes.
-// Counts keep a 3-level (1 / 32 / 1024) prefix structure; halving rescales
-// them with all lanes.
-template <bool kShared>
-__global__ void __launch_bounds__(32) ac_kernel(const u64* __restrict__ syms, const StreamOut* __restrict__ sout,
-                                                const AcDesc* __restrict__ desc, const int* __restrict__ ids,
-                                                int nstreams, u8* __restrict__ outbuf, u32* __restrict__ scratch,
-                                                u64* __restrict__ elen, u32 smem_cap, int* __restrict__ redo) {
-    extern __shared__ __align__(16) u8 ac_smem[];
-    const int lane = threadIdx.x;
-    const int sidx = ids ? ids[blockIdx.x] : static_cast<int>(blockIdx.x);
-    if (sidx >= nstreams) return;
-    const u64 ns = sout[sidx].nsyms;
-    if (ns == 0) {
-        if (lane == 0) elen[sidx] = 0;
-        return;
-    }
-    const AcDesc d = desc[sidx];
-    // kShared: the model lives in shared memory (LDS/STS, no generic accesses).
-    // Capacity from the actual symbol count (the host sizes buffers from bounds).
-    const u32 cap_need = static_cast<u32>(ns + 1);
-    const u32 cap = kShared ? min(cap_need, smem_cap) : cap_need;
-    u32* base = kShared ? reinterpret_cast<u32*>(ac_smem) : scratch + d.model_off;
-    u32* cnt = base;
-    u32* l1 = cnt + cap;
-    u32* l2 = l1 + (cap / 32 + 1);
-    u32* hidx = l2 + (cap / 1024 + 1);
-    const u32 hb = log2_at_least(2 * cap);
-    const u32 hmask = (1u << hb) - 1;
-    u64* val = reinterpret_cast<u64*>(base + ((cap + (cap / 32 + 1) + (cap / 1024 + 1) + (1u << hb) + 1) & ~1u));
-    for (u32 i = lane; i < cap; i += 32) cnt[i] = 0;
-    for (u32 i = lane; i <= cap / 32; i += 32) l1[i] = 0;
-    for (u32 i = lane; i <= cap / 1024; i += 32) l2[i] = 0;
-    for (u32 i = lane; i < (1u << hb); i += 32) hidx[i] = 0;
-    __syncwarp();
-    u8* out = outbuf + d.out_off;
-    if (lane == 0) {
-        out[0] = 0;  // coder id: arithmetic
-        const u32 cnt32 = static_cast<u32>(ns);
-        for (int i = 0; i < 4; ++i) out[1 + i] = static_cast<u8>(cnt32 >> (8 * i));
-        cnt[0] = 1;
-        val[0] = 0;
-        l1[0] = 1;
-        l2[0] = 1;
-    }
-    __syncwarp();
-    // range coder state (identical in every lane)
-    u64 low = 0, pending = 1, pos = 5;
-    u32 range = 0xFFFFFFFFu;
-    u8 cache = 0;
-    auto shift = [&]() {
-        if (static_cast<u32>(low) < 0xFF000000u || (low >> 32) != 0) {
-            // the cached byte and the pending 0xFF run (plus the carry), one byte per
-            // lane: no serial loop, no divergent branch
-            const u8 carry = static_cast<u8>(low >> 32);
-            for (u64 q0 = 0; q0 < pending; q0 += 32) {
-                const u64 q = q0 + static_cast<u64>(lane);
-                if (q < pending) out[pos + q] = static_cast<u8>((q == 0 ? cache : u8{0xFF}) + carry);
-            }
-            pos += pending;
-            pending = 0;
-            cache = static_cast<u8>(low >> 24);
-        }
-        ++pending;
-        low = (low << 8) & 0xFFFFFFFFull;
-    };
-    auto norm = [&]() {
-        while (range < (1u << 24)) {
-            shift();
-            range <<= 8;
-        }
-    };
-    u32 nsym = 1, total = 1;
-    auto halve = [&]() {
-        __syncwarp();
-        for (u32 i = lane; i <= cap / 32; i += 32) l1[i] = 0;
-        for (u32 i = lane; i <= cap / 1024; i += 32) l2[i] = 0;
-        __syncwarp();
-        u32 t = 0;
-        for (u32 i0 = 0; i0 < nsym; i0 += 32) {
-            const u32 i = i0 + lane;
-            u32 c = 0;
-            if (i < nsym) {
-                c = max(1u, cnt[i] >> 1);
-                cnt[i] = c;
-            }
-            u32 bs = c;  // block i0/32 sum
-            for (int o = 16; o > 0; o >>= 1) bs += __shfl_xor_sync(0xffffffffu, bs, o);
-            if (lane == 0) {
-                l1[i0 >> 5] = bs;
-                l2[i0 >> 10] += bs;
-            }
-            t += bs;
-            __syncwarp();
-        }
-        total = t;
-        __syncwarp();
-    };
-    // Chunked model: between halvings the adaptive model (entropy.cpp:155-239)
-    // has a closed form, so 32 symbols (lane l <-> symbol t0 + l) resolve in
-    // parallel against the model as of t0:
-    //   index I: hash lookup, else a new symbol; repeats inside the chunk share
-    //            the first occurrence's index (match_any), new indices follow
-    //            first-occurrence order (ballot prefix);
-    //   cum     = count below I at t0 + 32 * #{earlier chunk symbols with index < I};
-    //   freq    = count of I at t0 + 32 * #{earlier chunk occurrences of I};
-    //   total   = total(t0) + 32 l; escapes code (0, cnt[0] = 1, total).
-    // A chunk ends at the first halving point (after coding the symbol whose
-    // pre-update total + 32 reaches 2^16), applied between that symbol's
-    // coding and its increment.  Only the range-coder arithmetic is sequential.
-    const u64* sy = syms + d.sym_off;
-    const unsigned below_me = (1u << lane) - 1u;
-    u64 cur = lane < ns ? sy[lane] : 0;
-    for (u64 t0 = 0; t0 < ns;) {
-        u32 L = static_cast<u32>(ns - t0 < 32 ? ns - t0 : 32);
-        // first l with total + 32 l + 32 >= 2^16 (total < 2^16 between symbols)
-        const u32 lh = total >= 65504u ? 0u : (65504u - total + 31u) / 32u;
-        const bool halv = lh < L;
-        if (halv) L = lh + 1;
-        const u64 nxt = t0 + L + lane < ns ? sy[t0 + L + lane] : 0;  // next chunk, in flight
-        const bool act = static_cast<u32>(lane) < L;
-        const u64 sv = cur;
-        int I = -1;
-        if (act) {
-            u32 h = hslot(sv, hb);
-            while (true) {
-                const u32 e = hidx[h];
-                if (e == 0) break;
-                if (val[e - 1] == sv) {
-                    I = static_cast<int>(e) - 1;
-                    break;
-                }
-                h = (h + 1) & hmask;
-            }
-        }
-        const unsigned am = __ballot_sync(0xffffffffu, act);
-        const unsigned same = __match_any_sync(0xffffffffu, sv) & am;
-        const int leader = act ? __ffs(same) - 1 : lane;
-        const bool isnew = act && I < 0 && leader == lane;
-        const unsigned newm = __ballot_sync(0xffffffffu, isnew);
-        if (nsym + __popc(newm) > cap) {  // model full: rerun from global scratch
-            if (lane == 0) {
-                *redo = 1;
-                elen[sidx] = ~u64{0};
-            }
-            return;
-        }
-        if (isnew) I = static_cast<int>(nsym + __popc(newm & below_me));
-        const int IL = __shfl_sync(0xffffffffu, I, leader);
-        if (act && I < 0) I = IL;
-        u32 base = 0, f0 = 0;
-        if (act) {
-            const u32 ui = static_cast<u32>(I);
-            if (ui < nsym) {
-                const u32 b1 = ui >> 5, b2 = ui >> 10;
-                for (u32 j = b1 << 5; j < ui; ++j) base += cnt[j];
-                for (u32 j = b2 << 5; j < b1; ++j) base += l1[j];
-                for (u32 j = 0; j < b2; ++j) base += l2[j];
-                f0 = cnt[ui];
-            } else {
-                base = total;  // every index present at t0 is below a new one
-            }
-        }
-        u32 within = 0;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const int Ij = __shfl_sync(0xffffffffu, I, j);
-            within += (j < lane && Ij < I) ? 1u : 0u;
-        }
-        const u32 cum = isnew ? 0u : base + 32u * within;
-        const u32 freq = isnew ? 1u : f0 + 32u * __popc(same & below_me);
-        const u32 tot = total + 32u * static_cast<u32>(lane);
-        // floor(range / T) by multiply-high: with m = ceil(2^64 / T) the product's high
-        // word is exact for range < 2^32 and 1 < T < 2^32 (the error term is below
-        // 2^-32 while a non-integer quotient is at least 1/T below the next integer);
-        // each lane prepares its own T's multiplier off the sequential path.
-        const u64 magic = tot > 1u ? (~u64{0} / tot) + 1u : 0u;
-        // range coder over the chunk (identical state in every lane); symbol l + 1's
-        // operands are fetched while symbol l is coded (the shuffles are off the
-        // coder's dependency chain)
-        u32 c = __shfl_sync(0xffffffffu, cum, 0), f = __shfl_sync(0xffffffffu, freq, 0);
-        u32 T = __shfl_sync(0xffffffffu, tot, 0);
-        u64 v = __shfl_sync(0xffffffffu, sv, 0), M = __shfl_sync(0xffffffffu, magic, 0);
-        for (u32 l = 0; l < L; ++l) {
-            const u32 ln = l + 1 < L ? l + 1 : l;
-            const u32 c_n = __shfl_sync(0xffffffffu, cum, ln), f_n = __shfl_sync(0xffffffffu, freq, ln);
-            const u32 T_n = __shfl_sync(0xffffffffu, tot, ln);
-            const u64 v_n = __shfl_sync(0xffffffffu, sv, ln), M_n = __shfl_sync(0xffffffffu, magic, ln);
-            range = T > 1u ? static_cast<u32>(__umul64hi(static_cast<u64>(range), M)) : range;
-            low += static_cast<u64>(c) * range;
-            range *= f;
-            norm();
-            if ((newm >> l) & 1u) {
-                // 32 raw bits, MSB first, each encode(bit, 1, 2): range >>= 1; low += bit ?
-                // range : 0; norm().  With range in [2^24, 2^32) exactly k = floor(log2
-                // range) - 23 halvings happen before the next normalisation, so up to k
-                // bits go at once: low += sum_j bit_j (range >> j), range >>= k, norm().
-                // Identical arithmetic, about five groups instead of 32 steps.
-                const u32 raw = static_cast<u32>(v);
-                int left = 32;
-                while (left > 0) {
-                    const int k = min(left, (31 - __clz(static_cast<int>(range))) - 23);
-                    const u32 cb = (raw >> (left - k)) & ((1u << k) - 1u);
-                    u64 add = 0;
-#pragma unroll
-                    for (int j = 1; j <= 8; ++j)
-                        if (j <= k && ((cb >> (k - j)) & 1u)) add += range >> j;
-                    low += add;
-                    range >>= k;
-                    left -= k;
-                    norm();
-                }
-            }
-            c = c_n;
-            f = f_n;
-            T = T_n;
-            v = v_n;
-            M = M_n;
-        }
-        // model update: increments in symbol order, a halving before the last one
-        auto inc = [&](bool doit) {
-            if (!doit) return;
-            const u32 ui = static_cast<u32>(I);
-            if (isnew) {
-                val[ui] = sv;
-                u32 h = hslot(sv, hb);
-                while (atomicCAS(&hidx[h], 0u, ui + 1u) != 0u) h = (h + 1) & hmask;
-            }
-            atomicAdd(&cnt[ui], 32u);
-            atomicAdd(&l1[ui >> 5], 32u);
-            atomicAdd(&l2[ui >> 10], 32u);
-        };
-        if (halv) {
-            const unsigned lastbit = 1u << (L - 1);
-            inc(act && static_cast<u32>(lane) != L - 1);
-            nsym += __popc(newm & ~lastbit);
-            halve();
-            inc(static_cast<u32>(lane) == L - 1);
-            nsym += (newm & lastbit) ? 1u : 0u;
-            total += 32u;
-        } else {
-            inc(act);
-            nsym += __popc(newm);
-            total += 32u * L;
-        }
-        __syncwarp();
-        t0 += L;
-        cur = nxt;
-    }
-    for (int i = 0; i < 5; ++i) shift();
-    if (lane == 0) elen[sidx] = pos;
-}
-
-// Host side: shared-memory pass for every stream, global-scratch rerun for
-// the ones whose model overflowed.
-void run_ac(const u64* syms, const StreamOut* so, const AcDesc* dad, const std::vector<AcDesc>& ad,
-            const std::vector<StreamOut>& soh, int ns, u8* ent, u32* scratch, u64* elen, cudaStream_t s) {
-    u32 need = 0;
-    for (int i = 0; i < ns; ++i)
-        if (soh[i].nsyms) need = std::max<u32>(need, std::min<u32>(ad[i].cap, kAcSmemCap));
-    if (need == 0) {
-        TCB_CUDA(cudaMemsetAsync(elen, 0, ns * sizeof(u64), s));
-        return;
-    }
-    const u64 smem = ac_model_words(need) * 4 + 16;
-    static bool attr = [] {
-        cudaFuncSetAttribute(ac_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(ac_model_words(kAcSmemCap) * 4 + 16));
-        return true;
-    }();
-    (void)attr;
-    DevBuf<int> redo(1, s);
-    redo.zero();
-    {
-        ProfScope pa(kAc, s);
-        ac_kernel<true><<<static_cast<unsigned>(ns), 32, smem, s>>>(syms, so, dad, nullptr, ns, ent, scratch, elen, need,
-                                                             redo.p);
-    }
-    count_launch();
-    TCB_LAUNCH();
-    if (redo.to_host()[0] == 0) return;
-    std::vector<u64> el(ns);
-    d2h(el.data(), elen, ns * sizeof(u64), s);
-    stream_sync(s);
-    std::vector<int> ids;
-    for (int i = 0; i < ns; ++i)
-        if (el[i] == ~u64{0}) ids.push_back(i);
-    DevBuf<int> dids(ids.size(), s);
-    dids.upload(ids.data(), ids.size());
-    {
-        ProfScope pa(kAc, s);
-        ac_kernel<false><<<static_cast<unsigned>(ids.size()), 32, 0, s>>>(syms, so, dad, dids.p, ns, ent, scratch, elen, 0,
-                                                                  redo.p);
-    }
-    count_launch();
-    TCB_LAUNCH();
-}
-
-// Launch-only variant for emit_planes: every stream's shared-memory pass with
-// the largest model that fits; streams whose model overflows report ~0 in
-// elen and are rerun by the caller from global scratch once the lengths are
-// back on the host (no extra round trip in the common case).
-void launch_ac_shared(const u64* syms, const StreamOut* so, const AcDesc* dad, int ns, u8* ent, u64* elen,
-                      int* redo, cudaStream_t s) {
-    const u64 smem = ac_model_words(kAcSmemCap) * 4 + 16;
-    static bool attr = [] {
-        cudaFuncSetAttribute(ac_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(ac_model_words(kAcSmemCap) * 4 + 16));
-        return true;
-    }();
-    (void)attr;
-    ProfScope pa(kAc, s);
-    ac_kernel<true><<<static_cast<unsigned>(ns), 32, smem, s>>>(syms, so, dad, nullptr, ns, ent, nullptr, elen,
-                                                         kAcSmemCap, redo);
-    count_launch();
-    TCB_LAUNCH();
-}
-
-// ---------------------------------------------------------------- semi-static rANS (entropy.cpp:290-421)
-// One warp per stream, lane 0: histogram through an open-addressing hash
-// (first-occurrence indices), the distinct symbols heap-sorted by value, the
-// reference's table normalisation (floor-scaled counts, then +-1 on the first
-// largest count until the total is 2^bits, bits = max(12, ceil log2 distinct)),
-// then the backwards encode; output framing as the range coder's (coder id 1,
-// u32 count, varint table, 8-byte state, 32-bit words in reverse).
 __host__ __device__ inline u64 rans_scratch_words(u64 nsyms) {
     const u64 cap = nsyms + 1;
     const u64 hs = u64{1} << log2_at_least(static_cast<u32>(2 * cap));
@@ -1199,6 +867,60 @@ __global__ void assemble_kernel(const u8* __restrict__ ent, const AcDesc* __rest
     for (u64 i = threadIdx.x; i < rb; i += blockDim.x) o[8 + el + i] = rbytes[rbyte0 + i];
 }
 
+
+// ---------------------------------------------------------------- per-block msb histogram
+// bins 0..64 <-> msb -1..63; sizes every (plane, block) stream exactly
+__global__ void msb_hist_kernel(const u64* __restrict__ m, u64 n, u64 block, u64 cpb, u64 span,
+                                unsigned long long* __restrict__ hist) {
+    __shared__ u32 h[65];
+    for (int i = threadIdx.x; i < 65; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const u64 b = blockIdx.x / cpb, j = blockIdx.x % cpb;
+    const u64 blo = b * block, bhi = min(n, blo + block);
+    const u64 lo = blo + j * span, hi = min(bhi, lo + span);
+    for (u64 i0 = lo; i0 < hi; i0 += blockDim.x) {
+        const u64 i = i0 + threadIdx.x;
+        const int bin = i < hi ? top_bit(m[i]) + 1 : -1;
+        const unsigned act = __ballot_sync(0xffffffffu, bin >= 0);
+        const unsigned same = __match_any_sync(0xffffffffu, bin) & act;
+        if (bin >= 0 && (__ffs(same) - 1) == static_cast<int>(threadIdx.x & 31)) atomicAdd(&h[bin], __popc(same));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 65; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[b * 65 + i], static_cast<unsigned long long>(h[i]));
+}
+
+}  // namespace
+
+std::vector<u64> msb_histogram(const u64* m, u64 n, u64 block, cudaStream_t s) {
+    const u64 nb = n == 0 ? 0 : (n + block - 1) / block;
+    std::vector<u64> h(nb * 65, 0);
+    if (nb == 0) return h;
+    const u64 span = 1 << 16;
+    const u64 cpb = (block + span - 1) / span;
+    DevBuf<unsigned long long> d(nb * 65, s);
+    d.zero();
+    msb_hist_kernel<<<static_cast<unsigned>(nb * cpb), 256, 0, s>>>(m, n, block, cpb, span, d.p);
+    count_launch();
+    TCB_LAUNCH();
+    d2h(h.data(), d.p, nb * 65 * sizeof(u64), s);
+    stream_sync(s);
+    return h;
+}
+
+namespace {
+
+// exact sizes of the full-plane stream (plane p) of one block; bounds for a breakpoint plane
+struct StreamCaps {
+    u64 nsyms, nraw, lead;
+};
+StreamCaps stream_caps(const u64* hb, int p) {
+    u64 lead = 0, trail = 0;
+    for (int q = -1; q <= p; ++q) lead += hb[q + 1];
+    for (int q = p + 1; q < 64; ++q) trail += hb[q + 1];
+    const u64 ones = hb[p + 1];
+    return {lead > 0 ? ones + 1 : 0, trail + ones, lead};
+}
 }  // namespace
 
 // ================================================================ host launchers
@@ -1346,18 +1068,13 @@ std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cu
     if (n == 0) return out;
     DevBuf<u64> syms(n, s);
     syms.upload(syms_host, n);
-    StreamOut so{n, 0};
-    DevBuf<StreamOut> dso(1, s);
-    dso.upload(&so, 1);
-    AcDesc a{};
-    a.cap = static_cast<u32>(n + 1);
-    a.hbits = log2_at_least(2 * a.cap);
-    DevBuf<AcDesc> dad(1, s);
-    dad.upload(&a, 1);
-    DevBuf<u8> ent(5 + 7 * n + 16, s);
-    DevBuf<u32> scratch(ac_model_words(a.cap) + 2, s);
+    const u64 cnt[2] = {n, 0};
+    DevBuf<u64> dc(2, s);
+    dc.upload(cnt, 2);
+    const u64 cap = ac_out_cap(n, ~u64{0} >> 2);
+    DevBuf<u8> ent(cap, s);
     DevBuf<u64> elen(1, s);
-    run_ac(syms.p, dso.p, dad.p, std::vector<AcDesc>{a}, std::vector<StreamOut>{so}, 1, ent.p, scratch.p, elen.p, s);
+    ac_encode(syms.p, dc.p, 2, {AcJob{0, 0, n, ~u64{0} >> 2}}, ent.p, elen.p, s);
     const u64 el = elen.to_host()[0];
     out.resize(el);
     ent.download(out.data(), el);
@@ -1365,12 +1082,63 @@ std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cu
     return out;
 }
 
-struct ProbeCache {
-    u64 n = 0, nb = 0;
-    int coder = 0;
-    cudaStream_t s = nullptr;
+// Stream layout of planes [last_plane, top_plane] x blocks: symbols, raw bits and
+// entropy output sized exactly from the blocks' msb histogram (a breakpoint
+// plane with stops is bounded by its full-plane sizes).
+struct Layout {
     std::vector<StreamDesc> sd;
     std::vector<AcDesc> ad;
+    std::vector<AcJob> jobs;
+    u64 sym_total = 0, raw_words = 0, out_total = 0, scratch_total = 0;
+};
+
+Layout make_layout(const std::vector<u64>& hist, u64 n, u64 block, int last_plane, int top_plane,
+                   const u64* stops_host, int coder) {
+    Layout L;
+    const u64 nb = n == 0 ? 0 : (n + block - 1) / block;
+    const int np = top_plane - last_plane + 1;
+    const u64 ns = nb * static_cast<u64>(np);
+    L.sd.resize(ns);
+    L.ad.resize(ns);
+    L.jobs.resize(ns);
+    for (int pi = 0; pi < np; ++pi) {
+        const int p = top_plane - pi;
+        for (u64 b = 0; b < nb; ++b) {
+            const u64 i = pi * nb + b;
+            StreamDesc& d = L.sd[i];
+            d.lo = b * block;
+            d.hi = std::min<u64>(n, d.lo + block);
+            d.plane = p;
+            const bool bp = p == last_plane && stops_host != nullptr;
+            d.lstop = bp ? stops_host[2 * b] : kFull;
+            d.tstop = bp ? stops_host[2 * b + 1] : kFull;
+            const StreamCaps c = stream_caps(hist.data() + b * 65, p);
+            d.sym_off = L.sym_total;
+            L.sym_total += c.nsyms;
+            d.raw_off = L.raw_words * 32;
+            L.raw_words += (c.nraw + 31) / 32;
+            AcDesc& a = L.ad[i];
+            a.sym_off = d.sym_off;
+            a.out_off = L.out_total;
+            a.cap = static_cast<u32>(c.nsyms + 1);
+            a.fen = 0;
+            a.hbits = log2_at_least(2 * a.cap);
+            if (coder == 1) {
+                L.out_total += rans_out_cap(c.nsyms);
+                a.model_off = (L.scratch_total + 1) & ~u64{1};
+                L.scratch_total = a.model_off + rans_scratch_words(c.nsyms);
+            } else {
+                L.out_total += ac_out_cap(c.nsyms, c.lead);
+                a.model_off = 0;
+            }
+            L.jobs[i] = AcJob{d.sym_off, a.out_off, c.nsyms, c.lead};
+        }
+    }
+    return L;
+}
+
+// emit + entropy coding of a layout's streams (no host round trip)
+struct Coded {
     DevBuf<StreamDesc> dsd;
     DevBuf<u64> syms;
     DevBuf<u32> raw;
@@ -1379,7 +1147,39 @@ struct ProbeCache {
     DevBuf<u8> ent;
     DevBuf<u64> elen;
     DevBuf<u32> scratch;
-    DevBuf<int> redo;
+};
+
+void code_streams(Coded& c, const Layout& L, const u64* m, const u8* neg, int coder, cudaStream_t s) {
+    const u64 ns = L.sd.size();
+    c.dsd = DevBuf<StreamDesc>(ns, s);
+    c.dsd.upload(L.sd.data(), ns);
+    c.syms = DevBuf<u64>(L.sym_total + 1, s);
+    c.raw = DevBuf<u32>(L.raw_words + 1, s);
+    c.raw.zero();
+    c.so = DevBuf<StreamOut>(ns, s);
+    {
+        ProfScope pe(kEmit, s);
+        emit_kernel<<<static_cast<unsigned>(ns), kEmT, 0, s>>>(m, neg, c.dsd.p, c.syms.p, c.raw.p, c.so.p);
+    }
+    count_launch();
+    TCB_LAUNCH();
+    c.dad = DevBuf<AcDesc>(ns, s);
+    c.dad.upload(L.ad.data(), ns);
+    c.ent = DevBuf<u8>(L.out_total + 1, s);
+    c.elen = DevBuf<u64>(ns, s);
+    if (coder == 1) {
+        c.scratch = DevBuf<u32>(L.scratch_total + 2, s);
+        run_rans(c.syms.p, c.so.p, c.dad.p, static_cast<int>(ns), c.ent.p, c.scratch.p, c.elen.p, s);
+    } else {
+        ac_encode(c.syms.p, reinterpret_cast<const u64*>(c.so.p), 2, L.jobs, c.ent.p, c.elen.p, s);
+    }
+}
+
+struct ProbeCache {
+    u64 n = 0, nb = 0;
+    cudaStream_t s = nullptr;
+    Layout L;
+    Coded c;
     cudaEvent_t done = nullptr;
     bool ready = false;
     std::vector<u64> el;
@@ -1395,66 +1195,13 @@ struct ProbeCache {
 std::shared_ptr<ProbeCache> probe_planes_async(const u64* m, u64 n, u64 block, int coder, cudaStream_t side) {
     auto c = std::make_shared<ProbeCache>();
     c->n = n;
-    c->coder = coder;
     c->s = side;
     const u64 nb = n == 0 ? 0 : (n + block - 1) / block;
     c->nb = nb;
-    const u64 ns = nb * 64;
-    if (ns == 0) return c;
-    c->sd.resize(ns);
-    u64 sym_total = 0, raw_words = 0;
-    for (int pi = 0; pi < 64; ++pi)
-        for (u64 b = 0; b < nb; ++b) {
-            StreamDesc& d = c->sd[pi * nb + b];
-            d.lo = b * block;
-            d.hi = std::min<u64>(n, d.lo + block);
-            d.plane = 63 - pi;
-            d.lstop = d.tstop = kFull;
-            d.sym_off = sym_total;
-            sym_total += d.hi - d.lo + 1;
-            d.raw_off = raw_words * 32;
-            raw_words += (d.hi - d.lo + 31) / 32;
-        }
-    c->ad.resize(ns);
-    u64 out_total = 0, scratch_total = 0;
-    for (u64 i = 0; i < ns; ++i) {
-        AcDesc& a = c->ad[i];
-        const u64 kmax = c->sd[i].hi - c->sd[i].lo + 1;
-        a.sym_off = c->sd[i].sym_off;
-        a.out_off = out_total;
-        a.cap = static_cast<u32>(kmax + 1);
-        a.fen = 0;
-        a.hbits = log2_at_least(2 * a.cap);
-        if (coder == 1) {
-            out_total += rans_out_cap(kmax);
-            a.model_off = (scratch_total + 1) & ~u64{1};
-            scratch_total = a.model_off + rans_scratch_words(kmax);
-        } else {
-            out_total += 5 + 7 * kmax + 16;
-            a.model_off = 0;
-        }
-    }
-    c->dsd = DevBuf<StreamDesc>(ns, side);
-    c->dsd.upload(c->sd.data(), ns);
-    c->syms = DevBuf<u64>(sym_total, side);
-    c->raw = DevBuf<u32>(raw_words + 1, side);
-    c->raw.zero();
-    c->so = DevBuf<StreamOut>(ns, side);
-    emit_kernel<<<static_cast<unsigned>(ns), kEmT, 0, side>>>(m, nullptr, c->dsd.p, c->syms.p, c->raw.p, c->so.p);
-    count_launch();
-    TCB_LAUNCH();
-    c->dad = DevBuf<AcDesc>(ns, side);
-    c->dad.upload(c->ad.data(), ns);
-    c->ent = DevBuf<u8>(out_total + 1, side);
-    c->elen = DevBuf<u64>(ns, side);
-    c->scratch = DevBuf<u32>(coder == 1 ? scratch_total + 2 : 2, side);
-    c->redo = DevBuf<int>(1, side);
-    if (coder == 1) {
-        run_rans(c->syms.p, c->so.p, c->dad.p, static_cast<int>(ns), c->ent.p, c->scratch.p, c->elen.p, side);
-    } else {
-        c->redo.zero();
-        launch_ac_shared(c->syms.p, c->so.p, c->dad.p, static_cast<int>(ns), c->ent.p, c->elen.p, c->redo.p, side);
-    }
+    if (nb == 0) return c;
+    const auto hist = msb_histogram(m, n, block, side);
+    c->L = make_layout(hist, n, block, 0, 63, nullptr, coder);
+    code_streams(c->c, c->L, m, nullptr, coder, side);
     TCB_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
     TCB_CUDA(cudaEventRecord(c->done, side));
     return c;
@@ -1466,32 +1213,8 @@ std::vector<u64> probe_entropy_bytes(ProbeCache& c, int p) {
     if (!c.ready && ns > 0) {
         TCB_CUDA(cudaEventSynchronize(c.done));
         c.el.resize(ns);
-        std::vector<StreamOut> soh(ns);
-        c.elen.download(c.el.data(), ns);
-        c.so.download(soh.data(), ns);
+        c.c.elen.download(c.el.data(), ns);
         stream_sync(c.s);
-        if (c.coder == 0) {  // model overflow: rerun those streams from global scratch
-            std::vector<int> ids;
-            u64 words = 0;
-            for (u64 i = 0; i < ns; ++i)
-                if (c.el[i] == ~u64{0}) {
-                    ids.push_back(static_cast<int>(i));
-                    c.ad[i].model_off = words;
-                    words += ac_model_words(static_cast<u32>(soh[i].nsyms + 1));
-                }
-            if (!ids.empty()) {
-                DevBuf<u32> gscr(words + 2, c.s);
-                c.dad.upload(c.ad.data(), ns);
-                DevBuf<int> dids(ids.size(), c.s);
-                dids.upload(ids.data(), ids.size());
-                ac_kernel<false><<<static_cast<unsigned>(ids.size()), 32, 0, c.s>>>(
-                    c.syms.p, c.so.p, c.dad.p, dids.p, static_cast<int>(ns), c.ent.p, gscr.p, c.elen.p, 0, c.redo.p);
-                count_launch();
-                TCB_LAUNCH();
-                c.elen.download(c.el.data(), ns);
-                stream_sync(c.s);
-            }
-        }
         for (u64 v : c.el)
             if (v == ~u64{1}) throw Error("entropy: cannot normalize rans table");
         c.ready = true;
@@ -1509,104 +1232,30 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
     const int np = top_plane - last_plane + 1;
     const u64 ns = nb * static_cast<u64>(np);
     if (ns == 0 || np <= 0) return res;
-    // upper bounds per stream: symbols <= positions + 1, raw bits <= positions
-    std::vector<StreamDesc> sd(ns);
-    u64 sym_total = 0, raw_words = 0;
-    for (int pi = 0; pi < np; ++pi) {
-        const int p = top_plane - pi;
-        for (u64 b = 0; b < nb; ++b) {
-            StreamDesc& d = sd[pi * nb + b];
-            d.lo = b * block;
-            d.hi = std::min<u64>(n, d.lo + block);
-            d.plane = p;
-            const bool bp = p == last_plane && stops_host != nullptr;
-            d.lstop = bp ? stops_host[2 * b] : kFull;
-            d.tstop = bp ? stops_host[2 * b + 1] : kFull;
-            d.sym_off = sym_total;
-            sym_total += d.hi - d.lo + 1;
-            d.raw_off = raw_words * 32;
-            raw_words += (d.hi - d.lo + 31) / 32;
-        }
-    }
-    // No round trip between the symbol pass and the coder: entropy buffers are
-    // sized from per-stream bounds (symbols <= positions + 1); the coder reads
-    // the actual counts on the device.
     HostTrace ht_a("emit: symbols+entropy+sync");
-    DevBuf<StreamDesc> dsd(ns, s);
-    dsd.upload(sd.data(), ns);
-    DevBuf<u64> syms(sym_total, s);
-    DevBuf<u32> raw(raw_words + 1, s);
-    raw.zero();
-    DevBuf<StreamOut> so(ns, s);
-    {
-    ProfScope pe(kEmit, s);
-    emit_kernel<<<static_cast<unsigned>(ns), kEmT, 0, s>>>(m, neg, dsd.p, syms.p, raw.p, so.p);
-    }
-    count_launch();
-    TCB_LAUNCH();
-    std::vector<AcDesc> ad(ns);
-    u64 out_total = 0, scratch_total = 0;
-    for (u64 i = 0; i < ns; ++i) {
-        AcDesc& a = ad[i];
-        a.sym_off = sd[i].sym_off;
-        const u64 kmax = sd[i].hi - sd[i].lo + 1;
-        a.out_off = out_total;
-        a.cap = static_cast<u32>(kmax + 1);
-        a.fen = 0;
-        a.hbits = log2_at_least(2 * a.cap);
-        if (coder == 1) {
-            out_total += rans_out_cap(kmax);
-            a.model_off = (scratch_total + 1) & ~u64{1};
-            scratch_total = a.model_off + rans_scratch_words(kmax);
-        } else {
-            out_total += 5 + 7 * kmax + 16;
-            a.model_off = 0;  // global scratch only for an overflow rerun (set below)
-        }
-    }
-    DevBuf<AcDesc> dad(ns, s);
-    dad.upload(ad.data(), ns);
-    DevBuf<u8> ent(out_total + 1, s);
-    DevBuf<u64> elen(ns, s);
-    DevBuf<u32> scratch(coder == 1 ? scratch_total + 2 : 2, s);
-    DevBuf<int> redo(1, s);
-    if (coder == 1) {
-        run_rans(syms.p, so.p, dad.p, static_cast<int>(ns), ent.p, scratch.p, elen.p, s);
-    } else {
-        redo.zero();
-        launch_ac_shared(syms.p, so.p, dad.p, static_cast<int>(ns), ent.p, elen.p, redo.p, s);
-    }
+    const auto hist = msb_histogram(m, n, block, s);
+    const Layout L = make_layout(hist, n, block, last_plane, top_plane, stops_host, coder);
+    Coded c;
+    code_streams(c, L, m, neg, coder, s);
     std::vector<u64> el(ns);
     std::vector<StreamOut> soh(ns);
-    elen.download(el.data(), ns);
-    so.download(soh.data(), ns);
+    c.elen.download(el.data(), ns);
+    c.so.download(soh.data(), ns);
     stream_sync(s);
-    if (coder == 0) {  // rerun the streams whose model outgrew shared memory from global scratch
-        std::vector<int> ids;
-        u64 words = 0;
-        for (u64 i = 0; i < ns; ++i)
-            if (el[i] == ~u64{0}) {
-                ids.push_back(static_cast<int>(i));
-                ad[i].model_off = words;
-                words += ac_model_words(static_cast<u32>(soh[i].nsyms + 1));
-            }
-        if (!ids.empty()) {
-            DevBuf<u32> gscr(words + 2, s);
-            dad.upload(ad.data(), ns);
-            DevBuf<int> dids(ids.size(), s);
-            dids.upload(ids.data(), ids.size());
-            {
-                ProfScope pa(kAc, s);
-                ac_kernel<false><<<static_cast<unsigned>(ids.size()), 32, 0, s>>>(
-                    syms.p, so.p, dad.p, dids.p, static_cast<int>(ns), ent.p, gscr.p, elen.p, 0, redo.p);
-            }
-            count_launch();
-            TCB_LAUNCH();
-            elen.download(el.data(), ns);
-            stream_sync(s);
-        }
-    }
     for (u64 v : el)
         if (v == ~u64{1}) throw Error("entropy: cannot normalize rans table");
+    if (std::getenv("TCB_AC_STATS")) {
+        u64 mx = 0, tot = 0, eb = 0, rb = 0;
+        for (u64 i = 0; i < ns; ++i) {
+            mx = std::max(mx, soh[i].nsyms);
+            tot += soh[i].nsyms;
+            eb += el[i];
+            rb += (soh[i].nraw + 7) / 8;
+        }
+        std::fprintf(stderr, "[ac stats] planes %d..%d streams %llu symbols %llu (max %llu) entropy %llu B raw %llu B\n",
+                     last_plane, top_plane, (unsigned long long)ns, (unsigned long long)tot, (unsigned long long)mx,
+                     (unsigned long long)eb, (unsigned long long)rb);
+    }
     res.entropy_bytes = el;
     ht_a.stop();
     if (!want_body) return res;
@@ -1621,8 +1270,8 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
     doff.upload(off.data(), ns);
     DevBuf<u8> body(tot, s);
     ProfScope pz(kEmit, s);
-    assemble_kernel<<<static_cast<unsigned>(ns), 128, 0, s>>>(ent.p, dad.p, elen.p, raw.p, dsd.p, so.p, doff.p,
-                                                               body.p);
+    assemble_kernel<<<static_cast<unsigned>(ns), 128, 0, s>>>(c.ent.p, c.dad.p, c.elen.p, c.raw.p, c.dsd.p, c.so.p,
+                                                               doff.p, body.p);
     count_launch();
     TCB_LAUNCH();
     res.body.resize(tot);

@@ -47,6 +47,9 @@ std::vector<double> device_sums_serial(const std::vector<std::pair<SumKind, int>
 void crossing_scan(const u64* m, u64 n, u64 block, u64 b, int plane, int category, const double* cum,
                    const double* need, int npairs, u64* counts_host, cudaStream_t s);
 
+// per-block histogram of the magnitudes' top bit: nb x 65 (bins <-> msb -1..63)
+std::vector<u64> msb_histogram(const u64* m, u64 n, u64 block, cudaStream_t s);
+
 // decoded magnitudes implied by (last_plane, stops) (core_codec.cpp:344-367)
 void decode_model(const u64* m, u64 n, u64 block, int last_plane, const u64* stops_dev /*2*nb*/, u64* dec,
                   cudaStream_t s);

@@ -26,7 +26,8 @@ struct Error : std::runtime_error {
     do {                                                                                        \
         cudaError_t _e = (expr);                                                                \
         if (_e != cudaSuccess)                                                                  \
-            throw ::tcb::Error(std::string("cuda: ") + cudaGetErrorString(_e) + " at " + #expr); \
+            throw ::tcb::Error(std::string("cuda: ") + cudaGetErrorString(_e) + " at " + #expr + " (" + \
+                               __FILE__ + ":" + std::to_string(__LINE__) + ")");               \
     } while (0)
 
 #define TCB_LAUNCH() TCB_CUDA(cudaGetLastError())

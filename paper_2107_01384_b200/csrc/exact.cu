@@ -20,7 +20,6 @@ constexpr long long kBig = 1LL << 62;        // "no partial sum" sentinel for mi
 constexpr long long kLim = 1LL << 56;        // |increment| beyond any region's width: reject
 constexpr long long kAMax = (1LL << 53) - 1;  // strict interior of a region, in units
 constexpr long long kAMin = (1LL << 52) + 1;
-constexpr int kExThreads = 256;
 
 struct DevSeg {
     u64 lo, hi;
@@ -215,45 +214,86 @@ __device__ __forceinline__ Fn warp_scan_fn(Fn f) {
     return f;
 }
 
-// ---------------------------------------------------------------- pass 1: approximate chunk sums
-template <int PER>
-__global__ void __launch_bounds__(kExThreads) ex_approx_kernel(const u64* __restrict__ m, const u64* __restrict__ dec,
-                                                               const DevSeg* __restrict__ segs, int nseg,
-                                                               const u64* __restrict__ choff,
-                                                               const ExKind* __restrict__ kinds, int nk, u64 nch,
-                                                               double* __restrict__ A) {
-    constexpr u64 C = static_cast<u64>(kExThreads) * PER;
-    __shared__ double red[kExThreads / 32];
-    const u64 c = blockIdx.x;
-    const int g = seg_of(choff, nseg, c);
-    const DevSeg sg = segs[g];
+// ---------------------------------------------------------------- passes 1 and 2
+// Work item = (chunk, kind), one warp each; the warps of a CTA take
+// consecutive items, i.e. the kinds of one chunk, so a chunk's magnitudes are
+// read from DRAM once and from L1/L2 by the other kinds.  Lane l owns the
+// contiguous positions [l * LPE, (l + 1) * LPE) of the chunk, so its run of
+// terms is a contiguous piece of the serial order and the warp combines the
+// lanes' functions in lane order.
+constexpr int kExWarps = 8;
+
+// element positions of one lane: term value or 0, category counts; TERM is
+// resolved once per item (no per-element switch)
+template <int TERM, class F>
+__device__ __forceinline__ void lane_terms(const u64* __restrict__ m, const u64* __restrict__ dec, const DevSeg& sg,
+                                           u64 q0, int cnt, int p, F&& f) {
+    for (int i = 0; i < cnt; ++i) {
+        const u64 idx = elem_index(sg, q0 + i);
+        const u64 v = __ldg(m + idx);
+        if constexpr (TERM == kExLead) {
+            const int tb = top_bit64(v);
+            f(tb == p ? t_lead_gain(v, p) : 0.0, tb <= p, tb == p, tb == p);
+        } else if constexpr (TERM == kExTrail) {
+            const int tb = top_bit64(v);
+            f(tb > p ? t_trail_gain(v, p) : 0.0, 0u, tb > p, tb > p);
+        } else if constexpr (TERM == kExBoth) {
+            const int tb = top_bit64(v);
+            const bool tr = tb > p;
+            f(tr ? t_trail_gain(v, p) : (tb == p ? t_lead_gain(v, p) : 0.0), !tr, tr, tb >= p);
+        } else if constexpr (TERM == kExSq) {
+            f(t_insig2(v), 0u, 0u, v != 0);
+        } else if constexpr (TERM == kExRecal) {
+            f(t_recal(v, p), 0u, 0u, true);
+        } else {
+            f(t_diff2(v, __ldg(dec + idx)), 0u, 0u, true);
+        }
+    }
+}
+
+struct ItemGeom {
+    int g;
+    u64 q0;  // first position of this lane
+    int cnt; // positions of this lane
+};
+template <int LPE>
+__device__ __forceinline__ ItemGeom item_geom(const DevSeg* __restrict__ segs, int nseg, const u64* __restrict__ choff,
+                                              u64 c, DevSeg& sg) {
+    constexpr u64 C = 32ull * LPE;
+    ItemGeom ig;
+    ig.g = seg_of(choff, nseg, c);
+    sg = segs[ig.g];
     const u64 len = sg.hi - sg.lo;
-    const u64 q0 = (c - choff[g]) * C + static_cast<u64>(threadIdx.x) * PER;
-    u64 v[PER], dv[PER];
-#pragma unroll
-    for (int e = 0; e < PER; ++e) {
-        const u64 q = q0 + e;
-        v[e] = q < len ? m[elem_index(sg, q)] : 0;
-        dv[e] = (dec && q < len) ? dec[elem_index(sg, q)] : 0;
+    ig.q0 = (c - choff[ig.g]) * C + static_cast<u64>(threadIdx.x & 31) * LPE;
+    ig.cnt = ig.q0 >= len ? 0 : static_cast<int>(min(static_cast<u64>(LPE), len - ig.q0));
+    return ig;
+}
+
+template <int LPE>
+__global__ void __launch_bounds__(32 * kExWarps) ex_approx_kernel(const u64* __restrict__ m, const u64* __restrict__ dec,
+                                                                  const DevSeg* __restrict__ segs, int nseg,
+                                                                  const u64* __restrict__ choff,
+                                                                  const ExKind* __restrict__ kinds, int nk, u64 nch,
+                                                                  double* __restrict__ A) {
+    const u64 item = static_cast<u64>(blockIdx.x) * kExWarps + (threadIdx.x >> 5);
+    if (item >= nch * nk) return;
+    const u64 c = item / nk;
+    const int k = static_cast<int>(item % nk);
+    DevSeg sg;
+    const ItemGeom ig = item_geom<LPE>(segs, nseg, choff, c, sg);
+    const ExKind kd = kinds[k];
+    double acc = 0.0;
+    auto add = [&](double t, u32, u32, bool) { acc += t; };
+    switch (kd.term) {
+        case kExLead: lane_terms<kExLead>(m, dec, sg, ig.q0, ig.cnt, kd.plane, add); break;
+        case kExTrail: lane_terms<kExTrail>(m, dec, sg, ig.q0, ig.cnt, kd.plane, add); break;
+        case kExBoth: lane_terms<kExBoth>(m, dec, sg, ig.q0, ig.cnt, kd.plane, add); break;
+        case kExSq: lane_terms<kExSq>(m, dec, sg, ig.q0, ig.cnt, kd.plane, add); break;
+        case kExRecal: lane_terms<kExRecal>(m, dec, sg, ig.q0, ig.cnt, kd.plane, add); break;
+        default: lane_terms<kExDiff>(m, dec, sg, ig.q0, ig.cnt, kd.plane, add); break;
     }
-    for (int k = 0; k < nk; ++k) {
-        const ExKind kd = kinds[k];
-        double acc = 0.0;
-#pragma unroll
-        for (int e = 0; e < PER; ++e) {
-            u32 a0, a1;
-            if (q0 + e < len) acc += ex_term(kd.term, kd.plane, v[e], dv[e], a0, a1);
-        }
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int w = 0; w < kExThreads / 32; ++w) t += red[w];
-            A[static_cast<u64>(k) * nch + c] = t;
-        }
-        __syncthreads();
-    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) A[static_cast<u64>(k) * nch + c] = acc;
 }
 
 // exclusive prefix (plus s0) of the approximate chunk sums of each (kind, segment)
@@ -297,81 +337,59 @@ __global__ void __launch_bounds__(1024) ex_scan_kernel(const DevSeg* __restrict_
     }
 }
 
-// ---------------------------------------------------------------- pass 2: chunk functions
-template <int PER>
-__global__ void __launch_bounds__(kExThreads) ex_fn_kernel(const u64* __restrict__ m, const u64* __restrict__ dec,
-                                                           const DevSeg* __restrict__ segs, int nseg,
-                                                           const u64* __restrict__ choff,
-                                                           const ExKind* __restrict__ kinds, int nk, u64 nch,
-                                                           const double* __restrict__ P, ExRec* __restrict__ out) {
-    constexpr u64 C = static_cast<u64>(kExThreads) * PER;
-    __shared__ Fn wf[kExThreads / 32];
-    __shared__ u32 wc[2][kExThreads / 32];
-    const u64 c = blockIdx.x;
-    const int g = seg_of(choff, nseg, c);
-    const DevSeg sg = segs[g];
-    const u64 len = sg.hi - sg.lo;
-    const u64 q0 = (c - choff[g]) * C + static_cast<u64>(threadIdx.x) * PER;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    u64 v[PER], dv[PER];
-#pragma unroll
-    for (int e = 0; e < PER; ++e) {
-        const u64 q = q0 + e;
-        v[e] = q < len ? m[elem_index(sg, q)] : 0;
-        dv[e] = (dec && q < len) ? dec[elem_index(sg, q)] : 0;
+template <int LPE>
+__global__ void __launch_bounds__(32 * kExWarps) ex_fn_kernel(const u64* __restrict__ m, const u64* __restrict__ dec,
+                                                              const DevSeg* __restrict__ segs, int nseg,
+                                                              const u64* __restrict__ choff,
+                                                              const ExKind* __restrict__ kinds, int nk, u64 nch,
+                                                              const double* __restrict__ P, ExRec* __restrict__ out) {
+    const u64 item = static_cast<u64>(blockIdx.x) * kExWarps + (threadIdx.x >> 5);
+    if (item >= nch * nk) return;
+    const int lane = threadIdx.x & 31;
+    const u64 c = item / nk;
+    const int k = static_cast<int>(item % nk);
+    DevSeg sg;
+    const ItemGeom ig = item_geom<LPE>(segs, nseg, choff, c, sg);
+    const ExKind kd = kinds[k];
+    const int rid = region_of(P[static_cast<u64>(k) * nch + c]);
+    const int e = rexp(rid);
+    Fn f = fn_id();
+    u32 x0 = 0, x1 = 0;
+    auto push = [&](double t, u32 a0, u32 a1, bool nz) {
+        x0 += a0;
+        x1 += a1;
+        if (nz) fn_term(f, t, e);
+    };
+    switch (kd.term) {
+        case kExLead: lane_terms<kExLead>(m, dec, sg, ig.q0, ig.cnt, kd.plane, push); break;
+        case kExTrail: lane_terms<kExTrail>(m, dec, sg, ig.q0, ig.cnt, kd.plane, push); break;
+        case kExBoth: lane_terms<kExBoth>(m, dec, sg, ig.q0, ig.cnt, kd.plane, push); break;
+        case kExSq: lane_terms<kExSq>(m, dec, sg, ig.q0, ig.cnt, kd.plane, push); break;
+        case kExRecal: lane_terms<kExRecal>(m, dec, sg, ig.q0, ig.cnt, kd.plane, push); break;
+        default: lane_terms<kExDiff>(m, dec, sg, ig.q0, ig.cnt, kd.plane, push); break;
     }
-    for (int k = 0; k < nk; ++k) {
-        const ExKind kd = kinds[k];
-        const int rid = region_of(P[static_cast<u64>(k) * nch + c]);
-        const int e = rexp(rid);
-        Fn f = fn_id();
-        u32 x0 = 0, x1 = 0;
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            if (q0 + i >= len) break;
-            u32 a0, a1;
-            const double t = ex_term(kd.term, kd.plane, v[i], dv[i], a0, a1);
-            x0 += a0;
-            x1 += a1;
-            fn_term(f, t, e);
-        }
-        // ordered reduction: lane l (aligned) absorbs [l + o, l + 2o)
-        for (int o = 1; o < 32; o <<= 1) {
-            const Fn h = shfl_fn(f, (lane + o) & 31, false);
-            if ((lane & (2 * o - 1)) == 0) f = fn_then(f, h);
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            x0 += __shfl_down_sync(0xffffffffu, x0, o);
-            x1 += __shfl_down_sync(0xffffffffu, x1, o);
-        }
-        if (lane == 0) {
-            wf[w] = f;
-            wc[0][w] = x0;
-            wc[1][w] = x1;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            Fn t = wf[0];
-            u32 y0 = wc[0][0], y1 = wc[1][0];
-            for (int ww = 1; ww < kExThreads / 32; ++ww) {
-                t = fn_then(t, wf[ww]);
-                y0 += wc[0][ww];
-                y1 += wc[1][ww];
-            }
-            ExRec r;
-            r.K0 = t.K0;
-            r.K1 = t.K1;
-            r.mn0 = t.mn0;
-            r.mn1 = t.mn1;
-            r.mx0 = t.mx0;
-            r.mx1 = t.mx1;
-            r.rid = rid;
-            r.qbad = t.q | (t.bad << 2);
-            r.c0 = y0;
-            r.c1 = y1;
-            out[static_cast<u64>(k) * nch + c] = r;
-        }
-        __syncthreads();
+    // ordered reduction: lane l (aligned to 2o) absorbs lanes [l + o, l + 2o)
+    for (int o = 1; o < 32; o <<= 1) {
+        const Fn h = shfl_fn(f, (lane + o) & 31, false);
+        if ((lane & (2 * o - 1)) == 0) f = fn_then(f, h);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        x0 += __shfl_xor_sync(0xffffffffu, x0, o);
+        x1 += __shfl_xor_sync(0xffffffffu, x1, o);
+    }
+    if (lane == 0) {
+        ExRec r;
+        r.K0 = f.K0;
+        r.K1 = f.K1;
+        r.mn0 = f.mn0;
+        r.mn1 = f.mn1;
+        r.mx0 = f.mx0;
+        r.mx1 = f.mx1;
+        r.rid = rid;
+        r.qbad = f.q | (f.bad << 2);
+        r.c0 = x0;
+        r.c1 = x1;
+        out[static_cast<u64>(k) * nch + c] = r;
     }
 }
 
@@ -448,13 +466,13 @@ __device__ void ex_fine(const u64* __restrict__ m, const u64* __restrict__ dec, 
     }
 }
 
-template <int PER>
+template <int LPE>
 __global__ void __launch_bounds__(128) ex_walk_kernel(const u64* __restrict__ m, const u64* __restrict__ dec,
                                                       const DevSeg* __restrict__ segs, int nseg,
                                                       const u64* __restrict__ choff, const ExKind* __restrict__ kinds,
                                                       int njobs, u64 nch, const ExRec* __restrict__ recs,
                                                       ExOut* __restrict__ out) {
-    constexpr u64 C = static_cast<u64>(kExThreads) * PER;
+    constexpr u64 C = 32ull * LPE;
     const int job = static_cast<int>((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     if (job >= njobs) return;
     const int lane = threadIdx.x & 31;
@@ -580,10 +598,10 @@ Prepared prepare(const std::vector<ExSeg>& segs, const std::vector<ExKind>& kind
     return p;
 }
 
-template <int PER>
+template <int LPE>
 void run_exact(const u64* m, const u64* dec, const std::vector<ExSeg>& segs, const std::vector<ExKind>& kinds,
                ExOut* dout, cudaStream_t s) {
-    constexpr u64 C = static_cast<u64>(kExThreads) * PER;
+    constexpr u64 C = 32ull * LPE;
     Prepared p = prepare(segs, kinds, C, s);
     const int nseg = static_cast<int>(segs.size()), nk = static_cast<int>(kinds.size());
     const int njobs = nseg * nk;
@@ -595,15 +613,15 @@ void run_exact(const u64* m, const u64* dec, const std::vector<ExSeg>& segs, con
         A = DevBuf<double>(p.nch * nk, s);
         P = DevBuf<double>(p.nch * nk, s);
         recs = DevBuf<ExRec>(p.nch * nk, s);
-        ex_approx_kernel<PER><<<static_cast<unsigned>(p.nch), kExThreads, 0, s>>>(m, dec, p.segs.p, nseg, p.dch.p,
-                                                                                  p.dk.p, nk, p.nch, A.p);
+        const unsigned grid = cdiv(p.nch * nk, kExWarps);
+        ex_approx_kernel<LPE><<<grid, 32 * kExWarps, 0, s>>>(m, dec, p.segs.p, nseg, p.dch.p, p.dk.p, nk, p.nch, A.p);
         ex_scan_kernel<<<static_cast<unsigned>(njobs), 1024, 0, s>>>(p.segs.p, nseg, p.dch.p, p.nch, A.p, P.p);
-        ex_fn_kernel<PER><<<static_cast<unsigned>(p.nch), kExThreads, 0, s>>>(m, dec, p.segs.p, nseg, p.dch.p,
-                                                                              p.dk.p, nk, p.nch, P.p, recs.p);
+        ex_fn_kernel<LPE><<<grid, 32 * kExWarps, 0, s>>>(m, dec, p.segs.p, nseg, p.dch.p, p.dk.p, nk, p.nch, P.p,
+                                                         recs.p);
         count_launch(3);
         TCB_LAUNCH();
     }
-    ex_walk_kernel<PER><<<cdiv(static_cast<u64>(njobs) * 32, 128), 128, 0, s>>>(
+    ex_walk_kernel<LPE><<<cdiv(static_cast<u64>(njobs) * 32, 128), 128, 0, s>>>(
         m, dec, p.segs.p, nseg, p.dch.p, p.dk.p, njobs, p.nch, tables ? recs.p : nullptr, dout);
     count_launch();
     TCB_LAUNCH();
@@ -627,9 +645,9 @@ std::vector<ExOut> exact_serial(const u64* m, const u64* dec, const std::vector<
     for (const auto& g : segs) maxlen = std::max(maxlen, g.hi - g.lo);
     // few huge sums (the whole-core backward sums): longer chunks, a shorter walk
     if (njobs <= 4 && maxlen >= (u64{1} << 24))
-        run_exact<32>(m, dec, segs, kinds, d.p, s);
+        run_exact<256>(m, dec, segs, kinds, d.p, s);
     else
-        run_exact<8>(m, dec, segs, kinds, d.p, s);
+        run_exact<64>(m, dec, segs, kinds, d.p, s);
     d.download(out.data(), njobs);
     stream_sync(s);
     return out;

@@ -158,7 +158,7 @@ def test_encode_symbols_bit_exact(gpu_pkg, seed):
         assert gpu_pkg.encode_symbols(coder, []) == oracle.encode_symbols(coder, [])
 
 
-@pytest.mark.parametrize("kind", ["constant", "distinct", "long", "runs"])
+@pytest.mark.parametrize("kind", ["constant", "distinct", "long", "runs", "huge", "skewed"])
 def test_encode_symbols_model_edges(gpu_pkg, kind):
     """Chunked adaptive model: repeats inside a chunk, > 2048 distinct symbols
     (shared-memory model overflow -> global-scratch rerun), many halvings."""
@@ -169,6 +169,10 @@ def test_encode_symbols_model_edges(gpu_pkg, kind):
         syms = rng.permutation(np.arange(6000, dtype=np.uint64) * 2654435761 % (2 ** 32))
     elif kind == "long":
         syms = (rng.geometric(0.2, 40000) - 1).astype(np.uint64)
+    elif kind == "huge":  # thousands of output chunks, hundreds of halvings, carries across chunks
+        syms = (rng.geometric(0.02, 1_500_000) - 1).astype(np.uint64)
+    elif kind == "skewed":  # near-certain symbols: long 0xFF runs in the output, rare escapes
+        syms = np.where(rng.random(300_000) < 0.999, 0, rng.integers(1, 3000, 300_000)).astype(np.uint64)
     else:
         syms = np.repeat(rng.integers(0, 40, 700), rng.integers(1, 60, 700)).astype(np.uint64)
     assert gpu_pkg.encode_symbols(0, syms) == oracle.encode_symbols(0, syms)

@@ -14,7 +14,7 @@ re = float(sys.argv[1]) if len(sys.argv) > 1 else 1e-2
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 x = synth.grf_torch(n=n, kmax=n // 3)
 assert x.dtype == torch.float32 and x.is_cuda
-for it in range(2):
+for it in range(int(os.environ.get('C5_ITERS', '2'))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     r = tcb.compress_device(x.data_ptr(), x.numel() * 4, tcb.Dtype.float32, list(x.shape), tcb.Params(target_re=re))
@@ -22,6 +22,8 @@ for it in range(2):
     dt = time.perf_counter() - t0
     print(f"c5 n={n} re={re:g}: {dt * 1e3:.1f} ms, ranks {r.ranks}, bytes {len(r.container)}, "
           f"factor {r.compression_factor():.1f}, times {r.times}", flush=True)
+if os.environ.get('C5_NO_DEC'):
+    sys.exit(0)
 out = torch.empty(x.numel() * 4, dtype=torch.uint8, device="cuda")
 tcb.decompress_device(r.container, out.data_ptr(), out.numel())
 y = out.view(torch.float32).view(x.shape).double()
