@@ -228,65 +228,98 @@ __global__ void __launch_bounds__(128) ac_range_kernel(const u64* __restrict__ s
     const int j = static_cast<int>((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     if (j >= njobs) return;
     const int lane = threadIdx.x & 31;
+    __shared__ ulonglong2 stage[4][32];
+    const int wib = threadIdx.x >> 5;
     const JobDev jb = jobs[j];
     const u64 ns = counts[static_cast<u64>(j) * stride];
     if (ns == 0) {
         if (lane == 0) nout[j] = 0;
         return;
     }
-    const u64* rc = recs + jb.sym_off;
     const u64* sy = syms + jb.sym_off;
-    u64* w = W + jb.w_off;
-    auto ld_rec = [&](u64 k0) { return k0 + lane < ns ? rc[k0 + lane] : u64{0}; };
-    auto ld_raw = [&](u64 k0, u64 rec) { return ((rec >> 16) & 1u) ? static_cast<u32>(sy[k0 + lane]) : 0u; };
+    u64* const w0 = W + jb.w_off;
+    u64* w = w0;  // W[S]: running pointer (S = w - w0)
+    const bool l0 = lane == 0;
     u32 range = 0xFFFFFFFFu;
-    u64 acc = 0, S = 0;
-    u64 rec_a = ld_rec(0), rec_b = ld_rec(32);
-    u64 mag_a = magic[rec_a & 0xFFFFu];
-    u32 raw_a = ld_raw(0, rec_a);
-    for (u64 k0 = 0; k0 < ns; k0 += 32) {
-        const u64 rec_c = ld_rec(k0 + 64);
-        const u64 mag_b = magic[rec_b & 0xFFFFu];
-        const u32 raw_b = ld_raw(k0 + 32, rec_b);
-        const u32 L = static_cast<u32>(min(u64{32}, ns - k0));
-        for (u32 l = 0; l < L; ++l) {
-            const u64 rec = __shfl_sync(0xffffffffu, rec_a, l);
-            const u64 M = __shfl_sync(0xffffffffu, mag_a, l);
-            const u32 T = static_cast<u32>(rec & 0xFFFFu);
-            const u32 f = static_cast<u32>((rec >> 32) & 0xFFFFu);
-            const u32 cum = static_cast<u32>(rec >> 48);
-            u32 q = range;
-            if (T > 1) {
-                const u64 x = static_cast<u64>(range) * static_cast<u32>(M >> 32) + __umulhi(range, static_cast<u32>(M));
-                q = static_cast<u32>(x >> 32);
-            }
-            acc += static_cast<u64>(cum) * q;
-            range = q * f;
+    u64 acc = 0;
+    // 32 raw bits, MSB first, each encode(bit, 1, 2): with range in [2^24, 2^32)
+    // exactly floor(log2 range) - 23 halvings fit before a normalisation, so the
+    // bits go in groups: low += sum_j bit_j (range >> j), range >>= k
+    auto raw_bits = [&](u32 raw) {
+        int left = 32;
+        while (left > 0) {
+            const int kb = min(left, (31 - __clz(static_cast<int>(range))) - 23);
+            const u32 cb = (raw >> (left - kb)) & ((1u << kb) - 1u);
+            u64 add = 0;
+#pragma unroll
+            for (int jj = 1; jj <= 8; ++jj)
+                if (jj <= kb && ((cb >> (kb - jj)) & 1u)) add += range >> jj;
+            acc += add;
+            range >>= kb;
+            left -= kb;
             while (range < (1u << 24)) {
-                if (lane == 0) w[S] = acc;
-                ++S;
+                if (l0) *w = acc;
+                ++w;
                 acc = 0;
                 range <<= 8;
             }
-            if ((rec >> 16) & 1u) {  // 32 raw bits, MSB first, through encode(bit, 1, 2)
-                const u32 raw = __shfl_sync(0xffffffffu, raw_a, l);
-                int left = 32;
-                while (left > 0) {
-                    const int kb = min(left, (31 - __clz(static_cast<int>(range))) - 23);
-                    const u32 cb = (raw >> (left - kb)) & ((1u << kb) - 1u);
-                    u64 add = 0;
+        }
+    };
+    // the first symbol is always an escape against total 1: range / 1, cum 0, freq 1
+    raw_bits(static_cast<u32>(sy[0]));
+    // symbols 1.. : total >= 2 from here on
+    const u64* rc = recs + jb.sym_off + 1;
+    const u64* sy1 = sy + 1;
+    const u64 n1 = ns - 1;
+    auto ld_rec = [&](u64 k0) { return k0 + lane < n1 ? rc[k0 + lane] : u64{0}; };
+    auto ld_raw = [&](u64 k0, u64 rec) { return ((rec >> 16) & 1u) ? static_cast<u32>(sy1[k0 + lane]) : 0u; };
+    // one coding step: q = floor(range / T) by multiply-high with M = ceil(2^64 / T)
+    // (exact for range < 2^32, 1 < T < 2^16); q >= 2^8, so at most two shifts
+    auto step = [&](u64 rec, u64 M) {
+        const u32 hi = static_cast<u32>(rec >> 32);
+        const u32 t = __umulhi(range, static_cast<u32>(M));
+        const u32 q = static_cast<u32>((static_cast<u64>(range) * static_cast<u32>(M >> 32) + t) >> 32);
+        acc += static_cast<u64>(hi >> 16) * q;
+        const u32 rr = q * (hi & 0xFFFFu);
+        // every lane stores the running slot (identical values): the last store to
+        // a slot is its complete sum, a skipped slot gets its zero
+        w[0] = acc;
+        w[1] = 0;
+        const u32 r1 = rr < (1u << 24) ? rr << 8 : rr;
+        range = r1 < (1u << 24) ? r1 << 8 : r1;
+        const u32 sh = (rr < (1u << 24) ? 1u : 0u) + (rr < (1u << 16) ? 1u : 0u);
+        w += sh;
+        acc = sh ? 0 : acc;
+    };
+    u64 rec_a = ld_rec(0), rec_b = ld_rec(32);
+    u64 mag_a = magic[rec_a & 0xFFFFu];
+    u32 raw_a = ld_raw(0, rec_a);
+    for (u64 k0 = 0; k0 < n1; k0 += 32) {
+        const u64 rec_c = ld_rec(k0 + 64);
+        const u64 mag_b = magic[rec_b & 0xFFFFu];
+        const u32 raw_b = ld_raw(k0 + 32, rec_b);
+        const u32 L = static_cast<u32>(min(u64{32}, n1 - k0));
+        const unsigned escm = __ballot_sync(0xffffffffu, (rec_a >> 16) & 1u);
+        // the chunk's (record, reciprocal) pairs go through shared memory: the
+        // steps read them with broadcast loads the compiler issues ahead
+        __syncwarp();
+        stage[wib][lane] = make_ulonglong2(rec_a, mag_a);
+        __syncwarp();
+        for (u32 g = 0; g < L; g += 8) {
+            const unsigned em = (escm >> g) & 0xFFu;
+            if (em == 0 && g + 8 <= L) {
 #pragma unroll
-                    for (int jj = 1; jj <= 8; ++jj)
-                        if (jj <= kb && ((cb >> (kb - jj)) & 1u)) add += range >> jj;
-                    acc += add;
-                    range >>= kb;
-                    left -= kb;
-                    while (range < (1u << 24)) {
-                        if (lane == 0) w[S] = acc;
-                        ++S;
-                        acc = 0;
-                        range <<= 8;
-                    }
+                for (int u = 0; u < 8; ++u) {
+                    const ulonglong2 rm = stage[wib][g + u];
+                    step(rm.x, rm.y);
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (g + u >= L) break;
+                    const ulonglong2 rm = stage[wib][g + u];
+                    step(rm.x, rm.y);
+                    if ((em >> u) & 1u) raw_bits(__shfl_sync(0xffffffffu, raw_a, g + u));
                 }
             }
         }
@@ -296,9 +329,9 @@ __global__ void __launch_bounds__(128) ac_range_kernel(const u64* __restrict__ s
         rec_b = rec_c;
     }
     if (lane == 0) {  // flush: five shift_low calls
-        w[S] = acc;
-        for (int i = 1; i < 5; ++i) w[S + i] = 0;
-        nout[j] = S + 5;
+        w[0] = acc;
+        for (int i = 1; i < 5; ++i) w[i] = 0;
+        nout[j] = static_cast<u64>(w - w0) + 5;
     }
 }
 
