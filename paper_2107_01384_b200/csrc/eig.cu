@@ -376,6 +376,152 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_global(double* __restrict
     }
 }
 
+// ---------------------------------------------------------------- tridiagonalisation (whole GPU)
+// Large n: one persistent CTA per SM (cooperative launch), the matrix in L2.
+// Row r belongs to CTA r % G (warp (r / G) % nw).  Step k:
+//   1. wait for row k (the pivot row, updated eagerly by its owner at step
+//      k-1 and published with a release flag), read it; every CTA derives
+//      alpha / beta / tau / v redundantly (identical arithmetic, identical
+//      values everywhere);
+//   2. every owned row r > k takes the previous step's deferred rank-2 update
+//      (A_rj -= v_r w_j + w_r v_j) and, in the same pass, its dot product
+//      p_r = tau A_r . v: one read and one write of the trailing matrix per step;
+//   3. grid barrier (all of p), then every CTA forms K = tau/2 p.v and
+//      w = p - K v in the same fixed order;
+//   4. the owner of row k+1 applies this step's update to it at once (the next
+//      pivot row) and raises its flag; the other rows keep it deferred.
+// Same reflector convention and outputs as the cluster kernels.
+constexpr int kCoopThreads = 512;
+
+__device__ __forceinline__ void coop_barrier(unsigned* ctr, unsigned& phase) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ++phase;
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        const unsigned target = phase * gridDim.x;
+        while (*reinterpret_cast<volatile unsigned*>(ctr) < target) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kCoopThreads, 1) tridiag_coop(double* __restrict__ A, int n, double* __restrict__ d,
+                                                               double* __restrict__ e, double* __restrict__ V,
+                                                               double* __restrict__ tau, double* __restrict__ P,
+                                                               unsigned* __restrict__ ctr, int* __restrict__ flags) {
+    extern __shared__ double sh_coop[];
+    double* v = sh_coop;
+    double* w = v + n;
+    double* vp = w + n;
+    double* wp = vp + n;
+    double* red = wp + n;
+    const int G = static_cast<int>(gridDim.x), cta = static_cast<int>(blockIdx.x);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned phase = 0;
+    bool pend = false;  // a deferred update (vp, wp) of the previous step
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m = n - k - 1;
+        if (k > 0) {
+            if (threadIdx.x == 0) {
+                while (*reinterpret_cast<volatile int*>(flags + k) == 0) {
+                }
+                __threadfence();
+            }
+            __syncthreads();
+        }
+        double ss = 0.0;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const double x = __ldcg(A + static_cast<size_t>(k) * n + k + 1 + i);
+            v[i] = x;
+            ss += x * x;
+        }
+        const double alpha = sqrt(block_sum(ss, red));
+        const double x0 = v[0];
+        const double beta = x0 >= 0.0 ? -alpha : alpha;
+        __syncthreads();
+        if (threadIdx.x == 0) v[0] = x0 - beta;
+        __syncthreads();
+        double vv = 0.0;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) vv += v[i] * v[i];
+        vv = block_sum(vv, red);
+        const double t = (alpha == 0.0 || vv == 0.0) ? 0.0 : 2.0 / vv;
+        if (cta == 0) {
+            if (threadIdx.x == 0) {
+                e[k] = t == 0.0 ? x0 : beta;
+                tau[k] = t;
+                d[k] = __ldcg(A + static_cast<size_t>(k) * n + k);
+            }
+            for (int i = threadIdx.x; i < m; i += blockDim.x) V[static_cast<size_t>(k) * n + k + 1 + i] = v[i];
+        }
+        // owned rows r > k: deferred update of step k-1 (columns > k) + p_r
+        for (int q = warp;; q += nw) {
+            const int r = cta + G * q;
+            if (r >= n) break;
+            if (r <= k) continue;
+            double* row = A + static_cast<size_t>(r) * n + k + 1;
+            double s = 0.0;
+            if (pend) {
+                const double vr = vp[r - k], wr = wp[r - k];
+                for (int j = lane; j < m; j += 32) {
+                    const double a = __ldcg(row + j) - (vr * wp[j + 1] + wr * vp[j + 1]);
+                    row[j] = a;
+                    s += a * v[j];
+                }
+            } else {
+                for (int j = lane; j < m; j += 32) s += __ldcg(row + j) * v[j];
+            }
+            s = warp_sum(s);
+            if (lane == 0) P[r] = t * s;
+        }
+        coop_barrier(ctr, phase);
+        double pv = 0.0;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const double q = __ldcg(P + k + 1 + i);
+            w[i] = q;
+            pv += q * v[i];
+        }
+        const double K = 0.5 * t * block_sum(pv, red);
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            w[i] -= K * v[i];
+            vp[i] = v[i];
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += blockDim.x) wp[i] = w[i];
+        __syncthreads();
+        // vp / wp now index rows k+1+i: shift by one so that vp[r - (k+1)] ... the
+        // next step reads vp[r - (k + 1)] as vp[r - k'] with k' = k + 1
+        pend = t != 0.0;
+        if ((k + 1) % G == cta && warp == 0) {  // the next pivot row, at once
+            double* row = A + static_cast<size_t>(k + 1) * n + k + 1;
+            if (pend) {
+                const double v0 = v[0], w0 = w[0];
+                for (int j = lane; j < m; j += 32) row[j] = __ldcg(row + j) - (v0 * w[j] + w0 * v[j]);
+            }
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicExch(flags + k + 1, 1);
+        }
+        __syncthreads();
+    }
+    // the last two rows: row n-2 is current (pivot update), row n-1 takes its deferred update
+    coop_barrier(ctr, phase);
+    if (n >= 2 && cta == (n - 1) % G && threadIdx.x == 0) {
+        const int k = n - 2;  // vp/wp belong to step k-1 = n-3; row n-1 <-> index 1
+        double a_nn = __ldcg(A + static_cast<size_t>(n - 1) * n + n - 1);
+        double a_n1 = __ldcg(A + static_cast<size_t>(n - 1) * n + n - 2);
+        if (pend && n >= 3) {
+            const double vr = vp[(n - 1) - k], wr = wp[(n - 1) - k];
+            a_nn -= vr * wp[(n - 1) - k] + wr * vp[(n - 1) - k];
+            a_n1 -= vr * wp[(n - 2) - k] + wr * vp[(n - 2) - k];
+        }
+        d[n - 2] = __ldcg(A + static_cast<size_t>(n - 2) * n + n - 2);
+        e[n - 2] = a_n1;
+        d[n - 1] = a_nn;
+    }
+}
+
 // ---------------------------------------------------------------- eigenvalues
 __device__ __forceinline__ double frcp(double q) {
     double y;
@@ -1054,6 +1200,30 @@ SideStream& side_stream() {  // one per host thread and device
 }
 }  // namespace
 
+// the whole-GPU tridiagonalisation (false: not co-resident, use the cluster kernel)
+bool coop_tridiag(double* A, int n, double* d, double* e, double* V, double* tau, double* P, cudaStream_t s) {
+    if (std::getenv("TCB_TRIDIAG_CLUSTER")) return false;
+    int dev = 0, coop = 0;
+    TCB_CUDA(cudaGetDevice(&dev));
+    TCB_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    const size_t smem = (4 * static_cast<size_t>(n) + 32) * sizeof(double);
+    if (!coop || smem > 220 * 1024) return false;
+    TCB_CUDA(cudaFuncSetAttribute(tridiag_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int per_sm = 0;
+    TCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tridiag_coop, kCoopThreads, smem));
+    if (per_sm < 1) return false;
+    int G = std::min(sm_count(), n);
+    DevBuf<unsigned> ctr(1, s);
+    DevBuf<int> flags(n, s);
+    ctr.zero();
+    flags.zero();
+    void* args[] = {&A, &n, &d, &e, &V, &tau, &P, &ctr.p, &flags.p};
+    TCB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tridiag_coop), dim3(G), dim3(kCoopThreads), args,
+                                         smem, s));
+    count_launch();
+    return true;
+}
+
 std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_t s) {
     ProfScope prof_scope(kEig, s);
     const int n = static_cast<int>(n64);
@@ -1105,14 +1275,16 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
             if (dsmem) TCB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_dsmem, A, n, w.d.p, w.e.p, w.z.p, w.tau.p));
         }
         if (!dsmem) {
-            cfg.gridDim = dim3(kCluster);
-            cfg.blockDim = dim3(kTriThreads);
-            at[0].val.clusterDim.x = kCluster;
             w.a = DevBuf<double>(n64 * n64, s);
             DevBuf<double> P(n64, s);
             TCB_CUDA(cudaMemcpyAsync(w.a.p, A, n64 * n64 * sizeof(double), cudaMemcpyDeviceToDevice, s));
-            cfg.dynamicSmemBytes = (2 * n + 32) * sizeof(double);
-            TCB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_global, w.a.p, n, w.d.p, w.e.p, w.z.p, w.tau.p, P.p));
+            if (!coop_tridiag(w.a.p, n, w.d.p, w.e.p, w.z.p, w.tau.p, P.p, s)) {
+                cfg.gridDim = dim3(kCluster);
+                cfg.blockDim = dim3(kTriThreads);
+                at[0].val.clusterDim.x = kCluster;
+                cfg.dynamicSmemBytes = (2 * n + 32) * sizeof(double);
+                TCB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_global, w.a.p, n, w.d.p, w.e.p, w.z.p, w.tau.p, P.p));
+            }
         }
         count_launch();
     }
