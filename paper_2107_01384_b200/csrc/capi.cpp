@@ -281,6 +281,15 @@ bool host_release(void* p) {
     return true;
 }
 
+void host_free_any(void* p) {
+    if (p && !host_release(p)) std::free(p);
+}
+// compress results (container bytes) come from the pinned pool too
+const bool g_result_alloc_installed = [] {
+    set_result_allocator(host_alloc, host_free_any);
+    return true;
+}();
+
 template <class T>
 T* dup(const std::vector<T>& v) {
     T* p = static_cast<T*>(std::malloc(v.size() * sizeof(T) + 1));
@@ -306,10 +315,10 @@ Params to_params(const tcb_params* p, int d) {
     return o;
 }
 
-void fill(const Result& r, int d, tcb_result* out) {
+void fill(Result& r, int d, tcb_result* out) {
     std::memset(out, 0, sizeof(*out));
-    out->container = dup(r.container);
     out->container_size = r.container.size();
+    out->container = r.container.release();  // from host_alloc (installed below): tcb_free releases it
     out->truncation_sse = r.trunc;
     out->core_quantization_sse = r.core_quant;
     for (int i = 0; i < d && i < 8; ++i) {
@@ -454,7 +463,7 @@ int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_
         DevBuf<double> g0, ws;
         if (!upload_overlapping_gram(bytes + skip, nbytes - skip, dtype, sh, prm, dev.p, g0, ws, st.s))
             dev.upload(bytes + skip, nbytes - skip);
-        const Result r = compress_device(dev.p, nbytes - skip, dtype, sh, prm, st.s, g0.p);
+        Result r = compress_device(dev.p, nbytes - skip, dtype, sh, prm, st.s, g0.p);
         host_trace_dump();
         fill(r, d, out);
     });
@@ -488,7 +497,7 @@ int tcb_compress_sharded_device(void* comm, int world, int rank, const void* dev
         sc.world = world;
         sc.rank = rank;
         sc.local_extent = local_extent;
-        const Result r = compress_device(device_bytes, nbytes, dtype, sh, to_params(params, d), st.s, nullptr, &sc);
+        Result r = compress_device(device_bytes, nbytes, dtype, sh, to_params(params, d), st.s, nullptr, &sc);
         host_trace_dump();
         fill(r, d, out);
     });
@@ -499,7 +508,7 @@ int tcb_compress_device(const void* device_bytes, uint64_t nbytes, int dtype, co
     return guard([&] {
         std::vector<u64> sh(shape, shape + d);
         Stream st;
-        const Result r = compress_device(device_bytes, nbytes, dtype, sh, to_params(params, d), st.s);
+        Result r = compress_device(device_bytes, nbytes, dtype, sh, to_params(params, d), st.s);
         host_trace_dump();
         fill(r, d, out);
     });
@@ -904,7 +913,7 @@ int tcb_dev_encode_tucker(const double* core, const double* const* factors, cons
             TCB_CUDA(cudaMemcpyAsync(f.factors[i].p, factors[i], n[i] * r[i] * sizeof(double),
                                      cudaMemcpyDeviceToDevice, st.s));
         }
-        const Result res = encode_tucker_device(f, dtype, norm_sq, target_sse, to_params(params, d), st.s);
+        Result res = encode_tucker_device(f, dtype, norm_sq, target_sse, to_params(params, d), st.s);
         fill(res, d, out);
     });
 }

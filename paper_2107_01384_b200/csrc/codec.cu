@@ -1224,59 +1224,87 @@ std::vector<u64> probe_entropy_bytes(ProbeCache& c, int p) {
     return out;
 }
 
-EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
-                       const u64* stops_host, int coder, bool want_body, cudaStream_t s) {
-    EmitResult res;
+namespace {
+// symbols + entropy coding of planes [last_plane, top_plane]; lengths on the host
+struct Emitted {
+    Layout L;
+    Coded c;
+    std::vector<u64> el;
+    std::vector<StreamOut> soh;
+};
+bool emit_code(Emitted& E, const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
+               const u64* stops_host, int coder, cudaStream_t s) {
     if (coder != 0 && coder != 1) throw Error("entropy: unknown coder");
     const u64 nb = n == 0 ? 0 : (n + block - 1) / block;
     const int np = top_plane - last_plane + 1;
     const u64 ns = nb * static_cast<u64>(np);
-    if (ns == 0 || np <= 0) return res;
+    if (ns == 0 || np <= 0) return false;
     HostTrace ht_a("emit: symbols+entropy+sync");
     const auto hist = msb_histogram(m, n, block, s);
-    const Layout L = make_layout(hist, n, block, last_plane, top_plane, stops_host, coder);
-    Coded c;
-    code_streams(c, L, m, neg, coder, s);
-    std::vector<u64> el(ns);
-    std::vector<StreamOut> soh(ns);
-    c.elen.download(el.data(), ns);
-    c.so.download(soh.data(), ns);
+    E.L = make_layout(hist, n, block, last_plane, top_plane, stops_host, coder);
+    code_streams(E.c, E.L, m, neg, coder, s);
+    E.el.resize(ns);
+    E.soh.resize(ns);
+    E.c.elen.download(E.el.data(), ns);
+    E.c.so.download(E.soh.data(), ns);
     stream_sync(s);
-    for (u64 v : el)
+    for (u64 v : E.el)
         if (v == ~u64{1}) throw Error("entropy: cannot normalize rans table");
     if (std::getenv("TCB_AC_STATS")) {
         u64 mx = 0, tot = 0, eb = 0, rb = 0;
         for (u64 i = 0; i < ns; ++i) {
-            mx = std::max(mx, soh[i].nsyms);
-            tot += soh[i].nsyms;
-            eb += el[i];
-            rb += (soh[i].nraw + 7) / 8;
+            mx = std::max(mx, E.soh[i].nsyms);
+            tot += E.soh[i].nsyms;
+            eb += E.el[i];
+            rb += (E.soh[i].nraw + 7) / 8;
         }
         std::fprintf(stderr, "[ac stats] planes %d..%d streams %llu symbols %llu (max %llu) entropy %llu B raw %llu B\n",
                      last_plane, top_plane, (unsigned long long)ns, (unsigned long long)tot, (unsigned long long)mx,
                      (unsigned long long)eb, (unsigned long long)rb);
     }
-    res.entropy_bytes = el;
-    ht_a.stop();
-    if (!want_body) return res;
-    HostTrace ht_b("emit: assemble+sync");
+    return true;
+}
+}  // namespace
+
+EmitDev emit_planes_device(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
+                           const u64* stops_host, int coder, cudaStream_t s) {
+    EmitDev out;
+    Emitted E;
+    if (!emit_code(E, m, neg, n, block, last_plane, top_plane, stops_host, coder, s)) return out;
+    const u64 ns = E.el.size();
+    HostTrace ht_b("emit: assemble");
     std::vector<u64> off(ns);
     u64 tot = 0;
     for (u64 i = 0; i < ns; ++i) {
         off[i] = tot;
-        tot += 4 + 4 + el[i] + (soh[i].nraw + 7) / 8;
+        tot += 4 + 4 + E.el[i] + (E.soh[i].nraw + 7) / 8;
     }
     DevBuf<u64> doff(ns, s);
     doff.upload(off.data(), ns);
-    DevBuf<u8> body(tot, s);
+    out.body = DevBuf<u8>(tot, s);
+    out.size = tot;
     ProfScope pz(kEmit, s);
-    assemble_kernel<<<static_cast<unsigned>(ns), 128, 0, s>>>(c.ent.p, c.dad.p, c.elen.p, c.raw.p, c.dsd.p, c.so.p,
-                                                               doff.p, body.p);
+    assemble_kernel<<<static_cast<unsigned>(ns), 128, 0, s>>>(E.c.ent.p, E.c.dad.p, E.c.elen.p, E.c.raw.p, E.c.dsd.p,
+                                                               E.c.so.p, doff.p, out.body.p);
     count_launch();
     TCB_LAUNCH();
-    res.body.resize(tot);
-    body.download(res.body.data(), tot);
+    out.entropy_bytes = std::move(E.el);
+    return out;
+}
+
+EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
+                       const u64* stops_host, int coder, bool want_body, cudaStream_t s) {
+    EmitResult res;
+    if (!want_body) {
+        Emitted E;
+        if (emit_code(E, m, neg, n, block, last_plane, top_plane, stops_host, coder, s)) res.entropy_bytes = std::move(E.el);
+        return res;
+    }
+    EmitDev d = emit_planes_device(m, neg, n, block, last_plane, top_plane, stops_host, coder, s);
+    res.body.resize(d.size);
+    if (d.size) d.body.download(res.body.data(), d.size);
     stream_sync(s);
+    res.entropy_bytes = std::move(d.entropy_bytes);
     return res;
 }
 

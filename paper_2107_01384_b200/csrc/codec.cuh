@@ -61,6 +61,14 @@ struct EmitResult {
     std::vector<u8> body;  // concatenated (u32 size || payload) for every (plane, block)
     std::vector<u64> entropy_bytes;  // per stream, for split-plane priority probes
 };
+// the same with the assembled body left in device memory
+struct EmitDev {
+    DevBuf<u8> body;
+    u64 size = 0;
+    std::vector<u64> entropy_bytes;
+};
+EmitDev emit_planes_device(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
+                           const u64* stops_host, int coder, cudaStream_t s);
 EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
                        const u64* stops_host /*2*nb, for last_plane*/, int coder, bool want_body,
                        cudaStream_t s);

@@ -233,10 +233,11 @@ PlanResult plan_stream(const u64* m, u64 n, double target_int, const EncodeOpts&
     return pl.run(dec);
 }
 
-std::vector<u8> finalize_stream(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,
-                                cudaStream_t s) {
+StreamParts finalize_stream_parts(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,
+                                  cudaStream_t s) {
     const u64 nb = n == 0 ? 0 : (n + pl.block - 1) / pl.block;
-    std::vector<u8> o;
+    StreamParts out;
+    std::vector<u8>& o = out.head;
     put_le(o, count, 8);
     put_le(o, pl.block, 8);
     o.push_back(static_cast<u8>(pl.last_plane));
@@ -248,9 +249,21 @@ std::vector<u8> finalize_stream(const u64* m, const u8* neg, u64 n, const PlanRe
     put_le(o, static_cast<u64>(pl.nplanes), 4);
     if (pl.nplanes > 0 && nb > 0) {
         HostTrace ht("finalize: emit_planes");
-        const auto er = emit_planes(m, neg, n, pl.block, pl.last_plane, 63, pl.stops.data(), coder, true, s);
-        o.insert(o.end(), er.body.begin(), er.body.end());
+        EmitDev er = emit_planes_device(m, neg, n, pl.block, pl.last_plane, 63, pl.stops.data(), coder, s);
+        out.body = std::move(er.body);
+        out.body_size = er.size;
     }
+    return out;
+}
+
+std::vector<u8> finalize_stream(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,
+                                cudaStream_t s) {
+    StreamParts p = finalize_stream_parts(m, neg, n, pl, coder, count, s);
+    std::vector<u8> o = std::move(p.head);
+    const std::size_t h = o.size();
+    o.resize(h + p.body_size);
+    if (p.body_size) p.body.download(o.data() + h, p.body_size);
+    stream_sync(s);
     return o;
 }
 

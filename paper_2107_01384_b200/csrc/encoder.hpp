@@ -37,6 +37,15 @@ u64 default_block(u64 n);
 // arithmetic would; `dec` receives the decoder-side magnitudes.
 PlanResult plan_stream(const u64* m, u64 n, double target_int, const EncodeOpts& o, u64* dec, cudaStream_t s);
 
+// finalize() in two parts: the section head (count, block, last plane, stops,
+// plane count) on the host and the (u32 size || payload) body left on the device.
+struct StreamParts {
+    std::vector<u8> head;
+    DevBuf<u8> body;
+    u64 body_size = 0;
+};
+StreamParts finalize_stream_parts(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,
+                                  cudaStream_t s);
 // finalize(): emits planes [last_plane, 63] with the given signs and returns
 // the serialized stream section (container.cpp:231-247) for `count` elements.
 std::vector<u8> finalize_stream(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,

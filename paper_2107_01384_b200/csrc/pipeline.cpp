@@ -181,6 +181,40 @@ __attribute__((unused)) void sync(cudaStream_t s) { stream_sync(s); }
 
 }  // namespace
 
+namespace {
+void* (*g_res_alloc)(std::size_t) = nullptr;
+void (*g_res_release)(void*) = nullptr;
+}  // namespace
+
+void set_result_allocator(void* (*alloc)(std::size_t), void (*release)(void*)) {
+    g_res_alloc = alloc;
+    g_res_release = release;
+}
+
+HostBytes::HostBytes(std::size_t bytes) : n(bytes) {
+    p = static_cast<u8*>(g_res_alloc ? g_res_alloc(bytes + 1) : std::malloc(bytes + 1));
+    if (!p) throw Error("compress: out of host memory");
+}
+HostBytes& HostBytes::operator=(HostBytes&& o) noexcept {
+    if (this != &o) {
+        this->~HostBytes();
+        p = o.p;
+        n = o.n;
+        o.p = nullptr;
+        o.n = 0;
+    }
+    return *this;
+}
+HostBytes::~HostBytes() {
+    if (p) (g_res_release ? g_res_release : std::free)(p);
+    p = nullptr;
+}
+HostBytes HostBytes::from(const std::vector<u8>& v) {
+    HostBytes h(v.size());
+    if (!v.empty()) std::memcpy(h.p, v.data(), v.size());
+    return h;
+}
+
 std::vector<u64> stable_ascending(const std::vector<u64>& s) {
     std::vector<u64> p(s.size());
     std::iota(p.begin(), p.end(), u64{0});
@@ -679,7 +713,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
         res.estimate = trunc;
         w.f64v(0.0);
         w.f64v(trunc);
-        res.container = std::move(w.b);
+        res.container = HostBytes::from(w.b);
         res.times.total = ms_since(t_all);
         return;
     }
@@ -865,11 +899,11 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     sign_fold(neg.p, cs, flips_axis, s, vorder.p);
     u64 count = 1;
     for (auto v : f.r) count *= v;
-    std::vector<u8> core_stream;
+    StreamParts core_stream;
     double ach;
     {
         HostTrace ht("encode: core finalize+sum");
-        core_stream = finalize_stream(mag.p, neg.p, nc, plan, prm.coder, count, s);
+        core_stream = finalize_stream_parts(mag.p, neg.p, nc, plan, prm.coder, count, s);
         // achieved_sse_int, accumulated backward (core_codec.cpp:405-411)
         ach = exact_backward_sum(kExDiff, 0, mag.p, dec.p, nc, s);
     }
@@ -888,6 +922,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     w.f64v(est);
 
     t0 = Clock::now();
+    std::vector<std::vector<u8>> fsec(d);
     for (std::size_t i = 0; i < d; ++i) {
         W fw;
         const auto& fi = fe[i];
@@ -905,9 +940,16 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
         w.u64v(fw.b.size());
         w.raw(fw.b);
     }
-    w.u64v(core_stream.size());
-    w.raw(core_stream);
-    res.container = std::move(w.b);
+    // the core section's body goes from the device straight into its place
+    const u64 core_len = core_stream.head.size() + core_stream.body_size;
+    w.u64v(core_len);
+    w.raw(core_stream.head);
+    res.container = HostBytes(w.b.size() + core_stream.body_size);
+    std::memcpy(res.container.data(), w.b.data(), w.b.size());
+    if (core_stream.body_size)
+        TCB_CUDA(cudaMemcpyAsync(res.container.data() + w.b.size(), core_stream.body.p, core_stream.body_size,
+                                 cudaMemcpyDeviceToHost, s));
+    stream_sync(s);
     res.times.serialize = ms_since(t0);
     res.times.total = ms_since(t_all);
     res.peak_alloc = 2 * n_el * 8 + nc * 9 + res.container.size() * 2;

@@ -30,8 +30,35 @@ struct Times {
     double sthosvd = 0, quantize = 0, core = 0, factor = 0, serialize = 0, total = 0;
 };
 
+// Container bytes handed to the caller.  The memory comes from the result
+// allocator (the C ABI installs its pinned-block pool, so the core payload's
+// device-to-host copy lands in place at full PCIe rate); release() passes
+// ownership on.
+void set_result_allocator(void* (*alloc)(std::size_t), void (*release)(void*));
+struct HostBytes {
+    u8* p = nullptr;
+    std::size_t n = 0;
+    HostBytes() = default;
+    explicit HostBytes(std::size_t bytes);
+    HostBytes(const HostBytes&) = delete;
+    HostBytes& operator=(const HostBytes&) = delete;
+    HostBytes(HostBytes&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    HostBytes& operator=(HostBytes&& o) noexcept;
+    ~HostBytes();
+    u8* data() { return p; }
+    const u8* data() const { return p; }
+    std::size_t size() const { return n; }
+    u8* release() {
+        u8* q = p;
+        p = nullptr;
+        n = 0;
+        return q;
+    }
+    static HostBytes from(const std::vector<u8>& v);
+};
+
 struct Result {
-    std::vector<u8> container;
+    HostBytes container;
     double trunc = 0, core_quant = 0, estimate = 0, norm_sq = 0, target_sse = 0;
     std::vector<double> factor_terms;
     std::vector<u64> ranks;
