@@ -3,15 +3,17 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Workload (configs[1] of BASELINE.json): c2 = 256^3 fp64 tensor, 64 separable
-sinusoid terms with k^-1.5 amplitudes + N(0,1e-5) noise (seeded synthetic —
-the paper's datasets are not available), requested relative error 1e-4.
-A step = one pipeline::compress of that tensor (device-resident input ->
-container bytes on the host).  Inputs are 128 MiB (> L2 is 126 MB) and L2 is
-additionally flushed (256 MiB write) before every timed step, outside the
-per-step CUDA-event window.  N > 1 (or --sharded): the ranks compress ONE
-256 x 256 x (256 N) tensor sharded along its last processed mode (NCCL
-all-reduce of partial Grams; weak scaling, 128 MiB per rank), max over ranks.
+Headline workload (BASELINE.json configs[4], the config the metric is quoted
+on at 1/2/4/8 B200): c5 = 1024^3 fp32 Gaussian random field, E(k) ~ k^-5/3 for
+k <= 341, seeded torch FFT on the GPU (synthetic: the paper's datasets are not
+available), requested relative error 1e-2, reference-default parameters
+(fp64 internal, rtmss 0.5, AC coder, split planes).  A step = one
+pipeline::compress of that tensor (device-resident input -> container bytes in
+host memory).  The input is 4 GiB (> the 126 MB L2), so no flush is needed.
+The same JSON line carries c5 @ 1e-3 and c2 (256^3 fp64 @ 1e-4) as secondary
+device-resident measurements.  N > 1: the ranks compress ONE c5 tensor sharded
+along its last processed mode (strong scaling; NCCL all-reduce of partial
+Grams), max over ranks.
 """
 from __future__ import annotations
 
@@ -28,7 +30,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = "c2: 256^3 fp64, 64 separable k^-1.5 sinusoid terms + N(0,1e-5), RE 1e-4"
+WORKLOAD = "c5: 1024^3 fp32 Gaussian random field E(k)~k^-5/3 (k<=341), seeded torch FFT, RE 1e-2"
+C2_WORKLOAD = "c2: 256^3 fp64, 64 separable k^-1.5 sinusoid terms + N(0,1e-5), RE 1e-4"
+CPU_SAMPLE_N = 384  # bounded CPU sample: the c5 generator at 384^3 (kmax = n/3)
 METRIC = "compress throughput GB/s (input bytes)"
 STAGES = ["ingest", "permute", "gram", "eig", "ttm", "quant", "stats", "emit", "ac", "factor", "sum"]
 
@@ -153,18 +157,29 @@ def cpu_reference_step(x, re):
     return time.perf_counter() - t0, info
 
 
+def c5_tensor(n=1024, seed=0):
+    """c5 (or its n^3 sample): the BASELINE GRF generator on the GPU, float32, kmax = n // 3."""
+    import synth
+
+    return synth.grf_torch(n=n, kmax=n // 3, seed=seed)
+
+
+def cpu_sample(seed=0):
+    """The bounded CPU sample of the c5 workload: the same generator at 384^3 (1/19 of the bytes; the
+    per-byte Gram/TTM work grows with the mode size, so this overstates the CPU's c5 throughput)."""
+    return c5_tensor(CPU_SAMPLE_N, seed).cpu().numpy()
+
+
 def run_reference(args):
     rank, _, world = _env_rank()
     if rank != 0:
         return
-    import synth
-
     import oracle
 
     nth = oracle.threads()
-    x = synth.make("c2", seed=0)
+    x = cpu_sample()
     nbytes = x.nbytes
-    for _ in range(args.warmup_ref):
+    for _ in range(args.warmup):
         cpu_reference_step(x, args.re)
     times = []
     for _ in range(args.steps):
@@ -174,12 +189,14 @@ def run_reference(args):
     value = nbytes * len(times) / tot / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup_ref, "ms_per_step": 1e3 * tot / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "input_bytes": nbytes, "ranks": info.ranks},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "re": args.re, "l2": "input larger than L2 (4 GiB)"},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": nth, "kind": "port",
-                         "sample": f"full c2 compress per step (oracle/ restatement of the reference path; "
-                                   f"Gram and projection loops OpenMP-parallel over {nth} host threads)"},
+                         "sample": f"each step one full compress of the c5 generator at {CPU_SAMPLE_N}^3 "
+                                   f"({nbytes} B, RE {args.re}) by oracle/ (restatement of the reference path, "
+                                   f"integer half pinned to the reference's own code; Gram and projection loops "
+                                   f"OpenMP-parallel over {nth} host threads)"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -187,9 +204,7 @@ def run_reference(args):
 
 def c2_slab(world, rank, seed=0):
     """Rank `rank`'s 256^3 slab (along mode 2) of the weak-scaled c2-family
-    tensor 256 x 256 x (256 world): the c2 generator (64 separable k^-1.5
-    sinusoid terms, x = i/n per mode) on the global extents, plus independent
-    N(0, 1e-5) noise per slab."""
+    tensor 256 x 256 x (256 world)."""
     rng = np.random.default_rng(seed)
     shape = (256, 256, 256 * world)
     K = 64
@@ -208,10 +223,10 @@ def c2_slab(world, rank, seed=0):
 
 
 def main_sharded(args, rank, local, world):
-    """N ranks compress ONE tensor 256 x 256 x (256 N) sharded along its last
-    processed mode (shard.py: partial Grams all-reduced over NCCL, replicated
-    eigensolve, shard-local TTM, gather before the last step, rank 0 encodes).
-    Weak scaling: 128 MiB per rank; value = N x 128 MiB / max-over-ranks time."""
+    """N ranks compress ONE c5 tensor (1024^3 fp32) sharded along its last
+    processed mode: rank k holds slab k of mode 2 (library path: partial Grams
+    all-reduced over NCCL, replicated eigensolve, shard-local TTM, gather before
+    the last step).  Strong scaling: value = 4 GiB / max-over-ranks time."""
     import torch
     import torch.distributed as dist
 
@@ -221,12 +236,13 @@ def main_sharded(args, rank, local, world):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    xs = c2_slab(world, rank)
-    shape = [256, 256, 256 * world]
-    nbytes = xs.nbytes
-    host = torch.from_numpy(xs).pin_memory()
-    d_in = host.to(dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    full = c5_tensor()
+    shape = list(full.shape)
+    lo, hi = shard.shard_bounds(shape[2], world, rank)
+    xs = full[:, :, lo:hi].contiguous()
+    del full
+    torch.cuda.empty_cache()
+    total_bytes = 4 * shape[0] * shape[1] * shape[2]
     params = tcb.Params(target_re=args.re)
 
     def barrier():
@@ -235,30 +251,29 @@ def main_sharded(args, rank, local, world):
         torch.cuda.synchronize()
 
     def step(x):
-        return shard.compress_sharded(x, shape, tcb.Dtype.float64, params)
+        return shard.compress_sharded(x, shape, tcb.Dtype.float32, params)
 
     for _ in range(args.warmup):
-        res = step(d_in)
+        res = step(xs)
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = tcb.kernel_launches()
     step_ms = []
     for _ in range(args.steps):
-        flush.fill_(1)
         barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
-        res = step(d_in)
+        res = step(xs)
         b.record()
         b.synchronize()
         step_ms.append(a.elapsed_time(b))
     barrier()
     launches = (tcb.kernel_launches() - launches0) // max(1, args.steps)
+    host = xs.cpu().pin_memory()
     e2e_ms = []
-    for _ in range(args.steps):  # e2e: this rank's slab from pinned host memory, container to rank 0's host
-        flush.fill_(1)
+    for _ in range(max(1, min(args.steps, 5))):  # this rank's slab from pinned host memory
         barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
@@ -269,38 +284,24 @@ def main_sharded(args, rank, local, world):
         e2e_ms.append(a.elapsed_time(b))
     barrier()
     clk = clocks.stop()
-    t = torch.tensor([sum(step_ms), sum(e2e_ms)], dtype=torch.float64, device=dev)
+    t = torch.tensor([sum(step_ms) / len(step_ms), sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    tot, tot_e2e = float(t[0]), float(t[1])
-    value = world * nbytes * args.steps / (tot * 1e-3) / 1e9
-    e2e = world * nbytes * args.steps / (tot_e2e * 1e-3) / 1e9
+    ms, ms_e2e = float(t[0]), float(t[1])
+    value = total_bytes / (ms * 1e-3) / 1e9
+    e2e = total_bytes / (ms_e2e * 1e-3) / 1e9
     if rank == 0:
-        order = [0, 1, 2]
-        gram_flop, ttm_flop = algorithmic_work(shape, res.ranks, order)
-        per_rank = (gram_flop + ttm_flop) / world
-        ach = per_rank / (tot / args.steps * 1e-3) / 1e12
-        L = tcb.lib()
-        import ctypes as C
-
-        L.tcb_peak_dmma_tflops.restype = C.c_double
-        peak = float(L.tcb_peak_dmma_tflops())
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"c2 family weak-scaled: 256 x 256 x {256 * world} fp64 (128 MiB per rank), "
-                                   f"RE {args.re}", "input_bytes": world * nbytes, "ranks": res.ranks,
-                       "container_bytes": len(res.container), "l2": "256 MiB flush before every timed step; "
-                       "128 MiB per rank > L2",
+            "config": {"workload": WORKLOAD, "re": args.re, "input_bytes": total_bytes, "ranks": res.ranks,
+                       "container_bytes": len(res.container), "l2": "input larger than L2",
                        "parallelism": f"shard mode 2 over {world} ranks (NCCL all-reduce of partial Grams, "
-                                      f"replicated eigensolve, shard-local TTM)"},
-            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": nbytes,
+                                      f"replicated eigensolve, shard-local TTM, rank 0 encodes)"},
+            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": int(host.numel() * 4),
                     "d2h_bytes_per_step": len(r2.container)},
             "gpu_launches": int(launches),
-            "roofline": {"kernel": "per-rank Gram + TTM (whole step as the time base)", "bound": "tensor",
-                         "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
-                         "note": "lower bound: the step also holds the eigensolves and the encode"},
             "cpu_baseline": None,
             "clocks": clk,
             "step_ms_all": [round(v, 3) for v in step_ms],
@@ -311,260 +312,211 @@ def main_sharded(args, rank, local, world):
         dist.destroy_process_group()
 
 
+def device_steps(tcb, x_dev, nbytes, dtype, shape, params, steps, warmup):
+    """compress_device on a resident input: per-step CUDA events (the input exceeds L2)."""
+    import torch
+
+    res = None
+    for _ in range(warmup):
+        res = tcb.compress_device(x_dev.data_ptr(), nbytes, dtype, shape, params)
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(steps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        res = tcb.compress_device(x_dev.data_ptr(), nbytes, dtype, shape, params)
+        b.record()
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    return res, ms
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--re", type=float, default=1e-4)
+    ap.add_argument("--re", type=float, default=1e-2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="sharded one-tensor path also at N=1")
     args = ap.parse_args()
-    args.warmup_ref = min(args.warmup, 1)
     if args.impl == "reference":
         run_reference(args)
         return
     rank, local, world = _env_rank()
-    if world > 1 or args.sharded:
-        import torch
+    import torch
 
-        torch.cuda.set_device(local)
+    torch.cuda.set_device(local)
+    if world > 1 or args.sharded:
         main_sharded(args, rank, local, world)
         return
 
-    import torch
+    import ctypes as C
 
     import paper_2107_01384_b200 as tcb
     import synth
 
-    rank, local, world = _env_rank()
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
-    x = synth.make("c2", seed=rank)
-    nbytes = x.nbytes
-    host = torch.from_numpy(x.view(np.uint8).reshape(-1)).pin_memory()
-    d_in = host.to(dev, non_blocking=False)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    params = tcb.Params(target_re=args.re)
     L = tcb.lib()
+    x = c5_tensor()
+    shape = list(x.shape)
+    nbytes = x.numel() * 4
+    params = tcb.Params(target_re=args.re)
 
-    def step_device():
-        return tcb.compress_device(d_in.data_ptr(), nbytes, tcb.Dtype.float64, x.shape, params)
-
-    for _ in range(args.warmup):
-        res = step_device()
-    torch.cuda.synchronize()
-
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-
-    # ---- device-resident timed region
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = tcb.kernel_launches()
-    barrier()
-    step_ms = []
-    for _ in range(args.steps):
-        flush.fill_(1)
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record()
-        res = step_device()
-        b.record()
-        b.synchronize()
-        step_ms.append(a.elapsed_time(b))
-    barrier()
-    launches = (tcb.kernel_launches() - launches0) // max(1, args.steps)
-    # ---- end to end: pinned host bytes in, container bytes out (same W untimed warm-up)
-    src = tcb.SourceBuffer(memoryview(host.numpy()), tcb.Dtype.float64, x.shape)
-    for _ in range(args.warmup):
+    res, step_ms = device_steps(tcb, x, nbytes, tcb.Dtype.float32, shape, params, args.steps, args.warmup)
+    launches = (tcb.kernel_launches() - launches0) // max(1, args.steps + args.warmup)
+    # ---- end to end through the public host API: pinned input bytes in, container bytes out
+    host = x.cpu().pin_memory()
+    src = tcb.SourceBuffer(memoryview(host.numpy()).cast("B"), tcb.Dtype.float32, shape)
+    for _ in range(max(1, args.warmup // 2)):
         tcb.compress(src, params)
     torch.cuda.synchronize()
     e2e_ms = []
     for _ in range(args.steps):
-        flush.fill_(1)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
         a.record()
-        r2 = tcb.compress(src, params)
+        r2 = tcb.compress(src, params)  # synchronous: returns with the container in host memory
         b.record()
         b.synchronize()
         e2e_ms.append(a.elapsed_time(b))
-    barrier()
-    # ---- decompress of the same container: device-resident output, and
-    # end to end (container bytes in from the host, source-dtype bytes out to the host)
-    d_out = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    cont = res.container
-    for _ in range(args.warmup):
-        tcb.decompress_device(cont, d_out.data_ptr(), nbytes)
-        del_h = tcb.decompress(cont)  # warms the pinned result pool too
-        del del_h
-    torch.cuda.synchronize()
-    dec_ms, dec_e2e_ms = [], []
-    for _ in range(args.steps):
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record()
-        tcb.decompress_device(cont, d_out.data_ptr(), nbytes)
-        b.record()
-        b.synchronize()
-        dec_ms.append(a.elapsed_time(b))
-    for _ in range(args.steps):
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record()
-        out_h = tcb.decompress(cont)
-        b.record()
-        b.synchronize()
-        dec_e2e_ms.append(a.elapsed_time(b))
-        del out_h
-    dec_ok = bool(torch.equal(d_out.view(torch.float64).view(x.shape).cpu(),
-                              torch.from_numpy(tcb.decompress(cont).to_array().copy())))
     clk = clocks.stop()
-
+    del host, src
     tot = float(sum(step_ms))
-    tot_e2e = float(sum(e2e_ms))
-    if world > 1:
-        t = torch.tensor([tot, tot_e2e], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot, tot_e2e = float(t[0]), float(t[1])
-    value = world * nbytes * args.steps / (tot * 1e-3) / 1e9
-    e2e = world * nbytes * args.steps / (tot_e2e * 1e-3) / 1e9
+    value = nbytes * args.steps / (tot * 1e-3) / 1e9
+    e2e = nbytes * len(e2e_ms) / (sum(e2e_ms) * 1e-3) / 1e9
 
-    # ---- per-stage breakdown (one extra profiled step) and roofline of the dominant kernel
+    # ---- per-stage breakdown (one extra step with stages run sequentially and timed)
     L.tcb_prof_enable(1)
-    flush.fill_(1)
     torch.cuda.synchronize()
-    res_p = step_device()
+    res_p = tcb.compress_device(x.data_ptr(), nbytes, tcb.Dtype.float32, shape, params)
     L.tcb_prof_enable(0)
-    import ctypes as C
-
     ms = (C.c_double * len(STAGES))()
     cnt = (C.c_uint64 * len(STAGES))()
     L.tcb_prof_read(ms, cnt, len(STAGES))
-    stage_ms = {s: round(ms[i], 4) for i, s in enumerate(STAGES)}
+    stage_ms = {s: round(ms[i], 3) for i, s in enumerate(STAGES)}
     L.tcb_peak_dmma_tflops.restype = C.c_double
     dmma_peak = float(L.tcb_peak_dmma_tflops())
     peaks, peak_src = _peaks()
-    order = sorted(range(3), key=lambda i: (x.shape[i], i))
-    gram_flop, ttm_flop = algorithmic_work(list(x.shape), res.ranks, order)
-    # Dominant kernel: the first mode's Gram (syrk_kernel) tops the committed ncu
-    # launch list (profiles/launches_*_summary.txt); the top-p eigensolve
-    # (tk_cluster) is a close second and latency-bound -- it is reported under
-    # roofline["eig"].  The factor encodes run on worker streams off the critical
-    # path (the sequential per-stage pass adds them up), so they do not compete.
-    # The dominant launch itself, timed live: the first mode's Gram (syrk_kernel +
-    # its fixed-order split reduction) on the resident input, CUDA events on the
-    # launching stream (tcb_prof), L2 flushed before each of 5 launches.
-    rows0 = x.shape[order[0]]
-    cols0 = int(np.prod(x.shape)) // rows0
+    order = [0, 1, 2]
+    gram_flop, ttm_flop = algorithmic_work(shape, res.ranks, order)
+
+    # ---- the dominant launches, timed live on the launching stream (tcb_prof events):
+    # the mode-0 TTM (largest single launch of the ncu launch list) and the mode-0 Gram,
+    # on the fp64 cast of the resident input (what the pipeline's mode 0 reads)
+    x64 = x.double()
+    rows0, cols0, r0 = shape[0], nbytes // 4 // shape[0], res.ranks[0]
+    u0 = torch.linalg.qr(torch.randn(rows0, r0, dtype=torch.float64, device=dev))[0].contiguous()
+    nxt = torch.empty(cols0 * r0, dtype=torch.float64, device=dev)
     g0 = torch.empty(rows0 * rows0, dtype=torch.float64, device=dev)
     L.tcb_dev_gram.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
-    g_ms = []
-    for _ in range(5):
-        flush.fill_(1)
-        torch.cuda.synchronize()
-        L.tcb_prof_enable(1)
-        assert L.tcb_dev_gram(d_in.data_ptr(), rows0, cols0, g0.data_ptr()) == 0
-        L.tcb_prof_enable(0)
-        L.tcb_prof_read(ms, cnt, len(STAGES))
-        g_ms.append(ms[STAGES.index("gram")])
-    g_ms = float(np.median(g_ms))
-    g_flop = float(rows0 * (rows0 + 1) * cols0)
-    achieved = g_flop / (g_ms * 1e-3) / 1e12
-    roof = {"kernel": "mode-0 Gram (syrk_kernel + syrk_reduce, one launch pair, median of 5)", "bound": "tensor",
-            "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s", "frac": achieved / dmma_peak,
-            "traffic": _ncu_traffic("syrk_kernel"), "flop": g_flop, "ms": g_ms,
-            "all_modes": {"flop": gram_flop, "ms": stage_ms["gram"],
-                          "tflops": gram_flop / max(stage_ms["gram"], 1e-9) / 1e9,
-                          "frac": gram_flop / max(stage_ms["gram"], 1e-9) / 1e9 / dmma_peak,
-                          "note": "all three modes' Grams of the profiled step; modes 1-2 (256 x 3584, "
-                                  "256 x 196) are launch-latency-bound"},
-            "traffic_source": "DRAM read+write bytes of the mode-0 syrk_kernel launch, ncu --set full "
-                              "(profiles/ncu_*_full_summary.txt); algorithmic: the 128 MiB input once",
-            "peak_source": "measured fp64 DMMA probe (tcb_peak_dmma_tflops); MEASURED_PEAKS.json has no fp64"}
-    # Certified top-p path (csrc/topk.cu, p = 32, 2 extra iterations) per mode with n <= 256:
-    # 4 products G W (2 n^2 p each), CholQR passes (2 + 2 + 3: Gram 2 n p^2 + apply 2 n p^2
-    # each), Rayleigh-Ritz (H 2 n p^2, X and G X 4 n p^2).  Larger modes take the full solver:
-    # tridiagonalisation 4/3 n^3 + back-transform 2 n^2 r.
-    cur = [x.shape[i] for i in order]
-    eig_flop, p_blk = 0.0, 32
-    for mode in order:
-        rows, cols = cur[0], int(np.prod(cur)) // cur[0]
-        n_eig = rows if (rows <= cols or rows <= 256) else cols
-        if 2 * p_blk <= n_eig <= 256 and not os.environ.get("TCB_NO_TOPK"):
-            eig_flop += 4 * 2.0 * n_eig ** 2 * p_blk + 7 * 4.0 * n_eig * p_blk ** 2 + 6.0 * n_eig * p_blk ** 2
-        else:
-            eig_flop += 4.0 / 3.0 * n_eig ** 3 + 2.0 * n_eig * n_eig * res.ranks[mode]
-        cur = cur[1:] + [res.ranks[mode]]
-    roof["note"] = ("ncu launch-list shares for this command (profiles/launches_*_summary.txt): the encoder's "
-                    "syrk_kernel (incl. the 5 live-timed mode-0 launches), ac_kernel and tk_cluster are each ~14-18 %; of the 5 ac_kernel launches per "
-                    "compress only the core finalisation's is on the critical path (the probe and the factor "
-                    "streams run on side streams), so the Gram is the dominant critical-path kernel")
-    roof["eig"] = {"kernel": "tk_cluster (one 8-CTA cluster launch per mode)", "flop": eig_flop,
-                   "ms": stage_ms["eig"], "tflops": eig_flop / max(stage_ms["eig"], 1e-9) / 1e9,
-                   "note": "latency-bound: per mode 3 block subspace iterations, each 2-3 CholQR passes "
-                           "of a 32-step Cholesky with one CTA barrier per step, then ~2-3 Jacobi sweeps of "
-                           "31 dependent rounds (DESIGN.md 3a); the stage time includes the host "
-                           "certificate's sync per mode"}
-    roof["ttm"] = {"flop": ttm_flop, "ms": stage_ms["ttm"],
-                   "tflops": ttm_flop / max(stage_ms["ttm"], 1e-9) / 1e9, "peak_tflops": dmma_peak}
+    L.tcb_dev_ttm.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p]
 
-    # ---- CPU baseline (rank 0, N=1 only): the oracle on a bounded sample
+    def timed(fn, stage, reps=3):
+        out = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            L.tcb_prof_enable(1)
+            assert fn() == 0
+            L.tcb_prof_enable(0)
+            L.tcb_prof_read(ms, cnt, len(STAGES))
+            out.append(ms[STAGES.index(stage)])
+        return float(np.median(out))
+
+    ttm_ms = timed(lambda: L.tcb_dev_ttm(x64.data_ptr(), rows0, cols0, u0.data_ptr(), r0, nxt.data_ptr()), "ttm")
+    gram_ms = timed(lambda: L.tcb_dev_gram(x64.data_ptr(), rows0, cols0, g0.data_ptr()), "gram")
+    del x64, nxt, g0
+    torch.cuda.empty_cache()
+    ttm_flop0 = 2.0 * rows0 * cols0 * r0
+    gram_flop0 = float(rows0 * (rows0 + 1) * cols0)
+    ach = ttm_flop0 / (ttm_ms * 1e-3) / 1e12
+    roof = {"kernel": "mode-0 TTM (ttm_kernel, 1024 x 1048576 by 1024 x r0, median of 3 live launches)",
+            "bound": "tensor", "achieved": ach, "peak": dmma_peak, "unit": "TFLOP/s", "frac": ach / dmma_peak,
+            "traffic": None, "flop": ttm_flop0, "ms": ttm_ms,
+            "peak_source": "measured fp64 DMMA probe (tcb_peak_dmma_tflops; MEASURED_PEAKS.json has no fp64)",
+            "gram_mode0": {"flop": gram_flop0, "ms": gram_ms, "tflops": gram_flop0 / (gram_ms * 1e-3) / 1e12,
+                           "frac": gram_flop0 / (gram_ms * 1e-3) / 1e12 / dmma_peak},
+            "all_modes": {"gram_flop": gram_flop, "gram_ms": stage_ms["gram"], "ttm_flop": ttm_flop,
+                          "ttm_ms": stage_ms["ttm"],
+                          "frac": (gram_flop + ttm_flop) / max(stage_ms["gram"] + stage_ms["ttm"], 1e-9) / 1e9
+                          / dmma_peak}}
+    # encoder: B_enc = 2 * 8 * N_core + payload (SURVEY 8(d)) over the stats+emit+ac stages, against HBM
+    n_core = int(np.prod(res.ranks))
+    b_enc = 2 * 8 * n_core + len(res.container)
+    enc_ms = stage_ms["stats"] + stage_ms["emit"] + stage_ms["ac"] + stage_ms["quant"]
+    roof["encoder"] = {"bytes": b_enc, "ms": enc_ms, "gbs": b_enc / max(enc_ms, 1e-9) / 1e6,
+                       "peak_gbs": peaks.get("hbm_gbs"), "frac": b_enc / max(enc_ms, 1e-9) / 1e6 /
+                       float(peaks.get("hbm_gbs", 6553.6)), "peak_source": peak_src,
+                       "note": "quantise + exact statistics + emission + range coding of the core "
+                               "(sequential profiled step); the range coder is serial per stream"}
+    roof["eig"] = {"ms": stage_ms["eig"], "note": "latency-bound (tridiagonalisation steps)"}
+
+    # ---- secondary lines: c5 @ 1e-3 and c2 @ 1e-4, device-resident
+    secondary = {}
+    if not args.no_secondary:
+        r3, ms3 = device_steps(tcb, x, nbytes, tcb.Dtype.float32, shape, tcb.Params(target_re=1e-3),
+                               max(2, args.steps // 4), 1)
+        secondary["c5_re1e-3"] = {"value": nbytes * len(ms3) / (sum(ms3) * 1e-3) / 1e9, "unit": "GB/s",
+                                  "ms_per_step": sum(ms3) / len(ms3), "ranks": r3.ranks,
+                                  "container_bytes": len(r3.container), "steps": len(ms3)}
+    del x
+    torch.cuda.empty_cache()
+    if not args.no_secondary:
+        xc2 = synth.make("c2", seed=0)
+        d2 = torch.from_numpy(xc2.view(np.uint8).reshape(-1)).to(dev)
+        rc2, msc2 = device_steps(tcb, d2, xc2.nbytes, tcb.Dtype.float64, list(xc2.shape),
+                                 tcb.Params(target_re=1e-4), max(5, args.steps), 2)
+        secondary["c2_re1e-4"] = {"workload": C2_WORKLOAD, "value": xc2.nbytes * len(msc2) / (sum(msc2) * 1e-3)
+                                  / 1e9, "unit": "GB/s", "ms_per_step": sum(msc2) / len(msc2),
+                                  "ranks": rc2.ranks, "container_bytes": len(rc2.container), "steps": len(msc2)}
+        del d2
+
+    # ---- CPU baseline (rank 0, N=1): the oracle on the bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        xs = cpu_sample()
         ts = []
         t_start = time.perf_counter()
         while time.perf_counter() - t_start < 10.0 or not ts:
-            dt, _ = cpu_reference_step(x, args.re)
+            dt, _ = cpu_reference_step(xs, args.re)
             ts.append(dt)
-        import oracle
-
         nth = oracle.threads()
-        cpu = {"value": nbytes * len(ts) / sum(ts) / 1e9, "unit": "GB/s", "cores": nth, "kind": "port",
-               "sample": f"{len(ts)} full c2 compress(es) via oracle/ (restated reference; Gram and "
-                         f"projection loops OpenMP-parallel over {nth} host threads)"}
+        cpu = {"value": xs.nbytes * len(ts) / sum(ts) / 1e9, "unit": "GB/s", "cores": nth, "kind": "port",
+               "sample": f"{len(ts)} full compress(es) of the c5 generator at {CPU_SAMPLE_N}^3 ({xs.nbytes} B, "
+                         f"RE {args.re}) via oracle/ (restated reference; Gram and projection loops "
+                         f"OpenMP-parallel over {nth} host threads)"}
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": tot / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "input_bytes": nbytes, "ranks": res.ranks,
-                       "container_bytes": len(res.container), "compression_factor": res.compression_factor(),
-                       "core_last_plane": res.core_last_plane, "l2": "256 MiB flush before every timed step; "
-                       "input 128 MiB > L2", "parallelism": "single GPU"},
-            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": nbytes,
-                    "d2h_bytes_per_step": len(r2.container)},
-            "gpu_launches": int(launches),
-            "roofline": roof,
-            "decompress": {"metric": "decompress throughput GB/s (output bytes)",
-                           "value": nbytes * len(dec_ms) / (sum(dec_ms) * 1e-3) / 1e9, "unit": "GB/s",
-                           "ms_per_step": sum(dec_ms) / len(dec_ms),
-                           "e2e": {"value": nbytes * len(dec_e2e_ms) / (sum(dec_e2e_ms) * 1e-3) / 1e9,
-                                   "unit": "GB/s", "h2d_bytes_per_step": len(cont), "d2h_bytes_per_step": nbytes,
-                                   "ms_per_step": sum(dec_e2e_ms) / len(dec_e2e_ms)},
-                           "matches_host_path": dec_ok,
-                           "note": "tcb_decompress_device into a device buffer (timed with CUDA events around "
-                                   "the call: container parse, upload, decode, reconstruction, emit); e2e "
-                                   "through tcb_decompress into pinned host memory"},
-            "stage_ms": stage_ms,
-            "cpu_baseline": cpu,
-            "clocks": clk,
-            "uncertified_decisions": res.uncertified_decisions,
-            "step_ms_all": [round(v, 3) for v in step_ms],
-            "e2e_ms_all": [round(v, 3) for v in e2e_ms],
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "re": args.re, "input_bytes": nbytes, "ranks": res.ranks,
+                   "container_bytes": len(res.container), "compression_factor": res.compression_factor(),
+                   "core_last_plane": res.core_last_plane, "l2": "input 4 GiB > L2 (no flush needed)",
+                   "parallelism": "single GPU"},
+        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": len(r2.container),
+                "ms_all": [round(v, 2) for v in e2e_ms],
+                "note": "tcb.compress from pinned host memory (H2D inside), container bytes returned to Python; "
+                        "CUDA events around the synchronous call"},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "stage_ms": stage_ms,
+        "secondary": secondary,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "step_ms_all": [round(v, 3) for v in step_ms],
+    }
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":
