@@ -65,8 +65,10 @@ typedef struct tcb_result {
     int ingest_precision_loss;
     /* device-path diagnostics (no reference counterpart) */
     int core_last_plane, core_scale_exponent;
-    int uncertified_decisions;   /* plans decided by the serial-replay fallback */
+    int uncertified_decisions;   /* always 0: every encoder decision is made on exact serial sums */
     uint64_t kernel_launches;
+    uint32_t rank_tie_modes;     /* bit i: mode i's rank cut lies within the eigenvalue error band of the
+                                    budget (another fp64 solver may cut one vector apart) */
 } tcb_result;
 
 void tcb_default_params(tcb_params* p);
@@ -194,6 +196,13 @@ int tcb_exact_sums(const uint64_t* mag, const uint64_t* dec, uint64_t n, const u
                    const uint64_t* seg_hi, const int* seg_backward, const double* seg_s0, const double* seg_need,
                    int nseg, const int* kind_term, const int* kind_plane, int nk, int reference, double* sums,
                    uint64_t* c0, uint64_t* c1, int* crossed);
+
+/* build_block's per-block statistics (core_codec.cpp:131-155) of planes
+ * p_top .. p_top-np+1 (np <= 32) over blocks of block_size elements, bit-exact:
+ * outputs indexed (2 (p_top - p) + {0 lead, 1 trail}) * nblocks + b, as
+ * tcb_exact_sums returns them for those kinds. */
+int tcb_exact_plane_stats(const uint64_t* mag, uint64_t n, uint64_t block_size, int p_top, int np, double* sums,
+                          uint64_t* c0, uint64_t* c1, int* crossed);
 
 /* entropy::encode_symbols (entropy.cpp:429-445) for one symbol sequence. */
 int tcb_encode_symbols(int coder, const uint64_t* syms, uint64_t n, uint8_t** out, uint64_t* len);

@@ -79,7 +79,7 @@ class _CResult(C.Structure):
         ("target_sse", C.c_double), ("ranks", C.c_uint64 * 8), ("order", C.c_int), ("times", _CTimes),
         ("peak_alloc_estimate", C.c_uint64), ("original_bytes", C.c_uint64),
         ("ingest_precision_loss", C.c_int), ("core_last_plane", C.c_int), ("core_scale_exponent", C.c_int),
-        ("uncertified_decisions", C.c_int), ("kernel_launches", C.c_uint64),
+        ("uncertified_decisions", C.c_int), ("kernel_launches", C.c_uint64), ("rank_tie_modes", C.c_uint32),
     ]
 
 
@@ -212,6 +212,7 @@ class CompressResult:
     core_scale_exponent: int = 0
     uncertified_decisions: int = 0
     kernel_launches: int = 0
+    rank_tie_modes: int = 0
 
     def compression_factor(self) -> float:
         return 0.0 if not self.container else self.original_bytes / len(self.container)
@@ -229,7 +230,7 @@ def _result(r: _CResult) -> CompressResult:
         peak_alloc_estimate=r.peak_alloc_estimate, original_bytes=r.original_bytes,
         ingest_precision_loss=bool(r.ingest_precision_loss), core_last_plane=r.core_last_plane,
         core_scale_exponent=r.core_scale_exponent, uncertified_decisions=r.uncertified_decisions,
-        kernel_launches=int(r.kernel_launches))
+        kernel_launches=int(r.kernel_launches), rank_tie_modes=int(r.rank_tie_modes))
 
 
 def compress(src: SourceBuffer, params: Params) -> CompressResult:
@@ -515,6 +516,24 @@ def exact_sums(mag, segs, kinds, dec=None, reference=False):
     return sums[:nj].reshape(shp), c0[:nj].reshape(shp), c1[:nj].reshape(shp), cr[:nj].reshape(shp)
 
 
+def plane_stats(mag, block, p_top, np_):
+    """build_block's exact per-block statistics of planes p_top..p_top-np_+1 (tcb_exact_plane_stats);
+    same layout as exact_sums over kinds [(lead, p), (trail, p) for p descending] and the block segments."""
+    mag = np.ascontiguousarray(mag, np.uint64)
+    n = mag.size
+    nb = (n + block - 1) // block
+    nj = max(1, 2 * np_ * nb)
+    sums = np.zeros(nj, np.float64)
+    c0 = np.zeros(nj, np.uint64)
+    c1 = np.zeros(nj, np.uint64)
+    cr = np.zeros(nj, np.int32)
+    _check(lib().tcb_exact_plane_stats(_p(mag) if n else None, C.c_uint64(n), C.c_uint64(block), int(p_top), int(np_),
+                                       _p(sums), _p(c0), _p(c1), _p(cr)))
+    shp = (2 * np_, nb)
+    k = 2 * np_ * nb
+    return sums[:k].reshape(shp), c0[:k].reshape(shp), c1[:k].reshape(shp), cr[:k].reshape(shp)
+
+
 def encode_symbols(coder, syms) -> bytes:
     s = np.ascontiguousarray(syms, np.uint64)
     out = C.POINTER(C.c_uint8)()
@@ -547,4 +566,4 @@ EXPORTED = ("tcb_compress", "tcb_compress_device", "tcb_decompress", "tcb_decomp
             "tcb_nccl_unique_id", "tcb_nccl_comm_init", "tcb_nccl_comm_destroy", "tcb_compress_sharded_device", "tcb_measure_error",
             "tcb_default_params", "tcb_free", "tcb_last_error",
             "tcb_kernel_launches", "tcb_sthosvd_f64", "tcb_gram_f64", "tcb_ttm_f64", "tcb_eig_f64",
-            "tcb_quantize_f64", "tcb_encode", "tcb_exact_sums", "tcb_encode_symbols", "tcb_encode_factor_f64")
+            "tcb_quantize_f64", "tcb_encode", "tcb_exact_sums", "tcb_exact_plane_stats", "tcb_encode_symbols", "tcb_encode_factor_f64")

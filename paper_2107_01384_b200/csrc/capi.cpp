@@ -206,17 +206,13 @@ struct Stream {
         int lo = 0, hi = 0;
         TCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         TCB_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
-        static bool pool = [] {  // keep freed pool memory mapped between calls
-            int dev = 0;
-            cudaGetDevice(&dev);
+        TCB_ONCE_PER_DEVICE({  // keep freed pool memory mapped between calls
             cudaMemPool_t mp;
-            if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+            if (cudaDeviceGetDefaultMemPool(&mp, cur_device()) == cudaSuccess) {
                 u64 thr = ~u64{0};
                 cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
             }
-            return true;
-        }();
-        (void)pool;
+        });
     }
     ~Stream() {
         if (s) {
@@ -338,6 +334,7 @@ void fill(Result& r, int d, tcb_result* out) {
     out->core_scale_exponent = r.core_k;
     out->uncertified_decisions = r.uncertified;
     out->kernel_launches = launch_counter().load();
+    out->rank_tie_modes = r.rank_tie_modes;
 }
 
 std::size_t dtype_bytes(int t) {
@@ -419,11 +416,12 @@ bool upload_overlapping_gram(const u8* host, u64 nbytes, int dtype, const std::v
     const GramPlan gp = gram_plan(B, rows, cols);
     g0 = DevBuf<double>(rows * rows, s);
     ws = DevBuf<double>(gram_ws_doubles(gp), s);
-    static cudaStream_t copy = [] {
+    static PerDevice<cudaStream_t> copy_dev;
+    cudaStream_t copy = copy_dev.get([] {
         cudaStream_t c;
         TCB_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
         return c;
-    }();
+    });
     cudaEvent_t start;
     TCB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
     TCB_CUDA(cudaEventRecord(start, s));  // the buffers exist on `s`
@@ -782,6 +780,23 @@ int tcb_exact_sums(const uint64_t* mag, const uint64_t* dec, uint64_t n, const u
         }
         const auto out = reference ? exact_serial_reference(m.p, dec ? d.p : nullptr, segs, kinds, st.s)
                                    : exact_serial(m.p, dec ? d.p : nullptr, segs, kinds, st.s);
+        for (std::size_t j = 0; j < out.size(); ++j) {
+            sums[j] = out[j].sum;
+            c0[j] = out[j].c0;
+            c1[j] = out[j].c1;
+            crossed[j] = out[j].crossed;
+        }
+    });
+}
+
+int tcb_exact_plane_stats(const uint64_t* mag, uint64_t n, uint64_t block, int p_top, int np, double* sums,
+                          uint64_t* c0, uint64_t* c1, int* crossed) {
+    return guard([&] {
+        if (block == 0) throw Error("exact sums: zero block");
+        Stream st;
+        DevBuf<u64> m(n + 1, st.s);
+        m.upload(mag, n);
+        const auto out = exact_plane_stats(m.p, n, block, p_top, np, st.s);
         for (std::size_t j = 0; j < out.size(); ++j) {
             sums[j] = out[j].sum;
             c0[j] = out[j].c0;

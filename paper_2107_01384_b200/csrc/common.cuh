@@ -2,6 +2,8 @@
 #pragma once
 
 #include <atomic>
+#include <map>
+#include <mutex>
 
 #include <cuda_runtime.h>
 
@@ -84,14 +86,48 @@ struct DevBuf {
     }
 };
 
+inline int cur_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+// Per-device state built on first use on each device (function attributes,
+// occupancy results, side streams): the library runs on the calling thread's
+// current device, so nothing device-bound may be a plain process-wide static.
+template <class T>
+class PerDevice {
+public:
+    template <class Make>
+    T& get(Make&& make) {
+        const int dev = cur_device();
+        std::lock_guard<std::mutex> lk(mu_);
+        auto it = m_.find(dev);
+        if (it == m_.end()) it = m_.emplace(dev, make()).first;
+        return it->second;
+    }
+
+private:
+    std::mutex mu_;
+    std::map<int, T> m_;
+};
+// run `body` once per device at this call site
+#define TCB_ONCE_PER_DEVICE(...)                                                 \
+    do {                                                                          \
+        static ::tcb::PerDevice<bool> tcb_once_;                                  \
+        (void)tcb_once_.get([&] {                                                 \
+            __VA_ARGS__;                                                          \
+            return true;                                                          \
+        });                                                                       \
+    } while (0)
+
 inline int sm_count() {
-    static int n = [] {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    static PerDevice<int> n;
+    return n.get([] {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, cur_device());
         return v > 0 ? v : 148;
-    }();
-    return n;
+    });
 }
 
 inline unsigned cdiv(u64 a, u64 b) { return static_cast<unsigned>((a + b - 1) / b); }

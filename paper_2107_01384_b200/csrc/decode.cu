@@ -482,12 +482,8 @@ void decode_entropy(const u8* cont, const DecSection* sec_dev, const std::vector
         if (sec[i].cap <= kDecCap) small_ids.push_back(i);
         else big_ids.push_back(i);
     }
-    static bool attr = [] {
-        cudaFuncSetAttribute(dec_entropy_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(dec_model_words(kDecCap) * 4 + 16));
-        return true;
-    }();
-    (void)attr;
+    TCB_ONCE_PER_DEVICE(cudaFuncSetAttribute(dec_entropy_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(dec_model_words(kDecCap) * 4 + 16)));
     for (int pass = 0; pass < 2; ++pass) {
         const auto& ids = pass == 0 ? small_ids : big_ids;
         if (ids.empty()) continue;

@@ -394,11 +394,12 @@ DecompressOut decompress_device(const u8* c, u64 len, cudaStream_t s) {
     std::vector<DevBuf<double>> U(d);
     DevBuf<int> ferr(1, s);
     ferr.zero();
-    static std::vector<cudaStream_t> side = [] {
+    static PerDevice<std::vector<cudaStream_t>> side_dev;
+    const std::vector<cudaStream_t>& side = side_dev.get([] {
         std::vector<cudaStream_t> v(8);
         for (auto& st : v) TCB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         return v;
-    }();
+    });
     for (std::size_t i = 0; i < d; ++i) U[i] = DevBuf<double>(n[i] * rk[i], s);
     cudaEvent_t fork_ev, join_ev[8];
     TCB_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));

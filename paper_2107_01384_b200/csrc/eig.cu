@@ -1181,6 +1181,17 @@ __global__ void mgs_kernel(double* __restrict__ U, int n, int r, const int* __re
 }  // namespace
 
 namespace {
+constexpr size_t kEigSmemMax = 227 * 1024;
+constexpr int kEigMaxN = 2300;  // the compact-WY panels of the back-transform at kc = 4
+size_t wy_tmat_smem(int n, int kc) {
+    return (static_cast<size_t>(kc) * (n + 1) + 2 * kc * (kc + 1)) * sizeof(double);
+}
+size_t wy_apply_smem(int n, int kc) {
+    const int nslice = kBtThreads / (kc / 4);
+    return (2 * static_cast<size_t>(kc) * (n + 1) + 2 * kc * kc + static_cast<size_t>(n) * 4 +
+            static_cast<size_t>(nslice / 4 + 2) * kc * 4) * sizeof(double);
+}
+size_t invit_smem(int n) { return 5 * static_cast<size_t>(n) * sizeof(double) + n * sizeof(int); }
 struct SideStream {
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
@@ -1227,7 +1238,17 @@ bool coop_tridiag(double* A, int n, double* d, double* e, double* V, double* tau
 std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_t s) {
     ProfScope prof_scope(kEig, s);
     const int n = static_cast<int>(n64);
-    if (n64 > 1024) throw Error("sthosvd: device eigensolver supports mode sizes up to 1024");
+    // reflector chunk width of the compact-WY back-transform: the preferred width,
+    // narrowed until its shared-memory panels fit (larger modes)
+    int kc = n <= 256 ? 32 : n <= 512 ? 16 : 8;
+    while (kc > 4 && std::max(wy_tmat_smem(n, kc), wy_apply_smem(n, kc)) > kEigSmemMax) kc /= 2;
+    if (std::max(wy_tmat_smem(n, kc), wy_apply_smem(n, kc)) > kEigSmemMax ||
+        invit_smem(n) > kEigSmemMax || (4 * static_cast<size_t>(n) + 32) * sizeof(double) > kEigSmemMax)
+        throw Error("sthosvd: device eigensolver supports mode sizes up to " + std::to_string(kEigMaxN));
+    TCB_ONCE_PER_DEVICE({
+        cudaFuncSetAttribute(multisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kEigSmemMax);
+        cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kEigSmemMax);
+    });
     w.n = n64;
     w.d = DevBuf<double>(n64, s);
     w.e = DevBuf<double>(n64 + 1, s);
@@ -1254,12 +1275,10 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
         if (n <= kDsmemMaxN) {
             const int nloc = (n + kTdCluster - 1) / kTdCluster;
             const size_t smem = ((static_cast<size_t>(nloc) * n + 1) / 2 * 2 + 6 * n) * sizeof(double);
-            static bool attr = [] {
+            TCB_ONCE_PER_DEVICE({
                 cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
                 cudaFuncSetAttribute(tridiag_dsmem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-                return true;
-            }();
-            (void)attr;
+            });
             cfg.gridDim = dim3(kTdCluster);
             // one row slot per warp up to n = 256, two beyond (fewer redundant per-warp steps)
             cfg.blockDim = dim3(32 * (nloc <= 16 ? nloc : (nloc + 1) / 2));
@@ -1289,19 +1308,15 @@ std::vector<double> eig_values(const double* A, u64 n64, EigWork& w, cudaStream_
         count_launch();
     }
     // compact-WY T matrices of the reflector chunks on a side stream, overlapping the multisection
-    w.kc = n <= 256 ? 32 : n <= 512 ? 16 : 8;
+    w.kc = kc;
     w.nchunks = n >= 3 ? (n - 2 + w.kc - 1) / w.kc : 0;
     w.tg = DevBuf<double>(static_cast<u64>(std::max(w.nchunks, 1)) * w.kc * w.kc, s);
     SideStream& side = side_stream();
     if (w.nchunks > 0) {
-        static bool tattr = [] {
-            cudaFuncSetAttribute(wy_tmat, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            return true;
-        }();
-        (void)tattr;
+        TCB_ONCE_PER_DEVICE(cudaFuncSetAttribute(wy_tmat, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         TCB_CUDA(cudaEventRecord(side.fork, s));
         TCB_CUDA(cudaStreamWaitEvent(side.s, side.fork, 0));
-        const size_t tsm = (static_cast<size_t>(w.kc) * (n + 1) + 2 * w.kc * (w.kc + 1)) * sizeof(double);
+        const size_t tsm = wy_tmat_smem(n, w.kc);
         wy_tmat<<<static_cast<unsigned>(w.nchunks), kBtThreads, tsm, side.s>>>(w.z.p, w.tau.p, n, w.kc, w.tg.p);
         count_launch();
         TCB_CUDA(cudaEventRecord(side.join, side.s));
@@ -1352,7 +1367,7 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
     DevBuf<double> dsh(r, s);
     dsh.upload(shift.data(), r);
     DevBuf<double> Z(static_cast<u64>(n) * r, s);
-    const size_t smem = 5 * n * sizeof(double) + n * sizeof(int);
+    const size_t smem = invit_smem(n);
     invit_kernel<<<static_cast<unsigned>(r), 32, smem, s>>>(w.d.p, w.e.p, n, dsh.p, DBL_EPSILON * tnorm, Z.p);
     count_launch();
     if (!clusters.empty()) {
@@ -1383,14 +1398,9 @@ void eig_vectors(EigWork& w, u64 r64, double* U, cudaStream_t s) {
         }
     }
     // T matrices come from wy_tmat on the side stream (launched by eig_values)
-    static bool attr = [] {
-        cudaFuncSetAttribute(wy_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        return true;
-    }();
-    (void)attr;
-    const int KC = w.kc, nslice = kBtThreads / (KC / 4);
-    const size_t asm_ = (2 * static_cast<size_t>(KC) * (n + 1) + 2 * KC * KC + static_cast<size_t>(n) * 4 +
-                         static_cast<size_t>(nslice / 4 + 2) * KC * 4) * sizeof(double);
+    TCB_ONCE_PER_DEVICE(cudaFuncSetAttribute(wy_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    const int KC = w.kc;
+    const size_t asm_ = wy_apply_smem(n, KC);
     wy_apply<<<cdiv(r64, 4), kBtThreads, asm_, s>>>(w.z.p, w.tg.p, n, r, KC, w.nchunks, Z.p, U);
     count_launch();
     TCB_LAUNCH();

@@ -47,26 +47,32 @@ struct Planner {
     std::vector<PlaneStats> st = std::vector<PlaneStats>(64);
     std::vector<char> have = std::vector<char>(64, 0);
 
-    std::vector<ExSeg> block_segs(double s0 = 0.0, double need = HUGE_VAL) const {
-        std::vector<ExSeg> g(nb);
-        for (u64 b = 0; b < nb; ++b) g[b] = ExSeg{b * block, std::min(n, (b + 1) * block), 0, s0, need};
-        return g;
-    }
-    const PlaneStats& stats(int p) {
+    // Exact statistics from plane p down: 32 planes' approximate totals first,
+    // the approximate `tracked` trajectory from the current (exact) value marks
+    // the likely breakpoint, and only the planes down to it (+2) are computed
+    // exactly; a later plane triggers another batch.
+    const PlaneStats& stats(int p, double tracked_now) {
         if (!have[p]) {
-            // planes per launch: every remaining plane for a small core (one round
-            // trip), 8 planes (16 sums per block) for a large one
-            const int span = n <= (u64{1} << 18) ? 64 : 8;
-            const int lo = std::max(0, p - span + 1);
-            std::vector<ExKind> kinds;
-            for (int q = p; q >= lo; --q) {
-                kinds.push_back({kExLead, q});
-                kinds.push_back({kExTrail, q});
-            }
+            const int np = std::min(32, p + 1);
             HostTrace ht("plan: exact plane stats");
-            const auto out = serial_sums(m, nullptr, block_segs(), kinds, s);
-            for (int q = p; q >= lo; --q) {
-                const u64 kl = static_cast<u64>(2 * (p - q)), kt = kl + 1;
+            PlaneStatsJob job(m, n, block, p, np, s);
+            int need = np;
+            if (n > (u64{1} << 20)) {
+                const auto tot = job.approx_totals();
+                double tr = tracked_now;
+                for (int l = 0; l < np; ++l) {
+                    const double red = tot[2 * l] + tot[2 * l + 1];
+                    if (tr - red <= target * (1.0 + 1e-6)) {
+                        need = std::min(np, l + 3);
+                        break;
+                    }
+                    tr -= red;
+                }
+            }
+            const auto out = job.exact(need);
+            for (int l = 0; l < need; ++l) {
+                const int q = p - l;
+                const u64 kl = static_cast<u64>(2 * l), kt = kl + 1;
                 PlaneStats& ps = st[q];
                 ps.lead.resize(nb);
                 ps.trail.resize(nb);
@@ -175,7 +181,7 @@ struct Planner {
         Tot prev;
         bool have_prev = false;
         for (int p = 63; p >= 0; --p) {
-            const PlaneStats& per = stats(p);
+            const PlaneStats& per = stats(p, tracked);
             Tot tot;
             for (u64 b = 0; b < nb; ++b) {
                 tot.lead += per.lead[b];

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <memory>
 
 #include "exact.cuh"
 #include "terms.cuh"
@@ -567,6 +568,159 @@ __global__ void ex_serial_kernel(const u64* __restrict__ m, const u64* __restric
     out[job] = o;
 }
 
+// ---------------------------------------------------------------- plane statistics, lane = plane
+// build_block's statistics for up to 32 consecutive planes at once: one warp
+// streams a chunk's magnitudes once (every load a broadcast) and lane l owns
+// plane p_top - l, evaluating only its own lead / trail terms.  Kinds are
+// (lead, trail) of each plane in lane order: k = 2 l + {0, 1}.
+//
+// Compact transducer state: until the first exact tie both start parities
+// follow the same path (A, with its min / max); the tie sends them to
+// neighbouring values (k1 or k1 + 1 depending on the start parity) and leaves
+// an even result, after which the path is again parity independent (B).
+struct CFn {
+    long long A, mnA, mxA, k1, B, mnB, mxB;
+    int tie, bpar, bad;
+};
+__device__ __forceinline__ CFn cfn_id() { return CFn{0, kBig, -kBig, 0, 0, 0, 0, 0, 0, 0}; }
+__device__ __forceinline__ void cfn_term(CFn& f, double t, int e) {
+    if (t == 0.0 || f.bad) return;
+    long long j;
+    bool tie;
+    if (!unitize(t, e, j, tie)) {
+        f.bad = 1;
+        return;
+    }
+    if (!f.tie) {
+        if (!tie) {
+            f.A += j;
+            f.mnA = min(f.mnA, f.A);
+            f.mxA = max(f.mxA, f.A);
+        } else {
+            f.tie = 1;
+            f.k1 = j;
+        }
+    } else {
+        const int jb = static_cast<int>(j & 1);
+        f.B += tie ? j + ((f.bpar ^ jb) & 1) : j;
+        f.bpar = tie ? 0 : (f.bpar ^ jb);
+        f.mnB = min(f.mnB, f.B);
+        f.mxB = max(f.mxB, f.B);
+    }
+    if (llabs(f.A) > kLim || llabs(f.B) > kLim) f.bad = 1;
+}
+__device__ __forceinline__ ExRec cfn_rec(const CFn& f, int rid, u32 c0, u32 c1) {
+    ExRec r;
+    r.rid = rid;
+    r.c0 = c0;
+    r.c1 = c1;
+    if (f.bad) {
+        r.K0 = r.K1 = 0;
+        r.mn0 = r.mn1 = kBig;
+        r.mx0 = r.mx1 = -kBig;
+        r.qbad = 2 | 4;
+        return r;
+    }
+    if (!f.tie) {
+        r.K0 = r.K1 = f.A;
+        r.mn0 = r.mn1 = f.mnA;
+        r.mx0 = r.mx1 = f.mxA;
+        const int ap = static_cast<int>(f.A & 1);
+        r.qbad = ap | ((1 ^ ap) << 1);
+        return r;
+    }
+    const int ak = static_cast<int>((f.A ^ f.k1) & 1);
+    const long long t0 = f.A + f.k1 + (ak & 1), t1 = f.A + f.k1 + ((1 ^ ak) & 1);  // value after the tie
+    r.K0 = t0 + f.B;
+    r.K1 = t1 + f.B;
+    r.mn0 = min(f.mnA, t0 + f.mnB);
+    r.mn1 = min(f.mnA, t1 + f.mnB);
+    r.mx0 = max(f.mxA, t0 + f.mxB);
+    r.mx1 = max(f.mxA, t1 + f.mxB);
+    r.qbad = f.bpar | (f.bpar << 1);
+    return r;
+}
+
+// one warp per chunk; PASS 0: approximate sums, PASS 1: chunk functions
+template <int PASS>
+__global__ void __launch_bounds__(128) ex_plane_kernel(const u64* __restrict__ m, const DevSeg* __restrict__ segs,
+                                                       int nseg, const u64* __restrict__ choff, int p_top, int np,
+                                                       u64 nch, double* __restrict__ A, const double* __restrict__ P,
+                                                       ExRec* __restrict__ out) {
+    constexpr u64 C = 2048;
+    const u64 c = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (c >= nch) return;
+    const int lane = threadIdx.x & 31;
+    const int g = seg_of(choff, nseg, c);
+    const DevSeg sg = segs[g];
+    const u64 lo = sg.lo + (c - choff[g]) * C;
+    const int cnt = static_cast<int>(min(C, sg.hi - lo));
+    const int p = p_top - lane;
+    const bool on = lane < np;
+    const int p_low = p_top - np + 1;
+    double aL = 0.0, aT = 0.0;
+    CFn fL = cfn_id(), fT = cfn_id();
+    int eL = 52, eT = 52, rL = 52, rT = 52;
+    if (PASS == 1 && on) {
+        rL = region_of(P[static_cast<u64>(2 * lane) * nch + c]);
+        rT = region_of(P[static_cast<u64>(2 * lane + 1) * nch + c]);
+        eL = rexp(rL);
+        eT = rexp(rT);
+    }
+    u32 nle = 0, none = 0, ntr = 0;
+    const u64* mp = m + lo;
+    for (int i0 = 0; i0 < cnt; i0 += 8) {
+        u64 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = i0 + u < cnt ? __ldg(mp + i0 + u) : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (i0 + u >= cnt) break;
+            const int tb = top_bit64(v[u]);
+            if (!on) continue;
+            if (tb < p_low) {  // below every active plane: a lead zero for all of them
+                nle += 1;
+                continue;
+            }
+            nle += tb <= p;
+            none += tb == p;
+            ntr += tb > p;
+            if (tb > p) {
+                const double t = t_trail_gain(v[u], p);
+                if (PASS == 0) aT += t;
+                else cfn_term(fT, t, eT);
+            } else if (tb == p) {
+                const double t = t_lead_gain(v[u], p);
+                if (PASS == 0) aL += t;
+                else cfn_term(fL, t, eL);
+            }
+        }
+    }
+    if (!on) return;
+    if (PASS == 0) {
+        A[static_cast<u64>(2 * lane) * nch + c] = aL;
+        A[static_cast<u64>(2 * lane + 1) * nch + c] = aT;
+    } else {
+        out[static_cast<u64>(2 * lane) * nch + c] = cfn_rec(fL, rL, nle, none);
+        out[static_cast<u64>(2 * lane + 1) * nch + c] = cfn_rec(fT, rT, 0, ntr);
+    }
+}
+
+// approximate per-kind totals (sum of the pass-1 chunk sums): one CTA per kind
+__global__ void ex_kind_totals(const double* __restrict__ A, u64 nch, double* __restrict__ tot) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (u64 c = threadIdx.x; c < nch; c += blockDim.x) acc += A[static_cast<u64>(blockIdx.x) * nch + c];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += sh[w];
+        tot[blockIdx.x] = t;
+    }
+}
+
 struct Prepared {
     std::vector<DevSeg> hs;
     std::vector<u64> choff;
@@ -628,6 +782,98 @@ void run_exact(const u64* m, const u64* dec, const std::vector<ExSeg>& segs, con
 }
 
 }  // namespace
+
+struct PlaneStatsJob::Impl {
+    const u64* m = nullptr;
+    u64 n = 0, block = 0, nb = 0;
+    int p_top = 0, np = 0;
+    bool generic = false;
+    std::vector<ExSeg> segs;
+    std::vector<ExKind> kinds;
+    Prepared prep;
+    DevBuf<double> A, P;
+};
+
+PlaneStatsJob::PlaneStatsJob(const u64* m, u64 n, u64 block, int p_top, int np, cudaStream_t s)
+    : impl_(std::make_unique<Impl>()), s_(s) {
+    if (np < 1 || np > 32 || p_top - np + 1 < 0) throw Error("exact sums: bad plane range");
+    Impl& J = *impl_;
+    J.m = m;
+    J.n = n;
+    J.block = block;
+    J.p_top = p_top;
+    J.np = np;
+    J.nb = n == 0 ? 0 : (n + block - 1) / block;
+    J.segs.resize(J.nb);
+    for (u64 b = 0; b < J.nb; ++b) J.segs[b] = ExSeg{b * block, std::min(n, (b + 1) * block), 0, 0.0, HUGE_VAL};
+    for (int l = 0; l < np; ++l) {
+        J.kinds.push_back({kExLead, p_top - l});
+        J.kinds.push_back({kExTrail, p_top - l});
+    }
+    static const bool ref_chain = [] {
+        const char* e = std::getenv("TCB_EXACT_REFERENCE");
+        return e && *e && *e != '0';
+    }();
+    u64 maxlen = 0;
+    for (const auto& g : J.segs) maxlen = std::max(maxlen, g.hi - g.lo);
+    // small cores: the generic path (direct warp resolution, no tables)
+    J.generic = ref_chain || J.nb == 0 || maxlen < 8 * 2048;
+    if (J.generic) return;
+    ProfScope prof(kStats, s);
+    J.prep = prepare(J.segs, J.kinds, 2048, s);
+    const u64 nk = J.kinds.size();
+    J.A = DevBuf<double>(J.prep.nch * nk, s);
+    J.P = DevBuf<double>(J.prep.nch * nk, s);
+    ex_plane_kernel<0><<<cdiv(J.prep.nch * 32, 128), 128, 0, s>>>(m, J.prep.segs.p, static_cast<int>(J.nb), J.prep.dch.p,
+                                                                 p_top, np, J.prep.nch, J.A.p, nullptr, nullptr);
+    count_launch();
+    TCB_LAUNCH();
+}
+
+PlaneStatsJob::~PlaneStatsJob() = default;
+
+std::vector<double> PlaneStatsJob::approx_totals() {
+    Impl& J = *impl_;
+    const int nk = static_cast<int>(J.kinds.size());
+    std::vector<double> t(nk, 0.0);
+    if (J.generic) return t;
+    DevBuf<double> d(nk, s_);
+    ex_kind_totals<<<nk, 256, 0, s_>>>(J.A.p, J.prep.nch, d.p);
+    count_launch();
+    TCB_LAUNCH();
+    d.download(t.data(), nk);
+    stream_sync(s_);
+    return t;
+}
+
+std::vector<ExOut> PlaneStatsJob::exact(int np_exact) {
+    Impl& J = *impl_;
+    np_exact = std::max(1, std::min(np_exact, J.np));
+    std::vector<ExKind> kinds(J.kinds.begin(), J.kinds.begin() + 2 * np_exact);
+    if (J.generic) return exact_serial(J.m, nullptr, J.segs, kinds, s_);
+    ProfScope prof(kStats, s_);
+    const int nseg = static_cast<int>(J.nb);
+    const int njobs = nseg * 2 * np_exact;
+    const u64 nch = J.prep.nch;
+    ex_scan_kernel<<<static_cast<unsigned>(njobs), 1024, 0, s_>>>(J.prep.segs.p, nseg, J.prep.dch.p, nch, J.A.p, J.P.p);
+    DevBuf<ExRec> recs(nch * 2 * np_exact, s_);
+    ex_plane_kernel<1><<<cdiv(nch * 32, 128), 128, 0, s_>>>(J.m, J.prep.segs.p, nseg, J.prep.dch.p, J.p_top, np_exact,
+                                                            nch, nullptr, J.P.p, recs.p);
+    DevBuf<ExOut> d(njobs, s_);
+    ex_walk_kernel<64><<<cdiv(static_cast<u64>(njobs) * 32, 128), 128, 0, s_>>>(
+        J.m, nullptr, J.prep.segs.p, nseg, J.prep.dch.p, J.prep.dk.p, njobs, nch, recs.p, d.p);
+    count_launch(3);
+    TCB_LAUNCH();
+    std::vector<ExOut> out(njobs);
+    d.download(out.data(), njobs);
+    stream_sync(s_);
+    return out;
+}
+
+std::vector<ExOut> exact_plane_stats(const u64* m, u64 n, u64 block, int p_top, int np, cudaStream_t s) {
+    PlaneStatsJob job(m, n, block, p_top, np, s);
+    return job.exact(np);
+}
 
 std::vector<ExOut> exact_serial(const u64* m, const u64* dec, const std::vector<ExSeg>& segs,
                                 const std::vector<ExKind>& kinds, cudaStream_t s) {

@@ -32,6 +32,7 @@
 #pragma once
 
 #include <cmath>
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -72,6 +73,29 @@ struct ExOut {
 // TCB_EXACT_REFERENCE=1 routes every call through exact_serial_reference.
 std::vector<ExOut> exact_serial(const u64* m, const u64* dec, const std::vector<ExSeg>& segs,
                                 const std::vector<ExKind>& kinds, cudaStream_t s);
+
+// build_block's per-block statistics of planes p_top .. p_top - np + 1 (np <= 32)
+// over blocks of `block` elements: out[k * nb + b] with kinds k = 2 (p_top - p)
+// + {0: lead, 1: trail}, as exact_serial would return them.
+std::vector<ExOut> exact_plane_stats(const u64* m, u64 n, u64 block, int p_top, int np, cudaStream_t s);
+
+// The same in two steps: construction runs the approximate pass for planes
+// p_top .. p_top - np + 1 (np <= 32); approx_totals() gives every kind's
+// approximate total (k = 2 (p_top - p) + {0, 1}), so the caller can estimate
+// how many planes it needs; exact(np_exact) returns the exact statistics of
+// the first np_exact planes only (elements below them are skipped).
+class PlaneStatsJob {
+public:
+    PlaneStatsJob(const u64* m, u64 n, u64 block, int p_top, int np, cudaStream_t s);
+    ~PlaneStatsJob();
+    std::vector<double> approx_totals();
+    std::vector<ExOut> exact(int np_exact);
+
+private:
+    struct Impl;
+    std::unique_ptr<Impl> impl_;
+    cudaStream_t s_;
+};
 
 // Debug/verification: the same sums by the plain one-thread serial chain.
 std::vector<ExOut> exact_serial_reference(const u64* m, const u64* dec, const std::vector<ExSeg>& segs,

@@ -325,14 +325,12 @@ std::vector<double> factor_residuals(const u64* mag, const u8* neg, int k, u64 n
     err.zero();
     refl_from_stream<<<dim3(cdiv(rl, 4), np), 128, 0, s>>>(mag, neg, k, n, rl, dp.p, scales_dev, Vd.p, err.p);
     const size_t smem = static_cast<size_t>(kExChunk) * n * sizeof(double);
-    static bool attr = [] {
+    TCB_ONCE_PER_DEVICE({
         const int mx = kExChunk * 1024 * sizeof(double);
         cudaFuncSetAttribute(expand_residual<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(expand_residual<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(expand_residual<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        return true;
-    }();
-    (void)attr;
+    });
     const dim3 grid(cdiv(rl, 8), np);
     if (n <= 256) expand_residual<8><<<grid, 256, smem, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
     else if (n <= 512) expand_residual<16><<<grid, 256, smem, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
@@ -371,14 +369,12 @@ void factor_expand(const u64* mag, const u8* neg, int k, u64 n, u64 r, const std
     int* ep = err_dev ? err_dev : err.p;
     refl_from_stream<<<dim3(cdiv(rl, 4), 1), 128, 0, s>>>(mag, neg, k, n, rl, dp.p, scales_dev, Vd.p, ep);
     const size_t smem = static_cast<size_t>(kExChunk) * n * sizeof(double);
-    static bool attr = [] {
+    TCB_ONCE_PER_DEVICE({
         const int mx = kExChunk * 1024 * sizeof(double);
         cudaFuncSetAttribute(expand_columns<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(expand_columns<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(expand_columns<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        return true;
-    }();
-    (void)attr;
+    });
     const unsigned grid = cdiv(rl, 8);
     if (n <= 256) expand_columns<8><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);
     else if (n <= 512) expand_columns<16><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);

@@ -356,25 +356,12 @@ __global__ void __launch_bounds__(256) ttm_kernel(const double* __restrict__ B, 
 }
 
 // ------------------------------------------------------------------ small helpers
-__global__ void gram_cols_kernel(const double* __restrict__ B, u64 rows, u64 cols, double* __restrict__ G) {
+// G <- lower triangle mirrored (bitwise symmetric Gram for the eigensolver)
+__global__ void mirror_lower_kernel(double* __restrict__ G, u64 n) {
     const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= cols * cols) return;
-    const u64 i = idx / cols, j = idx % cols;
-    if (j > i) return;
-    double s = 0.0;
-    for (u64 k = 0; k < rows; ++k) s = fma(B[k * cols + i], B[k * cols + j], s);
-    G[i * cols + j] = s;
-    G[j * cols + i] = s;
-}
-
-__global__ void gemm_nn_kernel(const double* __restrict__ B, u64 rows, u64 cols, const double* __restrict__ V, u64 r,
-                               double* __restrict__ out) {
-    const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= rows * r) return;
-    const u64 i = idx / r, j = idx % r;
-    double s = 0.0;
-    for (u64 k = 0; k < cols; ++k) s = fma(B[i * cols + k], V[k * r + j], s);
-    out[idx] = s;
+    if (idx >= n * n) return;
+    const u64 i = idx / n, j = idx % n;
+    if (j > i) G[idx] = G[j * n + i];
 }
 
 // Peak probe: independent DMMA chains per warp, no memory traffic.
@@ -421,14 +408,15 @@ GramPlan gram_plan(const double* B, u64 rows, u64 cols) {
         const int v = e && *e ? std::atoi(e) : kSyrkDefault;
         return v >= 0 && v < kSyrkVariants ? v : kSyrkDefault;
     }();
-    static const int per_sm = [] {
+    static PerDevice<int> per_sm_dev;
+    const int per_sm = per_sm_dev.get([] {
         const SyrkVariant& k = kSyrk[variant];
         cudaFuncSetAttribute(k.k16, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem());
         cudaFuncSetAttribute(k.k8, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem());
         int b = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k.k16, k.threads, k.smem());
         return std::max(1, b);
-    }();
+    });
     GramPlan gp;
     gp.variant = variant;
     gp.bk = kSyrk[variant].bk;
@@ -510,9 +498,12 @@ void gram_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
     gram_reduce(gp, ws.p, rows, G, s);
 }
 
+// Gram of B^T (cols x cols, sthosvd.cpp:91-99 thin branch): B^T B is the TTM of
+// B with itself as the factor (DMMA), then mirrored from its lower triangle
 void gram_cols_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) {
+    ttm_f64(B, rows, cols, B, cols, G, s);
     ProfScope prof_scope(kGram, s);
-    gram_cols_kernel<<<cdiv(cols * cols, 256), 256, 0, s>>>(B, rows, cols, G);
+    mirror_lower_kernel<<<cdiv(cols * cols, 256), 256, 0, s>>>(G, cols);
     count_launch();
     TCB_LAUNCH();
 }
@@ -522,12 +513,10 @@ void launch_ttm(const double* B, u64 rows, u64 cols, const double* U, u64 r, dou
     dim3 grid(cdiv(cols, TM), cdiv(r, TN));
     const bool v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
     constexpr int smem = TtmShape<TN>::smem_doubles * sizeof(double);
-    static bool attr = [] {
+    TCB_ONCE_PER_DEVICE({
         cudaFuncSetAttribute(ttm_kernel<true, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(ttm_kernel<false, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        return true;
-    }();
-    (void)attr;
+    });
     if (v16) ttm_kernel<true, TN><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out);
     else ttm_kernel<false, TN><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out);
 }
@@ -541,11 +530,11 @@ void ttm_f64(const double* B, u64 rows, u64 cols, const double* U, u64 r, double
     TCB_LAUNCH();
 }
 
+// out = B V (rows x r): the TTM of B^T (materialised by the tiled permute) with V
 void gemm_nn_f64(const double* B, u64 rows, u64 cols, const double* V, u64 r, double* out, cudaStream_t s) {
-    ProfScope prof_scope(kTtm, s);
-    gemm_nn_kernel<<<cdiv(rows * r, 256), 256, 0, s>>>(B, rows, cols, V, r, out);
-    count_launch();
-    TCB_LAUNCH();
+    DevBuf<double> bt(rows * cols, s);
+    permute_axes(B, bt.p, {rows, cols}, {1, 0}, s);
+    ttm_f64(bt.p, cols, rows, V, r, out, s);
 }
 
 }  // namespace tcb

@@ -135,6 +135,19 @@ std::size_t dtype_size(int t) {
     throw Error("container: unknown dtype");
 }
 
+// SURVEY H3 tie band: the rank rule compares tail sums of eigenvalues with the
+// budget; a solver's eigenvalues carry an absolute error of a few n eps |G|, so
+// when the budget is closer than that to the sum at the chosen cutoff or at the
+// next one, another correct fp64 solver (the reference's) may cut one vector
+// earlier or later.  Reported, not corrected.
+bool rank_tie(const std::vector<double>& s2, u64 r, double gone, double budget) {
+    if (s2.empty()) return false;
+    const double n = static_cast<double>(s2.size());
+    const double err = 8.0 * n * DBL_EPSILON * std::max(s2[0], 0.0) * std::sqrt(n - static_cast<double>(r) + 1.0);
+    const double keep_next = r > 0 ? gone + s2[r - 1] : gone;  // the sum that stopped the discard loop
+    return std::fabs(budget - gone) <= err || std::fabs(keep_next - budget) <= err;
+}
+
 // sthosvd.cpp:13-26
 std::pair<u64, double> pick_rank(const std::vector<double>& s2, double budget) {
     if (s2.empty()) throw Error("rank choice: empty singular values");
@@ -253,7 +266,7 @@ std::vector<double> alpha_weights(const std::vector<double>& sn, u64 n) {
 //     the kept subspace's sine is <= 5e-7 (the parity tolerance is 1e-6).
 // V receives the n x r Ritz vectors (unsigned).  false: use the full solver.
 bool topk_factor(const double* G, u64 n, const Budget& bud, cudaStream_t s, u64& r_out, double& gone_out,
-                 std::vector<double>& s2_out, DevBuf<double>& V) {
+                 std::vector<double>& s2_out, DevBuf<double>& V, bool* tie_out = nullptr) {
     constexpr int p = 32, spare = 8;
     if (!topk_supported(n, p)) return false;
     if (const char* e = std::getenv("TCB_NO_TOPK"); e && *e && *e != '0') return false;
@@ -306,6 +319,12 @@ bool topk_factor(const double* G, u64 n, const Budget& bud, cudaStream_t s, u64&
         r_out = static_cast<u64>(r);
         gone_out = gone;
         s2_out = s2;
+        if (tie_out) {  // the tail beyond the block is trace - prefix: one more candidate sum
+            const double err = 8.0 * static_cast<double>(n) * DBL_EPSILON * std::max(th[0], 0.0) *
+                               std::sqrt(static_cast<double>(n) - r + 1.0);
+            const double next = gone + s2[r - 1];
+            *tie_out = std::fabs(budget - gone) <= err || std::fabs(next - budget) <= err;
+        }
         V = DevBuf<double>(n * r, s);
         TCB_CUDA(cudaMemcpy2DAsync(V.p, r * sizeof(double), X.p, p * sizeof(double), r * sizeof(double), n,
                                    cudaMemcpyDeviceToDevice, s));
@@ -318,7 +337,7 @@ StepOut factor_from_gram(const double* G, u64 n, const Budget& bud, cudaStream_t
     {
         StepOut o;
         std::vector<double> s2;
-        if (topk_factor(G, n, bud, s, o.r, o.discarded, s2, o.U)) {
+        if (topk_factor(G, n, bud, s, o.r, o.discarded, s2, o.U, &o.tie)) {
             fix_column_signs(o.U.p, n, o.r, s);
             return o;
         }
@@ -329,11 +348,13 @@ StepOut factor_from_gram(const double* G, u64 n, const Budget& bud, cudaStream_t
     std::vector<double> s2(n);
     for (u64 j = 0; j < n; ++j) s2[j] = std::max(0.0, ev[j]);
     auto [r, gone] = pick_rank(s2, budget);
+    const bool tie = rank_tie(s2, r, gone, budget);
     if (r == 0) {  // a budget above the whole mode energy still keeps one vector (sthosvd.cpp:146-150)
         r = 1;
         gone -= s2[0];
     }
     StepOut o;
+    o.tie = tie;
     o.r = r;
     o.discarded = gone;
     o.U = DevBuf<double>(n * r, s);
@@ -345,12 +366,12 @@ StepOut factor_from_gram(const double* G, u64 n, const Budget& bud, cudaStream_t
 StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int backend, cudaStream_t s,
                   const double* gram, const ShardComm* shard) {
     const bool sharded = shard && shard->world > 1;
-    // rows > cols is the reference's thin-SVD branch (sthosvd.cpp:91-99); its
-    // stand-in here (Gram of B^T, U = B V / sigma, re-orthonormalised) is no more
-    // accurate than the Gram of B itself -- both square the singular values -- so
-    // a small row count takes the cheaper direct Gram route
+    // rows > cols is the reference's thin-SVD branch (sthosvd.cpp:75-76,91-99): only
+    // cols singular values exist, so r <= cols whatever the budget; the stand-in is
+    // the Gram of B^T, U = B V / sigma, re-orthonormalised.  rows <= cols: the Gram
+    // of B (for SvdBackend::direct too -- its thin U has the same rows columns).
     const u64 cols_all = sharded ? cols * static_cast<u64>(shard->world) : cols;
-    const bool via_gram = backend == 1 || (backend == 0 && (rows <= cols_all || rows <= 256));
+    const bool via_gram = backend == 1 || rows <= cols_all;
     if (sharded && !via_gram) throw Error("sharded compress: a step off the Gram route (rows > cols)");
     StepOut o;
     if (via_gram) {
@@ -376,12 +397,13 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
         double gone = 0.0;
         std::vector<double> s2;
         DevBuf<double> V;
-        if (!topk_factor(G.p, cols, budget, s, r, gone, s2, V)) {
+        if (!topk_factor(G.p, cols, budget, s, r, gone, s2, V, &o.tie)) {
             const double bv = budget.eval(budget.trace_out ? gram_trace(G.p, cols, s) : 0.0);
             const auto ev = eig_values(G.p, cols, w, s);
             s2.assign(cols, 0.0);
             for (u64 j = 0; j < cols; ++j) s2[j] = std::max(0.0, ev[j]);
             std::tie(r, gone) = pick_rank(s2, bv);
+            o.tie = rank_tie(s2, r, gone, bv);
             if (r == 0) {
                 r = 1;
                 gone -= s2[0];
@@ -488,6 +510,7 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
         xp = x.p;
         f.factors[p[step]] = std::move(so.U);
         f.r[p[step]] = so.r;
+        if (so.tie) f.tie_modes |= 1u << p[step];
         if (on_factor) on_factor(p[step], f.factors[p[step]].p, rows, so.r);
         cur.erase(cur.begin());
         cur.push_back(so.r);
@@ -1119,6 +1142,7 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     res.times.sthosvd = ms_since(t0);
     res.trunc = trunc;
     res.ranks = f.r;
+    res.rank_tie_modes = f.tie_modes;
 
     encode_into(res, f, shape, dtype, target, core_target, trunc, prm, s, t_all, n_el, &preps);
     return res;

@@ -66,6 +66,7 @@ struct Result {
     u64 peak_alloc = 0, original_bytes = 0;
     bool precision_loss = false;
     int core_last_plane = 63, core_k = 0, uncertified = 0;
+    unsigned rank_tie_modes = 0;
 };
 
 // device_bytes: element bytes (skip already applied) resident on the device
@@ -83,6 +84,7 @@ struct Tucker {
     std::vector<DevBuf<double>> factors;  // n_i x r_i row-major, by original mode
     std::vector<u64> n, r, order;
     std::vector<double> trunc;
+    unsigned tie_modes = 0;  // bit i: mode i's rank decision sat in the tie band
 };
 // Sharded mode loop: the input is this rank's slab of the last
 // processed mode (equal slabs, rank order); the Grams of steps 0..d-2 are
@@ -100,6 +102,7 @@ struct ShardComm {
 struct StepOut {
     u64 r = 0;
     double discarded = 0.0;
+    bool tie = false;  // the budget lies within the eigenvalues' error band of a cutoff
     DevBuf<double> U, next;
 };
 // A mode step's SSE budget: a fixed value, or `scale` x trace(G) of the step's

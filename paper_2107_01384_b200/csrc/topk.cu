@@ -896,11 +896,7 @@ void topk_phase_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_tk_p
 
 bool cholqr_inplace(double* U, u64 n64, int r, int* fail_dev, cudaStream_t s) {
     if (n64 > 256 || r < 1 || r > kP || n64 < static_cast<u64>(r)) return false;
-    static const bool attr = [] {
-        cudaFuncSetAttribute(tk_cqr, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        return true;
-    }();
-    (void)attr;
+    TCB_ONCE_PER_DEVICE(cudaFuncSetAttribute(tk_cqr, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     TCB_CUDA(cudaMemsetAsync(fail_dev, 0, sizeof(int), s));
     const size_t qld = ((n64 + 15) & ~u64{15}) + 4;
     const size_t qsm = (kP * qld + 2 * kP * kS + kP) * sizeof(double);
@@ -918,13 +914,11 @@ void topk_eig(const double* G, u64 n64, int p, int extra_iters, double* X, std::
               std::vector<double>& resid, double& trace, cudaStream_t s) {
     ProfScope prof_scope(kEig, s);
     const int n = static_cast<int>(n64);
-    static bool attr = [] {
+    TCB_ONCE_PER_DEVICE({
         cudaFuncSetAttribute(tk_gq, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         cudaFuncSetAttribute(tk_cqr, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         cudaFuncSetAttribute(tk_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        return true;
-    }();
-    (void)attr;
+    });
     DevBuf<double> out(2 * p + 2, s);
     TCB_CUDA(cudaMemsetAsync(out.p, 0, (2 * p + 2) * sizeof(double), s));
     // one launch on an 8-CTA cluster when it fits (the multi-launch path below otherwise)
@@ -933,10 +927,11 @@ void topk_eig(const double* G, u64 n64, int p, int extra_iters, double* X, std::
         const int nb = (((n + kTkNC - 1) / kTkNC) + 7) & ~7, nw = std::max(nk, kTkNC * nb);
         const size_t smem = (static_cast<size_t>(nb) * gs + static_cast<size_t>(nw) * kS + nb * kS + 5 * kP * kS +
                              kP + kTkNC * (2 * kP + 1)) * sizeof(double);
-        static const bool cl_attr = [] {
+        static PerDevice<bool> cl_attr_dev;
+        const bool cl_attr = cl_attr_dev.get([] {
             return cudaFuncSetAttribute(tk_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024) ==
                    cudaSuccess;
-        }();
+        });
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(kTkNC);
         cfg.blockDim = dim3(256);
@@ -949,11 +944,13 @@ void topk_eig(const double* G, u64 n64, int p, int extra_iters, double* X, std::
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        static int ncl = -1;
-        if (ncl < 0) {
-            if (!cl_attr || cudaOccupancyMaxActiveClusters(&ncl, tk_cluster, &cfg) != cudaSuccess) ncl = 0;
+        static PerDevice<int> ncl_dev;
+        const int ncl = ncl_dev.get([&] {
+            int v = 0;
+            if (!cl_attr || cudaOccupancyMaxActiveClusters(&v, tk_cluster, &cfg) != cudaSuccess) v = 0;
             cudaGetLastError();
-        }
+            return v;
+        });
         const char* e = std::getenv("TCB_TOPK_NO_CLUSTER");
         if (ncl > 0 && smem <= 224 * 1024 && !(e && *e && *e != '0')) {
             TCB_CUDA(cudaLaunchKernelEx(&cfg, tk_cluster, G, n, p, extra_iters + 1, X, out.p));

@@ -152,3 +152,16 @@ def test_signed_trail_sums_cross_zero(gpu_pkg):
     m[::7] = hi | low[::7]
     segs = [(0, n, 0, 0.0, INF), (0, n, 1, 0.0, INF), (0, n, 0, -1e20, INF), (0, n, 0, 2.0 ** 70, INF)]
     check_same(gpu_pkg, m, segs, [(1, p), (2, p)])
+
+
+@pytest.mark.parametrize("gen,n,block,ptop,np_", [("hot", 3_000_017, 65536, 63, 32), ("hot0", 2_500_000, 40000, 50, 20),
+                                                  ("tie", 1 << 20, 1 << 18, 40, 32)])
+def test_plane_stats_lane_per_plane(gpu_pkg, gen, n, block, ptop, np_):
+    """exact_plane_stats (one lane per plane, compact transducer) == the generic engine == the serial chain"""
+    m = {"hot": lambda: hot_corner(n, 7), "tie": lambda: tie_heavy(n, 3),
+         "hot0": lambda: hot_corner(n, 9, zeros=0.5)}[gen]()
+    a = gpu_pkg.plane_stats(m, block, ptop, np_)
+    kinds = [(t, ptop - l) for l in range(np_) for t in (0, 1)]
+    b = gpu_pkg.exact_sums(m, blocks(n, block), kinds, reference=True)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)

@@ -46,7 +46,7 @@ def test_gram_is_deterministic(gpu_pkg):
     assert np.array_equal(gpu_pkg.gram(b), gpu_pkg.gram(b))
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 17, 64, 100, 256, 500, 601, 700, 1024])
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 64, 100, 256, 500, 601, 700, 1024, 1500, 2048])
 def test_eigensolver_matches_lapack(gpu_pkg, n):
     rng = np.random.default_rng(n)
     b = rng.standard_normal((n, 3 * n + 5))
