@@ -96,6 +96,20 @@ int tcb_compress_sharded_device(void* comm, int world, int rank, const void* dev
                                 int dtype, const uint64_t* shape, int d, uint64_t local_extent,
                                 const tcb_params* params, tcb_result* out);
 
+/* Collectives on host memory supplied by the caller, so the sharded pipeline can
+ * run over any transport (e.g. torch.distributed with gloo): in-place fp64 sum
+ * and a rank-major all-gather of equal-size byte blocks.  Return 0 on success. */
+typedef struct tcb_host_collectives {
+    void* ctx;
+    int (*allreduce_sum_f64)(void* ctx, double* buf, uint64_t n);
+    int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes_per_rank);
+} tcb_host_collectives;
+
+/* tcb_compress_sharded_device with the collectives above instead of NCCL. */
+int tcb_compress_sharded_host(const tcb_host_collectives* coll, int world, int rank, const void* device_bytes,
+                              uint64_t nbytes, int dtype, const uint64_t* shape, int d, uint64_t local_extent,
+                              const tcb_params* params, tcb_result* out);
+
 /* pipeline::DecompressResult (pipeline.hpp:59-64) */
 typedef struct tcb_decompress_result {
     uint8_t* bytes;              /* source-dtype bytes, owned by the library: release with tcb_free */
@@ -235,6 +249,13 @@ int tcb_dev_ttm(const double* b, uint64_t rows, uint64_t cols, const double* u, 
 int tcb_dev_encode_tucker(const double* core, const double* const* factors, const uint64_t* n, const uint64_t* r,
                           const uint64_t* order, const double* trunc, int d, int dtype, double norm_sq,
                           double target_sse, const tcb_params* params, tcb_result* out);
+/* The same encode split over `world` ranks (each rank holds the whole Tucker and
+ * codes its share of the core's blocks); coll == NULL with
+ * nccl_comm != NULL uses NCCL.  Rank 0's container equals the unsharded one. */
+int tcb_dev_encode_tucker_sharded(void* nccl_comm, const tcb_host_collectives* coll, int world, int rank,
+                                  const double* core, const double* const* factors, const uint64_t* n,
+                                  const uint64_t* r, const uint64_t* order, const double* trunc, int d, int dtype,
+                                  double norm_sq, double target_sse, const tcb_params* params, tcb_result* out);
 
 #ifdef __cplusplus
 }

@@ -563,7 +563,8 @@ def encode_factor(u, dead, slice_norms, coder=0, simple=False, core_step_log2=0,
 
 
 EXPORTED = ("tcb_compress", "tcb_compress_device", "tcb_decompress", "tcb_decompress_tensor_f64", "tcb_decompress_device", "tcb_read_container_header",
-            "tcb_nccl_unique_id", "tcb_nccl_comm_init", "tcb_nccl_comm_destroy", "tcb_compress_sharded_device", "tcb_measure_error",
+            "tcb_nccl_unique_id", "tcb_nccl_comm_init", "tcb_nccl_comm_destroy", "tcb_compress_sharded_device",
+            "tcb_compress_sharded_host", "tcb_dev_encode_tucker_sharded", "tcb_measure_error",
             "tcb_default_params", "tcb_free", "tcb_last_error",
             "tcb_kernel_launches", "tcb_sthosvd_f64", "tcb_gram_f64", "tcb_ttm_f64", "tcb_eig_f64",
             "tcb_quantize_f64", "tcb_encode", "tcb_exact_sums", "tcb_exact_plane_stats", "tcb_encode_symbols", "tcb_encode_factor_f64")

@@ -501,6 +501,25 @@ int tcb_compress_sharded_device(void* comm, int world, int rank, const void* dev
     });
 }
 
+int tcb_compress_sharded_host(const tcb_host_collectives* coll, int world, int rank, const void* device_bytes,
+                              uint64_t nbytes, int dtype, const uint64_t* shape, int d, uint64_t local_extent,
+                              const tcb_params* params, tcb_result* out) {
+    return guard([&] {
+        if (!coll || !coll->allreduce_sum_f64 || !coll->allgather) throw Error("sharded compress: no collectives");
+        std::vector<u64> sh(shape, shape + d);
+        Stream st;
+        HostCollectives hc{coll->ctx, coll->allreduce_sum_f64, coll->allgather};
+        ShardComm sc;
+        sc.host = &hc;
+        sc.world = world;
+        sc.rank = rank;
+        sc.local_extent = local_extent;
+        Result r = compress_device(device_bytes, nbytes, dtype, sh, to_params(params, d), st.s, nullptr, &sc);
+        host_trace_dump();
+        fill(r, d, out);
+    });
+}
+
 int tcb_compress_device(const void* device_bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d,
                         const tcb_params* params, tcb_result* out) {
     return guard([&] {
@@ -904,9 +923,10 @@ int tcb_dev_ttm(const double* b, uint64_t rows, uint64_t cols, const double* u, 
     });
 }
 
-int tcb_dev_encode_tucker(const double* core, const double* const* factors, const uint64_t* n, const uint64_t* r,
-                          const uint64_t* order, const double* trunc, int d, int dtype, double norm_sq,
-                          double target_sse, const tcb_params* params, tcb_result* out) {
+namespace {
+int encode_tucker_common(const ShardComm* sc, const double* core, const double* const* factors, const uint64_t* n,
+                         const uint64_t* r, const uint64_t* order, const double* trunc, int d, int dtype,
+                         double norm_sq, double target_sse, const tcb_params* params, tcb_result* out) {
     return guard([&] {
         Stream st;
         Tucker f;
@@ -928,9 +948,34 @@ int tcb_dev_encode_tucker(const double* core, const double* const* factors, cons
             TCB_CUDA(cudaMemcpyAsync(f.factors[i].p, factors[i], n[i] * r[i] * sizeof(double),
                                      cudaMemcpyDeviceToDevice, st.s));
         }
-        Result res = encode_tucker_device(f, dtype, norm_sq, target_sse, to_params(params, d), st.s);
+        Result res = encode_tucker_device(f, dtype, norm_sq, target_sse, to_params(params, d), st.s, sc);
         fill(res, d, out);
     });
+}
+}  // namespace
+
+int tcb_dev_encode_tucker(const double* core, const double* const* factors, const uint64_t* n, const uint64_t* r,
+                          const uint64_t* order, const double* trunc, int d, int dtype, double norm_sq,
+                          double target_sse, const tcb_params* params, tcb_result* out) {
+    return encode_tucker_common(nullptr, core, factors, n, r, order, trunc, d, dtype, norm_sq, target_sse, params,
+                                out);
+}
+
+int tcb_dev_encode_tucker_sharded(void* nccl_comm, const tcb_host_collectives* coll, int world, int rank,
+                                  const double* core, const double* const* factors, const uint64_t* n,
+                                  const uint64_t* r, const uint64_t* order, const double* trunc, int d, int dtype,
+                                  double norm_sq, double target_sse, const tcb_params* params, tcb_result* out) {
+    HostCollectives hc{};
+    ShardComm sc;
+    sc.world = world;
+    sc.rank = rank;
+    if (coll) {
+        hc = HostCollectives{coll->ctx, coll->allreduce_sum_f64, coll->allgather};
+        sc.host = &hc;
+    } else {
+        sc.comm = nccl_comm;
+    }
+    return encode_tucker_common(&sc, core, factors, n, r, order, trunc, d, dtype, norm_sq, target_sse, params, out);
 }
 
 }  // extern "C"

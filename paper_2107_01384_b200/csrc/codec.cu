@@ -1093,9 +1093,11 @@ struct Layout {
 };
 
 Layout make_layout(const std::vector<u64>& hist, u64 n, u64 block, int last_plane, int top_plane,
-                   const u64* stops_host, int coder) {
+                   const u64* stops_host, int coder, BlockRange br = {}) {
     Layout L;
-    const u64 nb = n == 0 ? 0 : (n + block - 1) / block;
+    const u64 nball = n == 0 ? 0 : (n + block - 1) / block;
+    const u64 b0 = std::min(br.b0, nball), b1 = std::min(br.b1, nball);
+    const u64 nb = b1 > b0 ? b1 - b0 : 0;
     const int np = top_plane - last_plane + 1;
     const u64 ns = nb * static_cast<u64>(np);
     L.sd.resize(ns);
@@ -1103,8 +1105,8 @@ Layout make_layout(const std::vector<u64>& hist, u64 n, u64 block, int last_plan
     L.jobs.resize(ns);
     for (int pi = 0; pi < np; ++pi) {
         const int p = top_plane - pi;
-        for (u64 b = 0; b < nb; ++b) {
-            const u64 i = pi * nb + b;
+        for (u64 b = b0; b < b1; ++b) {
+            const u64 i = pi * nb + (b - b0);
             StreamDesc& d = L.sd[i];
             d.lo = b * block;
             d.hi = std::min<u64>(n, d.lo + block);
@@ -1233,15 +1235,16 @@ struct Emitted {
     std::vector<StreamOut> soh;
 };
 bool emit_code(Emitted& E, const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
-               const u64* stops_host, int coder, cudaStream_t s) {
+               const u64* stops_host, int coder, cudaStream_t s, BlockRange br = {}) {
     if (coder != 0 && coder != 1) throw Error("entropy: unknown coder");
-    const u64 nb = n == 0 ? 0 : (n + block - 1) / block;
+    const u64 nball = n == 0 ? 0 : (n + block - 1) / block;
+    const u64 nb = std::min(br.b1, nball) > std::min(br.b0, nball) ? std::min(br.b1, nball) - std::min(br.b0, nball) : 0;
     const int np = top_plane - last_plane + 1;
     const u64 ns = nb * static_cast<u64>(np);
     if (ns == 0 || np <= 0) return false;
     HostTrace ht_a("emit: symbols+entropy+sync");
     const auto hist = msb_histogram(m, n, block, s);
-    E.L = make_layout(hist, n, block, last_plane, top_plane, stops_host, coder);
+    E.L = make_layout(hist, n, block, last_plane, top_plane, stops_host, coder, br);
     code_streams(E.c, E.L, m, neg, coder, s);
     E.el.resize(ns);
     E.soh.resize(ns);
@@ -1267,17 +1270,19 @@ bool emit_code(Emitted& E, const u64* m, const u8* neg, u64 n, u64 block, int la
 }  // namespace
 
 EmitDev emit_planes_device(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
-                           const u64* stops_host, int coder, cudaStream_t s) {
+                           const u64* stops_host, int coder, cudaStream_t s, BlockRange br) {
     EmitDev out;
     Emitted E;
-    if (!emit_code(E, m, neg, n, block, last_plane, top_plane, stops_host, coder, s)) return out;
+    if (!emit_code(E, m, neg, n, block, last_plane, top_plane, stops_host, coder, s, br)) return out;
     const u64 ns = E.el.size();
     HostTrace ht_b("emit: assemble");
     std::vector<u64> off(ns);
+    out.stream_bytes.resize(ns);
     u64 tot = 0;
     for (u64 i = 0; i < ns; ++i) {
         off[i] = tot;
-        tot += 4 + 4 + E.el[i] + (E.soh[i].nraw + 7) / 8;
+        out.stream_bytes[i] = 4 + 4 + E.el[i] + (E.soh[i].nraw + 7) / 8;
+        tot += out.stream_bytes[i];
     }
     DevBuf<u64> doff(ns, s);
     doff.upload(off.data(), ns);
@@ -1293,14 +1298,15 @@ EmitDev emit_planes_device(const u64* m, const u8* neg, u64 n, u64 block, int la
 }
 
 EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
-                       const u64* stops_host, int coder, bool want_body, cudaStream_t s) {
+                       const u64* stops_host, int coder, bool want_body, cudaStream_t s, BlockRange br) {
     EmitResult res;
     if (!want_body) {
         Emitted E;
-        if (emit_code(E, m, neg, n, block, last_plane, top_plane, stops_host, coder, s)) res.entropy_bytes = std::move(E.el);
+        if (emit_code(E, m, neg, n, block, last_plane, top_plane, stops_host, coder, s, br))
+            res.entropy_bytes = std::move(E.el);
         return res;
     }
-    EmitDev d = emit_planes_device(m, neg, n, block, last_plane, top_plane, stops_host, coder, s);
+    EmitDev d = emit_planes_device(m, neg, n, block, last_plane, top_plane, stops_host, coder, s, br);
     res.body.resize(d.size);
     if (d.size) d.body.download(res.body.data(), d.size);
     stream_sync(s);

@@ -61,17 +61,24 @@ struct EmitResult {
     std::vector<u8> body;  // concatenated (u32 size || payload) for every (plane, block)
     std::vector<u64> entropy_bytes;  // per stream, for split-plane priority probes
 };
-// the same with the assembled body left in device memory
+// A contiguous range of blocks [b0, b1) (a rank's share under sharded
+// encoding); the default is every block.
+struct BlockRange {
+    u64 b0 = 0, b1 = ~u64{0};
+};
+// the same with the assembled body left in device memory; streams are plane-major
+// over the range's blocks, stream_bytes[i] = 4 + payload of stream i
 struct EmitDev {
     DevBuf<u8> body;
     u64 size = 0;
     std::vector<u64> entropy_bytes;
+    std::vector<u64> stream_bytes;
 };
 EmitDev emit_planes_device(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
-                           const u64* stops_host, int coder, cudaStream_t s);
+                           const u64* stops_host, int coder, cudaStream_t s, BlockRange br = {});
 EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
                        const u64* stops_host /*2*nb, for last_plane*/, int coder, bool want_body,
-                       cudaStream_t s);
+                       cudaStream_t s, BlockRange br = {});
 
 // Speculative split-plane probe: the entropy-coded size of every full plane
 // stream (planes 63..0, no stops, signs not needed) launched on a side stream

@@ -14,10 +14,12 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <limits>
 
 #include "encoder.hpp"
 #include "exact.cuh"
+#include "pipeline.hpp"
 
 namespace tcb {
 
@@ -55,10 +57,18 @@ struct Planner {
         if (!have[p]) {
             const int np = std::min(32, p + 1);
             HostTrace ht("plan: exact plane stats");
-            PlaneStatsJob job(m, n, block, p, np, s);
+            const bool shd = o.shard && o.shard->world > 1;
+            const BlockRange br = shd ? rank_blocks(nb, o.shard->world, o.shard->rank) : BlockRange{0, nb};
+            PlaneStatsJob job(m, n, block, p, np, s, br.b0, br.b1);
             int need = np;
             if (n > (u64{1} << 20)) {
-                const auto tot = job.approx_totals();
+                auto tot = job.approx_totals();
+                if (shd) {  // every rank sums the same partial totals: the same `need` everywhere
+                    DevBuf<double> dt(tot.size(), s);
+                    dt.upload(tot.data(), tot.size());
+                    o.shard->allreduce_sum_f64(dt.p, tot.size(), s);
+                    tot = dt.to_host();
+                }
                 double tr = tracked_now;
                 for (int l = 0; l < np; ++l) {
                     const double red = tot[2 * l] + tot[2 * l + 1];
@@ -69,7 +79,23 @@ struct Planner {
                     tr -= red;
                 }
             }
-            const auto out = job.exact(need);
+            std::vector<ExOut> out = job.exact(need);
+            if (shd) {  // all-gather the ranks' blocks: out[k * nb + b] over every block
+                const u64 nk = static_cast<u64>(2 * need);
+                const std::vector<u8> mine(reinterpret_cast<const u8*>(out.data()),
+                                           reinterpret_cast<const u8*>(out.data() + out.size()));
+                const auto all = o.shard->allgather_blobs(mine, s);
+                std::vector<ExOut> full(nk * nb);
+                for (int r = 0; r < o.shard->world; ++r) {
+                    const BlockRange rb = rank_blocks(nb, o.shard->world, r);
+                    const u64 rn = rb.b1 - rb.b0;
+                    if (all[r].size() != nk * rn * sizeof(ExOut)) throw Error("sharded compress: stats exchange");
+                    const ExOut* src = reinterpret_cast<const ExOut*>(all[r].data());
+                    for (u64 k = 0; k < nk; ++k)
+                        for (u64 b = 0; b < rn; ++b) full[k * nb + rb.b0 + b] = src[k * rn + b];
+                }
+                out = std::move(full);
+            }
             for (int l = 0; l < need; ++l) {
                 const int q = p - l;
                 const u64 kl = static_cast<u64>(2 * l), kt = kl + 1;
@@ -97,11 +123,23 @@ struct Planner {
         HostTrace ht(term == kExSq ? "plan: exact initial sum" : "plan: exact recalibration sum");
         return serial_sums(m, nullptr, {ExSeg{0, n, 1, 0.0, HUGE_VAL}}, {{term, plane}}, s)[0].sum;
     }
-    // the per-coefficient scan of block b from `cum` until cum >= need
+    // the per-coefficient scan of block b from `cum` until cum >= need (by the
+    // block's owner when sharded, then shared)
     ExOut cross(u64 b, int p, int term, double cum, double need) {
         HostTrace ht("plan: exact crossing scan");
-        return serial_sums(m, nullptr, {ExSeg{b * block, std::min(n, (b + 1) * block), 0, cum, need}}, {{term, p}},
-                           s)[0];
+        const bool shd = o.shard && o.shard->world > 1;
+        const BlockRange br = shd ? rank_blocks(nb, o.shard->world, o.shard->rank) : BlockRange{0, nb};
+        ExOut x{};
+        const bool mine = b >= br.b0 && b < br.b1;
+        if (mine)
+            x = serial_sums(m, nullptr, {ExSeg{b * block, std::min(n, (b + 1) * block), 0, cum, need}}, {{term, p}},
+                            s)[0];
+        if (!shd) return x;
+        std::vector<u8> blob;
+        if (mine) blob.assign(reinterpret_cast<const u8*>(&x), reinterpret_cast<const u8*>(&x) + sizeof(x));
+        for (const auto& bl : o.shard->allgather_blobs(blob, s))
+            if (bl.size() == sizeof(ExOut)) std::memcpy(&x, bl.data(), sizeof(x));
+        return x;
     }
 
     void place_stops(int p, double need, const Tot& tot, const PlaneStats& per, const Tot* prev, u64 prev_ebits,
@@ -199,6 +237,18 @@ struct Planner {
                     HostTrace ht("plan: split probe emit");
                     if (o.probe) {
                         for (u64 e : probe_entropy_bytes(*o.probe, p + 1)) ebits += e * 8;
+                    } else if (o.shard && o.shard->world > 1) {  // own blocks, then the ranks' sums
+                        const BlockRange br = rank_blocks(nb, o.shard->world, o.shard->rank);
+                        const auto er = emit_planes(m, nullptr, n, block, p + 1, p + 1, nullptr, o.coder, false, s, br);
+                        u64 mine = 0;
+                        for (u64 e : er.entropy_bytes) mine += e * 8;
+                        const std::vector<u8> blob(reinterpret_cast<const u8*>(&mine),
+                                                   reinterpret_cast<const u8*>(&mine) + sizeof(mine));
+                        for (const auto& bl : o.shard->allgather_blobs(blob, s)) {
+                            u64 v = 0;
+                            std::memcpy(&v, bl.data(), sizeof(v));
+                            ebits += v;
+                        }
                     } else {
                         const auto er = emit_planes(m, nullptr, n, block, p + 1, p + 1, nullptr, o.coder, false, s);
                         for (u64 e : er.entropy_bytes) ebits += e * 8;
@@ -239,8 +289,18 @@ PlanResult plan_stream(const u64* m, u64 n, double target_int, const EncodeOpts&
     return pl.run(dec);
 }
 
+namespace {
+// (u32 size || payload) segments moved from the gathered per-rank bodies into
+// container order (planes major, blocks minor), one CTA per segment
+__global__ void gather_segments_kernel(const u8* __restrict__ src, u8* __restrict__ dst,
+                                       const u64* __restrict__ tab /* src_off, dst_off, len */) {
+    const u64 so = tab[3 * blockIdx.x], dof = tab[3 * blockIdx.x + 1], len = tab[3 * blockIdx.x + 2];
+    for (u64 i = threadIdx.x; i < len; i += blockDim.x) dst[dof + i] = src[so + i];
+}
+}  // namespace
+
 StreamParts finalize_stream_parts(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, const ShardComm* shard) {
     const u64 nb = n == 0 ? 0 : (n + pl.block - 1) / pl.block;
     StreamParts out;
     std::vector<u8>& o = out.head;
@@ -253,12 +313,69 @@ StreamParts finalize_stream_parts(const u64* m, const u8* neg, u64 n, const Plan
         put_le(o, pl.stops[2 * b + 1], 8);
     }
     put_le(o, static_cast<u64>(pl.nplanes), 4);
-    if (pl.nplanes > 0 && nb > 0) {
-        HostTrace ht("finalize: emit_planes");
+    if (pl.nplanes <= 0 || nb == 0) return out;
+    HostTrace ht("finalize: emit_planes");
+    if (!shard || shard->world <= 1) {
         EmitDev er = emit_planes_device(m, neg, n, pl.block, pl.last_plane, 63, pl.stops.data(), coder, s);
         out.body = std::move(er.body);
         out.body_size = er.size;
+        return out;
     }
+    // sharded: every rank emits and codes its own blocks of every plane; the
+    // segments are gathered and put in container order (the result is complete
+    // on every rank; rank 0 writes the container)
+    const int P = shard->world;
+    const BlockRange br = rank_blocks(nb, P, shard->rank);
+    EmitDev er = emit_planes_device(m, neg, n, pl.block, pl.last_plane, 63, pl.stops.data(), coder, s, br);
+    const std::vector<u8> mine(reinterpret_cast<const u8*>(er.stream_bytes.data()),
+                               reinterpret_cast<const u8*>(er.stream_bytes.data() + er.stream_bytes.size()));
+    const auto sizes = shard->allgather_blobs(mine, s);
+    u64 mx = 0;
+    std::vector<u64> rank_total(P, 0);
+    for (int r = 0; r < P; ++r) {
+        const u64* z = reinterpret_cast<const u64*>(sizes[r].data());
+        for (u64 i = 0; i < sizes[r].size() / sizeof(u64); ++i) rank_total[r] += z[i];
+        mx = std::max(mx, rank_total[r]);
+    }
+    DevBuf<u8> send(mx + 1, s), recv((mx + 1) * P, s);
+    if (er.size) TCB_CUDA(cudaMemcpyAsync(send.p, er.body.p, er.size, cudaMemcpyDeviceToDevice, s));
+    shard->allgather(send.p, recv.p, mx + 1, s);
+    // copy table: stream (plane pi, block b) of rank r sits at local index pi * nb_r + (b - b0_r)
+    const u64 np = static_cast<u64>(pl.nplanes);
+    std::vector<std::vector<u64>> loc_off(P);
+    for (int r = 0; r < P; ++r) {
+        const u64* z = reinterpret_cast<const u64*>(sizes[r].data());
+        const u64 cnt = sizes[r].size() / sizeof(u64);
+        loc_off[r].resize(cnt);
+        u64 acc = 0;
+        for (u64 i = 0; i < cnt; ++i) {
+            loc_off[r][i] = acc;
+            acc += z[i];
+        }
+    }
+    std::vector<u64> tab;
+    tab.reserve(3 * np * nb);
+    u64 dst = 0;
+    for (u64 pi = 0; pi < np; ++pi)
+        for (u64 b = 0; b < nb; ++b) {
+            int r = 0;
+            while (r + 1 < P && rank_blocks(nb, P, r + 1).b0 <= b) ++r;
+            const BlockRange rb = rank_blocks(nb, P, r);
+            const u64 i = pi * (rb.b1 - rb.b0) + (b - rb.b0);
+            const u64 len = reinterpret_cast<const u64*>(sizes[r].data())[i];
+            tab.push_back(static_cast<u64>(r) * (mx + 1) + loc_off[r][i]);
+            tab.push_back(dst);
+            tab.push_back(len);
+            dst += len;
+        }
+    DevBuf<u64> dtab(tab.size(), s);
+    dtab.upload(tab.data(), tab.size());
+    out.body = DevBuf<u8>(dst + 1, s);
+    out.body_size = dst;
+    gather_segments_kernel<<<static_cast<unsigned>(np * nb), 256, 0, s>>>(recv.p, out.body.p, dtab.p);
+    count_launch();
+    TCB_LAUNCH();
+    stream_sync(s);
     return out;
 }
 

@@ -8,6 +8,10 @@
 #include "codec.cuh"
 
 namespace tcb {
+struct ShardComm;  // pipeline.hpp
+}
+
+namespace tcb {
 
 struct EncodeOpts {
     int coder = 0;       // entropy::Coder (0 = arithmetic)
@@ -20,7 +24,17 @@ struct EncodeOpts {
     std::function<void(int)> on_last_plane;
     // speculative full-plane entropy sizes for the split probe (optional)
     ProbeCache* probe = nullptr;
+    // sharded encoding: this rank computes the statistics / crossing scans /
+    // probes of its own blocks and the ranks exchange them, so every rank takes
+    // the same decisions
+    const ShardComm* shard = nullptr;
 };
+
+// a rank's contiguous share of the nb blocks
+inline BlockRange rank_blocks(u64 nb, int world, int rank) {
+    return BlockRange{nb * static_cast<u64>(rank) / static_cast<u64>(world),
+                      nb * static_cast<u64>(rank + 1) / static_cast<u64>(world)};
+}
 
 struct PlanResult {
     int last_plane = 63;
@@ -45,7 +59,7 @@ struct StreamParts {
     u64 body_size = 0;
 };
 StreamParts finalize_stream_parts(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,
-                                  cudaStream_t s);
+                                  cudaStream_t s, const ShardComm* shard = nullptr);
 // finalize(): emits planes [last_plane, 63] with the given signs and returns
 // the serialized stream section (container.cpp:231-247) for `count` elements.
 std::vector<u8> finalize_stream(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,

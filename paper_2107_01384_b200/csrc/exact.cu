@@ -794,7 +794,7 @@ struct PlaneStatsJob::Impl {
     DevBuf<double> A, P;
 };
 
-PlaneStatsJob::PlaneStatsJob(const u64* m, u64 n, u64 block, int p_top, int np, cudaStream_t s)
+PlaneStatsJob::PlaneStatsJob(const u64* m, u64 n, u64 block, int p_top, int np, cudaStream_t s, u64 b0, u64 b1)
     : impl_(std::make_unique<Impl>()), s_(s) {
     if (np < 1 || np > 32 || p_top - np + 1 < 0) throw Error("exact sums: bad plane range");
     Impl& J = *impl_;
@@ -803,9 +803,13 @@ PlaneStatsJob::PlaneStatsJob(const u64* m, u64 n, u64 block, int p_top, int np, 
     J.block = block;
     J.p_top = p_top;
     J.np = np;
-    J.nb = n == 0 ? 0 : (n + block - 1) / block;
+    const u64 nball = n == 0 ? 0 : (n + block - 1) / block;
+    b1 = std::min(b1, nball);
+    b0 = std::min(b0, b1);
+    J.nb = b1 - b0;
     J.segs.resize(J.nb);
-    for (u64 b = 0; b < J.nb; ++b) J.segs[b] = ExSeg{b * block, std::min(n, (b + 1) * block), 0, 0.0, HUGE_VAL};
+    for (u64 b = b0; b < b1; ++b)
+        J.segs[b - b0] = ExSeg{b * block, std::min(n, (b + 1) * block), 0, 0.0, HUGE_VAL};
     for (int l = 0; l < np; ++l) {
         J.kinds.push_back({kExLead, p_top - l});
         J.kinds.push_back({kExTrail, p_top - l});

@@ -86,7 +86,9 @@ std::vector<ExOut> exact_plane_stats(const u64* m, u64 n, u64 block, int p_top, 
 // the first np_exact planes only (elements below them are skipped).
 class PlaneStatsJob {
 public:
-    PlaneStatsJob(const u64* m, u64 n, u64 block, int p_top, int np, cudaStream_t s);
+    // blocks [b0, b1) only (a rank's share); results index k * (b1 - b0) + (b - b0)
+    PlaneStatsJob(const u64* m, u64 n, u64 block, int p_top, int np, cudaStream_t s, u64 b0 = 0,
+                  u64 b1 = ~u64{0});
     ~PlaneStatsJob();
     std::vector<double> approx_totals();
     std::vector<ExOut> exact(int np_exact);

@@ -3,6 +3,7 @@
 // is opened once and the few entry points used here are resolved from it, so
 // the library neither pins an NCCL version nor conflicts with torch's copy.
 #include "nccl_shim.hpp"
+#include "pipeline.hpp"
 
 #include <dlfcn.h>
 
@@ -93,6 +94,64 @@ void nccl_allreduce_sum_f64(double* buf, u64 count, void* comm, cudaStream_t s) 
 void nccl_allgather_f64(const double* send, double* recv, u64 count_per_rank, void* comm, cudaStream_t s) {
     check(need().all_gather(send, recv, count_per_rank, ncclFloat64, static_cast<ncclComm_t>(comm), s),
           "ncclAllGather");
+}
+
+void nccl_allgather_bytes(const void* send, void* recv, u64 bytes_per_rank, void* comm, cudaStream_t s) {
+    check(need().all_gather(send, recv, bytes_per_rank, ncclUint8, static_cast<ncclComm_t>(comm), s),
+          "ncclAllGather");
+}
+
+// ---------------------------------------------------------------- ShardComm
+void ShardComm::allreduce_sum_f64(double* d, u64 n, cudaStream_t s) const {
+    if (!host) {
+        nccl_allreduce_sum_f64(d, n, comm, s);
+        return;
+    }
+    std::vector<double> h(n);
+    d2h(h.data(), d, n * sizeof(double), s);
+    stream_sync(s);
+    if (host->allreduce_sum_f64(host->ctx, h.data(), n) != 0) throw Error("sharded compress: host all-reduce failed");
+    TCB_CUDA(cudaMemcpyAsync(d, h.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+    stream_sync(s);
+}
+
+void ShardComm::allgather(const void* dsend, void* drecv, u64 bytes, cudaStream_t s) const {
+    if (!host) {
+        nccl_allgather_bytes(dsend, drecv, bytes, comm, s);
+        return;
+    }
+    std::vector<u8> hs(bytes), hr(bytes * static_cast<u64>(world));
+    if (bytes) d2h(hs.data(), dsend, bytes, s);
+    stream_sync(s);
+    if (host->allgather(host->ctx, hs.data(), hr.data(), bytes) != 0)
+        throw Error("sharded compress: host all-gather failed");
+    if (!hr.empty()) TCB_CUDA(cudaMemcpyAsync(drecv, hr.data(), hr.size(), cudaMemcpyHostToDevice, s));
+    stream_sync(s);
+}
+
+std::vector<std::vector<u8>> ShardComm::allgather_blobs(const std::vector<u8>& mine, cudaStream_t s) const {
+    // sizes first, then every blob padded to the largest
+    std::vector<std::vector<u8>> out(world);
+    if (world == 1) {
+        out[0] = mine;
+        return out;
+    }
+    DevBuf<u64> ds(1, s), dsa(world, s);
+    const u64 sz = mine.size();
+    ds.upload(&sz, 1);
+    allgather(ds.p, dsa.p, sizeof(u64), s);
+    const auto sizes = dsa.to_host();
+    u64 mx = 0;
+    for (u64 v : sizes) mx = std::max(mx, v);
+    if (mx == 0) return out;
+    DevBuf<u8> send(mx, s), recv(mx * world, s);
+    if (sz) send.upload(mine.data(), sz);
+    allgather(send.p, recv.p, mx, s);
+    std::vector<u8> all(mx * world);
+    recv.download(all.data(), all.size());
+    stream_sync(s);
+    for (int r = 0; r < world; ++r) out[r].assign(all.begin() + r * mx, all.begin() + r * mx + sizes[r]);
+    return out;
 }
 
 }  // namespace tcb

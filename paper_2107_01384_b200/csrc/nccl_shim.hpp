@@ -16,5 +16,6 @@ void nccl_comm_destroy(void* comm);
 void nccl_allreduce_sum_f64(double* buf, u64 count, void* comm, cudaStream_t s);
 // recv = the ranks' `send` blocks of count_per_rank doubles, rank-major
 void nccl_allgather_f64(const double* send, double* recv, u64 count_per_rank, void* comm, cudaStream_t s);
+void nccl_allgather_bytes(const void* send, void* recv, u64 bytes_per_rank, void* comm, cudaStream_t s);
 
 }  // namespace tcb

@@ -385,7 +385,7 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
                 G = DevBuf<double>(rows * rows, s);
                 TCB_CUDA(cudaMemcpyAsync(G.p, gram, rows * rows * sizeof(double), cudaMemcpyDeviceToDevice, s));
             }
-            nccl_allreduce_sum_f64(G.p, rows * rows, shard->comm, s);
+            shard->allreduce_sum_f64(G.p, rows * rows, s);
             gram = nullptr;
         }
         o = factor_from_gram(gram ? gram : G.p, rows, budget, s);
@@ -492,7 +492,7 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
             if (rows * static_cast<u64>(shard->world) != full_rows)
                 throw Error("sharded compress: slabs must split the last processed mode evenly");
             DevBuf<double> full(full_rows * cols, s);
-            nccl_allgather_f64(xp, full.p, rows * cols, shard->comm, s);
+            shard->allgather(xp, full.p, rows * cols * sizeof(double), s);
             x = std::move(full);
             xp = x.p;
             so = mode_step(xp, full_rows, cols, budget, backend, s);
@@ -669,7 +669,7 @@ void factor_finalize(FactorQuant& q, int coder, cudaStream_t s) {
 // quantisation, core plan, factors, sign fold, finalize, container.
 void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtype, double target,
                  double core_target, double trunc, const Params& prm, cudaStream_t s, Clock::time_point t_all,
-                 u64 n_el, std::vector<std::future<FactorPrep>>* preps = nullptr) {
+                 u64 n_el, std::vector<std::future<FactorPrep>>* preps = nullptr, const ShardComm* shard = nullptr) {
     const std::size_t d = shape.size();
     auto t0 = Clock::now();
     // phase 2: storage order + quantisation
@@ -763,6 +763,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     eo.coder = prm.coder;
     eo.block = block;
     eo.split = prm.split;
+    eo.shard = shard && shard->world > 1 ? shard : nullptr;
     DevBuf<u64> dec(nc, s);
     const double cap = 0.02 * target / static_cast<double>(d);
     std::vector<FactorEnc> fe(d);
@@ -926,7 +927,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     double ach;
     {
         HostTrace ht("encode: core finalize+sum");
-        core_stream = finalize_stream_parts(mag.p, neg.p, nc, plan, prm.coder, count, s);
+        core_stream = finalize_stream_parts(mag.p, neg.p, nc, plan, prm.coder, count, s, eo.shard);
         // achieved_sse_int, accumulated backward (core_codec.cpp:405-411)
         ach = exact_backward_sum(kExDiff, 0, mag.p, dec.p, nc, s);
     }
@@ -937,6 +938,10 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     }
     for (std::size_t i = 0; i < d; ++i) res.factor_terms[i] = fe[i].term;
     res.times.factor = ms_since(t0);
+    if (eo.shard && eo.shard->rank != 0) {  // rank 0 writes the container
+        res.times.total = ms_since(t_all);
+        return;
+    }
     res.core_quant = std::ldexp(ach, -2 * k);
     double est = trunc + res.core_quant;
     for (double v : res.factor_terms) est += v;
@@ -1045,7 +1050,7 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
         DevBuf<double> st(3, s);
         const double h[3] = {res.norm_sq, finite ? 0.0 : 1.0, res.precision_loss ? 1.0 : 0.0};
         st.upload(h, 3);
-        nccl_allreduce_sum_f64(st.p, 3, shard->comm, s);
+        shard->allreduce_sum_f64(st.p, 3, s);
         const auto g = st.to_host();
         res.norm_sq = g[0];
         finite = g[1] == 0.0;
@@ -1083,7 +1088,7 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
         const char* e = std::getenv("TCB_NO_EARLY_PREP");
         return e && *e && *e != '0';
     }();
-    if (dd > 1 && !prof_enabled() && !no_early_prep && !(shard && shard->rank != 0)) {  // only the encoding rank
+    if (dd > 1 && !prof_enabled() && !no_early_prep) {
         int dev = 0;
         TCB_CUDA(cudaGetDevice(&dev));
         on_factor = [&, dev](std::size_t mode, const double* U, u64 n, u64 r) {
@@ -1116,7 +1121,7 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
             DevBuf<double> f(1, s);
             const double h = fin ? 0.0 : 1.0;
             f.upload(&h, 1);
-            nccl_allreduce_sum_f64(f.p, 1, shard->comm, s);
+            shard->allreduce_sum_f64(f.p, 1, s);
             fin = f.to_host()[0] == 0.0;
         }
         if (!fin) throw Error("sthosvd: input contains non-finite values");
@@ -1130,11 +1135,6 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
             res.target_sse = target;
         }
     }
-    if (shard && shard->rank != 0) {  // the factorisation is replicated; rank 0 encodes
-        res.ranks = f.r;
-        res.times.total = ms_since(t_all);
-        return res;
-    }
     double trunc = 0;
     for (double v : f.trunc) trunc += v;
     double core_target = target - trunc;
@@ -1144,11 +1144,13 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     res.ranks = f.r;
     res.rank_tie_modes = f.tie_modes;
 
-    encode_into(res, f, shape, dtype, target, core_target, trunc, prm, s, t_all, n_el, &preps);
+    // every rank encodes its share of the core's blocks (the factorisation is replicated)
+    encode_into(res, f, shape, dtype, target, core_target, trunc, prm, s, t_all, n_el, &preps, shard);
     return res;
 }
 
-Result encode_tucker_device(Tucker& f, int dtype, double norm_sq, double target, const Params& prm, cudaStream_t s) {
+Result encode_tucker_device(Tucker& f, int dtype, double norm_sq, double target, const Params& prm, cudaStream_t s,
+                            const ShardComm* shard) {
     const auto t_all = Clock::now();
     Result res;
     const std::vector<u64> shape = f.n;
@@ -1163,7 +1165,7 @@ Result encode_tucker_device(Tucker& f, int dtype, double norm_sq, double target,
     if (core_target < 0) core_target = 0;
     res.trunc = trunc;
     res.ranks = f.r;
-    encode_into(res, f, shape, dtype, target, core_target, trunc, prm, s, t_all, n_el);
+    encode_into(res, f, shape, dtype, target, core_target, trunc, prm, s, t_all, n_el, nullptr, shard);
     return res;
 }
 

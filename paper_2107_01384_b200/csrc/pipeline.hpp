@@ -91,10 +91,23 @@ struct Tucker {
 // summed over the ranks with NCCL before the eigensolve (so every rank holds
 // the same factor), the TTMs stay shard-local, and the last step all-gathers
 // the small projected tensor.  Steps 0..d-2 must take the Gram route.
+// Collectives on host memory supplied by the caller (C ABI tcb_host_collectives):
+// lets the sharded pipeline run over any transport (e.g. torch.distributed gloo)
+struct HostCollectives {
+    void* ctx;
+    int (*allreduce_sum_f64)(void* ctx, double* buf, u64 n);                            // in place
+    int (*allgather)(void* ctx, const void* send, void* recv, u64 bytes_per_rank);      // rank-major recv
+};
 struct ShardComm {
-    void* comm = nullptr;   // ncclComm_t (nccl_shim)
+    void* comm = nullptr;                   // ncclComm_t (nccl_shim), or
+    const HostCollectives* host = nullptr;  // host-memory collectives through caller callbacks
     int world = 1, rank = 0;
     u64 local_extent = 0;   // this rank's slab of mode p[d-1]
+    // collectives on device buffers, ordered on s
+    void allreduce_sum_f64(double* d, u64 n, cudaStream_t s) const;
+    void allgather(const void* dsend, void* drecv, u64 bytes_per_rank, cudaStream_t s) const;
+    // host blobs of any size, one per rank
+    std::vector<std::vector<u8>> allgather_blobs(const std::vector<u8>& mine, cudaStream_t s) const;
 };
 
 // One mode step (sthosvd.cpp:136-166): factor U (rows x r, sign-fixed), the
@@ -158,7 +171,8 @@ struct FactorEnc {
 };
 // Phases 2-5 of compress_impl on an existing device factorization (used by
 // the sharded multi-GPU mode loop, whose rank 0 encodes the gathered core).
-Result encode_tucker_device(Tucker& f, int dtype, double norm_sq, double target, const Params& p, cudaStream_t s);
+Result encode_tucker_device(Tucker& f, int dtype, double norm_sq, double target, const Params& p, cudaStream_t s,
+                            const ShardComm* shard = nullptr);
 
 // The orthonormality check and Householder reflectors of a factor's live
 // columns (factor_codec.cpp:29-31,153-200); an error is captured in `err` and

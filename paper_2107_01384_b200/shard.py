@@ -234,6 +234,97 @@ def _nccl_comm(group, world, rank, device):
     return comm
 
 
+# ---------------------------------------------------------------- host-memory collectives
+_ALLREDUCE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_uint64)
+_ALLGATHER_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+
+
+class _CHostColl(C.Structure):  # tcb_host_collectives
+    _fields_ = [("ctx", C.c_void_p), ("allreduce_sum_f64", _ALLREDUCE_CB), ("allgather", _ALLGATHER_CB)]
+
+
+class HostCollectives:
+    """The library's collectives carried by torch.distributed on host tensors
+    (any backend with CPU support, e.g. gloo): the sharded C++ pipeline then
+    runs without NCCL -- several ranks may even share one GPU, since no kernel
+    of one rank waits on another rank."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+
+        def allreduce(ctx, buf, n):
+            try:
+                t = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(int(n),)))
+                dist.all_reduce(t, group=self.group)
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to the library as a failure
+                return 1
+
+        def allgather(ctx, send, recv, nbytes):
+            try:
+                nb = int(nbytes)
+                src = torch.from_numpy(np.ctypeslib.as_array((C.c_uint8 * nb).from_address(send))) if nb else \
+                    torch.zeros(0, dtype=torch.uint8)
+                out = [torch.empty(nb, dtype=torch.uint8) for _ in range(self.world)]
+                dist.all_gather(out, src.clone(), group=self.group)
+                if nb:
+                    dst = np.ctypeslib.as_array((C.c_uint8 * (nb * self.world)).from_address(recv))
+                    for r, t in enumerate(out):
+                        dst[r * nb:(r + 1) * nb] = t.numpy()
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        self._ar = _ALLREDUCE_CB(allreduce)  # keep the thunks alive
+        self._ag = _ALLGATHER_CB(allgather)
+        self.c = _CHostColl(None, self._ar, self._ag)
+
+
+def compress_sharded_host(x_local, shape, dtype, params: Params, group=None):
+    """The library's sharded compress with host collectives (HostCollectives):
+    rank 0 returns the CompressResult, the other ranks None."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    p = list(params.mode_order) if params.mode_order is not None else stable_ascending(shape)
+    lo, hi = shard_bounds(shape[p[-1]], world, rank)
+    hc = HostCollectives(group)
+    sh = np.asarray(list(shape), np.uint64)
+    res = _CResult()
+    with torch.cuda.device(x_local.device):
+        torch.cuda.synchronize()
+        _check(lib().tcb_compress_sharded_host(C.byref(hc.c), int(world), int(rank), C.c_void_p(x_local.data_ptr()),
+                                               C.c_uint64(x_local.numel() * x_local.element_size()), int(dtype),
+                                               sh.ctypes.data_as(C.c_void_p), len(shape), C.c_uint64(hi - lo),
+                                               C.byref(params.to_c(len(shape))), C.byref(res)))
+    out = _result(res)
+    return out if rank == 0 else None
+
+
+def encode_tucker_sharded(core, factors, n, r, order, trunc, dtype, norm_sq, target, params: Params, group=None,
+                          host=True):
+    """Encode an existing device Tucker factorization with the core's blocks split
+    over the ranks (every rank holds the whole factorization); rank 0 returns the
+    CompressResult."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    d = len(n)
+    arr = lambda v, t: np.asarray(v, t)  # noqa: E731
+    na, ra, oa, ta = arr(n, np.uint64), arr(r, np.uint64), arr(order, np.uint64), arr(trunc, np.float64)
+    fptr = (C.c_void_p * d)(*[f.data_ptr() for f in factors])
+    res = _CResult()
+    hc = HostCollectives(group) if host else None
+    comm = None if host else _nccl_comm(group, world, rank, core.device)
+    torch.cuda.synchronize()
+    _check(lib().tcb_dev_encode_tucker_sharded(comm, C.byref(hc.c) if hc else None, int(world), int(rank),
+                                               C.c_void_p(core.data_ptr()), fptr, na.ctypes.data_as(C.c_void_p),
+                                               ra.ctypes.data_as(C.c_void_p), oa.ctypes.data_as(C.c_void_p),
+                                               ta.ctypes.data_as(C.c_void_p), d, int(dtype), C.c_double(norm_sq),
+                                               C.c_double(target), C.byref(params.to_c(d)), C.byref(res)))
+    out = _result(res)
+    return out if rank == 0 else None
+
+
 def _compress_sharded_cpp(x_local, shape, dtype, params: Params, group, world, rank):
     """The whole sharded compress in the library (mode loop, NCCL collectives,
     encode on rank 0): the single-GPU pipeline's kernels and concurrency."""
