@@ -18,21 +18,19 @@ namespace {
 
 constexpr u64 kEmpty = ~u64{0};
 constexpr int kMT = 256;             // model threads = symbols per sub-chunk
-constexpr u32 kSmemEntries = 4096;   // model entries kept in shared memory
 constexpr int kBT = 256, kBPer = 8;  // byte pass: 2048 output bytes per CTA
 constexpr u64 kBChunk = static_cast<u64>(kBT) * kBPer;
 
 struct JobDev {
     u64 sym_off, out_off, w_off, gws_off;
-    u32 cap, hbits;
+    u64 fp_off, ep_off, snap_off;
+    u32 cap, hbits, ep_cap, pad;
 };
 
 __device__ __forceinline__ u32 hslot(u64 v, u32 hb) {
     return static_cast<u32>((v * 0x9E3779B97F4A7C15ull) >> (64 - hb));
 }
 
-// u32 words of one model: hkey (2H) | hval (H) | hpos (H) | cnt (cap) | pre (cap + 1)
-__host__ __device__ inline u64 model_words(u32 cap, u32 hbits) { return 4ull * (1ull << hbits) + 2ull * cap + 2; }
 
 template <int NT>
 __device__ __forceinline__ u32 block_excl_scan(u32 v, u32* red, u32& total) {
@@ -61,143 +59,230 @@ __device__ __forceinline__ u32 block_excl_scan(u32 v, u32* red, u32& total) {
 
 // ---------------------------------------------------------------- 1. model
 // Per symbol record: bits 0-15 total, bit 16 escape, 32-47 freq, 48-63 cum.
-__global__ void __launch_bounds__(kMT) ac_model_kernel(const u64* __restrict__ syms, const u64* __restrict__ counts,
-                                                       int stride, const JobDev* __restrict__ jobs, int njobs,
-                                                       const int* __restrict__ ids, u64* __restrict__ recs,
-                                                       u32* __restrict__ gws, u32 smem_cap) {
-    extern __shared__ __align__(16) u8 am_smem[];
-    __shared__ int si[kMT];
-    __shared__ u32 red[kMT / 32];
-    __shared__ u32 sh_nsym, sh_total, sh_lastesc;
+//
+// The adaptive model in three passes:
+//  1a. index: a symbol's model index is 1 + the rank of its value's first
+//      occurrence (escape = 0), so every symbol is indexed in parallel (hash of
+//      values with the minimum position, the distinct values sorted by it);
+//  1b. epochs: the only sequential part -- between two halvings every count is
+//      its epoch-start value plus 32 per occurrence, so one CTA walks the
+//      stream an epoch at a time (a histogram, the halving, the new total) and
+//      records each epoch's start counts;
+//  1c. code: every epoch of every stream at once, one CTA each: (cum, freq,
+//      total) of a symbol = the epoch-start prefix/count plus 32 per earlier
+//      occurrence inside the epoch (256-symbol sub-chunks: dominance counts,
+//      then a prefix rebuild).
+constexpr int kIxT = 1024;  // index / epoch passes
+constexpr u32 kIxSmemEntries = 4096;
+
+// u32 words of the index pass's tables: hkey (2H) | hpos (H) | hval (H) | list (2 cap)
+__host__ __device__ inline u64 index_words(u32 cap, u32 hbits) { return 4ull * (1ull << hbits) + 2ull * cap; }
+
+__global__ void __launch_bounds__(kIxT) ac_index_kernel(const u64* __restrict__ syms, const u64* __restrict__ counts,
+                                                        int stride, const JobDev* __restrict__ jobs, int njobs,
+                                                        const int* __restrict__ ids, u32* __restrict__ idx,
+                                                        u32* __restrict__ fp, u32* __restrict__ ndist,
+                                                        u32* __restrict__ gws, u32 smem_cap, int* __restrict__ err) {
+    extern __shared__ __align__(16) u8 ax_smem[];
+    __shared__ u32 nd_s;
     const int jid = ids ? ids[blockIdx.x] : static_cast<int>(blockIdx.x);
     if (jid >= njobs) return;
     const JobDev jb = jobs[jid];
     const u64 ns = counts[static_cast<u64>(jid) * stride];
-    if (ns == 0) return;
+    if (ns == 0) {
+        if (threadIdx.x == 0) ndist[jid] = 0;
+        return;
+    }
     const u32 H = 1u << jb.hbits, hmask = H - 1;
-    u32* base = jb.cap <= smem_cap ? reinterpret_cast<u32*>(am_smem) : gws + jb.gws_off;
+    u32* base = jb.cap <= smem_cap ? reinterpret_cast<u32*>(ax_smem) : gws + jb.gws_off;
     u64* hkey = reinterpret_cast<u64*>(base);
-    u32* hval = base + 2 * H;
-    u32* hpos = hval + H;
-    u32* cnt = hpos + H;
-    u32* pre = cnt + jb.cap;
-    const int t = threadIdx.x;
-    for (u32 i = t; i < H; i += kMT) {
+    u32* hpos = base + 2 * H;
+    u32* hval = hpos + H;
+    u64* list = reinterpret_cast<u64*>(hval + H);
+    const u64* sy = syms + jb.sym_off;
+    for (u32 i = threadIdx.x; i < H; i += kIxT) {
         hkey[i] = kEmpty;
-        hval[i] = 0;
         hpos[i] = 0xFFFFFFFFu;
     }
-    for (u32 i = t; i < jb.cap; i += kMT) cnt[i] = 0;
+    if (threadIdx.x == 0) nd_s = 0;
     __syncthreads();
-    if (t == 0) {
-        cnt[0] = 1;  // the escape
-        pre[0] = 0;
-        pre[1] = 1;
-        sh_nsym = 1;
-        sh_total = 1;
+    for (u64 k = threadIdx.x; k < ns; k += kIxT) {
+        const u64 v = sy[k];
+        u32 h = hslot(v, jb.hbits);
+        while (true) {
+            const u64 key = hkey[h];
+            if (key == v) break;
+            if (key == kEmpty) {
+                const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(&hkey[h]),
+                                           static_cast<unsigned long long>(kEmpty), static_cast<unsigned long long>(v));
+                if (prev == kEmpty || prev == v) break;
+                continue;
+            }
+            h = (h + 1) & hmask;
+        }
+        atomicMin(&hpos[h], static_cast<u32>(k));
     }
     __syncthreads();
-    u64* rc = recs + jb.sym_off;
-    const u64* sy = syms + jb.sym_off;
-    for (u64 k = 0; k < ns;) {
-        const u32 nsym = sh_nsym, total = sh_total;
-        // the first symbol whose update finds total + 32 >= 2^16 is coded, then
-        // the model halves, then its own increment is applied
+    // the distinct values (position, slot), then sorted by position
+    for (u32 i = threadIdx.x; i < H; i += kIxT)
+        if (hkey[i] != kEmpty) {
+            const u32 at = atomicAdd(&nd_s, 1u);
+            if (at < jb.cap) list[at] = (static_cast<u64>(hpos[i]) << 32) | i;
+            else *err = 1;
+        }
+    __syncthreads();
+    const u32 D = min(nd_s, jb.cap);
+    u32 P2 = 1;
+    while (P2 < D) P2 <<= 1;
+    for (u32 i = D + threadIdx.x; i < P2; i += kIxT) list[i] = ~u64{0};  // list holds 2 cap >= P2 entries
+    __syncthreads();
+    for (u32 k = 2; k <= P2; k <<= 1)
+        for (u32 j = k >> 1; j > 0; j >>= 1) {
+            for (u32 i = threadIdx.x; i < P2; i += kIxT) {
+                const u32 l = i ^ j;
+                if (l > i) {
+                    const u64 a = list[i], b = list[l];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        list[i] = b;
+                        list[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    u32* fpj = fp + jb.fp_off;
+    for (u32 r = threadIdx.x; r < D; r += kIxT) {
+        hval[static_cast<u32>(list[r])] = r + 1;
+        fpj[r] = static_cast<u32>(list[r] >> 32);
+    }
+    if (threadIdx.x == 0) ndist[jid] = D;
+    __syncthreads();
+    u32* ij = idx + jb.sym_off;
+    for (u64 k = threadIdx.x; k < ns; k += kIxT) {
+        const u64 v = sy[k];
+        u32 h = hslot(v, jb.hbits);
+        while (hkey[h] != v) h = (h + 1) & hmask;
+        ij[k] = hval[h];
+    }
+}
+
+// epoch records: (first symbol, total, model size) per epoch; counts snapshot u16 x cap
+__global__ void __launch_bounds__(kIxT) ac_epoch_kernel(const u64* __restrict__ counts, int stride,
+                                                        const JobDev* __restrict__ jobs, int njobs,
+                                                        const u32* __restrict__ idx, const u32* __restrict__ fp,
+                                                        const u32* __restrict__ ndist, uint4* __restrict__ eprec,
+                                                        u16* __restrict__ snap, u32* __restrict__ nep,
+                                                        int* __restrict__ err) {
+    extern __shared__ __align__(16) u32 ep_cnt[];
+    __shared__ u32 red[kIxT / 32];
+    __shared__ u32 sh_nh, sh_nsym;
+    const int jid = static_cast<int>(blockIdx.x);
+    if (jid >= njobs) return;
+    const JobDev jb = jobs[jid];
+    const u64 ns = counts[static_cast<u64>(jid) * stride];
+    if (ns == 0) {
+        if (threadIdx.x == 0) nep[jid] = 0;
+        return;
+    }
+    const u32 cap = jb.cap, D = ndist[jid];
+    const u32* ij = idx + jb.sym_off;
+    const u32* fpj = fp + jb.fp_off;
+    uint4* er = eprec + jb.ep_off;
+    u16* sn = snap + jb.snap_off;
+    for (u32 i = threadIdx.x; i < cap; i += kIxT) ep_cnt[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) ep_cnt[0] = 1;
+    __syncthreads();
+    u32 total = 1, nsym = 1, e = 0;
+    // number of distinct values whose first occurrence is before position k
+    auto first_before = [&](u64 k) {
+        u32 lo = 0, hi = D;
+        while (lo < hi) {
+            const u32 mid = (lo + hi) >> 1;
+            if (fpj[mid] < k) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    for (u64 k0 = 0; k0 < ns;) {
+        if (e >= jb.ep_cap) {
+            if (threadIdx.x == 0) *err = 2;
+            break;
+        }
         const u32 d = total >= 65504u ? 0u : (65504u - total + 31u) / 32u;
-        u32 L = static_cast<u32>(min(static_cast<u64>(kMT), ns - k));
-        bool halv = false;
-        if (d < L) {
-            L = d + 1;
-            halv = true;
-        }
-        const bool act = static_cast<u32>(t) < L;
-        u64 v = 0;
-        int I = -1;
-        u32 slot = 0;
-        if (act) {
-            v = sy[k + t];
-            u32 h = hslot(v, jb.hbits);
-            while (true) {
-                const u64 key = hkey[h];
-                if (key == v) {
-                    I = static_cast<int>(hval[h]) - 1;
-                    break;
-                }
-                if (key == kEmpty) break;
-                h = (h + 1) & hmask;
-            }
-        }
-        __syncthreads();  // every lookup before any claim
-        const bool claim = act && I < 0;
-        if (claim) {
-            u32 h = hslot(v, jb.hbits);
-            while (true) {
-                const u64 key = hkey[h];
-                if (key == v) break;
-                if (key == kEmpty) {
-                    const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(&hkey[h]),
-                                               static_cast<unsigned long long>(kEmpty),
-                                               static_cast<unsigned long long>(v));
-                    if (prev == kEmpty || prev == v) break;
-                    continue;
-                }
-                h = (h + 1) & hmask;
-            }
-            slot = h;
-            atomicMin(&hpos[h], static_cast<u32>(t));
+        const u64 kh = k0 + d;
+        const bool halv = kh < ns;
+        const u64 kend = halv ? kh : ns;
+        if (threadIdx.x == 0) er[e] = make_uint4(static_cast<u32>(k0), total, nsym, 0);
+        for (u32 i = threadIdx.x; i < nsym; i += kIxT) sn[static_cast<u64>(e) * cap + i] = static_cast<u16>(ep_cnt[i]);
+        __syncthreads();
+        for (u64 j = k0 + threadIdx.x; j < kend; j += kIxT) atomicAdd(&ep_cnt[ij[j]], 32u);
+        ++e;
+        if (!halv) break;
+        if (threadIdx.x == 0) {
+            sh_nh = 1 + first_before(kh);        // the model before the halving symbol's insert
+            sh_nsym = 1 + first_before(kh + 1);  // after it
         }
         __syncthreads();
-        // new values take indices in order of their first occurrence
-        const u32 first = (claim && hpos[slot] == static_cast<u32>(t)) ? 1u : 0u;
-        u32 nnew;
-        const u32 rank = block_excl_scan<kMT>(first, red, nnew);
-        if (first) hval[slot] = nsym + rank + 1;
+        const u32 nh = sh_nh;
+        nsym = sh_nsym;
+        for (u32 i = threadIdx.x; i < nh; i += kIxT) ep_cnt[i] = max(1u, ep_cnt[i] >> 1);
         __syncthreads();
-        bool esc = false;
-        if (claim) {
-            I = static_cast<int>(hval[slot]) - 1;
-            esc = first != 0;
-        }
-        si[t] = act ? I : 0x7fffffff;
-        if (act && static_cast<u32>(t) == L - 1) sh_lastesc = esc ? 1u : 0u;
+        if (threadIdx.x == 0) ep_cnt[ij[kh]] += 32u;
         __syncthreads();
-        if (act) {
-            // counts at this symbol: chunk-start count + 32 per earlier occurrence
-            u32 less = 0, same = 0;
-            for (int j = 0; j < t; ++j) {
-                const int Ij = si[j];
-                less += Ij < I ? 1u : 0u;
-                same += Ij == I ? 1u : 0u;
-            }
-            const u32 T = total + 32u * static_cast<u32>(t);
-            u64 rec;
-            if (esc) {
-                rec = (u64{1} << 32) | (u64{1} << 16) | T;  // escape interval: cum 0, freq 1
-            } else {
-                const bool old = static_cast<u32>(I) < nsym;
-                const u32 cum = (old ? pre[I] : total) + 32u * less;
-                const u32 f = (old ? cnt[I] : 0u) + 32u * same;
-                rec = (static_cast<u64>(cum) << 48) | (static_cast<u64>(f) << 32) | T;
-            }
-            rc[k + t] = rec;
-        }
-        __syncthreads();  // every read of cnt / pre / hpos done
-        if (act) {
-            if (claim) hpos[slot] = 0xFFFFFFFFu;
-            if (!(halv && static_cast<u32>(t) == L - 1)) atomicAdd(&cnt[I], 32u);
-        }
-        __syncthreads();
-        const u32 newn = nsym + nnew;
-        if (halv) {
-            // an inserted halving symbol is pushed after the halving
-            const u32 nh = newn - sh_lastesc;
-            for (u32 i = t; i < nh; i += kMT) cnt[i] = max(1u, cnt[i] >> 1);
-            __syncthreads();
-            if (static_cast<u32>(t) == L - 1) cnt[I] += 32u;
-            __syncthreads();
-        }
-        const u32 per = (newn + kMT - 1) / kMT;
-        const u32 i0 = min(newn, static_cast<u32>(t) * per), i1 = min(newn, i0 + per);
+        u32 loc = 0;
+        for (u32 i = threadIdx.x; i < nsym; i += kIxT) loc += ep_cnt[i];
+        u32 tot;
+        block_excl_scan<kIxT>(loc, red, tot);
+        total = tot;
+        k0 = kh + 1;
+    }
+    if (threadIdx.x == 0) nep[jid] = e;
+}
+
+__device__ __forceinline__ int job_of_slot(const u64* __restrict__ off, int njobs, u64 slot) {
+    int lo = 0, hi = njobs - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= slot) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kMT) ac_code_kernel(const u64* __restrict__ counts, int stride,
+                                                      const JobDev* __restrict__ jobs, int njobs,
+                                                      const u64* __restrict__ epslot, const u32* __restrict__ idx,
+                                                      const u32* __restrict__ fp, const u32* __restrict__ ndist,
+                                                      const uint4* __restrict__ eprec, const u16* __restrict__ snap,
+                                                      const u32* __restrict__ nep, u64* __restrict__ recs) {
+    extern __shared__ __align__(16) u32 cd_smem[];
+    __shared__ int si[kMT];
+    __shared__ u32 red[kMT / 32];
+    const u64 slot = blockIdx.x;
+    const int jid = job_of_slot(epslot, njobs, slot);
+    const u32 e = static_cast<u32>(slot - epslot[jid]);
+    const u32 ne = nep[jid];
+    if (e >= ne) return;
+    const JobDev jb = jobs[jid];
+    const u64 ns = counts[static_cast<u64>(jid) * stride];
+    const uint4 r0 = eprec[jb.ep_off + e];
+    const u64 k0 = r0.x, k1 = e + 1 < ne ? eprec[jb.ep_off + e + 1].x : ns;
+    const u32 T0 = r0.y, nsym0 = r0.z;
+    const u32 nend = e + 1 < ne ? eprec[jb.ep_off + e + 1].z : ndist[jid] + 1;  // model size at the epoch end
+    u32* cnt = cd_smem;
+    u32* pre = cnt + jb.cap;
+    const u16* sn = snap + jb.snap_off + static_cast<u64>(e) * jb.cap;
+    const u32* ij = idx + jb.sym_off;
+    const u32* fpj = fp + jb.fp_off;
+    u64* rc = recs + jb.sym_off;
+    const int t = threadIdx.x;
+    for (u32 i = t; i < nend; i += kMT) cnt[i] = i < nsym0 ? sn[i] : 0u;
+    __syncthreads();
+    auto rebuild_prefix = [&]() {
+        const u32 per = (nend + kMT - 1) / kMT;
+        const u32 i0 = min(nend, static_cast<u32>(t) * per), i1 = min(nend, i0 + per);
         u32 loc = 0;
         for (u32 i = i0; i < i1; ++i) loc += cnt[i];
         u32 tot;
@@ -206,13 +291,37 @@ __global__ void __launch_bounds__(kMT) ac_model_kernel(const u64* __restrict__ s
             pre[i] = off;
             off += cnt[i];
         }
-        if (t == 0) {
-            pre[newn] = tot;
-            sh_nsym = newn;
-            sh_total = tot;
+        __syncthreads();
+    };
+    rebuild_prefix();
+    for (u64 k = k0; k < k1; k += kMT) {
+        const u64 kk = k + t;
+        const bool act = kk < k1;
+        const int I = act ? static_cast<int>(ij[kk]) : 0x7fffffff;
+        si[t] = I;
+        __syncthreads();
+        if (act) {
+            u32 less = 0, same = 0;
+            for (int j = 0; j < t; ++j) {
+                const int Ij = si[j];
+                less += Ij < I ? 1u : 0u;
+                same += Ij == I ? 1u : 0u;
+            }
+            const u32 T = T0 + 32u * static_cast<u32>(kk - k0);
+            u64 rec;
+            if (fpj[I - 1] == static_cast<u32>(kk)) {
+                rec = (u64{1} << 32) | (u64{1} << 16) | T;  // escape: cum 0, freq 1
+            } else {
+                const u32 cum = pre[I] + 32u * less;
+                const u32 f = cnt[I] + 32u * same;
+                rec = (static_cast<u64>(cum) << 48) | (static_cast<u64>(f) << 32) | T;
+            }
+            rc[kk] = rec;
         }
         __syncthreads();
-        k += L;
+        if (act) atomicAdd(&cnt[I], 32u);
+        __syncthreads();
+        if (k + kMT < k1) rebuild_prefix();
     }
 }
 
@@ -490,19 +599,15 @@ const u64* magic_table(cudaStream_t s) {
 }
 
 u32 hash_bits(u32 cap);
-
-// the largest model's shared memory, opted in once per device (concurrent
-// callers on worker threads launch with different sizes below it)
+// the largest index-pass tables, opted in once per device (concurrent callers
+// on worker threads launch with different sizes below it)
 void model_smem_attr() {
-    static std::mutex mu;
-    static std::map<int, bool> done;
-    int dev = 0;
-    TCB_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(mu);
-    if (done[dev]) return;
-    TCB_CUDA(cudaFuncSetAttribute(ac_model_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(model_words(kSmemEntries, hash_bits(kSmemEntries)) * 4)));
-    done[dev] = true;
+    TCB_ONCE_PER_DEVICE({
+        cudaFuncSetAttribute(ac_index_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(index_words(kIxSmemEntries, hash_bits(kIxSmemEntries)) * 4));
+        cudaFuncSetAttribute(ac_epoch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(ac_code_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    });
 }
 
 u32 hash_bits(u32 cap) {
@@ -529,9 +634,9 @@ void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector
     if (nj == 0) return;
     TCB_CUDA(cudaMemsetAsync(elen, 0, nj * sizeof(u64), s));
     std::vector<JobDev> jd(nj);
-    std::vector<u64> choff(nj + 1, 0);
-    u64 wtot = 0, gtot = 0, rec_ext = 0;
-    std::vector<int> big;
+    std::vector<u64> choff(nj + 1, 0), epslot(nj + 1, 0);
+    u64 wtot = 0, gtot = 0, rec_ext = 0, fptot = 0, eptot = 0, sntot = 0;
+    u32 cap_max = 1;
     for (int j = 0; j < nj; ++j) {
         const AcJob& a = jobs[j];
         JobDev& d = jd[j];
@@ -540,52 +645,68 @@ void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector
         const u64 esc = ac_escape_bound(a.sym_cap, a.positions);
         d.cap = static_cast<u32>(esc + 1);
         d.hbits = hash_bits(d.cap);
+        cap_max = std::max(cap_max, d.cap);
         d.w_off = wtot;
         const u64 wcap = a.sym_cap ? 2 * a.sym_cap + 5 * esc + 8 : 0;
         wtot += wcap;
         choff[j + 1] = choff[j] + (wcap + kBChunk - 1) / kBChunk;
         rec_ext = std::max(rec_ext, a.sym_off + a.sym_cap);
-        if (d.cap <= kSmemEntries) {
+        d.fp_off = fptot;
+        fptot += d.cap;
+        // an epoch holds at least (65504 - 32768 - cap - 32) / 32 symbols after the first halving
+        const u64 dmin = d.cap < 32000 ? (65504 - 32768 - d.cap - 32) / 32 : 1;
+        d.ep_cap = static_cast<u32>(a.sym_cap / std::max<u64>(dmin, 1) + 4);
+        d.ep_off = eptot;
+        eptot += d.ep_cap;
+        epslot[j + 1] = eptot;
+        d.snap_off = sntot;
+        sntot += static_cast<u64>(d.ep_cap) * d.cap;
+        if (d.cap <= kIxSmemEntries) {
             d.gws_off = 0;
         } else {
             d.gws_off = gtot;
-            gtot += (model_words(d.cap, d.hbits) + 3) & ~u64{3};
-            big.push_back(j);
+            gtot += (index_words(d.cap, d.hbits) + 3) & ~u64{3};
         }
     }
-    // models of one launch share the dynamic shared-memory size: small ones (most
-    // planes) in their own launch so several fit per SM
+    if (cap_max > 40000) throw Error("entropy: too many distinct run lengths for the device model");
     DevBuf<JobDev> djobs(nj, s);
     djobs.upload(jd.data(), nj);
-    DevBuf<u64> recs(rec_ext + 1, s), W(wtot + 1, s), nout(nj, s), dch(nj + 1, s);
-    DevBuf<u32> gws(gtot + 4, s);
+    DevBuf<u64> recs(rec_ext + 1, s), W(wtot + 1, s), nout(nj, s), dch(nj + 1, s), dep(nj + 1, s);
+    DevBuf<u32> gws(gtot + 4, s), idx(rec_ext + 1, s), fp(fptot + 1, s), ndist(nj, s), nep(nj, s);
+    DevBuf<uint4> eprec(eptot + 1, s);
+    DevBuf<u16> snap(sntot + 1, s);
+    DevBuf<int> err(1, s);
+    err.zero();
     dch.upload(choff.data(), nj + 1);
+    dep.upload(epslot.data(), nj + 1);
     const u64 nchunk = choff.back();
     DevBuf<u8> csum(nchunk + 1, s), cin(nchunk + 1, s);
     const u64* magic = magic_table(s);
     {
         ProfScope pa(kAc, s);
+        model_smem_attr();
         constexpr u32 kSmall = 512;
         std::vector<int> small_ids, large_ids;
         for (int j = 0; j < nj; ++j) (jd[j].cap <= kSmall ? small_ids : large_ids).push_back(j);
-        auto launch = [&](const std::vector<int>& ids) {
-            if (ids.empty()) return;
-            // shared memory for the largest model of this launch that fits; larger
-            // models live in their global workspace
+        for (const auto* ids : {&small_ids, &large_ids}) {  // tables sized per launch: small models pack an SM
+            if (ids->empty()) continue;
             u32 mc = 0;
-            for (int j : ids)
-                if (jd[j].cap <= kSmemEntries) mc = std::max(mc, jd[j].cap);
-            const u64 sm = mc ? model_words(mc, hash_bits(mc)) * 4 : 0;
-            model_smem_attr();
-            DevBuf<int> dids(ids.size(), s);
-            dids.upload(ids.data(), ids.size());
-            ac_model_kernel<<<static_cast<unsigned>(ids.size()), kMT, sm, s>>>(syms, counts, stride, djobs.p, nj,
-                                                                               dids.p, recs.p, gws.p, mc);
+            for (int j : *ids)
+                if (jd[j].cap <= kIxSmemEntries) mc = std::max(mc, jd[j].cap);
+            const u64 sm = mc ? index_words(mc, hash_bits(mc)) * 4 : 0;
+            DevBuf<int> dids(ids->size(), s);
+            dids.upload(ids->data(), ids->size());
+            ac_index_kernel<<<static_cast<unsigned>(ids->size()), kIxT, sm, s>>>(
+                syms, counts, stride, djobs.p, nj, dids.p, idx.p, fp.p, ndist.p, gws.p, mc, err.p);
             count_launch();
             TCB_LAUNCH();
-        };
-        launch(small_ids);
-        launch(large_ids);
+        }
+        ac_epoch_kernel<<<static_cast<unsigned>(nj), kIxT, cap_max * sizeof(u32), s>>>(
+            counts, stride, djobs.p, nj, idx.p, fp.p, ndist.p, eprec.p, snap.p, nep.p, err.p);
+        ac_code_kernel<<<static_cast<unsigned>(eptot), kMT, 2 * (cap_max + 1) * sizeof(u32), s>>>(
+            counts, stride, djobs.p, nj, dep.p, idx.p, fp.p, ndist.p, eprec.p, snap.p, nep.p, recs.p);
+        count_launch(2);
+        TCB_LAUNCH();
         ac_range_kernel<<<cdiv(static_cast<u64>(nj) * 32, 128), 128, 0, s>>>(syms, counts, stride, djobs.p, nj, recs.p,
                                                                              magic, W.p, nout.p);
         count_launch();
@@ -602,6 +723,10 @@ void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector
         count_launch();
         TCB_LAUNCH();
     }
+    int herr = 0;
+    d2h(&herr, err.p, sizeof(int), s);
+    stream_sync(s);
+    if (herr) throw Error("entropy: device model capacity exceeded");
 }
 
 }  // namespace tcb

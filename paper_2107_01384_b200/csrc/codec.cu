@@ -507,57 +507,97 @@ __device__ __forceinline__ long long cta_excl_max(long long v, long long* sh, lo
 
 // ---------------------------------------------------------------- decoded model
 constexpr int kDecThreads = 256;
-constexpr int kDecPer = 4;
 
-__global__ void decode_model_kernel(const u64* __restrict__ m, u64 n, u64 block, int lp,
-                                    const u64* __restrict__ stops, u64* __restrict__ dec) {
+// In 8192-position sub-chunks (all at once): lead / trail counts per sub-chunk,
+// their prefix per block, then every position's decoded magnitude with the
+// block's stops (the lead / trail index of a position is its sub-chunk's prefix
+// plus a CTA scan).
+constexpr u64 kDmSc = static_cast<u64>(kDecThreads) * 32;
+
+__global__ void __launch_bounds__(kDecThreads) dm_count_kernel(const u64* __restrict__ m, u64 n, u64 block, u64 spb,
+                                                                int lp, unsigned long long* __restrict__ cnt) {
+    __shared__ unsigned long long sh[2];
+    const u64 b = blockIdx.x / spb, j = blockIdx.x % spb;
+    const u64 lo = b * block + j * kDmSc, hi = min(min(n, (b + 1) * block), lo + kDmSc);
+    if (threadIdx.x < 2) sh[threadIdx.x] = 0;
+    __syncthreads();
+    u32 nl = 0, nt = 0;
+    for (u64 i = lo + threadIdx.x; i < hi; i += kDecThreads) {
+        const int t = top_bit(m[i]);
+        nl += t <= lp;
+        nt += t > lp;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        nl += __shfl_xor_sync(0xffffffffu, nl, o);
+        nt += __shfl_xor_sync(0xffffffffu, nt, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&sh[0], static_cast<unsigned long long>(nl));
+        atomicAdd(&sh[1], static_cast<unsigned long long>(nt));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        cnt[2 * blockIdx.x] = sh[0];
+        cnt[2 * blockIdx.x + 1] = sh[1];
+    }
+}
+
+__global__ void dm_scan_kernel(unsigned long long* __restrict__ cnt, u64 nb, u64 spb) {
+    const u64 b = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    unsigned long long L = 0, T = 0;
+    for (u64 j = 0; j < spb; ++j) {
+        unsigned long long* c = cnt + 2 * (b * spb + j);
+        const unsigned long long l = c[0], t = c[1];
+        c[0] = L;
+        c[1] = T;
+        L += l;
+        T += t;
+    }
+}
+
+__global__ void __launch_bounds__(kDecThreads) dm_decode_kernel(const u64* __restrict__ m, u64 n, u64 block, u64 spb,
+                                                                 int lp, const u64* __restrict__ stops,
+                                                                 const unsigned long long* __restrict__ cnt,
+                                                                 u64* __restrict__ dec) {
     __shared__ u64 sh[kDecThreads / 32 + 1];
-    const u64 b = blockIdx.x;
-    const u64 lo = b * block, hi = min(n, lo + block);
+    const u64 b = blockIdx.x / spb, j = blockIdx.x % spb;
+    const u64 lo = b * block + j * kDmSc, hi = min(min(n, (b + 1) * block), lo + kDmSc);
     const u64 lstop = stops[2 * b], tstop = stops[2 * b + 1];
-    u64 lbase = 0, tbase = 0;
-    for (u64 c0 = lo; c0 < hi; c0 += static_cast<u64>(kDecThreads) * kDecPer) {
-        const u64 i0 = c0 + static_cast<u64>(threadIdx.x) * kDecPer;
-        u64 v[kDecPer];
-        int tb[kDecPer];
-        u32 nl = 0, nt = 0;
-#pragma unroll
-        for (int q = 0; q < kDecPer; ++q) {
-            const u64 i = i0 + q;
-            v[q] = i < hi ? m[i] : 0;
-            tb[q] = i < hi ? top_bit(v[q]) : -2;
-            nt += tb[q] > lp;
-            nl += (tb[q] <= lp && tb[q] > -2);
+    const u64 i0 = lo + static_cast<u64>(threadIdx.x) * 32;
+    u32 nl = 0, nt = 0;
+    for (int q = 0; q < 32; ++q) {
+        const u64 i = i0 + q;
+        if (i >= hi) break;
+        const int t = top_bit(m[i]);
+        nt += t > lp;
+        nl += t <= lp;
+    }
+    u64 tot;
+    const u64 pre = cta_excl_scan<kDecThreads>((static_cast<u64>(nt) << 32) | nl, sh, tot);
+    u64 li = cnt[2 * blockIdx.x] + (pre & 0xffffffffu), ti = cnt[2 * blockIdx.x + 1] + (pre >> 32);
+    for (int q = 0; q < 32; ++q) {
+        const u64 i = i0 + q;
+        if (i >= hi) break;
+        const u64 v = m[i];
+        const int t = top_bit(v);
+        int pe = -1;
+        if (t > lp) {
+            pe = (ti++ < tstop) ? lp : lp + 1;
+        } else {
+            const bool within = li++ < lstop;
+            if (t == lp && within) pe = lp;
         }
-        u64 tot;
-        const u64 pre = cta_excl_scan<kDecThreads>((static_cast<u64>(nt) << 32) | nl, sh, tot);
-        u64 li = lbase + (pre & 0xffffffffu), ti = tbase + (pre >> 32);
-#pragma unroll
-        for (int q = 0; q < kDecPer; ++q) {
-            const u64 i = i0 + q;
-            if (tb[q] == -2) continue;
-            int pe = -1;
-            if (tb[q] > lp) {
-                pe = (ti++ < tstop) ? lp : lp + 1;
-            } else {
-                const bool within = li++ < lstop;
-                if (tb[q] == lp && within) pe = lp;
-            }
-            u64 out = 0;
-            if (pe >= 0) {
-                out = pe >= 64 ? 0 : (v[q] >> pe) << pe;
-                if (pe >= 1 && pe < 64) out += u64{1} << (pe - 1);
-            }
-            dec[i] = out;
+        u64 out = 0;
+        if (pe >= 0) {
+            out = pe >= 64 ? 0 : (v >> pe) << pe;
+            if (pe >= 1 && pe < 64) out += u64{1} << (pe - 1);
         }
-        lbase += tot & 0xffffffffu;
-        tbase += tot >> 32;
+        dec[i] = out;
     }
 }
 
 // ---------------------------------------------------------------- emission
-constexpr int kEmT = 256;
-constexpr int kEmPer = 4;
 
 struct StreamDesc {
     u64 lo, hi;          // block range
@@ -573,70 +613,179 @@ struct StreamOut {
     u64 nraw;     // raw bits
 };
 
-__global__ void __launch_bounds__(kEmT) emit_kernel(const u64* __restrict__ m, const u8* __restrict__ neg,
-                                                    const StreamDesc* __restrict__ desc, u64* __restrict__ syms,
-                                                    u32* __restrict__ raw, StreamOut* __restrict__ sout) {
-    __shared__ u64 sh[kEmT / 32 + 1];
-    __shared__ long long shm[kEmT / 32 + 1];
-    const StreamDesc d = desc[blockIdx.x];
-    const int p = d.plane;
-    u64 lcnt = 0, tcnt = 0, rawcnt = 0, onecnt = 0;
-    long long last = -1;  // lead index of the previous one
-    for (u64 c0 = d.lo; c0 < d.hi; c0 += static_cast<u64>(kEmT) * kEmPer) {
-        const u64 i0 = c0 + static_cast<u64>(threadIdx.x) * kEmPer;
-        u64 v[kEmPer];
-        int tb[kEmPer];
+// ---------------------------------------------------------------- parallel emission
+// Every (plane, block) stream at once, in 8192-position sub-chunks: the
+// sub-chunks' msb histograms give each stream's lead / trail / one counts
+// before any sub-chunk (only a breakpoint stream's lead-stop crossing needs a
+// scan), so one CTA per sub-chunk emits every plane from register-resident
+// magnitudes: CTA scans place the symbols and raw bits; a sub-chunk's first
+// zero-run symbol (which needs the previous sub-chunk's last one) is fixed up
+// per stream afterwards.
+constexpr int kScT = 256, kScPer = 32;
+constexpr u64 kSc = static_cast<u64>(kScT) * kScPer;
+
+struct ScOff {
+    u64 lead_b, trail_b, ones_b, raw_b;  // positions / symbols / raw bits before the sub-chunk
+};
+
+__device__ __forceinline__ int sc_block(const u64* __restrict__ scoff, int nb, u64 g) {
+    int lo = 0, hi = nb - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (scoff[mid] <= g) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kScT) sc_hist_kernel(const u64* __restrict__ m, const StreamDesc* __restrict__ sd,
+                                                       const u64* __restrict__ scoff, int nb, u32* __restrict__ hist) {
+    __shared__ u32 h[65];
+    const u64 g = blockIdx.x;
+    const int bi = sc_block(scoff, nb, g);
+    const StreamDesc d = sd[bi];  // plane-major layout: stream bi is block bi of the top plane
+    const u64 lo = d.lo + (g - scoff[bi]) * kSc, hi = min(d.hi, lo + kSc);
+    for (int i = threadIdx.x; i < 65; i += kScT) h[i] = 0;
+    __syncthreads();
+    for (u64 i0 = lo; i0 < hi; i0 += kScT) {
+        const u64 i = i0 + threadIdx.x;
+        const int bin = i < hi ? top_bit(m[i]) + 1 : -1;
+        const unsigned act = __ballot_sync(0xffffffffu, bin >= 0);
+        const unsigned same = __match_any_sync(0xffffffffu, bin) & act;
+        if (bin >= 0 && (__ffs(same) - 1) == static_cast<int>(threadIdx.x & 31)) atomicAdd(&h[bin], __popc(same));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 65; i += kScT) hist[g * 65 + i] = h[i];
+}
+
+// one thread per stream: the offsets of every sub-chunk, and the stream's sizes
+__global__ void sc_scan_kernel(const u64* __restrict__ m, const StreamDesc* __restrict__ sd, int ns, int nb,
+                               const u64* __restrict__ scoff, u64 nsc_all, const u32* __restrict__ hist,
+                               ScOff* __restrict__ tab, StreamOut* __restrict__ so, u64* __restrict__ ncol_out) {
+    const int st = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
+    if (st >= ns) return;
+    const StreamDesc d = sd[st];
+    const int bi = st % nb, pi = st / nb, p = d.plane;
+    const u64 nsc = scoff[bi + 1] - scoff[bi];
+    ScOff* tb = tab + static_cast<u64>(pi) * nsc_all + scoff[bi];
+    u64 LB = 0, TB = 0, OB = 0;
+    bool crossed = false;
+    for (u64 j = 0; j < nsc; ++j) {
+        const u32* h = hist + (scoff[bi] + j) * 65;
+        u64 lead = 0, trail = 0;
+        for (int q = 0; q <= p + 1; ++q) lead += h[q];
+        for (int q = p + 2; q < 65; ++q) trail += h[q];
+        const u64 ones = h[p + 1];
+        tb[j] = ScOff{LB, TB, OB, min(TB, d.tstop) + OB};
+        if (!crossed) {
+            if (LB + lead > d.lstop) {  // the lead stop falls in this sub-chunk: its ones up to the stop
+                const u64 lo = d.lo + j * kSc, hi = min(d.hi, lo + kSc);
+                u64 li = LB, part = 0;
+                for (u64 i = lo; i < hi && li < d.lstop; ++i) {
+                    const int t = top_bit(m[i]);
+                    if (t <= p) {
+                        part += t == p;
+                        ++li;
+                    }
+                }
+                OB += part;
+                crossed = true;
+            } else {
+                OB += ones;
+            }
+        }
+        LB += lead;
+        TB += trail;
+    }
+    const u64 ncol = min(LB, d.lstop);
+    so[st] = StreamOut{ncol > 0 ? OB + 1 : 0, min(TB, d.tstop) + OB};
+    ncol_out[st] = ncol;
+}
+
+// one CTA per sub-chunk, every plane of the layout
+__global__ void __launch_bounds__(kScT) sc_emit_kernel(const u64* __restrict__ m, const u8* __restrict__ neg,
+                                                       const StreamDesc* __restrict__ sd, int np, int nb,
+                                                       const u64* __restrict__ scoff, u64 nsc_all,
+                                                       const ScOff* __restrict__ tab, u64* __restrict__ syms,
+                                                       u32* __restrict__ raw, long long* __restrict__ fx) {
+    __shared__ u64 sh[kScT / 32 + 1];
+    __shared__ long long shm[kScT / 32 + 1];
+    __shared__ long long sh_first;
+    const u64 g = blockIdx.x;
+    const int bi = sc_block(scoff, nb, g);
+    const u64 j = g - scoff[bi];
+    const StreamDesc d0 = sd[bi];
+    const u64 lo = d0.lo + j * kSc, hi = min(d0.hi, lo + kSc);
+    const u64 i0 = lo + static_cast<u64>(threadIdx.x) * kScPer;
+    u64 v[kScPer];
+    u32 negm = 0;
+#pragma unroll
+    for (int q = 0; q < kScPer; ++q) {
+        const u64 i = i0 + q;
+        v[q] = i < hi ? m[i] : 0;
+        if (neg && i < hi && neg[i]) negm |= 1u << q;
+    }
+    const int nv = i0 >= hi ? 0 : static_cast<int>(min(static_cast<u64>(kScPer), hi - i0));
+    for (int pi = 0; pi < np; ++pi) {
+        const StreamDesc d = sd[static_cast<u64>(pi) * nb + bi];
+        const int p = d.plane;
+        const ScOff off = tab[static_cast<u64>(pi) * nsc_all + g];
         u32 nl = 0, nt = 0;
 #pragma unroll
-        for (int q = 0; q < kEmPer; ++q) {
-            const u64 i = i0 + q;
-            const bool in = i < d.hi;
-            v[q] = in ? m[i] : 0;
-            tb[q] = in ? top_bit(v[q]) : -2;
-            nt += tb[q] > p;
-            nl += (tb[q] <= p && tb[q] > -2);
-        }
+        for (int q = 0; q < kScPer; ++q)
+            if (q < nv) {
+                const int t = top_bit(v[q]);
+                nt += t > p;
+                nl += t <= p;
+            }
         u64 tot;
-        const u64 pre = cta_excl_scan<kEmT>((static_cast<u64>(nt) << 32) | nl, sh, tot);
-        u64 li = lcnt + (pre & 0xffffffffu), ti = tcnt + (pre >> 32);
-        // classify within the stops
+        const u64 pre = cta_excl_scan<kScT>((static_cast<u64>(nt) << 32) | nl, sh, tot);
+        u64 li = off.lead_b + (pre & 0xffffffffu), ti = off.trail_b + (pre >> 32);
         u32 rflag = 0, oflag = 0, nr = 0, no = 0;
-        long long lastL = -1;
-        u64 lidx[kEmPer];
+        long long lastL = -1, firstL = -1;
 #pragma unroll
-        for (int q = 0; q < kEmPer; ++q) {
-            lidx[q] = 0;
-            if (tb[q] == -2) continue;
-            if (tb[q] > p) {
+        for (int q = 0; q < kScPer; ++q) {
+            if (q >= nv) continue;
+            const int t = top_bit(v[q]);
+            if (t > p) {
                 if (ti++ < d.tstop) {
                     rflag |= 1u << q;
                     ++nr;
                 }
             } else {
                 const u64 myl = li++;
-                if (myl < d.lstop && tb[q] == p) {
+                if (myl < d.lstop && t == p) {
                     oflag |= 1u << q;
                     rflag |= 1u << q;
                     ++nr;
                     ++no;
-                    lidx[q] = myl;
+                    if (firstL < 0) firstL = static_cast<long long>(myl);
                     lastL = static_cast<long long>(myl);
                 }
             }
         }
         u64 tot2;
-        const u64 pre2 = cta_excl_scan<kEmT>((static_cast<u64>(nr) << 32) | no, sh, tot2);
-        const long long prevL = cta_excl_max<kEmT>(lastL, shm, last);
-        u64 ri = rawcnt + (pre2 >> 32), oi = onecnt + (pre2 & 0xffffffffu);
+        const u64 pre2 = cta_excl_scan<kScT>((static_cast<u64>(nr) << 32) | no, sh, tot2);
+        // the lead index of the last one before this thread (-1: none in this sub-chunk yet)
+        const long long prevL = cta_excl_max<kScT>(lastL, shm, -1);
+        if (threadIdx.x == 0) sh_first = LLONG_MAX;
+        __syncthreads();
+        if (firstL >= 0) atomicMin(reinterpret_cast<long long*>(&sh_first), firstL);
+        u64 ri = off.raw_b + (pre2 >> 32), oi = off.ones_b + (pre2 & 0xffffffffu);
         long long pl = prevL;
+        li = off.lead_b + (pre & 0xffffffffu);
 #pragma unroll
-        for (int q = 0; q < kEmPer; ++q) {
+        for (int q = 0; q < kScPer; ++q) {
+            if (q >= nv) continue;
+            const int t = top_bit(v[q]);
+            u64 myl = 0;
+            if (t <= p) myl = li++;
             if (!(rflag >> q & 1u)) continue;
             bool bit;
             if (oflag >> q & 1u) {
-                bit = neg ? neg[i0 + q] != 0 : false;
-                syms[d.sym_off + oi] = static_cast<u64>(static_cast<long long>(lidx[q]) - pl - 1);
-                pl = static_cast<long long>(lidx[q]);
+                bit = (negm >> q) & 1u;
+                if (pl >= 0) syms[d.sym_off + oi] = static_cast<u64>(static_cast<long long>(myl) - pl - 1);
+                pl = static_cast<long long>(myl);
                 ++oi;
             } else {
                 bit = (v[q] >> p) & 1u;
@@ -647,32 +796,37 @@ __global__ void __launch_bounds__(kEmT) emit_kernel(const u64* __restrict__ m, c
             }
             ++ri;
         }
-        lcnt += tot & 0xffffffffu;
-        tcnt += tot >> 32;
-        rawcnt += tot2 >> 32;
-        onecnt += tot2 & 0xffffffffu;
-        // last one index so far
-        __shared__ long long shl;
-        if (threadIdx.x == kEmT - 1) shl = max(prevL, lastL);
         __syncthreads();
-        last = shl;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        const u64 ncol = min(lcnt, d.lstop);
-        StreamOut o;
-        o.nraw = rawcnt;
-        if (ncol > 0) {
-            syms[d.sym_off + onecnt] = static_cast<u64>(static_cast<long long>(ncol) - 1 - last);
-            o.nsyms = onecnt + 1;
-        } else {
-            o.nsyms = 0;
+        if (threadIdx.x == kScT - 1) {  // the sub-chunk's first and last one (fix-up of its first symbol)
+            long long* f = fx + 2 * (static_cast<u64>(pi) * nsc_all + g);
+            f[0] = sh_first == LLONG_MAX ? -1 : sh_first;
+            f[1] = max(prevL, lastL);
         }
-        sout[blockIdx.x] = o;
+        __syncthreads();
     }
 }
 
-// ---------------------------------------------------------------- adaptive range coder
+// one thread per stream: each sub-chunk's first symbol and the stream's final run
+__global__ void sc_fix_kernel(const StreamDesc* __restrict__ sd, int ns, int nb, const u64* __restrict__ scoff,
+                              u64 nsc_all, const ScOff* __restrict__ tab, const long long* __restrict__ fx,
+                              const StreamOut* __restrict__ so, const u64* __restrict__ ncol, u64* __restrict__ syms) {
+    const int st = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
+    if (st >= ns) return;
+    const StreamDesc d = sd[st];
+    const int bi = st % nb, pi = st / nb;
+    const u64 base = static_cast<u64>(pi) * nsc_all + scoff[bi];
+    long long prev = -1;
+    for (u64 j = 0; j < scoff[bi + 1] - scoff[bi]; ++j) {
+        const long long f = fx[2 * (base + j)], l = fx[2 * (base + j) + 1];
+        if (f >= 0) {
+            syms[d.sym_off + tab[base + j].ones_b] = static_cast<u64>(f - prev - 1);
+            prev = l;
+        }
+    }
+    const u64 nsy = so[st].nsyms;
+    if (nsy > 0) syms[d.sym_off + nsy - 1] = static_cast<u64>(static_cast<long long>(ncol[st]) - 1 - prev);
+}
+
 struct AcDesc {
     u64 sym_off;     // symbols
     u64 out_off;     // output byte offset (capacity 5 + 7*nsyms + 16)
@@ -1036,8 +1190,13 @@ void decode_model(const u64* m, u64 n, u64 block, int last_plane, const u64* sto
     ProfScope prof_scope(kStats, s);
     const u64 nb = (n + block - 1) / block;
     if (nb == 0) return;
-    decode_model_kernel<<<static_cast<unsigned>(nb), kDecThreads, 0, s>>>(m, n, block, last_plane, stops_dev, dec);
-    count_launch();
+    const u64 spb = (block + kDmSc - 1) / kDmSc;  // sub-chunks per block
+    DevBuf<unsigned long long> cnt(2 * nb * spb, s);
+    const unsigned grid = static_cast<unsigned>(nb * spb);
+    dm_count_kernel<<<grid, kDecThreads, 0, s>>>(m, n, block, spb, last_plane, cnt.p);
+    dm_scan_kernel<<<cdiv(nb, 64), 64, 0, s>>>(cnt.p, nb, spb);
+    dm_decode_kernel<<<grid, kDecThreads, 0, s>>>(m, n, block, spb, last_plane, stops_dev, cnt.p, dec);
+    count_launch(3);
     TCB_LAUNCH();
 }
 
@@ -1086,6 +1245,7 @@ std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cu
 // entropy output sized exactly from the blocks' msb histogram (a breakpoint
 // plane with stops is bounded by its full-plane sizes).
 struct Layout {
+    u64 nb = 0;  // blocks in the layout's range
     std::vector<StreamDesc> sd;
     std::vector<AcDesc> ad;
     std::vector<AcJob> jobs;
@@ -1100,6 +1260,7 @@ Layout make_layout(const std::vector<u64>& hist, u64 n, u64 block, int last_plan
     const u64 nb = b1 > b0 ? b1 - b0 : 0;
     const int np = top_plane - last_plane + 1;
     const u64 ns = nb * static_cast<u64>(np);
+    L.nb = nb;
     L.sd.resize(ns);
     L.ad.resize(ns);
     L.jobs.resize(ns);
@@ -1161,10 +1322,26 @@ void code_streams(Coded& c, const Layout& L, const u64* m, const u8* neg, int co
     c.so = DevBuf<StreamOut>(ns, s);
     {
         ProfScope pe(kEmit, s);
-        emit_kernel<<<static_cast<unsigned>(ns), kEmT, 0, s>>>(m, neg, c.dsd.p, c.syms.p, c.raw.p, c.so.p);
+        // blocks of the layout (plane-major: the first nb streams are the top plane's blocks)
+        const int nb = static_cast<int>(L.nb), np = static_cast<int>(ns / std::max<u64>(L.nb, 1));
+        std::vector<u64> scoff(nb + 1, 0);
+        for (int b = 0; b < nb; ++b) scoff[b + 1] = scoff[b] + (L.sd[b].hi - L.sd[b].lo + kSc - 1) / kSc;
+        const u64 nsc = scoff[nb];
+        DevBuf<u64> dsc(nb + 1, s), ncol(ns, s);
+        dsc.upload(scoff.data(), nb + 1);
+        DevBuf<u32> hist(nsc * 65 + 1, s);
+        DevBuf<ScOff> tab(nsc * np + 1, s);
+        DevBuf<long long> fx(2 * nsc * np + 2, s);
+        sc_hist_kernel<<<static_cast<unsigned>(nsc), kScT, 0, s>>>(m, c.dsd.p, dsc.p, nb, hist.p);
+        sc_scan_kernel<<<cdiv(ns, 64), 64, 0, s>>>(m, c.dsd.p, static_cast<int>(ns), nb, dsc.p, nsc, hist.p, tab.p,
+                                                  c.so.p, ncol.p);
+        sc_emit_kernel<<<static_cast<unsigned>(nsc), kScT, 0, s>>>(m, neg, c.dsd.p, np, nb, dsc.p, nsc, tab.p,
+                                                                   c.syms.p, c.raw.p, fx.p);
+        sc_fix_kernel<<<cdiv(ns, 64), 64, 0, s>>>(c.dsd.p, static_cast<int>(ns), nb, dsc.p, nsc, tab.p, fx.p, c.so.p,
+                                                 ncol.p, c.syms.p);
+        count_launch(4);
+        TCB_LAUNCH();
     }
-    count_launch();
-    TCB_LAUNCH();
     c.dad = DevBuf<AcDesc>(ns, s);
     c.dad.upload(L.ad.data(), ns);
     c.ent = DevBuf<u8>(L.out_total + 1, s);

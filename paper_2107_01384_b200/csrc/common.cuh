@@ -15,6 +15,7 @@
 namespace tcb {
 
 using u8 = std::uint8_t;
+using u16 = std::uint16_t;
 using u32 = std::uint32_t;
 using u64 = std::uint64_t;
 using i64 = std::int64_t;

@@ -118,28 +118,32 @@ __global__ void __launch_bounds__(kSnThreads) slice_norm_cta_kernel(const u64* _
     if (threadIdx.x == 0) out[t] = __dsqrt_rn(__dmul_rn(s, down));
 }
 
+// I = u32 when the core has fewer than 2^32 coefficients (32-bit index division)
+template <class I>
 __global__ void dead_kernel(const u64* __restrict__ dec, u64 n, const u64* __restrict__ meta /* shape, stride, off */,
                             int d, u8* __restrict__ dead, const u64* __restrict__ order) {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 v = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
         if (dec[v] == 0) continue;
-        const u64 pos = order ? order[v] : v;
+        const I pos = static_cast<I>(order ? order[v] : v);
         for (int a = 0; a < d; ++a) {
-            const u64 idx = (pos / meta[d + a]) % meta[a];
-            dead[meta[2 * d + a] + idx] = 0;
+            const I idx = (pos / static_cast<I>(meta[d + a])) % static_cast<I>(meta[a]);
+            u8* q = dead + meta[2 * d + a] + idx;
+            if (*q) *q = 0;  // most slices are live: read before write
         }
     }
 }
 
+template <class I>
 __global__ void signfold_kernel(u8* __restrict__ neg, u64 n, const u64* __restrict__ meta, int d,
                                 const signed char* __restrict__ flips /* concatenated per storage axis */,
                                 const u64* __restrict__ order) {
     const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
     for (u64 v = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-        const u64 pos = order ? order[v] : v;
+        const I pos = static_cast<I>(order ? order[v] : v);
         u8 par = 0;
         for (int a = 0; a < d; ++a) {
-            const u64 idx = (pos / meta[d + a]) % meta[a];
+            const I idx = (pos / static_cast<I>(meta[d + a])) % static_cast<I>(meta[a]);
             par ^= flips[meta[2 * d + a] + idx] < 0 ? 1 : 0;
         }
         neg[v] ^= par;
@@ -319,7 +323,12 @@ std::vector<u8> dead_slices(const u64* dec, const std::vector<u64>& shape, cudaS
     dm.upload(meta.data(), meta.size());
     DevBuf<u8> dead(total, s);
     TCB_CUDA(cudaMemsetAsync(dead.p, 1, total, s));
-    dead_kernel<<<grid_for(n, 256, 4, 4), 256, 0, s>>>(dec, n, dm.p, static_cast<int>(shape.size()), dead.p, order);
+    if (n < (u64{1} << 32))
+        dead_kernel<u32><<<grid_for(n, 256, 4, 4), 256, 0, s>>>(dec, n, dm.p, static_cast<int>(shape.size()), dead.p,
+                                                                 order);
+    else
+        dead_kernel<u64><<<grid_for(n, 256, 4, 4), 256, 0, s>>>(dec, n, dm.p, static_cast<int>(shape.size()), dead.p,
+                                                                 order);
     count_launch();
     TCB_LAUNCH();
     return dead.to_host();
@@ -335,7 +344,12 @@ void sign_fold(u8* neg, const std::vector<u64>& shape, const std::vector<signed 
     dm.upload(meta.data(), meta.size());
     DevBuf<signed char> fl(flips_by_axis.size(), s);
     fl.upload(flips_by_axis.data(), flips_by_axis.size());
-    signfold_kernel<<<grid_for(n, 256, 4, 4), 256, 0, s>>>(neg, n, dm.p, static_cast<int>(shape.size()), fl.p, order);
+    if (n < (u64{1} << 32))
+        signfold_kernel<u32><<<grid_for(n, 256, 4, 4), 256, 0, s>>>(neg, n, dm.p, static_cast<int>(shape.size()), fl.p,
+                                                                     order);
+    else
+        signfold_kernel<u64><<<grid_for(n, 256, 4, 4), 256, 0, s>>>(neg, n, dm.p, static_cast<int>(shape.size()), fl.p,
+                                                                     order);
     count_launch();
     TCB_LAUNCH();
 }
