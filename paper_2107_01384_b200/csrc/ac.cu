@@ -75,8 +75,9 @@ __device__ __forceinline__ u32 block_excl_scan(u32 v, u32* red, u32& total) {
 constexpr int kIxT = 1024;  // index / epoch passes
 constexpr u32 kIxSmemEntries = 4096;
 
-// u32 words of the index pass's tables: hkey (2H) | hpos (H) | hval (H) | list (2 cap)
-__host__ __device__ inline u64 index_words(u32 cap, u32 hbits) { return 4ull * (1ull << hbits) + 2ull * cap; }
+// u32 words of the index pass's tables: hkey (2H) | hpos (H) | hval (H) | list (2 cap u64:
+// the bitonic sort pads the distinct values to a power of two)
+__host__ __device__ inline u64 index_words(u32 cap, u32 hbits) { return 4ull * (1ull << hbits) + 4ull * cap; }
 
 __global__ void __launch_bounds__(kIxT) ac_index_kernel(const u64* __restrict__ syms, const u64* __restrict__ counts,
                                                         int stride, const JobDev* __restrict__ jobs, int njobs,
@@ -126,12 +127,12 @@ __global__ void __launch_bounds__(kIxT) ac_index_kernel(const u64* __restrict__ 
     // the distinct values (position, slot), then sorted by position
     for (u32 i = threadIdx.x; i < H; i += kIxT)
         if (hkey[i] != kEmpty) {
-            const u32 at = atomicAdd(&nd_s, 1u);
-            if (at < jb.cap) list[at] = (static_cast<u64>(hpos[i]) << 32) | i;
+            const u32 at = atomicAdd(&nd_s, 1u);  // index 0 is the escape: at most cap - 1 values
+            if (at + 1 < jb.cap) list[at] = (static_cast<u64>(hpos[i]) << 32) | i;
             else *err = 1;
         }
     __syncthreads();
-    const u32 D = min(nd_s, jb.cap);
+    const u32 D = min(nd_s, jb.cap - 1);
     u32 P2 = 1;
     while (P2 < D) P2 <<= 1;
     for (u32 i = D + threadIdx.x; i < P2; i += kIxT) list[i] = ~u64{0};  // list holds 2 cap >= P2 entries
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kMT) ac_code_kernel(const u64* __restrict__ co
             }
             const u32 T = T0 + 32u * static_cast<u32>(kk - k0);
             u64 rec;
-            if (fpj[I - 1] == static_cast<u32>(kk)) {
+            if (I == 0 || fpj[I - 1] == static_cast<u32>(kk)) {  // (I == 0 only after a capacity error)
                 rec = (u64{1} << 32) | (u64{1} << 16) | T;  // escape: cum 0, freq 1
             } else {
                 const u32 cum = pre[I] + 32u * less;
@@ -642,7 +643,7 @@ void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector
         JobDev& d = jd[j];
         d.sym_off = a.sym_off;
         d.out_off = a.out_off;
-        const u64 esc = ac_escape_bound(a.sym_cap, a.positions);
+        const u64 esc = a.distinct ? std::min(a.sym_cap, a.distinct) : ac_escape_bound(a.sym_cap, a.positions);
         d.cap = static_cast<u32>(esc + 1);
         d.hbits = hash_bits(d.cap);
         cap_max = std::max(cap_max, d.cap);
@@ -668,7 +669,7 @@ void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector
             gtot += (index_words(d.cap, d.hbits) + 3) & ~u64{3};
         }
     }
-    if (cap_max > 40000) throw Error("entropy: too many distinct run lengths for the device model");
+    if (cap_max > 24000) throw Error("entropy: more than 24000 distinct symbols in one stream");
     DevBuf<JobDev> djobs(nj, s);
     djobs.upload(jd.data(), nj);
     DevBuf<u64> recs(rec_ext + 1, s), W(wtot + 1, s), nout(nj, s), dch(nj + 1, s), dep(nj + 1, s);

@@ -28,6 +28,7 @@ struct AcJob {
     u64 out_off;    // output position in `ent` (capacity ac_out_cap)
     u64 sym_cap;    // symbol-count bound (the actual count is read on the device)
     u64 positions;  // column length (bounds the number of distinct run lengths)
+    u64 distinct = 0;  // a tighter bound on the distinct symbols when known (0: from positions)
 };
 
 // distinct run lengths of a column with `positions` bits: d(d-1)/2 <= zeros

@@ -1230,10 +1230,13 @@ std::vector<u8> encode_symbols_device(int coder, const u64* syms_host, u64 n, cu
     const u64 cnt[2] = {n, 0};
     DevBuf<u64> dc(2, s);
     dc.upload(cnt, 2);
+    std::vector<u64> uniq(syms_host, syms_host + n);
+    std::sort(uniq.begin(), uniq.end());
+    const u64 distinct = static_cast<u64>(std::unique(uniq.begin(), uniq.end()) - uniq.begin());
     const u64 cap = ac_out_cap(n, ~u64{0} >> 2);
     DevBuf<u8> ent(cap, s);
     DevBuf<u64> elen(1, s);
-    ac_encode(syms.p, dc.p, 2, {AcJob{0, 0, n, ~u64{0} >> 2}}, ent.p, elen.p, s);
+    ac_encode(syms.p, dc.p, 2, {AcJob{0, 0, n, ~u64{0} >> 2, distinct}}, ent.p, elen.p, s);
     const u64 el = elen.to_host()[0];
     out.resize(el);
     ent.download(out.data(), el);

@@ -511,7 +511,9 @@ Tucker sthosvd_device(DevBuf<double>&& owned, const double* ext, const std::vect
         f.factors[p[step]] = std::move(so.U);
         f.r[p[step]] = so.r;
         if (so.tie) f.tie_modes |= 1u << p[step];
-        if (on_factor) on_factor(p[step], f.factors[p[step]].p, rows, so.r);
+        // the factor's rows: the whole mode (the sharded last step ran on the gathered tensor)
+        const u64 frows = sharded && step == d - 1 ? shape[p[d - 1]] : rows;
+        if (on_factor) on_factor(p[step], f.factors[p[step]].p, frows, so.r);
         cur.erase(cur.begin());
         cur.push_back(so.r);
     }
