@@ -600,6 +600,62 @@ const u64* magic_table(cudaStream_t s) {
 }
 
 u32 hash_bits(u32 cap);
+// Code length bounds without the sequential range pass: the coder shifts out
+// S bytes with 24 <= log2(range_end) = log2(range_0) - C - E + 8 S < 32, where
+// C = sum log2(T / f) over the symbols (+ 1 per raw escape bit) and E = the
+// floor(range / T) truncation losses, each in [0, log2(1 / (1 - T / range)))
+// with range >= 2^24, T < 2^16.  Output bytes = 5 (framing) + S + 5 (flush).
+__global__ void __launch_bounds__(256) ac_bounds_kernel(const u64* __restrict__ counts, int stride,
+                                                        const JobDev* __restrict__ jobs, int njobs,
+                                                        const u64* __restrict__ recs, u64* __restrict__ lo_hi) {
+    __shared__ double red[2][8];
+    const int j = blockIdx.x;
+    if (j >= njobs) return;
+    const JobDev jb = jobs[j];
+    const u64 ns = counts[static_cast<u64>(j) * stride];
+    double c = 0.0, e = 0.0;
+    const u64* rc = recs + jb.sym_off;
+    for (u64 k = threadIdx.x; k < ns; k += blockDim.x) {
+        if (k == 0) {  // the first symbol (escape against total 1): 32 raw bits, log2(1) = 0
+            c += 32.0;
+            e += 32.0 * 1.8e-7;
+            continue;
+        }
+        const u64 r = rc[k];
+        const double T = static_cast<double>(r & 0xFFFFu), f = static_cast<double>((r >> 32) & 0xFFFFu);
+        c += log2(T) - log2(f);
+        e += 0.005646;  // log2(1 / (1 - 2^-8)) rounded up
+        if ((r >> 16) & 1u) {
+            c += 32.0;
+            e += 32.0 * 1.8e-7;  // a raw bit: floor(range / 2), range >= 2^24
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = c;
+        red[1][threadIdx.x >> 5] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double C = 0.0, E = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            C += red[0][w];
+            E += red[1][w];
+        }
+        if (ns == 0) {
+            lo_hi[2 * j] = lo_hi[2 * j + 1] = 0;
+            return;
+        }
+        const double slack = 1e-9 * C + 1e-6;  // rounding of the log sums
+        const double smin = ceil((C - slack - 8.0) / 8.0), smax = floor((C + E + slack + 1e-8) / 8.0);
+        lo_hi[2 * j] = 10 + static_cast<u64>(max(smin, 0.0));
+        lo_hi[2 * j + 1] = 10 + static_cast<u64>(max(smax, 0.0));
+    }
+}
+
 // the largest index-pass tables, opted in once per device (concurrent callers
 // on worker threads launch with different sizes below it)
 void model_smem_attr() {
@@ -629,11 +685,12 @@ u64 ac_out_cap(u64 sym_cap, u64 positions) {
     return 5 + 2 * sym_cap + 5 * ac_escape_bound(sym_cap, positions) + 8;
 }
 
-void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs, u8* ent, u64* elen,
-               cudaStream_t s) {
+namespace {
+void ac_run(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs, u8* ent, u64* elen,
+            u64* bounds, cudaStream_t s) {
     const int nj = static_cast<int>(jobs.size());
     if (nj == 0) return;
-    TCB_CUDA(cudaMemsetAsync(elen, 0, nj * sizeof(u64), s));
+    if (elen) TCB_CUDA(cudaMemsetAsync(elen, 0, nj * sizeof(u64), s));
     std::vector<JobDev> jd(nj);
     std::vector<u64> choff(nj + 1, 0), epslot(nj + 1, 0);
     u64 wtot = 0, gtot = 0, rec_ext = 0, fptot = 0, eptot = 0, sntot = 0;
@@ -708,6 +765,16 @@ void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector
             counts, stride, djobs.p, nj, dep.p, idx.p, fp.p, ndist.p, eprec.p, snap.p, nep.p, recs.p);
         count_launch(2);
         TCB_LAUNCH();
+        if (bounds) {  // code-length bounds only: no range recurrence, no bytes
+            ac_bounds_kernel<<<static_cast<unsigned>(nj), 256, 0, s>>>(counts, stride, djobs.p, nj, recs.p, bounds);
+            count_launch();
+            TCB_LAUNCH();
+            int herr = 0;
+            d2h(&herr, err.p, sizeof(int), s);
+            stream_sync(s);
+            if (herr) throw Error("entropy: device model capacity exceeded");
+            return;
+        }
         ac_range_kernel<<<cdiv(static_cast<u64>(nj) * 32, 128), 128, 0, s>>>(syms, counts, stride, djobs.p, nj, recs.p,
                                                                              magic, W.p, nout.p);
         count_launch();
@@ -728,6 +795,24 @@ void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector
     d2h(&herr, err.p, sizeof(int), s);
     stream_sync(s);
     if (herr) throw Error("entropy: device model capacity exceeded");
+}
+}  // namespace
+
+void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs, u8* ent, u64* elen,
+               cudaStream_t s) {
+    ac_run(syms, counts, stride, jobs, ent, elen, nullptr, s);
+}
+
+std::vector<u64> ac_size_bounds(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs,
+                                cudaStream_t s) {
+    const std::size_t nj = jobs.size();
+    std::vector<u64> out(2 * nj, 0);
+    if (nj == 0) return out;
+    DevBuf<u64> d(2 * nj, s);
+    ac_run(syms, counts, stride, jobs, nullptr, nullptr, d.p, s);
+    d.download(out.data(), 2 * nj);
+    stream_sync(s);
+    return out;
 }
 
 }  // namespace tcb

@@ -41,4 +41,9 @@ u64 ac_out_cap(u64 sym_cap, u64 positions);
 void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs, u8* ent, u64* elen,
                cudaStream_t s);
 
+// Bounds [lo, hi] (out[2 j], out[2 j + 1]) on each stream's encode_symbols size from
+// the adaptive model alone (no range recurrence); lo == hi == 0 for no symbols.
+std::vector<u64> ac_size_bounds(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs,
+                                cudaStream_t s);
+
 }  // namespace tcb

@@ -1315,7 +1315,8 @@ struct Coded {
     DevBuf<u32> scratch;
 };
 
-void code_streams(Coded& c, const Layout& L, const u64* m, const u8* neg, int coder, cudaStream_t s) {
+// symbols and raw bits of every stream of the layout (no entropy coding)
+void emit_streams(Coded& c, const Layout& L, const u64* m, const u8* neg, cudaStream_t s) {
     const u64 ns = L.sd.size();
     c.dsd = DevBuf<StreamDesc>(ns, s);
     c.dsd.upload(L.sd.data(), ns);
@@ -1345,6 +1346,11 @@ void code_streams(Coded& c, const Layout& L, const u64* m, const u8* neg, int co
         count_launch(4);
         TCB_LAUNCH();
     }
+}
+
+void code_streams(Coded& c, const Layout& L, const u64* m, const u8* neg, int coder, cudaStream_t s) {
+    const u64 ns = L.sd.size();
+    emit_streams(c, L, m, neg, s);
     c.dad = DevBuf<AcDesc>(ns, s);
     c.dad.upload(L.ad.data(), ns);
     c.ent = DevBuf<u8>(L.out_total + 1, s);
@@ -1492,6 +1498,19 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
     stream_sync(s);
     res.entropy_bytes = std::move(d.entropy_bytes);
     return res;
+}
+
+
+std::vector<u64> entropy_size_bounds(const u64* m, u64 n, u64 block, int plane, cudaStream_t s, BlockRange br) {
+    const u64 nball = n == 0 ? 0 : (n + block - 1) / block;
+    const u64 b0 = std::min(br.b0, nball), b1 = std::min(br.b1, nball);
+    if (b1 <= b0) return {};
+    HostTrace ht("emit: entropy size bounds");
+    const auto hist = msb_histogram(m, n, block, s);
+    const Layout L = make_layout(hist, n, block, plane, plane, nullptr, 0, br);
+    Coded c;
+    emit_streams(c, L, m, nullptr, s);
+    return ac_size_bounds(c.syms.p, reinterpret_cast<const u64*>(c.so.p), 2, L.jobs, s);
 }
 
 }  // namespace tcb

@@ -80,6 +80,11 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
                        const u64* stops_host /*2*nb, for last_plane*/, int coder, bool want_body,
                        cudaStream_t s, BlockRange br = {});
 
+// Arithmetic-coder size bounds [lo, hi] of plane `plane`'s full streams (blocks of
+// the range; out[2 i], out[2 i + 1]) from the adaptive model alone: enough to
+// decide the split-plane priority without the sequential range pass, usually.
+std::vector<u64> entropy_size_bounds(const u64* m, u64 n, u64 block, int plane, cudaStream_t s, BlockRange br = {});
+
 // Speculative split-plane probe: the entropy-coded size of every full plane
 // stream (planes 63..0, no stops, signs not needed) launched on a side stream
 // as soon as the magnitudes exist, so the planner's probe of plane p+1

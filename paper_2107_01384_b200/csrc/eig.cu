@@ -431,21 +431,22 @@ __global__ void __launch_bounds__(kCoopThreads, 1) tridiag_coop(double* __restri
             }
             __syncthreads();
         }
+        // one reduction: the tail |x_1..|^2 gives both alpha and |v|^2
         double ss = 0.0;
         for (int i = threadIdx.x; i < m; i += blockDim.x) {
             const double x = __ldcg(A + static_cast<size_t>(k) * n + k + 1 + i);
             v[i] = x;
-            ss += x * x;
+            if (i > 0) ss += x * x;
         }
-        const double alpha = sqrt(block_sum(ss, red));
+        const double tail = block_sum(ss, red);
         const double x0 = v[0];
+        const double alpha = sqrt(x0 * x0 + tail);
         const double beta = x0 >= 0.0 ? -alpha : alpha;
+        const double v0 = x0 - beta;
+        const double vv = v0 * v0 + tail;
         __syncthreads();
-        if (threadIdx.x == 0) v[0] = x0 - beta;
+        if (threadIdx.x == 0) v[0] = v0;
         __syncthreads();
-        double vv = 0.0;
-        for (int i = threadIdx.x; i < m; i += blockDim.x) vv += v[i] * v[i];
-        vv = block_sum(vv, red);
         const double t = (alpha == 0.0 || vv == 0.0) ? 0.0 : 2.0 / vv;
         if (cta == 0) {
             if (threadIdx.x == 0) {
@@ -460,14 +461,24 @@ __global__ void __launch_bounds__(kCoopThreads, 1) tridiag_coop(double* __restri
             const int r = cta + G * q;
             if (r >= n) break;
             if (r <= k) continue;
-            double* row = A + static_cast<size_t>(r) * n + k + 1;
+            double* __restrict__ row = A + static_cast<size_t>(r) * n + k + 1;
             double s = 0.0;
             if (pend) {
                 const double vr = vp[r - k], wr = wp[r - k];
-                for (int j = lane; j < m; j += 32) {
-                    const double a = __ldcg(row + j) - (vr * wp[j + 1] + wr * vp[j + 1]);
-                    row[j] = a;
-                    s += a * v[j];
+                // 4 columns per lane in flight: every load is issued before the stores
+                for (int j0 = lane; j0 < m; j0 += 128) {
+                    double a[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) a[u] = j0 + 32 * u < m ? __ldcg(row + j0 + 32 * u) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int j = j0 + 32 * u;
+                        if (j < m) {
+                            a[u] -= vr * wp[j + 1] + wr * vp[j + 1];
+                            row[j] = a[u];
+                            s += a[u] * v[j];
+                        }
+                    }
                 }
             } else {
                 for (int j = lane; j < m; j += 32) s += __ldcg(row + j) * v[j];

@@ -142,16 +142,17 @@ struct Planner {
         return x;
     }
 
-    void place_stops(int p, double need, const Tot& tot, const PlaneStats& per, const Tot* prev, u64 prev_ebits,
+    // the split-plane priority (core_codec.cpp:257-266) for a given entropy size of the previous plane
+    static bool lead_first_for(const Tot& prev, u64 prev_ebits) {
+        const double lead_cost = static_cast<double>(prev_ebits + prev.nones);
+        const double trail_cost = static_cast<double>(prev.ntrail);
+        const double eff_lead = lead_cost > 0 ? prev.lead / lead_cost : (prev.lead > 0 ? HUGE_VAL : 0.0);
+        const double eff_trail = trail_cost > 0 ? prev.trail / trail_cost : (prev.trail > 0 ? HUGE_VAL : 0.0);
+        return eff_lead >= eff_trail;
+    }
+
+    void place_stops(int p, double need, const Tot& tot, const PlaneStats& per, bool lead_first,
                      std::vector<u64>& stp) {
-        bool lead_first = true;
-        if (o.split && prev) {
-            const double lead_cost = static_cast<double>(prev_ebits + prev->nones);
-            const double trail_cost = static_cast<double>(prev->ntrail);
-            const double eff_lead = lead_cost > 0 ? prev->lead / lead_cost : (prev->lead > 0 ? HUGE_VAL : 0.0);
-            const double eff_trail = trail_cost > 0 ? prev->trail / trail_cost : (prev->trail > 0 ? HUGE_VAL : 0.0);
-            lead_first = eff_lead >= eff_trail;
-        }
         if (!o.split) {
             double cum = 0;
             u64 b = 0;
@@ -232,29 +233,54 @@ struct Planner {
             ++pr.nplanes;
             if (tracked - red <= target) {
                 if (o.on_last_plane) o.on_last_plane(p);
-                u64 ebits = 0;
+                bool lead_first = true;
                 if (o.split && have_prev) {
                     HostTrace ht("plan: split probe emit");
+                    const bool shd = o.shard && o.shard->world > 1;
+                    const BlockRange br = shd ? rank_blocks(nb, o.shard->world, o.shard->rank) : BlockRange{0, nb};
+                    // the ranks' sums of (lo, hi) or of exact sizes
+                    auto all_sum = [&](std::vector<u64> v) {
+                        if (!shd) return v;
+                        const std::vector<u8> blob(reinterpret_cast<const u8*>(v.data()),
+                                                   reinterpret_cast<const u8*>(v.data() + v.size()));
+                        std::vector<u64> tot(v.size(), 0);
+                        for (const auto& bl : o.shard->allgather_blobs(blob, s))
+                            for (std::size_t i = 0; i < tot.size() && (i + 1) * sizeof(u64) <= bl.size(); ++i) {
+                                u64 x;
+                                std::memcpy(&x, bl.data() + i * sizeof(u64), sizeof(u64));
+                                tot[i] += x;
+                            }
+                        return tot;
+                    };
+                    bool decided = false;
                     if (o.probe) {
+                        u64 ebits = 0;
                         for (u64 e : probe_entropy_bytes(*o.probe, p + 1)) ebits += e * 8;
-                    } else if (o.shard && o.shard->world > 1) {  // own blocks, then the ranks' sums
-                        const BlockRange br = rank_blocks(nb, o.shard->world, o.shard->rank);
+                        lead_first = lead_first_for(prev, ebits);
+                        decided = true;
+                    } else if (o.coder == 0) {
+                        // the coder's size bounds from the model alone usually decide it
+                        const auto b = entropy_size_bounds(m, n, block, p + 1, s, br);
+                        std::vector<u64> lh{0, 0};
+                        for (std::size_t i = 0; i + 1 < b.size(); i += 2) {
+                            lh[0] += b[i] * 8;
+                            lh[1] += b[i + 1] * 8;
+                        }
+                        lh = all_sum(lh);
+                        const bool a = lead_first_for(prev, lh[0]), z = lead_first_for(prev, lh[1]);
+                        if (a == z) {
+                            lead_first = a;
+                            decided = true;
+                        }
+                    }
+                    if (!decided) {  // the exact sizes: the full coder over plane p + 1
                         const auto er = emit_planes(m, nullptr, n, block, p + 1, p + 1, nullptr, o.coder, false, s, br);
                         u64 mine = 0;
                         for (u64 e : er.entropy_bytes) mine += e * 8;
-                        const std::vector<u8> blob(reinterpret_cast<const u8*>(&mine),
-                                                   reinterpret_cast<const u8*>(&mine) + sizeof(mine));
-                        for (const auto& bl : o.shard->allgather_blobs(blob, s)) {
-                            u64 v = 0;
-                            std::memcpy(&v, bl.data(), sizeof(v));
-                            ebits += v;
-                        }
-                    } else {
-                        const auto er = emit_planes(m, nullptr, n, block, p + 1, p + 1, nullptr, o.coder, false, s);
-                        for (u64 e : er.entropy_bytes) ebits += e * 8;
+                        lead_first = lead_first_for(prev, all_sum({mine})[0]);
                     }
                 }
-                place_stops(p, tracked - target, tot, per, have_prev ? &prev : nullptr, ebits, pr.stops);
+                place_stops(p, tracked - target, tot, per, lead_first, pr.stops);
                 return finish(p);
             }
             tracked -= red;
