@@ -702,12 +702,40 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     std::vector<double> sn_flat;
     u64 sum_ext = 0;
     for (auto v : cs) sum_ext += v;
+    // the slice norms (serial per slice) feed only the factor weights: on a worker
+    // stream, overlapping the core plan, when the encode runs concurrently
+    const bool par_sn = d > 1 && !prof_enabled();
+    std::shared_future<void> sn_ready;
     if (!zero) {
         quantize_f64(core_s.p, nc, k, mag.p, neg.p, s, vorder.p);
-        DevBuf<double> dsn(sum_ext, s);
-        slice_norms(mag.p, cs, std::ldexp(1.0, -2 * k), dsn.p, s, vorder.p);
-        sn_flat = dsn.to_host();
+        if (par_sn) {
+            const int dev = cur_device();
+            cudaStream_t side = Workers::get().stream(dev, static_cast<int>(d) + 1);
+            EventHandle q;
+            TCB_CUDA(cudaEventRecord(q.e, s));
+            TCB_CUDA(cudaStreamWaitEvent(side, q.e, 0));
+            const double scale = std::ldexp(1.0, -2 * k);
+            auto task = std::make_shared<std::packaged_task<void()>>([&, side, dev, scale, sum_ext] {
+                TCB_CUDA(cudaSetDevice(dev));
+                DevBuf<double> dsn(sum_ext, side);
+                slice_norms(mag.p, cs, scale, dsn.p, side, vorder.p);
+                sn_flat = dsn.to_host();
+            });
+            sn_ready = task->get_future().share();
+            Workers::get().submit([task] { (*task)(); });
+        } else {
+            DevBuf<double> dsn(sum_ext, s);
+            slice_norms(mag.p, cs, std::ldexp(1.0, -2 * k), dsn.p, s, vorder.p);
+            sn_flat = dsn.to_host();
+        }
     }
+    struct SnJoin {  // the slice-norm task reads mag / cs / vorder: join before they unwind
+        std::shared_future<void>& f;
+        ~SnJoin() {
+            if (f.valid()) f.wait();
+        }
+    } sn_join{sn_ready};
+    // core_s is read by nothing after the quantisation kernel (stream-ordered free)
     core_s.release();
     res.times.quantize = ms_since(t0);
     const u64 block = prm.block ? prm.block : default_block(zero ? 0 : nc);
@@ -746,13 +774,17 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     std::vector<u64> mode_of(d);
     for (std::size_t ax = 0; ax < d; ++ax) mode_of[ax] = f.order[storage[ax]];
     std::vector<std::vector<double>> sn_mode(d);
-    {
-        u64 o = 0;
-        for (std::size_t ax = 0; ax < d; ++ax) {
-            sn_mode[mode_of[ax]].assign(sn_flat.begin() + o, sn_flat.begin() + o + cs[ax]);
-            o += cs[ax];
-        }
-    }
+    std::once_flag sn_once;
+    auto need_sn = [&] {  // the slice norms by mode, once they exist
+        std::call_once(sn_once, [&] {
+            if (sn_ready.valid()) sn_ready.get();
+            u64 o = 0;
+            for (std::size_t ax = 0; ax < d; ++ax) {
+                sn_mode[mode_of[ax]].assign(sn_flat.begin() + o, sn_flat.begin() + o + cs[ax]);
+                o += cs[ax];
+            }
+        });
+    };
 
     // phases 3-4: the core plan on `s`; meanwhile every factor's orthonormality
     // check + reflectors run speculatively on a worker stream (assuming no dead
@@ -830,6 +862,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
                     FactorQuant spec;
                     bool have_spec = false;
                     if (!prep.err && !prep.live.empty()) {
+                        need_sn();
                         factor_quantize(spec, prep, f.n[i], sn_mode[i], prm.simple, si);
                         have_spec = true;
                         const int lp = lp_fut.get();
@@ -837,6 +870,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
                         factor_finalize(spec, prm.coder, si);
                     }
                     plan_fut.get();
+                    need_sn();
                     fe[i] = encode_factor_device(
                         f.factors[i].p, f.n[i], f.r[i], dead_mode[i], sn_mode[i], prm.coder, prm.simple, core_step,
                         cap, prm.f32, si,
@@ -910,6 +944,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
             }
         }
     } else {
+        need_sn();
         for (std::size_t i = 0; i < d; ++i)
             fe[i] = encode_factor_device(f.factors[i].p, f.n[i], f.r[i], dead_mode[i], sn_mode[i], prm.coder,
                                          prm.simple, core_step, cap, prm.f32, s,
@@ -926,12 +961,33 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     u64 count = 1;
     for (auto v : f.r) count *= v;
     StreamParts core_stream;
-    double ach;
+    double ach = 0.0;
     {
         HostTrace ht("encode: core finalize+sum");
+        // achieved_sse_int, accumulated backward (core_codec.cpp:405-411): needs only the
+        // magnitudes and the plan's decoded values, so it runs beside the finalisation
+        std::future<double> ach_fut;
+        if (par) {
+            const int dev = cur_device();
+            cudaStream_t side = Workers::get().stream(dev, static_cast<int>(d) + 2);
+            EventHandle q;
+            TCB_CUDA(cudaEventRecord(q.e, s));
+            TCB_CUDA(cudaStreamWaitEvent(side, q.e, 0));
+            auto task = std::make_shared<std::packaged_task<double()>>([&, side, dev] {
+                TCB_CUDA(cudaSetDevice(dev));
+                return exact_backward_sum(kExDiff, 0, mag.p, dec.p, nc, side);
+            });
+            ach_fut = task->get_future();
+            Workers::get().submit([task] { (*task)(); });
+        }
+        struct Join {
+            std::future<double>& f;
+            ~Join() {
+                if (f.valid()) f.wait();
+            }
+        } join_ach{ach_fut};
         core_stream = finalize_stream_parts(mag.p, neg.p, nc, plan, prm.coder, count, s, eo.shard);
-        // achieved_sse_int, accumulated backward (core_codec.cpp:405-411)
-        ach = exact_backward_sum(kExDiff, 0, mag.p, dec.p, nc, s);
+        ach = par ? ach_fut.get() : exact_backward_sum(kExDiff, 0, mag.p, dec.p, nc, s);
     }
     res.times.core += ms_since(t1);
     {
