@@ -109,7 +109,8 @@ def test_c5_against_oracle_fixture(gpu_pkg, re):
     y = out.view(torch.float32).view(x.shape).double()
     xd = x.double()
     e = float(torch.sqrt(((y - xd) ** 2).sum() / (xd * xd).sum()))
-    assert abs(e - case["re"]) <= 0.01 * case["re"], (e, case["re"])
+    ref_re = case.get("re", case["re_device_decoder"])  # the oracle decoder's RE when it finished
+    assert abs(e - ref_re) <= 0.01 * ref_re, (e, ref_re)
 
 
 # ---------------------------------------------------------------- the thin-SVD branch (rows > cols)

@@ -14,11 +14,17 @@ re = float(sys.argv[1]) if len(sys.argv) > 1 else 1e-2
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 x = synth.grf_torch(n=n, kmax=n // 3)
 assert x.dtype == torch.float32 and x.is_cuda
-for it in range(int(os.environ.get('C5_ITERS', '2'))):
+iters = int(os.environ.get('C5_ITERS', '2'))
+prof = os.environ.get('C5_PROFILE')  # ncu --profile-from-start off: only the last compress is captured
+for it in range(iters):
     torch.cuda.synchronize()
+    if prof and it == iters - 1:
+        torch.cuda.profiler.start()
     t0 = time.perf_counter()
     r = tcb.compress_device(x.data_ptr(), x.numel() * 4, tcb.Dtype.float32, list(x.shape), tcb.Params(target_re=re))
     torch.cuda.synchronize()
+    if prof and it == iters - 1:
+        torch.cuda.profiler.stop()
     dt = time.perf_counter() - t0
     print(f"c5 n={n} re={re:g}: {dt * 1e3:.1f} ms, ranks {r.ranks}, bytes {len(r.container)}, "
           f"factor {r.compression_factor():.1f}, times {r.times}", flush=True)
