@@ -131,6 +131,14 @@ inline int sm_count() {
     });
 }
 
+struct EventHandle {
+    cudaEvent_t e = nullptr;
+    EventHandle() { TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+    EventHandle(const EventHandle&) = delete;
+    EventHandle& operator=(const EventHandle&) = delete;
+    ~EventHandle() { cudaEventDestroy(e); }
+};
+
 inline unsigned cdiv(u64 a, u64 b) { return static_cast<unsigned>((a + b - 1) / b); }
 
 // Grid for a grid-stride pass over n elements: per_sm CTAs per SM for large n,

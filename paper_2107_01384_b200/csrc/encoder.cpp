@@ -48,6 +48,10 @@ struct Planner {
     cudaStream_t s;
     std::vector<PlaneStats> st = std::vector<PlaneStats>(64);
     std::vector<char> have = std::vector<char>(64, 0);
+    // the first plane batch, launched before the initial backward sum (which
+    // then runs on a side stream, its one-warp walk beside the batch's passes)
+    std::unique_ptr<PlaneStatsJob> pre;
+    int pre_p = -1;
 
     // Exact statistics from plane p down: 32 planes' approximate totals first,
     // the approximate `tracked` trajectory from the current (exact) value marks
@@ -59,7 +63,9 @@ struct Planner {
             HostTrace ht("plan: exact plane stats");
             const bool shd = o.shard && o.shard->world > 1;
             const BlockRange br = shd ? rank_blocks(nb, o.shard->world, o.shard->rank) : BlockRange{0, nb};
-            PlaneStatsJob job(m, n, block, p, np, s, br.b0, br.b1);
+            std::unique_ptr<PlaneStatsJob> own;
+            if (!(pre && pre_p == p)) own = std::make_unique<PlaneStatsJob>(m, n, block, p, np, s, br.b0, br.b1);
+            PlaneStatsJob& job = own ? *own : *pre;
             int need = np;
             if (n > (u64{1} << 20)) {
                 auto tot = job.approx_totals();
@@ -80,6 +86,7 @@ struct Planner {
                 }
             }
             std::vector<ExOut> out = job.exact(need);
+            if (!own) pre.reset();
             if (shd) {  // all-gather the ranks' blocks: out[k * nb + b] over every block
                 const u64 nk = static_cast<u64>(2 * need);
                 const std::vector<u8> mine(reinterpret_cast<const u8*>(out.data()),
@@ -213,7 +220,26 @@ struct Planner {
             for (auto& v : pr.stops) v = kFull;
             return finish(fp);
         }
-        double tracked = full_sum(kExSq, 0);  // backward_sum_sse (core_codec.cpp:183)
+        double tracked;
+        if (n > (u64{1} << 20)) {
+            const bool shd = o.shard && o.shard->world > 1;
+            const BlockRange br = shd ? rank_blocks(nb, o.shard->world, o.shard->rank) : BlockRange{0, nb};
+            pre = std::make_unique<PlaneStatsJob>(m, n, block, 63, 32, s, br.b0, br.b1);
+            pre_p = 63;
+            static PerDevice<cudaStream_t> side_streams;
+            cudaStream_t side = side_streams.get([] {
+                cudaStream_t x;
+                TCB_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+                return x;
+            });
+            EventHandle q;
+            TCB_CUDA(cudaEventRecord(q.e, s));
+            TCB_CUDA(cudaStreamWaitEvent(side, q.e, 0));
+            HostTrace ht("plan: exact initial sum");
+            tracked = serial_sums(m, nullptr, {ExSeg{0, n, 1, 0.0, HUGE_VAL}}, {{kExSq, 0}}, side)[0].sum;
+        } else {
+            tracked = full_sum(kExSq, 0);  // backward_sum_sse (core_codec.cpp:183)
+        }
         double ref = tracked;
         u64 terms = 0;
         if (tracked <= target) return finish(63);  // nothing worth encoding
@@ -233,6 +259,7 @@ struct Planner {
             ++pr.nplanes;
             if (tracked - red <= target) {
                 if (o.on_last_plane) o.on_last_plane(p);
+                if (o.on_breakpoint) o.on_breakpoint(p);
                 bool lead_first = true;
                 if (o.split && have_prev) {
                     HostTrace ht("plan: split probe emit");
@@ -326,7 +353,8 @@ __global__ void gather_segments_kernel(const u8* __restrict__ src, u8* __restric
 }  // namespace
 
 StreamParts finalize_stream_parts(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,
-                                  cudaStream_t s, const ShardComm* shard) {
+                                  cudaStream_t s, const ShardComm* shard,
+                                  const std::function<EmitDev*()>& upper) {
     const u64 nb = n == 0 ? 0 : (n + pl.block - 1) / pl.block;
     StreamParts out;
     std::vector<u8>& o = out.head;
@@ -341,6 +369,23 @@ StreamParts finalize_stream_parts(const u64* m, const u8* neg, u64 n, const Plan
     put_le(o, static_cast<u64>(pl.nplanes), 4);
     if (pl.nplanes <= 0 || nb == 0) return out;
     HostTrace ht("finalize: emit_planes");
+    if ((!shard || shard->world <= 1) && upper && pl.last_plane < 63) {
+        // the full planes were coded beside the plan: code the last plane, append it
+        EmitDev lo = emit_planes_device(m, neg, n, pl.block, pl.last_plane, pl.last_plane, pl.stops.data(), coder, s);
+        EmitDev own;
+        EmitDev* up = upper();
+        if (!up) {
+            own = emit_planes_device(m, neg, n, pl.block, pl.last_plane + 1, 63, nullptr, coder, s);
+            up = &own;
+        }
+        out.body_size = up->size + lo.size;
+        out.body = DevBuf<u8>(out.body_size + 1, s);
+        if (up->size) TCB_CUDA(cudaMemcpyAsync(out.body.p, up->body.p, up->size, cudaMemcpyDeviceToDevice, s));
+        if (lo.size)
+            TCB_CUDA(cudaMemcpyAsync(out.body.p + up->size, lo.body.p, lo.size, cudaMemcpyDeviceToDevice, s));
+        up->body.s = s;  // freed after the copy, in stream order
+        return out;
+    }
     if (!shard || shard->world <= 1) {
         EmitDev er = emit_planes_device(m, neg, n, pl.block, pl.last_plane, 63, pl.stops.data(), coder, s);
         out.body = std::move(er.body);

@@ -22,6 +22,9 @@ struct EncodeOpts {
     // work that depends only on it can start early; may be called again with
     // the same value by the exact-mode rerun
     std::function<void(int)> on_last_plane;
+    // called once when the breakpoint plane p is found, before the split probe:
+    // planes 63 .. p + 1 are full whatever the stops, so their coding can start
+    std::function<void(int)> on_breakpoint;
     // speculative full-plane entropy sizes for the split probe (optional)
     ProbeCache* probe = nullptr;
     // sharded encoding: this rank computes the statistics / crossing scans /
@@ -58,8 +61,12 @@ struct StreamParts {
     DevBuf<u8> body;
     u64 body_size = 0;
 };
+// `upper` (optional, unsharded): returns planes 63 .. last_plane + 1 already
+// emitted and coded with these signs (or nullptr); it is called after the last
+// plane has been coded, so whatever produces it overlaps that work.
 StreamParts finalize_stream_parts(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,
-                                  cudaStream_t s, const ShardComm* shard = nullptr);
+                                  cudaStream_t s, const ShardComm* shard = nullptr,
+                                  const std::function<EmitDev*()>& upper = {});
 // finalize(): emits planes [last_plane, 63] with the given signs and returns
 // the serialized stream section (container.cpp:231-247) for `count` elements.
 std::vector<u8> finalize_stream(const u64* m, const u8* neg, u64 n, const PlanResult& pl, int coder, u64 count,

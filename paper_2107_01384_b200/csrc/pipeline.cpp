@@ -102,11 +102,6 @@ struct JoinAll {
             if (x.valid()) x.wait();
     }
 };
-struct EventHandle {
-    cudaEvent_t e = nullptr;
-    EventHandle() { TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
-    ~EventHandle() { cudaEventDestroy(e); }
-};
 }  // namespace
 
 
@@ -819,7 +814,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     // plan kills no column of that mode, so the core need not wait for the worker
     std::vector<std::vector<signed char>> spec_flips(d);
     std::vector<std::promise<bool>> spec_ready(d);
-    std::vector<std::future<bool>> spec_fut;
+    std::vector<std::shared_future<bool>> spec_fut;
     JoinAll join{done};
     struct PlanGuard {  // a throwing plan must still release the workers
         std::promise<void>& p;
@@ -840,23 +835,20 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
         Workers& pool = Workers::get();
         for (std::size_t i = 0; i < d; ++i) {
             flips_fut.push_back(flips_ready[i].get_future());
-            spec_fut.push_back(spec_ready[i].get_future());
+            spec_fut.push_back(spec_ready[i].get_future().share());
             cudaStream_t si = pool.stream(dev, static_cast<int>(i));
             TCB_CUDA(cudaStreamWaitEvent(si, ready.e, 0));
             done.push_back(pool.submit([&, i, si, dev] {
-                bool sent = false;
+                bool sent = false, spec_sent = false;
                 try {
                     TCB_CUDA(cudaSetDevice(dev));
                     FactorPrep prep = preps && i < preps->size() && (*preps)[i].valid()
                                           ? (*preps)[i].get()  // made during the mode loop
                                           : factor_prepare(f.factors[i].p, f.n[i], f.r[i],
                                                            std::vector<u8>(f.r[i], 0), prm.f32, si);
-                    if (!prep.err && prep.live.size() == f.r[i]) {
-                        spec_flips[i] = prep.fl;
-                        spec_ready[i].set_value(true);
-                    } else {
-                        spec_ready[i].set_value(false);
-                    }
+                    if (!prep.err && prep.live.size() == f.r[i]) spec_flips[i] = prep.fl;
+                    spec_sent = true;
+                    spec_ready[i].set_value(!prep.err && prep.live.size() == f.r[i]);
                     // speculation "no dead columns": quantised stream now, plane search as
                     // soon as the core's last plane is certified
                     FactorQuant spec;
@@ -881,6 +873,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
                         },
                         &prep, have_spec ? &spec : nullptr);
                 } catch (...) {
+                    if (!spec_sent) spec_ready[i].set_value(false);
                     if (!sent) flips_ready[i].set_exception(std::current_exception());
                     throw;
                 }
@@ -903,6 +896,46 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
         eo.probe = probe.get();
     }
     ht_probe.stop();
+    // The full planes above the breakpoint do not depend on the stops, the probe
+    // or the dead slices: once the planner finds the breakpoint they are emitted
+    // and coded on a worker stream, with the signs folded by the speculative
+    // (every column live) flips.  Used when the final flips equal those.
+    struct Upper {
+        int p = -1;
+        std::future<EmitDev> fut;
+        ~Upper() {
+            if (fut.valid()) fut.wait();  // the task reads this frame's buffers
+        }
+    } upper;
+    if (par && !eo.shard && d + 3 <= 8 && !std::getenv("TCB_NO_EARLY_PLANES")) {
+        eo.on_breakpoint = [&](int p) {
+            if (p >= 63 || upper.fut.valid()) return;
+            const int dev = cur_device();
+            cudaStream_t side = Workers::get().stream(dev, static_cast<int>(d) + 3);
+            // the signs as they are now (the main stream folds them in place later)
+            auto negs = std::make_shared<DevBuf<u8>>(nc, s);
+            TCB_CUDA(cudaMemcpyAsync(negs->p, neg.p, nc, cudaMemcpyDeviceToDevice, s));
+            EventHandle q;
+            TCB_CUDA(cudaEventRecord(q.e, s));
+            TCB_CUDA(cudaStreamWaitEvent(side, q.e, 0));
+            upper.p = p;
+            auto task = std::make_shared<std::packaged_task<EmitDev()>>([&, side, dev, p, negs]() -> EmitDev {
+                TCB_CUDA(cudaSetDevice(dev));
+                std::vector<signed char> fl;
+                for (std::size_t i = 0; i < d; ++i)
+                    if (!spec_fut[i].get()) return EmitDev{};
+                for (std::size_t ax = 0; ax < d; ++ax)
+                    fl.insert(fl.end(), spec_flips[mode_of[ax]].begin(), spec_flips[mode_of[ax]].end());
+                negs->s = side;
+                sign_fold(negs->p, cs, fl, side, vorder.p);
+                EmitDev r = emit_planes_device(mag.p, negs->p, nc, block, p + 1, 63, nullptr, prm.coder, side);
+                stream_sync(side);
+                return r;
+            });
+            upper.fut = task->get_future();
+            Workers::get().submit([task] { (*task)(); });
+        };
+    }
     PlanResult plan;
     {
         HostTrace ht("encode: core plan");
@@ -986,7 +1019,17 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
                 if (f.valid()) f.wait();
             }
         } join_ach{ach_fut};
-        core_stream = finalize_stream_parts(mag.p, neg.p, nc, plan, prm.coder, count, s, eo.shard);
+        EmitDev up;
+        std::function<EmitDev*()> get_up;
+        if (upper.fut.valid())
+            get_up = [&]() -> EmitDev* {
+                HostTrace hu("encode: wait upper planes");
+                up = upper.fut.get();
+                bool ok = upper.p == plan.last_plane && up.body.p != nullptr;
+                for (std::size_t i = 0; ok && i < d; ++i) ok = flips_of_core[i] == spec_flips[i];
+                return ok ? &up : nullptr;
+            };
+        core_stream = finalize_stream_parts(mag.p, neg.p, nc, plan, prm.coder, count, s, eo.shard, get_up);
         ach = par ? ach_fut.get() : exact_backward_sum(kExDiff, 0, mag.p, dec.p, nc, s);
     }
     res.times.core += ms_since(t1);
