@@ -533,6 +533,150 @@ __global__ void __launch_bounds__(kCoopThreads, 1) tridiag_coop(double* __restri
     }
 }
 
+// The same algorithm with every CTA's rows resident in shared memory (Q rows of
+// n doubles per CTA: n <= ~1700 on 148 SMs): the per-step update + dot product
+// of a row is a pass over shared memory instead of an L2 round trip per 128
+// columns, so a step costs the pivot chain and one grid barrier.  The pivot
+// row is still published through global memory (with its flag); P through
+// global memory as before.  Row q of CTA c is matrix row c + G q; the warps
+// split each row into S column segments (Q S <= warps).
+__global__ void __launch_bounds__(kCoopThreads, 1) tridiag_coop_smem(double* __restrict__ A, int n,
+                                                                    double* __restrict__ d, double* __restrict__ e,
+                                                                    double* __restrict__ V, double* __restrict__ tau,
+                                                                    double* __restrict__ P, unsigned* __restrict__ ctr,
+                                                                    int* __restrict__ flags, int Q, int S) {
+    extern __shared__ double sh_coop[];
+    double* rows = sh_coop;
+    double* v = rows + static_cast<size_t>(Q) * n;
+    double* w = v + n;
+    double* vp = w + n;
+    double* wp = vp + n;
+    double* red = wp + n;
+    double* part = red + 32;
+    const int G = static_cast<int>(gridDim.x), cta = static_cast<int>(blockIdx.x);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int q = 0; q < Q; ++q) {
+        const int r = cta + G * q;
+        if (r >= n) break;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) rows[static_cast<size_t>(q) * n + j] = A[static_cast<size_t>(r) * n + j];
+    }
+    __syncthreads();
+    unsigned phase = 0;
+    bool pend = false;
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m = n - k - 1;
+        if (k > 0) {
+            if (threadIdx.x == 0) {
+                while (*reinterpret_cast<volatile int*>(flags + k) == 0) {
+                }
+                __threadfence();
+            }
+            __syncthreads();
+        }
+        double ss = 0.0;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const double x = __ldcg(A + static_cast<size_t>(k) * n + k + 1 + i);
+            v[i] = x;
+            if (i > 0) ss += x * x;
+        }
+        const double tail = block_sum(ss, red);
+        const double x0 = v[0];
+        const double alpha = sqrt(x0 * x0 + tail);
+        const double beta = x0 >= 0.0 ? -alpha : alpha;
+        const double v0 = x0 - beta;
+        const double vv = v0 * v0 + tail;
+        __syncthreads();
+        if (threadIdx.x == 0) v[0] = v0;
+        __syncthreads();
+        const double t = (alpha == 0.0 || vv == 0.0) ? 0.0 : 2.0 / vv;
+        if (cta == 0) {
+            if (threadIdx.x == 0) {
+                e[k] = t == 0.0 ? x0 : beta;
+                tau[k] = t;
+                d[k] = __ldcg(A + static_cast<size_t>(k) * n + k);
+            }
+            for (int i = threadIdx.x; i < m; i += blockDim.x) V[static_cast<size_t>(k) * n + k + 1 + i] = v[i];
+        }
+        // (row, segment) items: deferred update of step k-1 + partial dot with v
+        const int seg_len = ((m + S - 1) / S + 31) & ~31;
+        for (int it = warp; it < Q * S; it += nw) {
+            const int q = it / S, sg = it - q * S;
+            const int r = cta + G * q;
+            double s = 0.0;
+            if (r > k && r < n) {
+                double* __restrict__ row = rows + static_cast<size_t>(q) * n + k + 1;
+                const int j1 = min(m, (sg + 1) * seg_len);
+                if (pend) {
+                    const double vr = vp[r - k], wr = wp[r - k];
+                    for (int j = sg * seg_len + lane; j < j1; j += 32) {
+                        const double a = row[j] - (vr * wp[j + 1] + wr * vp[j + 1]);
+                        row[j] = a;
+                        s += a * v[j];
+                    }
+                } else {
+                    for (int j = sg * seg_len + lane; j < j1; j += 32) s += row[j] * v[j];
+                }
+            }
+            s = warp_sum(s);
+            if (lane == 0) part[it] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x < Q) {
+            const int r = cta + G * static_cast<int>(threadIdx.x);
+            if (r > k && r < n) {
+                double s = 0.0;
+                for (int sg = 0; sg < S; ++sg) s += part[threadIdx.x * S + sg];
+                P[r] = t * s;
+            }
+        }
+        coop_barrier(ctr, phase);
+        double pv = 0.0;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const double q = __ldcg(P + k + 1 + i);
+            w[i] = q;
+            pv += q * v[i];
+        }
+        const double K = 0.5 * t * block_sum(pv, red);
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            w[i] -= K * v[i];
+            vp[i] = v[i];
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += blockDim.x) wp[i] = w[i];
+        __syncthreads();
+        pend = t != 0.0;
+        if ((k + 1) % G == cta && warp == 0) {  // the next pivot row: update, publish, flag
+            double* row = rows + static_cast<size_t>((k + 1) / G) * n + k + 1;
+            double* out = A + static_cast<size_t>(k + 1) * n + k + 1;
+            const double v0 = v[0], w0 = w[0];
+            for (int j = lane; j < m; j += 32) {
+                const double a = pend ? row[j] - (v0 * w[j] + w0 * v[j]) : row[j];
+                row[j] = a;
+                out[j] = a;
+            }
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicExch(flags + k + 1, 1);
+        }
+        __syncthreads();
+    }
+    coop_barrier(ctr, phase);
+    if (n >= 2 && cta == (n - 1) % G && threadIdx.x == 0) {
+        const int k = n - 2;
+        const double* rl = rows + static_cast<size_t>((n - 1) / G) * n;
+        double a_nn = rl[n - 1];
+        double a_n1 = rl[n - 2];
+        if (pend && n >= 3) {
+            const double vr = vp[(n - 1) - k], wr = wp[(n - 1) - k];
+            a_nn -= vr * wp[(n - 1) - k] + wr * vp[(n - 1) - k];
+            a_n1 -= vr * wp[(n - 2) - k] + wr * vp[(n - 2) - k];
+        }
+        d[n - 2] = __ldcg(A + static_cast<size_t>(n - 2) * n + n - 2);
+        e[n - 2] = a_n1;
+        d[n - 1] = a_nn;
+    }
+}
+
 // ---------------------------------------------------------------- eigenvalues
 __device__ __forceinline__ double frcp(double q) {
     double y;
@@ -1228,8 +1372,34 @@ bool coop_tridiag(double* A, int n, double* d, double* e, double* V, double* tau
     int dev = 0, coop = 0;
     TCB_CUDA(cudaGetDevice(&dev));
     TCB_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    if (!coop) return false;
+    // shared-memory-resident rows when they fit (TCB_TRIDIAG_L2=1: the L2 variant)
+    {
+        const int G = std::min(sm_count(), n);
+        const int Q = (n + G - 1) / G;
+        const int S = std::max(1, (kCoopThreads / 32) / Q);
+        const size_t smem = (static_cast<size_t>(Q) * n + 4 * static_cast<size_t>(n) + 32 + Q * S) * sizeof(double);
+        if (smem <= 220 * 1024 && !std::getenv("TCB_TRIDIAG_L2")) {
+            TCB_ONCE_PER_DEVICE(cudaFuncSetAttribute(tridiag_coop_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     220 * 1024));
+            int per_sm = 0;
+            TCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tridiag_coop_smem, kCoopThreads, smem));
+            if (per_sm >= 1) {
+                DevBuf<unsigned> ctr(1, s);
+                DevBuf<int> flags(n, s);
+                ctr.zero();
+                flags.zero();
+                int q = Q, sg = S, nn = n;
+                void* args[] = {&A, &nn, &d, &e, &V, &tau, &P, &ctr.p, &flags.p, &q, &sg};
+                TCB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tridiag_coop_smem), dim3(G),
+                                                     dim3(kCoopThreads), args, smem, s));
+                count_launch();
+                return true;
+            }
+        }
+    }
     const size_t smem = (4 * static_cast<size_t>(n) + 32) * sizeof(double);
-    if (!coop || smem > 220 * 1024) return false;
+    if (smem > 220 * 1024) return false;
     TCB_CUDA(cudaFuncSetAttribute(tridiag_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
     TCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tridiag_coop, kCoopThreads, smem));
