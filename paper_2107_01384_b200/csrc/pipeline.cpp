@@ -907,7 +907,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
             if (fut.valid()) fut.wait();  // the task reads this frame's buffers
         }
     } upper;
-    if (par && !eo.shard && d + 3 <= 8 && !std::getenv("TCB_NO_EARLY_PLANES")) {
+    if (par && !eo.shard && d + 3 <= 8 && nc > (u64{1} << 20) && !std::getenv("TCB_NO_EARLY_PLANES")) {
         eo.on_breakpoint = [&](int p) {
             if (p >= 63 || upper.fut.valid()) return;
             const int dev = cur_device();

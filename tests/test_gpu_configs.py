@@ -166,3 +166,16 @@ def test_eigensolver_size_limit_message(gpu_pkg):
     g = np.eye(2400)
     with pytest.raises(gpu_pkg.TucompError, match="supports mode sizes up to"):
         gpu_pkg.eig(g, 1)
+
+
+def test_early_full_planes_same_container(gpu_pkg, monkeypatch):
+    """Large cores code the full planes above the breakpoint beside the plan
+    (speculative sign fold) and append the last plane at finalisation; the
+    container must be byte-identical to coding every plane at once."""
+    x = config_input("c2")
+    src = gpu_pkg.SourceBuffer.from_array(x)
+    a = gpu_pkg.compress(src, gpu_pkg.Params(target_re=1e-6))
+    assert int(np.prod(a.ranks)) > (1 << 20)
+    monkeypatch.setenv("TCB_NO_EARLY_PLANES", "1")
+    b = gpu_pkg.compress(src, gpu_pkg.Params(target_re=1e-6))
+    assert a.container == b.container
