@@ -91,6 +91,8 @@ def test_c5_against_oracle_fixture(gpu_pkg, re):
     import torch
 
     fx = _c5_fixture()
+    if f"{re:g}" not in fx["cases"]:
+        pytest.skip(f"no c5 fixture for RE {re:g}")
     case = fx["cases"][f"{re:g}"]
     x = synth.grf_torch(n=1024, kmax=341, seed=fx["seed"])
     xs = x.double()
