@@ -997,37 +997,44 @@ __global__ void cluster_mgs_kernel(const int* __restrict__ clusters, int n, doub
 // trailing update spread over the GPU), Z_c <- D^-1/2 E Z_c (the TTM kernel);
 // twice.  Like MGS it keeps the nested spans of the vectors in order; a
 // non-positive pivot falls back to MGS for that cluster.
-__global__ void bigchol_init_kernel(double* __restrict__ E, int k) {
+// All k elimination steps in one cooperative launch (one grid barrier per step
+// instead of one launch per step); C and E live in L2 (read with ld.cg: other
+// CTAs wrote them in earlier steps).  Elimination form: step j takes the Schur
+// complement of C below pivot j and accumulates E = L^-1 (C = L D L^T) beside it.
+__global__ void __launch_bounds__(256) bigchol_coop_kernel(double* __restrict__ C, double* __restrict__ E,
+                                                           double* __restrict__ rinv, int k, int* __restrict__ bad,
+                                                           unsigned* __restrict__ ctr) {
+    unsigned phase = 0;
     const u64 kk = static_cast<u64>(k) * k;
-    for (u64 e = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; e < kk; e += static_cast<u64>(gridDim.x) * blockDim.x)
-        E[e] = (e / k) == (e % k) ? 1.0 : 0.0;
-}
-
-__global__ void bigchol_step_kernel(double* __restrict__ C, double* __restrict__ E, double* __restrict__ rinv, int k,
-                                    int j, int* __restrict__ bad) {
-    const double djj = C[static_cast<u64>(j) * k + j];
-    if (!(djj >= DBL_MIN)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) *bad = 1;
-        return;
-    }
-    const double ri = rsqrt(djj), inv = ri * ri;
-    if (blockIdx.x == 0 && threadIdx.x == 0) rinv[j] = ri;
-    const u64 m = static_cast<u64>(k - j - 1);                 // trailing rows
-    const u64 nc = m, ne = static_cast<u64>(j + 1);             // C columns > j, E columns <= j
-    const u64 total = m * (nc + ne);
-    const double* rowj = C + static_cast<u64>(j) * k;
-    const double* erow = E + static_cast<u64>(j) * k;
-    for (u64 e = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-         e += static_cast<u64>(gridDim.x) * blockDim.x) {
-        const u64 i = j + 1 + e / (nc + ne), c = e % (nc + ne);
-        const double f = rowj[i] * inv;
-        if (c < nc) {
-            const u64 col = j + 1 + c;
-            C[i * k + col] = fma(-f, rowj[col], C[i * k + col]);
-        } else {
-            const u64 col = c - nc;
-            E[i * k + col] = fma(-f, erow[col], E[i * k + col]);
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    const u64 t0 = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (u64 e = t0; e < kk; e += stride) E[e] = (e / k) == (e % k) ? 1.0 : 0.0;
+    coop_barrier(ctr, phase);
+    for (int j = 0; j < k; ++j) {
+        const double djj = __ldcg(C + static_cast<u64>(j) * k + j);
+        if (!(djj >= DBL_MIN)) {
+            if (t0 == 0) *bad = 1;
+            return;  // every CTA reads the same pivot: all leave here
         }
+        const double ri = rsqrt(djj), inv = ri * ri;
+        if (t0 == 0) rinv[j] = ri;
+        const u64 m = static_cast<u64>(k - j - 1);
+        const u64 nc = m, ne = static_cast<u64>(j + 1);
+        const u64 total = m * (nc + ne);
+        const double* rowj = C + static_cast<u64>(j) * k;
+        const double* erow = E + static_cast<u64>(j) * k;
+        for (u64 e = t0; e < total; e += stride) {
+            const u64 i = j + 1 + e / (nc + ne), c = e % (nc + ne);
+            const double f = __ldcg(rowj + i) * inv;
+            if (c < nc) {
+                const u64 col = j + 1 + c;
+                C[i * k + col] = fma(-f, __ldcg(rowj + col), __ldcg(C + i * k + col));
+            } else {
+                const u64 col = c - nc;
+                E[i * k + col] = fma(-f, __ldcg(erow + col), __ldcg(E + i * k + col));
+            }
+        }
+        coop_barrier(ctr, phase);
     }
 }
 
@@ -1049,17 +1056,26 @@ bool cluster_cholqr2(double* Zc, int n, int k, cudaStream_t s) {
     bad.zero();
     for (int pass = 0; pass < 2; ++pass) {
         gram_f64(Zc, static_cast<u64>(k), static_cast<u64>(n), C.p, s);
-        bigchol_init_kernel<<<grid_for(static_cast<u64>(k) * k, 256, 4, 4), 256, 0, s>>>(E.p, k);
-        for (int j = 0; j < k; ++j) {
-            const u64 work = static_cast<u64>(k - j - 1) * static_cast<u64>(k);
-            bigchol_step_kernel<<<grid_for(std::max<u64>(work, 1), 256, 2, 2), 256, 0, s>>>(C.p, E.p, rinv.p, k, j,
-                                                                                        bad.p);
+        {
+            DevBuf<unsigned> ctr(1, s);
+            ctr.zero();
+            const unsigned grid = std::min<unsigned>(static_cast<unsigned>(sm_count()),
+                                                     cdiv(static_cast<u64>(k) * k, 256));
+            double* cp = C.p;
+            double* ep = E.p;
+            double* rp = rinv.p;
+            int* bp = bad.p;
+            unsigned* cq = ctr.p;
+            int kv = k;
+            void* args[] = {&cp, &ep, &rp, &kv, &bp, &cq};
+            TCB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bigchol_coop_kernel), dim3(grid), dim3(256),
+                                                 args, 0, s));
         }
         bigchol_w_kernel<<<grid_for(static_cast<u64>(k) * k, 256, 4, 4), 256, 0, s>>>(E.p, rinv.p, k, W.p);
         ttm_f64(Zc, static_cast<u64>(k), static_cast<u64>(n), W.p, static_cast<u64>(k), out.p, s);  // n x k
         permute_axes(out.p, Zc, std::vector<u64>{static_cast<u64>(n), static_cast<u64>(k)},
                      std::vector<u64>{1, 0}, s);
-        count_launch(static_cast<u64>(k) + 2);
+        count_launch(3);
     }
     TCB_LAUNCH();
     return bad.to_host()[0] == 0;

@@ -276,83 +276,119 @@ struct TtmShape {  // 8 warps: TN 64 -> 4x2 warps of 32x32; else 8x1 warps of 16
     static constexpr int smem_doubles = kTtmStages * TBK * (APAD + UPAD);
 };
 
+// One CTA computes output tiles (TM columns of B x TN of r) over a range of
+// TBK-row k slabs.  Tiles are numbered with the r tile fastest, so the CTAs
+// that read the same TM x rows panel of B run together and share it through
+// L2 (one DRAM pass over B even when r spans many tiles).  Regular mode: CTA
+// b owns tile b, every slab.  Stream-K mode (HBM-bound launches whose tile
+// count is close to the resident-CTA count, where the last partial wave would
+// idle most SMs): the tiles x slabs units are split evenly over `gridDim.x`
+// persistent CTAs; a tile cut into two pieces is summed by two atomic adds
+// into the zeroed output (0 + a + b == 0 + b + a: deterministic), which the
+// host guarantees by units per CTA >= slabs per tile.
 template <bool AV16, int TN>
 __global__ void __launch_bounds__(256) ttm_kernel(const double* __restrict__ B, u64 rows, u64 cols,
-                                                  const double* __restrict__ U, u64 r, double* __restrict__ out) {
+                                                  const double* __restrict__ U, u64 r, double* __restrict__ out,
+                                                  int stream_k) {
     using S = TtmShape<TN>;
     constexpr int MI = S::MI, NI = S::NI, UPAD = S::UPAD;
     extern __shared__ __align__(16) double smem_ttm[];
     auto As = reinterpret_cast<double (*)[TBK][APAD]>(smem_ttm);
     auto Us = reinterpret_cast<double (*)[TBK][UPAD]>(smem_ttm + kTtmStages * TBK * APAD);
-    const u64 m0 = static_cast<u64>(blockIdx.x) * TM;
-    const u64 n0 = static_cast<u64>(blockIdx.y) * TN;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = TN == 64 ? (warp >> 1) * 32 : warp * 16, wn = TN == 64 ? (warp & 1) * 32 : 0;
-    double acc[MI][NI][2];
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    auto load = [&](int buf, u64 k0) {
-        if constexpr (AV16) {
-            for (int c = threadIdx.x; c < TBK * (TM / 2); c += blockDim.x) {
-                const int kk = c / (TM / 2), mm = (c % (TM / 2)) * 2;
-                const u64 gk = k0 + kk, gm = m0 + mm;
-                const bool ok = gk < rows && gm < cols;  // cols even: pairs never straddle
-                cp_async16(&As[buf][kk][mm], ok ? B + gk * cols + gm : B, ok);
-            }
-        } else {
-            for (int c = threadIdx.x; c < TBK * TM; c += blockDim.x) {
-                const int kk = c / TM, mm = c % TM;
-                const u64 gk = k0 + kk, gm = m0 + mm;
-                const bool ok = gk < rows && gm < cols;
-                cp_async8(&As[buf][kk][mm], ok ? B + gk * cols + gm : B, ok);
-            }
-        }
-        for (int c = threadIdx.x; c < TBK * TN; c += blockDim.x) {
-            const int kk = c / TN, nn = c % TN;
-            const u64 gk = k0 + kk, gn = n0 + nn;
-            const bool ok = gk < rows && gn < r;
-            cp_async8(&Us[buf][kk][nn], ok ? U + gk * r + gn : U, ok);
-        }
-    };
+    const u64 nrt = (r + TN - 1) / TN, ntiles = ((cols + TM - 1) / TM) * nrt;
     const int nslab = static_cast<int>((rows + TBK - 1) / TBK);
-#pragma unroll
-    for (int st = 0; st < kTtmStages - 1; ++st) {
-        if (st < nslab) load(st, static_cast<u64>(st) * TBK);
-        cp_commit();
+    u64 u, u_end;  // k-slab units [u, u_end) of tile-major order
+    if (stream_k) {
+        const u64 units = ntiles * static_cast<u64>(nslab);
+        u = units * blockIdx.x / gridDim.x;
+        u_end = units * (blockIdx.x + 1) / gridDim.x;
+    } else {
+        u = static_cast<u64>(blockIdx.x) * nslab;
+        u_end = u + nslab;
     }
-    for (int sl = 0; sl < nslab; ++sl) {
-        const int cur = sl % kTtmStages;
-        cp_wait<kTtmStages - 2>();
-        __syncthreads();
-        // refill the stage consumed last iteration (all warps are past it)
-        if (sl + kTtmStages - 1 < nslab) load((sl + kTtmStages - 1) % kTtmStages, static_cast<u64>(sl + kTtmStages - 1) * TBK);
-        cp_commit();
+    while (u < u_end) {
+        const u64 tile = u / nslab;
+        const int s0 = static_cast<int>(u - tile * nslab);
+        const int s1 = static_cast<int>(min(static_cast<u64>(nslab), s0 + (u_end - u)));
+        u += static_cast<u64>(s1 - s0);
+        const u64 m0 = (tile / nrt) * TM;
+        const u64 n0 = (tile % nrt) * TN;
+        double acc[MI][NI][2];
 #pragma unroll
-        for (int kk = 0; kk < TBK; kk += 4) {
-            double a[MI], b[NI];
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
-            for (int mi = 0; mi < MI; ++mi) a[mi] = As[cur][kk + (lane & 3)][wm + mi * 8 + (lane >> 2)];
+            for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+        auto load = [&](int buf, u64 k0) {
+            if constexpr (AV16) {
+                for (int c = threadIdx.x; c < TBK * (TM / 2); c += blockDim.x) {
+                    const int kk = c / (TM / 2), mm = (c % (TM / 2)) * 2;
+                    const u64 gk = k0 + kk, gm = m0 + mm;
+                    const bool ok = gk < rows && gm < cols;  // cols even: pairs never straddle
+                    cp_async16(&As[buf][kk][mm], ok ? B + gk * cols + gm : B, ok);
+                }
+            } else {
+                for (int c = threadIdx.x; c < TBK * TM; c += blockDim.x) {
+                    const int kk = c / TM, mm = c % TM;
+                    const u64 gk = k0 + kk, gm = m0 + mm;
+                    const bool ok = gk < rows && gm < cols;
+                    cp_async8(&As[buf][kk][mm], ok ? B + gk * cols + gm : B, ok);
+                }
+            }
+            for (int c = threadIdx.x; c < TBK * TN; c += blockDim.x) {
+                const int kk = c / TN, nn = c % TN;
+                const u64 gk = k0 + kk, gn = n0 + nn;
+                const bool ok = gk < rows && gn < r;
+                cp_async8(&Us[buf][kk][nn], ok ? U + gk * r + gn : U, ok);
+            }
+        };
+        __syncthreads();  // the previous piece's readers are done with every stage
 #pragma unroll
-            for (int ni = 0; ni < NI; ++ni) b[ni] = Us[cur][kk + (lane & 3)][wn + ni * 8 + (lane >> 2)];
-#pragma unroll
-            for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-                for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        for (int st = 0; st < kTtmStages - 1; ++st) {
+            if (s0 + st < s1) load(st, static_cast<u64>(s0 + st) * TBK);
+            cp_commit();
         }
+        for (int sl = s0; sl < s1; ++sl) {
+            const int cur = (sl - s0) % kTtmStages;
+            cp_wait<kTtmStages - 2>();
+            __syncthreads();
+            // refill the stage consumed last iteration (all warps are past it)
+            if (sl + kTtmStages - 1 < s1)
+                load((sl - s0 + kTtmStages - 1) % kTtmStages, static_cast<u64>(sl + kTtmStages - 1) * TBK);
+            cp_commit();
+#pragma unroll
+            for (int kk = 0; kk < TBK; kk += 4) {
+                double a[MI], b[NI];
+#pragma unroll
+                for (int mi = 0; mi < MI; ++mi) a[mi] = As[cur][kk + (lane & 3)][wm + mi * 8 + (lane >> 2)];
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni) b[ni] = Us[cur][kk + (lane & 3)][wn + ni * 8 + (lane >> 2)];
+#pragma unroll
+                for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+            }
+        }
+        cp_wait<0>();
+        const bool whole = s0 == 0 && s1 == nslab;
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+                const u64 m = m0 + wm + mi * 8 + (lane >> 2);
+                const u64 n = n0 + wn + ni * 8 + 2 * (lane & 3);
+                if (m >= cols) continue;
+                if (whole) {
+                    if (n < r) out[m * r + n] = acc[mi][ni][0];
+                    if (n + 1 < r) out[m * r + n + 1] = acc[mi][ni][1];
+                } else {
+                    if (n < r) atomicAdd(out + m * r + n, acc[mi][ni][0]);
+                    if (n + 1 < r) atomicAdd(out + m * r + n + 1, acc[mi][ni][1]);
+                }
+            }
     }
-#pragma unroll
-    for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-            const u64 m = m0 + wm + mi * 8 + (lane >> 2);
-            const u64 n = n0 + wn + ni * 8 + 2 * (lane & 3);
-            if (m >= cols) continue;
-            if (n < r) out[m * r + n] = acc[mi][ni][0];
-            if (n + 1 < r) out[m * r + n + 1] = acc[mi][ni][1];
-        }
 }
 
 // ------------------------------------------------------------------ small helpers
@@ -510,15 +546,31 @@ void gram_cols_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t 
 
 template <int TN>
 void launch_ttm(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s) {
-    dim3 grid(cdiv(cols, TM), cdiv(r, TN));
+    const u64 ntiles = static_cast<u64>(cdiv(cols, TM)) * cdiv(r, TN);
+    const u64 nslab = (rows + TBK - 1) / TBK;
     const bool v16 = (cols % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
     constexpr int smem = TtmShape<TN>::smem_doubles * sizeof(double);
-    TCB_ONCE_PER_DEVICE({
+    struct Occ {
+        int a = 0, b = 0;
+    };
+    static PerDevice<Occ> occ;
+    const Occ& o = occ.get([] {
+        Occ x;
         cudaFuncSetAttribute(ttm_kernel<true, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(ttm_kernel<false, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x.a, ttm_kernel<true, TN>, 256, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x.b, ttm_kernel<false, TN>, 256, smem);
+        return x;
     });
-    if (v16) ttm_kernel<true, TN><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out);
-    else ttm_kernel<false, TN><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out);
+    // stream-K when the last partial wave would be large and every tile is cut at
+    // most once (the HBM-bound small-r projections, e.g. c2's 512 tiles on 444 slots)
+    const u64 slots = static_cast<u64>(sm_count()) * static_cast<u64>(std::max(1, v16 ? o.a : o.b));
+    const bool sk = TN <= 32 && ntiles > slots && ntiles < 4 * slots && !std::getenv("TCB_TTM_NO_STREAMK");
+    const unsigned grid = sk ? static_cast<unsigned>(slots) : static_cast<unsigned>(ntiles);
+    if (sk) TCB_CUDA(cudaMemsetAsync(out, 0, cols * r * sizeof(double), s));
+    if (v16) ttm_kernel<true, TN><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out, sk ? 1 : 0);
+    else ttm_kernel<false, TN><<<grid, 256, smem, s>>>(B, rows, cols, U, r, out, sk ? 1 : 0);
+    (void)nslab;
 }
 
 void ttm_f64(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s) {

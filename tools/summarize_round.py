@@ -15,35 +15,30 @@ PROF = os.path.join(ROOT, "profiles")
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 os.makedirs(PROF, exist_ok=True)
 
-shutil.copy(os.path.join(OUT, "bench.json"), os.path.join(PROF, f"bench_{tag}_c2_1e-4.json"))
+def launch_summary(src, dst, header):
+    if not os.path.exists(src):
+        return
+    shutil.copy(src, dst.replace("_summary.txt", ".csv"))
+    summ = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_summary.py"), src],
+                          capture_output=True, text=True).stdout
+    with open(dst, "w") as f:
+        f.write(header)
+        f.write(summ)
+
+
+shutil.copy(os.path.join(OUT, "bench.json"), os.path.join(PROF, f"bench_{tag}_c5_1e-2.json"))
 shutil.copy(os.path.join(OUT, "bench_ref.json"), os.path.join(PROF, f"bench_{tag}_reference.json"))
-shutil.copy(os.path.join(OUT, "launches.csv"), os.path.join(PROF, f"launches_{tag}_c2_1e-4.csv"))
-summ = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_summary.py"),
-                       os.path.join(OUT, "launches.csv")], capture_output=True, text=True).stdout
-with open(os.path.join(PROF, f"launches_{tag}_c2_1e-4_summary.txt"), "w") as f:
-    f.write("# ncu --metrics gpu__time_duration.sum --clock-control none, bench.py --steps 2 --warmup 3\n")
-    f.write("# (cold-cache, serialised launches; 6 compress calls: 3 warm-up, 2 timed, 1 profiled + e2e)\n")
-    f.write(summ)
-
-# decompress launch list (one c2 compress, then one decompress: the dec_* kernels onward)
-dec = os.path.join(OUT, "dec_launches.csv")
-if os.path.exists(dec):
-    rows = list(csv.DictReader(l for l in open(dec) if l.startswith('"')))
-    first = next((i for i, r in enumerate(rows) if "dec_entropy" in r["Kernel Name"]), None)
-    if first is not None:
-        with open(os.path.join(PROF, f"launches_{tag}_decompress_c2.txt"), "w") as f:
-            f.write("# ncu --metrics gpu__time_duration.sum --clock-control none, tools/decompress_once.py "
-                    "--steps 1 --warmup 0\n# (cold-cache, serialised): the decompress call's kernels\n")
-            tot = 0.0
-            for r in rows[first:]:
-                ns = float(r["Metric Value"].replace(",", ""))
-                tot += ns
-                f.write(f"{ns / 1e3:9.1f} us  grid {r['Grid Size']:>14} block {r['Block Size']:>12}  "
-                        f"{r['Kernel Name'][:90]}\n")
-            f.write(f"{tot / 1e3:9.1f} us  total\n")
-
+launch_summary(os.path.join(OUT, "launches_bench.csv"), os.path.join(PROF, f"launches_{tag}_bench_summary.txt"),
+               "# ncu --metrics gpu__time_duration.sum --clock-control none, python bench.py --steps 2 --warmup 3 "
+               "--no-cpu-baseline --no-secondary\n# (cold-cache, serialised launches of every compress the command "
+               "runs: 3 warm-up, 2 timed, e2e, profiled, roofline probes)\n")
+launch_summary(os.path.join(OUT, "launches.csv"), os.path.join(PROF, f"launches_{tag}_c5_1e-2_summary.txt"),
+               "# ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none,\n"
+               "# tools/c5_once.py 1e-2 (C5_PROFILE=1 C5_ITERS=2): the launches of ONE c5 compress after one\n"
+               "# warm-up (cold-cache, serialised: shares, not the overlapped wall time)\n")
 # full capture: per-kernel key metrics
-raw = subprocess.run(["ncu", "-i", os.path.join(OUT, "full.ncu-rep"), "--page", "raw", "--csv"],
+raw = subprocess.run(["ncu", "-i", os.path.join(OUT, sys.argv[2] if len(sys.argv) > 2 else "full.ncu-rep"),
+                      "--page", "raw", "--csv"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, units, data = rows[0], rows[1], rows[2:]
@@ -61,7 +56,7 @@ want = {
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
          "ns": 1e-3, "us": 1, "ms": 1e3}
 ki = hdr.index("Kernel Name")
-lines = ["# ncu --set full --clock-control none on one c2 compress (tools/profile_round.sh)",
+lines = ["# ncu --set full --clock-control none on one c5 compress (tools/profile_round.sh; first launches of each)",
          "# kernel | grid x block | us | DRAM read+write MB | DRAM GB/s | DRAM % elapsed | DMMA pipe % (of active) | SM % | warps active %"]
 for r in data:
     name = r[ki].split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
@@ -82,6 +77,6 @@ for r in data:
                  f"{vals.get('sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active', float('nan')):6.1f} "
                  f"{vals['sm__throughput.avg.pct_of_peak_sustained_elapsed']:6.1f} "
                  f"{vals['sm__warps_active.avg.pct_of_peak_sustained_active']:6.1f}")
-with open(os.path.join(PROF, f"ncu_{tag}_full_summary.txt"), "w") as f:
+with open(os.path.join(PROF, f"ncu_{tag}_{sys.argv[3] if len(sys.argv) > 3 else 'full'}_summary.txt"), "w") as f:
     f.write("\n".join(lines) + "\n")
 print("\n".join(lines))
