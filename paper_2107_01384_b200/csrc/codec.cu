@@ -774,6 +774,10 @@ __global__ void __launch_bounds__(kScT) sc_emit_kernel(const u64* __restrict__ m
         u64 ri = off.raw_b + (pre2 >> 32), oi = off.ones_b + (pre2 & 0xffffffffu);
         long long pl = prevL;
         li = off.lead_b + (pre & 0xffffffffu);
+        // this thread's raw bits are consecutive (at most 32): they touch at most
+        // two words, gathered in registers and or-ed in with two atomics
+        const u64 R0 = d.raw_off + ri, W0 = R0 >> 5;
+        u32 wlo = 0, whi = 0;
 #pragma unroll
         for (int q = 0; q < kScPer; ++q) {
             if (q >= nv) continue;
@@ -792,10 +796,14 @@ __global__ void __launch_bounds__(kScT) sc_emit_kernel(const u64* __restrict__ m
             }
             if (bit) {
                 const u64 R = d.raw_off + ri;
-                atomicOr(raw + (R >> 5), 1u << (8 * ((R >> 3) & 3) + (7 - (R & 7))));
+                const u32 mbit = 1u << (8 * ((R >> 3) & 3) + (7 - (R & 7)));
+                if ((R >> 5) == W0) wlo |= mbit;
+                else whi |= mbit;
             }
             ++ri;
         }
+        if (wlo) atomicOr(raw + W0, wlo);
+        if (whi) atomicOr(raw + W0 + 1, whi);
         __syncthreads();
         if (threadIdx.x == kScT - 1) {  // the sub-chunk's first and last one (fix-up of its first symbol)
             long long* f = fx + 2 * (static_cast<u64>(pi) * nsc_all + g);
