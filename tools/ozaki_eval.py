@@ -96,6 +96,12 @@ def main():
     _, ti = timeit(lambda: torch._int_mm(a, a.t()), reps=5)
     print(f"int8 GEMM 1024x1024x{KCH}: {ti:.3f} ms = {2 * 1024 * 1024 * KCH / ti / 1e9:.0f} TOP/s", flush=True)
     del a
+    # the library's rate on a shape with enough output tiles for every SM
+    a = torch.randint(-64, 65, (8192, 32768), dtype=torch.int8, device="cuda")
+    b = torch.randint(-64, 65, (8192, 32768), dtype=torch.int8, device="cuda")
+    _, ti = timeit(lambda: torch._int_mm(a, b.t()), reps=5)
+    print(f"int8 GEMM 8192x8192x32768: {ti:.3f} ms = {2 * 8192 * 8192 * 32768 / ti / 1e9:.0f} TOP/s", flush=True)
+    del a, b
     for S in Ss:
         g, t = timeit(lambda: ozaki_gram(x64, S), reps=2)
         err = ((g - g64).abs() / (nrm[:, None] * nrm[None, :])).max().item()
