@@ -104,7 +104,11 @@ def test_c5_against_oracle_fixture(gpu_pkg, re):
                                 gpu_pkg.Params(target_re=re))
     assert r.ranks == case["ranks"]
     assert abs(len(r.container) - case["container_bytes"]) <= 0.01 * case["container_bytes"]
-    assert r.norm_sq == pytest.approx(fx["norm_sq"], rel=1e-12)
+    # |A|^2 of 2^30 floats: the reference accumulates it serially in 4 double lanes
+    # (kernels_avx2.cpp:146-159), ~sqrt(n) eps = 2e-12 relative off the exact sum; the
+    # device's reduction tree is within 1e-15 of the exact sum (fixture checksum[1])
+    assert r.norm_sq == pytest.approx(fx["norm_sq"], rel=1e-10)
+    assert r.norm_sq == pytest.approx(fx["input_checksum"][1], rel=1e-14)
     assert r.estimate.truncation_sse == pytest.approx(case["truncation_sse"], rel=1e-6)
     out = torch.empty(x.numel() * 4, dtype=torch.uint8, device="cuda")
     gpu_pkg.decompress_device(r.container, out.data_ptr(), out.numel())
