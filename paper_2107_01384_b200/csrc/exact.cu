@@ -583,14 +583,19 @@ struct CFn {
     int tie, bpar, bad;
 };
 __device__ __forceinline__ CFn cfn_id() { return CFn{0, kBig, -kBig, 0, 0, 0, 0, 0, 0, 0}; }
-__device__ __forceinline__ void cfn_term(CFn& f, double t, int e) {
-    if (t == 0.0 || f.bad) return;
-    long long j;
-    bool tie;
-    if (!unitize(t, e, j, tie)) {
-        f.bad = 1;
-        return;
-    }
+// unitize() in floating point: y = t / u exactly (u = 2^(e-52) = 1 / scale), the
+// round-half-even increment by one conversion, a tie when y - j is exactly 1/2
+// (then j = floor(y), as unitize returns); |y| >= 2^61 is unitize's rejection.
+__device__ __forceinline__ bool unit_fp(double t, double scale, long long& j, bool& tie) {
+    const double y = t * scale;
+    if (fabs(y) >= 0x1p61) return false;
+    j = __double2ll_rn(y);
+    const double d = y - static_cast<double>(j);  // exact: |d| <= 1/2
+    tie = fabs(d) == 0.5;
+    if (tie && d < 0.0) j -= 1;
+    return true;
+}
+__device__ __forceinline__ void cfn_push(CFn& f, long long j, bool tie) {
     if (!f.tie) {
         if (!tie) {
             f.A += j;
@@ -660,13 +665,22 @@ __global__ void __launch_bounds__(128) ex_plane_kernel(const u64* __restrict__ m
     const int p_low = p_top - np + 1;
     double aL = 0.0, aT = 0.0;
     CFn fL = cfn_id(), fT = cfn_id();
-    int eL = 52, eT = 52, rL = 52, rT = 52;
+    int rL = 52, rT = 52;
+    double sL = 1.0, sT = 1.0;  // 2^(52 - e) of each function's region
     if (PASS == 1 && on) {
         rL = region_of(P[static_cast<u64>(2 * lane) * nch + c]);
         rT = region_of(P[static_cast<u64>(2 * lane + 1) * nch + c]);
-        eL = rexp(rL);
-        eT = rexp(rT);
+        sL = scalbn(1.0, 52 - rexp(rL));
+        sT = scalbn(1.0, 52 - rexp(rT));
     }
+    // the lead and trail gains share one form (terms.cuh):
+    //   t = (double(a) - c)^2 - sig2(m, p),  trail (msb > p): a = m mod 2^(p+1), c = 2^p
+    //                                        lead (msb == p): a = m,            c = 0
+    const int pc = p < 0 ? 0 : p;
+    const u64 mask_p = pc == 0 ? 0 : (u64{1} << pc) - 1;
+    const u64 mask_p1 = pc >= 63 ? ~u64{0} : (u64{1} << (pc + 1)) - 1;
+    const double half_p = pc == 0 ? 0.0 : __ull2double_rn(u64{1} << (pc - 1));
+    const double c_p = __ull2double_rn(u64{1} << (pc > 63 ? 63 : pc));
     u32 nle = 0, none = 0, ntr = 0;
     const u64* mp = m + lo;
     for (int i0 = 0; i0 < cnt; i0 += 8) {
@@ -685,14 +699,25 @@ __global__ void __launch_bounds__(128) ex_plane_kernel(const u64* __restrict__ m
             nle += tb <= p;
             none += tb == p;
             ntr += tb > p;
-            if (tb > p) {
-                const double t = t_trail_gain(v[u], p);
-                if (PASS == 0) aT += t;
-                else cfn_term(fT, t, eT);
-            } else if (tb == p) {
-                const double t = t_lead_gain(v[u], p);
-                if (PASS == 0) aL += t;
-                else cfn_term(fL, t, eL);
+            if (tb < p) continue;
+            const bool tr = tb > p;
+            const double x0 = __dsub_rn(__ull2double_rn(tr ? (v[u] & mask_p1) : v[u]), tr ? c_p : 0.0);
+            const double r0 = __dsub_rn(__ull2double_rn(v[u] & mask_p), half_p);
+            const double t = __dsub_rn(__dmul_rn(x0, x0), pc == 0 ? 0.0 : __dmul_rn(r0, r0));
+            if (PASS == 0) {
+                aT += tr ? t : 0.0;
+                aL += tr ? 0.0 : t;
+            } else if (t != 0.0) {
+                long long j = 0;
+                bool tie = false;
+                const bool ok = unit_fp(t, tr ? sT : sL, j, tie);
+                if (tr) {
+                    if (!ok) fT.bad = 1;
+                    else if (!fT.bad) cfn_push(fT, j, tie);
+                } else {
+                    if (!ok) fL.bad = 1;
+                    else if (!fL.bad) cfn_push(fL, j, tie);
+                }
             }
         }
     }
