@@ -907,7 +907,10 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
             if (fut.valid()) fut.wait();  // the task reads this frame's buffers
         }
     } upper;
-    if (par && !eo.shard && d + 3 <= 8 && nc > (u64{1} << 20) && !std::getenv("TCB_NO_EARLY_PLANES")) {
+    // Off by default: on c5 the upper planes' emission competes with the probe and
+    // the plane statistics for the SMs and the wait at finalisation cost more than
+    // the overlap saved (542 vs 560 ms); TCB_EARLY_PLANES=1 turns it on.
+    if (par && !eo.shard && d + 3 <= 8 && nc > (u64{1} << 20) && std::getenv("TCB_EARLY_PLANES")) {
         eo.on_breakpoint = [&](int p) {
             if (p >= 63 || upper.fut.valid()) return;
             const int dev = cur_device();

@@ -65,7 +65,11 @@ def test_config_full_size_against_oracle(gpu_pkg, name, re):
     assert abs(len(res.container) - len(ref.container)) <= 0.01 * len(ref.container), (
         len(res.container), len(ref.container))
     assert res.norm_sq == pytest.approx(ref.norm_sq, rel=1e-12)
-    assert res.estimate.truncation_sse == pytest.approx(ref.truncation_sse, rel=1e-6)
+    # the discarded energy is a difference of Gram spectra: both sides carry an
+    # absolute error ~ n eps |A|^2 (c2 @ 1e-4: 5.5e-3 out of |A|^2 = 1.1e6)
+    n_max = max(x.shape)
+    assert abs(res.estimate.truncation_sse - ref.truncation_sse) <= max(
+        1e-6 * ref.truncation_sse, n_max * np.finfo(np.float64).eps * ref.norm_sq)
     e = rel_err(oracle.decompress(res.container, x.shape), x)
     er = rel_err(oracle.decompress(ref.container, x.shape), x)
     assert abs(e - er) <= 0.01 * er, (e, er)
@@ -182,6 +186,6 @@ def test_early_full_planes_same_container(gpu_pkg, monkeypatch):
     src = gpu_pkg.SourceBuffer.from_array(x)
     a = gpu_pkg.compress(src, gpu_pkg.Params(target_re=1e-6))
     assert int(np.prod(a.ranks)) > (1 << 20)
-    monkeypatch.setenv("TCB_NO_EARLY_PLANES", "1")
+    monkeypatch.setenv("TCB_EARLY_PLANES", "1")
     b = gpu_pkg.compress(src, gpu_pkg.Params(target_re=1e-6))
     assert a.container == b.container
