@@ -687,7 +687,7 @@ u64 ac_out_cap(u64 sym_cap, u64 positions) {
 
 namespace {
 void ac_run(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs, u8* ent, u64* elen,
-            u64* bounds, cudaStream_t s) {
+            u64* bounds, cudaStream_t s, int* err_ext = nullptr) {
     const int nj = static_cast<int>(jobs.size());
     if (nj == 0) return;
     if (elen) TCB_CUDA(cudaMemsetAsync(elen, 0, nj * sizeof(u64), s));
@@ -733,8 +733,13 @@ void ac_run(const u64* syms, const u64* counts, int stride, const std::vector<Ac
     DevBuf<u32> gws(gtot + 4, s), idx(rec_ext + 1, s), fp(fptot + 1, s), ndist(nj, s), nep(nj, s);
     DevBuf<uint4> eprec(eptot + 1, s);
     DevBuf<u16> snap(sntot + 1, s);
-    DevBuf<int> err(1, s);
-    err.zero();
+    DevBuf<int> err_own;
+    int* errp = err_ext;
+    if (!errp) {
+        err_own = DevBuf<int>(1, s);
+        err_own.zero();
+        errp = err_own.p;
+    }
     dch.upload(choff.data(), nj + 1);
     dep.upload(epslot.data(), nj + 1);
     const u64 nchunk = choff.back();
@@ -755,12 +760,12 @@ void ac_run(const u64* syms, const u64* counts, int stride, const std::vector<Ac
             DevBuf<int> dids(ids->size(), s);
             dids.upload(ids->data(), ids->size());
             ac_index_kernel<<<static_cast<unsigned>(ids->size()), kIxT, sm, s>>>(
-                syms, counts, stride, djobs.p, nj, dids.p, idx.p, fp.p, ndist.p, gws.p, mc, err.p);
+                syms, counts, stride, djobs.p, nj, dids.p, idx.p, fp.p, ndist.p, gws.p, mc, errp);
             count_launch();
             TCB_LAUNCH();
         }
         ac_epoch_kernel<<<static_cast<unsigned>(nj), kIxT, cap_max * sizeof(u32), s>>>(
-            counts, stride, djobs.p, nj, idx.p, fp.p, ndist.p, eprec.p, snap.p, nep.p, err.p);
+            counts, stride, djobs.p, nj, idx.p, fp.p, ndist.p, eprec.p, snap.p, nep.p, errp);
         ac_code_kernel<<<static_cast<unsigned>(eptot), kMT, 2 * (cap_max + 1) * sizeof(u32), s>>>(
             counts, stride, djobs.p, nj, dep.p, idx.p, fp.p, ndist.p, eprec.p, snap.p, nep.p, recs.p);
         count_launch(2);
@@ -769,8 +774,9 @@ void ac_run(const u64* syms, const u64* counts, int stride, const std::vector<Ac
             ac_bounds_kernel<<<static_cast<unsigned>(nj), 256, 0, s>>>(counts, stride, djobs.p, nj, recs.p, bounds);
             count_launch();
             TCB_LAUNCH();
+            if (err_ext) return;
             int herr = 0;
-            d2h(&herr, err.p, sizeof(int), s);
+            d2h(&herr, errp, sizeof(int), s);
             stream_sync(s);
             if (herr) throw Error("entropy: device model capacity exceeded");
             return;
@@ -791,16 +797,17 @@ void ac_run(const u64* syms, const u64* counts, int stride, const std::vector<Ac
         count_launch();
         TCB_LAUNCH();
     }
+    if (err_ext) return;  // the caller reads the flag with its results
     int herr = 0;
-    d2h(&herr, err.p, sizeof(int), s);
+    d2h(&herr, errp, sizeof(int), s);
     stream_sync(s);
     if (herr) throw Error("entropy: device model capacity exceeded");
 }
 }  // namespace
 
 void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs, u8* ent, u64* elen,
-               cudaStream_t s) {
-    ac_run(syms, counts, stride, jobs, ent, elen, nullptr, s);
+               cudaStream_t s, int* err_dev) {
+    ac_run(syms, counts, stride, jobs, ent, elen, nullptr, s, err_dev);
 }
 
 std::vector<u64> ac_size_bounds(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs,

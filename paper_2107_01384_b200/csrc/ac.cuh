@@ -38,8 +38,11 @@ u64 ac_out_cap(u64 sym_cap, u64 positions);
 
 // Codes every stream: symbols syms[job.sym_off + i], i < counts[j * stride]
 // (device), into ent + job.out_off; elen[j] = total bytes, 0 for no symbols.
+// err_dev (zeroed by the caller): no host sync here -- the flag is set on a
+// model-capacity overflow and the caller checks it with its results; null:
+// checked (synchronously) before returning.
 void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs, u8* ent, u64* elen,
-               cudaStream_t s);
+               cudaStream_t s, int* err_dev = nullptr);
 
 // Bounds [lo, hi] (out[2 j], out[2 j + 1]) on each stream's encode_symbols size from
 // the adaptive model alone (no range recurrence); lo == hi == 0 for no symbols.

@@ -1321,6 +1321,7 @@ struct Coded {
     DevBuf<u8> ent;
     DevBuf<u64> elen;
     DevBuf<u32> scratch;
+    DevBuf<int> err;  // the range coder's capacity flag, read with the lengths
 };
 
 // symbols and raw bits of every stream of the layout (no entropy coding)
@@ -1367,7 +1368,9 @@ void code_streams(Coded& c, const Layout& L, const u64* m, const u8* neg, int co
         c.scratch = DevBuf<u32>(L.scratch_total + 2, s);
         run_rans(c.syms.p, c.so.p, c.dad.p, static_cast<int>(ns), c.ent.p, c.scratch.p, c.elen.p, s);
     } else {
-        ac_encode(c.syms.p, reinterpret_cast<const u64*>(c.so.p), 2, L.jobs, c.ent.p, c.elen.p, s);
+        c.err = DevBuf<int>(1, s);
+        c.err.zero();
+        ac_encode(c.syms.p, reinterpret_cast<const u64*>(c.so.p), 2, L.jobs, c.ent.p, c.elen.p, s, c.err.p);
     }
 }
 
@@ -1410,7 +1413,10 @@ std::vector<u64> probe_entropy_bytes(ProbeCache& c, int p) {
         TCB_CUDA(cudaEventSynchronize(c.done));
         c.el.resize(ns);
         c.c.elen.download(c.el.data(), ns);
+        int herr = 0;
+        if (c.c.err.p) d2h(&herr, c.c.err.p, sizeof(int), c.s);
         stream_sync(c.s);
+        if (herr) throw Error("entropy: device model capacity exceeded");
         for (u64 v : c.el)
             if (v == ~u64{1}) throw Error("entropy: cannot normalize rans table");
         c.ready = true;
@@ -1444,7 +1450,10 @@ bool emit_code(Emitted& E, const u64* m, const u8* neg, u64 n, u64 block, int la
     E.soh.resize(ns);
     E.c.elen.download(E.el.data(), ns);
     E.c.so.download(E.soh.data(), ns);
+    int herr = 0;
+    if (E.c.err.p) d2h(&herr, E.c.err.p, sizeof(int), s);
     stream_sync(s);
+    if (herr) throw Error("entropy: device model capacity exceeded");
     for (u64 v : E.el)
         if (v == ~u64{1}) throw Error("entropy: cannot normalize rans table");
     if (std::getenv("TCB_AC_STATS")) {
