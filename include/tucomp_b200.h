@@ -244,6 +244,11 @@ int tcb_dev_mode_step(const double* b, uint64_t rows, uint64_t cols, double budg
                       double* next, uint64_t* r, double* discarded);
 /* shard-local projection next (cols x r) = b^T u (sthosvd.cpp:158-166). */
 int tcb_dev_ttm(const double* b, uint64_t rows, uint64_t cols, const double* u, uint64_t r, double* next);
+/* the same Gram / projection by the Ozaki scheme on the INT8 tensor cores (five
+ * digit slices per row / column, exact integer recombination; what the mode loop
+ * uses for large unfoldings); any rows / cols / r. */
+int tcb_dev_gram_ozaki(const double* b, uint64_t rows, uint64_t cols, double* g);
+int tcb_dev_ttm_ozaki(const double* b, uint64_t rows, uint64_t cols, const double* u, uint64_t r, double* next);
 /* phases 2-5 of compress_impl (pipeline.cpp:77-189) on a device factorization
  * (core in processing order, factors[i] n_i x r_i row-major). */
 int tcb_dev_encode_tucker(const double* core, const double* const* factors, const uint64_t* n, const uint64_t* r,

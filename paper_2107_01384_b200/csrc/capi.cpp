@@ -891,6 +891,23 @@ int tcb_dev_gram(const double* b, uint64_t rows, uint64_t cols, double* g) {
     });
 }
 
+int tcb_dev_gram_ozaki(const double* b, uint64_t rows, uint64_t cols, double* g) {
+    return guard([&] {
+        Stream st;
+        if (cols == 0) TCB_CUDA(cudaMemsetAsync(g, 0, rows * rows * sizeof(double), st.s));
+        else gram_ozaki(b, rows, cols, g, st.s);
+        stream_sync(st.s);
+    });
+}
+
+int tcb_dev_ttm_ozaki(const double* b, uint64_t rows, uint64_t cols, const double* u, uint64_t r, double* next) {
+    return guard([&] {
+        Stream st;
+        if (cols > 0 && r > 0) ttm_ozaki(b, rows, cols, u, r, next, st.s);
+        stream_sync(st.s);
+    });
+}
+
 int tcb_dev_factor_from_gram(const double* g, uint64_t n, double budget, double* u, uint64_t* r, double* discarded) {
     return guard([&] {
         Stream st;

@@ -53,6 +53,14 @@ void gram_cols_f64(const double* B, u64 rows, u64 cols, double* G, cudaStream_t 
 
 // ---- ttm.cu: out (cols x r, row-major) = B^T U (sthosvd.cpp:158-166), fp64 DMMA.
 void ttm_f64(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s);
+
+// ---- ozaki.cu: the same Gram (full, bitwise symmetric) and TTM by the Ozaki
+// scheme on the INT8 tensor cores (5 digit slices, exact int recombination);
+// used by the mode loop for shapes where it pays (ozaki_*_ok; TCB_OZAKI=0: never).
+bool ozaki_gram_ok(u64 rows, u64 cols);
+bool ozaki_ttm_ok(u64 rows, u64 cols, u64 r);
+void gram_ozaki(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s);
+void ttm_ozaki(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s);
 // out (rows x r) = B V  (B rows x cols row-major, V cols x r row-major); small.
 void gemm_nn_f64(const double* B, u64 rows, u64 cols, const double* V, u64 r, double* out, cudaStream_t s);
 

@@ -373,7 +373,8 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
         DevBuf<double> G;
         if (!gram) {
             G = DevBuf<double>(rows * rows, s);
-            gram_f64(x, rows, cols, G.p, s);
+            if (ozaki_gram_ok(rows, cols)) gram_ozaki(x, rows, cols, G.p, s);
+            else gram_f64(x, rows, cols, G.p, s);
         }
         if (sharded) {  // the columns are spread over the ranks: sum the partial Grams
             if (gram) {
@@ -419,7 +420,8 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
         fix_column_signs(o.U.p, rows, r, s);
     }
     o.next = DevBuf<double>(cols * o.r, s);
-    ttm_f64(x, rows, cols, o.U.p, o.r, o.next.p, s);
+    if (ozaki_ttm_ok(rows, cols, o.r)) ttm_ozaki(x, rows, cols, o.U.p, o.r, o.next.p, s);
+    else ttm_f64(x, rows, cols, o.U.p, o.r, o.next.p, s);
     return o;
 }
 

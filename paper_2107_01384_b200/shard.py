@@ -71,6 +71,22 @@ class DeviceOps:
         _check(lib().tcb_dev_gram(self._p(b2), C.c_uint64(rows), C.c_uint64(cols), self._p(g)))
         return g
 
+    def gram_ozaki(self, b2):
+        rows, cols = b2.shape
+        g = torch.empty((rows, rows), dtype=torch.float64, device=b2.device)
+        torch.cuda.synchronize()
+        _check(lib().tcb_dev_gram_ozaki(self._p(b2), C.c_uint64(rows), C.c_uint64(cols), self._p(g)))
+        return g
+
+    def ttm_ozaki(self, b2, u):
+        rows, cols = b2.shape
+        r = u.shape[1]
+        out = torch.empty((cols, r), dtype=torch.float64, device=b2.device)
+        torch.cuda.synchronize()
+        _check(lib().tcb_dev_ttm_ozaki(self._p(b2), C.c_uint64(rows), C.c_uint64(cols), self._p(u.contiguous()),
+                                       C.c_uint64(r), self._p(out)))
+        return out
+
     def factor_from_gram(self, g, budget):
         n = g.shape[0]
         u = torch.empty(n * n, dtype=torch.float64, device=g.device)
