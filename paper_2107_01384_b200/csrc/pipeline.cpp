@@ -328,7 +328,20 @@ bool topk_factor(const double* G, u64 n, const Budget& bud, cudaStream_t s, u64&
     return false;
 }
 
-StepOut factor_from_gram(const double* G, u64 n, const Budget& bud, cudaStream_t s) {
+// The discarded energy as trace(G) - (kept eigenvalues) instead of the sum of the
+// clipped tail: for a Gram whose null space carries rounding noise of one sign
+// more than the other (the INT8 path's truncated digit products), summing
+// max(0, noise) over hundreds of null eigenvalues biases the tail upwards.
+std::pair<u64, double> pick_rank_trace(const std::vector<double>& s2, double trace, double budget) {
+    if (s2.empty()) throw Error("rank choice: empty singular values");
+    if (budget < 0) throw Error("rank choice: negative budget");
+    u64 r = 0;
+    double kept = 0.0;
+    while (r < s2.size() && std::max(0.0, trace - kept) > budget) kept += s2[r++];
+    return {r, std::max(0.0, trace - kept)};
+}
+
+StepOut factor_from_gram(const double* G, u64 n, const Budget& bud, cudaStream_t s, bool tail_from_trace) {
     {
         StepOut o;
         std::vector<double> s2;
@@ -342,7 +355,7 @@ StepOut factor_from_gram(const double* G, u64 n, const Budget& bud, cudaStream_t
     const auto ev = eig_values(G, n, w, s);
     std::vector<double> s2(n);
     for (u64 j = 0; j < n; ++j) s2[j] = std::max(0.0, ev[j]);
-    auto [r, gone] = pick_rank(s2, budget);
+    auto [r, gone] = tail_from_trace ? pick_rank_trace(s2, gram_trace(G, n, s), budget) : pick_rank(s2, budget);
     const bool tie = rank_tie(s2, r, gone, budget);
     if (r == 0) {  // a budget above the whole mode energy still keeps one vector (sthosvd.cpp:146-150)
         r = 1;
@@ -371,10 +384,15 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
     StepOut o;
     if (via_gram) {
         DevBuf<double> G;
+        bool oz = false;
         if (!gram) {
             G = DevBuf<double>(rows * rows, s);
-            if (ozaki_gram_ok(rows, cols)) gram_ozaki(x, rows, cols, G.p, s);
-            else gram_f64(x, rows, cols, G.p, s);
+            if (ozaki_gram_ok(rows, cols)) {
+                gram_ozaki(x, rows, cols, G.p, s);
+                oz = true;
+            } else {
+                gram_f64(x, rows, cols, G.p, s);
+            }
         }
         if (sharded) {  // the columns are spread over the ranks: sum the partial Grams
             if (gram) {
@@ -384,7 +402,7 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
             shard->allreduce_sum_f64(G.p, rows * rows, s);
             gram = nullptr;
         }
-        o = factor_from_gram(gram ? gram : G.p, rows, budget, s);
+        o = factor_from_gram(gram ? gram : G.p, rows, budget, s, oz);
     } else {  // thin left singular vectors from the Gram of B^T (sthosvd.cpp:91-99)
         EigWork w;
         DevBuf<double> G(cols * cols, s);

@@ -139,7 +139,7 @@ struct Budget {
 StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int backend, cudaStream_t s,
                   const double* gram = nullptr, const ShardComm* shard = nullptr);
 // eigensolve + rank rule + sign fix on an (all-reduced) Gram; U is n x r
-StepOut factor_from_gram(const double* G, u64 n, const Budget& budget, cudaStream_t s);
+StepOut factor_from_gram(const double* G, u64 n, const Budget& budget, cudaStream_t s, bool tail_from_trace = false);
 // sthosvd::compress (sthosvd.cpp:114-171) on a device tensor.  The input is
 // `ext` when non-null (read-only, e.g. the caller's fp64 buffer: with an
 // identity processing order mode 0 reads it in place), else `owned`, which is
