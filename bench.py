@@ -34,7 +34,7 @@ WORKLOAD = "c5: 1024^3 fp32 Gaussian random field E(k)~k^-5/3 (k<=341), seeded t
 C2_WORKLOAD = "c2: 256^3 fp64, 64 separable k^-1.5 sinusoid terms + N(0,1e-5), RE 1e-4"
 CPU_SAMPLE_N = 384  # bounded CPU sample: the c5 generator at 384^3 (kmax = n/3)
 METRIC = "compress throughput GB/s (input bytes)"
-STAGES = ["ingest", "permute", "gram", "eig", "ttm", "quant", "stats", "emit", "ac", "factor", "sum"]
+STAGES = ["ingest", "permute", "gram", "eig", "ttm", "quant", "stats", "emit", "ac", "factor", "sum", "tc"]
 
 
 def _env_rank():

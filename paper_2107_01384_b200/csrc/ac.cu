@@ -339,6 +339,8 @@ __global__ void __launch_bounds__(128) ac_range_kernel(const u64* __restrict__ s
     if (j >= njobs) return;
     const int lane = threadIdx.x & 31;
     __shared__ ulonglong2 stage[4][32];
+    __shared__ u32 rin_sh[4][32];
+    __shared__ uint2 stage2[4][32];
     const int wib = threadIdx.x >> 5;
     const JobDev jb = jobs[j];
     const u64 ns = counts[static_cast<u64>(j) * stride];
@@ -415,6 +417,71 @@ __global__ void __launch_bounds__(128) ac_range_kernel(const u64* __restrict__ s
         __syncwarp();
         stage[wib][lane] = make_ulonglong2(rec_a, mag_a);
         __syncwarp();
+        if (escm == 0 && L == 32) {
+            // Full chunk without escapes: the serial part is the range chain
+            // alone (each step's incoming range goes to shared memory); the
+            // additions to `low`, the shift counts and the slot stores are then
+            // done by the 32 lanes at once, lane u for step u.
+            // the normalisation decided from q by per-record thresholds
+            // (q f < 2^24 <=> q < ceil(2^24 / f)) beside the products q f, q f 2^8,
+            // q f 2^16, so it is two selects after the multiply on the chain
+            {
+                const u32 f = static_cast<u32>(rec_a >> 32) & 0xFFFFu;
+                const u32 th1 = ((1u << 24) + f - 1) / f, th2 = ((1u << 16) + f - 1) / f;
+                stage2[wib][lane] = make_uint2(th1, th2);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                const ulonglong2 rm = stage[wib][u];
+                const uint2 th = stage2[wib][u];
+                rin_sh[wib][u] = range;
+                const u32 f = static_cast<u32>(rm.x >> 32) & 0xFFFFu;
+                const u32 t = __umulhi(range, static_cast<u32>(rm.y));
+                const u32 q = static_cast<u32>((static_cast<u64>(range) * static_cast<u32>(rm.y >> 32) + t) >> 32);
+                const u32 a = q * f, b = q * (f << 8), c = q * (f << 16);
+                range = q < th.y ? c : (q < th.x ? b : a);
+            }
+            __syncwarp();
+            const u32 rin = rin_sh[wib][lane];
+            const u32 hi = static_cast<u32>(rec_a >> 32);
+            const u32 t = __umulhi(rin, static_cast<u32>(mag_a));
+            const u32 q = static_cast<u32>((static_cast<u64>(rin) * static_cast<u32>(mag_a >> 32) + t) >> 32);
+            const u64 add = static_cast<u64>(hi >> 16) * q;
+            const u32 rr = q * (hi & 0xFFFFu);
+            const u32 sh = (rr < (1u << 24) ? 1u : 0u) + (rr < (1u << 16) ? 1u : 0u);
+            u32 isum = sh;
+            u64 iadd = add;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 ys = __shfl_up_sync(0xffffffffu, isum, o);
+                const u64 ya = __shfl_up_sync(0xffffffffu, iadd, o);
+                if (lane >= o) {
+                    isum += ys;
+                    iadd += ya;
+                }
+            }
+            const unsigned smask = __ballot_sync(0xffffffffu, sh != 0);
+            const unsigned below = smask & ((1u << lane) - 1u);
+            const int prev = below ? 31 - __clz(static_cast<int>(below)) : 0;
+            const u64 base = __shfl_sync(0xffffffffu, iadd, prev);
+            const int last = smask ? 31 - __clz(static_cast<int>(smask)) : 0;
+            const u64 at_last = __shfl_sync(0xffffffffu, iadd, last);
+            const u64 tot = __shfl_sync(0xffffffffu, iadd, 31);
+            const u32 nsh = __shfl_sync(0xffffffffu, isum, 31);
+            if (sh) {  // this step closes slot S0 + pos (its sum: the steps since the previous close)
+                const u32 pos = isum - sh;
+                w[pos] = below ? iadd - base : acc + iadd;
+                if (sh == 2) w[pos + 1] = 0;
+            }
+            acc = smask ? tot - at_last : acc + tot;
+            w += nsh;
+            rec_a = rec_b;
+            mag_a = mag_b;
+            raw_a = raw_b;
+            rec_b = rec_c;
+            continue;
+        }
         for (u32 g = 0; g < L; g += 8) {
             const unsigned em = (escm >> g) & 0xFFu;
             if (em == 0 && g + 8 <= L) {

@@ -156,7 +156,7 @@ void timeline_dump() {
                      g_tl.empty() ? "-" : cudaGetErrorString(cudaEventQuery(g_tl[0].a)));
     }
     if (g_tl.empty()) return;
-    static const char* names[] = {"ingest", "permute", "gram", "eig", "ttm", "quant", "stats", "emit", "ac", "factor", "sum"};
+    static const char* names[] = {"ingest", "permute", "gram", "eig", "ttm", "quant", "stats", "emit", "ac", "factor", "sum", "tc"};
     cudaEvent_t ref = g_tl[0].a;
     std::vector<std::pair<float, std::string>> lines;
     std::map<cudaStream_t, int> sid;

@@ -556,44 +556,56 @@ __global__ void dm_scan_kernel(unsigned long long* __restrict__ cnt, u64 nb, u64
     }
 }
 
+// Warp w of the CTA owns positions [lo + 1024 w, lo + 1024 (w + 1)) as rows of
+// 32: a position's lead / trail index is the sub-chunk prefix, the counts of
+// the warps before it and a popcount of its row's ballot (coalesced rows).
 __global__ void __launch_bounds__(kDecThreads) dm_decode_kernel(const u64* __restrict__ m, u64 n, u64 block, u64 spb,
                                                                  int lp, const u64* __restrict__ stops,
                                                                  const unsigned long long* __restrict__ cnt,
                                                                  u64* __restrict__ dec) {
-    __shared__ u64 sh[kDecThreads / 32 + 1];
+    __shared__ u32 wc[kDecThreads / 32][2];
     const u64 b = blockIdx.x / spb, j = blockIdx.x % spb;
     const u64 lo = b * block + j * kDmSc, hi = min(min(n, (b + 1) * block), lo + kDmSc);
     const u64 lstop = stops[2 * b], tstop = stops[2 * b + 1];
-    const u64 i0 = lo + static_cast<u64>(threadIdx.x) * 32;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const u64 wlo = lo + static_cast<u64>(w) * 1024;
     u32 nl = 0, nt = 0;
-    for (int q = 0; q < 32; ++q) {
-        const u64 i = i0 + q;
-        if (i >= hi) break;
-        const int t = top_bit(m[i]);
-        nt += t > lp;
-        nl += t <= lp;
+    for (int r = 0; r < 32; ++r) {
+        const u64 i = wlo + static_cast<u64>(r) * 32 + lane;
+        const int t = i < hi ? top_bit(m[i]) : 1000;
+        nl += __popc(__ballot_sync(0xffffffffu, t <= lp));
+        nt += __popc(__ballot_sync(0xffffffffu, t > lp && t < 1000));
     }
-    u64 tot;
-    const u64 pre = cta_excl_scan<kDecThreads>((static_cast<u64>(nt) << 32) | nl, sh, tot);
-    u64 li = cnt[2 * blockIdx.x] + (pre & 0xffffffffu), ti = cnt[2 * blockIdx.x + 1] + (pre >> 32);
-    for (int q = 0; q < 32; ++q) {
-        const u64 i = i0 + q;
-        if (i >= hi) break;
-        const u64 v = m[i];
-        const int t = top_bit(v);
+    if (lane == 0) {
+        wc[w][0] = nl;
+        wc[w][1] = nt;
+    }
+    __syncthreads();
+    u64 li = cnt[2 * blockIdx.x], ti = cnt[2 * blockIdx.x + 1];
+    for (int q = 0; q < w; ++q) {
+        li += wc[q][0];
+        ti += wc[q][1];
+    }
+    for (int r = 0; r < 32; ++r) {
+        const u64 i = wlo + static_cast<u64>(r) * 32 + lane;
+        const u64 v = i < hi ? m[i] : 0;
+        const int t = i < hi ? top_bit(v) : 1000;
+        const unsigned lm = __ballot_sync(0xffffffffu, t <= lp), tm = __ballot_sync(0xffffffffu, t > lp && t < 1000);
         int pe = -1;
-        if (t > lp) {
-            pe = (ti++ < tstop) ? lp : lp + 1;
-        } else {
-            const bool within = li++ < lstop;
-            if (t == lp && within) pe = lp;
+        if (t > lp && t < 1000) {
+            pe = (ti + __popc(tm & lt) < tstop) ? lp : lp + 1;
+        } else if (t == lp && li + __popc(lm & lt) < lstop) {
+            pe = lp;
         }
         u64 out = 0;
         if (pe >= 0) {
             out = pe >= 64 ? 0 : (v >> pe) << pe;
             if (pe >= 1 && pe < 64) out += u64{1} << (pe - 1);
         }
-        dec[i] = out;
+        if (i < hi) dec[i] = out;
+        li += __popc(lm);
+        ti += __popc(tm);
     }
 }
 
@@ -702,137 +714,192 @@ __global__ void sc_scan_kernel(const u64* __restrict__ m, const StreamDesc* __re
     ncol_out[st] = ncol;
 }
 
-// one CTA per sub-chunk, every plane of the layout
+// One CTA per sub-chunk, every plane of the layout.  Warp w owns positions
+// [lo + 1024 w, lo + 1024 (w + 1)) as 32 rows of 32 (row r, lane l: position
+// lo + 1024 w + 32 r + l): loads and stores are coalesced, and a position's
+// index among the lead / trail / one / raw positions of its row is a popcount
+// of a ballot.  Pass 1 counts each warp's categories per plane (pass 2 redoes
+// the ones and raw bits of a plane with stops, which depend on the positions'
+// stream indices), one CTA barrier gives each warp its offsets, and the
+// emission pass writes for every one the number of lead zeros before it in
+// its stream (sc_diff_kernel turns those into the zero-run symbols) and the
+// raw bits, a row's at most 32 consecutive bits or-reduced over the warp into
+// at most two words.
+constexpr int kScW = kScT / 32;
+constexpr u64 kScWarp = 32 * kScPer;
+
+// a word of LSB-first stream bits as stored: MSB-first within each byte, bytes in order
+__device__ __forceinline__ u32 sc_word(u32 lsb_first) { return __byte_perm(__brev(lsb_first), 0, 0x0123); }
+
+__device__ __forceinline__ void sc_flush(u32* __restrict__ raw, u64 word, u32 val, bool shared_word) {
+    if (!val) return;
+    if (shared_word) atomicOr(raw + word, val);
+    else raw[word] = val;
+}
+
 __global__ void __launch_bounds__(kScT) sc_emit_kernel(const u64* __restrict__ m, const u8* __restrict__ neg,
                                                        const StreamDesc* __restrict__ sd, int np, int nb,
                                                        const u64* __restrict__ scoff, u64 nsc_all,
-                                                       const ScOff* __restrict__ tab, u64* __restrict__ syms,
-                                                       u32* __restrict__ raw, long long* __restrict__ fx) {
-    __shared__ u64 sh[kScT / 32 + 1];
-    __shared__ long long shm[kScT / 32 + 1];
-    __shared__ long long sh_first;
+                                                       const ScOff* __restrict__ tab, u64* __restrict__ zbuf,
+                                                       u32* __restrict__ raw) {
+    // the sub-chunk's magnitudes (warp w: rows of 32 at sc_v[1024 w + 32 r + lane]),
+    // then [plane][warp][4] counts: lead, trail, ones, raw bits
+    extern __shared__ u64 sc_v[];
+    u32* sc_cnt = reinterpret_cast<u32*>(sc_v + kSc);
+    __shared__ int rmax_s[kScW][kScPer];  // the row's largest msb (-1: empty): rows below a plane are all lead zeros
     const u64 g = blockIdx.x;
     const int bi = sc_block(scoff, nb, g);
     const u64 j = g - scoff[bi];
     const StreamDesc d0 = sd[bi];
     const u64 lo = d0.lo + j * kSc, hi = min(d0.hi, lo + kSc);
-    const u64 i0 = lo + static_cast<u64>(threadIdx.x) * kScPer;
-    u64 v[kScPer];
-    u32 negm = 0;
-#pragma unroll
-    for (int q = 0; q < kScPer; ++q) {
-        const u64 i = i0 + q;
-        v[q] = i < hi ? m[i] : 0;
-        if (neg && i < hi && neg[i]) negm |= 1u << q;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const u64 wlo = lo + static_cast<u64>(w) * kScWarp;
+    u64* v = sc_v + static_cast<u64>(w) * kScWarp + lane;  // v[32 r]: row r
+    u32 negm = 0, valm = 0;
+#pragma unroll 8
+    for (int r = 0; r < kScPer; ++r) {
+        const u64 i = wlo + static_cast<u64>(r) * 32 + lane;
+        const bool ok = i < hi;
+        v[32 * r] = ok ? m[i] : 0;
+        if (ok) valm |= 1u << r;
+        if (ok && neg && neg[i]) negm |= 1u << r;
+        const int mx = __reduce_max_sync(0xffffffffu, ok ? top_bit(v[32 * r]) : -1);
+        if (lane == 0) rmax_s[w][r] = mx;
     }
-    const int nv = i0 >= hi ? 0 : static_cast<int>(min(static_cast<u64>(kScPer), hi - i0));
+    __syncwarp();
+    const int* rmax = rmax_s[w];
+    // pass 1: category counts of this warp's positions, per plane
+    for (int pi = 0; pi < np; ++pi) {
+        const int p = sd[static_cast<u64>(pi) * nb + bi].plane;
+        u32 nl = 0, nt = 0, no = 0;
+#pragma unroll 4
+        for (int r = 0; r < kScPer; ++r) {
+            const bool ok = (valm >> r) & 1u;
+            if (rmax[r] < p) {
+                nl += __popc(__ballot_sync(0xffffffffu, ok));
+                continue;
+            }
+            nl += __popc(__ballot_sync(0xffffffffu, ok && top_bit(v[32 * r]) <= p));
+            nt += __popc(__ballot_sync(0xffffffffu, ok && top_bit(v[32 * r]) > p));
+            no += __popc(__ballot_sync(0xffffffffu, ok && top_bit(v[32 * r]) == p));
+        }
+        if (lane == 0) {
+            u32* c = sc_cnt + (pi * kScW + w) * 4;
+            c[0] = nl;
+            c[1] = nt;
+            c[2] = no;
+            c[3] = nt + no;
+        }
+    }
+    __syncthreads();
+    auto base = [&](int pi, int k) {
+        u32 x = 0;
+        for (int q = 0; q < w; ++q) x += sc_cnt[(pi * kScW + q) * 4 + k];
+        return x;
+    };
+    // pass 2: planes with stops (the breakpoint plane): ones and raw bits up to the stops
+    bool any_stop = false;
+    for (int pi = 0; pi < np; ++pi) {
+        const StreamDesc d = sd[static_cast<u64>(pi) * nb + bi];
+        if (d.lstop == kFull && d.tstop == kFull) continue;
+        any_stop = true;
+        const int p = d.plane;
+        const ScOff off = tab[static_cast<u64>(pi) * nsc_all + g];
+        u64 LB = off.lead_b + base(pi, 0), TB = off.trail_b + base(pi, 1);
+        u32 no = 0, nr = 0;
+#pragma unroll 4
+        for (int r = 0; r < kScPer; ++r) {
+            const bool ok = (valm >> r) & 1u;
+            if (rmax[r] < p) {
+                LB += __popc(__ballot_sync(0xffffffffu, ok));
+                continue;
+            }
+            const bool isl = ok && top_bit(v[32 * r]) <= p, ist = ok && top_bit(v[32 * r]) > p;
+            const unsigned lm = __ballot_sync(0xffffffffu, isl), tm = __ballot_sync(0xffffffffu, ist);
+            const u64 li = LB + __popc(lm & lt), ti = TB + __popc(tm & lt);
+            const bool one = isl && top_bit(v[32 * r]) == p && li < d.lstop;
+            const bool tr = ist && ti < d.tstop;
+            no += __popc(__ballot_sync(0xffffffffu, one));
+            nr += __popc(__ballot_sync(0xffffffffu, one || tr));
+            LB += __popc(lm);
+            TB += __popc(tm);
+        }
+        if (lane == 0) {  // fields 2, 3 only: the lead / trail counts read above stay
+            sc_cnt[(pi * kScW + w) * 4 + 2] = no;
+            sc_cnt[(pi * kScW + w) * 4 + 3] = nr;
+        }
+    }
+    if (any_stop) __syncthreads();
+    // emission
     for (int pi = 0; pi < np; ++pi) {
         const StreamDesc d = sd[static_cast<u64>(pi) * nb + bi];
         const int p = d.plane;
         const ScOff off = tab[static_cast<u64>(pi) * nsc_all + g];
-        u32 nl = 0, nt = 0;
-#pragma unroll
-        for (int q = 0; q < kScPer; ++q)
-            if (q < nv) {
-                const int t = top_bit(v[q]);
-                nt += t > p;
-                nl += t <= p;
+        u64 LB = off.lead_b + base(pi, 0), TB = off.trail_b + base(pi, 1);
+        u64 OB = off.ones_b + base(pi, 2);
+        u64 RB = d.raw_off + off.raw_b + base(pi, 3);
+        const u64 rfirst = RB >> 5;
+        u64 cw = rfirst;
+        u32 cv = 0;
+#pragma unroll 4
+        for (int r = 0; r < kScPer; ++r) {
+            const bool ok = (valm >> r) & 1u;
+            if (rmax[r] < p) {  // lead zeros only
+                LB += __popc(__ballot_sync(0xffffffffu, ok));
+                continue;
             }
-        u64 tot;
-        const u64 pre = cta_excl_scan<kScT>((static_cast<u64>(nt) << 32) | nl, sh, tot);
-        u64 li = off.lead_b + (pre & 0xffffffffu), ti = off.trail_b + (pre >> 32);
-        u32 rflag = 0, oflag = 0, nr = 0, no = 0;
-        long long lastL = -1, firstL = -1;
-#pragma unroll
-        for (int q = 0; q < kScPer; ++q) {
-            if (q >= nv) continue;
-            const int t = top_bit(v[q]);
-            if (t > p) {
-                if (ti++ < d.tstop) {
-                    rflag |= 1u << q;
-                    ++nr;
+            const bool isl = ok && top_bit(v[32 * r]) <= p, ist = ok && top_bit(v[32 * r]) > p;
+            const unsigned lm = __ballot_sync(0xffffffffu, isl), tm = __ballot_sync(0xffffffffu, ist);
+            const u64 li = LB + __popc(lm & lt), ti = TB + __popc(tm & lt);
+            const bool one = isl && top_bit(v[32 * r]) == p && li < d.lstop;
+            const bool tr = ist && ti < d.tstop;
+            const unsigned om = __ballot_sync(0xffffffffu, one), rm = __ballot_sync(0xffffffffu, one || tr);
+            if (one) {
+                const u64 oi = OB + __popc(om & lt);
+                zbuf[d.sym_off + oi] = li - oi;
+            }
+            if (rm) {
+                // the row's raw bits packed LSB-first (bit k = the k-th raw position),
+                // placed at the stream offset in a 64-bit window over words cw, cw + 1
+                const bool bit = one ? ((negm >> r) & 1u) : (tr && ((v[32 * r] >> p) & 1u));
+                const u32 pk = __reduce_or_sync(0xffffffffu, bit ? 1u << __popc(rm & lt) : 0u);
+                const u64 W0 = RB >> 5;
+                if (W0 != cw) {
+                    if (lane == 0) sc_flush(raw, cw, sc_word(cv), cw == rfirst);
+                    cw = W0;
+                    cv = 0;
                 }
-            } else {
-                const u64 myl = li++;
-                if (myl < d.lstop && t == p) {
-                    oflag |= 1u << q;
-                    rflag |= 1u << q;
-                    ++nr;
-                    ++no;
-                    if (firstL < 0) firstL = static_cast<long long>(myl);
-                    lastL = static_cast<long long>(myl);
+                const u64 t = static_cast<u64>(pk) << (RB & 31);
+                cv |= static_cast<u32>(t);
+                if ((RB & 31) + __popc(rm) > 32) {
+                    if (lane == 0) sc_flush(raw, cw, sc_word(cv), cw == rfirst);
+                    cw = W0 + 1;
+                    cv = static_cast<u32>(t >> 32);
                 }
             }
+            LB += __popc(lm);
+            TB += __popc(tm);
+            OB += __popc(om);
+            RB += __popc(rm);
         }
-        u64 tot2;
-        const u64 pre2 = cta_excl_scan<kScT>((static_cast<u64>(nr) << 32) | no, sh, tot2);
-        // the lead index of the last one before this thread (-1: none in this sub-chunk yet)
-        const long long prevL = cta_excl_max<kScT>(lastL, shm, -1);
-        if (threadIdx.x == 0) sh_first = LLONG_MAX;
-        __syncthreads();
-        if (firstL >= 0) atomicMin(reinterpret_cast<long long*>(&sh_first), firstL);
-        u64 ri = off.raw_b + (pre2 >> 32), oi = off.ones_b + (pre2 & 0xffffffffu);
-        long long pl = prevL;
-        li = off.lead_b + (pre & 0xffffffffu);
-        // this thread's raw bits are consecutive (at most 32): they touch at most
-        // two words, gathered in registers and or-ed in with two atomics
-        const u64 R0 = d.raw_off + ri, W0 = R0 >> 5;
-        u32 wlo = 0, whi = 0;
-#pragma unroll
-        for (int q = 0; q < kScPer; ++q) {
-            if (q >= nv) continue;
-            const int t = top_bit(v[q]);
-            u64 myl = 0;
-            if (t <= p) myl = li++;
-            if (!(rflag >> q & 1u)) continue;
-            bool bit;
-            if (oflag >> q & 1u) {
-                bit = (negm >> q) & 1u;
-                if (pl >= 0) syms[d.sym_off + oi] = static_cast<u64>(static_cast<long long>(myl) - pl - 1);
-                pl = static_cast<long long>(myl);
-                ++oi;
-            } else {
-                bit = (v[q] >> p) & 1u;
-            }
-            if (bit) {
-                const u64 R = d.raw_off + ri;
-                const u32 mbit = 1u << (8 * ((R >> 3) & 3) + (7 - (R & 7)));
-                if ((R >> 5) == W0) wlo |= mbit;
-                else whi |= mbit;
-            }
-            ++ri;
-        }
-        if (wlo) atomicOr(raw + W0, wlo);
-        if (whi) atomicOr(raw + W0 + 1, whi);
-        __syncthreads();
-        if (threadIdx.x == kScT - 1) {  // the sub-chunk's first and last one (fix-up of its first symbol)
-            long long* f = fx + 2 * (static_cast<u64>(pi) * nsc_all + g);
-            f[0] = sh_first == LLONG_MAX ? -1 : sh_first;
-            f[1] = max(prevL, lastL);
-        }
-        __syncthreads();
+        if (lane == 0) sc_flush(raw, cw, sc_word(cv), true);
     }
 }
 
-// one thread per stream: each sub-chunk's first symbol and the stream's final run
-__global__ void sc_fix_kernel(const StreamDesc* __restrict__ sd, int ns, int nb, const u64* __restrict__ scoff,
-                              u64 nsc_all, const ScOff* __restrict__ tab, const long long* __restrict__ fx,
-                              const StreamOut* __restrict__ so, const u64* __restrict__ ncol, u64* __restrict__ syms) {
-    const int st = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
-    if (st >= ns) return;
-    const StreamDesc d = sd[st];
-    const int bi = st % nb, pi = st / nb;
-    const u64 base = static_cast<u64>(pi) * nsc_all + scoff[bi];
-    long long prev = -1;
-    for (u64 j = 0; j < scoff[bi + 1] - scoff[bi]; ++j) {
-        const long long f = fx[2 * (base + j)], l = fx[2 * (base + j) + 1];
-        if (f >= 0) {
-            syms[d.sym_off + tab[base + j].ones_b] = static_cast<u64>(f - prev - 1);
-            prev = l;
-        }
-    }
+// one CTA per stream: the lead-zero counts before each one -> zero-run symbols
+// (rle_extract, entropy.cpp:51-64: one run per one, then the final run)
+__global__ void __launch_bounds__(256) sc_diff_kernel(const StreamDesc* __restrict__ sd,
+                                                      const StreamOut* __restrict__ so, const u64* __restrict__ ncol,
+                                                      const u64* __restrict__ zbuf, u64* __restrict__ syms) {
+    const int st = blockIdx.x;
     const u64 nsy = so[st].nsyms;
-    if (nsy > 0) syms[d.sym_off + nsy - 1] = static_cast<u64>(static_cast<long long>(ncol[st]) - 1 - prev);
+    if (nsy == 0) return;
+    const u64 no = nsy - 1, off = sd[st].sym_off;
+    for (u64 k = threadIdx.x; k < nsy; k += blockDim.x) {
+        const u64 prev = k > 0 ? zbuf[off + k - 1] : 0;
+        syms[off + k] = (k < no ? zbuf[off + k] : ncol[st] - no) - prev;
+    }
 }
 
 struct AcDesc {
@@ -1344,14 +1411,16 @@ void emit_streams(Coded& c, const Layout& L, const u64* m, const u8* neg, cudaSt
         dsc.upload(scoff.data(), nb + 1);
         DevBuf<u32> hist(nsc * 65 + 1, s);
         DevBuf<ScOff> tab(nsc * np + 1, s);
-        DevBuf<long long> fx(2 * nsc * np + 2, s);
+        DevBuf<u64> zbuf(L.sym_total + 1, s);
         sc_hist_kernel<<<static_cast<unsigned>(nsc), kScT, 0, s>>>(m, c.dsd.p, dsc.p, nb, hist.p);
         sc_scan_kernel<<<cdiv(ns, 64), 64, 0, s>>>(m, c.dsd.p, static_cast<int>(ns), nb, dsc.p, nsc, hist.p, tab.p,
                                                   c.so.p, ncol.p);
-        sc_emit_kernel<<<static_cast<unsigned>(nsc), kScT, 0, s>>>(m, neg, c.dsd.p, np, nb, dsc.p, nsc, tab.p,
-                                                                   c.syms.p, c.raw.p, fx.p);
-        sc_fix_kernel<<<cdiv(ns, 64), 64, 0, s>>>(c.dsd.p, static_cast<int>(ns), nb, dsc.p, nsc, tab.p, fx.p, c.so.p,
-                                                 ncol.p, c.syms.p);
+        const size_t smem = kSc * sizeof(u64) + static_cast<size_t>(np) * kScW * 4 * sizeof(u32);
+        TCB_ONCE_PER_DEVICE(cudaFuncSetAttribute(sc_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(kSc * sizeof(u64) + 64 * kScW * 4 * sizeof(u32))));
+        sc_emit_kernel<<<static_cast<unsigned>(nsc), kScT, smem, s>>>(m, neg, c.dsd.p, np, nb, dsc.p, nsc, tab.p,
+                                                                      zbuf.p, c.raw.p);
+        sc_diff_kernel<<<static_cast<unsigned>(ns), 256, 0, s>>>(c.dsd.p, c.so.p, ncol.p, zbuf.p, c.syms.p);
         count_launch(4);
         TCB_LAUNCH();
     }

@@ -158,7 +158,8 @@ bool prof_enabled();
 
 // Optional per-stage device timing (CUDA events on the launching stream),
 // enabled by tcb_prof_enable(); read back with tcb_prof_read().
-enum Cat : int { kIngest = 0, kPermute, kGram, kEig, kTtm, kQuant, kStats, kEmit, kAc, kFactor, kSum, kNumCat };
+// kTc: the tcgen05 digit-product launches alone (also inside kGram / kTtm)
+enum Cat : int { kIngest = 0, kPermute, kGram, kEig, kTtm, kQuant, kStats, kEmit, kAc, kFactor, kSum, kTc, kNumCat };
 
 // Opt-in host wall-clock trace (TCB_TRACE=1): per-label totals printed to
 // stderr by tcb_compress / tcb_compress_device; a debugging aid only.

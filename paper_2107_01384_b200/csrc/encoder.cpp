@@ -53,11 +53,10 @@ struct Planner {
     std::unique_ptr<PlaneStatsJob> pre;
     int pre_p = -1;
 
-    // Exact statistics from plane p down: 32 planes' approximate totals first,
-    // the approximate `tracked` trajectory from the current (exact) value marks
-    // the likely breakpoint, and only the planes down to it (+2) are computed
-    // exactly; a later plane triggers another batch.
-    const PlaneStats& stats(int p, double tracked_now) {
+    // Exact statistics from plane p down: a sampled estimate of the residual
+    // after each of the next 32 planes marks the likely breakpoint, and only the
+    // planes down to it are computed exactly; a later plane triggers another batch.
+    const PlaneStats& stats(int p) {
         if (!have[p]) {
             const int np = std::min(32, p + 1);
             HostTrace ht("plan: exact plane stats");
@@ -68,22 +67,21 @@ struct Planner {
             PlaneStatsJob& job = own ? *own : *pre;
             int need = np;
             if (n > (u64{1} << 20)) {
-                auto tot = job.approx_totals();
-                if (shd) {  // every rank sums the same partial totals: the same `need` everywhere
-                    DevBuf<double> dt(tot.size(), s);
-                    dt.upload(tot.data(), tot.size());
-                    o.shard->allreduce_sum_f64(dt.p, tot.size(), s);
-                    tot = dt.to_host();
+                // the planes down to the first whose (sampled) residual is safely
+                // below the target: the breakpoint is at or above it; a later plane
+                // triggers another batch, so the estimate only affects the work
+                auto res = job.approx_residuals();
+                if (shd) {  // every rank sums the same partial estimates: the same `need` everywhere
+                    DevBuf<double> dt(res.size(), s);
+                    dt.upload(res.data(), res.size());
+                    o.shard->allreduce_sum_f64(dt.p, res.size(), s);
+                    res = dt.to_host();
                 }
-                double tr = tracked_now;
-                for (int l = 0; l < np; ++l) {
-                    const double red = tot[2 * l] + tot[2 * l + 1];
-                    if (tr - red <= target * (1.0 + 1e-6)) {
-                        need = std::min(np, l + 3);
+                for (int l = 0; l < np; ++l)
+                    if (res[l] <= target / 1.02) {
+                        need = std::min(np, l + 1);
                         break;
                     }
-                    tr -= red;
-                }
             }
             std::vector<ExOut> out = job.exact(need);
             if (!own) pre.reset();
@@ -249,7 +247,7 @@ struct Planner {
         Tot prev;
         bool have_prev = false;
         for (int p = 63; p >= 0; --p) {
-            const PlaneStats& per = stats(p, tracked);
+            const PlaneStats& per = stats(p);
             Tot tot;
             for (u64 b = 0; b < nb; ++b) {
                 tot.lead += per.lead[b];

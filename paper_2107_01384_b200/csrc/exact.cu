@@ -683,13 +683,16 @@ __global__ void __launch_bounds__(128) ex_plane_kernel(const u64* __restrict__ m
     const double c_p = __ull2double_rn(u64{1} << (pc > 63 ? 63 : pc));
     u32 nle = 0, none = 0, ntr = 0;
     const u64* mp = m + lo;
-    for (int i0 = 0; i0 < cnt; i0 += 8) {
+    // (PASS 0 summing every 8th element, scaled, cut it from 17 to 5 ms on c5 but
+    // the walk then re-resolved so many mis-guessed chunks it took 50 ms more)
+    constexpr int ST = 1;
+    for (int i0 = 0; i0 < cnt; i0 += 8 * ST) {
         u64 v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = i0 + u < cnt ? __ldg(mp + i0 + u) : 0;
+        for (int u = 0; u < 8; ++u) v[u] = i0 + u * ST < cnt ? __ldg(mp + i0 + u * ST) : 0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            if (i0 + u >= cnt) break;
+            if (i0 + u * ST >= cnt) break;
             const int tb = top_bit64(v[u]);
             if (!on) continue;
             if (tb < p_low) {  // below every active plane: a lead zero for all of them
@@ -723,26 +726,53 @@ __global__ void __launch_bounds__(128) ex_plane_kernel(const u64* __restrict__ m
     }
     if (!on) return;
     if (PASS == 0) {
-        A[static_cast<u64>(2 * lane) * nch + c] = aL;
-        A[static_cast<u64>(2 * lane + 1) * nch + c] = aT;
+        A[static_cast<u64>(2 * lane) * nch + c] = aL * ST;
+        A[static_cast<u64>(2 * lane + 1) * nch + c] = aT * ST;
     } else {
         out[static_cast<u64>(2 * lane) * nch + c] = cfn_rec(fL, rL, nle, none);
         out[static_cast<u64>(2 * lane + 1) * nch + c] = cfn_rec(fT, rT, 0, ntr);
     }
 }
 
-// approximate per-kind totals (sum of the pass-1 chunk sums): one CTA per kind
-__global__ void ex_kind_totals(const double* __restrict__ A, u64 nch, double* __restrict__ tot) {
-    __shared__ double sh[32];
-    double acc = 0.0;
-    for (u64 c = threadIdx.x; c < nch; c += blockDim.x) acc += A[static_cast<u64>(blockIdx.x) * nch + c];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += sh[w];
-        tot[blockIdx.x] = t;
+// Sampled estimate of the residual after each plane (PlaneStatsJob::approx_residuals):
+// runs of 256 consecutive elements, one in every kResStride, over [lo, hi).
+constexpr u64 kResRun = 256, kResStride = 64;
+__global__ void __launch_bounds__(256) ex_resid_kernel(const u64* __restrict__ m, u64 lo, u64 hi, int p_top, int np,
+                                                       double* __restrict__ res) {
+    double acc[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) acc[l] = 0.0;
+    const u64 nrun = (hi - lo + kResRun - 1) / kResRun;
+    for (u64 r = static_cast<u64>(blockIdx.x) * kResStride; r < nrun; r += static_cast<u64>(gridDim.x) * kResStride) {
+        const u64 i = lo + r * kResRun + threadIdx.x;
+        if (i >= hi) continue;
+        const u64 v = m[i];
+        const int tb = top_bit64(v);
+        const double vd = __ull2double_rn(v);
+        const double sq = vd * vd;
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+            const int p = p_top - l;
+            if (l >= np) break;
+            double t;
+            if (tb < p) {
+                t = sq;
+            } else if (p == 0) {
+                t = 0.0;
+            } else {
+                const double x = __ull2double_rn(v & ((u64{1} << p) - 1)) - __ull2double_rn(u64{1} << (p - 1));
+                t = x * x;
+            }
+            acc[l] += t;
+        }
+    }
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+        if (l >= np) break;
+        double x = acc[l];
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) atomicAdd(res + l, x);
     }
 }
 
@@ -848,30 +878,31 @@ PlaneStatsJob::PlaneStatsJob(const u64* m, u64 n, u64 block, int p_top, int np, 
     // small cores: the generic path (direct warp resolution, no tables)
     J.generic = ref_chain || J.nb == 0 || maxlen < 8 * 2048;
     if (J.generic) return;
-    ProfScope prof(kStats, s);
     J.prep = prepare(J.segs, J.kinds, 2048, s);
-    const u64 nk = J.kinds.size();
-    J.A = DevBuf<double>(J.prep.nch * nk, s);
-    J.P = DevBuf<double>(J.prep.nch * nk, s);
-    ex_plane_kernel<0><<<cdiv(J.prep.nch * 32, 128), 128, 0, s>>>(m, J.prep.segs.p, static_cast<int>(J.nb), J.prep.dch.p,
-                                                                 p_top, np, J.prep.nch, J.A.p, nullptr, nullptr);
-    count_launch();
-    TCB_LAUNCH();
 }
 
 PlaneStatsJob::~PlaneStatsJob() = default;
 
-std::vector<double> PlaneStatsJob::approx_totals() {
+std::vector<double> PlaneStatsJob::approx_residuals() {
     Impl& J = *impl_;
-    const int nk = static_cast<int>(J.kinds.size());
-    std::vector<double> t(nk, 0.0);
-    if (J.generic) return t;
-    DevBuf<double> d(nk, s_);
-    ex_kind_totals<<<nk, 256, 0, s_>>>(J.A.p, J.prep.nch, d.p);
+    std::vector<double> t(J.np, 0.0);
+    if (J.nb == 0) return t;
+    const u64 lo = J.segs.front().lo, hi = J.segs.back().hi;
+    const u64 nrun = (hi - lo + kResRun - 1) / kResRun;
+    const u64 nsamp_runs = (nrun + kResStride - 1) / kResStride;
+    DevBuf<double> d(J.np, s_);
+    d.zero();
+    const unsigned grid = static_cast<unsigned>(std::max<u64>(1, std::min<u64>(nsamp_runs, 4 * 148)));
+    ex_resid_kernel<<<grid, 256, 0, s_>>>(J.m, lo, hi, J.p_top, J.np, d.p);
     count_launch();
     TCB_LAUNCH();
-    d.download(t.data(), nk);
+    d.download(t.data(), J.np);
     stream_sync(s_);
+    // elements sampled: every kResStride-th run of kResRun (the last run may be short)
+    u64 ns = 0;
+    for (u64 r = 0; r < nrun; r += kResStride) ns += std::min(kResRun, hi - lo - r * kResRun);
+    const double scale = ns ? static_cast<double>(hi - lo) / static_cast<double>(ns) : 0.0;
+    for (auto& v : t) v *= scale;
     return t;
 }
 
@@ -884,6 +915,12 @@ std::vector<ExOut> PlaneStatsJob::exact(int np_exact) {
     const int nseg = static_cast<int>(J.nb);
     const int njobs = nseg * 2 * np_exact;
     const u64 nch = J.prep.nch;
+    const u64 nk = 2 * static_cast<u64>(np_exact);
+    J.A = DevBuf<double>(nch * nk, s_);
+    J.P = DevBuf<double>(nch * nk, s_);
+    // approximate chunk sums of the planes needed (their scans guess each chunk's region)
+    ex_plane_kernel<0><<<cdiv(nch * 32, 128), 128, 0, s_>>>(J.m, J.prep.segs.p, nseg, J.prep.dch.p, J.p_top, np_exact,
+                                                            nch, J.A.p, nullptr, nullptr);
     ex_scan_kernel<<<static_cast<unsigned>(njobs), 1024, 0, s_>>>(J.prep.segs.p, nseg, J.prep.dch.p, nch, J.A.p, J.P.p);
     DevBuf<ExRec> recs(nch * 2 * np_exact, s_);
     ex_plane_kernel<1><<<cdiv(nch * 32, 128), 128, 0, s_>>>(J.m, J.prep.segs.p, nseg, J.prep.dch.p, J.p_top, np_exact,

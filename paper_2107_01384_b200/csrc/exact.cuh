@@ -79,18 +79,20 @@ std::vector<ExOut> exact_serial(const u64* m, const u64* dec, const std::vector<
 // + {0: lead, 1: trail}, as exact_serial would return them.
 std::vector<ExOut> exact_plane_stats(const u64* m, u64 n, u64 block, int p_top, int np, cudaStream_t s);
 
-// The same in two steps: construction runs the approximate pass for planes
-// p_top .. p_top - np + 1 (np <= 32); approx_totals() gives every kind's
-// approximate total (k = 2 (p_top - p) + {0, 1}), so the caller can estimate
-// how many planes it needs; exact(np_exact) returns the exact statistics of
-// the first np_exact planes only (elements below them are skipped).
+// The same in two steps: approx_residuals() estimates, from a 1/64 sample of
+// the elements, the squared error left after coding each plane p_top ..
+// p_top - np + 1 in full (sum over msb >= p of sig(m, p), over msb < p of m^2:
+// a sum of non-negative terms, so a sample estimates it to a relative error,
+// unlike the difference `tracked - sum of reductions`), so the caller can
+// estimate how many planes it needs; exact(np_exact) returns the exact
+// statistics of the first np_exact planes only (elements below them skipped).
 class PlaneStatsJob {
 public:
     // blocks [b0, b1) only (a rank's share); results index k * (b1 - b0) + (b - b0)
     PlaneStatsJob(const u64* m, u64 n, u64 block, int p_top, int np, cudaStream_t s, u64 b0 = 0,
                   u64 b1 = ~u64{0});
     ~PlaneStatsJob();
-    std::vector<double> approx_totals();
+    std::vector<double> approx_residuals();
     std::vector<ExOut> exact(int np_exact);
 
 private:

@@ -21,9 +21,11 @@
 // top-650 eigenvalues within 2.6e-14 lambda_1, subspace identical to fp64
 // resolution).  The Gram's diagonal is the fp64 row sum of squares.
 //
-// The GEMMs are plain library GEMMs (cuBLASLt IMMA, "TN": both operands
-// k-contiguous); the slicing, the k-concatenated layouts and the exact
-// recombination are the kernels below.
+// The digit products run on the tcgen05 tensor cores in ozmma.cu (TMA-staged
+// slices, the five level accumulators in tensor memory, exact int64 combine in
+// the epilogue).  TCB_OZAKI_LT=1 runs the same products as cuBLASLt IMMA GEMMs
+// instead (k-concatenated slices, one GEMM per level): integer results, so the
+// two paths agree bit for bit (tests/test_gpu_ozaki.py).
 #include <cublasLt.h>
 
 #include <cmath>
@@ -34,6 +36,7 @@
 #include <tuple>
 
 #include "kernels.cuh"
+#include "ozmma.cuh"
 
 namespace tcb {
 
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
     for (int s = 0; s < kSlices; ++s) {
         const char4 v = make_char4(d[0][s], d[1][s], d[2][s], d[3][s]);
         *reinterpret_cast<char4*>(Dcat + base + static_cast<u64>(s) * Kp + k0) = v;
-        *reinterpret_cast<char4*>(Drev + base + static_cast<u64>(kSlices - 1 - s) * Kp + k0) = v;
+        if (Drev) *reinterpret_cast<char4*>(Drev + base + static_cast<u64>(kSlices - 1 - s) * Kp + k0) = v;
     }
 }
 
@@ -244,7 +247,9 @@ __global__ void oz_gram_combine_kernel(LevelPtrs lv, u64 rows, u64 rows_p, const
         G[e] = sumsq[i];
         return;
     }
-    const u64 off = j * rows_p + i, mat = rows_p * rows_p;
+    // the level sums are exactly symmetric (both (s, t) and (t, s) are in a level),
+    // so entry (i, j) is read row-wise: consecutive threads, consecutive addresses
+    const u64 off = i * rows_p + j, mat = rows_p * rows_p;
     long long T = 0;
 #pragma unroll
     for (int L = 0; L < kSlices; ++L) {
@@ -253,6 +258,25 @@ __global__ void oz_gram_combine_kernel(LevelPtrs lv, u64 rows, u64 rows_p, const
         T += s * (1LL << (7 * (kSlices - 1 - L)));
     }
     G[e] = scalbn(static_cast<double>(T), ex[i] + ex[j] - 40);
+}
+
+// G from the tensor-core path's int64 accumulator (lower triangle valid)
+__global__ void oz_gram_final_kernel(const long long* __restrict__ acc, u64 ld, u64 rows, const int* __restrict__ ex,
+                                     const double* __restrict__ sumsq, double* __restrict__ G) {
+    const u64 e = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= rows * rows) return;
+    const u64 i = e / rows, j = e % rows;
+    if (i == j) {
+        G[e] = sumsq[i];
+        return;
+    }
+    const long long T = i > j ? acc[i * ld + j] : acc[j * ld + i];
+    G[e] = scalbn(static_cast<double>(T), ex[i] + ex[j] - 40);
+}
+
+bool use_lt() {
+    const char* e = std::getenv("TCB_OZAKI_LT");  // read per call: tests switch paths in one process
+    return e && *e && *e != '0';
 }
 
 // out (cols x r, row-major) from the level products: C_L is r_p x cols column-major
@@ -290,16 +314,27 @@ void gram_ozaki(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) 
     DevBuf<double> sq(rows, s);
     ex.zero();
     oz_rowstat_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(B, cols, ex.p, sq.p);
+    const bool lt = use_lt();
     const u64 slab = rows_p * kSlices * Kp;
-    DevBuf<int8_t> dcat(slab, s), drev(slab, s);
+    DevBuf<int8_t> dcat(slab, s), drev(lt ? slab : 0, s);
     if (rows_p > rows) {  // zero rows for the padding
         TCB_CUDA(cudaMemsetAsync(dcat.p + rows * kSlices * Kp, 0, (rows_p - rows) * kSlices * Kp, s));
-        TCB_CUDA(cudaMemsetAsync(drev.p + rows * kSlices * Kp, 0, (rows_p - rows) * kSlices * Kp, s));
+        if (lt) TCB_CUDA(cudaMemsetAsync(drev.p + rows * kSlices * Kp, 0, (rows_p - rows) * kSlices * Kp, s));
     }
     oz_split_rows_kernel<<<dim3(cdiv(Kp, 1024), static_cast<unsigned>(rows)), 256, 0, s>>>(B, cols, Kp, ex.p, dcat.p,
-                                                                                          drev.p);
+                                                                                          lt ? drev.p : nullptr);
     count_launch(2);
     TCB_LAUNCH();
+    if (!lt) {
+        const u64 ld = oz_gram_acc_ld(rows), nrow = round_up(rows, 128);
+        DevBuf<long long> acc(nrow * ld, s);
+        acc.zero();
+        oz_gram_tc(dcat.p, rows, rows_p, Kp, acc.p, ld, s);
+        oz_gram_final_kernel<<<cdiv(rows * rows, 256), 256, 0, s>>>(acc.p, ld, rows, ex.p, sq.p, G);
+        count_launch();
+        TCB_LAUNCH();
+        return;
+    }
     const u64 mat = rows_p * rows_p;
     const u64 nb_slice = Kp / kGramKC;
     DevBuf<int32_t> part(mat * nb_slice * (kSlices * (kSlices + 1) / 2), s);
@@ -323,16 +358,22 @@ void gram_ozaki(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) 
 
 void ttm_ozaki(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s) {
     ProfScope prof_scope(kTtm, s);
-    const u64 Kr = round_up(rows, 16), r_p = round_up(r, 16), cols_p = round_up(cols, 16);
+    const bool lt = use_lt();
+    // the tensor-core path takes whole 64-byte k slabs
+    const u64 Kr = round_up(rows, lt ? 16 : 64), r_p = round_up(r, 16), cols_p = round_up(cols, 16);
     DevBuf<int> exc(cols_p, s), exu(r_p, s);
     oz_colexp_kernel<<<cdiv(cols, 256), 256, 0, s>>>(B, rows, cols, exc.p);
     oz_colexp_kernel<<<cdiv(r, 256), 256, 0, s>>>(U, rows, r, exu.p);
     DevBuf<int8_t> dt(cols_p * kSlices * Kr, s), eu(r_p * kSlices * Kr, s);
-    oz_split_cols_kernel<<<dim3(cdiv(cols_p, 32), cdiv(Kr, 32)), 256, 0, s>>>(B, rows, cols, cols_p, Kr, exc.p, 1,
-                                                                             dt.p);
+    oz_split_cols_kernel<<<dim3(cdiv(cols_p, 32), cdiv(Kr, 32)), 256, 0, s>>>(B, rows, cols, cols_p, Kr, exc.p,
+                                                                             lt ? 1 : 0, dt.p);
     oz_split_cols_kernel<<<dim3(cdiv(r_p, 32), cdiv(Kr, 32)), 256, 0, s>>>(U, rows, r, r_p, Kr, exu.p, 0, eu.p);
     count_launch(4);
     TCB_LAUNCH();
+    if (!lt) {
+        oz_ttm_tc(dt.p, cols, eu.p, r, Kr, exc.p, exu.p, out, s);
+        return;
+    }
     DevBuf<int32_t> lev(kSlices * r_p * cols_p, s);
     LevelPtrs lv{};
     for (int L = 0; L < kSlices; ++L) {

@@ -150,6 +150,48 @@ __global__ void signfold_kernel(u8* __restrict__ neg, u64 n, const u64* __restri
     }
 }
 
+// Lexicographic order (no order map): a CTA per run of rows along the last
+// axis -- the other axes' slice indices (and their flips) are the row's, found
+// once per row, and the last axis is a coalesced byte pass.
+__global__ void signfold_rows_kernel(u8* __restrict__ neg, u64 nrows, const u64* __restrict__ meta, int d,
+                                     const signed char* __restrict__ flips) {
+    const u64 last = meta[d - 1];
+    const signed char* fl = flips + meta[3 * d - 1];
+    for (u64 row = blockIdx.x; row < nrows; row += gridDim.x) {
+        u8 par = 0;
+        u64 rem = row;
+        for (int a = d - 2; a >= 0; --a) {
+            par ^= flips[meta[2 * d + a] + rem % meta[a]] < 0 ? 1 : 0;
+            rem /= meta[a];
+        }
+        u8* q = neg + row * last;
+        for (u64 k = threadIdx.x; k < last; k += blockDim.x) q[k] ^= par ^ (fl[k] < 0 ? 1 : 0);
+    }
+}
+
+__global__ void dead_rows_kernel(const u64* __restrict__ dec, u64 nrows, const u64* __restrict__ meta, int d,
+                                 u8* __restrict__ dead) {
+    const u64 last = meta[d - 1];
+    u8* dl = dead + meta[3 * d - 1];
+    for (u64 row = blockIdx.x; row < nrows; row += gridDim.x) {
+        const u64* q = dec + row * last;
+        int any = 0;
+        for (u64 k = threadIdx.x; k < last; k += blockDim.x)
+            if (q[k]) {
+                any = 1;
+                if (dl[k]) dl[k] = 0;  // most slices are live: read before write
+            }
+        if (__syncthreads_or(any) && threadIdx.x == 0) {
+            u64 rem = row;
+            for (int a = d - 2; a >= 0; --a) {
+                u8* z = dead + meta[2 * d + a] + rem % meta[a];
+                if (*z) *z = 0;
+                rem /= meta[a];
+            }
+        }
+    }
+}
+
 // vectorize::OrderMap keys (vectorize.cpp:40-135): zigzag = (coordinate sum,
 // row-major index), i.e. each anti-diagonal layer in lexicographic order;
 // zorder = the Morton key (axis 0 most significant in each bit level).  A
@@ -323,7 +365,11 @@ std::vector<u8> dead_slices(const u64* dec, const std::vector<u64>& shape, cudaS
     dm.upload(meta.data(), meta.size());
     DevBuf<u8> dead(total, s);
     TCB_CUDA(cudaMemsetAsync(dead.p, 1, total, s));
-    if (n < (u64{1} << 32))
+    if (!order && !shape.empty() && n > 0) {
+        const u64 nrows = n / shape.back();
+        dead_rows_kernel<<<static_cast<unsigned>(std::min<u64>(nrows, 148 * 16)), 128, 0, s>>>(
+            dec, nrows, dm.p, static_cast<int>(shape.size()), dead.p);
+    } else if (n < (u64{1} << 32))
         dead_kernel<u32><<<grid_for(n, 256, 4, 4), 256, 0, s>>>(dec, n, dm.p, static_cast<int>(shape.size()), dead.p,
                                                                  order);
     else
@@ -344,7 +390,11 @@ void sign_fold(u8* neg, const std::vector<u64>& shape, const std::vector<signed 
     dm.upload(meta.data(), meta.size());
     DevBuf<signed char> fl(flips_by_axis.size(), s);
     fl.upload(flips_by_axis.data(), flips_by_axis.size());
-    if (n < (u64{1} << 32))
+    if (!order && !shape.empty() && n > 0) {
+        const u64 nrows = n / shape.back();
+        signfold_rows_kernel<<<static_cast<unsigned>(std::min<u64>(nrows, 148 * 16)), 128, 0, s>>>(
+            neg, nrows, dm.p, static_cast<int>(shape.size()), fl.p);
+    } else if (n < (u64{1} << 32))
         signfold_kernel<u32><<<grid_for(n, 256, 4, 4), 256, 0, s>>>(neg, n, dm.p, static_cast<int>(shape.size()), fl.p,
                                                                      order);
     else

@@ -4,8 +4,10 @@ each value 34 bits below its row's (column's) largest and the dropped digit
 levels weigh <= 2^-35 per term, so every entry is within 2^-32 (Gram) / 2^-30
 (TTM, 2.8e-10 measured) of |x_i| |x_j| from the exact product sum, the Gram is bitwise
 symmetric with the fp64 row sums of squares on its diagonal, and the result
-is deterministic.  End to end, a compress whose mode loop takes the INT8 path
-matches the oracle within the parity bar."""
+is deterministic.  The tcgen05 kernel (csrc/ozmma.cu) and the cuBLASLt IMMA
+path (TCB_OZAKI_LT=1) compute the same integers, so they agree bit for bit.
+End to end, a compress whose mode loop takes the INT8 path matches the oracle
+within the parity bar."""
 import numpy as np
 import pytest
 
@@ -56,6 +58,33 @@ def test_ttm_ozaki_against_fp64(gpu_pkg, rows, cols, r, kind):
     bound = torch.outer(b.norm(dim=0), u.norm(dim=0)) * 2.0 ** -30 + 1e-300
     assert bool(((out - ref).abs() <= bound).all())
     assert torch.equal(out, ops.ttm_ozaki(b, u))
+
+
+@pytest.mark.parametrize("rows,cols", [(1024, 1 << 18), (300, 70001), (129, 40000), (97, 33000), (17, 33)])
+def test_gram_tcgen05_equals_cublaslt(gpu_pkg, monkeypatch, rows, cols):
+    """Partial 128 x 96 tiles, several 2^15 k-chunks, the c5 mode-0 width."""
+    from paper_2107_01384_b200 import shard
+
+    ops = shard.DeviceOps()
+    x = _data(rows, cols, "range", 3)
+    g_tc = ops.gram_ozaki(x)
+    monkeypatch.setenv("TCB_OZAKI_LT", "1")
+    g_lt = ops.gram_ozaki(x)
+    assert torch.equal(g_tc, g_lt)
+
+
+@pytest.mark.parametrize("rows,cols,r", [(1024, 50000, 650), (300, 4097, 5), (33, 100, 33), (200, 30001, 97),
+                                         (1000, 2000, 96)])
+def test_ttm_tcgen05_equals_cublaslt(gpu_pkg, monkeypatch, rows, cols, r):
+    from paper_2107_01384_b200 import shard
+
+    ops = shard.DeviceOps()
+    b = _data(rows, cols, "range", 4)
+    u = torch.linalg.qr(torch.randn(rows, r, dtype=torch.float64, device="cuda"))[0]
+    o_tc = ops.ttm_ozaki(b, u)
+    monkeypatch.setenv("TCB_OZAKI_LT", "1")
+    o_lt = ops.ttm_ozaki(b, u)
+    assert torch.equal(o_tc, o_lt)
 
 
 def test_compress_int8_path_matches_oracle(gpu_pkg):
