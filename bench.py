@@ -410,44 +410,59 @@ def main():
     gram_flop, ttm_flop = algorithmic_work(shape, res.ranks, order)
 
     # ---- the dominant launches, timed live on the launching stream (tcb_prof events):
-    # the mode-0 TTM (largest single launch of the ncu launch list) and the mode-0 Gram,
-    # on the fp64 cast of the resident input (what the pipeline's mode 0 reads)
+    # mode 0's Gram and TTM exactly as the pipeline runs them on c5 (fp64 unfolding ->
+    # Ozaki digit slices -> tcgen05 kind::i8 products in TMEM -> exact int64 combine),
+    # on the fp64 cast of the resident input; "tc" = the tcgen05 kernel alone
     x64 = x.double()
     rows0, cols0, r0 = shape[0], nbytes // 4 // shape[0], res.ranks[0]
     u0 = torch.linalg.qr(torch.randn(rows0, r0, dtype=torch.float64, device=dev))[0].contiguous()
     nxt = torch.empty(cols0 * r0, dtype=torch.float64, device=dev)
     g0 = torch.empty(rows0 * rows0, dtype=torch.float64, device=dev)
-    L.tcb_dev_gram.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
-    L.tcb_dev_ttm.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p]
+    L.tcb_dev_gram_ozaki.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
+    L.tcb_dev_ttm_ozaki.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p]
 
-    def timed(fn, stage, reps=3):
-        out = []
+    def timed(fn, stages, reps=3):
+        out = {k: [] for k in stages}
         for _ in range(reps):
             torch.cuda.synchronize()
             L.tcb_prof_enable(1)
             assert fn() == 0
             L.tcb_prof_enable(0)
             L.tcb_prof_read(ms, cnt, len(STAGES))
-            out.append(ms[STAGES.index(stage)])
-        return float(np.median(out))
+            for k in stages:
+                out[k].append(ms[STAGES.index(k)])
+        return {k: float(np.median(v)) for k, v in out.items()}
 
-    ttm_ms = timed(lambda: L.tcb_dev_ttm(x64.data_ptr(), rows0, cols0, u0.data_ptr(), r0, nxt.data_ptr()), "ttm")
-    gram_ms = timed(lambda: L.tcb_dev_gram(x64.data_ptr(), rows0, cols0, g0.data_ptr()), "gram")
+    tt = timed(lambda: L.tcb_dev_ttm_ozaki(x64.data_ptr(), rows0, cols0, u0.data_ptr(), r0, nxt.data_ptr()),
+               ["ttm", "tc"])
+    tg = timed(lambda: L.tcb_dev_gram_ozaki(x64.data_ptr(), rows0, cols0, g0.data_ptr()), ["gram", "tc"])
     del x64, nxt, g0
     torch.cuda.empty_cache()
     ttm_flop0 = 2.0 * rows0 * cols0 * r0
     gram_flop0 = float(rows0 * (rows0 + 1) * cols0)
-    ach = ttm_flop0 / (ttm_ms * 1e-3) / 1e12
-    roof = {"kernel": "mode-0 TTM (ttm_kernel, 1024 x 1048576 by 1024 x r0, median of 3 live launches)",
-            "bound": "tensor", "achieved": ach, "peak": dmma_peak, "unit": "TFLOP/s", "frac": ach / dmma_peak,
-            "traffic": None, "flop": ttm_flop0, "ms": ttm_ms,
-            "peak_source": "measured fp64 DMMA probe (tcb_peak_dmma_tflops; MEASURED_PEAKS.json has no fp64)",
-            "gram_mode0": {"flop": gram_flop0, "ms": gram_ms, "tflops": gram_flop0 / (gram_ms * 1e-3) / 1e12,
-                           "frac": gram_flop0 / (gram_ms * 1e-3) / 1e12 / dmma_peak},
+    pairs = 15  # digit-slice pairs (s, t) with s + t <= 4 (five slices)
+    int8_peak = 2.0 * float(peaks.get("bf16_tflops", 1652.1))
+    ttm_ops, gram_ops = pairs * ttm_flop0, pairs * gram_flop0
+    ach = ttm_ops / (tt["tc"] * 1e-3) / 1e12
+    roof = {"kernel": "oz_mma_kernel (tcgen05.mma kind::i8, TMA-staged, 5 int32 accumulators in TMEM) for the "
+                      "mode-0 TTM, 1048576 x r0 by 1024 x 5 digit slices, median of 3 live launches",
+            "bound": "tensor", "achieved": ach, "peak": int8_peak, "unit": "TOP/s (int8)", "frac": ach / int8_peak,
+            "traffic": None, "ops": ttm_ops, "ms": tt["tc"],
+            "peak_source": "2 x measured bf16 burst (MEASURED_PEAKS.json): B200 int8 dense runs at twice bf16",
+            "work": "15 slice-pair products of the TTM: 15 * 2 * rows * cols * r int8 ops (algorithmic)",
+            "fp64_equivalent": {"flop": ttm_flop0, "ms_with_split_and_combine": tt["ttm"],
+                                "tflops": ttm_flop0 / (tt["ttm"] * 1e-3) / 1e12, "dmma_peak": dmma_peak,
+                                "frac_of_dmma_peak": ttm_flop0 / (tt["ttm"] * 1e-3) / 1e12 / dmma_peak},
+            "gram_mode0": {"ops": gram_ops, "ms_tc": tg["tc"], "tops": gram_ops / (tg["tc"] * 1e-3) / 1e12,
+                           "frac": gram_ops / (tg["tc"] * 1e-3) / 1e12 / int8_peak,
+                           "work": "15 * rows * (rows + 1) * cols (SYRK count per slice pair)",
+                           "ms_with_split_and_combine": tg["gram"],
+                           "fp64_equivalent_tflops": gram_flop0 / (tg["gram"] * 1e-3) / 1e12,
+                           "frac_of_dmma_peak": gram_flop0 / (tg["gram"] * 1e-3) / 1e12 / dmma_peak},
             "all_modes": {"gram_flop": gram_flop, "gram_ms": stage_ms["gram"], "ttm_flop": ttm_flop,
-                          "ttm_ms": stage_ms["ttm"],
-                          "frac": (gram_flop + ttm_flop) / max(stage_ms["gram"] + stage_ms["ttm"], 1e-9) / 1e9
-                          / dmma_peak}}
+                          "ttm_ms": stage_ms["ttm"], "tc_ms": stage_ms.get("tc"),
+                          "fp64_equivalent_frac_of_dmma_peak": (gram_flop + ttm_flop)
+                          / max(stage_ms["gram"] + stage_ms["ttm"], 1e-9) / 1e9 / dmma_peak}}
     # encoder: B_enc = 2 * 8 * N_core + payload over the stats+emit+ac stages, against HBM
     n_core = int(np.prod(res.ranks))
     b_enc = 2 * 8 * n_core + len(res.container)

@@ -339,8 +339,8 @@ __global__ void __launch_bounds__(128) ac_range_kernel(const u64* __restrict__ s
     if (j >= njobs) return;
     const int lane = threadIdx.x & 31;
     __shared__ ulonglong2 stage[4][32];
+    __shared__ uint4 stage4[4][32];
     __shared__ u32 rin_sh[4][32];
-    __shared__ uint2 stage2[4][32];
     const int wib = threadIdx.x >> 5;
     const JobDev jb = jobs[j];
     const u64 ns = counts[static_cast<u64>(j) * stride];
@@ -423,24 +423,25 @@ __global__ void __launch_bounds__(128) ac_range_kernel(const u64* __restrict__ s
             // additions to `low`, the shift counts and the slot stores are then
             // done by the 32 lanes at once, lane u for step u.
             // the normalisation decided from q by per-record thresholds
-            // (q f < 2^24 <=> q < ceil(2^24 / f)) beside the products q f, q f 2^8,
-            // q f 2^16, so it is two selects after the multiply on the chain
+            // (q f < 2^24 <=> q < ceil(2^24 / f)), so it is a select of the
+            // multiplier beside the quotient; each step's (M, f, thresholds) is one
+            // 16-byte record
             {
                 const u32 f = static_cast<u32>(rec_a >> 32) & 0xFFFFu;
                 const u32 th1 = ((1u << 24) + f - 1) / f, th2 = ((1u << 16) + f - 1) / f;
-                stage2[wib][lane] = make_uint2(th1, th2);
+                stage4[wib][lane] = make_uint4(static_cast<u32>(mag_a), static_cast<u32>(mag_a >> 32),
+                                               f | ((th2 - 1) << 16), th1);
             }
             __syncwarp();
 #pragma unroll
             for (int u = 0; u < 32; ++u) {
-                const ulonglong2 rm = stage[wib][u];
-                const uint2 th = stage2[wib][u];
+                const uint4 d = stage4[wib][u];
                 rin_sh[wib][u] = range;
-                const u32 f = static_cast<u32>(rm.x >> 32) & 0xFFFFu;
-                const u32 t = __umulhi(range, static_cast<u32>(rm.y));
-                const u32 q = static_cast<u32>((static_cast<u64>(range) * static_cast<u32>(rm.y >> 32) + t) >> 32);
-                const u32 a = q * f, b = q * (f << 8), c = q * (f << 16);
-                range = q < th.y ? c : (q < th.x ? b : a);
+                const u32 f = d.z & 0xFFFFu;
+                const u32 t = __umulhi(range, d.x);
+                const u32 q = static_cast<u32>((static_cast<u64>(range) * d.y + t) >> 32);
+                const u32 mul = q <= (d.z >> 16) ? f << 16 : (q < d.w ? f << 8 : f);
+                range = q * mul;
             }
             __syncwarp();
             const u32 rin = rin_sh[wib][lane];

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <limits>
 
 #include "encoder.hpp"
@@ -52,6 +53,41 @@ struct Planner {
     // then runs on a side stream, its one-warp walk beside the batch's passes)
     std::unique_ptr<PlaneStatsJob> pre;
     int pre_p = -1;
+    // The split probe's coder size bounds of the plane above the breakpoint the
+    // sampled residuals predict, computed on a side stream while the exact plane
+    // statistics run (used only when the exact breakpoint is the predicted one:
+    // a full plane's sizes depend on nothing else).
+    struct SpecProbe {
+        int plane = -1;
+        std::future<std::vector<u64>> fut;
+        ~SpecProbe() {
+            if (fut.valid()) fut.wait();
+        }
+    } spec;
+
+    void speculate_probe(int plane) {
+        if (spec.fut.valid() || plane > 63 || plane < 0 || !o.split || o.coder != 0 || o.probe ||
+            (o.shard && o.shard->world > 1))
+            return;
+        static PerDevice<cudaStream_t> side_streams;
+        cudaStream_t side = side_streams.get([] {
+            cudaStream_t x;
+            TCB_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+            return x;
+        });
+        int dev = 0;
+        TCB_CUDA(cudaGetDevice(&dev));
+        EventHandle q;
+        TCB_CUDA(cudaEventRecord(q.e, s));
+        TCB_CUDA(cudaStreamWaitEvent(side, q.e, 0));
+        spec.plane = plane;
+        const u64* mm = m;
+        const u64 nn = n, bl = block;
+        spec.fut = std::async(std::launch::async, [mm, nn, bl, plane, side, dev] {
+            TCB_CUDA(cudaSetDevice(dev));
+            return entropy_size_bounds(mm, nn, bl, plane, side);
+        });
+    }
 
     // Exact statistics from plane p down: a sampled estimate of the residual
     // after each of the next 32 planes marks the likely breakpoint, and only the
@@ -80,6 +116,7 @@ struct Planner {
                 for (int l = 0; l < np; ++l)
                     if (res[l] <= target / 1.02) {
                         need = std::min(np, l + 1);
+                        if (l > 0) speculate_probe(p - l + 1);  // the probe plane of a breakpoint at p - l
                         break;
                     }
             }
@@ -288,7 +325,9 @@ struct Planner {
                         decided = true;
                     } else if (o.coder == 0) {
                         // the coder's size bounds from the model alone usually decide it
-                        const auto b = entropy_size_bounds(m, n, block, p + 1, s, br);
+                        const auto b = spec.fut.valid() && spec.plane == p + 1
+                                           ? spec.fut.get()
+                                           : entropy_size_bounds(m, n, block, p + 1, s, br);
                         std::vector<u64> lh{0, 0};
                         for (std::size_t i = 0; i + 1 < b.size(); i += 2) {
                             lh[0] += b[i] * 8;

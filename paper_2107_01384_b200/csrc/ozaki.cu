@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
     for (int s = 0; s < kSlices; ++s) {
         const char4 v = make_char4(d[0][s], d[1][s], d[2][s], d[3][s]);
         *reinterpret_cast<char4*>(Dcat + base + static_cast<u64>(s) * Kp + k0) = v;
-        if (Drev) *reinterpret_cast<char4*>(Drev + base + static_cast<u64>(kSlices - 1 - s) * Kp + k0) = v;
+        *reinterpret_cast<char4*>(Drev + base + static_cast<u64>(kSlices - 1 - s) * Kp + k0) = v;
     }
 }
 
@@ -229,6 +229,66 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
             const int seg = rev ? kSlices - 1 - s : s;
             out[c * kSlices * Kr + static_cast<u64>(seg) * Kr + k] = t[s][cc][tx];
         }
+    }
+}
+
+// Blocked digit layouts for the tcgen05 path (ozmma.cuh): row i of B split as
+// oz_split_rows_kernel does, written into the 128-row and the 96-row blocking
+// (rows up to either padding are zero); 4 consecutive k per thread.
+__global__ void __launch_bounds__(256) oz_split_rows_blk_kernel(const double* __restrict__ B, u64 rows, u64 cols,
+                                                                u64 nslab, const int* __restrict__ ex,
+                                                                int8_t* __restrict__ DA, u64 rows_a,
+                                                                int8_t* __restrict__ DB, u64 rows_b) {
+    const u64 i = blockIdx.y;
+    const u64 k0 = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if (k0 >= nslab * kOzSlab) return;
+    int8_t d[4][kSlices];
+    const double sc = i < rows ? scalbn(1.0, -ex[i]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const u64 k = k0 + q;
+        const double x = i < rows && k < cols ? B[i * cols + k] : 0.0;
+        digits(x * sc, d[q]);
+    }
+#pragma unroll
+    for (int s = 0; s < kSlices; ++s) {
+        const char4 v = make_char4(d[0][s], d[1][s], d[2][s], d[3][s]);
+        if (i < rows_a) *reinterpret_cast<char4*>(DA + oz_block_off(i, k0, s, kOzBM, nslab)) = v;
+        if (i < rows_b) *reinterpret_cast<char4*>(DB + oz_block_off(i, k0, s, kOzBN, nslab)) = v;
+    }
+}
+
+// Columns of a rows x cols matrix as rows of the blocked layout (block rows br):
+// output row c holds the digits of column c over k < 64 nslab (zero beyond rows
+// and for c >= cols up to the padding).  32 columns x 32 k per CTA through shared
+// memory; each thread writes 4 consecutive k of one column per slice.
+__global__ void __launch_bounds__(256) oz_split_cols_blk_kernel(const double* __restrict__ B, u64 rows, u64 cols,
+                                                                u64 cols_pad, u64 nslab, const int* __restrict__ ex,
+                                                                u32 br, int8_t* __restrict__ out) {
+    __shared__ int8_t t[kSlices][32][36];
+    const u64 c0 = static_cast<u64>(blockIdx.x) * 32, k0 = static_cast<u64>(blockIdx.y) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
+    for (int kk = ty; kk < 32; kk += 8) {
+        const u64 k = k0 + kk, c = c0 + tx;
+        double x = 0.0;
+        int e = 0;
+        if (c < cols) {
+            e = ex[c];
+            if (k < rows) x = B[k * cols + c];
+        }
+        int8_t d[kSlices];
+        digits(x * scalbn(1.0, -e), d);
+#pragma unroll
+        for (int s = 0; s < kSlices; ++s) t[s][tx][kk] = d[s];
+    }
+    __syncthreads();
+    const int cc = threadIdx.x >> 3, kq = (threadIdx.x & 7) * 4;
+    const u64 c = c0 + cc, k = k0 + kq;
+    if (c >= cols_pad || k >= nslab * kOzSlab) return;
+#pragma unroll
+    for (int s = 0; s < kSlices; ++s) {
+        const char4 v = make_char4(t[s][cc][kq], t[s][cc][kq + 1], t[s][cc][kq + 2], t[s][cc][kq + 3]);
+        *reinterpret_cast<char4*>(out + oz_block_off(c, k, s, br, nslab)) = v;
     }
 }
 
@@ -314,27 +374,35 @@ void gram_ozaki(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) 
     DevBuf<double> sq(rows, s);
     ex.zero();
     oz_rowstat_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(B, cols, ex.p, sq.p);
-    const bool lt = use_lt();
-    const u64 slab = rows_p * kSlices * Kp;
-    DevBuf<int8_t> dcat(slab, s), drev(lt ? slab : 0, s);
-    if (rows_p > rows) {  // zero rows for the padding
-        TCB_CUDA(cudaMemsetAsync(dcat.p + rows * kSlices * Kp, 0, (rows_p - rows) * kSlices * Kp, s));
-        if (lt) TCB_CUDA(cudaMemsetAsync(drev.p + rows * kSlices * Kp, 0, (rows_p - rows) * kSlices * Kp, s));
-    }
-    oz_split_rows_kernel<<<dim3(cdiv(Kp, 1024), static_cast<unsigned>(rows)), 256, 0, s>>>(B, cols, Kp, ex.p, dcat.p,
-                                                                                          lt ? drev.p : nullptr);
-    count_launch(2);
+    count_launch();
     TCB_LAUNCH();
-    if (!lt) {
-        const u64 ld = oz_gram_acc_ld(rows), nrow = round_up(rows, 128);
-        DevBuf<long long> acc(nrow * ld, s);
+    if (!use_lt()) {
+        const u64 nslab = Kp / kOzSlab;
+        const u64 ra = oz_block_rows(rows, kOzBM), rb = oz_block_rows(rows, kOzBN);
+        DevBuf<int8_t> da(oz_block_bytes(rows, nslab, kOzBM), s), db(oz_block_bytes(rows, nslab, kOzBN), s);
+        oz_split_rows_blk_kernel<<<dim3(cdiv(Kp, 1024), static_cast<unsigned>(std::max(ra, rb))), 256, 0, s>>>(
+            B, rows, cols, nslab, ex.p, da.p, ra, db.p, rb);
+        count_launch();
+        TCB_LAUNCH();
+        const u64 ld = oz_gram_acc_ld(rows);
+        DevBuf<long long> acc(ra * ld, s);
         acc.zero();
-        oz_gram_tc(dcat.p, rows, rows_p, Kp, acc.p, ld, s);
+        oz_gram_tc(da.p, db.p, rows, nslab, acc.p, ld, s);
         oz_gram_final_kernel<<<cdiv(rows * rows, 256), 256, 0, s>>>(acc.p, ld, rows, ex.p, sq.p, G);
         count_launch();
         TCB_LAUNCH();
         return;
     }
+    const u64 slab = rows_p * kSlices * Kp;
+    DevBuf<int8_t> dcat(slab, s), drev(slab, s);
+    if (rows_p > rows) {  // zero rows for the padding
+        TCB_CUDA(cudaMemsetAsync(dcat.p + rows * kSlices * Kp, 0, (rows_p - rows) * kSlices * Kp, s));
+        TCB_CUDA(cudaMemsetAsync(drev.p + rows * kSlices * Kp, 0, (rows_p - rows) * kSlices * Kp, s));
+    }
+    oz_split_rows_kernel<<<dim3(cdiv(Kp, 1024), static_cast<unsigned>(rows)), 256, 0, s>>>(B, cols, Kp, ex.p, dcat.p,
+                                                                                          drev.p);
+    count_launch();
+    TCB_LAUNCH();
     const u64 mat = rows_p * rows_p;
     const u64 nb_slice = Kp / kGramKC;
     DevBuf<int32_t> part(mat * nb_slice * (kSlices * (kSlices + 1) / 2), s);
@@ -359,21 +427,31 @@ void gram_ozaki(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) 
 void ttm_ozaki(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s) {
     ProfScope prof_scope(kTtm, s);
     const bool lt = use_lt();
-    // the tensor-core path takes whole 64-byte k slabs
-    const u64 Kr = round_up(rows, lt ? 16 : 64), r_p = round_up(r, 16), cols_p = round_up(cols, 16);
+    const u64 r_p = round_up(r, 16), cols_p = round_up(cols, 16);
     DevBuf<int> exc(cols_p, s), exu(r_p, s);
     oz_colexp_kernel<<<cdiv(cols, 256), 256, 0, s>>>(B, rows, cols, exc.p);
     oz_colexp_kernel<<<cdiv(r, 256), 256, 0, s>>>(U, rows, r, exu.p);
-    DevBuf<int8_t> dt(cols_p * kSlices * Kr, s), eu(r_p * kSlices * Kr, s);
-    oz_split_cols_kernel<<<dim3(cdiv(cols_p, 32), cdiv(Kr, 32)), 256, 0, s>>>(B, rows, cols, cols_p, Kr, exc.p,
-                                                                             lt ? 1 : 0, dt.p);
-    oz_split_cols_kernel<<<dim3(cdiv(r_p, 32), cdiv(Kr, 32)), 256, 0, s>>>(U, rows, r, r_p, Kr, exu.p, 0, eu.p);
-    count_launch(4);
-    TCB_LAUNCH();
+    count_launch(2);
     if (!lt) {
-        oz_ttm_tc(dt.p, cols, eu.p, r, Kr, exc.p, exu.p, out, s);
+        const u64 nslab = cdiv(rows, kOzSlab), Kr = nslab * kOzSlab;
+        const u64 ca = oz_block_rows(cols, kOzBM), ub = oz_block_rows(r, kOzBN);
+        DevBuf<int8_t> dt(oz_block_bytes(cols, nslab, kOzBM), s), eu(oz_block_bytes(r, nslab, kOzBN), s);
+        oz_split_cols_blk_kernel<<<dim3(cdiv(ca, 32), cdiv(Kr, 32)), 256, 0, s>>>(B, rows, cols, ca, nslab, exc.p,
+                                                                                kOzBM, dt.p);
+        oz_split_cols_blk_kernel<<<dim3(cdiv(ub, 32), cdiv(Kr, 32)), 256, 0, s>>>(U, rows, r, ub, nslab, exu.p,
+                                                                                kOzBN, eu.p);
+        count_launch(2);
+        TCB_LAUNCH();
+        oz_ttm_tc(dt.p, cols, eu.p, r, nslab, exc.p, exu.p, out, s);
         return;
     }
+    const u64 Kr = round_up(rows, 16);
+    DevBuf<int8_t> dt(cols_p * kSlices * Kr, s), eu(r_p * kSlices * Kr, s);
+    oz_split_cols_kernel<<<dim3(cdiv(cols_p, 32), cdiv(Kr, 32)), 256, 0, s>>>(B, rows, cols, cols_p, Kr, exc.p, 1,
+                                                                             dt.p);
+    oz_split_cols_kernel<<<dim3(cdiv(r_p, 32), cdiv(Kr, 32)), 256, 0, s>>>(U, rows, r, r_p, Kr, exu.p, 0, eu.p);
+    count_launch(2);
+    TCB_LAUNCH();
     DevBuf<int32_t> lev(kSlices * r_p * cols_p, s);
     LevelPtrs lv{};
     for (int L = 0; L < kSlices; ++L) {

@@ -7,9 +7,9 @@
 //
 // * warp 0 (one thread) stages, per 64-byte k slab, the five A slices
 //   (128 rows x 64 B each) and the five B slices (96 rows) into shared memory
-//   with TMA (cp.async.bulk.tensor, 64-byte swizzle), in a 3-stage mbarrier
-//   ring -- 10 tiles feed 15 slice-pair products, so each byte fetched from
-//   L2 is used three times on average;
+//   with two bulk copies (cp.async.bulk: the operands are stored blocked and
+//   pre-swizzled, ozmma.cuh), in a 3-stage mbarrier ring -- 10 tiles feed 15
+//   slice-pair products, so each byte fetched from L2 is used three times;
 // * warp 1 (one thread) issues tcgen05.mma.kind::i8 (M 128, N 96, K 32) for
 //   every pair (s, t), s + t <= 4, into accumulator L = s + t: five int32
 //   128 x 96 accumulators side by side in tensor memory (480 of its 512
@@ -23,8 +23,7 @@
 // int32 is exact per accumulation: |digit| <= 64, so a level-L term is at
 // most (L + 1) 2^12 per k; the Gram runs k-chunks of 2^15 (5 * 2^27 < 2^31),
 // the TTM at most 4096 k per slice.
-#include <cuda.h>
-
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -42,7 +41,8 @@ constexpr u32 kBTile = kTN * kBK;     // 6144 B
 constexpr u32 kStageBytes = kOzSlices * (kATile + kBTile);  // 71680 B
 constexpr u64 kGramKC = u64{1} << 15;  // k per Gram work item (int32-exact)
 constexpr int kThreads = 192;          // producer, MMA, 4 epilogue warps
-constexpr size_t kSmem = static_cast<size_t>(kStages) * kStageBytes + 1024 /* alignment */ + 256 /* barriers */;
+constexpr size_t kSmem = static_cast<size_t>(kStages) * kStageBytes + 4 * 32 * 9 * sizeof(double) /* epilogue staging */ +
+                         1024 /* alignment */ + 256 /* barriers */;
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ u32 smem_u32(const void* p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
@@ -64,12 +64,10 @@ __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(u32 dst, const CUtensorMap* map, int x, int y, u32 bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            dst),
-        "l"(reinterpret_cast<u64>(map)), "r"(x), "r"(y), "r"(bar)
-        : "memory");
+__device__ __forceinline__ void bulk_load(u32 dst, const void* src, u32 bytes, u32 bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(reinterpret_cast<u64>(src)), "r"(bytes), "r"(bar)
+                 : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -109,8 +107,11 @@ constexpr u32 kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<u32>(kT
                        (static_cast<u32>(kTM >> 4) << 24);
 
 struct OzParams {
-    u64 ka, kb;         // bytes between consecutive slices along k (A, B)
-    u32 nslab;          // 64-byte slabs per work item
+    u32 items;          // work items (the grid strides over them)
+    const int8_t* A;    // M operand, 128-row blocks
+    const int8_t* B;    // N operand, 96-row blocks
+    u64 nslab_all;      // slabs per block row (both operands)
+    u32 nslab;          // slabs per work item
     int mode;           // 0: Gram (int64 atomics into acc), 1: TTM (fp64 into out)
     // Gram: item -> (lower-triangle tile, k-chunk), chunk-major
     const int2* tiles;  // (m tile, n tile)
@@ -123,39 +124,44 @@ struct OzParams {
     const int* exa;
     const int* exb;
     double* out;
+    int dbg;  // measurement only (TCB_OZ_DBG): 1 = no loads, 2 = no MMAs
 };
 
-__global__ void __launch_bounds__(kThreads, 1) oz_mma_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                             const __grid_constant__ CUtensorMap tmB,
-                                                             const OzParams P) {
-    extern __shared__ u8 oz_smem_raw[];
-    u8* smem = reinterpret_cast<u8*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t{1023});
-    u64* bars = reinterpret_cast<u64*>(smem + kStages * kStageBytes);  // full[3], empty[3], done
-    u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * kStages + 1);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    int mt, nt;
-    u64 kbase = 0;
+__device__ __forceinline__ void item_coords(const OzParams& P, u32 item, int& mt, int& nt, u64& kbase) {
     if (P.mode == 0) {
-        const u32 t = blockIdx.x % P.ntiles, c = blockIdx.x / P.ntiles;
+        const u32 t = item % P.ntiles, c = item / P.ntiles;
         const int2 tl = P.tiles[t];
         mt = tl.x;
         nt = tl.y;
-        kbase = static_cast<u64>(c) * kGramKC;
+        kbase = static_cast<u64>(c) * (kGramKC / kBK);  // in slabs
     } else {
-        mt = static_cast<int>(blockIdx.x / P.ntn);
-        nt = static_cast<int>(blockIdx.x % P.ntn);
+        mt = static_cast<int>(item / P.ntn);
+        nt = static_cast<int>(item % P.ntn);
+        kbase = 0;
     }
+}
+
+// Persistent: CTA b takes items b, b + grid, ...  The producer runs ahead into
+// the next item's slabs while the last MMAs and the epilogue of the current one
+// finish; the MMA issuer waits for the epilogue to drain the accumulators
+// (tmem_empty) before it starts the next item.
+__global__ void __launch_bounds__(kThreads, 1) oz_mma_kernel(const OzParams P) {
+    extern __shared__ u8 oz_smem_raw[];
+    u8* smem = reinterpret_cast<u8*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t{1023});
+    double* stage_out = reinterpret_cast<double*>(smem + kStages * kStageBytes);  // 4 warps x 32 x 9 doubles
+    u64* bars = reinterpret_cast<u64*>(stage_out + 4 * 32 * 9);  // full[3], empty[3], tmem_full, tmem_empty
+    u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * kStages + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const u32 bar_tfull = smem_u32(&bars[2 * kStages]), bar_tempty = smem_u32(&bars[2 * kStages + 1]);
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kStages; ++i) {
             mbar_init(smem_u32(&bars[i]), 1);
             mbar_init(smem_u32(&bars[kStages + i]), 1);
         }
-        mbar_init(smem_u32(&bars[2 * kStages]), 1);
+        mbar_init(bar_tfull, 1);
+        mbar_init(bar_tempty, 4);  // one arrival per epilogue warp
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmB)) : "memory");
     }
     if (warp == 1) {  // the whole warp allocates the 512 TMEM columns (one CTA per SM)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -169,73 +175,119 @@ __global__ void __launch_bounds__(kThreads, 1) oz_mma_kernel(const __grid_consta
     const u32 sbase = smem_u32(smem);
 
     if (warp == 0 && lane == 0) {
-        // ---------------- TMA producer
-        const int ya = mt * kTM, yb = nt * kTN;
-        for (u32 q = 0; q < P.nslab; ++q) {
-            const u32 st = q % kStages, ph = (q / kStages) & 1u;
-            mbar_wait(smem_u32(&bars[kStages + st]), ph ^ 1u);
-            const u32 full = smem_u32(&bars[st]);
-            mbar_expect_tx(full, kStageBytes);
-            const u32 sa = sbase + st * kStageBytes, sb = sa + kOzSlices * kATile;
-            const u64 k = kbase + static_cast<u64>(q) * kBK;
-#pragma unroll
-            for (int s = 0; s < kOzSlices; ++s) {
-                tma_load_2d(sa + s * kATile, &tmA, static_cast<int>(s * P.ka + k), ya, full);
-                tma_load_2d(sb + s * kBTile, &tmB, static_cast<int>(s * P.kb + k), yb, full);
+        // ---------------- producer: two bulk copies per slab
+        u32 g = 0;  // slab counter over all of this CTA's items (stage ring position)
+        for (u32 item = blockIdx.x; item < P.items; item += gridDim.x) {
+            int mt, nt;
+            u64 kbase;
+            item_coords(P, item, mt, nt, kbase);
+            const int8_t* srcA = P.A + (static_cast<u64>(mt) * P.nslab_all + kbase) * (kOzSlices * kATile);
+            const int8_t* srcB = P.B + (static_cast<u64>(nt) * P.nslab_all + kbase) * (kOzSlices * kBTile);
+            for (u32 q = 0; q < P.nslab; ++q, ++g) {
+                const u32 st = g % kStages, ph = (g / kStages) & 1u;
+                mbar_wait(smem_u32(&bars[kStages + st]), ph ^ 1u);
+                const u32 full = smem_u32(&bars[st]);
+                if (P.dbg == 1) {
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full) : "memory");
+                    continue;
+                }
+                mbar_expect_tx(full, kStageBytes);
+                const u32 sa = sbase + st * kStageBytes, sb = sa + kOzSlices * kATile;
+                bulk_load(sa, srcA + static_cast<u64>(q) * (kOzSlices * kATile), kOzSlices * kATile, full);
+                bulk_load(sb, srcB + static_cast<u64>(q) * (kOzSlices * kBTile), kOzSlices * kBTile, full);
             }
         }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer
-        for (u32 q = 0; q < P.nslab; ++q) {
-            const u32 st = q % kStages, ph = (q / kStages) & 1u;
-            mbar_wait(smem_u32(&bars[st]), ph);
-            tc_fence_after();
-            const u32 sa = sbase + st * kStageBytes, sb = sa + kOzSlices * kATile;
-#pragma unroll
-            for (int L = 0; L < kOzSlices; ++L) {
-#pragma unroll
-                for (int s = 0; s <= L; ++s) {
-                    const u64 da = smem_desc(sa + s * kATile), db = smem_desc(sb + (L - s) * kBTile);
-#pragma unroll
-                    for (int kk = 0; kk < kBK / 32; ++kk)  // K = 32 bytes per MMA: +32 B = +2 in the address field
-                        tc_mma_i8(tmem + L * kTN, da + 2 * kk, db + 2 * kk, kIdesc, (q | s | kk) != 0);
-                }
+        u32 g = 0, it = 0;
+        for (u32 item = blockIdx.x; item < P.items; item += gridDim.x, ++it) {
+            if (it > 0) {  // the epilogue has read the previous item's accumulators
+                mbar_wait(bar_tempty, (it - 1) & 1u);
+                tc_fence_after();
             }
-            tc_commit(smem_u32(&bars[kStages + st]));  // the stage is free once these MMAs have read it
+            for (u32 q = 0; q < P.nslab; ++q, ++g) {
+                const u32 st = g % kStages, ph = (g / kStages) & 1u;
+                mbar_wait(smem_u32(&bars[st]), ph);
+                tc_fence_after();
+                const u32 sa = sbase + st * kStageBytes, sb = sa + kOzSlices * kATile;
+                if (P.dbg != 2) {
+#pragma unroll
+                    for (int L = 0; L < kOzSlices; ++L) {
+#pragma unroll
+                        for (int s = 0; s <= L; ++s) {
+                            const u64 da = smem_desc(sa + s * kATile), db = smem_desc(sb + (L - s) * kBTile);
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 32; ++kk)  // K = 32 bytes per MMA: +32 B = +2 in the address field
+                                tc_mma_i8(tmem + L * kTN, da + 2 * kk, db + 2 * kk, kIdesc, (q | s | kk) != 0);
+                        }
+                    }
+                }
+                tc_commit(smem_u32(&bars[kStages + st]));  // the stage is free once these MMAs have read it
+            }
+            tc_commit(bar_tfull);  // this item's accumulators are complete
         }
-        tc_commit(smem_u32(&bars[2 * kStages]));  // all accumulators complete
     } else if (warp >= 2) {
         // ---------------- epilogue: lane quarter (warp % 4) of the tile's rows
         const int quarter = warp & 3;
-        mbar_wait(smem_u32(&bars[2 * kStages]), 0);
-        tc_fence_after();
-        const u64 m = static_cast<u64>(mt) * kTM + quarter * 32 + lane;
         const u32 trow = tmem + (static_cast<u32>(quarter * 32) << 16);
+        double* stg = stage_out + (warp - 2) * (32 * 9);
+        u32 it = 0;
+        for (u32 item = blockIdx.x; item < P.items; item += gridDim.x, ++it) {
+            int mt, nt;
+            u64 kbase;
+            item_coords(P, item, mt, nt, kbase);
+            mbar_wait(bar_tfull, it & 1u);
+            tc_fence_after();
+            const u64 m0 = static_cast<u64>(mt) * kTM + quarter * 32, m = m0 + lane;
+            const int ea = P.mode == 1 && m < P.m_rows ? P.exa[m] - 40 : 0;
 #pragma unroll 1
-        for (int j0 = 0; j0 < kTN; j0 += 16) {
-            long long T[16];
+            for (int j0 = 0; j0 < kTN; j0 += 16) {
+                long long T[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) T[j] = 0;
+                for (int j = 0; j < 16; ++j) T[j] = 0;
 #pragma unroll
-            for (int L = 0; L < kOzSlices; ++L) {
-                int v[16];
-                tc_ld16(trow + L * kTN + j0, v);
-                tc_wait_ld();
+                for (int L = 0; L < kOzSlices; ++L) {
+                    int v[16];
+                    tc_ld16(trow + L * kTN + j0, v);
+                    tc_wait_ld();
 #pragma unroll
-                for (int j = 0; j < 16; ++j) T[j] += static_cast<long long>(v[j]) << (7 * (kOzSlices - 1 - L));
-            }
-            const u64 n0 = static_cast<u64>(nt) * kTN + j0;
-            if (P.mode == 0) {
-                unsigned long long* a = reinterpret_cast<unsigned long long*>(P.acc + m * P.acc_ld + n0);
+                    for (int j = 0; j < 16; ++j) T[j] += static_cast<long long>(v[j]) << (7 * (kOzSlices - 1 - L));
+                }
+                if (j0 + 16 >= kTN) {  // every accumulator read: the MMA issuer may start the next item
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_tempty) : "memory");
+                }
+                const u64 n0 = static_cast<u64>(nt) * kTN + j0;
+                if (P.mode == 0) {
+                    unsigned long long* a = reinterpret_cast<unsigned long long*>(P.acc + m * P.acc_ld + n0);
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (T[j]) atomicAdd(a + j, static_cast<unsigned long long>(T[j]));
-            } else if (m < P.m_rows) {
-                const int ea = P.exa[m] - 40;
-                double* o = P.out + m * P.n_rows + n0;
+                    for (int j = 0; j < 16; ++j)
+                        if (T[j]) atomicAdd(a + j, static_cast<unsigned long long>(T[j]));
+                    continue;
+                }
+                // TTM: scale by the power of two 2^(exa + exb - 40) (exact: normal results),
+                // then, per 8 columns, 32 rows x 64 B through shared memory (coalesced stores)
+                const int eb = n0 + (lane & 15) < P.n_rows ? P.exb[n0 + (lane & 15)] : 0;
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (n0 + j < P.n_rows) o[j] = scalbn(static_cast<double>(T[j]), ea + P.exb[n0 + j]);
+                for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int e = ea + __shfl_sync(0xffffffffu, eb, 8 * h + j);
+                        const double sc = __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+                        const double x = static_cast<double>(T[8 * h + j]);
+                        stg[lane * 9 + j] = e > -1000 && e < 1000 ? x * sc : scalbn(x, e);
+                    }
+                    __syncwarp();
+                    const int j = lane & 7;
+                    const u64 n = n0 + 8 * h + j;
+#pragma unroll
+                    for (int rr = lane >> 3; rr < 32; rr += 4) {
+                        const u64 mr = m0 + rr;
+                        if (mr < P.m_rows && n < P.n_rows) P.out[mr * P.n_rows + n] = stg[rr * 9 + j];
+                    }
+                    __syncwarp();
+                }
             }
         }
     }
@@ -248,34 +300,9 @@ __global__ void __launch_bounds__(kThreads, 1) oz_mma_kernel(const __grid_consta
 }
 
 // ------------------------------------------------------------------ host side
-using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiled encode_fn() {
-    static EncodeTiled fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        TCB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-        if (!p || q != cudaDriverEntryPointSuccess) throw Error("ozaki: cuTensorMapEncodeTiled unavailable");
-        return reinterpret_cast<EncodeTiled>(p);
-    }();
-    return fn;
-}
-
-// int8 matrix of `rows` rows, `width` bytes each, row pitch `pitch`: 64-byte x box_rows boxes
-CUtensorMap make_map(const int8_t* base, u64 rows, u64 width, u64 pitch, u32 box_rows) {
-    if (reinterpret_cast<uintptr_t>(base) % 16 || pitch % 16) throw Error("ozaki: operand not 16-byte aligned");
-    CUtensorMap m;
-    const cuuint64_t dims[2] = {width, rows};
-    const cuuint64_t strides[1] = {pitch};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), box_rows};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides,
-                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw Error("ozaki: cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
-    return m;
+int dbg_mode() {
+    const char* e = std::getenv("TCB_OZ_DBG");
+    return e ? std::atoi(e) : 0;
 }
 
 void set_smem_attr() {
@@ -287,47 +314,48 @@ void set_smem_attr() {
 
 u64 oz_gram_acc_ld(u64 rows) { return (rows + kTN - 1) / kTN * kTN; }
 
-void oz_gram_tc(const int8_t* D, u64 rows, u64 rows_p, u64 Kp, long long* acc, u64 acc_ld, cudaStream_t s) {
-    if (Kp % kGramKC) throw Error("ozaki: Gram k not a multiple of the chunk");
+void oz_gram_tc(const int8_t* DA, const int8_t* DB, u64 rows, u64 nslab, long long* acc, u64 acc_ld, cudaStream_t s) {
+    if (nslab % (kGramKC / kBK)) throw Error("ozaki: Gram k not a multiple of the chunk");
     set_smem_attr();
-    const u64 pitch = kOzSlices * Kp;
-    const CUtensorMap ma = make_map(D, rows_p, pitch, pitch, kTM);
-    const CUtensorMap mb = make_map(D, rows_p, pitch, pitch, kTN);
     // tiles (a, b) meeting the lower triangle: 96 b <= 128 a + 127
     std::vector<int2> tl;
     const u64 nta = (rows + kTM - 1) / kTM, ntb = (rows + kTN - 1) / kTN;
     for (u64 a = 0; a < nta; ++a)
         for (u64 b = 0; b < ntb; ++b)
             if (b * kTN <= a * kTM + kTM - 1) tl.push_back(make_int2(static_cast<int>(a), static_cast<int>(b)));
+    if (acc_ld < ntb * kTN) throw Error("ozaki: Gram accumulator too narrow");
     DevBuf<int2> dtl(tl.size(), s);
     dtl.upload(tl.data(), tl.size());
     OzParams P{};
-    P.ka = P.kb = Kp;
+    P.A = DA;
+    P.B = DB;
+    P.nslab_all = nslab;
     P.nslab = static_cast<u32>(kGramKC / kBK);
     P.mode = 0;
+    P.dbg = dbg_mode();
     P.tiles = dtl.p;
     P.ntiles = static_cast<u32>(tl.size());
     P.acc = acc;
     P.acc_ld = acc_ld;
-    const u64 items = tl.size() * (Kp / kGramKC);
-    if (acc_ld < ntb * kTN) throw Error("ozaki: Gram accumulator too narrow");
+    const u64 items = tl.size() * (nslab / P.nslab);
+    P.items = static_cast<u32>(items);
     ProfScope prof(kTc, s);
-    oz_mma_kernel<<<static_cast<unsigned>(items), kThreads, kSmem, s>>>(ma, mb, P);
+    oz_mma_kernel<<<static_cast<unsigned>(std::min<u64>(items, sm_count())), kThreads, kSmem, s>>>(P);
     count_launch();
     TCB_LAUNCH();
 }
 
-void oz_ttm_tc(const int8_t* A, u64 m_rows, const int8_t* B, u64 n_rows, u64 Ka, const int* exa, const int* exb,
+void oz_ttm_tc(const int8_t* A, u64 m_rows, const int8_t* B, u64 n_rows, u64 nslab, const int* exa, const int* exb,
                double* out, cudaStream_t s) {
-    if (Ka % kBK || Ka > 4096) throw Error("ozaki: TTM k must be a multiple of 64, at most 4096");
+    if (nslab == 0 || nslab > 64) throw Error("ozaki: TTM k must be at most 4096");
     set_smem_attr();
-    const u64 pitch = kOzSlices * Ka;
-    const CUtensorMap ma = make_map(A, m_rows, pitch, pitch, kTM);
-    const CUtensorMap mb = make_map(B, n_rows, pitch, pitch, kTN);
     OzParams P{};
-    P.ka = P.kb = Ka;
-    P.nslab = static_cast<u32>(Ka / kBK);
+    P.A = A;
+    P.B = B;
+    P.nslab_all = nslab;
+    P.nslab = static_cast<u32>(nslab);
     P.mode = 1;
+    P.dbg = dbg_mode();
     P.ntn = static_cast<u32>((n_rows + kTN - 1) / kTN);
     P.m_rows = m_rows;
     P.n_rows = n_rows;
@@ -335,8 +363,9 @@ void oz_ttm_tc(const int8_t* A, u64 m_rows, const int8_t* B, u64 n_rows, u64 Ka,
     P.exb = exb;
     P.out = out;
     const u64 items = (m_rows + kTM - 1) / kTM * P.ntn;
+    P.items = static_cast<u32>(items);
     ProfScope prof(kTc, s);
-    oz_mma_kernel<<<static_cast<unsigned>(items), kThreads, kSmem, s>>>(ma, mb, P);
+    oz_mma_kernel<<<static_cast<unsigned>(std::min<u64>(items, sm_count())), kThreads, kSmem, s>>>(P);
     count_launch();
     TCB_LAUNCH();
 }

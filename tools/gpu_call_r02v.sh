@@ -1,0 +1,9 @@
+#!/usr/bin/env bash
+set -u
+mkdir -p gpurun_out
+timeout 120 python tools/ac_bench.py 1000000 > gpurun_out/ac_bench_v.log 2>&1
+timeout 300 python tools/timeline.py 1e-2 > gpurun_out/timeline_v.log 2>&1
+cp gpurun_out/timeline.json gpurun_out/timeline_v.json
+timeout 2400 python -m pytest tests -m gpu -q -x --timeout 900 > gpurun_out/t_all_v.log 2>&1
+echo "pytest exit $?" >> gpurun_out/t_all_v.log
+echo done
