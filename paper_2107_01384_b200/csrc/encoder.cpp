@@ -69,10 +69,13 @@ struct Planner {
         if (spec.fut.valid() || plane > 63 || plane < 0 || !o.split || o.coder != 0 || o.probe ||
             (o.shard && o.shard->world > 1))
             return;
+        // highest priority: its CTAs are dispatched ahead of the plane statistics'
         static PerDevice<cudaStream_t> side_streams;
         cudaStream_t side = side_streams.get([] {
+            int lo = 0, hi = 0;
+            TCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
             cudaStream_t x;
-            TCB_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+            TCB_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, hi));
             return x;
         });
         int dev = 0;

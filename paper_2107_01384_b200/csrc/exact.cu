@@ -646,91 +646,148 @@ __device__ __forceinline__ ExRec cfn_rec(const CFn& f, int rid, u32 c0, u32 c1) 
     return r;
 }
 
-// one warp per chunk; PASS 0: approximate sums, PASS 1: chunk functions
+// CFn -> the composable Fn (the same fields cfn_rec writes)
+__device__ __forceinline__ Fn cfn_fn(const CFn& f) {
+    const ExRec r = cfn_rec(f, 0, 0, 0);
+    return Fn{r.K0, r.K1, r.mn0, r.mn1, r.mx0, r.mx1, r.qbad & 3, (r.qbad >> 2) & 1};
+}
+__device__ __forceinline__ Fn fn_shfl_down(const Fn& f, int o) {
+    Fn g;
+    g.K0 = __shfl_down_sync(0xffffffffu, f.K0, o);
+    g.K1 = __shfl_down_sync(0xffffffffu, f.K1, o);
+    g.mn0 = __shfl_down_sync(0xffffffffu, f.mn0, o);
+    g.mn1 = __shfl_down_sync(0xffffffffu, f.mn1, o);
+    g.mx0 = __shfl_down_sync(0xffffffffu, f.mx0, o);
+    g.mx1 = __shfl_down_sync(0xffffffffu, f.mx1, o);
+    g.q = __shfl_down_sync(0xffffffffu, f.q, o);
+    g.bad = __shfl_down_sync(0xffffffffu, f.bad, o);
+    return g;
+}
+// the lanes' functions composed in lane order (lane 0 first); valid in lane 0
+__device__ __forceinline__ Fn fn_warp_compose(Fn f) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const Fn g = fn_shfl_down(f, o);
+        if ((lane & (2 * o - 1)) == 0) f = fn_then(f, g);
+    }
+    return f;
+}
+__device__ __forceinline__ ExRec fn_rec(const Fn& f, int rid, u32 c0, u32 c1) {
+    ExRec r;
+    r.K0 = f.K0;
+    r.K1 = f.K1;
+    r.mn0 = f.mn0;
+    r.mn1 = f.mn1;
+    r.mx0 = f.mx0;
+    r.mx1 = f.mx1;
+    r.rid = rid;
+    r.qbad = (f.q & 3) | (f.bad << 2);
+    r.c0 = c0;
+    r.c1 = c1;
+    return r;
+}
+
+// One warp per 2048-element chunk, staged in shared memory; lane l takes the
+// contiguous run [64 l, 64 l + 64) and the planes one after another: its run's
+// lead and trail functions (PASS 1) or approximate sums (PASS 0) per plane,
+// then the 32 runs are composed (summed) in lane order.  Per plane a lane
+// touches only its elements with msb >= p, so the work follows the active
+// (element, plane) pairs instead of one element at a time across 32 plane lanes.
+constexpr int kPlRun = 64, kPlPad = kPlRun + 1;
 template <int PASS>
 __global__ void __launch_bounds__(128) ex_plane_kernel(const u64* __restrict__ m, const DevSeg* __restrict__ segs,
                                                        int nseg, const u64* __restrict__ choff, int p_top, int np,
                                                        u64 nch, double* __restrict__ A, const double* __restrict__ P,
                                                        ExRec* __restrict__ out) {
     constexpr u64 C = 2048;
+    extern __shared__ u64 ex_sv[];  // 4 warps x 32 runs x kPlPad
     const u64 c = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (c >= nch) return;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 3;
     const int g = seg_of(choff, nseg, c);
     const DevSeg sg = segs[g];
     const u64 lo = sg.lo + (c - choff[g]) * C;
     const int cnt = static_cast<int>(min(C, sg.hi - lo));
-    const int p = p_top - lane;
-    const bool on = lane < np;
-    const int p_low = p_top - np + 1;
-    double aL = 0.0, aT = 0.0;
-    CFn fL = cfn_id(), fT = cfn_id();
-    int rL = 52, rT = 52;
-    double sL = 1.0, sT = 1.0;  // 2^(52 - e) of each function's region
-    if (PASS == 1 && on) {
-        rL = region_of(P[static_cast<u64>(2 * lane) * nch + c]);
-        rT = region_of(P[static_cast<u64>(2 * lane + 1) * nch + c]);
-        sL = scalbn(1.0, 52 - rexp(rL));
-        sT = scalbn(1.0, 52 - rexp(rT));
-    }
-    // the lead and trail gains share one form (terms.cuh):
-    //   t = (double(a) - c)^2 - sig2(m, p),  trail (msb > p): a = m mod 2^(p+1), c = 2^p
-    //                                        lead (msb == p): a = m,            c = 0
-    const int pc = p < 0 ? 0 : p;
-    const u64 mask_p = pc == 0 ? 0 : (u64{1} << pc) - 1;
-    const u64 mask_p1 = pc >= 63 ? ~u64{0} : (u64{1} << (pc + 1)) - 1;
-    const double half_p = pc == 0 ? 0.0 : __ull2double_rn(u64{1} << (pc - 1));
-    const double c_p = __ull2double_rn(u64{1} << (pc > 63 ? 63 : pc));
-    u32 nle = 0, none = 0, ntr = 0;
-    const u64* mp = m + lo;
-    // (PASS 0 summing every 8th element, scaled, cut it from 17 to 5 ms on c5 but
-    // the walk then re-resolved so many mis-guessed chunks it took 50 ms more)
-    constexpr int ST = 1;
-    for (int i0 = 0; i0 < cnt; i0 += 8 * ST) {
-        u64 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = i0 + u * ST < cnt ? __ldg(mp + i0 + u * ST) : 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            if (i0 + u * ST >= cnt) break;
-            const int tb = top_bit64(v[u]);
-            if (!on) continue;
-            if (tb < p_low) {  // below every active plane: a lead zero for all of them
-                nle += 1;
-                continue;
-            }
-            nle += tb <= p;
-            none += tb == p;
-            ntr += tb > p;
-            if (tb < p) continue;
-            const bool tr = tb > p;
-            const double x0 = __dsub_rn(__ull2double_rn(tr ? (v[u] & mask_p1) : v[u]), tr ? c_p : 0.0);
-            const double r0 = __dsub_rn(__ull2double_rn(v[u] & mask_p), half_p);
-            const double t = __dsub_rn(__dmul_rn(x0, x0), pc == 0 ? 0.0 : __dmul_rn(r0, r0));
-            if (PASS == 0) {
-                aT += tr ? t : 0.0;
-                aL += tr ? 0.0 : t;
-            } else if (t != 0.0) {
-                long long j = 0;
-                bool tie = false;
-                const bool ok = unit_fp(t, tr ? sT : sL, j, tie);
-                if (tr) {
-                    if (!ok) fT.bad = 1;
-                    else if (!fT.bad) cfn_push(fT, j, tie);
-                } else {
-                    if (!ok) fL.bad = 1;
-                    else if (!fL.bad) cfn_push(fL, j, tie);
+    u64* v = ex_sv + w * (32 * kPlPad);
+    for (int e = lane; e < static_cast<int>(C); e += 32) v[(e >> 6) * kPlPad + (e & 63)] = e < cnt ? __ldg(m + lo + e) : 0;
+    __syncwarp();
+    const u64* mine = v + lane * kPlPad;
+    const int n_mine = max(0, min(kPlRun, cnt - lane * kPlRun));
+    int tmax = -1;  // the run's largest msb: planes above it see only lead zeros
+    for (int i = 0; i < n_mine; ++i) tmax = max(tmax, top_bit64(mine[i]));
+    for (int l = 0; l < np; ++l) {
+        const int p = p_top - l;
+        // the lead / trail gains share one form (terms.cuh):
+        //   t = (double(a) - c)^2 - sig2(m, p),  trail (msb > p): a = m mod 2^(p+1), c = 2^p
+        //                                        lead (msb == p): a = m,            c = 0
+        const int pc = p < 0 ? 0 : p;
+        const u64 mask_p = pc == 0 ? 0 : (u64{1} << pc) - 1;
+        const u64 mask_p1 = pc >= 63 ? ~u64{0} : (u64{1} << (pc + 1)) - 1;
+        const double half_p = pc == 0 ? 0.0 : __ull2double_rn(u64{1} << (pc - 1));
+        const double c_p = __ull2double_rn(u64{1} << (pc > 63 ? 63 : pc));
+        double aL = 0.0, aT = 0.0;
+        CFn fL = cfn_id(), fT = cfn_id();
+        int rL = 52, rT = 52;
+        double sL = 1.0, sT = 1.0;  // 2^(52 - e) of each function's region
+        if (PASS == 1) {
+            rL = region_of(P[static_cast<u64>(2 * l) * nch + c]);
+            rT = region_of(P[static_cast<u64>(2 * l + 1) * nch + c]);
+            sL = scalbn(1.0, 52 - rexp(rL));
+            sT = scalbn(1.0, 52 - rexp(rT));
+        }
+        u32 nle = 0, none = 0, ntr = 0;
+        if (tmax >= p) {
+            for (int i = 0; i < n_mine; ++i) {
+                const u64 x = mine[i];
+                const int tb = top_bit64(x);
+                if (tb < p) continue;
+                const bool tr = tb > p;
+                none += !tr;
+                ntr += tr;
+                const double x0 = __dsub_rn(__ull2double_rn(tr ? (x & mask_p1) : x), tr ? c_p : 0.0);
+                const double r0 = __dsub_rn(__ull2double_rn(x & mask_p), half_p);
+                const double t = __dsub_rn(__dmul_rn(x0, x0), pc == 0 ? 0.0 : __dmul_rn(r0, r0));
+                if (PASS == 0) {
+                    aT += tr ? t : 0.0;
+                    aL += tr ? 0.0 : t;
+                } else if (t != 0.0) {
+                    long long j = 0;
+                    bool tie = false;
+                    const bool ok = unit_fp(t, tr ? sT : sL, j, tie);
+                    if (tr) {
+                        if (!ok) fT.bad = 1;
+                        else if (!fT.bad) cfn_push(fT, j, tie);
+                    } else {
+                        if (!ok) fL.bad = 1;
+                        else if (!fL.bad) cfn_push(fL, j, tie);
+                    }
                 }
             }
         }
-    }
-    if (!on) return;
-    if (PASS == 0) {
-        A[static_cast<u64>(2 * lane) * nch + c] = aL * ST;
-        A[static_cast<u64>(2 * lane + 1) * nch + c] = aT * ST;
-    } else {
-        out[static_cast<u64>(2 * lane) * nch + c] = cfn_rec(fL, rL, nle, none);
-        out[static_cast<u64>(2 * lane + 1) * nch + c] = cfn_rec(fT, rT, 0, ntr);
+        nle = static_cast<u32>(n_mine) - ntr;  // lead positions: msb <= p
+        if (PASS == 0) {
+            for (int o = 16; o > 0; o >>= 1) {
+                aL += __shfl_down_sync(0xffffffffu, aL, o);
+                aT += __shfl_down_sync(0xffffffffu, aT, o);
+            }
+            if (lane == 0) {
+                A[static_cast<u64>(2 * l) * nch + c] = aL;
+                A[static_cast<u64>(2 * l + 1) * nch + c] = aT;
+            }
+        } else {
+            const Fn FL = fn_warp_compose(cfn_fn(fL));
+            const Fn FT = fn_warp_compose(cfn_fn(fT));
+            for (int o = 16; o > 0; o >>= 1) {
+                nle += __shfl_down_sync(0xffffffffu, nle, o);
+                none += __shfl_down_sync(0xffffffffu, none, o);
+                ntr += __shfl_down_sync(0xffffffffu, ntr, o);
+            }
+            if (lane == 0) {
+                out[static_cast<u64>(2 * l) * nch + c] = fn_rec(FL, rL, nle, none);
+                out[static_cast<u64>(2 * l + 1) * nch + c] = fn_rec(FT, rT, 0, ntr);
+            }
+        }
     }
 }
 
@@ -919,12 +976,17 @@ std::vector<ExOut> PlaneStatsJob::exact(int np_exact) {
     J.A = DevBuf<double>(nch * nk, s_);
     J.P = DevBuf<double>(nch * nk, s_);
     // approximate chunk sums of the planes needed (their scans guess each chunk's region)
-    ex_plane_kernel<0><<<cdiv(nch * 32, 128), 128, 0, s_>>>(J.m, J.prep.segs.p, nseg, J.prep.dch.p, J.p_top, np_exact,
-                                                            nch, J.A.p, nullptr, nullptr);
+    constexpr size_t kPlSmem = 4 * 32 * kPlPad * sizeof(u64);
+    TCB_ONCE_PER_DEVICE(cudaFuncSetAttribute(ex_plane_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kPlSmem));
+                        cudaFuncSetAttribute(ex_plane_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kPlSmem)));
+    ex_plane_kernel<0><<<cdiv(nch * 32, 128), 128, kPlSmem, s_>>>(J.m, J.prep.segs.p, nseg, J.prep.dch.p, J.p_top,
+                                                                  np_exact, nch, J.A.p, nullptr, nullptr);
     ex_scan_kernel<<<static_cast<unsigned>(njobs), 1024, 0, s_>>>(J.prep.segs.p, nseg, J.prep.dch.p, nch, J.A.p, J.P.p);
     DevBuf<ExRec> recs(nch * 2 * np_exact, s_);
-    ex_plane_kernel<1><<<cdiv(nch * 32, 128), 128, 0, s_>>>(J.m, J.prep.segs.p, nseg, J.prep.dch.p, J.p_top, np_exact,
-                                                            nch, nullptr, J.P.p, recs.p);
+    ex_plane_kernel<1><<<cdiv(nch * 32, 128), 128, kPlSmem, s_>>>(J.m, J.prep.segs.p, nseg, J.prep.dch.p, J.p_top,
+                                                                  np_exact, nch, nullptr, J.P.p, recs.p);
     DevBuf<ExOut> d(njobs, s_);
     ex_walk_kernel<64><<<cdiv(static_cast<u64>(njobs) * 32, 128), 128, 0, s_>>>(
         J.m, nullptr, J.prep.segs.p, nseg, J.prep.dch.p, J.prep.dk.p, njobs, nch, recs.p, d.p);

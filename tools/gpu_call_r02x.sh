@@ -1,0 +1,10 @@
+#!/usr/bin/env bash
+set -u
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_exact.py -q -x --timeout 300 > gpurun_out/t_x.log 2>&1
+echo "pytest exit $?" >> gpurun_out/t_x.log
+timeout 300 python tools/timeline.py 1e-2 > gpurun_out/timeline_x.log 2>&1
+cp gpurun_out/timeline.json gpurun_out/timeline_x.json
+timeout 1500 python -m pytest tests/test_gpu_configs.py tests/test_gpu_parity.py -q -x --timeout 900 >> gpurun_out/t_x.log 2>&1
+echo "pytest exit $?" >> gpurun_out/t_x.log
+echo done
