@@ -13,6 +13,6 @@ C5_PROFILE=1 C5_NO_DEC=1 C5_ITERS=2 ncu --profile-from-start off --metrics gpu__
     --clock-control none --csv --log-file gpurun_out/launches.csv python tools/c5_once.py 1e-2 \
     > gpurun_out/ncu_c5.log 2>&1
 C5_PROFILE=1 C5_NO_DEC=1 C5_ITERS=2 ncu --profile-from-start off --set full --import-source on --clock-control none \
-    -k regex:"ttm_kernel|syrk_kernel|ex_plane_kernel|ex_walk_kernel|ac_range_kernel|ac_code_kernel|ac_epoch_kernel|sc_emit|tridiag_coop" \
+    -k regex:"oz_mma_kernel|oz_split_rows_blk|oz_split_cols_blk|ex_plane_kernel|ex_walk_kernel|ac_range_kernel|ac_code_kernel|sc_emit|tridiag_coop|dm_decode" \
     -c 16 -o gpurun_out/full python tools/c5_once.py 1e-2 > gpurun_out/ncu_full.log 2>&1
 echo done

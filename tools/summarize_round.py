@@ -47,6 +47,9 @@ want = {
     "dram__bytes_read.sum": "B",
     "dram__bytes_write.sum": "B",
     "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active": "%",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "%",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "%",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "%",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "%",
     "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed": "%",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "%",
@@ -57,7 +60,8 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "
          "ns": 1e-3, "us": 1, "ms": 1e3}
 ki = hdr.index("Kernel Name")
 lines = ["# ncu --set full --clock-control none on one c5 compress (tools/profile_round.sh; first launches of each)",
-         "# kernel | grid x block | us | DRAM read+write MB | DRAM GB/s | DRAM % elapsed | DMMA pipe % (of active) | SM % | warps active %"]
+         "# kernel | grid x block | us | DRAM read+write MB | DRAM GB/s | DRAM % elapsed | DMMA pipe % (of active) | "
+         "tensor pipe (tcgen05) active % of elapsed | L2 % | SM % | warps active %"]
 for r in data:
     name = r[ki].split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
     vals = {}
@@ -73,8 +77,10 @@ for r in data:
     tb = vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
     lines.append(f"{name:24s} {int(vals['launch__grid_size']):5d} x {int(vals['launch__block_size']):4d} "
                  f"{us:9.1f} {tb / 1e6:9.2f} {tb / us / 1e3:8.1f} "
-                 f"{vals.get('FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed', float('nan')):6.1f} "
+                 f"{vals.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', float('nan')):6.1f} "
                  f"{vals.get('sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active', float('nan')):6.1f} "
+                 f"{vals.get('TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed', float('nan')):6.1f} "
+                 f"{vals.get('lts__throughput.avg.pct_of_peak_sustained_elapsed', float('nan')):6.1f} "
                  f"{vals['sm__throughput.avg.pct_of_peak_sustained_elapsed']:6.1f} "
                  f"{vals['sm__warps_active.avg.pct_of_peak_sustained_active']:6.1f}")
 with open(os.path.join(PROF, f"ncu_{tag}_{sys.argv[3] if len(sys.argv) > 3 else 'full'}_summary.txt"), "w") as f:
