@@ -742,10 +742,10 @@ __global__ void __launch_bounds__(kScT) sc_emit_kernel(const u64* __restrict__ m
                                                        const u64* __restrict__ scoff, u64 nsc_all,
                                                        const ScOff* __restrict__ tab, u64* __restrict__ zbuf,
                                                        u32* __restrict__ raw) {
-    // [plane][warp][4] counts: lead, trail, ones, raw bits; the magnitudes are
-    // re-read per plane from global memory (L1-resident: 64 KB per CTA), which
-    // leaves the shared memory small enough for ~5 CTAs per SM
-    extern __shared__ u32 sc_cnt[];
+    // the sub-chunk's magnitudes (warp w: rows of 32 at sc_v[1024 w + 32 r + lane]),
+    // then [plane][warp][4] counts: lead, trail, ones, raw bits
+    extern __shared__ u64 sc_v[];
+    u32* sc_cnt = reinterpret_cast<u32*>(sc_v + kSc);
     __shared__ int rmax_s[kScW][kScPer];  // the row's largest msb (-1: empty): rows below a plane are all lead zeros
     const u64 g = blockIdx.x;
     const int bi = sc_block(scoff, nb, g);
@@ -755,19 +755,16 @@ __global__ void __launch_bounds__(kScT) sc_emit_kernel(const u64* __restrict__ m
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const u64 wlo = lo + static_cast<u64>(w) * kScWarp;
-    // V(r): row r's magnitude (zero past the sub-chunk's end)
-    const u64 nv = hi > wlo ? hi - wlo : 0;
-    const u64* vsrc = m + wlo + lane;
-    auto V = [&](int r) -> u64 { return static_cast<u64>(r) * 32 + lane < nv ? __ldg(vsrc + 32 * r) : 0; };
+    u64* v = sc_v + static_cast<u64>(w) * kScWarp + lane;  // v[32 r]: row r
     u32 negm = 0, valm = 0;
 #pragma unroll 8
     for (int r = 0; r < kScPer; ++r) {
         const u64 i = wlo + static_cast<u64>(r) * 32 + lane;
         const bool ok = i < hi;
-        const u64 x = V(r);
+        v[32 * r] = ok ? m[i] : 0;
         if (ok) valm |= 1u << r;
         if (ok && neg && neg[i]) negm |= 1u << r;
-        const int mx = __reduce_max_sync(0xffffffffu, ok ? top_bit(x) : -1);
+        const int mx = __reduce_max_sync(0xffffffffu, ok ? top_bit(v[32 * r]) : -1);
         if (lane == 0) rmax_s[w][r] = mx;
     }
     __syncwarp();
@@ -783,9 +780,9 @@ __global__ void __launch_bounds__(kScT) sc_emit_kernel(const u64* __restrict__ m
                 nl += __popc(__ballot_sync(0xffffffffu, ok));
                 continue;
             }
-            nl += __popc(__ballot_sync(0xffffffffu, ok && top_bit(V(r)) <= p));
-            nt += __popc(__ballot_sync(0xffffffffu, ok && top_bit(V(r)) > p));
-            no += __popc(__ballot_sync(0xffffffffu, ok && top_bit(V(r)) == p));
+            nl += __popc(__ballot_sync(0xffffffffu, ok && top_bit(v[32 * r]) <= p));
+            nt += __popc(__ballot_sync(0xffffffffu, ok && top_bit(v[32 * r]) > p));
+            no += __popc(__ballot_sync(0xffffffffu, ok && top_bit(v[32 * r]) == p));
         }
         if (lane == 0) {
             u32* c = sc_cnt + (pi * kScW + w) * 4;
@@ -818,10 +815,10 @@ __global__ void __launch_bounds__(kScT) sc_emit_kernel(const u64* __restrict__ m
                 LB += __popc(__ballot_sync(0xffffffffu, ok));
                 continue;
             }
-            const bool isl = ok && top_bit(V(r)) <= p, ist = ok && top_bit(V(r)) > p;
+            const bool isl = ok && top_bit(v[32 * r]) <= p, ist = ok && top_bit(v[32 * r]) > p;
             const unsigned lm = __ballot_sync(0xffffffffu, isl), tm = __ballot_sync(0xffffffffu, ist);
             const u64 li = LB + __popc(lm & lt), ti = TB + __popc(tm & lt);
-            const bool one = isl && top_bit(V(r)) == p && li < d.lstop;
+            const bool one = isl && top_bit(v[32 * r]) == p && li < d.lstop;
             const bool tr = ist && ti < d.tstop;
             no += __popc(__ballot_sync(0xffffffffu, one));
             nr += __popc(__ballot_sync(0xffffffffu, one || tr));
@@ -852,10 +849,10 @@ __global__ void __launch_bounds__(kScT) sc_emit_kernel(const u64* __restrict__ m
                 LB += __popc(__ballot_sync(0xffffffffu, ok));
                 continue;
             }
-            const bool isl = ok && top_bit(V(r)) <= p, ist = ok && top_bit(V(r)) > p;
+            const bool isl = ok && top_bit(v[32 * r]) <= p, ist = ok && top_bit(v[32 * r]) > p;
             const unsigned lm = __ballot_sync(0xffffffffu, isl), tm = __ballot_sync(0xffffffffu, ist);
             const u64 li = LB + __popc(lm & lt), ti = TB + __popc(tm & lt);
-            const bool one = isl && top_bit(V(r)) == p && li < d.lstop;
+            const bool one = isl && top_bit(v[32 * r]) == p && li < d.lstop;
             const bool tr = ist && ti < d.tstop;
             const unsigned om = __ballot_sync(0xffffffffu, one), rm = __ballot_sync(0xffffffffu, one || tr);
             if (one) {
@@ -865,7 +862,7 @@ __global__ void __launch_bounds__(kScT) sc_emit_kernel(const u64* __restrict__ m
             if (rm) {
                 // the row's raw bits packed LSB-first (bit k = the k-th raw position),
                 // placed at the stream offset in a 64-bit window over words cw, cw + 1
-                const bool bit = one ? ((negm >> r) & 1u) : (tr && ((V(r) >> p) & 1u));
+                const bool bit = one ? ((negm >> r) & 1u) : (tr && ((v[32 * r] >> p) & 1u));
                 const u32 pk = __reduce_or_sync(0xffffffffu, bit ? 1u << __popc(rm & lt) : 0u);
                 const u64 W0 = RB >> 5;
                 if (W0 != cw) {
@@ -1418,7 +1415,9 @@ void emit_streams(Coded& c, const Layout& L, const u64* m, const u8* neg, cudaSt
         sc_hist_kernel<<<static_cast<unsigned>(nsc), kScT, 0, s>>>(m, c.dsd.p, dsc.p, nb, hist.p);
         sc_scan_kernel<<<cdiv(ns, 64), 64, 0, s>>>(m, c.dsd.p, static_cast<int>(ns), nb, dsc.p, nsc, hist.p, tab.p,
                                                   c.so.p, ncol.p);
-        const size_t smem = static_cast<size_t>(np) * kScW * 4 * sizeof(u32);
+        const size_t smem = kSc * sizeof(u64) + static_cast<size_t>(np) * kScW * 4 * sizeof(u32);
+        TCB_ONCE_PER_DEVICE(cudaFuncSetAttribute(sc_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(kSc * sizeof(u64) + 64 * kScW * 4 * sizeof(u32))));
         sc_emit_kernel<<<static_cast<unsigned>(nsc), kScT, smem, s>>>(m, neg, c.dsd.p, np, nb, dsc.p, nsc, tab.p,
                                                                       zbuf.p, c.raw.p);
         sc_diff_kernel<<<static_cast<unsigned>(ns), 256, 0, s>>>(c.dsd.p, c.so.p, ncol.p, zbuf.p, c.syms.p);

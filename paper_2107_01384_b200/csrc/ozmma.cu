@@ -40,9 +40,9 @@ constexpr u32 kATile = kTM * kBK;     // 8192 B
 constexpr u32 kBTile = kTN * kBK;     // 6144 B
 constexpr u32 kStageBytes = kOzSlices * (kATile + kBTile);  // 71680 B
 constexpr u64 kGramKC = u64{1} << 15;  // k per Gram work item (int32-exact)
-constexpr int kThreads = 192;          // producer, MMA, 4 epilogue warps
-constexpr size_t kSmem = static_cast<size_t>(kStages) * kStageBytes + 4 * 32 * 9 * sizeof(double) /* epilogue staging */ +
-                         1024 /* alignment */ + 256 /* barriers */;
+constexpr int kEpiWarps = 8;           // two per TMEM lane quarter, each half of the columns
+constexpr int kThreads = 32 * (2 + kEpiWarps);  // producer, MMA, epilogue
+constexpr size_t kSmem = static_cast<size_t>(kStages) * kStageBytes + 1024 /* alignment */ + 256 /* barriers */;
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ u32 smem_u32(const void* p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
@@ -124,7 +124,7 @@ struct OzParams {
     const int* exa;
     const int* exb;
     double* out;
-    int dbg;  // measurement only (TCB_OZ_DBG): 1 = no loads, 2 = no MMAs
+    int dbg;  // measurement only (TCB_OZ_DBG): 1 = no loads, 2 = no MMAs, 3 = no epilogue
 };
 
 __device__ __forceinline__ void item_coords(const OzParams& P, u32 item, int& mt, int& nt, u64& kbase) {
@@ -148,8 +148,7 @@ __device__ __forceinline__ void item_coords(const OzParams& P, u32 item, int& mt
 __global__ void __launch_bounds__(kThreads, 1) oz_mma_kernel(const OzParams P) {
     extern __shared__ u8 oz_smem_raw[];
     u8* smem = reinterpret_cast<u8*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t{1023});
-    double* stage_out = reinterpret_cast<double*>(smem + kStages * kStageBytes);  // 4 warps x 32 x 9 doubles
-    u64* bars = reinterpret_cast<u64*>(stage_out + 4 * 32 * 9);  // full[3], empty[3], tmem_full, tmem_empty
+    u64* bars = reinterpret_cast<u64*>(smem + kStages * kStageBytes);  // full[3], empty[3], tmem_full, tmem_empty
     u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * kStages + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const u32 bar_tfull = smem_u32(&bars[2 * kStages]), bar_tempty = smem_u32(&bars[2 * kStages + 1]);
@@ -160,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_mma_kernel(const OzParams P) {
             mbar_init(smem_u32(&bars[kStages + i]), 1);
         }
         mbar_init(bar_tfull, 1);
-        mbar_init(bar_tempty, 4);  // one arrival per epilogue warp
+        mbar_init(bar_tempty, kEpiWarps);  // one arrival per epilogue warp
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {  // the whole warp allocates the 512 TMEM columns (one CTA per SM)
@@ -227,10 +226,9 @@ __global__ void __launch_bounds__(kThreads, 1) oz_mma_kernel(const OzParams P) {
             tc_commit(bar_tfull);  // this item's accumulators are complete
         }
     } else if (warp >= 2) {
-        // ---------------- epilogue: lane quarter (warp % 4) of the tile's rows
-        const int quarter = warp & 3;
+        // ---------------- epilogue: lane quarter (warp % 4) of the tile's rows, half of its columns
+        const int quarter = warp & 3, half = (warp - 2) >> 2;
         const u32 trow = tmem + (static_cast<u32>(quarter * 32) << 16);
-        double* stg = stage_out + (warp - 2) * (32 * 9);
         u32 it = 0;
         for (u32 item = blockIdx.x; item < P.items; item += gridDim.x, ++it) {
             int mt, nt;
@@ -238,10 +236,11 @@ __global__ void __launch_bounds__(kThreads, 1) oz_mma_kernel(const OzParams P) {
             item_coords(P, item, mt, nt, kbase);
             mbar_wait(bar_tfull, it & 1u);
             tc_fence_after();
-            const u64 m0 = static_cast<u64>(mt) * kTM + quarter * 32, m = m0 + lane;
+            const u64 m = static_cast<u64>(mt) * kTM + quarter * 32 + lane;
             const int ea = P.mode == 1 && m < P.m_rows ? P.exa[m] - 40 : 0;
+            constexpr int kHalf = kTN / 2;
 #pragma unroll 1
-            for (int j0 = 0; j0 < kTN; j0 += 16) {
+            for (int j0 = half * kHalf; j0 < (half + 1) * kHalf; j0 += 16) {
                 long long T[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) T[j] = 0;
@@ -253,12 +252,14 @@ __global__ void __launch_bounds__(kThreads, 1) oz_mma_kernel(const OzParams P) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) T[j] += static_cast<long long>(v[j]) << (7 * (kOzSlices - 1 - L));
                 }
-                if (j0 + 16 >= kTN) {  // every accumulator read: the MMA issuer may start the next item
+                if (P.dbg == 3 && j0 + 16 < (half + 1) * kHalf) continue;  // measurement: accumulators not drained
+                if (j0 + 16 >= (half + 1) * kHalf) {  // this warp's accumulators read: the next item may start
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_tempty) : "memory");
                 }
                 const u64 n0 = static_cast<u64>(nt) * kTN + j0;
+                if (P.dbg == 3) continue;
                 if (P.mode == 0) {
                     unsigned long long* a = reinterpret_cast<unsigned long long*>(P.acc + m * P.acc_ld + n0);
 #pragma unroll
@@ -266,27 +267,25 @@ __global__ void __launch_bounds__(kThreads, 1) oz_mma_kernel(const OzParams P) {
                         if (T[j]) atomicAdd(a + j, static_cast<unsigned long long>(T[j]));
                     continue;
                 }
-                // TTM: scale by the power of two 2^(exa + exb - 40) (exact: normal results),
-                // then, per 8 columns, 32 rows x 64 B through shared memory (coalesced stores)
-                const int eb = n0 + (lane & 15) < P.n_rows ? P.exb[n0 + (lane & 15)] : 0;
+                if (m >= P.m_rows) continue;
+                // TTM: scale by the power of two 2^(exa + exb - 40) (exact: normal results);
+                // this thread's 16 consecutive outputs of row m, 16 bytes per store
+                double o[16];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int j = 0; j < 16; ++j) {
+                    const int e = ea + (n0 + j < P.n_rows ? __ldg(P.exb + n0 + j) : 0);
+                    const double sc = __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+                    const double x = static_cast<double>(T[j]);
+                    o[j] = e > -1000 && e < 1000 ? x * sc : scalbn(x, e);
+                }
+                double* dst = P.out + m * P.n_rows + n0;
+                if (n0 + 16 <= P.n_rows && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int e = ea + __shfl_sync(0xffffffffu, eb, 8 * h + j);
-                        const double sc = __longlong_as_double(static_cast<long long>(e + 1023) << 52);
-                        const double x = static_cast<double>(T[8 * h + j]);
-                        stg[lane * 9 + j] = e > -1000 && e < 1000 ? x * sc : scalbn(x, e);
-                    }
-                    __syncwarp();
-                    const int j = lane & 7;
-                    const u64 n = n0 + 8 * h + j;
+                    for (int j = 0; j < 16; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(o[j], o[j + 1]);
+                } else {
 #pragma unroll
-                    for (int rr = lane >> 3; rr < 32; rr += 4) {
-                        const u64 mr = m0 + rr;
-                        if (mr < P.m_rows && n < P.n_rows) P.out[mr * P.n_rows + n] = stg[rr * 9 + j];
-                    }
-                    __syncwarp();
+                    for (int j = 0; j < 16; ++j)
+                        if (n0 + j < P.n_rows) dst[j] = o[j];
                 }
             }
         }
