@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(128) ac_range_kernel(const u64* __restrict__ s
     const int lane = threadIdx.x & 31;
     __shared__ ulonglong2 stage[4][32];
     __shared__ uint4 stage4[4][32];
-    __shared__ u32 rin_sh[4][32];
+    __shared__ u32 rin_sh[2][4][32];
     const int wib = threadIdx.x >> 5;
     const JobDev jb = jobs[j];
     const u64 ns = counts[static_cast<u64>(j) * stride];
@@ -406,98 +406,112 @@ __global__ void __launch_bounds__(128) ac_range_kernel(const u64* __restrict__ s
     u64 rec_a = ld_rec(0), rec_b = ld_rec(32);
     u64 mag_a = magic[rec_a & 0xFFFFu];
     u32 raw_a = ld_raw(0, rec_a);
+    // Full chunks without escapes run software-pipelined: the range chain of
+    // chunk k (32 dependent steps, each step's incoming range kept per lane)
+    // sits in one basic block with the parallel part of chunk k - 1 (the
+    // additions to `low`, shift counts and slot stores by the 32 lanes), whose
+    // independent instructions fill the chain's latency gaps.  A chunk with an
+    // escape (or the partial last one) first completes the pending parallel
+    // part, then steps serially.
+    bool pend = false;          // a chunk's parallel part is pending
+    u32 p_rin = 0;              // its lane's incoming range
+    u64 p_rec = 0, p_mag = 0;   // its lane's record and reciprocal
+    int buf = 0;
+    auto finish = [&](u32 rin, u64 rec, u64 mag) {  // the parallel part of one chunk
+        const u32 hi = static_cast<u32>(rec >> 32);
+        const u32 t = __umulhi(rin, static_cast<u32>(mag));
+        const u32 q = static_cast<u32>((static_cast<u64>(rin) * static_cast<u32>(mag >> 32) + t) >> 32);
+        const u64 add = static_cast<u64>(hi >> 16) * q;
+        const u32 rr = q * (hi & 0xFFFFu);
+        const u32 sh = (rr < (1u << 24) ? 1u : 0u) + (rr < (1u << 16) ? 1u : 0u);
+        u32 isum = sh;
+        u64 iadd = add;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 ys = __shfl_up_sync(0xffffffffu, isum, o);
+            const u64 ya = __shfl_up_sync(0xffffffffu, iadd, o);
+            if (lane >= o) {
+                isum += ys;
+                iadd += ya;
+            }
+        }
+        const unsigned smask = __ballot_sync(0xffffffffu, sh != 0);
+        const unsigned below = smask & ((1u << lane) - 1u);
+        const int prev = below ? 31 - __clz(static_cast<int>(below)) : 0;
+        const u64 base = __shfl_sync(0xffffffffu, iadd, prev);
+        const int last = smask ? 31 - __clz(static_cast<int>(smask)) : 0;
+        const u64 at_last = __shfl_sync(0xffffffffu, iadd, last);
+        const u64 tot = __shfl_sync(0xffffffffu, iadd, 31);
+        const u32 nsh = __shfl_sync(0xffffffffu, isum, 31);
+        if (sh) {  // this step closes slot S0 + pos (its sum: the steps since the previous close)
+            const u32 pos = isum - sh;
+            w[pos] = below ? iadd - base : acc + iadd;
+            if (sh == 2) w[pos + 1] = 0;
+        }
+        acc = smask ? tot - at_last : acc + tot;
+        w += nsh;
+    };
     for (u64 k0 = 0; k0 < n1; k0 += 32) {
         const u64 rec_c = ld_rec(k0 + 64);
         const u64 mag_b = magic[rec_b & 0xFFFFu];
         const u32 raw_b = ld_raw(k0 + 32, rec_b);
         const u32 L = static_cast<u32>(min(u64{32}, n1 - k0));
         const unsigned escm = __ballot_sync(0xffffffffu, (rec_a >> 16) & 1u);
-        // the chunk's (record, reciprocal) pairs go through shared memory: the
-        // steps read them with broadcast loads the compiler issues ahead
-        __syncwarp();
-        stage[wib][lane] = make_ulonglong2(rec_a, mag_a);
-        __syncwarp();
         if (escm == 0 && L == 32) {
-            // Full chunk without escapes: the serial part is the range chain
-            // alone (each step's incoming range goes to shared memory); the
-            // additions to `low`, the shift counts and the slot stores are then
-            // done by the 32 lanes at once, lane u for step u.
-            // the normalisation decided from q by per-record thresholds
-            // (q f < 2^24 <=> q < ceil(2^24 / f)), so it is a select of the
-            // multiplier beside the quotient; each step's (M, f, thresholds) is one
-            // 16-byte record
+            // per-step 16-byte records: reciprocal, and the normalisation decided
+            // from q by thresholds (q f < 2^24 <=> q < ceil(2^24 / f)), so it is a
+            // select of the multiplier beside the quotient
             {
                 const u32 f = static_cast<u32>(rec_a >> 32) & 0xFFFFu;
                 const u32 th1 = ((1u << 24) + f - 1) / f, th2 = ((1u << 16) + f - 1) / f;
+                __syncwarp();
                 stage4[wib][lane] = make_uint4(static_cast<u32>(mag_a), static_cast<u32>(mag_a >> 32),
                                                f | ((th2 - 1) << 16), th1);
+                __syncwarp();
             }
-            __syncwarp();
 #pragma unroll
             for (int u = 0; u < 32; ++u) {
                 const uint4 d = stage4[wib][u];
-                rin_sh[wib][u] = range;
+                rin_sh[buf][wib][u] = range;
                 const u32 f = d.z & 0xFFFFu;
                 const u32 t = __umulhi(range, d.x);
                 const u32 q = static_cast<u32>((static_cast<u64>(range) * d.y + t) >> 32);
                 const u32 mul = q <= (d.z >> 16) ? f << 16 : (q < d.w ? f << 8 : f);
                 range = q * mul;
             }
+            if (pend) finish(p_rin, p_rec, p_mag);  // the previous chunk, beside this chain
             __syncwarp();
-            const u32 rin = rin_sh[wib][lane];
-            const u32 hi = static_cast<u32>(rec_a >> 32);
-            const u32 t = __umulhi(rin, static_cast<u32>(mag_a));
-            const u32 q = static_cast<u32>((static_cast<u64>(rin) * static_cast<u32>(mag_a >> 32) + t) >> 32);
-            const u64 add = static_cast<u64>(hi >> 16) * q;
-            const u32 rr = q * (hi & 0xFFFFu);
-            const u32 sh = (rr < (1u << 24) ? 1u : 0u) + (rr < (1u << 16) ? 1u : 0u);
-            u32 isum = sh;
-            u64 iadd = add;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const u32 ys = __shfl_up_sync(0xffffffffu, isum, o);
-                const u64 ya = __shfl_up_sync(0xffffffffu, iadd, o);
-                if (lane >= o) {
-                    isum += ys;
-                    iadd += ya;
-                }
+            p_rin = rin_sh[buf][wib][lane];
+            p_rec = rec_a;
+            p_mag = mag_a;
+            pend = true;
+            buf ^= 1;
+        } else {
+            if (pend) {
+                finish(p_rin, p_rec, p_mag);
+                pend = false;
             }
-            const unsigned smask = __ballot_sync(0xffffffffu, sh != 0);
-            const unsigned below = smask & ((1u << lane) - 1u);
-            const int prev = below ? 31 - __clz(static_cast<int>(below)) : 0;
-            const u64 base = __shfl_sync(0xffffffffu, iadd, prev);
-            const int last = smask ? 31 - __clz(static_cast<int>(smask)) : 0;
-            const u64 at_last = __shfl_sync(0xffffffffu, iadd, last);
-            const u64 tot = __shfl_sync(0xffffffffu, iadd, 31);
-            const u32 nsh = __shfl_sync(0xffffffffu, isum, 31);
-            if (sh) {  // this step closes slot S0 + pos (its sum: the steps since the previous close)
-                const u32 pos = isum - sh;
-                w[pos] = below ? iadd - base : acc + iadd;
-                if (sh == 2) w[pos + 1] = 0;
-            }
-            acc = smask ? tot - at_last : acc + tot;
-            w += nsh;
-            rec_a = rec_b;
-            mag_a = mag_b;
-            raw_a = raw_b;
-            rec_b = rec_c;
-            continue;
-        }
-        for (u32 g = 0; g < L; g += 8) {
-            const unsigned em = (escm >> g) & 0xFFu;
-            if (em == 0 && g + 8 <= L) {
+            // the chunk's (record, reciprocal) pairs go through shared memory: the
+            // steps read them with broadcast loads the compiler issues ahead
+            __syncwarp();
+            stage[wib][lane] = make_ulonglong2(rec_a, mag_a);
+            __syncwarp();
+            for (u32 g = 0; g < L; g += 8) {
+                const unsigned em = (escm >> g) & 0xFFu;
+                if (em == 0 && g + 8 <= L) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const ulonglong2 rm = stage[wib][g + u];
-                    step(rm.x, rm.y);
-                }
-            } else {
+                    for (int u = 0; u < 8; ++u) {
+                        const ulonglong2 rm = stage[wib][g + u];
+                        step(rm.x, rm.y);
+                    }
+                } else {
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (g + u >= L) break;
-                    const ulonglong2 rm = stage[wib][g + u];
-                    step(rm.x, rm.y);
-                    if ((em >> u) & 1u) raw_bits(__shfl_sync(0xffffffffu, raw_a, g + u));
+                    for (int u = 0; u < 8; ++u) {
+                        if (g + u >= L) break;
+                        const ulonglong2 rm = stage[wib][g + u];
+                        step(rm.x, rm.y);
+                        if ((em >> u) & 1u) raw_bits(__shfl_sync(0xffffffffu, raw_a, g + u));
+                    }
                 }
             }
         }
@@ -506,6 +520,7 @@ __global__ void __launch_bounds__(128) ac_range_kernel(const u64* __restrict__ s
         raw_a = raw_b;
         rec_b = rec_c;
     }
+    if (pend) finish(p_rin, p_rec, p_mag);
     if (lane == 0) {  // flush: five shift_low calls
         w[0] = acc;
         for (int i = 1; i < 5; ++i) w[i] = 0;
@@ -755,7 +770,7 @@ u64 ac_out_cap(u64 sym_cap, u64 positions) {
 
 namespace {
 void ac_run(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs, u8* ent, u64* elen,
-            u64* bounds, cudaStream_t s, int* err_ext = nullptr) {
+            u64* bounds, cudaStream_t s, int* err_ext = nullptr, const std::function<void()>* launched = nullptr) {
     const int nj = static_cast<int>(jobs.size());
     if (nj == 0) return;
     if (elen) TCB_CUDA(cudaMemsetAsync(elen, 0, nj * sizeof(u64), s));
@@ -842,6 +857,7 @@ void ac_run(const u64* syms, const u64* counts, int stride, const std::vector<Ac
             ac_bounds_kernel<<<static_cast<unsigned>(nj), 256, 0, s>>>(counts, stride, djobs.p, nj, recs.p, bounds);
             count_launch();
             TCB_LAUNCH();
+            if (launched && *launched) (*launched)();
             if (err_ext) return;
             int herr = 0;
             d2h(&herr, errp, sizeof(int), s);
@@ -879,12 +895,15 @@ void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector
 }
 
 std::vector<u64> ac_size_bounds(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs,
-                                cudaStream_t s) {
+                                cudaStream_t s, const std::function<void()>& launched) {
     const std::size_t nj = jobs.size();
     std::vector<u64> out(2 * nj, 0);
-    if (nj == 0) return out;
+    if (nj == 0) {
+        if (launched) launched();
+        return out;
+    }
     DevBuf<u64> d(2 * nj, s);
-    ac_run(syms, counts, stride, jobs, nullptr, nullptr, d.p, s);
+    ac_run(syms, counts, stride, jobs, nullptr, nullptr, d.p, s, nullptr, &launched);
     d.download(out.data(), 2 * nj);
     stream_sync(s);
     return out;

@@ -17,6 +17,7 @@
 //    generate/propagate scan.
 #pragma once
 
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -46,7 +47,8 @@ void ac_encode(const u64* syms, const u64* counts, int stride, const std::vector
 
 // Bounds [lo, hi] (out[2 j], out[2 j + 1]) on each stream's encode_symbols size from
 // the adaptive model alone (no range recurrence); lo == hi == 0 for no symbols.
+// `launched` (optional) runs once every kernel is enqueued, before the wait.
 std::vector<u64> ac_size_bounds(const u64* syms, const u64* counts, int stride, const std::vector<AcJob>& jobs,
-                                cudaStream_t s);
+                                cudaStream_t s, const std::function<void()>& launched = {});
 
 }  // namespace tcb

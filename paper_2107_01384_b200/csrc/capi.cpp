@@ -202,10 +202,11 @@ struct Stream {
         if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
             throw Error("tucomp_b200: no CUDA device (the B200 path has no CPU fallback)");
         // the call's own stream carries the critical path (sthosvd, core plan and
-        // finalisation): highest priority over the factor workers' streams
+        // finalisation): priority over the factor workers' streams, one level
+        // below the highest (kept for short speculative work that must overtake it)
         int lo = 0, hi = 0;
         TCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        TCB_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
+        TCB_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
         TCB_ONCE_PER_DEVICE({  // keep freed pool memory mapped between calls
             cudaMemPool_t mp;
             if (cudaDeviceGetDefaultMemPool(&mp, cur_device()) == cudaSuccess) {

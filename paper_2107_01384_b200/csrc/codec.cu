@@ -1587,16 +1587,20 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
 }
 
 
-std::vector<u64> entropy_size_bounds(const u64* m, u64 n, u64 block, int plane, cudaStream_t s, BlockRange br) {
+std::vector<u64> entropy_size_bounds(const u64* m, u64 n, u64 block, int plane, cudaStream_t s, BlockRange br,
+                                     const std::function<void()>& launched) {
     const u64 nball = n == 0 ? 0 : (n + block - 1) / block;
     const u64 b0 = std::min(br.b0, nball), b1 = std::min(br.b1, nball);
-    if (b1 <= b0) return {};
+    if (b1 <= b0) {
+        if (launched) launched();
+        return {};
+    }
     HostTrace ht("emit: entropy size bounds");
     const auto hist = msb_histogram(m, n, block, s);
     const Layout L = make_layout(hist, n, block, plane, plane, nullptr, 0, br);
     Coded c;
     emit_streams(c, L, m, nullptr, s);
-    return ac_size_bounds(c.syms.p, reinterpret_cast<const u64*>(c.so.p), 2, L.jobs, s);
+    return ac_size_bounds(c.syms.p, reinterpret_cast<const u64*>(c.so.p), 2, L.jobs, s, launched);
 }
 
 }  // namespace tcb

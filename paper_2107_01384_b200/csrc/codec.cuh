@@ -1,6 +1,8 @@
 // Bit-plane codec kernels (core_codec.cpp / entropy.cpp / error_model.cpp).
 #pragma once
 
+#include <functional>
+
 #include <memory>
 #include <utility>
 #include <vector>
@@ -83,7 +85,9 @@ EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_p
 // Arithmetic-coder size bounds [lo, hi] of plane `plane`'s full streams (blocks of
 // the range; out[2 i], out[2 i + 1]) from the adaptive model alone: enough to
 // decide the split-plane priority without the sequential range pass, usually.
-std::vector<u64> entropy_size_bounds(const u64* m, u64 n, u64 block, int plane, cudaStream_t s, BlockRange br = {});
+// `launched` (optional) runs once every kernel is enqueued, before the host waits.
+std::vector<u64> entropy_size_bounds(const u64* m, u64 n, u64 block, int plane, cudaStream_t s, BlockRange br = {},
+                                     const std::function<void()>& launched = {});
 
 // Speculative split-plane probe: the entropy-coded size of every full plane
 // stream (planes 63..0, no stops, signs not needed) launched on a side stream

@@ -69,7 +69,8 @@ struct Planner {
         if (spec.fut.valid() || plane > 63 || plane < 0 || !o.split || o.coder != 0 || o.probe ||
             (o.shard && o.shard->world > 1))
             return;
-        // highest priority: its CTAs are dispatched ahead of the plane statistics'
+        // the highest priority (one above the call's stream): the probe's CTAs are
+        // dispatched ahead of the plane statistics' as soon as they are enqueued
         static PerDevice<cudaStream_t> side_streams;
         cudaStream_t side = side_streams.get([] {
             int lo = 0, hi = 0;
@@ -86,10 +87,28 @@ struct Planner {
         spec.plane = plane;
         const u64* mm = m;
         const u64 nn = n, bl = block;
-        spec.fut = std::async(std::launch::async, [mm, nn, bl, plane, side, dev] {
-            TCB_CUDA(cudaSetDevice(dev));
-            return entropy_size_bounds(mm, nn, bl, plane, side);
+        // the caller waits until the probe's kernels are enqueued: queued ahead of
+        // the plane statistics (same stream priority), its few CTAs start first and
+        // the statistics fill the remaining SMs, instead of the probe waiting for
+        // every statistics CTA to be dispatched
+        auto enq = std::make_shared<std::promise<void>>();
+        auto enq_f = enq->get_future();
+        spec.fut = std::async(std::launch::async, [mm, nn, bl, plane, side, dev, enq] {
+            bool sent = false;
+            try {
+                TCB_CUDA(cudaSetDevice(dev));
+                auto r = entropy_size_bounds(mm, nn, bl, plane, side, {}, [&] {
+                    sent = true;
+                    enq->set_value();
+                });
+                if (!sent) enq->set_value();
+                return r;
+            } catch (...) {
+                if (!sent) enq->set_value();
+                throw;
+            }
         });
+        enq_f.wait();
     }
 
     // Exact statistics from plane p down: a sampled estimate of the residual

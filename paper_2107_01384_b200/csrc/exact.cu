@@ -868,7 +868,10 @@ template <int LPE>
 void run_exact(const u64* m, const u64* dec, const std::vector<ExSeg>& segs, const std::vector<ExKind>& kinds,
                ExOut* dout, cudaStream_t s) {
     constexpr u64 C = 32ull * LPE;
+    HostTrace ht_prep("exact: prepare");
     Prepared p = prepare(segs, kinds, C, s);
+    ht_prep.stop();
+    HostTrace ht_launch("exact: launch");
     const int nseg = static_cast<int>(segs.size()), nk = static_cast<int>(kinds.size());
     const int njobs = nseg * nk;
     // short segments: the warp resolves them directly (no tables)

@@ -707,6 +707,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
         ingest_cast(cf.p, 8, nc, core_s.p, s);
     }
     bool core_finite = true;
+    HostTrace ht_q("encode: max + quantize launch");
     const double mx = max_abs_finite(core_s.p, nc, &core_finite, s);
     if (!core_finite) throw Error("quantize: non-finite core values");
     const bool zero = mx == 0.0;
@@ -752,6 +753,7 @@ void encode_into(Result& res, Tucker& f, const std::vector<u64>& shape, int dtyp
     } sn_join{sn_ready};
     // core_s is read by nothing after the quantisation kernel (stream-ordered free)
     core_s.release();
+    ht_q.stop();
     res.times.quantize = ms_since(t0);
     const u64 block = prm.block ? prm.block : default_block(zero ? 0 : nc);
 
