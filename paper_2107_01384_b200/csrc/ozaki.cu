@@ -260,35 +260,41 @@ __global__ void __launch_bounds__(256) oz_split_rows_blk_kernel(const double* __
 
 // Columns of a rows x cols matrix as rows of the blocked layout (block rows br):
 // output row c holds the digits of column c over k < 64 nslab (zero beyond rows
-// and for c >= cols up to the padding).  32 columns x 32 k per CTA through shared
-// memory; each thread writes 4 consecutive k of one column per slice.
+// and for c >= cols up to the padding).  32 columns x 128 k per CTA, through
+// shared memory 32 k at a time; each thread writes 4 consecutive k of one
+// column per slice.
+constexpr int kColK = 128;
 __global__ void __launch_bounds__(256) oz_split_cols_blk_kernel(const double* __restrict__ B, u64 rows, u64 cols,
                                                                 u64 cols_pad, u64 nslab, const int* __restrict__ ex,
                                                                 u32 br, int8_t* __restrict__ out) {
     __shared__ int8_t t[kSlices][32][36];
-    const u64 c0 = static_cast<u64>(blockIdx.x) * 32, k0 = static_cast<u64>(blockIdx.y) * 32;
+    const u64 c0 = static_cast<u64>(blockIdx.x) * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
-    for (int kk = ty; kk < 32; kk += 8) {
-        const u64 k = k0 + kk, c = c0 + tx;
-        double x = 0.0;
-        int e = 0;
-        if (c < cols) {
-            e = ex[c];
-            if (k < rows) x = B[k * cols + c];
-        }
-        int8_t d[kSlices];
-        digits(x * scalbn(1.0, -e), d);
-#pragma unroll
-        for (int s = 0; s < kSlices; ++s) t[s][tx][kk] = d[s];
-    }
-    __syncthreads();
+    const u64 cr = c0 + tx;
+    const double sc = cr < cols ? scalbn(1.0, -ex[cr]) : 0.0;
     const int cc = threadIdx.x >> 3, kq = (threadIdx.x & 7) * 4;
-    const u64 c = c0 + cc, k = k0 + kq;
-    if (c >= cols_pad || k >= nslab * kOzSlab) return;
+    const u64 cw = c0 + cc;
+    for (int sub = 0; sub < kColK / 32; ++sub) {
+        const u64 k0 = static_cast<u64>(blockIdx.y) * kColK + sub * 32;
+        if (k0 >= nslab * kOzSlab) break;
+        for (int kk = ty; kk < 32; kk += 8) {
+            const u64 k = k0 + kk;
+            const double x = cr < cols && k < rows ? B[k * cols + cr] : 0.0;
+            int8_t d[kSlices];
+            digits(x * sc, d);
 #pragma unroll
-    for (int s = 0; s < kSlices; ++s) {
-        const char4 v = make_char4(t[s][cc][kq], t[s][cc][kq + 1], t[s][cc][kq + 2], t[s][cc][kq + 3]);
-        *reinterpret_cast<char4*>(out + oz_block_off(c, k, s, br, nslab)) = v;
+            for (int s = 0; s < kSlices; ++s) t[s][tx][kk] = d[s];
+        }
+        __syncthreads();
+        const u64 k = k0 + kq;
+        if (cw < cols_pad && k < nslab * kOzSlab) {
+#pragma unroll
+            for (int s = 0; s < kSlices; ++s) {
+                const char4 v = make_char4(t[s][cc][kq], t[s][cc][kq + 1], t[s][cc][kq + 2], t[s][cc][kq + 3]);
+                *reinterpret_cast<char4*>(out + oz_block_off(cw, k, s, br, nslab)) = v;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -436,10 +442,10 @@ void ttm_ozaki(const double* B, u64 rows, u64 cols, const double* U, u64 r, doub
         const u64 nslab = cdiv(rows, kOzSlab), Kr = nslab * kOzSlab;
         const u64 ca = oz_block_rows(cols, kOzBM), ub = oz_block_rows(r, kOzBN);
         DevBuf<int8_t> dt(oz_block_bytes(cols, nslab, kOzBM), s), eu(oz_block_bytes(r, nslab, kOzBN), s);
-        oz_split_cols_blk_kernel<<<dim3(cdiv(ca, 32), cdiv(Kr, 32)), 256, 0, s>>>(B, rows, cols, ca, nslab, exc.p,
-                                                                                kOzBM, dt.p);
-        oz_split_cols_blk_kernel<<<dim3(cdiv(ub, 32), cdiv(Kr, 32)), 256, 0, s>>>(U, rows, r, ub, nslab, exu.p,
-                                                                                kOzBN, eu.p);
+        oz_split_cols_blk_kernel<<<dim3(cdiv(ca, 32), cdiv(Kr, kColK)), 256, 0, s>>>(B, rows, cols, ca, nslab,
+                                                                                    exc.p, kOzBM, dt.p);
+        oz_split_cols_blk_kernel<<<dim3(cdiv(ub, 32), cdiv(Kr, kColK)), 256, 0, s>>>(U, rows, r, ub, nslab,
+                                                                                    exu.p, kOzBN, eu.p);
         count_launch(2);
         TCB_LAUNCH();
         oz_ttm_tc(dt.p, cols, eu.p, r, nslab, exc.p, exu.p, out, s);

@@ -588,15 +588,17 @@ void factor_plane_search(FactorQuant& q, const double* U, u64 n, u64 r, int core
     const u64 rl = q.live.size();
     int plane = std::clamp(core_step_log2 + q.k, 0, 63);
     // The reference deepens the plane while the factor term exceeds the cap
-    // (factor_codec.cpp:218-243).  Terms for a window of candidate planes are
-    // evaluated in one batched launch; the host then replays the reference's
-    // deepening decisions over them.
+    // (factor_codec.cpp:218-243).  Terms for a window of 4 candidate planes are
+    // evaluated in one batched launch (each candidate expands every reflector:
+    // a wider window cost more GPU time beside the core's encoder than the extra
+    // round trip it saves); the host then replays the reference's deepening
+    // decisions over them.
     std::vector<double> term_of(64, -1.0);
     double term = 0.0;
     while (true) {
         if (term_of[plane] < 0.0) {
             std::vector<int> cand;
-            for (int p = plane; p >= 0 && static_cast<int>(cand.size()) < 16; --p)
+            for (int p = plane; p >= 0 && static_cast<int>(cand.size()) < 4; --p)
                 if (term_of[p] < 0.0) cand.push_back(p);
             const auto res = factor_residuals(q.mag.p, q.neg.p, q.k, n, r, q.live, q.dsc.p, U, q.dfl.p, cand, s);
             for (std::size_t c = 0; c < cand.size(); ++c) {
