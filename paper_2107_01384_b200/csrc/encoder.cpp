@@ -448,6 +448,67 @@ StreamParts finalize_stream_parts(const u64* m, const u8* neg, u64 n, const Plan
         up->body.s = s;  // freed after the copy, in stream order
         return out;
     }
+    if ((!shard || shard->world <= 1) && pl.nplanes >= 4 && n > (u64{1} << 20)) {
+        // The range coder's time is set by the longest streams, which sit in the
+        // densest planes: those planes are emitted, modelled and coded on this
+        // (higher-priority) stream while the planes above and below them go
+        // through the same steps on two side streams, instead of the longest
+        // recurrences starting only after every plane's emission and model.
+        const int lp = pl.last_plane;
+        const auto hist = msb_histogram(m, n, pl.block, s);
+        int best = lp;
+        u64 bestc = 0;
+        for (int p = lp; p <= 63; ++p) {
+            u64 c = 0;
+            for (u64 b = 0; b < nb; ++b) c = std::max(c, hist[b * 65 + static_cast<u64>(p + 1)]);
+            if (c > bestc) {
+                bestc = c;
+                best = p;
+            }
+        }
+        const int h_lo = std::max(lp, best - 1), h_hi = std::min(63, best + 1);
+        // the planes above and below the densest ones, each on its own side stream
+        // (driven by its own thread), all three groups started together
+        static PerDevice<std::pair<cudaStream_t, cudaStream_t>> side_streams;
+        const auto sides = side_streams.get([] {
+            std::pair<cudaStream_t, cudaStream_t> x;
+            TCB_CUDA(cudaStreamCreateWithFlags(&x.first, cudaStreamNonBlocking));
+            TCB_CUDA(cudaStreamCreateWithFlags(&x.second, cudaStreamNonBlocking));
+            return x;
+        });
+        const int dev = cur_device();
+        EventHandle q;
+        TCB_CUDA(cudaEventRecord(q.e, s));
+        TCB_CUDA(cudaStreamWaitEvent(sides.first, q.e, 0));
+        TCB_CUDA(cudaStreamWaitEvent(sides.second, q.e, 0));
+        auto run = [&, dev](int lo_p, int hi_p, const u64* stops, cudaStream_t st) {
+            return std::async(std::launch::async, [&, dev, lo_p, hi_p, stops, st] {
+                TCB_CUDA(cudaSetDevice(dev));
+                EmitDev e;
+                if (lo_p <= hi_p) e = emit_planes_device(m, neg, n, pl.block, lo_p, hi_p, stops, coder, st);
+                return e;
+            });
+        };
+        auto f_up = run(h_hi + 1, 63, nullptr, sides.first);
+        auto f_lo = run(lp, h_lo - 1, pl.stops.data(), sides.second);
+        EmitDev mid = emit_planes_device(m, neg, n, pl.block, h_lo, h_hi, h_lo == lp ? pl.stops.data() : nullptr,
+                                         coder, s);
+        EmitDev up = f_up.get(), lo = f_lo.get();
+        for (cudaStream_t st : {sides.first, sides.second}) {  // their assembly kernels, before the copies
+            EventHandle fin;
+            TCB_CUDA(cudaEventRecord(fin.e, st));
+            TCB_CUDA(cudaStreamWaitEvent(s, fin.e, 0));
+        }
+        out.body_size = up.size + mid.size + lo.size;
+        out.body = DevBuf<u8>(out.body_size + 1, s);
+        u64 at = 0;
+        for (EmitDev* e : {&up, &mid, &lo}) {  // container order: planes from the top down
+            if (e->size) TCB_CUDA(cudaMemcpyAsync(out.body.p + at, e->body.p, e->size, cudaMemcpyDeviceToDevice, s));
+            at += e->size;
+            e->body.s = s;  // freed after the copy, in stream order
+        }
+        return out;
+    }
     if (!shard || shard->world <= 1) {
         EmitDev er = emit_planes_device(m, neg, n, pl.block, pl.last_plane, 63, pl.stops.data(), coder, s);
         out.body = std::move(er.body);

@@ -1,6 +1,8 @@
 // Host-callable launchers for every sm_100a kernel of the compress path.
 #pragma once
 
+#include <memory>
+
 #include "common.cuh"
 
 namespace tcb {
@@ -60,7 +62,22 @@ void ttm_f64(const double* B, u64 rows, u64 cols, const double* U, u64 r, double
 bool ozaki_gram_ok(u64 rows, u64 cols);
 bool ozaki_ttm_ok(u64 rows, u64 cols, u64 r);
 void gram_ozaki(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s);
-void ttm_ozaki(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s);
+// The TTM's B-side work (column exponents, column digits) depends only on B:
+// ttm_ozaki_prepare runs it on `side` (e.g. beside the eigensolve that produces
+// U) and ttm_ozaki, given the handle, waits for it instead of redoing it.
+struct OzTtmPrep {
+    u64 rows = 0, cols = 0, nslab = 0;
+    DevBuf<int> exc;
+    DevBuf<int8_t> dt;
+    cudaEvent_t done = nullptr;
+    OzTtmPrep() = default;
+    OzTtmPrep(const OzTtmPrep&) = delete;
+    OzTtmPrep& operator=(const OzTtmPrep&) = delete;
+    ~OzTtmPrep();
+};
+std::unique_ptr<OzTtmPrep> ttm_ozaki_prepare(const double* B, u64 rows, u64 cols, cudaStream_t side);
+void ttm_ozaki(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s,
+               OzTtmPrep* prep = nullptr);
 // out (rows x r) = B V  (B rows x cols row-major, V cols x r row-major); small.
 void gemm_nn_f64(const double* B, u64 rows, u64 cols, const double* V, u64 r, double* out, cudaStream_t s);
 

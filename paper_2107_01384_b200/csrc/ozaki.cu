@@ -430,10 +430,48 @@ void gram_ozaki(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) 
     TCB_LAUNCH();
 }
 
-void ttm_ozaki(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s) {
+OzTtmPrep::~OzTtmPrep() {
+    if (done) cudaEventDestroy(done);
+}
+
+std::unique_ptr<OzTtmPrep> ttm_ozaki_prepare(const double* B, u64 rows, u64 cols, cudaStream_t side) {
+    auto p = std::make_unique<OzTtmPrep>();
+    p->rows = rows;
+    p->cols = cols;
+    p->nslab = cdiv(rows, kOzSlab);
+    const u64 Kr = p->nslab * kOzSlab, ca = oz_block_rows(cols, kOzBM);
+    p->exc = DevBuf<int>(round_up(cols, 16), side);
+    p->dt = DevBuf<int8_t>(oz_block_bytes(cols, p->nslab, kOzBM), side);
+    oz_colexp_kernel<<<cdiv(cols, 256), 256, 0, side>>>(B, rows, cols, p->exc.p);
+    oz_split_cols_blk_kernel<<<dim3(cdiv(ca, 32), cdiv(Kr, kColK)), 256, 0, side>>>(B, rows, cols, ca, p->nslab,
+                                                                                   p->exc.p, kOzBM, p->dt.p);
+    count_launch(2);
+    TCB_LAUNCH();
+    TCB_CUDA(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
+    TCB_CUDA(cudaEventRecord(p->done, side));
+    return p;
+}
+
+void ttm_ozaki(const double* B, u64 rows, u64 cols, const double* U, u64 r, double* out, cudaStream_t s,
+               OzTtmPrep* prep) {
     ProfScope prof_scope(kTtm, s);
     const bool lt = use_lt();
     const u64 r_p = round_up(r, 16), cols_p = round_up(cols, 16);
+    if (!lt && prep && prep->rows == rows && prep->cols == cols) {
+        TCB_CUDA(cudaStreamWaitEvent(s, prep->done, 0));
+        prep->exc.s = s;  // freed in this stream's order, after the products
+        prep->dt.s = s;
+        const u64 nslab = prep->nslab, Kr = nslab * kOzSlab, ub = oz_block_rows(r, kOzBN);
+        DevBuf<int> exu(r_p, s);
+        DevBuf<int8_t> eu(oz_block_bytes(r, nslab, kOzBN), s);
+        oz_colexp_kernel<<<cdiv(r, 256), 256, 0, s>>>(U, rows, r, exu.p);
+        oz_split_cols_blk_kernel<<<dim3(cdiv(ub, 32), cdiv(Kr, kColK)), 256, 0, s>>>(U, rows, r, ub, nslab,
+                                                                                    exu.p, kOzBN, eu.p);
+        count_launch(2);
+        TCB_LAUNCH();
+        oz_ttm_tc(prep->dt.p, cols, eu.p, r, nslab, prep->exc.p, exu.p, out, s);
+        return;
+    }
     DevBuf<int> exc(cols_p, s), exu(r_p, s);
     oz_colexp_kernel<<<cdiv(cols, 256), 256, 0, s>>>(B, rows, cols, exc.p);
     oz_colexp_kernel<<<cdiv(r, 256), 256, 0, s>>>(U, rows, r, exu.p);

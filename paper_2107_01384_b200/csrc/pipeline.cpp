@@ -382,6 +382,7 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
     const bool via_gram = backend == 1 || rows <= cols_all;
     if (sharded && !via_gram) throw Error("sharded compress: a step off the Gram route (rows > cols)");
     StepOut o;
+    std::unique_ptr<OzTtmPrep> tprep;
     if (via_gram) {
         DevBuf<double> G;
         bool oz = false;
@@ -393,6 +394,22 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
             } else {
                 gram_f64(x, rows, cols, G.p, s);
             }
+        }
+        // the TTM's B-side digits need only x: on a low-priority side stream they
+        // fill the eigensolve's latency-bound SMs (wasted when r < 64 or thin)
+        if (ozaki_gram_ok(rows, cols) && rows <= 4096) {
+            static PerDevice<cudaStream_t> prep_streams;
+            cudaStream_t side = prep_streams.get([] {
+                int lo = 0, hi = 0;
+                TCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+                cudaStream_t x2;
+                TCB_CUDA(cudaStreamCreateWithPriority(&x2, cudaStreamNonBlocking, lo));
+                return x2;
+            });
+            EventHandle q;
+            TCB_CUDA(cudaEventRecord(q.e, s));
+            TCB_CUDA(cudaStreamWaitEvent(side, q.e, 0));
+            tprep = ttm_ozaki_prepare(x, rows, cols, side);
         }
         if (sharded) {  // the columns are spread over the ranks: sum the partial Grams
             if (gram) {
@@ -438,8 +455,16 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
         fix_column_signs(o.U.p, rows, r, s);
     }
     o.next = DevBuf<double>(cols * o.r, s);
-    if (ozaki_ttm_ok(rows, cols, o.r)) ttm_ozaki(x, rows, cols, o.U.p, o.r, o.next.p, s);
-    else ttm_f64(x, rows, cols, o.U.p, o.r, o.next.p, s);
+    if (ozaki_ttm_ok(rows, cols, o.r)) {
+        ttm_ozaki(x, rows, cols, o.U.p, o.r, o.next.p, s, tprep.get());
+    } else {
+        ttm_f64(x, rows, cols, o.U.p, o.r, o.next.p, s);
+        if (tprep) {  // unused: released after its kernels, in the call's stream order
+            TCB_CUDA(cudaStreamWaitEvent(s, tprep->done, 0));
+            tprep->exc.s = s;
+            tprep->dt.s = s;
+        }
+    }
     return o;
 }
 
@@ -1152,13 +1177,19 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     // internal_float32 the values are first rounded to float as the reference does
     // fp64 input (container::Dtype 9) is used in place: no ingest copy
     const bool direct = !prm.f32 && dtype == 9 && reinterpret_cast<uintptr_t>(device_bytes) % 16 == 0;
-    // fp64 in place: |A|^2 is read off the first mode's Gram (its trace), so no
-    // separate norm pass precedes the mode loop; a non-finite trace falls back to
-    // the element scan (the reference's non-finite error, or a huge finite input)
-    const bool norm_from_gram = direct && !norm_pass_forced();
+    // fp64 in place or an fp32 source: |A|^2 is read off the first mode's Gram
+    // (its trace: every unfolding holds every element), so no separate norm pass
+    // precedes the mode loop; a non-finite trace falls back to the element scan
+    // (the reference's non-finite error, or a huge finite input)
+    const bool src_f32 = dtype == 8;
+    const bool norm_from_gram = !prm.f32 && (direct || src_f32) && !norm_pass_forced();
     DevBuf<double> a;
     bool finite = true;
     if (direct && norm_from_gram) {
+        res.norm_sq = 0.0;  // set after the first mode step
+    } else if (src_f32 && norm_from_gram) {
+        a = DevBuf<double>(n_el, s);
+        ingest_cast(device_bytes, dtype, n_el, a.p, s);
         res.norm_sq = 0.0;  // set after the first mode step
     } else if (direct) {
         res.norm_sq = sum_squares(static_cast<const double*>(device_bytes), n_el, &finite, s);
@@ -1174,7 +1205,7 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
         res.norm_sq = sum_squares(a.p, n_el, &finite, s);
     }
     if (dtype == 6 || dtype == 7) res.precision_loss = ingest_precision_loss(device_bytes, dtype, n_el, s);
-    if (sharded && !(direct && norm_from_gram)) {  // global norm, finite flag and precision flag
+    if (sharded && !norm_from_gram) {  // global norm, finite flag and precision flag
         DevBuf<double> st(3, s);
         const double h[3] = {res.norm_sq, finite ? 0.0 : 1.0, res.precision_loss ? 1.0 : 0.0};
         st.upload(h, 3);
@@ -1244,7 +1275,8 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
                            norm_scale, norm_from_gram ? &norm_trace : nullptr, direct ? gram0 : nullptr, shard);
     } catch (const TraceNonFinite&) {  // scan the elements: the reference error, or a norm pass rerun
         bool fin = true;
-        sum_squares(static_cast<const double*>(device_bytes), n_el, &fin, s);
+        if (direct) sum_squares(static_cast<const double*>(device_bytes), n_el, &fin, s);
+        else sum_squares(static_cast<const float*>(device_bytes), n_el, &fin, s);
         if (sharded) {  // every rank sees the same trace, so every rank is here: agree on the verdict
             DevBuf<double> f(1, s);
             const double h = fin ? 0.0 : 1.0;

@@ -121,6 +121,24 @@ def test_encoder_bitstream_bit_exact(gpu_pkg, frac, split, coder):
     assert ach_gpu == pytest.approx(ach_ref, rel=1e-12, abs=0)
 
 
+@pytest.mark.parametrize("frac", [1e-3, 1e-6])
+@pytest.mark.parametrize("split", [True, False])
+def test_encoder_bitstream_bit_exact_large(gpu_pkg, frac, split):
+    """A 2.2M-coefficient core (above 2^20): the sampled breakpoint estimate, the
+    table-driven exact plane statistics, the speculative split probe and the
+    densest planes coded on their own stream all take part; the stream is the
+    oracle's byte for byte."""
+    mag, neg = _core_mags(shape=(130, 130, 131), seed=4, decay=9.0)
+    tot = float((mag.astype(np.float64) ** 2).sum())
+    tgt = tot * frac
+    s_gpu, lp_gpu, ach_gpu, dec_gpu, _ = gpu_pkg.encode(mag, neg, tgt, coder=0, split=split)
+    s_ref, lp_ref, ach_ref, dec_ref = oracle.encode(mag, neg, tgt, coder=0, split=split)
+    assert lp_gpu == lp_ref
+    assert np.array_equal(dec_gpu, dec_ref)
+    assert s_gpu == s_ref
+    assert ach_gpu == pytest.approx(ach_ref, rel=1e-12, abs=0)
+
+
 @pytest.mark.parametrize("fixed", [63, 50, 40, 10, 0])
 def test_encoder_fixed_plane_bit_exact(gpu_pkg, fixed):
     mag, neg = _core_mags((17, 19, 23), seed=5)
