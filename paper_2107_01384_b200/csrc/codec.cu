@@ -892,11 +892,12 @@ __global__ void __launch_bounds__(kScT) sc_emit_kernel(const u64* __restrict__ m
 __global__ void __launch_bounds__(256) sc_diff_kernel(const StreamDesc* __restrict__ sd,
                                                       const StreamOut* __restrict__ so, const u64* __restrict__ ncol,
                                                       const u64* __restrict__ zbuf, u64* __restrict__ syms) {
-    const int st = blockIdx.x;
+    const int st = blockIdx.x;  // blockIdx.y: 64K-symbol segments of the stream
     const u64 nsy = so[st].nsyms;
-    if (nsy == 0) return;
-    const u64 no = nsy - 1, off = sd[st].sym_off;
-    for (u64 k = threadIdx.x; k < nsy; k += blockDim.x) {
+    const u64 k0 = static_cast<u64>(blockIdx.y) << 16;
+    if (k0 >= nsy) return;
+    const u64 no = nsy - 1, off = sd[st].sym_off, k1 = min(nsy, k0 + (u64{1} << 16));
+    for (u64 k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
         const u64 prev = k > 0 ? zbuf[off + k - 1] : 0;
         syms[off + k] = (k < no ? zbuf[off + k] : ncol[st] - no) - prev;
     }
@@ -1420,7 +1421,10 @@ void emit_streams(Coded& c, const Layout& L, const u64* m, const u8* neg, cudaSt
                                                  static_cast<int>(kSc * sizeof(u64) + 64 * kScW * 4 * sizeof(u32))));
         sc_emit_kernel<<<static_cast<unsigned>(nsc), kScT, smem, s>>>(m, neg, c.dsd.p, np, nb, dsc.p, nsc, tab.p,
                                                                       zbuf.p, c.raw.p);
-        sc_diff_kernel<<<static_cast<unsigned>(ns), 256, 0, s>>>(c.dsd.p, c.so.p, ncol.p, zbuf.p, c.syms.p);
+        u64 maxsym = 1;
+        for (const AcJob& jb : L.jobs) maxsym = std::max(maxsym, jb.sym_cap);
+        sc_diff_kernel<<<dim3(static_cast<unsigned>(ns), static_cast<unsigned>(cdiv(maxsym, u64{1} << 16))), 256, 0,
+                         s>>>(c.dsd.p, c.so.p, ncol.p, zbuf.p, c.syms.p);
         count_launch(4);
         TCB_LAUNCH();
     }
@@ -1504,7 +1508,8 @@ struct Emitted {
     std::vector<StreamOut> soh;
 };
 bool emit_code(Emitted& E, const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
-               const u64* stops_host, int coder, cudaStream_t s, BlockRange br = {}) {
+               const u64* stops_host, int coder, cudaStream_t s, BlockRange br = {},
+               const std::vector<u64>* hist_in = nullptr) {
     if (coder != 0 && coder != 1) throw Error("entropy: unknown coder");
     const u64 nball = n == 0 ? 0 : (n + block - 1) / block;
     const u64 nb = std::min(br.b1, nball) > std::min(br.b0, nball) ? std::min(br.b1, nball) - std::min(br.b0, nball) : 0;
@@ -1512,7 +1517,7 @@ bool emit_code(Emitted& E, const u64* m, const u8* neg, u64 n, u64 block, int la
     const u64 ns = nb * static_cast<u64>(np);
     if (ns == 0 || np <= 0) return false;
     HostTrace ht_a("emit: symbols+entropy+sync");
-    const auto hist = msb_histogram(m, n, block, s);
+    const auto hist = hist_in ? *hist_in : msb_histogram(m, n, block, s);
     E.L = make_layout(hist, n, block, last_plane, top_plane, stops_host, coder, br);
     code_streams(E.c, E.L, m, neg, coder, s);
     E.el.resize(ns);
@@ -1542,10 +1547,11 @@ bool emit_code(Emitted& E, const u64* m, const u8* neg, u64 n, u64 block, int la
 }  // namespace
 
 EmitDev emit_planes_device(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
-                           const u64* stops_host, int coder, cudaStream_t s, BlockRange br) {
+                           const u64* stops_host, int coder, cudaStream_t s, BlockRange br,
+                           const std::vector<u64>* hist) {
     EmitDev out;
     Emitted E;
-    if (!emit_code(E, m, neg, n, block, last_plane, top_plane, stops_host, coder, s, br)) return out;
+    if (!emit_code(E, m, neg, n, block, last_plane, top_plane, stops_host, coder, s, br, hist)) return out;
     const u64 ns = E.el.size();
     HostTrace ht_b("emit: assemble");
     std::vector<u64> off(ns);

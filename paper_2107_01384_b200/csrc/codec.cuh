@@ -76,8 +76,10 @@ struct EmitDev {
     std::vector<u64> entropy_bytes;
     std::vector<u64> stream_bytes;
 };
+// `hist` (optional): the per-block msb histogram (msb_histogram) when the caller has it
 EmitDev emit_planes_device(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
-                           const u64* stops_host, int coder, cudaStream_t s, BlockRange br = {});
+                           const u64* stops_host, int coder, cudaStream_t s, BlockRange br = {},
+                           const std::vector<u64>* hist = nullptr);
 EmitResult emit_planes(const u64* m, const u8* neg, u64 n, u64 block, int last_plane, int top_plane,
                        const u64* stops_host /*2*nb, for last_plane*/, int coder, bool want_body,
                        cudaStream_t s, BlockRange br = {});

@@ -485,14 +485,14 @@ StreamParts finalize_stream_parts(const u64* m, const u8* neg, u64 n, const Plan
             return std::async(std::launch::async, [&, dev, lo_p, hi_p, stops, st] {
                 TCB_CUDA(cudaSetDevice(dev));
                 EmitDev e;
-                if (lo_p <= hi_p) e = emit_planes_device(m, neg, n, pl.block, lo_p, hi_p, stops, coder, st);
+                if (lo_p <= hi_p) e = emit_planes_device(m, neg, n, pl.block, lo_p, hi_p, stops, coder, st, {}, &hist);
                 return e;
             });
         };
         auto f_up = run(h_hi + 1, 63, nullptr, sides.first);
         auto f_lo = run(lp, h_lo - 1, pl.stops.data(), sides.second);
         EmitDev mid = emit_planes_device(m, neg, n, pl.block, h_lo, h_hi, h_lo == lp ? pl.stops.data() : nullptr,
-                                         coder, s);
+                                         coder, s, {}, &hist);
         EmitDev up = f_up.get(), lo = f_lo.get();
         for (cudaStream_t st : {sides.first, sides.second}) {  // their assembly kernels, before the copies
             EventHandle fin;

@@ -1181,8 +1181,16 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     // (its trace: every unfolding holds every element), so no separate norm pass
     // precedes the mode loop; a non-finite trace falls back to the element scan
     // (the reference's non-finite error, or a huge finite input)
+    // (for an fp32 source only when the first Gram is the Ozaki one, whose diagonal
+    // is a fixed-tree fp64 row sum of squares; the DMMA Gram's split-K diagonal is
+    // ~1e-13 off the exact sum, where the element scan is within 1e-15)
     const bool src_f32 = dtype == 8;
-    const bool norm_from_gram = !prm.f32 && (direct || src_f32) && !norm_pass_forced();
+    bool first_oz = false;
+    if (src_f32 && !shape.empty()) {
+        const std::vector<u64> pp = prm.mode_order ? *prm.mode_order : stable_ascending(shape);
+        if (valid_perm(pp, d) && shape[pp[0]] > 0) first_oz = ozaki_gram_ok(shape[pp[0]], n_el / shape[pp[0]]);
+    }
+    const bool norm_from_gram = !prm.f32 && (direct || (src_f32 && first_oz)) && !norm_pass_forced();
     DevBuf<double> a;
     bool finite = true;
     if (direct && norm_from_gram) {
