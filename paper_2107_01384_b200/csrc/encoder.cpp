@@ -469,11 +469,15 @@ StreamParts finalize_stream_parts(const u64* m, const u8* neg, u64 n, const Plan
         const int h_lo = std::max(lp, best - 1), h_hi = std::min(63, best + 1);
         // the planes above and below the densest ones, each on its own side stream
         // (driven by its own thread), all three groups started together
+        // (the planes below are dense too: their stream at the call's priority; the
+        // sparse planes above at the lowest)
         static PerDevice<std::pair<cudaStream_t, cudaStream_t>> side_streams;
         const auto sides = side_streams.get([] {
+            int lo = 0, hi = 0;
+            TCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
             std::pair<cudaStream_t, cudaStream_t> x;
-            TCB_CUDA(cudaStreamCreateWithFlags(&x.first, cudaStreamNonBlocking));
-            TCB_CUDA(cudaStreamCreateWithFlags(&x.second, cudaStreamNonBlocking));
+            TCB_CUDA(cudaStreamCreateWithPriority(&x.first, cudaStreamNonBlocking, lo));
+            TCB_CUDA(cudaStreamCreateWithPriority(&x.second, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
             return x;
         });
         const int dev = cur_device();

@@ -15,4 +15,7 @@ C5_PROFILE=1 C5_NO_DEC=1 C5_ITERS=2 ncu --profile-from-start off --metrics gpu__
 C5_PROFILE=1 C5_NO_DEC=1 C5_ITERS=2 ncu --profile-from-start off --set full --import-source on --clock-control none \
     -k regex:"oz_mma_kernel|oz_split_rows_blk|oz_split_cols_blk|ex_plane_kernel|ex_walk_kernel|ac_range_kernel|ac_code_kernel|sc_emit|tridiag_coop|dm_decode" \
     -c 16 -o gpurun_out/full python tools/c5_once.py 1e-2 > gpurun_out/ncu_full.log 2>&1
+C5_PROFILE=1 C5_NO_DEC=1 C5_ITERS=2 ncu --profile-from-start off --set full --import-source on --clock-control none \
+    -k regex:"ex_plane_kernel|sc_emit_kernel|ac_range_kernel|ac_code_kernel|ex_walk_kernel|dm_decode" \
+    -c 10 -o gpurun_out/full_enc python tools/c5_once.py 1e-2 > gpurun_out/ncu_full_enc.log 2>&1
 echo done
