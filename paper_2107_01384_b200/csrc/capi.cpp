@@ -118,6 +118,40 @@ void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t s) {
     std::memcpy(h, buf, bytes);
 }
 
+// Host-to-device uploads of small host arrays go through a per-thread ring of
+// pinned slots: a copy from pageable memory waits for everything queued on the
+// stream before it starts (so the host could not enqueue the kernels that
+// follow until the stream drained); from a pinned slot it is asynchronous.  A
+// slot is reused once the copy that last read it has completed (its event).
+void h2d(void* d, const void* h, std::size_t bytes, cudaStream_t s) {
+    if (!bytes) return;
+    constexpr std::size_t kSlot = std::size_t{1} << 19;
+    constexpr int kSlots = 8;
+    if (bytes > kSlot) {
+        TCB_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+        return;
+    }
+    struct Ring {
+        void* buf = nullptr;
+        cudaEvent_t ev[kSlots] = {};
+        bool used[kSlots] = {};
+        int next = 0;
+    };
+    thread_local Ring r;  // lives for the thread (never freed: exit order vs. the context)
+    if (!r.buf) {
+        TCB_CUDA(cudaMallocHost(&r.buf, kSlot * kSlots));
+        for (auto& e : r.ev) TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int i = r.next;
+    r.next = (r.next + 1) % kSlots;
+    if (r.used[i]) TCB_CUDA(cudaEventSynchronize(r.ev[i]));
+    u8* slot = static_cast<u8*>(r.buf) + static_cast<std::size_t>(i) * kSlot;
+    std::memcpy(slot, h, bytes);
+    TCB_CUDA(cudaMemcpyAsync(d, slot, bytes, cudaMemcpyHostToDevice, s));
+    TCB_CUDA(cudaEventRecord(r.ev[i], s));
+    r.used[i] = true;
+}
+
 void timeline_dump();
 void host_trace_dump() {
     timeline_dump();

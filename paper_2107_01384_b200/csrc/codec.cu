@@ -670,48 +670,110 @@ __global__ void __launch_bounds__(kScT) sc_hist_kernel(const u64* __restrict__ m
     for (int i = threadIdx.x; i < 65; i += kScT) hist[g * 65 + i] = h[i];
 }
 
-// one thread per stream: the offsets of every sub-chunk, and the stream's sizes
-__global__ void sc_scan_kernel(const u64* __restrict__ m, const StreamDesc* __restrict__ sd, int ns, int nb,
-                               const u64* __restrict__ scoff, u64 nsc_all, const u32* __restrict__ hist,
-                               ScOff* __restrict__ tab, StreamOut* __restrict__ so, u64* __restrict__ ncol_out) {
-    const int st = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
+// One warp per stream: the offsets of every sub-chunk, and the stream's sizes.
+// Lane l takes a contiguous range of the stream's sub-chunks; the lead / trail
+// / one counts come from the sub-chunk msb histograms, prefixes by warp scans;
+// only the sub-chunk where the lead stop falls (a breakpoint plane) is scanned
+// element by element, by the lane that owns it.
+__device__ __forceinline__ u64 warp_excl_scan_u64(u64 v, u64& total) {
+    const int lane = threadIdx.x & 31;
+    u64 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+}
+
+__global__ void __launch_bounds__(128) sc_scan_kernel(const u64* __restrict__ m, const StreamDesc* __restrict__ sd,
+                                                      int ns, int nb, const u64* __restrict__ scoff, u64 nsc_all,
+                                                      const u32* __restrict__ hist, ScOff* __restrict__ tab,
+                                                      StreamOut* __restrict__ so, u64* __restrict__ ncol_out) {
+    const int st = static_cast<int>((static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     if (st >= ns) return;
+    const int lane = threadIdx.x & 31;
     const StreamDesc d = sd[st];
     const int bi = st % nb, pi = st / nb, p = d.plane;
     const u64 nsc = scoff[bi + 1] - scoff[bi];
     ScOff* tb = tab + static_cast<u64>(pi) * nsc_all + scoff[bi];
-    u64 LB = 0, TB = 0, OB = 0;
-    bool crossed = false;
-    for (u64 j = 0; j < nsc; ++j) {
-        const u32* h = hist + (scoff[bi] + j) * 65;
-        u64 lead = 0, trail = 0;
+    const u32* hb = hist + scoff[bi] * 65;
+    const u64 per = (nsc + 31) / 32, j0 = min(nsc, lane * per), j1 = min(nsc, j0 + per);
+    auto counts = [&](u64 j, u64& lead, u64& trail, u64& ones) {
+        const u32* h = hb + j * 65;
+        lead = 0;
+        trail = 0;
         for (int q = 0; q <= p + 1; ++q) lead += h[q];
         for (int q = p + 2; q < 65; ++q) trail += h[q];
-        const u64 ones = h[p + 1];
-        tb[j] = ScOff{LB, TB, OB, min(TB, d.tstop) + OB};
-        if (!crossed) {
-            if (LB + lead > d.lstop) {  // the lead stop falls in this sub-chunk: its ones up to the stop
-                const u64 lo = d.lo + j * kSc, hi = min(d.hi, lo + kSc);
-                u64 li = LB, part = 0;
-                for (u64 i = lo; i < hi && li < d.lstop; ++i) {
-                    const int t = top_bit(m[i]);
-                    if (t <= p) {
-                        part += t == p;
-                        ++li;
-                    }
-                }
-                OB += part;
-                crossed = true;
-            } else {
-                OB += ones;
+        ones = h[p + 1];
+    };
+    // pass 1: lead / trail totals of this lane's range, their prefixes
+    u64 Ll = 0, Tl = 0;
+    for (u64 j = j0; j < j1; ++j) {
+        u64 l, t, o;
+        counts(j, l, t, o);
+        Ll += l;
+        Tl += t;
+    }
+    u64 LT, TT;
+    const u64 LB0 = warp_excl_scan_u64(Ll, LT), TB0 = warp_excl_scan_u64(Tl, TT);
+    // the sub-chunk where the lead stop falls (LB + lead > lstop), if any
+    u64 jc = ~u64{0};
+    {
+        u64 LB = LB0;
+        for (u64 j = j0; j < j1 && jc == ~u64{0}; ++j) {
+            u64 l, t, o;
+            counts(j, l, t, o);
+            if (LB + l > d.lstop) jc = j;
+            LB += l;
+        }
+    }
+    const unsigned has = __ballot_sync(0xffffffffu, jc != ~u64{0});
+    const int owner = has ? __ffs(has) - 1 : -1;
+    jc = owner >= 0 ? __shfl_sync(0xffffffffu, jc, owner) : ~u64{0};
+    u64 part = 0;  // the crossing sub-chunk's ones up to the stop
+    if (lane == owner) {
+        u64 li = LB0;
+        for (u64 j = j0; j < jc; ++j) {
+            u64 l, t, o;
+            counts(j, l, t, o);
+            li += l;
+        }
+        const u64 lo = d.lo + jc * kSc, hi = min(d.hi, lo + kSc);
+        for (u64 i = lo; i < hi && li < d.lstop; ++i) {
+            const int t = top_bit(m[i]);
+            if (t <= p) {
+                part += t == p;
+                ++li;
             }
         }
-        LB += lead;
-        TB += trail;
     }
-    const u64 ncol = min(LB, d.lstop);
-    so[st] = StreamOut{ncol > 0 ? OB + 1 : 0, min(TB, d.tstop) + OB};
-    ncol_out[st] = ncol;
+    part = owner >= 0 ? __shfl_sync(0xffffffffu, part, owner) : 0;
+    // pass 2: ones before each sub-chunk (all of them before the crossing, `part` at it)
+    u64 Ol = 0;
+    for (u64 j = j0; j < j1; ++j) {
+        u64 l, t, o;
+        counts(j, l, t, o);
+        Ol += j < jc ? o : (j == jc ? part : 0);
+    }
+    u64 OT;
+    const u64 OB0 = warp_excl_scan_u64(Ol, OT);
+    // pass 3: the table
+    u64 LB = LB0, TB = TB0, OB = OB0;
+    for (u64 j = j0; j < j1; ++j) {
+        u64 l, t, o;
+        counts(j, l, t, o);
+        tb[j] = ScOff{LB, TB, OB, min(TB, d.tstop) + OB};
+        LB += l;
+        TB += t;
+        OB += j < jc ? o : (j == jc ? part : 0);
+    }
+    if (lane == 0) {
+        const u64 ncol = min(LT, d.lstop);
+        so[st] = StreamOut{ncol > 0 ? OT + 1 : 0, min(TT, d.tstop) + OT};
+        ncol_out[st] = ncol;
+    }
 }
 
 // One CTA per sub-chunk, every plane of the layout.  Warp w owns positions
@@ -1414,7 +1476,7 @@ void emit_streams(Coded& c, const Layout& L, const u64* m, const u8* neg, cudaSt
         DevBuf<ScOff> tab(nsc * np + 1, s);
         DevBuf<u64> zbuf(L.sym_total + 1, s);
         sc_hist_kernel<<<static_cast<unsigned>(nsc), kScT, 0, s>>>(m, c.dsd.p, dsc.p, nb, hist.p);
-        sc_scan_kernel<<<cdiv(ns, 64), 64, 0, s>>>(m, c.dsd.p, static_cast<int>(ns), nb, dsc.p, nsc, hist.p, tab.p,
+        sc_scan_kernel<<<cdiv(ns * 32, 128), 128, 0, s>>>(m, c.dsd.p, static_cast<int>(ns), nb, dsc.p, nsc, hist.p, tab.p,
                                                   c.so.p, ncol.p);
         const size_t smem = kSc * sizeof(u64) + static_cast<size_t>(np) * kScW * 4 * sizeof(u32);
         TCB_ONCE_PER_DEVICE(cudaFuncSetAttribute(sc_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

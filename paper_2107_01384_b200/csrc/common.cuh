@@ -42,6 +42,8 @@ void stream_sync(cudaStream_t s);
 // device-to-host read; the caller syncs `s` before using `h` (pageable `h` up
 // to 1 MiB: through a pinned bounce buffer, complete on return)
 void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t s);
+// host-to-device copy of a small host array, asynchronous (through pinned staging)
+void h2d(void* d, const void* h, std::size_t bytes, cudaStream_t s);
 
 // Stream-ordered device buffer (cudaMallocAsync pool; freed on the same stream).
 template <class T>
@@ -74,7 +76,7 @@ struct DevBuf {
         if (n) TCB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
     }
     void upload(const T* h, std::size_t cnt) {
-        if (cnt) TCB_CUDA(cudaMemcpyAsync(p, h, cnt * sizeof(T), cudaMemcpyHostToDevice, s));
+        if (cnt) h2d(p, h, cnt * sizeof(T), s);
     }
     void download(T* h, std::size_t cnt) const {
         d2h(h, p, cnt * sizeof(T), s);

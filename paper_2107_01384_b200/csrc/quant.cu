@@ -161,34 +161,53 @@ __global__ void signfold_rows_kernel(u8* __restrict__ neg, u64 nrows, const u64*
         u8 par = 0;
         u64 rem = row;
         for (int a = d - 2; a >= 0; --a) {
-            par ^= flips[meta[2 * d + a] + rem % meta[a]] < 0 ? 1 : 0;
-            rem /= meta[a];
+            const u64 e = meta[a];
+            u64 q, r;
+            if (rem < (u64{1} << 32) && e < (u64{1} << 32)) {  // 32-bit division where it fits
+                q = static_cast<u32>(rem) / static_cast<u32>(e);
+                r = static_cast<u32>(rem) - static_cast<u32>(q) * static_cast<u32>(e);
+            } else {
+                q = rem / e;
+                r = rem - q * e;
+            }
+            par ^= flips[meta[2 * d + a] + r] < 0 ? 1 : 0;
+            rem = q;
         }
-        u8* q = neg + row * last;
-        for (u64 k = threadIdx.x; k < last; k += blockDim.x) q[k] ^= par ^ (fl[k] < 0 ? 1 : 0);
+        u8* q8 = neg + row * last;
+        for (u64 k = threadIdx.x; k < last; k += blockDim.x) q8[k] ^= par ^ (fl[k] < 0 ? 1 : 0);
     }
 }
 
+// 8 rows per step: one barrier per step decides which rows are live
 __global__ void dead_rows_kernel(const u64* __restrict__ dec, u64 nrows, const u64* __restrict__ meta, int d,
                                  u8* __restrict__ dead) {
+    __shared__ int live[8];
     const u64 last = meta[d - 1];
     u8* dl = dead + meta[3 * d - 1];
-    for (u64 row = blockIdx.x; row < nrows; row += gridDim.x) {
-        const u64* q = dec + row * last;
-        int any = 0;
-        for (u64 k = threadIdx.x; k < last; k += blockDim.x)
-            if (q[k]) {
-                any = 1;
-                if (dl[k]) dl[k] = 0;  // most slices are live: read before write
-            }
-        if (__syncthreads_or(any) && threadIdx.x == 0) {
-            u64 rem = row;
+    for (u64 row0 = static_cast<u64>(blockIdx.x) * 8; row0 < nrows; row0 += static_cast<u64>(gridDim.x) * 8) {
+        if (threadIdx.x < 8) live[threadIdx.x] = 0;
+        __syncthreads();
+        const u64 nr = min(u64{8}, nrows - row0);
+        for (u64 rr = 0; rr < nr; ++rr) {
+            const u64* q = dec + (row0 + rr) * last;
+            bool any = false;
+            for (u64 k = threadIdx.x; k < last; k += blockDim.x)
+                if (q[k]) {
+                    any = true;
+                    if (dl[k]) dl[k] = 0;  // most slices are live: read before write
+                }
+            if (any) live[rr] = 1;
+        }
+        __syncthreads();
+        if (threadIdx.x < nr && live[threadIdx.x]) {
+            u64 rem = row0 + threadIdx.x;
             for (int a = d - 2; a >= 0; --a) {
                 u8* z = dead + meta[2 * d + a] + rem % meta[a];
                 if (*z) *z = 0;
                 rem /= meta[a];
             }
         }
+        __syncthreads();
     }
 }
 
@@ -367,7 +386,7 @@ std::vector<u8> dead_slices(const u64* dec, const std::vector<u64>& shape, cudaS
     TCB_CUDA(cudaMemsetAsync(dead.p, 1, total, s));
     if (!order && !shape.empty() && n > 0) {
         const u64 nrows = n / shape.back();
-        dead_rows_kernel<<<static_cast<unsigned>(std::min<u64>(nrows, 148 * 16)), 128, 0, s>>>(
+        dead_rows_kernel<<<static_cast<unsigned>(std::min<u64>(cdiv(nrows, 8), 148 * 16)), 256, 0, s>>>(
             dec, nrows, dm.p, static_cast<int>(shape.size()), dead.p);
     } else if (n < (u64{1} << 32))
         dead_kernel<u32><<<grid_for(n, 256, 4, 4), 256, 0, s>>>(dec, n, dm.p, static_cast<int>(shape.size()), dead.p,
