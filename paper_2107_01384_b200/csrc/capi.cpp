@@ -442,6 +442,7 @@ bool upload_overlapping_gram(const u8* host, u64 nbytes, int dtype, const std::v
         if (p[i] != i) return false;
     const u64 rows = sh[0], cols = nbytes / 8 / rows;
     if (!(prm.backend == 1 || (prm.backend == 0 && rows <= cols))) return false;
+    if (ozaki_gram_ok(rows, cols)) return false;  // the mode loop's Gram is the Ozaki one
     cudaPointerAttributes pa{};
     if (cudaPointerGetAttributes(&pa, host) != cudaSuccess || pa.type != cudaMemoryTypeHost) {
         cudaGetLastError();
@@ -479,6 +480,66 @@ bool upload_overlapping_gram(const u8* host, u64 nbytes, int dtype, const std::v
     cudaEventDestroy(start);
     return true;
 }
+
+// fp32 / fp64 from pinned host memory, identity processing order, a first
+// unfolding on the Ozaki route: the upload goes in row slabs of the first
+// unfolding (rows x cols, row-major: a slab is contiguous) on a copy stream; as
+// each lands, its rows are cast to fp64 (fp32 source), their exponents, sums of
+// squares and digits computed, and every Gram product tile whose rows are all
+// present runs, so the first Gram hides under the PCIe transfer.  Bitwise the
+// mode loop's own Gram (exact integer tile products).  false: not applicable.
+bool upload_overlapping_ozaki(const u8* host, u64 nbytes, int dtype, const std::vector<u64>& sh, const Params& prm,
+                              u8* dev, DevBuf<double>& g0, DevBuf<double>& cast, cudaStream_t s) {
+    if ((dtype != 8 && dtype != 9) || prm.f32 || sh.size() < 2 || nbytes < (u64{32} << 20)) return false;
+    if (const char* e = std::getenv("TCB_PLAIN_UPLOAD"); e && *e && *e != '0') return false;
+    if (ozaki_lt_forced()) return false;
+    const std::vector<u64> p = prm.mode_order ? *prm.mode_order : stable_ascending(sh);
+    for (std::size_t i = 0; i < p.size(); ++i)
+        if (p[i] != i) return false;
+    const u64 es = dtype == 8 ? 4 : 8;
+    const u64 rows = sh[0], cols = nbytes / es / rows;
+    if (rows * cols * es != nbytes || !ozaki_gram_ok(rows, cols)) return false;
+    if (!(prm.backend == 1 || (prm.backend == 0 && rows <= cols))) return false;
+    if (dtype == 9 && reinterpret_cast<uintptr_t>(dev) % 16) return false;
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, host) != cudaSuccess || pa.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        return false;  // pageable memory: the copies would not overlap anyway
+    }
+    if (dtype == 8) cast = DevBuf<double>(rows * cols, s);
+    const double* B = dtype == 8 ? cast.p : reinterpret_cast<const double*>(dev);
+    OzGramRows gr(rows, cols, s);
+    g0 = DevBuf<double>(rows * rows, s);
+    static PerDevice<cudaStream_t> copy_dev;
+    cudaStream_t copy = copy_dev.get([] {
+        cudaStream_t c;
+        TCB_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+        return c;
+    });
+    cudaEvent_t start;
+    TCB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    TCB_CUDA(cudaEventRecord(start, s));  // the buffers exist on `s`
+    TCB_CUDA(cudaStreamWaitEvent(copy, start, 0));
+    // slabs of 128 rows (the tensor-core tile's row block), at most 16
+    const u64 slab = std::max<u64>(128, (rows + 16 * 128 - 1) / (16 * 128) * 128);
+    std::vector<cudaEvent_t> ev;
+    for (u64 r0 = 0; r0 < rows; r0 += slab) {
+        const u64 r1 = std::min(rows, r0 + slab);
+        TCB_CUDA(cudaMemcpyAsync(dev + r0 * cols * es, host + r0 * cols * es, (r1 - r0) * cols * es,
+                                 cudaMemcpyHostToDevice, copy));
+        cudaEvent_t e;
+        TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev.push_back(e);
+        TCB_CUDA(cudaEventRecord(e, copy));
+        TCB_CUDA(cudaStreamWaitEvent(s, e, 0));
+        if (dtype == 8) ingest_cast(dev + r0 * cols * es, 8, (r1 - r0) * cols, cast.p + r0 * cols, s);
+        gr.rows_ready(B, r1);
+    }
+    gr.finish(g0.p);
+    for (auto e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(start);
+    return true;
+}
 }  // namespace
 
 int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_t* shape, int d, uint64_t skip,
@@ -493,10 +554,11 @@ int tcb_compress(const uint8_t* bytes, uint64_t nbytes, int dtype, const uint64_
         Stream st;
         const Params prm = to_params(params, d);
         DevBuf<u8> dev(nbytes - skip + 16, st.s);
-        DevBuf<double> g0, ws;
-        if (!upload_overlapping_gram(bytes + skip, nbytes - skip, dtype, sh, prm, dev.p, g0, ws, st.s))
+        DevBuf<double> g0, ws, cast;
+        if (!upload_overlapping_ozaki(bytes + skip, nbytes - skip, dtype, sh, prm, dev.p, g0, cast, st.s) &&
+            !upload_overlapping_gram(bytes + skip, nbytes - skip, dtype, sh, prm, dev.p, g0, ws, st.s))
             dev.upload(bytes + skip, nbytes - skip);
-        Result r = compress_device(dev.p, nbytes - skip, dtype, sh, prm, st.s, g0.p);
+        Result r = compress_device(dev.p, nbytes - skip, dtype, sh, prm, st.s, g0.p, nullptr, &cast);
         host_trace_dump();
         fill(r, d, out);
     });

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <memory>
+#include <vector>
 
 #include "common.cuh"
 
@@ -61,7 +62,25 @@ void ttm_f64(const double* B, u64 rows, u64 cols, const double* U, u64 r, double
 // used by the mode loop for shapes where it pays (ozaki_*_ok; TCB_OZAKI=0: never).
 bool ozaki_gram_ok(u64 rows, u64 cols);
 bool ozaki_ttm_ok(u64 rows, u64 cols, u64 r);
+bool ozaki_lt_forced();  // TCB_OZAKI_LT=1: the cuBLASLt cross-check path
 void gram_ozaki(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s);
+// The same Gram with the rows of B (row-major rows x cols) arriving in order
+// (e.g. row slabs of a host upload): rows_ready(B, r1) once rows < r1 are valid
+// on s runs their exponents, sums of squares and digits and every product tile
+// whose row blocks are complete; finish writes G.  Bitwise gram_ozaki's G (the
+// digit products accumulate exactly in int64, the diagonal is per-row).
+struct OzGramRows {
+    u64 rows, cols, nslab = 0, ra = 0, rb = 0, ld = 0, done = 0;
+    cudaStream_t s;
+    DevBuf<int> ex;
+    DevBuf<double> sq;
+    DevBuf<int8_t> da, db;
+    DevBuf<long long> acc;
+    std::vector<int2> pending;
+    OzGramRows(u64 rows, u64 cols, cudaStream_t s);
+    void rows_ready(const double* B, u64 r1);
+    void finish(double* G);
+};
 // The TTM's B-side work (column exponents, column digits) depends only on B:
 // ttm_ozaki_prepare runs it on `side` (e.g. beside the eigensolve that produces
 // U) and ttm_ozaki, given the handle, waits for it instead of redoing it.

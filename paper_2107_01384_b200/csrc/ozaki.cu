@@ -238,8 +238,8 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
 __global__ void __launch_bounds__(256) oz_split_rows_blk_kernel(const double* __restrict__ B, u64 rows, u64 cols,
                                                                 u64 nslab, const int* __restrict__ ex,
                                                                 int8_t* __restrict__ DA, u64 rows_a,
-                                                                int8_t* __restrict__ DB, u64 rows_b) {
-    const u64 i = blockIdx.y;
+                                                                int8_t* __restrict__ DB, u64 rows_b, u64 i0) {
+    const u64 i = i0 + blockIdx.y;
     const u64 k0 = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
     if (k0 >= nslab * kOzSlab) return;
     int8_t d[4][kSlices];
@@ -362,6 +362,8 @@ u64 round_up(u64 v, u64 m) { return (v + m - 1) / m * m; }
 
 }  // namespace
 
+bool ozaki_lt_forced() { return use_lt(); }
+
 bool ozaki_gram_ok(u64 rows, u64 cols) {
     const char* e = std::getenv("TCB_OZAKI");  // read per call: tests switch paths in one process
     const bool off = e && *e == '0';
@@ -387,7 +389,7 @@ void gram_ozaki(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) 
         const u64 ra = oz_block_rows(rows, kOzBM), rb = oz_block_rows(rows, kOzBN);
         DevBuf<int8_t> da(oz_block_bytes(rows, nslab, kOzBM), s), db(oz_block_bytes(rows, nslab, kOzBN), s);
         oz_split_rows_blk_kernel<<<dim3(cdiv(Kp, 1024), static_cast<unsigned>(std::max(ra, rb))), 256, 0, s>>>(
-            B, rows, cols, nslab, ex.p, da.p, ra, db.p, rb);
+            B, rows, cols, nslab, ex.p, da.p, ra, db.p, rb, 0);
         count_launch();
         TCB_LAUNCH();
         const u64 ld = oz_gram_acc_ld(rows);
@@ -426,6 +428,57 @@ void gram_ozaki(const double* B, u64 rows, u64 cols, double* G, cudaStream_t s) 
         at += mat * static_cast<u64>(nb);
     }
     oz_gram_combine_kernel<<<cdiv(rows * rows, 256), 256, 0, s>>>(lv, rows, rows_p, ex.p, sq.p, G);
+    count_launch();
+    TCB_LAUNCH();
+}
+
+// ---- the first Gram while the rows are still arriving (host upload in row slabs)
+OzGramRows::OzGramRows(u64 rows_, u64 cols_, cudaStream_t s_) : rows(rows_), cols(cols_), s(s_) {
+    nslab = round_up(cols, kGramKC) / kOzSlab;
+    ra = oz_block_rows(rows, kOzBM);
+    rb = oz_block_rows(rows, kOzBN);
+    ld = oz_gram_acc_ld(rows);
+    ex = DevBuf<int>(round_up(rows, 16), s);
+    ex.zero();
+    sq = DevBuf<double>(rows, s);
+    da = DevBuf<int8_t>(oz_block_bytes(rows, nslab, kOzBM), s);
+    db = DevBuf<int8_t>(oz_block_bytes(rows, nslab, kOzBN), s);
+    acc = DevBuf<long long>(ra * ld, s);
+    acc.zero();
+    const u64 nta = ra / kOzBM, ntb = rb / kOzBN;
+    for (u64 a = 0; a < nta; ++a)
+        for (u64 b = 0; b < ntb; ++b)
+            if (b * kOzBN <= a * kOzBM + kOzBM - 1) pending.push_back(make_int2(static_cast<int>(a), static_cast<int>(b)));
+}
+
+void OzGramRows::rows_ready(const double* B, u64 r1) {
+    if (r1 <= done || r1 > rows) throw Error("ozaki: rows must arrive in order");
+    const u64 r0 = done;
+    ProfScope prof_scope(kGram, s);
+    oz_rowstat_kernel<<<static_cast<unsigned>(r1 - r0), 256, 0, s>>>(B + r0 * cols, cols, ex.p + r0, sq.p + r0);
+    count_launch();
+    TCB_LAUNCH();
+    // the last slab also writes the zero digits of the padding rows
+    const u64 hi = r1 == rows ? std::max(ra, rb) : r1;
+    oz_split_rows_blk_kernel<<<dim3(cdiv(nslab * kOzSlab, 1024), static_cast<unsigned>(hi - r0)), 256, 0, s>>>(
+        B, rows, cols, nslab, ex.p, da.p, ra, db.p, rb, r0);
+    count_launch();
+    TCB_LAUNCH();
+    done = r1;
+    // the tiles whose row blocks are complete now
+    std::vector<int2> now, later;
+    for (const int2 t : pending) {
+        const u64 ea = std::min<u64>(static_cast<u64>(t.x) * kOzBM + kOzBM, rows);
+        const u64 eb = std::min<u64>(static_cast<u64>(t.y) * kOzBN + kOzBN, rows);
+        (std::max(ea, eb) <= done ? now : later).push_back(t);
+    }
+    pending.swap(later);
+    oz_gram_tc_tiles(da.p, db.p, rows, nslab, now, acc.p, ld, s);
+}
+
+void OzGramRows::finish(double* G) {
+    if (done != rows || !pending.empty()) throw Error("ozaki: Gram finished before every row arrived");
+    oz_gram_final_kernel<<<cdiv(rows * rows, 256), 256, 0, s>>>(acc.p, ld, rows, ex.p, sq.p, G);
     count_launch();
     TCB_LAUNCH();
 }

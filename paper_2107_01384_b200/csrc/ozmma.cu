@@ -314,14 +314,21 @@ void set_smem_attr() {
 u64 oz_gram_acc_ld(u64 rows) { return (rows + kTN - 1) / kTN * kTN; }
 
 void oz_gram_tc(const int8_t* DA, const int8_t* DB, u64 rows, u64 nslab, long long* acc, u64 acc_ld, cudaStream_t s) {
-    if (nslab % (kGramKC / kBK)) throw Error("ozaki: Gram k not a multiple of the chunk");
-    set_smem_attr();
     // tiles (a, b) meeting the lower triangle: 96 b <= 128 a + 127
     std::vector<int2> tl;
     const u64 nta = (rows + kTM - 1) / kTM, ntb = (rows + kTN - 1) / kTN;
     for (u64 a = 0; a < nta; ++a)
         for (u64 b = 0; b < ntb; ++b)
             if (b * kTN <= a * kTM + kTM - 1) tl.push_back(make_int2(static_cast<int>(a), static_cast<int>(b)));
+    oz_gram_tc_tiles(DA, DB, rows, nslab, tl, acc, acc_ld, s);
+}
+
+void oz_gram_tc_tiles(const int8_t* DA, const int8_t* DB, u64 rows, u64 nslab, const std::vector<int2>& tl,
+                      long long* acc, u64 acc_ld, cudaStream_t s) {
+    if (nslab % (kGramKC / kBK)) throw Error("ozaki: Gram k not a multiple of the chunk");
+    if (tl.empty()) return;
+    set_smem_attr();
+    const u64 ntb = (rows + kTN - 1) / kTN;
     if (acc_ld < ntb * kTN) throw Error("ozaki: Gram accumulator too narrow");
     DevBuf<int2> dtl(tl.size(), s);
     dtl.upload(tl.data(), tl.size());

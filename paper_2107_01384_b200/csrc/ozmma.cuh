@@ -3,6 +3,8 @@
 // five digit levels combined exactly in int64 by the epilogue.  See ozmma.cu.
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace tcb {
@@ -31,6 +33,10 @@ inline u64 oz_block_bytes(u64 rows, u64 nslab, u32 br) { return oz_block_rows(ro
 // lower triangle incl. the diagonal valid; acc zeroed by the caller; nslab a
 // multiple of 512 (2^15-byte k-chunks: int32-exact accumulation).
 void oz_gram_tc(const int8_t* DA, const int8_t* DB, u64 rows, u64 nslab, long long* acc, u64 acc_ld, cudaStream_t s);
+// the same for a subset of the (128-row a, 96-row b) tiles: the accumulation is
+// exact integer, so any partition of the tiles over launches gives the same acc
+void oz_gram_tc_tiles(const int8_t* DA, const int8_t* DB, u64 rows, u64 nslab, const std::vector<int2>& tiles,
+                      long long* acc, u64 acc_ld, cudaStream_t s);
 u64 oz_gram_acc_ld(u64 rows);  // the accumulator's leading dimension (tile-padded)
 
 // TTM: A (m_rows, 128-row blocks), B (n_rows, 96-row blocks), nslab <= 64 ->

@@ -385,7 +385,9 @@ StepOut mode_step(const double* x, u64 rows, u64 cols, const Budget& budget, int
     std::unique_ptr<OzTtmPrep> tprep;
     if (via_gram) {
         DevBuf<double> G;
-        bool oz = false;
+        // a Gram handed in (the host upload's) is the one this step would compute:
+        // the Ozaki one exactly where ozaki_gram_ok holds
+        bool oz = gram && ozaki_gram_ok(rows, cols);
         if (!gram) {
             G = DevBuf<double>(rows * rows, s);
             if (ozaki_gram_ok(rows, cols)) {
@@ -1149,7 +1151,8 @@ bool norm_pass_forced() {
 }  // namespace
 
 Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,
-                       const Params& prm, cudaStream_t s, const double* gram0, const ShardComm* shard) {
+                       const Params& prm, cudaStream_t s, const double* gram0, const ShardComm* shard,
+                       DevBuf<double>* precast) {
     const auto t_all = Clock::now();
     Result res;
     const std::size_t d = shape.size();
@@ -1196,8 +1199,13 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     if (direct && norm_from_gram) {
         res.norm_sq = 0.0;  // set after the first mode step
     } else if (src_f32 && norm_from_gram) {
-        a = DevBuf<double>(n_el, s);
-        ingest_cast(device_bytes, dtype, n_el, a.p, s);
+        if (precast && precast->p && precast->n == n_el) {
+            a = std::move(*precast);
+        } else {
+            a = DevBuf<double>(n_el, s);
+            ingest_cast(device_bytes, dtype, n_el, a.p, s);
+            gram0 = nullptr;  // computed for a cast that did not arrive
+        }
         res.norm_sq = 0.0;  // set after the first mode step
     } else if (direct) {
         res.norm_sq = sum_squares(static_cast<const double*>(device_bytes), n_el, &finite, s);
@@ -1280,7 +1288,8 @@ Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const st
     try {
         f = sthosvd_device(std::move(a), direct ? static_cast<const double*>(device_bytes) : nullptr, shape,
                            prm.rtmss * target, prm.mode_order, prm.backend, s, finite ? 1 : 0, on_factor,
-                           norm_scale, norm_from_gram ? &norm_trace : nullptr, direct ? gram0 : nullptr, shard);
+                           norm_scale, norm_from_gram ? &norm_trace : nullptr,
+                           direct || (src_f32 && norm_from_gram) ? gram0 : nullptr, shard);
     } catch (const TraceNonFinite&) {  // scan the elements: the reference error, or a norm pass rerun
         bool fin = true;
         if (direct) sum_squares(static_cast<const double*>(device_bytes), n_el, &fin, s);

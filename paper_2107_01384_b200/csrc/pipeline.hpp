@@ -71,12 +71,14 @@ struct Result {
 
 // device_bytes: element bytes (skip already applied) resident on the device
 // gram0 (optional): the first mode's Gram of the fp64 input, already computed
-// (bitwise as gram_f64 would; the host entry point overlaps it with the upload)
+// (bitwise as the mode loop would; the host entry point overlaps it with the upload)
+// precast (optional, fp32 source): the input already cast to fp64 (moved from)
 struct ShardComm;  // below
 Result compress_device(const void* device_bytes, u64 nbytes, int dtype, const std::vector<u64>& shape,
                        const Params& p, cudaStream_t s,
                        const double* gram0 = nullptr,
-                       const ShardComm* shard = nullptr);
+                       const ShardComm* shard = nullptr,
+                       DevBuf<double>* precast = nullptr);
 
 struct Tucker {
     DevBuf<double> core;

@@ -435,6 +435,28 @@ def test_chunked_upload_gram_is_bitwise(gpu_pkg):
     assert abs(len(a) - len(ref.container)) <= 0.01 * len(ref.container)
 
 
+@pytest.mark.parametrize("dtype,shape", [(np.float32, (300, 512, 640)), (np.float64, (256, 512, 520)),
+                                          (np.float32, (1000, 256, 1024))])
+def test_row_slab_upload_ozaki_gram_is_bitwise(gpu_pkg, dtype, shape):
+    """Pinned uploads whose first unfolding takes the Ozaki Gram arrive in row
+    slabs, each slab's digits and complete product tiles running while the
+    next is in flight (ragged last slab, rows not a tile multiple, 8 slabs):
+    the container equals the device-resident path's byte for byte."""
+    torch = pytest.importorskip("torch")
+    x = np.random.default_rng(3).standard_normal(shape).astype(dtype)
+    x *= np.exp(-np.arange(shape[0]) / 40.0).astype(dtype)[:, None, None]
+    prm = gpu_pkg.Params(target_re=1e-2)
+    dt = gpu_pkg.Dtype.float32 if dtype == np.float32 else gpu_pkg.Dtype.float64
+    host = torch.from_numpy(x.reshape(-1).view(np.uint8)).pin_memory()
+    src = gpu_pkg.SourceBuffer(memoryview(host.numpy()), dt, list(x.shape))
+    a = gpu_pkg.compress(src, prm)
+    dev = host.to("cuda")
+    torch.cuda.synchronize()
+    b = gpu_pkg.compress_device(dev.data_ptr(), x.nbytes, dt, x.shape, prm)
+    assert a.ranks == b.ranks
+    assert a.container == b.container
+
+
 def test_eig_large_cluster_cholqr(gpu_pkg):
     """A mode whose kept eigenvalues include a big noise-floor cluster (c3's
     500-row modes): the cluster is orthonormalised by CholQR2 (MGS only on a
