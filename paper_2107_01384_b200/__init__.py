@@ -235,12 +235,23 @@ def _result(r: _CResult) -> CompressResult:
 
 def compress(src: SourceBuffer, params: Params) -> CompressResult:
     """tucomp::pipeline::compress (pipeline.cpp:240-252) on the B200."""
+    return _result(compress_raw(src, params))
+
+
+def compress_raw(src: SourceBuffer, params: Params) -> "_CResult":
+    """tcb_compress itself (the C ABI a reference-side binding calls): the
+    container is in host memory when this returns; free it with
+    free_raw() or turn the result into a CompressResult with _result()."""
     shape = np.asarray(list(src.shape), np.uint64)
     buf = np.frombuffer(src.bytes, np.uint8) if len(src.bytes) else np.zeros(1, np.uint8)
     res = _CResult()
     _check(lib().tcb_compress(_p(buf), C.c_uint64(len(src.bytes)), int(src.dtype), _p(shape), len(shape),
                               C.c_uint64(src.skip_bytes), C.byref(params.to_c(len(shape))), C.byref(res)))
-    return _result(res)
+    return res
+
+
+def free_raw(res: "_CResult") -> None:
+    lib().tcb_free(C.cast(res.container, C.c_void_p))
 
 
 def compress_device(ptr: int, nbytes: int, dtype: Dtype, shape: Sequence[int], params: Params) -> CompressResult:

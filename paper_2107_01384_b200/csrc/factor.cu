@@ -153,9 +153,11 @@ __global__ void refl_from_stream(const u64* __restrict__ mag, const u8* __restri
 }
 
 // X(:, c) = H_0 ... H_{rl-1} e_c ; res[c] = |X(:,c) - flip_c U(:, live_c)|^2.
-// Warp per column, NQ entries per lane; reflectors staged 16 at a time in smem.
+// Warp per column, NQ entries per lane; reflectors staged CH at a time in smem
+// (16, or 8 above 1024 rows: CH n doubles must fit the 227 KB of shared memory).
 constexpr int kExChunk = 16;
-template <int NQ>
+constexpr u64 kExMaxN = 2304;  // NQ = 72
+template <int NQ, int CH = kExChunk>
 __global__ void __launch_bounds__(256) expand_residual(const double* __restrict__ Vd, u64 n, u64 rl,
                                                        const double* __restrict__ U, u64 r,
                                                        const u64* __restrict__ live,
@@ -169,8 +171,8 @@ __global__ void __launch_bounds__(256) expand_residual(const double* __restrict_
     double x[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) x[q] = (static_cast<u64>(lane + 32 * q) == c) ? 1.0 : 0.0;
-    for (long long hi = static_cast<long long>(rl) - 1; hi >= 0; hi -= kExChunk) {
-        const long long lo = hi - kExChunk + 1 < 0 ? 0 : hi - kExChunk + 1;
+    for (long long hi = static_cast<long long>(rl) - 1; hi >= 0; hi -= CH) {
+        const long long lo = hi - CH + 1 < 0 ? 0 : hi - CH + 1;
         __syncthreads();
         for (long long jj = lo; jj <= hi; ++jj)
             for (u64 i = threadIdx.x; i < n; i += blockDim.x) sv[(jj - lo) * n + i] = V[jj * n + i];
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(256) expand_residual(const double* __restrict_
 
 // Decoder side (factor_codec.cpp:246-264): X(:, c) = H_0 ... H_{rl-1} e_c written
 // to U(:, live_c) (row-major n x r).  Same warp-per-column expansion as above.
-template <int NQ>
+template <int NQ, int CH = kExChunk>
 __global__ void __launch_bounds__(256) expand_columns(const double* __restrict__ V, u64 n, u64 rl,
                                                       const u64* __restrict__ live, double* __restrict__ U, u64 r) {
     extern __shared__ double sv[];
@@ -219,8 +221,8 @@ __global__ void __launch_bounds__(256) expand_columns(const double* __restrict__
     double x[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) x[q] = (static_cast<u64>(lane + 32 * q) == c) ? 1.0 : 0.0;
-    for (long long hi = static_cast<long long>(rl) - 1; hi >= 0; hi -= kExChunk) {
-        const long long lo = hi - kExChunk + 1 < 0 ? 0 : hi - kExChunk + 1;
+    for (long long hi = static_cast<long long>(rl) - 1; hi >= 0; hi -= CH) {
+        const long long lo = hi - CH + 1 < 0 ? 0 : hi - CH + 1;
         __syncthreads();
         for (long long jj = lo; jj <= hi; ++jj)
             for (u64 i = threadIdx.x; i < n; i += blockDim.x) sv[(jj - lo) * n + i] = V[jj * n + i];
@@ -315,7 +317,7 @@ std::vector<double> factor_residuals(const u64* mag, const u8* neg, int k, u64 n
     ProfScope prof_scope(kFactor, s);
     const u64 rl = live.size();
     const unsigned np = static_cast<unsigned>(planes.size());
-    if (n > 1024) throw Error("factor codec: mode sizes above 1024 unsupported on the device path");
+    if (n > kExMaxN) throw Error("factor codec: mode sizes above 2304 unsupported on the device path");
     DevBuf<u64> dl(rl, s);
     dl.upload(live.data(), rl);
     DevBuf<int> dp(np, s);
@@ -324,17 +326,21 @@ std::vector<double> factor_residuals(const u64* mag, const u8* neg, int k, u64 n
     DevBuf<int> err(1, s);
     err.zero();
     refl_from_stream<<<dim3(cdiv(rl, 4), np), 128, 0, s>>>(mag, neg, k, n, rl, dp.p, scales_dev, Vd.p, err.p);
-    const size_t smem = static_cast<size_t>(kExChunk) * n * sizeof(double);
+    const size_t smem = static_cast<size_t>(n <= 1024 ? kExChunk : 8) * n * sizeof(double);
     TCB_ONCE_PER_DEVICE({
-        const int mx = kExChunk * 1024 * sizeof(double);
+        const int mx = kExChunk * 1024 * sizeof(double), mx8 = 8 * static_cast<int>(kExMaxN) * sizeof(double);
         cudaFuncSetAttribute(expand_residual<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(expand_residual<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(expand_residual<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(expand_residual<48, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx8);
+        cudaFuncSetAttribute(expand_residual<72, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx8);
     });
     const dim3 grid(cdiv(rl, 8), np);
     if (n <= 256) expand_residual<8><<<grid, 256, smem, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
     else if (n <= 512) expand_residual<16><<<grid, 256, smem, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
-    else expand_residual<32><<<grid, 256, smem, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
+    else if (n <= 1024) expand_residual<32><<<grid, 256, smem, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
+    else if (n <= 1536) expand_residual<48, 8><<<grid, 256, smem, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
+    else expand_residual<72, 8><<<grid, 256, smem, s>>>(Vd.p, n, rl, U, r, dl.p, flips_dev, res.p);
     count_launch(2);
     TCB_LAUNCH();
     int e = 0;
@@ -354,7 +360,7 @@ void factor_expand(const u64* mag, const u8* neg, int k, u64 n, u64 r, const std
     TCB_CUDA(cudaMemsetAsync(U, 0, n * r * sizeof(double), s));
     const u64 rl = live.size();
     if (rl == 0) return;
-    if (n > 1024) throw Error("factor codec: mode sizes above 1024 unsupported on the device path");
+    if (n > kExMaxN) throw Error("factor codec: mode sizes above 2304 unsupported on the device path");
     DevBuf<u64> dl(rl, s);
     dl.upload(live.data(), rl);
     const int zero = 0;
@@ -368,17 +374,21 @@ void factor_expand(const u64* mag, const u8* neg, int k, u64 n, u64 r, const std
     }
     int* ep = err_dev ? err_dev : err.p;
     refl_from_stream<<<dim3(cdiv(rl, 4), 1), 128, 0, s>>>(mag, neg, k, n, rl, dp.p, scales_dev, Vd.p, ep);
-    const size_t smem = static_cast<size_t>(kExChunk) * n * sizeof(double);
+    const size_t smem = static_cast<size_t>(n <= 1024 ? kExChunk : 8) * n * sizeof(double);
     TCB_ONCE_PER_DEVICE({
-        const int mx = kExChunk * 1024 * sizeof(double);
+        const int mx = kExChunk * 1024 * sizeof(double), mx8 = 8 * static_cast<int>(kExMaxN) * sizeof(double);
         cudaFuncSetAttribute(expand_columns<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(expand_columns<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(expand_columns<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(expand_columns<48, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx8);
+        cudaFuncSetAttribute(expand_columns<72, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx8);
     });
     const unsigned grid = cdiv(rl, 8);
     if (n <= 256) expand_columns<8><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);
     else if (n <= 512) expand_columns<16><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);
-    else expand_columns<32><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);
+    else if (n <= 1024) expand_columns<32><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);
+    else if (n <= 1536) expand_columns<48, 8><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);
+    else expand_columns<72, 8><<<grid, 256, smem, s>>>(Vd.p, n, rl, dl.p, U, r);
     count_launch(2);
     TCB_LAUNCH();
     if (err_dev) return;  // the caller checks the shared flag once

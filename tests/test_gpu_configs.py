@@ -182,6 +182,29 @@ def test_rank_tie_band_reported(gpu_pkg):
     assert not (res2.rank_tie_modes & 1)
 
 
+@pytest.mark.parametrize("n0", [1300, 1700])
+def test_mode_above_1024_against_oracle(gpu_pkg, n0):
+    """A mode of more than 1024 rows processed first (Gram route, full
+    eigensolver at n0, the factor codec's reflectors and expansion on n0-row
+    columns): ranks, container size and RE against the oracle, and the
+    device decompress of the container."""
+    rng = np.random.default_rng(n0)
+    shape, terms = (n0, 40, 36), 32
+    w = 0.82 ** np.arange(terms)
+    u = [np.linalg.qr(rng.standard_normal((m, terms)))[0] for m in shape]
+    x = np.einsum("t,it,jt,kt->ijk", w, *u) + 1e-7 * rng.standard_normal(shape)
+    prm = dict(target_re=1e-3)
+    res = gpu_pkg.compress(gpu_pkg.SourceBuffer.from_array(x), gpu_pkg.Params(mode_order=[0, 1, 2], **prm))
+    ref = oracle.compress(x, mode_order=[0, 1, 2], **prm)
+    assert res.ranks == ref.ranks, (res.ranks, ref.ranks)
+    assert abs(len(res.container) - len(ref.container)) <= 0.01 * len(ref.container)
+    e = rel_err(oracle.decompress(res.container, x.shape), x)
+    er = rel_err(oracle.decompress(ref.container, x.shape), x)
+    assert abs(e - er) <= 0.01 * er, (e, er)
+    y = gpu_pkg.decompress_tensor(res.container)
+    assert abs(rel_err(np.asarray(y, np.float64).reshape(x.shape), x) - e) <= 1e-3 * e
+
+
 def test_eigensolver_size_limit_message(gpu_pkg):
     g = np.eye(2400)
     with pytest.raises(gpu_pkg.TucompError, match="supports mode sizes up to"):
