@@ -37,6 +37,11 @@ METRIC = "compress throughput GB/s (input bytes)"
 STAGES = ["ingest", "permute", "gram", "eig", "ttm", "quant", "stats", "emit", "ac", "factor", "sum", "tc"]
 
 
+def _config(re):
+    """The workload description, identical on both arms (the driver compares the dicts)."""
+    return {"workload": WORKLOAD, "re": re, "l2": "input 4 GiB > L2 (no flush needed)"}
+
+
 def _env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
@@ -191,7 +196,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "re": args.re, "l2": "input larger than L2 (4 GiB)"},
+        "config": _config(args.re),
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": nth, "kind": "port",
                          "sample": f"each step one full compress of the c5 generator at {CPU_SAMPLE_N}^3 "
                                    f"({nbytes} B, RE {args.re}) by oracle/ (restatement of the reference path, "
@@ -295,10 +300,10 @@ def main_sharded(args, rank, local, world):
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "re": args.re, "input_bytes": total_bytes, "ranks": res.ranks,
-                       "container_bytes": len(res.container), "l2": "input larger than L2",
-                       "parallelism": f"shard mode 2 over {world} ranks (NCCL all-reduce of partial Grams, "
-                                      f"replicated eigensolve, shard-local TTM, rank 0 encodes)"},
+            "config": _config(args.re),
+            "result": {"input_bytes": total_bytes, "ranks": res.ranks, "container_bytes": len(res.container)},
+            "parallelism": f"shard mode 2 over {world} ranks (NCCL all-reduce of partial Grams, "
+                           f"replicated eigensolve, shard-local TTM and block-sharded encoding)",
             "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": int(host.numel() * 4),
                     "d2h_bytes_per_step": len(r2.container)},
             "gpu_launches": int(launches),
@@ -528,10 +533,10 @@ def main():
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "re": args.re, "input_bytes": nbytes, "ranks": res.ranks,
-                   "container_bytes": len(res.container), "compression_factor": res.compression_factor(),
-                   "core_last_plane": res.core_last_plane, "l2": "input 4 GiB > L2 (no flush needed)",
-                   "parallelism": "single GPU"},
+        "config": _config(args.re),
+        "result": {"input_bytes": nbytes, "ranks": res.ranks, "container_bytes": len(res.container),
+                   "compression_factor": res.compression_factor(), "core_last_plane": res.core_last_plane},
+        "parallelism": "single GPU",
         "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": len(r2.container),
                 "ms_all": [round(v, 2) for v in e2e_ms],
                 "python_bytes_ms": round(py_ms, 2),

@@ -13,7 +13,8 @@ import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SHAPES = [(1, 5), (20, 33), (64, 64), (100, 301), (130, 257), (200, 4096), (256, 20000)]
+SHAPES = [(1, 5), (20, 33), (64, 64), (100, 301), (130, 257), (200, 4096), (256, 20000),
+          (700, 3001), (1024, 8192)]  # multi-tile triangular index math and split plan (c5's 1024-row modes)
 
 CHILD = r"""
 import json, sys
