@@ -42,6 +42,10 @@ def _config(re):
     return {"workload": WORKLOAD, "re": re, "l2": "input 4 GiB > L2 (no flush needed)"}
 
 
+def round_up(a, b):
+    return (a + b - 1) // b * b
+
+
 def _env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
@@ -54,9 +58,9 @@ def _peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
-def _ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary
-    (the first, i.e. mode-0, launch), or None."""
+def _ncu_traffic(kernel, nth=0):
+    """DRAM bytes (read + write) of the nth launch of `kernel` in the committed
+    ncu --set full summary of one c5 compress (profiles/), or None."""
     import glob
 
     for path in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
@@ -64,6 +68,9 @@ def _ncu_traffic(kernel):
         for line in open(path):
             f = line.split()
             if f and f[0] == kernel and len(f) > 5:
+                if nth > 0:
+                    nth -= 1
+                    continue
                 try:
                     return float(f[5]) * 1e6
                 except ValueError:
@@ -465,7 +472,13 @@ def main():
     roof = {"kernel": "oz_mma_kernel (tcgen05.mma kind::i8, TMA-staged, 5 int32 accumulators in TMEM) for the "
                       "mode-0 TTM, 1048576 x r0 by 1024 x 5 digit slices, median of 3 live launches",
             "bound": "tensor", "achieved": ach, "peak": int8_peak, "unit": "TOP/s (int8)", "frac": ach / int8_peak,
-            "traffic": None, "ops": ttm_ops, "ms": tt["tc"],
+            # one c5 compress launches oz_mma_kernel as Gram 0, TTM 0, Gram 1, ...: the 2nd is this one
+            "traffic": _ncu_traffic("oz_mma_kernel", 1),
+            "traffic_algorithmic": float(5 * round_up(rows0, 128) * cols0 + 8 * cols0 * r0),
+            "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of the mode-0 TTM launch, ncu --set full "
+                              "(profiles/ncu_r02_full_summary.txt); algorithmic = the unfolding's five digit slices "
+                              "read once + the fp64 output written once",
+            "ops": ttm_ops, "ms": tt["tc"],
             "peak_source": "2 x measured bf16 burst (MEASURED_PEAKS.json): B200 int8 dense runs at twice bf16",
             "work": "15 slice-pair products of the TTM: 15 * 2 * rows * cols * r int8 ops (algorithmic)",
             "fp64_equivalent": {"flop": ttm_flop0, "ms_with_split_and_combine": tt["ttm"],

@@ -75,3 +75,9 @@ def test_topk_end_to_end(gpu_pkg, kind, shape, re):
     rel = [np.linalg.norm(oracle.decompress(r.container, shape) - x) / np.linalg.norm(x) for r in (fast, full)]
     assert max(rel) <= 1.05 * re  # the hybrid error model's slack, as in the oracle parity tests
     assert abs(rel[0] - rel[1]) <= 0.01 * rel[1]
+    # and both against the CPU oracle, not only each other
+    ref = oracle.compress(x, target_re=re)
+    assert fast.ranks == ref.ranks, (fast.ranks, ref.ranks)
+    assert abs(len(fast.container) - len(ref.container)) <= 0.01 * len(ref.container)
+    rel_ref = np.linalg.norm(oracle.decompress(ref.container, shape) - x) / np.linalg.norm(x)
+    assert abs(rel[0] - rel_ref) <= 0.01 * rel_ref

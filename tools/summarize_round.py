@@ -37,9 +37,11 @@ launch_summary(os.path.join(OUT, "launches.csv"), os.path.join(PROF, f"launches_
                "# tools/c5_once.py 1e-2 (C5_PROFILE=1 C5_ITERS=2): the launches of ONE c5 compress after one\n"
                "# warm-up (cold-cache, serialised: shares, not the overlapped wall time)\n")
 # full capture: per-kernel key metrics
-raw = subprocess.run(["ncu", "-i", os.path.join(OUT, sys.argv[2] if len(sys.argv) > 2 else "full.ncu-rep"),
-                      "--page", "raw", "--csv"],
-                     capture_output=True, text=True).stdout
+rep = os.path.join(OUT, sys.argv[2] if len(sys.argv) > 2 else "full.ncu-rep")
+if os.path.exists(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+else:  # profile_round.sh already reduced the report to its raw page on the GPU box
+    raw = open(rep.replace(".ncu-rep", "_raw.csv")).read()
 rows = list(csv.reader(raw.splitlines()))
 hdr, units, data = rows[0], rows[1], rows[2:]
 want = {
