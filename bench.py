@@ -388,7 +388,7 @@ def main():
     # ---- end to end through the public host API: pinned input bytes in, container bytes out
     host = x.cpu().pin_memory()
     src = tcb.SourceBuffer(memoryview(host.numpy()).cast("B"), tcb.Dtype.float32, shape)
-    for _ in range(max(1, args.warmup // 2)):
+    for _ in range(args.warmup):  # the same W as the device-resident steps (the upload path's pool growth)
         tcb.free_raw(tcb.compress_raw(src, params))
     torch.cuda.synchronize()
     e2e_ms, e2e_bytes = [], []

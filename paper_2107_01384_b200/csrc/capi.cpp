@@ -111,11 +111,40 @@ void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t s) {
         TCB_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
         return;
     }
-    thread_local void* buf = nullptr;  // lives for the thread (never freed: exit order vs. the context)
-    if (!buf) TCB_CUDA(cudaMallocHost(&buf, kBounce));
-    TCB_CUDA(cudaMemcpyAsync(buf, d, bytes, cudaMemcpyDeviceToHost, s));
+    // per thread; handed back to a process-wide free list when the thread ends
+    // (the per-call std::async threads would otherwise pin a fresh buffer each
+    // call) and never freed (exit order vs. the context)
+    struct Bounce {
+        void* buf = nullptr;
+        ~Bounce() {
+            if (buf) {
+                std::lock_guard<std::mutex> lk(pool_mu());
+                pool().push_back(buf);
+            }
+        }
+        static std::mutex& pool_mu() {
+            static std::mutex* m = new std::mutex;  // leaked: threads may end after static destruction
+            return *m;
+        }
+        static std::vector<void*>& pool() {
+            static auto* v = new std::vector<void*>;
+            return *v;
+        }
+    };
+    thread_local Bounce b;
+    if (!b.buf) {
+        {
+            std::lock_guard<std::mutex> lk(Bounce::pool_mu());
+            if (!Bounce::pool().empty()) {
+                b.buf = Bounce::pool().back();
+                Bounce::pool().pop_back();
+            }
+        }
+        if (!b.buf) TCB_CUDA(cudaMallocHost(&b.buf, kBounce));
+    }
+    TCB_CUDA(cudaMemcpyAsync(b.buf, d, bytes, cudaMemcpyDeviceToHost, s));
     stream_sync(s);
-    std::memcpy(h, buf, bytes);
+    std::memcpy(h, b.buf, bytes);
 }
 
 // Host-to-device uploads of small host arrays go through a per-thread ring of
@@ -137,10 +166,49 @@ void h2d(void* d, const void* h, std::size_t bytes, cudaStream_t s) {
         bool used[kSlots] = {};
         int next = 0;
     };
-    thread_local Ring r;  // lives for the thread (never freed: exit order vs. the context)
+    // per thread and device; a thread that ends hands its ring (slots, events and
+    // their pending state) to a process-wide free list for the next new thread on
+    // that device; never freed (exit order vs. the context)
+    struct Held {
+        Ring r;
+        int dev = -1;
+        ~Held() {
+            if (r.buf) {
+                std::lock_guard<std::mutex> lk(pool_mu());
+                pool()[dev].push_back(r);
+            }
+        }
+        static std::mutex& pool_mu() {
+            static std::mutex* m = new std::mutex;
+            return *m;
+        }
+        static std::map<int, std::vector<Ring>>& pool() {
+            static auto* v = new std::map<int, std::vector<Ring>>;
+            return *v;
+        }
+    };
+    thread_local Held held;
+    const int dev_now = cur_device();
+    if (held.r.buf && held.dev != dev_now) {  // the thread moved to another device: its events belong to the old one
+        std::lock_guard<std::mutex> lk(Held::pool_mu());
+        Held::pool()[held.dev].push_back(held.r);
+        held.r = Ring{};
+    }
+    Ring& r = held.r;
     if (!r.buf) {
-        TCB_CUDA(cudaMallocHost(&r.buf, kSlot * kSlots));
-        for (auto& e : r.ev) TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        held.dev = dev_now;
+        {
+            std::lock_guard<std::mutex> lk(Held::pool_mu());
+            auto& free_list = Held::pool()[dev_now];
+            if (!free_list.empty()) {
+                r = free_list.back();
+                free_list.pop_back();
+            }
+        }
+        if (!r.buf) {
+            TCB_CUDA(cudaMallocHost(&r.buf, kSlot * kSlots));
+            for (auto& e : r.ev) TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
     }
     const int i = r.next;
     r.next = (r.next + 1) % kSlots;
@@ -246,6 +314,15 @@ struct Stream {
             if (cudaDeviceGetDefaultMemPool(&mp, cur_device()) == cudaSuccess) {
                 u64 thr = ~u64{0};
                 cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+                // A block freed on another stream is reused only once that free has
+                // completed: never by making this stream wait for the other stream's
+                // pending kernels (the core's emission stalled behind a factor worker's
+                // 15 ms kernels in ~1 call of 5: +30..130 ms).  TCB_POOL_DEPS=1 restores
+                // the driver default for measurements.
+                if (!std::getenv("TCB_POOL_DEPS")) {
+                    int off = 0;
+                    cudaMemPoolSetAttribute(mp, cudaMemPoolReuseAllowInternalDependencies, &off);
+                }
             }
         });
     }

@@ -108,7 +108,9 @@ struct Planner {
                 throw;
             }
         });
-        enq_f.wait();
+        // TCB_PROBE_NOWAIT=1: rely on the side stream's priority alone (measurement switch)
+        static const bool nowait = std::getenv("TCB_PROBE_NOWAIT") != nullptr;
+        if (!nowait) enq_f.wait();
     }
 
     // Exact statistics from plane p down: a sampled estimate of the residual

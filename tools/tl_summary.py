@@ -1,6 +1,7 @@
 """Summarise a timeline.json written by tools/timeline.py: kernels by wall time and
-the main stream's sequence (segments over 1.5 ms)."""
+the main stream's sequence (segments over TL_MIN_US, default 1500 us)."""
 import json
+import os
 import re
 import sys
 from collections import defaultdict
@@ -37,5 +38,5 @@ for st in sorted(cnt):
             out.append([a, b, n, 1])
     print("stream", st, "(main)" if st == main else "", len(seq))
     for a, b, n, c in out:
-        if b - a > 1500:
+        if b - a > float(os.environ.get("TL_MIN_US", 1500)):
             print(f"   {a / 1e3:7.1f}-{b / 1e3:7.1f} {n} x{c}")
