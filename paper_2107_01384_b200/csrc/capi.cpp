@@ -293,6 +293,36 @@ double peak_dmma_tflops();
 
 using namespace tcb;
 
+namespace tcb {
+cudaMemPool_t device_pool() {
+    static PerDevice<cudaMemPool_t> pools;
+    return pools.get([] {
+        cudaMemPool_t mp = nullptr;
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.handleTypes = cudaMemHandleTypeNone;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = cur_device();
+        if (cudaMemPoolCreate(&mp, &pp) != cudaSuccess) {  // the default pool, as the driver configured it
+            cudaGetLastError();
+            TCB_CUDA(cudaDeviceGetDefaultMemPool(&mp, cur_device()));
+            return mp;
+        }
+        u64 thr = ~u64{0};  // keep freed memory mapped between calls
+        TCB_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
+        // A block freed on another stream is reused only once that free has
+        // completed: never by making this stream wait for the other stream's
+        // pending kernels (the core's emission stalled behind a factor worker's
+        // 15 ms kernels in ~1 call of 5: +30..130 ms).  TCB_POOL_DEPS=1 keeps the
+        // driver default for measurements.
+        if (!std::getenv("TCB_POOL_DEPS")) {
+            int off = 0;
+            TCB_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolReuseAllowInternalDependencies, &off));
+        }
+        return mp;
+    });
+}
+}  // namespace tcb
 namespace {
 
 thread_local std::string g_err;
@@ -309,22 +339,7 @@ struct Stream {
         int lo = 0, hi = 0;
         TCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         TCB_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
-        TCB_ONCE_PER_DEVICE({  // keep freed pool memory mapped between calls
-            cudaMemPool_t mp;
-            if (cudaDeviceGetDefaultMemPool(&mp, cur_device()) == cudaSuccess) {
-                u64 thr = ~u64{0};
-                cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
-                // A block freed on another stream is reused only once that free has
-                // completed: never by making this stream wait for the other stream's
-                // pending kernels (the core's emission stalled behind a factor worker's
-                // 15 ms kernels in ~1 call of 5: +30..130 ms).  TCB_POOL_DEPS=1 restores
-                // the driver default for measurements.
-                if (!std::getenv("TCB_POOL_DEPS")) {
-                    int off = 0;
-                    cudaMemPoolSetAttribute(mp, cudaMemPoolReuseAllowInternalDependencies, &off);
-                }
-            }
-        });
+        (void)device_pool();
     }
     ~Stream() {
         if (s) {

@@ -45,7 +45,13 @@ void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t s);
 // host-to-device copy of a small host array, asynchronous (through pinned staging)
 void h2d(void* d, const void* h, std::size_t bytes, cudaStream_t s);
 
-// Stream-ordered device buffer (cudaMallocAsync pool; freed on the same stream).
+// The library's own stream-ordered memory pool on the current device (capi.cpp):
+// freed blocks stay mapped between calls, and a block freed on another stream is
+// reused only once that free has completed.  The device's default pool, which
+// the host application may be using, is left as the driver set it up.
+cudaMemPool_t device_pool();
+
+// Stream-ordered device buffer (from device_pool(); freed on the same stream).
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -53,7 +59,7 @@ struct DevBuf {
     cudaStream_t s = nullptr;
     DevBuf() = default;
     DevBuf(std::size_t count, cudaStream_t st) : n(count), s(st) {
-        if (n) TCB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), s));
+        if (n) TCB_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), n * sizeof(T), device_pool(), s));
     }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
