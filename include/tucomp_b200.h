@@ -156,6 +156,10 @@ int tcb_read_container_header(const uint8_t* container, uint64_t len, tcb_contai
 void tcb_free(void* p);
 const char* tcb_last_error(void);
 uint64_t tcb_kernel_launches(void);
+/* Pinned staging buffers (per-thread bounce buffers and upload rings) allocated
+ * so far in this process: stops growing once every helper thread has one,
+ * since ending threads hand theirs on (a leak check for tests). */
+uint64_t tcb_pinned_staging_allocs(void);
 
 /* Per-stage device timing with CUDA events on the launching stream (no
  * reference counterpart; replaces PhaseTimes' wall clocks for roofline work).

@@ -92,6 +92,7 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.tcb_last_error.restype = C.c_char_p
         L.tcb_kernel_launches.restype = C.c_uint64
+        L.tcb_pinned_staging_allocs.restype = C.c_uint64
         _LIB = L
     return _LIB
 
@@ -113,6 +114,10 @@ def _take_bytes(ptr, n) -> bytes:
 
 def kernel_launches() -> int:
     return int(lib().tcb_kernel_launches())
+
+
+def pinned_staging_allocs() -> int:
+    return int(lib().tcb_pinned_staging_allocs())
 
 
 # ---------------------------------------------------------------- pipeline API
@@ -583,5 +588,5 @@ EXPORTED = ("tcb_compress", "tcb_compress_device", "tcb_decompress", "tcb_decomp
             "tcb_nccl_unique_id", "tcb_nccl_comm_init", "tcb_nccl_comm_destroy", "tcb_compress_sharded_device",
             "tcb_compress_sharded_host", "tcb_dev_encode_tucker_sharded", "tcb_measure_error",
             "tcb_default_params", "tcb_free", "tcb_last_error",
-            "tcb_kernel_launches", "tcb_sthosvd_f64", "tcb_gram_f64", "tcb_ttm_f64", "tcb_eig_f64",
+            "tcb_kernel_launches", "tcb_pinned_staging_allocs", "tcb_sthosvd_f64", "tcb_gram_f64", "tcb_ttm_f64", "tcb_eig_f64",
             "tcb_quantize_f64", "tcb_encode", "tcb_exact_sums", "tcb_exact_plane_stats", "tcb_encode_symbols", "tcb_encode_factor_f64")

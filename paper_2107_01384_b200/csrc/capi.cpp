@@ -102,6 +102,11 @@ void stream_sync(cudaStream_t s) {
 // stalls the other host threads' CUDA calls for its duration (measured: a
 // factor-prep worker's pageable reads held the mode loop's launches back by
 // ~0.15 ms per mode); a pinned copy + stream sync blocks only this thread.
+std::atomic<u64>& pinned_staging_allocs() {
+    static std::atomic<u64> n{0};
+    return n;
+}
+
 void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t s) {
     if (!bytes) return;
     constexpr std::size_t kBounce = std::size_t{1} << 20;
@@ -140,7 +145,10 @@ void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t s) {
                 Bounce::pool().pop_back();
             }
         }
-        if (!b.buf) TCB_CUDA(cudaMallocHost(&b.buf, kBounce));
+        if (!b.buf) {
+            TCB_CUDA(cudaMallocHost(&b.buf, kBounce));
+            ++pinned_staging_allocs();
+        }
     }
     TCB_CUDA(cudaMemcpyAsync(b.buf, d, bytes, cudaMemcpyDeviceToHost, s));
     stream_sync(s);
@@ -207,6 +215,7 @@ void h2d(void* d, const void* h, std::size_t bytes, cudaStream_t s) {
         }
         if (!r.buf) {
             TCB_CUDA(cudaMallocHost(&r.buf, kSlot * kSlots));
+            ++pinned_staging_allocs();
             for (auto& e : r.ev) TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
     }
@@ -518,6 +527,7 @@ void tcb_free(void* p) {
     if (p && !host_release(p)) std::free(p);
 }
 uint64_t tcb_kernel_launches(void) { return launch_counter().load(); }
+uint64_t tcb_pinned_staging_allocs(void) { return pinned_staging_allocs().load(); }
 
 namespace {
 // fp64 from pinned host memory with the identity processing order: the upload
