@@ -388,11 +388,10 @@ def main():
     # ---- end to end through the public host API: pinned input bytes in, container bytes out
     host = x.cpu().pin_memory()
     src = tcb.SourceBuffer(memoryview(host.numpy()).cast("B"), tcb.Dtype.float32, shape)
-    for _ in range(args.warmup):  # the same W as the device-resident steps (the upload path's pool growth)
-        tcb.free_raw(tcb.compress_raw(src, params))
-    torch.cuda.synchronize()
+    # W warm-up + K timed steps of one identical loop (events, synchronisation and
+    # frees included), the first W discarded
     e2e_ms, e2e_bytes = [], []
-    for _ in range(args.steps):
+    for it in range(args.warmup + args.steps):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -400,8 +399,9 @@ def main():
         raw = tcb.compress_raw(src, params)  # tcb_compress: returns with the container in host memory
         b.record()
         b.synchronize()
-        e2e_ms.append(a.elapsed_time(b))
-        e2e_bytes.append(int(raw.container_size))
+        if it >= args.warmup:
+            e2e_ms.append(a.elapsed_time(b))
+            e2e_bytes.append(int(raw.container_size))
         tcb.free_raw(raw)
     # the Python mirror's compress() on top: the container copied into a Python bytes
     a = torch.cuda.Event(enable_timing=True)
